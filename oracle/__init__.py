@@ -1,0 +1,240 @@
+"""CPU oracle of the RPD hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline leg and
+``--impl reference``) may import this package.  It shares no code with
+``paper_2403_18761_b200`` (the CUDA path); the only common module is ``rpd_workloads``, the
+seeded input generator, which holds none of the method's arithmetic.
+
+``oracle.c`` is the plain C implementation (see its header for the definitions and the
+PAPER.md passages they follow); this file compiles it with gcc and marshals numpy arrays.
+``exact_checker.py`` is the independent brute-force rational checker that pins it.
+
+Parity status of each function (DESIGN.md §Oracle pins):
+  relation / candidate lists ... pinned (brute-force soundness, single sphere, SPEC examples)
+  pieces: non-empty, facemask, incidences, vol, m1 ... pinned (exact checker, brute force,
+          Kuhn closed forms, partition, Voronoi reduction, power membership)
+  partial update (R11) ... pinned (partial == full recompute, M = 0 identity)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc, -O2, OpenMP) if missing or stale."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".{os.getpid()}.tmp"
+        cmd = ["gcc", "-O2", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC", "-std=gnu11",
+               "-o", tmp, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Input(C.Structure):
+    _fields_ = [("V", C.c_int64), ("T", C.c_int64), ("N", C.c_int64),
+                ("verts", C.c_void_p), ("tets", C.c_void_p), ("spheres", C.c_void_p),
+                ("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("brute", C.c_int)]
+
+
+class _Result(C.Structure):
+    _fields_ = [("n_tets", C.c_int64),
+                ("cand_off", C.POINTER(C.c_int32)), ("cand_idx", C.POINTER(C.c_int32)),
+                ("n_cand", C.c_int64),
+                ("piece_off", C.POINTER(C.c_int32)), ("piece_sphere", C.POINTER(C.c_int32)),
+                ("piece_vol", C.POINTER(C.c_double)), ("piece_m1", C.POINTER(C.c_double)),
+                ("piece_facemask", C.POINTER(C.c_uint8)),
+                ("inc_off", C.POINTER(C.c_int32)), ("inc_sphere", C.POINTER(C.c_int32)),
+                ("n_pieces", C.c_int64), ("n_inc", C.c_int64),
+                ("n_rel_tests", C.c_int64), ("n_clip_tests", C.c_int64),
+                ("n_constructions", C.c_int64), ("n_fan_triangles", C.c_int64),
+                ("n_zero_hits", C.c_int64),
+                ("status", C.c_int), ("err", C.c_char * 256)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build())
+            L.oracle_rpd.restype = C.POINTER(_Result)
+            L.oracle_rpd.argtypes = [C.POINTER(_Input), C.c_void_p, C.c_int64, C.c_int, C.c_int]
+            L.oracle_free.argtypes = [C.POINTER(_Result)]
+            L.oracle_relation_matrix.restype = C.c_int
+            L.oracle_relation_matrix.argtypes = [C.POINTER(_Input), C.c_void_p, C.c_int64,
+                                                 C.c_int64, C.c_int64, C.c_void_p, C.c_int]
+            L.oracle_power_distance.restype = C.c_double
+            L.oracle_power_distance.argtypes = [C.c_void_p, C.c_void_p]
+            L.oracle_max_threads.restype = C.c_int
+            _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _prep(verts, tets, spheres, nbr_off, nbr_idx, brute):
+    keep = [np.ascontiguousarray(verts, dtype=np.float64),
+            np.ascontiguousarray(tets, dtype=np.int32),
+            np.ascontiguousarray(spheres, dtype=np.float64).reshape(-1, 4),
+            np.ascontiguousarray(nbr_off, dtype=np.int32),
+            np.ascontiguousarray(nbr_idx if len(nbr_idx) else np.zeros(1), dtype=np.int32)]
+    inp = _Input(len(keep[0]), len(keep[1]), len(keep[2]), keep[0].ctypes.data,
+                 keep[1].ctypes.data, keep[2].ctypes.data, keep[3].ctypes.data,
+                 keep[4].ctypes.data, int(brute))
+    return inp, keep
+
+
+def power_distance(sphere, x) -> float:
+    """PD(m, x) = |x - theta|^2 - r^2."""
+    s = np.ascontiguousarray(sphere, dtype=np.float64)
+    p = np.ascontiguousarray(x, dtype=np.float64)
+    return lib().oracle_power_distance(s.ctypes.data, p.ctypes.data)
+
+
+def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=True,
+        nthreads=0):
+    """Oracle RPD of ``tet_ids`` (all tets when None).  Returns a dict of numpy arrays in the
+    boundary's layout (cand CSR, piece CSR, incidence CSR) plus instrumentation counters."""
+    inp, keep = _prep(verts, tets, spheres, nbr_off, nbr_idx, brute)
+    if tet_ids is None:
+        ids_p, n = None, len(keep[1])
+    else:
+        ids = np.ascontiguousarray(tet_ids, dtype=np.int32)
+        keep.append(ids)
+        ids_p, n = ids.ctypes.data, len(ids)
+    L = lib()
+    rp = L.oracle_rpd(C.byref(inp), ids_p, n, int(clip), int(nthreads))
+    try:
+        r = rp.contents
+        if r.status != 0:
+            raise OracleError(f"oracle status {r.status}: {r.err.decode()}")
+
+        def arr(p, n, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(p, shape=(n,)).copy()
+        out = {
+            "cand_off": arr(r.cand_off, r.n_tets + 1, np.int32),
+            "cand_idx": arr(r.cand_idx, r.n_cand, np.int32),
+            "piece_off": arr(r.piece_off, r.n_tets + 1, np.int32),
+            "piece_sphere": arr(r.piece_sphere, r.n_pieces, np.int32),
+            "piece_vol": arr(r.piece_vol, r.n_pieces, np.float64),
+            "piece_m1": arr(r.piece_m1, 3 * r.n_pieces, np.float64).reshape(-1, 3),
+            "piece_facemask": arr(r.piece_facemask, r.n_pieces, np.uint8),
+            "inc_off": arr(r.inc_off, r.n_pieces + 1, np.int32),
+            "inc_sphere": arr(r.inc_sphere, r.n_inc, np.int32),
+            "stats": {k: int(getattr(r, k)) for k in ("n_rel_tests", "n_clip_tests",
+                                                      "n_constructions", "n_fan_triangles",
+                                                      "n_zero_hits")},
+        }
+    finally:
+        L.oracle_free(rp)
+    return out
+
+
+def relation_matrix(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, sphere_lo=0,
+                    sphere_hi=None, nthreads=0):
+    """Literal Alg. 1 booleans rel(t, i) for t in tet_ids, i in [sphere_lo, sphere_hi)."""
+    inp, keep = _prep(verts, tets, spheres, nbr_off, nbr_idx, False)
+    N = len(keep[2])
+    hi = N if sphere_hi is None else sphere_hi
+    if tet_ids is None:
+        ids_p, n = None, len(keep[1])
+    else:
+        ids = np.ascontiguousarray(tet_ids, dtype=np.int32)
+        keep.append(ids)
+        ids_p, n = ids.ctypes.data, len(ids)
+    out = np.zeros((n, max(hi - sphere_lo, 0)), dtype=np.uint8)
+    st = lib().oracle_relation_matrix(C.byref(inp), ids_p, n, sphere_lo, hi, out.ctypes.data,
+                                      int(nthreads))
+    if st:
+        raise OracleError(f"oracle status {st}")
+    return out.astype(bool)
+
+
+def rpd_workload(w, **kw):
+    return rpd(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx, **kw)
+
+
+def partial_update(old, verts, tets, spheres_new, nbr_off_new, nbr_idx_new, n_old,
+                   nthreads=0):
+    """Partial RPD update, reading R11: spheres [n_old, N_new) are new; dirty tets =
+    {t : exists new n with rel_new(t, n)}; dirty tets get a full re-candidate + clip with the
+    new neighbour lists; clean tets keep ``old``'s candidates and pieces.  Returns
+    (merged result dict, dirty tet ids ascending)."""
+    N_new = len(spheres_new)
+    T = len(tets)
+    if N_new > n_old:
+        R = relation_matrix(verts, tets, spheres_new, nbr_off_new, nbr_idx_new,
+                            sphere_lo=n_old, sphere_hi=N_new, nthreads=nthreads)
+        dirty = np.nonzero(R.any(1))[0].astype(np.int32)
+    else:
+        dirty = np.zeros(0, dtype=np.int32)
+    new = rpd(verts, tets, spheres_new, nbr_off_new, nbr_idx_new, tet_ids=dirty,
+              nthreads=nthreads) if len(dirty) else None
+    return merge_per_tet(old, new, dirty, T), dirty
+
+
+def per_tet_lists(res, T):
+    """Split a result dict into per-tet python lists (used to merge and compare)."""
+    out = []
+    co, ci = res["cand_off"], res["cand_idx"]
+    po = res["piece_off"]
+    io = res["inc_off"]
+    for a in range(T):
+        cands = ci[co[a]:co[a + 1]].tolist()
+        pcs = []
+        for p in range(po[a], po[a + 1]):
+            pcs.append((int(res["piece_sphere"][p]), float(res["piece_vol"][p]),
+                        tuple(res["piece_m1"][p].tolist()), int(res["piece_facemask"][p]),
+                        tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist())))
+        out.append((cands, pcs))
+    return out
+
+
+def from_per_tet_lists(L):
+    cand_off = [0]
+    cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
+    for cands, pcs in L:
+        cand_idx += cands
+        cand_off.append(len(cand_idx))
+        for (s, v, m, f, ii) in pcs:
+            ps.append(s)
+            pv.append(v)
+            pm.append(m)
+            pf.append(f)
+            inc += list(ii)
+            inc_off.append(len(inc))
+        piece_off.append(len(ps))
+    return {"cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
+            "piece_off": np.array(piece_off, np.int32), "piece_sphere": np.array(ps, np.int32),
+            "piece_vol": np.array(pv, np.float64),
+            "piece_m1": np.array(pm, np.float64).reshape(-1, 3),
+            "piece_facemask": np.array(pf, np.uint8), "inc_off": np.array(inc_off, np.int32),
+            "inc_sphere": np.array(inc, np.int32)}
+
+
+def merge_per_tet(old, new, dirty, T):
+    L = per_tet_lists(old, T)
+    if new is not None:
+        Ln = per_tet_lists(new, len(dirty))
+        for a, t in enumerate(dirty):
+            L[t] = Ln[a]
+    return from_per_tet_lists(L)
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())

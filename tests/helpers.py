@@ -1,0 +1,57 @@
+"""Shared test helpers: comparing RPD results element by element (no method arithmetic)."""
+import numpy as np
+
+
+def tet_volumes(verts, tets):
+    P = np.asarray(verts)[np.asarray(tets)]
+    a, b, c = P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]
+    return np.einsum("ij,ij->i", a, np.cross(b, c)) / 6.0
+
+
+def tet_diams(verts, tets):
+    P = np.asarray(verts)[np.asarray(tets)]
+    d = 0
+    for a in range(4):
+        for b in range(a + 1, 4):
+            d = np.maximum(d, np.linalg.norm(P[:, a] - P[:, b], axis=1))
+    return d
+
+
+def piece_tet(res):
+    """tet index (local) of every piece"""
+    po = np.asarray(res["piece_off"])
+    return np.repeat(np.arange(len(po) - 1), np.diff(po))
+
+
+def compare_results(a, b, verts, tets, tet_ids=None, rel=1e-9, check_cands=True, label=""):
+    """Parity bar: candidate CSR, piece set, facemask and incidence CSR
+    bit-exact; |dvol| <= rel*vol(t); |dm1| <= rel*vol(t)*diam(t).  Returns a list of
+    human-readable mismatches (empty = pass)."""
+    errs = []
+    ids = np.arange(len(tets)) if tet_ids is None else np.asarray(tet_ids)
+    vt = tet_volumes(verts, np.asarray(tets)[ids])
+    dt = tet_diams(verts, np.asarray(tets)[ids])
+    if check_cands:
+        for k in ("cand_off", "cand_idx"):
+            if not np.array_equal(np.asarray(a[k]), np.asarray(b[k])):
+                errs.append(f"{label}{k} differs")
+    for k in ("piece_off", "piece_sphere", "piece_facemask", "inc_off", "inc_sphere"):
+        x, y = np.asarray(a[k]), np.asarray(b[k])
+        if x.shape != y.shape or not np.array_equal(x, y):
+            if x.shape == y.shape:
+                bad = np.nonzero(x != y)[0][:5]
+                errs.append(f"{label}{k} differs at {bad.tolist()}")
+            else:
+                errs.append(f"{label}{k} shape {x.shape} vs {y.shape}")
+    if errs:
+        return errs
+    pt = piece_tet(a)
+    dv = np.abs(np.asarray(a["piece_vol"]) - np.asarray(b["piece_vol"]))
+    if len(dv) and np.any(dv > rel * vt[pt]):
+        k = int(np.argmax(dv / (rel * vt[pt])))
+        errs.append(f"{label}vol piece {k}: {a['piece_vol'][k]} vs {b['piece_vol'][k]}")
+    dm = np.linalg.norm(np.asarray(a["piece_m1"]) - np.asarray(b["piece_m1"]), axis=1)
+    if len(dm) and np.any(dm > rel * vt[pt] * dt[pt]):
+        k = int(np.argmax(dm / (rel * vt[pt] * dt[pt])))
+        errs.append(f"{label}m1 piece {k}: {a['piece_m1'][k]} vs {b['piece_m1'][k]}")
+    return errs

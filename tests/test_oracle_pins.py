@@ -1,0 +1,311 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (-m "not gpu").
+
+Each test names the passage it follows.  None of them re-types the oracle's formulas: they
+check it against the exact rational checker (brute-force vertex enumeration, no SoS), brute
+force over all spheres, closed forms, SPEC.md worked examples and invariants.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import rpd_workloads as W
+from oracle import exact_checker as X
+from tests.helpers import compare_results, piece_tet, tet_diams, tet_volumes
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------------------------- SPEC examples
+
+
+@pytest.mark.parametrize("case", GOLD["power_distance"])
+def test_power_distance_spec(case):
+    """PD(m, x) = |x - theta|^2 - r^2."""
+    assert oracle.power_distance(case["sphere"], case["x"]) == case["pd"]
+
+
+def _cube_mesh(side):
+    return W.unit_cube_6tets(scale=side)
+
+
+def _axis_pair(xi, ri, xj, rj, y=1.0, z=1.0):
+    sph = np.array([[xi, y, z, ri], [xj, y, z, rj]], dtype=np.float64)
+    off = np.array([0, 1, 2], np.int32)
+    idx = np.array([1, 0], np.int32)
+    return sph, off, idx
+
+
+@pytest.mark.parametrize("case", GOLD["radical_plane"])
+def test_radical_plane_spec_via_volumes(case):
+    """the radical plane of the two spheres is x = plane_x; cutting the
+    [0,2]^3 cube (6 Kuhn tets) must give volume 4*plane_x to sphere i (x < plane_x).  Spheres
+    are shifted by +1 in y,z (and x by 0) to stay in the lattice box."""
+    verts, tets = _cube_mesh(2.0)
+    si, sj = case["sphere_i"], case["sphere_j"]
+    sph, off, idx = _axis_pair(si[0], si[3], sj[0], sj[3])
+    r = oracle.rpd(verts, tets, sph, off, idx)
+    vol_i = r["piece_vol"][r["piece_sphere"] == 0].sum()
+    vol_j = r["piece_vol"][r["piece_sphere"] == 1].sum()
+    assert abs(vol_i - 4.0 * case["plane_x"]) < 1e-12
+    assert abs(vol_j - (8.0 - 4.0 * case["plane_x"])) < 1e-12
+    # swapping the arguments gives the same plane with opposite orientation
+    r2 = oracle.rpd(verts, tets, sph[::-1].copy(), off, idx)
+    assert abs(r2["piece_vol"][r2["piece_sphere"] == 1].sum() - vol_i) < 1e-12
+
+
+@pytest.mark.parametrize("case", GOLD["kuhn_axis_plane"]["cases"])
+def test_kuhn_closed_forms(case):
+    """per-Kuhn-tet volumes of the part x < c of the unit cube."""
+    c = case["c"]
+    verts, tets = _cube_mesh(1.0)
+    # equal radii at x = c -/+ 1/4 (y, z = 1/2): bisector x = c
+    sph = np.array([[c - 0.25, 0.5, 0.5, 0.125], [c + 0.25, 0.5, 0.5, 0.125]])
+    off, idx = np.array([0, 1, 2], np.int32), np.array([1, 0], np.int32)
+    r = oracle.rpd(verts, tets, sph, off, idx)
+    cen = verts[tets].mean(1)
+    for t in range(6):
+        order = np.argsort(cen[t])
+        kind = "largest" if order[2] == 0 else ("smallest" if order[0] == 0 else "middle")
+        p = [k for k in range(r["piece_off"][t], r["piece_off"][t + 1])
+             if r["piece_sphere"][k] == 0]
+        v = r["piece_vol"][p[0]] if p else 0.0
+        assert abs(v - case[kind]) < 1e-14, (t, kind, v, case[kind])
+        # the bisector is a positive-area 2-face of both pieces: incidences list each other
+        io = r["inc_off"]
+        for k in range(r["piece_off"][t], r["piece_off"][t + 1]):
+            other = 1 - r["piece_sphere"][k]
+            assert r["inc_sphere"][io[k]:io[k + 1]].tolist() == [other]
+
+
+# ----------------------------------------------------------------------------- special cases
+
+
+def test_single_sphere_whole_tet():
+    """SPEC.md:228 / north star: one sphere -> every tet relates and its cell is the whole
+    mesh: piece = tet, facemask 0xF, no incidences, m1 = vol * centroid."""
+    w = W.make_shape_workload("one", 600, 1, seed=2, cache=False)
+    assert w.N == 1
+    r = oracle.rpd_workload(w)
+    assert np.array_equal(r["cand_off"], np.arange(w.T + 1))
+    assert np.all(r["piece_facemask"] == 15) and len(r["inc_sphere"]) == 0
+    vt = tet_volumes(w.verts, w.tets)
+    assert np.allclose(r["piece_vol"], vt, rtol=1e-13, atol=0)
+    cen = w.verts[w.tets].mean(1)
+    assert np.allclose(r["piece_m1"], cen * vt[:, None], rtol=1e-12, atol=0)
+
+
+def test_relation_rejects_dominated_tet():
+    """a tet whose 4 vertices are all power-closer to neighbour j than to i is
+    not related to i."""
+    verts, tets = _cube_mesh(1.0)
+    sph = np.array([[10.0, 10.0, 10.0, 0.0], [0.5, 0.5, 0.5, 0.0]])
+    off, idx = np.array([0, 1, 2], np.int32), np.array([1, 0], np.int32)
+    R = oracle.relation_matrix(verts, tets, sph, off, idx)
+    assert not R[:, 0].any() and R[:, 1].all()
+
+
+def test_hidden_spheres_have_no_candidates():
+    """DESIGN.md R4: k_site = 0 and N > 1 -> hidden -> no candidates; brute force agrees that
+    the cell is empty (all N-1 planes)."""
+    w = W.make_c1(5, degenerate=True, big=True)
+    k = np.diff(w.nbr_off)
+    hidden = np.nonzero(k == 0)[0]
+    r = oracle.rpd_workload(w)
+    assert not np.isin(r["cand_idx"], hidden).any()
+    rb = oracle.rpd_workload(w, brute=True)
+    assert not np.isin(rb["piece_sphere"], hidden).any()
+
+
+# ----------------------------------------------------------------------------- exact checker
+
+
+def _exact_compare(w, brute):
+    r = oracle.rpd_workload(w, brute=brute)
+    L = oracle.per_tet_lists(r, w.T)
+    n_nonempty = 0
+    for t in range(w.T):
+        cands, pcs = L[t]
+        pmap = {p[0]: p for p in pcs}
+        for i in (range(w.N) if brute else cands):
+            if brute:
+                S = [j for j in range(w.N) if j != i]
+            else:
+                S = w.nbr_idx[w.nbr_off[i]:w.nbr_off[i + 1]].tolist()
+            e = X.check_tet(w.verts, w.tets, w.spheres, t, i, S)
+            p = pmap.get(i)
+            if e is None:
+                assert p is None, ("spurious piece", t, i)
+                continue
+            n_nonempty += 1
+            assert p is not None, ("missing piece", t, i)
+            assert p[3] == e["facemask"], (t, i, p[3], e["facemask"])
+            assert list(p[4]) == e["inc"], (t, i, p[4], e["inc"])
+            assert abs(p[1] - float(e["vol"])) <= 1e-13
+            assert max(abs(p[2][d] - float(e["m1"][d])) for d in range(3)) <= 1e-13
+    return r, n_nonempty
+
+
+@pytest.mark.parametrize("seed,deg,big", [(0, False, False), (1, False, False),
+                                          (0, True, False), (1, True, False), (2, True, False),
+                                          (5, True, True), (6, True, True)])
+def test_oracle_equals_exact_checker_c1(seed, deg, big):
+    """the oracle's pieces (non-empty, facemask, incidences, vol, m1)
+    equal exact rational vertex enumeration on C1a (generic) and C1b (degenerate: radical
+    planes through Kuhn faces and vertices, exercising the SoS rule), k_site and brute mode."""
+    w = W.make_c1(seed, degenerate=deg, big=big)
+    r, n1 = _exact_compare(w, brute=False)
+    rb, n2 = _exact_compare(w, brute=True)
+    assert n1 == n2 > 0
+    if deg:
+        assert rb["stats"]["n_zero_hits"] > 0   # the degenerate configs do hit exact zeros
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_oracle_equals_exact_checker_tiny_grid(seed):
+    """Random tiny configs on a 2^3-cube Kuhn mesh (48 tets), coarse (degenerate) spheres."""
+    w = W.random_tiny(seed, n_spheres=10, grid=2, coarse=(seed % 2 == 1))
+    _exact_compare(w, brute=False)
+
+
+# ----------------------------------------------------------------------------- invariants
+
+
+@pytest.fixture(scope="module")
+def small_shape():
+    return W.make_shape_workload("S", 2000, 150, seed=3, n_batches=2, batch_m=12, clusters=3,
+                                 cache=False)
+
+
+def test_partition(small_shape):
+    """SPEC.md:251 / north star: per tet, restricted cell volumes sum to the tet volume."""
+    w = small_shape
+    r = oracle.rpd_workload(w)
+    s = np.zeros(w.T)
+    np.add.at(s, piece_tet(r), r["piece_vol"])
+    vt = tet_volumes(w.verts, w.tets)
+    assert np.max(np.abs(s - vt) / vt) < 1e-12
+    assert np.all(r["piece_vol"] > 0)
+
+
+def test_brute_force_equals_ksite(small_shape):
+    """North star: on tiny inputs the oracle must agree with brute force (all N spheres as
+    candidates and as clipping planes).  Incidences compared after restricting brute force
+    to N(i) (they differ only if a non-neighbour plane coincides with a 2-face)."""
+    w = small_shape
+    ids = np.arange(0, w.T, 23, dtype=np.int32)
+    r = oracle.rpd_workload(w, tet_ids=ids)
+    rb = oracle.rpd_workload(w, tet_ids=ids, brute=True)
+    rb = dict(rb)
+    io = rb["inc_off"]
+    keep_inc, new_off = [], [0]
+    for p in range(len(rb["piece_sphere"])):
+        i = rb["piece_sphere"][p]
+        nb = set(w.nbr_idx[w.nbr_off[i]:w.nbr_off[i + 1]].tolist())
+        keep_inc += [j for j in rb["inc_sphere"][io[p]:io[p + 1]] if j in nb]
+        new_off.append(len(keep_inc))
+    rb["inc_sphere"] = np.array(keep_inc, np.int32)
+    rb["inc_off"] = np.array(new_off, np.int32)
+    errs = compare_results(r, rb, w.verts, w.tets, tet_ids=ids, rel=1e-12, check_cands=False)
+    assert not errs, errs
+    # Alg. 1 soundness: every brute-force non-empty piece is a candidate
+    for a in range(len(ids)):
+        cands = set(r["cand_idx"][r["cand_off"][a]:r["cand_off"][a + 1]].tolist())
+        for p in range(rb["piece_off"][a], rb["piece_off"][a + 1]):
+            assert rb["piece_sphere"][p] in cands
+
+
+def test_voronoi_reduction():
+    """PAPER.md:347 (power diagram = Voronoi diagram for equal weights): radii all equal to c
+    and radii all 0 give byte-identical outputs; the neighbour lists equal Delaunay edges."""
+    from scipy.spatial import Delaunay
+    w = W.make_shape_workload("V", 1500, 120, seed=4, radius_mode="equal", cache=False)
+    s0 = w.spheres.copy()
+    s0[:, 3] = 0.0
+    sc = w.spheres.copy()
+    sc[:, 3] = 0.75
+    off, idx = W.power_neighbours(s0)
+    d = Delaunay(s0[:, :3])
+    ed = set()
+    for simp in d.simplices:
+        for a in range(4):
+            for b in range(4):
+                if a != b:
+                    ed.add((simp[a], simp[b]))
+    mine = {(i, j) for i in range(len(s0)) for j in idx[off[i]:off[i + 1]]}
+    assert mine == ed
+    r0 = oracle.rpd(w.verts, w.tets, s0, off, idx)
+    rc = oracle.rpd(w.verts, w.tets, sc, off, idx)
+    for k in r0:
+        if k != "stats":
+            assert np.array_equal(r0[k], rc[k]), k
+    # Euclidean membership: each piece's centroid is nearest (Euclidean) to its sphere
+    from scipy.spatial import cKDTree
+    cen = r0["piece_m1"] / r0["piece_vol"][:, None]
+    dist, nn = cKDTree(s0[:, :3]).query(cen, k=2)
+    own = np.linalg.norm(cen - s0[r0["piece_sphere"], :3], axis=1)
+    assert np.all(own <= dist[:, 0] + 1e-9)
+
+
+def test_power_membership(small_shape):
+    """Power-cell membership: a piece's centroid is power-nearest to its sphere; dyadic sample
+    points with a unique power-nearest sphere lie in a tet whose candidates contain it."""
+    w = small_shape
+    r = oracle.rpd_workload(w)
+    cen = r["piece_m1"] / r["piece_vol"][:, None]
+    th, rad = w.spheres[:, :3], w.spheres[:, 3]
+    pd = ((cen[:, None, :] - th[None]) ** 2).sum(-1) - rad[None] ** 2
+    own = pd[np.arange(len(cen)), r["piece_sphere"]]
+    assert np.all(own <= pd.min(1) + 1e-9 * (1 + np.abs(own)))
+    rng = np.random.default_rng(0)
+    pt = piece_tet(r)
+    for t in rng.choice(w.T, 60, replace=False):
+        P = w.verts[w.tets[t]]
+        lam = rng.dirichlet(np.ones(4))
+        x = W.to_lattice(lam @ P)
+        pdx = ((x - th) ** 2).sum(1) - rad ** 2
+        o = np.argsort(pdx)
+        if pdx[o[1]] - pdx[o[0]] < 1e-6:
+            continue
+        # x may fall just outside t after rounding; only check interior-by-margin points
+        lam_chk = np.linalg.solve(np.c_[P.T[:, 1:] - P.T[:, :1]], x - P[0])
+        lam4 = np.r_[1 - lam_chk.sum(), lam_chk]
+        if lam4.min() <= 1e-9:
+            continue
+        cands = r["cand_idx"][r["cand_off"][t]:r["cand_off"][t + 1]]
+        assert o[0] in cands
+        assert o[0] in r["piece_sphere"][pt == t]
+
+
+def test_partial_update_equals_full(small_shape):
+    """DESIGN.md R11/R12: partial update == full
+    recompute (pieces) for inputs with no exact-degeneracy hits; M = 0 is the identity;
+    clean tets keep their previous pieces byte-identically."""
+    w = small_shape
+    r = oracle.rpd_workload(w)
+    n_old = w.N
+    prev = r
+    for (sph, off, idx) in w.batches:
+        part, dirty = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old)
+        full = oracle.rpd(w.verts, w.tets, sph, off, idx)
+        assert full["stats"]["n_zero_hits"] == 0
+        errs = compare_results(part, full, w.verts, w.tets, rel=1e-12, check_cands=False)
+        assert not errs, errs
+        # dirty tets: candidates equal full recompute
+        clean = np.setdiff1d(np.arange(w.T), dirty)
+        Lp, Lf, Lprev = (oracle.per_tet_lists(x, w.T) for x in (part, full, prev))
+        for t in dirty:
+            assert Lp[t][0] == Lf[t][0]
+        for t in clean:
+            assert Lp[t] == Lprev[t]
+        assert 0 < len(dirty) < w.T
+        prev, n_old = part, len(sph)
+    # identity
+    same, dirty = oracle.partial_update(prev, w.verts, w.tets, *w.batches[-1], n_old)
+    assert len(dirty) == 0
+    for k in same:
+        assert np.array_equal(same[k], oracle.from_per_tet_lists(
+            oracle.per_tet_lists(prev, w.T))[k])
