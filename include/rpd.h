@@ -1,0 +1,163 @@
+/*
+ * rpd.h -- C ABI of the B200 RPD hot path of MATTopo (arXiv 2403.18761).
+ *
+ * The library computes the volumetric restricted power diagram (RPD) of medial spheres over
+ * a tetrahedral mesh with the paper's modified Tet-Cell strategy:
+ *
+ *   rpd_relations       Alg. 1 tet-sphere relation filter over every (tet, sphere) pair and
+ *                       per-tet compaction into k_tet candidate lists
+ *                       (PAPER.md:21-50 Supp. §1.2 Alg. 1; "every pair")
+ *   rpd_clip            per (tet, candidate sphere) convex clipping of the tet by the radical
+ *                       half-spaces of that sphere against all its power neighbours, giving the
+ *                       restricted-power-cell pieces with volume, first moment and
+ *                       face/neighbour incidences (§3.3, 488 §4.1.2)
+ *   rpd_update_partial  partial update after appending M new spheres: only tets related to a
+ *                       new sphere are re-filtered and re-clipped
+ *
+ * Inputs are the paper's problem statement: tets with 4 ordered vertices,
+ * medial spheres m = (theta, r) and the sphere neighbour lists k_site that the
+ * paper obtains from CGAL's regular triangulation.
+ *
+ * Conventions:
+ *  - Exact mode (default): every coordinate and radius must be a multiple of 2^-10 in
+ *    [0, 64); then relation booleans, candidate lists, non-empty flags, facemasks and
+ *    incidences are bit-exact (exact integer predicates + symbolic perturbation).  Inputs off
+ *    that lattice fail with RPD_ENOTEXACT.
+ *  - Pointers: every array argument may be a CUDA device pointer or a host pointer (pinned
+ *    or pageable); host arrays are copied to ctx-owned device memory on the ctx stream.
+ *    Inputs are borrowed for the duration of the call only.
+ *  - Outputs are ctx-owned DEVICE arrays, valid until the next mutating call on the ctx or
+ *    rpd_destroy.  Host scalars (counts) are returned by value; reading them is the only
+ *    device->host synchronisation of each call.
+ *  - Every call is stream-ordered on the ctx stream.  One ctx per device; a ctx is not
+ *    thread-safe.  No exception crosses the ABI; every call returns an rpd_status and
+ *    rpd_last_error() describes the last failure.  Asynchronous kernel faults surface as
+ *    RPD_ECUDA at the next call that synchronises.
+ */
+#ifndef RPD_H
+#define RPD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rpd_ctx rpd_ctx;
+
+typedef enum {
+  RPD_OK = 0,
+  RPD_EINVAL = -1,     /* bad argument: tet index out of range, non-positive tet orientation,
+                          r < 0, NaN/Inf, neighbour out of range / self / duplicate, neighbour
+                          with the same centre, new_ids not the appended range, NULL ctx */
+  RPD_ENOMEM = -2,     /* device allocation failed */
+  RPD_ECUDA = -3,      /* CUDA runtime error (launch failure, fault) */
+  RPD_EOVERFLOW = -4,  /* a piece exceeded even the slow-path capacity (should be unreachable) */
+  RPD_ESTATE = -5,     /* call order: rpd_clip / rpd_update_partial before rpd_relations */
+  RPD_ENOTEXACT = -6   /* exact mode on and an input is off the 2^-10 lattice or out of box */
+} rpd_status;
+
+/* Create a context on CUDA `device`.  `cuda_stream` is a cudaStream_t to order all work on
+ * (NULL: the ctx creates its own non-blocking stream). */
+rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream);
+void rpd_destroy(rpd_ctx* ctx);
+/* Human-readable description of the last failure on ctx (host string owned by ctx, valid
+ * until the next call).  Safe with ctx == NULL. */
+const char* rpd_last_error(const rpd_ctx* ctx);
+
+/* Options (rpd_set_option). */
+enum {
+  RPD_OPT_FILTER_MODE = 1,   /* RPD_FILTER_ALL_PAIRS (literal Alg. 1 over all T*N pairs,
+                                default) or RPD_FILTER_PRUNED (identical booleans; pairs that
+                                provably fail Alg. 1 are skipped) */
+  RPD_OPT_VALIDATE = 2,      /* 1 (default): validate inputs on device; 0: skip */
+  RPD_OPT_STREAM = 3         /* value = (intptr_t) cudaStream_t to switch the ctx stream */
+};
+enum { RPD_FILTER_ALL_PAIRS = 0, RPD_FILTER_PRUNED = 1 };
+rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
+
+/* Step 1 -- Alg. 1 relation filter + per-tet compaction.
+ *   verts    [V][3] double   vertex coordinates
+ *   tets     [T][4] int32    vertex indices; positively oriented; face k = opposite vertex k
+ *                            (this rank's tet shard; the caller keeps the local->global map)
+ *   spheres  [N][4] double   (x, y, z, r), r >= 0
+ *   nbr_off  [N+1]  int32    CSR offsets of the k_site neighbour lists
+ *   nbr_idx  [nbr_off[N]] int32 neighbour sphere ids (any order; the ctx sorts a copy)
+ * Outputs (ctx-owned device arrays):
+ *   *cand_off [T+1] int32    per-tet candidate offsets (k_tet(t) = cand_off[t+1]-cand_off[t])
+ *   *cand_idx [n_cand] int32 candidate sphere ids, ascending per tet
+ *   *n_cand   host int64
+ * Relation (R1, R2, R4): for k_site(i) > 0, t relates to i iff for every neighbour
+ * j some vertex v of t has PD_i(v) < PD_j(v) strictly; for k_site(i) = 0, iff N == 1. */
+rpd_status rpd_relations(rpd_ctx* ctx, const double* verts, int64_t V, const int32_t* tets,
+                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
+                         const int32_t* nbr_idx, const int32_t** cand_off,
+                         const int32_t** cand_idx, int64_t* n_cand);
+
+/* Pieces of the RPD restricted to the ctx's tets (device arrays owned by ctx). */
+typedef struct {
+  const int32_t* piece_off;      /* [T+1] pieces of tet t: [piece_off[t], piece_off[t+1]),
+                                    ascending sphere id */
+  const int32_t* piece_sphere;   /* [n_pieces] owning sphere i */
+  const double* piece_vol;       /* [n_pieces] volume of P(t,i) > 0 */
+  const double* piece_m1;        /* [n_pieces][3] first moment = vol * centroid */
+  const uint8_t* piece_facemask; /* [n_pieces] bit k: a positive-area 2-face of P lies on tet
+                                    face k (opposite vertex k) */
+  const int32_t* inc_off;        /* [n_pieces+1] */
+  const int32_t* inc_sphere;     /* neighbour ids j whose radical plane holds a positive-area
+                                    2-face of the piece, ascending; coincident sources all
+                                    listed (R7) */
+  int64_t n_pieces, n_inc;       /* host values */
+} rpd_pieces;
+
+/* Step 2 -- clip every candidate of the last rpd_relations:
+ *   P(t,i) = t  n  { x : PD_i(x) <= PD_j(x) for all j in N(i) }
+ * Non-empty means positive volume (inward symbolic perturbation, C4, R8).
+ * Returns RPD_ESTATE if rpd_relations has not run on this ctx. */
+rpd_status rpd_clip(rpd_ctx* ctx, rpd_pieces* out);
+
+/* Partial update ("only select a subset of tets ... relating to new spheres").
+ * spheres [N_new][4]: the first N_old are unchanged, new sphere ids [N_old, N_new) appended;
+ * nbr_off/nbr_idx: the new neighbour CSR over all N_new spheres; new_ids [M] int32 must equal
+ * N_old..N_new-1 (else RPD_EINVAL); M == 0 is the identity.
+ * Dirty tets = { t : rel_new(t, n) for some new n } (R11); they get a full
+ * re-filter + clip with the new neighbour lists; clean tets keep candidates and pieces
+ * byte-identically.  Outputs: the merged pieces (as rpd_clip), the dirty tets (device int32,
+ * ascending) and their count (host).  The ctx candidate CSR is updated the same way.
+ * Requires a prior rpd_relations + rpd_clip (else RPD_ESTATE). */
+rpd_status rpd_update_partial(rpd_ctx* ctx, const double* spheres, int64_t N_new,
+                              const int32_t* nbr_off, const int32_t* nbr_idx,
+                              const int32_t* new_ids, int64_t M, rpd_pieces* out,
+                              const int32_t** dirty_tets, int64_t* n_dirty);
+
+/* Copy the current pieces to caller-owned arrays (host or device memory) (sizes from the last rpd_pieces):
+ * piece_off [T+1], piece_sphere/vol/facemask [n_pieces], piece_m1 [3 n_pieces],
+ * inc_off [n_pieces+1], inc_sphere [n_inc].  Any pointer may be NULL (skipped). */
+rpd_status rpd_download_pieces(rpd_ctx* ctx, int32_t* piece_off, int32_t* piece_sphere,
+                               double* piece_vol, double* piece_m1, uint8_t* piece_facemask,
+                               int32_t* inc_off, int32_t* inc_sphere);
+
+/* Copy the current candidate CSR to caller-owned arrays (host or device memory): cand_off [T+1],
+ * cand_idx [n_cand].  Either pointer may be NULL. */
+rpd_status rpd_download_cands(rpd_ctx* ctx, int32_t* cand_off, int32_t* cand_idx);
+
+/* Counters of the last call (host).  Algorithmic counts are what the method computed (for
+ * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */
+typedef struct {
+  int64_t T, N, n_cand, n_pieces, n_inc, n_dirty;
+  int64_t pairs_filtered;        /* (tet, sphere) pairs whose Alg. 1 boolean was decided */
+  int64_t pairs_tested;          /* pairs on which Alg. 1 was actually evaluated (pruned mode) */
+  int64_t exact_fallbacks;       /* clip predicates decided by the int128 path */
+  int64_t zero_hits;             /* exact-zero predicates resolved by symbolic perturbation */
+  int64_t kernel_launches;
+  int32_t max_k_tet, max_vertices, max_planes;
+} rpd_stats;
+rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
+
+/* Library version string. */
+const char* rpd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPD_H */

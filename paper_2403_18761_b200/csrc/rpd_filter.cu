@@ -1,0 +1,108 @@
+// rpd_filter.cu -- SURVEY.md §8(a) rows a2 (Alg. 1 relation filter) and a3 (per-tet k_tet
+// candidate compaction).
+//
+// Alg. 1, prose reading (R1), strict (R2), hidden spheres (R4):
+//   k_site(i) = 0:  rel(t, i) = (N == 1)
+//   otherwise:      rel(t, i) = for all j in N(i): exists vertex v of t with h_ij(v) > 0,
+//                   h_ij = PD_j - PD_i (v strictly power-closer to m_i than to m_j).
+// Every h_ij(v) is an integer-valued double < 2^35.4 computed exactly (three FMAs on exact
+// integer operands with exact partial sums), so the booleans are exact; the "> 0" test reads
+// the fp64 bit pattern as int64, which keeps the compares off the FP64 pipe.
+//
+// Kernel shape: lane = tet (tets are Morton-sorted, so a warp covers a compact region), the
+// warp sweeps all spheres in id order and, per sphere, its planes in CSR order until every
+// lane has failed a plane (warp-uniform early exit, the paper's outer loop); planes are
+// warp-uniform broadcast loads.  Positive spheres are appended to a per-tet slab
+// slab[c * n + t] (c < cap, coalesced over t), already in ascending sphere id.
+#include "rpd_ctx.h"
+#include "rpd_internal.cuh"
+
+namespace rpd {
+
+__device__ __forceinline__ bool pos(double h) { return __double_as_longlong(h) > 0; }
+
+__global__ void __launch_bounds__(256) k_filter_allpairs(
+    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
+    const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes, int N, int lo,
+    int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
+    unsigned long long* __restrict__ stats) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool valid = a < n;
+  int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
+  double X[4], Y[4], Z[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    X[k] = valid ? tx[(3 * k + 0) * T + t] : 0.0;
+    Y[k] = valid ? tx[(3 * k + 1) * T + t] : 0.0;
+    Z[k] = valid ? tx[(3 * k + 2) * T + t] : 0.0;
+  }
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) {
+    int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+    bool alive = valid;
+    if (e0 == e1) {
+      alive = alive && (N == 1);
+    } else {
+      for (int e = e0; e < e1; ++e) {
+        double4 p = planes[e];
+        bool hit = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double h = fma(p.x, X[k], fma(p.y, Y[k], fma(p.z, Z[k], p.w)));
+          hit |= pos(h);
+        }
+        alive = alive && hit;
+        if (!__any_sync(0xffffffffu, alive)) break;
+      }
+    }
+    if (alive) {
+      if (cnt < cap) slab[(int64_t)cnt * n + a] = i;
+      ++cnt;
+    }
+  }
+  if (valid) k_tet[a] = cnt;
+  // max k_tet (warp-aggregated)
+  int m = cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(stats + ST_MAXK, (unsigned long long)m);
+}
+
+__global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,
+                                const int32_t* __restrict__ slab,
+                                const int32_t* __restrict__ cand_off,
+                                int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  int k = k_tet[a];
+  int o = cand_off[a];
+  for (int c = 0; c < k && c < cap; ++c) {
+    cand_idx[o + c] = slab[(int64_t)c * n + a];
+    if (pair_tet) pair_tet[o + c] = (int32_t)a;
+  }
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
+                          int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab) {
+  if (n_tets == 0) return cudaSuccess;
+  k_filter_allpairs<<<nblk(n_tets, 256), 256, 0, c->stream>>>(
+      c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, c->st.nbr_off.as<int32_t>(),
+      c->st.planes.as<double4>(), (int)c->st.N, sphere_lo, sphere_hi, cap, k_tet, slab,
+      c->stats.as<unsigned long long>());
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* k_tet,
+                                 const int32_t* slab, const int32_t* cand_off,
+                                 int32_t* cand_idx, int32_t* pair_tet) {
+  if (n == 0) return cudaSuccess;
+  k_compact_cands<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off, cand_idx,
+                                                       pair_tet);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rpd

@@ -1,0 +1,197 @@
+// rpd_stage.cu -- SURVEY.md §8(a) row a1: input validation and staging.
+//
+// Converts inputs to lattice units (x * 2^10, exact), gathers tet corner coordinates into a
+// coalesced SoA table, builds W = |Theta|^2 - R^2 per sphere, sorts each neighbour row
+// ascending, and builds the radical plane h_ij = n . X + d of every CSR entry
+// (n = 2 (Theta_i - Theta_j), d = W_j - W_i) plus the
+// "twin" chain of entries of the same row whose oriented planes coincide (R7).
+// Every value is an integer-valued double below 2^53, so all of it is exact.
+#include <math.h>
+
+#include "rpd_ctx.h"
+#include "rpd_internal.cuh"
+
+namespace rpd {
+
+__device__ inline void report(int* err, int status, int kind, long long idx) {
+  if (atomicCAS(err, 0, status) == 0) {
+    err[1] = kind;
+    err[2] = (int)(idx > 0x7fffffff ? 0x7fffffff : idx);
+  }
+}
+
+// x real -> lattice; returns false if off the 2^-10 lattice box [0, 64)
+__device__ inline bool to_lat(double x, double* X) {
+  double v = x * RPD_LATTICE;
+  *X = v;
+  return (x >= 0.0) && (x < 64.0) && (v == rint(v));
+}
+
+__global__ void k_check_verts(const double* __restrict__ verts, int64_t n, int* err) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double x = verts[k], X;
+  if (!isfinite(x)) report(err, RPD_EINVAL, ERR_VERT_NAN, k / 3);
+  else if (!to_lat(x, &X)) report(err, RPD_ENOTEXACT, ERR_VERT_LATTICE, k / 3);
+}
+
+__global__ void k_stage_tets(const double* __restrict__ verts, int64_t V,
+                             const int32_t* __restrict__ tets, int64_t T,
+                             double* __restrict__ tx, int* err) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  double P[4][3];
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int32_t v = tets[4 * t + k];
+    if (v < 0 || v >= V) {
+      ok = false;
+      v = 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      P[k][c] = verts[3 * (int64_t)v + c] * RPD_LATTICE;
+      tx[(3 * k + c) * T + t] = P[k][c];
+    }
+  }
+  if (!ok) {
+    report(err, RPD_EINVAL, ERR_TET_INDEX, t);
+    return;
+  }
+  // orientation: det(V1-V0, V2-V0, V3-V0) > 0, exact (integers, partial sums < 2^53)
+  double a[3], b[3], d[3];
+  for (int c = 0; c < 3; ++c) {
+    a[c] = P[1][c] - P[0][c];
+    b[c] = P[2][c] - P[0][c];
+    d[c] = P[3][c] - P[0][c];
+  }
+  double det = a[0] * (b[1] * d[2] - b[2] * d[1]) - a[1] * (b[0] * d[2] - b[2] * d[0]) +
+               a[2] * (b[0] * d[1] - b[1] * d[0]);
+  if (!(det > 0.0)) report(err, RPD_EINVAL, ERR_TET_ORIENT, t);
+}
+
+__global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
+                                double4* __restrict__ sw, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double S[4];
+  for (int c = 0; c < 4; ++c) {
+    double x = spheres[4 * i + c];
+    if (!isfinite(x)) {
+      report(err, RPD_EINVAL, ERR_SPHERE_NAN, i);
+      return;
+    }
+    if (c == 3 && x < 0.0) {
+      report(err, RPD_EINVAL, ERR_RADIUS_NEG, i);
+      return;
+    }
+    if (!to_lat(x, &S[c])) {
+      report(err, RPD_ENOTEXACT, ERR_SPHERE_LATTICE, i);
+      return;
+    }
+  }
+  double W = S[0] * S[0] + S[1] * S[1] + S[2] * S[2] - S[3] * S[3];
+  sw[i] = make_double4(S[0], S[1], S[2], W);
+}
+
+// One thread per sphere row: copy + insertion sort + validation + planes + twins.
+__global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
+                             int64_t N, int64_t E, const double4* __restrict__ sw,
+                             int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
+                             double4* __restrict__ planes, int32_t* __restrict__ twin, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int32_t e0 = off_in[i], e1 = off_in[i + 1];
+  off_out[i] = e0;
+  if (i == N - 1) off_out[N] = e1;
+  if (e0 < 0 || e1 < e0 || e1 > E || (i == 0 && e0 != 0) || (i == N - 1 && e1 != E)) {
+    report(err, RPD_EINVAL, ERR_NBR_OFF, i);
+    return;
+  }
+  for (int32_t e = e0; e < e1; ++e) {
+    int32_t j = idx_in[e];
+    if (j < 0 || j >= N) {
+      report(err, RPD_EINVAL, ERR_NBR_INDEX, i);
+      return;
+    }
+    if (j == i) {
+      report(err, RPD_EINVAL, ERR_NBR_SELF, i);
+      return;
+    }
+    // insertion into the sorted prefix
+    int32_t q = e;
+    while (q > e0 && idx_out[q - 1] > j) {
+      idx_out[q] = idx_out[q - 1];
+      --q;
+    }
+    idx_out[q] = j;
+  }
+  double4 si = sw[i];
+  for (int32_t e = e0; e < e1; ++e) {
+    int32_t j = idx_out[e];
+    if (e > e0 && idx_out[e - 1] == j) {
+      report(err, RPD_EINVAL, ERR_NBR_DUP, i);
+      return;
+    }
+    double4 sj = sw[j];
+    double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
+    if (nx == 0.0 && ny == 0.0 && nz == 0.0) {
+      report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
+      return;
+    }
+    planes[e] = make_double4(nx, ny, nz, sj.w - si.w);
+  }
+  // twins: next entry of the row with the same oriented plane (exact: products < 2^53)
+  for (int32_t e = e0; e < e1; ++e) {
+    double4 a = planes[e];
+    int32_t tw = -1;
+    for (int32_t f = e + 1; f < e1 && tw < 0; ++f) {
+      double4 b = planes[f];
+      bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x && a.y * b.z == a.z * b.y &&
+                  a.x * b.w == a.w * b.x && a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
+      double dot = a.x * b.x + a.y * b.y + a.z * b.z;
+      if (prop && dot > 0.0) tw = f;
+    }
+    twin[e] = tw;
+  }
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
+                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
+                         const int32_t* nbr_idx, int64_t E) {
+  Stage& s = c->st;
+  cudaError_t e;
+  if ((e = s.tx.ensure(sizeof(double) * 12 * (T > 0 ? T : 1)))) return e;
+  if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
+  if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
+  if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  s.T = T;
+  s.N = N;
+  s.V = V;
+  s.E = E;
+  int* err = c->errw.as<int>();
+  if (c->validate && V > 0) {
+    k_check_verts<<<nblk(3 * V, 256), 256, 0, c->stream>>>(verts, 3 * V, err);
+    ++c->launches;
+  }
+  if (T > 0) {
+    k_stage_tets<<<nblk(T, 256), 256, 0, c->stream>>>(verts, V, tets, T, s.tx.as<double>(), err);
+    ++c->launches;
+  }
+  if (N > 0) {
+    k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(spheres, N, s.sw.as<double4>(), err);
+    ++c->launches;
+    k_stage_rows<<<nblk(N, 128), 128, 0, c->stream>>>(
+        nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
+        s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(), err);
+    ++c->launches;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rpd

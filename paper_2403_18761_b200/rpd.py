@@ -1,0 +1,250 @@
+"""Thin Python binding of librpd (include/rpd.h) -- argument marshalling only.
+
+Every step of the RPD path runs in librpd's CUDA kernels; this module passes pointers of
+torch tensors (device or host) or numpy arrays to the C ABI and wraps the results.  There is
+no CPU fallback: if librpd.so is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librpd.so")
+
+RPD_OK, RPD_EINVAL, RPD_ENOMEM, RPD_ECUDA, RPD_EOVERFLOW, RPD_ESTATE, RPD_ENOTEXACT = \
+    0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "RPD_OK", -1: "RPD_EINVAL", -2: "RPD_ENOMEM", -3: "RPD_ECUDA",
+                -4: "RPD_EOVERFLOW", -5: "RPD_ESTATE", -6: "RPD_ENOTEXACT"}
+OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM = 1, 2, 3
+FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
+
+EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
+            "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
+            "rpd_get_stats", "rpd_version"]
+
+
+class RPDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Pieces(C.Structure):
+    _fields_ = [("piece_off", C.c_void_p), ("piece_sphere", C.c_void_p),
+                ("piece_vol", C.c_void_p), ("piece_m1", C.c_void_p),
+                ("piece_facemask", C.c_void_p), ("inc_off", C.c_void_p),
+                ("inc_sphere", C.c_void_p), ("n_pieces", C.c_int64), ("n_inc", C.c_int64)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("T", C.c_int64), ("N", C.c_int64), ("n_cand", C.c_int64),
+                ("n_pieces", C.c_int64), ("n_inc", C.c_int64), ("n_dirty", C.c_int64),
+                ("pairs_filtered", C.c_int64), ("pairs_tested", C.c_int64),
+                ("exact_fallbacks", C.c_int64), ("zero_hits", C.c_int64),
+                ("kernel_launches", C.c_int64), ("max_k_tet", C.c_int32),
+                ("max_vertices", C.c_int32), ("max_planes", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load librpd.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"librpd.so not built at {path}: run __graft_entry__.build()")
+    L = C.CDLL(path)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.rpd_create.argtypes = [C.POINTER(vp), i32, vp]
+    L.rpd_destroy.argtypes = [vp]
+    L.rpd_destroy.restype = None
+    L.rpd_last_error.argtypes = [vp]
+    L.rpd_last_error.restype = C.c_char_p
+    L.rpd_set_option.argtypes = [vp, i32, i64]
+    L.rpd_relations.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(vp),
+                                C.POINTER(vp), C.POINTER(i64)]
+    L.rpd_clip.argtypes = [vp, C.POINTER(_Pieces)]
+    L.rpd_update_partial.argtypes = [vp, vp, i64, vp, vp, vp, i64, C.POINTER(_Pieces),
+                                     C.POINTER(vp), C.POINTER(i64)]
+    L.rpd_download_pieces.argtypes = [vp] * 8
+    L.rpd_download_cands.argtypes = [vp, vp, vp]
+    L.rpd_get_stats.argtypes = [vp, C.POINTER(_Stats)]
+    L.rpd_version.restype = C.c_char_p
+    for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
+              "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _ptr(x, dtype):
+    """(pointer, keepalive) of a torch tensor (CUDA or CPU) or array-like, C-contiguous."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+            x = x.to(tdt).contiguous()
+            return (x.data_ptr() if x.numel() else None), x
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return (a.ctypes.data if a.size else None), a
+
+
+@dataclass
+class PieceCounts:
+    n_pieces: int
+    n_inc: int
+
+
+class RPDContext:
+    """One librpd context on one CUDA device (stream-ordered on ``stream``; default: the
+    current torch stream of that device)."""
+
+    def __init__(self, device: int = 0, stream=None, filter_mode: str = "all_pairs",
+                 validate: bool = True):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("RPDContext needs a CUDA device (no CPU fallback)")
+        self.L = load_library()
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self._stream = stream
+        h = C.c_void_p()
+        st = self.L.rpd_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
+        if st != 0:
+            raise RPDError(st, "rpd_create failed")
+        self.h = h
+        self.set_filter_mode(filter_mode)
+        self.L.rpd_set_option(self.h, OPT_VALIDATE, int(bool(validate)))
+        self.T = 0
+        self.N = 0
+        self.n_cand = 0
+        self.counts = None
+
+    def _check(self, st):
+        if st != 0:
+            raise RPDError(st, self.L.rpd_last_error(self.h).decode())
+
+    def set_filter_mode(self, mode: str):
+        m = {"all_pairs": FILTER_ALL_PAIRS, "pruned": FILTER_PRUNED}[mode]
+        self._check(self.L.rpd_set_option(self.h, OPT_FILTER_MODE, m))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.rpd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ calls
+    def relations(self, verts, tets, spheres, nbr_off, nbr_idx) -> int:
+        """Alg. 1 + k_tet compaction; returns n_cand (candidates stay on the device)."""
+        pv, kv = _ptr(verts, np.float64)
+        pt, kt = _ptr(tets, np.int32)
+        ps, ks = _ptr(spheres, np.float64)
+        po, ko = _ptr(nbr_off, np.int32)
+        pi, ki = _ptr(nbr_idx, np.int32)
+        V = int(np.prod(kv.shape)) // 3
+        T = int(np.prod(kt.shape)) // 4
+        N = int(np.prod(ks.shape)) // 4
+        co, ci, nc = C.c_void_p(), C.c_void_p(), C.c_int64()
+        self._check(self.L.rpd_relations(self.h, pv, V, pt, T, ps, N, po, pi, C.byref(co),
+                                         C.byref(ci), C.byref(nc)))
+        self.T, self.N, self.n_cand = T, N, nc.value
+        self._keep = (kv, kt, ks, ko, ki)
+        return nc.value
+
+    def clip(self) -> PieceCounts:
+        P = _Pieces()
+        self._check(self.L.rpd_clip(self.h, C.byref(P)))
+        self.counts = PieceCounts(P.n_pieces, P.n_inc)
+        return self.counts
+
+    def update_partial(self, spheres, nbr_off, nbr_idx, new_ids):
+        ps, ks = _ptr(spheres, np.float64)
+        po, ko = _ptr(nbr_off, np.int32)
+        pi, ki = _ptr(nbr_idx, np.int32)
+        pn, kn = _ptr(new_ids, np.int32)
+        N_new = int(np.prod(ks.shape)) // 4
+        M = int(np.prod(kn.shape))
+        P = _Pieces()
+        dt, nd = C.c_void_p(), C.c_int64()
+        self._check(self.L.rpd_update_partial(self.h, ps, N_new, po, pi, pn, M, C.byref(P),
+                                              C.byref(dt), C.byref(nd)))
+        self.N = N_new
+        self.counts = PieceCounts(P.n_pieces, P.n_inc)
+        self._dirty_ptr = dt.value
+        self._keep_p = (ks, ko, ki, kn)
+        return self.counts, nd.value
+
+    # ------------------------------------------------------------------ outputs
+    def download_cands(self, device=False):
+        """Candidate CSR as numpy (host) or torch CUDA tensors (device=True)."""
+        T, n = self.T, self.n_cand
+        off, idx = self._alloc([(T + 1, np.int32), (n, np.int32)], device)
+        self._check(self.L.rpd_download_cands(self.h, self._p(off), self._p(idx)))
+        return {"cand_off": off, "cand_idx": idx}
+
+    def download_pieces(self, device=False):
+        T = self.T
+        npc, ni = self.counts.n_pieces, self.counts.n_inc
+        arrs = self._alloc([(T + 1, np.int32), (npc, np.int32), (npc, np.float64),
+                            (3 * npc, np.float64), (npc, np.uint8), (npc + 1, np.int32),
+                            (ni, np.int32)], device)
+        self._check(self.L.rpd_download_pieces(self.h, *[self._p(a) for a in arrs]))
+        keys = ["piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
+                "inc_off", "inc_sphere"]
+        out = dict(zip(keys, arrs))
+        out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
+        return out
+
+    def stats(self) -> dict:
+        s = _Stats()
+        self._check(self.L.rpd_get_stats(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in _Stats._fields_}
+
+    @staticmethod
+    def _alloc(specs, device):
+        if device:
+            import torch
+            tdt = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8}
+            return [torch.empty(max(n, 0), dtype=tdt[dt], device="cuda") for n, dt in specs]
+        return [np.empty(max(n, 0), dtype=dt) for n, dt in specs]
+
+    @staticmethod
+    def _p(a):
+        try:
+            import torch
+            if isinstance(a, torch.Tensor):
+                return a.data_ptr() if a.numel() else None
+        except ImportError:
+            pass
+        return a.ctypes.data if a.size else None
+
+
+def rpd_full(verts, tets, spheres, nbr_off, nbr_idx, ctx: RPDContext = None, **kw):
+    """Convenience: relations + clip, results as numpy dicts (host)."""
+    own = ctx is None
+    ctx = ctx or RPDContext(**kw)
+    try:
+        ctx.relations(verts, tets, spheres, nbr_off, nbr_idx)
+        ctx.clip()
+        out = ctx.download_cands()
+        out.update(ctx.download_pieces())
+        out["stats"] = ctx.stats()
+        return out
+    finally:
+        if own:
+            ctx.close()

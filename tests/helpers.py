@@ -55,3 +55,24 @@ def compare_results(a, b, verts, tets, tet_ids=None, rel=1e-9, check_cands=True,
         k = int(np.argmax(dm / (rel * vt[pt] * dt[pt])))
         errs.append(f"{label}m1 piece {k}: {a['piece_m1'][k]} vs {b['piece_m1'][k]}")
     return errs
+
+
+def slice_tets(res, ids):
+    """Sub-result of the tets ``ids`` (CSR slicing with numpy)."""
+    ids = np.asarray(ids)
+    co, po, io = (np.asarray(res[k]) for k in ("cand_off", "piece_off", "inc_off"))
+    out = {}
+    cs = [np.arange(co[t], co[t + 1]) for t in ids]
+    ps = [np.arange(po[t], po[t + 1]) for t in ids]
+    cidx = np.concatenate(cs) if cs else np.zeros(0, int)
+    pidx = np.concatenate(ps) if ps else np.zeros(0, int)
+    out["cand_off"] = np.r_[0, np.cumsum([len(c) for c in cs])].astype(np.int32)
+    out["cand_idx"] = np.asarray(res["cand_idx"])[cidx]
+    out["piece_off"] = np.r_[0, np.cumsum([len(p) for p in ps])].astype(np.int32)
+    for k in ("piece_sphere", "piece_vol", "piece_m1", "piece_facemask"):
+        out[k] = np.asarray(res[k])[pidx]
+    incs = [np.arange(io[p], io[p + 1]) for p in pidx]
+    out["inc_off"] = np.r_[0, np.cumsum([len(x) for x in incs])].astype(np.int32)
+    out["inc_sphere"] = np.asarray(res["inc_sphere"])[np.concatenate(incs) if incs else
+                                                      np.zeros(0, int)]
+    return out

@@ -1,0 +1,169 @@
+"""CUDA path vs the CPU oracle, element by element, through the C ABI (-m gpu).
+
+Bar: candidate CSR, non-empty set, facemasks and incidences bit-exact;
+|dvol| <= 1e-9 vol(t), |dm1| <= 1e-9 vol(t) diam(t) (north star tolerance, R10).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import rpd_workloads as W
+from tests.helpers import compare_results, piece_tet, slice_tets, tet_volumes
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2403_18761_b200 as P
+    P.build()
+    c = P.RPDContext(0)
+    yield c
+    c.close()
+
+
+def run_gpu(ctx, w, device_inputs=True):
+    import torch
+    args = [w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx]
+    if device_inputs:
+        args = [torch.as_tensor(np.asarray(a)).cuda() for a in args]
+    ctx.relations(*args)
+    ctx.clip()
+    out = ctx.download_cands()
+    out.update(ctx.download_pieces())
+    out["stats"] = ctx.stats()
+    return out
+
+
+def check(ctx, w, **kw):
+    got = run_gpu(ctx, w, **kw)
+    ref = oracle.rpd_workload(w)
+    errs = compare_results(got, ref, w.verts, w.tets, rel=REL)
+    assert not errs, errs[:5]
+    return got, ref
+
+
+@pytest.mark.parametrize("seed,deg,big", [(0, False, False), (1, False, False), (2, False, False),
+                                          (0, True, False), (1, True, False), (2, True, False),
+                                          (5, True, True), (6, True, True)])
+def test_c1_unit_cube(ctx, seed, deg, big):
+    """BASELINE.json configs[0]: unit cube, 6 Kuhn tets, 16 dyadic spheres; C1b is degenerate
+    (radical planes through Kuhn faces/vertices) and exercises the exact SoS path."""
+    got, ref = check(ctx, W.make_c1(seed, degenerate=deg, big=big))
+    if deg:
+        assert got["stats"]["zero_hits"] > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tiny_grids(ctx, seed):
+    check(ctx, W.random_tiny(seed, n_spheres=14, grid=2, coarse=(seed % 2 == 1)))
+
+
+@pytest.mark.parametrize("seed,tets,sph,mode", [(3, 2000, 150, "uniform"),
+                                                (4, 5000, 400, "uniform"),
+                                                (5, 3000, 300, "high_variance"),
+                                                (6, 4000, 60, "uniform")])
+def test_shape_workloads(ctx, seed, tets, sph, mode):
+    """Several tiles (256-tet filter blocks, 8-pair clip blocks) and a ragged tail."""
+    w = W.make_shape_workload(f"P{seed}", tets, sph, seed=seed, radius_mode=mode, cache=False)
+    assert w.T % 256 != 0
+    got, _ = check(ctx, w)
+    vt = tet_volumes(w.verts, w.tets)
+    s = np.zeros(w.T)
+    np.add.at(s, piece_tet(got), got["piece_vol"])
+    assert np.max(np.abs(s - vt) / vt) < 1e-9
+
+
+def test_host_inputs_equal_device_inputs(ctx):
+    w = W.make_shape_workload("H", 1500, 120, seed=8, cache=False)
+    a = run_gpu(ctx, w, device_inputs=True)
+    b = run_gpu(ctx, w, device_inputs=False)
+    for k in a:
+        if k != "stats":
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+
+
+def test_single_sphere(ctx):
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    got, _ = check(ctx, w)
+    assert np.all(got["piece_facemask"] == 15) and len(got["inc_sphere"]) == 0
+
+
+def test_equal_radii_vs_zero_radii(ctx):
+    """equal weights -> Voronoi; r = c and r = 0 give byte-identical output."""
+    w = W.make_shape_workload("V", 1500, 120, seed=4, radius_mode="equal", cache=False)
+    s0 = w.spheres.copy()
+    s0[:, 3] = 0.0
+    sc = w.spheres.copy()
+    sc[:, 3] = 0.75
+    off, idx = W.power_neighbours(s0)
+    import copy
+    w0 = copy.copy(w)
+    w0.spheres, w0.nbr_off, w0.nbr_idx = s0, off, idx
+    wc = copy.copy(w0)
+    wc.spheres = sc
+    a = run_gpu(ctx, w0)
+    b = run_gpu(ctx, wc)
+    for k in a:
+        if k != "stats":
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+
+
+def test_empty_inputs(ctx):
+    w = W.make_c1(0)
+    n = ctx.relations(w.verts, np.zeros((0, 4), np.int32), w.spheres, w.nbr_off, w.nbr_idx)
+    assert n == 0
+    c = ctx.clip()
+    assert c.n_pieces == 0
+    n = ctx.relations(w.verts, w.tets, np.zeros((0, 4)), np.zeros(1, np.int32),
+                      np.zeros(0, np.int32))
+    assert n == 0
+
+
+def test_input_errors(ctx):
+    import paper_2403_18761_b200 as P
+    w = W.make_c1(0)
+    bad = w.verts.copy()
+    bad[0, 0] = 1.0 / 3.0
+    with pytest.raises(P.RPDError) as e:
+        ctx.relations(bad, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    assert e.value.status == -6
+    flipped = w.tets.copy()
+    flipped[0, [1, 2]] = flipped[0, [2, 1]]
+    with pytest.raises(P.RPDError) as e:
+        ctx.relations(w.verts, flipped, w.spheres, w.nbr_off, w.nbr_idx)
+    assert e.value.status == -1
+    idx = w.nbr_idx.copy()
+    idx[0] = 0  # sphere 0 lists itself
+    with pytest.raises(P.RPDError) as e:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, idx)
+    assert e.value.status == -1
+    sph = w.spheres.copy()
+    sph[3, 3] = -1.0 / 1024
+    with pytest.raises(P.RPDError) as e:
+        ctx.relations(w.verts, w.tets, sph, w.nbr_off, w.nbr_idx)
+    assert e.value.status == -1
+    # clip after a failed relations call is a state error
+    with pytest.raises(P.RPDError) as e:
+        ctx.clip()
+    assert e.value.status == -5
+
+
+def test_bench_config_sampled(ctx):
+    """At BASELINE.json's full size (C3: ~200k tets, 20k spheres), in the launch configuration
+    bench.py times: sampled tets compared one by one with the oracle, partition on all."""
+    w = W.make_config("C3")
+    got = run_gpu(ctx, w)
+    rng = np.random.default_rng(0)
+    ids = np.sort(rng.choice(w.T, 48, replace=False)).astype(np.int32)
+    ref = oracle.rpd_workload(w, tet_ids=ids)
+    # slice the GPU result to the sampled tets
+    sub = slice_tets(got, ids)
+    errs = compare_results(sub, ref, w.verts, w.tets, tet_ids=ids, rel=REL)
+    assert not errs, errs[:5]
+    vt = tet_volumes(w.verts, w.tets)
+    s = np.zeros(w.T)
+    np.add.at(s, piece_tet(got), got["piece_vol"])
+    assert np.max(np.abs(s - vt) / vt) < 1e-9
