@@ -71,7 +71,9 @@ enum {
                                 default) or RPD_FILTER_PRUNED (identical booleans; pairs that
                                 provably fail Alg. 1 are skipped) */
   RPD_OPT_VALIDATE = 2,      /* 1 (default): validate inputs on device; 0: skip */
-  RPD_OPT_STREAM = 3         /* value = (intptr_t) cudaStream_t to switch the ctx stream */
+  RPD_OPT_STREAM = 3,        /* value = (intptr_t) cudaStream_t to switch the ctx stream */
+  RPD_OPT_CLIP_WIDE = 4      /* 1: clip every pair with the wide (128-vertex) kernel instead of
+                                only the pairs that overflow the fast (32-vertex) one; for tests */
 };
 enum { RPD_FILTER_ALL_PAIRS = 0, RPD_FILTER_PRUNED = 1 };
 rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
@@ -151,6 +153,7 @@ typedef struct {
   int64_t zero_hits;             /* exact-zero predicates resolved by symbolic perturbation */
   int64_t kernel_launches;
   int32_t max_k_tet, max_vertices, max_planes;
+  int32_t n_wide;                /* pairs re-clipped by the wide kernel */
 } rpd_stats;
 rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
 

@@ -136,7 +136,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
                     &c->st.twin, &c->verts_lat, &c->tets, &c->errw, &c->stats, &c->scratch,
                     &c->k_tet, &c->slab, &c->cand_off, &c->cand_idx, &c->pair_tet, &c->p_flag,
-                    &c->p_vol, &c->p_m1, &c->p_fm, &c->p_ninc, &c->p_inc, &c->p_scan,
+                    &c->p_vol, &c->p_m1, &c->p_fm, &c->p_ninc, &c->p_f01, &c->p_words,
+                    &c->p_moff, &c->p_mask, &c->p_over, &c->k_words, &c->w_off, &c->p_scan,
                     &c->i_scan, &c->piece_off, &c->piece_sphere, &c->piece_vol, &c->piece_m1,
                     &c->piece_fm, &c->inc_off, &c->inc_sphere, &c->dirty_flag, &c->dirty_list,
                     &c->dirty_scan};
@@ -161,6 +162,9 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
       return RPD_OK;
     case RPD_OPT_VALIDATE:
       c->validate = value ? 1 : 0;
+      return RPD_OK;
+    case RPD_OPT_CLIP_WIDE:
+      c->clip_wide = value ? 1 : 0;
       return RPD_OK;
     case RPD_OPT_STREAM:
       if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -219,14 +223,19 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
                        c->stream), "copy tets");
 
   CK(c->k_tet.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
+  CK(c->k_words.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
   CK(c->cand_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(c->w_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
   for (int attempt = 0; attempt < 2; ++attempt) {
     int cap = c->slab_cap;
     CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * (T > 0 ? T : 1)), "alloc slab");
     CK(launch_filter(c, nullptr, T, cap, 0, (int)N, c->k_tet.as<int32_t>(),
-                     c->slab.as<int32_t>()), "filter");
+                     c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
     CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), c->cand_off.as<int32_t>(), T), "scan");
+    CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), T), "scan");
     CK(cudaMemcpyAsync(&rb->i32[0], c->cand_off.as<int32_t>() + T, sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(cudaMemcpyAsync(&rb->i32[1], c->w_off.as<int32_t>() + T, sizeof(int32_t),
                        cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                        cudaMemcpyDeviceToHost, c->stream), "readback");
@@ -242,11 +251,14 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
     c->slab_cap = nc;
   }
   int64_t nc = rb->i32[0];
+  c->n_mask_words = rb->i32[1];
   CK(c->cand_idx.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
   CK(c->pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
+  CK(c->p_moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
   CK(launch_compact_cands(c, T, c->slab_cap, c->k_tet.as<int32_t>(), c->slab.as<int32_t>(),
                           c->cand_off.as<int32_t>(), c->cand_idx.as<int32_t>(),
-                          c->pair_tet.as<int32_t>()), "compact");
+                          c->pair_tet.as<int32_t>(), c->w_off.as<int32_t>(),
+                          c->p_moff.as<int32_t>(), nc), "compact");
   c->n_cand = nc;
   c->have_rel = true;
   c->last = rpd_stats{};
@@ -282,25 +294,35 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   const int64_t n = c->n_cand, T = c->st.T;
   size_t nn = n > 0 ? n : 1;
   CK(c->p_flag.ensure(nn), "alloc");
+  CK(c->p_f01.ensure(nn), "alloc");
   CK(c->p_fm.ensure(nn), "alloc");
   CK(c->p_vol.ensure(sizeof(double) * nn), "alloc");
   CK(c->p_m1.ensure(sizeof(double) * 3 * nn), "alloc");
   CK(c->p_ninc.ensure(sizeof(int32_t) * nn), "alloc");
-  CK(c->p_inc.ensure(sizeof(int32_t) * RPD_INC_CAP * nn), "alloc");
+  CK(c->p_over.ensure(sizeof(int32_t) * (n + 1)), "alloc");
+  CK(c->p_mask.ensure(sizeof(unsigned) * (c->n_mask_words > 0 ? c->n_mask_words : 1)), "alloc");
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
-  CK(launch_clip(c, n, c->pair_tet.as<int32_t>(), nullptr, c->cand_idx.as<int32_t>()), "clip");
+  CK(cudaMemsetAsync(c->p_mask.p, 0, sizeof(unsigned) * c->n_mask_words, c->stream), "memset");
+  CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
+  CK(launch_clip(c, n, c->pair_tet.as<int32_t>(), nullptr, c->cand_idx.as<int32_t>(),
+                 c->clip_wide), "clip");
+  if (!c->clip_wide && n > 0)
+    CK(launch_clip_overflow(c, c->pair_tet.as<int32_t>(), nullptr, c->cand_idx.as<int32_t>()),
+       "clip (wide)");
   CK(launch_piece_scans(c, n), "scan");
   Readback* rb = (Readback*)c->pinned;
   CK(cudaMemcpyAsync(&rb->i32[0], c->p_scan.as<int32_t>() + n, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaMemcpyAsync(&rb->i32[1], c->i_scan.as<int32_t>() + n, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[2], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                     c->stream), "readback");
   CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                      cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaStreamSynchronize(c->stream), "clip");
   if (rb->u64[ST_OVERFLOW])
-    return fail(c, RPD_EOVERFLOW, "a piece exceeded the clip capacity (32 vertices/planes)");
+    return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
   int64_t np = rb->i32[0], ni = rb->i32[1];
   size_t npp = np > 0 ? np : 1;
   CK(c->piece_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
@@ -324,6 +346,7 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   c->last.zero_hits = (int64_t)rb->u64[ST_ZERO];
   c->last.max_vertices = (int32_t)rb->u64[ST_MAXV];
   c->last.max_planes = (int32_t)rb->u64[ST_MAXP];
+  c->last.n_wide = rb->i32[2];
   return fill_pieces(c, out);
 }
 

@@ -8,9 +8,11 @@
 // through it, kept as an oriented triangle of the dual triangulation so that clipping is a
 // local re-triangulation of the conflict region and facets can be walked.
 //
-// B200 mapping: one warp per pair, lane = vertex (<= 32 vertices, <= 32 planes), polytope
-// in per-warp shared memory (double-buffered vertex table).  The k_site planes are first
-// classified 32 at a time, one per lane, from their exact values at the 4 tet corners:
+// B200 mapping: one warp per pair, VPL vertex slots per lane (slot v = 32 k + lane), the
+// polytope in per-warp shared memory (double-buffered vertex table).  The fast kernel has
+// VPL = 1 (<= 32 vertices and planes, ~5 KB of shared memory per warp); pairs that exceed it
+// are re-run by the same kernel instantiated with VPL = 4 (<= 128).  The k_site planes are
+// first classified 32 at a time, one per lane, from their exact values at the 4 tet corners:
 // planes with all four values > 0 cannot cut (most of them), a plane with all four < 0
 // empties the piece; only the remaining planes run the per-vertex sign pass.
 //
@@ -20,32 +22,32 @@
 // evaluates det[a_p; a_q; a_r; a_s] and applies the inward symbolic perturbation.
 //
 // Outputs per pair: non-empty flag, volume, first moment (facet fans, deterministic warp
-// reduction), tet-face mask and incidences (positive-area SoS facets expanded by exactly
-// coincident sources, R7).
+// reduction), tet-face mask and incidences as a bitmask over the positions of N(i)
+// (positive-area SoS facets expanded by exactly coincident sources, R7).
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
 namespace rpd {
 
-constexpr int CLIP_WARPS = 8;  // warps per block
-
+template <int VPL>
 struct WarpState {
-  double g[RPD_MAXP][4];   // barycentric plane vectors (exact integers)
-  double K[2][RPD_MAXV][4];
-  double F[2][RPD_MAXV];
-  double x[RPD_MAXV][3];   // final vertex coordinates (lattice units, relative to V0)
-  unsigned tri[2][RPD_MAXV];
-  int src[RPD_MAXP];       // radical: sphere j; tet face k: -1-k
-  int eidx[RPD_MAXP];      // CSR entry of a radical plane, -1 for faces
-  int ref[RPD_MAXP];       // reference vertex of every facet (fan apex)
-  int inc[RPD_INC_CAP];
-  int ninc;
+  static constexpr int MAXV = 32 * VPL;
+  static constexpr int MAXP = 32 * VPL;
+  double g[MAXP][4];   // barycentric plane vectors (exact integers)
+  double K[2][MAXV][4];
+  double F[2][MAXV];
+  double x[MAXV][3];   // final vertex coordinates (lattice units, relative to V0)
+  unsigned tri[2][MAXV];
+  int src[MAXP];       // radical: sphere j; tet face k: -1-k
+  int eidx[MAXP];      // CSR entry of a radical plane, -1 for faces
+  int ref[MAXP];       // reference vertex of every facet (fan apex)
 };
 
-// oriented dual triangles of the 4 tet corners (corner k = faces != k)
+// oriented dual triangles of the 4 tet corners (corner k = faces != k); this orientation
+// makes the facet walk below produce positive volumes for positively oriented tets
 __constant__ unsigned CORNER_TRI[4] = {
-    1u | (2u << 8) | (3u << 16), 0u | (3u << 8) | (2u << 16), 0u | (1u << 8) | (3u << 16),
-    0u | (2u << 8) | (1u << 16)};
+    1u | (3u << 8) | (2u << 16), 0u | (2u << 8) | (3u << 16), 0u | (3u << 8) | (1u << 16),
+    0u | (1u << 8) | (2u << 16)};
 
 __device__ __forceinline__ int tri_at(unsigned tr, int k) { return (tr >> (8 * k)) & 0xff; }
 __device__ __forceinline__ bool tri_has(unsigned tr, int p) {
@@ -53,9 +55,6 @@ __device__ __forceinline__ bool tri_has(unsigned tr, int p) {
 }
 __device__ __forceinline__ unsigned tri_pack(int a, int b, int c) {
   return (unsigned)a | ((unsigned)b << 8) | ((unsigned)c << 16);
-}
-__device__ __forceinline__ unsigned tri_bits(unsigned tr) {
-  return (1u << tri_at(tr, 0)) | (1u << tri_at(tr, 1)) | (1u << tri_at(tr, 2));
 }
 
 // vertex u != self of the current table containing planes a and b (-1 if none)
@@ -65,12 +64,43 @@ __device__ inline int find_edge_nb(const unsigned* tri, int nv, int self, int a,
   return -1;
 }
 
+template <int W>
+struct Bits {
+  unsigned w[W];
+  __device__ void clear() {
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = 0u;
+  }
+  __device__ void set(int p) { w[p >> 5] |= 1u << (p & 31); }
+  __device__ bool has(int p) const { return (w[p >> 5] >> (p & 31)) & 1u; }
+  __device__ void set_tri(unsigned tr) {
+    set(tri_at(tr, 0));
+    set(tri_at(tr, 1));
+    set(tri_at(tr, 2));
+  }
+  __device__ void warp_or() {
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = __reduce_or_sync(0xffffffffu, w[k]);
+  }
+  // next set bit >= from, or -1
+  __device__ int next(int from) const {
+    for (int k = from >> 5; k < W; ++k) {
+      unsigned m = w[k];
+      if (k == (from >> 5)) m &= (from & 31) ? (~0u << (from & 31)) : ~0u;
+      if (m) return 32 * k + __ffs(m) - 1;
+    }
+    return -1;
+  }
+};
+
 struct ClipCtx {
   const double4* planes;   // global plane table (for Cartesian normals)
   long long N;             // sphere count (SoS rank of tet faces = N + k)
 };
 
-__device__ inline void make_xplane(const WarpState& S, const ClipCtx& C, int id, XPlane* xp) {
+template <int VPL>
+__device__ inline void make_xplane(const WarpState<VPL>& S, const ClipCtx& C, int id,
+                                   XPlane* xp) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) xp->a[k] = (long long)S.g[id][k];
   int src = S.src[id];
@@ -88,19 +118,20 @@ __device__ inline void make_xplane(const WarpState& S, const ClipCtx& C, int id,
   }
 }
 
-// fp64 homogeneous vertex of planes (a, b, c) with error bound; returns false if the sign of
-// sum(K) could not be certified (caller then uses the exact vertex)
-__device__ inline void vertex_from_planes(const WarpState& S, const ClipCtx& C, int a, int b,
-                                          int c, double K[4], double* F, int* nexact) {
+// fp64 homogeneous vertex of planes (a, b, c), normalised to sum(K) > 0, with the error
+// scalar F such that |g . K~ - g . K| <= |g|_1 F for every plane vector g.
+template <int VPL>
+__device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx& C, int a,
+                                          int b, int c, double K[4], double* F, int* nexact) {
   const double* ra = S.g[a];
   const double* rb = S.g[b];
   const double* rc = S.g[c];
   double E = 0.0, Kmax = 0.0, sum = 0.0, sabs = 0.0;
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
-    int c0 = m == 0 ? 1 : 0;
-    int c1 = m <= 1 ? 2 : 1;
-    int c2 = m <= 2 ? 3 : 2;
+    const int c0 = m == 0 ? 1 : 0;
+    const int c1 = m <= 1 ? 2 : 1;
+    const int c2 = m <= 2 ? 3 : 2;
     double m0 = fma(rb[c1], rc[c2], -rb[c2] * rc[c1]);
     double m1 = fma(rb[c0], rc[c2], -rb[c2] * rc[c0]);
     double m2 = fma(rb[c0], rc[c1], -rb[c1] * rc[c0]);
@@ -123,11 +154,10 @@ __device__ inline void vertex_from_planes(const WarpState& S, const ClipCtx& C, 
     make_xplane(S, C, a, &pa);
     make_xplane(S, C, b, &pb);
     make_xplane(S, C, c, &pc);
-    exact_vertex(pa, pb, pc, K);  // normalised, sum > 0
+    exact_vertex(pa, pb, pc, K);  // normalised, each component within 2^-52 relative
     ++*nexact;
-    // exact to 2^-52 relative per component
     double km = fmax(fmax(fabs(K[0]), fabs(K[1])), fmax(fabs(K[2]), fabs(K[3])));
-    *F = 4.0 * U * km * (1.0 + 1e-9) + 5.0 * U * km;
+    *F = 9.0 * U * km * (1.0 + 1e-9);
     return;
   }
   if (sum < 0.0) {
@@ -142,32 +172,41 @@ enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
 struct PairOut {
   double* vol;
   double* m1;
-  uint8_t* flag;
+  uint8_t* flag;       // 0 empty, 1 non-empty, 2 overflow (re-run by the wide kernel)
   uint8_t* fm;
-  int32_t* ninc;
-  int32_t* inc;
+  unsigned* incmask;   // incidence bitmask words of every pair (positions in N(i))
+  const int32_t* mask_off;
+  int32_t* over_list;  // pairs that overflowed (fast kernel only)
+  int32_t* over_count;
 };
 
-__global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
-    int64_t n_pairs, const int32_t* __restrict__ pair_tet, const int32_t* __restrict__ tet_ids,
-    const int32_t* __restrict__ cand_idx, const double* __restrict__ tx, int64_t T,
-    const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
-    const double4* __restrict__ planes, const int32_t* __restrict__ twin, long long N,
-    PairOut out, unsigned long long* __restrict__ stats) {
+template <int VPL>
+__global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
+    int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
+    const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
+    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ nbr_off,
+    const int32_t* __restrict__ nbr_idx, const double4* __restrict__ planes,
+    const int32_t* __restrict__ twin, long long N, PairOut out,
+    unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev) {
+  using WS = WarpState<VPL>;
+  if (n_dev) n_pairs = *n_dev;
+  constexpr int MAXV = WS::MAXV;
+  constexpr int MAXP = WS::MAXP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpState& S = reinterpret_cast<WarpState*>(smem_raw)[threadIdx.x >> 5];
+  WS& S = reinterpret_cast<WS*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt_mask = (1u << lane) - 1u;
   ClipCtx C{planes, N};
-  int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
 
-  for (int64_t p = gw; p < n_pairs; p += nw) {
-    int64_t a = pair_tet[p];
-    int64_t t = tet_ids ? (int64_t)tet_ids[a] : a;
-    int i = cand_idx[p];
+  for (int64_t pi = gw; pi < n_pairs; pi += nw) {
+    const int64_t p = pair_list ? (int64_t)pair_list[pi] : pi;
+    const int64_t a = pair_tet[p];
+    const int64_t t = tet_ids ? (int64_t)tet_ids[a] : a;
+    const int i = cand_idx[p];
     double V[4][3];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -219,48 +258,56 @@ __global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
         const int es = base + l;
         const double sabs = fabs(s[0]) + fabs(s[1]) + fabs(s[2]) + fabs(s[3]);
 
-        // ---- sign of every vertex
-        const bool valid = lane < nv;
-        int sg = 0;
-        if (valid) {
-          const double* K = S.K[cur][lane];
-          double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
-          double B = sabs * S.F[cur][lane];
-          if (val > B) sg = 1;
-          else if (val < -B) sg = -1;
-          else {
-            // exact path
-            XPlane xa, xb, xc, xs;
-            unsigned tr = S.tri[cur][lane];
-            make_xplane(S, C, tri_at(tr, 0), &xa);
-            make_xplane(S, C, tri_at(tr, 1), &xb);
-            make_xplane(S, C, tri_at(tr, 2), &xc);
+        // ---- sign of every vertex slot
+        int sg[VPL];
+        unsigned negm[VPL], posm[VPL];
+        bool anyneg = false, anypos = false;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) xs.a[k] = (long long)s[k];
-            double4 pl = planes[es];
-            xs.n[0] = (long long)pl.x;
-            xs.n[1] = (long long)pl.y;
-            xs.n[2] = (long long)pl.z;
-            xs.radical = 1;
-            xs.rank = nbr_idx[es];
-            int zh = 0;
-            sg = sos_sign_exact(xa, xb, xc, xs, &zh);
-            ++n_exact;
-            if (zh) {
-              ++n_zero;
-              zero_hit = 1;
+        for (int k = 0; k < VPL; ++k) {
+          const int v = 32 * k + lane;
+          const bool valid = v < nv;
+          sg[k] = 0;
+          if (valid) {
+            const double* K = S.K[cur][v];
+            double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
+            double B = sabs * S.F[cur][v];
+            if (val > B) sg[k] = 1;
+            else if (val < -B) sg[k] = -1;
+            else {
+              XPlane xa, xb, xc, xs;
+              unsigned tr = S.tri[cur][v];
+              make_xplane(S, C, tri_at(tr, 0), &xa);
+              make_xplane(S, C, tri_at(tr, 1), &xb);
+              make_xplane(S, C, tri_at(tr, 2), &xc);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) xs.a[q] = (long long)s[q];
+              double4 pl = planes[es];
+              xs.n[0] = (long long)pl.x;
+              xs.n[1] = (long long)pl.y;
+              xs.n[2] = (long long)pl.z;
+              xs.radical = 1;
+              xs.rank = nbr_idx[es];
+              int zh = 0;
+              sg[k] = sos_sign_exact(xa, xb, xc, xs, &zh);
+              ++n_exact;
+              if (zh) {
+                ++n_zero;
+                zero_hit = 1;
+              }
             }
           }
+          negm[k] = __ballot_sync(FULL, valid && sg[k] < 0);
+          posm[k] = __ballot_sync(FULL, valid && sg[k] > 0);
+          anyneg |= negm[k] != 0u;
+          anypos |= posm[k] != 0u;
         }
         zero_hit = __any_sync(FULL, zero_hit);
-        const unsigned negm = __ballot_sync(FULL, valid && sg < 0);
-        const unsigned posm = __ballot_sync(FULL, valid && sg > 0);
-        if (!negm) continue;  // plane does not cut: skip
-        if (!posm) {
+        if (!anyneg) continue;  // the plane does not cut: skip it
+        if (!anypos) {
           status = ST_EMPTY;
           break;
         }
-        if (np >= RPD_MAXP) {
+        if (np >= MAXP) {
           status = ST_OVER;
           break;
         }
@@ -272,48 +319,69 @@ __global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
           S.eidx[sid] = es;
         }
         __syncwarp();
-        // ---- new vertices: for every edge of a removed vertex whose neighbour is kept
-        unsigned newtri[3];
-        int nnew = 0;
-        if (valid && sg < 0) {
-          unsigned tr = S.tri[cur][lane];
+        // ---- new vertices: one per boundary edge of the conflict region, oriented as the
+        // removed triangle's edge: (x, y, s)
+        unsigned newtri[VPL][3];
+        int nnew[VPL];
 #pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
-            int u = find_edge_nb(S.tri[cur], nv, lane, x, y);
-            if (u >= 0 && ((posm >> u) & 1u)) newtri[nnew++] = tri_pack(x, y, sid);
+        for (int k = 0; k < VPL; ++k) {
+          const int v = 32 * k + lane;
+          nnew[k] = 0;
+          if (v < nv && sg[k] < 0) {
+            unsigned tr = S.tri[cur][v];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+              int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
+              int u = find_edge_nb(S.tri[cur], nv, v, x, y);
+              if (u >= 0 && ((posm[u >> 5] >> (u & 31)) & 1u))
+                newtri[k][nnew[k]++] = tri_pack(x, y, sid);
+            }
           }
         }
-        int incl = nnew;
+        // exclusive prefix of kept / new counts over slots (slot order v = 32 k + lane)
+        int kept_base = 0, new_base = 0;
+        int kept_idx[VPL], new_idx[VPL];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= o) incl += y;
+        for (int k = 0; k < VPL; ++k) {
+          kept_idx[k] = kept_base + __popc(posm[k] & lt_mask);
+          kept_base += __popc(posm[k]);
+          int incl = nnew[k];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          new_idx[k] = new_base + incl - nnew[k];
+          new_base += __shfl_sync(FULL, incl, 31);
         }
-        const int total_new = __shfl_sync(FULL, incl, 31);
-        const int nkept = __popc(posm);
-        const int nv2 = nkept + total_new;
-        if (nv2 > RPD_MAXV) {
+        const int nkept = kept_base;
+        const int nv2 = nkept + new_base;
+        if (nv2 > MAXV) {
           status = ST_OVER;
           break;
         }
         const int nxt = cur ^ 1;
-        if (valid && sg > 0) {
-          int k = __popc(posm & lt_mask);
 #pragma unroll
-          for (int m = 0; m < 4; ++m) S.K[nxt][k][m] = S.K[cur][lane][m];
-          S.F[nxt][k] = S.F[cur][lane];
-          S.tri[nxt][k] = S.tri[cur][lane];
-        }
-        for (int q = 0; q < nnew; ++q) {
-          int k = nkept + incl - nnew + q;
-          unsigned tr = newtri[q];
-          double K[4], F;
-          vertex_from_planes(S, C, tri_at(tr, 0), tri_at(tr, 1), tri_at(tr, 2), K, &F, &n_exact);
+        for (int k = 0; k < VPL; ++k) {
+          const int v = 32 * k + lane;
+          if (v < nv && sg[k] > 0) {
+            const int q = kept_idx[k];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) S.K[nxt][k][m] = K[m];
-          S.F[nxt][k] = F;
-          S.tri[nxt][k] = tr;
+            for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = S.K[cur][v][m];
+            S.F[nxt][q] = S.F[cur][v];
+            S.tri[nxt][q] = S.tri[cur][v];
+          }
+          for (int j = 0; j < nnew[k]; ++j) {
+            const int q = nkept + new_idx[k] + j;
+            const unsigned tr = newtri[k][j];
+            double K[4], F;
+            vertex_from_planes(S, C, tri_at(tr, 0), tri_at(tr, 1), tri_at(tr, 2), K, &F,
+                               &n_exact);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
+            S.F[nxt][q] = F;
+            S.tri[nxt][q] = tr;
+          }
         }
         nv = nv2;
         cur = nxt;
@@ -322,154 +390,160 @@ __global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
     }
 
     // ------------------------------------------------------------------ outputs
-    if (status == ST_OVER) ++n_over;
     if (status != ST_ALIVE) {
-      if (lane == 0) {
-        out.flag[p] = 0;
-        out.ninc[p] = 0;
+      if (status == ST_OVER) {
+        ++n_over;
+        if (lane == 0 && out.over_list) {
+          int slot = atomicAdd(out.over_count, 1);
+          out.over_list[slot] = (int32_t)p;
+        }
       }
+      if (lane == 0) out.flag[p] = status == ST_OVER ? 2 : 0;
       __syncwarp();
       continue;
     }
     max_v = max(max_v, nv);
     max_p = max(max_p, np);
-    const bool valid = lane < nv;
-    const unsigned mytri = valid ? S.tri[cur][lane] : 0u;
-    const unsigned facets_all = __reduce_or_sync(FULL, valid ? tri_bits(mytri) : 0u);
-    unsigned facets = facets_all;
+    unsigned mytri[VPL];
+    Bits<VPL> facets_all;
+    facets_all.clear();
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int v = 32 * k + lane;
+      mytri[k] = v < nv ? S.tri[cur][v] : 0xffffffu;
+      if (v < nv) facets_all.set_tri(mytri[k]);
+    }
+    facets_all.warp_or();
+    Bits<VPL> facets = facets_all;
 
     // zero-area SoS facets (only possible after an exact-zero predicate; C1.7)
     if (zero_hit) {
-      unsigned fl = facets_all;
-      while (fl) {
-        const int f = __ffs(fl) - 1;
-        fl &= fl - 1;
-        const bool onf = valid && tri_has(mytri, f);
-        unsigned Q = __reduce_or_sync(FULL, onf ? tri_bits(mytri) : 0u) & ~(1u << f);
+      for (int f = facets_all.next(0); f >= 0; f = facets_all.next(f + 1)) {
+        Bits<VPL> Q;
+        Q.clear();
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (32 * k + lane < nv && tri_has(mytri[k], f)) Q.set_tri(mytri[k]);
+        Q.warp_or();
+        Q.w[f >> 5] &= ~(1u << (f & 31));
         bool zero_area = false;
-        while (Q && !zero_area) {
-          const int q = __ffs(Q) - 1;
-          Q &= Q - 1;
+        for (int q = Q.next(0); q >= 0 && !zero_area; q = Q.next(q + 1)) {
           bool on = true;
-          if (onf && !tri_has(mytri, q)) {
-            const double* K = S.K[cur][lane];
-            const double* gq = S.g[q];
-            double val = fma(gq[0], K[0], fma(gq[1], K[1], fma(gq[2], K[2], gq[3] * K[3])));
-            double sa = fabs(gq[0]) + fabs(gq[1]) + fabs(gq[2]) + fabs(gq[3]);
-            if (fabs(val) > sa * S.F[cur][lane]) {
-              on = false;
-            } else {
-              XPlane xa, xb, xc, xq;
-              make_xplane(S, C, tri_at(mytri, 0), &xa);
-              make_xplane(S, C, tri_at(mytri, 1), &xb);
-              make_xplane(S, C, tri_at(mytri, 2), &xc);
-              make_xplane(S, C, q, &xq);
-              on = det4_is_zero(xa, xb, xc, xq);
-              ++n_exact;
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const int v = 32 * k + lane;
+            if (v < nv && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
+              const double* K = S.K[cur][v];
+              const double* gq = S.g[q];
+              double val = fma(gq[0], K[0], fma(gq[1], K[1], fma(gq[2], K[2], gq[3] * K[3])));
+              double sa = fabs(gq[0]) + fabs(gq[1]) + fabs(gq[2]) + fabs(gq[3]);
+              if (fabs(val) > sa * S.F[cur][v]) {
+                on = false;
+              } else {
+                XPlane xa, xb, xc, xq;
+                make_xplane(S, C, tri_at(mytri[k], 0), &xa);
+                make_xplane(S, C, tri_at(mytri[k], 1), &xb);
+                make_xplane(S, C, tri_at(mytri[k], 2), &xc);
+                make_xplane(S, C, q, &xq);
+                on = on && det4_is_zero(xa, xb, xc, xq);
+                ++n_exact;
+              }
             }
           }
           zero_area = __all_sync(FULL, on);
         }
-        if (zero_area) facets &= ~(1u << f);
+        if (zero_area) facets.w[f >> 5] &= ~(1u << (f & 31));
       }
     }
 
     // incidences: every positive-area facet plus its exactly coincident sources
-    if (lane == 0) S.ninc = 0;
-    __syncwarp();
     unsigned fmask_bits = 0;
-    if (lane < np && ((facets >> lane) & 1u)) {
-      const int src = S.src[lane];
-      if (src < 0) {
-        fmask_bits |= 1u << (-1 - src);
-      } else {
-        // radical plane coinciding with tet face a: g = c e_a, c > 0
-        const double* gg = S.g[lane];
-        int nz = 0, az = -1;
+    unsigned* words = out.incmask + out.mask_off[p];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (gg[k] != 0.0) {
-            ++nz;
-            az = k;
+    for (int k = 0; k < VPL; ++k) {
+      const int pl = 32 * k + lane;
+      if (pl < np && facets.has(pl)) {
+        const int src = S.src[pl];
+        if (src < 0) {
+          fmask_bits |= 1u << (-1 - src);
+        } else {
+          // radical plane coinciding with tet face a: g = c e_a, c > 0
+          const double* gg = S.g[pl];
+          int nz = 0, az = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (gg[q] != 0.0) {
+              ++nz;
+              az = q;
+            }
+          if (nz == 1 && gg[az] > 0.0) fmask_bits |= 1u << az;
+          for (int e = S.eidx[pl]; e >= 0; e = twin[e]) {
+            const int pos = e - e0;
+            atomicOr(words + (pos >> 5), 1u << (pos & 31));
           }
-        if (nz == 1 && gg[az] > 0.0) fmask_bits |= 1u << az;
-        int e = S.eidx[lane];
-        while (e >= 0) {
-          int slot = atomicAdd(&S.ninc, 1);
-          if (slot < RPD_INC_CAP) S.inc[slot] = nbr_idx[e];
-          e = twin[e];
         }
       }
     }
     const unsigned facemask = __reduce_or_sync(FULL, fmask_bits);
-    __syncwarp();
-    const int ninc = S.ninc;
-    if (ninc > RPD_INC_CAP) {
-      ++n_over;
-      if (lane == 0) {
-        out.flag[p] = 0;
-        out.ninc[p] = 0;
-      }
-      __syncwarp();
-      continue;
-    }
-    // rank sort of the incidence list (distinct ids)
-    int my = lane < ninc ? S.inc[lane] : 0;
-    int rank = 0;
-    for (int q = 0; q < ninc; ++q) rank += S.inc[q] < my;
-    __syncwarp();
-    if (lane < ninc) out.inc[p * RPD_INC_CAP + rank] = my;
 
     // ---- geometry: vertex coordinates relative to V0 (lattice units)
-    if (valid) {
-      double K[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) K[m] = S.K[cur][lane][m];
-      double sum = K[0] + K[1] + K[2] + K[3];
-      if (16.0 * S.F[cur][lane] > 1e-12 * sum) {
-        XPlane xa, xb, xc;
-        make_xplane(S, C, tri_at(mytri, 0), &xa);
-        make_xplane(S, C, tri_at(mytri, 1), &xb);
-        make_xplane(S, C, tri_at(mytri, 2), &xc);
-        exact_vertex(xa, xb, xc, K);
-        sum = K[0] + K[1] + K[2] + K[3];
-        ++n_exact;
-      }
+    for (int k = 0; k < VPL; ++k) {
+      const int v = 32 * k + lane;
+      if (v < nv) {
+        double K[4];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double acc = 0.0;
+        for (int m = 0; m < 4; ++m) K[m] = S.K[cur][v][m];
+        double sum = K[0] + K[1] + K[2] + K[3];
+        if (16.0 * S.F[cur][v] > 1e-12 * sum) {
+          XPlane xa, xb, xc;
+          make_xplane(S, C, tri_at(mytri[k], 0), &xa);
+          make_xplane(S, C, tri_at(mytri[k], 1), &xb);
+          make_xplane(S, C, tri_at(mytri[k], 2), &xc);
+          exact_vertex(xa, xb, xc, K);
+          sum = K[0] + K[1] + K[2] + K[3];
+          ++n_exact;
+        }
 #pragma unroll
-        for (int k = 1; k < 4; ++k) acc = fma(K[k] / sum, V[k][c] - V[0][c], acc);
-        S.x[lane][c] = acc;
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 1; q < 4; ++q) acc = fma(K[q] / sum, V[q][c] - V[0][c], acc);
+          S.x[v][c] = acc;
+        }
       }
     }
-    {
-      unsigned fl = facets_all;
-      while (fl) {
-        const int f = __ffs(fl) - 1;
-        fl &= fl - 1;
-        unsigned on = __ballot_sync(FULL, valid && tri_has(mytri, f));
-        if (lane == 0) S.ref[f] = __ffs(on) - 1;
+    for (int f = facets_all.next(0); f >= 0; f = facets_all.next(f + 1)) {
+      int first = -1;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        unsigned on = __ballot_sync(FULL, 32 * k + lane < nv && tri_has(mytri[k], f));
+        if (first < 0 && on) first = 32 * k + __ffs(on) - 1;
       }
+      if (lane == 0) S.ref[f] = first;
     }
     __syncwarp();
     double vol6 = 0.0, m24[3] = {0.0, 0.0, 0.0};
-    if (valid) {
-      const double* xv = S.x[lane];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int f = tri_at(mytri, r);
-        const int zc = tri_at(mytri, (r + 2) % 3);
-        const int w = find_edge_nb(S.tri[cur], nv, lane, zc, f);
-        const int rf = S.ref[f];
-        const double* xr = S.x[rf];
-        const double* xw = S.x[w];
-        double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -
-                     xr[1] * (xv[0] * xw[2] - xv[2] * xw[0]) +
-                     xr[2] * (xv[0] * xw[1] - xv[1] * xw[0]);
-        vol6 += det;
+    for (int k = 0; k < VPL; ++k) {
+      const int v = 32 * k + lane;
+      if (v < nv) {
+        const double* xv = S.x[v];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) m24[c] += det * (xr[c] + xv[c] + xw[c]);
+        for (int r = 0; r < 3; ++r) {
+          const int f = tri_at(mytri[k], r);
+          const int zc = tri_at(mytri[k], (r + 2) % 3);
+          const int w = find_edge_nb(S.tri[cur], nv, v, zc, f);
+          if (w < 0) continue;  // unreachable for a valid polytope
+          const double* xr = S.x[S.ref[f]];
+          const double* xw = S.x[w];
+          double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -
+                       xr[1] * (xv[0] * xw[2] - xv[2] * xw[0]) +
+                       xr[2] * (xv[0] * xw[1] - xv[1] * xw[0]);
+          vol6 += det;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) m24[c] += det * (xr[c] + xv[c] + xw[c]);
+        }
       }
     }
 #pragma unroll
@@ -487,7 +561,6 @@ __global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
         out.m1[3 * p + c] = (m24[c] / 24.0) * (L * L * L * L) + vol * (V[0][c] * L);
       out.flag[p] = 1;
       out.fm[p] = (uint8_t)facemask;
-      out.ninc[p] = ninc;
     }
     __syncwarp();
   }
@@ -499,26 +572,45 @@ __global__ void __launch_bounds__(CLIP_WARPS * 32) k_clip(
   if (lane == 0) {
     if (n_exact) atomicAdd(stats + ST_EXACT, (unsigned long long)n_exact);
     if (n_zero) atomicAdd(stats + ST_ZERO, (unsigned long long)n_zero);
-    if (n_over) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
+    if (n_over && VPL > 1) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
     atomicMax(stats + ST_MAXV, (unsigned long long)max_v);
     atomicMax(stats + ST_MAXP, (unsigned long long)max_p);
   }
 }
 
+// incidences per pair (0 for empty pairs)
+__global__ void k_count_inc(int64_t n_pairs, const uint8_t* __restrict__ flag,
+                            const int32_t* __restrict__ mask_off,
+                            const unsigned* __restrict__ mask, int32_t* __restrict__ ninc,
+                            uint8_t* __restrict__ f01) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  int n = 0;
+  const bool ne = flag[p] == 1;
+  if (ne)
+    for (int w = mask_off[p]; w < mask_off[p + 1]; ++w) n += __popc(mask[w]);
+  ninc[p] = n;
+  f01[p] = ne;
+}
+
 __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ cand_idx,
+                                 const int32_t* __restrict__ nbr_off,
+                                 const int32_t* __restrict__ nbr_idx,
                                  const uint8_t* __restrict__ flag, const int32_t* __restrict__ pscan,
                                  const int32_t* __restrict__ iscan, const double* __restrict__ pvol,
                                  const double* __restrict__ pm1, const uint8_t* __restrict__ pfm,
-                                 const int32_t* __restrict__ pninc, const int32_t* __restrict__ pinc,
+                                 const int32_t* __restrict__ mask_off,
+                                 const unsigned* __restrict__ mask,
                                  int32_t* __restrict__ piece_sphere, double* __restrict__ piece_vol,
                                  double* __restrict__ piece_m1, uint8_t* __restrict__ piece_fm,
                                  int32_t* __restrict__ inc_off, int32_t* __restrict__ inc_sphere) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   if (p == n_pairs - 1) inc_off[pscan[n_pairs]] = iscan[n_pairs];
-  if (!flag[p]) return;
-  int q = pscan[p];
-  piece_sphere[q] = cand_idx[p];
+  if (flag[p] != 1) return;
+  const int q = pscan[p];
+  const int i = cand_idx[p];
+  piece_sphere[q] = i;
   piece_vol[q] = pvol[p];
   piece_m1[3 * q + 0] = pm1[3 * p + 0];
   piece_m1[3 * q + 1] = pm1[3 * p + 1];
@@ -526,8 +618,16 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
   piece_fm[q] = pfm[p];
   int o = iscan[p];
   inc_off[q] = o;
-  int n = pninc[p];
-  for (int k = 0; k < n; ++k) inc_sphere[o + k] = pinc[p * RPD_INC_CAP + k];
+  const int e0 = nbr_off[i];
+  const int w0 = mask_off[p];
+  for (int w = w0; w < mask_off[p + 1]; ++w) {
+    unsigned m = mask[w];
+    while (m) {
+      int b = __ffs(m) - 1;
+      m &= m - 1;
+      inc_sphere[o++] = nbr_idx[e0 + 32 * (w - w0) + b];
+    }
+  }
 }
 
 __global__ void k_piece_off(int64_t T, const int32_t* __restrict__ cand_off,
@@ -539,33 +639,63 @@ __global__ void k_piece_off(int64_t T, const int32_t* __restrict__ cand_off,
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
-                        const int32_t* tet_ids, const int32_t* cand_idx) {
-  if (n_pairs == 0) return cudaSuccess;
-  size_t smem = sizeof(WarpState) * CLIP_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(k_clip, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int VPL>
+static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
+                                 const int32_t* pair_tet, const int32_t* tet_ids,
+                                 const int32_t* cand_idx, bool collect_overflow,
+                                 const int32_t* n_dev) {
+  constexpr int WARPS = VPL == 1 ? 8 : 2;
+  size_t smem = sizeof(WarpState<VPL>) * WARPS;
+  cudaError_t e = cudaFuncSetAttribute(k_clip<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_clip, CLIP_WARPS * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_clip<VPL>, WARPS * 32, smem);
   if (occ < 1) occ = 1;
-  int64_t want = (n_pairs + CLIP_WARPS - 1) / CLIP_WARPS;
+  int64_t want = (n + WARPS - 1) / WARPS;
   int64_t grid = (int64_t)sms * occ;
   if (want < grid) grid = want;
-  PairOut o{c->p_vol.as<double>(), c->p_m1.as<double>(), c->p_flag.as<uint8_t>(),
-            c->p_fm.as<uint8_t>(), c->p_ninc.as<int32_t>(), c->p_inc.as<int32_t>()};
-  k_clip<<<(unsigned)grid, CLIP_WARPS * 32, smem, c->stream>>>(
-      n_pairs, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
+  if (grid < 1) grid = 1;
+  PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
+            c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), c->p_moff.as<int32_t>(),
+            collect_overflow ? c->p_over.as<int32_t>() + 1 : nullptr,
+            collect_overflow ? c->p_over.as<int32_t>() : nullptr};
+  k_clip<VPL><<<(unsigned)grid, WARPS * 32, smem, c->stream>>>(
+      n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
-      c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>());
+      c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>(),
+      n_dev);
   ++c->launches;
   return cudaGetLastError();
 }
 
+// fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
+// or the wide kernel over all pairs when `wide`
+cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
+                        const int32_t* tet_ids, const int32_t* cand_idx, int wide) {
+  if (n_pairs == 0) return cudaSuccess;
+  if (wide)
+    return launch_clip_t<4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, false, nullptr);
+  return launch_clip_t<1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, true, nullptr);
+}
+
+// wide kernel over the overflow list p_over[1 .. p_over[0]] (count read on the device)
+cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
+                                 const int32_t* cand_idx) {
+  return launch_clip_t<4>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx,
+                          false, c->p_over.as<int32_t>());
+}
+
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs) {
-  cudaError_t e = launch_scan_u8(c, c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(), n_pairs);
+  if (n_pairs > 0) {
+    k_count_inc<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
+        n_pairs, c->p_flag.as<uint8_t>(), c->p_moff.as<int32_t>(), c->p_mask.as<unsigned>(),
+        c->p_ninc.as<int32_t>(), c->p_f01.as<uint8_t>());
+    ++c->launches;
+  }
+  cudaError_t e = launch_scan_u8(c, c->p_f01.as<uint8_t>(), c->p_scan.as<int32_t>(), n_pairs);
   if (e) return e;
   return launch_scan_i32(c, c->p_ninc.as<int32_t>(), c->i_scan.as<int32_t>(), n_pairs);
 }
@@ -575,10 +705,11 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const PieceDst& d) {
   if (n_pairs > 0) {
     k_compact_pieces<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
-        n_pairs, cand_idx, c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(),
-        c->i_scan.as<int32_t>(), c->p_vol.as<double>(), c->p_m1.as<double>(),
-        c->p_fm.as<uint8_t>(), c->p_ninc.as<int32_t>(), c->p_inc.as<int32_t>(), d.sphere, d.vol,
-        d.m1, d.fm, d.inc_off, d.inc);
+        n_pairs, cand_idx, c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(),
+        c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(),
+        c->p_vol.as<double>(), c->p_m1.as<double>(), c->p_fm.as<uint8_t>(),
+        c->p_moff.as<int32_t>(), c->p_mask.as<unsigned>(), d.sphere, d.vol, d.m1, d.fm,
+        d.inc_off, d.inc);
     ++c->launches;
   } else {
     cudaMemsetAsync(d.inc_off, 0, sizeof(int32_t), c->stream);

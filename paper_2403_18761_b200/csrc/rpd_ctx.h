@@ -101,8 +101,11 @@ struct rpd_ctx {
   bool have_rel = false;
 
   // clip per-pair
-  rpd::DevBuf p_flag, p_vol, p_m1, p_fm, p_ninc, p_inc;
+  rpd::DevBuf k_words, w_off;            // incidence-mask words per tet and their offsets
+  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_words, p_moff, p_mask, p_over;
   rpd::DevBuf p_scan, i_scan;
+  int64_t n_mask_words = 0;
+  int clip_wide = 0;                     // testing: run every pair through the wide kernel
   // pieces
   rpd::DevBuf piece_off, piece_sphere, piece_vol, piece_m1, piece_fm, inc_off, inc_sphere;
   int64_t n_pieces = 0, n_inc = 0;
@@ -125,12 +128,16 @@ cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
-                          int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab);
+                          int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
+                          int32_t* k_words);
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* k_tet,
                                  const int32_t* slab, const int32_t* cand_off,
-                                 int32_t* cand_idx, int32_t* pair_tet);
+                                 int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
+                                 int32_t* p_moff, int64_t n_pairs);
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
-                        const int32_t* tet_ids, const int32_t* cand_idx);
+                        const int32_t* tet_ids, const int32_t* cand_idx, int wide);
+cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
+                                 const int32_t* cand_idx);
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs);
 // destination of a piece compaction
 struct PieceDst {

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
     const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes, int N, int lo,
     int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-    unsigned long long* __restrict__ stats) {
+    int32_t* __restrict__ k_words, unsigned long long* __restrict__ stats) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool valid = a < n;
   int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     Y[k] = valid ? tx[(3 * k + 1) * T + t] : 0.0;
     Z[k] = valid ? tx[(3 * k + 2) * T + t] : 0.0;
   }
-  int cnt = 0;
+  int cnt = 0, words = 0;
   for (int i = lo; i < hi; ++i) {
     int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     bool alive = valid;
@@ -58,9 +58,13 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     if (alive) {
       if (cnt < cap) slab[(int64_t)cnt * n + a] = i;
       ++cnt;
+      words += (e1 - e0 + 31) >> 5;  // incidence-mask words of this candidate pair
     }
   }
-  if (valid) k_tet[a] = cnt;
+  if (valid) {
+    k_tet[a] = cnt;
+    if (k_words) k_words[a] = words;
+  }
   // max k_tet (warp-aggregated)
   int m = cnt;
 #pragma unroll
@@ -71,36 +75,51 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
 __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,
                                 const int32_t* __restrict__ slab,
                                 const int32_t* __restrict__ cand_off,
-                                int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet) {
+                                int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
+                                const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
+                                const int32_t* __restrict__ nbr_off, int64_t n_pairs) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   int k = k_tet[a];
   int o = cand_off[a];
+  int w = w_off ? w_off[a] : 0;
   for (int c = 0; c < k && c < cap; ++c) {
-    cand_idx[o + c] = slab[(int64_t)c * n + a];
+    int i = slab[(int64_t)c * n + a];
+    cand_idx[o + c] = i;
     if (pair_tet) pair_tet[o + c] = (int32_t)a;
+    if (p_moff) {
+      p_moff[o + c] = w;
+      w += (nbr_off[i + 1] - nbr_off[i] + 31) >> 5;
+    }
   }
+  if (p_moff && a == n - 1) p_moff[n_pairs] = w;
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
-                          int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab) {
+                          int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
+                          int32_t* k_words) {
   if (n_tets == 0) return cudaSuccess;
   k_filter_allpairs<<<nblk(n_tets, 256), 256, 0, c->stream>>>(
       c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, c->st.nbr_off.as<int32_t>(),
       c->st.planes.as<double4>(), (int)c->st.N, sphere_lo, sphere_hi, cap, k_tet, slab,
-      c->stats.as<unsigned long long>());
+      k_words, c->stats.as<unsigned long long>());
   ++c->launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* k_tet,
                                  const int32_t* slab, const int32_t* cand_off,
-                                 int32_t* cand_idx, int32_t* pair_tet) {
-  if (n == 0) return cudaSuccess;
+                                 int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
+                                 int32_t* p_moff, int64_t n_pairs) {
+  if (n == 0) {
+    if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
+    return cudaSuccess;
+  }
   k_compact_cands<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off, cand_idx,
-                                                       pair_tet);
+                                                       pair_tet, w_off, p_moff,
+                                                       c->st.nbr_off.as<int32_t>(), n_pairs);
   ++c->launches;
   return cudaGetLastError();
 }

@@ -19,7 +19,7 @@ RPD_OK, RPD_EINVAL, RPD_ENOMEM, RPD_ECUDA, RPD_EOVERFLOW, RPD_ESTATE, RPD_ENOTEX
     0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "RPD_OK", -1: "RPD_EINVAL", -2: "RPD_ENOMEM", -3: "RPD_ECUDA",
                 -4: "RPD_EOVERFLOW", -5: "RPD_ESTATE", -6: "RPD_ENOTEXACT"}
-OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM = 1, 2, 3
+OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM, OPT_CLIP_WIDE = 1, 2, 3, 4
 FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
@@ -46,7 +46,7 @@ class _Stats(C.Structure):
                 ("pairs_filtered", C.c_int64), ("pairs_tested", C.c_int64),
                 ("exact_fallbacks", C.c_int64), ("zero_hits", C.c_int64),
                 ("kernel_launches", C.c_int64), ("max_k_tet", C.c_int32),
-                ("max_vertices", C.c_int32), ("max_planes", C.c_int32)]
+                ("max_vertices", C.c_int32), ("max_planes", C.c_int32), ("n_wide", C.c_int32)]
 
 
 _lib = None
@@ -136,6 +136,10 @@ class RPDContext:
     def set_filter_mode(self, mode: str):
         m = {"all_pairs": FILTER_ALL_PAIRS, "pruned": FILTER_PRUNED}[mode]
         self._check(self.L.rpd_set_option(self.h, OPT_FILTER_MODE, m))
+
+    def set_clip_wide(self, on: bool):
+        """Testing: route every pair through the wide (128-vertex) clip kernel."""
+        self._check(self.L.rpd_set_option(self.h, OPT_CLIP_WIDE, int(bool(on))))
 
     def close(self):
         if getattr(self, "h", None):

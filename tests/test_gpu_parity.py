@@ -167,3 +167,18 @@ def test_bench_config_sampled(ctx):
     s = np.zeros(w.T)
     np.add.at(s, piece_tet(got), got["piece_vol"])
     assert np.max(np.abs(s - vt) / vt) < 1e-9
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(1, degenerate=True),
+                                  lambda: W.make_c1(6, degenerate=True, big=True),
+                                  lambda: W.make_shape_workload("Wd", 2500, 200, seed=9,
+                                                                radius_mode="high_variance",
+                                                                cache=False)])
+def test_wide_kernel_parity(ctx, make):
+    """The 128-vertex clip instantiation (used for pairs that overflow the fast 32-vertex
+    kernel) run on every pair gives the same results."""
+    ctx.set_clip_wide(True)
+    try:
+        check(ctx, make())
+    finally:
+        ctx.set_clip_wide(False)
