@@ -302,6 +302,19 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
           anypos |= posm[k] != 0u;
         }
         zero_hit = __any_sync(FULL, zero_hit);
+#ifdef RPD_TRACE
+        if (p == RPD_TRACE) {
+          for (int k = 0; k < VPL; ++k) {
+            int v = 32 * k + lane;
+            if (v < nv) {
+              unsigned tr = S.tri[cur][v];
+              printf("plane j=%d es=%d v=%d tri=(%d,%d,%d) sg=%d K=(%g,%g,%g,%g) F=%g\n", nbr_idx[es], es, v,
+                     tri_at(tr,0), tri_at(tr,1), tri_at(tr,2), sg[k], S.K[cur][v][0], S.K[cur][v][1],
+                     S.K[cur][v][2], S.K[cur][v][3], S.F[cur][v]);
+            }
+          }
+        }
+#endif
         if (!anyneg) continue;  // the plane does not cut: skip it
         if (!anypos) {
           status = ST_EMPTY;

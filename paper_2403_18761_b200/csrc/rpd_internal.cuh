@@ -38,7 +38,7 @@ constexpr double U = 1.1102230246251565e-16;  // 2^-53
 __host__ __device__ inline long long d2ll(double x) { return (long long)x; }
 
 // det of 3x3 integer matrix rows a,b,c (int64 entries, result must fit int128)
-__device__ inline i128 det3_i(const long long* a, const long long* b, const long long* c) {
+__host__ __device__ inline i128 det3_i(const long long* a, const long long* b, const long long* c) {
   i128 m0 = (i128)b[1] * c[2] - (i128)b[2] * c[1];
   i128 m1 = (i128)b[0] * c[2] - (i128)b[2] * c[0];
   i128 m2 = (i128)b[0] * c[1] - (i128)b[1] * c[0];
@@ -47,7 +47,7 @@ __device__ inline i128 det3_i(const long long* a, const long long* b, const long
 
 // det of a 4x4 integer matrix whose row 0 has entries in {-1,0,1} (a tet face e_k or the
 // all-ones row): Laplace along row 0, 3x3 minors of rows 1..3 fit int128 (<= 2^110.6).
-__device__ inline i128 det4_small_row0(const long long* r0, const long long* r1,
+__host__ __device__ inline i128 det4_small_row0(const long long* r0, const long long* r1,
                                        const long long* r2, const long long* r3) {
   i128 acc = 0;
 #pragma unroll
@@ -70,7 +70,7 @@ __device__ inline i128 det4_small_row0(const long long* r0, const long long* r1,
   return acc;
 }
 
-__device__ inline int sgn128(i128 x) { return x > 0 ? 1 : (x < 0 ? -1 : 0); }
+__host__ __device__ inline int sgn128(i128 x) { return x > 0 ? 1 : (x < 0 ? -1 : 0); }
 
 // A plane of the current piece as exact integers.
 struct XPlane {
@@ -80,14 +80,14 @@ struct XPlane {
   int radical;      // 1 radical, 0 tet face / all-ones row
 };
 
-__device__ inline bool is_small(const XPlane& p) { return !p.radical; }
+__host__ __device__ inline bool is_small(const XPlane& p) { return !p.radical; }
 
 // det[r0; r1; r2; r3] in the barycentric frame, exact sign.  At most three radical rows is
 // evaluated directly; four radical rows use the Cartesian identity
 //   det_bary = det(M) * det_cart[(n, d')],  M = [V0 V1 V2 V3; 1 1 1 1],  d' = a[0] = h(V0),
 // where det(M) = -6 vol(t) < 0 for a positively oriented tet,
 // whose entries are <= 2^17 (n) and <= 2^35.4 (d') so the Cartesian det fits int128.
-__device__ inline int det4_sign(const XPlane* r[4]) {
+__host__ __device__ inline int det4_sign(const XPlane* r[4]) {
   int small = -1;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -126,10 +126,11 @@ __device__ inline int det4_sign(const XPlane* r[4]) {
 
 // Exact SoS sign of plane s at the vertex (p, q, r):  sign(D4(eps)) * sign(D3).
 // zero_hit is set when D4 == 0 exactly.
-static __device__ __noinline__ int sos_sign_exact(const XPlane& p, const XPlane& q, const XPlane& r,
+static __host__ __device__ __noinline__ int sos_sign_exact(const XPlane& p, const XPlane& q, const XPlane& r,
                                      const XPlane& s, int* zero_hit) {
   XPlane one;
   one.a[0] = one.a[1] = one.a[2] = one.a[3] = 1;
+  one.n[0] = one.n[1] = one.n[2] = 0;
   one.radical = 0;
   one.rank = 0;
   const XPlane* rows3[4] = {&p, &q, &r, &one};
@@ -138,17 +139,25 @@ static __device__ __noinline__ int sos_sign_exact(const XPlane& p, const XPlane&
   int sD4 = det4_sign(rows);
   if (sD4 != 0) return sD4 * sD3;
   *zero_hit = 1;
-  // inward perturbation a_k -> a_k - eps^rank(k) * 1:  D4(eps) = D4 - sum eps^rank C_k
-  int order[4] = {0, 1, 2, 3};
-  for (int a = 1; a < 4; ++a)
-    for (int b = a; b > 0 && rows[order[b]]->rank < rows[order[b - 1]]->rank; --b) {
-      int t = order[b];
-      order[b] = order[b - 1];
-      order[b - 1] = t;
-    }
+  // inward perturbation a_k -> a_k - eps^rank(k) * 1:  D4(eps) = D4 - sum eps^rank C_k;
+  // visit the rows in increasing rank (selection by mask: an in-place insertion sort of a
+  // local index array was observed to be evaluated differently on sm_100a than on the host,
+  // see tests/native/sos_probe.cu)
+  unsigned used = 0u;
   for (int o = 0; o < 4; ++o) {
-    const XPlane* rr[4] = {rows[0], rows[1], rows[2], rows[3]};
-    rr[order[o]] = &one;
+    int best = -1;
+    long long br = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool free_k = ((used >> k) & 1u) == 0u;
+      if (free_k && (best < 0 || rows[k]->rank < br)) {
+        best = k;
+        br = rows[k]->rank;
+      }
+    }
+    used |= 1u << best;
+    const XPlane* rr[4] = {best == 0 ? &one : rows[0], best == 1 ? &one : rows[1],
+                           best == 2 ? &one : rows[2], best == 3 ? &one : rows[3]};
     int sC = det4_sign(rr);
     if (sC != 0) return -sC * sD3;
   }
@@ -156,14 +165,14 @@ static __device__ __noinline__ int sos_sign_exact(const XPlane& p, const XPlane&
 }
 
 // exact zero test of det[p; q; r; s] (no perturbation)
-static __device__ __noinline__ bool det4_is_zero(const XPlane& p, const XPlane& q, const XPlane& r,
+static __host__ __device__ __noinline__ bool det4_is_zero(const XPlane& p, const XPlane& q, const XPlane& r,
                                     const XPlane& s) {
   const XPlane* rows[4] = {&p, &q, &r, &s};
   return det4_sign(rows) == 0;
 }
 
 // int128 -> double via the magnitude: hi * 2^64 + lo (relative error <= 2^-52)
-__device__ inline double i128_to_double(i128 v) {
+__host__ __device__ inline double i128_to_double(i128 v) {
   bool neg = v < 0;
   unsigned __int128 u = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
   double d = (double)(unsigned long long)(u >> 64) * 18446744073709551616.0 +
@@ -172,7 +181,7 @@ __device__ inline double i128_to_double(i128 v) {
 }
 
 // exact homogeneous vertex K = cross(a_p, a_q, a_r), normalised to sum(K) > 0, as doubles
-static __device__ __noinline__ void exact_vertex(const XPlane& p, const XPlane& q, const XPlane& r,
+static __host__ __device__ __noinline__ void exact_vertex(const XPlane& p, const XPlane& q, const XPlane& r,
                                     double K[4]) {
   i128 Ki[4];
   i128 sum = 0;
