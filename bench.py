@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RPD hot path (BASELINE.json metric: tet-sphere pairs clipped/s and
+full/partial RPD ms at 1/2/4/8 B200).
+
+One step = one pass of the hot path over the bench workload:
+full RPD of the C3 sphere set (stage + Alg. 1 filter + k_tet compaction + clip + piece
+output), then the C4 partial updates (10 iterations inserting M = 500 spheres each,
+re-filtering and re-clipping only touched tets), and with N > 1 GPUs the NCCL all-gather of
+the pieces.  Tets are sharded block-cyclically over the ranks; spheres are replicated.
+
+value = candidate (tet, sphere) pairs clipped per second by the whole job (all ranks, full +
+partial), device time (CUDA events, max over ranks), inputs resident in HBM.
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK = os.path.join(ROOT, "profiles", "fp64_peak.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+WORKLOAD_NAME = ("C3+C4: ~200k-tet box-with-hole Kuhn mesh, 20k medial-like spheres full RPD "
+                 "+ 10 partial updates x M=500 (final 25.5k spheres)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--filter", default="all_pairs", choices=["all_pairs", "pruned"])
+    ap.add_argument("--partial-iters", type=int, default=-1,
+                    help="partial updates per step (-1: all batches of the config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 6:
+                for k, name in enumerate(self.NAMES):
+                    if r[2 + k] == "Active":
+                        reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak_tflops():
+    """Measured DFMA peak (tools/fp64_peak.cu, committed under profiles/), else the nominal
+    148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz."""
+    try:
+        d = json.load(open(FP64_PEAK))
+        return float(d["fp64_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "nominal 148x64x2x1.965GHz (no measurement found)"
+
+
+def hbm_peak_gbs():
+    try:
+        return float(json.load(open(MEASURED))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args):
+    """The oracle (plain CPU implementation, as it stands) on the host cores, on a bounded
+    sample of the same workload per step (reference arm)."""
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    import oracle
+    import rpd_workloads as W
+    w = W.make_config(args.config)
+    cores = oracle.max_threads()
+    rng = np.random.default_rng(0)
+    # calibrate the sample so the whole run ends in a few minutes
+    probe = np.sort(rng.choice(w.T, 32, replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.rpd_workload(w, tet_ids=probe)
+    per_tet = (time.perf_counter() - t0) / len(probe)
+    budget = 150.0 / max(args.steps + args.warmup, 1)
+    n_s = int(min(max(budget / max(per_tet, 1e-6), 16), w.T))
+    times, pairs = [], []
+    for s in range(args.warmup + args.steps):
+        ids = np.sort(np.random.default_rng(100 + s).choice(w.T, n_s, replace=False)).astype(np.int32)
+        t0 = time.perf_counter()
+        r = oracle.rpd_workload(w, tet_ids=ids)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            pairs.append(len(r["cand_idx"]))
+    value = float(np.sum(pairs) / np.sum(times))
+    sample = (f"{n_s} random tets per step of the {args.config} mesh (T={w.T}), full Alg. 1 over "
+              f"all N={w.N} spheres + clip of their candidates")
+    line = {"metric": "tet-sphere pairs clipped/s", "value": value, "unit": "pairs/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": WORKLOAD_NAME, "config": args.config},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(w, seconds):
+    """The oracle timed on a bounded sample of the bench workload (rank 0, N = 1)."""
+    import oracle
+    cores = oracle.max_threads()
+    rng = np.random.default_rng(1)
+    probe = np.sort(rng.choice(w.T, 32, replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.rpd_workload(w, tet_ids=probe)
+    per_tet = (time.perf_counter() - t0) / len(probe)
+    n_s = int(min(max(seconds / max(per_tet, 1e-6), 32), w.T))
+    ids = np.sort(rng.choice(w.T, n_s, replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    r = oracle.rpd_workload(w, tet_ids=ids)
+    dt = time.perf_counter() - t0
+    return {"value": len(r["cand_idx"]) / dt, "unit": "pairs/s", "cores": cores,
+            "kind": "oracle",
+            "sample": f"{n_s} random tets of {w.T} (full RPD of the 20k-sphere set: Alg. 1 over "
+                      f"all {w.N} spheres + clip), {dt:.1f} s; partial updates not sampled"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_18761_b200 as P
+    import rpd_workloads as W
+    from paper_2403_18761_b200.dist import gather_pieces, shard_tets
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    P.build() if rank == 0 and world == 1 else None
+    if world > 1:
+        dist.barrier()
+
+    w = W.make_config(args.config)
+    batches = w.batches if args.partial_iters < 0 else w.batches[:args.partial_iters]
+    ids = shard_tets(w.T, world, rank)
+    tets_local = w.tets[ids]
+
+    ctx = P.RPDContext(local, filter_mode=args.filter)
+    ctx.set_profile(True)
+    to_dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
+    d_verts, d_tets = to_dev(w.verts), to_dev(tets_local)
+    d_base = [to_dev(w.spheres), to_dev(w.nbr_off), to_dev(w.nbr_idx)]
+    d_batches = []
+    n_prev = w.N
+    for (sph, off, idx) in batches:
+        d_batches.append((to_dev(sph), to_dev(off), to_dev(idx),
+                          to_dev(np.arange(n_prev, len(sph), dtype=np.int32))))
+        n_prev = len(sph)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(record):
+        nc = ctx.relations(d_verts, d_tets, *d_base)
+        ctx.clip()
+        st = ctx.stats()
+        rec = {"n_cand": nc, "filter_ms": st["filter_ms"], "clip_ms": st["clip_ms"],
+               "rel_tests": st["rel_tests"], "pairs_filtered": st["pairs_filtered"],
+               "clip_work": (24 * st["clip_plane_evals"] + 8 * st["clip_vertex_tests"] +
+                             40 * st["clip_constructions"] + 30 * st["clip_fan_triangles"]),
+               "partial": []}
+        for (sph, off, idx, new) in d_batches:
+            counts, nd = ctx.update_partial(sph, off, idx, new)
+            st = ctx.stats()
+            rec["partial"].append({"n_dirty": nd, "n_cand": st["n_cand"]})
+        if world > 1:
+            loc = ctx.download_pieces(device=True)
+            gather_pieces(loc, ids, w.T)
+        record.append(rec)
+
+    launches0 = None
+    recs, times = [], []
+    for s in range(args.warmup):
+        step([])
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = ctx.stats()["kernel_launches"]
+    for s in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(recs)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    launches = ctx.stats()["kernel_launches"] - launches0
+    clocks = sampler.stop()
+    total_ms = float(np.sum(times))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    pairs_local = sum(r["n_cand"] + sum(p["n_cand"] for p in r["partial"]) for r in recs)
+    pl = torch.tensor([pairs_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(pl, op=dist.ReduceOp.SUM)
+    total_ms = float(t.item())
+    pairs_total = float(pl.item())
+    value = pairs_total / (total_ms * 1e-3)
+
+    # ---- e2e: the public API with HOST buffers, H2D and D2H inside the timed region
+    pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory().numpy()
+    h_in = [pin(w.verts), pin(tets_local), pin(w.spheres), pin(w.nbr_off), pin(w.nbr_idx)]
+    h2d = sum(a.nbytes for a in h_in)
+    e2e_times, d2h = [], 0
+    for s in range(max(2, min(args.steps, 5)) + 1):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nc = ctx.relations(*h_in)
+        cnt = ctx.clip()
+        out = ctx.download_pieces()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if s > 0:
+            e2e_times.append(dt)
+        d2h = sum(np.asarray(v).nbytes for v in out.values())
+    e2e_pairs = recs[0]["n_cand"]   # full RPD only (the e2e loop runs the full RPD)
+    e2e_value = e2e_pairs * world / float(np.mean(e2e_times))
+
+    # ---- roofline of the dominant kernel
+    fmed = float(np.median([r["filter_ms"] for r in recs]))
+    cmed = float(np.median([r["clip_ms"] for r in recs]))
+    peak, peak_src = fp64_peak_tflops()
+    if fmed >= cmed:
+        kern, kms = "k_filter_allpairs", fmed
+        flops = 7.0 * float(np.median([r["rel_tests"] for r in recs]))
+        per_unit = "7 flop per literal Alg. 1 vertex test (3 FMA + compare), tests counted by the kernel"
+    else:
+        kern, kms = "k_clip<1>+k_clip<4>", cmed
+        flops = float(np.median([r["clip_work"] for r in recs]))
+        per_unit = ("24 flop per (pair, plane) corner classification + 8 per vertex sign test + "
+                    "40 per vertex construction + 30 per fan triangle, counted by the kernel")
+    achieved = flops / (kms * 1e-3) / 1e12
+    traffic = None
+    try:
+        traffic = json.load(open(NCU_TRAFFIC)).get(kern)
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": kern,
+                "kernel_ms": kms, "algorithmic_flops": flops, "per_unit": per_unit,
+                "peak_source": peak_src + "; FP64 DFMA pipe (fp64 ALU bound, no tensor cores)"}
+
+    line = {
+        "metric": "tet-sphere pairs clipped/s",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAME, "T": w.T, "N": w.N,
+                   "partial_iters": len(d_batches),
+                   "M": (len(batches[0][0]) - w.N) if batches else 0,
+                   "filter": args.filter, "parallelism": f"tet-shard x{world}",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "full_rpd_ms": float(np.median([r["filter_ms"] + r["clip_ms"] for r in recs])),
+        "filter_ms": fmed, "clip_ms": cmed,
+        "pairs_filtered_per_s": float(recs[0]["pairs_filtered"]) * world / (fmed * 1e-3),
+        "pairs_clipped_per_s_clip_kernel": recs[0]["n_cand"] * world / (cmed * 1e-3),
+        "partial_rpd_ms": None,
+        "roofline": roofline,
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "note": "full RPD through the C ABI with host inputs and a host download"},
+        "gpu_launches": int(launches // max(args.steps, 1)),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -72,8 +72,10 @@ enum {
                                 provably fail Alg. 1 are skipped) */
   RPD_OPT_VALIDATE = 2,      /* 1 (default): validate inputs on device; 0: skip */
   RPD_OPT_STREAM = 3,        /* value = (intptr_t) cudaStream_t to switch the ctx stream */
-  RPD_OPT_CLIP_WIDE = 4      /* 1: clip every pair with the wide (128-vertex) kernel instead of
+  RPD_OPT_CLIP_WIDE = 4,     /* 1: clip every pair with the wide (128-vertex) kernel instead of
                                 only the pairs that overflow the fast (32-vertex) one; for tests */
+  RPD_OPT_PROFILE = 5        /* 1: time the filter and clip kernels with CUDA events on the ctx
+                                stream (rpd_stats.filter_ms / clip_ms) */
 };
 enum { RPD_FILTER_ALL_PAIRS = 0, RPD_FILTER_PRUNED = 1 };
 rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
@@ -154,6 +156,13 @@ typedef struct {
   int64_t kernel_launches;
   int32_t max_k_tet, max_vertices, max_planes;
   int32_t n_wide;                /* pairs re-clipped by the wide kernel */
+  /* algorithmic work counted by the kernels */
+  int64_t rel_tests;             /* literal Alg. 1 vertex tests (inner break, outer early exit) */
+  int64_t clip_plane_evals;      /* (pair, neighbour plane) corner classifications */
+  int64_t clip_vertex_tests;     /* vertex sign tests of cutting candidates */
+  int64_t clip_constructions;    /* new vertices */
+  int64_t clip_fan_triangles;    /* fan triangles integrated for volume and first moment */
+  double filter_ms, clip_ms;     /* kernel times of the last call (RPD_OPT_PROFILE only) */
 } rpd_stats;
 rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
 

@@ -134,15 +134,31 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->h_verts, &c->h_tets, &c->h_spheres, &c->h_off, &c->h_idx, &c->h_new,
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
-                    &c->st.twin, &c->verts_lat, &c->tets, &c->errw, &c->stats, &c->scratch,
-                    &c->k_tet, &c->slab, &c->cand_off, &c->cand_idx, &c->pair_tet, &c->p_flag,
-                    &c->p_vol, &c->p_m1, &c->p_fm, &c->p_ninc, &c->p_f01, &c->p_words,
-                    &c->p_moff, &c->p_mask, &c->p_over, &c->k_words, &c->w_off, &c->p_scan,
-                    &c->i_scan, &c->piece_off, &c->piece_sphere, &c->piece_vol, &c->piece_m1,
-                    &c->piece_fm, &c->inc_off, &c->inc_sphere, &c->dirty_flag, &c->dirty_list,
-                    &c->dirty_scan};
+                    &c->st.twin, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
+                    &c->slab, &c->w_off, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
+                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
+                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off};
   for (DevBuf* b : bufs) b->release();
+  CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
+  for (CandSet* x : cs) {
+    x->off.release();
+    x->idx.release();
+    x->pair_tet.release();
+    x->moff.release();
+  }
+  PieceSet* ps[] = {&c->pcs[0], &c->pcs[1], &c->pcs_d};
+  for (PieceSet* x : ps) {
+    x->off.release();
+    x->sphere.release();
+    x->vol.release();
+    x->m1.release();
+    x->fm.release();
+    x->inc_off.release();
+    x->inc.release();
+  }
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (int k = 0; k < 4; ++k)
+    if (c->ev[k]) cudaEventDestroy(c->ev[k]);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -163,6 +179,11 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
     case RPD_OPT_VALIDATE:
       c->validate = value ? 1 : 0;
       return RPD_OK;
+    case RPD_OPT_PROFILE:
+      c->profile = value ? 1 : 0;
+      if (c->profile && !c->ev[0])
+        for (int k = 0; k < 4; ++k) cudaEventCreate(&c->ev[k]);
+      return RPD_OK;
     case RPD_OPT_CLIP_WIDE:
       c->clip_wide = value ? 1 : 0;
       return RPD_OK;
@@ -176,122 +197,101 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
   }
 }
 
-rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
-                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
-                         const int32_t* nbr_idx, const int32_t** cand_off,
-                         const int32_t** cand_idx, int64_t* n_cand) {
-  if (!c) return RPD_EINVAL;
-  if (V < 0 || T < 0 || N < 0 || T > 0x7fffffff || N > 0x7fffffff || (T > 0 && !tets) ||
-      (V > 0 && !verts) || (N > 0 && (!spheres || !nbr_off)) || !cand_off || !cand_idx ||
-      !n_cand)
-    return fail(c, RPD_EINVAL, "rpd_relations: bad argument");
-  CK(cudaSetDevice(c->device), "cudaSetDevice");
-  c->have_rel = false;
-  c->have_pieces = false;
-  Readback* rb = (Readback*)c->pinned;
+// ------------------------------------------------------------------ internal steps
 
-  // neighbour count E = nbr_off[N]
-  int64_t E = 0;
-  const int32_t* d_off = nullptr;
-  if (N > 0) {
-    if (is_host_ptr(nbr_off)) {
-      E = nbr_off[N];
-    } else {
-      CK(cudaMemcpyAsync(&rb->i32[0], nbr_off + N, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                         c->stream), "read nbr_off[N]");
-      CK(cudaStreamSynchronize(c->stream), "sync");
-      E = rb->i32[0];
-    }
-    if (E < 0) return fail(c, RPD_EINVAL, "nbr_off[N] < 0");
-    if (E > 0 && !nbr_idx) return fail(c, RPD_EINVAL, "nbr_idx is NULL");
+// E = nbr_off[N] (host or device pointer)
+static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t* E) {
+  *E = 0;
+  if (N <= 0) return RPD_OK;
+  if (is_host_ptr(nbr_off)) {
+    *E = nbr_off[N];
+  } else {
+    Readback* rb = (Readback*)c->pinned;
+    CK(cudaMemcpyAsync(&rb->i32[0], nbr_off + N, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream), "read nbr_off[N]");
+    CK(cudaStreamSynchronize(c->stream), "sync");
+    *E = rb->i32[0];
   }
-  const double *d_verts = nullptr, *d_sph = nullptr;
-  const int32_t *d_tets = nullptr, *d_idx = nullptr;
-  CK(resolve(c, verts, 3 * V, c->h_verts, &d_verts), "stage verts");
-  CK(resolve(c, tets, 4 * T, c->h_tets, &d_tets), "stage tets");
+  if (*E < 0) return fail(c, RPD_EINVAL, "nbr_off[N] < 0");
+  return RPD_OK;
+}
+
+static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
+                                const int32_t* nbr_off, const int32_t* nbr_idx) {
+  int64_t E = 0;
+  rpd_status s = read_E(c, nbr_off, N, &E);
+  if (s) return s;
+  if (E > 0 && !nbr_idx) return fail(c, RPD_EINVAL, "nbr_idx is NULL");
+  const double* d_sph = nullptr;
+  const int32_t *d_off = nullptr, *d_idx = nullptr;
   CK(resolve(c, spheres, 4 * N, c->h_spheres, &d_sph), "stage spheres");
   CK(resolve(c, nbr_off, N > 0 ? N + 1 : 0, c->h_off, &d_off), "stage nbr_off");
   CK(resolve(c, nbr_idx, E, c->h_idx, &d_idx), "stage nbr_idx");
+  CK(launch_stage_spheres(c, d_sph, N, d_off, d_idx, E), "stage spheres");
+  return RPD_OK;
+}
 
-  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
-  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
-  CK(launch_stage(c, d_verts, V, d_tets, T, d_sph, N, d_off, d_idx, E), "stage");
-  // keep a copy of the tets for later partial updates
-  CK(c->tets.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1)), "alloc");
-  if (T > 0)
-    CK(cudaMemcpyAsync(c->tets.p, d_tets, sizeof(int32_t) * 4 * T, cudaMemcpyDeviceToDevice,
-                       c->stream), "copy tets");
-
-  CK(c->k_tet.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
-  CK(c->k_words.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
-  CK(c->cand_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  CK(c->w_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+// Alg. 1 over tets (tet_ids, or all ctx tets when NULL) x spheres [lo, hi) -> candidate set
+static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int lo,
+                             int hi, CandSet& cs, bool timed) {
+  Readback* rb = (Readback*)c->pinned;
+  size_t nt = n_tets > 0 ? n_tets : 1;
+  CK(c->k_tet.ensure(sizeof(int32_t) * nt), "alloc");
+  CK(c->k_words.ensure(sizeof(int32_t) * nt), "alloc");
+  CK(cs.off.ensure(sizeof(int32_t) * (n_tets + 1)), "alloc");
+  CK(c->w_off.ensure(sizeof(int32_t) * (n_tets + 1)), "alloc");
   for (int attempt = 0; attempt < 2; ++attempt) {
-    int cap = c->slab_cap;
-    CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * (T > 0 ? T : 1)), "alloc slab");
-    CK(launch_filter(c, nullptr, T, cap, 0, (int)N, c->k_tet.as<int32_t>(),
+    const int cap = c->slab_cap;
+    CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * nt), "alloc slab");
+    CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
+                       sizeof(unsigned long long), c->stream), "memset");
+    if (timed && c->profile) cudaEventRecord(c->ev[0], c->stream);
+    CK(launch_filter(c, tet_ids, n_tets, cap, lo, hi, c->k_tet.as<int32_t>(),
                      c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
-    CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), c->cand_off.as<int32_t>(), T), "scan");
-    CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), T), "scan");
-    CK(cudaMemcpyAsync(&rb->i32[0], c->cand_off.as<int32_t>() + T, sizeof(int32_t),
+    if (timed && c->profile) cudaEventRecord(c->ev[1], c->stream);
+    CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), cs.off.as<int32_t>(), n_tets), "scan");
+    CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), n_tets), "scan");
+    CK(cudaMemcpyAsync(&rb->i32[0], cs.off.as<int32_t>() + n_tets, sizeof(int32_t),
                        cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(&rb->i32[1], c->w_off.as<int32_t>() + T, sizeof(int32_t),
+    CK(cudaMemcpyAsync(&rb->i32[1], c->w_off.as<int32_t>() + n_tets, sizeof(int32_t),
                        cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                        cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
        "readback");
-    CK(cudaStreamSynchronize(c->stream), "relations");
+    CK(cudaStreamSynchronize(c->stream), "filter");
     rpd_status s = check_err(c, rb);
     if (s) return s;
-    int maxk = (int)rb->u64[ST_MAXK];
+    const int maxk = (int)rb->u64[ST_MAXK];
     if (maxk <= cap) break;
     int nc = 32;
     while (nc < maxk) nc *= 2;
     c->slab_cap = nc;
   }
-  int64_t nc = rb->i32[0];
-  c->n_mask_words = rb->i32[1];
-  CK(c->cand_idx.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
-  CK(c->pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
-  CK(c->p_moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
-  CK(launch_compact_cands(c, T, c->slab_cap, c->k_tet.as<int32_t>(), c->slab.as<int32_t>(),
-                          c->cand_off.as<int32_t>(), c->cand_idx.as<int32_t>(),
-                          c->pair_tet.as<int32_t>(), c->w_off.as<int32_t>(),
-                          c->p_moff.as<int32_t>(), nc), "compact");
-  c->n_cand = nc;
-  c->have_rel = true;
-  c->last = rpd_stats{};
-  c->last.T = T;
-  c->last.N = N;
-  c->last.n_cand = nc;
-  c->last.pairs_filtered = T * N;
-  c->last.pairs_tested = T * N;
+  const int64_t nc = rb->i32[0];
+  cs.n = nc;
+  cs.n_tets = n_tets;
+  cs.n_words = rb->i32[1];
+  CK(cs.idx.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
+  CK(cs.pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
+  CK(cs.moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
+  CK(launch_compact_cands(c, n_tets, c->slab_cap, c->k_tet.as<int32_t>(), c->slab.as<int32_t>(),
+                          cs.off.as<int32_t>(), cs.idx.as<int32_t>(), cs.pair_tet.as<int32_t>(),
+                          c->w_off.as<int32_t>(), cs.moff.as<int32_t>(), nc), "compact");
   c->last.max_k_tet = (int32_t)rb->u64[ST_MAXK];
-  *cand_off = c->cand_off.as<int32_t>();
-  *cand_idx = c->cand_idx.as<int32_t>();
-  *n_cand = nc;
+  c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
+  if (timed && c->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->last.filter_ms += ms;
+  }
   return RPD_OK;
 }
 
-static rpd_status fill_pieces(rpd_ctx* c, rpd_pieces* out) {
-  out->piece_off = c->piece_off.as<int32_t>();
-  out->piece_sphere = c->piece_sphere.as<int32_t>();
-  out->piece_vol = c->piece_vol.as<double>();
-  out->piece_m1 = c->piece_m1.as<double>();
-  out->piece_facemask = c->piece_fm.as<uint8_t>();
-  out->inc_off = c->inc_off.as<int32_t>();
-  out->inc_sphere = c->inc_sphere.as<int32_t>();
-  out->n_pieces = c->n_pieces;
-  out->n_inc = c->n_inc;
-  return RPD_OK;
-}
-
-rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
-  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_clip: bad argument");
-  if (!c->have_rel) return fail(c, RPD_ESTATE, "rpd_clip before rpd_relations");
-  CK(cudaSetDevice(c->device), "cudaSetDevice");
-  const int64_t n = c->n_cand, T = c->st.T;
+// clip every pair of cs (tets tet_ids or all) -> piece set
+static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids,
+                           PieceSet& ps) {
+  const int64_t n = cs.n, nt = cs.n_tets;
   size_t nn = n > 0 ? n : 1;
   CK(c->p_flag.ensure(nn), "alloc");
   CK(c->p_f01.ensure(nn), "alloc");
@@ -300,17 +300,24 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   CK(c->p_m1.ensure(sizeof(double) * 3 * nn), "alloc");
   CK(c->p_ninc.ensure(sizeof(int32_t) * nn), "alloc");
   CK(c->p_over.ensure(sizeof(int32_t) * (n + 1)), "alloc");
-  CK(c->p_mask.ensure(sizeof(unsigned) * (c->n_mask_words > 0 ? c->n_mask_words : 1)), "alloc");
+  CK(c->p_mask.ensure(sizeof(unsigned) * (cs.n_words > 0 ? cs.n_words : 1)), "alloc");
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
-  CK(cudaMemsetAsync(c->p_mask.p, 0, sizeof(unsigned) * c->n_mask_words, c->stream), "memset");
+  const int32_t* moff = cs.moff.as<int32_t>();
+  CK(cudaMemsetAsync(c->p_mask.p, 0, sizeof(unsigned) * cs.n_words, c->stream), "memset");
   CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
-  CK(launch_clip(c, n, c->pair_tet.as<int32_t>(), nullptr, c->cand_idx.as<int32_t>(),
+  CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
+                     sizeof(unsigned long long) * 5, c->stream), "memset");
+  CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
+                     sizeof(unsigned long long) * 4, c->stream), "memset");
+  if (c->profile) cudaEventRecord(c->ev[2], c->stream);
+  CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff,
                  c->clip_wide), "clip");
   if (!c->clip_wide && n > 0)
-    CK(launch_clip_overflow(c, c->pair_tet.as<int32_t>(), nullptr, c->cand_idx.as<int32_t>()),
+    CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff),
        "clip (wide)");
-  CK(launch_piece_scans(c, n), "scan");
+  if (c->profile) cudaEventRecord(c->ev[3], c->stream);
+  CK(launch_piece_scans(c, n, moff), "scan");
   Readback* rb = (Readback*)c->pinned;
   CK(cudaMemcpyAsync(&rb->i32[0], c->p_scan.as<int32_t>() + n, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
@@ -323,30 +330,109 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   CK(cudaStreamSynchronize(c->stream), "clip");
   if (rb->u64[ST_OVERFLOW])
     return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
-  int64_t np = rb->i32[0], ni = rb->i32[1];
-  size_t npp = np > 0 ? np : 1;
-  CK(c->piece_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  CK(c->piece_sphere.ensure(sizeof(int32_t) * npp), "alloc");
-  CK(c->piece_vol.ensure(sizeof(double) * npp), "alloc");
-  CK(c->piece_m1.ensure(sizeof(double) * 3 * npp), "alloc");
-  CK(c->piece_fm.ensure(npp), "alloc");
-  CK(c->inc_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
-  CK(c->inc_sphere.ensure(sizeof(int32_t) * (ni > 0 ? ni : 1)), "alloc");
-  PieceDst d{c->piece_off.as<int32_t>(), c->piece_sphere.as<int32_t>(), c->piece_vol.as<double>(),
-             c->piece_m1.as<double>(), c->piece_fm.as<uint8_t>(), c->inc_off.as<int32_t>(),
-             c->inc_sphere.as<int32_t>()};
-  CK(launch_compact_pieces(c, T, n, c->cand_off.as<int32_t>(), c->cand_idx.as<int32_t>(), d),
+  const int64_t np = rb->i32[0], ni = rb->i32[1];
+  const size_t npp = np > 0 ? np : 1;
+  CK(ps.off.ensure(sizeof(int32_t) * (nt + 1)), "alloc");
+  CK(ps.sphere.ensure(sizeof(int32_t) * npp), "alloc");
+  CK(ps.vol.ensure(sizeof(double) * npp), "alloc");
+  CK(ps.m1.ensure(sizeof(double) * 3 * npp), "alloc");
+  CK(ps.fm.ensure(npp), "alloc");
+  CK(ps.inc_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
+  CK(ps.inc.ensure(sizeof(int32_t) * (ni > 0 ? ni : 1)), "alloc");
+  PieceDst d{ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.vol.as<double>(),
+             ps.m1.as<double>(),  ps.fm.as<uint8_t>(),     ps.inc_off.as<int32_t>(),
+             ps.inc.as<int32_t>()};
+  CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idx.as<int32_t>(), moff, d),
      "compact pieces");
-  c->n_pieces = np;
-  c->n_inc = ni;
+  ps.n_tets = nt;
+  ps.n_pieces = np;
+  ps.n_inc = ni;
+  c->last.exact_fallbacks += (int64_t)rb->u64[ST_EXACT];
+  c->last.zero_hits += (int64_t)rb->u64[ST_ZERO];
+  c->last.max_vertices = max(c->last.max_vertices, (int32_t)rb->u64[ST_MAXV]);
+  c->last.max_planes = max(c->last.max_planes, (int32_t)rb->u64[ST_MAXP]);
+  c->last.n_wide += rb->i32[2];
+  c->last.clip_plane_evals += (int64_t)rb->u64[ST_CLIP_PLANES];
+  c->last.clip_vertex_tests += (int64_t)rb->u64[ST_CLIP_TESTS];
+  c->last.clip_constructions += (int64_t)rb->u64[ST_CLIP_CONSTR];
+  c->last.clip_fan_triangles += (int64_t)rb->u64[ST_CLIP_FAN];
+  if (c->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    c->last.clip_ms += ms;
+  }
+  return RPD_OK;
+}
+
+static void reset_last(rpd_ctx* c) {
+  c->last = rpd_stats{};
+  c->last.T = c->st.T;
+  c->last.N = c->st.N;
+}
+
+static rpd_status fill_pieces(rpd_ctx* c, rpd_pieces* out) {
+  const PieceSet& ps = c->pcs[c->cur];
+  out->piece_off = ps.off.as<int32_t>();
+  out->piece_sphere = ps.sphere.as<int32_t>();
+  out->piece_vol = ps.vol.as<double>();
+  out->piece_m1 = ps.m1.as<double>();
+  out->piece_facemask = ps.fm.as<uint8_t>();
+  out->inc_off = ps.inc_off.as<int32_t>();
+  out->inc_sphere = ps.inc.as<int32_t>();
+  out->n_pieces = ps.n_pieces;
+  out->n_inc = ps.n_inc;
+  return RPD_OK;
+}
+
+// ------------------------------------------------------------------ public calls
+
+rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
+                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
+                         const int32_t* nbr_idx, const int32_t** cand_off,
+                         const int32_t** cand_idx, int64_t* n_cand) {
+  if (!c) return RPD_EINVAL;
+  if (V < 0 || T < 0 || N < 0 || T > 0x7fffffff || N > 0x7fffffff || (T > 0 && !tets) ||
+      (V > 0 && !verts) || (N > 0 && (!spheres || !nbr_off)) || !cand_off || !cand_idx ||
+      !n_cand)
+    return fail(c, RPD_EINVAL, "rpd_relations: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  c->have_rel = false;
+  c->have_pieces = false;
+  const double* d_verts = nullptr;
+  const int32_t* d_tets = nullptr;
+  CK(resolve(c, verts, 3 * V, c->h_verts, &d_verts), "stage verts");
+  CK(resolve(c, tets, 4 * T, c->h_tets, &d_tets), "stage tets");
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
+  CK(launch_stage_mesh(c, d_verts, V, d_tets, T), "stage mesh");
+  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx);
+  if (s) return s;
+  reset_last(c);
+  c->cur = 0;
+  CandSet& cs = c->cand[0];
+  s = run_filter(c, nullptr, T, 0, (int)N, cs, true);
+  if (s) return s;
+  c->have_rel = true;
+  c->last.n_cand = cs.n;
+  c->last.pairs_filtered = T * N;
+  c->last.pairs_tested = T * N;
+  *cand_off = cs.off.as<int32_t>();
+  *cand_idx = cs.idx.as<int32_t>();
+  *n_cand = cs.n;
+  return RPD_OK;
+}
+
+rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_clip: bad argument");
+  if (!c->have_rel) return fail(c, RPD_ESTATE, "rpd_clip before rpd_relations");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CandSet& cs = c->cand[c->cur];
+  c->last.clip_ms = 0.0;
+  rpd_status s = run_clip(c, cs, nullptr, c->pcs[c->cur]);
+  if (s) return s;
   c->have_pieces = true;
-  c->last.n_pieces = np;
-  c->last.n_inc = ni;
-  c->last.exact_fallbacks = (int64_t)rb->u64[ST_EXACT];
-  c->last.zero_hits = (int64_t)rb->u64[ST_ZERO];
-  c->last.max_vertices = (int32_t)rb->u64[ST_MAXV];
-  c->last.max_planes = (int32_t)rb->u64[ST_MAXP];
-  c->last.n_wide = rb->i32[2];
+  c->last.n_pieces = c->pcs[c->cur].n_pieces;
+  c->last.n_inc = c->pcs[c->cur].n_inc;
   return fill_pieces(c, out);
 }
 
@@ -354,16 +440,125 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
                               const int32_t* nbr_off, const int32_t* nbr_idx,
                               const int32_t* new_ids, int64_t M, rpd_pieces* out,
                               const int32_t** dirty_tets, int64_t* n_dirty) {
-  (void)spheres;
-  (void)N_new;
-  (void)nbr_off;
-  (void)nbr_idx;
-  (void)new_ids;
-  (void)M;
-  (void)out;
-  (void)dirty_tets;
-  (void)n_dirty;
-  return fail(c, RPD_ESTATE, "rpd_update_partial: not built yet");
+  if (!c) return RPD_EINVAL;
+  if (!out || !dirty_tets || !n_dirty || M < 0 || (M > 0 && !new_ids))
+    return fail(c, RPD_EINVAL, "rpd_update_partial: bad argument");
+  if (!c->have_pieces) return fail(c, RPD_ESTATE, "rpd_update_partial before rpd_clip");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int64_t N_old = c->st.N, T = c->st.T;
+  if (N_new != N_old + M)
+    return fail(c, RPD_EINVAL, "N_new must equal N_old + M (new spheres are appended)");
+  if (!spheres || (N_new > 0 && !nbr_off))
+    return fail(c, RPD_EINVAL, "rpd_update_partial: bad argument");
+  reset_last(c);
+  CK(c->d_list.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
+  if (M == 0) {  // identity
+    c->n_dirty = 0;
+    *dirty_tets = c->d_list.as<int32_t>();
+    *n_dirty = 0;
+    c->last.n_cand = c->cand[c->cur].n;
+    c->last.n_pieces = c->pcs[c->cur].n_pieces;
+    c->last.n_inc = c->pcs[c->cur].n_inc;
+    return fill_pieces(c, out);
+  }
+  const int32_t* d_new = nullptr;
+  CK(resolve(c, new_ids, M, c->h_new, &d_new), "stage new ids");
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
+  CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
+  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx);
+  if (s) return s;
+  c->last.N = N_new;
+
+  // (1) dirty tets: Alg. 1 of every tet against the new spheres only
+  CK(c->d_count.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
+  CK(c->d_flag.ensure(T > 0 ? T : 1), "alloc");
+  CK(c->d_scan.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(c->d_pos.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
+  if (c->profile) cudaEventRecord(c->ev[0], c->stream);
+  CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(), nullptr,
+                   nullptr), "dirty filter");
+  if (c->profile) cudaEventRecord(c->ev[1], c->stream);
+  CK(launch_dirty_list(c, T), "dirty list");
+  Readback* rb = (Readback*)c->pinned;
+  CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
+     "readback");
+  CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaStreamSynchronize(c->stream), "dirty");
+  if (rb->err[0] != 0) {
+    if (rb->err[1] == 100) return fail(c, RPD_EINVAL, "new_ids is not the appended id range");
+    return check_err(c, rb);
+  }
+  const int64_t nd = rb->i32[0];
+  c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
+  if (c->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->last.filter_ms += ms;
+  }
+  const int32_t* dl = c->d_list.as<int32_t>();
+
+  // (2) re-candidate the dirty tets against all spheres, (3) clip them
+  s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
+  if (s) return s;
+  s = run_clip(c, c->cand_d, dl, c->pcs_d);
+  if (s) return s;
+
+  // (4) merge clean old tets + dirty new tets into the other buffer set
+  const int nxt = c->cur ^ 1;
+  CandSet& co = c->cand[c->cur];
+  PieceSet& po = c->pcs[c->cur];
+  CandSet& cn = c->cand[nxt];
+  PieceSet& pn = c->pcs[nxt];
+  CK(c->m_cnt.ensure(sizeof(int32_t) * 3 * (T > 0 ? T : 1)), "alloc");
+  CK(c->m_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(launch_merge(c, T, co, po, c->cand_d, c->pcs_d, cn, pn, 0), "merge counts");
+  CK(cudaMemcpyAsync(&rb->i32[0], cn.off.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[1], pn.off.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[2], c->m_off.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaStreamSynchronize(c->stream), "merge");
+  cn.n = rb->i32[0];
+  cn.n_tets = T;
+  pn.n_pieces = rb->i32[1];
+  pn.n_inc = rb->i32[2];
+  pn.n_tets = T;
+  const size_t ncn = cn.n > 0 ? cn.n : 1, npn = pn.n_pieces > 0 ? pn.n_pieces : 1;
+  CK(cn.idx.ensure(sizeof(int32_t) * ncn), "alloc");
+  CK(cn.pair_tet.ensure(sizeof(int32_t) * ncn), "alloc");
+  CK(cn.moff.ensure(sizeof(int32_t) * (cn.n + 1)), "alloc");
+  CK(pn.sphere.ensure(sizeof(int32_t) * npn), "alloc");
+  CK(pn.vol.ensure(sizeof(double) * npn), "alloc");
+  CK(pn.m1.ensure(sizeof(double) * 3 * npn), "alloc");
+  CK(pn.fm.ensure(npn), "alloc");
+  CK(pn.inc_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
+  CK(pn.inc.ensure(sizeof(int32_t) * (pn.n_inc > 0 ? pn.n_inc : 1)), "alloc");
+  CK(launch_merge(c, T, co, po, c->cand_d, c->pcs_d, cn, pn, 1), "merge copy");
+  // incidence-mask offsets of the merged candidates (for a later rpd_clip)
+  CK(c->p_ninc.ensure(sizeof(int32_t) * ncn), "alloc");
+  CK(launch_moff(c, cn.n, cn.idx.as<int32_t>(), cn.moff.as<int32_t>()), "moff");
+  CK(cudaMemcpyAsync(&rb->i32[3], cn.moff.as<int32_t>() + cn.n, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaStreamSynchronize(c->stream), "merge");
+  cn.n_words = rb->i32[3];
+  c->cur = nxt;
+  c->n_dirty = nd;
+  c->last.n_dirty = nd;
+  c->last.n_cand = cn.n;
+  c->last.n_pieces = pn.n_pieces;
+  c->last.n_inc = pn.n_inc;
+  c->last.pairs_filtered = T * M + nd * N_new;
+  c->last.pairs_tested = T * M + nd * N_new;
+  *dirty_tets = dl;
+  *n_dirty = nd;
+  return fill_pieces(c, out);
 }
 
 rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sphere,
@@ -371,18 +566,19 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
                                int32_t* inc_off, int32_t* inc_sphere) {
   if (!c) return RPD_EINVAL;
   if (!c->have_pieces) return fail(c, RPD_ESTATE, "no pieces");
-  const int64_t T = c->st.T, np = c->n_pieces, ni = c->n_inc;
+  const PieceSet& ps = c->pcs[c->cur];
+  const int64_t T = c->st.T, np = ps.n_pieces, ni = ps.n_inc;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
     if (!dst || bytes == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
   };
-  CK(cp(piece_off, c->piece_off.p, sizeof(int32_t) * (T + 1)), "download");
-  CK(cp(piece_sphere, c->piece_sphere.p, sizeof(int32_t) * np), "download");
-  CK(cp(piece_vol, c->piece_vol.p, sizeof(double) * np), "download");
-  CK(cp(piece_m1, c->piece_m1.p, sizeof(double) * 3 * np), "download");
-  CK(cp(piece_facemask, c->piece_fm.p, np), "download");
-  CK(cp(inc_off, c->inc_off.p, sizeof(int32_t) * (np + 1)), "download");
-  CK(cp(inc_sphere, c->inc_sphere.p, sizeof(int32_t) * ni), "download");
+  CK(cp(piece_off, ps.off.p, sizeof(int32_t) * (T + 1)), "download");
+  CK(cp(piece_sphere, ps.sphere.p, sizeof(int32_t) * np), "download");
+  CK(cp(piece_vol, ps.vol.p, sizeof(double) * np), "download");
+  CK(cp(piece_m1, ps.m1.p, sizeof(double) * 3 * np), "download");
+  CK(cp(piece_facemask, ps.fm.p, np), "download");
+  CK(cp(inc_off, ps.inc_off.p, sizeof(int32_t) * (np + 1)), "download");
+  CK(cp(inc_sphere, ps.inc.p, sizeof(int32_t) * ni), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }
@@ -390,12 +586,13 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
 rpd_status rpd_download_cands(rpd_ctx* c, int32_t* cand_off, int32_t* cand_idx) {
   if (!c) return RPD_EINVAL;
   if (!c->have_rel) return fail(c, RPD_ESTATE, "no candidates");
+  const CandSet& cs = c->cand[c->cur];
   if (cand_off)
-    CK(cudaMemcpyAsync(cand_off, c->cand_off.p, sizeof(int32_t) * (c->st.T + 1),
+    CK(cudaMemcpyAsync(cand_off, cs.off.p, sizeof(int32_t) * (c->st.T + 1),
                        cudaMemcpyDefault, c->stream), "download");
-  if (cand_idx && c->n_cand > 0)
-    CK(cudaMemcpyAsync(cand_idx, c->cand_idx.p, sizeof(int32_t) * c->n_cand,
-                       cudaMemcpyDefault, c->stream), "download");
+  if (cand_idx && cs.n > 0)
+    CK(cudaMemcpyAsync(cand_idx, cs.idx.p, sizeof(int32_t) * cs.n, cudaMemcpyDefault,
+                       c->stream), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }

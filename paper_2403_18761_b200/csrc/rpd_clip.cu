@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
+  // algorithmic work (lane 0 counts; warp-uniform quantities)
+  long long c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;
 
   for (int64_t pi = gw; pi < n_pairs; pi += nw) {
     const int64_t p = pair_list ? (int64_t)pair_list[pi] : pi;
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
     __syncwarp();
     int np = 4, nv = 4, cur = 0, status = ST_ALIVE, zero_hit = 0;
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+    c_planes += e1 - e0;
 
     for (int base = e0; base < e1 && status == ST_ALIVE; base += 32) {
       const int e = base + lane;
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
           anypos |= posm[k] != 0u;
         }
         zero_hit = __any_sync(FULL, zero_hit);
+        c_tests += nv;
 #ifdef RPD_TRACE
         if (p == RPD_TRACE) {
           for (int k = 0; k < VPL; ++k) {
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
             S.tri[nxt][q] = tr;
           }
         }
+        c_constr += new_base;
         nv = nv2;
         cur = nxt;
         __syncwarp();
@@ -428,6 +433,12 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
     }
     facets_all.warp_or();
     Bits<VPL> facets = facets_all;
+    {
+      int nf = 0;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) nf += __popc(facets_all.w[k]);
+      c_fan += 3 * nv - 2 * nf;  // sum over facets of (vertices - 2)
+    }
 
     // zero-area SoS facets (only possible after an exact-zero predicate; C1.7)
     if (zero_hit) {
@@ -583,6 +594,10 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
     n_zero += __shfl_xor_sync(0xffffffffu, n_zero, o);
   }
   if (lane == 0) {
+    atomicAdd(stats + ST_CLIP_PLANES, (unsigned long long)c_planes);
+    atomicAdd(stats + ST_CLIP_TESTS, (unsigned long long)c_tests);
+    atomicAdd(stats + ST_CLIP_CONSTR, (unsigned long long)c_constr);
+    atomicAdd(stats + ST_CLIP_FAN, (unsigned long long)c_fan);
     if (n_exact) atomicAdd(stats + ST_EXACT, (unsigned long long)n_exact);
     if (n_zero) atomicAdd(stats + ST_ZERO, (unsigned long long)n_zero);
     if (n_over && VPL > 1) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
@@ -655,8 +670,8 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 template <int VPL>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
-                                 const int32_t* cand_idx, bool collect_overflow,
-                                 const int32_t* n_dev) {
+                                 const int32_t* cand_idx, const int32_t* moff,
+                                 bool collect_overflow, const int32_t* n_dev) {
   constexpr int WARPS = VPL == 1 ? 8 : 2;
   size_t smem = sizeof(WarpState<VPL>) * WARPS;
   cudaError_t e = cudaFuncSetAttribute(k_clip<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -672,7 +687,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
-            c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), c->p_moff.as<int32_t>(),
+            c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
             collect_overflow ? c->p_over.as<int32_t>() + 1 : nullptr,
             collect_overflow ? c->p_over.as<int32_t>() : nullptr};
   k_clip<VPL><<<(unsigned)grid, WARPS * 32, smem, c->stream>>>(
@@ -687,24 +702,26 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
 // fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
 // or the wide kernel over all pairs when `wide`
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
-                        const int32_t* tet_ids, const int32_t* cand_idx, int wide) {
+                        const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
+                        int wide) {
   if (n_pairs == 0) return cudaSuccess;
   if (wide)
-    return launch_clip_t<4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, false, nullptr);
-  return launch_clip_t<1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, true, nullptr);
+    return launch_clip_t<4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, false,
+                            nullptr);
+  return launch_clip_t<1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, true, nullptr);
 }
 
 // wide kernel over the overflow list p_over[1 .. p_over[0]] (count read on the device)
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
-                                 const int32_t* cand_idx) {
+                                 const int32_t* cand_idx, const int32_t* moff) {
   return launch_clip_t<4>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx,
-                          false, c->p_over.as<int32_t>());
+                          moff, false, c->p_over.as<int32_t>());
 }
 
-cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs) {
+cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {
   if (n_pairs > 0) {
     k_count_inc<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
-        n_pairs, c->p_flag.as<uint8_t>(), c->p_moff.as<int32_t>(), c->p_mask.as<unsigned>(),
+        n_pairs, c->p_flag.as<uint8_t>(), moff, c->p_mask.as<unsigned>(),
         c->p_ninc.as<int32_t>(), c->p_f01.as<uint8_t>());
     ++c->launches;
   }
@@ -715,13 +732,13 @@ cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs) {
 
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
-                                  const PieceDst& d) {
+                                  const int32_t* moff, const PieceDst& d) {
   if (n_pairs > 0) {
     k_compact_pieces<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, cand_idx, c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(),
         c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(),
         c->p_vol.as<double>(), c->p_m1.as<double>(), c->p_fm.as<uint8_t>(),
-        c->p_moff.as<int32_t>(), c->p_mask.as<unsigned>(), d.sphere, d.vol, d.m1, d.fm,
+        moff, c->p_mask.as<unsigned>(), d.sphere, d.vol, d.m1, d.fm,
         d.inc_off, d.inc);
     ++c->launches;
   } else {

@@ -59,7 +59,12 @@ enum StatIdx {
   ST_OVERFLOW = 4,   // pieces that exceeded RPD_MAXV / RPD_MAXP / RPD_INC_CAP
   ST_MAXK = 5,       // max k_tet of the last filter
   ST_TESTED = 6,     // pairs evaluated by Alg. 1 (pruned mode)
-  ST_N = 8
+  ST_REL_TESTS = 7,  // literal Alg. 1 vertex tests (inner break, outer early exit)
+  ST_CLIP_PLANES = 8,   // (pair, plane) corner classifications in the clip
+  ST_CLIP_TESTS = 9,    // vertex sign tests in the clip
+  ST_CLIP_CONSTR = 10,  // vertex constructions
+  ST_CLIP_FAN = 11,     // fan triangles of the volume/moment integration
+  ST_N = 16
 };
 
 struct Stage {
@@ -75,6 +80,22 @@ struct Stage {
 
 }  // namespace rpd
 
+namespace rpd {
+// candidate CSR over a list of tets (all tets of the ctx, or the dirty tets of an update)
+struct CandSet {
+  DevBuf off;       // int32 [n_tets+1]
+  DevBuf idx;       // int32 [n]   candidate sphere ids, ascending per tet
+  DevBuf pair_tet;  // int32 [n]   local tet index of every pair
+  DevBuf moff;      // int32 [n+1] incidence-mask word offsets of every pair
+  int64_t n = 0, n_tets = 0, n_words = 0;
+};
+// piece CSR over a list of tets
+struct PieceSet {
+  DevBuf off, sphere, vol, m1, fm, inc_off, inc;
+  int64_t n_tets = 0, n_pieces = 0, n_inc = 0;
+};
+}  // namespace rpd
+
 struct rpd_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -88,43 +109,41 @@ struct rpd_ctx {
   rpd::DevBuf h_verts, h_tets, h_spheres, h_off, h_idx, h_new;
 
   rpd::Stage st;
-  rpd::DevBuf verts_lat;   // unused placeholder for future
-  rpd::DevBuf tets;        // int32 [T][4] copy (for partial updates)
   rpd::DevBuf errw;        // int32[4]
   rpd::DevBuf stats;       // uint64[ST_N]
   rpd::DevBuf scratch;     // scan block sums
 
-  // relations
-  rpd::DevBuf k_tet, slab, cand_off, cand_idx, pair_tet;
+  // filter scratch
+  rpd::DevBuf k_tet, k_words, slab, w_off;
   int slab_cap = 32;
-  int64_t n_cand = 0;
-  bool have_rel = false;
 
-  // clip per-pair
-  rpd::DevBuf k_words, w_off;            // incidence-mask words per tet and their offsets
-  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_words, p_moff, p_mask, p_over;
-  rpd::DevBuf p_scan, i_scan;
-  int64_t n_mask_words = 0;
-  int clip_wide = 0;                     // testing: run every pair through the wide kernel
-  // pieces
-  rpd::DevBuf piece_off, piece_sphere, piece_vol, piece_m1, piece_fm, inc_off, inc_sphere;
-  int64_t n_pieces = 0, n_inc = 0;
-  bool have_pieces = false;
+  // current candidates / pieces (double-buffered for partial updates) and the dirty sets
+  rpd::CandSet cand[2], cand_d;
+  rpd::PieceSet pcs[2], pcs_d;
+  int cur = 0;
+  bool have_rel = false, have_pieces = false;
 
-  // partial update
-  rpd::DevBuf dirty_flag, dirty_list, dirty_scan;
+  // clip per-pair scratch
+  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_scan, i_scan;
+
+  // partial update scratch
+  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off;
   int64_t n_dirty = 0;
 
   rpd_stats last{};
-  void* pinned = nullptr;  // small pinned host buffer for scalar readbacks
+  int profile = 0;             // record CUDA events around the filter and clip kernels
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* pinned = nullptr;      // small pinned host buffer for scalar readbacks
+  int clip_wide = 0;           // testing: run every pair through the wide kernel
 };
 
 namespace rpd {
 
 // launchers (all on ctx->stream; each increments ctx->launches)
-cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
-                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
-                         const int32_t* nbr_idx, int64_t E);
+cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
+                              int64_t T);
+cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
+                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E);
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
@@ -135,10 +154,11 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* 
                                  int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
                                  int32_t* p_moff, int64_t n_pairs);
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
-                        const int32_t* tet_ids, const int32_t* cand_idx, int wide);
+                        const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
+                        int wide);
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
-                                 const int32_t* cand_idx);
-cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs);
+                                 const int32_t* cand_idx, const int32_t* moff);
+cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff);
 // destination of a piece compaction
 struct PieceDst {
   int32_t* off;      // [n_tets+1]
@@ -151,6 +171,13 @@ struct PieceDst {
 };
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
-                                  const PieceDst& d);
+                                  const int32_t* moff, const PieceDst& d);
+// partial update (rpd_partial.cu)
+cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old);
+cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
+cudaError_t launch_moff(rpd_ctx* c, int64_t n, const int32_t* cand_idx, int32_t* moff);
+cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
+                         const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
+                         int phase);
 
 }  // namespace rpd

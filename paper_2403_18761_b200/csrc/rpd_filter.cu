@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     Z[k] = valid ? tx[(3 * k + 2) * T + t] : 0.0;
   }
   int cnt = 0, words = 0;
+  long long ntests = 0;  // literal Alg. 1 vertex tests of this lane
   for (int i = lo; i < hi; ++i) {
     int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     bool alive = valid;
@@ -45,12 +46,14 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     } else {
       for (int e = e0; e < e1; ++e) {
         double4 p = planes[e];
-        bool hit = false;
+        bool hk[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           double h = fma(p.x, X[k], fma(p.y, Y[k], fma(p.z, Z[k], p.w)));
-          hit |= pos(h);
+          hk[k] = pos(h);
         }
+        const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+        if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
         alive = alive && hit;
         if (!__any_sync(0xffffffffu, alive)) break;
       }
@@ -69,7 +72,12 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
   int m = cnt;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(stats + ST_MAXK, (unsigned long long)m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ntests += __shfl_xor_sync(0xffffffffu, ntests, o);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(stats + ST_MAXK, (unsigned long long)m);
+    atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
+  }
 }
 
 __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,

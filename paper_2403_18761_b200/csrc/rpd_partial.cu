@@ -1,0 +1,195 @@
+// rpd_partial.cu -- SURVEY.md §8(a) row a6: partial RPD update.
+//
+// "We only select a subset of tets from T relating to new spheres {m_j} and compute the
+// intersection among them.  Thus, the RPD is updated partially instead of re-computing as a
+// whole" (also 384, 396).  Reading R11: dirty tets are the tets that
+// Alg. 1 relates to at least one new sphere; they are re-filtered against all spheres and
+// re-clipped with the new neighbour lists, every other tet keeps its candidates and pieces.
+//
+// Kernels here: new-id validation, dirty-tet list (flag -> scan -> ascending list + position
+// map), incidence-mask offsets of a candidate set, and the two-phase CSR merge (per-tet
+// counts -> scans -> per-tet copies) of the clean old tets and the re-clipped dirty tets.
+#include "rpd_ctx.h"
+#include "rpd_internal.cuh"
+
+namespace rpd {
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+__global__ void k_check_new_ids(const int32_t* __restrict__ new_ids, int64_t M, int64_t N_old,
+                                int* err) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= M) return;
+  if (new_ids[k] != N_old + k && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+    err[1] = 100;  // new ids not the appended range
+    err[2] = (int)k;
+  }
+}
+
+__global__ void k_dirty_flag(int64_t T, const int32_t* __restrict__ count,
+                             uint8_t* __restrict__ flag) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < T) flag[t] = count[t] > 0;
+}
+
+__global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
+                             const int32_t* __restrict__ scan, int32_t* __restrict__ list,
+                             int32_t* __restrict__ pos) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  if (flag[t]) {
+    list[scan[t]] = (int32_t)t;
+    pos[t] = scan[t];
+  } else {
+    pos[t] = -1;
+  }
+}
+
+cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old) {
+  if (M == 0) return cudaSuccess;
+  k_check_new_ids<<<nblk(M, 256), 256, 0, c->stream>>>(new_ids, M, N_old, c->errw.as<int>());
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+// d_count (filter counts over the new spheres) -> d_flag -> d_scan -> d_list, d_pos
+cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
+  if (T == 0) return cudaMemsetAsync(c->d_scan.p, 0, sizeof(int32_t), c->stream);
+  k_dirty_flag<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_count.as<int32_t>(),
+                                                    c->d_flag.as<uint8_t>());
+  ++c->launches;
+  cudaError_t e = launch_scan_u8(c, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), T);
+  if (e) return e;
+  k_dirty_list<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_flag.as<uint8_t>(),
+                                                    c->d_scan.as<int32_t>(),
+                                                    c->d_list.as<int32_t>(),
+                                                    c->d_pos.as<int32_t>());
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- incidence-mask offsets
+
+__global__ void k_pair_words(int64_t n, const int32_t* __restrict__ cand_idx,
+                             const int32_t* __restrict__ nbr_off, int32_t* __restrict__ words) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int i = cand_idx[p];
+  words[p] = (nbr_off[i + 1] - nbr_off[i] + 31) >> 5;
+}
+
+// moff = exclusive scan of ceil(k_site(i)/32) over the pairs (uses p_ninc as scratch)
+cudaError_t launch_moff(rpd_ctx* c, int64_t n, const int32_t* cand_idx, int32_t* moff) {
+  if (n > 0) {
+    k_pair_words<<<nblk(n, 256), 256, 0, c->stream>>>(n, cand_idx, c->st.nbr_off.as<int32_t>(),
+                                                      c->p_ninc.as<int32_t>());
+    ++c->launches;
+  }
+  return launch_scan_i32(c, c->p_ninc.as<int32_t>(), moff, n);
+}
+
+// ---------------------------------------------------------------- merge
+
+struct MergeSrc {
+  const int32_t *c_off, *c_idx;
+  const int32_t *p_off, *p_sphere, *p_inc_off, *p_inc;
+  const double *p_vol, *p_m1;
+  const uint8_t* p_fm;
+};
+
+__device__ inline MergeSrc pick(int d, const MergeSrc& o, const MergeSrc& n) {
+  return d >= 0 ? n : o;
+}
+
+__global__ void k_merge_counts(int64_t T, const int32_t* __restrict__ dpos, MergeSrc o,
+                               MergeSrc n, int32_t* __restrict__ cnt) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int d = dpos[t];
+  const MergeSrc s = pick(d, o, n);
+  const int64_t k = d >= 0 ? d : t;
+  const int p0 = s.p_off[k], p1 = s.p_off[k + 1];
+  cnt[t] = s.c_off[k + 1] - s.c_off[k];
+  cnt[T + t] = p1 - p0;
+  cnt[2 * T + t] = s.p_inc_off[p1] - s.p_inc_off[p0];
+}
+
+struct MergeDst {
+  const int32_t *c_off, *p_off, *i_tet;  // scans of the counts (new offsets)
+  int32_t *c_idx, *pair_tet, *p_sphere, *p_inc_off, *p_inc;
+  double *p_vol, *p_m1;
+  uint8_t* p_fm;
+};
+
+__global__ void k_merge_copy(int64_t T, const int32_t* __restrict__ dpos, MergeSrc o,
+                             MergeSrc n, MergeDst D, int64_t n_pieces_new, int64_t n_inc_new) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  if (t == T - 1) D.p_inc_off[n_pieces_new] = (int32_t)n_inc_new;
+  const int d = dpos[t];
+  const MergeSrc s = pick(d, o, n);
+  const int64_t k = d >= 0 ? d : t;
+  // candidates
+  const int c0 = s.c_off[k], c1 = s.c_off[k + 1];
+  int dc = D.c_off[t];
+  for (int q = c0; q < c1; ++q, ++dc) {
+    D.c_idx[dc] = s.c_idx[q];
+    D.pair_tet[dc] = (int32_t)t;
+  }
+  // pieces and incidences
+  const int p0 = s.p_off[k], p1 = s.p_off[k + 1];
+  const int ibase = s.p_inc_off[p0];
+  int dp = D.p_off[t];
+  const int di = D.i_tet[t];
+  for (int q = p0; q < p1; ++q, ++dp) {
+    D.p_sphere[dp] = s.p_sphere[q];
+    D.p_vol[dp] = s.p_vol[q];
+    D.p_m1[3 * dp + 0] = s.p_m1[3 * q + 0];
+    D.p_m1[3 * dp + 1] = s.p_m1[3 * q + 1];
+    D.p_m1[3 * dp + 2] = s.p_m1[3 * q + 2];
+    D.p_fm[dp] = s.p_fm[q];
+    D.p_inc_off[dp] = di + (s.p_inc_off[q] - ibase);
+    for (int r = s.p_inc_off[q]; r < s.p_inc_off[q + 1]; ++r)
+      D.p_inc[di + (r - ibase)] = s.p_inc[r];
+  }
+}
+
+static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
+  return MergeSrc{cs.off.as<int32_t>(),     cs.idx.as<int32_t>(),    ps.off.as<int32_t>(),
+                  ps.sphere.as<int32_t>(),  ps.inc_off.as<int32_t>(), ps.inc.as<int32_t>(),
+                  ps.vol.as<double>(),      ps.m1.as<double>(),      ps.fm.as<uint8_t>()};
+}
+
+// phase 0: per-tet counts and their scans (new cand offsets -> cn.off, new piece offsets ->
+// pn.off, tet-level incidence offsets -> m_off); totals at [T] of each.
+// phase 1: copies (requires cn / pn buffers sized from the phase-0 totals).
+cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
+                         const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
+                         int phase) {
+  MergeSrc o = src_of(co, po), n = src_of(cd, pd);
+  if (phase == 0) {
+    if (T > 0) {
+      k_merge_counts<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n,
+                                                          c->m_cnt.as<int32_t>());
+      ++c->launches;
+    }
+    cudaError_t e;
+    if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>(), cn.off.as<int32_t>(), T))) return e;
+    if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>() + T, pn.off.as<int32_t>(), T))) return e;
+    return launch_scan_i32(c, c->m_cnt.as<int32_t>() + 2 * T, c->m_off.as<int32_t>(), T);
+  }
+  MergeDst D{cn.off.as<int32_t>(),     pn.off.as<int32_t>(),    c->m_off.as<int32_t>(),
+             cn.idx.as<int32_t>(),     cn.pair_tet.as<int32_t>(), pn.sphere.as<int32_t>(),
+             pn.inc_off.as<int32_t>(), pn.inc.as<int32_t>(),     pn.vol.as<double>(),
+             pn.m1.as<double>(),       pn.fm.as<uint8_t>()};
+  if (T > 0) {
+    k_merge_copy<<<nblk(T, 128), 128, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D,
+                                                      pn.n_pieces, pn.n_inc);
+    ++c->launches;
+  } else {
+    cudaMemsetAsync(pn.inc_off.p, 0, sizeof(int32_t), c->stream);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rpd

@@ -159,21 +159,13 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
-                         int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
-                         const int32_t* nbr_idx, int64_t E) {
+cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
+                              int64_t T) {
   Stage& s = c->st;
-  cudaError_t e;
-  if ((e = s.tx.ensure(sizeof(double) * 12 * (T > 0 ? T : 1)))) return e;
-  if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
-  if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
-  if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
-  if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
-  if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  cudaError_t e = s.tx.ensure(sizeof(double) * 12 * (T > 0 ? T : 1));
+  if (e) return e;
   s.T = T;
-  s.N = N;
   s.V = V;
-  s.E = E;
   int* err = c->errw.as<int>();
   if (c->validate && V > 0) {
     k_check_verts<<<nblk(3 * V, 256), 256, 0, c->stream>>>(verts, 3 * V, err);
@@ -183,6 +175,21 @@ cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32
     k_stage_tets<<<nblk(T, 256), 256, 0, c->stream>>>(verts, V, tets, T, s.tx.as<double>(), err);
     ++c->launches;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
+                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E) {
+  Stage& s = c->st;
+  cudaError_t e;
+  if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
+  if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
+  if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  s.N = N;
+  s.E = E;
+  int* err = c->errw.as<int>();
   if (N > 0) {
     k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(spheres, N, s.sw.as<double4>(), err);
     ++c->launches;
@@ -190,6 +197,9 @@ cudaError_t launch_stage(rpd_ctx* c, const double* verts, int64_t V, const int32
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(), err);
     ++c->launches;
+  } else {
+    e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
+    if (e) return e;
   }
   return cudaGetLastError();
 }

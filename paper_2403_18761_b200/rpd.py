@@ -19,7 +19,7 @@ RPD_OK, RPD_EINVAL, RPD_ENOMEM, RPD_ECUDA, RPD_EOVERFLOW, RPD_ESTATE, RPD_ENOTEX
     0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "RPD_OK", -1: "RPD_EINVAL", -2: "RPD_ENOMEM", -3: "RPD_ECUDA",
                 -4: "RPD_EOVERFLOW", -5: "RPD_ESTATE", -6: "RPD_ENOTEXACT"}
-OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM, OPT_CLIP_WIDE = 1, 2, 3, 4
+OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM, OPT_CLIP_WIDE, OPT_PROFILE = 1, 2, 3, 4, 5
 FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
@@ -46,7 +46,11 @@ class _Stats(C.Structure):
                 ("pairs_filtered", C.c_int64), ("pairs_tested", C.c_int64),
                 ("exact_fallbacks", C.c_int64), ("zero_hits", C.c_int64),
                 ("kernel_launches", C.c_int64), ("max_k_tet", C.c_int32),
-                ("max_vertices", C.c_int32), ("max_planes", C.c_int32), ("n_wide", C.c_int32)]
+                ("max_vertices", C.c_int32), ("max_planes", C.c_int32), ("n_wide", C.c_int32),
+                ("rel_tests", C.c_int64), ("clip_plane_evals", C.c_int64),
+                ("clip_vertex_tests", C.c_int64), ("clip_constructions", C.c_int64),
+                ("clip_fan_triangles", C.c_int64), ("filter_ms", C.c_double),
+                ("clip_ms", C.c_double)]
 
 
 _lib = None
@@ -141,6 +145,10 @@ class RPDContext:
         """Testing: route every pair through the wide (128-vertex) clip kernel."""
         self._check(self.L.rpd_set_option(self.h, OPT_CLIP_WIDE, int(bool(on))))
 
+    def set_profile(self, on: bool):
+        """Time the filter and clip kernels with CUDA events (stats filter_ms / clip_ms)."""
+        self._check(self.L.rpd_set_option(self.h, OPT_PROFILE, int(bool(on))))
+
     def close(self):
         if getattr(self, "h", None):
             self.L.rpd_destroy(self.h)
@@ -189,6 +197,8 @@ class RPDContext:
                                               C.byref(dt), C.byref(nd)))
         self.N = N_new
         self.counts = PieceCounts(P.n_pieces, P.n_inc)
+        self.n_cand = self.stats()["n_cand"]
+        self.n_dirty = nd.value
         self._dirty_ptr = dt.value
         self._keep_p = (ks, ko, ki, kn)
         return self.counts, nd.value

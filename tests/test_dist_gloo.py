@@ -1,0 +1,70 @@
+"""Multi-rank path on CPU (gloo, world_size 2): block-cyclic tet shards of the oracle's
+results all-gathered and reordered equal the single-rank result byte for byte (SURVEY.md
+§8(e) P8).  The CUDA kernels are per-tet independent, so the same holds on NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import rpd_workloads as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_18761_b200.dist import gather_pieces, shard_tets
+        w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
+        ids = shard_tets(w.T, world, rank, block=256)
+        r = oracle.rpd_workload(w, tet_ids=ids)
+        local = {k: torch.as_tensor(np.asarray(v)) for k, v in r.items() if k != "stats"}
+        local["piece_m1"] = local["piece_m1"].reshape(-1, 3)
+        out = gather_pieces(local, ids, w.T)
+        if rank == 0:
+            q.put({k: v.numpy() for k, v in out.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_equals_single_rank():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
+    ref = oracle.rpd_workload(w)
+    for k in ("piece_off", "piece_sphere", "piece_vol", "piece_facemask", "inc_off",
+              "inc_sphere"):
+        assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), k
+    assert np.array_equal(got["piece_m1"].reshape(-1, 3), ref["piece_m1"])
+
+
+def test_shards_partition_the_tets():
+    from paper_2403_18761_b200.dist import shard_tets
+    T = 100_003
+    for world in (1, 2, 4, 8):
+        ids = np.concatenate([shard_tets(T, world, r) for r in range(world)])
+        assert np.array_equal(np.sort(ids), np.arange(T))
+        sizes = [len(shard_tets(T, world, r)) for r in range(world)]
+        assert max(sizes) - min(sizes) <= 4096

@@ -1,0 +1,101 @@
+"""Partial RPD update on the GPU vs the oracle (-m gpu).  DESIGN.md R11/R12: dirty tets =
+tets related (Alg. 1) to a new sphere, re-filtered and re-clipped; clean tets keep their
+pieces byte-identically; pieces equal a full recompute (inputs without exact-zero hits)."""
+import numpy as np
+import pytest
+
+import oracle
+import rpd_workloads as W
+from tests.helpers import compare_results, slice_tets
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2403_18761_b200 as P
+    P.build()
+    c = P.RPDContext(0)
+    yield c
+    c.close()
+
+
+def gpu_state(ctx):
+    out = ctx.download_cands()
+    out.update(ctx.download_pieces())
+    return out
+
+
+@pytest.mark.parametrize("seed", [3, 7])
+def test_partial_equals_oracle_partial(ctx, seed):
+    w = W.make_shape_workload("S", 2000, 150, seed=seed, n_batches=3, batch_m=12, clusters=3,
+                              cache=False)
+    ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    ctx.clip()
+    prev = oracle.rpd_workload(w)
+    n_old = w.N
+    for (sph, off, idx) in w.batches:
+        new = np.arange(n_old, len(sph), dtype=np.int32)
+        counts, nd = ctx.update_partial(sph, off, idx, new)
+        got = gpu_state(ctx)
+        ref, dirty = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old)
+        assert nd == len(dirty) and nd > 0
+        errs = compare_results(got, ref, w.verts, w.tets, rel=1e-9)
+        assert not errs, errs[:5]
+        # pieces also equal a full recompute (no exact-zero hits on this generic input)
+        full = oracle.rpd(w.verts, w.tets, sph, off, idx)
+        errs = compare_results(got, full, w.verts, w.tets, rel=1e-9, check_cands=False)
+        assert not errs, errs[:5]
+        prev, n_old = ref, len(sph)
+
+
+def test_partial_identity_and_errors(ctx):
+    import paper_2403_18761_b200 as P
+    w = W.make_shape_workload("S", 2000, 150, seed=3, n_batches=1, batch_m=12, clusters=3,
+                              cache=False)
+    ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    ctx.clip()
+    before = gpu_state(ctx)
+    counts, nd = ctx.update_partial(w.spheres, w.nbr_off, w.nbr_idx, np.zeros(0, np.int32))
+    assert nd == 0
+    after = gpu_state(ctx)
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+    sph, off, idx = w.batches[0]
+    bad = np.arange(w.N, len(sph), dtype=np.int32)[::-1].copy()
+    with pytest.raises(P.RPDError) as e:
+        ctx.update_partial(sph, off, idx, bad)
+    assert e.value.status == -1
+
+
+def test_partial_before_clip_is_state_error():
+    import paper_2403_18761_b200 as P
+    c = P.RPDContext(0)
+    w = W.make_c1(0)
+    with pytest.raises(P.RPDError) as e:
+        c.update_partial(w.spheres, w.nbr_off, w.nbr_idx, np.zeros(0, np.int32))
+    assert e.value.status == -5
+    c.close()
+
+
+def test_c4_sampled(ctx):
+    """BASELINE.json configs[3] at full size: 10 iterations x M = 500 on the 200k-tet mesh;
+    after the last one, sampled tets equal the oracle's full recompute on the final sphere set,
+    and the last batch's dirty set equals Alg. 1 against the new spheres on the sample."""
+    w = W.make_config("C4")
+    ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    ctx.clip()
+    n_old = w.N
+    for (sph, off, idx) in w.batches:
+        new = np.arange(n_old, len(sph), dtype=np.int32)
+        counts, nd = ctx.update_partial(sph, off, idx, new)
+        assert 0 < nd < w.T
+        n_prev, n_old = n_old, len(sph)
+    got = gpu_state(ctx)
+    sph, off, idx = w.batches[-1]
+    rng = np.random.default_rng(1)
+    ids = np.sort(rng.choice(w.T, 40, replace=False)).astype(np.int32)
+    full = oracle.rpd(w.verts, w.tets, sph, off, idx, tet_ids=ids)
+    sub = slice_tets(got, ids)
+    errs = compare_results(sub, full, w.verts, w.tets, tet_ids=ids, rel=1e-9, check_cands=False)
+    assert not errs, errs[:5]
