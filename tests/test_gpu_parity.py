@@ -69,7 +69,9 @@ def test_shape_workloads(ctx, seed, tets, sph, mode):
     """Several tiles (256-tet filter blocks, 8-pair clip blocks) and a ragged tail."""
     w = W.make_shape_workload(f"P{seed}", tets, sph, seed=seed, radius_mode=mode, cache=False)
     assert w.T % 256 != 0
-    got, _ = check(ctx, w)
+    got, ref = check(ctx, w)
+    # the kernel's algorithmic-work counter equals the oracle's literal Alg. 1 test count
+    assert got["stats"]["rel_tests"] == ref["stats"]["n_rel_tests"]
     vt = tet_volumes(w.verts, w.tets)
     s = np.zeros(w.T)
     np.add.at(s, piece_tet(got), got["piece_vol"])
