@@ -243,8 +243,9 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   for (int attempt = 0; attempt < 2; ++attempt) {
     const int cap = c->slab_cap;
     CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * nt), "alloc slab");
+    // ST_MAXK, ST_TESTED, ST_REL_TESTS
     CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
-                       sizeof(unsigned long long), c->stream), "memset");
+                       sizeof(unsigned long long) * 3, c->stream), "memset");
     if (timed && c->profile) cudaEventRecord(c->ev[0], c->stream);
     CK(launch_filter(c, tet_ids, n_tets, cap, lo, hi, c->k_tet.as<int32_t>(),
                      c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
@@ -280,6 +281,9 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                           c->w_off.as<int32_t>(), cs.moff.as<int32_t>(), nc), "compact");
   c->last.max_k_tet = (int32_t)rb->u64[ST_MAXK];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
+  c->last.pairs_tested += c->filter_mode == RPD_FILTER_PRUNED
+                              ? (int64_t)rb->u64[ST_TESTED]
+                              : n_tets * (int64_t)(hi - lo);
   if (timed && c->profile) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
@@ -415,7 +419,6 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   c->have_rel = true;
   c->last.n_cand = cs.n;
   c->last.pairs_filtered = T * N;
-  c->last.pairs_tested = T * N;
   *cand_off = cs.off.as<int32_t>();
   *cand_idx = cs.idx.as<int32_t>();
   *n_cand = cs.n;
@@ -494,6 +497,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   }
   const int64_t nd = rb->i32[0];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
+  c->last.pairs_tested += c->filter_mode == RPD_FILTER_PRUNED ? (int64_t)rb->u64[ST_TESTED]
+                                                              : T * M;
   if (c->profile) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
@@ -555,7 +560,6 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   c->last.n_pieces = pn.n_pieces;
   c->last.n_inc = pn.n_inc;
   c->last.pairs_filtered = T * M + nd * N_new;
-  c->last.pairs_tested = T * M + nd * N_new;
   *dirty_tets = dl;
   *n_dirty = nd;
   return fill_pieces(c, out);

@@ -184,3 +184,41 @@ def test_wide_kernel_parity(ctx, make):
         check(ctx, make())
     finally:
         ctx.set_clip_wide(False)
+
+
+@pytest.fixture(scope="module")
+def ctx_pruned():
+    import paper_2403_18761_b200 as P
+    P.build()
+    c = P.RPDContext(0, filter_mode="pruned")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(1, degenerate=True),
+                                  lambda: W.make_c1(6, degenerate=True, big=True),
+                                  lambda: W.random_tiny(3, n_spheres=14, grid=2, coarse=True),
+                                  lambda: W.make_shape_workload("P3", 2000, 150, seed=3,
+                                                                cache=False),
+                                  lambda: W.make_shape_workload("P5", 3000, 300, seed=5,
+                                                                radius_mode="high_variance",
+                                                                cache=False),
+                                  lambda: W.make_shape_workload("one", 700, 1, seed=2,
+                                                                cache=False)])
+def test_pruned_filter_parity(ctx_pruned, make):
+    """the pruned filter gives the same candidate lists (and pieces) as the
+    literal all-pairs Alg. 1 / the oracle, while evaluating fewer pairs."""
+    w = make()
+    got, ref = check(ctx_pruned, w)
+    st = got["stats"]
+    assert st["pairs_tested"] <= st["pairs_filtered"]
+
+
+def test_pruned_equals_allpairs_c3(ctx, ctx_pruned):
+    w = W.make_config("C3")
+    a = run_gpu(ctx, w)
+    b = run_gpu(ctx_pruned, w)
+    for k in ("cand_off", "cand_idx", "piece_off", "piece_sphere", "piece_vol", "piece_m1",
+              "piece_facemask", "inc_off", "inc_sphere"):
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+    assert b["stats"]["pairs_tested"] < a["stats"]["pairs_tested"] / 20

@@ -11,11 +11,11 @@ from tests.helpers import compare_results, slice_tets
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def ctx():
+@pytest.fixture(scope="module", params=["all_pairs", "pruned"])
+def ctx(request):
     import paper_2403_18761_b200 as P
     P.build()
-    c = P.RPDContext(0)
+    c = P.RPDContext(0, filter_mode=request.param)
     yield c
     c.close()
 
