@@ -115,6 +115,7 @@ struct rpd_ctx {
 
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
+  rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
   int slab_cap = 32;
 
   // current candidates / pieces (double-buffered for partial updates) and the dirty sets
@@ -150,7 +151,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
                           int32_t* k_words);
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* k_tet,
-                                 const int32_t* slab, const int32_t* cand_off,
+                                 int32_t* slab, const int32_t* cand_off,
                                  int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
                                  int32_t* p_moff, int64_t n_pairs);
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,

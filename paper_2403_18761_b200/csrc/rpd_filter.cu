@@ -9,11 +9,18 @@
 // integer operands with exact partial sums), so the booleans are exact; the "> 0" test reads
 // the fp64 bit pattern as int64, which keeps the compares off the FP64 pipe.
 //
-// Kernel shape: lane = tet (tets are Morton-sorted, so a warp covers a compact region), the
-// warp sweeps all spheres in id order and, per sphere, its planes in CSR order until every
-// lane has failed a plane (warp-uniform early exit, the paper's outer loop); planes are
-// warp-uniform broadcast loads.  Positive spheres are appended to a per-tet slab
-// slab[c * n + t] (c < cap, coalesced over t), already in ascending sphere id.
+// Two kernels compute the same booleans:
+//  * k_filter_allpairs -- literal "every pair of tet-sphere": lane = tet
+//    (Morton order), the warp sweeps all spheres and their planes with a warp-uniform early
+//    exit.
+//  * k_filter_bvh (RPD_FILTER_PRUNED) -- sphere-centric traversal of a 2-level box hierarchy
+//    over the Morton-ordered tets (leaves = 32 tets, super nodes = 32 leaves).  A node is
+//    skipped when some plane h_ij has max over the node's exact lattice AABB <= 0: then every
+//    vertex of every tet below fails that plane and Alg. 1 rejects them all.  Leaves that
+//    survive run the exact Alg. 1, lane = tet.  Work is proportional to the relations, not to
+//    T x N.
+// Positive pairs go to a per-tet slab slab[a * cap + c]; the compaction sorts each tet's list
+// (ascending sphere id, R9) and writes the CSR.
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -21,172 +28,7 @@ namespace rpd {
 
 __device__ __forceinline__ bool pos(double h) { return __double_as_longlong(h) > 0; }
 
-// Alg. 1 for sphere i and this lane's tet (warp-uniform i; all 32 lanes must call).  The
-// loop over neighbours stops when every lane of the warp has failed a plane.
-__device__ __forceinline__ bool alg1_warp(int i, const double (&X)[4], const double (&Y)[4],
-                                          const double (&Z)[4], bool valid,
-                                          const int32_t* __restrict__ nbr_off,
-                                          const double4* __restrict__ planes, int N,
-                                          long long& ntests, int& e0_out, int& e1_out) {
-  const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
-  e0_out = e0;
-  e1_out = e1;
-  bool alive = valid;
-  if (e0 == e1) return alive && (N == 1);
-  for (int e = e0; e < e1; ++e) {
-    const double4 p = planes[e];
-    bool hk[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double h = fma(p.x, X[k], fma(p.y, Y[k], fma(p.z, Z[k], p.w)));
-      hk[k] = pos(h);
-    }
-    const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
-    if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
-    alive = alive && hit;
-    if (!__any_sync(0xffffffffu, alive)) break;
-  }
-  return alive;
-}
-
-// ------------------------------------------------------------------ pruned filter
-// Same booleans as the all-pairs kernel, without evaluating pairs that provably fail:
-// a CTA of PF_T Morton-consecutive tets computes the exact lattice AABB B of their vertices;
-// sphere i can relate to one of them only if every plane h_ij has max_B h_ij > 0 (if some
-// plane has max_B h_ij <= 0, every vertex of every tet of the CTA fails that plane, so Alg. 1
-// rejects all of them).  max_B h = d + sum_c max(n_c lo_c, n_c hi_c) is exact (integers).
-// The CTA sweeps all spheres with lane = sphere (level 1), compacts the survivors in
-// ascending id into shared memory, and its warps then run the exact Alg. 1 (lane = tet) on
-// the survivors only (level 2).  DESIGN.md §Prune.
-constexpr int PF_T = 128;
-constexpr int PF_LIST = 3072;
-
-__global__ void __launch_bounds__(PF_T) k_filter_pruned(
-    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
-    const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes, int N, int lo,
-    int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-    int32_t* __restrict__ k_words, unsigned long long* __restrict__ stats) {
-  __shared__ double s_box[PF_T / 32][6];
-  __shared__ int s_list[PF_LIST];
-  __shared__ int s_wc[PF_T / 32];
-  __shared__ int s_cnt;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned FULL = 0xffffffffu;
-  const int64_t a = blockIdx.x * (int64_t)PF_T + tid;
-  const bool valid = a < n;
-  const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
-  double X[4], Y[4], Z[4];
-  double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    X[k] = valid ? tx[(3 * k + 0) * T + t] : 0.0;
-    Y[k] = valid ? tx[(3 * k + 1) * T + t] : 0.0;
-    Z[k] = valid ? tx[(3 * k + 2) * T + t] : 0.0;
-    if (valid) {
-      bl[0] = fmin(bl[0], X[k]);
-      bh[0] = fmax(bh[0], X[k]);
-      bl[1] = fmin(bl[1], Y[k]);
-      bh[1] = fmax(bh[1], Y[k]);
-      bl[2] = fmin(bl[2], Z[k]);
-      bh[2] = fmax(bh[2], Z[k]);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      bl[c] = fmin(bl[c], __shfl_xor_sync(FULL, bl[c], o));
-      bh[c] = fmax(bh[c], __shfl_xor_sync(FULL, bh[c], o));
-    }
-  if (lane == 0) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      s_box[warp][c] = bl[c];
-      s_box[warp][3 + c] = bh[c];
-    }
-  }
-  if (tid == 0) s_cnt = 0;
-  __syncthreads();
-#pragma unroll
-  for (int w = 0; w < PF_T / 32; ++w)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      bl[c] = fmin(bl[c], s_box[w][c]);
-      bh[c] = fmax(bh[c], s_box[w][3 + c]);
-    }
-
-  int cnt = 0, words = 0;
-  long long ntests = 0, npairs = 0;
-  for (int base = lo; base < hi; base += PF_T) {
-    // ---- level 1: lane = sphere, exact box rejection
-    const int i = base + tid;
-    bool pass = false;
-    if (i < hi) {
-      const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
-      if (e0 == e1) {
-        pass = (N == 1);
-      } else {
-        pass = true;
-        for (int e = e0; e < e1; ++e) {
-          const double4 p = planes[e];
-          const double mh = p.w + fmax(p.x * bl[0], p.x * bh[0]) +
-                            fmax(p.y * bl[1], p.y * bh[1]) + fmax(p.z * bl[2], p.z * bh[2]);
-          if (!pos(mh)) {
-            pass = false;
-            break;
-          }
-        }
-      }
-    }
-    const unsigned b = __ballot_sync(FULL, pass);
-    if (lane == 0) s_wc[warp] = __popc(b);
-    __syncthreads();
-    int off = s_cnt, tot = 0;
-#pragma unroll
-    for (int w = 0; w < PF_T / 32; ++w) {
-      if (w < warp) off += s_wc[w];
-      tot += s_wc[w];
-    }
-    if (pass) s_list[off + __popc(b & ((1u << lane) - 1u))] = i;
-    __syncthreads();
-    if (tid == 0) s_cnt += tot;
-    __syncthreads();
-    // ---- level 2: exact Alg. 1 on the survivors, lane = tet
-    const int nl = s_cnt;
-    if (nl > PF_LIST - PF_T || base + PF_T >= hi) {
-      for (int q = 0; q < nl; ++q) {
-        const int si = s_list[q];
-        int e0, e1;
-        const bool alive = alg1_warp(si, X, Y, Z, valid, nbr_off, planes, N, ntests, e0, e1);
-        npairs += valid;
-        if (alive) {
-          if (cnt < cap) slab[(int64_t)cnt * n + a] = si;
-          ++cnt;
-          words += (e1 - e0 + 31) >> 5;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) s_cnt = 0;
-      __syncthreads();
-    }
-  }
-  if (valid) {
-    k_tet[a] = cnt;
-    if (k_words) k_words[a] = words;
-  }
-  int m = cnt;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    m = max(m, __shfl_xor_sync(FULL, m, o));
-    ntests += __shfl_xor_sync(FULL, ntests, o);
-    npairs += __shfl_xor_sync(FULL, npairs, o);
-  }
-  if (lane == 0) {
-    atomicMax(stats + ST_MAXK, (unsigned long long)m);
-    atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
-    atomicAdd(stats + ST_TESTED, (unsigned long long)npairs);
-  }
-}
+// ------------------------------------------------------------------ literal all-pairs
 
 __global__ void __launch_bounds__(256) k_filter_allpairs(
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
@@ -226,7 +68,7 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
       }
     }
     if (alive) {
-      if (cnt < cap) slab[(int64_t)cnt * n + a] = i;
+      if (cnt < cap) slab[a * cap + cnt] = i;
       ++cnt;
       words += (e1 - e0 + 31) >> 5;  // incidence-mask words of this candidate pair
     }
@@ -235,31 +77,220 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     k_tet[a] = cnt;
     if (k_words) k_words[a] = words;
   }
-  // max k_tet (warp-aggregated)
   int m = cnt;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ntests += __shfl_xor_sync(0xffffffffu, ntests, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    ntests += __shfl_xor_sync(0xffffffffu, ntests, o);
+  }
   if ((threadIdx.x & 31) == 0) {
     atomicMax(stats + ST_MAXK, (unsigned long long)m);
     atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
   }
 }
 
+// ------------------------------------------------------------------ box hierarchy
+
+constexpr int BVH_LEAF = 32;    // tets per leaf (one warp)
+constexpr int BVH_FAN = 32;     // leaves per super node
+constexpr int BVH_PCAP = 64;    // planes of a sphere staged in shared memory
+
+// exact lattice AABB of every leaf (32 consecutive tets of the list)
+__global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
+                             const int32_t* __restrict__ tet_ids, int64_t n,
+                             double* __restrict__ leaf, int64_t n_leaf) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = a < n;
+  const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
+  double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double x = tx[(3 * k + c) * T + t];
+        bl[c] = fmin(bl[c], x);
+        bh[c] = fmax(bh[c], x);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      bl[c] = fmin(bl[c], __shfl_xor_sync(0xffffffffu, bl[c], o));
+      bh[c] = fmax(bh[c], __shfl_xor_sync(0xffffffffu, bh[c], o));
+    }
+  const int64_t l = a / BVH_LEAF;
+  if (lane == 0 && l < n_leaf) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      leaf[6 * l + c] = bl[c];
+      leaf[6 * l + 3 + c] = bh[c];
+    }
+  }
+}
+
+// AABB of every super node (32 consecutive leaves)
+__global__ void k_super_boxes(const double* __restrict__ leaf, int64_t n_leaf,
+                              double* __restrict__ sup, int64_t n_sup) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
+  if (l < n_leaf) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      bl[c] = leaf[6 * l + c];
+      bh[c] = leaf[6 * l + 3 + c];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      bl[c] = fmin(bl[c], __shfl_xor_sync(0xffffffffu, bl[c], o));
+      bh[c] = fmax(bh[c], __shfl_xor_sync(0xffffffffu, bh[c], o));
+    }
+  const int64_t s = l / BVH_FAN;
+  if (lane == 0 && s < n_sup) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sup[6 * s + c] = bl[c];
+      sup[6 * s + 3 + c] = bh[c];
+    }
+  }
+}
+
+// can some tet inside box B pass every plane of the sphere?  (exact, conservative)
+__device__ __forceinline__ bool box_passes(const double* __restrict__ B,
+                                           const double4* __restrict__ sp, int k,
+                                           const double4* __restrict__ gp) {
+  const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
+  for (int e = 0; e < k; ++e) {
+    const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
+    const double mh =
+        p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) + fmax(p.z * l2, p.z * h2);
+    if (!pos(mh)) return false;
+  }
+  return true;
+}
+
+constexpr int BVH_WARPS = 4;
+
+__global__ void __launch_bounds__(BVH_WARPS * 32) k_filter_bvh(
+    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
+    const double* __restrict__ leaf, int64_t n_leaf, const double* __restrict__ sup,
+    int64_t n_sup, const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes,
+    int N, int lo, int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
+    int32_t* __restrict__ k_words, unsigned long long* __restrict__ stats) {
+  __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  double4* sp = s_pl[warp];
+  long long ntests = 0, npairs = 0;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t ii = lo + gw; ii < hi; ii += nw) {
+    const int i = (int)ii;
+    const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+    const int k = e1 - e0;
+    if (k == 0 && N != 1) continue;  // hidden sphere (R4): relates to no tet
+    const double4* gp = planes + e0;
+    __syncwarp();
+    for (int e = lane; e < k && e < BVH_PCAP; e += 32) sp[e] = gp[e];
+    __syncwarp();
+    const int words = (k + 31) >> 5;
+    for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
+      const int64_t s = s0 + lane;
+      unsigned sm = __ballot_sync(FULL, s < n_sup && box_passes(sup + 6 * s, sp, k, gp));
+      while (sm) {
+        const int64_t sl = s0 + __ffs(sm) - 1;
+        sm &= sm - 1;
+        const int64_t l = sl * BVH_FAN + lane;
+        unsigned lm = __ballot_sync(FULL, l < n_leaf && box_passes(leaf + 6 * l, sp, k, gp));
+        while (lm) {
+          const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
+          lm &= lm - 1;
+          // exact Alg. 1, lane = tet
+          const int64_t a = ll * BVH_LEAF + lane;
+          const bool valid = a < n;
+          const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
+          double X[4], Y[4], Z[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            X[q] = valid ? tx[(3 * q + 0) * T + t] : 0.0;
+            Y[q] = valid ? tx[(3 * q + 1) * T + t] : 0.0;
+            Z[q] = valid ? tx[(3 * q + 2) * T + t] : 0.0;
+          }
+          bool alive = valid;
+          for (int e = 0; e < k; ++e) {
+            const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
+            bool hk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double h = fma(p.x, X[q], fma(p.y, Y[q], fma(p.z, Z[q], p.w)));
+              hk[q] = pos(h);
+            }
+            const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+            if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
+            alive = alive && hit;
+            if (!__any_sync(FULL, alive)) break;
+          }
+          npairs += valid;
+          if (alive) {
+            const int slot = atomicAdd(k_tet + a, 1);
+            if (slot < cap) slab[a * cap + slot] = i;
+            if (k_words) atomicAdd(k_words + a, words);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ntests += __shfl_xor_sync(FULL, ntests, o);
+    npairs += __shfl_xor_sync(FULL, npairs, o);
+  }
+  if (lane == 0) {
+    atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
+    atomicAdd(stats + ST_TESTED, (unsigned long long)npairs);
+  }
+}
+
+__global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
+                           unsigned long long* __restrict__ stats) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int m = a < n ? k_tet[a] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(stats + ST_MAXK, (unsigned long long)m);
+}
+
+// ------------------------------------------------------------------ compaction
+
 __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,
-                                const int32_t* __restrict__ slab,
-                                const int32_t* __restrict__ cand_off,
+                                int32_t* __restrict__ slab, const int32_t* __restrict__ cand_off,
                                 int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
                                 const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
                                 const int32_t* __restrict__ nbr_off, int64_t n_pairs) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
-  int k = k_tet[a];
-  int o = cand_off[a];
+  const int k = min(k_tet[a], cap);
+  int32_t* s = slab + a * cap;
+  // ascending sphere id (the BVH filter appends in arbitrary order)
+  for (int x = 1; x < k; ++x) {
+    const int v = s[x];
+    int y = x;
+    while (y > 0 && s[y - 1] > v) {
+      s[y] = s[y - 1];
+      --y;
+    }
+    s[y] = v;
+  }
+  const int o = cand_off[a];
   int w = w_off ? w_off[a] : 0;
-  for (int c = 0; c < k && c < cap; ++c) {
-    int i = slab[(int64_t)c * n + a];
+  for (int c = 0; c < k; ++c) {
+    const int i = s[c];
     cand_idx[o + c] = i;
     if (pair_tet) pair_tet[o + c] = (int32_t)a;
     if (p_moff) {
@@ -277,10 +308,34 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
                           int32_t* k_words) {
   if (n_tets == 0) return cudaSuccess;
   if (c->filter_mode == RPD_FILTER_PRUNED) {
-    k_filter_pruned<<<nblk(n_tets, PF_T), PF_T, 0, c->stream>>>(
-        c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, c->st.nbr_off.as<int32_t>(),
-        c->st.planes.as<double4>(), (int)c->st.N, sphere_lo, sphere_hi, cap, k_tet, slab,
-        k_words, c->stats.as<unsigned long long>());
+    const int64_t n_leaf = (n_tets + BVH_LEAF - 1) / BVH_LEAF;
+    const int64_t n_sup = (n_leaf + BVH_FAN - 1) / BVH_FAN;
+    cudaError_t e = c->bvh.ensure(sizeof(double) * 6 * (n_leaf + n_sup));
+    if (e) return e;
+    double* leaf = c->bvh.as<double>();
+    double* sup = leaf + 6 * n_leaf;
+    e = cudaMemsetAsync(k_tet, 0, sizeof(int32_t) * n_tets, c->stream);
+    if (!e && k_words) e = cudaMemsetAsync(k_words, 0, sizeof(int32_t) * n_tets, c->stream);
+    if (e) return e;
+    k_leaf_boxes<<<nblk(n_leaf * BVH_LEAF, 256), 256, 0, c->stream>>>(
+        c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf);
+    k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup);
+    c->launches += 2;
+    const int64_t ns = sphere_hi - sphere_lo;
+    if (ns > 0) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      int64_t blocks = (ns + BVH_WARPS - 1) / BVH_WARPS;
+      const int64_t maxb = (int64_t)sms * 16;
+      if (blocks > maxb) blocks = maxb;
+      k_filter_bvh<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
+          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf, sup, n_sup,
+          c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N, sphere_lo,
+          sphere_hi, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
+      ++c->launches;
+    }
+    k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
+                                                        c->stats.as<unsigned long long>());
     ++c->launches;
     return cudaGetLastError();
   }
@@ -293,9 +348,9 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
 }
 
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* k_tet,
-                                 const int32_t* slab, const int32_t* cand_off,
-                                 int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
-                                 int32_t* p_moff, int64_t n_pairs) {
+                                 int32_t* slab, const int32_t* cand_off, int32_t* cand_idx,
+                                 int32_t* pair_tet, const int32_t* w_off, int32_t* p_moff,
+                                 int64_t n_pairs) {
   if (n == 0) {
     if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
     return cudaSuccess;
