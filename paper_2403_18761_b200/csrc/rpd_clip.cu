@@ -27,20 +27,26 @@
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
+#ifndef RPD_CLIP_MINB
+#define RPD_CLIP_MINB 3  // min resident 256-thread blocks per SM for the fast kernel
+#endif
+
 namespace rpd {
 
 template <int VPL>
 struct WarpState {
   static constexpr int MAXV = 32 * VPL;
   static constexpr int MAXP = 32 * VPL;
-  double g[MAXP][4];   // barycentric plane vectors (exact integers)
-  double K[2][MAXV][4];
-  double F[2][MAXV];
-  double x[MAXV][3];   // final vertex coordinates (lattice units, relative to V0)
-  unsigned tri[2][MAXV];
-  int src[MAXP];       // radical: sphere j; tet face k: -1-k
-  int eidx[MAXP];      // CSR entry of a radical plane, -1 for faces
-  int ref[MAXP];       // reference vertex of every facet (fan apex)
+  double g[MAXP][4];       // barycentric plane vectors (exact integers)
+  double K[2][MAXV][4];    // homogeneous vertices (double-buffered vertex table)
+  double F[2][MAXV];       // error scalars
+  double x[MAXV][3];       // final vertex coordinates (lattice units, relative to V0)
+  double V[4][3];          // tet corners (lattice units)
+  unsigned tri[2][MAXV];   // oriented plane triplet of every vertex (3 x 8 bits)
+  unsigned pm[2][MAXV][VPL];  // plane bitmask of every vertex (3 bits set)
+  int src[MAXP];           // radical: sphere j; tet face k: -1-k
+  int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
+  int ref[MAXP];           // reference vertex of every facet (fan apex)
 };
 
 // oriented dual triangles of the 4 tet corners (corner k = faces != k); this orientation
@@ -57,10 +63,26 @@ __device__ __forceinline__ unsigned tri_pack(int a, int b, int c) {
   return (unsigned)a | ((unsigned)b << 8) | ((unsigned)c << 16);
 }
 
-// vertex u != self of the current table containing planes a and b (-1 if none)
-__device__ inline int find_edge_nb(const unsigned* tri, int nv, int self, int a, int b) {
+template <int VPL>
+__device__ __forceinline__ void pm_set(unsigned (&m)[VPL], unsigned tr) {
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) m[k] = 0u;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int p = tri_at(tr, r);
+    m[p >> 5] |= 1u << (p & 31);
+  }
+}
+
+// vertex u != self of the current table whose planes include a and b (-1 if none): the
+// other end of the polytope edge a n b
+template <int VPL>
+__device__ __forceinline__ int find_nb(const unsigned (*pm)[VPL], int nv, int self, int a,
+                                       int b) {
+  const int wa = a >> 5, wb = b >> 5;
+  const unsigned ba = 1u << (a & 31), bb = 1u << (b & 31);
   for (int u = 0; u < nv; ++u)
-    if (u != self && tri_has(tri[u], a) && tri_has(tri[u], b)) return u;
+    if (u != self && (pm[u][wa] & ba) && (pm[u][wb] & bb)) return u;
   return -1;
 }
 
@@ -118,6 +140,54 @@ __device__ inline void make_xplane(const WarpState<VPL>& S, const ClipCtx& C, in
   }
 }
 
+// ---- exact slow paths (out of line, so their int128 state does not weigh on the kernel)
+
+// SoS sign of the plane s (table id sid, or a new plane given by its vector, CSR entry and
+// rank when sid < 0) at the vertex with planes tr
+template <int VPL>
+__device__ __noinline__ int exact_sign(const WarpState<VPL>& S, const ClipCtx& C, unsigned tr,
+                                       int sid, const double* s, int es, int rank,
+                                       int* zero_hit) {
+  XPlane xa, xb, xc, xs;
+  make_xplane(S, C, tri_at(tr, 0), &xa);
+  make_xplane(S, C, tri_at(tr, 1), &xb);
+  make_xplane(S, C, tri_at(tr, 2), &xc);
+  if (sid >= 0) {
+    make_xplane(S, C, sid, &xs);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xs.a[q] = (long long)s[q];
+    const double4 pl = C.planes[es];
+    xs.n[0] = (long long)pl.x;
+    xs.n[1] = (long long)pl.y;
+    xs.n[2] = (long long)pl.z;
+    xs.radical = 1;
+    xs.rank = rank;
+  }
+  return sos_sign_exact(xa, xb, xc, xs, zero_hit);
+}
+
+template <int VPL>
+__device__ __noinline__ bool exact_is_zero(const WarpState<VPL>& S, const ClipCtx& C,
+                                           unsigned tr, int q) {
+  XPlane xa, xb, xc, xq;
+  make_xplane(S, C, tri_at(tr, 0), &xa);
+  make_xplane(S, C, tri_at(tr, 1), &xb);
+  make_xplane(S, C, tri_at(tr, 2), &xc);
+  make_xplane(S, C, q, &xq);
+  return det4_is_zero(xa, xb, xc, xq);
+}
+
+template <int VPL>
+__device__ __noinline__ void exact_vertex_of(const WarpState<VPL>& S, const ClipCtx& C, int a,
+                                             int b, int c, double* K) {
+  XPlane pa, pb, pc;
+  make_xplane(S, C, a, &pa);
+  make_xplane(S, C, b, &pb);
+  make_xplane(S, C, c, &pc);
+  exact_vertex(pa, pb, pc, K);
+}
+
 // fp64 homogeneous vertex of planes (a, b, c), normalised to sum(K) > 0, with the error
 // scalar F such that |g . K~ - g . K| <= |g|_1 F for every plane vector g.
 template <int VPL>
@@ -150,11 +220,7 @@ __device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx
   // certify sign(sum K) = sign(D3)
   double sb = (4.0 * E + 4.0 * U * sabs) * (1.0 + 1e-9);
   if (!(fabs(sum) > sb)) {
-    XPlane pa, pb, pc;
-    make_xplane(S, C, a, &pa);
-    make_xplane(S, C, b, &pb);
-    make_xplane(S, C, c, &pc);
-    exact_vertex(pa, pb, pc, K);  // normalised, each component within 2^-52 relative
+    exact_vertex_of(S, C, a, b, c, K);  // normalised, each component within 2^-52 relative
     ++*nexact;
     double km = fmax(fmax(fabs(K[0]), fabs(K[1])), fmax(fabs(K[2]), fabs(K[3])));
     *F = 9.0 * U * km * (1.0 + 1e-9);
@@ -181,7 +247,7 @@ struct PairOut {
 };
 
 template <int VPL>
-__global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
+__global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB : 1) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
     const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ nbr_off,
@@ -201,7 +267,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
-  // algorithmic work (lane 0 counts; warp-uniform quantities)
+  // algorithmic work (warp-uniform quantities, counted once per warp)
   long long c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;
 
   for (int64_t pi = gw; pi < n_pairs; pi += nw) {
@@ -209,12 +275,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
     const int64_t a = pair_tet[p];
     const int64_t t = tet_ids ? (int64_t)tet_ids[a] : a;
     const int i = cand_idx[p];
-    double V[4][3];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) V[k][c] = __ldg(tx + (3 * k + c) * T + t);
-
+    if (lane < 12) (&S.V[0][0])[lane] = __ldg(tx + lane * T + t);
     if (lane < 4) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -225,6 +286,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
       S.eidx[lane] = -1;
       S.F[0][lane] = 0.0;
       S.tri[0][lane] = CORNER_TRI[lane];
+      pm_set<VPL>(S.pm[0][lane], CORNER_TRI[lane]);
     }
     __syncwarp();
     int np = 4, nv = 4, cur = 0, status = ST_ALIVE, zero_hit = 0;
@@ -237,12 +299,12 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
       double g[4] = {0.0, 0.0, 0.0, 0.0};
       bool allpos = false, allneg = false;
       if (have) {
-        double4 pl = planes[e];
+        const double4 pl = planes[e];
         allpos = true;
         allneg = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          g[k] = fma(pl.x, V[k][0], fma(pl.y, V[k][1], fma(pl.z, V[k][2], pl.w)));
+          g[k] = fma(pl.x, S.V[k][0], fma(pl.y, S.V[k][1], fma(pl.z, S.V[k][2], pl.w)));
           allpos &= g[k] > 0.0;
           allneg &= g[k] < 0.0;
         }
@@ -272,26 +334,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
           sg[k] = 0;
           if (valid) {
             const double* K = S.K[cur][v];
-            double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
-            double B = sabs * S.F[cur][v];
+            const double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
+            const double B = sabs * S.F[cur][v];
             if (val > B) sg[k] = 1;
             else if (val < -B) sg[k] = -1;
             else {
-              XPlane xa, xb, xc, xs;
-              unsigned tr = S.tri[cur][v];
-              make_xplane(S, C, tri_at(tr, 0), &xa);
-              make_xplane(S, C, tri_at(tr, 1), &xb);
-              make_xplane(S, C, tri_at(tr, 2), &xc);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) xs.a[q] = (long long)s[q];
-              double4 pl = planes[es];
-              xs.n[0] = (long long)pl.x;
-              xs.n[1] = (long long)pl.y;
-              xs.n[2] = (long long)pl.z;
-              xs.radical = 1;
-              xs.rank = nbr_idx[es];
               int zh = 0;
-              sg[k] = sos_sign_exact(xa, xb, xc, xs, &zh);
+              sg[k] = exact_sign(S, C, S.tri[cur][v], -1, s, es, nbr_idx[es], &zh);
               ++n_exact;
               if (zh) {
                 ++n_zero;
@@ -312,9 +361,10 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
             int v = 32 * k + lane;
             if (v < nv) {
               unsigned tr = S.tri[cur][v];
-              printf("plane j=%d es=%d v=%d tri=(%d,%d,%d) sg=%d K=(%g,%g,%g,%g) F=%g\n", nbr_idx[es], es, v,
-                     tri_at(tr,0), tri_at(tr,1), tri_at(tr,2), sg[k], S.K[cur][v][0], S.K[cur][v][1],
-                     S.K[cur][v][2], S.K[cur][v][3], S.F[cur][v]);
+              printf("plane j=%d es=%d v=%d tri=(%d,%d,%d) sg=%d K=(%g,%g,%g,%g) F=%g\n",
+                     nbr_idx[es], es, v, tri_at(tr, 0), tri_at(tr, 1), tri_at(tr, 2), sg[k],
+                     S.K[cur][v][0], S.K[cur][v][1], S.K[cur][v][2], S.K[cur][v][3],
+                     S.F[cur][v]);
             }
           }
         }
@@ -345,11 +395,11 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
           const int v = 32 * k + lane;
           nnew[k] = 0;
           if (v < nv && sg[k] < 0) {
-            unsigned tr = S.tri[cur][v];
+            const unsigned tr = S.tri[cur][v];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
-              int u = find_edge_nb(S.tri[cur], nv, v, x, y);
+              const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
+              const int u = find_nb<VPL>(S.pm[cur], nv, v, x, y);
               if (u >= 0 && ((posm[u >> 5] >> (u & 31)) & 1u))
                 newtri[k][nnew[k]++] = tri_pack(x, y, sid);
             }
@@ -365,7 +415,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
           int incl = nnew[k];
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(FULL, incl, o);
+            const int y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
           }
           new_idx[k] = new_base + incl - nnew[k];
@@ -387,6 +437,8 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
             for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = S.K[cur][v][m];
             S.F[nxt][q] = S.F[cur][v];
             S.tri[nxt][q] = S.tri[cur][v];
+#pragma unroll
+            for (int w = 0; w < VPL; ++w) S.pm[nxt][q][w] = S.pm[cur][v][w];
           }
           for (int j = 0; j < nnew[k]; ++j) {
             const int q = nkept + new_idx[k] + j;
@@ -398,6 +450,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
             for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
             S.F[nxt][q] = F;
             S.tri[nxt][q] = tr;
+            pm_set<VPL>(S.pm[nxt][q], tr);
           }
         }
         c_constr += new_base;
@@ -412,7 +465,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
       if (status == ST_OVER) {
         ++n_over;
         if (lane == 0 && out.over_list) {
-          int slot = atomicAdd(out.over_count, 1);
+          const int slot = atomicAdd(out.over_count, 1);
           out.over_list[slot] = (int32_t)p;
         }
       }
@@ -459,17 +512,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
             if (v < nv && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
               const double* K = S.K[cur][v];
               const double* gq = S.g[q];
-              double val = fma(gq[0], K[0], fma(gq[1], K[1], fma(gq[2], K[2], gq[3] * K[3])));
-              double sa = fabs(gq[0]) + fabs(gq[1]) + fabs(gq[2]) + fabs(gq[3]);
+              const double val =
+                  fma(gq[0], K[0], fma(gq[1], K[1], fma(gq[2], K[2], gq[3] * K[3])));
+              const double sa = fabs(gq[0]) + fabs(gq[1]) + fabs(gq[2]) + fabs(gq[3]);
               if (fabs(val) > sa * S.F[cur][v]) {
                 on = false;
               } else {
-                XPlane xa, xb, xc, xq;
-                make_xplane(S, C, tri_at(mytri[k], 0), &xa);
-                make_xplane(S, C, tri_at(mytri[k], 1), &xb);
-                make_xplane(S, C, tri_at(mytri[k], 2), &xc);
-                make_xplane(S, C, q, &xq);
-                on = on && det4_is_zero(xa, xb, xc, xq);
+                on = on && exact_is_zero(S, C, mytri[k], q);
                 ++n_exact;
               }
             }
@@ -486,6 +535,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int pl = 32 * k + lane;
+      if (pl < np) S.ref[pl] = 0x7fffffff;
       if (pl < np && facets.has(pl)) {
         const int src = S.src[pl];
         if (src < 0) {
@@ -509,8 +559,10 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
       }
     }
     const unsigned facemask = __reduce_or_sync(FULL, fmask_bits);
+    __syncwarp();
 
-    // ---- geometry: vertex coordinates relative to V0 (lattice units)
+    // ---- geometry: vertex coordinates relative to V0 (lattice units); facet fan apex =
+    // lowest vertex of the facet
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int v = 32 * k + lane;
@@ -520,31 +572,22 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
         for (int m = 0; m < 4; ++m) K[m] = S.K[cur][v][m];
         double sum = K[0] + K[1] + K[2] + K[3];
         if (16.0 * S.F[cur][v] > 1e-12 * sum) {
-          XPlane xa, xb, xc;
-          make_xplane(S, C, tri_at(mytri[k], 0), &xa);
-          make_xplane(S, C, tri_at(mytri[k], 1), &xb);
-          make_xplane(S, C, tri_at(mytri[k], 2), &xc);
-          exact_vertex(xa, xb, xc, K);
+          exact_vertex_of(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1), tri_at(mytri[k], 2),
+                          K);
           sum = K[0] + K[1] + K[2] + K[3];
           ++n_exact;
         }
+        const double inv = 1.0 / sum;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           double acc = 0.0;
 #pragma unroll
-          for (int q = 1; q < 4; ++q) acc = fma(K[q] / sum, V[q][c] - V[0][c], acc);
+          for (int q = 1; q < 4; ++q) acc = fma(K[q] * inv, S.V[q][c] - S.V[0][c], acc);
           S.x[v][c] = acc;
         }
-      }
-    }
-    for (int f = facets_all.next(0); f >= 0; f = facets_all.next(f + 1)) {
-      int first = -1;
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        unsigned on = __ballot_sync(FULL, 32 * k + lane < nv && tri_has(mytri[k], f));
-        if (first < 0 && on) first = 32 * k + __ffs(on) - 1;
+        for (int r = 0; r < 3; ++r) atomicMin(&S.ref[tri_at(mytri[k], r)], v);
       }
-      if (lane == 0) S.ref[f] = first;
     }
     __syncwarp();
     double vol6 = 0.0, m24[3] = {0.0, 0.0, 0.0};
@@ -557,13 +600,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
         for (int r = 0; r < 3; ++r) {
           const int f = tri_at(mytri[k], r);
           const int zc = tri_at(mytri[k], (r + 2) % 3);
-          const int w = find_edge_nb(S.tri[cur], nv, v, zc, f);
+          const int w = find_nb<VPL>(S.pm[cur], nv, v, zc, f);
           if (w < 0) continue;  // unreachable for a valid polytope
           const double* xr = S.x[S.ref[f]];
           const double* xw = S.x[w];
-          double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -
-                       xr[1] * (xv[0] * xw[2] - xv[2] * xw[0]) +
-                       xr[2] * (xv[0] * xw[1] - xv[1] * xw[0]);
+          const double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -
+                             xr[1] * (xv[0] * xw[2] - xv[2] * xw[0]) +
+                             xr[2] * (xv[0] * xw[1] - xv[1] * xw[0]);
           vol6 += det;
 #pragma unroll
           for (int c = 0; c < 3; ++c) m24[c] += det * (xr[c] + xv[c] + xw[c]);
@@ -582,7 +625,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64) k_clip(
       out.vol[p] = vol;
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        out.m1[3 * p + c] = (m24[c] / 24.0) * (L * L * L * L) + vol * (V[0][c] * L);
+        out.m1[3 * p + c] = (m24[c] / 24.0) * (L * L * L * L) + vol * (S.V[0][c] * L);
       out.flag[p] = 1;
       out.fm[p] = (uint8_t)facemask;
     }
