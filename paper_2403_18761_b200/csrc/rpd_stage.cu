@@ -95,62 +95,70 @@ __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
   sw[i] = make_double4(S[0], S[1], S[2], W);
 }
 
-// One thread per sphere row: copy + insertion sort + validation + planes + twins.
+// One warp per sphere row: validation, rank sort (ascending neighbour id), radical planes
+// and twins.  The sort and the twin search are O(k^2 / 32) per row (k = k_site <= ~1000).
 __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin, int* err) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= N) return;
-  int32_t e0 = off_in[i], e1 = off_in[i + 1];
-  off_out[i] = e0;
-  if (i == N - 1) off_out[N] = e1;
+  const int32_t e0 = off_in[i], e1 = off_in[i + 1];
+  if (lane == 0) {
+    off_out[i] = e0;
+    if (i == N - 1) off_out[N] = e1;
+  }
   if (e0 < 0 || e1 < e0 || e1 > E || (i == 0 && e0 != 0) || (i == N - 1 && e1 != E)) {
-    report(err, RPD_EINVAL, ERR_NBR_OFF, i);
+    if (lane == 0) report(err, RPD_EINVAL, ERR_NBR_OFF, i);
     return;
   }
-  for (int32_t e = e0; e < e1; ++e) {
-    int32_t j = idx_in[e];
+  bool bad = false;
+  for (int32_t e = e0 + lane; e < e1; e += 32) {
+    const int32_t j = idx_in[e];
     if (j < 0 || j >= N) {
       report(err, RPD_EINVAL, ERR_NBR_INDEX, i);
-      return;
+      bad = true;
+      break;
     }
     if (j == i) {
       report(err, RPD_EINVAL, ERR_NBR_SELF, i);
-      return;
+      bad = true;
+      break;
     }
-    // insertion into the sorted prefix
-    int32_t q = e;
-    while (q > e0 && idx_out[q - 1] > j) {
-      idx_out[q] = idx_out[q - 1];
-      --q;
+    int rank = 0;
+    for (int32_t f = e0; f < e1; ++f) {
+      const int32_t x = idx_in[f];
+      if (x == j && f != e) {
+        report(err, RPD_EINVAL, ERR_NBR_DUP, i);
+        bad = true;
+      }
+      rank += x < j;
     }
-    idx_out[q] = j;
+    if (bad) break;
+    idx_out[e0 + rank] = j;
   }
-  double4 si = sw[i];
-  for (int32_t e = e0; e < e1; ++e) {
-    int32_t j = idx_out[e];
-    if (e > e0 && idx_out[e - 1] == j) {
-      report(err, RPD_EINVAL, ERR_NBR_DUP, i);
-      return;
-    }
-    double4 sj = sw[j];
-    double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
-    if (nx == 0.0 && ny == 0.0 && nz == 0.0) {
-      report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
-      return;
-    }
+  if (__any_sync(0xffffffffu, bad)) return;
+  __syncwarp();
+  const double4 si = sw[i];
+  for (int32_t e = e0 + lane; e < e1; e += 32) {
+    const int32_t j = idx_out[e];
+    const double4 sj = sw[j];
+    const double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
+    if (nx == 0.0 && ny == 0.0 && nz == 0.0) report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
     planes[e] = make_double4(nx, ny, nz, sj.w - si.w);
   }
+  __syncwarp();
   // twins: next entry of the row with the same oriented plane (exact: products < 2^53)
-  for (int32_t e = e0; e < e1; ++e) {
-    double4 a = planes[e];
+  for (int32_t e = e0 + lane; e < e1; e += 32) {
+    const double4 a = planes[e];
     int32_t tw = -1;
     for (int32_t f = e + 1; f < e1 && tw < 0; ++f) {
-      double4 b = planes[f];
-      bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x && a.y * b.z == a.z * b.y &&
-                  a.x * b.w == a.w * b.x && a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
-      double dot = a.x * b.x + a.y * b.y + a.z * b.z;
+      const double4 b = planes[f];
+      const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
+                        a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
+                        a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
+      const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
       if (prop && dot > 0.0) tw = f;
     }
     twin[e] = tw;
@@ -193,7 +201,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if (N > 0) {
     k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(spheres, N, s.sw.as<double4>(), err);
     ++c->launches;
-    k_stage_rows<<<nblk(N, 128), 128, 0, c->stream>>>(
+    k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(), err);
     ++c->launches;
