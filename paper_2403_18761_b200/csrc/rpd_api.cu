@@ -135,7 +135,7 @@ void rpd_destroy(rpd_ctx* c) {
   DevBuf* bufs[] = {&c->h_verts, &c->h_tets, &c->h_spheres, &c->h_off, &c->h_idx, &c->h_new,
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
                     &c->st.twin, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
-                    &c->slab, &c->w_off, &c->bvh, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
+                    &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off};
   for (DevBuf* b : bufs) b->release();
@@ -240,7 +240,7 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   CK(c->k_words.ensure(sizeof(int32_t) * nt), "alloc");
   CK(cs.off.ensure(sizeof(int32_t) * (n_tets + 1)), "alloc");
   CK(c->w_off.ensure(sizeof(int32_t) * (n_tets + 1)), "alloc");
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  for (int attempt = 0; attempt < 3; ++attempt) {
     const int cap = c->slab_cap;
     CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * nt), "alloc slab");
     // ST_MAXK, ST_TESTED, ST_REL_TESTS
@@ -260,14 +260,28 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                        cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
        "readback");
+    rb->i32[2] = 0;
+    if (c->filter_mode == RPD_FILTER_PRUNED && hi > lo && n_tets > 0)
+      CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                         c->stream), "readback");
     CK(cudaStreamSynchronize(c->stream), "filter");
     rpd_status s = check_err(c, rb);
     if (s) return s;
+    bool retry = false;
+    if (rb->i32[2] > c->bvh_cap_items) {  // work queue overflow: grow and redo
+      c->bvh_min_items = (int64_t)rb->i32[2] + 1024;
+      retry = true;
+    }
     const int maxk = (int)rb->u64[ST_MAXK];
-    if (maxk <= cap) break;
-    int nc = 32;
-    while (nc < maxk) nc *= 2;
-    c->slab_cap = nc;
+    if (maxk > cap) {
+      int ncap = 32;
+      while (ncap < maxk) ncap *= 2;
+      c->slab_cap = ncap;
+      retry = true;
+    }
+    if (!retry) break;
+    if (attempt == 2) return fail(c, RPD_EOVERFLOW, "filter capacity");
+    continue;
   }
   const int64_t nc = rb->i32[0];
   cs.n = nc;
@@ -490,7 +504,21 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
      "readback");
   CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                      cudaMemcpyDeviceToHost, c->stream), "readback");
+  rb->i32[2] = 0;
+  if (c->filter_mode == RPD_FILTER_PRUNED && T > 0)
+    CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream), "readback");
   CK(cudaStreamSynchronize(c->stream), "dirty");
+  if (rb->i32[2] > c->bvh_cap_items) {
+    // work queue overflow (never seen): grow it and redo the dirty detection
+    c->bvh_min_items = (int64_t)rb->i32[2] + 1024;
+    CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(),
+                     nullptr, nullptr), "dirty filter");
+    CK(launch_dirty_list(c, T), "dirty list");
+    CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(cudaStreamSynchronize(c->stream), "dirty");
+  }
   if (rb->err[0] != 0) {
     if (rb->err[1] == 100) return fail(c, RPD_EINVAL, "new_ids is not the appended id range");
     return check_err(c, rb);

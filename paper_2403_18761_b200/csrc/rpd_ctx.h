@@ -116,6 +116,8 @@ struct rpd_ctx {
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
+  rpd::DevBuf bvh_items;   // (sphere, super node) work queue of the pruned filter
+  int64_t bvh_cap_items = 0, bvh_min_items = 0;
   int slab_cap = 32;
 
   // current candidates / pieces (double-buffered for partial updates) and the dirty sets

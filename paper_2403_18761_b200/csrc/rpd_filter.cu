@@ -177,17 +177,16 @@ __device__ __forceinline__ bool box_passes(const double* __restrict__ B,
 
 constexpr int BVH_WARPS = 4;
 
-__global__ void __launch_bounds__(BVH_WARPS * 32) k_filter_bvh(
-    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
-    const double* __restrict__ leaf, int64_t n_leaf, const double* __restrict__ sup,
-    int64_t n_sup, const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes,
-    int N, int lo, int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-    int32_t* __restrict__ k_words, unsigned long long* __restrict__ stats) {
+// phase 1: one warp per sphere tests the super-node boxes and queues (sphere, super node)
+// work items (a sphere with a huge cell becomes many items: load balance)
+__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
+    const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
+    const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
+    int cap_items, int* __restrict__ n_items) {
   __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   double4* sp = s_pl[warp];
-  long long ntests = 0, npairs = 0;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t ii = lo + gw; ii < hi; ii += nw) {
@@ -199,50 +198,88 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_filter_bvh(
     __syncwarp();
     for (int e = lane; e < k && e < BVH_PCAP; e += 32) sp[e] = gp[e];
     __syncwarp();
-    const int words = (k + 31) >> 5;
     for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
       const int64_t s = s0 + lane;
-      unsigned sm = __ballot_sync(FULL, s < n_sup && box_passes(sup + 6 * s, sp, k, gp));
-      while (sm) {
-        const int64_t sl = s0 + __ffs(sm) - 1;
-        sm &= sm - 1;
-        const int64_t l = sl * BVH_FAN + lane;
-        unsigned lm = __ballot_sync(FULL, l < n_leaf && box_passes(leaf + 6 * l, sp, k, gp));
-        while (lm) {
-          const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
-          lm &= lm - 1;
-          // exact Alg. 1, lane = tet
-          const int64_t a = ll * BVH_LEAF + lane;
-          const bool valid = a < n;
-          const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
-          double X[4], Y[4], Z[4];
+      const bool ok = s < n_sup && box_passes(sup + 6 * s, sp, k, gp);
+      const unsigned sm = __ballot_sync(FULL, ok);
+      if (!sm) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(n_items, __popc(sm));
+      base = __shfl_sync(FULL, base, 0);
+      if (ok) {
+        const int slot = base + __popc(sm & ((1u << lane) - 1u));
+        if (slot < cap_items) items[slot] = make_int2(i, (int)s);
+      }
+    }
+  }
+}
+
+// phase 2: one warp per (sphere, super node) item: leaf boxes, then the exact Alg. 1
+// (lane = tet) on the surviving leaves
+__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
+    const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
+    const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
+    const double4* __restrict__ planes, const int2* __restrict__ items,
+    const int* __restrict__ n_items_p, int cap_items, int cap, int32_t* __restrict__ k_tet,
+    int32_t* __restrict__ slab, int32_t* __restrict__ k_words,
+    unsigned long long* __restrict__ stats) {
+  __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  double4* sp = s_pl[warp];
+  long long ntests = 0, npairs = 0;
+  const int n_items = min(*n_items_p, cap_items);
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int cur_i = -1;
+  for (int64_t it = gw; it < n_items; it += nw) {
+    const int2 item = items[it];
+    const int i = item.x;
+    const int64_t sl = item.y;
+    const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+    const int k = e1 - e0;
+    const double4* gp = planes + e0;
+    if (i != cur_i) {
+      __syncwarp();
+      for (int e = lane; e < k && e < BVH_PCAP; e += 32) sp[e] = gp[e];
+      __syncwarp();
+      cur_i = i;
+    }
+    const int words = (k + 31) >> 5;
+    const int64_t l = sl * BVH_FAN + lane;
+    unsigned lm = __ballot_sync(FULL, l < n_leaf && box_passes(leaf + 6 * l, sp, k, gp));
+    while (lm) {
+      const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int64_t a = ll * BVH_LEAF + lane;
+      const bool valid = a < n;
+      const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
+      double X[4], Y[4], Z[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            X[q] = valid ? tx[(3 * q + 0) * T + t] : 0.0;
-            Y[q] = valid ? tx[(3 * q + 1) * T + t] : 0.0;
-            Z[q] = valid ? tx[(3 * q + 2) * T + t] : 0.0;
-          }
-          bool alive = valid;
-          for (int e = 0; e < k; ++e) {
-            const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
-            bool hk[4];
+      for (int q = 0; q < 4; ++q) {
+        X[q] = valid ? tx[(3 * q + 0) * T + t] : 0.0;
+        Y[q] = valid ? tx[(3 * q + 1) * T + t] : 0.0;
+        Z[q] = valid ? tx[(3 * q + 2) * T + t] : 0.0;
+      }
+      bool alive = valid;
+      for (int e = 0; e < k; ++e) {
+        const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
+        bool hk[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double h = fma(p.x, X[q], fma(p.y, Y[q], fma(p.z, Z[q], p.w)));
-              hk[q] = pos(h);
-            }
-            const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
-            if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
-            alive = alive && hit;
-            if (!__any_sync(FULL, alive)) break;
-          }
-          npairs += valid;
-          if (alive) {
-            const int slot = atomicAdd(k_tet + a, 1);
-            if (slot < cap) slab[a * cap + slot] = i;
-            if (k_words) atomicAdd(k_words + a, words);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const double h = fma(p.x, X[q], fma(p.y, Y[q], fma(p.z, Z[q], p.w)));
+          hk[q] = pos(h);
         }
+        const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+        if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
+        alive = alive && hit;
+        if (!__any_sync(FULL, alive)) break;
+      }
+      npairs += valid;
+      if (alive) {
+        const int slot = atomicAdd(k_tet + a, 1);
+        if (slot < cap) slab[a * cap + slot] = i;
+        if (k_words) atomicAdd(k_words + a, words);
       }
     }
   }
@@ -325,14 +362,27 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
     if (ns > 0) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      // work-item queue: [0] = count, then int2 items
+      int64_t cap_items = 8 * ns + 4 * n_sup + 1024;
+      if (cap_items < c->bvh_min_items) cap_items = c->bvh_min_items;
+      if (cap_items > (1 << 30)) cap_items = 1 << 30;
+      e = c->bvh_items.ensure(sizeof(int2) * (cap_items + 1));
+      if (e) return e;
+      int* n_items = c->bvh_items.as<int>();
+      int2* items = reinterpret_cast<int2*>(c->bvh_items.as<char>() + sizeof(int2));
+      e = cudaMemsetAsync(n_items, 0, sizeof(int), c->stream);
+      if (e) return e;
       int64_t blocks = (ns + BVH_WARPS - 1) / BVH_WARPS;
-      const int64_t maxb = (int64_t)sms * 16;
-      if (blocks > maxb) blocks = maxb;
-      k_filter_bvh<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
-          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf, sup, n_sup,
-          c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N, sphere_lo,
-          sphere_hi, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
-      ++c->launches;
+      if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+      k_bvh_super<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
+          sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
+          sphere_lo, sphere_hi, items, (int)cap_items, n_items);
+      k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
+          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
+          c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,
+          (int)cap_items, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
+      c->launches += 2;
+      c->bvh_cap_items = cap_items;
     }
     k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
                                                         c->stats.as<unsigned long long>());
