@@ -134,7 +134,7 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->h_verts, &c->h_tets, &c->h_spheres, &c->h_off, &c->h_idx, &c->h_new,
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
-                    &c->st.twin, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
+                    &c->st.twin, &c->st.hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off};

@@ -75,6 +75,7 @@ struct Stage {
   DevBuf nbr_idx;  // int32 [E], rows sorted ascending
   DevBuf planes;   // double4 per CSR entry: (n, d) of h_ij
   DevBuf twin;     // int32 per CSR entry: next entry of the row with the same oriented plane
+  DevBuf hkey;     // uint64 per CSR entry: hash of the canonical plane (twin search)
   int64_t T = 0, N = 0, V = 0, E = 0;
 };
 

@@ -261,18 +261,36 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
         Y[q] = valid ? tx[(3 * q + 1) * T + t] : 0.0;
         Z[q] = valid ? tx[(3 * q + 2) * T + t] : 0.0;
       }
+      // planes with min over the leaf box > 0 hold at every vertex of every tet of the leaf;
+      // only the planes crossing the box are tested per tet
+      const double* B = leaf + 6 * ll;
+      const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
       bool alive = valid;
-      for (int e = 0; e < k; ++e) {
-        const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
-        bool hk[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double h = fma(p.x, X[q], fma(p.y, Y[q], fma(p.z, Z[q], p.w)));
-          hk[q] = pos(h);
+      for (int c0 = 0; c0 < k; c0 += 32) {
+        const int ec = c0 + lane;
+        bool crosses = false;
+        if (ec < k) {
+          const double4 p = ec < BVH_PCAP ? sp[ec] : gp[ec];
+          const double mn = p.w + fmin(p.x * l0, p.x * h0) + fmin(p.y * l1, p.y * h1) +
+                            fmin(p.z * l2, p.z * h2);
+          crosses = !pos(mn);
         }
-        const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
-        if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
-        alive = alive && hit;
+        unsigned cm = __ballot_sync(FULL, crosses);
+        while (cm) {
+          const int e = c0 + __ffs(cm) - 1;
+          cm &= cm - 1;
+          const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
+          bool hk[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double h = fma(p.x, X[q], fma(p.y, Y[q], fma(p.z, Z[q], p.w)));
+            hk[q] = pos(h);
+          }
+          const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+          if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
+          alive = alive && hit;
+          if (!__any_sync(FULL, alive)) break;
+        }
         if (!__any_sync(FULL, alive)) break;
       }
       npairs += valid;

@@ -100,7 +100,8 @@ __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
 __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
-                             double4* __restrict__ planes, int32_t* __restrict__ twin, int* err) {
+                             double4* __restrict__ planes, int32_t* __restrict__ twin,
+                             unsigned long long* __restrict__ hkey, int* err) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
@@ -149,12 +150,35 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     planes[e] = make_double4(nx, ny, nz, sj.w - si.w);
   }
   __syncwarp();
-  // twins: next entry of the row with the same oriented plane (exact: products < 2^53)
+  // twins: next entry of the row with the same oriented plane.  Canonical form (n, d) / gcd
+  // hashed to 64 bits; only equal hashes are compared exactly (products < 2^53).
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const double4 a = planes[e];
+    long long q[4] = {(long long)a.x, (long long)a.y, (long long)a.z, (long long)a.w};
+    unsigned long long g = 0;
+    for (int c = 0; c < 4; ++c) {
+      unsigned long long x = (unsigned long long)(q[c] < 0 ? -q[c] : q[c]);
+      while (x) {
+        const unsigned long long r = g % x;
+        g = x;
+        x = r;
+      }
+    }
+    if (g == 0) g = 1;
+    unsigned long long h = 1469598103934665603ull;
+    for (int c = 0; c < 4; ++c) {
+      h ^= (unsigned long long)(q[c] / (long long)g);
+      h *= 1099511628211ull;
+    }
+    hkey[e] = h;
+  }
+  __syncwarp();
+  for (int32_t e = e0 + lane; e < e1; e += 32) {
+    const unsigned long long h = hkey[e];
     int32_t tw = -1;
     for (int32_t f = e + 1; f < e1 && tw < 0; ++f) {
-      const double4 b = planes[f];
+      if (hkey[f] != h) continue;
+      const double4 a = planes[e], b = planes[f];
       const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
                         a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
                         a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
@@ -195,6 +219,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
   if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
   s.N = N;
   s.E = E;
   int* err = c->errw.as<int>();
@@ -203,7 +228,8 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
     ++c->launches;
     k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
-        s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(), err);
+        s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
+        s.hkey.as<unsigned long long>(), err);
     ++c->launches;
   } else {
     e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
