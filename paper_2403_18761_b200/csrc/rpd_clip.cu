@@ -42,8 +42,11 @@ struct WarpState {
   double F[2][MAXV];       // error scalars
   double x[MAXV][3];       // final vertex coordinates (lattice units, relative to V0)
   double V[4][3];          // tet corners (lattice units)
+  double val[MAXV];        // plane value g_s . K of every vertex in the current sign pass
   unsigned tri[2][MAXV];   // oriented plane triplet of every vertex (3 x 8 bits)
-  unsigned pm[2][MAXV][VPL];  // plane bitmask of every vertex (3 bits set)
+  unsigned char nb[2][MAXV][4];  // vertex across edge r = (tri[r], tri[r+1]) of the dual
+  unsigned char vx[MAXV];  // 1 if the current sign was decided by the exact path
+  unsigned char map[MAXV]; // old slot -> new slot of the kept vertices
   int src[MAXP];           // radical: sphere j; tet face k: -1-k
   int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
   int ref[MAXP];           // reference vertex of every facet (fan apex)
@@ -63,28 +66,8 @@ __device__ __forceinline__ unsigned tri_pack(int a, int b, int c) {
   return (unsigned)a | ((unsigned)b << 8) | ((unsigned)c << 16);
 }
 
-template <int VPL>
-__device__ __forceinline__ void pm_set(unsigned (&m)[VPL], unsigned tr) {
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) m[k] = 0u;
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    const int p = tri_at(tr, r);
-    m[p >> 5] |= 1u << (p & 31);
-  }
-}
-
-// vertex u != self of the current table whose planes include a and b (-1 if none): the
-// other end of the polytope edge a n b
-template <int VPL>
-__device__ __forceinline__ int find_nb(const unsigned (*pm)[VPL], int nv, int self, int a,
-                                       int b) {
-  const int wa = a >> 5, wb = b >> 5;
-  const unsigned ba = 1u << (a & 31), bb = 1u << (b & 31);
-  for (int u = 0; u < nv; ++u)
-    if (u != self && (pm[u][wa] & ba) && (pm[u][wb] & bb)) return u;
-  return -1;
-}
+// neighbours of the 4 tet corners across their dual edges (CORNER_TRI orientation)
+__constant__ unsigned char CORNER_NB[4][3] = {{2, 1, 3}, {3, 0, 2}, {1, 0, 3}, {2, 0, 1}};
 
 template <int W>
 struct Bits {
@@ -233,6 +216,45 @@ __device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx
   *F = (E + 5.0 * U * Kmax) * (1.0 + 1e-9);
 }
 
+// New vertex on the edge from the kept vertex u to the removed vertex v where plane s
+// vanishes: K = val_u K_v - val_v K_u (a positive combination; g_s . K = 0).  Error bound
+// from the endpoints' bounds and the plane values' bounds; rescaled by a power of two.
+// Falls back to the exact-cofactor construction from the three planes when an endpoint's
+// sign came from the exact path or the bound is too loose.
+template <int VPL>
+__device__ inline void new_vertex(const WarpState<VPL>& S, const ClipCtx& C, int cur, int u,
+                                  int v, int x, int y, int sid, double sabs, double K[4],
+                                  double* F, int* nexact) {
+  if (!S.vx[u] && !S.vx[v]) {
+    const double vu = S.val[u], avv = -S.val[v];  // vu > B_u > 0, -val_v > B_v > 0
+    const double* Ku = S.K[cur][u];
+    const double* Kv = S.K[cur][v];
+    const double Fu = S.F[cur][u], Fv = S.F[cur][v];
+    double ku = 0.0, kv = 0.0, km = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      ku = fmax(ku, fabs(Ku[m]));
+      kv = fmax(kv, fabs(Kv[m]));
+      K[m] = fma(vu, Kv[m], avv * Ku[m]);
+      km = fmax(km, fabs(K[m]));
+    }
+    const double Bu = sabs * Fu, Bv = sabs * Fv;
+    const double E = Bu * kv + (vu + Bu) * Fv + Bv * ku + (avv + Bv) * Fu +
+                     3.0 * U * (vu * kv + avv * ku);
+    const double Fn = (E + 5.0 * U * km) * (1.0 + 1e-9);
+    if (Fn <= 1e-6 * km && km > 0.0) {
+      int ex;
+      frexp(km, &ex);
+      const double sc = ldexp(1.0, -ex);  // exact power-of-two rescale
+#pragma unroll
+      for (int m = 0; m < 4; ++m) K[m] *= sc;
+      *F = Fn * sc;
+      return;
+    }
+  }
+  vertex_from_planes(S, C, x, y, sid, K, F, nexact);
+}
+
 enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
 
 struct PairOut {
@@ -286,7 +308,8 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
       S.eidx[lane] = -1;
       S.F[0][lane] = 0.0;
       S.tri[0][lane] = CORNER_TRI[lane];
-      pm_set<VPL>(S.pm[0][lane], CORNER_TRI[lane]);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) S.nb[0][lane][r] = CORNER_NB[lane][r];
     }
     __syncwarp();
     int np = 4, nv = 4, cur = 0, status = ST_ALIVE, zero_hit = 0;
@@ -336,11 +359,14 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
             const double* K = S.K[cur][v];
             const double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
             const double B = sabs * S.F[cur][v];
+            S.val[v] = val;
+            S.vx[v] = 0;
             if (val > B) sg[k] = 1;
             else if (val < -B) sg[k] = -1;
             else {
               int zh = 0;
               sg[k] = exact_sign(S, C, S.tri[cur][v], -1, s, es, nbr_idx[es], &zh);
+              S.vx[v] = 1;
               ++n_exact;
               if (zh) {
                 ++n_zero;
@@ -386,22 +412,20 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
           S.eidx[sid] = es;
         }
         __syncwarp();
-        // ---- new vertices: one per boundary edge of the conflict region, oriented as the
-        // removed triangle's edge: (x, y, s)
-        unsigned newtri[VPL][3];
+        // ---- new vertices: one per boundary edge of the conflict region (a removed vertex v
+        // with a kept neighbour u across its dual edge (x, y)), oriented as that edge:
+        // (x, y, s).  Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring
+        // new vertices around the new facet s.
         int nnew[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
           const int v = 32 * k + lane;
           nnew[k] = 0;
           if (v < nv && sg[k] < 0) {
-            const unsigned tr = S.tri[cur][v];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
-              const int u = find_nb<VPL>(S.pm[cur], nv, v, x, y);
-              if (u >= 0 && ((posm[u >> 5] >> (u & 31)) & 1u))
-                newtri[k][nnew[k]++] = tri_pack(x, y, sid);
+              const int u = S.nb[cur][v][r];
+              nnew[k] += (posm[u >> 5] >> (u & 31)) & 1u;
             }
           }
         }
@@ -431,26 +455,62 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
           const int v = 32 * k + lane;
-          if (v < nv && sg[k] > 0) {
+          if (v < nv && sg[k] > 0) S.map[v] = (unsigned char)kept_idx[k];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const int v = 32 * k + lane;
+          if (v >= nv) continue;
+          if (sg[k] > 0) {
             const int q = kept_idx[k];
 #pragma unroll
             for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = S.K[cur][v][m];
             S.F[nxt][q] = S.F[cur][v];
             S.tri[nxt][q] = S.tri[cur][v];
 #pragma unroll
-            for (int w = 0; w < VPL; ++w) S.pm[nxt][q][w] = S.pm[cur][v][w];
-          }
-          for (int j = 0; j < nnew[k]; ++j) {
-            const int q = nkept + new_idx[k] + j;
-            const unsigned tr = newtri[k][j];
-            double K[4], F;
-            vertex_from_planes(S, C, tri_at(tr, 0), tri_at(tr, 1), tri_at(tr, 2), K, &F,
-                               &n_exact);
+            for (int r = 0; r < 3; ++r) {
+              const int u = S.nb[cur][v][r];
+              if ((posm[u >> 5] >> (u & 31)) & 1u) S.nb[nxt][q][r] = S.map[u];
+            }
+          } else {
+            const unsigned tr = S.tri[cur][v];
+            int j = 0;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
-            S.F[nxt][q] = F;
-            S.tri[nxt][q] = tr;
-            pm_set<VPL>(S.pm[nxt][q], tr);
+            for (int r = 0; r < 3; ++r) {
+              const int u = S.nb[cur][v][r];
+              if (!((posm[u >> 5] >> (u & 31)) & 1u)) continue;
+              const int q = nkept + new_idx[k] + j++;
+              const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
+              double K[4], F;
+              new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &n_exact);
+#pragma unroll
+              for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
+              S.F[nxt][q] = F;
+              S.tri[nxt][q] = tri_pack(x, y, sid);
+              const int mu = S.map[u];
+              S.nb[nxt][q][0] = (unsigned char)mu;
+              const int ru = S.nb[cur][u][0] == v ? 0 : (S.nb[cur][u][1] == v ? 1 : 2);
+              S.nb[nxt][mu][ru] = (unsigned char)q;
+            }
+          }
+        }
+        __syncwarp();
+        // close the cycle of new vertices around the new facet s
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const int q = 32 * k + lane;
+          if (q >= nkept && q < nv2) {
+            const unsigned tr = S.tri[nxt][q];
+            const int x = tri_at(tr, 0), y = tri_at(tr, 1);
+            int n1 = q, n2 = q;
+            for (int w = nkept; w < nv2; ++w) {
+              const unsigned tw = S.tri[nxt][w];
+              if (tri_at(tw, 0) == y) n1 = w;
+              if (tri_at(tw, 1) == x) n2 = w;
+            }
+            S.nb[nxt][q][1] = (unsigned char)n1;
+            S.nb[nxt][q][2] = (unsigned char)n2;
           }
         }
         c_constr += new_base;
@@ -599,9 +659,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
           const int f = tri_at(mytri[k], r);
-          const int zc = tri_at(mytri[k], (r + 2) % 3);
-          const int w = find_nb<VPL>(S.pm[cur], nv, v, zc, f);
-          if (w < 0) continue;  // unreachable for a valid polytope
+          const int w = S.nb[cur][v][(r + 2) % 3];  // next vertex of facet f (edge (., f))
           const double* xr = S.x[S.ref[f]];
           const double* xw = S.x[w];
           const double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -

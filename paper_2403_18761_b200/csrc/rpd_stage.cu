@@ -150,26 +150,20 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     planes[e] = make_double4(nx, ny, nz, sj.w - si.w);
   }
   __syncwarp();
-  // twins: next entry of the row with the same oriented plane.  Canonical form (n, d) / gcd
-  // hashed to 64 bits; only equal hashes are compared exactly (products < 2^53).
+  // twins: next entry of the row with the same oriented plane.  Key = bit patterns of the
+  // ratios to the first non-zero normal component (correctly rounded quotients of exactly
+  // proportional integers are equal) and its sign; equal keys are then compared exactly.
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const double4 a = planes[e];
-    long long q[4] = {(long long)a.x, (long long)a.y, (long long)a.z, (long long)a.w};
-    unsigned long long g = 0;
-    for (int c = 0; c < 4; ++c) {
-      unsigned long long x = (unsigned long long)(q[c] < 0 ? -q[c] : q[c]);
-      while (x) {
-        const unsigned long long r = g % x;
-        g = x;
-        x = r;
-      }
-    }
-    if (g == 0) g = 1;
-    unsigned long long h = 1469598103934665603ull;
-    for (int c = 0; c < 4; ++c) {
-      h ^= (unsigned long long)(q[c] / (long long)g);
-      h *= 1099511628211ull;
-    }
+    const double piv = a.x != 0.0 ? a.x : (a.y != 0.0 ? a.y : a.z);
+    const int which = a.x != 0.0 ? 0 : (a.y != 0.0 ? 1 : 2);
+    const double r0 = a.x / fabs(piv), r1 = a.y / fabs(piv), r2 = a.z / fabs(piv),
+                 r3 = a.w / fabs(piv);
+    unsigned long long h = 1469598103934665603ull ^ (unsigned long long)which;
+    h = (h ^ (unsigned long long)__double_as_longlong(r0)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(r1)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(r2)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(r3)) * 1099511628211ull;
     hkey[e] = h;
   }
   __syncwarp();
