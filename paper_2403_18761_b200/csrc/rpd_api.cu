@@ -2,6 +2,7 @@
 // step of the path runs in the kernels of rpd_stage.cu, rpd_filter.cu, rpd_scan.cu,
 // rpd_clip.cu and rpd_partial.cu.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -327,7 +328,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
                      sizeof(unsigned long long) * 5, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
-                     sizeof(unsigned long long) * 4, c->stream), "memset");
+                     sizeof(unsigned long long) * 7, c->stream), "memset");
   if (c->profile) cudaEventRecord(c->ev[2], c->stream);
   CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff,
                  c->clip_wide), "clip");
@@ -348,6 +349,9 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(cudaStreamSynchronize(c->stream), "clip");
   if (rb->u64[ST_OVERFLOW])
     return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+  if (getenv("RPD_DEBUG_STATS"))
+    fprintf(stderr, "[rpd clip] pairs %lld exact sign %llu exact out-vertex %llu plane-fallback %llu\n",
+            (long long)n, rb->u64[12], rb->u64[13], rb->u64[14]);
   const int64_t np = rb->i32[0], ni = rb->i32[1];
   const size_t npp = np > 0 ? np : 1;
   CK(ps.off.ensure(sizeof(int32_t) * (nt + 1)), "alloc");

@@ -222,7 +222,7 @@ __device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx
 // Falls back to the exact-cofactor construction from the three planes when an endpoint's
 // sign came from the exact path or the bound is too loose.
 template <int VPL>
-__device__ inline void new_vertex(const WarpState<VPL>& S, const ClipCtx& C, int cur, int u,
+__device__ inline int new_vertex(const WarpState<VPL>& S, const ClipCtx& C, int cur, int u,
                                   int v, int x, int y, int sid, double sabs, double K[4],
                                   double* F, int* nexact) {
   if (!S.vx[u] && !S.vx[v]) {
@@ -249,10 +249,11 @@ __device__ inline void new_vertex(const WarpState<VPL>& S, const ClipCtx& C, int
 #pragma unroll
       for (int m = 0; m < 4; ++m) K[m] *= sc;
       *F = Fn * sc;
-      return;
+      return 0;
     }
   }
   vertex_from_planes(S, C, x, y, sid, K, F, nexact);
+  return 1;
 }
 
 enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
+  int d_sign = 0, d_out = 0, d_fb = 0;  // diagnostics
   // algorithmic work (warp-uniform quantities, counted once per warp)
   long long c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;
 
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
               sg[k] = exact_sign(S, C, S.tri[cur][v], -1, s, es, nbr_idx[es], &zh);
               S.vx[v] = 1;
               ++n_exact;
+              ++d_sign;
               if (zh) {
                 ++n_zero;
                 zero_hit = 1;
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
               const int q = nkept + new_idx[k] + j++;
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
               double K[4], F;
-              new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &n_exact);
+              d_fb += new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &n_exact);
 #pragma unroll
               for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
               S.F[nxt][q] = F;
@@ -631,11 +634,21 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
         for (int m = 0; m < 4; ++m) K[m] = S.K[cur][v][m];
         double sum = K[0] + K[1] + K[2] + K[3];
+        // coordinates need |dx| <= 1.5e-11 diam(t): 15 F / sum <= 1.5e-11;
+        // edge-interpolated vertices that miss it are rebuilt from their planes, then exactly
         if (16.0 * S.F[cur][v] > 1e-12 * sum) {
-          exact_vertex_of(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1), tri_at(mytri[k], 2),
-                          K);
+          double F2;
+          int dummy = 0;
+          vertex_from_planes(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1),
+                             tri_at(mytri[k], 2), K, &F2, &dummy);
           sum = K[0] + K[1] + K[2] + K[3];
-          ++n_exact;
+          if (16.0 * F2 > 1e-12 * sum) {
+            exact_vertex_of(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1), tri_at(mytri[k], 2),
+                            K);
+            sum = K[0] + K[1] + K[2] + K[3];
+            ++n_exact;
+            ++d_out;
+          }
         }
         const double inv = 1.0 / sum;
 #pragma unroll
@@ -694,7 +707,15 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
     n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
     n_zero += __shfl_xor_sync(0xffffffffu, n_zero, o);
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    d_sign += __shfl_xor_sync(0xffffffffu, d_sign, o);
+    d_out += __shfl_xor_sync(0xffffffffu, d_out, o);
+    d_fb += __shfl_xor_sync(0xffffffffu, d_fb, o);
+  }
   if (lane == 0) {
+    atomicAdd(stats + 12, (unsigned long long)d_sign);
+    atomicAdd(stats + 13, (unsigned long long)d_out);
+    atomicAdd(stats + 14, (unsigned long long)d_fb);
     atomicAdd(stats + ST_CLIP_PLANES, (unsigned long long)c_planes);
     atomicAdd(stats + ST_CLIP_TESTS, (unsigned long long)c_tests);
     atomicAdd(stats + ST_CLIP_CONSTR, (unsigned long long)c_constr);
