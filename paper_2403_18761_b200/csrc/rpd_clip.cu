@@ -8,11 +8,12 @@
 // through it, kept as an oriented triangle of the dual triangulation so that clipping is a
 // local re-triangulation of the conflict region and facets can be walked.
 //
-// B200 mapping: one warp per pair, VPL vertex slots per lane (slot v = 32 k + lane), the
-// polytope in per-warp shared memory (double-buffered vertex table).  The fast kernel has
-// VPL = 1 (<= 32 vertices and planes, ~5 KB of shared memory per warp); pairs that exceed it
-// are re-run by the same kernel instantiated with VPL = 4 (<= 128).  The k_site planes are
-// first classified 32 at a time, one per lane, from their exact values at the 4 tet corners:
+// B200 mapping: a group of GW lanes per pair (GW = 16: two pairs per warp run in lockstep),
+// VPL vertex slots per lane (slot v = GW k + lane), the polytope in per-group shared memory
+// (double-buffered vertex table with explicit dual-edge links).  The fast kernel has GW = 16,
+// VPL = 1 (<= 16 vertices and planes); pairs that exceed it are re-run by the same kernel
+// instantiated with GW = 32, VPL = 4 (<= 128).  The k_site planes are first classified GW at a
+// time, one per lane, from their exact values at the 4 tet corners:
 // planes with all four values > 0 cannot cut (most of them), a plane with all four < 0
 // empties the piece; only the remaining planes run the per-vertex sign pass.
 //
@@ -27,16 +28,19 @@
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
+#ifndef RPD_CLIP_GW
+#define RPD_CLIP_GW 16   // lanes per pair in the fast kernel (2 pairs per warp)
+#endif
 #ifndef RPD_CLIP_MINB
 #define RPD_CLIP_MINB 3  // min resident 256-thread blocks per SM for the fast kernel
 #endif
 
 namespace rpd {
 
-template <int VPL>
+template <int GW, int VPL>
 struct WarpState {
-  static constexpr int MAXV = 32 * VPL;
-  static constexpr int MAXP = 32 * VPL;
+  static constexpr int MAXV = GW * VPL;
+  static constexpr int MAXP = GW * VPL;
   double g[MAXP][4];       // barycentric plane vectors (exact integers)
   double K[2][MAXV][4];    // homogeneous vertices (double-buffered vertex table)
   double F[2][MAXV];       // error scalars
@@ -83,9 +87,9 @@ struct Bits {
     set(tri_at(tr, 1));
     set(tri_at(tr, 2));
   }
-  __device__ void warp_or() {
+  __device__ void warp_or(unsigned mask) {
 #pragma unroll
-    for (int k = 0; k < W; ++k) w[k] = __reduce_or_sync(0xffffffffu, w[k]);
+    for (int k = 0; k < W; ++k) w[k] = __reduce_or_sync(mask, w[k]);
   }
   // next set bit >= from, or -1
   __device__ int next(int from) const {
@@ -103,8 +107,8 @@ struct ClipCtx {
   long long N;             // sphere count (SoS rank of tet faces = N + k)
 };
 
-template <int VPL>
-__device__ inline void make_xplane(const WarpState<VPL>& S, const ClipCtx& C, int id,
+template <int GW, int VPL>
+__device__ inline void make_xplane(const WarpState<GW, VPL>& S, const ClipCtx& C, int id,
                                    XPlane* xp) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) xp->a[k] = (long long)S.g[id][k];
@@ -127,8 +131,8 @@ __device__ inline void make_xplane(const WarpState<VPL>& S, const ClipCtx& C, in
 
 // SoS sign of the plane s (table id sid, or a new plane given by its vector, CSR entry and
 // rank when sid < 0) at the vertex with planes tr
-template <int VPL>
-__device__ __noinline__ int exact_sign(const WarpState<VPL>& S, const ClipCtx& C, unsigned tr,
+template <int GW, int VPL>
+__device__ __noinline__ int exact_sign(const WarpState<GW, VPL>& S, const ClipCtx& C, unsigned tr,
                                        int sid, const double* s, int es, int rank,
                                        int* zero_hit) {
   XPlane xa, xb, xc, xs;
@@ -150,8 +154,8 @@ __device__ __noinline__ int exact_sign(const WarpState<VPL>& S, const ClipCtx& C
   return sos_sign_exact(xa, xb, xc, xs, zero_hit);
 }
 
-template <int VPL>
-__device__ __noinline__ bool exact_is_zero(const WarpState<VPL>& S, const ClipCtx& C,
+template <int GW, int VPL>
+__device__ __noinline__ bool exact_is_zero(const WarpState<GW, VPL>& S, const ClipCtx& C,
                                            unsigned tr, int q) {
   XPlane xa, xb, xc, xq;
   make_xplane(S, C, tri_at(tr, 0), &xa);
@@ -161,8 +165,8 @@ __device__ __noinline__ bool exact_is_zero(const WarpState<VPL>& S, const ClipCt
   return det4_is_zero(xa, xb, xc, xq);
 }
 
-template <int VPL>
-__device__ __noinline__ void exact_vertex_of(const WarpState<VPL>& S, const ClipCtx& C, int a,
+template <int GW, int VPL>
+__device__ __noinline__ void exact_vertex_of(const WarpState<GW, VPL>& S, const ClipCtx& C, int a,
                                              int b, int c, double* K) {
   XPlane pa, pb, pc;
   make_xplane(S, C, a, &pa);
@@ -173,8 +177,8 @@ __device__ __noinline__ void exact_vertex_of(const WarpState<VPL>& S, const Clip
 
 // fp64 homogeneous vertex of planes (a, b, c), normalised to sum(K) > 0, with the error
 // scalar F such that |g . K~ - g . K| <= |g|_1 F for every plane vector g.
-template <int VPL>
-__device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx& C, int a,
+template <int GW, int VPL>
+__device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const ClipCtx& C, int a,
                                           int b, int c, double K[4], double* F, int* nexact) {
   const double* ra = S.g[a];
   const double* rb = S.g[b];
@@ -221,8 +225,8 @@ __device__ inline void vertex_from_planes(const WarpState<VPL>& S, const ClipCtx
 // from the endpoints' bounds and the plane values' bounds; rescaled by a power of two.
 // Falls back to the exact-cofactor construction from the three planes when an endpoint's
 // sign came from the exact path or the bound is too loose.
-template <int VPL>
-__device__ inline int new_vertex(const WarpState<VPL>& S, const ClipCtx& C, int cur, int u,
+template <int GW, int VPL>
+__device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, int cur, int u,
                                   int v, int x, int y, int sid, double sabs, double K[4],
                                   double* F, int* nexact) {
   if (!S.vx[u] && !S.vx[v]) {
@@ -269,7 +273,7 @@ struct PairOut {
   int32_t* over_count;
 };
 
-template <int VPL>
+template <int GW, int VPL>
 __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB : 1) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
     const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
@@ -277,18 +281,21 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
     const int32_t* __restrict__ nbr_idx, const double4* __restrict__ planes,
     const int32_t* __restrict__ twin, long long N, PairOut out,
     unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev) {
-  using WS = WarpState<VPL>;
+  using WS = WarpState<GW, VPL>;
   if (n_dev) n_pairs = *n_dev;
   constexpr int MAXV = WS::MAXV;
   constexpr int MAXP = WS::MAXP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WS& S = reinterpret_cast<WS*>(smem_raw)[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  const unsigned FULL = 0xffffffffu;
+  WS& S = reinterpret_cast<WS*>(smem_raw)[threadIdx.x / GW];
+  // GW lanes clip one pair (a "group"); 32 / GW groups per warp run in lockstep
+  const int lane = threadIdx.x & (GW - 1);
+  const int grp = (threadIdx.x & 31) / GW;
+  const unsigned GLOW = GW == 32 ? 0xffffffffu : ((1u << GW) - 1u);
+  const unsigned FULL = GLOW << (GW * grp);  // this group's lanes
   const unsigned lt_mask = (1u << lane) - 1u;
   ClipCtx C{planes, N};
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GW;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) / GW;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
   int d_sign = 0, d_out = 0, d_fb = 0;  // diagnostics
   // algorithmic work (warp-uniform quantities, counted once per warp)
@@ -313,12 +320,12 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
       for (int r = 0; r < 3; ++r) S.nb[0][lane][r] = CORNER_NB[lane][r];
     }
-    __syncwarp();
+    __syncwarp(FULL);
     int np = 4, nv = 4, cur = 0, status = ST_ALIVE, zero_hit = 0;
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     c_planes += e1 - e0;
 
-    for (int base = e0; base < e1 && status == ST_ALIVE; base += 32) {
+    for (int base = e0; base < e1 && status == ST_ALIVE; base += GW) {
       const int e = base + lane;
       const bool have = e < e1;
       double g[4] = {0.0, 0.0, 0.0, 0.0};
@@ -338,13 +345,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         status = ST_EMPTY;
         break;
       }
-      unsigned act = __ballot_sync(FULL, have && !allpos);
+      unsigned act = (__ballot_sync(FULL, have && !allpos) >> (GW * grp)) & GLOW;
       while (act && status == ST_ALIVE) {
         const int l = __ffs(act) - 1;
         act &= act - 1;
         double s[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s[k] = __shfl_sync(FULL, g[k], l);
+        for (int k = 0; k < 4; ++k) s[k] = __shfl_sync(FULL, g[k], l, GW);
         const int es = base + l;
         const double sabs = fabs(s[0]) + fabs(s[1]) + fabs(s[2]) + fabs(s[3]);
 
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         bool anyneg = false, anypos = false;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          const int v = 32 * k + lane;
+          const int v = GW * k + lane;
           const bool valid = v < nv;
           sg[k] = 0;
           if (valid) {
@@ -377,8 +384,8 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
               }
             }
           }
-          negm[k] = __ballot_sync(FULL, valid && sg[k] < 0);
-          posm[k] = __ballot_sync(FULL, valid && sg[k] > 0);
+          negm[k] = (__ballot_sync(FULL, valid && sg[k] < 0) >> (GW * grp)) & GLOW;
+          posm[k] = (__ballot_sync(FULL, valid && sg[k] > 0) >> (GW * grp)) & GLOW;
           anyneg |= negm[k] != 0u;
           anypos |= posm[k] != 0u;
         }
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #ifdef RPD_TRACE
         if (p == RPD_TRACE) {
           for (int k = 0; k < VPL; ++k) {
-            int v = 32 * k + lane;
+            int v = GW * k + lane;
             if (v < nv) {
               unsigned tr = S.tri[cur][v];
               printf("plane j=%d es=%d v=%d tri=(%d,%d,%d) sg=%d K=(%g,%g,%g,%g) F=%g\n",
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
           S.src[sid] = nbr_idx[es];
           S.eidx[sid] = es;
         }
-        __syncwarp();
+        __syncwarp(FULL);
         // ---- new vertices: one per boundary edge of the conflict region (a removed vertex v
         // with a kept neighbour u across its dual edge (x, y)), oriented as that edge:
         // (x, y, s).  Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring
@@ -422,13 +429,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         int nnew[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          const int v = 32 * k + lane;
+          const int v = GW * k + lane;
           nnew[k] = 0;
           if (v < nv && sg[k] < 0) {
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
               const int u = S.nb[cur][v][r];
-              nnew[k] += (posm[u >> 5] >> (u & 31)) & 1u;
+              nnew[k] += (posm[u / GW] >> (u % GW)) & 1u;
             }
           }
         }
@@ -441,12 +448,12 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
           kept_base += __popc(posm[k]);
           int incl = nnew[k];
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
+          for (int o = 1; o < GW; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o, GW);
             if (lane >= o) incl += y;
           }
           new_idx[k] = new_base + incl - nnew[k];
-          new_base += __shfl_sync(FULL, incl, 31);
+          new_base += __shfl_sync(FULL, incl, GW - 1, GW);
         }
         const int nkept = kept_base;
         const int nv2 = nkept + new_base;
@@ -457,13 +464,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         const int nxt = cur ^ 1;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          const int v = 32 * k + lane;
+          const int v = GW * k + lane;
           if (v < nv && sg[k] > 0) S.map[v] = (unsigned char)kept_idx[k];
         }
-        __syncwarp();
+        __syncwarp(FULL);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          const int v = 32 * k + lane;
+          const int v = GW * k + lane;
           if (v >= nv) continue;
           if (sg[k] > 0) {
             const int q = kept_idx[k];
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
               const int u = S.nb[cur][v][r];
-              if ((posm[u >> 5] >> (u & 31)) & 1u) S.nb[nxt][q][r] = S.map[u];
+              if ((posm[u / GW] >> (u % GW)) & 1u) S.nb[nxt][q][r] = S.map[u];
             }
           } else {
             const unsigned tr = S.tri[cur][v];
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
               const int u = S.nb[cur][v][r];
-              if (!((posm[u >> 5] >> (u & 31)) & 1u)) continue;
+              if (!((posm[u / GW] >> (u % GW)) & 1u)) continue;
               const int q = nkept + new_idx[k] + j++;
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
               double K[4], F;
@@ -498,11 +505,11 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
             }
           }
         }
-        __syncwarp();
+        __syncwarp(FULL);
         // close the cycle of new vertices around the new facet s
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          const int q = 32 * k + lane;
+          const int q = GW * k + lane;
           if (q >= nkept && q < nv2) {
             const unsigned tr = S.tri[nxt][q];
             const int x = tri_at(tr, 0), y = tri_at(tr, 1);
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         c_constr += new_base;
         nv = nv2;
         cur = nxt;
-        __syncwarp();
+        __syncwarp(FULL);
       }
     }
 
@@ -533,7 +540,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         }
       }
       if (lane == 0) out.flag[p] = status == ST_OVER ? 2 : 0;
-      __syncwarp();
+      __syncwarp(FULL);
       continue;
     }
     max_v = max(max_v, nv);
@@ -543,11 +550,11 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
     facets_all.clear();
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      const int v = 32 * k + lane;
+      const int v = GW * k + lane;
       mytri[k] = v < nv ? S.tri[cur][v] : 0xffffffu;
       if (v < nv) facets_all.set_tri(mytri[k]);
     }
-    facets_all.warp_or();
+    facets_all.warp_or(FULL);
     Bits<VPL> facets = facets_all;
     {
       int nf = 0;
@@ -563,15 +570,15 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         Q.clear();
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
-          if (32 * k + lane < nv && tri_has(mytri[k], f)) Q.set_tri(mytri[k]);
-        Q.warp_or();
+          if (GW * k + lane < nv && tri_has(mytri[k], f)) Q.set_tri(mytri[k]);
+        Q.warp_or(FULL);
         Q.w[f >> 5] &= ~(1u << (f & 31));
         bool zero_area = false;
         for (int q = Q.next(0); q >= 0 && !zero_area; q = Q.next(q + 1)) {
           bool on = true;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
-            const int v = 32 * k + lane;
+            const int v = GW * k + lane;
             if (v < nv && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
               const double* K = S.K[cur][v];
               const double* gq = S.g[q];
@@ -597,7 +604,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
     unsigned* words = out.incmask + out.mask_off[p];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      const int pl = 32 * k + lane;
+      const int pl = GW * k + lane;
       if (pl < np) S.ref[pl] = 0x7fffffff;
       if (pl < np && facets.has(pl)) {
         const int src = S.src[pl];
@@ -622,13 +629,13 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
       }
     }
     const unsigned facemask = __reduce_or_sync(FULL, fmask_bits);
-    __syncwarp();
+    __syncwarp(FULL);
 
     // ---- geometry: vertex coordinates relative to V0 (lattice units); facet fan apex =
     // lowest vertex of the facet
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      const int v = 32 * k + lane;
+      const int v = GW * k + lane;
       if (v < nv) {
         double K[4];
 #pragma unroll
@@ -662,11 +669,11 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         for (int r = 0; r < 3; ++r) atomicMin(&S.ref[tri_at(mytri[k], r)], v);
       }
     }
-    __syncwarp();
+    __syncwarp(FULL);
     double vol6 = 0.0, m24[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      const int v = 32 * k + lane;
+      const int v = GW * k + lane;
       if (v < nv) {
         const double* xv = S.x[v];
 #pragma unroll
@@ -685,10 +692,10 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      vol6 += __shfl_xor_sync(FULL, vol6, o);
+    for (int o = GW / 2; o > 0; o >>= 1) {
+      vol6 += __shfl_xor_sync(FULL, vol6, o, GW);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) m24[c] += __shfl_xor_sync(FULL, m24[c], o);
+      for (int c = 0; c < 3; ++c) m24[c] += __shfl_xor_sync(FULL, m24[c], o, GW);
     }
     if (lane == 0) {
       const double L = 1.0 / RPD_LATTICE;
@@ -700,28 +707,28 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
       out.flag[p] = 1;
       out.fm[p] = (uint8_t)facemask;
     }
-    __syncwarp();
+    __syncwarp(FULL);
   }
-  // statistics (warp-aggregated)
+  // statistics: per-lane counters summed over the warp, group-uniform ones by group leaders
   for (int o = 16; o > 0; o >>= 1) {
     n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
     n_zero += __shfl_xor_sync(0xffffffffu, n_zero, o);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
     d_sign += __shfl_xor_sync(0xffffffffu, d_sign, o);
     d_out += __shfl_xor_sync(0xffffffffu, d_out, o);
     d_fb += __shfl_xor_sync(0xffffffffu, d_fb, o);
   }
-  if (lane == 0) {
+  if ((threadIdx.x & 31) == 0) {
     atomicAdd(stats + 12, (unsigned long long)d_sign);
     atomicAdd(stats + 13, (unsigned long long)d_out);
     atomicAdd(stats + 14, (unsigned long long)d_fb);
+    if (n_exact) atomicAdd(stats + ST_EXACT, (unsigned long long)n_exact);
+    if (n_zero) atomicAdd(stats + ST_ZERO, (unsigned long long)n_zero);
+  }
+  if (lane == 0) {
     atomicAdd(stats + ST_CLIP_PLANES, (unsigned long long)c_planes);
     atomicAdd(stats + ST_CLIP_TESTS, (unsigned long long)c_tests);
     atomicAdd(stats + ST_CLIP_CONSTR, (unsigned long long)c_constr);
     atomicAdd(stats + ST_CLIP_FAN, (unsigned long long)c_fan);
-    if (n_exact) atomicAdd(stats + ST_EXACT, (unsigned long long)n_exact);
-    if (n_zero) atomicAdd(stats + ST_ZERO, (unsigned long long)n_zero);
     if (n_over && VPL > 1) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
     atomicMax(stats + ST_MAXV, (unsigned long long)max_v);
     atomicMax(stats + ST_MAXP, (unsigned long long)max_p);
@@ -789,22 +796,23 @@ __global__ void k_piece_off(int64_t T, const int32_t* __restrict__ cand_off,
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-template <int VPL>
+template <int GW, int VPL>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
                                  bool collect_overflow, const int32_t* n_dev) {
-  constexpr int WARPS = VPL == 1 ? 8 : 2;
-  size_t smem = sizeof(WarpState<VPL>) * WARPS;
-  cudaError_t e = cudaFuncSetAttribute(k_clip<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  constexpr int THREADS = VPL == 1 ? 256 : 64;
+  constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
+  size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
+  cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_clip<VPL>, WARPS * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_clip<GW, VPL>, THREADS, smem);
   if (occ < 1) occ = 1;
-  int64_t want = (n + WARPS - 1) / WARPS;
+  int64_t want = (n + GROUPS - 1) / GROUPS;
   int64_t grid = (int64_t)sms * occ;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
@@ -812,7 +820,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
             collect_overflow ? c->p_over.as<int32_t>() + 1 : nullptr,
             collect_overflow ? c->p_over.as<int32_t>() : nullptr};
-  k_clip<VPL><<<(unsigned)grid, WARPS * 32, smem, c->stream>>>(
+  k_clip<GW, VPL><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
       c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>(),
@@ -828,16 +836,17 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         int wide) {
   if (n_pairs == 0) return cudaSuccess;
   if (wide)
-    return launch_clip_t<4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, false,
-                            nullptr);
-  return launch_clip_t<1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, true, nullptr);
+    return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, false,
+                                nullptr);
+  return launch_clip_t<RPD_CLIP_GW, 1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff,
+                                       true, nullptr);
 }
 
 // wide kernel over the overflow list p_over[1 .. p_over[0]] (count read on the device)
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
-  return launch_clip_t<4>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx,
-                          moff, false, c->p_over.as<int32_t>());
+  return launch_clip_t<32, 4>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids,
+                              cand_idx, moff, false, c->p_over.as<int32_t>());
 }
 
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {
