@@ -32,7 +32,7 @@
 #define RPD_CLIP_GW 16   // lanes per pair in the fast kernel (2 pairs per warp)
 #endif
 #ifndef RPD_CLIP_MINB
-#define RPD_CLIP_MINB 3  // min resident 256-thread blocks per SM for the fast kernel
+#define RPD_CLIP_MINB 2  // min resident 256-thread blocks per SM for the fast kernel
 #endif
 
 namespace rpd {
