@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--filter", default="all_pairs", choices=["all_pairs", "pruned"])
+    ap.add_argument("--filter", default="pruned", choices=["all_pairs", "pruned"])
     ap.add_argument("--partial-iters", type=int, default=-1,
                     help="partial updates per step (-1: all batches of the config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -139,10 +139,7 @@ def run_reference(args):
     cores = oracle.max_threads()
     rng = np.random.default_rng(0)
     # calibrate the sample so the whole run ends in a few minutes
-    probe = np.sort(rng.choice(w.T, 32, replace=False)).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.rpd_workload(w, tet_ids=probe)
-    per_tet = (time.perf_counter() - t0) / len(probe)
+    per_tet = _oracle_per_tet(oracle, w, rng)
     budget = 150.0 / max(args.steps + args.warmup, 1)
     n_s = int(min(max(budget / max(per_tet, 1e-6), 16), w.T))
     times, pairs = [], []
@@ -169,15 +166,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _oracle_per_tet(oracle, w, rng):
+    """Oracle seconds per tet (two probe sizes, removing the per-call input validation)."""
+    ts = []
+    for n in (16, 80):
+        ids = np.sort(rng.choice(w.T, n, replace=False)).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.rpd_workload(w, tet_ids=ids)
+        ts.append(time.perf_counter() - t0)
+    return max((ts[1] - ts[0]) / 64.0, 1e-6)
+
+
 def cpu_baseline(w, seconds):
     """The oracle timed on a bounded sample of the bench workload (rank 0, N = 1)."""
     import oracle
     cores = oracle.max_threads()
     rng = np.random.default_rng(1)
-    probe = np.sort(rng.choice(w.T, 32, replace=False)).astype(np.int32)
-    t0 = time.perf_counter()
-    oracle.rpd_workload(w, tet_ids=probe)
-    per_tet = (time.perf_counter() - t0) / len(probe)
+    per_tet = _oracle_per_tet(oracle, w, rng)
     n_s = int(min(max(seconds / max(per_tet, 1e-6), 32), w.T))
     ids = np.sort(rng.choice(w.T, n_s, replace=False)).astype(np.int32)
     t0 = time.perf_counter()
@@ -241,9 +246,13 @@ def main():
                              40 * st["clip_constructions"] + 30 * st["clip_fan_triangles"]),
                "partial": []}
         for (sph, off, idx, new) in d_batches:
+            pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pe0.record()
             counts, nd = ctx.update_partial(sph, off, idx, new)
+            pe1.record()
             st = ctx.stats()
-            rec["partial"].append({"n_dirty": nd, "n_cand": st["n_cand"]})
+            rec["partial"].append({"n_dirty": nd, "n_cand": st["n_cand"], "ev": (pe0, pe1),
+                                   "clipped": st["pairs_clipped"]})
         if world > 1:
             loc = ctx.download_pieces(device=True)
             gather_pieces(loc, ids, w.T)
@@ -272,7 +281,10 @@ def main():
     clocks = sampler.stop()
     total_ms = float(np.sum(times))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    pairs_local = sum(r["n_cand"] + sum(p["n_cand"] for p in r["partial"]) for r in recs)
+    torch.cuda.synchronize()
+    partial_ms = [p["ev"][0].elapsed_time(p["ev"][1]) for r in recs for p in r["partial"]]
+    # pairs clipped: all candidates of the full RPD + the re-clipped pairs of the dirty tets
+    pairs_local = sum(r["n_cand"] + sum(p["clipped"] for p in r["partial"]) for r in recs)
     pl = torch.tensor([pairs_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -340,7 +352,9 @@ def main():
         "filter_ms": fmed, "clip_ms": cmed,
         "pairs_filtered_per_s": float(recs[0]["pairs_filtered"]) * world / (fmed * 1e-3),
         "pairs_clipped_per_s_clip_kernel": recs[0]["n_cand"] * world / (cmed * 1e-3),
-        "partial_rpd_ms": None,
+        "partial_rpd_ms": float(np.median(partial_ms)) if partial_ms else None,
+        "partial_dirty_tets": float(np.median([p["n_dirty"] for r in recs for p in r["partial"]]))
+        if partial_ms else None,
         "roofline": roofline,
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),

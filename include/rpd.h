@@ -151,6 +151,7 @@ typedef struct {
   int64_t T, N, n_cand, n_pieces, n_inc, n_dirty;
   int64_t pairs_filtered;        /* (tet, sphere) pairs whose Alg. 1 boolean was decided */
   int64_t pairs_tested;          /* pairs on which Alg. 1 was actually evaluated (pruned mode) */
+  int64_t pairs_clipped;         /* candidate pairs clipped by the last call */
   int64_t exact_fallbacks;       /* clip predicates decided by the int128 path */
   int64_t zero_hits;             /* exact-zero predicates resolved by symbolic perturbation */
   int64_t kernel_launches;

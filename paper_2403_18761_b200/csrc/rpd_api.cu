@@ -369,6 +369,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   ps.n_tets = nt;
   ps.n_pieces = np;
   ps.n_inc = ni;
+  c->last.pairs_clipped += n;
   c->last.exact_fallbacks += (int64_t)rb->u64[ST_EXACT];
   c->last.zero_hits += (int64_t)rb->u64[ST_ZERO];
   c->last.max_vertices = max(c->last.max_vertices, (int32_t)rb->u64[ST_MAXV]);

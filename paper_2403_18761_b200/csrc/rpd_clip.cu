@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
     const int64_t a = pair_tet[p];
     const int64_t t = tet_ids ? (int64_t)tet_ids[a] : a;
     const int i = cand_idx[p];
-    if (lane < 12) (&S.V[0][0])[lane] = __ldg(tx + lane * T + t);
+    for (int q = lane; q < 12; q += GW) (&S.V[0][0])[q] = __ldg(tx + q * T + t);
     if (lane < 4) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {

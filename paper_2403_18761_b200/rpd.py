@@ -44,6 +44,7 @@ class _Stats(C.Structure):
     _fields_ = [("T", C.c_int64), ("N", C.c_int64), ("n_cand", C.c_int64),
                 ("n_pieces", C.c_int64), ("n_inc", C.c_int64), ("n_dirty", C.c_int64),
                 ("pairs_filtered", C.c_int64), ("pairs_tested", C.c_int64),
+                ("pairs_clipped", C.c_int64),
                 ("exact_fallbacks", C.c_int64), ("zero_hits", C.c_int64),
                 ("kernel_launches", C.c_int64), ("max_k_tet", C.c_int32),
                 ("max_vertices", C.c_int32), ("max_planes", C.c_int32), ("n_wide", C.c_int32),
