@@ -135,7 +135,8 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->h_verts, &c->h_tets, &c->h_spheres, &c->h_off, &c->h_idx, &c->h_new,
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
-                    &c->st.twin, &c->st.hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
+                    &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
+                    &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off};
@@ -218,7 +219,8 @@ static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t*
 }
 
 static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
-                                const int32_t* nbr_off, const int32_t* nbr_idx) {
+                                const int32_t* nbr_off, const int32_t* nbr_idx,
+                                bool reuse_rows) {
   int64_t E = 0;
   rpd_status s = read_E(c, nbr_off, N, &E);
   if (s) return s;
@@ -228,7 +230,7 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   CK(resolve(c, spheres, 4 * N, c->h_spheres, &d_sph), "stage spheres");
   CK(resolve(c, nbr_off, N > 0 ? N + 1 : 0, c->h_off, &d_off), "stage nbr_off");
   CK(resolve(c, nbr_idx, E, c->h_idx, &d_idx), "stage nbr_idx");
-  CK(launch_stage_spheres(c, d_sph, N, d_off, d_idx, E), "stage spheres");
+  CK(launch_stage_spheres(c, d_sph, N, d_off, d_idx, E, reuse_rows), "stage spheres");
   return RPD_OK;
 }
 
@@ -428,7 +430,7 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_stage_mesh(c, d_verts, V, d_tets, T), "stage mesh");
-  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx);
+  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx, false);
   if (s) return s;
   reset_last(c);
   c->cur = 0;
@@ -488,7 +490,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
-  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx);
+  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, true);
   if (s) return s;
   c->last.N = N_new;
 

@@ -76,6 +76,8 @@ struct Stage {
   DevBuf planes;   // double4 per CSR entry: (n, d) of h_ij
   DevBuf twin;     // int32 per CSR entry: next entry of the row with the same oriented plane
   DevBuf hkey;     // uint64 per CSR entry: hash of the canonical plane (twin search)
+  // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
+  DevBuf old_off, old_idx, old_planes, old_twin, old_hkey;
   int64_t T = 0, N = 0, V = 0, E = 0;
 };
 
@@ -147,7 +149,8 @@ namespace rpd {
 cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
                               int64_t T);
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
-                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E);
+                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                 bool reuse_rows);
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,

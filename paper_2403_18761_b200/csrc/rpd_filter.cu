@@ -161,18 +161,47 @@ __global__ void k_super_boxes(const double* __restrict__ leaf, int64_t n_leaf,
   }
 }
 
-// can some tet inside box B pass every plane of the sphere?  (exact, conservative)
-__device__ __forceinline__ bool box_passes(const double* __restrict__ B,
-                                           const double4* __restrict__ sp, int k,
-                                           const double4* __restrict__ gp) {
-  const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
-  for (int e = 0; e < k; ++e) {
-    const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
-    const double mh =
-        p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) + fmax(p.z * l2, p.z * h2);
-    if (!pos(mh)) return false;
+// Can some tet inside the lane's box B pass every plane of the sphere?  (exact, conservative)
+// Warp-cooperative: planes beyond the first BVH_PCAP are staged into shared memory chunk by
+// chunk (never read one by one from global memory); staged = first plane currently in sp.
+__device__ __forceinline__ bool box_passes_w(const double* __restrict__ B, bool valid,
+                                             double4* __restrict__ sp,
+                                             const double4* __restrict__ gp, int k,
+                                             int& staged) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double l0 = 0, l1 = 0, l2 = 0, h0 = 0, h1 = 0, h2 = 0;
+  if (valid) {
+    l0 = B[0];
+    l1 = B[1];
+    l2 = B[2];
+    h0 = B[3];
+    h1 = B[4];
+    h2 = B[5];
   }
-  return true;
+  bool alive = valid;
+  for (int c0 = 0; c0 < k; c0 += BVH_PCAP) {
+    if (!__any_sync(FULL, alive)) break;
+    if (staged != c0) {
+      __syncwarp();
+      for (int e = lane; e < BVH_PCAP && c0 + e < k; e += 32) sp[e] = gp[c0 + e];
+      __syncwarp();
+      staged = c0;
+    }
+    const int ce = min(k - c0, BVH_PCAP);
+    if (alive) {
+      for (int e = 0; e < ce; ++e) {
+        const double4 p = sp[e];
+        const double mh = p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) +
+                          fmax(p.z * l2, p.z * h2);
+        if (!pos(mh)) {
+          alive = false;
+          break;
+        }
+      }
+    }
+  }
+  return alive;
 }
 
 constexpr int BVH_WARPS = 4;
@@ -195,12 +224,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
     const int k = e1 - e0;
     if (k == 0 && N != 1) continue;  // hidden sphere (R4): relates to no tet
     const double4* gp = planes + e0;
-    __syncwarp();
-    for (int e = lane; e < k && e < BVH_PCAP; e += 32) sp[e] = gp[e];
-    __syncwarp();
+    int staged = -1;
     for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
       const int64_t s = s0 + lane;
-      const bool ok = s < n_sup && box_passes(sup + 6 * s, sp, k, gp);
+      const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, gp, k, staged);
       const unsigned sm = __ballot_sync(FULL, ok);
       if (!sm) continue;
       int base = 0;
@@ -231,7 +258,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
   const int n_items = min(*n_items_p, cap_items);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int cur_i = -1;
+  int cur_i = -1, staged = -1;
   for (int64_t it = gw; it < n_items; it += nw) {
     const int2 item = items[it];
     const int i = item.x;
@@ -240,14 +267,19 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const int k = e1 - e0;
     const double4* gp = planes + e0;
     if (i != cur_i) {
-      __syncwarp();
-      for (int e = lane; e < k && e < BVH_PCAP; e += 32) sp[e] = gp[e];
-      __syncwarp();
+      staged = -1;
       cur_i = i;
     }
     const int words = (k + 31) >> 5;
     const int64_t l = sl * BVH_FAN + lane;
-    unsigned lm = __ballot_sync(FULL, l < n_leaf && box_passes(leaf + 6 * l, sp, k, gp));
+    unsigned lm = __ballot_sync(FULL, box_passes_w(leaf + 6 * l, l < n_leaf, sp, gp, k, staged));
+    // the per-tet tests below read planes < BVH_PCAP from shared memory: restage chunk 0
+    if (staged != 0 && lm) {
+      __syncwarp();
+      for (int e = lane; e < BVH_PCAP && e < k; e += 32) sp[e] = gp[e];
+      __syncwarp();
+      staged = 0;
+    }
     while (lm) {
       const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
       lm &= lm - 1;

@@ -8,6 +8,8 @@
 // Every value is an integer-valued double below 2^53, so all of it is exact.
 #include <math.h>
 
+#include <utility>
+
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -95,15 +97,26 @@ __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
   sw[i] = make_double4(S[0], S[1], S[2], W);
 }
 
-// One warp per sphere row: validation, rank sort (ascending neighbour id), radical planes
-// and twins.  The sort and the twin search are O(k^2 / 32) per row (k = k_site <= ~1000).
+struct OldRows {  // previous staged CSR (partial updates: unchanged rows are copied)
+  const int32_t* off;
+  const int32_t* idx;
+  const double4* planes;
+  const int32_t* twin;
+  const unsigned long long* hkey;
+  int64_t N;
+};
+
+// One warp per sphere row: validation, ascending order (fast path for sorted input rows,
+// else rank sort), radical planes and twins.  In a partial update a row of an old sphere
+// whose neighbour list is unchanged is copied from the previous stage instead.
 __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
-                             unsigned long long* __restrict__ hkey, int* err) {
+                             unsigned long long* __restrict__ hkey, OldRows old, int* err) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
   if (i >= N) return;
   const int32_t e0 = off_in[i], e1 = off_in[i + 1];
   if (lane == 0) {
@@ -113,6 +126,27 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   if (e0 < 0 || e1 < e0 || e1 > E || (i == 0 && e0 != 0) || (i == N - 1 && e1 != E)) {
     if (lane == 0) report(err, RPD_EINVAL, ERR_NBR_OFF, i);
     return;
+  }
+  const int k = e1 - e0;
+  // sorted strictly ascending?  (then no duplicates either)
+  bool sorted = true;
+  for (int32_t e = e0 + lane; e + 1 < e1; e += 32) sorted &= idx_in[e] < idx_in[e + 1];
+  sorted = __all_sync(FULL, sorted);
+  // unchanged row of an old sphere: copy the previous stage
+  if (old.off && i < old.N && sorted) {
+    const int32_t o0 = old.off[i], o1 = old.off[i + 1];
+    bool same = (o1 - o0) == k;
+    for (int32_t q = lane; same && q < k; q += 32) same = old.idx[o0 + q] == idx_in[e0 + q];
+    if (__all_sync(FULL, same)) {
+      for (int32_t q = lane; q < k; q += 32) {
+        idx_out[e0 + q] = old.idx[o0 + q];
+        planes[e0 + q] = old.planes[o0 + q];
+        hkey[e0 + q] = old.hkey[o0 + q];
+        const int32_t tw = old.twin[o0 + q];
+        twin[e0 + q] = tw < 0 ? -1 : tw - o0 + e0;
+      }
+      return;
+    }
   }
   bool bad = false;
   for (int32_t e = e0 + lane; e < e1; e += 32) {
@@ -127,6 +161,10 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
       bad = true;
       break;
     }
+    if (sorted) {
+      idx_out[e] = j;
+      continue;
+    }
     int rank = 0;
     for (int32_t f = e0; f < e1; ++f) {
       const int32_t x = idx_in[f];
@@ -139,45 +177,46 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     if (bad) break;
     idx_out[e0 + rank] = j;
   }
-  if (__any_sync(0xffffffffu, bad)) return;
+  if (__any_sync(FULL, bad)) return;
   __syncwarp();
   const double4 si = sw[i];
+  // planes, and the twin key: bit patterns of the ratios to the first non-zero normal
+  // component (correctly rounded quotients of exactly proportional integers are equal)
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const int32_t j = idx_out[e];
     const double4 sj = sw[j];
     const double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
     if (nx == 0.0 && ny == 0.0 && nz == 0.0) report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
-    planes[e] = make_double4(nx, ny, nz, sj.w - si.w);
-  }
-  __syncwarp();
-  // twins: next entry of the row with the same oriented plane.  Key = bit patterns of the
-  // ratios to the first non-zero normal component (correctly rounded quotients of exactly
-  // proportional integers are equal) and its sign; equal keys are then compared exactly.
-  for (int32_t e = e0 + lane; e < e1; e += 32) {
-    const double4 a = planes[e];
-    const double piv = a.x != 0.0 ? a.x : (a.y != 0.0 ? a.y : a.z);
+    const double4 a = make_double4(nx, ny, nz, sj.w - si.w);
+    planes[e] = a;
+    const double piv = fabs(a.x != 0.0 ? a.x : (a.y != 0.0 ? a.y : a.z));
     const int which = a.x != 0.0 ? 0 : (a.y != 0.0 ? 1 : 2);
-    const double r0 = a.x / fabs(piv), r1 = a.y / fabs(piv), r2 = a.z / fabs(piv),
-                 r3 = a.w / fabs(piv);
     unsigned long long h = 1469598103934665603ull ^ (unsigned long long)which;
-    h = (h ^ (unsigned long long)__double_as_longlong(r0)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(r1)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(r2)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(r3)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.x / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.y / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.z / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.w / piv)) * 1099511628211ull;
     hkey[e] = h;
   }
   __syncwarp();
+  // twins: next entry of the row with the same oriented plane (equal keys compared exactly)
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const unsigned long long h = hkey[e];
     int32_t tw = -1;
-    for (int32_t f = e + 1; f < e1 && tw < 0; ++f) {
-      if (hkey[f] != h) continue;
-      const double4 a = planes[e], b = planes[f];
-      const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
-                        a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
-                        a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
-      const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
-      if (prop && dot > 0.0) tw = f;
+    for (int32_t f = e + 1; f < e1 && tw < 0; f += 4) {
+      unsigned long long hf[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) hf[q] = f + q < e1 ? hkey[f + q] : ~h;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (tw >= 0 || hf[q] != h) continue;
+        const double4 a = planes[e], b = planes[f + q];
+        const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
+                          a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
+                          a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
+        const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
+        if (prop && dot > 0.0) tw = f + q;
+      }
     }
     twin[e] = tw;
   }
@@ -205,15 +244,28 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
 }
 
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
-                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E) {
+                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                 bool reuse_rows) {
   Stage& s = c->st;
   cudaError_t e;
+  // the previous rows become the "old" buffers (copied for unchanged rows when reuse_rows)
+  std::swap(s.nbr_off, s.old_off);
+  std::swap(s.nbr_idx, s.old_idx);
+  std::swap(s.planes, s.old_planes);
+  std::swap(s.twin, s.old_twin);
+  std::swap(s.hkey, s.old_hkey);
+  const int64_t N_old = s.N;
   if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
   if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
   if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
   if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
+  OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  if (reuse_rows && s.old_off.p)
+    old = OldRows{s.old_off.as<int32_t>(),  s.old_idx.as<int32_t>(),
+                  s.old_planes.as<double4>(), s.old_twin.as<int32_t>(),
+                  s.old_hkey.as<unsigned long long>(), N_old};
   s.N = N;
   s.E = E;
   int* err = c->errw.as<int>();
@@ -223,7 +275,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
     k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
-        s.hkey.as<unsigned long long>(), err);
+        s.hkey.as<unsigned long long>(), old, err);
     ++c->launches;
   } else {
     e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
