@@ -133,7 +133,7 @@ struct rpd_ctx {
   rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_scan, i_scan;
 
   // partial update scratch
-  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off;
+  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off, m_src;
   int64_t n_dirty = 0;
 
   rpd_stats last{};

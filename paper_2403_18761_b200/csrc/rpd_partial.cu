@@ -119,39 +119,65 @@ struct MergeDst {
   int32_t *c_idx, *pair_tet, *p_sphere, *p_inc_off, *p_inc;
   double *p_vol, *p_m1;
   uint8_t* p_fm;
+  int32_t* src_piece;  // per new piece: source piece index, +(1 << 30) when from the dirty set
 };
 
-__global__ void k_merge_copy(int64_t T, const int32_t* __restrict__ dpos, MergeSrc o,
-                             MergeSrc n, MergeDst D, int64_t n_pieces_new, int64_t n_inc_new) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  if (t == T - 1) D.p_inc_off[n_pieces_new] = (int32_t)n_inc_new;
+// last index t in [0, n) with off[t] <= q (off non-decreasing, off[0] = 0)
+__device__ __forceinline__ int64_t seg_of(const int32_t* __restrict__ off, int64_t n, int64_t q) {
+  int64_t lo = 0, hi = n;  // invariant: off[lo] <= q < off[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= q) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// one thread per merged candidate
+__global__ void k_merge_cands(int64_t T, int64_t n_new, const int32_t* __restrict__ dpos,
+                              MergeSrc o, MergeSrc n, MergeDst D) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_new) return;
+  const int64_t t = seg_of(D.c_off, T, q);
   const int d = dpos[t];
-  const MergeSrc s = pick(d, o, n);
+  const MergeSrc& s = d >= 0 ? n : o;
   const int64_t k = d >= 0 ? d : t;
-  // candidates
-  const int c0 = s.c_off[k], c1 = s.c_off[k + 1];
-  int dc = D.c_off[t];
-  for (int q = c0; q < c1; ++q, ++dc) {
-    D.c_idx[dc] = s.c_idx[q];
-    D.pair_tet[dc] = (int32_t)t;
-  }
-  // pieces and incidences
-  const int p0 = s.p_off[k], p1 = s.p_off[k + 1];
-  const int ibase = s.p_inc_off[p0];
-  int dp = D.p_off[t];
-  const int di = D.i_tet[t];
-  for (int q = p0; q < p1; ++q, ++dp) {
-    D.p_sphere[dp] = s.p_sphere[q];
-    D.p_vol[dp] = s.p_vol[q];
-    D.p_m1[3 * dp + 0] = s.p_m1[3 * q + 0];
-    D.p_m1[3 * dp + 1] = s.p_m1[3 * q + 1];
-    D.p_m1[3 * dp + 2] = s.p_m1[3 * q + 2];
-    D.p_fm[dp] = s.p_fm[q];
-    D.p_inc_off[dp] = di + (s.p_inc_off[q] - ibase);
-    for (int r = s.p_inc_off[q]; r < s.p_inc_off[q + 1]; ++r)
-      D.p_inc[di + (r - ibase)] = s.p_inc[r];
-  }
+  D.c_idx[q] = s.c_idx[s.c_off[k] + (q - D.c_off[t])];
+  D.pair_tet[q] = (int32_t)t;
+}
+
+// one thread per merged piece
+__global__ void k_merge_pieces(int64_t T, int64_t n_new, const int32_t* __restrict__ dpos,
+                               MergeSrc o, MergeSrc n, MergeDst D, int64_t n_inc_new) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q == 0) D.p_inc_off[n_new] = (int32_t)n_inc_new;
+  if (q >= n_new) return;
+  const int64_t t = seg_of(D.p_off, T, q);
+  const int d = dpos[t];
+  const MergeSrc& s = d >= 0 ? n : o;
+  const int64_t k = d >= 0 ? d : t;
+  const int p0 = s.p_off[k];
+  const int sp = p0 + (int)(q - D.p_off[t]);
+  D.p_sphere[q] = s.p_sphere[sp];
+  D.p_vol[q] = s.p_vol[sp];
+  D.p_m1[3 * q + 0] = s.p_m1[3 * sp + 0];
+  D.p_m1[3 * q + 1] = s.p_m1[3 * sp + 1];
+  D.p_m1[3 * q + 2] = s.p_m1[3 * sp + 2];
+  D.p_fm[q] = s.p_fm[sp];
+  D.p_inc_off[q] = D.i_tet[t] + (s.p_inc_off[sp] - s.p_inc_off[p0]);
+  D.src_piece[q] = sp + (d >= 0 ? (1 << 30) : 0);
+}
+
+// one thread per merged incidence
+__global__ void k_merge_incs(int64_t n_pieces_new, int64_t n_inc_new, MergeSrc o, MergeSrc n,
+                             MergeDst D) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_inc_new) return;
+  const int64_t q = seg_of(D.p_inc_off, n_pieces_new, r);
+  const int code = D.src_piece[q];
+  const MergeSrc& s = code >= (1 << 30) ? n : o;
+  const int sp = code & ((1 << 30) - 1);
+  D.p_inc[r] = s.p_inc[s.p_inc_off[sp] + (r - D.p_inc_off[q])];
 }
 
 static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
@@ -178,16 +204,23 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
     if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>() + T, pn.off.as<int32_t>(), T))) return e;
     return launch_scan_i32(c, c->m_cnt.as<int32_t>() + 2 * T, c->m_off.as<int32_t>(), T);
   }
+  cudaError_t e = c->m_src.ensure(sizeof(int32_t) * (pn.n_pieces > 0 ? pn.n_pieces : 1));
+  if (e) return e;
   MergeDst D{cn.off.as<int32_t>(),     pn.off.as<int32_t>(),    c->m_off.as<int32_t>(),
              cn.idx.as<int32_t>(),     cn.pair_tet.as<int32_t>(), pn.sphere.as<int32_t>(),
              pn.inc_off.as<int32_t>(), pn.inc.as<int32_t>(),     pn.vol.as<double>(),
-             pn.m1.as<double>(),       pn.fm.as<uint8_t>()};
-  if (T > 0) {
-    k_merge_copy<<<nblk(T, 128), 128, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D,
-                                                      pn.n_pieces, pn.n_inc);
+             pn.m1.as<double>(),       pn.fm.as<uint8_t>(),     c->m_src.as<int32_t>()};
+  if (cn.n > 0) {
+    k_merge_cands<<<nblk(cn.n, 256), 256, 0, c->stream>>>(T, cn.n, c->d_pos.as<int32_t>(), o, n,
+                                                          D);
     ++c->launches;
-  } else {
-    cudaMemsetAsync(pn.inc_off.p, 0, sizeof(int32_t), c->stream);
+  }
+  k_merge_pieces<<<nblk(pn.n_pieces > 0 ? pn.n_pieces : 1, 256), 256, 0, c->stream>>>(
+      T, pn.n_pieces, c->d_pos.as<int32_t>(), o, n, D, pn.n_inc);
+  ++c->launches;
+  if (pn.n_inc > 0) {
+    k_merge_incs<<<nblk(pn.n_inc, 256), 256, 0, c->stream>>>(pn.n_pieces, pn.n_inc, o, n, D);
+    ++c->launches;
   }
   return cudaGetLastError();
 }
