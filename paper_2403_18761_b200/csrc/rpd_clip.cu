@@ -44,6 +44,7 @@ struct WarpState {
   double g[MAXP][4];       // barycentric plane vectors (exact integers)
   double K[2][MAXV][4];    // homogeneous vertices (double-buffered vertex table)
   double F[2][MAXV];       // error scalars
+  double KM[2][MAXV];      // max |K_m| of every vertex
   double x[MAXV][3];       // final vertex coordinates (lattice units, relative to V0)
   double V[4][3];          // tet corners (lattice units)
   double val[MAXV];        // plane value g_s . K of every vertex in the current sign pass
@@ -72,6 +73,18 @@ __device__ __forceinline__ unsigned tri_pack(int a, int b, int c) {
 
 // neighbours of the 4 tet corners across their dual edges (CORNER_TRI orientation)
 __constant__ unsigned char CORNER_NB[4][3] = {{2, 1, 3}, {3, 0, 2}, {1, 0, 3}, {2, 0, 1}};
+
+// max(|a|, |b|) of doubles through their bit patterns (no FP64 min/max instructions)
+__device__ __forceinline__ double absmax(double a, double b) {
+  const long long x = __double_as_longlong(a) & 0x7fffffffffffffffll;
+  const long long y = __double_as_longlong(b) & 0x7fffffffffffffffll;
+  return __longlong_as_double(x > y ? x : y);
+}
+// 2^-e with 2^(e-1) <= m < 2^e for a normal m > 0 (so m * scale is in [0.5, 1))
+__device__ __forceinline__ double inv_pow2_ceil(double m) {
+  const long long ex = ((__double_as_longlong(m) >> 52) & 0x7ff) - 1022;
+  return __longlong_as_double((1023 - ex) << 52);
+}
 
 template <int W>
 struct Bits {
@@ -179,7 +192,8 @@ __device__ __noinline__ void exact_vertex_of(const WarpState<GW, VPL>& S, const 
 // scalar F such that |g . K~ - g . K| <= |g|_1 F for every plane vector g.
 template <int GW, int VPL>
 __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const ClipCtx& C, int a,
-                                          int b, int c, double K[4], double* F, int* nexact) {
+                                          int b, int c, double K[4], double* F, double* KMo,
+                                          int* nexact) {
   const double* ra = S.g[a];
   const double* rb = S.g[b];
   const double* rc = S.g[c];
@@ -198,8 +212,8 @@ __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const Cli
     double p2 = fabs(rb[c0] * rc[c1]) + fabs(rb[c1] * rc[c0]);
     double perm = fabs(ra[c0]) * p0 + fabs(ra[c1]) * p1 + fabs(ra[c2]) * p2;
     K[m] = (m & 1) ? d : -d;  // (-1)^(3+m)
-    E = fmax(E, perm);
-    Kmax = fmax(Kmax, fabs(d));
+    E = absmax(E, perm);
+    Kmax = absmax(Kmax, d);
     sum += K[m];
     sabs += fabs(K[m]);
   }
@@ -209,8 +223,9 @@ __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const Cli
   if (!(fabs(sum) > sb)) {
     exact_vertex_of(S, C, a, b, c, K);  // normalised, each component within 2^-52 relative
     ++*nexact;
-    double km = fmax(fmax(fabs(K[0]), fabs(K[1])), fmax(fabs(K[2]), fabs(K[3])));
+    const double km = absmax(absmax(K[0], K[1]), absmax(K[2], K[3]));
     *F = 9.0 * U * km * (1.0 + 1e-9);
+    *KMo = km;
     return;
   }
   if (sum < 0.0) {
@@ -218,6 +233,7 @@ __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const Cli
     for (int m = 0; m < 4; ++m) K[m] = -K[m];
   }
   *F = (E + 5.0 * U * Kmax) * (1.0 + 1e-9);
+  *KMo = Kmax;
 }
 
 // New vertex on the edge from the kept vertex u to the removed vertex v where plane s
@@ -227,36 +243,31 @@ __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const Cli
 // sign came from the exact path or the bound is too loose.
 template <int GW, int VPL>
 __device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, int cur, int u,
-                                  int v, int x, int y, int sid, double sabs, double K[4],
-                                  double* F, int* nexact) {
+                                 int v, int x, int y, int sid, double sabs, double K[4],
+                                 double* F, double* KMo, int* nexact) {
   if (!S.vx[u] && !S.vx[v]) {
     const double vu = S.val[u], avv = -S.val[v];  // vu > B_u > 0, -val_v > B_v > 0
     const double* Ku = S.K[cur][u];
     const double* Kv = S.K[cur][v];
     const double Fu = S.F[cur][u], Fv = S.F[cur][v];
-    double ku = 0.0, kv = 0.0, km = 0.0;
+    const double ku = S.KM[cur][u], kv = S.KM[cur][v];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      ku = fmax(ku, fabs(Ku[m]));
-      kv = fmax(kv, fabs(Kv[m]));
-      K[m] = fma(vu, Kv[m], avv * Ku[m]);
-      km = fmax(km, fabs(K[m]));
-    }
+    for (int m = 0; m < 4; ++m) K[m] = fma(vu, Kv[m], avv * Ku[m]);
+    const double km = absmax(absmax(K[0], K[1]), absmax(K[2], K[3]));
     const double Bu = sabs * Fu, Bv = sabs * Fv;
     const double E = Bu * kv + (vu + Bu) * Fv + Bv * ku + (avv + Bv) * Fu +
                      3.0 * U * (vu * kv + avv * ku);
     const double Fn = (E + 5.0 * U * km) * (1.0 + 1e-9);
-    if (Fn <= 1e-6 * km && km > 0.0) {
-      int ex;
-      frexp(km, &ex);
-      const double sc = ldexp(1.0, -ex);  // exact power-of-two rescale
+    if (Fn <= 1e-6 * km && km > 1e-300) {
+      const double sc = inv_pow2_ceil(km);  // exact power-of-two rescale to [0.5, 1)
 #pragma unroll
       for (int m = 0; m < 4; ++m) K[m] *= sc;
       *F = Fn * sc;
+      *KMo = km * sc;
       return 0;
     }
   }
-  vertex_from_planes(S, C, x, y, sid, K, F, nexact);
+  vertex_from_planes(S, C, x, y, sid, K, F, KMo, nexact);
   return 1;
 }
 
@@ -316,6 +327,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
       S.src[lane] = -1 - lane;
       S.eidx[lane] = -1;
       S.F[0][lane] = 0.0;
+      S.KM[0][lane] = 1.0;
       S.tri[0][lane] = CORNER_TRI[lane];
 #pragma unroll
       for (int r = 0; r < 3; ++r) S.nb[0][lane][r] = CORNER_NB[lane][r];
@@ -477,6 +489,7 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
 #pragma unroll
             for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = S.K[cur][v][m];
             S.F[nxt][q] = S.F[cur][v];
+            S.KM[nxt][q] = S.KM[cur][v];
             S.tri[nxt][q] = S.tri[cur][v];
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
@@ -492,11 +505,12 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
               if (!((posm[u / GW] >> (u % GW)) & 1u)) continue;
               const int q = nkept + new_idx[k] + j++;
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
-              double K[4], F;
-              d_fb += new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &n_exact);
+              double K[4], F, KMv;
+              d_fb += new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
 #pragma unroll
               for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
               S.F[nxt][q] = F;
+              S.KM[nxt][q] = KMv;
               S.tri[nxt][q] = tri_pack(x, y, sid);
               const int mu = S.map[u];
               S.nb[nxt][q][0] = (unsigned char)mu;
@@ -644,10 +658,10 @@ __global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB 
         // coordinates need |dx| <= 1.5e-11 diam(t): 15 F / sum <= 1.5e-11;
         // edge-interpolated vertices that miss it are rebuilt from their planes, then exactly
         if (16.0 * S.F[cur][v] > 1e-12 * sum) {
-          double F2;
+          double F2, KM2;
           int dummy = 0;
           vertex_from_planes(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1),
-                             tri_at(mytri[k], 2), K, &F2, &dummy);
+                             tri_at(mytri[k], 2), K, &F2, &KM2, &dummy);
           sum = K[0] + K[1] + K[2] + K[3];
           if (16.0 * F2 > 1e-12 * sum) {
             exact_vertex_of(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1), tri_at(mytri[k], 2),
