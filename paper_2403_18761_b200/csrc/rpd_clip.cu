@@ -31,6 +31,9 @@
 #ifndef RPD_CLIP_GW
 #define RPD_CLIP_GW 16   // lanes per pair in the fast kernel (2 pairs per warp)
 #endif
+#ifndef RPD_CLIP_VPL
+#define RPD_CLIP_VPL 1   // vertex slots per lane in the fast kernel
+#endif
 #ifndef RPD_CLIP_MINB
 #define RPD_CLIP_MINB 2  // min resident 256-thread blocks per SM for the fast kernel
 #endif
@@ -285,7 +288,7 @@ struct PairOut {
 };
 
 template <int GW, int VPL>
-__global__ void __launch_bounds__(VPL == 1 ? 256 : 64, VPL == 1 ? RPD_CLIP_MINB : 1) k_clip(
+__global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB : 1) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
     const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ nbr_off,
@@ -815,7 +818,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
                                  bool collect_overflow, const int32_t* n_dev) {
-  constexpr int THREADS = VPL == 1 ? 256 : 64;
+  constexpr int THREADS = VPL <= 2 ? 256 : 64;
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
   cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,
@@ -852,8 +855,8 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
   if (wide)
     return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, false,
                                 nullptr);
-  return launch_clip_t<RPD_CLIP_GW, 1>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff,
-                                       true, nullptr);
+  return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                  cand_idx, moff, true, nullptr);
 }
 
 // wide kernel over the overflow list p_over[1 .. p_over[0]] (count read on the device)
