@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     atomicAdd(stats + ST_CLIP_TESTS, (unsigned long long)c_tests);
     atomicAdd(stats + ST_CLIP_CONSTR, (unsigned long long)c_constr);
     atomicAdd(stats + ST_CLIP_FAN, (unsigned long long)c_fan);
-    if (n_over && VPL > 1) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
+    if (n_over && !out.over_list) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
     atomicMax(stats + ST_MAXV, (unsigned long long)max_v);
     atomicMax(stats + ST_MAXP, (unsigned long long)max_p);
   }
