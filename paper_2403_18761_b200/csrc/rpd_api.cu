@@ -139,7 +139,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
-                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src};
+                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src, &c->c_scan, &c->c_list,
+                    &c->st.chg};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -235,8 +236,16 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
 }
 
 // Alg. 1 over tets (tet_ids, or all ctx tets when NULL) x spheres [lo, hi) -> candidate set
+// restricted re-filter of dirty tets (partial update, pruned mode): only the spheres of
+// `list` (changed rows) are traversed, the old candidates with unchanged rows are kept
+struct Restrict {
+  const int32_t* list;
+  int n_list;
+  const CandSet* old;
+};
+
 static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int lo,
-                             int hi, CandSet& cs, bool timed) {
+                             int hi, CandSet& cs, bool timed, const Restrict* rs = nullptr) {
   Readback* rb = (Readback*)c->pinned;
   size_t nt = n_tets > 0 ? n_tets : 1;
   CK(c->k_tet.ensure(sizeof(int32_t) * nt), "alloc");
@@ -250,8 +259,19 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
     CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
                        sizeof(unsigned long long) * 3, c->stream), "memset");
     if (timed && c->profile) cudaEventRecord(c->ev[0], c->stream);
-    CK(launch_filter(c, tet_ids, n_tets, cap, lo, hi, c->k_tet.as<int32_t>(),
-                     c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
+    if (rs) {
+      CK(launch_filter(c, tet_ids, n_tets, cap, 0, rs->n_list, c->k_tet.as<int32_t>(),
+                       c->slab.as<int32_t>(), c->k_words.as<int32_t>(), rs->list), "filter");
+      CK(launch_keep_old(c, tet_ids, n_tets, *rs->old, cap, c->k_tet.as<int32_t>(),
+                         c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "keep old");
+      // the all-pairs kernel counted its own max; the BVH path recomputes it
+      CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
+                         sizeof(unsigned long long), c->stream), "memset");
+      CK(launch_max_ktet(c, n_tets, c->k_tet.as<int32_t>()), "max k");
+    } else {
+      CK(launch_filter(c, tet_ids, n_tets, cap, lo, hi, c->k_tet.as<int32_t>(),
+                       c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
+    }
     if (timed && c->profile) cudaEventRecord(c->ev[1], c->stream);
     CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), cs.off.as<int32_t>(), n_tets), "scan");
     CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), n_tets), "scan");
@@ -264,7 +284,7 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
     CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
        "readback");
     rb->i32[2] = 0;
-    if (c->filter_mode == RPD_FILTER_PRUNED && hi > lo && n_tets > 0)
+    if (c->filter_mode == RPD_FILTER_PRUNED && (rs ? rs->n_list > 0 : hi > lo) && n_tets > 0)
       CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
                          c->stream), "readback");
     CK(cudaStreamSynchronize(c->stream), "filter");
@@ -504,8 +524,13 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
                    nullptr), "dirty filter");
   if (c->profile) cudaEventRecord(c->ev[1], c->stream);
   CK(launch_dirty_list(c, T), "dirty list");
+  CK(c->c_scan.ensure(sizeof(int32_t) * (N_new + 1)), "alloc");
+  CK(c->c_list.ensure(sizeof(int32_t) * (N_new > 0 ? N_new : 1)), "alloc");
+  CK(launch_changed_list(c, N_new), "changed rows");
   Readback* rb = (Readback*)c->pinned;
   CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[4], c->c_scan.as<int32_t>() + N_new, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
      "readback");
@@ -531,6 +556,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     return check_err(c, rb);
   }
   const int64_t nd = rb->i32[0];
+  const int n_chg = rb->i32[4];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
   c->last.pairs_tested += c->filter_mode == RPD_FILTER_PRUNED ? (int64_t)rb->u64[ST_TESTED]
                                                               : T * M;
@@ -542,7 +568,12 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   const int32_t* dl = c->d_list.as<int32_t>();
 
   // (2) re-candidate the dirty tets against all spheres, (3) clip them
-  s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
+  if (c->filter_mode == RPD_FILTER_PRUNED) {
+    Restrict rs{c->c_list.as<int32_t>(), n_chg, &c->cand[c->cur]};
+    s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true, &rs);
+  } else {
+    s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
+  }
   if (s) return s;
   s = run_clip(c, c->cand_d, dl, c->pcs_d);
   if (s) return s;

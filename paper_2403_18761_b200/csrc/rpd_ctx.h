@@ -76,6 +76,7 @@ struct Stage {
   DevBuf planes;   // double4 per CSR entry: (n, d) of h_ij
   DevBuf twin;     // int32 per CSR entry: next entry of the row with the same oriented plane
   DevBuf hkey;     // uint64 per CSR entry: hash of the canonical plane (twin search)
+  DevBuf chg;      // uint8 per sphere: 1 if its row was (re)built by the last staging
   // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
   DevBuf old_off, old_idx, old_planes, old_twin, old_hkey;
   int64_t T = 0, N = 0, V = 0, E = 0;
@@ -134,6 +135,7 @@ struct rpd_ctx {
 
   // partial update scratch
   rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off, m_src;
+  rpd::DevBuf c_scan, c_list;  // changed-row spheres of a partial update (scan, list)
   int64_t n_dirty = 0;
 
   rpd_stats last{};
@@ -155,7 +157,13 @@ cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
-                          int32_t* k_words);
+                          int32_t* k_words, const int32_t* sphere_list = nullptr);
+// dirty tets: keep the old candidates whose neighbour row did not change (same booleans)
+cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
+                            const CandSet& co, int cap, int32_t* k_tet, int32_t* slab,
+                            int32_t* k_words);
+cudaError_t launch_changed_list(rpd_ctx* c, int64_t N);
+cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet);
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* k_tet,
                                  int32_t* slab, const int32_t* cand_off,
                                  int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,

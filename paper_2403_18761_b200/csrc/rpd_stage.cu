@@ -113,7 +113,8 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
-                             unsigned long long* __restrict__ hkey, OldRows old, int* err) {
+                             unsigned long long* __restrict__ hkey, uint8_t* __restrict__ chg,
+                             OldRows old, int* err) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
@@ -133,11 +134,13 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   for (int32_t e = e0 + lane; e + 1 < e1; e += 32) sorted &= idx_in[e] < idx_in[e + 1];
   sorted = __all_sync(FULL, sorted);
   // unchanged row of an old sphere: copy the previous stage
-  if (old.off && i < old.N && sorted) {
+  // (empty rows are never reused: their Alg. 1 boolean depends on N, R4)
+  if (old.off && i < old.N && sorted && k > 0) {
     const int32_t o0 = old.off[i], o1 = old.off[i + 1];
     bool same = (o1 - o0) == k;
     for (int32_t q = lane; same && q < k; q += 32) same = old.idx[o0 + q] == idx_in[e0 + q];
     if (__all_sync(FULL, same)) {
+      if (lane == 0) chg[i] = 0;
       for (int32_t q = lane; q < k; q += 32) {
         idx_out[e0 + q] = old.idx[o0 + q];
         planes[e0 + q] = old.planes[o0 + q];
@@ -148,6 +151,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
       return;
     }
   }
+  if (lane == 0) chg[i] = 1;
   bool bad = false;
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const int32_t j = idx_in[e];
@@ -261,6 +265,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
   if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
+  if ((e = s.chg.ensure(N > 0 ? N : 1))) return e;
   OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (reuse_rows && s.old_off.p)
     old = OldRows{s.old_off.as<int32_t>(),  s.old_idx.as<int32_t>(),
@@ -275,7 +280,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
     k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
-        s.hkey.as<unsigned long long>(), old, err);
+        s.hkey.as<unsigned long long>(), s.chg.as<uint8_t>(), old, err);
     ++c->launches;
   } else {
     e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
