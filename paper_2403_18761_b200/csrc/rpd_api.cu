@@ -140,7 +140,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src, &c->c_scan, &c->c_list,
-                    &c->st.chg};
+                    &c->st.chg, &c->st.htab};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {

@@ -77,6 +77,7 @@ struct Stage {
   DevBuf twin;     // int32 per CSR entry: next entry of the row with the same oriented plane
   DevBuf hkey;     // uint64 per CSR entry: hash of the canonical plane (twin search)
   DevBuf chg;      // uint8 per sphere: 1 if its row was (re)built by the last staging
+  DevBuf htab;     // uint64 scratch: per-row hash tables of the twin search
   // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
   DevBuf old_off, old_idx, old_planes, old_twin, old_hkey;
   int64_t T = 0, N = 0, V = 0, E = 0;

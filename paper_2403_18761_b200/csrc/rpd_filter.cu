@@ -161,47 +161,29 @@ __global__ void k_super_boxes(const double* __restrict__ leaf, int64_t n_leaf,
   }
 }
 
-// Can some tet inside the lane's box B pass every plane of the sphere?  (exact, conservative)
-// Warp-cooperative: planes beyond the first BVH_PCAP are staged into shared memory chunk by
-// chunk (never read one by one from global memory); staged = first plane currently in sp.
+// Can some tet inside the lane's box B pass the first min(k, BVH_PCAP) planes of the sphere?
+// (exact and conservative: passing a subset of the planes is necessary for passing all; the
+// leaf kernel checks every plane).  The planes are staged in shared memory once per sphere.
 __device__ __forceinline__ bool box_passes_w(const double* __restrict__ B, bool valid,
-                                             double4* __restrict__ sp,
-                                             const double4* __restrict__ gp, int k,
-                                             int& staged) {
-  const unsigned FULL = 0xffffffffu;
+                                             const double4* __restrict__ sp, int k) {
+  if (!valid) return false;
+  const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
+  const int ce = min(k, BVH_PCAP);
+  for (int e = 0; e < ce; ++e) {
+    const double4 p = sp[e];
+    const double mh =
+        p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) + fmax(p.z * l2, p.z * h2);
+    if (!pos(mh)) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void stage_planes(double4* __restrict__ sp,
+                                             const double4* __restrict__ gp, int k) {
   const int lane = threadIdx.x & 31;
-  double l0 = 0, l1 = 0, l2 = 0, h0 = 0, h1 = 0, h2 = 0;
-  if (valid) {
-    l0 = B[0];
-    l1 = B[1];
-    l2 = B[2];
-    h0 = B[3];
-    h1 = B[4];
-    h2 = B[5];
-  }
-  bool alive = valid;
-  for (int c0 = 0; c0 < k; c0 += BVH_PCAP) {
-    if (!__any_sync(FULL, alive)) break;
-    if (staged != c0) {
-      __syncwarp();
-      for (int e = lane; e < BVH_PCAP && c0 + e < k; e += 32) sp[e] = gp[c0 + e];
-      __syncwarp();
-      staged = c0;
-    }
-    const int ce = min(k - c0, BVH_PCAP);
-    if (alive) {
-      for (int e = 0; e < ce; ++e) {
-        const double4 p = sp[e];
-        const double mh = p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) +
-                          fmax(p.z * l2, p.z * h2);
-        if (!pos(mh)) {
-          alive = false;
-          break;
-        }
-      }
-    }
-  }
-  return alive;
+  __syncwarp();
+  for (int e = lane; e < BVH_PCAP && e < k; e += 32) sp[e] = gp[e];
+  __syncwarp();
 }
 
 constexpr int BVH_WARPS = 4;
@@ -224,10 +206,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
     const int k = e1 - e0;
     if (k == 0 && N != 1) continue;  // hidden sphere (R4): relates to no tet
     const double4* gp = planes + e0;
-    int staged = -1;
+    stage_planes(sp, gp, k);
     for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
       const int64_t s = s0 + lane;
-      const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, gp, k, staged);
+      const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, k);
       const unsigned sm = __ballot_sync(FULL, ok);
       if (!sm) continue;
       int base = 0;
@@ -258,7 +240,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
   const int n_items = min(*n_items_p, cap_items);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int cur_i = -1, staged = -1;
+  int cur_i = -1;
   for (int64_t it = gw; it < n_items; it += nw) {
     const int2 item = items[it];
     const int i = item.x;
@@ -267,22 +249,28 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const int k = e1 - e0;
     const double4* gp = planes + e0;
     if (i != cur_i) {
-      staged = -1;
+      stage_planes(sp, gp, k);
       cur_i = i;
     }
     const int words = (k + 31) >> 5;
     const int64_t l = sl * BVH_FAN + lane;
-    unsigned lm = __ballot_sync(FULL, box_passes_w(leaf + 6 * l, l < n_leaf, sp, gp, k, staged));
-    // the per-tet tests below read planes < BVH_PCAP from shared memory: restage chunk 0
-    if (staged != 0 && lm) {
-      __syncwarp();
-      for (int e = lane; e < BVH_PCAP && e < k; e += 32) sp[e] = gp[e];
-      __syncwarp();
-      staged = 0;
-    }
+    unsigned lm = __ballot_sync(FULL, box_passes_w(leaf + 6 * l, l < n_leaf, sp, k));
     while (lm) {
       const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
       lm &= lm - 1;
+      const double* B = leaf + 6 * ll;
+      const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
+      if (k > BVH_PCAP) {
+        // the box test saw only the first BVH_PCAP planes: check the rest (lane = plane)
+        bool rej = false;
+        for (int ec = BVH_PCAP + lane; ec < k; ec += 32) {
+          const double4 p = gp[ec];
+          const double mx = p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) +
+                            fmax(p.z * l2, p.z * h2);
+          rej |= !pos(mx);
+        }
+        if (__any_sync(FULL, rej)) continue;
+      }
       const int64_t a = ll * BVH_LEAF + lane;
       const bool valid = a < n;
       const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
@@ -295,8 +283,6 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
       }
       // planes with min over the leaf box > 0 hold at every vertex of every tet of the leaf;
       // only the planes crossing the box are tested per tet
-      const double* B = leaf + 6 * ll;
-      const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
       bool alive = valid;
       for (int c0 = 0; c0 < k; c0 += 32) {
         const int ec = c0 + lane;

@@ -114,7 +114,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
                              unsigned long long* __restrict__ hkey, uint8_t* __restrict__ chg,
-                             OldRows old, int* err) {
+                             unsigned long long* __restrict__ htab, OldRows old, int* err) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
@@ -203,23 +203,50 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     hkey[e] = h;
   }
   __syncwarp();
-  // twins: next entry of the row with the same oriented plane (equal keys compared exactly)
+  // twins: next entry of the row with the same oriented plane (equal keys compared exactly).
+  // Long rows first check for a repeated key with a per-row hash table in global scratch
+  // (region [4 e0, 4 e0 + 4k)); without a repeat every entry has no twin.
+  bool maybe = true;
+  if (k > 64) {
+    int tsz = 1;
+    while (tsz < 2 * k) tsz <<= 1;
+    unsigned long long* tab = htab + 4 * (int64_t)e0;
+    for (int q = lane; q < tsz; q += 32) tab[q] = 0ull;
+    __syncwarp();
+    bool dup = false;
+    for (int32_t e = e0 + lane; e < e1; e += 32) {
+      const unsigned long long h = hkey[e] | 1ull;
+      int slot = (int)(h & (unsigned long long)(tsz - 1));
+      while (true) {
+        const unsigned long long prev = atomicCAS(tab + slot, 0ull, h);
+        if (prev == 0ull) break;
+        if (prev == h) {
+          dup = true;
+          break;
+        }
+        slot = (slot + 1) & (tsz - 1);
+      }
+    }
+    maybe = __any_sync(FULL, dup);
+  }
   for (int32_t e = e0 + lane; e < e1; e += 32) {
-    const unsigned long long h = hkey[e];
     int32_t tw = -1;
-    for (int32_t f = e + 1; f < e1 && tw < 0; f += 4) {
-      unsigned long long hf[4];
+    if (maybe) {
+      const unsigned long long h = hkey[e];
+      for (int32_t f = e + 1; f < e1 && tw < 0; f += 4) {
+        unsigned long long hf[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) hf[q] = f + q < e1 ? hkey[f + q] : ~h;
+        for (int q = 0; q < 4; ++q) hf[q] = f + q < e1 ? hkey[f + q] : ~h;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (tw >= 0 || hf[q] != h) continue;
-        const double4 a = planes[e], b = planes[f + q];
-        const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
-                          a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
-                          a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
-        const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
-        if (prop && dot > 0.0) tw = f + q;
+        for (int q = 0; q < 4; ++q) {
+          if (tw >= 0 || hf[q] != h) continue;
+          const double4 a = planes[e], b = planes[f + q];
+          const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
+                            a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
+                            a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
+          const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
+          if (prop && dot > 0.0) tw = f + q;
+        }
       }
     }
     twin[e] = tw;
@@ -266,6 +293,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
   if ((e = s.chg.ensure(N > 0 ? N : 1))) return e;
+  if ((e = s.htab.ensure(sizeof(unsigned long long) * 4 * (E > 0 ? E : 1)))) return e;
   OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (reuse_rows && s.old_off.p)
     old = OldRows{s.old_off.as<int32_t>(),  s.old_idx.as<int32_t>(),
@@ -280,7 +308,8 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
     k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
-        s.hkey.as<unsigned long long>(), s.chg.as<uint8_t>(), old, err);
+        s.hkey.as<unsigned long long>(), s.chg.as<uint8_t>(), s.htab.as<unsigned long long>(),
+        old, err);
     ++c->launches;
   } else {
     e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
