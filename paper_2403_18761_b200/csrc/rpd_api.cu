@@ -140,7 +140,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src, &c->c_scan, &c->c_list,
-                    &c->st.chg, &c->st.htab};
+                    &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
+                    &c->min_epoch};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -221,7 +222,7 @@ static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t*
 
 static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                 const int32_t* nbr_off, const int32_t* nbr_idx,
-                                bool reuse_rows) {
+                                bool reuse_rows, int epoch) {
   int64_t E = 0;
   rpd_status s = read_E(c, nbr_off, N, &E);
   if (s) return s;
@@ -231,7 +232,7 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   CK(resolve(c, spheres, 4 * N, c->h_spheres, &d_sph), "stage spheres");
   CK(resolve(c, nbr_off, N > 0 ? N + 1 : 0, c->h_off, &d_off), "stage nbr_off");
   CK(resolve(c, nbr_idx, E, c->h_idx, &d_idx), "stage nbr_idx");
-  CK(launch_stage_spheres(c, d_sph, N, d_off, d_idx, E, reuse_rows), "stage spheres");
+  CK(launch_stage_spheres(c, d_sph, N, d_off, d_idx, E, reuse_rows, epoch), "stage spheres");
   return RPD_OK;
 }
 
@@ -240,7 +241,8 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
 // `list` (changed rows) are traversed, the old candidates with unchanged rows are kept
 struct Restrict {
   const int32_t* list;
-  int n_list;
+  const int* n_list_dev;  // device count of `list`
+  int n_list_max;         // host upper bound
   const CandSet* old;
 };
 
@@ -260,8 +262,9 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                        sizeof(unsigned long long) * 3, c->stream), "memset");
     if (timed && c->profile) cudaEventRecord(c->ev[0], c->stream);
     if (rs) {
-      CK(launch_filter(c, tet_ids, n_tets, cap, 0, rs->n_list, c->k_tet.as<int32_t>(),
-                       c->slab.as<int32_t>(), c->k_words.as<int32_t>(), rs->list), "filter");
+      CK(launch_filter(c, tet_ids, n_tets, cap, 0, rs->n_list_max, c->k_tet.as<int32_t>(),
+                       c->slab.as<int32_t>(), c->k_words.as<int32_t>(), rs->list,
+                       rs->n_list_dev), "filter");
       CK(launch_keep_old(c, tet_ids, n_tets, *rs->old, cap, c->k_tet.as<int32_t>(),
                          c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "keep old");
       // the all-pairs kernel counted its own max; the BVH path recomputes it
@@ -284,7 +287,7 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
     CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
        "readback");
     rb->i32[2] = 0;
-    if (c->filter_mode == RPD_FILTER_PRUNED && (rs ? rs->n_list > 0 : hi > lo) && n_tets > 0)
+    if (c->filter_mode == RPD_FILTER_PRUNED && (rs ? rs->n_list_max > 0 : hi > lo) && n_tets > 0)
       CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
                          c->stream), "readback");
     CK(cudaStreamSynchronize(c->stream), "filter");
@@ -450,8 +453,11 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_stage_mesh(c, d_verts, V, d_tets, T), "stage mesh");
-  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx, false);
+  c->epoch = 0;
+  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx, false, 0);
   if (s) return s;
+  CK(c->cepoch.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
+  CK(cudaMemsetAsync(c->cepoch.p, 0, sizeof(int32_t) * (T > 0 ? T : 1), c->stream), "memset");
   reset_last(c);
   c->cur = 0;
   CandSet& cs = c->cand[0];
@@ -510,7 +516,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
-  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, true);
+  ++c->epoch;
+  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, true, c->epoch);
   if (s) return s;
   c->last.N = N_new;
 
@@ -523,14 +530,14 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(), nullptr,
                    nullptr), "dirty filter");
   if (c->profile) cudaEventRecord(c->ev[1], c->stream);
+  CK(c->min_epoch.ensure(sizeof(int)), "alloc");
   CK(launch_dirty_list(c, T), "dirty list");
+  CK(c->c_flag.ensure(N_new > 0 ? N_new : 1), "alloc");
   CK(c->c_scan.ensure(sizeof(int32_t) * (N_new + 1)), "alloc");
   CK(c->c_list.ensure(sizeof(int32_t) * (N_new > 0 ? N_new : 1)), "alloc");
   CK(launch_changed_list(c, N_new), "changed rows");
   Readback* rb = (Readback*)c->pinned;
   CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[4], c->c_scan.as<int32_t>() + N_new, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
      "readback");
@@ -556,7 +563,6 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     return check_err(c, rb);
   }
   const int64_t nd = rb->i32[0];
-  const int n_chg = rb->i32[4];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
   c->last.pairs_tested += c->filter_mode == RPD_FILTER_PRUNED ? (int64_t)rb->u64[ST_TESTED]
                                                               : T * M;
@@ -569,7 +575,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
 
   // (2) re-candidate the dirty tets against all spheres, (3) clip them
   if (c->filter_mode == RPD_FILTER_PRUNED) {
-    Restrict rs{c->c_list.as<int32_t>(), n_chg, &c->cand[c->cur]};
+    Restrict rs{c->c_list.as<int32_t>(), c->c_scan.as<int>() + N_new, (int)N_new,
+                &c->cand[c->cur]};
     s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true, &rs);
   } else {
     s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);

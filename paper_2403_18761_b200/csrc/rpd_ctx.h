@@ -76,10 +76,10 @@ struct Stage {
   DevBuf planes;   // double4 per CSR entry: (n, d) of h_ij
   DevBuf twin;     // int32 per CSR entry: next entry of the row with the same oriented plane
   DevBuf hkey;     // uint64 per CSR entry: hash of the canonical plane (twin search)
-  DevBuf chg;      // uint8 per sphere: 1 if its row was (re)built by the last staging
+  DevBuf repoch;   // int32 per sphere: epoch (update index) at which its row was last built
   DevBuf htab;     // uint64 scratch: per-row hash tables of the twin search
   // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
-  DevBuf old_off, old_idx, old_planes, old_twin, old_hkey;
+  DevBuf old_off, old_idx, old_planes, old_twin, old_hkey, old_repoch;
   int64_t T = 0, N = 0, V = 0, E = 0;
 };
 
@@ -136,7 +136,10 @@ struct rpd_ctx {
 
   // partial update scratch
   rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off, m_src;
-  rpd::DevBuf c_scan, c_list;  // changed-row spheres of a partial update (scan, list)
+  rpd::DevBuf c_flag, c_scan, c_list;  // changed-row spheres of a partial update
+  rpd::DevBuf cepoch;          // int32 per tet: epoch of its candidate list
+  rpd::DevBuf min_epoch;       // int32: oldest candidate-list epoch among the dirty tets
+  int epoch = 0;               // 0 after rpd_relations, +1 per partial update
   int64_t n_dirty = 0;
 
   rpd_stats last{};
@@ -153,16 +156,18 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
                               int64_t T);
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                  const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
-                                 bool reuse_rows);
+                                 bool reuse_rows, int epoch);
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
-                          int32_t* k_words, const int32_t* sphere_list = nullptr);
+                          int32_t* k_words, const int32_t* sphere_list = nullptr,
+                          const int* n_list_dev = nullptr);
 // dirty tets: keep the old candidates whose neighbour row did not change (same booleans)
 cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
                             const CandSet& co, int cap, int32_t* k_tet, int32_t* slab,
                             int32_t* k_words);
+// spheres whose rows were rebuilt after the oldest candidate list of the dirty tets
 cudaError_t launch_changed_list(rpd_ctx* c, int64_t N);
 cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet);
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* k_tet,

@@ -193,7 +193,9 @@ constexpr int BVH_WARPS = 4;
 __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
     const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
-    int cap_items, int* __restrict__ n_items, const int32_t* __restrict__ list) {
+    int cap_items, int* __restrict__ n_items, const int32_t* __restrict__ list,
+    const int* __restrict__ n_list_dev) {
+  if (n_list_dev) hi = lo + *n_list_dev;
   __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -380,15 +382,17 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 // depends on t and N(i), so the boolean is the same as before (R11).
 __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
                            const int32_t* __restrict__ co_off, const int32_t* __restrict__ co_idx,
-                           const uint8_t* __restrict__ chg, const int32_t* __restrict__ nbr_off,
-                           int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
+                           const int32_t* __restrict__ repoch, const int* __restrict__ min_epoch,
+                           const int32_t* __restrict__ nbr_off, int cap,
+                           int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
                            int32_t* __restrict__ k_words) {
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   const int t = dirty[a];
+  const int me = *min_epoch;
   for (int q = co_off[t]; q < co_off[t + 1]; ++q) {
     const int i = co_idx[q];
-    if (chg[i]) continue;
+    if (repoch[i] > me) continue;  // re-tested by the traversal
     const int slot = atomicAdd(k_tet + a, 1);
     if (slot < cap) slab[a * cap + slot] = i;
     atomicAdd(k_words + a, (nbr_off[i + 1] - nbr_off[i] + 31) >> 5);
@@ -400,16 +404,22 @@ cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
                             int32_t* k_words) {
   if (n_dirty == 0) return cudaSuccess;
   k_keep_old<<<nblk(n_dirty, 256), 256, 0, c->stream>>>(
-      n_dirty, dirty, co.off.as<int32_t>(), co.idx.as<int32_t>(), c->st.chg.as<uint8_t>(),
-      c->st.nbr_off.as<int32_t>(), cap, k_tet, slab, k_words);
+      n_dirty, dirty, co.off.as<int32_t>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
+      c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab, k_words);
   ++c->launches;
   return cudaGetLastError();
 }
 
-__global__ void k_chg_list(int64_t N, const uint8_t* __restrict__ chg,
+__global__ void k_chg_flags(int64_t N, const int32_t* __restrict__ repoch,
+                            const int* __restrict__ min_epoch, uint8_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) flag[i] = repoch[i] > *min_epoch;
+}
+
+__global__ void k_chg_list(int64_t N, const uint8_t* __restrict__ flag,
                            const int32_t* __restrict__ scan, int32_t* __restrict__ list) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N && chg[i]) list[scan[i]] = (int32_t)i;
+  if (i < N && flag[i]) list[scan[i]] = (int32_t)i;
 }
 
 // list of the spheres whose rows changed (count at c_scan[N])
@@ -421,9 +431,15 @@ cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet) {
 }
 
 cudaError_t launch_changed_list(rpd_ctx* c, int64_t N) {
-  cudaError_t e = launch_scan_u8(c, c->st.chg.as<uint8_t>(), c->c_scan.as<int32_t>(), N);
+  if (N > 0) {
+    k_chg_flags<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->st.repoch.as<int32_t>(),
+                                                     c->min_epoch.as<int>(),
+                                                     c->c_flag.as<uint8_t>());
+    ++c->launches;
+  }
+  cudaError_t e = launch_scan_u8(c, c->c_flag.as<uint8_t>(), c->c_scan.as<int32_t>(), N);
   if (e || N == 0) return e;
-  k_chg_list<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->st.chg.as<uint8_t>(),
+  k_chg_list<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->c_flag.as<uint8_t>(),
                                                   c->c_scan.as<int32_t>(),
                                                   c->c_list.as<int32_t>());
   ++c->launches;
@@ -432,7 +448,8 @@ cudaError_t launch_changed_list(rpd_ctx* c, int64_t N) {
 
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
-                          int32_t* k_words, const int32_t* sphere_list) {
+                          int32_t* k_words, const int32_t* sphere_list,
+                          const int* n_list_dev) {
   if (n_tets == 0) return cudaSuccess;
   if (c->filter_mode == RPD_FILTER_PRUNED) {
     const int64_t n_leaf = (n_tets + BVH_LEAF - 1) / BVH_LEAF;
@@ -466,7 +483,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
       k_bvh_super<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
           sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
-          sphere_lo, sphere_hi, items, (int)cap_items, n_items, sphere_list);
+          sphere_lo, sphere_hi, items, (int)cap_items, n_items, sphere_list, n_list_dev);
       k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
           c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,

@@ -32,14 +32,19 @@ __global__ void k_dirty_flag(int64_t T, const int32_t* __restrict__ count,
   if (t < T) flag[t] = count[t] > 0;
 }
 
+// dirty list + position map; the oldest candidate-list epoch among the dirty tets, whose
+// lists are re-stamped with the current epoch
 __global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
                              const int32_t* __restrict__ scan, int32_t* __restrict__ list,
-                             int32_t* __restrict__ pos) {
+                             int32_t* __restrict__ pos, int32_t* __restrict__ cepoch,
+                             int* __restrict__ min_epoch, int epoch) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   if (flag[t]) {
     list[scan[t]] = (int32_t)t;
     pos[t] = scan[t];
+    atomicMin(min_epoch, cepoch[t]);
+    cepoch[t] = epoch;
   } else {
     pos[t] = -1;
   }
@@ -60,10 +65,11 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
   ++c->launches;
   cudaError_t e = launch_scan_u8(c, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), T);
   if (e) return e;
-  k_dirty_list<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_flag.as<uint8_t>(),
-                                                    c->d_scan.as<int32_t>(),
-                                                    c->d_list.as<int32_t>(),
-                                                    c->d_pos.as<int32_t>());
+  e = cudaMemsetAsync(c->min_epoch.p, 0x7f, sizeof(int), c->stream);
+  if (e) return e;
+  k_dirty_list<<<nblk(T, 256), 256, 0, c->stream>>>(
+      T, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), c->d_list.as<int32_t>(),
+      c->d_pos.as<int32_t>(), c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch);
   ++c->launches;
   return cudaGetLastError();
 }

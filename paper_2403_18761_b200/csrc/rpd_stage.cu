@@ -103,6 +103,7 @@ struct OldRows {  // previous staged CSR (partial updates: unchanged rows are co
   const double4* planes;
   const int32_t* twin;
   const unsigned long long* hkey;
+  const int32_t* repoch;
   int64_t N;
 };
 
@@ -113,8 +114,9 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
-                             unsigned long long* __restrict__ hkey, uint8_t* __restrict__ chg,
-                             unsigned long long* __restrict__ htab, OldRows old, int* err) {
+                             unsigned long long* __restrict__ hkey, int32_t* __restrict__ repoch,
+                             int epoch, unsigned long long* __restrict__ htab, OldRows old,
+                             int* err) {
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
@@ -140,7 +142,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     bool same = (o1 - o0) == k;
     for (int32_t q = lane; same && q < k; q += 32) same = old.idx[o0 + q] == idx_in[e0 + q];
     if (__all_sync(FULL, same)) {
-      if (lane == 0) chg[i] = 0;
+      if (lane == 0) repoch[i] = old.repoch[i];
       for (int32_t q = lane; q < k; q += 32) {
         idx_out[e0 + q] = old.idx[o0 + q];
         planes[e0 + q] = old.planes[o0 + q];
@@ -151,7 +153,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
       return;
     }
   }
-  if (lane == 0) chg[i] = 1;
+  if (lane == 0) repoch[i] = epoch;
   bool bad = false;
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     const int32_t j = idx_in[e];
@@ -276,7 +278,7 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
 
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                  const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
-                                 bool reuse_rows) {
+                                 bool reuse_rows, int epoch) {
   Stage& s = c->st;
   cudaError_t e;
   // the previous rows become the "old" buffers (copied for unchanged rows when reuse_rows)
@@ -285,6 +287,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   std::swap(s.planes, s.old_planes);
   std::swap(s.twin, s.old_twin);
   std::swap(s.hkey, s.old_hkey);
+  std::swap(s.repoch, s.old_repoch);
   const int64_t N_old = s.N;
   if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
   if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
@@ -292,13 +295,13 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if ((e = s.planes.ensure(sizeof(double4) * (E > 0 ? E : 1)))) return e;
   if ((e = s.twin.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
-  if ((e = s.chg.ensure(N > 0 ? N : 1))) return e;
+  if ((e = s.repoch.ensure(sizeof(int32_t) * (N > 0 ? N : 1)))) return e;
   if ((e = s.htab.ensure(sizeof(unsigned long long) * 4 * (E > 0 ? E : 1)))) return e;
-  OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (reuse_rows && s.old_off.p)
     old = OldRows{s.old_off.as<int32_t>(),  s.old_idx.as<int32_t>(),
                   s.old_planes.as<double4>(), s.old_twin.as<int32_t>(),
-                  s.old_hkey.as<unsigned long long>(), N_old};
+                  s.old_hkey.as<unsigned long long>(), s.old_repoch.as<int32_t>(), N_old};
   s.N = N;
   s.E = E;
   int* err = c->errw.as<int>();
@@ -308,8 +311,8 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
     k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
-        s.hkey.as<unsigned long long>(), s.chg.as<uint8_t>(), s.htab.as<unsigned long long>(),
-        old, err);
+        s.hkey.as<unsigned long long>(), s.repoch.as<int32_t>(), epoch,
+        s.htab.as<unsigned long long>(), old, err);
     ++c->launches;
   } else {
     e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
