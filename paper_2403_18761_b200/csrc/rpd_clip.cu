@@ -373,9 +373,12 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         // ---- sign of every vertex slot
         int sg[VPL];
         unsigned negm[VPL], posm[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) negm[k] = posm[k] = 0u;
         bool anyneg = false, anypos = false;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv) break;  // slots beyond the vertex count
           const int v = GW * k + lane;
           const bool valid = v < nv;
           sg[k] = 0;
@@ -443,7 +446,10 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         // new vertices around the new facet s.
         int nnew[VPL];
 #pragma unroll
+        for (int k = 0; k < VPL; ++k) nnew[k] = 0;
+#pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv) break;  // slots beyond the vertex count
           const int v = GW * k + lane;
           nnew[k] = 0;
           if (v < nv && sg[k] < 0) {
@@ -459,6 +465,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         int kept_idx[VPL], new_idx[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv) break;  // slots beyond the vertex count
           kept_idx[k] = kept_base + __popc(posm[k] & lt_mask);
           kept_base += __popc(posm[k]);
           int incl = nnew[k];
@@ -479,12 +486,14 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         const int nxt = cur ^ 1;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv) break;  // slots beyond the vertex count
           const int v = GW * k + lane;
           if (v < nv && sg[k] > 0) S.map[v] = (unsigned char)kept_idx[k];
         }
         __syncwarp(FULL);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv) break;  // slots beyond the vertex count
           const int v = GW * k + lane;
           if (v >= nv) continue;
           if (sg[k] > 0) {
@@ -526,6 +535,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         // close the cycle of new vertices around the new facet s
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
+          if (GW * k >= nv2) break;  // slots beyond the vertex count
           const int q = GW * k + lane;
           if (q >= nkept && q < nv2) {
             const unsigned tr = S.tri[nxt][q];
@@ -567,6 +577,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     facets_all.clear();
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
+      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
       mytri[k] = v < nv ? S.tri[cur][v] : 0xffffffu;
       if (v < nv) facets_all.set_tri(mytri[k]);
@@ -595,6 +606,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           bool on = true;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
+            if (GW * k >= nv) break;  // slots beyond the vertex count
             const int v = GW * k + lane;
             if (v < nv && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
               const double* K = S.K[cur][v];
@@ -652,6 +664,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     // lowest vertex of the facet
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
+      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
       if (v < nv) {
         double K[4];
@@ -690,6 +703,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     double vol6 = 0.0, m24[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
+      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
       if (v < nv) {
         const double* xv = S.x[v];

@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
 
 constexpr int BVH_LEAF = 32;    // tets per leaf (one warp)
 constexpr int BVH_FAN = 32;     // leaves per super node
-constexpr int BVH_PCAP = 64;    // planes of a sphere staged in shared memory
+constexpr int BVH_PCAP = 64;    // planes of a sphere staged in shared memory (super level)
+constexpr int BVH_LCAP = 256;   // planes staged per warp in the leaf kernel
 
 // exact lattice AABB of every leaf (32 consecutive tets of the list)
 __global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
@@ -234,10 +235,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const int* __restrict__ n_items_p, int cap_items, int cap, int32_t* __restrict__ k_tet,
     int32_t* __restrict__ slab, int32_t* __restrict__ k_words,
     unsigned long long* __restrict__ stats) {
-  __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
+  extern __shared__ double4 s_lpl[];  // BVH_WARPS x BVH_LCAP planes
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
-  double4* sp = s_pl[warp];
+  double4* sp = s_lpl + warp * BVH_LCAP;
   long long ntests = 0, npairs = 0;
   const int n_items = min(*n_items_p, cap_items);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -251,7 +252,9 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const int k = e1 - e0;
     const double4* gp = planes + e0;
     if (i != cur_i) {
-      stage_planes(sp, gp, k);
+      __syncwarp();
+      for (int e = lane; e < BVH_LCAP && e < k; e += 32) sp[e] = gp[e];
+      __syncwarp();
       cur_i = i;
     }
     const int words = (k + 31) >> 5;
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
         // the box test saw only the first BVH_PCAP planes: check the rest (lane = plane)
         bool rej = false;
         for (int ec = BVH_PCAP + lane; ec < k; ec += 32) {
-          const double4 p = gp[ec];
+          const double4 p = ec < BVH_LCAP ? sp[ec] : gp[ec];
           const double mx = p.w + fmax(p.x * l0, p.x * h0) + fmax(p.y * l1, p.y * h1) +
                             fmax(p.z * l2, p.z * h2);
           rej |= !pos(mx);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
         const int ec = c0 + lane;
         bool crosses = false;
         if (ec < k) {
-          const double4 p = ec < BVH_PCAP ? sp[ec] : gp[ec];
+          const double4 p = ec < BVH_LCAP ? sp[ec] : gp[ec];
           const double mn = p.w + fmin(p.x * l0, p.x * h0) + fmin(p.y * l1, p.y * h1) +
                             fmin(p.z * l2, p.z * h2);
           crosses = !pos(mn);
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
         while (cm) {
           const int e = c0 + __ffs(cm) - 1;
           cm &= cm - 1;
-          const double4 p = e < BVH_PCAP ? sp[e] : gp[e];
+          const double4 p = e < BVH_LCAP ? sp[e] : gp[e];
           bool hk[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -484,7 +487,14 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       k_bvh_super<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
           sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
           sphere_lo, sphere_hi, items, (int)cap_items, n_items, sphere_list, n_list_dev);
-      k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
+      static bool attr_set = false;
+      const int lsmem = (int)(sizeof(double4) * BVH_LCAP * BVH_WARPS);
+      if (!attr_set) {
+        e = cudaFuncSetAttribute(k_bvh_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
+        if (e) return e;
+        attr_set = true;
+      }
+      k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, lsmem, c->stream>>>(
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
           c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,
           (int)cap_items, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
