@@ -192,7 +192,8 @@ constexpr int BVH_WARPS = 4;
 // phase 1: one warp per sphere tests the super-node boxes and queues (sphere, super node)
 // work items (a sphere with a huge cell becomes many items: load balance)
 __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
-    const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
+    const double* __restrict__ sup, int64_t n_sup, const double* __restrict__ leaf,
+    int64_t n_leaf, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
     int cap_items, int* __restrict__ n_items, const int32_t* __restrict__ list,
     const int* __restrict__ n_list_dev) {
@@ -212,15 +213,22 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
     stage_planes(sp, gp, k);
     for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
       const int64_t s = s0 + lane;
-      const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, k);
-      const unsigned sm = __ballot_sync(FULL, ok);
-      if (!sm) continue;
-      int base = 0;
-      if (lane == 0) base = atomicAdd(n_items, __popc(sm));
-      base = __shfl_sync(FULL, base, 0);
-      if (ok) {
-        const int slot = base + __popc(sm & ((1u << lane) - 1u));
-        if (slot < cap_items) items[slot] = make_int2(i, (int)s);
+      unsigned sm = __ballot_sync(FULL, box_passes_w(sup + 6 * s, s < n_sup, sp, k));
+      while (sm) {
+        const int64_t sl = s0 + __ffs(sm) - 1;
+        sm &= sm - 1;
+        // leaves of the surviving super node (lane = leaf) -> (sphere, leaf) work items
+        const int64_t l = sl * BVH_FAN + lane;
+        const bool ok = box_passes_w(leaf + 6 * l, l < n_leaf, sp, k);
+        const unsigned lm = __ballot_sync(FULL, ok);
+        if (!lm) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(n_items, __popc(lm));
+        base = __shfl_sync(FULL, base, 0);
+        if (ok) {
+          const int slot = base + __popc(lm & ((1u << lane) - 1u));
+          if (slot < cap_items) items[slot] = make_int2(i, (int)l);
+        }
       }
     }
   }
@@ -245,9 +253,13 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int cur_i = -1;
   for (int64_t it = gw; it < n_items; it += nw) {
+#ifdef RPD_DEBUG_BVH
+    const long long t_start = clock64();
+    int dbg_leaves = 0, dbg_cross = 0;
+#endif
     const int2 item = items[it];
     const int i = item.x;
-    const int64_t sl = item.y;
+    const int64_t sl = item.y;  // leaf index
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     const int k = e1 - e0;
     const double4* gp = planes + e0;
@@ -258,11 +270,8 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
       cur_i = i;
     }
     const int words = (k + 31) >> 5;
-    const int64_t l = sl * BVH_FAN + lane;
-    unsigned lm = __ballot_sync(FULL, box_passes_w(leaf + 6 * l, l < n_leaf, sp, k));
-    while (lm) {
-      const int64_t ll = sl * BVH_FAN + __ffs(lm) - 1;
-      lm &= lm - 1;
+    {
+      const int64_t ll = sl;  // the item's leaf (its box passed the first planes)
       const double* B = leaf + 6 * ll;
       const double l0 = B[0], l1 = B[1], l2 = B[2], h0 = B[3], h1 = B[4], h2 = B[5];
       if (k > BVH_PCAP) {
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
                             fmax(p.z * l2, p.z * h2);
           rej |= !pos(mx);
         }
-        if (__any_sync(FULL, rej)) continue;
+        if (__any_sync(FULL, rej)) continue;  // next item
       }
       const int64_t a = ll * BVH_LEAF + lane;
       const bool valid = a < n;
@@ -299,6 +308,9 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
           crosses = !pos(mn);
         }
         unsigned cm = __ballot_sync(FULL, crosses);
+#ifdef RPD_DEBUG_BVH
+        dbg_cross += __popc(cm);
+#endif
         while (cm) {
           const int e = c0 + __ffs(cm) - 1;
           cm &= cm - 1;
@@ -317,12 +329,21 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
         if (!__any_sync(FULL, alive)) break;
       }
       npairs += valid;
+#ifdef RPD_DEBUG_BVH
+      ++dbg_leaves;
+#endif
       if (alive) {
         const int slot = atomicAdd(k_tet + a, 1);
         if (slot < cap) slab[a * cap + slot] = i;
         if (k_words) atomicAdd(k_words + a, words);
       }
     }
+#ifdef RPD_DEBUG_BVH
+    const long long dt = clock64() - t_start;
+    if (lane == 0 && dt > 40000)
+      printf("bvh_leaf item %lld of %d: sphere %d k %d super %lld leaves %d crossing %d cycles %lld\n",
+             (long long)it, n_items, i, k, (long long)sl, dbg_leaves, dbg_cross, dt);
+#endif
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -473,7 +494,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
       // work-item queue: [0] = count, then int2 items
-      int64_t cap_items = 8 * ns + 4 * n_sup + 1024;
+      int64_t cap_items = 48 * ns + 4 * n_leaf + 4096;
       if (cap_items < c->bvh_min_items) cap_items = c->bvh_min_items;
       if (cap_items > (1 << 30)) cap_items = 1 << 30;
       e = c->bvh_items.ensure(sizeof(int2) * (cap_items + 1));
@@ -485,7 +506,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       int64_t blocks = (ns + BVH_WARPS - 1) / BVH_WARPS;
       if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
       k_bvh_super<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
-          sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
+          sup, n_sup, leaf, n_leaf, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
           sphere_lo, sphere_hi, items, (int)cap_items, n_items, sphere_list, n_list_dev);
       static bool attr_set = false;
       const int lsmem = (int)(sizeof(double4) * BVH_LCAP * BVH_WARPS);
