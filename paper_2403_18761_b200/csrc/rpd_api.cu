@@ -286,16 +286,17 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                        cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
        "readback");
-    rb->i32[2] = 0;
+    rb->i32[2] = rb->i32[3] = 0;
     if (c->filter_mode == RPD_FILTER_PRUNED && (rs ? rs->n_list_max > 0 : hi > lo) && n_tets > 0)
-      CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                         c->stream), "readback");
+      CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, 2 * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaStreamSynchronize(c->stream), "filter");
     rpd_status s = check_err(c, rb);
     if (s) return s;
     bool retry = false;
-    if (rb->i32[2] > c->bvh_cap_items) {  // work queue overflow: grow and redo
-      c->bvh_min_items = (int64_t)rb->i32[2] + 1024;
+    const int32_t need = rb->i32[2] > rb->i32[3] ? rb->i32[2] : rb->i32[3];
+    if (need > c->bvh_cap_items) {  // work queue overflow: grow and redo
+      c->bvh_min_items = (int64_t)need + 1024;
       retry = true;
     }
     const int maxk = (int)rb->u64[ST_MAXK];
@@ -332,9 +333,27 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   return RPD_OK;
 }
 
-// clip every pair of cs (tets tet_ids or all) -> piece set
+static void absorb_clip_stats(rpd_ctx* c, const Readback* rb, int n_wide) {
+  c->last.exact_fallbacks += (int64_t)rb->u64[ST_EXACT];
+  c->last.zero_hits += (int64_t)rb->u64[ST_ZERO];
+  c->last.max_vertices = max(c->last.max_vertices, (int32_t)rb->u64[ST_MAXV]);
+  c->last.max_planes = max(c->last.max_planes, (int32_t)rb->u64[ST_MAXP]);
+  c->last.n_wide += n_wide;
+  c->last.clip_plane_evals += (int64_t)rb->u64[ST_CLIP_PLANES];
+  c->last.clip_vertex_tests += (int64_t)rb->u64[ST_CLIP_TESTS];
+  c->last.clip_constructions += (int64_t)rb->u64[ST_CLIP_CONSTR];
+  c->last.clip_fan_triangles += (int64_t)rb->u64[ST_CLIP_FAN];
+  if (getenv("RPD_DEBUG_STATS"))
+    fprintf(stderr, "[rpd clip] exact sign %llu exact out-vertex %llu plane-fallback %llu\n",
+            rb->u64[12], rb->u64[13], rb->u64[14]);
+}
+
+// clip every pair of cs (tets tet_ids or all) -> piece set.
+// deferred: no host round trip; the piece set is sized by upper bounds (one piece per pair,
+// 32 incidences per mask word) and ps.n_pieces / ps.n_inc hold those bounds until the caller
+// reads the exact totals (p_scan[n], i_scan[n]), the overflow counter and the clip stats.
 static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids,
-                           PieceSet& ps) {
+                           PieceSet& ps, bool deferred = false) {
   const int64_t n = cs.n, nt = cs.n_tets;
   size_t nn = n > 0 ? n : 1;
   CK(c->p_flag.ensure(nn), "alloc");
@@ -363,21 +382,23 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   if (c->profile) cudaEventRecord(c->ev[3], c->stream);
   CK(launch_piece_scans(c, n, moff), "scan");
   Readback* rb = (Readback*)c->pinned;
-  CK(cudaMemcpyAsync(&rb->i32[0], c->p_scan.as<int32_t>() + n, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[1], c->i_scan.as<int32_t>() + n, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[2], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                     c->stream), "readback");
-  CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaStreamSynchronize(c->stream), "clip");
-  if (rb->u64[ST_OVERFLOW])
-    return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
-  if (getenv("RPD_DEBUG_STATS"))
-    fprintf(stderr, "[rpd clip] pairs %lld exact sign %llu exact out-vertex %llu plane-fallback %llu\n",
-            (long long)n, rb->u64[12], rb->u64[13], rb->u64[14]);
-  const int64_t np = rb->i32[0], ni = rb->i32[1];
+  int64_t np = n, ni = 32 * (int64_t)cs.n_words;
+  if (!deferred) {
+    CK(cudaMemcpyAsync(&rb->i32[0], c->p_scan.as<int32_t>() + n, sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(cudaMemcpyAsync(&rb->i32[1], c->i_scan.as<int32_t>() + n, sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(cudaMemcpyAsync(&rb->i32[2], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream), "readback");
+    CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(cudaStreamSynchronize(c->stream), "clip");
+    if (rb->u64[ST_OVERFLOW])
+      return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+    np = rb->i32[0];
+    ni = rb->i32[1];
+    absorb_clip_stats(c, rb, rb->i32[2]);
+  }
   const size_t npp = np > 0 ? np : 1;
   CK(ps.off.ensure(sizeof(int32_t) * (nt + 1)), "alloc");
   CK(ps.sphere.ensure(sizeof(int32_t) * npp), "alloc");
@@ -395,15 +416,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   ps.n_pieces = np;
   ps.n_inc = ni;
   c->last.pairs_clipped += n;
-  c->last.exact_fallbacks += (int64_t)rb->u64[ST_EXACT];
-  c->last.zero_hits += (int64_t)rb->u64[ST_ZERO];
-  c->last.max_vertices = max(c->last.max_vertices, (int32_t)rb->u64[ST_MAXV]);
-  c->last.max_planes = max(c->last.max_planes, (int32_t)rb->u64[ST_MAXP]);
-  c->last.n_wide += rb->i32[2];
-  c->last.clip_plane_evals += (int64_t)rb->u64[ST_CLIP_PLANES];
-  c->last.clip_vertex_tests += (int64_t)rb->u64[ST_CLIP_TESTS];
-  c->last.clip_constructions += (int64_t)rb->u64[ST_CLIP_CONSTR];
-  c->last.clip_fan_triangles += (int64_t)rb->u64[ST_CLIP_FAN];
+  if (deferred) return RPD_OK;
   if (c->profile) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
@@ -543,14 +556,15 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
      "readback");
   CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                      cudaMemcpyDeviceToHost, c->stream), "readback");
-  rb->i32[2] = 0;
+  rb->i32[2] = rb->i32[3] = 0;
   if (c->filter_mode == RPD_FILTER_PRUNED && T > 0)
-    CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       c->stream), "readback");
+    CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, 2 * sizeof(int32_t),
+                       cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaStreamSynchronize(c->stream), "dirty");
-  if (rb->i32[2] > c->bvh_cap_items) {
+  const int32_t need = rb->i32[2] > rb->i32[3] ? rb->i32[2] : rb->i32[3];
+  if (need > c->bvh_cap_items) {
     // work queue overflow (never seen): grow it and redo the dirty detection
-    c->bvh_min_items = (int64_t)rb->i32[2] + 1024;
+    c->bvh_min_items = (int64_t)need + 1024;
     CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(),
                      nullptr, nullptr), "dirty filter");
     CK(launch_dirty_list(c, T), "dirty list");
@@ -582,32 +596,26 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
   }
   if (s) return s;
-  s = run_clip(c, c->cand_d, dl, c->pcs_d);
+  s = run_clip(c, c->cand_d, dl, c->pcs_d, /*deferred=*/true);
   if (s) return s;
 
-  // (4) merge clean old tets + dirty new tets into the other buffer set
+  // (4) merge clean old tets + dirty new tets into the other buffer set.  Sized by host upper
+  // bounds; the exact totals, the clip overflow counter and the stats come back in one
+  // readback at the end (the only host round trip after the re-filter).
   const int nxt = c->cur ^ 1;
   CandSet& co = c->cand[c->cur];
   PieceSet& po = c->pcs[c->cur];
+  CandSet& cd = c->cand_d;
+  PieceSet& pd = c->pcs_d;
   CandSet& cn = c->cand[nxt];
   PieceSet& pn = c->pcs[nxt];
-  CK(c->m_cnt.ensure(sizeof(int32_t) * 3 * (T > 0 ? T : 1)), "alloc");
-  CK(c->m_off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(c->m_cnt.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1)), "alloc");
+  CK(c->m_off.ensure(sizeof(int32_t) * 2 * (T + 1)), "alloc");
   CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
   CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  CK(launch_merge(c, T, co, po, c->cand_d, c->pcs_d, cn, pn, 0), "merge counts");
-  CK(cudaMemcpyAsync(&rb->i32[0], cn.off.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[1], pn.off.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[2], c->m_off.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaStreamSynchronize(c->stream), "merge");
-  cn.n = rb->i32[0];
-  cn.n_tets = T;
-  pn.n_pieces = rb->i32[1];
-  pn.n_inc = rb->i32[2];
-  pn.n_tets = T;
+  cn.n = co.n + cd.n;
+  pn.n_pieces = po.n_pieces + pd.n_pieces;
+  pn.n_inc = po.n_inc + pd.n_inc;
   const size_t ncn = cn.n > 0 ? cn.n : 1, npn = pn.n_pieces > 0 ? pn.n_pieces : 1;
   CK(cn.idx.ensure(sizeof(int32_t) * ncn), "alloc");
   CK(cn.pair_tet.ensure(sizeof(int32_t) * ncn), "alloc");
@@ -618,14 +626,42 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(pn.fm.ensure(npn), "alloc");
   CK(pn.inc_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
   CK(pn.inc.ensure(sizeof(int32_t) * (pn.n_inc > 0 ? pn.n_inc : 1)), "alloc");
-  CK(launch_merge(c, T, co, po, c->cand_d, c->pcs_d, cn, pn, 1), "merge copy");
-  // incidence-mask offsets of the merged candidates (for a later rpd_clip)
-  CK(c->p_ninc.ensure(sizeof(int32_t) * ncn), "alloc");
-  CK(launch_moff(c, cn.n, cn.idx.as<int32_t>(), cn.moff.as<int32_t>()), "moff");
-  CK(cudaMemcpyAsync(&rb->i32[3], cn.moff.as<int32_t>() + cn.n, sizeof(int32_t),
+  CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
+  CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 1), "merge copy");
+  const int32_t* m_off = c->m_off.as<int32_t>();
+  CK(cudaMemcpyAsync(&rb->i32[0], cn.off.as<int32_t>() + T, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaStreamSynchronize(c->stream), "merge");
+  CK(cudaMemcpyAsync(&rb->i32[1], pn.off.as<int32_t>() + T, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[2], m_off + T, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                     c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[3], m_off + (T + 1) + T, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                     c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[4], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                     c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[5], c->p_scan.as<int32_t>() + cd.n, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(&rb->i32[6], c->i_scan.as<int32_t>() + cd.n, sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
+                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(cudaStreamSynchronize(c->stream), "partial update");
+  if (rb->u64[ST_OVERFLOW])
+    return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+  absorb_clip_stats(c, rb, rb->i32[4]);
+  if (c->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    c->last.clip_ms += ms;
+  }
+  pd.n_pieces = rb->i32[5];
+  pd.n_inc = rb->i32[6];
+  cn.n = rb->i32[0];
+  cn.n_tets = T;
   cn.n_words = rb->i32[3];
+  pn.n_pieces = rb->i32[1];
+  pn.n_inc = rb->i32[2];
+  pn.n_tets = T;
   c->cur = nxt;
   c->n_dirty = nd;
   c->last.n_dirty = nd;

@@ -116,7 +116,9 @@ struct rpd_ctx {
   rpd::Stage st;
   rpd::DevBuf errw;        // int32[4]
   rpd::DevBuf stats;       // uint64[ST_N]
-  rpd::DevBuf scratch;     // scan block sums
+  rpd::DevBuf scratch;     // scan: u64 ticket counter + per-tile look-back state words
+  unsigned long long scan_ticket = 0;  // tickets consumed so far (device counter value)
+  unsigned scan_epoch = 0;             // call sequence number tagged into the state words
 
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
@@ -196,7 +198,6 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
 // partial update (rpd_partial.cu)
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old);
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
-cudaError_t launch_moff(rpd_ctx* c, int64_t n, const int32_t* cand_idx, int32_t* moff);
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase);

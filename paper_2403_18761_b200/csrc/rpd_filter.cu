@@ -189,11 +189,10 @@ __device__ __forceinline__ void stage_planes(double4* __restrict__ sp,
 
 constexpr int BVH_WARPS = 4;
 
-// phase 1: one warp per sphere tests the super-node boxes and queues (sphere, super node)
-// work items (a sphere with a huge cell becomes many items: load balance)
-__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
-    const double* __restrict__ sup, int64_t n_sup, const double* __restrict__ leaf,
-    int64_t n_leaf, const int32_t* __restrict__ nbr_off,
+// phase 1: one warp per (sphere, chunk of 32 super nodes) tests the super-node boxes and queues
+// (sphere, super node) items; a sphere with a huge cell becomes many items (load balance)
+__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_top(
+    const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
     int cap_items, int* __restrict__ n_items, const int32_t* __restrict__ list,
     const int* __restrict__ n_list_dev) {
@@ -202,40 +201,75 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
   double4* sp = s_pl[warp];
+  const int64_t n_chunk = (n_sup + 31) >> 5;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t ii = lo + gw; ii < hi; ii += nw) {
+  const int64_t n_work = (int64_t)(hi - lo) * n_chunk;
+  int cur_i = -1;
+  for (int64_t w = gw; w < n_work; w += nw) {
+    const int64_t ii = lo + w / n_chunk;
+    const int64_t s = (w % n_chunk) * 32 + lane;
     const int i = list ? list[ii] : (int)ii;
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     const int k = e1 - e0;
     if (k == 0 && N != 1) continue;  // hidden sphere (R4): relates to no tet
-    const double4* gp = planes + e0;
-    stage_planes(sp, gp, k);
-    for (int64_t s0 = 0; s0 < n_sup; s0 += 32) {
-      const int64_t s = s0 + lane;
-      unsigned sm = __ballot_sync(FULL, box_passes_w(sup + 6 * s, s < n_sup, sp, k));
-      while (sm) {
-        const int64_t sl = s0 + __ffs(sm) - 1;
-        sm &= sm - 1;
-        // leaves of the surviving super node (lane = leaf) -> (sphere, leaf) work items
-        const int64_t l = sl * BVH_FAN + lane;
-        const bool ok = box_passes_w(leaf + 6 * l, l < n_leaf, sp, k);
-        const unsigned lm = __ballot_sync(FULL, ok);
-        if (!lm) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(n_items, __popc(lm));
-        base = __shfl_sync(FULL, base, 0);
-        if (ok) {
-          const int slot = base + __popc(lm & ((1u << lane) - 1u));
-          if (slot < cap_items) items[slot] = make_int2(i, (int)l);
-        }
-      }
+    if (i != cur_i) {
+      stage_planes(sp, planes + e0, k);
+      cur_i = i;
+    }
+    const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, k);
+    const unsigned sm = __ballot_sync(FULL, ok);
+    if (!sm) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(n_items, __popc(sm));
+    base = __shfl_sync(FULL, base, 0);
+    if (ok) {
+      const int slot = base + __popc(sm & ((1u << lane) - 1u));
+      if (slot < cap_items) items[slot] = make_int2(i, (int)s);
     }
   }
 }
 
-// phase 2: one warp per (sphere, super node) item: leaf boxes, then the exact Alg. 1
-// (lane = tet) on the surviving leaves
+// phase 2: one warp per (sphere, super node) item tests the 32 leaf boxes of the super node
+// and queues (sphere, leaf) items
+__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
+    const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
+    const double4* __restrict__ planes, const int2* __restrict__ sitems,
+    const int* __restrict__ n_sitems_p, int cap_sitems, int2* __restrict__ items,
+    int cap_items, int* __restrict__ n_items) {
+  __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  double4* sp = s_pl[warp];
+  const int n_sitems = min(*n_sitems_p, cap_sitems);
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int cur_i = -1;
+  for (int64_t it = gw; it < n_sitems; it += nw) {
+    const int2 item = sitems[it];
+    const int i = item.x;
+    const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+    const int k = e1 - e0;
+    if (i != cur_i) {
+      stage_planes(sp, planes + e0, k);
+      cur_i = i;
+    }
+    const int64_t l = (int64_t)item.y * BVH_FAN + lane;
+    const bool ok = box_passes_w(leaf + 6 * l, l < n_leaf, sp, k);
+    const unsigned lm = __ballot_sync(FULL, ok);
+    if (!lm) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(n_items, __popc(lm));
+    base = __shfl_sync(FULL, base, 0);
+    if (ok) {
+      const int slot = base + __popc(lm & ((1u << lane) - 1u));
+      if (slot < cap_items) items[slot] = make_int2(i, (int)l);
+    }
+  }
+}
+
+// phase 3: one warp per (sphere, leaf) item: the remaining planes on the leaf box, then the
+// exact Alg. 1 (lane = tet)
 __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
     const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
@@ -367,37 +401,56 @@ __global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
 
 // ------------------------------------------------------------------ compaction
 
+// one warp per tet: its candidate ids (distinct) are rank-sorted ascending (the BVH filter
+// appends in arbitrary order) and written coalesced; then the incidence-word offsets of the
+// pairs are a running warp scan in sorted order
 __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,
-                                int32_t* __restrict__ slab, const int32_t* __restrict__ cand_off,
+                                const int32_t* __restrict__ slab,
+                                const int32_t* __restrict__ cand_off,
                                 int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
                                 const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
                                 const int32_t* __restrict__ nbr_off, int64_t n_pairs) {
-  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (a >= n) return;
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (a >= n) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
   const int k = min(k_tet[a], cap);
-  int32_t* s = slab + a * cap;
-  // ascending sphere id (the BVH filter appends in arbitrary order)
-  for (int x = 1; x < k; ++x) {
-    const int v = s[x];
-    int y = x;
-    while (y > 0 && s[y - 1] > v) {
-      s[y] = s[y - 1];
-      --y;
-    }
-    s[y] = v;
-  }
+  const int32_t* s = slab + a * cap;
   const int o = cand_off[a];
-  int w = w_off ? w_off[a] : 0;
-  for (int c = 0; c < k; ++c) {
-    const int i = s[c];
-    cand_idx[o + c] = i;
-    if (pair_tet) pair_tet[o + c] = (int32_t)a;
-    if (p_moff) {
-      p_moff[o + c] = w;
-      w += (nbr_off[i + 1] - nbr_off[i] + 31) >> 5;
+  for (int r0 = 0; r0 < k; r0 += 32) {
+    const int j = r0 + lane;
+    const int v = j < k ? s[j] : INT_MAX;
+    int rank = 0;
+    for (int q0 = 0; q0 < k; q0 += 32) {
+      const int u = q0 + lane < k ? s[q0 + lane] : INT_MAX;
+#pragma unroll 8
+      for (int m = 0; m < 32; ++m) rank += __shfl_sync(FULL, u, m) < v;
+    }
+    if (j < k) {
+      cand_idx[o + rank] = v;
+      if (pair_tet) pair_tet[o + rank] = (int32_t)a;
     }
   }
-  if (p_moff && a == n - 1) p_moff[n_pairs] = w;
+  if (!p_moff) return;
+  __syncwarp();
+  int w = w_off ? w_off[a] : 0;
+  for (int r0 = 0; r0 < k; r0 += 32) {
+    const int j = r0 + lane;
+    int words = 0;
+    if (j < k) {
+      const int i = cand_idx[o + j];
+      words = (__ldg(nbr_off + i + 1) - __ldg(nbr_off + i) + 31) >> 5;
+    }
+    int x = words;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, x, d);
+      if (lane >= d) x += y;
+    }
+    if (j < k) p_moff[o + j] = w + x - words;
+    w += __shfl_sync(FULL, x, 31);
+  }
+  if (a == n - 1 && lane == 0) p_moff[n_pairs] = w;
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -410,16 +463,32 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
                            const int32_t* __restrict__ nbr_off, int cap,
                            int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
                            int32_t* __restrict__ k_words) {
-  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;  // warp per tet
   if (a >= n) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
   const int t = dirty[a];
   const int me = *min_epoch;
-  for (int q = co_off[t]; q < co_off[t + 1]; ++q) {
-    const int i = co_idx[q];
-    if (repoch[i] > me) continue;  // re-tested by the traversal
-    const int slot = atomicAdd(k_tet + a, 1);
-    if (slot < cap) slab[a * cap + slot] = i;
-    atomicAdd(k_words + a, (nbr_off[i + 1] - nbr_off[i] + 31) >> 5);
+  const int q0 = co_off[t], q1 = co_off[t + 1];
+  for (int qb = q0; qb < q1; qb += 32) {
+    const int q = qb + lane;
+    const int i = q < q1 ? co_idx[q] : 0;
+    const bool keep = q < q1 && repoch[i] <= me;  // else re-tested by the traversal
+    const unsigned km = __ballot_sync(FULL, keep);
+    if (!km) continue;
+    int words = keep ? (nbr_off[i + 1] - nbr_off[i] + 31) >> 5 : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) words += __shfl_xor_sync(FULL, words, d);
+    int base = 0;
+    if (lane == 0) {
+      base = atomicAdd(k_tet + a, __popc(km));
+      atomicAdd(k_words + a, words);
+    }
+    base = __shfl_sync(FULL, base, 0);
+    if (keep) {
+      const int slot = base + __popc(km & ((1u << lane) - 1u));
+      if (slot < cap) slab[a * cap + slot] = i;
+    }
   }
 }
 
@@ -427,7 +496,7 @@ cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
                             const CandSet& co, int cap, int32_t* k_tet, int32_t* slab,
                             int32_t* k_words) {
   if (n_dirty == 0) return cudaSuccess;
-  k_keep_old<<<nblk(n_dirty, 256), 256, 0, c->stream>>>(
+  k_keep_old<<<nblk(n_dirty * 32, 256), 256, 0, c->stream>>>(
       n_dirty, dirty, co.off.as<int32_t>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
       c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab, k_words);
   ++c->launches;
@@ -493,21 +562,30 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
     if (ns > 0) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      // work-item queue: [0] = count, then int2 items
+      // work-item queues: int2 header {leaf items, super items}, leaf items, super items
       int64_t cap_items = 48 * ns + 4 * n_leaf + 4096;
+      int64_t cap_sup = 8 * ns + 4 * n_sup + 4096;
       if (cap_items < c->bvh_min_items) cap_items = c->bvh_min_items;
+      if (cap_sup < c->bvh_min_items) cap_sup = c->bvh_min_items;
       if (cap_items > (1 << 30)) cap_items = 1 << 30;
-      e = c->bvh_items.ensure(sizeof(int2) * (cap_items + 1));
+      if (cap_sup > (1 << 30)) cap_sup = 1 << 30;
+      e = c->bvh_items.ensure(sizeof(int2) * (cap_items + cap_sup + 1));
       if (e) return e;
       int* n_items = c->bvh_items.as<int>();
+      int* n_sitems = n_items + 1;
       int2* items = reinterpret_cast<int2*>(c->bvh_items.as<char>() + sizeof(int2));
-      e = cudaMemsetAsync(n_items, 0, sizeof(int), c->stream);
+      int2* sitems = items + cap_items;
+      e = cudaMemsetAsync(n_items, 0, sizeof(int2), c->stream);
       if (e) return e;
-      int64_t blocks = (ns + BVH_WARPS - 1) / BVH_WARPS;
+      const int64_t n_chunk = (n_sup + 31) / 32;
+      int64_t blocks = (ns * n_chunk + BVH_WARPS - 1) / BVH_WARPS;
       if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-      k_bvh_super<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
-          sup, n_sup, leaf, n_leaf, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
-          sphere_lo, sphere_hi, items, (int)cap_items, n_items, sphere_list, n_list_dev);
+      k_bvh_top<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
+          sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
+          sphere_lo, sphere_hi, sitems, (int)cap_sup, n_sitems, sphere_list, n_list_dev);
+      k_bvh_super<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
+          leaf, n_leaf, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), sitems,
+          n_sitems, (int)cap_sup, items, (int)cap_items, n_items);
       static bool attr_set = false;
       const int lsmem = (int)(sizeof(double4) * BVH_LCAP * BVH_WARPS);
       if (!attr_set) {
@@ -519,8 +597,8 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
           c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,
           (int)cap_items, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
-      c->launches += 2;
-      c->bvh_cap_items = cap_items;
+      c->launches += 3;
+      c->bvh_cap_items = cap_items < cap_sup ? cap_items : cap_sup;
     }
     k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
                                                         c->stats.as<unsigned long long>());
@@ -543,7 +621,7 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
     if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
     return cudaSuccess;
   }
-  k_compact_cands<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off, cand_idx,
+  k_compact_cands<<<nblk(n * 32, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off, cand_idx,
                                                        pair_tet, w_off, p_moff,
                                                        c->st.nbr_off.as<int32_t>(), n_pairs);
   ++c->launches;

@@ -1,6 +1,6 @@
 // rpd_scan.cu -- exclusive prefix sums used by the compaction steps:
-// out[k] = sum_{m<k} in[m] for k in [0, n], out[n] = total.  Three phases: per-tile reduce,
-// one-block scan of tile sums, per-tile scan + offset.  Deterministic (integer).
+// out[k] = sum_{m<k} in[m] for k in [0, n], out[n] = total.  One launch per scan (decoupled
+// look-back over 4096-element tiles).  Deterministic (integer).
 #include "rpd_ctx.h"
 
 namespace rpd {
@@ -42,37 +42,29 @@ __device__ inline int block_exclusive_scan(int v, int* smem, int* total) {
   return base + x - v;
 }
 
-template <class T>
-__global__ void k_scan_reduce(const T* __restrict__ in, int64_t n, int* __restrict__ sums) {
-  __shared__ int sm[32];
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
-  int s = 0;
-#pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; ++k) s += load_item(in, base + k, n);
-  int tot;
-  block_exclusive_scan(s, sm, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
+// Single pass (decoupled look-back): tiles take tickets in launch order, publish their
+// aggregate, then warp 0 walks back over the predecessors' published aggregates / inclusive
+// prefixes.  Each state word packs {call epoch (30 bit), flag (2 bit), value (32 bit)} so that
+// stale words of earlier calls read as "not yet published" and no reset launch is needed.
+constexpr unsigned long long F_AGG = 1ull, F_INC = 2ull;
 
-__global__ void k_scan_sums(int* __restrict__ sums, int nb) {
-  __shared__ int sm[32];
-  int carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
-    int k = b0 + threadIdx.x;
-    int v = k < nb ? sums[k] : 0;
-    int tot;
-    int ex = block_exclusive_scan(v, sm, &tot);
-    if (k < nb) sums[k] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) sums[nb] = carry;
+__device__ __forceinline__ unsigned long long st_pack(unsigned epoch, unsigned long long f,
+                                                      int v) {
+  return ((unsigned long long)epoch << 34) | (f << 32) | (unsigned)v;
 }
 
 template <class T>
-__global__ void k_scan_apply(const T* __restrict__ in, int64_t n, const int* __restrict__ sums,
-                             int* __restrict__ out, int nb) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(const T* __restrict__ in, int64_t n,
+                                                      int* __restrict__ out, int nb,
+                                                      unsigned long long* __restrict__ ticket,
+                                                      unsigned long long ticket_base,
+                                                      unsigned long long* state, unsigned epoch) {
   __shared__ int sm[32];
-  int64_t base = (int64_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
+  __shared__ int s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ticket, 1ull) - ticket_base);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   int v[SCAN_ITEMS];
   int s = 0;
 #pragma unroll
@@ -81,13 +73,48 @@ __global__ void k_scan_apply(const T* __restrict__ in, int64_t n, const int* __r
     s += v[k];
   }
   int tot;
-  int ex = block_exclusive_scan(s, sm, &tot) + sums[blockIdx.x];
+  int ex = block_exclusive_scan(s, sm, &tot);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) atomicExch(state, st_pack(epoch, F_INC, tot));
+    } else {
+      if (lane == 0) atomicExch(state + tile, st_pack(epoch, F_AGG, tot));
+      int j = tile - 1;
+      while (true) {
+        const int idx = j - lane;
+        unsigned long long w = 0;
+        unsigned f = 0;
+        if (idx >= 0) {
+          do {
+            w = *(volatile unsigned long long*)(state + idx);
+            f = (unsigned)(w >> 34) == epoch ? (unsigned)(w >> 32) & 3u : 0u;
+          } while (f == 0);
+        }
+        const int val = idx >= 0 ? (int)(unsigned)w : 0;
+        const unsigned inc = __ballot_sync(0xffffffffu, f == F_INC);
+        // lanes up to (and including) the nearest inclusive prefix contribute
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        int x = lane <= stop ? val : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        prefix += x;
+        if (inc) break;
+        j -= 32;
+      }
+      if (lane == 0) atomicExch(state + tile, st_pack(epoch, F_INC, prefix + tot));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  ex += s_prefix;
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     if (base + k < n) out[base + k] = ex;
     ex += v[k];
   }
-  if (blockIdx.x == nb - 1 && threadIdx.x == 0) out[n] = sums[nb];
+  if (tile == nb - 1 && threadIdx.x == 0) out[n] = s_prefix + tot;
 }
 
 template <class T>
@@ -95,14 +122,22 @@ static cudaError_t scan_impl(rpd_ctx* c, const T* in, int32_t* out, int64_t n) {
   if (n == 0) {
     return cudaMemsetAsync(out, 0, sizeof(int32_t), c->stream);
   }
-  int nb = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
-  cudaError_t e = c->scratch.ensure(sizeof(int) * (nb + 1));
-  if (e) return e;
-  int* sums = c->scratch.as<int>();
-  k_scan_reduce<T><<<nb, SCAN_THREADS, 0, c->stream>>>(in, n, sums);
-  k_scan_sums<<<1, 1024, 0, c->stream>>>(sums, nb);
-  k_scan_apply<T><<<nb, SCAN_THREADS, 0, c->stream>>>(in, n, sums, out, nb);
-  c->launches += 3;
+  const int nb = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
+  const size_t bytes = sizeof(unsigned long long) * (nb + 1);
+  if (bytes > c->scratch.cap || !c->scratch.p) {
+    cudaError_t e = c->scratch.ensure(bytes);
+    if (e) return e;
+    e = cudaMemsetAsync(c->scratch.p, 0, c->scratch.cap, c->stream);
+    if (e) return e;
+    c->scan_ticket = 0;
+  }
+  unsigned long long* ticket = c->scratch.as<unsigned long long>();
+  c->scan_epoch = (c->scan_epoch + 1) & ((1u << 30) - 1);
+  if (c->scan_epoch == 0) c->scan_epoch = 1;
+  k_scan<T><<<nb, SCAN_THREADS, 0, c->stream>>>(in, n, out, nb, ticket, c->scan_ticket,
+                                                 ticket + 1, c->scan_epoch);
+  c->scan_ticket += (unsigned long long)nb;
+  ++c->launches;
   return cudaGetLastError();
 }
 

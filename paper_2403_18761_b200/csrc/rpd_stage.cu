@@ -121,6 +121,10 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   if (i >= N) return;
+#ifdef RPD_DEBUG_STAGE
+  long long dbg_t[5];
+  dbg_t[0] = clock64();
+#endif
   const int32_t e0 = off_in[i], e1 = off_in[i + 1];
   if (lane == 0) {
     off_out[i] = e0;
@@ -185,6 +189,9 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   }
   if (__any_sync(FULL, bad)) return;
   __syncwarp();
+#ifdef RPD_DEBUG_STAGE
+  dbg_t[1] = clock64();
+#endif
   const double4 si = sw[i];
   // planes, and the twin key: bit patterns of the ratios to the first non-zero normal
   // component (correctly rounded quotients of exactly proportional integers are equal)
@@ -202,9 +209,19 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     h = (h ^ (unsigned long long)__double_as_longlong(a.y / piv)) * 1099511628211ull;
     h = (h ^ (unsigned long long)__double_as_longlong(a.z / piv)) * 1099511628211ull;
     h = (h ^ (unsigned long long)__double_as_longlong(a.w / piv)) * 1099511628211ull;
+    // final avalanche (the ratios of small integers have all-zero low mantissa bits, so the
+    // low bits of the raw product barely vary and would cluster the hash-table slots)
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
     hkey[e] = h;
   }
   __syncwarp();
+#ifdef RPD_DEBUG_STAGE
+  dbg_t[2] = clock64();
+#endif
   // twins: next entry of the row with the same oriented plane (equal keys compared exactly).
   // Long rows first check for a repeated key with a per-row hash table in global scratch
   // (region [4 e0, 4 e0 + 4k)); without a repeat every entry has no twin.
@@ -231,6 +248,9 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     }
     maybe = __any_sync(FULL, dup);
   }
+#ifdef RPD_DEBUG_STAGE
+  dbg_t[3] = clock64();
+#endif
   for (int32_t e = e0 + lane; e < e1; e += 32) {
     int32_t tw = -1;
     if (maybe) {
@@ -253,6 +273,13 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     }
     twin[e] = tw;
   }
+#ifdef RPD_DEBUG_STAGE
+  dbg_t[4] = clock64();
+  if (lane == 0 && dbg_t[4] - dbg_t[0] > 100000)
+    printf("stage row %lld k %d sorted %d maybe %d cycles sort %lld planes %lld hash %lld twins %lld\n",
+           (long long)i, k, (int)sorted, (int)maybe, dbg_t[1] - dbg_t[0], dbg_t[2] - dbg_t[1],
+           dbg_t[3] - dbg_t[2], dbg_t[4] - dbg_t[3]);
+#endif
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }

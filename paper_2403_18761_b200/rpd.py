@@ -212,15 +212,26 @@ class RPDContext:
         self._check(self.L.rpd_download_cands(self.h, self._p(off), self._p(idx)))
         return {"cand_off": off, "cand_idx": idx}
 
-    def download_pieces(self, device=False):
+    def download_pieces(self, device=False, out=None):
+        """Piece CSR as numpy (host) or torch CUDA tensors (device=True).  `out`: optional
+        preallocated destinations (e.g. pinned host arrays), a dict with the returned keys,
+        each at least as long as the current piece set needs; views of them are returned."""
         T = self.T
         npc, ni = self.counts.n_pieces, self.counts.n_inc
-        arrs = self._alloc([(T + 1, np.int32), (npc, np.int32), (npc, np.float64),
-                            (3 * npc, np.float64), (npc, np.uint8), (npc + 1, np.int32),
-                            (ni, np.int32)], device)
-        self._check(self.L.rpd_download_pieces(self.h, *[self._p(a) for a in arrs]))
+        specs = [(T + 1, np.int32), (npc, np.int32), (npc, np.float64),
+                 (3 * npc, np.float64), (npc, np.uint8), (npc + 1, np.int32), (ni, np.int32)]
         keys = ["piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
                 "inc_off", "inc_sphere"]
+        if out is None:
+            arrs = self._alloc(specs, device)
+        else:
+            arrs = []
+            for k, (n, dt) in zip(keys, specs):
+                a = out[k].reshape(-1)
+                if a.dtype != dt or a.size < n:
+                    raise ValueError(f"download_pieces: out[{k!r}] needs {n} x {np.dtype(dt)}")
+                arrs.append(a[:n])
+        self._check(self.L.rpd_download_pieces(self.h, *[self._p(a) for a in arrs]))
         out = dict(zip(keys, arrs))
         out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
         return out
