@@ -343,6 +343,7 @@ static void absorb_clip_stats(rpd_ctx* c, const Readback* rb, int n_wide) {
   c->last.clip_vertex_tests += (int64_t)rb->u64[ST_CLIP_TESTS];
   c->last.clip_constructions += (int64_t)rb->u64[ST_CLIP_CONSTR];
   c->last.clip_fan_triangles += (int64_t)rb->u64[ST_CLIP_FAN];
+  if (getenv("RPD_DEBUG_STATS")) clip_phase_dump();
   if (getenv("RPD_DEBUG_STATS"))
     fprintf(stderr, "[rpd clip] exact sign %llu exact out-vertex %llu plane-fallback %llu\n",
             rb->u64[12], rb->u64[13], rb->u64[14]);

@@ -10,7 +10,7 @@
 //
 // B200 mapping: a group of GW lanes per pair (GW = 16: two pairs per warp run in lockstep),
 // VPL vertex slots per lane (slot v = GW k + lane), the polytope in per-group shared memory
-// (double-buffered vertex table with explicit dual-edge links).  The fast kernel has GW = 16,
+// (vertex slots updated in place, a live-slot mask, explicit dual-edge links).  The fast kernel has GW = 16,
 // VPL = 1 (<= 16 vertices and planes); pairs that exceed it are re-run by the same kernel
 // instantiated with GW = 32, VPL = 4 (<= 128).  The k_site planes are first classified GW at a
 // time, one per lane, from their exact values at the 4 tet corners:
@@ -45,16 +45,20 @@ struct WarpState {
   static constexpr int MAXV = GW * VPL;
   static constexpr int MAXP = GW * VPL;
   double g[MAXP][4];       // barycentric plane vectors (exact integers)
-  double K[2][MAXV][4];    // homogeneous vertices (double-buffered vertex table)
-  double F[2][MAXV];       // error scalars
-  double KM[2][MAXV];      // max |K_m| of every vertex
+  double K[MAXV][4];       // homogeneous vertices (slots; the live set is a group mask)
+  double F[MAXV];          // error scalars
+  double KM[MAXV];         // max |K_m| of every vertex
   double x[MAXV][3];       // final vertex coordinates (lattice units, relative to V0)
   double V[4][3];          // tet corners (lattice units)
   double val[MAXV];        // plane value g_s . K of every vertex in the current sign pass
-  unsigned tri[2][MAXV];   // oriented plane triplet of every vertex (3 x 8 bits)
-  unsigned char nb[2][MAXV][4];  // vertex across edge r = (tri[r], tri[r+1]) of the dual
+  unsigned tri[MAXV];      // oriented plane triplet of every vertex (3 x 8 bits)
+  unsigned char nb[MAXV][4];  // vertex across edge r = (tri[r], tri[r+1]) of the dual
   unsigned char vx[MAXV];  // 1 if the current sign was decided by the exact path
-  unsigned char map[MAXV]; // old slot -> new slot of the kept vertices
+  double Kn[MAXV][4];      // staging of the new vertices of a cut (K, F, KM)
+  double Fn[MAXV];
+  double KMn[MAXV];
+  unsigned dsc[MAXV];      // new-vertex descriptors: u | v << 8 | x << 16 | y << 24
+  unsigned char dq[MAXV];  // and their target slots
   int src[MAXP];           // radical: sphere j; tet face k: -1-k
   int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
   int ref[MAXP];           // reference vertex of every facet (fan apex)
@@ -117,6 +121,34 @@ struct Bits {
     return -1;
   }
 };
+
+// slot masks: word k, bit l <-> slot GW k + l (group-local bits)
+template <int VPL>
+__device__ __forceinline__ int mask_count(const unsigned (&m)[VPL]) {
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) c += __popc(m[k]);
+  return c;
+}
+// slot of the j-th (0-based) set bit
+template <int GW, int VPL>
+__device__ __forceinline__ int mask_nth(const unsigned (&m)[VPL], int j) {
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = __popc(m[k]);
+    if (j < c) {
+      unsigned w = m[k];
+      for (int q = 0; q < j; ++q) w &= w - 1u;
+      return GW * k + __ffs(w) - 1;
+    }
+    j -= c;
+  }
+  return -1;
+}
+template <int GW>
+__device__ __forceinline__ bool slot_in(const unsigned* m, int v) {
+  return (m[v / GW] >> (v % GW)) & 1u;
+}
 
 struct ClipCtx {
   const double4* planes;   // global plane table (for Cartesian normals)
@@ -245,15 +277,15 @@ __device__ inline void vertex_from_planes(const WarpState<GW, VPL>& S, const Cli
 // Falls back to the exact-cofactor construction from the three planes when an endpoint's
 // sign came from the exact path or the bound is too loose.
 template <int GW, int VPL>
-__device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, int cur, int u,
+__device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, int u,
                                  int v, int x, int y, int sid, double sabs, double K[4],
                                  double* F, double* KMo, int* nexact) {
   if (!S.vx[u] && !S.vx[v]) {
     const double vu = S.val[u], avv = -S.val[v];  // vu > B_u > 0, -val_v > B_v > 0
-    const double* Ku = S.K[cur][u];
-    const double* Kv = S.K[cur][v];
-    const double Fu = S.F[cur][u], Fv = S.F[cur][v];
-    const double ku = S.KM[cur][u], kv = S.KM[cur][v];
+    const double* Ku = S.K[u];
+    const double* Kv = S.K[v];
+    const double Fu = S.F[u], Fv = S.F[v];
+    const double ku = S.KM[u], kv = S.KM[v];
 #pragma unroll
     for (int m = 0; m < 4; ++m) K[m] = fma(vu, Kv[m], avv * Ku[m]);
     const double km = absmax(absmax(K[0], K[1]), absmax(K[2], K[3]));
@@ -276,6 +308,21 @@ __device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, 
 
 enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
 
+#ifdef RPD_CLIP_PHASES
+// development aid: cycles per clip phase summed over groups (lane 0 of each group)
+__device__ unsigned long long g_phase[8];
+#define PHASE_MARK(k)                      \
+  do {                                     \
+    const long long _t = clock64();        \
+    ph[k] += _t - ph_t;                    \
+    ph_t = _t;                             \
+  } while (0)
+#else
+#define PHASE_MARK(k) \
+  do {                \
+  } while (0)
+#endif
+
 struct PairOut {
   double* vol;
   double* m1;
@@ -297,7 +344,6 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev) {
   using WS = WarpState<GW, VPL>;
   if (n_dev) n_pairs = *n_dev;
-  constexpr int MAXV = WS::MAXV;
   constexpr int MAXP = WS::MAXP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WS& S = reinterpret_cast<WS*>(smem_raw)[threadIdx.x / GW];
@@ -306,7 +352,6 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   const int grp = (threadIdx.x & 31) / GW;
   const unsigned GLOW = GW == 32 ? 0xffffffffu : ((1u << GW) - 1u);
   const unsigned FULL = GLOW << (GW * grp);  // this group's lanes
-  const unsigned lt_mask = (1u << lane) - 1u;
   ClipCtx C{planes, N};
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GW;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) / GW;
@@ -314,6 +359,10 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   int d_sign = 0, d_out = 0, d_fb = 0;  // diagnostics
   // algorithmic work (warp-uniform quantities, counted once per warp)
   long long c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;
+#ifdef RPD_CLIP_PHASES
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_t = clock64();
+#endif
 
   for (int64_t pi = gw; pi < n_pairs; pi += nw) {
     const int64_t p = pair_list ? (int64_t)pair_list[pi] : pi;
@@ -325,18 +374,22 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         S.g[lane][k] = (k == lane) ? 1.0 : 0.0;
-        S.K[0][lane][k] = (k == lane) ? 1.0 : 0.0;
+        S.K[lane][k] = (k == lane) ? 1.0 : 0.0;
       }
       S.src[lane] = -1 - lane;
       S.eidx[lane] = -1;
-      S.F[0][lane] = 0.0;
-      S.KM[0][lane] = 1.0;
-      S.tri[0][lane] = CORNER_TRI[lane];
+      S.F[lane] = 0.0;
+      S.KM[lane] = 1.0;
+      S.tri[lane] = CORNER_TRI[lane];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) S.nb[0][lane][r] = CORNER_NB[lane][r];
+      for (int r = 0; r < 3; ++r) S.nb[lane][r] = CORNER_NB[lane][r];
     }
     __syncwarp(FULL);
-    int np = 4, nv = 4, cur = 0, status = ST_ALIVE, zero_hit = 0;
+    PHASE_MARK(0);
+    int np = 4, nv = 4, status = ST_ALIVE, zero_hit = 0;
+    unsigned live[VPL];  // live vertex slots (group-uniform)
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) live[k] = k == 0 ? 0xfu : 0u;
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     c_planes += e1 - e0;
 
@@ -361,6 +414,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         break;
       }
       unsigned act = (__ballot_sync(FULL, have && !allpos) >> (GW * grp)) & GLOW;
+      PHASE_MARK(1);
       while (act && status == ST_ALIVE) {
         const int l = __ffs(act) - 1;
         act &= act - 1;
@@ -378,21 +432,21 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         bool anyneg = false, anypos = false;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv) break;  // slots beyond the vertex count
-          const int v = GW * k + lane;
-          const bool valid = v < nv;
           sg[k] = 0;
+          if (!live[k]) continue;  // no live slot in this word (group-uniform)
+          const int v = GW * k + lane;
+          const bool valid = (live[k] >> lane) & 1u;
           if (valid) {
-            const double* K = S.K[cur][v];
+            const double* K = S.K[v];
             const double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
-            const double B = sabs * S.F[cur][v];
+            const double B = sabs * S.F[v];
             S.val[v] = val;
             S.vx[v] = 0;
             if (val > B) sg[k] = 1;
             else if (val < -B) sg[k] = -1;
             else {
               int zh = 0;
-              sg[k] = exact_sign(S, C, S.tri[cur][v], -1, s, es, nbr_idx[es], &zh);
+              sg[k] = exact_sign(S, C, S.tri[v], -1, s, es, nbr_idx[es], &zh);
               S.vx[v] = 1;
               ++n_exact;
               ++d_sign;
@@ -413,16 +467,16 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         if (p == RPD_TRACE) {
           for (int k = 0; k < VPL; ++k) {
             int v = GW * k + lane;
-            if (v < nv) {
-              unsigned tr = S.tri[cur][v];
+            if ((live[k] >> lane) & 1u) {
+              unsigned tr = S.tri[v];
               printf("plane j=%d es=%d v=%d tri=(%d,%d,%d) sg=%d K=(%g,%g,%g,%g) F=%g\n",
                      nbr_idx[es], es, v, tri_at(tr, 0), tri_at(tr, 1), tri_at(tr, 2), sg[k],
-                     S.K[cur][v][0], S.K[cur][v][1], S.K[cur][v][2], S.K[cur][v][3],
-                     S.F[cur][v]);
+                     S.K[v][0], S.K[v][1], S.K[v][2], S.K[v][3], S.F[v]);
             }
           }
         }
 #endif
+        PHASE_MARK(2);
         if (!anyneg) continue;  // the plane does not cut: skip it
         if (!anypos) {
           status = ST_EMPTY;
@@ -440,120 +494,145 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           S.eidx[sid] = es;
         }
         __syncwarp(FULL);
-        // ---- new vertices: one per boundary edge of the conflict region (a removed vertex v
-        // with a kept neighbour u across its dual edge (x, y)), oriented as that edge:
-        // (x, y, s).  Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring
-        // new vertices around the new facet s.
-        int nnew[VPL];
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) nnew[k] = 0;
+        // ---- new vertices, in place: one per boundary edge of the conflict region (a removed
+        // vertex v with a kept neighbour u across its dual edge (x, y)), oriented as that edge:
+        // (x, y, s).  Kept vertices stay in their slots; the first new vertex of v takes v's
+        // slot, further ones take free slots (holes, removed vertices without new ones).
+        // Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring new vertices
+        // around the new facet s.  Only lane v reads slot v during the step, so writing slot v
+        // last (r descending) is race-free.
+        unsigned nbw[VPL], hasnew[VPL], extra[VPL], freem[VPL];
+        int nnew[VPL], ex_idx[VPL];
+        int ex_base = 0;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv) break;  // slots beyond the vertex count
-          const int v = GW * k + lane;
           nnew[k] = 0;
-          if (v < nv && sg[k] < 0) {
+          nbw[k] = 0u;
+          ex_idx[k] = 0;
+          hasnew[k] = 0u;
+          if (!live[k]) continue;
+          const int v = GW * k + lane;
+          if ((negm[k] >> lane) & 1u) {
+            nbw[k] = *reinterpret_cast<const unsigned*>(S.nb[v]);
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-              const int u = S.nb[cur][v][r];
-              nnew[k] += (posm[u / GW] >> (u % GW)) & 1u;
-            }
+            for (int r = 0; r < 3; ++r) nnew[k] += slot_in<GW>(posm, (nbw[k] >> (8 * r)) & 0xff);
           }
-        }
-        // exclusive prefix of kept / new counts over slots (slot order v = 32 k + lane)
-        int kept_base = 0, new_base = 0;
-        int kept_idx[VPL], new_idx[VPL];
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv) break;  // slots beyond the vertex count
-          kept_idx[k] = kept_base + __popc(posm[k] & lt_mask);
-          kept_base += __popc(posm[k]);
-          int incl = nnew[k];
+          hasnew[k] = (__ballot_sync(FULL, nnew[k] > 0) >> (GW * grp)) & GLOW;
+          const int ex = nnew[k] > 0 ? nnew[k] - 1 : 0;
+          int incl = ex;
 #pragma unroll
           for (int o = 1; o < GW; o <<= 1) {
             const int y = __shfl_up_sync(FULL, incl, o, GW);
             if (lane >= o) incl += y;
           }
-          new_idx[k] = new_base + incl - nnew[k];
-          new_base += __shfl_sync(FULL, incl, GW - 1, GW);
+          ex_idx[k] = ex_base + incl - ex;
+          ex_base += __shfl_sync(FULL, incl, GW - 1, GW);
         }
-        const int nkept = kept_base;
-        const int nv2 = nkept + new_base;
-        if (nv2 > MAXV) {
+        // free slots, and the lowest ex_base of them for the extra new vertices
+        int rem = ex_base;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          freem[k] = ~(posm[k] | hasnew[k]) & GLOW;
+          unsigned f = freem[k];
+          extra[k] = 0u;
+          while (rem > 0 && f) {
+            extra[k] |= f & (0u - f);
+            f &= f - 1u;
+            --rem;
+          }
+        }
+        if (rem > 0) {  // more than MAXV vertices
           status = ST_OVER;
           break;
         }
-        const int nxt = cur ^ 1;
+        // descriptors of the new vertices (edge (u, v), planes (x, y), target slot q), numbered
+        // in slot order of v; then one lane per new vertex builds it into the staging area,
+        // and after a sync the staged vertices move into their slots (slot v may be read as an
+        // edge endpoint until then)
+        {
+          int hb = 0;
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv) break;  // slots beyond the vertex count
-          const int v = GW * k + lane;
-          if (v < nv && sg[k] > 0) S.map[v] = (unsigned char)kept_idx[k];
-        }
-        __syncwarp(FULL);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv) break;  // slots beyond the vertex count
-          const int v = GW * k + lane;
-          if (v >= nv) continue;
-          if (sg[k] > 0) {
-            const int q = kept_idx[k];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = S.K[cur][v][m];
-            S.F[nxt][q] = S.F[cur][v];
-            S.KM[nxt][q] = S.KM[cur][v];
-            S.tri[nxt][q] = S.tri[cur][v];
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-              const int u = S.nb[cur][v][r];
-              if ((posm[u / GW] >> (u % GW)) & 1u) S.nb[nxt][q][r] = S.map[u];
-            }
-          } else {
-            const unsigned tr = S.tri[cur][v];
+          for (int k = 0; k < VPL; ++k) {
+            const int d0 = ex_idx[k] + hb + __popc(hasnew[k] & ((1u << lane) - 1u));
+            hb += __popc(hasnew[k]);
+            if (nnew[k] == 0) continue;
+            const int v = GW * k + lane;
+            const unsigned tr = S.tri[v];
             int j = 0;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              const int u = S.nb[cur][v][r];
-              if (!((posm[u / GW] >> (u % GW)) & 1u)) continue;
-              const int q = nkept + new_idx[k] + j++;
+              const int u = (nbw[k] >> (8 * r)) & 0xff;
+              if (!slot_in<GW>(posm, u)) continue;
+              const int q = j == 0 ? v : mask_nth<GW, VPL>(extra, ex_idx[k] + j - 1);
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
-              double K[4], F, KMv;
-              d_fb += new_vertex(S, C, cur, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
-#pragma unroll
-              for (int m = 0; m < 4; ++m) S.K[nxt][q][m] = K[m];
-              S.F[nxt][q] = F;
-              S.KM[nxt][q] = KMv;
-              S.tri[nxt][q] = tri_pack(x, y, sid);
-              const int mu = S.map[u];
-              S.nb[nxt][q][0] = (unsigned char)mu;
-              const int ru = S.nb[cur][u][0] == v ? 0 : (S.nb[cur][u][1] == v ? 1 : 2);
-              S.nb[nxt][mu][ru] = (unsigned char)q;
+              S.dsc[d0 + j] = (unsigned)u | ((unsigned)v << 8) | ((unsigned)x << 16) |
+                              ((unsigned)y << 24);
+              S.dq[d0 + j] = (unsigned char)q;
+              ++j;
             }
           }
+        }
+        const int n_new = mask_count<VPL>(hasnew) + ex_base;
+        __syncwarp(FULL);
+        for (int d = lane; d < n_new; d += GW) {
+          const unsigned ds = S.dsc[d];
+          const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
+          double K[4], F, KMv;
+          d_fb += new_vertex(S, C, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) S.Kn[d][m] = K[m];
+          S.Fn[d] = F;
+          S.KMn[d] = KMv;
+          // u's link across the edge to v now leads to the new vertex (only this lane touches
+          // that byte; the entries other lanes search for are never equal to v)
+          const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
+          S.nb[u][ru] = S.dq[d];
+        }
+        __syncwarp(FULL);
+        for (int d = lane; d < n_new; d += GW) {
+          const unsigned ds = S.dsc[d];
+          const int q = S.dq[d];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) S.K[q][m] = S.Kn[d][m];
+          S.F[q] = S.Fn[d];
+          S.KM[q] = S.KMn[d];
+          S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
+          S.nb[q][0] = (unsigned char)(ds & 0xff);
         }
         __syncwarp(FULL);
         // close the cycle of new vertices around the new facet s
+        unsigned newm[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) newm[k] = hasnew[k] | extra[k];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          if (GW * k >= nv2) break;  // slots beyond the vertex count
+          if (!newm[k]) continue;
           const int q = GW * k + lane;
-          if (q >= nkept && q < nv2) {
-            const unsigned tr = S.tri[nxt][q];
+          if ((newm[k] >> lane) & 1u) {
+            const unsigned tr = S.tri[q];
             const int x = tri_at(tr, 0), y = tri_at(tr, 1);
             int n1 = q, n2 = q;
-            for (int w = nkept; w < nv2; ++w) {
-              const unsigned tw = S.tri[nxt][w];
-              if (tri_at(tw, 0) == y) n1 = w;
-              if (tri_at(tw, 1) == x) n2 = w;
+#pragma unroll
+            for (int kk = 0; kk < VPL; ++kk) {
+              unsigned m = newm[kk];
+              while (m) {
+                const int w = GW * kk + __ffs(m) - 1;
+                m &= m - 1u;
+                const unsigned tw = S.tri[w];
+                if (tri_at(tw, 0) == y) n1 = w;
+                if (tri_at(tw, 1) == x) n2 = w;
+              }
             }
-            S.nb[nxt][q][1] = (unsigned char)n1;
-            S.nb[nxt][q][2] = (unsigned char)n2;
+            S.nb[q][1] = (unsigned char)n1;
+            S.nb[q][2] = (unsigned char)n2;
           }
         }
-        c_constr += new_base;
-        nv = nv2;
-        cur = nxt;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) live[k] = posm[k] | newm[k];
+        c_constr += n_new;
+        nv = mask_count<VPL>(live);
         __syncwarp(FULL);
+        PHASE_MARK(3);
       }
     }
 
@@ -577,10 +656,10 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     facets_all.clear();
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
-      mytri[k] = v < nv ? S.tri[cur][v] : 0xffffffu;
-      if (v < nv) facets_all.set_tri(mytri[k]);
+      const bool lv = (live[k] >> lane) & 1u;
+      mytri[k] = lv ? S.tri[v] : 0xffffffu;
+      if (lv) facets_all.set_tri(mytri[k]);
     }
     facets_all.warp_or(FULL);
     Bits<VPL> facets = facets_all;
@@ -598,7 +677,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         Q.clear();
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
-          if (GW * k + lane < nv && tri_has(mytri[k], f)) Q.set_tri(mytri[k]);
+          if (((live[k] >> lane) & 1u) && tri_has(mytri[k], f)) Q.set_tri(mytri[k]);
         Q.warp_or(FULL);
         Q.w[f >> 5] &= ~(1u << (f & 31));
         bool zero_area = false;
@@ -606,15 +685,14 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           bool on = true;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
-            if (GW * k >= nv) break;  // slots beyond the vertex count
             const int v = GW * k + lane;
-            if (v < nv && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
-              const double* K = S.K[cur][v];
+            if (((live[k] >> lane) & 1u) && tri_has(mytri[k], f) && !tri_has(mytri[k], q)) {
+              const double* K = S.K[v];
               const double* gq = S.g[q];
               const double val =
                   fma(gq[0], K[0], fma(gq[1], K[1], fma(gq[2], K[2], gq[3] * K[3])));
               const double sa = fabs(gq[0]) + fabs(gq[1]) + fabs(gq[2]) + fabs(gq[3]);
-              if (fabs(val) > sa * S.F[cur][v]) {
+              if (fabs(val) > sa * S.F[v]) {
                 on = false;
               } else {
                 on = on && exact_is_zero(S, C, mytri[k], q);
@@ -659,21 +737,21 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     }
     const unsigned facemask = __reduce_or_sync(FULL, fmask_bits);
     __syncwarp(FULL);
+    PHASE_MARK(4);
 
     // ---- geometry: vertex coordinates relative to V0 (lattice units); facet fan apex =
     // lowest vertex of the facet
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
-      if (v < nv) {
+      if ((live[k] >> lane) & 1u) {
         double K[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) K[m] = S.K[cur][v][m];
+        for (int m = 0; m < 4; ++m) K[m] = S.K[v][m];
         double sum = K[0] + K[1] + K[2] + K[3];
         // coordinates need |dx| <= 1.5e-11 diam(t): 15 F / sum <= 1.5e-11;
         // edge-interpolated vertices that miss it are rebuilt from their planes, then exactly
-        if (16.0 * S.F[cur][v] > 1e-12 * sum) {
+        if (16.0 * S.F[v] > 1e-12 * sum) {
           double F2, KM2;
           int dummy = 0;
           vertex_from_planes(S, C, tri_at(mytri[k], 0), tri_at(mytri[k], 1),
@@ -703,14 +781,13 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     double vol6 = 0.0, m24[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      if (GW * k >= nv) break;  // slots beyond the vertex count
       const int v = GW * k + lane;
-      if (v < nv) {
+      if ((live[k] >> lane) & 1u) {
         const double* xv = S.x[v];
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
           const int f = tri_at(mytri[k], r);
-          const int w = S.nb[cur][v][(r + 2) % 3];  // next vertex of facet f (edge (., f))
+          const int w = S.nb[v][(r + 2) % 3];  // next vertex of facet f (edge (., f))
           const double* xr = S.x[S.ref[f]];
           const double* xw = S.x[w];
           const double det = xr[0] * (xv[1] * xw[2] - xv[2] * xw[1]) -
@@ -739,7 +816,12 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       out.fm[p] = (uint8_t)facemask;
     }
     __syncwarp(FULL);
+    PHASE_MARK(5);
   }
+#ifdef RPD_CLIP_PHASES
+  if (lane == 0)
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_phase[k], (unsigned long long)ph[k]);
+#endif
   // statistics: per-lane counters summed over the warp, group-uniform ones by group leaders
   for (int o = 16; o > 0; o >>= 1) {
     n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
@@ -826,6 +908,21 @@ __global__ void k_piece_off(int64_t T, const int32_t* __restrict__ cand_off,
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+void clip_phase_dump() {
+#ifdef RPD_CLIP_PHASES
+  unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyFromSymbol(h, g_phase, sizeof(h));
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  double tot = 0;
+  for (int k = 0; k < 6; ++k) tot += (double)h[k];
+  const char* nm[6] = {"setup", "classify", "sign", "cut", "facets+inc", "geometry+store"};
+  fprintf(stderr, "[rpd clip phases] group-cycles");
+  for (int k = 0; k < 6; ++k) fprintf(stderr, "  %s %.1f%%", nm[k], 100.0 * h[k] / (tot > 0 ? tot : 1));
+  fprintf(stderr, "  total %.3e\n", tot);
+#endif
+}
 
 template <int GW, int VPL>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,

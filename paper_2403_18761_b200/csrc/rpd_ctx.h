@@ -159,6 +159,7 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                  const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                                  bool reuse_rows, int epoch);
+void clip_phase_dump();  // development aid (RPD_CLIP_PHASES builds)
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
