@@ -368,7 +368,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   const int32_t* moff = cs.moff.as<int32_t>();
-  CK(cudaMemsetAsync(c->p_mask.p, 0, sizeof(unsigned) * cs.n_words, c->stream), "memset");
+  // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
   CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
                      sizeof(unsigned long long) * 5, c->stream), "memset");

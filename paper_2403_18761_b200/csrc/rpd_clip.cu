@@ -38,6 +38,10 @@
 #define RPD_CLIP_MINB 2  // min resident 256-thread blocks per SM for the fast kernel
 #endif
 
+#ifndef RPD_CLIP_PRELOAD
+#define RPD_CLIP_PRELOAD 0  // 1: load nbr_idx / twin of every classified plane (not only cutters)
+#endif
+
 namespace rpd {
 
 template <int GW, int VPL>
@@ -54,13 +58,15 @@ struct WarpState {
   unsigned tri[MAXV];      // oriented plane triplet of every vertex (3 x 8 bits)
   unsigned char nb[MAXV][4];  // vertex across edge r = (tri[r], tri[r+1]) of the dual
   unsigned char vx[MAXV];  // 1 if the current sign was decided by the exact path
-  double Kn[MAXV][4];      // staging of the new vertices of a cut (K, F, KM)
-  double Fn[MAXV];
-  double KMn[MAXV];
+  static constexpr int MAXS = VPL > 1 ? MAXV : 1;
+  double Kn[MAXS][4];      // staging of the new vertices of a cut when they outnumber the lanes
+  double Fn[MAXS];
+  double KMn[MAXS];
   unsigned dsc[MAXV];      // new-vertex descriptors: u | v << 8 | x << 16 | y << 24
   unsigned char dq[MAXV];  // and their target slots
   int src[MAXP];           // radical: sphere j; tet face k: -1-k
   int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
+  int tw[MAXP];            // twin[eidx] (next coincident CSR entry of the row), -1 if none
   int ref[MAXP];           // reference vertex of every facet (fan apex)
 };
 
@@ -358,18 +364,41 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
   int d_sign = 0, d_out = 0, d_fb = 0;  // diagnostics
   // algorithmic work (warp-uniform quantities, counted once per warp)
-  long long c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;
+  unsigned c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;  // per group: small
 #ifdef RPD_CLIP_PHASES
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ph_t = clock64();
 #endif
 
+  // software pipeline of the pair's index loads: level 1 (pair -> tet, sphere) is fetched one
+  // pair ahead at the top of the loop, level 2 (tet corners, CSR row bounds) once the plane
+  // loop is done, so the dependent global loads overlap the previous pair's work
+  int64_t pf_p = 0;
+  int pf_a = 0, pf_i = 0, pf_e0 = 0, pf_e1 = 0, pf_mo = 0;
+  double pf_tx = 0.0;
+  auto fetch1 = [&](int64_t pj) {
+    pf_p = pair_list ? (int64_t)pair_list[pj] : pj;
+    pf_a = pair_tet[pf_p];
+    pf_i = cand_idx[pf_p];
+    pf_mo = out.mask_off[pf_p];
+  };
+  auto fetch2 = [&]() {
+    const int64_t t = tet_ids ? (int64_t)tet_ids[pf_a] : (int64_t)pf_a;
+    if (lane < 12) pf_tx = __ldg(tx + lane * T + t);
+    pf_e0 = __ldg(nbr_off + pf_i);
+    pf_e1 = __ldg(nbr_off + pf_i + 1);
+  };
+  if (gw < n_pairs) {
+    fetch1(gw);
+    fetch2();
+  }
   for (int64_t pi = gw; pi < n_pairs; pi += nw) {
-    const int64_t p = pair_list ? (int64_t)pair_list[pi] : pi;
-    const int64_t a = pair_tet[p];
-    const int64_t t = tet_ids ? (int64_t)tet_ids[a] : a;
-    const int i = cand_idx[p];
-    for (int q = lane; q < 12; q += GW) (&S.V[0][0])[q] = __ldg(tx + q * T + t);
+    const int64_t p = pf_p;
+    const int e0 = pf_e0, e1 = pf_e1, mo = pf_mo;
+    const int nwp = (e1 - e0 + 31) >> 5;  // incidence-mask words of the pair
+    if (lane < 12) (&S.V[0][0])[lane] = pf_tx;
+    const bool has_next = pi + nw < n_pairs;
+    if (has_next) fetch1(pi + nw);
     if (lane < 4) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -378,6 +407,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       }
       S.src[lane] = -1 - lane;
       S.eidx[lane] = -1;
+      S.tw[lane] = -1;
       S.F[lane] = 0.0;
       S.KM[lane] = 1.0;
       S.tri[lane] = CORNER_TRI[lane];
@@ -390,7 +420,6 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     unsigned live[VPL];  // live vertex slots (group-uniform)
 #pragma unroll
     for (int k = 0; k < VPL; ++k) live[k] = k == 0 ? 0xfu : 0u;
-    const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     c_planes += e1 - e0;
 
     for (int base = e0; base < e1 && status == ST_ALIVE; base += GW) {
@@ -398,8 +427,13 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       const bool have = e < e1;
       double g[4] = {0.0, 0.0, 0.0, 0.0};
       bool allpos = false, allneg = false;
+      int jn = 0, twn = -1;
       if (have) {
         const double4 pl = planes[e];
+#if RPD_CLIP_PRELOAD
+        jn = __ldg(nbr_idx + e);
+        twn = __ldg(twin + e);
+#endif
         allpos = true;
         allneg = true;
 #pragma unroll
@@ -422,6 +456,13 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #pragma unroll
         for (int k = 0; k < 4; ++k) s[k] = __shfl_sync(FULL, g[k], l, GW);
         const int es = base + l;
+#if RPD_CLIP_PRELOAD
+        const int js = __shfl_sync(FULL, jn, l, GW);
+        const int tws = __shfl_sync(FULL, twn, l, GW);
+#else
+        const int js = __ldg(nbr_idx + es);
+        const int tws = __ldg(twin + es);
+#endif
         const double sabs = fabs(s[0]) + fabs(s[1]) + fabs(s[2]) + fabs(s[3]);
 
         // ---- sign of every vertex slot
@@ -446,7 +487,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
             else if (val < -B) sg[k] = -1;
             else {
               int zh = 0;
-              sg[k] = exact_sign(S, C, S.tri[v], -1, s, es, nbr_idx[es], &zh);
+              sg[k] = exact_sign(S, C, S.tri[v], -1, s, es, js, &zh);
               S.vx[v] = 1;
               ++n_exact;
               ++d_sign;
@@ -490,8 +531,9 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) S.g[sid][k] = s[k];
-          S.src[sid] = nbr_idx[es];
+          S.src[sid] = js;
           S.eidx[sid] = es;
+          S.tw[sid] = tws;
         }
         __syncwarp(FULL);
         // ---- new vertices, in place: one per boundary edge of the conflict region (a removed
@@ -574,30 +616,55 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         }
         const int n_new = mask_count<VPL>(hasnew) + ex_base;
         __syncwarp(FULL);
-        for (int d = lane; d < n_new; d += GW) {
-          const unsigned ds = S.dsc[d];
-          const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
-          double K[4], F, KMv;
-          d_fb += new_vertex(S, C, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
+        if (VPL == 1 || n_new <= GW) {  // (VPL == 1: n_new <= MAXV = GW always)
+          // one new vertex per lane, held in registers across the sync
+          double K[4], F = 0.0, KMv = 0.0;
+          unsigned ds = 0u;
+          int q = 0;
+          if (lane < n_new) {
+            ds = S.dsc[lane];
+            q = S.dq[lane];
+            const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
+            d_fb += new_vertex(S, C, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
+            // u's link across the edge to v now leads to the new vertex (only this lane
+            // touches that byte; the entries other lanes search for are never equal to v)
+            const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
+            S.nb[u][ru] = (unsigned char)q;
+          }
+          __syncwarp(FULL);
+          if (lane < n_new) {
 #pragma unroll
-          for (int m = 0; m < 4; ++m) S.Kn[d][m] = K[m];
-          S.Fn[d] = F;
-          S.KMn[d] = KMv;
-          // u's link across the edge to v now leads to the new vertex (only this lane touches
-          // that byte; the entries other lanes search for are never equal to v)
-          const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
-          S.nb[u][ru] = S.dq[d];
-        }
-        __syncwarp(FULL);
-        for (int d = lane; d < n_new; d += GW) {
-          const unsigned ds = S.dsc[d];
-          const int q = S.dq[d];
+            for (int m = 0; m < 4; ++m) S.K[q][m] = K[m];
+            S.F[q] = F;
+            S.KM[q] = KMv;
+            S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
+            S.nb[q][0] = (unsigned char)(ds & 0xff);
+          }
+        } else {
+          // more new vertices than lanes (wide kernel only): staged in shared memory
+          for (int d = lane; d < n_new; d += GW) {
+            const unsigned ds = S.dsc[d];
+            const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
+            double K[4], F, KMv;
+            d_fb += new_vertex(S, C, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
 #pragma unroll
-          for (int m = 0; m < 4; ++m) S.K[q][m] = S.Kn[d][m];
-          S.F[q] = S.Fn[d];
-          S.KM[q] = S.KMn[d];
-          S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
-          S.nb[q][0] = (unsigned char)(ds & 0xff);
+            for (int m = 0; m < 4; ++m) S.Kn[d][m] = K[m];
+            S.Fn[d] = F;
+            S.KMn[d] = KMv;
+            const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
+            S.nb[u][ru] = S.dq[d];
+          }
+          __syncwarp(FULL);
+          for (int d = lane; d < n_new; d += GW) {
+            const unsigned ds = S.dsc[d];
+            const int q = S.dq[d];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) S.K[q][m] = S.Kn[d][m];
+            S.F[q] = S.Fn[d];
+            S.KM[q] = S.KMn[d];
+            S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
+            S.nb[q][0] = (unsigned char)(ds & 0xff);
+          }
         }
         __syncwarp(FULL);
         // close the cycle of new vertices around the new facet s
@@ -636,6 +703,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       }
     }
 
+    if (has_next) fetch2();
     // ------------------------------------------------------------------ outputs
     if (status != ST_ALIVE) {
       if (status == ST_OVER) {
@@ -708,7 +776,11 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 
     // incidences: every positive-area facet plus its exactly coincident sources
     unsigned fmask_bits = 0;
-    unsigned* words = out.incmask + out.mask_off[p];
+    unsigned* words = out.incmask + mo;
+    // the pair's mask words are zeroed here (no memset pass) and then set by fire-and-forget
+    // atomics (the group's zero stores are ordered before them by the warp sync)
+    for (int w = lane; w < nwp; w += GW) words[w] = 0u;
+    __syncwarp(FULL);
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int pl = GW * k + lane;
@@ -728,9 +800,13 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
               az = q;
             }
           if (nz == 1 && gg[az] > 0.0) fmask_bits |= 1u << az;
-          for (int e = S.eidx[pl]; e >= 0; e = twin[e]) {
+          int e = S.eidx[pl];
+          int nx = S.tw[pl];
+          while (e >= 0) {
             const int pos = e - e0;
             atomicOr(words + (pos >> 5), 1u << (pos & 31));
+            e = nx;
+            if (e >= 0) nx = twin[e];
           }
         }
       }
