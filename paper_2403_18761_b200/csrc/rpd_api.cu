@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -137,8 +139,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
                     &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
                     &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
-                    &c->slab, &c->w_off, &c->bvh, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
-                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_scan, &c->i_scan, &c->d_count,
+                    &c->slab, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
+                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch};
@@ -236,6 +238,29 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   return RPD_OK;
 }
 
+// development trace (env RPD_TRACE_HOST=1): marks on the host clock and on the ctx stream
+static void tmark(rpd_ctx* c, const char* name) {
+  if (c->tr_on < 0) c->tr_on = getenv("RPD_TRACE_HOST") ? 1 : 0;
+  if (!c->tr_on || c->tr_n >= 16) return;
+  if (!c->tr_ev[c->tr_n]) cudaEventCreate(&c->tr_ev[c->tr_n]);
+  cudaEventRecord(c->tr_ev[c->tr_n], c->stream);
+  c->tr_h[c->tr_n] = std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now().time_since_epoch()).count();
+  c->tr_nm[c->tr_n++] = name;
+}
+static void tdump(rpd_ctx* c) {
+  if (c->tr_on != 1 || c->tr_n == 0) return;
+  cudaEventSynchronize(c->tr_ev[c->tr_n - 1]);
+  fprintf(stderr, "[rpd trace]");
+  for (int k = 0; k < c->tr_n; ++k) {
+    float g = 0.f;
+    cudaEventElapsedTime(&g, c->tr_ev[0], c->tr_ev[k]);
+    fprintf(stderr, " %s h%.3f/g%.3f", c->tr_nm[k], c->tr_h[k] - c->tr_h[0], g);
+  }
+  fprintf(stderr, "\n");
+  c->tr_n = 0;
+}
+
 // Alg. 1 over tets (tet_ids, or all ctx tets when NULL) x spheres [lo, hi) -> candidate set
 // restricted re-filter of dirty tets (partial update, pruned mode): only the spheres of
 // `list` (changed rows) are traversed, the old candidates with unchanged rows are kept
@@ -267,6 +292,7 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                        rs->n_list_dev), "filter");
       CK(launch_keep_old(c, tet_ids, n_tets, *rs->old, cap, c->k_tet.as<int32_t>(),
                          c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "keep old");
+      tmark(c, "refilter+keep");
       // the all-pairs kernel counted its own max; the BVH path recomputes it
       CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
                          sizeof(unsigned long long), c->stream), "memset");
@@ -364,12 +390,14 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(c->p_m1.ensure(sizeof(double) * 3 * nn), "alloc");
   CK(c->p_ninc.ensure(sizeof(int32_t) * nn), "alloc");
   CK(c->p_over.ensure(sizeof(int32_t) * (n + 1)), "alloc");
+  CK(c->p_over2.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->p_mask.ensure(sizeof(unsigned) * (cs.n_words > 0 ? cs.n_words : 1)), "alloc");
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   const int32_t* moff = cs.moff.as<int32_t>();
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
   CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
+  CK(cudaMemsetAsync(c->p_over2.p, 0, sizeof(int32_t), c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
                      sizeof(unsigned long long) * 5, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
@@ -377,11 +405,14 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   if (c->profile) cudaEventRecord(c->ev[2], c->stream);
   CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff,
                  c->clip_wide), "clip");
+  tmark(c, "clip-fast");
   if (!c->clip_wide && n > 0)
     CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff),
        "clip (wide)");
+  tmark(c, "clip-wide");
   if (c->profile) cudaEventRecord(c->ev[3], c->stream);
   CK(launch_piece_scans(c, n, moff), "scan");
+  tmark(c, "piece-scans");
   Readback* rb = (Readback*)c->pinned;
   int64_t np = n, ni = 32 * (int64_t)cs.n_words;
   if (!deferred) {
@@ -526,6 +557,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     return fill_pieces(c, out);
   }
   const int32_t* d_new = nullptr;
+  tmark(c, "start");
   CK(resolve(c, new_ids, M, c->h_new, &d_new), "stage new ids");
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
@@ -533,6 +565,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   ++c->epoch;
   rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, true, c->epoch);
   if (s) return s;
+  tmark(c, "staged");
   c->last.N = N_new;
 
   // (1) dirty tets: Alg. 1 of every tet against the new spheres only
@@ -543,6 +576,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   if (c->profile) cudaEventRecord(c->ev[0], c->stream);
   CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(), nullptr,
                    nullptr), "dirty filter");
+  tmark(c, "dirty-filter");
   if (c->profile) cudaEventRecord(c->ev[1], c->stream);
   CK(c->min_epoch.ensure(sizeof(int)), "alloc");
   CK(launch_dirty_list(c, T), "dirty list");
@@ -562,6 +596,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, 2 * sizeof(int32_t),
                        cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaStreamSynchronize(c->stream), "dirty");
+  tmark(c, "dirty-sync");
   const int32_t need = rb->i32[2] > rb->i32[3] ? rb->i32[2] : rb->i32[3];
   if (need > c->bvh_cap_items) {
     // work queue overflow (never seen): grow it and redo the dirty detection
@@ -597,8 +632,10 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
   }
   if (s) return s;
+  tmark(c, "filter-sync");
   s = run_clip(c, c->cand_d, dl, c->pcs_d, /*deferred=*/true);
   if (s) return s;
+  tmark(c, "clip-launched");
 
   // (4) merge clean old tets + dirty new tets into the other buffer set.  Sized by host upper
   // bounds; the exact totals, the clip overflow counter and the stats come back in one
@@ -628,6 +665,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(pn.inc_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
   CK(pn.inc.ensure(sizeof(int32_t) * (pn.n_inc > 0 ? pn.n_inc : 1)), "alloc");
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
+  tmark(c, "merge-counts");
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 1), "merge copy");
   const int32_t* m_off = c->m_off.as<int32_t>();
   CK(cudaMemcpyAsync(&rb->i32[0], cn.off.as<int32_t>() + T, sizeof(int32_t),
@@ -647,6 +685,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
                      cudaMemcpyDeviceToHost, c->stream), "readback");
   CK(cudaStreamSynchronize(c->stream), "partial update");
+  tmark(c, "final-sync");
+  tdump(c);
   if (rb->u64[ST_OVERFLOW])
     return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
   absorb_clip_stats(c, rb, rb->i32[4]);

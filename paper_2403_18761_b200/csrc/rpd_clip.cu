@@ -336,7 +336,7 @@ struct PairOut {
   uint8_t* fm;
   unsigned* incmask;   // incidence bitmask words of every pair (positions in N(i))
   const int32_t* mask_off;
-  int32_t* over_list;  // pairs that overflowed (fast kernel only)
+  int32_t* over_list;  // pairs that overflowed (re-run by the next wider kernel)
   int32_t* over_count;
 };
 
@@ -1004,7 +1004,7 @@ template <int GW, int VPL>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
-                                 bool collect_overflow, const int32_t* n_dev) {
+                                 int32_t* over, const int32_t* n_dev) {
   constexpr int THREADS = VPL <= 2 ? 256 : 64;
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
@@ -1022,8 +1022,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
-            collect_overflow ? c->p_over.as<int32_t>() + 1 : nullptr,
-            collect_overflow ? c->p_over.as<int32_t>() : nullptr};
+            over ? over + 1 : nullptr, over};
   k_clip<GW, VPL><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
@@ -1034,23 +1033,29 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
 }
 
 // fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
-// or the wide kernel over all pairs when `wide`
+// or the widest kernel over all pairs when `wide`
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
                         int wide) {
   if (n_pairs == 0) return cudaSuccess;
   if (wide)
-    return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, false,
+    return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, nullptr,
                                 nullptr);
   return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                  cand_idx, moff, true, nullptr);
+                                                  cand_idx, moff, c->p_over.as<int32_t>(),
+                                                  nullptr);
 }
 
-// wide kernel over the overflow list p_over[1 .. p_over[0]] (count read on the device)
+// the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
+// 64-slot kernel <32, 2>; its own overflows (p_over2) by the 128-slot kernel <32, 4>
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
-  return launch_clip_t<32, 4>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids,
-                              cand_idx, moff, false, c->p_over.as<int32_t>());
+  cudaError_t e = launch_clip_t<32, 2>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet,
+                                       tet_ids, cand_idx, moff, c->p_over2.as<int32_t>(),
+                                       c->p_over.as<int32_t>());
+  if (e) return e;
+  return launch_clip_t<32, 4>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
+                              cand_idx, moff, nullptr, c->p_over2.as<int32_t>());
 }
 
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {

@@ -123,6 +123,8 @@ struct rpd_ctx {
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
+  rpd::DevBuf bvh_all;     // leaf + super boxes of the whole mesh (valid per staged mesh)
+  bool bvh_all_valid = false;
   rpd::DevBuf bvh_items;   // (sphere, super node) work queue of the pruned filter
   int64_t bvh_cap_items = 0, bvh_min_items = 0;
   int slab_cap = 32;
@@ -134,7 +136,7 @@ struct rpd_ctx {
   bool have_rel = false, have_pieces = false;
 
   // clip per-pair scratch
-  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_scan, i_scan;
+  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_scan, i_scan;
 
   // partial update scratch
   rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off, m_src;
@@ -147,6 +149,11 @@ struct rpd_ctx {
   rpd_stats last{};
   int profile = 0;             // record CUDA events around the filter and clip kernels
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // development trace of a partial update (env RPD_TRACE_HOST): host and stream timestamps
+  int tr_on = -1, tr_n = 0;
+  cudaEvent_t tr_ev[16] = {};
+  double tr_h[16] = {};
+  const char* tr_nm[16] = {};
   void* pinned = nullptr;      // small pinned host buffer for scalar readbacks
   int clip_wide = 0;           // testing: run every pair through the wide kernel
 };

@@ -547,17 +547,23 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
   if (c->filter_mode == RPD_FILTER_PRUNED) {
     const int64_t n_leaf = (n_tets + BVH_LEAF - 1) / BVH_LEAF;
     const int64_t n_sup = (n_leaf + BVH_FAN - 1) / BVH_FAN;
-    cudaError_t e = c->bvh.ensure(sizeof(double) * 6 * (n_leaf + n_sup));
+    // boxes of the whole mesh depend on the mesh only: built once per rpd_relations and
+    // reused by the dirty-tet detection of every partial update; subsets are rebuilt
+    DevBuf& bb = tet_ids ? c->bvh : c->bvh_all;
+    cudaError_t e = bb.ensure(sizeof(double) * 6 * (n_leaf + n_sup));
     if (e) return e;
-    double* leaf = c->bvh.as<double>();
+    double* leaf = bb.as<double>();
     double* sup = leaf + 6 * n_leaf;
     e = cudaMemsetAsync(k_tet, 0, sizeof(int32_t) * n_tets, c->stream);
     if (!e && k_words) e = cudaMemsetAsync(k_words, 0, sizeof(int32_t) * n_tets, c->stream);
     if (e) return e;
-    k_leaf_boxes<<<nblk(n_leaf * BVH_LEAF, 256), 256, 0, c->stream>>>(
-        c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf);
-    k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup);
-    c->launches += 2;
+    if (tet_ids || !c->bvh_all_valid) {
+      k_leaf_boxes<<<nblk(n_leaf * BVH_LEAF, 256), 256, 0, c->stream>>>(
+          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf);
+      k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup);
+      c->launches += 2;
+      if (!tet_ids) c->bvh_all_valid = true;
+    }
     const int64_t ns = sphere_hi - sphere_lo;
     if (ns > 0) {
       int sms = 148;

@@ -291,6 +291,7 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
   if (e) return e;
   s.T = T;
   s.V = V;
+  c->bvh_all_valid = false;
   int* err = c->errw.as<int>();
   if (c->validate && V > 0) {
     k_check_verts<<<nblk(3 * V, 256), 256, 0, c->stream>>>(verts, 3 * V, err);
