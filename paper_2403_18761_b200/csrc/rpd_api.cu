@@ -81,12 +81,33 @@ const char* err_kind_str(int k) {
   }
 }
 
-// read k int32/int64 device scalars into the pinned buffer and synchronise
+// host round trips: up to 8 int32 device scalars, the stats and the error word are gathered
+// by one tiny kernel straight into mapped pinned memory (no copy-engine operations)
 struct Readback {
   int32_t i32[8];
   unsigned long long u64[ST_N];
   int32_t err[4];
 };
+
+struct RbSpec {
+  const int32_t* i32[8];           // nullptr -> 0
+  const unsigned long long* u64;   // stats (ST_N words) or nullptr (kept)
+  const int* err;                  // error word (4) or nullptr (kept)
+};
+
+__global__ void k_readback(RbSpec s, Readback* rb) {
+  const int t = threadIdx.x;
+  if (t < 8) rb->i32[t] = s.i32[t] ? *s.i32[t] : 0;
+  if (s.u64 && t < ST_N) rb->u64[t] = s.u64[t];
+  if (s.err && t < 4) rb->err[t] = s.err[t];
+  __threadfence_system();
+}
+
+cudaError_t readback(rpd_ctx* c, const RbSpec& s) {
+  k_readback<<<1, 32, 0, c->stream>>>(s, (Readback*)c->pinned_dev);
+  ++c->launches;
+  return cudaGetLastError();
+}
 
 rpd_status check_err(rpd_ctx* c, const Readback* rb) {
   if (rb->err[0] != 0) {
@@ -123,7 +144,8 @@ rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream) {
     c->own_stream = true;
   }
   if (c->errw.ensure(sizeof(int) * 4) || c->stats.ensure(sizeof(unsigned long long) * ST_N) ||
-      cudaMallocHost(&c->pinned, sizeof(Readback))) {
+      cudaHostAlloc(&c->pinned, sizeof(Readback), cudaHostAllocMapped) ||
+      cudaHostGetDevicePointer(&c->pinned_dev, c->pinned, 0)) {
     rpd_destroy(c);
     return RPD_ENOMEM;
   }
@@ -141,7 +163,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_scan, &c->i_scan, &c->d_count,
-                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->m_src, &c->c_scan, &c->c_list,
+                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch};
   for (DevBuf* b : bufs) b->release();
@@ -213,8 +235,7 @@ static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t*
     *E = nbr_off[N];
   } else {
     Readback* rb = (Readback*)c->pinned;
-    CK(cudaMemcpyAsync(&rb->i32[0], nbr_off + N, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       c->stream), "read nbr_off[N]");
+    CK(readback(c, RbSpec{{nbr_off + N}, nullptr, nullptr}), "read nbr_off[N]");
     CK(cudaStreamSynchronize(c->stream), "sync");
     *E = rb->i32[0];
   }
@@ -304,18 +325,13 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
     if (timed && c->profile) cudaEventRecord(c->ev[1], c->stream);
     CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), cs.off.as<int32_t>(), n_tets), "scan");
     CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), n_tets), "scan");
-    CK(cudaMemcpyAsync(&rb->i32[0], cs.off.as<int32_t>() + n_tets, sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(&rb->i32[1], c->w_off.as<int32_t>() + n_tets, sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
+    const bool bvh = c->filter_mode == RPD_FILTER_PRUNED &&
+                     (rs ? rs->n_list_max > 0 : hi > lo) && n_tets > 0;
+    const int32_t* nq = bvh ? c->bvh_items.as<int32_t>() : nullptr;  // queue counts
+    CK(readback(c, RbSpec{{cs.off.as<int32_t>() + n_tets, c->w_off.as<int32_t>() + n_tets, nq,
+                           nq ? nq + 1 : nullptr},
+                          c->stats.as<unsigned long long>(), c->errw.as<int>()}),
        "readback");
-    rb->i32[2] = rb->i32[3] = 0;
-    if (c->filter_mode == RPD_FILTER_PRUNED && (rs ? rs->n_list_max > 0 : hi > lo) && n_tets > 0)
-      CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, 2 * sizeof(int32_t),
-                         cudaMemcpyDeviceToHost, c->stream), "readback");
     CK(cudaStreamSynchronize(c->stream), "filter");
     rpd_status s = check_err(c, rb);
     if (s) return s;
@@ -416,14 +432,10 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   Readback* rb = (Readback*)c->pinned;
   int64_t np = n, ni = 32 * (int64_t)cs.n_words;
   if (!deferred) {
-    CK(cudaMemcpyAsync(&rb->i32[0], c->p_scan.as<int32_t>() + n, sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(&rb->i32[1], c->i_scan.as<int32_t>() + n, sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
-    CK(cudaMemcpyAsync(&rb->i32[2], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       c->stream), "readback");
-    CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(readback(c, RbSpec{{c->p_scan.as<int32_t>() + n, c->i_scan.as<int32_t>() + n,
+                           c->p_over.as<int32_t>()},
+                          c->stats.as<unsigned long long>(), nullptr}),
+       "readback");
     CK(cudaStreamSynchronize(c->stream), "clip");
     if (rb->u64[ST_OVERFLOW])
       return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
@@ -585,16 +597,13 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(c->c_list.ensure(sizeof(int32_t) * (N_new > 0 ? N_new : 1)), "alloc");
   CK(launch_changed_list(c, N_new), "changed rows");
   Readback* rb = (Readback*)c->pinned;
-  CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(rb->err, c->errw.p, sizeof(int) * 4, cudaMemcpyDeviceToHost, c->stream),
-     "readback");
-  CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  rb->i32[2] = rb->i32[3] = 0;
-  if (c->filter_mode == RPD_FILTER_PRUNED && T > 0)
-    CK(cudaMemcpyAsync(&rb->i32[2], c->bvh_items.p, 2 * sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
+  {
+    const int32_t* nq =
+        c->filter_mode == RPD_FILTER_PRUNED && T > 0 ? c->bvh_items.as<int32_t>() : nullptr;
+    CK(readback(c, RbSpec{{c->d_scan.as<int32_t>() + T, nullptr, nq, nq ? nq + 1 : nullptr},
+                          c->stats.as<unsigned long long>(), c->errw.as<int>()}),
+       "readback");
+  }
   CK(cudaStreamSynchronize(c->stream), "dirty");
   tmark(c, "dirty-sync");
   const int32_t need = rb->i32[2] > rb->i32[3] ? rb->i32[2] : rb->i32[3];
@@ -604,8 +613,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(),
                      nullptr, nullptr), "dirty filter");
     CK(launch_dirty_list(c, T), "dirty list");
-    CK(cudaMemcpyAsync(&rb->i32[0], c->d_scan.as<int32_t>() + T, sizeof(int32_t),
-                       cudaMemcpyDeviceToHost, c->stream), "readback");
+    CK(readback(c, RbSpec{{c->d_scan.as<int32_t>() + T}, nullptr, nullptr}), "readback");
     CK(cudaStreamSynchronize(c->stream), "dirty");
   }
   if (rb->err[0] != 0) {
@@ -668,22 +676,11 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   tmark(c, "merge-counts");
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 1), "merge copy");
   const int32_t* m_off = c->m_off.as<int32_t>();
-  CK(cudaMemcpyAsync(&rb->i32[0], cn.off.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[1], pn.off.as<int32_t>() + T, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[2], m_off + T, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                     c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[3], m_off + (T + 1) + T, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                     c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[4], c->p_over.p, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                     c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[5], c->p_scan.as<int32_t>() + cd.n, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(&rb->i32[6], c->i_scan.as<int32_t>() + cd.n, sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
-  CK(cudaMemcpyAsync(rb->u64, c->stats.p, sizeof(unsigned long long) * ST_N,
-                     cudaMemcpyDeviceToHost, c->stream), "readback");
+  CK(readback(c, RbSpec{{cn.off.as<int32_t>() + T, pn.off.as<int32_t>() + T, m_off + T,
+                         m_off + (T + 1) + T, c->p_over.as<int32_t>(),
+                         c->p_scan.as<int32_t>() + cd.n, c->i_scan.as<int32_t>() + cd.n},
+                        c->stats.as<unsigned long long>(), nullptr}),
+     "readback");
   CK(cudaStreamSynchronize(c->stream), "partial update");
   tmark(c, "final-sync");
   tdump(c);

@@ -139,7 +139,7 @@ struct rpd_ctx {
   rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_scan, i_scan;
 
   // partial update scratch
-  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off, m_src;
+  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off;
   rpd::DevBuf c_flag, c_scan, c_list;  // changed-row spheres of a partial update
   rpd::DevBuf cepoch;          // int32 per tet: epoch of its candidate list
   rpd::DevBuf min_epoch;       // int32: oldest candidate-list epoch among the dirty tets
@@ -154,7 +154,8 @@ struct rpd_ctx {
   cudaEvent_t tr_ev[16] = {};
   double tr_h[16] = {};
   const char* tr_nm[16] = {};
-  void* pinned = nullptr;      // small pinned host buffer for scalar readbacks
+  void* pinned = nullptr;      // small mapped pinned host buffer for scalar readbacks
+  void* pinned_dev = nullptr;  // its device-side address
   int clip_wide = 0;           // testing: run every pair through the wide kernel
 };
 

@@ -108,75 +108,83 @@ struct MergeDst {
   int32_t *c_idx, *pair_tet, *c_moff, *p_sphere, *p_inc_off, *p_inc;
   double *p_vol, *p_m1;
   uint8_t* p_fm;
-  int32_t* src_piece;  // per new piece: source piece index, +(1 << 30) when from the dirty set
 };
 
-// last index t in [0, n) with off[t] <= q (off non-decreasing, off[0] = 0)
-__device__ __forceinline__ int64_t seg_of(const int32_t* __restrict__ off, int64_t n, int64_t q) {
-  int64_t lo = 0, hi = n;  // invariant: off[lo] <= q < off[hi]
+constexpr int MT = 256;  // tets per merge tile (one block)
+
+// upper_bound(off[0..n], q) - 1 in shared memory: the tile-local tet of element q
+__device__ __forceinline__ int tile_seg(const int* off, int n, int q) {
+  int lo = 0, hi = n;  // off[lo] <= q < off[hi]
   while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
+    const int mid = (lo + hi) >> 1;
     if (off[mid] <= q) lo = mid;
     else hi = mid;
   }
   return lo;
 }
 
-// The copy kernels read their element counts from the device scans (no host round trip) and
-// stride over them with a grid sized from a host upper bound.
-
-// one thread per merged candidate (+ its incidence-mask word offset)
-__global__ void k_merge_cands(int64_t T, const int32_t* __restrict__ dpos, MergeSrc o,
-                              MergeSrc n, MergeDst D) {
-  const int64_t n_new = D.c_off[T];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_new; q += stride) {
-    const int64_t t = seg_of(D.c_off, T, q);
-    const int d = dpos[t];
-    const MergeSrc& s = d >= 0 ? n : o;
-    const int64_t k = d >= 0 ? d : t;
-    const int64_t src = s.c_off[k] + (q - D.c_off[t]);
-    D.c_idx[q] = s.c_idx[src];
-    D.pair_tet[q] = (int32_t)t;
-    D.c_moff[q] = D.w_tet[t] + (s.c_moff[src] - s.c_moff[s.c_off[k]]);
+// One block per tile of MT consecutive tets: the tile's per-tet destination offsets and
+// source bases (clean tet: old set at t, dirty tet: re-clipped set at its dirty position) are
+// staged in shared memory, then the block copies the tile's candidates, pieces and incidences
+// (each a contiguous destination range) with coalesced element loops; an element's tet is
+// found by binary search over the staged offsets (no global-memory searches).
+__global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __restrict__ dpos,
+                                                    MergeSrc o, MergeSrc n, MergeDst D) {
+  __shared__ int s_nc[MT + 1], s_np[MT + 1], s_ni[MT + 1];
+  __shared__ int s_sc[MT], s_sp[MT], s_si[MT], s_nw[MT], s_sw[MT];
+  __shared__ unsigned char s_dirty[MT];
+  const int64_t t0 = (int64_t)blockIdx.x * MT;
+  const int nt = (int)min((int64_t)MT, T - t0);
+  for (int l = threadIdx.x; l <= nt; l += blockDim.x) {
+    const int64_t t = t0 + l;
+    s_nc[l] = D.c_off[t];
+    s_np[l] = D.p_off[t];
+    s_ni[l] = D.i_tet[t];
+    if (l < nt) {
+      const int d = dpos[t];
+      const MergeSrc& s = d >= 0 ? n : o;
+      const int64_t k = d >= 0 ? d : t;
+      const int c0 = s.c_off[k], p0 = s.p_off[k];
+      s_dirty[l] = d >= 0;
+      s_sc[l] = c0;
+      s_sp[l] = p0;
+      s_si[l] = s.p_inc_off[p0];
+      s_nw[l] = D.w_tet[t];
+      s_sw[l] = s.c_moff[c0];
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) D.c_moff[n_new] = D.w_tet[T];
-}
-
-// one thread per merged piece
-__global__ void k_merge_pieces(int64_t T, const int32_t* __restrict__ dpos, MergeSrc o,
-                               MergeSrc n, MergeDst D) {
-  const int64_t n_new = D.p_off[T];
-  if (blockIdx.x == 0 && threadIdx.x == 0) D.p_inc_off[n_new] = D.i_tet[T];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_new; q += stride) {
-    const int64_t t = seg_of(D.p_off, T, q);
-    const int d = dpos[t];
-    const MergeSrc& s = d >= 0 ? n : o;
-    const int64_t k = d >= 0 ? d : t;
-    const int p0 = s.p_off[k];
-    const int sp = p0 + (int)(q - D.p_off[t]);
+  __syncthreads();
+  // candidates (+ their incidence-mask word offsets)
+  for (int q = s_nc[0] + threadIdx.x; q < s_nc[nt]; q += blockDim.x) {
+    const int l = tile_seg(s_nc, nt, q);
+    const MergeSrc& s = s_dirty[l] ? n : o;
+    const int src = s_sc[l] + (q - s_nc[l]);
+    D.c_idx[q] = s.c_idx[src];
+    D.pair_tet[q] = (int32_t)(t0 + l);
+    D.c_moff[q] = s_nw[l] + (s.c_moff[src] - s_sw[l]);
+  }
+  // pieces
+  for (int q = s_np[0] + threadIdx.x; q < s_np[nt]; q += blockDim.x) {
+    const int l = tile_seg(s_np, nt, q);
+    const MergeSrc& s = s_dirty[l] ? n : o;
+    const int sp = s_sp[l] + (q - s_np[l]);
     D.p_sphere[q] = s.p_sphere[sp];
     D.p_vol[q] = s.p_vol[sp];
-    D.p_m1[3 * q + 0] = s.p_m1[3 * sp + 0];
-    D.p_m1[3 * q + 1] = s.p_m1[3 * sp + 1];
-    D.p_m1[3 * q + 2] = s.p_m1[3 * sp + 2];
+    D.p_m1[3 * (int64_t)q + 0] = s.p_m1[3 * (int64_t)sp + 0];
+    D.p_m1[3 * (int64_t)q + 1] = s.p_m1[3 * (int64_t)sp + 1];
+    D.p_m1[3 * (int64_t)q + 2] = s.p_m1[3 * (int64_t)sp + 2];
     D.p_fm[q] = s.p_fm[sp];
-    D.p_inc_off[q] = D.i_tet[t] + (s.p_inc_off[sp] - s.p_inc_off[p0]);
-    D.src_piece[q] = sp + (d >= 0 ? (1 << 30) : 0);
+    D.p_inc_off[q] = s_ni[l] + (s.p_inc_off[sp] - s_si[l]);
   }
-}
-
-// one thread per merged incidence (after k_merge_pieces: needs p_inc_off and src_piece)
-__global__ void k_merge_incs(int64_t T, MergeSrc o, MergeSrc n, MergeDst D) {
-  const int64_t n_pieces_new = D.p_off[T], n_inc_new = D.i_tet[T];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_inc_new; r += stride) {
-    const int64_t q = seg_of(D.p_inc_off, n_pieces_new, r);
-    const int code = D.src_piece[q];
-    const MergeSrc& s = code >= (1 << 30) ? n : o;
-    const int sp = code & ((1 << 30) - 1);
-    D.p_inc[r] = s.p_inc[s.p_inc_off[sp] + (r - D.p_inc_off[q])];
+  // incidences (a tet's incidences are contiguous in its source set)
+  for (int r = s_ni[0] + threadIdx.x; r < s_ni[nt]; r += blockDim.x) {
+    const int l = tile_seg(s_ni, nt, r);
+    const MergeSrc& s = s_dirty[l] ? n : o;
+    D.p_inc[r] = s.p_inc[s_si[l] + (r - s_ni[l])];
+  }
+  if (t0 + nt == T && threadIdx.x == 0) {  // terminal entries
+    D.c_moff[s_nc[nt]] = D.w_tet[T];
+    D.p_inc_off[s_np[nt]] = s_ni[nt];
   }
 }
 
@@ -187,16 +195,11 @@ static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
                   ps.fm.as<uint8_t>()};
 }
 
-static inline unsigned grid_for(int64_t n_ub) {
-  const int64_t g = (n_ub + 255) / 256;
-  return (unsigned)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
-}
-
 // phase 0: per-tet counts and their scans (new cand offsets -> cn.off, new piece offsets ->
 // pn.off, tet-level incidence offsets -> m_off, tet-level mask-word offsets -> m_off + T + 1);
 // totals at [T] of each.
-// phase 1: copies into cn / pn, sized by the host upper bounds cn.n, pn.n_pieces, pn.n_inc
-// (exact totals are read back by the caller after the copies).
+// phase 1: the tiled copy into cn / pn (allocated by the caller from host upper bounds; the
+// exact totals are read back after the copy).
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase) {
@@ -215,18 +218,15 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
     if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>() + 2 * T, m_off, T))) return e;
     return launch_scan_i32(c, c->m_cnt.as<int32_t>() + 3 * T, w_off, T);
   }
-  cudaError_t e = c->m_src.ensure(sizeof(int32_t) * (pn.n_pieces > 0 ? pn.n_pieces : 1));
-  if (e) return e;
   MergeDst D{cn.off.as<int32_t>(),     pn.off.as<int32_t>(),      m_off,
              w_off,                    cn.idx.as<int32_t>(),      cn.pair_tet.as<int32_t>(),
              cn.moff.as<int32_t>(),    pn.sphere.as<int32_t>(),   pn.inc_off.as<int32_t>(),
              pn.inc.as<int32_t>(),     pn.vol.as<double>(),       pn.m1.as<double>(),
-             pn.fm.as<uint8_t>(),      c->m_src.as<int32_t>()};
-  const int32_t* dpos = c->d_pos.as<int32_t>();
-  k_merge_cands<<<grid_for(cn.n), 256, 0, c->stream>>>(T, dpos, o, n, D);
-  k_merge_pieces<<<grid_for(pn.n_pieces), 256, 0, c->stream>>>(T, dpos, o, n, D);
-  k_merge_incs<<<grid_for(pn.n_inc), 256, 0, c->stream>>>(T, o, n, D);
-  c->launches += 3;
+             pn.fm.as<uint8_t>()};
+  if (T > 0) {
+    k_merge_copy<<<nblk(T, MT), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
+    ++c->launches;
+  }
   return cudaGetLastError();
 }
 
