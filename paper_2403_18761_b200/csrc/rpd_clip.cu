@@ -38,6 +38,9 @@
 #define RPD_CLIP_MINB 2  // min resident 256-thread blocks per SM for the fast kernel
 #endif
 
+#ifndef RPD_CLIP_MID_VPL
+#define RPD_CLIP_MID_VPL 1  // vertex slots per lane of the middle (first overflow) tier, GW = 32
+#endif
 #ifndef RPD_CLIP_PRELOAD
 #define RPD_CLIP_PRELOAD 0  // 1: load nbr_idx / twin of every classified plane (not only cutters)
 #endif
@@ -1047,10 +1050,10 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
 }
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
-// 64-slot kernel <32, 2>; its own overflows (p_over2) by the 128-slot kernel <32, 4>
+// 32-slot kernel <RPD_CLIP_MID_VPL = 1>; its own overflows (p_over2) by the 128-slot <32, 4>
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
-  cudaError_t e = launch_clip_t<32, 2>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet,
+  cudaError_t e = launch_clip_t<32, RPD_CLIP_MID_VPL>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet,
                                        tet_ids, cand_idx, moff, c->p_over2.as<int32_t>(),
                                        c->p_over.as<int32_t>());
   if (e) return e;
