@@ -342,7 +342,7 @@ def main():
         flops = 7.0 * float(np.median([r["rel_tests"] for r in recs]))
         per_unit = "7 flop per literal Alg. 1 vertex test (3 FMA + compare), tests counted by the kernel"
     else:
-        kern, kms = "k_clip<1>+k_clip<4>", cmed
+        kern, kms = "k_clip<16,1>+k_clip<32,1>+k_clip<32,4>", cmed
         flops = float(np.median([r["clip_work"] for r in recs]))
         per_unit = ("24 flop per (pair, plane) corner classification + 8 per vertex sign test + "
                     "40 per vertex construction + 30 per fan triangle, counted by the kernel")
@@ -381,7 +381,8 @@ def main():
                 "d2h_bytes_per_step": int(d2h),
                 "note": "the bench step (full RPD + partial updates) through the C ABI with pinned "
                         "host inputs and a pinned host download of the final pieces"},
-        "gpu_launches": int(launches // max(args.steps, 1)),
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": int(launches // max(args.steps, 1)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
