@@ -323,8 +323,11 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
                        c->slab.as<int32_t>(), c->k_words.as<int32_t>()), "filter");
     }
     if (timed && c->profile) cudaEventRecord(c->ev[1], c->stream);
-    CK(launch_scan_i32(c, c->k_tet.as<int32_t>(), cs.off.as<int32_t>(), n_tets), "scan");
-    CK(launch_scan_i32(c, c->k_words.as<int32_t>(), c->w_off.as<int32_t>(), n_tets), "scan");
+    {
+      const int32_t* in[2] = {c->k_tet.as<int32_t>(), c->k_words.as<int32_t>()};
+      int32_t* out[2] = {cs.off.as<int32_t>(), c->w_off.as<int32_t>()};
+      CK(launch_scan_i32_multi(c, in, out, 2, n_tets), "scan");
+    }
     const bool bvh = c->filter_mode == RPD_FILTER_PRUNED &&
                      (rs ? rs->n_list_max > 0 : hi > lo) && n_tets > 0;
     const int32_t* nq = bvh ? c->bvh_items.as<int32_t>() : nullptr;  // queue counts
@@ -400,7 +403,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   const int64_t n = cs.n, nt = cs.n_tets;
   size_t nn = n > 0 ? n : 1;
   CK(c->p_flag.ensure(nn), "alloc");
-  CK(c->p_f01.ensure(nn), "alloc");
+  CK(c->p_f01.ensure(sizeof(int32_t) * nn), "alloc");
   CK(c->p_fm.ensure(nn), "alloc");
   CK(c->p_vol.ensure(sizeof(double) * nn), "alloc");
   CK(c->p_m1.ensure(sizeof(double) * 3 * nn), "alloc");

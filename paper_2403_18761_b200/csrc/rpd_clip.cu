@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   // loop is done, so the dependent global loads overlap the previous pair's work
   int64_t pf_p = 0;
   int pf_a = 0, pf_i = 0, pf_e0 = 0, pf_e1 = 0, pf_mo = 0;
-  double pf_tx = 0.0;
+  constexpr int NTX = (12 + GW - 1) / GW;  // tet corner coordinates per lane
+  double pf_tx[NTX];
   auto fetch1 = [&](int64_t pj) {
     pf_p = pair_list ? (int64_t)pair_list[pj] : pj;
     pf_a = pair_tet[pf_p];
@@ -387,7 +388,9 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   };
   auto fetch2 = [&]() {
     const int64_t t = tet_ids ? (int64_t)tet_ids[pf_a] : (int64_t)pf_a;
-    if (lane < 12) pf_tx = __ldg(tx + lane * T + t);
+#pragma unroll
+    for (int q = 0; q < NTX; ++q)
+      if (lane + GW * q < 12) pf_tx[q] = __ldg(tx + (lane + GW * q) * T + t);
     pf_e0 = __ldg(nbr_off + pf_i);
     pf_e1 = __ldg(nbr_off + pf_i + 1);
   };
@@ -399,7 +402,9 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     const int64_t p = pf_p;
     const int e0 = pf_e0, e1 = pf_e1, mo = pf_mo;
     const int nwp = (e1 - e0 + 31) >> 5;  // incidence-mask words of the pair
-    if (lane < 12) (&S.V[0][0])[lane] = pf_tx;
+#pragma unroll
+    for (int q = 0; q < NTX; ++q)
+      if (lane + GW * q < 12) (&S.V[0][0])[lane + GW * q] = pf_tx[q];
     const bool has_next = pi + nw < n_pairs;
     if (has_next) fetch1(pi + nw);
     if (lane < 4) {
@@ -455,6 +460,9 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       while (act && status == ST_ALIVE) {
         const int l = __ffs(act) - 1;
         act &= act - 1;
+#ifdef RPD_CLIP_PHASES
+        ++ph[6];
+#endif
         double s[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) s[k] = __shfl_sync(FULL, g[k], l, GW);
@@ -531,6 +539,9 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           break;
         }
         const int sid = np++;
+#ifdef RPD_CLIP_PHASES
+        ++ph[7];
+#endif
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) S.g[sid][k] = s[k];
@@ -899,7 +910,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   }
 #ifdef RPD_CLIP_PHASES
   if (lane == 0)
-    for (int k = 0; k < 6; ++k) atomicAdd(&g_phase[k], (unsigned long long)ph[k]);
+    for (int k = 0; k < 8; ++k) atomicAdd(&g_phase[k], (unsigned long long)ph[k]);
 #endif
   // statistics: per-lane counters summed over the warp, group-uniform ones by group leaders
   for (int o = 16; o > 0; o >>= 1) {
@@ -931,7 +942,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 __global__ void k_count_inc(int64_t n_pairs, const uint8_t* __restrict__ flag,
                             const int32_t* __restrict__ mask_off,
                             const unsigned* __restrict__ mask, int32_t* __restrict__ ninc,
-                            uint8_t* __restrict__ f01) {
+                            int32_t* __restrict__ f01) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   int n = 0;
@@ -999,7 +1010,7 @@ void clip_phase_dump() {
   const char* nm[6] = {"setup", "classify", "sign", "cut", "facets+inc", "geometry+store"};
   fprintf(stderr, "[rpd clip phases] group-cycles");
   for (int k = 0; k < 6; ++k) fprintf(stderr, "  %s %.1f%%", nm[k], 100.0 * h[k] / (tot > 0 ? tot : 1));
-  fprintf(stderr, "  total %.3e\n", tot);
+  fprintf(stderr, "  total %.3e  sign-passes %llu cuts %llu\n", tot, h[6], h[7]);
 #endif
 }
 
@@ -1065,12 +1076,12 @@ cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff)
   if (n_pairs > 0) {
     k_count_inc<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, c->p_flag.as<uint8_t>(), moff, c->p_mask.as<unsigned>(),
-        c->p_ninc.as<int32_t>(), c->p_f01.as<uint8_t>());
+        c->p_ninc.as<int32_t>(), c->p_f01.as<int32_t>());
     ++c->launches;
   }
-  cudaError_t e = launch_scan_u8(c, c->p_f01.as<uint8_t>(), c->p_scan.as<int32_t>(), n_pairs);
-  if (e) return e;
-  return launch_scan_i32(c, c->p_ninc.as<int32_t>(), c->i_scan.as<int32_t>(), n_pairs);
+  const int32_t* in[2] = {c->p_f01.as<int32_t>(), c->p_ninc.as<int32_t>()};
+  int32_t* out[2] = {c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>()};
+  return launch_scan_i32_multi(c, in, out, 2, n_pairs);
 }
 
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,

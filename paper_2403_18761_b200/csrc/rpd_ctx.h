@@ -170,6 +170,8 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
 void clip_phase_dump();  // development aid (RPD_CLIP_PHASES builds)
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
+cudaError_t launch_scan_i32_multi(rpd_ctx* c, const int32_t* const* in, int32_t* const* out,
+                                  int K, int64_t n);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
                           int32_t* k_words, const int32_t* sphere_list = nullptr,

@@ -77,7 +77,7 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
 // ---------------------------------------------------------------- merge
 
 struct MergeSrc {
-  const int32_t *c_off, *c_idx, *c_moff;
+  const int32_t *c_off, *c_idx, *c_moff, *c_pt;
   const int32_t *p_off, *p_sphere, *p_inc_off, *p_inc;
   const double *p_vol, *p_m1;
   const uint8_t* p_fm;
@@ -153,7 +153,35 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       s_sw[l] = s.c_moff[c0];
     }
   }
-  __syncthreads();
+  // a tile without dirty tets is one contiguous range of the old set in every array, moved
+  // by a constant offset: straight streaming copies (most tiles: insertions are local)
+  // (also the barrier after the staging; blockDim.x == MT, so thread l staged s_dirty[l])
+  const int any_dirty = __syncthreads_or(threadIdx.x < nt && s_dirty[threadIdx.x]);
+  if (!any_dirty) {
+    const int nc = s_nc[nt] - s_nc[0], npc = s_np[nt] - s_np[0], ni = s_ni[nt] - s_ni[0];
+    const int c_src = s_sc[0], p_src = s_sp[0], i_src = s_si[0];
+    const int c_dst = s_nc[0], p_dst = s_np[0], i_dst = s_ni[0];
+    const int wshift = s_nw[0] - s_sw[0], ishift = s_ni[0] - s_si[0];
+    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+      D.c_idx[c_dst + k] = o.c_idx[c_src + k];
+      D.pair_tet[c_dst + k] = o.c_pt[c_src + k];
+      D.c_moff[c_dst + k] = o.c_moff[c_src + k] + wshift;
+    }
+    for (int k = threadIdx.x; k < npc; k += blockDim.x) {
+      D.p_sphere[p_dst + k] = o.p_sphere[p_src + k];
+      D.p_vol[p_dst + k] = o.p_vol[p_src + k];
+      D.p_fm[p_dst + k] = o.p_fm[p_src + k];
+      D.p_inc_off[p_dst + k] = o.p_inc_off[p_src + k] + ishift;
+    }
+    for (int k = threadIdx.x; k < 3 * npc; k += blockDim.x)
+      D.p_m1[3 * (int64_t)p_dst + k] = o.p_m1[3 * (int64_t)p_src + k];
+    for (int k = threadIdx.x; k < ni; k += blockDim.x) D.p_inc[i_dst + k] = o.p_inc[i_src + k];
+    if (t0 + nt == T && threadIdx.x == 0) {
+      D.c_moff[s_nc[nt]] = D.w_tet[T];
+      D.p_inc_off[s_np[nt]] = s_ni[nt];
+    }
+    return;
+  }
   // candidates (+ their incidence-mask word offsets)
   for (int q = s_nc[0] + threadIdx.x; q < s_nc[nt]; q += blockDim.x) {
     const int l = tile_seg(s_nc, nt, q);
@@ -190,6 +218,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
 
 static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
   return MergeSrc{cs.off.as<int32_t>(),     cs.idx.as<int32_t>(),     cs.moff.as<int32_t>(),
+                  cs.pair_tet.as<int32_t>(),
                   ps.off.as<int32_t>(),     ps.sphere.as<int32_t>(),  ps.inc_off.as<int32_t>(),
                   ps.inc.as<int32_t>(),     ps.vol.as<double>(),      ps.m1.as<double>(),
                   ps.fm.as<uint8_t>()};
@@ -212,11 +241,10 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
                                                           c->m_cnt.as<int32_t>());
       ++c->launches;
     }
-    cudaError_t e;
-    if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>(), cn.off.as<int32_t>(), T))) return e;
-    if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>() + T, pn.off.as<int32_t>(), T))) return e;
-    if ((e = launch_scan_i32(c, c->m_cnt.as<int32_t>() + 2 * T, m_off, T))) return e;
-    return launch_scan_i32(c, c->m_cnt.as<int32_t>() + 3 * T, w_off, T);
+    const int32_t* cnt = c->m_cnt.as<int32_t>();
+    const int32_t* in[4] = {cnt, cnt + T, cnt + 2 * T, cnt + 3 * T};
+    int32_t* out[4] = {cn.off.as<int32_t>(), pn.off.as<int32_t>(), m_off, w_off};
+    return launch_scan_i32_multi(c, in, out, 4, T);
   }
   MergeDst D{cn.off.as<int32_t>(),     pn.off.as<int32_t>(),      m_off,
              w_off,                    cn.idx.as<int32_t>(),      cn.pair_tet.as<int32_t>(),

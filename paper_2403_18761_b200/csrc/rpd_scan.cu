@@ -1,6 +1,6 @@
 // rpd_scan.cu -- exclusive prefix sums used by the compaction steps:
-// out[k] = sum_{m<k} in[m] for k in [0, n], out[n] = total.  One launch per scan (decoupled
-// look-back over 4096-element tiles).  Deterministic (integer).
+// out[k] = sum_{m<k} in[m] for k in [0, n], out[n] = total.  One launch per scan, or per group of up to
+// four equal-length scans (decoupled look-back over 4096-element tiles).  Deterministic (integer).
 #include "rpd_ctx.h"
 
 namespace rpd {
@@ -53,17 +53,29 @@ __device__ __forceinline__ unsigned long long st_pack(unsigned epoch, unsigned l
   return ((unsigned long long)epoch << 34) | (f << 32) | (unsigned)v;
 }
 
+// K <= 4 arrays of n elements (io.in[a] -> io.out[a]) in one launch: ticket q is tile q % nb
+// of array q / nb, so every tile's look-back predecessors hold smaller tickets.
 template <class T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(const T* __restrict__ in, int64_t n,
-                                                      int* __restrict__ out, int nb,
+struct ScanIO {
+  const T* in[4];
+  int* out[4];
+};
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanIO<T> io, int64_t n, int nb,
                                                       unsigned long long* __restrict__ ticket,
                                                       unsigned long long ticket_base,
-                                                      unsigned long long* state, unsigned epoch) {
+                                                      unsigned long long* state_base,
+                                                      unsigned epoch) {
   __shared__ int sm[32];
   __shared__ int s_tile, s_prefix;
   if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ticket, 1ull) - ticket_base);
   __syncthreads();
-  const int tile = s_tile;
+  const int arr = s_tile / nb;
+  const int tile = s_tile - arr * nb;
+  const T* __restrict__ in = io.in[arr];
+  int* __restrict__ out = io.out[arr];
+  unsigned long long* state = state_base + (int64_t)arr * nb;
   const int64_t base = (int64_t)tile * SCAN_TILE + threadIdx.x * SCAN_ITEMS;
   int v[SCAN_ITEMS];
   int s = 0;
@@ -118,12 +130,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const T* __restrict__ in,
 }
 
 template <class T>
-static cudaError_t scan_impl(rpd_ctx* c, const T* in, int32_t* out, int64_t n) {
+static cudaError_t scan_impl(rpd_ctx* c, const ScanIO<T>& io, int K, int64_t n) {
   if (n == 0) {
-    return cudaMemsetAsync(out, 0, sizeof(int32_t), c->stream);
+    for (int a = 0; a < K; ++a) {
+      cudaError_t e = cudaMemsetAsync(io.out[a], 0, sizeof(int32_t), c->stream);
+      if (e) return e;
+    }
+    return cudaSuccess;
   }
   const int nb = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
-  const size_t bytes = sizeof(unsigned long long) * (nb + 1);
+  const size_t bytes = sizeof(unsigned long long) * ((size_t)K * nb + 1);
   if (bytes > c->scratch.cap || !c->scratch.p) {
     cudaError_t e = c->scratch.ensure(bytes);
     if (e) return e;
@@ -134,18 +150,28 @@ static cudaError_t scan_impl(rpd_ctx* c, const T* in, int32_t* out, int64_t n) {
   unsigned long long* ticket = c->scratch.as<unsigned long long>();
   c->scan_epoch = (c->scan_epoch + 1) & ((1u << 30) - 1);
   if (c->scan_epoch == 0) c->scan_epoch = 1;
-  k_scan<T><<<nb, SCAN_THREADS, 0, c->stream>>>(in, n, out, nb, ticket, c->scan_ticket,
-                                                 ticket + 1, c->scan_epoch);
-  c->scan_ticket += (unsigned long long)nb;
+  k_scan<T><<<nb * K, SCAN_THREADS, 0, c->stream>>>(io, n, nb, ticket,
+                                                     c->scan_ticket, ticket + 1, c->scan_epoch);
+  c->scan_ticket += (unsigned long long)nb * K;
   ++c->launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
-  return scan_impl<int32_t>(c, in, out, n);
+  return scan_impl<int32_t>(c, ScanIO<int32_t>{{in}, {out}}, 1, n);
 }
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n) {
-  return scan_impl<uint8_t>(c, in, out, n);
+  return scan_impl<uint8_t>(c, ScanIO<uint8_t>{{in}, {out}}, 1, n);
+}
+// K <= 4 equal-length int32 scans in[a] -> out[a] in one launch
+cudaError_t launch_scan_i32_multi(rpd_ctx* c, const int32_t* const* in, int32_t* const* out,
+                                  int K, int64_t n) {
+  ScanIO<int32_t> io{{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
+  for (int a = 0; a < K; ++a) {
+    io.in[a] = in[a];
+    io.out[a] = out[a];
+  }
+  return scan_impl<int32_t>(c, io, K, n);
 }
 
 }  // namespace rpd
