@@ -436,7 +436,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   int64_t np = n, ni = 32 * (int64_t)cs.n_words;
   if (!deferred) {
     CK(readback(c, RbSpec{{c->p_scan.as<int32_t>() + n, c->i_scan.as<int32_t>() + n,
-                           c->p_over.as<int32_t>()},
+                           c->p_over.as<int32_t>(), c->p_over2.as<int32_t>()},
                           c->stats.as<unsigned long long>(), nullptr}),
        "readback");
     CK(cudaStreamSynchronize(c->stream), "clip");
@@ -445,6 +445,9 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     np = rb->i32[0];
     ni = rb->i32[1];
     absorb_clip_stats(c, rb, rb->i32[2]);
+    if (getenv("RPD_DEBUG_STATS"))
+      fprintf(stderr, "[rpd clip] pairs %lld overflow 16->32 %d 32->128 %d maxv %d maxp %d\n",
+              (long long)n, rb->i32[2], rb->i32[3], c->last.max_vertices, c->last.max_planes);
   }
   const size_t npp = np > 0 ? np : 1;
   CK(ps.off.ensure(sizeof(int32_t) * (nt + 1)), "alloc");

@@ -39,7 +39,7 @@
 #endif
 
 #ifndef RPD_CLIP_MID_VPL
-#define RPD_CLIP_MID_VPL 1  // vertex slots per lane of the middle (first overflow) tier, GW = 32
+#define RPD_CLIP_MID_VPL 2  // vertex slots per lane of the middle (first overflow) tier, GW = 32
 #endif
 #ifndef RPD_CLIP_PRELOAD
 #define RPD_CLIP_PRELOAD 0  // 1: load nbr_idx / twin of every classified plane (not only cutters)
@@ -316,6 +316,7 @@ __device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, 
 }
 
 enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
+constexpr int ST_N_CLIP = 12;  // statistics counters reduced by the clip kernels
 
 #ifdef RPD_CLIP_PHASES
 // development aid: cycles per clip phase summed over groups (lane 0 of each group)
@@ -912,30 +913,28 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
   if (lane == 0)
     for (int k = 0; k < 8; ++k) atomicAdd(&g_phase[k], (unsigned long long)ph[k]);
 #endif
-  // statistics: per-lane counters summed over the warp, group-uniform ones by group leaders
+  // statistics: per-lane counters summed over the warp, group-uniform ones over the warp's
+  // group leaders, then one global atomic per non-zero counter per block (block_stats)
+  const bool lead = lane == 0;
+  unsigned long long v[ST_N_CLIP] = {(unsigned long long)n_exact, (unsigned long long)n_zero,
+                                     (unsigned long long)d_sign,  (unsigned long long)d_out,
+                                     (unsigned long long)d_fb,    lead ? c_planes : 0u,
+                                     lead ? c_tests : 0u,         lead ? c_constr : 0u,
+                                     lead ? c_fan : 0u,
+                                     lead && !out.over_list ? (unsigned long long)n_over : 0ull,
+                                     (unsigned long long)max_v,   (unsigned long long)max_p};
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
-    n_zero += __shfl_xor_sync(0xffffffffu, n_zero, o);
-    d_sign += __shfl_xor_sync(0xffffffffu, d_sign, o);
-    d_out += __shfl_xor_sync(0xffffffffu, d_out, o);
-    d_fb += __shfl_xor_sync(0xffffffffu, d_fb, o);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+#pragma unroll
+    for (int k = 10; k < 12; ++k) v[k] = max(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(stats + 12, (unsigned long long)d_sign);
-    atomicAdd(stats + 13, (unsigned long long)d_out);
-    atomicAdd(stats + 14, (unsigned long long)d_fb);
-    if (n_exact) atomicAdd(stats + ST_EXACT, (unsigned long long)n_exact);
-    if (n_zero) atomicAdd(stats + ST_ZERO, (unsigned long long)n_zero);
-  }
-  if (lane == 0) {
-    atomicAdd(stats + ST_CLIP_PLANES, (unsigned long long)c_planes);
-    atomicAdd(stats + ST_CLIP_TESTS, (unsigned long long)c_tests);
-    atomicAdd(stats + ST_CLIP_CONSTR, (unsigned long long)c_constr);
-    atomicAdd(stats + ST_CLIP_FAN, (unsigned long long)c_fan);
-    if (n_over && !out.over_list) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_over);
-    atomicMax(stats + ST_MAXV, (unsigned long long)max_v);
-    atomicMax(stats + ST_MAXP, (unsigned long long)max_p);
-  }
+  const int slot[ST_N_CLIP] = {ST_EXACT,    ST_ZERO,        12,            13,
+                               14,          ST_CLIP_PLANES, ST_CLIP_TESTS, ST_CLIP_CONSTR,
+                               ST_CLIP_FAN, ST_OVERFLOW,    ST_MAXV,       ST_MAXP};
+  const int kind[ST_N_CLIP] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1};
+  block_stats<ST_N_CLIP>(stats, slot, kind, v);
 }
 
 // incidences per pair (0 for empty pairs)
@@ -1061,7 +1060,7 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
 }
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
-// 32-slot kernel <RPD_CLIP_MID_VPL = 1>; its own overflows (p_over2) by the 128-slot <32, 4>
+// 64-slot kernel <32, RPD_CLIP_MID_VPL = 2>; its own overflows (p_over2) by the 128-slot <32, 4>
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
   cudaError_t e = launch_clip_t<32, RPD_CLIP_MID_VPL>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet,

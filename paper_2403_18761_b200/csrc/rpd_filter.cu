@@ -83,9 +83,10 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     ntests += __shfl_xor_sync(0xffffffffu, ntests, o);
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMax(stats + ST_MAXK, (unsigned long long)m);
-    atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
+  {
+    const int slot[2] = {ST_MAXK, ST_REL_TESTS}, kind[2] = {1, 0};
+    const unsigned long long v[2] = {(unsigned long long)m, (unsigned long long)ntests};
+    block_stats<2>(stats, slot, kind, v);
   }
 }
 
@@ -384,9 +385,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     ntests += __shfl_xor_sync(FULL, ntests, o);
     npairs += __shfl_xor_sync(FULL, npairs, o);
   }
-  if (lane == 0) {
-    atomicAdd(stats + ST_REL_TESTS, (unsigned long long)ntests);
-    atomicAdd(stats + ST_TESTED, (unsigned long long)npairs);
+  {
+    const int slot[2] = {ST_REL_TESTS, ST_TESTED}, kind[2] = {0, 0};
+    const unsigned long long v[2] = {(unsigned long long)ntests, (unsigned long long)npairs};
+    block_stats<2>(stats, slot, kind, v);
   }
 }
 
@@ -396,7 +398,9 @@ __global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
   int m = a < n ? k_tet[a] : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(stats + ST_MAXK, (unsigned long long)m);
+  const int slot[1] = {ST_MAXK}, kind[1] = {1};
+  const unsigned long long v[1] = {(unsigned long long)(m > 0 ? m : 0)};
+  block_stats<1>(stats, slot, kind, v);
 }
 
 // ------------------------------------------------------------------ compaction

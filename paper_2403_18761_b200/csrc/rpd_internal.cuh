@@ -208,4 +208,34 @@ static __host__ __device__ __noinline__ void exact_vertex(const XPlane& p, const
   }
 }
 
+// Statistics counters of a kernel: every thread passes its warp-reduced values (only the
+// warp leader's count); warp leaders combine them in shared memory and one thread per block
+// issues one global atomic per non-zero counter.  Must be called by every thread of the block.
+// (Per-warp atomics on the same few addresses serialise in L2: tens of microseconds per
+// launch.)  kind[k]: 0 = add, 1 = max.
+template <int K>
+__device__ inline void block_stats(unsigned long long* stats, const int (&slot)[K],
+                                   const int (&kind)[K], const unsigned long long (&v)[K]) {
+  __shared__ unsigned long long s_red[K];
+  if (threadIdx.x < K) s_red[threadIdx.x] = 0ull;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (v[k]) {
+        if (kind[k]) atomicMax(&s_red[k], v[k]);
+        else atomicAdd(&s_red[k], v[k]);
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (s_red[k]) {
+        if (kind[k]) atomicMax(stats + slot[k], s_red[k]);
+        else atomicAdd(stats + slot[k], s_red[k]);
+      }
+  }
+}
+
 }  // namespace rpd

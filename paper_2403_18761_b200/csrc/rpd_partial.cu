@@ -39,15 +39,20 @@ __global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
                              int32_t* __restrict__ pos, int32_t* __restrict__ cepoch,
                              int* __restrict__ min_epoch, int epoch) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  if (flag[t]) {
-    list[scan[t]] = (int32_t)t;
-    pos[t] = scan[t];
-    atomicMin(min_epoch, cepoch[t]);
-    cepoch[t] = epoch;
-  } else {
-    pos[t] = -1;
+  int ep = 0x7fffffff;
+  if (t < T) {
+    if (flag[t]) {
+      list[scan[t]] = (int32_t)t;
+      pos[t] = scan[t];
+      ep = cepoch[t];
+      cepoch[t] = epoch;
+    } else {
+      pos[t] = -1;
+    }
   }
+  // one atomic per warp (per-tet atomics on one address serialise in L2)
+  ep = __reduce_min_sync(0xffffffffu, ep);
+  if ((threadIdx.x & 31) == 0 && ep != 0x7fffffff) atomicMin(min_epoch, ep);
 }
 
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old) {
