@@ -67,6 +67,8 @@ struct WarpState {
   double KMn[MAXS];
   unsigned dsc[MAXV];      // new-vertex descriptors: u | v << 8 | x << 16 | y << 24
   unsigned char dq[MAXV];  // and their target slots
+  unsigned char c0[MAXP];  // cut step: the new vertex whose first (second) plane is p
+  unsigned char c1[MAXP];
   int src[MAXP];           // radical: sphere j; tet face k: -1-k
   int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
   int tw[MAXP];            // twin[eidx] (next coincident CSR entry of the row), -1 if none
@@ -139,17 +141,26 @@ __device__ __forceinline__ int mask_count(const unsigned (&m)[VPL]) {
   for (int k = 0; k < VPL; ++k) c += __popc(m[k]);
   return c;
 }
+// position of the j-th (0-based) set bit of m (m has more than j set bits); loop-free
+__device__ __forceinline__ int nth_bit(unsigned m, int j) {
+  int pos = 0, c;
+  c = __popc(m & 0xffffu);
+  if (j >= c) { j -= c; m >>= 16; pos += 16; }
+  c = __popc(m & 0xffu);
+  if (j >= c) { j -= c; m >>= 8; pos += 8; }
+  c = __popc(m & 0xfu);
+  if (j >= c) { j -= c; m >>= 4; pos += 4; }
+  c = __popc(m & 0x3u);
+  if (j >= c) { j -= c; m >>= 2; pos += 2; }
+  return pos + (j >= (int)(m & 1u) ? 1 : 0);
+}
 // slot of the j-th (0-based) set bit
 template <int GW, int VPL>
 __device__ __forceinline__ int mask_nth(const unsigned (&m)[VPL], int j) {
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const int c = __popc(m[k]);
-    if (j < c) {
-      unsigned w = m[k];
-      for (int q = 0; q < j; ++q) w &= w - 1u;
-      return GW * k + __ffs(w) - 1;
-    }
+    if (j < c) return GW * k + nth_bit(m[k], j);
     j -= c;
   }
   return -1;
@@ -543,22 +554,21 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #ifdef RPD_CLIP_PHASES
         ++ph[7];
 #endif
-        if (lane == 0) {
+        if (lane == 0) {  // (read by other lanes only after the descriptor sync below)
 #pragma unroll
           for (int k = 0; k < 4; ++k) S.g[sid][k] = s[k];
           S.src[sid] = js;
           S.eidx[sid] = es;
           S.tw[sid] = tws;
         }
-        __syncwarp(FULL);
         // ---- new vertices, in place: one per boundary edge of the conflict region (a removed
         // vertex v with a kept neighbour u across its dual edge (x, y)), oriented as that edge:
         // (x, y, s).  Kept vertices stay in their slots; the first new vertex of v takes v's
-        // slot, further ones take free slots (holes, removed vertices without new ones).
-        // Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring new vertices
-        // around the new facet s.  Only lane v reads slot v during the step, so writing slot v
-        // last (r descending) is race-free.
-        unsigned nbw[VPL], hasnew[VPL], extra[VPL], freem[VPL];
+        // slot, further ones ("extras") take free slots (holes, removed vertices without new
+        // ones).  Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring new
+        // vertices around the new facet s, found through per-plane tables.
+        const unsigned lt = (1u << lane) - 1u;  // group lanes below this one
+        unsigned nbw[VPL], hasnew[VPL], extra[VPL];
         int nnew[VPL], ex_idx[VPL];
         int ex_base = 0;
 #pragma unroll
@@ -574,43 +584,38 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #pragma unroll
             for (int r = 0; r < 3; ++r) nnew[k] += slot_in<GW>(posm, (nbw[k] >> (8 * r)) & 0xff);
           }
-          hasnew[k] = (__ballot_sync(FULL, nnew[k] > 0) >> (GW * grp)) & GLOW;
+          // extras per removed vertex: ex = nnew - 1 in {0, 1, 2}; prefix over the lanes by
+          // its two bit planes
           const int ex = nnew[k] > 0 ? nnew[k] - 1 : 0;
-          int incl = ex;
-#pragma unroll
-          for (int o = 1; o < GW; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o, GW);
-            if (lane >= o) incl += y;
-          }
-          ex_idx[k] = ex_base + incl - ex;
-          ex_base += __shfl_sync(FULL, incl, GW - 1, GW);
+          hasnew[k] = (__ballot_sync(FULL, nnew[k] > 0) >> (GW * grp)) & GLOW;
+          const unsigned b0 = (__ballot_sync(FULL, ex & 1) >> (GW * grp)) & GLOW;
+          const unsigned b1 = (__ballot_sync(FULL, ex & 2) >> (GW * grp)) & GLOW;
+          ex_idx[k] = ex_base + __popc(b0 & lt) + 2 * __popc(b1 & lt);
+          ex_base += __popc(b0) + 2 * __popc(b1);
         }
-        // free slots, and the lowest ex_base of them for the extra new vertices
-        int rem = ex_base;
+        // the lowest ex_base free slots take the extras
+        {
+          int rem = ex_base;
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          freem[k] = ~(posm[k] | hasnew[k]) & GLOW;
-          unsigned f = freem[k];
-          extra[k] = 0u;
-          while (rem > 0 && f) {
-            extra[k] |= f & (0u - f);
-            f &= f - 1u;
-            --rem;
+          for (int k = 0; k < VPL; ++k) {
+            const unsigned f = ~(posm[k] | hasnew[k]) & GLOW;
+            const int c = __popc(f);
+            extra[k] = rem <= 0 ? 0u : (rem >= c ? f : f & ((2u << nth_bit(f, rem - 1)) - 1u));
+            rem -= c;
           }
-        }
-        if (rem > 0) {  // more than MAXV vertices
-          status = ST_OVER;
-          break;
+          if (rem > 0) {  // more than MAXV vertices
+            status = ST_OVER;
+            break;
+          }
         }
         // descriptors of the new vertices (edge (u, v), planes (x, y), target slot q), numbered
-        // in slot order of v; then one lane per new vertex builds it into the staging area,
-        // and after a sync the staged vertices move into their slots (slot v may be read as an
-        // edge endpoint until then)
+        // in slot order of v; then one lane per new vertex builds it (slot v may be read as an
+        // edge endpoint until the following sync)
         {
           int hb = 0;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
-            const int d0 = ex_idx[k] + hb + __popc(hasnew[k] & ((1u << lane) - 1u));
+            const int d0 = ex_idx[k] + hb + __popc(hasnew[k] & lt);
             hb += __popc(hasnew[k]);
             if (nnew[k] == 0) continue;
             const int v = GW * k + lane;
@@ -648,15 +653,26 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           }
           __syncwarp(FULL);
           if (lane < n_new) {
+            const int x = (ds >> 16) & 0xff, y = ds >> 24;
 #pragma unroll
             for (int m = 0; m < 4; ++m) S.K[q][m] = K[m];
             S.F[q] = F;
             S.KM[q] = KMv;
-            S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
+            S.tri[q] = tri_pack(x, y, sid);
             S.nb[q][0] = (unsigned char)(ds & 0xff);
+            S.c0[x] = (unsigned char)q;  // the new vertex whose first plane is x
+            S.c1[y] = (unsigned char)q;  // ... whose second plane is y
+          }
+          __syncwarp(FULL);
+          // close the cycle around the new facet s: across (y, s) the new vertex (y, ., s),
+          // across (s, x) the new vertex (., x, s)
+          if (lane < n_new) {
+            const int x = (ds >> 16) & 0xff, y = ds >> 24;
+            S.nb[q][1] = S.c0[y];
+            S.nb[q][2] = S.c1[x];
           }
         } else {
-          // more new vertices than lanes (wide kernel only): staged in shared memory
+          // more new vertices than lanes (wide kernels only): staged in shared memory
           for (int d = lane; d < n_new; d += GW) {
             const unsigned ds = S.dsc[d];
             const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
@@ -673,44 +689,27 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           for (int d = lane; d < n_new; d += GW) {
             const unsigned ds = S.dsc[d];
             const int q = S.dq[d];
+            const int x = (ds >> 16) & 0xff, y = ds >> 24;
 #pragma unroll
             for (int m = 0; m < 4; ++m) S.K[q][m] = S.Kn[d][m];
             S.F[q] = S.Fn[d];
             S.KM[q] = S.KMn[d];
-            S.tri[q] = tri_pack((ds >> 16) & 0xff, ds >> 24, sid);
+            S.tri[q] = tri_pack(x, y, sid);
             S.nb[q][0] = (unsigned char)(ds & 0xff);
+            S.c0[x] = (unsigned char)q;
+            S.c1[y] = (unsigned char)q;
           }
-        }
-        __syncwarp(FULL);
-        // close the cycle of new vertices around the new facet s
-        unsigned newm[VPL];
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) newm[k] = hasnew[k] | extra[k];
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          if (!newm[k]) continue;
-          const int q = GW * k + lane;
-          if ((newm[k] >> lane) & 1u) {
-            const unsigned tr = S.tri[q];
-            const int x = tri_at(tr, 0), y = tri_at(tr, 1);
-            int n1 = q, n2 = q;
-#pragma unroll
-            for (int kk = 0; kk < VPL; ++kk) {
-              unsigned m = newm[kk];
-              while (m) {
-                const int w = GW * kk + __ffs(m) - 1;
-                m &= m - 1u;
-                const unsigned tw = S.tri[w];
-                if (tri_at(tw, 0) == y) n1 = w;
-                if (tri_at(tw, 1) == x) n2 = w;
-              }
-            }
-            S.nb[q][1] = (unsigned char)n1;
-            S.nb[q][2] = (unsigned char)n2;
+          __syncwarp(FULL);
+          for (int d = lane; d < n_new; d += GW) {
+            const unsigned ds = S.dsc[d];
+            const int q = S.dq[d];
+            const int x = (ds >> 16) & 0xff, y = ds >> 24;
+            S.nb[q][1] = S.c0[y];
+            S.nb[q][2] = S.c1[x];
           }
         }
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) live[k] = posm[k] | newm[k];
+        for (int k = 0; k < VPL; ++k) live[k] = posm[k] | hasnew[k] | extra[k];
         c_constr += n_new;
         nv = mask_count<VPL>(live);
         __syncwarp(FULL);
