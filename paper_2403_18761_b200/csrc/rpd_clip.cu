@@ -141,26 +141,17 @@ __device__ __forceinline__ int mask_count(const unsigned (&m)[VPL]) {
   for (int k = 0; k < VPL; ++k) c += __popc(m[k]);
   return c;
 }
-// position of the j-th (0-based) set bit of m (m has more than j set bits); loop-free
-__device__ __forceinline__ int nth_bit(unsigned m, int j) {
-  int pos = 0, c;
-  c = __popc(m & 0xffffu);
-  if (j >= c) { j -= c; m >>= 16; pos += 16; }
-  c = __popc(m & 0xffu);
-  if (j >= c) { j -= c; m >>= 8; pos += 8; }
-  c = __popc(m & 0xfu);
-  if (j >= c) { j -= c; m >>= 4; pos += 4; }
-  c = __popc(m & 0x3u);
-  if (j >= c) { j -= c; m >>= 2; pos += 2; }
-  return pos + (j >= (int)(m & 1u) ? 1 : 0);
-}
-// slot of the j-th (0-based) set bit
+// slot of the j-th (0-based) set bit (j is small: clear the j lowest bits, take the next)
 template <int GW, int VPL>
 __device__ __forceinline__ int mask_nth(const unsigned (&m)[VPL], int j) {
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const int c = __popc(m[k]);
-    if (j < c) return GW * k + nth_bit(m[k], j);
+    if (j < c) {
+      unsigned w = m[k];
+      for (int q = 0; q < j; ++q) w &= w - 1u;
+      return GW * k + __ffs(w) - 1;
+    }
     j -= c;
   }
   return -1;
@@ -525,7 +516,6 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           anyneg |= negm[k] != 0u;
           anypos |= posm[k] != 0u;
         }
-        zero_hit = __any_sync(FULL, zero_hit);
         c_tests += nv;
 #ifdef RPD_TRACE
         if (p == RPD_TRACE) {
@@ -599,9 +589,10 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
             const unsigned f = ~(posm[k] | hasnew[k]) & GLOW;
-            const int c = __popc(f);
-            extra[k] = rem <= 0 ? 0u : (rem >= c ? f : f & ((2u << nth_bit(f, rem - 1)) - 1u));
-            rem -= c;
+            unsigned hi = f;  // f without its rem lowest bits
+            for (int q = 0; q < rem && hi; ++q) hi &= hi - 1u;
+            extra[k] = f ^ hi;
+            rem -= __popc(f);
           }
           if (rem > 0) {  // more than MAXV vertices
             status = ST_OVER;
@@ -753,6 +744,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     }
 
     // zero-area SoS facets (only possible after an exact-zero predicate; C1.7)
+    zero_hit = __any_sync(FULL, zero_hit);  // (per lane until here)
     if (zero_hit) {
       for (int f = facets_all.next(0); f >= 0; f = facets_all.next(f + 1)) {
         Bits<VPL> Q;
@@ -897,11 +889,11 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     }
     if (lane == 0) {
       const double L = 1.0 / RPD_LATTICE;
-      const double vol = (vol6 / 6.0) * (L * L * L);
+      const double vol = vol6 * (L * L * L / 6.0);
       out.vol[p] = vol;
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        out.m1[3 * p + c] = (m24[c] / 24.0) * (L * L * L * L) + vol * (S.V[0][c] * L);
+        out.m1[3 * p + c] = m24[c] * (L * L * L * L / 24.0) + vol * (S.V[0][c] * L);
       out.flag[p] = 1;
       out.fm[p] = (uint8_t)facemask;
     }
