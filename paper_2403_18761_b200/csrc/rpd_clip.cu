@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       const int e = base + lane;
       const bool have = e < e1;
       double g[4] = {0.0, 0.0, 0.0, 0.0};
-      bool allpos = false, allneg = false;
+      bool allpos = false;
       int jn = 0, twn = -1;
       if (have) {
         const double4 pl = planes[e];
@@ -446,18 +446,15 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
         twn = __ldg(twin + e);
 #endif
         allpos = true;
-        allneg = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           g[k] = fma(pl.x, S.V[k][0], fma(pl.y, S.V[k][1], fma(pl.z, S.V[k][2], pl.w)));
           allpos &= g[k] > 0.0;
-          allneg &= g[k] < 0.0;
         }
       }
-      if (__any_sync(FULL, allneg)) {
-        status = ST_EMPTY;
-        break;
-      }
+      // (no "negative at all four corners" early exit: Alg. 1 admits a candidate only if
+      // every plane is positive at some corner -- the same exact values -- and such a plane
+      // would empty the piece in its sign pass anyway)
       unsigned act = (__ballot_sync(FULL, have && !allpos) >> (GW * grp)) & GLOW;
       PHASE_MARK(1);
       while (act && status == ST_ALIVE) {
@@ -481,6 +478,8 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 
         // ---- sign of every vertex slot
         int sg[VPL];
+        double valr[VPL];
+        unsigned char vxr[VPL];
         unsigned negm[VPL], posm[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) negm[k] = posm[k] = 0u;
@@ -495,14 +494,14 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
             const double* K = S.K[v];
             const double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
             const double B = sabs * S.F[v];
-            S.val[v] = val;
-            S.vx[v] = 0;
+            valr[k] = val;
+            vxr[k] = 0;
             if (val > B) sg[k] = 1;
             else if (val < -B) sg[k] = -1;
             else {
               int zh = 0;
               sg[k] = exact_sign(S, C, S.tri[v], -1, s, es, js, &zh);
-              S.vx[v] = 1;
+              vxr[k] = 1;
               ++n_exact;
               ++d_sign;
               if (zh) {
@@ -532,6 +531,16 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #endif
         PHASE_MARK(2);
         if (!anyneg) continue;  // the plane does not cut: skip it
+        if (anypos) {  // a cut: the signs' values for the new-vertex construction
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const int v = GW * k + lane;
+            if ((live[k] >> lane) & 1u) {
+              S.val[v] = valr[k];
+              S.vx[v] = vxr[k];
+            }
+          }
+        }
         if (!anypos) {
           status = ST_EMPTY;
           break;
@@ -781,12 +790,16 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     }
 
     // incidences: every positive-area facet plus its exactly coincident sources
-    unsigned fmask_bits = 0;
+    unsigned fmask_bits = 0, ibits = 0;
     unsigned* words = out.incmask + mo;
-    // the pair's mask words are zeroed here (no memset pass) and then set by fire-and-forget
-    // atomics (the group's zero stores are ordered before them by the warp sync)
-    for (int w = lane; w < nwp; w += GW) words[w] = 0u;
-    __syncwarp(FULL);
+    // k_site <= 32 (one mask word, most pairs): bits or-reduced over the group and stored
+    // once; otherwise the words are zeroed here (no memset pass) and then set by
+    // fire-and-forget atomics (the zero stores are ordered before them by the warp sync)
+    const bool one_word = nwp == 1;
+    if (!one_word) {
+      for (int w = lane; w < nwp; w += GW) words[w] = 0u;
+      __syncwarp(FULL);
+    }
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int pl = GW * k + lane;
@@ -810,7 +823,8 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
           int nx = S.tw[pl];
           while (e >= 0) {
             const int pos = e - e0;
-            atomicOr(words + (pos >> 5), 1u << (pos & 31));
+            if (one_word) ibits |= 1u << pos;
+            else atomicOr(words + (pos >> 5), 1u << (pos & 31));
             e = nx;
             if (e >= 0) nx = twin[e];
           }
@@ -818,6 +832,10 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
       }
     }
     const unsigned facemask = __reduce_or_sync(FULL, fmask_bits);
+    if (one_word) {
+      const unsigned w = __reduce_or_sync(FULL, ibits);
+      if (lane == 0) words[0] = w;
+    }
     __syncwarp(FULL);
     PHASE_MARK(4);
 
