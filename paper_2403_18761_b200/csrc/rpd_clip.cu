@@ -35,14 +35,14 @@
 #define RPD_CLIP_VPL 1   // vertex slots per lane in the fast kernel
 #endif
 #ifndef RPD_CLIP_MINB
-#define RPD_CLIP_MINB 2  // min resident 256-thread blocks per SM for the fast kernel
+#define RPD_CLIP_MINB 2  // min resident blocks per SM for the fast kernel
+#endif
+#ifndef RPD_CLIP_THREADS
+#define RPD_CLIP_THREADS 256  // threads per block of the fast kernel
 #endif
 
 #ifndef RPD_CLIP_MID_VPL
 #define RPD_CLIP_MID_VPL 2  // vertex slots per lane of the middle (first overflow) tier, GW = 32
-#endif
-#ifndef RPD_CLIP_PRELOAD
-#define RPD_CLIP_PRELOAD 0  // 1: load nbr_idx / twin of every classified plane (not only cutters)
 #endif
 
 namespace rpd {
@@ -52,6 +52,7 @@ struct WarpState {
   static constexpr int MAXV = GW * VPL;
   static constexpr int MAXP = GW * VPL;
   double g[MAXP][4];       // barycentric plane vectors (exact integers)
+  double gb[GW][4];        // the current batch of classified planes (one per lane)
   double K[MAXV][4];       // homogeneous vertices (slots; the live set is a group mask)
   double F[MAXV];          // error scalars
   double KM[MAXV];         // max |K_m| of every vertex
@@ -347,7 +348,8 @@ struct PairOut {
 };
 
 template <int GW, int VPL>
-__global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB : 1) k_clip(
+__global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64),
+                                  VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_MINB : (VPL <= 2 ? 2 : 1)) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
     const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ nbr_off,
@@ -436,26 +438,26 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
     for (int base = e0; base < e1 && status == ST_ALIVE; base += GW) {
       const int e = base + lane;
       const bool have = e < e1;
-      double g[4] = {0.0, 0.0, 0.0, 0.0};
+      double g[4];
       bool allpos = false;
-      int jn = 0, twn = -1;
       if (have) {
         const double4 pl = planes[e];
-#if RPD_CLIP_PRELOAD
-        jn = __ldg(nbr_idx + e);
-        twn = __ldg(twin + e);
-#endif
         allpos = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           g[k] = fma(pl.x, S.V[k][0], fma(pl.y, S.V[k][1], fma(pl.z, S.V[k][2], pl.w)));
           allpos &= g[k] > 0.0;
         }
+        if (!allpos) {  // staged for the sign passes (read by all lanes after the sync)
+          reinterpret_cast<double2*>(S.gb[lane])[0] = make_double2(g[0], g[1]);
+          reinterpret_cast<double2*>(S.gb[lane])[1] = make_double2(g[2], g[3]);
+        }
       }
       // (no "negative at all four corners" early exit: Alg. 1 admits a candidate only if
       // every plane is positive at some corner -- the same exact values -- and such a plane
       // would empty the piece in its sign pass anyway)
       unsigned act = (__ballot_sync(FULL, have && !allpos) >> (GW * grp)) & GLOW;
+      if (act) __syncwarp(FULL);
       PHASE_MARK(1);
       while (act && status == ST_ALIVE) {
         const int l = __ffs(act) - 1;
@@ -463,17 +465,18 @@ __global__ void __launch_bounds__(VPL <= 2 ? 256 : 64, VPL <= 2 ? RPD_CLIP_MINB 
 #ifdef RPD_CLIP_PHASES
         ++ph[6];
 #endif
-        double s[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) s[k] = __shfl_sync(FULL, g[k], l, GW);
+        double s[4];  // the plane's values at the 4 tet corners (its barycentric vector)
+        {
+          const double2 a = reinterpret_cast<const double2*>(S.gb[l])[0];
+          const double2 b = reinterpret_cast<const double2*>(S.gb[l])[1];
+          s[0] = a.x;
+          s[1] = a.y;
+          s[2] = b.x;
+          s[3] = b.y;
+        }
         const int es = base + l;
-#if RPD_CLIP_PRELOAD
-        const int js = __shfl_sync(FULL, jn, l, GW);
-        const int tws = __shfl_sync(FULL, twn, l, GW);
-#else
         const int js = __ldg(nbr_idx + es);
         const int tws = __ldg(twin + es);
-#endif
         const double sabs = fabs(s[0]) + fabs(s[1]) + fabs(s[2]) + fabs(s[3]);
 
         // ---- sign of every vertex slot
@@ -1027,7 +1030,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
                                  int32_t* over, const int32_t* n_dev) {
-  constexpr int THREADS = VPL <= 2 ? 256 : 64;
+  constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
   cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,

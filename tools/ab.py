@@ -1,6 +1,6 @@
 """A/B timing of librpd build variants (development aid; bench.py is the contract).
 
-usage: python tools/ab.py CONFIG tag1:"-DFOO=1" tag2:"..." ...
+usage: python tools/ab.py CONFIG tag1:"-DFOO=1" tag2:"..." tag3:@path/to/librpd.so ...
 Builds each variant (extra nvcc flags), runs full RPD (relations + clip) 5x and, when the
 config has partial batches, the partial updates; prints median filter / clip / full ms, mean
 partial ms, and whether the outputs are byte-identical to the first variant's.
@@ -33,9 +33,12 @@ for spec in sys.argv[2:]:
     import paper_2403_18761_b200._build as B
     import paper_2403_18761_b200.rpd as R
     B = importlib.reload(B)
-    B.NVCC_FLAGS += flags.split()
-    B.LIB = B.LIB.replace("librpd.so", f"librpd_{tag}.so")
-    B.build(force=True)
+    if flags.startswith("@"):   # a prebuilt library (e.g. of another commit)
+        B.LIB = flags[1:]
+    else:
+        B.NVCC_FLAGS += flags.split()
+        B.LIB = B.LIB.replace("librpd.so", f"librpd_{tag}.so")
+        B.build(force=True)
     R._lib = None
     R.load_library(B.LIB)
     ctx = R.RPDContext(0, filter_mode="pruned")
