@@ -67,7 +67,8 @@ struct WarpState {
   double Fn[MAXS];
   double KMn[MAXS];
   unsigned dsc[MAXV];      // new-vertex descriptors: u | v << 8 | x << 16 | y << 24
-  unsigned char dq[MAXV];  // and their target slots
+  unsigned char dq[MAXV];  // and their target slot codes (slot, or MAXV + extra number)
+  unsigned char xs[MAXV];  // slot of every extra new vertex of the current cut
   unsigned char c0[MAXP];  // cut step: the new vertex whose first (second) plane is p
   unsigned char c1[MAXP];
   int src[MAXP];           // radical: sphere j; tet face k: -1-k
@@ -570,12 +571,12 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         // ones).  Links: across (x, y) -> u; across (y, s) and (s, x) -> the neighbouring new
         // vertices around the new facet s, found through per-plane tables.
         const unsigned lt = (1u << lane) - 1u;  // group lanes below this one
-        unsigned nbw[VPL], hasnew[VPL], extra[VPL];
-        int nnew[VPL], ex_idx[VPL];
+        unsigned nbw[VPL], hasnew[VPL], extra[VPL], keptr[VPL];
+        int ex_idx[VPL];
         int ex_base = 0;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-          nnew[k] = 0;
+          keptr[k] = 0u;  // bit r: the neighbour across dual edge r is kept
           nbw[k] = 0u;
           ex_idx[k] = 0;
           hasnew[k] = 0u;
@@ -584,55 +585,59 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           if ((negm[k] >> lane) & 1u) {
             nbw[k] = *reinterpret_cast<const unsigned*>(S.nb[v]);
 #pragma unroll
-            for (int r = 0; r < 3; ++r) nnew[k] += slot_in<GW>(posm, (nbw[k] >> (8 * r)) & 0xff);
+            for (int r = 0; r < 3; ++r)
+              keptr[k] |= (unsigned)slot_in<GW>(posm, (nbw[k] >> (8 * r)) & 0xff) << r;
           }
           // extras per removed vertex: ex = nnew - 1 in {0, 1, 2}; prefix over the lanes by
           // its two bit planes
-          const int ex = nnew[k] > 0 ? nnew[k] - 1 : 0;
-          hasnew[k] = (__ballot_sync(FULL, nnew[k] > 0) >> (GW * grp)) & GLOW;
+          const int nnew = __popc(keptr[k]);
+          const int ex = nnew > 0 ? nnew - 1 : 0;
+          hasnew[k] = (__ballot_sync(FULL, nnew > 0) >> (GW * grp)) & GLOW;
           const unsigned b0 = (__ballot_sync(FULL, ex & 1) >> (GW * grp)) & GLOW;
           const unsigned b1 = (__ballot_sync(FULL, ex & 2) >> (GW * grp)) & GLOW;
           ex_idx[k] = ex_base + __popc(b0 & lt) + 2 * __popc(b1 & lt);
           ex_base += __popc(b0) + 2 * __popc(b1);
         }
-        // the lowest ex_base free slots take the extras
+        // the lowest ex_base free slots take the extras: the free slot of rank r (in slot order)
+        // holds extra r; S.xs maps extra numbers to slots
         {
-          int rem = ex_base;
+          int rank_base = 0;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
             const unsigned f = ~(posm[k] | hasnew[k]) & GLOW;
-            unsigned hi = f;  // f without its rem lowest bits
-            for (int q = 0; q < rem && hi; ++q) hi &= hi - 1u;
-            extra[k] = f ^ hi;
-            rem -= __popc(f);
+            const int rk = rank_base + __popc(f & lt);
+            const bool mine = ((f >> lane) & 1u) && rk < ex_base;
+            if (mine) S.xs[rk] = (unsigned char)(GW * k + lane);
+            extra[k] = (__ballot_sync(FULL, mine) >> (GW * grp)) & GLOW;
+            rank_base += __popc(f);
           }
-          if (rem > 0) {  // more than MAXV vertices
+          if (rank_base < ex_base) {  // more than MAXV vertices
             status = ST_OVER;
             break;
           }
         }
-        // descriptors of the new vertices (edge (u, v), planes (x, y), target slot q), numbered
-        // in slot order of v; then one lane per new vertex builds it (slot v may be read as an
-        // edge endpoint until the following sync)
+        // descriptors of the new vertices (edge (u, v), planes (x, y), target slot code:
+        // the slot v, or MAXV + extra number), numbered in slot order of v; then one lane per
+        // new vertex builds it (slot v may be read as an edge endpoint until the following sync)
         {
           int hb = 0;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
             const int d0 = ex_idx[k] + hb + __popc(hasnew[k] & lt);
             hb += __popc(hasnew[k]);
-            if (nnew[k] == 0) continue;
+            if (!keptr[k]) continue;
             const int v = GW * k + lane;
             const unsigned tr = S.tri[v];
             int j = 0;
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
+              if (!((keptr[k] >> r) & 1u)) continue;
               const int u = (nbw[k] >> (8 * r)) & 0xff;
-              if (!slot_in<GW>(posm, u)) continue;
-              const int q = j == 0 ? v : mask_nth<GW, VPL>(extra, ex_idx[k] + j - 1);
+              const int qc = j == 0 ? v : WS::MAXV + ex_idx[k] + j - 1;
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
               S.dsc[d0 + j] = (unsigned)u | ((unsigned)v << 8) | ((unsigned)x << 16) |
                               ((unsigned)y << 24);
-              S.dq[d0 + j] = (unsigned char)q;
+              S.dq[d0 + j] = (unsigned char)qc;
               ++j;
             }
           }
@@ -647,6 +652,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           if (lane < n_new) {
             ds = S.dsc[lane];
             q = S.dq[lane];
+            if (q >= WS::MAXV) q = S.xs[q - WS::MAXV];
             const int u = ds & 0xff, v = (ds >> 8) & 0xff, x = (ds >> 16) & 0xff, y = ds >> 24;
             d_fb += new_vertex(S, C, u, v, x, y, sid, sabs, K, &F, &KMv, &n_exact);
             // u's link across the edge to v now leads to the new vertex (only this lane
@@ -685,8 +691,11 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
             for (int m = 0; m < 4; ++m) S.Kn[d][m] = K[m];
             S.Fn[d] = F;
             S.KMn[d] = KMv;
+            int qd = S.dq[d];
+            if (qd >= WS::MAXV) qd = S.xs[qd - WS::MAXV];
+            S.dq[d] = (unsigned char)qd;  // decoded for the store loop below
             const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
-            S.nb[u][ru] = S.dq[d];
+            S.nb[u][ru] = (unsigned char)qd;
           }
           __syncwarp(FULL);
           for (int d = lane; d < n_new; d += GW) {
