@@ -48,7 +48,7 @@
 namespace rpd {
 
 template <int GW, int VPL>
-struct WarpState {
+struct alignas(16) WarpState {  // (16-byte aligned: double2 accesses)
   static constexpr int MAXV = GW * VPL;
   static constexpr int MAXP = GW * VPL;
   double g[MAXP][4];       // barycentric plane vectors (exact integers)
@@ -495,8 +495,9 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           const int v = GW * k + lane;
           const bool valid = (live[k] >> lane) & 1u;
           if (valid) {
-            const double* K = S.K[v];
-            const double val = fma(s[0], K[0], fma(s[1], K[1], fma(s[2], K[2], s[3] * K[3])));
+            const double2 k01 = reinterpret_cast<const double2*>(S.K[v])[0];
+            const double2 k23 = reinterpret_cast<const double2*>(S.K[v])[1];
+            const double val = fma(s[0], k01.x, fma(s[1], k01.y, fma(s[2], k23.x, s[3] * k23.y)));
             const double B = sabs * S.F[v];
             valr[k] = val;
             vxr[k] = 0;
@@ -514,8 +515,9 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
               }
             }
           }
-          negm[k] = (__ballot_sync(FULL, valid && sg[k] < 0) >> (GW * grp)) & GLOW;
+          // (signs are never zero: the SoS rule decides every tie)
           posm[k] = (__ballot_sync(FULL, valid && sg[k] > 0) >> (GW * grp)) & GLOW;
+          negm[k] = live[k] & ~posm[k];
           anyneg |= negm[k] != 0u;
           anypos |= posm[k] != 0u;
         }
@@ -664,7 +666,8 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           if (lane < n_new) {
             const int x = (ds >> 16) & 0xff, y = ds >> 24;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) S.K[q][m] = K[m];
+            reinterpret_cast<double2*>(S.K[q])[0] = make_double2(K[0], K[1]);
+            reinterpret_cast<double2*>(S.K[q])[1] = make_double2(K[2], K[3]);
             S.F[q] = F;
             S.KM[q] = KMv;
             S.tri[q] = tri_pack(x, y, sid);
