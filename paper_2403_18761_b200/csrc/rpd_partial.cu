@@ -117,6 +117,27 @@ struct MergeDst {
 
 constexpr int MT = 256;  // tets per merge tile (one block)
 
+// block-wide copy dst[k] = f(src[k]), k < n, with 8 independent loads in flight per thread
+// before their stores (the source and destination sets never overlap)
+template <class T, class F>
+__device__ __forceinline__ void tile_copy(T* __restrict__ dst, const T* __restrict__ src, int n,
+                                          F f) {
+  constexpr int U = 8;
+  for (int k0 = threadIdx.x; k0 < n; k0 += U * blockDim.x) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k < n) v[u] = __ldg(src + k);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k < n) dst[k] = f(v[u]);
+    }
+  }
+}
+
 // upper_bound(off[0..n], q) - 1 in shared memory: the tile-local tet of element q
 __device__ __forceinline__ int tile_seg(const int* off, int n, int q) {
   int lo = 0, hi = n;  // off[lo] <= q < off[hi]
@@ -167,20 +188,16 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
     const int c_src = s_sc[0], p_src = s_sp[0], i_src = s_si[0];
     const int c_dst = s_nc[0], p_dst = s_np[0], i_dst = s_ni[0];
     const int wshift = s_nw[0] - s_sw[0], ishift = s_ni[0] - s_si[0];
-    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
-      D.c_idx[c_dst + k] = o.c_idx[c_src + k];
-      D.pair_tet[c_dst + k] = o.c_pt[c_src + k];
-      D.c_moff[c_dst + k] = o.c_moff[c_src + k] + wshift;
-    }
-    for (int k = threadIdx.x; k < npc; k += blockDim.x) {
-      D.p_sphere[p_dst + k] = o.p_sphere[p_src + k];
-      D.p_vol[p_dst + k] = o.p_vol[p_src + k];
-      D.p_fm[p_dst + k] = o.p_fm[p_src + k];
-      D.p_inc_off[p_dst + k] = o.p_inc_off[p_src + k] + ishift;
-    }
-    for (int k = threadIdx.x; k < 3 * npc; k += blockDim.x)
-      D.p_m1[3 * (int64_t)p_dst + k] = o.p_m1[3 * (int64_t)p_src + k];
-    for (int k = threadIdx.x; k < ni; k += blockDim.x) D.p_inc[i_dst + k] = o.p_inc[i_src + k];
+    auto same = [](auto x) { return x; };
+    tile_copy(D.c_idx + c_dst, o.c_idx + c_src, nc, same);
+    tile_copy(D.pair_tet + c_dst, o.c_pt + c_src, nc, same);
+    tile_copy(D.c_moff + c_dst, o.c_moff + c_src, nc, [=](int32_t x) { return x + wshift; });
+    tile_copy(D.p_sphere + p_dst, o.p_sphere + p_src, npc, same);
+    tile_copy(D.p_vol + p_dst, o.p_vol + p_src, npc, same);
+    tile_copy(D.p_fm + p_dst, o.p_fm + p_src, npc, same);
+    tile_copy(D.p_inc_off + p_dst, o.p_inc_off + p_src, npc, [=](int32_t x) { return x + ishift; });
+    tile_copy(D.p_m1 + 3 * (int64_t)p_dst, o.p_m1 + 3 * (int64_t)p_src, 3 * npc, same);
+    tile_copy(D.p_inc + i_dst, o.p_inc + i_src, ni, same);
     if (t0 + nt == T && threadIdx.x == 0) {
       D.c_moff[s_nc[nt]] = D.w_tet[T];
       D.p_inc_off[s_np[nt]] = s_ni[nt];

@@ -107,9 +107,10 @@ struct OldRows {  // previous staged CSR (partial updates: unchanged rows are co
   int64_t N;
 };
 
-// One warp per sphere row: validation, ascending order (fast path for sorted input rows,
+// One group of RG lanes per sphere row (STAGE_RG): validation, ascending order (fast path for sorted input rows,
 // else rank sort), radical planes and twins.  In a partial update a row of an old sphere
 // whose neighbour list is unchanged is copied from the previous stage instead.
+template <int RG>
 __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
@@ -117,9 +118,10 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
                              unsigned long long* __restrict__ hkey, int32_t* __restrict__ repoch,
                              int epoch, unsigned long long* __restrict__ htab, OldRows old,
                              int* err) {
-  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const unsigned FULL = 0xffffffffu;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / RG;
+  const int lane = threadIdx.x & (RG - 1);
+  const unsigned FULL = (RG == 32 ? 0xffffffffu : ((1u << RG) - 1u))
+                        << (RG * ((threadIdx.x & 31) / RG));  // this row's lanes
   if (i >= N) return;
 #ifdef RPD_DEBUG_STAGE
   long long dbg_t[5];
@@ -137,17 +139,17 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   const int k = e1 - e0;
   // sorted strictly ascending?  (then no duplicates either)
   bool sorted = true;
-  for (int32_t e = e0 + lane; e + 1 < e1; e += 32) sorted &= idx_in[e] < idx_in[e + 1];
+  for (int32_t e = e0 + lane; e + 1 < e1; e += RG) sorted &= idx_in[e] < idx_in[e + 1];
   sorted = __all_sync(FULL, sorted);
   // unchanged row of an old sphere: copy the previous stage
   // (empty rows are never reused: their Alg. 1 boolean depends on N, R4)
   if (old.off && i < old.N && sorted && k > 0) {
     const int32_t o0 = old.off[i], o1 = old.off[i + 1];
     bool same = (o1 - o0) == k;
-    for (int32_t q = lane; same && q < k; q += 32) same = old.idx[o0 + q] == idx_in[e0 + q];
+    for (int32_t q = lane; same && q < k; q += RG) same = old.idx[o0 + q] == idx_in[e0 + q];
     if (__all_sync(FULL, same)) {
       if (lane == 0) repoch[i] = old.repoch[i];
-      for (int32_t q = lane; q < k; q += 32) {
+      for (int32_t q = lane; q < k; q += RG) {
         idx_out[e0 + q] = old.idx[o0 + q];
         planes[e0 + q] = old.planes[o0 + q];
         hkey[e0 + q] = old.hkey[o0 + q];
@@ -159,7 +161,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   }
   if (lane == 0) repoch[i] = epoch;
   bool bad = false;
-  for (int32_t e = e0 + lane; e < e1; e += 32) {
+  for (int32_t e = e0 + lane; e < e1; e += RG) {
     const int32_t j = idx_in[e];
     if (j < 0 || j >= N) {
       report(err, RPD_EINVAL, ERR_NBR_INDEX, i);
@@ -188,14 +190,14 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     idx_out[e0 + rank] = j;
   }
   if (__any_sync(FULL, bad)) return;
-  __syncwarp();
+  __syncwarp(FULL);
 #ifdef RPD_DEBUG_STAGE
   dbg_t[1] = clock64();
 #endif
   const double4 si = sw[i];
   // planes, and the twin key: bit patterns of the ratios to the first non-zero normal
   // component (correctly rounded quotients of exactly proportional integers are equal)
-  for (int32_t e = e0 + lane; e < e1; e += 32) {
+  for (int32_t e = e0 + lane; e < e1; e += RG) {
     const int32_t j = idx_out[e];
     const double4 sj = sw[j];
     const double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
@@ -218,7 +220,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     h ^= h >> 33;
     hkey[e] = h;
   }
-  __syncwarp();
+  __syncwarp(FULL);
 #ifdef RPD_DEBUG_STAGE
   dbg_t[2] = clock64();
 #endif
@@ -230,10 +232,10 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     int tsz = 1;
     while (tsz < 2 * k) tsz <<= 1;
     unsigned long long* tab = htab + 4 * (int64_t)e0;
-    for (int q = lane; q < tsz; q += 32) tab[q] = 0ull;
-    __syncwarp();
+    for (int q = lane; q < tsz; q += RG) tab[q] = 0ull;
+    __syncwarp(FULL);
     bool dup = false;
-    for (int32_t e = e0 + lane; e < e1; e += 32) {
+    for (int32_t e = e0 + lane; e < e1; e += RG) {
       const unsigned long long h = hkey[e] | 1ull;
       int slot = (int)(h & (unsigned long long)(tsz - 1));
       while (true) {
@@ -251,7 +253,7 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
 #ifdef RPD_DEBUG_STAGE
   dbg_t[3] = clock64();
 #endif
-  for (int32_t e = e0 + lane; e < e1; e += 32) {
+  for (int32_t e = e0 + lane; e < e1; e += RG) {
     int32_t tw = -1;
     if (maybe) {
       const unsigned long long h = hkey[e];
@@ -281,6 +283,10 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
            dbg_t[3] - dbg_t[2], dbg_t[4] - dbg_t[3]);
 #endif
 }
+
+#ifndef STAGE_RG
+#define STAGE_RG 32  // lanes per row of k_stage_rows (8 and 16 measured slower)
+#endif
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
@@ -336,7 +342,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if (N > 0) {
     k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(spheres, N, s.sw.as<double4>(), err);
     ++c->launches;
-    k_stage_rows<<<nblk(32 * N, 256), 256, 0, c->stream>>>(
+    k_stage_rows<STAGE_RG><<<nblk(STAGE_RG * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
         s.hkey.as<unsigned long long>(), s.repoch.as<int32_t>(), epoch,
