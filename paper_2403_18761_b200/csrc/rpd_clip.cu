@@ -37,6 +37,9 @@
 #ifndef RPD_CLIP_MINB
 #define RPD_CLIP_MINB 2  // min resident blocks per SM for the fast kernel
 #endif
+#ifndef RPD_CLIP_STATIC
+#define RPD_CLIP_STATIC 70  // percent of the fast kernel's pairs assigned grid-stride
+#endif
 #ifndef RPD_CLIP_THREADS
 #define RPD_CLIP_THREADS 256  // threads per block of the fast kernel
 #endif
@@ -356,7 +359,8 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ nbr_off,
     const int32_t* __restrict__ nbr_idx, const double4* __restrict__ planes,
     const int32_t* __restrict__ twin, long long N, PairOut out,
-    unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev) {
+    unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev,
+    int* __restrict__ dyn) {
   using WS = WarpState<GW, VPL>;
   if (n_dev) n_pairs = *n_dev;
   constexpr int MAXP = WS::MAXP;
@@ -400,19 +404,33 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     pf_e0 = __ldg(nbr_off + pf_i);
     pf_e1 = __ldg(nbr_off + pf_i + 1);
   };
-  if (gw < n_pairs) {
-    fetch1(gw);
+  // pair order: the first RPD_CLIP_STATIC percent grid-stride (no atomics), the rest taken
+  // one at a time from a counter (dyn), so that the groups finish together instead of the
+  // kernel waiting for the groups whose static share drew the most expensive pieces
+  const int64_t n_static = dyn ? n_pairs * RPD_CLIP_STATIC / 100 : n_pairs;
+  auto next_of = [&](int64_t cur) -> int64_t {
+    if (cur + nw < n_static) return cur + nw;
+    if (!dyn) return n_pairs;
+    long long v = 0;
+    if (lane == 0) v = n_static + atomicAdd(dyn, 1);
+    return (int64_t)__shfl_sync(FULL, v, 0, GW);
+  };
+  const int64_t first = gw < n_static ? gw : next_of(n_pairs);
+  if (first < n_pairs) {
+    fetch1(first);
     fetch2();
   }
-  for (int64_t pi = gw; pi < n_pairs; pi += nw) {
+  int64_t nxt = n_pairs;
+  for (int64_t pi = first; pi < n_pairs; pi = nxt) {
+    nxt = next_of(pi);
     const int64_t p = pf_p;
     const int e0 = pf_e0, e1 = pf_e1, mo = pf_mo;
     const int nwp = (e1 - e0 + 31) >> 5;  // incidence-mask words of the pair
 #pragma unroll
     for (int q = 0; q < NTX; ++q)
       if (lane + GW * q < 12) (&S.V[0][0])[lane + GW * q] = pf_tx[q];
-    const bool has_next = pi + nw < n_pairs;
-    if (has_next) fetch1(pi + nw);
+    const bool has_next = nxt < n_pairs;
+    if (has_next) fetch1(nxt);
     if (lane < 4) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -1041,7 +1059,7 @@ template <int GW, int VPL>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
-                                 int32_t* over, const int32_t* n_dev) {
+                                 int32_t* over, const int32_t* n_dev, int* dyn = nullptr) {
   constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
@@ -1064,7 +1082,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
       c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>(),
-      n_dev);
+      n_dev, dyn);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -1078,9 +1096,12 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
   if (wide)
     return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, nullptr,
                                 nullptr);
+  cudaError_t e = c->p_dyn.ensure(sizeof(int));
+  if (e) return e;
+  if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
   return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL>(c, n_pairs, nullptr, pair_tet, tet_ids,
                                                   cand_idx, moff, c->p_over.as<int32_t>(),
-                                                  nullptr);
+                                                  nullptr, c->p_dyn.as<int>());
 }
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
