@@ -86,7 +86,10 @@ rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
  *                            (this rank's tet shard; the caller keeps the local->global map)
  *   spheres  [N][4] double   (x, y, z, r), r >= 0
  *   nbr_off  [N+1]  int32    CSR offsets of the k_site neighbour lists
- *   nbr_idx  [nbr_off[N]] int32 neighbour sphere ids (any order; the ctx sorts a copy)
+ *   nbr_idx  [E]    int32    neighbour sphere ids (any order; the ctx sorts a copy)
+ *   E        host int64      length of nbr_idx; must equal nbr_off[N] (else RPD_EINVAL at the
+ *                            call's readback); E < 0: read nbr_off[N] (one extra host round
+ *                            trip when nbr_off is a device pointer)
  * Outputs (ctx-owned device arrays):
  *   *cand_off [T+1] int32    per-tet candidate offsets (k_tet(t) = cand_off[t+1]-cand_off[t])
  *   *cand_idx [n_cand] int32 candidate sphere ids, ascending per tet
@@ -95,7 +98,7 @@ rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
  * j some vertex v of t has PD_i(v) < PD_j(v) strictly; for k_site(i) = 0, iff N == 1. */
 rpd_status rpd_relations(rpd_ctx* ctx, const double* verts, int64_t V, const int32_t* tets,
                          int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
-                         const int32_t* nbr_idx, const int32_t** cand_off,
+                         const int32_t* nbr_idx, int64_t E, const int32_t** cand_off,
                          const int32_t** cand_idx, int64_t* n_cand);
 
 /* Pieces of the RPD restricted to the ctx's tets (device arrays owned by ctx). */
@@ -122,7 +125,8 @@ rpd_status rpd_clip(rpd_ctx* ctx, rpd_pieces* out);
 
 /* Partial update ("only select a subset of tets ... relating to new spheres").
  * spheres [N_new][4]: the first N_old are unchanged, new sphere ids [N_old, N_new) appended;
- * nbr_off/nbr_idx: the new neighbour CSR over all N_new spheres; new_ids [M] int32 must equal
+ * nbr_off/nbr_idx/E: the new neighbour CSR over all N_new spheres (E as in rpd_relations);
+ * new_ids [M] int32 must equal
  * N_old..N_new-1 (else RPD_EINVAL); M == 0 is the identity.
  * Dirty tets = { t : rel_new(t, n) for some new n } (R11); they get a full
  * re-filter + clip with the new neighbour lists; clean tets keep candidates and pieces
@@ -130,7 +134,7 @@ rpd_status rpd_clip(rpd_ctx* ctx, rpd_pieces* out);
  * ascending) and their count (host).  The ctx candidate CSR is updated the same way.
  * Requires a prior rpd_relations + rpd_clip (else RPD_ESTATE). */
 rpd_status rpd_update_partial(rpd_ctx* ctx, const double* spheres, int64_t N_new,
-                              const int32_t* nbr_off, const int32_t* nbr_idx,
+                              const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                               const int32_t* new_ids, int64_t M, rpd_pieces* out,
                               const int32_t** dirty_tets, int64_t* n_dirty);
 

@@ -130,6 +130,7 @@ rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream) {
   rpd_ctx* c = new rpd_ctx();
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
+  if (!e) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   if (e) {
     delete c;
     return RPD_ECUDA;
@@ -229,8 +230,10 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
 
 // E = nbr_off[N] (host or device pointer)
 static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t* E) {
-  *E = 0;
-  if (N <= 0) return RPD_OK;
+  if (*E >= 0 || N <= 0) {  // given by the caller (checked against nbr_off[N] on the device)
+    if (N <= 0) *E = 0;
+    return RPD_OK;
+  }
   if (is_host_ptr(nbr_off)) {
     *E = nbr_off[N];
   } else {
@@ -244,9 +247,8 @@ static rpd_status read_E(rpd_ctx* c, const int32_t* nbr_off, int64_t N, int64_t*
 }
 
 static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
-                                const int32_t* nbr_off, const int32_t* nbr_idx,
+                                const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                                 bool reuse_rows, int epoch) {
-  int64_t E = 0;
   rpd_status s = read_E(c, nbr_off, N, &E);
   if (s) return s;
   if (E > 0 && !nbr_idx) return fail(c, RPD_EINVAL, "nbr_idx is NULL");
@@ -499,7 +501,7 @@ static rpd_status fill_pieces(rpd_ctx* c, rpd_pieces* out) {
 
 rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32_t* tets,
                          int64_t T, const double* spheres, int64_t N, const int32_t* nbr_off,
-                         const int32_t* nbr_idx, const int32_t** cand_off,
+                         const int32_t* nbr_idx, int64_t E, const int32_t** cand_off,
                          const int32_t** cand_idx, int64_t* n_cand) {
   if (!c) return RPD_EINVAL;
   if (V < 0 || T < 0 || N < 0 || T > 0x7fffffff || N > 0x7fffffff || (T > 0 && !tets) ||
@@ -517,7 +519,7 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_stage_mesh(c, d_verts, V, d_tets, T), "stage mesh");
   c->epoch = 0;
-  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx, false, 0);
+  rpd_status s = stage_spheres(c, spheres, N, nbr_off, nbr_idx, E, false, 0);
   if (s) return s;
   CK(c->cepoch.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
   CK(cudaMemsetAsync(c->cepoch.p, 0, sizeof(int32_t) * (T > 0 ? T : 1), c->stream), "memset");
@@ -550,7 +552,7 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
 }
 
 rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
-                              const int32_t* nbr_off, const int32_t* nbr_idx,
+                              const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                               const int32_t* new_ids, int64_t M, rpd_pieces* out,
                               const int32_t** dirty_tets, int64_t* n_dirty) {
   if (!c) return RPD_EINVAL;
@@ -581,7 +583,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
   ++c->epoch;
-  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, true, c->epoch);
+  rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, E, true, c->epoch);
   if (s) return s;
   tmark(c, "staged");
   c->last.N = N_new;

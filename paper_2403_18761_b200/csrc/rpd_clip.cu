@@ -1063,14 +1063,18 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
-  cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e) return e;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_clip<GW, VPL>, THREADS, smem);
-  if (occ < 1) occ = 1;
+  // kernel attributes and occupancy are set / queried once per instantiation (host API calls
+  // cost microseconds per launch)
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e) return e;
+    int o = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_clip<GW, VPL>, THREADS, smem);
+    occ = o < 1 ? 1 : o;
+  }
+  const int sms = c->sms;
   int64_t want = (n + GROUPS - 1) / GROUPS;
   int64_t grid = (int64_t)sms * occ;
   if (want < grid) grid = want;

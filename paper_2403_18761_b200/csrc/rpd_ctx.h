@@ -103,6 +103,7 @@ struct PieceSet {
 
 struct rpd_ctx {
   int device = 0;
+  int sms = 148;  // multiprocessor count of the device (queried at create)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int filter_mode = RPD_FILTER_ALL_PAIRS;

@@ -570,8 +570,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
     }
     const int64_t ns = sphere_hi - sphere_lo;
     if (ns > 0) {
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const int sms = c->sms;
       // work-item queues: int2 header {leaf items, super items}, leaf items, super items
       int64_t cap_items = 48 * ns + 4 * n_leaf + 4096;
       int64_t cap_sup = 8 * ns + 4 * n_sup + 4096;

@@ -128,6 +128,9 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   dbg_t[0] = clock64();
 #endif
   const int32_t e0 = off_in[i], e1 = off_in[i + 1];
+  // the previous stage's row bounds, loaded together with the new ones (partial updates)
+  const bool has_old = old.off && i < old.N;
+  const int32_t o0 = has_old ? old.off[i] : 0, o1 = has_old ? old.off[i + 1] : 0;
   if (lane == 0) {
     off_out[i] = e0;
     if (i == N - 1) off_out[N] = e1;
@@ -137,16 +140,24 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
     return;
   }
   const int k = e1 - e0;
-  // sorted strictly ascending?  (then no duplicates either)
-  bool sorted = true;
-  for (int32_t e = e0 + lane; e + 1 < e1; e += RG) sorted &= idx_in[e] < idx_in[e + 1];
+  // sorted strictly ascending?  (then no duplicates either); rows of at most RG entries hold
+  // one entry per lane, and the old row's entries are loaded alongside for the reuse test
+  bool sorted = true, same = has_old && (o1 - o0) == k;
+  if (k <= RG) {
+    const bool have = lane < k;
+    const int32_t x = have ? idx_in[e0 + lane] : 0;
+    const int32_t ox = have && same ? old.idx[o0 + lane] : 0;
+    const int32_t xn = __shfl_down_sync(FULL, x, 1, RG);
+    sorted = !(have && lane + 1 < k) || x < xn;
+    same = same && (!have || ox == x);
+  } else {
+    for (int32_t e = e0 + lane; e + 1 < e1; e += RG) sorted &= idx_in[e] < idx_in[e + 1];
+    for (int32_t q = lane; same && q < k; q += RG) same = old.idx[o0 + q] == idx_in[e0 + q];
+  }
   sorted = __all_sync(FULL, sorted);
   // unchanged row of an old sphere: copy the previous stage
   // (empty rows are never reused: their Alg. 1 boolean depends on N, R4)
-  if (old.off && i < old.N && sorted && k > 0) {
-    const int32_t o0 = old.off[i], o1 = old.off[i + 1];
-    bool same = (o1 - o0) == k;
-    for (int32_t q = lane; same && q < k; q += RG) same = old.idx[o0 + q] == idx_in[e0 + q];
+  if (has_old && sorted && k > 0) {
     if (__all_sync(FULL, same)) {
       if (lane == 0) repoch[i] = old.repoch[i];
       for (int32_t q = lane; q < k; q += RG) {

@@ -72,10 +72,10 @@ def load_library(path: str = LIB_PATH):
     L.rpd_last_error.argtypes = [vp]
     L.rpd_last_error.restype = C.c_char_p
     L.rpd_set_option.argtypes = [vp, i32, i64]
-    L.rpd_relations.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(vp),
+    L.rpd_relations.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, vp, i64, C.POINTER(vp),
                                 C.POINTER(vp), C.POINTER(i64)]
     L.rpd_clip.argtypes = [vp, C.POINTER(_Pieces)]
-    L.rpd_update_partial.argtypes = [vp, vp, i64, vp, vp, vp, i64, C.POINTER(_Pieces),
+    L.rpd_update_partial.argtypes = [vp, vp, i64, vp, vp, i64, vp, i64, C.POINTER(_Pieces),
                                      C.POINTER(vp), C.POINTER(i64)]
     L.rpd_download_pieces.argtypes = [vp] * 8
     L.rpd_download_cands.argtypes = [vp, vp, vp]
@@ -173,7 +173,8 @@ class RPDContext:
         T = int(np.prod(kt.shape)) // 4
         N = int(np.prod(ks.shape)) // 4
         co, ci, nc = C.c_void_p(), C.c_void_p(), C.c_int64()
-        self._check(self.L.rpd_relations(self.h, pv, V, pt, T, ps, N, po, pi, C.byref(co),
+        E = int(np.prod(ki.shape))  # length of nbr_idx (no device read of nbr_off[N])
+        self._check(self.L.rpd_relations(self.h, pv, V, pt, T, ps, N, po, pi, E, C.byref(co),
                                          C.byref(ci), C.byref(nc)))
         self.T, self.N, self.n_cand = T, N, nc.value
         self._keep = (kv, kt, ks, ko, ki)
@@ -194,7 +195,8 @@ class RPDContext:
         M = int(np.prod(kn.shape))
         P = _Pieces()
         dt, nd = C.c_void_p(), C.c_int64()
-        self._check(self.L.rpd_update_partial(self.h, ps, N_new, po, pi, pn, M, C.byref(P),
+        E = int(np.prod(ki.shape))
+        self._check(self.L.rpd_update_partial(self.h, ps, N_new, po, pi, E, pn, M, C.byref(P),
                                               C.byref(dt), C.byref(nd)))
         self.N = N_new
         self.counts = PieceCounts(P.n_pieces, P.n_inc)
