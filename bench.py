@@ -342,20 +342,26 @@ def main():
         flops = 7.0 * float(np.median([r["rel_tests"] for r in recs]))
         per_unit = "7 flop per literal Alg. 1 vertex test (3 FMA + compare), tests counted by the kernel"
     else:
-        kern, kms = "k_clip<16,1>+k_clip<32,1>+k_clip<32,4>", cmed
+        kern, kms = "k_clip<16,1>+k_clip<32,2>+k_clip<32,4>", cmed
         flops = float(np.median([r["clip_work"] for r in recs]))
         per_unit = ("24 flop per (pair, plane) corner classification + 8 per vertex sign test + "
                     "40 per vertex construction + 30 per fan triangle, counted by the kernel")
     achieved = flops / (kms * 1e-3) / 1e12
-    traffic = None
+    traffic, ncu = None, None
     try:
-        traffic = json.load(open(NCU_TRAFFIC)).get(kern)
+        ncu = json.load(open(NCU_TRAFFIC)).get(kern)
+        traffic = ncu.get("traffic") if isinstance(ncu, dict) else ncu
     except Exception:
         pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": kern,
                 "kernel_ms": kms, "algorithmic_flops": flops, "per_unit": per_unit,
                 "peak_source": peak_src + "; FP64 DFMA pipe (fp64 ALU bound, no tensor cores)"}
+    if isinstance(ncu, dict):
+        # what bounds the kernel: instruction issue and latency of a branchy
+        # per-pair program, not the FP64 pipe -- from the committed ncu capture
+        roofline["ncu"] = {k: ncu[k] for k in ("ipc", "issue_frac", "fp64_pipe_frac",
+                                               "warps_active_frac", "note") if k in ncu}
 
     line = {
         "metric": "tet-sphere pairs clipped/s",
