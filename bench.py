@@ -29,8 +29,18 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK = os.path.join(ROOT, "profiles", "fp64_peak.json")
 NCU_TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
-WORKLOAD_NAME = ("C3+C4: ~200k-tet box-with-hole Kuhn mesh, 20k medial-like spheres full RPD "
-                 "+ 10 partial updates x M=500 (final 25.5k spheres)")
+WORKLOADS = {
+    "C4": ("C3+C4: ~200k-tet box-with-hole Kuhn mesh, 20k medial-like spheres full RPD "
+           "+ 10 partial updates x M=500 (final 25.5k spheres)"),
+    "C3": "C3: ~200k-tet box-with-hole Kuhn mesh, 20k medial-like spheres, full RPD",
+    "C5": ("C5: ~4M-tet box-with-hole Kuhn mesh, 50k medial-like spheres with high radius "
+           "variance, full RPD"),
+    "C2": "C2: ~50k-tet box-with-hole Kuhn mesh, 2k medial-like spheres, full RPD",
+}
+
+
+def workload_name(cfg):
+    return WORKLOADS.get(cfg, cfg)
 
 
 def parse():
@@ -39,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C4")
+    ap.add_argument("--config", default="C4", choices=sorted(WORKLOADS),
+                    help="C4 (default): C3 full RPD + 10 partial updates; C5: 4M tets, 50k spheres")
     ap.add_argument("--filter", default="pruned", choices=["all_pairs", "pruned"])
     ap.add_argument("--partial-iters", type=int, default=-1,
                     help="partial updates per step (-1: all batches of the config)")
@@ -158,7 +169,7 @@ def run_reference(args):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": WORKLOAD_NAME, "config": args.config},
+            "data": "synthetic", "config": {"workload": workload_name(args.config), "config": args.config},
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
@@ -190,7 +201,7 @@ def cpu_baseline(w, seconds):
     dt = time.perf_counter() - t0
     return {"value": len(r["cand_idx"]) / dt, "unit": "pairs/s", "cores": cores,
             "kind": "oracle",
-            "sample": f"{n_s} random tets of {w.T} (full RPD of the 20k-sphere set: Alg. 1 over "
+            "sample": f"{n_s} random tets of {w.T} (full RPD of the {w.N}-sphere set: Alg. 1 over "
                       f"all {w.N} spheres + clip), {dt:.1f} s; partial updates not sampled"}
 
 
@@ -369,7 +380,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_NAME, "T": w.T, "N": w.N,
+        "config": {"workload": workload_name(args.config), "config": args.config, "T": w.T, "N": w.N,
                    "partial_iters": len(d_batches),
                    "M": (len(batches[0][0]) - w.N) if batches else 0,
                    "filter": args.filter, "parallelism": f"tet-shard x{world}",

@@ -14,6 +14,9 @@ Parity status of each function (DESIGN.md §Oracle pins):
   pieces: non-empty, facemask, incidences, vol, m1 ... pinned (exact checker, brute force,
           Kuhn closed forms, partition, Voronoi reduction, power membership)
   partial update (R11) ... pinned (partial == full recompute, M = 0 identity)
+  fractional Euler characteristics (NEXT-1) ... pinned (mesh Euler by V-E+F-T, a single
+          sphere gives the mesh's Euler, explicit extraction of every RPC / RPF complex by
+          exact rational vertex enumeration, RPF symmetry on generic inputs)
 """
 from __future__ import annotations
 
@@ -45,7 +48,8 @@ def build(force: bool = False) -> str:
 class _Input(C.Structure):
     _fields_ = [("V", C.c_int64), ("T", C.c_int64), ("N", C.c_int64),
                 ("verts", C.c_void_p), ("tets", C.c_void_p), ("spheres", C.c_void_p),
-                ("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("brute", C.c_int)]
+                ("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("brute", C.c_int),
+                ("euler", C.c_int)]
 
 
 class _Result(C.Structure):
@@ -57,6 +61,9 @@ class _Result(C.Structure):
                 ("piece_facemask", C.POINTER(C.c_uint8)),
                 ("inc_off", C.POINTER(C.c_int32)), ("inc_sphere", C.POINTER(C.c_int32)),
                 ("n_pieces", C.c_int64), ("n_inc", C.c_int64),
+                ("euler_denom", C.c_int64), ("piece_euler", C.POINTER(C.c_int64)),
+                ("rpf_off", C.POINTER(C.c_int32)), ("rpf_sphere", C.POINTER(C.c_int32)),
+                ("rpf_euler", C.POINTER(C.c_int64)), ("n_rpf", C.c_int64),
                 ("n_rel_tests", C.c_int64), ("n_clip_tests", C.c_int64),
                 ("n_constructions", C.c_int64), ("n_fan_triangles", C.c_int64),
                 ("n_zero_hits", C.c_int64),
@@ -85,7 +92,7 @@ class OracleError(RuntimeError):
     pass
 
 
-def _prep(verts, tets, spheres, nbr_off, nbr_idx, brute):
+def _prep(verts, tets, spheres, nbr_off, nbr_idx, brute, euler=False):
     keep = [np.ascontiguousarray(verts, dtype=np.float64),
             np.ascontiguousarray(tets, dtype=np.int32),
             np.ascontiguousarray(spheres, dtype=np.float64).reshape(-1, 4),
@@ -93,7 +100,7 @@ def _prep(verts, tets, spheres, nbr_off, nbr_idx, brute):
             np.ascontiguousarray(nbr_idx if len(nbr_idx) else np.zeros(1), dtype=np.int32)]
     inp = _Input(len(keep[0]), len(keep[1]), len(keep[2]), keep[0].ctypes.data,
                  keep[1].ctypes.data, keep[2].ctypes.data, keep[3].ctypes.data,
-                 keep[4].ctypes.data, int(brute))
+                 keep[4].ctypes.data, int(brute), int(euler))
     return inp, keep
 
 
@@ -105,10 +112,13 @@ def power_distance(sphere, x) -> float:
 
 
 def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=True,
-        nthreads=0):
+        nthreads=0, euler=False):
     """Oracle RPD of ``tet_ids`` (all tets when None).  Returns a dict of numpy arrays in the
-    boundary's layout (cand CSR, piece CSR, incidence CSR) plus instrumentation counters."""
-    inp, keep = _prep(verts, tets, spheres, nbr_off, nbr_idx, brute)
+    boundary's layout (cand CSR, piece CSR, incidence CSR) plus instrumentation counters.
+    ``euler``: also the fractional Euler characteristics -- per piece
+    ``piece_euler`` and per radical facet ``rpf_off/rpf_sphere/rpf_euler``, exact numerators
+    over ``euler_denom`` (payloads from the whole mesh, even when ``tet_ids`` is a subset)."""
+    inp, keep = _prep(verts, tets, spheres, nbr_off, nbr_idx, brute, euler)
     if tet_ids is None:
         ids_p, n = None, len(keep[1])
     else:
@@ -140,6 +150,12 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
                                                       "n_constructions", "n_fan_triangles",
                                                       "n_zero_hits")},
         }
+        if euler and clip:
+            out.update({"euler_denom": int(r.euler_denom),
+                        "piece_euler": arr(r.piece_euler, r.n_pieces, np.int64),
+                        "rpf_off": arr(r.rpf_off, r.n_pieces + 1, np.int32),
+                        "rpf_sphere": arr(r.rpf_sphere, r.n_rpf, np.int32),
+                        "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64)})
     finally:
         L.oracle_free(rp)
     return out
@@ -170,7 +186,7 @@ def rpd_workload(w, **kw):
 
 
 def partial_update(old, verts, tets, spheres_new, nbr_off_new, nbr_idx_new, n_old,
-                   nthreads=0):
+                   nthreads=0, euler=False):
     """Partial RPD update, reading R11: spheres [n_old, N_new) are new; dirty tets =
     {t : exists new n with rel_new(t, n)}; dirty tets get a full re-candidate + clip with the
     new neighbour lists; clean tets keep ``old``'s candidates and pieces.  Returns
@@ -184,7 +200,7 @@ def partial_update(old, verts, tets, spheres_new, nbr_off_new, nbr_idx_new, n_ol
     else:
         dirty = np.zeros(0, dtype=np.int32)
     new = rpd(verts, tets, spheres_new, nbr_off_new, nbr_idx_new, tet_ids=dirty,
-              nthreads=nthreads) if len(dirty) else None
+              nthreads=nthreads, euler=euler) if len(dirty) else None
     return merge_per_tet(old, new, dirty, T), dirty
 
 
@@ -194,13 +210,19 @@ def per_tet_lists(res, T):
     co, ci = res["cand_off"], res["cand_idx"]
     po = res["piece_off"]
     io = res["inc_off"]
+    ro = res.get("rpf_off")
     for a in range(T):
         cands = ci[co[a]:co[a + 1]].tolist()
         pcs = []
         for p in range(po[a], po[a + 1]):
+            eu = None
+            if ro is not None and len(ro) == len(res["piece_sphere"]) + 1:
+                eu = (int(res["piece_euler"][p]),
+                      tuple(res["rpf_sphere"][ro[p]:ro[p + 1]].tolist()),
+                      tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()))
             pcs.append((int(res["piece_sphere"][p]), float(res["piece_vol"][p]),
                         tuple(res["piece_m1"][p].tolist()), int(res["piece_facemask"][p]),
-                        tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist())))
+                        tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist()), eu))
         out.append((cands, pcs))
     return out
 
@@ -208,18 +230,28 @@ def per_tet_lists(res, T):
 def from_per_tet_lists(L):
     cand_off = [0]
     cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
+    pe, rpf_off, rpf_j, rpf_e = [], [0], [], []
     for cands, pcs in L:
         cand_idx += cands
         cand_off.append(len(cand_idx))
-        for (s, v, m, f, ii) in pcs:
+        for (s, v, m, f, ii, eu) in pcs:
             ps.append(s)
             pv.append(v)
             pm.append(m)
             pf.append(f)
             inc += list(ii)
             inc_off.append(len(inc))
+            if eu is not None:
+                pe.append(eu[0])
+                rpf_j += list(eu[1])
+                rpf_e += list(eu[2])
+                rpf_off.append(len(rpf_j))
         piece_off.append(len(ps))
-    return {"cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
+    eul = {}
+    if len(pe) == len(ps) and len(rpf_off) == len(ps) + 1:
+        eul = {"piece_euler": np.array(pe, np.int64), "rpf_off": np.array(rpf_off, np.int32),
+               "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64)}
+    return {**eul, "cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
             "piece_off": np.array(piece_off, np.int32), "piece_sphere": np.array(ps, np.int32),
             "piece_vol": np.array(pv, np.float64),
             "piece_m1": np.array(pm, np.float64).reshape(-1, 3),
@@ -233,7 +265,30 @@ def merge_per_tet(old, new, dirty, T):
         Ln = per_tet_lists(new, len(dirty))
         for a, t in enumerate(dirty):
             L[t] = Ln[a]
-    return from_per_tet_lists(L)
+    out = from_per_tet_lists(L)
+    if "euler_denom" in old:
+        out["euler_denom"] = old["euler_denom"]
+        if new is not None and new.get("euler_denom", 0) != old["euler_denom"]:
+            raise OracleError("partial update: Euler denominators differ")
+    return out
+
+
+def euler_sums(res, N, nbr_off, nbr_idx):
+    """Per-sphere fractional Euler sums ("For each medial sphere, we collect
+    the fractional Euler characteristics for all of its restricted elements"), as exact Python
+    Fractions: rpc[i] = Euler(RPC(m_i)) = sum over the pieces of m_i; rpf[(i, j)] =
+    Euler(RPF(m_i, m_j)) seen from m_i = sum over its pieces' facets on h_ij."""
+    from fractions import Fraction
+    L = res["euler_denom"]
+    rpc = [Fraction(0)] * N
+    rpf = {}
+    po, ro = res["piece_off"], res["rpf_off"]
+    for p, i in enumerate(res["piece_sphere"].tolist()):
+        rpc[i] += Fraction(int(res["piece_euler"][p]), L)
+        for r in range(ro[p], ro[p + 1]):
+            key = (i, int(res["rpf_sphere"][r]))
+            rpf[key] = rpf.get(key, Fraction(0)) + Fraction(int(res["rpf_euler"][r]), L)
+    return rpc, rpf
 
 
 def max_threads() -> int:

@@ -189,3 +189,68 @@ def check_tet(verts, tets, spheres, t, i, S):
     r["vol"] = r["vol"] / L ** 3
     r["m1"] = [m / L ** 4 for m in r["m1"]]
     return r
+
+
+def exact_piece_cells(tet_X, spheres_X, i, S):
+    """The piece P(t, i) as a cell complex, exactly (no SoS): None if empty, else
+    (vertices, edges, facets) with vertices as exact homogeneous lattice points (X, Y, Z, D),
+    edges as frozensets of two vertices that share two active planes and facets as
+    (source, frozenset of vertices) for every plane holding a positive-area 2-face.
+    ``generic`` is False when some vertex has more than three active planes (then the cell
+    structure of the symbolically perturbed polytope may differ)."""
+    pls = planes_for(tet_X, spheres_X, i, S)
+    verts = set()
+    for a, b, c in itertools.combinations(range(len(pls)), 3):
+        v = _solve(pls[a], pls[b], pls[c])
+        if v is not None and all(_val(pl, v) >= 0 for pl in pls):
+            verts.add(v)
+    pts = {v: (Fraction(v[0], v[3]), Fraction(v[1], v[3]), Fraction(v[2], v[3])) for v in verts}
+    if _affine_rank(list(pts.values())) < 3:
+        return None
+    active = {v: frozenset(k for k, pl in enumerate(pls) if _val(pl, v) == 0) for v in verts}
+    generic = all(len(a) == 3 for a in active.values())
+    vl = list(verts)
+    edges = set()
+    for a in range(len(vl)):
+        for b in range(a + 1, len(vl)):
+            if len(active[vl[a]] & active[vl[b]]) >= 2:
+                edges.add(frozenset((vl[a], vl[b])))
+    facets = []
+    for k, pl in enumerate(pls):
+        on = [v for v in vl if k in active[v]]
+        if _affine_rank([pts[v] for v in on]) == 2:
+            facets.append((pl[2], frozenset(on)))
+    return {"vertices": set(vl), "edges": edges, "facets": facets, "generic": generic}
+
+
+def explicit_euler(verts, tets, spheres, nbr_off, nbr_idx, i):
+    """Euler characteristics of the restricted elements of sphere i extracted explicitly
+    (SPEC.md:346, "rpc_euler equals V-E+F-C computed from an explicitly extracted ... complex"):
+    the pieces of i in all tets are glued by their exact vertex coordinates into one cell
+    complex; Euler(RPC) = V - E + F - C over it, and for each neighbour j Euler(RPF(i, j)) =
+    V - E + F over its 2-faces on the radical plane h_ij.  Returns (rpc, {j: rpf}, generic)."""
+    sph_X = [tuple(_lat(s[c]) for c in range(4)) for s in spheres]
+    S = [int(j) for j in nbr_idx[nbr_off[i]:nbr_off[i + 1]]]
+    if not S and len(spheres) > 1:
+        return 0, {}, True  # hidden sphere (DESIGN.md R4): no pieces
+    V, E, F, C = set(), set(), set(), 0
+    rpf = {}
+    generic = True
+    for t in range(len(tets)):
+        tet_X = [tuple(_lat(verts[v][c]) for c in range(3)) for v in tets[t]]
+        cell = exact_piece_cells(tet_X, sph_X, i, S)
+        if cell is None:
+            continue
+        generic &= cell["generic"]
+        C += 1
+        V |= cell["vertices"]
+        E |= cell["edges"]
+        for src, on in cell["facets"]:
+            F.add(on)
+            if src[0] == "r":
+                fv, fe, ff = rpf.setdefault(src[1], (set(), set(), set()))
+                fv |= on
+                fe |= {e for e in cell["edges"] if e <= on}
+                ff.add(on)
+    return (len(V) - len(E) + len(F) - C,
+            {j: len(a) - len(b) + len(c) for j, (a, b, c) in rpf.items()}, generic)

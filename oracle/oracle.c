@@ -149,6 +149,7 @@ typedef struct {
   const int32_t* nbr_off;
   const int32_t* nbr_idx;
   int brute; /* 1: cand(t) = all spheres and N(i) = all j != i (C1 step 8) */
+  int euler; /* 1: fractional Euler characteristics of the pieces */
 } oracle_input;
 
 typedef struct {
@@ -160,6 +161,12 @@ typedef struct {
   uint8_t* piece_facemask;
   int32_t *inc_off, *inc_sphere;
   int64_t n_pieces, n_inc;
+  /* fractional Euler characteristics (euler = 1): exact rationals num / euler_denom */
+  int64_t euler_denom;
+  int64_t* piece_euler;          /* [n_pieces] Euler of the piece's fractional complex */
+  int32_t *rpf_off, *rpf_sphere; /* [n_pieces + 1], [n_rpf]: radical facets j, ascending */
+  int64_t* rpf_euler;            /* [n_rpf] Euler of the piece's facet on h_ij */
+  int64_t n_rpf;
   /* instrumentation (C1 step 9) */
   int64_t n_rel_tests, n_clip_tests, n_constructions, n_fan_triangles, n_zero_hits;
   int status;
@@ -306,6 +313,136 @@ int oracle_relation_matrix(const oracle_input* in, const int32_t* tet_ids, int64
   return 0;
 }
 
+/* ------------------------------------------------------------------ fractional Euler payloads
+ *
+ * PAPER.md:488-491 (Sec. 4.1.2, Fig. 5): "such fractional Euler characteristics are inputted
+ * together with the mesh, based on the combinatorial structure of the tetrahedral mesh" -- every
+ * vertex / edge / face of the tet complex carries 1 / (number of tets sharing it) inside each
+ * of those tets ("both vertex b or d are shared between A and B, so their fractional Euler
+ * characteristic inside each triangle is only 1/2"), a tet carries 1.  The oracle keeps every
+ * payload as an exact integer numerator over the common denominator L = lcm of all sharing
+ * counts: payload(element) = L / count.
+ *
+ * Per tet t, A[14 t + m]: m = 0..3 corners, 4..9 edges (corner pairs 01 02 03 12 13 23),
+ * 10..13 faces (face k opposite corner k).  Counts come from sorting the keys of all
+ * simplices of all tets (plain counting, no hashing). */
+
+typedef struct { int32_t v[3]; } key3;
+
+static int cmp_i64(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return (x > y) - (x < y);
+}
+static int cmp_key3(const void* a, const void* b) {
+  const key3 *x = (const key3*)a, *y = (const key3*)b;
+  for (int k = 0; k < 3; ++k)
+    if (x->v[k] != y->v[k]) return x->v[k] < y->v[k] ? -1 : 1;
+  return 0;
+}
+static void sort3(int32_t* a) {
+  for (int p = 0; p < 3; ++p)
+    for (int q = p + 1; q < 3; ++q)
+      if (a[q] < a[p]) { int32_t t = a[p]; a[p] = a[q]; a[q] = t; }
+}
+static int64_t gcd64(int64_t a, int64_t b) {
+  while (b) { int64_t t = a % b; a = b; b = t; }
+  return a;
+}
+/* number of entries equal to the key in a sorted array */
+static int64_t count_i64(const int64_t* sorted, int64_t n, int64_t key) {
+  int64_t lo = 0, hi = n;  /* first >= key */
+  while (lo < hi) { int64_t m = (lo + hi) / 2; if (sorted[m] < key) lo = m + 1; else hi = m; }
+  int64_t c = 0;
+  while (lo + c < n && sorted[lo + c] == key) ++c;
+  return c;
+}
+static int64_t count_key3(const key3* sorted, int64_t n, const key3* key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) { int64_t m = (lo + hi) / 2; if (cmp_key3(&sorted[m], key) < 0) lo = m + 1; else hi = m; }
+  int64_t c = 0;
+  while (lo + c < n && cmp_key3(&sorted[lo + c], key) == 0) ++c;
+  return c;
+}
+
+static const int EDGE_CORNERS[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+/* payload numerators of every element of every tet and their denominator; 0 or -2 (L too big) */
+static int euler_payloads(const oracle_input* in, int64_t** A_out, int64_t* L_out) {
+  int64_t T = in->T, n = T > 0 ? T : 1;
+  int64_t* cnt14 = (int64_t*)malloc(sizeof(int64_t) * 14 * n);
+  int64_t* vkeys = (int64_t*)malloc(sizeof(int64_t) * 4 * n);
+  int64_t* ekeys = (int64_t*)malloc(sizeof(int64_t) * 6 * n);
+  key3* fkeys = (key3*)malloc(sizeof(key3) * 4 * n);
+  for (int64_t t = 0; t < T; ++t) {
+    const int32_t* tv = in->tets + 4 * t;
+    for (int k = 0; k < 4; ++k) vkeys[4 * t + k] = tv[k];
+    for (int e = 0; e < 6; ++e) {
+      int64_t a = tv[EDGE_CORNERS[e][0]], b = tv[EDGE_CORNERS[e][1]];
+      ekeys[6 * t + e] = a < b ? a * in->V + b : b * in->V + a;
+    }
+    for (int k = 0; k < 4; ++k) {
+      key3 f;
+      int m2 = 0;
+      for (int m = 0; m < 4; ++m)
+        if (m != k) f.v[m2++] = tv[m];
+      sort3(f.v);
+      fkeys[4 * t + k] = f;
+    }
+  }
+  int64_t* vs = (int64_t*)malloc(sizeof(int64_t) * 4 * n);
+  int64_t* es = (int64_t*)malloc(sizeof(int64_t) * 6 * n);
+  key3* fs = (key3*)malloc(sizeof(key3) * 4 * n);
+  memcpy(vs, vkeys, sizeof(int64_t) * 4 * T);
+  memcpy(es, ekeys, sizeof(int64_t) * 6 * T);
+  memcpy(fs, fkeys, sizeof(key3) * 4 * T);
+  qsort(vs, 4 * T, sizeof(int64_t), cmp_i64);
+  qsort(es, 6 * T, sizeof(int64_t), cmp_i64);
+  qsort(fs, 4 * T, sizeof(key3), cmp_key3);
+  int64_t L = 1;
+  int st = 0;
+  for (int64_t t = 0; t < T; ++t) {
+    for (int k = 0; k < 4; ++k) cnt14[14 * t + k] = count_i64(vs, 4 * T, vkeys[4 * t + k]);
+    for (int e = 0; e < 6; ++e) cnt14[14 * t + 4 + e] = count_i64(es, 6 * T, ekeys[6 * t + e]);
+    for (int k = 0; k < 4; ++k) cnt14[14 * t + 10 + k] = count_key3(fs, 4 * T, &fkeys[4 * t + k]);
+    for (int m = 0; m < 14 && !st; ++m) {
+      int64_t c = cnt14[14 * t + m];
+      int64_t g = gcd64(L, c);
+      if (L / g > ((int64_t)1 << 50) / c) st = -2;
+      else L = L / g * c;
+    }
+  }
+  for (int64_t k = 0; k < 14 * T; ++k) cnt14[k] = L / cnt14[k];
+  free(vkeys); free(ekeys); free(fkeys); free(vs); free(es); free(fs);
+  *A_out = cnt14;
+  *L_out = L;
+  return st;
+}
+
+/* payload numerator of a piece element (vertex, edge or facet) from the tet faces among the
+ * planes that define it (face mask fm, bit k = tet face k): no face -> the element is inside
+ * the tet (payload of the cell, 1); one face k -> inside tet face k; two faces -> on the tet
+ * edge joining the two corners that are on neither face; three faces -> the corner on none.
+ * This is the paper's inheritance rule: a vertex cut on an edge takes the
+ * edge's payload, an edge cut inside a face takes the face's, and new elements are never
+ * re-divided -- the carrier of an element is the smallest tet simplex containing it. */
+static int64_t carrier_payload(const int64_t* A14, int64_t L, unsigned fm) {
+  int nf = 0;
+  for (int k = 0; k < 4; ++k) nf += (fm >> k) & 1;
+  if (nf == 0) return L;
+  if (nf == 1) {
+    for (int k = 0; k < 4; ++k)
+      if (fm == (1u << k)) return A14[10 + k];
+  }
+  unsigned corners = 0xFu & ~fm;  /* corners on none of the faces */
+  if (nf == 2) {
+    for (int e = 0; e < 6; ++e)
+      if (corners == ((1u << EDGE_CORNERS[e][0]) | (1u << EDGE_CORNERS[e][1]))) return A14[4 + e];
+  }
+  for (int k = 0; k < 4; ++k)
+    if (corners == (1u << k)) return A14[k];
+  return 0; /* unreachable */
+}
+
 /* ------------------------------------------------------------------ clipping */
 
 typedef struct {
@@ -435,6 +572,10 @@ typedef struct {
   uint8_t facemask;
   int32_t* inc;
   int32_t ninc;
+  int64_t euler;      /* fractional Euler characteristic of the piece, numerator over L */
+  int32_t* rpf_j;     /* radical facets of the piece (neighbour j) ... */
+  int64_t* rpf_e;     /* ... and the fractional Euler characteristic of each, over L */
+  int32_t nrpf;
 } piece_t;
 
 static int cmp_i32(const void* a, const void* b) {
@@ -442,9 +583,80 @@ static int cmp_i32(const void* a, const void* b) {
   return (x > y) - (x < y);
 }
 
-/* P(t, i): returns 1 and fills *out if non-empty */
+static unsigned faces_of(const poly_t* P, const int32_t* planes, int n) {
+  unsigned fm = 0;
+  for (int k = 0; k < n; ++k)
+    if (P->pl[planes[k]].src < 0) fm |= 1u << (-1 - P->pl[planes[k]].src);
+  return fm;
+}
+
+static int cmp_rpf(const void* a, const void* b) {
+  const int64_t *x = (const int64_t*)a, *y = (const int64_t*)b;
+  return (x[0] > y[0]) - (x[0] < y[0]);
+}
+
+/* Fractional Euler characteristics of a finished piece (Eq. (1)):
+ *   Euler(piece)   = sum_vertices payload - sum_edges payload + sum_facets payload - 1 (cell)
+ *   Euler(facet f) = sum_{vertices on f} payload - sum_{edges on f} payload + payload(f)
+ * for every radical facet f (the piece's part of the RPF between m_i and m_j).  Vertices are
+ * the clipped polytope's plane triplets, edges every pair of vertices sharing two planes,
+ * facets the planes appearing in the triplets (the symbolically perturbed, simple polytope). */
+static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t* out) {
+  int nv = P->nv, npl = P->npl;
+  int64_t chi = -L;
+  int* is_facet = (int*)calloc(npl, sizeof(int));
+  int64_t* fe = (int64_t*)calloc(npl, sizeof(int64_t)); /* Euler of each facet */
+  for (int v = 0; v < nv; ++v) {
+    int64_t pv = carrier_payload(A14, L, faces_of(P, P->v[v].p, 3));
+    chi += pv;
+    for (int c = 0; c < 3; ++c) {
+      is_facet[P->v[v].p[c]] = 1;
+      fe[P->v[v].p[c]] += pv;
+    }
+  }
+  for (int u = 0; u < nv; ++u)
+    for (int w = u + 1; w < nv; ++w) {
+      int32_t e[2];
+      if (!shares_two(&P->v[u], &P->v[w], &e[0], &e[1])) continue;
+      int64_t pe = carrier_payload(A14, L, faces_of(P, e, 2));
+      chi -= pe;
+      fe[e[0]] -= pe;
+      fe[e[1]] -= pe;
+    }
+  int nr = 0;
+  for (int f = 0; f < npl; ++f) {
+    if (!is_facet[f]) continue;
+    int64_t pf = carrier_payload(A14, L, faces_of(P, &f, 1));
+    chi += pf;
+    fe[f] += pf;
+    if (P->pl[f].src >= 0) ++nr;
+  }
+  int64_t* pairs = (int64_t*)malloc(sizeof(int64_t) * 2 * (nr > 0 ? nr : 1));
+  int m = 0;
+  for (int f = 0; f < npl; ++f)
+    if (is_facet[f] && P->pl[f].src >= 0) {
+      pairs[2 * m] = P->pl[f].src;
+      pairs[2 * m + 1] = fe[f];
+      ++m;
+    }
+  qsort(pairs, nr, 2 * sizeof(int64_t), cmp_rpf);
+  out->euler = chi;
+  out->nrpf = nr;
+  out->rpf_j = (int32_t*)malloc(sizeof(int32_t) * (nr > 0 ? nr : 1));
+  out->rpf_e = (int64_t*)malloc(sizeof(int64_t) * (nr > 0 ? nr : 1));
+  for (int k = 0; k < nr; ++k) {
+    out->rpf_j[k] = (int32_t)pairs[2 * k];
+    out->rpf_e[k] = pairs[2 * k + 1];
+  }
+  free(pairs);
+  free(fe);
+  free(is_facet);
+}
+
+/* P(t, i): returns 1 and fills *out if non-empty.  A14 (payload numerators of the tet's
+ * elements over L, or NULL) switches on the fractional Euler characteristics. */
 static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piece_t* out,
-                      oracle_result* stats_acc) {
+                      oracle_result* stats_acc, const int64_t* A14, int64_t Lden) {
   int32_t k_site = nbr_count(in, i);
   int64_t Si[4], Sj[4];
   load_sphere(in, i, Si);
@@ -606,6 +818,11 @@ static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piec
     out->facemask = facemask;
     out->inc = inc;
     out->ninc = ninc;
+    out->euler = 0;
+    out->nrpf = 0;
+    out->rpf_j = NULL;
+    out->rpf_e = NULL;
+    if (A14) piece_euler(&P, A14, Lden, out);
   }
   stats_acc->n_clip_tests += P.n_clip_tests;
   stats_acc->n_constructions += P.n_constructions;
@@ -638,6 +855,10 @@ void oracle_free(oracle_result* r) {
   free(r->piece_facemask);
   free(r->inc_off);
   free(r->inc_sphere);
+  free(r->piece_euler);
+  free(r->rpf_off);
+  free(r->rpf_sphere);
+  free(r->rpf_euler);
   free(r);
 }
 
@@ -650,6 +871,17 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
   if (R->status) return R;
   if (!tet_ids) n_tets = in->T;
   R->n_tets = n_tets;
+  int64_t* A = NULL;
+  int64_t Lden = 0;
+  if (in->euler && do_clip) {
+    if (euler_payloads(in, &A, &Lden)) {
+      R->status = -4;
+      snprintf(R->err, 256, "Euler payload denominator exceeds 2^50");
+      free(A);
+      return R;
+    }
+  }
+  R->euler_denom = Lden;
   tet_out* O = (tet_out*)calloc(n_tets > 0 ? n_tets : 1, sizeof(tet_out));
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -674,16 +906,29 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
     if (do_clip) {
       to->pieces = (piece_t*)malloc(sizeof(piece_t) * (to->ncand > 0 ? to->ncand : 1));
       for (int32_t c = 0; c < to->ncand; ++c)
-        if (clip_piece(in, &tl, to->cand[c], &to->pieces[to->npieces], &to->st)) ++to->npieces;
+        if (clip_piece(in, &tl, to->cand[c], &to->pieces[to->npieces], &to->st,
+                       A ? A + 14 * t : NULL, Lden))
+          ++to->npieces;
     }
   }
   /* concatenate in tet order */
-  int64_t nc = 0, np = 0, ni = 0;
+  int64_t nc = 0, np = 0, ni = 0, nr = 0;
   for (int64_t a = 0; a < n_tets; ++a) {
     nc += O[a].ncand;
     np += O[a].npieces;
-    for (int32_t p = 0; p < O[a].npieces; ++p) ni += O[a].pieces[p].ninc;
+    for (int32_t p = 0; p < O[a].npieces; ++p) {
+      ni += O[a].pieces[p].ninc;
+      nr += O[a].pieces[p].nrpf;
+    }
   }
+  free(A);
+  R->n_rpf = nr;
+  R->piece_euler = (int64_t*)malloc(sizeof(int64_t) * (np ? np : 1));
+  R->rpf_off = (int32_t*)malloc(sizeof(int32_t) * (np + 1));
+  R->rpf_sphere = (int32_t*)malloc(sizeof(int32_t) * (nr ? nr : 1));
+  R->rpf_euler = (int64_t*)malloc(sizeof(int64_t) * (nr ? nr : 1));
+  R->rpf_off[0] = 0;
+  int64_t r0 = 0;
   R->n_cand = nc;
   R->n_pieces = np;
   R->n_inc = ni;
@@ -713,6 +958,15 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
       R->piece_facemask[p0] = pc->facemask;
       memcpy(R->inc_sphere + i0, pc->inc, sizeof(int32_t) * pc->ninc);
       i0 += pc->ninc;
+      R->piece_euler[p0] = pc->euler;
+      if (pc->nrpf) {
+        memcpy(R->rpf_sphere + r0, pc->rpf_j, sizeof(int32_t) * pc->nrpf);
+        memcpy(R->rpf_euler + r0, pc->rpf_e, sizeof(int64_t) * pc->nrpf);
+      }
+      r0 += pc->nrpf;
+      R->rpf_off[p0 + 1] = (int32_t)r0;
+      free(pc->rpf_j);
+      free(pc->rpf_e);
       ++p0;
       R->inc_off[p0] = (int32_t)i0;
       free(pc->inc);

@@ -222,3 +222,20 @@ def test_pruned_equals_allpairs_c3(ctx, ctx_pruned):
               "piece_facemask", "inc_off", "inc_sphere"):
         assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
     assert b["stats"]["pairs_tested"] < a["stats"]["pairs_tested"] / 20
+
+
+def test_c5_sampled(ctx_pruned):
+    """BASELINE.json configs[4] at full size (C5: ~4M tets, 50k spheres, high radius variance,
+    k_site tails of 1000+), pruned filter as bench.py --config C5 runs it: sampled tets compared
+    one by one with the oracle (Alg. 1 over all 50k spheres), partition on every tet."""
+    w = W.make_config("C5")
+    got = run_gpu(ctx_pruned, w)
+    rng = np.random.default_rng(5)
+    ids = np.sort(rng.choice(w.T, 64, replace=False)).astype(np.int32)
+    ref = oracle.rpd_workload(w, tet_ids=ids)
+    errs = compare_results(slice_tets(got, ids), ref, w.verts, w.tets, tet_ids=ids, rel=REL)
+    assert not errs, errs[:5]
+    vt = tet_volumes(w.verts, w.tets)
+    s = np.zeros(w.T)
+    np.add.at(s, piece_tet(got), got["piece_vol"])
+    assert np.max(np.abs(s - vt) / vt) < 1e-9

@@ -309,3 +309,91 @@ def test_partial_update_equals_full(small_shape):
     for k in same:
         assert np.array_equal(same[k], oracle.from_per_tet_lists(
             oracle.per_tet_lists(prev, w.T))[k])
+
+
+# ----------------------------------------------------------------------------- fractional Euler
+# "Fractional Euler Characteristic"
+
+
+def _mesh_euler(tets):
+    """V - E + F - T of a tet mesh, by counting its distinct simplices (plain definition)."""
+    Vs, Es, Fs = set(), set(), set()
+    for t in np.asarray(tets).tolist():
+        Vs |= set(t)
+        Es |= {frozenset((t[a], t[b])) for a in range(4) for b in range(a + 1, 4)}
+        Fs |= {frozenset(t[:k] + t[k + 1:]) for k in range(4)}
+    return len(Vs) - len(Es) + len(Fs) - len(tets)
+
+
+@pytest.mark.parametrize("make,expect", [
+    (lambda: W.unit_cube_6tets(), 1),
+    (lambda: W.kuhn_grid_mesh((2, 2, 2), 512, (0, 0, 0), morton=False), 1),
+    (lambda: (lambda w: (w.verts, w.tets))(
+        W.make_shape_workload("one", 700, 1, seed=2, cache=False)), 0)])
+def test_euler_single_sphere_is_mesh_euler(make, expect):
+    """the payloads 1/(tets sharing the element) make the per-tet sums add up
+    to the mesh's Euler characteristic; with one sphere every tet is one whole piece, so
+    Euler(RPC) = V - E + F - T.  The box with a through-hole (genus 1) gives 0: the paper's
+    Fig. 4(a) "CC = 1 but Euler = 0" for one sphere covering a torus-like solid."""
+    verts, tets = make()
+    sph = np.array([[0.5, 0.5, 0.5, 0.25]])
+    r = oracle.rpd(verts, tets, sph, np.zeros(2, np.int32), np.zeros(0, np.int32), euler=True)
+    rpc, rpf = oracle.euler_sums(r, 1, np.zeros(2, np.int32), np.zeros(0, np.int32))
+    assert _mesh_euler(tets) == expect
+    assert rpc[0] == expect and not rpf
+    assert len(r["piece_euler"]) == len(tets)
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(1), lambda: W.make_c1(3),
+                                  lambda: W.random_tiny(0, n_spheres=14, grid=2),
+                                  lambda: W.random_tiny(2, n_spheres=14, grid=2)])
+def test_euler_equals_explicit_extraction(make):
+    """on small inputs the fractional sums equal V - E + F - C of the restricted
+    elements extracted explicitly -- every piece of sphere i enumerated exactly (rational
+    vertices, no SoS) and glued across tets by coordinates -- for every RPC and every RPF."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    rpc, rpf = oracle.euler_sums(r, w.N, w.nbr_off, w.nbr_idx)
+    for i in range(w.N):
+        e_rpc, e_rpf, generic = X.explicit_euler(w.verts, w.tets, w.spheres, w.nbr_off,
+                                                 w.nbr_idx, i)
+        assert generic
+        assert rpc[i] == e_rpc, i
+        assert {j: v for (a, j), v in rpf.items() if a == i} == e_rpf, i
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0, degenerate=True),
+                                  lambda: W.make_c1(6, degenerate=True, big=True),
+                                  lambda: W.random_tiny(3, n_spheres=14, grid=2, coarse=True),
+                                  lambda: W.make_shape_workload("E", 1500, 120, seed=4,
+                                                                cache=False)])
+def test_euler_sums_are_integers(make):
+    """The fractional payloads of the elements shared between tets add up across the pieces
+    of one sphere (Eq. (1): 1/2 + 1/2 = 1), so every RPC and RPF sum is an integer, also on
+    degenerate inputs (symbolically perturbed complex); RPF(m_i, m_j) seen from m_i equals
+    the one seen from m_j when no exact-zero predicate occurred."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    rpc, rpf = oracle.euler_sums(r, w.N, w.nbr_off, w.nbr_idx)
+    assert all(x.denominator == 1 for x in rpc)
+    assert all(x.denominator == 1 for x in rpf.values())
+    if r["stats"]["n_zero_hits"] == 0:
+        for (i, j), v in rpf.items():
+            assert rpf.get((j, i)) == v, (i, j)
+    # pieces of a mesh whose spheres all have cells inside it are mostly balls (Euler 1)
+    assert sum(1 for x in rpc if x == 1) >= 0.5 * sum(1 for x in rpc if x != 0)
+
+
+def test_euler_partial_update_equals_full(small_shape):
+    """R11 with the Euler payloads: the partially updated pieces carry the same fractional
+    Euler characteristics as a full recompute."""
+    w = small_shape
+    prev = oracle.rpd_workload(w, euler=True)
+    n_old = w.N
+    for (sph, off, idx) in w.batches:
+        part, _ = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old, euler=True)
+        full = oracle.rpd(w.verts, w.tets, sph, off, idx, euler=True)
+        assert part["euler_denom"] == full["euler_denom"]
+        for k in ("piece_euler", "rpf_off", "rpf_sphere", "rpf_euler"):
+            assert np.array_equal(part[k], full[k]), k
+        prev, n_old = part, len(sph)
