@@ -13,6 +13,8 @@
  *                       face/neighbour incidences (§3.3, 488 §4.1.2)
  *   rpd_update_partial  partial update after appending M new spheres: only tets related to a
  *                       new sphere are re-filtered and re-clipped
+ *   rpd_set_euler /     fractional Euler characteristics of the restricted power cells and
+ *   rpd_get_euler       faces, collected on the fly by the clip (Sec. 4.1.2)
  *
  * Inputs are the paper's problem statement: tets with 4 ordered vertices,
  * medial spheres m = (theta, r) and the sphere neighbour lists k_site that the
@@ -148,6 +150,60 @@ rpd_status rpd_download_pieces(rpd_ctx* ctx, int32_t* piece_off, int32_t* piece_
 /* Copy the current candidate CSR to caller-owned arrays (host or device memory): cand_off [T+1],
  * cand_idx [n_cand].  Either pointer may be NULL. */
 rpd_status rpd_download_cands(rpd_ctx* ctx, int32_t* cand_off, int32_t* cand_idx);
+
+/* ---- Fractional Euler characteristics (Sec. 4.1.2)
+ *
+ * "such fractional Euler characteristics are inputted together with the mesh":
+ * every vertex / edge / face of the tet mesh carries 1/(number of tets sharing it) inside each
+ * tet, a tet carries 1.  While clipping, a new vertex inherits the payload of the tet simplex
+ * it lies on, a new edge that of the face it cuts, a new facet that of the cell; new elements
+ * are not re-divided.  Per piece and per radical facet the clip then sums
+ *   Euler(piece)     = sum_vertices - sum_edges + sum_facets - 1      (Eq. (1))
+ *   Euler(facet j)   = sum_{vertices on it} - sum_{edges on it} + 1
+ * over the symbolically perturbed (simple) polytope, and the library reduces them per sphere:
+ *   Euler(RPC(m_i))      = sum over the pieces of m_i
+ *   Euler(RPF(m_i, m_j)) = sum over their facets on the radical plane h_ij (seen from m_i).
+ * All values are EXACT rationals num / denom with denom = lcm of the sharing counts present
+ * (integer arithmetic: identical across kernels, launches and ranks); the per-sphere sums of
+ * a closed mesh are integers.
+ *
+ * rpd_set_euler: build the payloads of the ctx's tets (call after or before rpd_relations,
+ * before rpd_clip; stays on until switched off with tets_all = NULL, T_all = 0).
+ *   tets_all  [T_all][4] int32  the WHOLE mesh (sharing counts are global; a sharded rank
+ *                               passes every tet, not only its own)
+ *   V         host int64        vertex count, 0 < V < 2^21
+ *   local_ids [T_local] int32   global index of every ctx-local tet (the tets given to
+ *                               rpd_relations), or NULL when the ctx holds all tets in order
+ *                               (then T_local must equal T_all)
+ *   *denom    host out          the common denominator L (< 2^50)
+ * Errors: RPD_EINVAL (bad argument, vertex index out of range), RPD_EOVERFLOW (an element
+ * shared by more than 255 tets, or L >= 2^50), RPD_ENOMEM.  rpd_clip fails with RPD_EINVAL
+ * if the ctx's tet count differs from T_local. */
+rpd_status rpd_set_euler(rpd_ctx* ctx, const int32_t* tets_all, int64_t T_all, int64_t V,
+                         const int32_t* local_ids, int64_t T_local, int64_t* denom);
+
+/* Euler data of the current pieces (ctx-owned device arrays, valid until the next mutating
+ * call).  RPD_ESTATE unless rpd_set_euler preceded the last rpd_clip / rpd_update_partial. */
+typedef struct {
+  int64_t denom;               /* L: every value below is a numerator over L */
+  const int64_t* piece_euler;  /* [n_pieces] Euler of each piece (rpd_pieces order) */
+  const int32_t* rpf_off;      /* [n_pieces+1] radical facets of each piece ... */
+  const int32_t* rpf_sphere;   /* [n_rpf] ... their neighbour j, ascending */
+  const int64_t* rpf_euler;    /* [n_rpf] ... and the Euler of the facet */
+  const int64_t* rpc_sum;      /* [N] Euler(RPC(m_i)) x L over this ctx's tets */
+  const int64_t* rpf_sum;      /* [E] Euler(RPF(m_i, m_j)) x L at the CSR entry of j in row i,
+                                  rows sorted ascending by neighbour id (the input order when
+                                  the caller's rows are sorted) */
+  int64_t n_pieces, n_rpf, N, E;
+} rpd_euler;
+rpd_status rpd_get_euler(rpd_ctx* ctx, rpd_euler* out);
+
+/* Copy the Euler data to caller-owned arrays (host or device; any pointer may be NULL):
+ * piece_euler [n_pieces], rpf_off [n_pieces+1], rpf_sphere / rpf_euler [n_rpf],
+ * rpc_sum [N], rpf_sum [E].  A sharded job adds rpc_sum / rpf_sum over the ranks. */
+rpd_status rpd_download_euler(rpd_ctx* ctx, int64_t* piece_euler, int32_t* rpf_off,
+                              int32_t* rpf_sphere, int64_t* rpf_euler, int64_t* rpc_sum,
+                              int64_t* rpf_sum);
 
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */

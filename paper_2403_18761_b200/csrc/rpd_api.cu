@@ -166,7 +166,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
-                    &c->min_epoch};
+                    &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
+                    &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -184,6 +185,10 @@ void rpd_destroy(rpd_ctx* c) {
     x->fm.release();
     x->inc_off.release();
     x->inc.release();
+    x->eu.release();
+    x->rpf_off.release();
+    x->rpf_j.release();
+    x->rpf_e.release();
   }
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
@@ -415,6 +420,16 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(c->p_mask.ensure(sizeof(unsigned) * (cs.n_words > 0 ? cs.n_words : 1)), "alloc");
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
+  if (c->euler) {
+    if (c->eu_T != cs.n_tets && tet_ids == nullptr)
+      return fail(c, RPD_EINVAL, "Euler payloads were set for a different tet count");
+    const size_t nw = cs.n_words > 0 ? cs.n_words : 1;
+    CK(c->p_eu.ensure(sizeof(long long) * nn), "alloc");
+    CK(c->p_nrpf.ensure(sizeof(int32_t) * nn), "alloc");
+    CK(c->r_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
+    CK(c->p_rmask.ensure(sizeof(unsigned) * nw), "alloc");
+    CK(c->p_rval.ensure(sizeof(long long) * 32 * nw), "alloc");
+  }
   const int32_t* moff = cs.moff.as<int32_t>();
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
   CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
@@ -435,10 +450,11 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(launch_piece_scans(c, n, moff), "scan");
   tmark(c, "piece-scans");
   Readback* rb = (Readback*)c->pinned;
-  int64_t np = n, ni = 32 * (int64_t)cs.n_words;
+  int64_t np = n, ni = 32 * (int64_t)cs.n_words, nr = c->euler ? ni : 0;
   if (!deferred) {
     CK(readback(c, RbSpec{{c->p_scan.as<int32_t>() + n, c->i_scan.as<int32_t>() + n,
-                           c->p_over.as<int32_t>(), c->p_over2.as<int32_t>()},
+                           c->p_over.as<int32_t>(), c->p_over2.as<int32_t>(),
+                           c->euler ? c->r_scan.as<int32_t>() + n : nullptr},
                           c->stats.as<unsigned long long>(), nullptr}),
        "readback");
     CK(cudaStreamSynchronize(c->stream), "clip");
@@ -446,6 +462,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
       return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
     np = rb->i32[0];
     ni = rb->i32[1];
+    nr = rb->i32[4];
     absorb_clip_stats(c, rb, rb->i32[2]);
     if (getenv("RPD_DEBUG_STATS"))
       fprintf(stderr, "[rpd clip] pairs %lld overflow 16->32 %d 32->128 %d maxv %d maxp %d\n",
@@ -459,16 +476,25 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(ps.fm.ensure(npp), "alloc");
   CK(ps.inc_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
   CK(ps.inc.ensure(sizeof(int32_t) * (ni > 0 ? ni : 1)), "alloc");
+  if (c->euler) {
+    CK(ps.eu.ensure(sizeof(long long) * npp), "alloc");
+    CK(ps.rpf_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
+    CK(ps.rpf_j.ensure(sizeof(int32_t) * (nr > 0 ? nr : 1)), "alloc");
+    CK(ps.rpf_e.ensure(sizeof(long long) * (nr > 0 ? nr : 1)), "alloc");
+  }
   PieceDst d{ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.vol.as<double>(),
              ps.m1.as<double>(),  ps.fm.as<uint8_t>(),     ps.inc_off.as<int32_t>(),
-             ps.inc.as<int32_t>()};
+             ps.inc.as<int32_t>(), ps.eu.as<long long>(),  ps.rpf_off.as<int32_t>(),
+             ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>()};
   CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idx.as<int32_t>(), moff, d),
      "compact pieces");
   ps.n_tets = nt;
   ps.n_pieces = np;
   ps.n_inc = ni;
+  ps.n_rpf = nr;
   c->last.pairs_clipped += n;
   if (deferred) return RPD_OK;
+  if (c->euler) CK(launch_euler_sums(c, ps), "euler sums");
   if (c->profile) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
@@ -511,6 +537,7 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   c->have_rel = false;
   c->have_pieces = false;
+  c->eu_valid = false;
   const double* d_verts = nullptr;
   const int32_t* d_tets = nullptr;
   CK(resolve(c, verts, 3 * V, c->h_verts, &d_verts), "stage verts");
@@ -543,9 +570,11 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   CandSet& cs = c->cand[c->cur];
   c->last.clip_ms = 0.0;
+  c->eu_valid = false;
   rpd_status s = run_clip(c, cs, nullptr, c->pcs[c->cur]);
   if (s) return s;
   c->have_pieces = true;
+  c->eu_valid = c->euler != 0;
   c->last.n_pieces = c->pcs[c->cur].n_pieces;
   c->last.n_inc = c->pcs[c->cur].n_inc;
   return fill_pieces(c, out);
@@ -559,6 +588,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   if (!out || !dirty_tets || !n_dirty || M < 0 || (M > 0 && !new_ids))
     return fail(c, RPD_EINVAL, "rpd_update_partial: bad argument");
   if (!c->have_pieces) return fail(c, RPD_ESTATE, "rpd_update_partial before rpd_clip");
+  if (c->euler && !c->eu_valid)
+    return fail(c, RPD_ESTATE, "Euler mode: the current pieces were clipped without payloads");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   const int64_t N_old = c->st.N, T = c->st.T;
   if (N_new != N_old + M)
@@ -663,8 +694,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   PieceSet& pd = c->pcs_d;
   CandSet& cn = c->cand[nxt];
   PieceSet& pn = c->pcs[nxt];
-  CK(c->m_cnt.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1)), "alloc");
-  CK(c->m_off.ensure(sizeof(int32_t) * 2 * (T + 1)), "alloc");
+  CK(c->m_cnt.ensure(sizeof(int32_t) * 5 * (T > 0 ? T : 1)), "alloc");
+  CK(c->m_off.ensure(sizeof(int32_t) * 3 * (T + 1)), "alloc");
   CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
   CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
   cn.n = co.n + cd.n;
@@ -680,13 +711,21 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(pn.fm.ensure(npn), "alloc");
   CK(pn.inc_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
   CK(pn.inc.ensure(sizeof(int32_t) * (pn.n_inc > 0 ? pn.n_inc : 1)), "alloc");
+  if (c->euler) {
+    pn.n_rpf = po.n_rpf + pd.n_rpf;
+    CK(pn.eu.ensure(sizeof(long long) * npn), "alloc");
+    CK(pn.rpf_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
+    CK(pn.rpf_j.ensure(sizeof(int32_t) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
+    CK(pn.rpf_e.ensure(sizeof(long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
+  }
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
   tmark(c, "merge-counts");
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 1), "merge copy");
   const int32_t* m_off = c->m_off.as<int32_t>();
   CK(readback(c, RbSpec{{cn.off.as<int32_t>() + T, pn.off.as<int32_t>() + T, m_off + T,
                          m_off + (T + 1) + T, c->p_over.as<int32_t>(),
-                         c->p_scan.as<int32_t>() + cd.n, c->i_scan.as<int32_t>() + cd.n},
+                         c->p_scan.as<int32_t>() + cd.n, c->i_scan.as<int32_t>() + cd.n,
+                         c->euler ? m_off + 2 * (T + 1) + T : nullptr},
                         c->stats.as<unsigned long long>(), nullptr}),
      "readback");
   CK(cudaStreamSynchronize(c->stream), "partial update");
@@ -707,8 +746,14 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   cn.n_words = rb->i32[3];
   pn.n_pieces = rb->i32[1];
   pn.n_inc = rb->i32[2];
+  pn.n_rpf = rb->i32[7];
   pn.n_tets = T;
+  if (c->euler) {
+    CK(launch_euler_sums(c, pn), "euler sums");
+    pd.n_rpf = 0;
+  }
   c->cur = nxt;
+  c->eu_valid = c->euler != 0;
   c->n_dirty = nd;
   c->last.n_dirty = nd;
   c->last.n_cand = cn.n;
@@ -738,6 +783,85 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
   CK(cp(piece_facemask, ps.fm.p, np), "download");
   CK(cp(inc_off, ps.inc_off.p, sizeof(int32_t) * (np + 1)), "download");
   CK(cp(inc_sphere, ps.inc.p, sizeof(int32_t) * ni), "download");
+  CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
+                         const int32_t* local_ids, int64_t T_local, int64_t* denom) {
+  if (!c) return RPD_EINVAL;
+  c->eu_valid = false;
+  if (!tets_all && T_all == 0) {  // switch off
+    c->euler = 0;
+    if (denom) *denom = 0;
+    return RPD_OK;
+  }
+  if (!tets_all || T_all < 0 || T_all > 0x7fffffff || V <= 0 || V >= (1ll << 21) ||
+      T_local < 0 || T_local > 0x7fffffff || (!local_ids && T_local != T_all) || !denom)
+    return fail(c, RPD_EINVAL, "rpd_set_euler: bad argument (V must be in (0, 2^21))");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int32_t *d_tets = nullptr, *d_ids = nullptr;
+  CK(resolve(c, tets_all, 4 * T_all, c->h_eut, &d_tets), "stage tets");
+  CK(resolve(c, local_ids, local_ids ? T_local : 0, c->h_euid, &d_ids), "stage ids");
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  CK(c->eu_A.ensure(sizeof(long long) * 512), "alloc");
+  CK(launch_euler_setup(c, d_tets, T_all, V, d_ids, T_local), "euler setup");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{}, reinterpret_cast<const unsigned long long*>(c->eu_A.as<long long>() + 256),
+                        c->errw.as<int>()}),
+     "readback");
+  CK(cudaStreamSynchronize(c->stream), "euler setup");
+  c->eu_tab.release();  // (hash tables: scratch of the setup only)
+  if (rb->err[0] != 0) {
+    if (rb->err[1] == 200)
+      return fail(c, RPD_EOVERFLOW, "Euler mode: a mesh element is shared by more than 255 tets");
+    if (rb->err[0] == RPD_ENOMEM) return fail(c, RPD_ENOMEM, "Euler mode: hash table full");
+    return check_err(c, rb);
+  }
+  const long long L = (long long)rb->u64[0];
+  if (L <= 0) return fail(c, RPD_EOVERFLOW, "Euler payload denominator exceeds 2^50");
+  c->euler = 1;
+  c->eu_L = L;
+  c->eu_T = T_local;
+  *denom = L;
+  return RPD_OK;
+}
+
+rpd_status rpd_get_euler(rpd_ctx* c, rpd_euler* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_get_euler: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no Euler data (rpd_set_euler, then rpd_clip)");
+  const PieceSet& ps = c->pcs[c->cur];
+  out->denom = c->eu_L;
+  out->piece_euler = ps.eu.as<int64_t>();
+  out->rpf_off = ps.rpf_off.as<int32_t>();
+  out->rpf_sphere = ps.rpf_j.as<int32_t>();
+  out->rpf_euler = ps.rpf_e.as<int64_t>();
+  out->rpc_sum = c->eu_sum.as<int64_t>();
+  out->rpf_sum = c->eu_sum.as<int64_t>() + c->st.N;
+  out->n_pieces = ps.n_pieces;
+  out->n_rpf = ps.n_rpf;
+  out->N = c->st.N;
+  out->E = c->st.E;
+  return RPD_OK;
+}
+
+rpd_status rpd_download_euler(rpd_ctx* c, int64_t* piece_euler, int32_t* rpf_off,
+                              int32_t* rpf_sphere, int64_t* rpf_euler, int64_t* rpc_sum,
+                              int64_t* rpf_sum) {
+  rpd_euler e;
+  rpd_status s = rpd_get_euler(c, &e);
+  if (s) return s;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+  };
+  CK(cp(piece_euler, e.piece_euler, sizeof(int64_t) * e.n_pieces), "download");
+  CK(cp(rpf_off, e.rpf_off, sizeof(int32_t) * (e.n_pieces + 1)), "download");
+  CK(cp(rpf_sphere, e.rpf_sphere, sizeof(int32_t) * e.n_rpf), "download");
+  CK(cp(rpf_euler, e.rpf_euler, sizeof(int64_t) * e.n_rpf), "download");
+  CK(cp(rpc_sum, e.rpc_sum, sizeof(int64_t) * e.N), "download");
+  CK(cp(rpf_sum, e.rpf_sum, sizeof(int64_t) * e.E), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }

@@ -78,6 +78,7 @@ struct alignas(16) WarpState {  // (16-byte aligned: double2 accesses)
   int eidx[MAXP];          // CSR entry of a radical plane, -1 for faces
   int tw[MAXP];            // twin[eidx] (next coincident CSR entry of the row), -1 if none
   int ref[MAXP];           // reference vertex of every facet (fan apex)
+  long long pay[16];       // Euler payload numerators of the tet's elements (rpd_euler.cu)
 };
 
 // oriented dual triangles of the 4 tet corners (corner k = faces != k); this orientation
@@ -340,6 +341,13 @@ __device__ unsigned long long g_phase[8];
   } while (0)
 #endif
 
+// fractional Euler characteristics: carrier of a piece element from the
+// tet faces among its planes (bit k = tet face k) -> index into WarpState::pay: 14 = inside
+// the tet (payload 1 = L), 10 + k = face k, 4 + e = tet edge e (corner pairs 01 02 03 12 13 23)
+// when two faces meet, corner c when three do
+__constant__ unsigned char EU_BIDX[16] = {14, 10, 11, 9, 12, 8, 6, 3, 13, 7, 5, 2, 4, 1, 0, 14};
+__device__ __forceinline__ unsigned eu_pm(int p) { return p < 4 ? 1u << p : 0u; }
+
 struct PairOut {
   double* vol;
   double* m1;
@@ -349,9 +357,18 @@ struct PairOut {
   const int32_t* mask_off;
   int32_t* over_list;  // pairs that overflowed (re-run by the next wider kernel)
   int32_t* over_count;
+  // Euler (eu_rec == nullptr: off)
+  const uint4* eu_rec;      // per ctx-local tet: the 14 sharing counts of its elements
+  const long long* eu_A;    // A[n] = L / n
+  long long eu_L;           // common denominator
+  long long* eu_piece;      // per pair: Euler of the piece x L
+  unsigned* rmask;          // per pair: SoS radical facets (bits over N(i), incmask layout)
+  long long* rval;          // per (pair, row position): Euler of that facet x L
 };
 
-template <int GW, int VPL>
+// EU: also the fractional Euler characteristics (a separate instantiation, so that the plain
+// clip keeps its register allocation)
+template <int GW, int VPL, bool EU>
 __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64),
                                   VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_MINB : (VPL <= 2 ? 2 : 1)) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
@@ -386,7 +403,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
   // software pipeline of the pair's index loads: level 1 (pair -> tet, sphere) is fetched one
   // pair ahead at the top of the loop, level 2 (tet corners, CSR row bounds) once the plane
   // loop is done, so the dependent global loads overlap the previous pair's work
-  int64_t pf_p = 0;
+  int64_t pf_p = 0, pf_t = 0;
   int pf_a = 0, pf_i = 0, pf_e0 = 0, pf_e1 = 0, pf_mo = 0;
   constexpr int NTX = (12 + GW - 1) / GW;  // tet corner coordinates per lane
   double pf_tx[NTX];
@@ -398,6 +415,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
   };
   auto fetch2 = [&]() {
     const int64_t t = tet_ids ? (int64_t)tet_ids[pf_a] : (int64_t)pf_a;
+    pf_t = t;
 #pragma unroll
     for (int q = 0; q < NTX; ++q)
       if (lane + GW * q < 12) pf_tx[q] = __ldg(tx + (lane + GW * q) * T + t);
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
   int64_t nxt = n_pairs;
   for (int64_t pi = first; pi < n_pairs; pi = nxt) {
     nxt = next_of(pi);
-    const int64_t p = pf_p;
+    const int64_t p = pf_p, t_cur = pf_t;
     const int e0 = pf_e0, e1 = pf_e1, mo = pf_mo;
     const int nwp = (e1 - e0 + 31) >> 5;  // incidence-mask words of the pair
 #pragma unroll
@@ -872,6 +890,79 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     __syncwarp(FULL);
     PHASE_MARK(4);
 
+    // ---- fractional Euler characteristics (Eq. (1)) of the SoS polytope:
+    // Euler(piece) = sum_v pay(v) - sum_e pay(e) + sum_f pay(f) - 1 and, per radical facet f,
+    // Euler(f) = sum_{v on f} pay(v) - sum_{e on f} pay(e) + pay(f).  Every vertex is simple
+    // (3 planes), so each of its 3 plane pairs is an edge counted at both of its ends: edges
+    // enter as halves, accumulated doubled (exact integers over L).  The payload of an element
+    // is inherited from the smallest tet simplex holding it: new vertices from
+    // the edge they cut, new edges from the face they cut, new facets from the cell.
+    if constexpr (EU) {
+      long long* acc = reinterpret_cast<long long*>(S.val);  // per plane: doubled facet sums
+      {
+        const uint4 rc = __ldg(out.eu_rec + t_cur);
+        if (lane < 14) {
+          const unsigned w = lane < 4 ? rc.x : (lane < 8 ? rc.y : (lane < 12 ? rc.z : rc.w));
+          S.pay[lane] = __ldg(out.eu_A + ((w >> (8 * (lane & 3))) & 0xffu));
+        } else if (lane == 14) {
+          S.pay[14] = out.eu_L;
+        }
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (GW * k + lane < np) acc[GW * k + lane] = 0;
+      }
+      __syncwarp(FULL);
+      long long c2 = 0, cf = 0;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        if (!((live[k] >> lane) & 1u)) continue;
+        const int a = tri_at(mytri[k], 0), b = tri_at(mytri[k], 1), cc = tri_at(mytri[k], 2);
+        const unsigned ma = eu_pm(a), mb = eu_pm(b), mc = eu_pm(cc);
+        const long long pv2 = 2 * S.pay[EU_BIDX[ma | mb | mc]];
+        const long long pab = S.pay[EU_BIDX[ma | mb]], pbc = S.pay[EU_BIDX[mb | mc]],
+                        pca = S.pay[EU_BIDX[mc | ma]];
+        c2 += pv2 - pab - pbc - pca;
+        if (a >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(acc + a),
+                              (unsigned long long)(pv2 - pab - pca));
+        if (b >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(acc + b),
+                              (unsigned long long)(pv2 - pab - pbc));
+        if (cc >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(acc + cc),
+                               (unsigned long long)(pv2 - pbc - pca));
+      }
+      __syncwarp(FULL);
+      unsigned* rw = out.rmask + mo;
+      long long* rv = out.rval + 32 * (int64_t)mo;
+      if (!one_word) {
+        for (int w = lane; w < nwp; w += GW) rw[w] = 0u;
+        __syncwarp(FULL);
+      }
+      unsigned rbits = 0u;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int pl = GW * k + lane;
+        if (pl < np && facets_all.has(pl)) {
+          cf += S.pay[EU_BIDX[eu_pm(pl)]];
+          if (pl >= 4) {  // radical facet: its part of the RPF between m_i and m_j
+            const int pos = S.eidx[pl] - e0;
+            rv[pos] = acc[pl] / 2 + out.eu_L;
+            if (one_word) rbits |= 1u << pos;
+            else atomicOr(rw + (pos >> 5), 1u << (pos & 31));
+          }
+        }
+      }
+#pragma unroll
+      for (int o = GW / 2; o > 0; o >>= 1) {
+        c2 += __shfl_xor_sync(FULL, c2, o, GW);
+        cf += __shfl_xor_sync(FULL, cf, o, GW);
+      }
+      if (one_word) {
+        const unsigned w = __reduce_or_sync(FULL, rbits);
+        if (lane == 0) rw[0] = w;
+      }
+      if (lane == 0) out.eu_piece[p] = c2 / 2 + cf - out.eu_L;
+      __syncwarp(FULL);
+    }
+
     // ---- geometry: vertex coordinates relative to V0 (lattice units); facet fan apex =
     // lowest vertex of the facet
 #pragma unroll
@@ -983,16 +1074,31 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
 __global__ void k_count_inc(int64_t n_pairs, const uint8_t* __restrict__ flag,
                             const int32_t* __restrict__ mask_off,
                             const unsigned* __restrict__ mask, int32_t* __restrict__ ninc,
-                            int32_t* __restrict__ f01) {
+                            int32_t* __restrict__ f01, const unsigned* __restrict__ rmask,
+                            int32_t* __restrict__ nrpf) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
-  int n = 0;
+  int n = 0, r = 0;
   const bool ne = flag[p] == 1;
   if (ne)
-    for (int w = mask_off[p]; w < mask_off[p + 1]; ++w) n += __popc(mask[w]);
+    for (int w = mask_off[p]; w < mask_off[p + 1]; ++w) {
+      n += __popc(mask[w]);
+      if (rmask) r += __popc(rmask[w]);
+    }
   ninc[p] = n;
   f01[p] = ne;
+  if (rmask) nrpf[p] = r;
 }
+
+struct EuCompact {
+  const unsigned* rmask;     // nullptr: Euler off
+  const long long* rval;
+  const long long* p_eu;
+  const int32_t* rscan;
+  long long* piece;
+  int32_t *rpf_off, *rpf_j;
+  long long* rpf_e;
+};
 
 __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ cand_idx,
                                  const int32_t* __restrict__ nbr_off,
@@ -1004,10 +1110,14 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
                                  const unsigned* __restrict__ mask,
                                  int32_t* __restrict__ piece_sphere, double* __restrict__ piece_vol,
                                  double* __restrict__ piece_m1, uint8_t* __restrict__ piece_fm,
-                                 int32_t* __restrict__ inc_off, int32_t* __restrict__ inc_sphere) {
+                                 int32_t* __restrict__ inc_off, int32_t* __restrict__ inc_sphere,
+                                 EuCompact eu) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
-  if (p == n_pairs - 1) inc_off[pscan[n_pairs]] = iscan[n_pairs];
+  if (p == n_pairs - 1) {
+    inc_off[pscan[n_pairs]] = iscan[n_pairs];
+    if (eu.rmask) eu.rpf_off[pscan[n_pairs]] = eu.rscan[n_pairs];
+  }
   if (flag[p] != 1) return;
   const int q = pscan[p];
   const int i = cand_idx[p];
@@ -1027,6 +1137,22 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
       int b = __ffs(m) - 1;
       m &= m - 1;
       inc_sphere[o++] = nbr_idx[e0 + 32 * (w - w0) + b];
+    }
+  }
+  if (eu.rmask) {  // Euler: the piece's value and its radical facets, ascending neighbour id
+    eu.piece[q] = eu.p_eu[p];
+    int r = eu.rscan[p];
+    eu.rpf_off[q] = r;
+    for (int w = w0; w < mask_off[p + 1]; ++w) {
+      unsigned m = eu.rmask[w];
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int pos = 32 * (w - w0) + b;
+        eu.rpf_j[r] = nbr_idx[e0 + pos];
+        eu.rpf_e[r] = eu.rval[32 * (int64_t)w0 + pos];
+        ++r;
+      }
     }
   }
 }
@@ -1055,7 +1181,7 @@ void clip_phase_dump() {
 #endif
 }
 
-template <int GW, int VPL>
+template <int GW, int VPL, bool EU>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
@@ -1067,11 +1193,11 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   // cost microseconds per launch)
   static int occ = 0;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL>,
+    cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL, EU>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e) return e;
     int o = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_clip<GW, VPL>, THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_clip<GW, VPL, EU>, THREADS, smem);
     occ = o < 1 ? 1 : o;
   }
   const int sms = c->sms;
@@ -1081,8 +1207,10 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
-            over ? over + 1 : nullptr, over};
-  k_clip<GW, VPL><<<(unsigned)grid, THREADS, smem, c->stream>>>(
+            over ? over + 1 : nullptr, over,
+            c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
+            c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>()};
+  k_clip<GW, VPL, EU><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
       c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>(),
@@ -1093,43 +1221,61 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
 
 // fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
 // or the widest kernel over all pairs when `wide`
+template <bool EU>
+static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
+                                  const int32_t* tet_ids, const int32_t* cand_idx,
+                                  const int32_t* moff, int wide) {
+  if (wide)
+    return launch_clip_t<32, 4, EU>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff,
+                                    nullptr, nullptr);
+  cudaError_t e = c->p_dyn.ensure(sizeof(int));
+  if (e) return e;
+  if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
+  return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, EU>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                      cand_idx, moff, c->p_over.as<int32_t>(),
+                                                      nullptr, c->p_dyn.as<int>());
+}
+
+// fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
+// or the widest kernel over all pairs when `wide`
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
                         int wide) {
   if (n_pairs == 0) return cudaSuccess;
-  if (wide)
-    return launch_clip_t<32, 4>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, nullptr,
-                                nullptr);
-  cudaError_t e = c->p_dyn.ensure(sizeof(int));
-  if (e) return e;
-  if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
-  return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                  cand_idx, moff, c->p_over.as<int32_t>(),
-                                                  nullptr, c->p_dyn.as<int>());
+  return c->euler ? launch_clip_eu<true>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide)
+                  : launch_clip_eu<false>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide);
 }
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
 // 64-slot kernel <32, RPD_CLIP_MID_VPL = 2>; its own overflows (p_over2) by the 128-slot <32, 4>
+template <bool EU>
+static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
+                                      const int32_t* cand_idx, const int32_t* moff) {
+  cudaError_t e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
+      c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff,
+      c->p_over2.as<int32_t>(), c->p_over.as<int32_t>());
+  if (e) return e;
+  return launch_clip_t<32, 4, EU>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
+                                  cand_idx, moff, nullptr, c->p_over2.as<int32_t>());
+}
+
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
-  cudaError_t e = launch_clip_t<32, RPD_CLIP_MID_VPL>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet,
-                                       tet_ids, cand_idx, moff, c->p_over2.as<int32_t>(),
-                                       c->p_over.as<int32_t>());
-  if (e) return e;
-  return launch_clip_t<32, 4>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
-                              cand_idx, moff, nullptr, c->p_over2.as<int32_t>());
+  return c->euler ? launch_overflow_eu<true>(c, pair_tet, tet_ids, cand_idx, moff)
+                  : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff);
 }
 
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {
   if (n_pairs > 0) {
     k_count_inc<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, c->p_flag.as<uint8_t>(), moff, c->p_mask.as<unsigned>(),
-        c->p_ninc.as<int32_t>(), c->p_f01.as<int32_t>());
+        c->p_ninc.as<int32_t>(), c->p_f01.as<int32_t>(),
+        c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_nrpf.as<int32_t>());
     ++c->launches;
   }
-  const int32_t* in[2] = {c->p_f01.as<int32_t>(), c->p_ninc.as<int32_t>()};
-  int32_t* out[2] = {c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>()};
-  return launch_scan_i32_multi(c, in, out, 2, n_pairs);
+  const int32_t* in[3] = {c->p_f01.as<int32_t>(), c->p_ninc.as<int32_t>(), c->p_nrpf.as<int32_t>()};
+  int32_t* out[3] = {c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(), c->r_scan.as<int32_t>()};
+  return launch_scan_i32_multi(c, in, out, c->euler ? 3 : 2, n_pairs);
 }
 
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
@@ -1141,10 +1287,14 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
         c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(),
         c->p_vol.as<double>(), c->p_m1.as<double>(), c->p_fm.as<uint8_t>(),
         moff, c->p_mask.as<unsigned>(), d.sphere, d.vol, d.m1, d.fm,
-        d.inc_off, d.inc);
+        d.inc_off, d.inc,
+        EuCompact{c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_rval.as<long long>(),
+                  c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
+                  d.rpf_e});
     ++c->launches;
   } else {
     cudaMemsetAsync(d.inc_off, 0, sizeof(int32_t), c->stream);
+    if (c->euler) cudaMemsetAsync(d.rpf_off, 0, sizeof(int32_t), c->stream);
   }
   k_piece_off<<<nblk(n_tets + 1, 256), 256, 0, c->stream>>>(n_tets, cand_off,
                                                           c->p_scan.as<int32_t>(), d.off);

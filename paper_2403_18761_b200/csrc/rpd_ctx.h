@@ -97,7 +97,9 @@ struct CandSet {
 // piece CSR over a list of tets
 struct PieceSet {
   DevBuf off, sphere, vol, m1, fm, inc_off, inc;
-  int64_t n_tets = 0, n_pieces = 0, n_inc = 0;
+  // fractional Euler characteristics (Euler mode): per piece, and per radical SoS facet
+  DevBuf eu, rpf_off, rpf_j, rpf_e;
+  int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;
 };
 }  // namespace rpd
 
@@ -159,6 +161,17 @@ struct rpd_ctx {
   void* pinned = nullptr;      // small mapped pinned host buffer for scalar readbacks
   void* pinned_dev = nullptr;  // its device-side address
   int clip_wide = 0;           // testing: run every pair through the wide kernel
+
+  // fractional Euler characteristics (rpd_euler.cu; rpd_set_euler)
+  int euler = 0;               // payloads set for the current tets
+  bool eu_valid = false;       // the current pieces carry Euler data
+  rpd::DevBuf h_eut, h_euid;   // host-input staging of rpd_set_euler
+  int64_t eu_L = 0, eu_T = 0;  // denominator; ctx-local tet count the payloads were built for
+  rpd::DevBuf eu_tab;          // scratch hash tables of the payload setup
+  rpd::DevBuf eu_rec;          // uint4 per local tet: sharing counts of its 14 elements
+  rpd::DevBuf eu_A;            // int64 [256] L / n, then L, then the counts-present bitmap
+  rpd::DevBuf eu_sum;          // int64 [N + E + 1]: per-sphere RPC, per-CSR-entry RPF, misses
+  rpd::DevBuf p_eu, p_rmask, p_rval, p_nrpf, r_scan;  // per-pair clip outputs
 };
 
 namespace rpd {
@@ -204,6 +217,10 @@ struct PieceDst {
   uint8_t* fm;
   int32_t* inc_off;  // [n_pieces+1]
   int32_t* inc;
+  long long* eu;      // Euler mode: [n_pieces], rpf CSR [n_pieces+1] / [n_rpf]
+  int32_t* rpf_off;
+  int32_t* rpf_j;
+  long long* rpf_e;
 };
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
@@ -214,5 +231,9 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase);
+// fractional Euler characteristics (rpd_euler.cu)
+cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
+                               const int32_t* local_ids, int64_t T_local);
+cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps);
 
 }  // namespace rpd

@@ -86,6 +86,10 @@ struct MergeSrc {
   const int32_t *p_off, *p_sphere, *p_inc_off, *p_inc;
   const double *p_vol, *p_m1;
   const uint8_t* p_fm;
+  // Euler mode (p_eu == nullptr: off): per-piece value and the radical-facet CSR
+  const long long* p_eu;
+  const int32_t *p_rpf_off, *p_rpf_j;
+  const long long* p_rpf_e;
 };
 
 __device__ inline MergeSrc pick(int d, const MergeSrc& o, const MergeSrc& n) {
@@ -106,6 +110,7 @@ __global__ void k_merge_counts(int64_t T, const int32_t* __restrict__ dpos, Merg
   cnt[T + t] = p1 - p0;
   cnt[2 * T + t] = s.p_inc_off[p1] - s.p_inc_off[p0];
   cnt[3 * T + t] = s.c_moff[c1] - s.c_moff[c0];
+  if (s.p_eu) cnt[4 * T + t] = s.p_rpf_off[p1] - s.p_rpf_off[p0];
 }
 
 struct MergeDst {
@@ -113,6 +118,10 @@ struct MergeDst {
   int32_t *c_idx, *pair_tet, *c_moff, *p_sphere, *p_inc_off, *p_inc;
   double *p_vol, *p_m1;
   uint8_t* p_fm;
+  const int32_t* r_tet;  // Euler mode: scan of the per-tet radical-facet counts
+  long long* p_eu;
+  int32_t *p_rpf_off, *p_rpf_j;
+  long long* p_rpf_e;
 };
 
 constexpr int MT = 256;  // tets per merge tile (one block)
@@ -158,6 +167,8 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
                                                     MergeSrc o, MergeSrc n, MergeDst D) {
   __shared__ int s_nc[MT + 1], s_np[MT + 1], s_ni[MT + 1];
   __shared__ int s_sc[MT], s_sp[MT], s_si[MT], s_nw[MT], s_sw[MT];
+  __shared__ int s_nr[MT + 1], s_sr[MT];
+  const bool eu = D.p_eu != nullptr;
   __shared__ unsigned char s_dirty[MT];
   const int64_t t0 = (int64_t)blockIdx.x * MT;
   const int nt = (int)min((int64_t)MT, T - t0);
@@ -166,6 +177,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
     s_nc[l] = D.c_off[t];
     s_np[l] = D.p_off[t];
     s_ni[l] = D.i_tet[t];
+    if (eu) s_nr[l] = D.r_tet[t];
     if (l < nt) {
       const int d = dpos[t];
       const MergeSrc& s = d >= 0 ? n : o;
@@ -177,6 +189,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       s_si[l] = s.p_inc_off[p0];
       s_nw[l] = D.w_tet[t];
       s_sw[l] = s.c_moff[c0];
+      if (eu) s_sr[l] = s.p_rpf_off[p0];
     }
   }
   // a tile without dirty tets is one contiguous range of the old set in every array, moved
@@ -198,9 +211,19 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
     tile_copy(D.p_inc_off + p_dst, o.p_inc_off + p_src, npc, [=](int32_t x) { return x + ishift; });
     tile_copy(D.p_m1 + 3 * (int64_t)p_dst, o.p_m1 + 3 * (int64_t)p_src, 3 * npc, same);
     tile_copy(D.p_inc + i_dst, o.p_inc + i_src, ni, same);
+    if (eu) {
+      const int nr = s_nr[nt] - s_nr[0], r_src = s_sr[0], r_dst = s_nr[0];
+      const int rshift = s_nr[0] - s_sr[0];
+      tile_copy(D.p_eu + p_dst, o.p_eu + p_src, npc, same);
+      tile_copy(D.p_rpf_off + p_dst, o.p_rpf_off + p_src, npc,
+                [=](int32_t x) { return x + rshift; });
+      tile_copy(D.p_rpf_j + r_dst, o.p_rpf_j + r_src, nr, same);
+      tile_copy(D.p_rpf_e + r_dst, o.p_rpf_e + r_src, nr, same);
+    }
     if (t0 + nt == T && threadIdx.x == 0) {
       D.c_moff[s_nc[nt]] = D.w_tet[T];
       D.p_inc_off[s_np[nt]] = s_ni[nt];
+      if (eu) D.p_rpf_off[s_np[nt]] = s_nr[nt];
     }
     return;
   }
@@ -225,7 +248,20 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
     D.p_m1[3 * (int64_t)q + 2] = s.p_m1[3 * (int64_t)sp + 2];
     D.p_fm[q] = s.p_fm[sp];
     D.p_inc_off[q] = s_ni[l] + (s.p_inc_off[sp] - s_si[l]);
+    if (eu) {
+      D.p_eu[q] = s.p_eu[sp];
+      D.p_rpf_off[q] = s_nr[l] + (s.p_rpf_off[sp] - s_sr[l]);
+    }
   }
+  // radical facets of the pieces (Euler mode)
+  if (eu)
+    for (int r = s_nr[0] + threadIdx.x; r < s_nr[nt]; r += blockDim.x) {
+      const int l = tile_seg(s_nr, nt, r);
+      const MergeSrc& s = s_dirty[l] ? n : o;
+      const int src = s_sr[l] + (r - s_nr[l]);
+      D.p_rpf_j[r] = s.p_rpf_j[src];
+      D.p_rpf_e[r] = s.p_rpf_e[src];
+    }
   // incidences (a tet's incidences are contiguous in its source set)
   for (int r = s_ni[0] + threadIdx.x; r < s_ni[nt]; r += blockDim.x) {
     const int l = tile_seg(s_ni, nt, r);
@@ -235,15 +271,18 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
   if (t0 + nt == T && threadIdx.x == 0) {  // terminal entries
     D.c_moff[s_nc[nt]] = D.w_tet[T];
     D.p_inc_off[s_np[nt]] = s_ni[nt];
+    if (eu) D.p_rpf_off[s_np[nt]] = s_nr[nt];
   }
 }
 
-static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
+static MergeSrc src_of(const CandSet& cs, const PieceSet& ps, bool eu) {
   return MergeSrc{cs.off.as<int32_t>(),     cs.idx.as<int32_t>(),     cs.moff.as<int32_t>(),
                   cs.pair_tet.as<int32_t>(),
                   ps.off.as<int32_t>(),     ps.sphere.as<int32_t>(),  ps.inc_off.as<int32_t>(),
                   ps.inc.as<int32_t>(),     ps.vol.as<double>(),      ps.m1.as<double>(),
-                  ps.fm.as<uint8_t>()};
+                  ps.fm.as<uint8_t>(),
+                  eu ? ps.eu.as<long long>() : nullptr, ps.rpf_off.as<int32_t>(),
+                  ps.rpf_j.as<int32_t>(),   ps.rpf_e.as<long long>()};
 }
 
 // phase 0: per-tet counts and their scans (new cand offsets -> cn.off, new piece offsets ->
@@ -254,9 +293,11 @@ static MergeSrc src_of(const CandSet& cs, const PieceSet& ps) {
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase) {
-  MergeSrc o = src_of(co, po), n = src_of(cd, pd);
+  const bool eu = c->euler != 0;
+  MergeSrc o = src_of(co, po, eu), n = src_of(cd, pd, eu);
   int32_t* m_off = c->m_off.as<int32_t>();
   int32_t* w_off = m_off + (T + 1);
+  int32_t* r_off = m_off + 2 * (T + 1);
   if (phase == 0) {
     if (T > 0) {
       k_merge_counts<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n,
@@ -264,15 +305,17 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
       ++c->launches;
     }
     const int32_t* cnt = c->m_cnt.as<int32_t>();
-    const int32_t* in[4] = {cnt, cnt + T, cnt + 2 * T, cnt + 3 * T};
-    int32_t* out[4] = {cn.off.as<int32_t>(), pn.off.as<int32_t>(), m_off, w_off};
-    return launch_scan_i32_multi(c, in, out, 4, T);
+    const int32_t* in[5] = {cnt, cnt + T, cnt + 2 * T, cnt + 3 * T, cnt + 4 * T};
+    int32_t* out[5] = {cn.off.as<int32_t>(), pn.off.as<int32_t>(), m_off, w_off, r_off};
+    return launch_scan_i32_multi(c, in, out, eu ? 5 : 4, T);
   }
   MergeDst D{cn.off.as<int32_t>(),     pn.off.as<int32_t>(),      m_off,
              w_off,                    cn.idx.as<int32_t>(),      cn.pair_tet.as<int32_t>(),
              cn.moff.as<int32_t>(),    pn.sphere.as<int32_t>(),   pn.inc_off.as<int32_t>(),
              pn.inc.as<int32_t>(),     pn.vol.as<double>(),       pn.m1.as<double>(),
-             pn.fm.as<uint8_t>()};
+             pn.fm.as<uint8_t>(),      r_off,
+             eu ? pn.eu.as<long long>() : nullptr, pn.rpf_off.as<int32_t>(),
+             pn.rpf_j.as<int32_t>(),   pn.rpf_e.as<long long>()};
   if (T > 0) {
     k_merge_copy<<<nblk(T, MT), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
     ++c->launches;

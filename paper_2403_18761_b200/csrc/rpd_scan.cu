@@ -1,6 +1,6 @@
 // rpd_scan.cu -- exclusive prefix sums used by the compaction steps:
 // out[k] = sum_{m<k} in[m] for k in [0, n], out[n] = total.  One launch per scan, or per group of up to
-// four equal-length scans (decoupled look-back over 4096-element tiles).  Deterministic (integer).
+// five equal-length scans (decoupled look-back over 4096-element tiles).  Deterministic (integer).
 #include "rpd_ctx.h"
 
 namespace rpd {
@@ -53,12 +53,12 @@ __device__ __forceinline__ unsigned long long st_pack(unsigned epoch, unsigned l
   return ((unsigned long long)epoch << 34) | (f << 32) | (unsigned)v;
 }
 
-// K <= 4 arrays of n elements (io.in[a] -> io.out[a]) in one launch: ticket q is tile q % nb
+// K <= 5 arrays of n elements (io.in[a] -> io.out[a]) in one launch: ticket q is tile q % nb
 // of array q / nb, so every tile's look-back predecessors hold smaller tickets.
 template <class T>
 struct ScanIO {
-  const T* in[4];
-  int* out[4];
+  const T* in[5];
+  int* out[5];
 };
 
 template <class T>
@@ -163,10 +163,10 @@ cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n) {
   return scan_impl<uint8_t>(c, ScanIO<uint8_t>{{in}, {out}}, 1, n);
 }
-// K <= 4 equal-length int32 scans in[a] -> out[a] in one launch
+// K <= 5 equal-length int32 scans in[a] -> out[a] in one launch
 cudaError_t launch_scan_i32_multi(rpd_ctx* c, const int32_t* const* in, int32_t* const* out,
                                   int K, int64_t n) {
-  ScanIO<int32_t> io{{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
+  ScanIO<int32_t> io{};
   for (int a = 0; a < K; ++a) {
     io.in[a] = in[a];
     io.out[a] = out[a];

@@ -24,7 +24,8 @@ FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
-            "rpd_get_stats", "rpd_version"]
+            "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
+            "rpd_download_euler"]
 
 
 class RPDError(RuntimeError):
@@ -38,6 +39,13 @@ class _Pieces(C.Structure):
                 ("piece_vol", C.c_void_p), ("piece_m1", C.c_void_p),
                 ("piece_facemask", C.c_void_p), ("inc_off", C.c_void_p),
                 ("inc_sphere", C.c_void_p), ("n_pieces", C.c_int64), ("n_inc", C.c_int64)]
+
+
+class _Euler(C.Structure):
+    _fields_ = [("denom", C.c_int64), ("piece_euler", C.c_void_p), ("rpf_off", C.c_void_p),
+                ("rpf_sphere", C.c_void_p), ("rpf_euler", C.c_void_p), ("rpc_sum", C.c_void_p),
+                ("rpf_sum", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64),
+                ("N", C.c_int64), ("E", C.c_int64)]
 
 
 class _Stats(C.Structure):
@@ -80,9 +88,13 @@ def load_library(path: str = LIB_PATH):
     L.rpd_download_pieces.argtypes = [vp] * 8
     L.rpd_download_cands.argtypes = [vp, vp, vp]
     L.rpd_get_stats.argtypes = [vp, C.POINTER(_Stats)]
+    L.rpd_set_euler.argtypes = [vp, vp, i64, i64, vp, i64, C.POINTER(i64)]
+    L.rpd_get_euler.argtypes = [vp, C.POINTER(_Euler)]
+    L.rpd_download_euler.argtypes = [vp] * 7
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
-              "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats"):
+              "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
+              "rpd_get_euler", "rpd_download_euler"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -238,6 +250,41 @@ class RPDContext:
         out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
         return out
 
+    def set_euler(self, tets_all, V: int, local_ids=None) -> int:
+        """Fractional Euler payloads of the ctx's tets from the whole mesh ``tets_all``
+        (PAPER.md:491); ``local_ids``: global index of every ctx-local tet (None: the ctx holds
+        all tets in order).  Returns the common denominator L.  ``tets_all=None`` switches
+        Euler mode off."""
+        L = C.c_int64()
+        if tets_all is None:
+            self._check(self.L.rpd_set_euler(self.h, None, 0, 0, None, 0, C.byref(L)))
+            return 0
+        pt, kt = _ptr(tets_all, np.int32)
+        T_all = int(np.prod(kt.shape)) // 4
+        if local_ids is None:
+            pl, kl, T_local = None, None, T_all
+        else:
+            pl, kl = _ptr(local_ids, np.int32)
+            T_local = int(np.prod(kl.shape))
+        self._check(self.L.rpd_set_euler(self.h, pt, T_all, int(V), pl, T_local, C.byref(L)))
+        self._keep_eu = (kt, kl)
+        return L.value
+
+    def download_euler(self, device=False) -> dict:
+        """Euler data of the current pieces (exact numerators over ``euler_denom``):
+        piece_euler, rpf_off / rpf_sphere / rpf_euler (radical facets of each piece),
+        rpc_sum [N] and rpf_sum [E] (per sphere / per CSR entry of the row-sorted CSR)."""
+        e = _Euler()
+        self._check(self.L.rpd_get_euler(self.h, C.byref(e)))
+        specs = [(e.n_pieces, np.int64), (e.n_pieces + 1, np.int32), (e.n_rpf, np.int32),
+                 (e.n_rpf, np.int64), (e.N, np.int64), (e.E, np.int64)]
+        arrs = self._alloc(specs, device)
+        self._check(self.L.rpd_download_euler(self.h, *[self._p(a) for a in arrs]))
+        out = dict(zip(["piece_euler", "rpf_off", "rpf_sphere", "rpf_euler", "rpc_sum",
+                        "rpf_sum"], arrs))
+        out["euler_denom"] = int(e.denom)
+        return out
+
     def stats(self) -> dict:
         s = _Stats()
         self._check(self.L.rpd_get_stats(self.h, C.byref(s)))
@@ -247,7 +294,8 @@ class RPDContext:
     def _alloc(specs, device):
         if device:
             import torch
-            tdt = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8}
+            tdt = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8,
+                   np.int64: torch.int64}
             return [torch.empty(max(n, 0), dtype=tdt[dt], device="cuda") for n, dt in specs]
         return [np.empty(max(n, 0), dtype=dt) for n, dt in specs]
 

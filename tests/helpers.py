@@ -76,3 +76,32 @@ def slice_tets(res, ids):
     out["inc_sphere"] = np.asarray(res["inc_sphere"])[np.concatenate(incs) if incs else
                                                       np.zeros(0, int)]
     return out
+
+
+def slice_euler(res, piece_ids):
+    """Euler arrays of the pieces ``piece_ids`` (per-piece value and radical-facet CSR)."""
+    ro = np.asarray(res["rpf_off"])
+    rs = [np.arange(ro[p], ro[p + 1]) for p in piece_ids]
+    ridx = np.concatenate(rs) if rs else np.zeros(0, int)
+    return {"piece_euler": np.asarray(res["piece_euler"])[np.asarray(piece_ids, int)],
+            "rpf_off": np.r_[0, np.cumsum([len(r) for r in rs])].astype(np.int32),
+            "rpf_sphere": np.asarray(res["rpf_sphere"])[ridx],
+            "rpf_euler": np.asarray(res["rpf_euler"])[ridx], "euler_denom": res["euler_denom"]}
+
+
+def compare_euler(a, b):
+    """Exact comparison of two Euler results (numerators over their own denominators):
+    a[x] / La == b[x] / Lb  <=>  a[x] * Lb == b[x] * La (Python integers)."""
+    errs = []
+    La, Lb = int(a["euler_denom"]), int(b["euler_denom"])
+    for k in ("rpf_off", "rpf_sphere"):
+        if not np.array_equal(np.asarray(a[k]), np.asarray(b[k])):
+            errs.append(f"{k} differs")
+            return errs
+    for k in ("piece_euler", "rpf_euler"):
+        x = [int(v) * Lb for v in np.asarray(a[k]).tolist()]
+        y = [int(v) * La for v in np.asarray(b[k]).tolist()]
+        bad = [i for i in range(len(x)) if x[i] != y[i]]
+        if len(x) != len(y) or bad:
+            errs.append(f"{k}: {len(bad)} of {len(x)} differ (first {bad[:3]})")
+    return errs

@@ -1,0 +1,176 @@
+"""Fractional Euler characteristics: the clip
+kernel's on-the-fly payload sums vs the CPU oracle, exactly (rational numerators), through the
+C ABI (-m gpu)."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import rpd_workloads as W
+from tests.helpers import compare_euler, piece_tet, slice_euler, slice_tets
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=["all_pairs", "pruned"])
+def ctx(request):
+    import paper_2403_18761_b200 as P
+    P.build()
+    c = P.RPDContext(0, filter_mode=request.param)
+    yield c
+    c.close()
+
+
+def run_gpu_euler(ctx, w, tets=None, local_ids=None):
+    tets_local = w.tets if tets is None else tets
+    L = ctx.set_euler(w.tets, len(w.verts), local_ids)
+    try:
+        ctx.relations(w.verts, tets_local, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        out = ctx.download_cands()
+        out.update(ctx.download_pieces())
+        out.update(ctx.download_euler())
+    finally:
+        ctx.set_euler(None, 0)
+    assert out["euler_denom"] == L
+    return out
+
+
+def check_sums(got, ref, w):
+    """Per-sphere RPC and per-CSR-entry RPF sums against the oracle's sums (Fractions)."""
+    rpc, rpf = oracle.euler_sums(ref, w.N, w.nbr_off, w.nbr_idx)
+    L = got["euler_denom"]
+    assert [Fraction(int(v), L) for v in got["rpc_sum"]] == rpc
+    for i in range(w.N):
+        for e in range(w.nbr_off[i], w.nbr_off[i + 1]):
+            j = int(w.nbr_idx[e])
+            assert Fraction(int(got["rpf_sum"][e]), L) == rpf.get((i, j), 0), (i, j)
+
+
+MAKERS = [lambda: W.make_c1(0), lambda: W.make_c1(1, degenerate=True),
+          lambda: W.make_c1(6, degenerate=True, big=True),
+          lambda: W.random_tiny(0, n_spheres=14, grid=2),
+          lambda: W.random_tiny(3, n_spheres=14, grid=2, coarse=True),
+          lambda: W.make_shape_workload("E3", 2000, 150, seed=3, cache=False),
+          lambda: W.make_shape_workload("E5", 3000, 300, seed=5, radius_mode="high_variance",
+                                        cache=False)]
+
+
+@pytest.mark.parametrize("make", MAKERS)
+def test_euler_parity(ctx, make):
+    w = make()
+    got = run_gpu_euler(ctx, w)
+    ref = oracle.rpd_workload(w, euler=True)
+    errs = compare_euler(got, ref)
+    assert not errs, errs
+    check_sums(got, ref, w)
+
+
+def test_euler_single_sphere_genus_one(ctx):
+    """PAPER.md Fig. 4(a): one sphere covering the genus-1 solid has Euler(RPC) = 0."""
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    got = run_gpu_euler(ctx, w)
+    assert int(got["rpc_sum"][0]) == 0 and len(got["piece_euler"]) == w.T
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(1, degenerate=True),
+                                  lambda: W.make_shape_workload("Wd", 2500, 200, seed=9,
+                                                                radius_mode="high_variance",
+                                                                cache=False)])
+def test_euler_wide_kernel(ctx, make):
+    """The 128-vertex instantiation with Euler payloads gives the same values."""
+    w = make()
+    ctx.set_clip_wide(True)
+    try:
+        got = run_gpu_euler(ctx, w)
+    finally:
+        ctx.set_clip_wide(False)
+    assert not compare_euler(got, oracle.rpd_workload(w, euler=True))
+
+
+def test_euler_sharded_local_ids(ctx):
+    """Tet shards with global payloads (rpd_set_euler local_ids): each shard's pieces match
+    the oracle's, and the per-sphere sums of the shards add up to the whole mesh's."""
+    w = W.make_shape_workload("Sh", 3000, 200, seed=6, cache=False)
+    ref = oracle.rpd_workload(w, euler=True)
+    tot_rpc = np.zeros(w.N, np.int64)
+    tot_rpf = np.zeros(len(w.nbr_idx), np.int64)
+    for rank in range(2):
+        ids = W.block_cyclic_shard(w.T, 2, rank, block=256).astype(np.int32)
+        got = run_gpu_euler(ctx, w, tets=w.tets[ids], local_ids=ids)
+        sub = slice_tets(ref, ids)
+        pidx = np.concatenate([np.arange(ref["piece_off"][t], ref["piece_off"][t + 1])
+                               for t in ids])
+        errs = compare_euler(got, slice_euler(ref, pidx))
+        assert not errs, errs
+        assert np.array_equal(got["piece_sphere"], sub["piece_sphere"])
+        tot_rpc += got["rpc_sum"]
+        tot_rpf += got["rpf_sum"]
+    full = run_gpu_euler(ctx, w)
+    assert np.array_equal(tot_rpc, full["rpc_sum"]) and np.array_equal(tot_rpf, full["rpf_sum"])
+
+
+def test_euler_partial_update(ctx):
+    """Partial updates carry the Euler data: equal to the oracle's partial update (R11)."""
+    w = W.make_shape_workload("S", 2000, 150, seed=3, n_batches=2, batch_m=12, clusters=3,
+                              cache=False)
+    ctx.set_euler(w.tets, len(w.verts))
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        prev = oracle.rpd_workload(w, euler=True)
+        n_old = w.N
+        for (sph, off, idx) in w.batches:
+            ctx.update_partial(sph, off, idx, np.arange(n_old, len(sph), dtype=np.int32))
+            got = ctx.download_pieces()
+            got.update(ctx.download_euler())
+            part, dirty = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old,
+                                                euler=True)
+            assert len(dirty) == ctx.n_dirty
+            errs = compare_euler(got, part)
+            assert not errs, errs
+            import copy
+            w2 = copy.copy(w)
+            w2.spheres, w2.nbr_off, w2.nbr_idx = sph, off, idx
+            check_sums(got, part, w2)
+            prev, n_old = part, len(sph)
+    finally:
+        ctx.set_euler(None, 0)
+
+
+def test_euler_errors(ctx):
+    import paper_2403_18761_b200 as P
+    w = W.make_c1(0)
+    with pytest.raises(P.RPDError) as e:   # V beyond the face-key range
+        ctx.set_euler(w.tets, 1 << 21)
+    assert e.value.status == -1
+    ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    ctx.clip()
+    with pytest.raises(P.RPDError) as e:   # no Euler data for these pieces
+        ctx.download_euler()
+    assert e.value.status == -5
+    ctx.set_euler(w.tets[:3], len(w.verts))  # payloads for 3 tets, ctx holds 6
+    try:
+        with pytest.raises(P.RPDError) as e:
+            ctx.clip()
+        assert e.value.status == -1
+    finally:
+        ctx.set_euler(None, 0)
+
+
+def test_euler_c3_sampled(ctx):
+    """BASELINE.json configs[2] at full size: sampled pieces vs the oracle, every RPC / RPF
+    sum an integer (the fractional payloads of shared elements add up)."""
+    w = W.make_config("C3")
+    got = run_gpu_euler(ctx, w)
+    rng = np.random.default_rng(3)
+    ids = np.sort(rng.choice(w.T, 40, replace=False)).astype(np.int32)
+    ref = oracle.rpd_workload(w, tet_ids=ids, euler=True)
+    pidx = np.concatenate([np.arange(got["piece_off"][t], got["piece_off"][t + 1]) for t in ids])
+    errs = compare_euler(slice_euler(got, pidx), ref)
+    assert not errs, errs
+    L = got["euler_denom"]
+    assert np.all(got["rpc_sum"] % L == 0) and np.all(got["rpf_sum"] % L == 0)
+    chi = got["rpc_sum"] // L
+    assert np.sum(chi == 1) > 0.5 * np.sum(chi != 0)
