@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--partial-iters", type=int, default=-1,
                     help="partial updates per step (-1: all batches of the config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-euler", action="store_true",
+                    help="skip the fractional-Euler (NEXT-1) side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -347,6 +349,47 @@ def main():
         d2h = sum(np.asarray(v).nbytes for v in out.values())
     e2e_value = float(np.mean(e2e_pairs)) * world / float(np.mean(e2e_times))
 
+    # ---- NEXT-1 side measurement: the full RPD with the fractional Euler characteristics
+    # fused into the clip (payloads from the whole mesh, per-sphere sums all-reduced)
+    euler = None
+    if not args.no_euler:
+        from paper_2403_18761_b200.dist import allreduce_euler
+        L = ctx.set_euler(w.tets, len(w.verts), ids if world > 1 else None)
+        e_full, e_clip = [], []
+        for s in range(args.warmup + args.steps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            ctx.relations(d_verts, d_tets, *d_base)
+            ctx.clip()
+            ev1.record()
+            torch.cuda.synchronize()
+            if s >= args.warmup:
+                st = ctx.stats()
+                e_full.append(ev0.elapsed_time(ev1))
+                e_clip.append(st["clip_ms"])
+        eu = ctx.download_euler(device=True)
+        if world > 1:
+            eu = allreduce_euler(eu)
+        chi = (eu["rpc_sum"] // L).cpu().numpy()
+        integral = bool(torch.all(eu["rpc_sum"] % L == 0).item())
+        ctx.set_euler(None, 0)
+        ef = torch.tensor([float(np.median(e_full)), float(np.median(e_clip))],
+                          dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ef, op=dist.ReduceOp.MAX)
+        euler = {"full_rpd_ms": float(ef[0]), "clip_ms": float(ef[1]),
+                 "clip_overhead_vs_plain": float(ef[1]) / max(float(np.median(
+                     [r["clip_ms"] for r in recs])), 1e-9) - 1.0,
+                 "denominator": int(L), "rpc_sums_integral": integral,
+                 "spheres_with_cells": int(np.sum(chi != 0)),
+                 "rpc_euler_eq_1": int(np.sum(chi == 1)),
+                 "note": "fractional Euler characteristics (PAPER.md:482-506) fused into the "
+                         "clip; full_rpd_ms = relations + clip + per-sphere sums (CUDA events)"}
+
     # ---- roofline of the dominant kernel
     fmed = float(np.median([r["filter_ms"] for r in recs]))
     cmed = float(np.median([r["clip_ms"] for r in recs]))
@@ -401,6 +444,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h),
                 "note": "the bench step (full RPD + partial updates) through the C ABI with pinned "
                         "host inputs and a pinned host download of the final pieces"},
+        "euler": euler,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches // max(args.steps, 1)),
     }

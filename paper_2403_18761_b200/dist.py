@@ -92,3 +92,16 @@ def gather_pieces(local: dict, tet_ids_local, T: int, group=None) -> dict:
     out["inc_sphere"] = inc
     out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
     return out
+
+
+def allreduce_euler(local: dict, group=None) -> dict:
+    """Per-sphere fractional Euler sums of the whole job (SURVEY.md §8(e) "validation
+    aggregates"): every rank's rpc_sum [N] and rpf_sum [E] (int64 numerators over the common
+    denominator, identical on all ranks because the payloads are built from the whole mesh)
+    are summed by one all-reduce each.  Integer sums: exact and order-independent."""
+    out = dict(local)
+    for k in ("rpc_sum", "rpf_sum"):
+        t = local[k].to(torch.int64).clone()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        out[k] = t
+    return out

@@ -68,3 +68,56 @@ def test_shards_partition_the_tets():
         assert np.array_equal(np.sort(ids), np.arange(T))
         sizes = [len(shard_tets(T, world, r)) for r in range(world)]
         assert max(sizes) - min(sizes) <= 4096
+
+
+def _euler_csr(r, w):
+    """Oracle per-piece Euler numerators summed per sphere (rpc [N]) and per CSR entry of its
+    neighbour row (rpf [E]) as int64 -- the layout of rpd_download_euler."""
+    rpc = np.zeros(w.N, np.int64)
+    rpf = np.zeros(len(w.nbr_idx), np.int64)
+    ro = r["rpf_off"]
+    for p, i in enumerate(r["piece_sphere"].tolist()):
+        rpc[i] += r["piece_euler"][p]
+        row = w.nbr_idx[w.nbr_off[i]:w.nbr_off[i + 1]]
+        for k in range(ro[p], ro[p + 1]):
+            e = w.nbr_off[i] + int(np.nonzero(row == r["rpf_sphere"][k])[0][0])
+            rpf[e] += r["rpf_euler"][k]
+    return rpc, rpf
+
+
+def _euler_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_18761_b200.dist import allreduce_euler, shard_tets
+        w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
+        ids = shard_tets(w.T, world, rank, block=256)
+        r = oracle.rpd_workload(w, tet_ids=ids, euler=True)
+        rpc, rpf = _euler_csr(r, w)
+        out = allreduce_euler({"rpc_sum": torch.as_tensor(rpc), "rpf_sum": torch.as_tensor(rpf)})
+        if rank == 0:
+            q.put({k: v.numpy() for k, v in out.items()} | {"L": r["euler_denom"]})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_euler_allreduce_equals_single_rank():
+    """NEXT-1 on the sharded path: the per-rank RPC / RPF sums of the tet shards, all-reduced,
+    equal the single-rank sums (payloads built from the whole mesh on every rank)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_euler_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
+    ref = oracle.rpd_workload(w, euler=True)
+    rpc, rpf = _euler_csr(ref, w)
+    assert got["L"] == ref["euler_denom"]
+    assert np.array_equal(got["rpc_sum"], rpc) and np.array_equal(got["rpf_sum"], rpf)
