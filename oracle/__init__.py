@@ -63,7 +63,9 @@ class _Result(C.Structure):
                 ("n_pieces", C.c_int64), ("n_inc", C.c_int64),
                 ("euler_denom", C.c_int64), ("piece_euler", C.POINTER(C.c_int64)),
                 ("rpf_off", C.POINTER(C.c_int32)), ("rpf_sphere", C.POINTER(C.c_int32)),
-                ("rpf_euler", C.POINTER(C.c_int64)), ("n_rpf", C.c_int64),
+                ("rpf_euler", C.POINTER(C.c_int64)),
+                ("piece_sosfm", C.POINTER(C.c_uint8)), ("rpf_fm", C.POINTER(C.c_uint8)),
+                ("n_rpf", C.c_int64),
                 ("n_rel_tests", C.c_int64), ("n_clip_tests", C.c_int64),
                 ("n_constructions", C.c_int64), ("n_fan_triangles", C.c_int64),
                 ("n_zero_hits", C.c_int64),
@@ -155,7 +157,9 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
                         "piece_euler": arr(r.piece_euler, r.n_pieces, np.int64),
                         "rpf_off": arr(r.rpf_off, r.n_pieces + 1, np.int32),
                         "rpf_sphere": arr(r.rpf_sphere, r.n_rpf, np.int32),
-                        "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64)})
+                        "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64),
+                        "piece_sosfm": arr(r.piece_sosfm, r.n_pieces, np.uint8),
+                        "rpf_fm": arr(r.rpf_fm, r.n_rpf, np.uint8)})
     finally:
         L.oracle_free(rp)
     return out
@@ -219,7 +223,9 @@ def per_tet_lists(res, T):
             if ro is not None and len(ro) == len(res["piece_sphere"]) + 1:
                 eu = (int(res["piece_euler"][p]),
                       tuple(res["rpf_sphere"][ro[p]:ro[p + 1]].tolist()),
-                      tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()))
+                      tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()),
+                      int(res["piece_sosfm"][p]),
+                      tuple(res["rpf_fm"][ro[p]:ro[p + 1]].tolist()))
             pcs.append((int(res["piece_sphere"][p]), float(res["piece_vol"][p]),
                         tuple(res["piece_m1"][p].tolist()), int(res["piece_facemask"][p]),
                         tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist()), eu))
@@ -230,7 +236,7 @@ def per_tet_lists(res, T):
 def from_per_tet_lists(L):
     cand_off = [0]
     cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
-    pe, rpf_off, rpf_j, rpf_e = [], [0], [], []
+    pe, rpf_off, rpf_j, rpf_e, sfm, rfm = [], [0], [], [], [], []
     for cands, pcs in L:
         cand_idx += cands
         cand_off.append(len(cand_idx))
@@ -245,12 +251,15 @@ def from_per_tet_lists(L):
                 pe.append(eu[0])
                 rpf_j += list(eu[1])
                 rpf_e += list(eu[2])
+                sfm.append(eu[3])
+                rfm += list(eu[4])
                 rpf_off.append(len(rpf_j))
         piece_off.append(len(ps))
     eul = {}
     if len(pe) == len(ps) and len(rpf_off) == len(ps) + 1:
         eul = {"piece_euler": np.array(pe, np.int64), "rpf_off": np.array(rpf_off, np.int32),
-               "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64)}
+               "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64),
+               "piece_sosfm": np.array(sfm, np.uint8), "rpf_fm": np.array(rfm, np.uint8)}
     return {**eul, "cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
             "piece_off": np.array(piece_off, np.int32), "piece_sphere": np.array(ps, np.int32),
             "piece_vol": np.array(pv, np.float64),
@@ -289,6 +298,84 @@ def euler_sums(res, N, nbr_off, nbr_idx):
             key = (i, int(res["rpf_sphere"][r]))
             rpf[key] = rpf.get(key, Fraction(0)) + Fraction(int(res["rpf_euler"][r]), L)
     return rpc, rpf
+
+
+def face_adjacency(tets):
+    """adj[t][k] = (t', k'): the tet sharing face k of t (face k = opposite vertex k), or None
+    (boundary).  Plain dictionary of sorted vertex triples."""
+    owners = {}
+    for t, tv in enumerate(np.asarray(tets).tolist()):
+        for k in range(4):
+            owners.setdefault(tuple(sorted(tv[:k] + tv[k + 1:])), []).append((t, k))
+    adj = [[None] * 4 for _ in range(len(tets))]
+    for own in owners.values():
+        if len(own) == 2:
+            (a, ka), (b, kb) = own
+            adj[a][ka] = (b, kb)
+            adj[b][kb] = (a, ka)
+    return adj
+
+
+def topology(res, tets, N):
+    """CC numbers ("trace their CC numbers using a simple traversal"):
+    components of every RPC(m_i) -- the pieces of m_i, two pieces in tets sharing face f
+    connected when f is a facet of both -- and of every RPF(m_i, m_j) seen from m_i -- the
+    facets of m_i's pieces on h_ij, connected across a shared tet face f when both have an
+    edge on f.  Elements of the symbolically perturbed pieces (R26-R27), so they
+    match the Euler sums.  Plain union-find over Python objects.  Returns (rpc_cc [N],
+    {(i, j): cc})."""
+    parent = {}
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    def union(a, b):
+        ra, rb = find(a), find(b)
+        if ra != rb:
+            parent[max(ra, rb)] = min(ra, rb)
+
+    adj = face_adjacency(tets)
+    po, ro = res["piece_off"], res["rpf_off"]
+    ps = res["piece_sphere"].tolist()
+    piece_of = {}          # (t, i) -> piece index
+    for t in range(len(tets)):
+        for q in range(po[t], po[t + 1]):
+            piece_of[(t, ps[q])] = q
+            parent[("c", q)] = ("c", q)
+            for r in range(ro[q], ro[q + 1]):
+                parent[("f", ps[q], int(res["rpf_sphere"][r]), t)] = \
+                    ("f", ps[q], int(res["rpf_sphere"][r]), t)
+    for t in range(len(tets)):
+        for q in range(po[t], po[t + 1]):
+            i = ps[q]
+            for k in range(4):
+                nb = adj[t][k]
+                if nb is None:
+                    continue
+                t2, k2 = nb
+                q2 = piece_of.get((t2, i))
+                if q2 is None:
+                    continue
+                if (res["piece_sosfm"][q] >> k) & 1 and (res["piece_sosfm"][q2] >> k2) & 1:
+                    union(("c", q), ("c", q2))
+                f2 = {int(res["rpf_sphere"][r]): int(res["rpf_fm"][r])
+                      for r in range(ro[q2], ro[q2 + 1])}
+                for r in range(ro[q], ro[q + 1]):
+                    j = int(res["rpf_sphere"][r])
+                    if (res["rpf_fm"][r] >> k) & 1 and j in f2 and (f2[j] >> k2) & 1:
+                        union(("f", i, j, t), ("f", i, j, t2))
+    rpc_cc = [0] * N
+    rpf_cc = {}
+    for x in parent:
+        if find(x) == x:
+            if x[0] == "c":
+                rpc_cc[ps[x[1]]] += 1
+            else:
+                rpf_cc[(x[1], x[2])] = rpf_cc.get((x[1], x[2]), 0) + 1
+    return rpc_cc, rpf_cc
 
 
 def max_threads() -> int:

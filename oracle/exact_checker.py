@@ -254,3 +254,50 @@ def explicit_euler(verts, tets, spheres, nbr_off, nbr_idx, i):
                 ff.add(on)
     return (len(V) - len(E) + len(F) - C,
             {j: len(a) - len(b) + len(c) for j, (a, b, c) in rpf.items()}, generic)
+
+
+def explicit_cc(verts, tets, spheres, nbr_off, nbr_idx, i):
+    """CC numbers of the restricted elements of sphere i from the explicitly extracted complex
+    (exact rational vertices, no SoS): pieces are connected when they share a 2-face (equal
+    vertex sets), facets on the radical plane h_ij when they share an edge.  Returns
+    (cc of RPC(m_i), {j: cc of RPF(m_i, m_j)}, generic)."""
+    sph_X = [tuple(_lat(s[c]) for c in range(4)) for s in spheres]
+    S = [int(j) for j in nbr_idx[nbr_off[i]:nbr_off[i + 1]]]
+    if not S and len(spheres) > 1:
+        return 0, {}, True
+    cells, generic = [], True
+    for t in range(len(tets)):
+        tet_X = [tuple(_lat(verts[v][c]) for c in range(3)) for v in tets[t]]
+        cell = exact_piece_cells(tet_X, sph_X, i, S)
+        if cell is not None:
+            generic &= cell["generic"]
+            cells.append(cell)
+
+    def components(items, keys):
+        parent = list(range(len(items)))
+
+        def find(x):
+            while parent[x] != x:
+                parent[x] = parent[parent[x]]
+                x = parent[x]
+            return x
+        owner = {}
+        for a, ks in enumerate(keys):
+            for k in ks:
+                if k in owner:
+                    ra, rb = find(a), find(owner[k])
+                    parent[max(ra, rb)] = min(ra, rb)
+                else:
+                    owner[k] = a
+        return len({find(a) for a in range(len(items))})
+
+    rpc = components(cells, [[on for _, on in c["facets"]] for c in cells])
+    rpf = {}
+    per_j = {}
+    for c in cells:
+        for src, on in c["facets"]:
+            if src[0] == "r":
+                per_j.setdefault(src[1], []).append([e for e in c["edges"] if e <= on])
+    for j, facet_edges in per_j.items():
+        rpf[j] = components(facet_edges, facet_edges)
+    return rpc, rpf, generic

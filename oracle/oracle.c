@@ -166,6 +166,8 @@ typedef struct {
   int64_t* piece_euler;          /* [n_pieces] Euler of the piece's fractional complex */
   int32_t *rpf_off, *rpf_sphere; /* [n_pieces + 1], [n_rpf]: radical facets j, ascending */
   int64_t* rpf_euler;            /* [n_rpf] Euler of the piece's facet on h_ij */
+  uint8_t* piece_sosfm;          /* [n_pieces] tet faces that are facets of the piece (SoS) */
+  uint8_t* rpf_fm;               /* [n_rpf] tet faces the radical facet has an edge on (SoS) */
   int64_t n_rpf;
   /* instrumentation (C1 step 9) */
   int64_t n_rel_tests, n_clip_tests, n_constructions, n_fan_triangles, n_zero_hits;
@@ -575,7 +577,9 @@ typedef struct {
   int64_t euler;      /* fractional Euler characteristic of the piece, numerator over L */
   int32_t* rpf_j;     /* radical facets of the piece (neighbour j) ... */
   int64_t* rpf_e;     /* ... and the fractional Euler characteristic of each, over L */
+  uint8_t* rpf_fm;    /* ... and the tet faces it has an edge on */
   int32_t nrpf;
+  uint8_t sosfm;      /* tet faces among the piece's facets */
 } piece_t;
 
 static int cmp_i32(const void* a, const void* b) {
@@ -606,6 +610,7 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
   int64_t chi = -L;
   int* is_facet = (int*)calloc(npl, sizeof(int));
   int64_t* fe = (int64_t*)calloc(npl, sizeof(int64_t)); /* Euler of each facet */
+  unsigned* ffm = (unsigned*)calloc(npl, sizeof(unsigned)); /* tet faces sharing an edge */
   for (int v = 0; v < nv; ++v) {
     int64_t pv = carrier_payload(A14, L, faces_of(P, P->v[v].p, 3));
     chi += pv;
@@ -622,33 +627,42 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
       chi -= pe;
       fe[e[0]] -= pe;
       fe[e[1]] -= pe;
+      /* topology (NEXT-2): an edge between facet x and tet face k joins x to face k */
+      for (int a = 0; a < 2; ++a)
+        if (P->pl[e[1 - a]].src < 0) ffm[e[a]] |= 1u << (-1 - P->pl[e[1 - a]].src);
     }
   int nr = 0;
+  out->sosfm = 0;
   for (int f = 0; f < npl; ++f) {
     if (!is_facet[f]) continue;
     int64_t pf = carrier_payload(A14, L, faces_of(P, &f, 1));
     chi += pf;
     fe[f] += pf;
     if (P->pl[f].src >= 0) ++nr;
+    else out->sosfm |= (uint8_t)(1u << (-1 - P->pl[f].src));
   }
-  int64_t* pairs = (int64_t*)malloc(sizeof(int64_t) * 2 * (nr > 0 ? nr : 1));
+  int64_t* pairs = (int64_t*)malloc(sizeof(int64_t) * 3 * (nr > 0 ? nr : 1));
   int m = 0;
   for (int f = 0; f < npl; ++f)
     if (is_facet[f] && P->pl[f].src >= 0) {
-      pairs[2 * m] = P->pl[f].src;
-      pairs[2 * m + 1] = fe[f];
+      pairs[3 * m] = P->pl[f].src;
+      pairs[3 * m + 1] = fe[f];
+      pairs[3 * m + 2] = ffm[f];
       ++m;
     }
-  qsort(pairs, nr, 2 * sizeof(int64_t), cmp_rpf);
+  qsort(pairs, nr, 3 * sizeof(int64_t), cmp_rpf);
   out->euler = chi;
   out->nrpf = nr;
   out->rpf_j = (int32_t*)malloc(sizeof(int32_t) * (nr > 0 ? nr : 1));
   out->rpf_e = (int64_t*)malloc(sizeof(int64_t) * (nr > 0 ? nr : 1));
+  out->rpf_fm = (uint8_t*)malloc(nr > 0 ? nr : 1);
   for (int k = 0; k < nr; ++k) {
-    out->rpf_j[k] = (int32_t)pairs[2 * k];
-    out->rpf_e[k] = pairs[2 * k + 1];
+    out->rpf_j[k] = (int32_t)pairs[3 * k];
+    out->rpf_e[k] = pairs[3 * k + 1];
+    out->rpf_fm[k] = (uint8_t)pairs[3 * k + 2];
   }
   free(pairs);
+  free(ffm);
   free(fe);
   free(is_facet);
 }
@@ -822,6 +836,8 @@ static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piec
     out->nrpf = 0;
     out->rpf_j = NULL;
     out->rpf_e = NULL;
+    out->rpf_fm = NULL;
+    out->sosfm = 0;
     if (A14) piece_euler(&P, A14, Lden, out);
   }
   stats_acc->n_clip_tests += P.n_clip_tests;
@@ -859,6 +875,8 @@ void oracle_free(oracle_result* r) {
   free(r->rpf_off);
   free(r->rpf_sphere);
   free(r->rpf_euler);
+  free(r->piece_sosfm);
+  free(r->rpf_fm);
   free(r);
 }
 
@@ -927,6 +945,8 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
   R->rpf_off = (int32_t*)malloc(sizeof(int32_t) * (np + 1));
   R->rpf_sphere = (int32_t*)malloc(sizeof(int32_t) * (nr ? nr : 1));
   R->rpf_euler = (int64_t*)malloc(sizeof(int64_t) * (nr ? nr : 1));
+  R->piece_sosfm = (uint8_t*)malloc(np ? np : 1);
+  R->rpf_fm = (uint8_t*)malloc(nr ? nr : 1);
   R->rpf_off[0] = 0;
   int64_t r0 = 0;
   R->n_cand = nc;
@@ -959,14 +979,17 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
       memcpy(R->inc_sphere + i0, pc->inc, sizeof(int32_t) * pc->ninc);
       i0 += pc->ninc;
       R->piece_euler[p0] = pc->euler;
+      R->piece_sosfm[p0] = pc->sosfm;
       if (pc->nrpf) {
         memcpy(R->rpf_sphere + r0, pc->rpf_j, sizeof(int32_t) * pc->nrpf);
         memcpy(R->rpf_euler + r0, pc->rpf_e, sizeof(int64_t) * pc->nrpf);
+        memcpy(R->rpf_fm + r0, pc->rpf_fm, pc->nrpf);
       }
       r0 += pc->nrpf;
       R->rpf_off[p0 + 1] = (int32_t)r0;
       free(pc->rpf_j);
       free(pc->rpf_e);
+      free(pc->rpf_fm);
       ++p0;
       R->inc_off[p0] = (int32_t)i0;
       free(pc->inc);

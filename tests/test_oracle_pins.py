@@ -397,3 +397,67 @@ def test_euler_partial_update_equals_full(small_shape):
         for k in ("piece_euler", "rpf_off", "rpf_sphere", "rpf_euler"):
             assert np.array_equal(part[k], full[k]), k
         prev, n_old = part, len(sph)
+
+
+# ----------------------------------------------------------------------------- CC numbers
+# "CC Number"
+
+
+def _genus_one_spheres(xs, r=1.0):
+    """Spheres on the hole's axis line (y = 26, z = 20) of the box-with-hole solid (hole:
+    centre (32, 26), radius 9), neighbours = consecutive spheres."""
+    n = len(xs)
+    sph = np.array([[x, 26.0, 20.0, r] for x in xs])
+    idx, off = [], [0]
+    for a in range(n):
+        idx += [b for b in (a - 1, a + 1) if 0 <= b < n]
+        off.append(len(idx))
+    return sph, np.array(off, np.int32), np.array(idx, np.int32)
+
+
+def test_cc_torus_two_spheres_rpf_has_two_components():
+    """PAPER.md Fig. 4(b): two spheres on a torus-like solid -- the RPF between them has
+    CC = 2 (and Euler 2: two disks), each RPC is one contractible C-shaped half."""
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    sph, off, idx = _genus_one_spheres([20.0, 44.0])
+    r = oracle.rpd(w.verts, w.tets, sph, off, idx, euler=True)
+    rpc_cc, rpf_cc = oracle.topology(r, w.tets, 2)
+    rpc_eu, rpf_eu = oracle.euler_sums(r, 2, off, idx)
+    assert rpc_cc == [1, 1] and rpf_cc == {(0, 1): 2, (1, 0): 2}
+    assert rpc_eu == [1, 1] and rpf_eu == {(0, 1): 2, (1, 0): 2}
+
+
+def test_cc_slab_cell_has_two_components():
+    """PAPER.md Fig. 6(a): the RPC of the middle sphere is a slab narrower than the hole, cut
+    into two components (CC = 2, Euler 2); its RPFs are two segments-wide strips each."""
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    sph, off, idx = _genus_one_spheres([26.0, 32.0, 38.0])
+    r = oracle.rpd(w.verts, w.tets, sph, off, idx, euler=True)
+    rpc_cc, rpf_cc = oracle.topology(r, w.tets, 3)
+    rpc_eu, _ = oracle.euler_sums(r, 3, off, idx)
+    assert rpc_cc == [1, 2, 1] and rpc_eu == [1, 2, 1]
+    assert rpf_cc == {(0, 1): 2, (1, 0): 2, (1, 2): 2, (2, 1): 2}
+
+
+def test_cc_single_sphere():
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    r = oracle.rpd_workload(w, euler=True)
+    assert oracle.topology(r, w.tets, 1) == ([1], {})
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(3),
+                                  lambda: W.random_tiny(0, n_spheres=14, grid=2),
+                                  lambda: W.random_tiny(2, n_spheres=14, grid=2)])
+def test_cc_equals_explicit_extraction(make):
+    """The CC numbers from the pieces' facet / edge flags equal the components of the
+    explicitly extracted complexes (pieces glued by shared exact 2-faces, RPF facets by shared
+    exact edges)."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    rpc_cc, rpf_cc = oracle.topology(r, w.tets, w.N)
+    for i in range(w.N):
+        e_rpc, e_rpf, generic = X.explicit_cc(w.verts, w.tets, w.spheres, w.nbr_off,
+                                              w.nbr_idx, i)
+        assert generic
+        assert rpc_cc[i] == e_rpc, i
+        assert {j: v for (a, j), v in rpf_cc.items() if a == i} == e_rpf, i
