@@ -205,6 +205,39 @@ rpd_status rpd_download_euler(rpd_ctx* ctx, int64_t* piece_euler, int32_t* rpf_o
                               int32_t* rpf_sphere, int64_t* rpf_euler, int64_t* rpc_sum,
                               int64_t* rpf_sum);
 
+/* ---- CC numbers (Sec. 4.1.1)
+ *
+ * "we can trace their CC numbers using a simple traversal algorithm": the
+ * number of connected components of every RPC(m_i) and every RPF(m_i, m_j) (seen from m_i).
+ * Two pieces of m_i in tets sharing a face f are connected when f is a facet of both; two of
+ * its facets on h_ij in such tets when both have an edge on f (elements of the symbolically
+ * perturbed pieces, like the Euler sums; R26-R27).  Union-find on the device over
+ * the current pieces; needs rpd_set_euler with the ctx holding the whole mesh
+ * (local_ids == NULL, else RPD_ESTATE) before the last rpd_clip / rpd_update_partial.
+ * Outputs (ctx-owned device arrays, valid until the next mutating call):
+ *   rpc_cc     [N]        components of RPC(m_i) (0: no cell)
+ *   rpf_cc     [E]        components of RPF(m_i, m_j) at the CSR entry of j in row i (rows
+ *                         sorted ascending; 0: no face)
+ *   piece_comp [n_pieces] component label of every piece (its smallest piece index) -- the
+ *                         paper picks a surface point on a component other than m_i's own
+ *   rpf_comp   [n_rpf]    component label of every radical facet (smallest rpf index)
+ *   piece_sosfm[n_pieces] tet faces that are facets of the piece (bit k: face k)
+ *   rpf_fm     [n_rpf]    tet faces the radical facet has an edge on */
+typedef struct {
+  const int32_t* rpc_cc;
+  const int32_t* rpf_cc;
+  const int32_t* piece_comp;
+  const int32_t* rpf_comp;
+  const uint8_t* piece_sosfm;
+  const uint8_t* rpf_fm;
+  int64_t n_pieces, n_rpf, N, E;
+} rpd_topology;
+rpd_status rpd_get_topology(rpd_ctx* ctx, rpd_topology* out);
+/* Copy (host or device destinations; any pointer may be NULL). */
+rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
+                                 int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,
+                                 uint8_t* rpf_fm);
+
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */
 typedef struct {

@@ -167,7 +167,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
-                    &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid};
+                    &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -189,6 +190,8 @@ void rpd_destroy(rpd_ctx* c) {
     x->rpf_off.release();
     x->rpf_j.release();
     x->rpf_e.release();
+    x->sfm.release();
+    x->rfm.release();
   }
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
@@ -429,6 +432,8 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(c->r_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
     CK(c->p_rmask.ensure(sizeof(unsigned) * nw), "alloc");
     CK(c->p_rval.ensure(sizeof(long long) * 32 * nw), "alloc");
+    CK(c->p_sfm.ensure(nn), "alloc");
+    CK(c->p_rfm.ensure(32 * nw), "alloc");
   }
   const int32_t* moff = cs.moff.as<int32_t>();
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
@@ -481,11 +486,14 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(ps.rpf_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
     CK(ps.rpf_j.ensure(sizeof(int32_t) * (nr > 0 ? nr : 1)), "alloc");
     CK(ps.rpf_e.ensure(sizeof(long long) * (nr > 0 ? nr : 1)), "alloc");
+    CK(ps.sfm.ensure(npp), "alloc");
+    CK(ps.rfm.ensure(nr > 0 ? nr : 1), "alloc");
   }
   PieceDst d{ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.vol.as<double>(),
              ps.m1.as<double>(),  ps.fm.as<uint8_t>(),     ps.inc_off.as<int32_t>(),
              ps.inc.as<int32_t>(), ps.eu.as<long long>(),  ps.rpf_off.as<int32_t>(),
-             ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>()};
+             ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
+             ps.rfm.as<uint8_t>()};
   CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idx.as<int32_t>(), moff, d),
      "compact pieces");
   ps.n_tets = nt;
@@ -717,6 +725,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     CK(pn.rpf_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
     CK(pn.rpf_j.ensure(sizeof(int32_t) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
     CK(pn.rpf_e.ensure(sizeof(long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
+    CK(pn.sfm.ensure(npn), "alloc");
+    CK(pn.rfm.ensure(pn.n_rpf > 0 ? pn.n_rpf : 1), "alloc");
   }
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
   tmark(c, "merge-counts");
@@ -821,6 +831,7 @@ rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int
   const long long L = (long long)rb->u64[0];
   if (L <= 0) return fail(c, RPD_EOVERFLOW, "Euler payload denominator exceeds 2^50");
   c->euler = 1;
+  c->eu_whole = local_ids == nullptr;
   c->eu_L = L;
   c->eu_T = T_local;
   *denom = L;
@@ -862,6 +873,48 @@ rpd_status rpd_download_euler(rpd_ctx* c, int64_t* piece_euler, int32_t* rpf_off
   CK(cp(rpf_euler, e.rpf_euler, sizeof(int64_t) * e.n_rpf), "download");
   CK(cp(rpc_sum, e.rpc_sum, sizeof(int64_t) * e.N), "download");
   CK(cp(rpf_sum, e.rpf_sum, sizeof(int64_t) * e.E), "download");
+  CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_get_topology(rpd_ctx* c, rpd_topology* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_get_topology: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no topology data (rpd_set_euler, then rpd_clip)");
+  if (!c->eu_whole)
+    return fail(c, RPD_ESTATE, "CC numbers need the whole mesh in the ctx (local_ids == NULL)");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const PieceSet& ps = c->pcs[c->cur];
+  CK(launch_cc(c, ps), "cc");
+  out->rpc_cc = c->cc_out.as<int32_t>();
+  out->rpf_cc = c->cc_out.as<int32_t>() + c->st.N;
+  out->piece_comp = c->cc_par.as<int32_t>();
+  out->rpf_comp = c->cc_par.as<int32_t>() + ps.n_pieces;
+  out->piece_sosfm = ps.sfm.as<uint8_t>();
+  out->rpf_fm = ps.rfm.as<uint8_t>();
+  out->n_pieces = ps.n_pieces;
+  out->n_rpf = ps.n_rpf;
+  out->N = c->st.N;
+  out->E = c->st.E;
+  return RPD_OK;
+}
+
+rpd_status rpd_download_topology(rpd_ctx* c, int32_t* rpc_cc, int32_t* rpf_cc,
+                                 int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,
+                                 uint8_t* rpf_fm) {
+  rpd_topology t;
+  rpd_status s = rpd_get_topology(c, &t);
+  if (s) return s;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+  };
+  CK(cp(rpc_cc, t.rpc_cc, sizeof(int32_t) * t.N), "download");
+  CK(cp(rpf_cc, t.rpf_cc, sizeof(int32_t) * t.E), "download");
+  CK(cp(piece_comp, t.piece_comp, sizeof(int32_t) * t.n_pieces), "download");
+  CK(cp(rpf_comp, t.rpf_comp, sizeof(int32_t) * t.n_rpf), "download");
+  CK(cp(piece_sosfm, t.piece_sosfm, t.n_pieces), "download");
+  CK(cp(rpf_fm, t.rpf_fm, t.n_rpf), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }

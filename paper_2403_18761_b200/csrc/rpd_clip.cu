@@ -364,6 +364,8 @@ struct PairOut {
   long long* eu_piece;      // per pair: Euler of the piece x L
   unsigned* rmask;          // per pair: SoS radical facets (bits over N(i), incmask layout)
   long long* rval;          // per (pair, row position): Euler of that facet x L
+  uint8_t* sfm;             // per pair: tet faces that are SoS facets (CC numbers, NEXT-2)
+  uint8_t* rfm;             // per (pair, row position): tet faces the facet has an edge on
 };
 
 // EU: also the fractional Euler characteristics (a separate instantiation, so that the plain
@@ -909,7 +911,10 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         }
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
-          if (GW * k + lane < np) acc[GW * k + lane] = 0;
+          if (GW * k + lane < np) {
+            acc[GW * k + lane] = 0;
+            S.dsc[GW * k + lane] = 0u;  // (free after the cuts) tet faces next to each facet
+          }
       }
       __syncwarp(FULL);
       long long c2 = 0, cf = 0;
@@ -928,6 +933,11 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
                               (unsigned long long)(pv2 - pab - pbc));
         if (cc >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(acc + cc),
                                (unsigned long long)(pv2 - pbc - pca));
+        // CC numbers: every plane pair of the triplet is an edge, so a radical facet has an
+        // edge on each tet face of its vertices' triplets
+        if (a >= 4 && (mb | mc)) atomicOr(S.dsc + a, mb | mc);
+        if (b >= 4 && (ma | mc)) atomicOr(S.dsc + b, ma | mc);
+        if (cc >= 4 && (ma | mb)) atomicOr(S.dsc + cc, ma | mb);
       }
       __syncwarp(FULL);
       unsigned* rw = out.rmask + mo;
@@ -936,15 +946,17 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         for (int w = lane; w < nwp; w += GW) rw[w] = 0u;
         __syncwarp(FULL);
       }
-      unsigned rbits = 0u;
+      unsigned rbits = 0u, sbits = 0u;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) {
         const int pl = GW * k + lane;
         if (pl < np && facets_all.has(pl)) {
           cf += S.pay[EU_BIDX[eu_pm(pl)]];
+          sbits |= eu_pm(pl);
           if (pl >= 4) {  // radical facet: its part of the RPF between m_i and m_j
             const int pos = S.eidx[pl] - e0;
             rv[pos] = acc[pl] / 2 + out.eu_L;
+            out.rfm[32 * (int64_t)mo + pos] = (uint8_t)S.dsc[pl];
             if (one_word) rbits |= 1u << pos;
             else atomicOr(rw + (pos >> 5), 1u << (pos & 31));
           }
@@ -959,7 +971,11 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         const unsigned w = __reduce_or_sync(FULL, rbits);
         if (lane == 0) rw[0] = w;
       }
-      if (lane == 0) out.eu_piece[p] = c2 / 2 + cf - out.eu_L;
+      sbits = __reduce_or_sync(FULL, sbits);
+      if (lane == 0) {
+        out.eu_piece[p] = c2 / 2 + cf - out.eu_L;
+        out.sfm[p] = (uint8_t)sbits;
+      }
       __syncwarp(FULL);
     }
 
@@ -1098,6 +1114,8 @@ struct EuCompact {
   long long* piece;
   int32_t *rpf_off, *rpf_j;
   long long* rpf_e;
+  const uint8_t *p_sfm, *p_rfm;  // CC flags (per pair, per pair slot)
+  uint8_t *sfm, *rfm;            // ... compacted (per piece, per radical facet)
 };
 
 __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ cand_idx,
@@ -1141,6 +1159,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
   }
   if (eu.rmask) {  // Euler: the piece's value and its radical facets, ascending neighbour id
     eu.piece[q] = eu.p_eu[p];
+    eu.sfm[q] = eu.p_sfm[p];
     int r = eu.rscan[p];
     eu.rpf_off[q] = r;
     for (int w = w0; w < mask_off[p + 1]; ++w) {
@@ -1151,6 +1170,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
         const int pos = 32 * (w - w0) + b;
         eu.rpf_j[r] = nbr_idx[e0 + pos];
         eu.rpf_e[r] = eu.rval[32 * (int64_t)w0 + pos];
+        eu.rfm[r] = eu.p_rfm[32 * (int64_t)w0 + pos];
         ++r;
       }
     }
@@ -1209,7 +1229,8 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
             over ? over + 1 : nullptr, over,
             c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
-            c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>()};
+            c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>(),
+            c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>()};
   k_clip<GW, VPL, EU><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
@@ -1290,7 +1311,7 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
         d.inc_off, d.inc,
         EuCompact{c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_rval.as<long long>(),
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
-                  d.rpf_e});
+                  d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm});
     ++c->launches;
   } else {
     cudaMemsetAsync(d.inc_off, 0, sizeof(int32_t), c->stream);

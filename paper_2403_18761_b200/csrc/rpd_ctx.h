@@ -99,6 +99,7 @@ struct PieceSet {
   DevBuf off, sphere, vol, m1, fm, inc_off, inc;
   // fractional Euler characteristics (Euler mode): per piece, and per radical SoS facet
   DevBuf eu, rpf_off, rpf_j, rpf_e;
+  DevBuf sfm, rfm;  // CC flags: SoS tet facets per piece, tet faces next to each radical facet
   int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;
 };
 }  // namespace rpd
@@ -172,6 +173,10 @@ struct rpd_ctx {
   rpd::DevBuf eu_A;            // int64 [256] L / n, then L, then the counts-present bitmap
   rpd::DevBuf eu_sum;          // int64 [N + E + 1]: per-sphere RPC, per-CSR-entry RPF, misses
   rpd::DevBuf p_eu, p_rmask, p_rval, p_nrpf, r_scan;  // per-pair clip outputs
+  rpd::DevBuf p_sfm, p_rfm;                           // per-pair CC flags
+  bool eu_whole = false;       // payloads built with the ctx holding the whole mesh in order
+  rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
+  rpd::DevBuf cc_par, cc_out;  // CC numbers: union-find parents, outputs
 };
 
 namespace rpd {
@@ -221,6 +226,8 @@ struct PieceDst {
   int32_t* rpf_off;
   int32_t* rpf_j;
   long long* rpf_e;
+  uint8_t* sfm;       // [n_pieces], [n_rpf]
+  uint8_t* rfm;
 };
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
@@ -235,5 +242,6 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
 cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
                                const int32_t* local_ids, int64_t T_local);
 cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps);
+cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
 
 }  // namespace rpd

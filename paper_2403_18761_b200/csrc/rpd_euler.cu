@@ -38,19 +38,33 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   return x;
 }
 
-// insert-or-count; returns false if the table is full (never with the sizing below)
-__device__ bool ht_add(unsigned long long* keys, unsigned* cnt, unsigned long long mask,
-                       unsigned long long key) {
+// insert-or-count; returns the slot (and the count before this insertion in *before), or -1
+// if the table is full (never with the sizing below)
+__device__ long long ht_add(unsigned long long* keys, unsigned* cnt, unsigned long long mask,
+                            unsigned long long key, unsigned* before = nullptr) {
   unsigned long long h = mix64(key) & mask;
   for (unsigned long long probe = 0; probe <= mask; ++probe) {
     const unsigned long long prev = atomicCAS(keys + h, EMPTY_KEY, key);
     if (prev == EMPTY_KEY || prev == key) {
-      atomicAdd(cnt + h, 1u);
-      return true;
+      const unsigned b = atomicAdd(cnt + h, 1u);
+      if (before) *before = b;
+      return (long long)h;
     }
     h = (h + 1) & mask;
   }
-  return false;
+  return -1;
+}
+
+__device__ long long ht_find(const unsigned long long* keys, unsigned long long mask,
+                             unsigned long long key) {
+  unsigned long long h = mix64(key) & mask;
+  for (unsigned long long probe = 0; probe <= mask; ++probe) {
+    const unsigned long long k = keys[h];
+    if (k == key) return (long long)h;
+    if (k == EMPTY_KEY) return -1;
+    h = (h + 1) & mask;
+  }
+  return -1;
 }
 
 __device__ unsigned ht_get(const unsigned long long* keys, const unsigned* cnt,
@@ -76,7 +90,7 @@ __device__ __forceinline__ void sort3(long long& a, long long& b, long long& c) 
 __global__ void k_eu_count(int64_t T, const int32_t* __restrict__ tets, int64_t V,
                            unsigned* __restrict__ vcnt, unsigned long long* ekeys,
                            unsigned* ecnt, unsigned long long emask, unsigned long long* fkeys,
-                           unsigned* fcnt, unsigned long long fmask, int* err) {
+                           unsigned* fcnt, unsigned long long fmask, int* fown, int* err) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   const int4 q = reinterpret_cast<const int4*>(tets)[t];
@@ -98,13 +112,17 @@ __global__ void k_eu_count(int64_t T, const int32_t* __restrict__ tets, int64_t 
   for (int e = 0; e < 6; ++e) {
     long long a = v[EU_EDGE[e][0]], b = v[EU_EDGE[e][1]];
     if (b < a) { const long long x = a; a = b; b = x; }
-    ok &= ht_add(ekeys, ecnt, emask, (unsigned long long)(a * V + b));
+    ok &= ht_add(ekeys, ecnt, emask, (unsigned long long)(a * V + b)) >= 0;
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     long long a = v[k == 0 ? 1 : 0], b = v[k <= 1 ? 2 : 1], c = v[k <= 2 ? 3 : 2];
     sort3(a, b, c);
-    ok &= ht_add(fkeys, fcnt, fmask, (unsigned long long)((a * V + b) * V + c));
+    unsigned before = 0u;
+    const long long h = ht_add(fkeys, fcnt, fmask, (unsigned long long)((a * V + b) * V + c),
+                               &before);
+    ok &= h >= 0;
+    if (h >= 0 && before < 2u) fown[2 * h + before] = (int)(4 * t + k);  // face owners
   }
   if (!ok && atomicCAS(err, 0, (int)RPD_ENOMEM) == 0) err[1] = 0;
 }
@@ -117,6 +135,7 @@ __global__ void k_eu_records(int64_t T_local, const int32_t* __restrict__ local_
                              const unsigned* __restrict__ ecnt, unsigned long long emask,
                              const unsigned long long* __restrict__ fkeys,
                              const unsigned* __restrict__ fcnt, unsigned long long fmask,
+                             const int* __restrict__ fown, int* __restrict__ adj,
                              uint4* __restrict__ rec, unsigned* __restrict__ present, int* err) {
   const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (l >= T_local) return;
@@ -136,7 +155,15 @@ __global__ void k_eu_records(int64_t T_local, const int32_t* __restrict__ local_
   for (int k = 0; k < 4; ++k) {
     long long a = v[k == 0 ? 1 : 0], b = v[k <= 1 ? 2 : 1], cc = v[k <= 2 ? 3 : 2];
     sort3(a, b, cc);
-    c[10 + k] = ht_get(fkeys, fcnt, fmask, (unsigned long long)((a * V + b) * V + cc));
+    const long long h = ht_find(fkeys, fmask, (unsigned long long)((a * V + b) * V + cc));
+    c[10 + k] = h >= 0 ? fcnt[h] : 0u;
+    // face neighbour (4 t' + k'), -1 on the boundary or at a non-manifold face
+    int nb = -1;
+    if (h >= 0 && c[10 + k] == 2u) {
+      const int o0 = fown[2 * h], o1 = fown[2 * h + 1];
+      nb = o0 == (int)(4 * t + k) ? o1 : o0;
+    }
+    adj[4 * l + k] = nb;
   }
   c[14] = c[15] = 0u;
   unsigned w[4] = {0u, 0u, 0u, 0u};
@@ -191,17 +218,19 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
   hf <<= 1;
   cudaError_t e;
   if ((e = c->eu_tab.ensure((he + hf) * (sizeof(unsigned long long) + sizeof(unsigned)) +
-                            sizeof(unsigned) * (V > 0 ? V : 1))))
+                            sizeof(unsigned) * (V > 0 ? V : 1) + sizeof(int) * 2 * hf)))
     return e;
   unsigned long long* ekeys = c->eu_tab.as<unsigned long long>();
   unsigned long long* fkeys = ekeys + he;
   unsigned* ecnt = reinterpret_cast<unsigned*>(fkeys + hf);
   unsigned* fcnt = ecnt + he;
   unsigned* vcnt = fcnt + hf;
+  int* fown = reinterpret_cast<int*>(vcnt + (V > 0 ? V : 1));
   if ((e = cudaMemsetAsync(ekeys, 0xff, sizeof(unsigned long long) * (he + hf), c->stream))) return e;
   if ((e = cudaMemsetAsync(ecnt, 0, sizeof(unsigned) * (he + hf + (V > 0 ? V : 1)), c->stream)))
     return e;
   if ((e = c->eu_rec.ensure(sizeof(uint4) * (T_local > 0 ? T_local : 1)))) return e;
+  if ((e = c->eu_adj.ensure(sizeof(int) * 4 * (T_local > 0 ? T_local : 1)))) return e;
   if ((e = c->eu_A.ensure(sizeof(long long) * 256 + sizeof(unsigned) * 8 + sizeof(long long))))
     return e;
   unsigned* present = reinterpret_cast<unsigned*>(c->eu_A.as<long long>() + 257);
@@ -209,13 +238,13 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
   int* err = c->errw.as<int>();
   if (T_all > 0) {
     k_eu_count<<<nblk(T_all, 256), 256, 0, c->stream>>>(T_all, tets_all, V, vcnt, ekeys, ecnt,
-                                                        he - 1, fkeys, fcnt, hf - 1, err);
+                                                        he - 1, fkeys, fcnt, hf - 1, fown, err);
     ++c->launches;
   }
   if (T_local > 0) {
     k_eu_records<<<nblk(T_local, 256), 256, 0, c->stream>>>(
-        T_local, local_ids, tets_all, V, vcnt, ekeys, ecnt, he - 1, fkeys, fcnt, hf - 1,
-        c->eu_rec.as<uint4>(), present, err);
+        T_local, local_ids, tets_all, V, vcnt, ekeys, ecnt, he - 1, fkeys, fcnt, hf - 1, fown,
+        c->eu_adj.as<int>(), c->eu_rec.as<uint4>(), present, err);
     ++c->launches;
   }
   k_eu_lcm<<<1, 32, 0, c->stream>>>(present, c->eu_A.as<long long>(),
@@ -267,6 +296,154 @@ cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps) {
         reinterpret_cast<unsigned long long*>(rpc + N),
         reinterpret_cast<unsigned long long*>(rpc + N + E));
     ++c->launches;
+  }
+  return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------- CC numbers (NEXT-2)
+//
+// "we can trace their CC numbers using a simple traversal algorithm".  The
+// pieces of sphere i are the nodes of RPC(m_i); two pieces in tets sharing face f are joined
+// when f is an SoS facet of both (the perturbed cell meets f in a 2-face).  The radical facets
+// of m_i on h_ij are the nodes of RPF(m_i, m_j); two in face-adjacent tets are joined when both
+// have an edge on the shared face.  Union-find with atomic hooking of the larger root onto the
+// smaller (lock-free, the result is the same partition whatever the order), then one count
+// per root.
+
+__device__ __forceinline__ int uf_find(int* par, int x) {
+  while (true) {
+    const int y = par[x];
+    if (y == x) return x;
+    const int z = par[y];
+    if (z != y) par[x] = z;  // path halving (a benign race: z is an ancestor of x)
+    x = y;
+  }
+}
+
+__device__ void uf_union(int* par, int a, int b) {
+  while (true) {
+    a = uf_find(par, a);
+    b = uf_find(par, b);
+    if (a == b) return;
+    if (a < b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    if (atomicCAS(par + a, a, b) == a) return;
+  }
+}
+
+__global__ void k_cc_init(int64_t n, int* __restrict__ par) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < n) par[x] = (int)x;
+}
+
+// index in [lo, hi) of v in an ascending array, or -1
+__device__ __forceinline__ int find_sorted(const int32_t* a, int lo, int hi, int v) {
+  const int end = hi;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < end && a[lo] == v) ? lo : -1;
+}
+
+// one thread per tet: joins its pieces (and their radical facets) with the face neighbours'
+// of larger index
+__global__ void k_cc_link(int64_t T, const int* __restrict__ adj, const int32_t* __restrict__ poff,
+                          const int32_t* __restrict__ psph, const uint8_t* __restrict__ sfm,
+                          const int32_t* __restrict__ roff, const int32_t* __restrict__ rj,
+                          const uint8_t* __restrict__ rfm, int* __restrict__ par_c,
+                          int* __restrict__ par_f) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  if (p0 == p1) return;
+  for (int k = 0; k < 4; ++k) {
+    const int nb = adj[4 * t + k];
+    if (nb < 0 || (nb >> 2) < t) continue;  // each shared face once
+    const int t2 = nb >> 2, k2 = nb & 3;
+    const int q0 = poff[t2], q1 = poff[t2 + 1];
+    for (int q = p0; q < p1; ++q) {
+      const int i = psph[q];
+      const int q2 = find_sorted(psph, q0, q1, i);
+      if (q2 < 0) continue;
+      if (((sfm[q] >> k) & 1) && ((sfm[q2] >> k2) & 1)) uf_union(par_c, q, q2);
+      const int r20 = roff[q2], r21 = roff[q2 + 1];
+      for (int r = roff[q]; r < roff[q + 1]; ++r) {
+        if (!((rfm[r] >> k) & 1)) continue;
+        const int r2 = find_sorted(rj, r20, r21, rj[r]);
+        if (r2 >= 0 && ((rfm[r2] >> k2) & 1)) uf_union(par_f, r, r2);
+      }
+    }
+  }
+}
+
+// one thread per piece: a root piece counts one RPC component of its sphere, a root facet one
+// RPF component at the CSR entry of (i, j); comp = the root (smallest index of the component)
+__global__ void k_cc_count(int64_t n_pieces, const int32_t* __restrict__ psph,
+                           const int32_t* __restrict__ roff, const int32_t* __restrict__ rj,
+                           const int32_t* __restrict__ nbr_off,
+                           const int32_t* __restrict__ nbr_idx, int* __restrict__ par_c,
+                           int* __restrict__ par_f, int* __restrict__ rpc_cc,
+                           int* __restrict__ rpf_cc) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_pieces) return;
+  const int i = psph[q];
+  const int rc = uf_find(par_c, (int)q);
+  if (rc == q) atomicAdd(rpc_cc + i, 1);
+  const int e0 = nbr_off[i], e1 = nbr_off[i + 1];
+  for (int r = roff[q]; r < roff[q + 1]; ++r) {
+    if (uf_find(par_f, r) != r) continue;
+    const int e = find_sorted(nbr_idx, e0, e1, rj[r]);
+    if (e >= 0) atomicAdd(rpf_cc + e, 1);
+  }
+}
+
+// final labels (a second pass: roots are final once every union has returned)
+__global__ void k_cc_label(int64_t n, int* __restrict__ par) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < n) par[x] = uf_find(par, (int)x);
+}
+
+// cc_out layout: rpc_cc [N], rpf_cc [E]; cc_par: piece parents [n_pieces], facet parents [n_rpf]
+cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps) {
+  const int64_t N = c->st.N, E = c->st.E, T = ps.n_tets, np = ps.n_pieces, nr = ps.n_rpf;
+  cudaError_t e;
+  if ((e = c->cc_par.ensure(sizeof(int) * (np + nr + 1)))) return e;
+  if ((e = c->cc_out.ensure(sizeof(int) * (N + E + 1)))) return e;
+  int* par_c = c->cc_par.as<int>();
+  int* par_f = par_c + np;
+  int* rpc_cc = c->cc_out.as<int>();
+  if ((e = cudaMemsetAsync(rpc_cc, 0, sizeof(int) * (N + E + 1), c->stream))) return e;
+  if (np > 0) {  // (separate index spaces: pieces and radical facets)
+    k_cc_init<<<nblk(np, 256), 256, 0, c->stream>>>(np, par_c);
+    ++c->launches;
+  }
+  if (nr > 0) {
+    k_cc_init<<<nblk(nr, 256), 256, 0, c->stream>>>(nr, par_f);
+    ++c->launches;
+  }
+  if (T > 0 && np > 0) {
+    k_cc_link<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, c->eu_adj.as<int>(), ps.off.as<int32_t>(), ps.sphere.as<int32_t>(),
+        ps.sfm.as<uint8_t>(), ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(),
+        ps.rfm.as<uint8_t>(), par_c, par_f);
+    ++c->launches;
+    k_cc_count<<<nblk(np, 256), 256, 0, c->stream>>>(
+        np, ps.sphere.as<int32_t>(), ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(),
+        c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), par_c, par_f, rpc_cc,
+        rpc_cc + N);
+    ++c->launches;
+    k_cc_label<<<nblk(np, 256), 256, 0, c->stream>>>(np, par_c);
+    ++c->launches;
+    if (nr > 0) {
+      k_cc_label<<<nblk(nr, 256), 256, 0, c->stream>>>(nr, par_f);
+      ++c->launches;
+    }
   }
   return cudaGetLastError();
 }

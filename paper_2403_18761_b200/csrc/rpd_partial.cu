@@ -90,6 +90,7 @@ struct MergeSrc {
   const long long* p_eu;
   const int32_t *p_rpf_off, *p_rpf_j;
   const long long* p_rpf_e;
+  const uint8_t *p_sfm, *p_rfm;
 };
 
 __device__ inline MergeSrc pick(int d, const MergeSrc& o, const MergeSrc& n) {
@@ -122,6 +123,7 @@ struct MergeDst {
   long long* p_eu;
   int32_t *p_rpf_off, *p_rpf_j;
   long long* p_rpf_e;
+  uint8_t *p_sfm, *p_rfm;
 };
 
 constexpr int MT = 256;  // tets per merge tile (one block)
@@ -215,6 +217,8 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       const int nr = s_nr[nt] - s_nr[0], r_src = s_sr[0], r_dst = s_nr[0];
       const int rshift = s_nr[0] - s_sr[0];
       tile_copy(D.p_eu + p_dst, o.p_eu + p_src, npc, same);
+      tile_copy(D.p_sfm + p_dst, o.p_sfm + p_src, npc, same);
+      tile_copy(D.p_rfm + r_dst, o.p_rfm + r_src, nr, same);
       tile_copy(D.p_rpf_off + p_dst, o.p_rpf_off + p_src, npc,
                 [=](int32_t x) { return x + rshift; });
       tile_copy(D.p_rpf_j + r_dst, o.p_rpf_j + r_src, nr, same);
@@ -250,6 +254,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
     D.p_inc_off[q] = s_ni[l] + (s.p_inc_off[sp] - s_si[l]);
     if (eu) {
       D.p_eu[q] = s.p_eu[sp];
+      D.p_sfm[q] = s.p_sfm[sp];
       D.p_rpf_off[q] = s_nr[l] + (s.p_rpf_off[sp] - s_sr[l]);
     }
   }
@@ -261,6 +266,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       const int src = s_sr[l] + (r - s_nr[l]);
       D.p_rpf_j[r] = s.p_rpf_j[src];
       D.p_rpf_e[r] = s.p_rpf_e[src];
+      D.p_rfm[r] = s.p_rfm[src];
     }
   // incidences (a tet's incidences are contiguous in its source set)
   for (int r = s_ni[0] + threadIdx.x; r < s_ni[nt]; r += blockDim.x) {
@@ -282,7 +288,8 @@ static MergeSrc src_of(const CandSet& cs, const PieceSet& ps, bool eu) {
                   ps.inc.as<int32_t>(),     ps.vol.as<double>(),      ps.m1.as<double>(),
                   ps.fm.as<uint8_t>(),
                   eu ? ps.eu.as<long long>() : nullptr, ps.rpf_off.as<int32_t>(),
-                  ps.rpf_j.as<int32_t>(),   ps.rpf_e.as<long long>()};
+                  ps.rpf_j.as<int32_t>(),   ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
+                  ps.rfm.as<uint8_t>()};
 }
 
 // phase 0: per-tet counts and their scans (new cand offsets -> cn.off, new piece offsets ->
@@ -315,7 +322,8 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
              pn.inc.as<int32_t>(),     pn.vol.as<double>(),       pn.m1.as<double>(),
              pn.fm.as<uint8_t>(),      r_off,
              eu ? pn.eu.as<long long>() : nullptr, pn.rpf_off.as<int32_t>(),
-             pn.rpf_j.as<int32_t>(),   pn.rpf_e.as<long long>()};
+             pn.rpf_j.as<int32_t>(),   pn.rpf_e.as<long long>(), pn.sfm.as<uint8_t>(),
+             pn.rfm.as<uint8_t>()};
   if (T > 0) {
     k_merge_copy<<<nblk(T, MT), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
     ++c->launches;

@@ -25,7 +25,7 @@ FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
-            "rpd_download_euler"]
+            "rpd_download_euler", "rpd_get_topology", "rpd_download_topology"]
 
 
 class RPDError(RuntimeError):
@@ -46,6 +46,13 @@ class _Euler(C.Structure):
                 ("rpf_sphere", C.c_void_p), ("rpf_euler", C.c_void_p), ("rpc_sum", C.c_void_p),
                 ("rpf_sum", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64),
                 ("N", C.c_int64), ("E", C.c_int64)]
+
+
+class _Topology(C.Structure):
+    _fields_ = [("rpc_cc", C.c_void_p), ("rpf_cc", C.c_void_p), ("piece_comp", C.c_void_p),
+                ("rpf_comp", C.c_void_p), ("piece_sosfm", C.c_void_p), ("rpf_fm", C.c_void_p),
+                ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
+                ("E", C.c_int64)]
 
 
 class _Stats(C.Structure):
@@ -91,10 +98,13 @@ def load_library(path: str = LIB_PATH):
     L.rpd_set_euler.argtypes = [vp, vp, i64, i64, vp, i64, C.POINTER(i64)]
     L.rpd_get_euler.argtypes = [vp, C.POINTER(_Euler)]
     L.rpd_download_euler.argtypes = [vp] * 7
+    L.rpd_get_topology.argtypes = [vp, C.POINTER(_Topology)]
+    L.rpd_download_topology.argtypes = [vp] * 7
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
               "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
-              "rpd_get_euler", "rpd_download_euler"):
+              "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
+              "rpd_download_topology"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -284,6 +294,19 @@ class RPDContext:
                         "rpf_sum"], arrs))
         out["euler_denom"] = int(e.denom)
         return out
+
+    def download_topology(self, device=False) -> dict:
+        """CC numbers of the current pieces: rpc_cc [N], rpf_cc [E]
+        (row-sorted CSR), component labels piece_comp / rpf_comp and the SoS facet flags
+        piece_sosfm / rpf_fm.  Needs Euler mode with the whole mesh in the ctx."""
+        t = _Topology()
+        self._check(self.L.rpd_get_topology(self.h, C.byref(t)))
+        specs = [(t.N, np.int32), (t.E, np.int32), (t.n_pieces, np.int32), (t.n_rpf, np.int32),
+                 (t.n_pieces, np.uint8), (t.n_rpf, np.uint8)]
+        arrs = self._alloc(specs, device)
+        self._check(self.L.rpd_download_topology(self.h, *[self._p(a) for a in arrs]))
+        return dict(zip(["rpc_cc", "rpf_cc", "piece_comp", "rpf_comp", "piece_sosfm", "rpf_fm"],
+                        arrs))
 
     def stats(self) -> dict:
         s = _Stats()

@@ -174,3 +174,112 @@ def test_euler_c3_sampled(ctx):
     assert np.all(got["rpc_sum"] % L == 0) and np.all(got["rpf_sum"] % L == 0)
     chi = got["rpc_sum"] // L
     assert np.sum(chi == 1) > 0.5 * np.sum(chi != 0)
+
+
+# ----------------------------------------------------------------------------- CC numbers
+# SURVEY.md §8(f) NEXT-2
+
+
+def run_gpu_topology(ctx, w):
+    ctx.set_euler(w.tets, len(w.verts))
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        out = ctx.download_pieces()
+        out.update(ctx.download_euler())
+        out.update(ctx.download_topology())
+    finally:
+        ctx.set_euler(None, 0)
+    return out
+
+
+def check_topology(got, ref, w):
+    assert np.array_equal(got["piece_sosfm"], ref["piece_sosfm"])
+    assert np.array_equal(got["rpf_fm"], ref["rpf_fm"])
+    rpc_cc, rpf_cc = oracle.topology(ref, w.tets, w.N)
+    assert got["rpc_cc"].tolist() == rpc_cc
+    for i in range(w.N):
+        for e in range(w.nbr_off[i], w.nbr_off[i + 1]):
+            assert got["rpf_cc"][e] == rpf_cc.get((i, int(w.nbr_idx[e])), 0)
+    # component labels: one root per component, labels are roots of the same sphere's pieces
+    roots = got["piece_comp"] == np.arange(len(got["piece_comp"]))
+    assert roots.sum() == sum(rpc_cc)
+    assert np.array_equal(got["piece_sphere"][got["piece_comp"]], got["piece_sphere"])
+
+
+@pytest.mark.parametrize("make", MAKERS)
+def test_topology_parity(ctx, make):
+    w = make()
+    got = run_gpu_topology(ctx, w)
+    check_topology(got, oracle.rpd_workload(w, euler=True), w)
+
+
+@pytest.mark.parametrize("xs,rpc,rpf", [([20.0, 44.0], [1, 1], 2),
+                                        ([26.0, 32.0, 38.0], [1, 2, 1], 2)])
+def test_topology_paper_figures(ctx, xs, rpc, rpf):
+    """PAPER.md Fig. 4(b) (torus, two spheres: RPF CC = 2) and Fig. 6(a) (the middle sphere's
+    RPC cut by the hole: CC = 2) on the genus-1 box with a hole."""
+    import copy
+    w = copy.copy(W.make_shape_workload("one", 700, 1, seed=2, cache=False))
+    n = len(xs)
+    w.spheres = np.array([[x, 26.0, 20.0, 1.0] for x in xs])
+    idx, off = [], [0]
+    for a in range(n):
+        idx += [b for b in (a - 1, a + 1) if 0 <= b < n]
+        off.append(len(idx))
+    w.nbr_off, w.nbr_idx = np.array(off, np.int32), np.array(idx, np.int32)
+    got = run_gpu_topology(ctx, w)
+    assert got["rpc_cc"].tolist() == rpc
+    assert np.all(got["rpf_cc"] == rpf)
+    assert (got["rpc_sum"] // got["euler_denom"]).tolist() == rpc  # contractible components
+
+
+def test_topology_after_partial_update(ctx):
+    w = W.make_shape_workload("S", 2000, 150, seed=3, n_batches=2, batch_m=12, clusters=3,
+                              cache=False)
+    ctx.set_euler(w.tets, len(w.verts))
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        prev = oracle.rpd_workload(w, euler=True)
+        n_old = w.N
+        import copy
+        for (sph, off, idx) in w.batches:
+            ctx.update_partial(sph, off, idx, np.arange(n_old, len(sph), dtype=np.int32))
+            got = ctx.download_pieces()
+            got.update(ctx.download_topology())
+            part, _ = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old,
+                                            euler=True)
+            w2 = copy.copy(w)
+            w2.spheres, w2.nbr_off, w2.nbr_idx = sph, off, idx
+            check_topology(got, part, w2)
+            prev, n_old = part, len(sph)
+    finally:
+        ctx.set_euler(None, 0)
+
+
+def test_topology_needs_whole_mesh(ctx):
+    import paper_2403_18761_b200 as P
+    w = W.make_c1(0)
+    ids = np.arange(3, dtype=np.int32)
+    ctx.set_euler(w.tets, len(w.verts), ids)
+    try:
+        ctx.relations(w.verts, w.tets[ids], w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        with pytest.raises(P.RPDError) as e:
+            ctx.download_topology()
+        assert e.value.status == -5
+    finally:
+        ctx.set_euler(None, 0)
+
+
+def test_topology_c3(ctx):
+    """At full C3 size: every sphere with pieces has >= 1 component, labels consistent, and
+    most cells are connected (CC = 1)."""
+    w = W.make_config("C3")
+    got = run_gpu_topology(ctx, w)
+    has = np.bincount(got["piece_sphere"], minlength=w.N) > 0
+    assert np.all((got["rpc_cc"] > 0) == has)
+    roots = got["piece_comp"] == np.arange(len(got["piece_comp"]))
+    assert roots.sum() == got["rpc_cc"].sum()
+    assert np.mean(got["rpc_cc"][has] == 1) > 0.9
