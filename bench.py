@@ -371,6 +371,19 @@ def main():
                 st = ctx.stats()
                 e_full.append(ev0.elapsed_time(ev1))
                 e_clip.append(st["clip_ms"])
+        cc_ms = None
+        if world == 1:  # CC numbers (NEXT-2) need the whole mesh in one ctx
+            cc = []
+            for s in range(args.warmup + args.steps):
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                ctx.topology()
+                ev1.record()
+                torch.cuda.synchronize()
+                if s >= args.warmup:
+                    cc.append(ev0.elapsed_time(ev1))
+            cc_ms = float(np.median(cc))
+            topo = ctx.download_topology()
         eu = ctx.download_euler(device=True)
         if world > 1:
             eu = allreduce_euler(eu)
@@ -387,8 +400,12 @@ def main():
                  "denominator": int(L), "rpc_sums_integral": integral,
                  "spheres_with_cells": int(np.sum(chi != 0)),
                  "rpc_euler_eq_1": int(np.sum(chi == 1)),
+                 "cc_ms": cc_ms,
+                 "rpc_cc_eq_1": int(np.sum(topo["rpc_cc"] == 1)) if cc_ms is not None else None,
+                 "rpc_cc_gt_1": int(np.sum(topo["rpc_cc"] > 1)) if cc_ms is not None else None,
                  "note": "fractional Euler characteristics (PAPER.md:482-506) fused into the "
-                         "clip; full_rpd_ms = relations + clip + per-sphere sums (CUDA events)"}
+                         "clip; full_rpd_ms = relations + clip + per-sphere sums (CUDA events); "
+                         "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find)"}
 
     # ---- roofline of the dominant kernel
     fmed = float(np.median([r["filter_ms"] for r in recs]))

@@ -126,6 +126,7 @@ struct rpd_ctx {
 
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
+  rpd::DevBuf cand_long;   // compaction: count + tets with more than 16 candidates
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
   rpd::DevBuf bvh_all;     // leaf + super boxes of the whole mesh (valid per staged mesh)
   bool bvh_all_valid = false;

@@ -96,6 +96,17 @@ constexpr int BVH_LEAF = 32;    // tets per leaf (one warp)
 constexpr int BVH_FAN = 32;     // leaves per super node
 constexpr int BVH_PCAP = 64;    // planes of a sphere staged in shared memory (super level)
 constexpr int BVH_LCAP = 256;   // planes staged per warp in the leaf kernel
+// work distribution of the BVH kernels: 1 = contiguous item ranges per warp (staged planes
+// reused across consecutive items of one sphere), 0 = grid-stride (better load balance)
+#ifndef RPD_BVH_CONTIG_TOP
+#define RPD_BVH_CONTIG_TOP 1
+#endif
+#ifndef RPD_BVH_CONTIG_SUPER
+#define RPD_BVH_CONTIG_SUPER 0
+#endif
+#ifndef RPD_BVH_CONTIG_LEAF
+#define RPD_BVH_CONTIG_LEAF 0
+#endif
 
 // exact lattice AABB of every leaf (32 consecutive tets of the list)
 __global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
@@ -191,7 +202,10 @@ __device__ __forceinline__ void stage_planes(double4* __restrict__ sp,
 constexpr int BVH_WARPS = 4;
 
 // phase 1: one warp per (sphere, chunk of 32 super nodes) tests the super-node boxes and queues
-// (sphere, super node) items; a sphere with a huge cell becomes many items (load balance)
+// (sphere, super node) items; a sphere with a huge cell becomes many items (load balance).
+// Every warp takes a contiguous range of the (sphere, chunk) work so that consecutive chunks
+// share the sphere's staged planes (staged once per sphere per warp, not once per chunk), and
+// skips the rest of a hidden sphere's chunks at once.
 __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_top(
     const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
@@ -206,17 +220,25 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_top(
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_work = (int64_t)(hi - lo) * n_chunk;
-  int cur_i = -1;
-  for (int64_t w = gw; w < n_work; w += nw) {
+  const int64_t per = RPD_BVH_CONTIG_TOP ? (n_work + nw - 1) / nw : 1;
+  const int64_t w_end = RPD_BVH_CONTIG_TOP ? min(n_work, (gw + 1) * per) : n_work;
+  const int64_t w_step = RPD_BVH_CONTIG_TOP ? 1 : nw;
+  int cur_i = -1, k = 0;
+  for (int64_t w = gw * per; w < w_end; w += w_step) {
     const int64_t ii = lo + w / n_chunk;
     const int64_t s = (w % n_chunk) * 32 + lane;
     const int i = list ? list[ii] : (int)ii;
-    const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
-    const int k = e1 - e0;
-    if (k == 0 && N != 1) continue;  // hidden sphere (R4): relates to no tet
     if (i != cur_i) {
-      stage_planes(sp, planes + e0, k);
+      const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
+      k = e1 - e0;
       cur_i = i;
+      if (k == 0 && N != 1) {  // hidden sphere (R4): relates to no tet
+        if (RPD_BVH_CONTIG_TOP) w = (w / n_chunk + 1) * n_chunk - 1;  // its other chunks
+        continue;
+      }
+      stage_planes(sp, planes + e0, k);
+    } else if (k == 0 && N != 1) {
+      continue;
     }
     const bool ok = box_passes_w(sup + 6 * s, s < n_sup, sp, k);
     const unsigned sm = __ballot_sync(FULL, ok);
@@ -245,8 +267,12 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
   const int n_sitems = min(*n_sitems_p, cap_sitems);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // contiguous item ranges per warp (RPD_BVH_CONTIG_SUPER): the items of one sphere are
+  // queued in runs, so the staged planes are reused across consecutive items
+  const int64_t per = RPD_BVH_CONTIG_SUPER ? (n_sitems + nw - 1) / nw : 1;
+  const int64_t it_end = RPD_BVH_CONTIG_SUPER ? min((int64_t)n_sitems, (gw + 1) * per) : n_sitems;
   int cur_i = -1;
-  for (int64_t it = gw; it < n_sitems; it += nw) {
+  for (int64_t it = gw * per; it < it_end; it += RPD_BVH_CONTIG_SUPER ? 1 : nw) {
     const int2 item = sitems[it];
     const int i = item.x;
     const int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
@@ -286,8 +312,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
   const int n_items = min(*n_items_p, cap_items);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t per = RPD_BVH_CONTIG_LEAF ? (n_items + nw - 1) / nw : 1;  // (see k_bvh_super)
+  const int64_t it_end = RPD_BVH_CONTIG_LEAF ? min((int64_t)n_items, (gw + 1) * per) : n_items;
   int cur_i = -1;
-  for (int64_t it = gw; it < n_items; it += nw) {
+  for (int64_t it = gw * per; it < it_end; it += RPD_BVH_CONTIG_LEAF ? 1 : nw) {
 #ifdef RPD_DEBUG_BVH
     const long long t_start = clock64();
     int dbg_leaves = 0, dbg_cross = 0;
@@ -405,19 +433,80 @@ __global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
 
 // ------------------------------------------------------------------ compaction
 
-// one warp per tet: its candidate ids (distinct) are rank-sorted ascending (the BVH filter
-// appends in arbitrary order) and written coalesced; then the incidence-word offsets of the
-// pairs are a running warp scan in sorted order
-__global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ k_tet,
+// Candidate ids of a tet (distinct) sorted ascending (the BVH filter appends them in arbitrary
+// order) with the incidence-mask word offsets of the pairs in sorted order.
+// One thread per tet (most lists are short: k_tet mean 2-4, p99 ~11): the tet's slab entries
+// are loaded into registers (<= CC_REG of them), each one's rank among them (and the prefix of
+// the incidence-mask words of the smaller ids) counted by compare loops, and written to its
+// sorted position -- no warp-wide shuffles for lists of one or two entries.  Longer lists go
+// to a warp each (second kernel).
+constexpr int CC_REG = 16;
+__global__ void __launch_bounds__(256) k_compact_cands_t(
+    int64_t n, int cap, const int32_t* __restrict__ k_tet, const int32_t* __restrict__ slab,
+    const int32_t* __restrict__ cand_off, int32_t* __restrict__ cand_idx,
+    int32_t* __restrict__ pair_tet, const int32_t* __restrict__ w_off,
+    int32_t* __restrict__ p_moff, const int32_t* __restrict__ nbr_off, int64_t n_pairs,
+    int32_t* __restrict__ long_list, int* __restrict__ n_long) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int k = min(k_tet[a], cap);
+  const int32_t* s = slab + a * cap;
+  const int o = cand_off[a];
+  const int w0 = w_off ? w_off[a] : 0;
+  if (k <= CC_REG) {
+    int v[CC_REG], wd[CC_REG];
+#pragma unroll
+    for (int m = 0; m < CC_REG; ++m) {
+      v[m] = m < k ? __ldg(s + m) : INT_MAX;
+      wd[m] = 0;
+    }
+    if (p_moff) {
+#pragma unroll
+      for (int m = 0; m < CC_REG; ++m)
+        if (m < k) wd[m] = (__ldg(nbr_off + v[m] + 1) - __ldg(nbr_off + v[m]) + 31) >> 5;
+    }
+#pragma unroll
+    for (int j = 0; j < CC_REG; ++j) {
+      if (j >= k) break;
+      int rank = 0, pre = 0;
+#pragma unroll
+      for (int m = 0; m < CC_REG; ++m) {
+        const bool lt = v[m] < v[j];
+        rank += lt;
+        pre += lt ? wd[m] : 0;
+      }
+      cand_idx[o + rank] = v[j];
+      if (pair_tet) pair_tet[o + rank] = (int32_t)a;
+      if (p_moff) p_moff[o + rank] = w0 + pre;
+    }
+  } else {  // a long list: one warp per tet in k_compact_cands_w (rare)
+    long_list[atomicAdd(n_long, 1)] = (int32_t)a;
+  }
+  if (p_moff && a == n - 1) {  // terminal word offset
+    int tot = 0;
+    for (int m = 0; m < k; ++m) {
+      const int vm = s[m];
+      tot += (__ldg(nbr_off + vm + 1) - __ldg(nbr_off + vm) + 31) >> 5;
+    }
+    p_moff[n_pairs] = w0 + tot;
+  }
+}
+
+// the long lists: rank-sorted by a warp each (their ids distinct), then the incidence-word
+// offsets of the pairs by a running warp scan in sorted order
+__global__ void k_compact_cands_w(const int32_t* __restrict__ list, const int* __restrict__ n_list,
+                                  int64_t n, int cap, const int32_t* __restrict__ k_tet,
                                 const int32_t* __restrict__ slab,
                                 const int32_t* __restrict__ cand_off,
                                 int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
                                 const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
                                 const int32_t* __restrict__ nbr_off, int64_t n_pairs) {
-  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (a >= n) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nl = *n_list;
+  for (int64_t li = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; li < nl; li += nw) {
+  const int64_t a = list[li];
   const int k = min(k_tet[a], cap);
   const int32_t* s = slab + a * cap;
   const int o = cand_off[a];
@@ -435,7 +524,7 @@ __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ 
       if (pair_tet) pair_tet[o + rank] = (int32_t)a;
     }
   }
-  if (!p_moff) return;
+  if (!p_moff) continue;
   __syncwarp();
   int w = w_off ? w_off[a] : 0;
   for (int r0 = 0; r0 < k; r0 += 32) {
@@ -454,8 +543,10 @@ __global__ void k_compact_cands(int64_t n, int cap, const int32_t* __restrict__ 
     if (j < k) p_moff[o + j] = w + x - words;
     w += __shfl_sync(FULL, x, 31);
   }
-  if (a == n - 1 && lane == 0) p_moff[n_pairs] = w;
+  __syncwarp();
+  }  // (the terminal word offset is written by k_compact_cands_t)
 }
+
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
@@ -630,10 +721,20 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
     if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
     return cudaSuccess;
   }
-  k_compact_cands<<<nblk(n * 32, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off, cand_idx,
-                                                       pair_tet, w_off, p_moff,
-                                                       c->st.nbr_off.as<int32_t>(), n_pairs);
-  ++c->launches;
+  cudaError_t e = c->cand_long.ensure(sizeof(int32_t) * (n + 1));
+  if (e) return e;
+  int* n_long = c->cand_long.as<int>();
+  int32_t* long_list = c->cand_long.as<int32_t>() + 1;
+  if ((e = cudaMemsetAsync(n_long, 0, sizeof(int), c->stream))) return e;
+  k_compact_cands_t<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off,
+                                                        cand_idx, pair_tet, w_off, p_moff,
+                                                        c->st.nbr_off.as<int32_t>(), n_pairs,
+                                                        long_list, n_long);
+  // (grid for every list, exits on the device count: long lists are rare)
+  k_compact_cands_w<<<(unsigned)c->sms * 4, 256, 0, c->stream>>>(
+      long_list, n_long, n, cap, k_tet, slab, cand_off, cand_idx, pair_tet, w_off, p_moff,
+      c->st.nbr_off.as<int32_t>(), n_pairs);
+  c->launches += 2;
   return cudaGetLastError();
 }
 

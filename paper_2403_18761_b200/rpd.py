@@ -295,6 +295,12 @@ class RPDContext:
         out["euler_denom"] = int(e.denom)
         return out
 
+    def topology(self):
+        """Run the CC-number kernels on the current pieces (results stay on the device)."""
+        t = _Topology()
+        self._check(self.L.rpd_get_topology(self.h, C.byref(t)))
+        return t
+
     def download_topology(self, device=False) -> dict:
         """CC numbers of the current pieces: rpc_cc [N], rpf_cc [E]
         (row-sorted CSR), component labels piece_comp / rpf_comp and the SoS facet flags
