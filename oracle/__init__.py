@@ -65,6 +65,7 @@ class _Result(C.Structure):
                 ("rpf_off", C.POINTER(C.c_int32)), ("rpf_sphere", C.POINTER(C.c_int32)),
                 ("rpf_euler", C.POINTER(C.c_int64)),
                 ("piece_sosfm", C.POINTER(C.c_uint8)), ("rpf_fm", C.POINTER(C.c_uint8)),
+                ("rpf_adj", C.POINTER(C.c_uint64)),
                 ("n_rpf", C.c_int64),
                 ("n_rel_tests", C.c_int64), ("n_clip_tests", C.c_int64),
                 ("n_constructions", C.c_int64), ("n_fan_triangles", C.c_int64),
@@ -159,7 +160,8 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
                         "rpf_sphere": arr(r.rpf_sphere, r.n_rpf, np.int32),
                         "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64),
                         "piece_sosfm": arr(r.piece_sosfm, r.n_pieces, np.uint8),
-                        "rpf_fm": arr(r.rpf_fm, r.n_rpf, np.uint8)})
+                        "rpf_fm": arr(r.rpf_fm, r.n_rpf, np.uint8),
+                        "rpf_adj": arr(r.rpf_adj, r.n_rpf, np.uint64)})
     finally:
         L.oracle_free(rp)
     return out
@@ -225,7 +227,8 @@ def per_tet_lists(res, T):
                       tuple(res["rpf_sphere"][ro[p]:ro[p + 1]].tolist()),
                       tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()),
                       int(res["piece_sosfm"][p]),
-                      tuple(res["rpf_fm"][ro[p]:ro[p + 1]].tolist()))
+                      tuple(res["rpf_fm"][ro[p]:ro[p + 1]].tolist()),
+                      tuple(res["rpf_adj"][ro[p]:ro[p + 1]].tolist()))
             pcs.append((int(res["piece_sphere"][p]), float(res["piece_vol"][p]),
                         tuple(res["piece_m1"][p].tolist()), int(res["piece_facemask"][p]),
                         tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist()), eu))
@@ -236,7 +239,7 @@ def per_tet_lists(res, T):
 def from_per_tet_lists(L):
     cand_off = [0]
     cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
-    pe, rpf_off, rpf_j, rpf_e, sfm, rfm = [], [0], [], [], [], []
+    pe, rpf_off, rpf_j, rpf_e, sfm, rfm, radj = [], [0], [], [], [], [], []
     for cands, pcs in L:
         cand_idx += cands
         cand_off.append(len(cand_idx))
@@ -253,13 +256,15 @@ def from_per_tet_lists(L):
                 rpf_e += list(eu[2])
                 sfm.append(eu[3])
                 rfm += list(eu[4])
+                radj += list(eu[5])
                 rpf_off.append(len(rpf_j))
         piece_off.append(len(ps))
     eul = {}
     if len(pe) == len(ps) and len(rpf_off) == len(ps) + 1:
         eul = {"piece_euler": np.array(pe, np.int64), "rpf_off": np.array(rpf_off, np.int32),
                "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64),
-               "piece_sosfm": np.array(sfm, np.uint8), "rpf_fm": np.array(rfm, np.uint8)}
+               "piece_sosfm": np.array(sfm, np.uint8), "rpf_fm": np.array(rfm, np.uint8),
+               "rpf_adj": np.array(radj, np.uint64)}
     return {**eul, "cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
             "piece_off": np.array(piece_off, np.int32), "piece_sphere": np.array(ps, np.int32),
             "piece_vol": np.array(pv, np.float64),
@@ -376,6 +381,25 @@ def topology(res, tets, N):
             else:
                 rpf_cc[(x[1], x[2])] = rpf_cc.get((x[1], x[2]), 0) + 1
     return rpc_cc, rpf_cc
+
+
+def medial_mesh(res):
+    """The dual medial mesh of the RPD: a vertex per sphere with a cell, an
+    edge e_ij per restricted power face RPF(m_i, m_j) and a triangle f_ijk per restricted power
+    edge RPE(m_i, m_j, m_k) -- an edge of a piece of m_i lying on the radical planes of m_j and
+    m_k (symbolically perturbed pieces).  Seen from every sphere's pieces and merged: sorted
+    unique (i, j) with i < j and (i, j, k) with i < j < k."""
+    edges, faces = set(), set()
+    ro = res["rpf_off"]
+    for q, i in enumerate(res["piece_sphere"].tolist()):
+        js = res["rpf_sphere"][ro[q]:ro[q + 1]].tolist()
+        adj = res["rpf_adj"][ro[q]:ro[q + 1]].tolist()
+        for a, j in enumerate(js):
+            edges.add((min(i, j), max(i, j)))
+            for b in range(a + 1, len(js)):
+                if (int(adj[a]) >> b) & 1:
+                    faces.add(tuple(sorted((i, j, js[b]))))
+    return sorted(edges), sorted(faces)
 
 
 def max_threads() -> int:

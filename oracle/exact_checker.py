@@ -301,3 +301,31 @@ def explicit_cc(verts, tets, spheres, nbr_off, nbr_idx, i):
     for j, facet_edges in per_j.items():
         rpf[j] = components(facet_edges, facet_edges)
     return rpc, rpf, generic
+
+
+def explicit_medial_faces(verts, tets, spheres, nbr_off, nbr_idx):
+    """Triangles (i, j, k) of the dual medial mesh from the exact pieces (no SoS): sphere i's
+    piece has an edge of positive length on both radical planes h_ij and h_ik."""
+    sph_X = [tuple(_lat(s[c]) for c in range(4)) for s in spheres]
+    faces = set()
+    generic = True
+    for i in range(len(spheres)):
+        S = [int(j) for j in nbr_idx[nbr_off[i]:nbr_off[i + 1]]]
+        if not S and len(spheres) > 1:
+            continue
+        for t in range(len(tets)):
+            tet_X = [tuple(_lat(verts[v][c]) for c in range(3)) for v in tets[t]]
+            cell = exact_piece_cells(tet_X, sph_X, i, S)
+            if cell is None:
+                continue
+            generic &= cell["generic"]
+            pls = planes_for(tet_X, sph_X, i, S)
+            act = {v: frozenset(k for k, pl in enumerate(pls) if _val(pl, v) == 0)
+                   for v in cell["vertices"]}
+            for e in cell["edges"]:
+                u, w = tuple(e)
+                rad = sorted(pls[k][2][1] for k in act[u] & act[w] if pls[k][2][0] == "r")
+                for a in range(len(rad)):
+                    for b in range(a + 1, len(rad)):
+                        faces.add(tuple(sorted((i, rad[a], rad[b]))))
+    return sorted(faces), generic

@@ -168,6 +168,8 @@ typedef struct {
   int64_t* rpf_euler;            /* [n_rpf] Euler of the piece's facet on h_ij */
   uint8_t* piece_sosfm;          /* [n_pieces] tet faces that are facets of the piece (SoS) */
   uint8_t* rpf_fm;               /* [n_rpf] tet faces the radical facet has an edge on (SoS) */
+  uint64_t* rpf_adj;             /* [n_rpf] the piece's radical facets (bit = rank by ascending
+                                    j) this one shares an edge with: restricted power edges */
   int64_t n_rpf;
   /* instrumentation (C1 step 9) */
   int64_t n_rel_tests, n_clip_tests, n_constructions, n_fan_triangles, n_zero_hits;
@@ -578,6 +580,7 @@ typedef struct {
   int32_t* rpf_j;     /* radical facets of the piece (neighbour j) ... */
   int64_t* rpf_e;     /* ... and the fractional Euler characteristic of each, over L */
   uint8_t* rpf_fm;    /* ... and the tet faces it has an edge on */
+  uint64_t* rpf_adj;  /* ... and the radical facets it shares an edge with (by rank) */
   int32_t nrpf;
   uint8_t sosfm;      /* tet faces among the piece's facets */
 } piece_t;
@@ -611,6 +614,8 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
   int* is_facet = (int*)calloc(npl, sizeof(int));
   int64_t* fe = (int64_t*)calloc(npl, sizeof(int64_t)); /* Euler of each facet */
   unsigned* ffm = (unsigned*)calloc(npl, sizeof(unsigned)); /* tet faces sharing an edge */
+  int32_t* rre = (int32_t*)malloc(sizeof(int32_t) * 2 * (3 * nv / 2 + 1)); /* radical-radical edges */
+  int nrre = 0;
   for (int v = 0; v < nv; ++v) {
     int64_t pv = carrier_payload(A14, L, faces_of(P, P->v[v].p, 3));
     chi += pv;
@@ -630,6 +635,12 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
       /* topology (NEXT-2): an edge between facet x and tet face k joins x to face k */
       for (int a = 0; a < 2; ++a)
         if (P->pl[e[1 - a]].src < 0) ffm[e[a]] |= 1u << (-1 - P->pl[e[1 - a]].src);
+      /* an edge on two radical planes: a restricted power edge RPE(m_i, m_j, m_k) */
+      if (P->pl[e[0]].src >= 0 && P->pl[e[1]].src >= 0) {
+        rre[2 * nrre] = e[0];
+        rre[2 * nrre + 1] = e[1];
+        ++nrre;
+      }
     }
   int nr = 0;
   out->sosfm = 0;
@@ -641,26 +652,39 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
     if (P->pl[f].src >= 0) ++nr;
     else out->sosfm |= (uint8_t)(1u << (-1 - P->pl[f].src));
   }
-  int64_t* pairs = (int64_t*)malloc(sizeof(int64_t) * 3 * (nr > 0 ? nr : 1));
+  int64_t* pairs = (int64_t*)malloc(sizeof(int64_t) * 4 * (nr > 0 ? nr : 1));
   int m = 0;
   for (int f = 0; f < npl; ++f)
     if (is_facet[f] && P->pl[f].src >= 0) {
-      pairs[3 * m] = P->pl[f].src;
-      pairs[3 * m + 1] = fe[f];
-      pairs[3 * m + 2] = ffm[f];
+      pairs[4 * m] = P->pl[f].src;
+      pairs[4 * m + 1] = fe[f];
+      pairs[4 * m + 2] = ffm[f];
+      pairs[4 * m + 3] = f;
       ++m;
     }
-  qsort(pairs, nr, 3 * sizeof(int64_t), cmp_rpf);
+  qsort(pairs, nr, 4 * sizeof(int64_t), cmp_rpf);
+  int* rank_of = (int*)malloc(sizeof(int) * npl);
+  for (int k = 0; k < nr; ++k) rank_of[pairs[4 * k + 3]] = k;
   out->euler = chi;
   out->nrpf = nr;
   out->rpf_j = (int32_t*)malloc(sizeof(int32_t) * (nr > 0 ? nr : 1));
   out->rpf_e = (int64_t*)malloc(sizeof(int64_t) * (nr > 0 ? nr : 1));
   out->rpf_fm = (uint8_t*)malloc(nr > 0 ? nr : 1);
+  out->rpf_adj = (uint64_t*)calloc(nr > 0 ? nr : 1, sizeof(uint64_t));
   for (int k = 0; k < nr; ++k) {
-    out->rpf_j[k] = (int32_t)pairs[3 * k];
-    out->rpf_e[k] = pairs[3 * k + 1];
-    out->rpf_fm[k] = (uint8_t)pairs[3 * k + 2];
+    out->rpf_j[k] = (int32_t)pairs[4 * k];
+    out->rpf_e[k] = pairs[4 * k + 1];
+    out->rpf_fm[k] = (uint8_t)pairs[4 * k + 2];
   }
+  for (int k = 0; k < nrre; ++k) {
+    int a = rank_of[rre[2 * k]], b = rank_of[rre[2 * k + 1]];
+    if (a < 64 && b < 64) {
+      out->rpf_adj[a] |= (uint64_t)1 << b;
+      out->rpf_adj[b] |= (uint64_t)1 << a;
+    }
+  }
+  free(rank_of);
+  free(rre);
   free(pairs);
   free(ffm);
   free(fe);
@@ -837,6 +861,7 @@ static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piec
     out->rpf_j = NULL;
     out->rpf_e = NULL;
     out->rpf_fm = NULL;
+    out->rpf_adj = NULL;
     out->sosfm = 0;
     if (A14) piece_euler(&P, A14, Lden, out);
   }
@@ -877,6 +902,7 @@ void oracle_free(oracle_result* r) {
   free(r->rpf_euler);
   free(r->piece_sosfm);
   free(r->rpf_fm);
+  free(r->rpf_adj);
   free(r);
 }
 
@@ -947,6 +973,7 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
   R->rpf_euler = (int64_t*)malloc(sizeof(int64_t) * (nr ? nr : 1));
   R->piece_sosfm = (uint8_t*)malloc(np ? np : 1);
   R->rpf_fm = (uint8_t*)malloc(nr ? nr : 1);
+  R->rpf_adj = (uint64_t*)malloc(sizeof(uint64_t) * (nr ? nr : 1));
   R->rpf_off[0] = 0;
   int64_t r0 = 0;
   R->n_cand = nc;
@@ -984,12 +1011,14 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
         memcpy(R->rpf_sphere + r0, pc->rpf_j, sizeof(int32_t) * pc->nrpf);
         memcpy(R->rpf_euler + r0, pc->rpf_e, sizeof(int64_t) * pc->nrpf);
         memcpy(R->rpf_fm + r0, pc->rpf_fm, pc->nrpf);
+        memcpy(R->rpf_adj + r0, pc->rpf_adj, sizeof(uint64_t) * pc->nrpf);
       }
       r0 += pc->nrpf;
       R->rpf_off[p0 + 1] = (int32_t)r0;
       free(pc->rpf_j);
       free(pc->rpf_e);
       free(pc->rpf_fm);
+      free(pc->rpf_adj);
       ++p0;
       R->inc_off[p0] = (int32_t)i0;
       free(pc->inc);

@@ -461,3 +461,38 @@ def test_cc_equals_explicit_extraction(make):
         assert generic
         assert rpc_cc[i] == e_rpc, i
         assert {j: v for (a, j), v in rpf_cc.items() if a == i} == e_rpf, i
+
+
+# ----------------------------------------------------------------------------- medial mesh
+# the dual medial mesh
+
+
+def test_medial_mesh_three_spheres_one_triangle():
+    """PAPER.md:353-357 (Fig. 2): the RPD of three spheres -- three cells meeting along one
+    restricted power edge inside the solid -- is dual to one triangle with its three edges."""
+    verts, tets = W.kuhn_grid_mesh((2, 2, 2), 512, (0, 0, 0), morton=False)
+    sph = np.array([[0.25, 0.25, 0.5, 0.0], [0.75, 0.3125, 0.5, 0.0], [0.4375, 0.75, 0.5, 0.0]])
+    off = np.array([0, 2, 4, 6], np.int32)
+    idx = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    r = oracle.rpd(verts, tets, sph, off, idx, euler=True)
+    edges, faces = oracle.medial_mesh(r)
+    assert edges == [(0, 1), (0, 2), (1, 2)] and faces == [(0, 1, 2)]
+    rpc_cc, rpf_cc = oracle.topology(r, tets, 3)
+    assert rpc_cc == [1, 1, 1] and set(rpf_cc.values()) == {1}
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(3),
+                                  lambda: W.random_tiny(0, n_spheres=14, grid=2),
+                                  lambda: W.random_tiny(2, n_spheres=14, grid=2)])
+def test_medial_faces_equal_explicit_extraction(make):
+    """Triangles of the medial mesh = the restricted power edges found in the exact pieces
+    (edges of positive length on two radical planes), on generic inputs."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    _, faces = oracle.medial_mesh(r)
+    e_faces, generic = X.explicit_medial_faces(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+    assert generic and faces == e_faces
+    # every triangle's three edges are medial edges
+    edges = set(oracle.medial_mesh(r)[0])
+    for (i, j, k) in faces:
+        assert {(i, j), (i, k), (j, k)} <= edges
