@@ -384,6 +384,14 @@ def main():
                     cc.append(ev0.elapsed_time(ev1))
             cc_ms = float(np.median(cc))
             topo = ctx.download_topology()
+            mm = []
+            for s in range(args.warmup + args.steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                med = ctx.medial_mesh(device=True)
+                torch.cuda.synchronize()
+                if s >= args.warmup:
+                    mm.append(1e3 * (time.perf_counter() - t0))
         eu = ctx.download_euler(device=True)
         if world > 1:
             eu = allreduce_euler(eu)
@@ -403,9 +411,13 @@ def main():
                  "cc_ms": cc_ms,
                  "rpc_cc_eq_1": int(np.sum(topo["rpc_cc"] == 1)) if cc_ms is not None else None,
                  "rpc_cc_gt_1": int(np.sum(topo["rpc_cc"] > 1)) if cc_ms is not None else None,
+                 "medial_mesh_ms": float(np.median(mm)) if cc_ms is not None else None,
+                 "medial_edges": int(med["edges"].shape[0]) if cc_ms is not None else None,
+                 "medial_faces": int(med["faces"].shape[0]) if cc_ms is not None else None,
                  "note": "fractional Euler characteristics (PAPER.md:482-506) fused into the "
                          "clip; full_rpd_ms = relations + clip + per-sphere sums (CUDA events); "
-                         "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find)"}
+                         "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find); "
+                         "medial_mesh_ms = dual medial mesh extraction (host-timed, two syncs)"}
 
     # ---- roofline of the dominant kernel
     fmed = float(np.median([r["filter_ms"] for r in recs]))

@@ -222,7 +222,11 @@ rpd_status rpd_download_euler(rpd_ctx* ctx, int64_t* piece_euler, int32_t* rpf_o
  *                         paper picks a surface point on a component other than m_i's own
  *   rpf_comp   [n_rpf]    component label of every radical facet (smallest rpf index)
  *   piece_sosfm[n_pieces] tet faces that are facets of the piece (bit k: face k)
- *   rpf_fm     [n_rpf]    tet faces the radical facet has an edge on */
+ *   rpf_fm     [n_rpf]    tet faces the radical facet has an edge on
+ *   rpf_adj    [n_rpf]    the piece's radical facets this one shares an edge with (bit b: the
+ *                         piece's b-th rpf entry): its restricted power edges RPE(m_i, m_j,
+ *                         m_k).  A piece with more than 64 radical facets fails the clip with
+ *                         RPD_EOVERFLOW in Euler mode (never seen: pieces have <= 20 planes) */
 typedef struct {
   const int32_t* rpc_cc;
   const int32_t* rpf_cc;
@@ -230,13 +234,33 @@ typedef struct {
   const int32_t* rpf_comp;
   const uint8_t* piece_sosfm;
   const uint8_t* rpf_fm;
+  const uint64_t* rpf_adj;
   int64_t n_pieces, n_rpf, N, E;
 } rpd_topology;
 rpd_status rpd_get_topology(rpd_ctx* ctx, rpd_topology* out);
 /* Copy (host or device destinations; any pointer may be NULL). */
 rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
                                  int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,
-                                 uint8_t* rpf_fm);
+                                 uint8_t* rpf_fm, uint64_t* rpf_adj);
+
+/* ---- Dual medial mesh
+ * "Each sub-domain RPC(m_i) ... is dual to a vertex", "the face shared by two adjacent RPCs
+ * (RPF) ... dual to an edge e_ij", "the edge shared by three RPCs (RPE) ... dual to a triangle
+ * face f_ijk".  From the current pieces (Euler mode, whole mesh or shard): every radical facet
+ * gives the edge (i, j), every restricted power edge of a piece of m_i on h_ij and h_ik the
+ * triangle (i, j, k); keys sorted and deduplicated on the device.  Outputs (ctx-owned device
+ * arrays, valid until the next mutating call): edges [n_edges][2] (i < j), faces [n_faces][3]
+ * (i < j < k), both ascending lexicographically.  A sharded job concatenates the ranks' lists
+ * and deduplicates.  Needs N < 2^21 (RPD_EINVAL). */
+typedef struct {
+  const int32_t* edges;
+  const int32_t* faces;
+  int64_t n_edges, n_faces;
+} rpd_medial;
+rpd_status rpd_medial_mesh(rpd_ctx* ctx, rpd_medial* out);
+/* Copy the last extraction to caller-owned arrays (host or device; NULL skips): edges
+ * [n_edges][2], faces [n_faces][3].  RPD_ESTATE before any rpd_medial_mesh. */
+rpd_status rpd_download_medial_mesh(rpd_ctx* ctx, int32_t* edges, int32_t* faces);
 
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */

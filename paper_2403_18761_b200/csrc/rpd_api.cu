@@ -168,7 +168,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
-                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long};
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -192,6 +192,7 @@ void rpd_destroy(rpd_ctx* c) {
     x->rpf_e.release();
     x->sfm.release();
     x->rfm.release();
+    x->radj.release();
   }
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
@@ -434,6 +435,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(c->p_rval.ensure(sizeof(long long) * 32 * nw), "alloc");
     CK(c->p_sfm.ensure(nn), "alloc");
     CK(c->p_rfm.ensure(32 * nw), "alloc");
+    CK(c->p_radj.ensure(sizeof(unsigned long long) * 32 * nw), "alloc");
   }
   const int32_t* moff = cs.moff.as<int32_t>();
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
@@ -442,7 +444,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
                      sizeof(unsigned long long) * 5, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
-                     sizeof(unsigned long long) * 7, c->stream), "memset");
+                     sizeof(unsigned long long) * 8, c->stream), "memset");
   if (c->profile) cudaEventRecord(c->ev[2], c->stream);
   CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff,
                  c->clip_wide), "clip");
@@ -465,6 +467,8 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(cudaStreamSynchronize(c->stream), "clip");
     if (rb->u64[ST_OVERFLOW])
       return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+    if (rb->u64[ST_EU_OVER])
+      return fail(c, RPD_EOVERFLOW, "topology mode: a piece has more than 64 radical facets");
     np = rb->i32[0];
     ni = rb->i32[1];
     nr = rb->i32[4];
@@ -488,12 +492,13 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(ps.rpf_e.ensure(sizeof(long long) * (nr > 0 ? nr : 1)), "alloc");
     CK(ps.sfm.ensure(npp), "alloc");
     CK(ps.rfm.ensure(nr > 0 ? nr : 1), "alloc");
+    CK(ps.radj.ensure(sizeof(unsigned long long) * (nr > 0 ? nr : 1)), "alloc");
   }
   PieceDst d{ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.vol.as<double>(),
              ps.m1.as<double>(),  ps.fm.as<uint8_t>(),     ps.inc_off.as<int32_t>(),
              ps.inc.as<int32_t>(), ps.eu.as<long long>(),  ps.rpf_off.as<int32_t>(),
              ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
-             ps.rfm.as<uint8_t>()};
+             ps.rfm.as<uint8_t>(), ps.radj.as<unsigned long long>()};
   CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idx.as<int32_t>(), moff, d),
      "compact pieces");
   ps.n_tets = nt;
@@ -727,6 +732,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
     CK(pn.rpf_e.ensure(sizeof(long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
     CK(pn.sfm.ensure(npn), "alloc");
     CK(pn.rfm.ensure(pn.n_rpf > 0 ? pn.n_rpf : 1), "alloc");
+    CK(pn.radj.ensure(sizeof(unsigned long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
   }
   CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
   tmark(c, "merge-counts");
@@ -743,6 +749,8 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   tdump(c);
   if (rb->u64[ST_OVERFLOW])
     return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+  if (rb->u64[ST_EU_OVER])
+    return fail(c, RPD_EOVERFLOW, "topology mode: a piece has more than 64 radical facets");
   absorb_clip_stats(c, rb, rb->i32[4]);
   if (c->profile) {
     float ms = 0.f;
@@ -892,6 +900,7 @@ rpd_status rpd_get_topology(rpd_ctx* c, rpd_topology* out) {
   out->rpf_comp = c->cc_par.as<int32_t>() + ps.n_pieces;
   out->piece_sosfm = ps.sfm.as<uint8_t>();
   out->rpf_fm = ps.rfm.as<uint8_t>();
+  out->rpf_adj = ps.radj.as<uint64_t>();
   out->n_pieces = ps.n_pieces;
   out->n_rpf = ps.n_rpf;
   out->N = c->st.N;
@@ -901,7 +910,7 @@ rpd_status rpd_get_topology(rpd_ctx* c, rpd_topology* out) {
 
 rpd_status rpd_download_topology(rpd_ctx* c, int32_t* rpc_cc, int32_t* rpf_cc,
                                  int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,
-                                 uint8_t* rpf_fm) {
+                                 uint8_t* rpf_fm, uint64_t* rpf_adj) {
   rpd_topology t;
   rpd_status s = rpd_get_topology(c, &t);
   if (s) return s;
@@ -915,6 +924,37 @@ rpd_status rpd_download_topology(rpd_ctx* c, int32_t* rpc_cc, int32_t* rpf_cc,
   CK(cp(rpf_comp, t.rpf_comp, sizeof(int32_t) * t.n_rpf), "download");
   CK(cp(piece_sosfm, t.piece_sosfm, t.n_pieces), "download");
   CK(cp(rpf_fm, t.rpf_fm, t.n_rpf), "download");
+  CK(cp(rpf_adj, t.rpf_adj, sizeof(uint64_t) * t.n_rpf), "download");
+  CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_medial_mesh(rpd_ctx* c, rpd_medial* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_medial_mesh: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no topology data (rpd_set_euler, then rpd_clip)");
+  if (c->st.N >= (1 << 21)) return fail(c, RPD_EINVAL, "medial mesh keys need N < 2^21");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  int64_t ne = 0, nf = 0;
+  CK(launch_medial_mesh(c, c->pcs[c->cur], &ne, &nf), "medial mesh");
+  out->edges = c->mm_out.as<int32_t>();
+  out->faces = c->mm_out.as<int32_t>() + 2 * ne;
+  out->n_edges = ne;
+  out->n_faces = nf;
+  c->mm_ne = ne;
+  c->mm_nf = nf;
+  return RPD_OK;
+}
+
+rpd_status rpd_download_medial_mesh(rpd_ctx* c, int32_t* edges, int32_t* faces) {
+  if (!c) return RPD_EINVAL;
+  if (c->mm_ne < 0) return fail(c, RPD_ESTATE, "no medial mesh (call rpd_medial_mesh)");
+  if (edges && c->mm_ne)
+    CK(cudaMemcpyAsync(edges, c->mm_out.p, sizeof(int32_t) * 2 * c->mm_ne, cudaMemcpyDefault,
+                       c->stream), "download");
+  if (faces && c->mm_nf)
+    CK(cudaMemcpyAsync(faces, c->mm_out.as<int32_t>() + 2 * c->mm_ne,
+                       sizeof(int32_t) * 3 * c->mm_nf, cudaMemcpyDefault, c->stream), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }

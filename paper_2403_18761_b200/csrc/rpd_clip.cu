@@ -324,7 +324,7 @@ __device__ inline int new_vertex(const WarpState<GW, VPL>& S, const ClipCtx& C, 
 }
 
 enum { ST_ALIVE = 0, ST_EMPTY = 1, ST_OVER = 2 };
-constexpr int ST_N_CLIP = 12;  // statistics counters reduced by the clip kernels
+constexpr int ST_N_CLIP = 13;  // statistics counters reduced by the clip kernels
 
 #ifdef RPD_CLIP_PHASES
 // development aid: cycles per clip phase summed over groups (lane 0 of each group)
@@ -366,6 +366,7 @@ struct PairOut {
   long long* rval;          // per (pair, row position): Euler of that facet x L
   uint8_t* sfm;             // per pair: tet faces that are SoS facets (CC numbers, NEXT-2)
   uint8_t* rfm;             // per (pair, row position): tet faces the facet has an edge on
+  unsigned long long* radj; // per (pair, row position): radical facets sharing an edge (rank)
 };
 
 // EU: also the fractional Euler characteristics (a separate instantiation, so that the plain
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) / GW;
   int n_exact = 0, n_zero = 0, max_v = 0, max_p = 0, n_over = 0;
   int d_sign = 0, d_out = 0, d_fb = 0;  // diagnostics
+  int n_euover = 0;  // pieces with more than 64 radical facets (Euler/topology mode)
   // algorithmic work (warp-uniform quantities, counted once per warp)
   unsigned c_planes = 0, c_tests = 0, c_constr = 0, c_fan = 0;  // per group: small
 #ifdef RPD_CLIP_PHASES
@@ -910,13 +912,25 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           S.pay[14] = out.eu_L;
         }
 #pragma unroll
-        for (int k = 0; k < VPL; ++k)
-          if (GW * k + lane < np) {
-            acc[GW * k + lane] = 0;
-            S.dsc[GW * k + lane] = 0u;  // (free after the cuts) tet faces next to each facet
+        for (int k = 0; k < VPL; ++k) {
+          const int pl = GW * k + lane;
+          if (pl < np) {
+            acc[pl] = 0;
+            S.dsc[pl] = 0u;  // (free after the cuts) tet faces next to each facet
+            reinterpret_cast<unsigned long long*>(S.KM)[pl] = 0ull;  // adjacent radical facets
+            // rank of a radical facet among the piece's radical facets by ascending j (the
+            // order of the compacted rpf entries)
+            if (pl >= 4 && facets_all.has(pl)) {
+              int rk = 0;
+              for (int f = facets_all.next(4); f >= 0; f = facets_all.next(f + 1))
+                rk += S.src[f] < S.src[pl];
+              S.c0[pl] = (unsigned char)(rk < 64 ? rk : 255);
+            }
           }
+        }
       }
       __syncwarp(FULL);
+      unsigned long long* adj = reinterpret_cast<unsigned long long*>(S.KM);
       long long c2 = 0, cf = 0;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) {
@@ -938,6 +952,22 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         if (a >= 4 && (mb | mc)) atomicOr(S.dsc + a, mb | mc);
         if (b >= 4 && (ma | mc)) atomicOr(S.dsc + b, ma | mc);
         if (cc >= 4 && (ma | mb)) atomicOr(S.dsc + cc, ma | mb);
+        // medial mesh: a plane pair of the triplet on two radical planes is a restricted power
+        // edge RPE(m_i, m_j, m_k) (a triangle of the dual medial mesh)
+        const int pr[3][2] = {{a, b}, {b, cc}, {cc, a}};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int x = pr[r][0], y = pr[r][1];
+          if (x >= 4 && y >= 4) {
+            const int rx = S.c0[x], ry = S.c0[y];
+            if (rx < 64 && ry < 64) {
+              atomicOr(adj + x, 1ull << ry);
+              atomicOr(adj + y, 1ull << rx);
+            } else {
+              ++n_euover;
+            }
+          }
+        }
       }
       __syncwarp(FULL);
       unsigned* rw = out.rmask + mo;
@@ -957,6 +987,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
             const int pos = S.eidx[pl] - e0;
             rv[pos] = acc[pl] / 2 + out.eu_L;
             out.rfm[32 * (int64_t)mo + pos] = (uint8_t)S.dsc[pl];
+            out.radj[32 * (int64_t)mo + pos] = adj[pl];
             if (one_word) rbits |= 1u << pos;
             else atomicOr(rw + (pos >> 5), 1u << (pos & 31));
           }
@@ -1071,18 +1102,20 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
                                      lead ? c_tests : 0u,         lead ? c_constr : 0u,
                                      lead ? c_fan : 0u,
                                      lead && !out.over_list ? (unsigned long long)n_over : 0ull,
+                                     (unsigned long long)n_euover,
                                      (unsigned long long)max_v,   (unsigned long long)max_p};
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-    for (int k = 0; k < 10; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    for (int k = 0; k < 11; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
 #pragma unroll
-    for (int k = 10; k < 12; ++k) v[k] = max(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    for (int k = 11; k < 13; ++k) v[k] = max(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
   }
   const int slot[ST_N_CLIP] = {ST_EXACT,    ST_ZERO,        12,            13,
                                14,          ST_CLIP_PLANES, ST_CLIP_TESTS, ST_CLIP_CONSTR,
-                               ST_CLIP_FAN, ST_OVERFLOW,    ST_MAXV,       ST_MAXP};
-  const int kind[ST_N_CLIP] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1};
+                               ST_CLIP_FAN, ST_OVERFLOW,    ST_EU_OVER,    ST_MAXV,
+                               ST_MAXP};
+  const int kind[ST_N_CLIP] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1};
   block_stats<ST_N_CLIP>(stats, slot, kind, v);
 }
 
@@ -1116,6 +1149,8 @@ struct EuCompact {
   long long* rpf_e;
   const uint8_t *p_sfm, *p_rfm;  // CC flags (per pair, per pair slot)
   uint8_t *sfm, *rfm;            // ... compacted (per piece, per radical facet)
+  const unsigned long long* p_radj;  // radical-facet adjacency (per pair slot)
+  unsigned long long* radj;          // ... compacted (per radical facet)
 };
 
 __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ cand_idx,
@@ -1171,6 +1206,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
         eu.rpf_j[r] = nbr_idx[e0 + pos];
         eu.rpf_e[r] = eu.rval[32 * (int64_t)w0 + pos];
         eu.rfm[r] = eu.p_rfm[32 * (int64_t)w0 + pos];
+        eu.radj[r] = eu.p_radj[32 * (int64_t)w0 + pos];
         ++r;
       }
     }
@@ -1230,7 +1266,8 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
             over ? over + 1 : nullptr, over,
             c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
             c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>(),
-            c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>()};
+            c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(),
+            c->p_radj.as<unsigned long long>()};
   k_clip<GW, VPL, EU><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
@@ -1311,7 +1348,8 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
         d.inc_off, d.inc,
         EuCompact{c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_rval.as<long long>(),
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
-                  d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm});
+                  d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm,
+                  c->p_radj.as<unsigned long long>(), d.radj});
     ++c->launches;
   } else {
     cudaMemsetAsync(d.inc_off, 0, sizeof(int32_t), c->stream);

@@ -64,6 +64,7 @@ enum StatIdx {
   ST_CLIP_TESTS = 9,    // vertex sign tests in the clip
   ST_CLIP_CONSTR = 10,  // vertex constructions
   ST_CLIP_FAN = 11,     // fan triangles of the volume/moment integration
+  ST_EU_OVER = 15,      // pieces with more than 64 radical facets (topology mode)
   ST_N = 16
 };
 
@@ -100,6 +101,7 @@ struct PieceSet {
   // fractional Euler characteristics (Euler mode): per piece, and per radical SoS facet
   DevBuf eu, rpf_off, rpf_j, rpf_e;
   DevBuf sfm, rfm;  // CC flags: SoS tet facets per piece, tet faces next to each radical facet
+  DevBuf radj;      // per radical facet: the piece's radical facets sharing an edge (by rank)
   int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;
 };
 }  // namespace rpd
@@ -174,7 +176,9 @@ struct rpd_ctx {
   rpd::DevBuf eu_A;            // int64 [256] L / n, then L, then the counts-present bitmap
   rpd::DevBuf eu_sum;          // int64 [N + E + 1]: per-sphere RPC, per-CSR-entry RPF, misses
   rpd::DevBuf p_eu, p_rmask, p_rval, p_nrpf, r_scan;  // per-pair clip outputs
-  rpd::DevBuf p_sfm, p_rfm;                           // per-pair CC flags
+  rpd::DevBuf p_sfm, p_rfm, p_radj;                   // per-pair CC / medial-mesh flags
+  rpd::DevBuf mm_keys, mm_tmp, mm_out;                // medial-mesh extraction scratch
+  int64_t mm_ne = -1, mm_nf = -1;                     // sizes of the last extraction
   bool eu_whole = false;       // payloads built with the ctx holding the whole mesh in order
   rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
   rpd::DevBuf cc_par, cc_out;  // CC numbers: union-find parents, outputs
@@ -229,6 +233,7 @@ struct PieceDst {
   long long* rpf_e;
   uint8_t* sfm;       // [n_pieces], [n_rpf]
   uint8_t* rfm;
+  unsigned long long* radj;  // [n_rpf]
 };
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
@@ -244,5 +249,8 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
                                const int32_t* local_ids, int64_t T_local);
 cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps);
 cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
+// medial mesh: unique sorted edge keys (i << 32 | j) and face keys (i << 42 | j << 21 | k)
+cudaError_t launch_medial_mesh(rpd_ctx* c, const PieceSet& ps, int64_t* n_edges,
+                               int64_t* n_faces);
 
 }  // namespace rpd

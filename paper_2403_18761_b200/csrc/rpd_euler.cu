@@ -19,6 +19,8 @@
 // collect the fractional Euler characteristics for all of its restricted elements",
 // PAPER.md:506): Euler(RPC(m_i)) over the pieces of m_i and Euler(RPF(m_i, m_j)) over their
 // facets on h_ij, by integer atomics into arrays aligned with the sphere ids and the CSR.
+#include <cub/cub.cuh>
+
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -445,6 +447,143 @@ cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps) {
       ++c->launches;
     }
   }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- dual medial mesh (NEXT-2)
+//
+// RPC -> vertex, RPF(m_i, m_j) -> edge e_ij, RPE(m_i, m_j, m_k) -> triangle
+// f_ijk.  One thread per piece emits an edge key per radical facet and a triangle key per pair
+// of its radical facets that share an edge (rpf_adj); keys are sorted and deduplicated with
+// CUB's radix sort / unique (library primitives) and decoded.
+
+__global__ void k_mm_count(int64_t n_pieces, const int32_t* __restrict__ roff,
+                           const unsigned long long* __restrict__ radj, int32_t* __restrict__ cnt) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_pieces) return;
+  int n = 0;
+  for (int r = roff[q]; r < roff[q + 1]; ++r) {
+    const int a = r - roff[q];
+    n += a < 63 ? __popcll(radj[r] >> (a + 1)) : 0;
+  }
+  cnt[q] = n;
+}
+
+__global__ void k_mm_emit(int64_t n_pieces, const int32_t* __restrict__ psph,
+                          const int32_t* __restrict__ roff, const int32_t* __restrict__ rj,
+                          const unsigned long long* __restrict__ radj,
+                          const int32_t* __restrict__ foff, unsigned long long* __restrict__ ekeys,
+                          unsigned long long* __restrict__ fkeys) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_pieces) return;
+  const long long i = psph[q];
+  const int r0 = roff[q], r1 = roff[q + 1];
+  int m = foff[q];
+  for (int r = r0; r < r1; ++r) {
+    const long long j = rj[r];
+    ekeys[r] = ((unsigned long long)min(i, j) << 32) | (unsigned long long)max(i, j);
+    const int a = r - r0;
+    unsigned long long bits = a < 63 ? radj[r] >> (a + 1) : 0ull;
+    while (bits) {
+      const int b = a + __ffsll((long long)bits);  // (a + 1) + bit index
+      bits &= bits - 1ull;
+      long long x = i, y = j, z = rj[r0 + b];
+      sort3(x, y, z);
+      fkeys[m++] = ((unsigned long long)x << 42) | ((unsigned long long)y << 21) |
+                   (unsigned long long)z;
+    }
+  }
+}
+
+__global__ void k_mm_decode(int64_t ne, const unsigned long long* __restrict__ ek, int64_t nf,
+                            const unsigned long long* __restrict__ fk, int32_t* __restrict__ out) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < ne) {
+    out[2 * x] = (int32_t)(ek[x] >> 32);
+    out[2 * x + 1] = (int32_t)(ek[x] & 0xffffffffull);
+  } else if (x < ne + nf) {
+    const int64_t f = x - ne;
+    const unsigned long long k = fk[f];
+    int32_t* o = out + 2 * ne + 3 * f;
+    o[0] = (int32_t)(k >> 42);
+    o[1] = (int32_t)((k >> 21) & 0x1fffffull);
+    o[2] = (int32_t)(k & 0x1fffffull);
+  }
+}
+
+// sorted unique keys: in -> out (count to *n_out, device), temp in c->mm_tmp
+static cudaError_t sort_unique(rpd_ctx* c, unsigned long long* keys, unsigned long long* tmp_keys,
+                               int64_t n, int* n_out) {
+  size_t b1 = 0, b2 = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, b1, keys, tmp_keys, (int)n, 0, 64,
+                                                 c->stream);
+  if (e) return e;
+  e = cub::DeviceSelect::Unique(nullptr, b2, tmp_keys, keys, n_out, (int)n, c->stream);
+  if (e) return e;
+  if ((e = c->mm_tmp.ensure(b1 > b2 ? b1 : b2))) return e;
+  size_t bt = c->mm_tmp.cap;
+  if ((e = cub::DeviceRadixSort::SortKeys(c->mm_tmp.p, bt, keys, tmp_keys, (int)n, 0, 64,
+                                          c->stream)))
+    return e;
+  bt = c->mm_tmp.cap;
+  e = cub::DeviceSelect::Unique(c->mm_tmp.p, bt, tmp_keys, keys, n_out, (int)n, c->stream);
+  c->launches += 2;
+  return e;
+}
+
+cudaError_t launch_medial_mesh(rpd_ctx* c, const PieceSet& ps, int64_t* n_edges,
+                               int64_t* n_faces) {
+  const int64_t np = ps.n_pieces, nr = ps.n_rpf;
+  cudaError_t e;
+  // face counts per piece -> offsets (total read back)
+  if ((e = c->cc_par.ensure(sizeof(int32_t) * (2 * np + 2)))) return e;
+  int32_t* cnt = c->cc_par.as<int32_t>();
+  int32_t* foff = cnt + np + 1;
+  if (np > 0) {
+    k_mm_count<<<nblk(np, 256), 256, 0, c->stream>>>(np, ps.rpf_off.as<int32_t>(),
+                                                     ps.radj.as<unsigned long long>(), cnt);
+    ++c->launches;
+  }
+  if ((e = launch_scan_i32(c, cnt, foff, np))) return e;
+  int32_t nf_all = 0;
+  if ((e = cudaMemcpyAsync(&nf_all, foff + np, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           c->stream)))
+    return e;
+  if ((e = cudaStreamSynchronize(c->stream))) return e;
+  const int64_t tot = nr + nf_all;
+  if ((e = c->mm_keys.ensure(sizeof(unsigned long long) * 2 * (tot > 0 ? tot : 1) + 64)))
+    return e;
+  unsigned long long* ek = c->mm_keys.as<unsigned long long>();
+  unsigned long long* fk = ek + nr;
+  unsigned long long* tk = ek + tot;  // sort output scratch
+  int* n_sel = reinterpret_cast<int*>(tk + (tot > 0 ? tot : 1));
+  if (np > 0) {
+    k_mm_emit<<<nblk(np, 256), 256, 0, c->stream>>>(
+        np, ps.sphere.as<int32_t>(), ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(),
+        ps.radj.as<unsigned long long>(), foff, ek, fk);
+    ++c->launches;
+  }
+  int hs[2] = {0, 0};
+  if (nr > 0) {
+    if ((e = sort_unique(c, ek, tk, nr, n_sel))) return e;
+    if ((e = cudaMemcpyAsync(hs, n_sel, sizeof(int), cudaMemcpyDeviceToHost, c->stream)))
+      return e;
+  }
+  if (nf_all > 0) {
+    if ((e = sort_unique(c, fk, tk, nf_all, n_sel + 1))) return e;
+    if ((e = cudaMemcpyAsync(hs + 1, n_sel + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream)))
+      return e;
+  }
+  if ((e = cudaStreamSynchronize(c->stream))) return e;
+  const int64_t ne = hs[0], nf = hs[1];
+  if ((e = c->mm_out.ensure(sizeof(int32_t) * (2 * ne + 3 * nf + 1)))) return e;
+  if (ne + nf > 0) {
+    k_mm_decode<<<nblk(ne + nf, 256), 256, 0, c->stream>>>(ne, ek, nf, fk,
+                                                           c->mm_out.as<int32_t>());
+    ++c->launches;
+  }
+  *n_edges = ne;
+  *n_faces = nf;
   return cudaGetLastError();
 }
 

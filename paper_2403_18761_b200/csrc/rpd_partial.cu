@@ -91,6 +91,7 @@ struct MergeSrc {
   const int32_t *p_rpf_off, *p_rpf_j;
   const long long* p_rpf_e;
   const uint8_t *p_sfm, *p_rfm;
+  const unsigned long long* p_radj;
 };
 
 __device__ inline MergeSrc pick(int d, const MergeSrc& o, const MergeSrc& n) {
@@ -124,6 +125,7 @@ struct MergeDst {
   int32_t *p_rpf_off, *p_rpf_j;
   long long* p_rpf_e;
   uint8_t *p_sfm, *p_rfm;
+  unsigned long long* p_radj;
 };
 
 constexpr int MT = 256;  // tets per merge tile (one block)
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       tile_copy(D.p_eu + p_dst, o.p_eu + p_src, npc, same);
       tile_copy(D.p_sfm + p_dst, o.p_sfm + p_src, npc, same);
       tile_copy(D.p_rfm + r_dst, o.p_rfm + r_src, nr, same);
+      tile_copy(D.p_radj + r_dst, o.p_radj + r_src, nr, same);
       tile_copy(D.p_rpf_off + p_dst, o.p_rpf_off + p_src, npc,
                 [=](int32_t x) { return x + rshift; });
       tile_copy(D.p_rpf_j + r_dst, o.p_rpf_j + r_src, nr, same);
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __
       D.p_rpf_j[r] = s.p_rpf_j[src];
       D.p_rpf_e[r] = s.p_rpf_e[src];
       D.p_rfm[r] = s.p_rfm[src];
+      D.p_radj[r] = s.p_radj[src];
     }
   // incidences (a tet's incidences are contiguous in its source set)
   for (int r = s_ni[0] + threadIdx.x; r < s_ni[nt]; r += blockDim.x) {
@@ -289,7 +293,7 @@ static MergeSrc src_of(const CandSet& cs, const PieceSet& ps, bool eu) {
                   ps.fm.as<uint8_t>(),
                   eu ? ps.eu.as<long long>() : nullptr, ps.rpf_off.as<int32_t>(),
                   ps.rpf_j.as<int32_t>(),   ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
-                  ps.rfm.as<uint8_t>()};
+                  ps.rfm.as<uint8_t>(),     ps.radj.as<unsigned long long>()};
 }
 
 // phase 0: per-tet counts and their scans (new cand offsets -> cn.off, new piece offsets ->
@@ -323,7 +327,7 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
              pn.fm.as<uint8_t>(),      r_off,
              eu ? pn.eu.as<long long>() : nullptr, pn.rpf_off.as<int32_t>(),
              pn.rpf_j.as<int32_t>(),   pn.rpf_e.as<long long>(), pn.sfm.as<uint8_t>(),
-             pn.rfm.as<uint8_t>()};
+             pn.rfm.as<uint8_t>(),     pn.radj.as<unsigned long long>()};
   if (T > 0) {
     k_merge_copy<<<nblk(T, MT), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
     ++c->launches;

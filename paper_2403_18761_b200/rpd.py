@@ -25,7 +25,8 @@ FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
-            "rpd_download_euler", "rpd_get_topology", "rpd_download_topology"]
+            "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
+            "rpd_medial_mesh", "rpd_download_medial_mesh"]
 
 
 class RPDError(RuntimeError):
@@ -51,8 +52,13 @@ class _Euler(C.Structure):
 class _Topology(C.Structure):
     _fields_ = [("rpc_cc", C.c_void_p), ("rpf_cc", C.c_void_p), ("piece_comp", C.c_void_p),
                 ("rpf_comp", C.c_void_p), ("piece_sosfm", C.c_void_p), ("rpf_fm", C.c_void_p),
-                ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
+                ("rpf_adj", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
                 ("E", C.c_int64)]
+
+
+class _Medial(C.Structure):
+    _fields_ = [("edges", C.c_void_p), ("faces", C.c_void_p), ("n_edges", C.c_int64),
+                ("n_faces", C.c_int64)]
 
 
 class _Stats(C.Structure):
@@ -99,12 +105,14 @@ def load_library(path: str = LIB_PATH):
     L.rpd_get_euler.argtypes = [vp, C.POINTER(_Euler)]
     L.rpd_download_euler.argtypes = [vp] * 7
     L.rpd_get_topology.argtypes = [vp, C.POINTER(_Topology)]
-    L.rpd_download_topology.argtypes = [vp] * 7
+    L.rpd_download_topology.argtypes = [vp] * 8
+    L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
+    L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
               "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
               "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
-              "rpd_download_topology"):
+              "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -308,11 +316,20 @@ class RPDContext:
         t = _Topology()
         self._check(self.L.rpd_get_topology(self.h, C.byref(t)))
         specs = [(t.N, np.int32), (t.E, np.int32), (t.n_pieces, np.int32), (t.n_rpf, np.int32),
-                 (t.n_pieces, np.uint8), (t.n_rpf, np.uint8)]
+                 (t.n_pieces, np.uint8), (t.n_rpf, np.uint8), (t.n_rpf, np.uint64)]
         arrs = self._alloc(specs, device)
         self._check(self.L.rpd_download_topology(self.h, *[self._p(a) for a in arrs]))
-        return dict(zip(["rpc_cc", "rpf_cc", "piece_comp", "rpf_comp", "piece_sosfm", "rpf_fm"],
-                        arrs))
+        return dict(zip(["rpc_cc", "rpf_cc", "piece_comp", "rpf_comp", "piece_sosfm", "rpf_fm",
+                         "rpf_adj"], arrs))
+
+    def medial_mesh(self, device=False) -> dict:
+        """The dual medial mesh of the current pieces: unique sorted edges
+        [n, 2] (i < j) and triangles [n, 3] (i < j < k)."""
+        m = _Medial()
+        self._check(self.L.rpd_medial_mesh(self.h, C.byref(m)))
+        e, f = self._alloc([(2 * m.n_edges, np.int32), (3 * m.n_faces, np.int32)], device)
+        self._check(self.L.rpd_download_medial_mesh(self.h, self._p(e), self._p(f)))
+        return {"edges": e.reshape(-1, 2), "faces": f.reshape(-1, 3)}
 
     def stats(self) -> dict:
         s = _Stats()
@@ -324,7 +341,7 @@ class RPDContext:
         if device:
             import torch
             tdt = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8,
-                   np.int64: torch.int64}
+                   np.int64: torch.int64, np.uint64: torch.int64}
             return [torch.empty(max(n, 0), dtype=tdt[dt], device="cuda") for n, dt in specs]
         return [np.empty(max(n, 0), dtype=dt) for n, dt in specs]
 

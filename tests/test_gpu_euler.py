@@ -196,6 +196,7 @@ def run_gpu_topology(ctx, w):
 def check_topology(got, ref, w):
     assert np.array_equal(got["piece_sosfm"], ref["piece_sosfm"])
     assert np.array_equal(got["rpf_fm"], ref["rpf_fm"])
+    assert np.array_equal(got["rpf_adj"].astype(np.uint64), ref["rpf_adj"])
     rpc_cc, rpf_cc = oracle.topology(ref, w.tets, w.N)
     assert got["rpc_cc"].tolist() == rpc_cc
     for i in range(w.N):
@@ -283,3 +284,66 @@ def test_topology_c3(ctx):
     roots = got["piece_comp"] == np.arange(len(got["piece_comp"]))
     assert roots.sum() == got["rpc_cc"].sum()
     assert np.mean(got["rpc_cc"][has] == 1) > 0.9
+
+
+
+# ----------------------------------------------------------------------------- medial mesh
+# the dual medial mesh
+
+
+def gpu_medial(ctx, w, tets=None, local_ids=None):
+    ctx.set_euler(w.tets, len(w.verts), local_ids)
+    try:
+        ctx.relations(w.verts, w.tets if tets is None else tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        return ctx.medial_mesh()
+    finally:
+        ctx.set_euler(None, 0)
+
+
+@pytest.mark.parametrize("make", MAKERS)
+def test_medial_mesh_parity(ctx, make):
+    w = make()
+    got = gpu_medial(ctx, w)
+    edges, faces = oracle.medial_mesh(oracle.rpd_workload(w, euler=True))
+    assert [tuple(e) for e in got["edges"].tolist()] == edges
+    assert [tuple(f) for f in got["faces"].tolist()] == faces
+
+
+def test_medial_mesh_three_spheres(ctx):
+    """three cells meeting along one RPE -> one triangle, three edges."""
+    import copy
+    verts, tets = W.kuhn_grid_mesh((2, 2, 2), 512, (0, 0, 0), morton=False)
+    w = copy.copy(W.make_c1(0))
+    w.verts, w.tets = verts, tets
+    w.spheres = np.array([[0.25, 0.25, 0.5, 0.0], [0.75, 0.3125, 0.5, 0.0],
+                          [0.4375, 0.75, 0.5, 0.0]])
+    w.nbr_off = np.array([0, 2, 4, 6], np.int32)
+    w.nbr_idx = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    got = gpu_medial(ctx, w)
+    assert got["edges"].tolist() == [[0, 1], [0, 2], [1, 2]]
+    assert got["faces"].tolist() == [[0, 1, 2]]
+
+
+def test_medial_mesh_shards_union(ctx):
+    """Tet shards: the union of the shards' medial meshes is the whole mesh's."""
+    w = W.make_shape_workload("Sh", 3000, 200, seed=6, cache=False)
+    full = gpu_medial(ctx, w)
+    E, F = set(), set()
+    for rank in range(2):
+        ids = W.block_cyclic_shard(w.T, 2, rank, block=256).astype(np.int32)
+        part = gpu_medial(ctx, w, tets=w.tets[ids], local_ids=ids)
+        E |= {tuple(e) for e in part["edges"].tolist()}
+        F |= {tuple(f) for f in part["faces"].tolist()}
+    assert sorted(E) == [tuple(e) for e in full["edges"].tolist()]
+    assert sorted(F) == [tuple(f) for f in full["faces"].tolist()]
+
+
+def test_medial_mesh_c3(ctx):
+    """Full C3 size: every triangle's edges are medial edges; the mesh is non-trivial."""
+    w = W.make_config("C3")
+    got = gpu_medial(ctx, w)
+    E = {tuple(e) for e in got["edges"].tolist()}
+    assert len(got["faces"]) > 1000
+    for (i, j, k) in got["faces"][:: max(1, len(got["faces"]) // 2000)].tolist():
+        assert (i, j) in E and (i, k) in E and (j, k) in E
