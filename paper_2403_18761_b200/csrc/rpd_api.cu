@@ -163,7 +163,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
                     &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
-                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
+                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
@@ -421,6 +421,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(c->p_ninc.ensure(sizeof(int32_t) * nn), "alloc");
   CK(c->p_over.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->p_over2.ensure(sizeof(int32_t) * (n + 1)), "alloc");
+  CK(c->p_over3.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->p_mask.ensure(sizeof(unsigned) * (cs.n_words > 0 ? cs.n_words : 1)), "alloc");
   CK(c->p_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
   CK(c->i_scan.ensure(sizeof(int32_t) * (n + 1)), "alloc");
@@ -441,6 +442,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
   CK(cudaMemsetAsync(c->p_over.p, 0, sizeof(int32_t), c->stream), "memset");
   CK(cudaMemsetAsync(c->p_over2.p, 0, sizeof(int32_t), c->stream), "memset");
+  CK(cudaMemsetAsync(c->p_over3.p, 0, sizeof(int32_t), c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_EXACT, 0,
                      sizeof(unsigned long long) * 5, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,

@@ -47,6 +47,9 @@
 #ifndef RPD_CLIP_MID_VPL
 #define RPD_CLIP_MID_VPL 2  // vertex slots per lane of the middle (first overflow) tier, GW = 32
 #endif
+#ifndef RPD_CLIP_MID32
+#define RPD_CLIP_MID32 0    // 1: a 32-slot tier (GW = 32, one slot per lane) before the middle one (measured slower)
+#endif
 
 namespace rpd {
 
@@ -1309,9 +1312,21 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
 template <bool EU>
 static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                       const int32_t* cand_idx, const int32_t* moff) {
-  cudaError_t e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
+  cudaError_t e;
+#if RPD_CLIP_MID32
+  // 32-slot tier (one slot per lane: the fast tier's program on a full warp) for the fast
+  // tier's overflows; its own overflows go on to the 64-slot tier
+  e = launch_clip_t<32, 1, EU>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids,
+                               cand_idx, moff, c->p_over3.as<int32_t>(), c->p_over.as<int32_t>());
+  if (e) return e;
+  e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
+      c, 1 << 30, c->p_over3.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff,
+      c->p_over2.as<int32_t>(), c->p_over3.as<int32_t>());
+#else
+  e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
       c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff,
       c->p_over2.as<int32_t>(), c->p_over.as<int32_t>());
+#endif
   if (e) return e;
   return launch_clip_t<32, 4, EU>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
                                   cand_idx, moff, nullptr, c->p_over2.as<int32_t>());

@@ -143,7 +143,7 @@ struct rpd_ctx {
   bool have_rel = false, have_pieces = false;
 
   // clip per-pair scratch
-  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_scan, i_scan;
+  rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_over3, p_scan, i_scan;
   rpd::DevBuf p_dyn;  // dynamic pair counter of the fast clip kernel
 
   // partial update scratch
