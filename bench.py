@@ -276,7 +276,7 @@ def main():
                                    "clipped": st["pairs_clipped"]})
         if world > 1:
             loc = ctx.download_pieces(device=True)
-            gather_pieces(loc, ids, w.T)
+            gather_pieces(loc, ids, w.T, ctx)
         record.append(rec)
 
     launches0 = None

@@ -262,6 +262,35 @@ rpd_status rpd_medial_mesh(rpd_ctx* ctx, rpd_medial* out);
  * [n_edges][2], faces [n_faces][3].  RPD_ESTATE before any rpd_medial_mesh. */
 rpd_status rpd_download_medial_mesh(rpd_ctx* ctx, int32_t* edges, int32_t* faces);
 
+/* ---- Multi-GPU gather of the pieces
+ *
+ * Each rank clips its own tet shard (rpd_relations on its tets); the per-rank piece CSRs are
+ * all-gathered by the caller (NCCL over NVLink) and rpd_gather_pieces puts them back into
+ * global tet order, on the ctx's device.  Every array below is a DEVICE pointer (the gathered
+ * buffers); rank r holds n_tets[r] tets whose global ids are tet_ids[r] (each global tet in
+ * exactly one rank), with its local piece CSR piece_off[r] [n_tets[r]+1] ... inc_sphere[r].
+ * Outputs (caller-allocated device arrays): piece_off [T+1], piece_sphere / piece_vol /
+ * piece_facemask [sum n_pieces], piece_m1 [3 sum n_pieces], inc_off [sum n_pieces + 1],
+ * inc_sphere [sum n_inc] -- byte-identical to a single-GPU rpd_clip of all T tets.
+ * RPD_EINVAL: world outside [1, RPD_MAX_RANKS] or a NULL array. */
+#define RPD_MAX_RANKS 16
+typedef struct {
+  int32_t world;
+  int64_t T;
+  int64_t n_tets[RPD_MAX_RANKS];
+  const int32_t* tet_ids[RPD_MAX_RANKS];
+  const int32_t* piece_off[RPD_MAX_RANKS];
+  const int32_t* piece_sphere[RPD_MAX_RANKS];
+  const double* piece_vol[RPD_MAX_RANKS];
+  const double* piece_m1[RPD_MAX_RANKS];
+  const uint8_t* piece_facemask[RPD_MAX_RANKS];
+  const int32_t* inc_off[RPD_MAX_RANKS];
+  const int32_t* inc_sphere[RPD_MAX_RANKS];
+} rpd_shards;
+rpd_status rpd_gather_pieces(rpd_ctx* ctx, const rpd_shards* shards, int32_t* piece_off,
+                             int32_t* piece_sphere, double* piece_vol, double* piece_m1,
+                             uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
+
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */
 typedef struct {

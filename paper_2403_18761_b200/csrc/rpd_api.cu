@@ -168,7 +168,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
-                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -958,6 +958,24 @@ rpd_status rpd_download_medial_mesh(rpd_ctx* c, int32_t* edges, int32_t* faces) 
     CK(cudaMemcpyAsync(faces, c->mm_out.as<int32_t>() + 2 * c->mm_ne,
                        sizeof(int32_t) * 3 * c->mm_nf, cudaMemcpyDefault, c->stream), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_gather_pieces(rpd_ctx* c, const rpd_shards* sh, int32_t* piece_off,
+                             int32_t* piece_sphere, double* piece_vol, double* piece_m1,
+                             uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere) {
+  if (!c) return RPD_EINVAL;
+  if (!sh || sh->world < 1 || sh->world > RPD_MAX_RANKS || sh->T < 0 || sh->T > 0x7fffffff ||
+      !piece_off || !inc_off)
+    return fail(c, RPD_EINVAL, "rpd_gather_pieces: bad argument");
+  for (int r = 0; r < sh->world; ++r)
+    if (sh->n_tets[r] < 0 || (sh->n_tets[r] > 0 && (!sh->tet_ids[r] || !sh->piece_off[r] ||
+                                                    !sh->inc_off[r])))
+      return fail(c, RPD_EINVAL, "rpd_gather_pieces: bad shard");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(launch_gather(c, sh, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask, inc_off,
+                   inc_sphere), "gather");
+  CK(cudaStreamSynchronize(c->stream), "gather");
   return RPD_OK;
 }
 

@@ -129,6 +129,7 @@ struct rpd_ctx {
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
   rpd::DevBuf cand_long;   // compaction: count + tets with more than 16 candidates
+  rpd::DevBuf g_cnt;       // multi-GPU gather: per global tet piece / incidence counts, offsets
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
   rpd::DevBuf bvh_all;     // leaf + super boxes of the whole mesh (valid per staged mesh)
   bool bvh_all_valid = false;
@@ -244,6 +245,10 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase);
+// multi-GPU gather of the pieces (rpd_gather.cu)
+cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
+                          int32_t* piece_sphere, double* piece_vol, double* piece_m1,
+                          uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
 // fractional Euler characteristics (rpd_euler.cu)
 cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
                                const int32_t* local_ids, int64_t T_local);

@@ -26,7 +26,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
-            "rpd_medial_mesh", "rpd_download_medial_mesh"]
+            "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces"]
 
 
 class RPDError(RuntimeError):
@@ -59,6 +59,16 @@ class _Topology(C.Structure):
 class _Medial(C.Structure):
     _fields_ = [("edges", C.c_void_p), ("faces", C.c_void_p), ("n_edges", C.c_int64),
                 ("n_faces", C.c_int64)]
+
+
+MAX_RANKS = 16
+
+
+class _Shards(C.Structure):
+    _fields_ = [("world", C.c_int32), ("T", C.c_int64), ("n_tets", C.c_int64 * MAX_RANKS)] + \
+               [(k, C.c_void_p * MAX_RANKS) for k in
+                ("tet_ids", "piece_off", "piece_sphere", "piece_vol", "piece_m1",
+                 "piece_facemask", "inc_off", "inc_sphere")]
 
 
 class _Stats(C.Structure):
@@ -108,11 +118,13 @@ def load_library(path: str = LIB_PATH):
     L.rpd_download_topology.argtypes = [vp] * 8
     L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
     L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
+    L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
               "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
               "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
-              "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh"):
+              "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
+              "rpd_gather_pieces"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -330,6 +342,43 @@ class RPDContext:
         e, f = self._alloc([(2 * m.n_edges, np.int32), (3 * m.n_faces, np.int32)], device)
         self._check(self.L.rpd_download_medial_mesh(self.h, self._p(e), self._p(f)))
         return {"edges": e.reshape(-1, 2), "faces": f.reshape(-1, 3)}
+
+    def gather_pieces(self, shards, tet_ids, T: int) -> dict:
+        """Global piece CSR (torch CUDA tensors) from per-rank piece CSRs (``shards``: one dict
+        per rank of CUDA tensors piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask,
+        inc_off, inc_sphere; ``tet_ids``: per rank the CUDA int32 global ids of its tets), put
+        in global tet order by rpd_gather_pieces."""
+        import torch
+        world = len(shards)
+        if world > MAX_RANKS:
+            raise ValueError("too many ranks")
+        sh = _Shards()
+        sh.world, sh.T = world, int(T)
+        keep = []
+        for r, (d, ids) in enumerate(zip(shards, tet_ids)):
+            sh.n_tets[r] = int(ids.numel())
+            for k in ("piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
+                      "inc_off", "inc_sphere"):
+                t = d[k].contiguous()
+                keep.append(t)
+                getattr(sh, k)[r] = t.data_ptr() if t.numel() else None
+            ids = ids.to(torch.int32).contiguous()
+            keep.append(ids)
+            sh.tet_ids[r] = ids.data_ptr() if ids.numel() else None
+        npc = sum(int(d["piece_sphere"].numel()) for d in shards)
+        ninc = sum(int(d["inc_sphere"].numel()) for d in shards)
+        dev = shards[0]["piece_vol"].device
+        out = {"piece_off": torch.empty(T + 1, dtype=torch.int32, device=dev),
+               "piece_sphere": torch.empty(npc, dtype=torch.int32, device=dev),
+               "piece_vol": torch.empty(npc, dtype=torch.float64, device=dev),
+               "piece_m1": torch.empty((npc, 3), dtype=torch.float64, device=dev),
+               "piece_facemask": torch.empty(npc, dtype=torch.uint8, device=dev),
+               "inc_off": torch.empty(npc + 1, dtype=torch.int32, device=dev),
+               "inc_sphere": torch.empty(ninc, dtype=torch.int32, device=dev)}
+        self._check(self.L.rpd_gather_pieces(self.h, C.byref(sh), *[
+            self._p(out[k]) for k in ("piece_off", "piece_sphere", "piece_vol", "piece_m1",
+                                      "piece_facemask", "inc_off", "inc_sphere")]))
+        return out
 
     def stats(self) -> dict:
         s = _Stats()

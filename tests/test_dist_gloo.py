@@ -1,6 +1,8 @@
 """Multi-rank path on CPU (gloo, world_size 2): block-cyclic tet shards of the oracle's
-results all-gathered and reordered equal the single-rank result byte for byte (SURVEY.md
-§8(e) P8).  The CUDA kernels are per-tet independent, so the same holds on NCCL."""
+results all-gathered (dist.all_gather_pieces, the collective of the gather) and reordered
+equal the single-rank result byte for byte.  The CUDA kernels are
+per-tet independent, so the same holds on NCCL; the reorder kernel (rpd_gather_pieces) is
+tested against a single-GPU run in tests/test_gpu_gather.py."""
 import os
 import socket
 
@@ -27,17 +29,47 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2403_18761_b200.dist import gather_pieces, shard_tets
+        from paper_2403_18761_b200.dist import all_gather_pieces, shard_tets
         w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
         ids = shard_tets(w.T, world, rank, block=256)
         r = oracle.rpd_workload(w, tet_ids=ids)
         local = {k: torch.as_tensor(np.asarray(v)) for k, v in r.items() if k != "stats"}
         local["piece_m1"] = local["piece_m1"].reshape(-1, 3)
-        out = gather_pieces(local, ids, w.T)
+        shards = all_gather_pieces(local)
         if rank == 0:
-            q.put({k: v.numpy() for k, v in out.items()})
+            q.put(_reorder([{k: v.numpy() for k, v in d.items()} for d in shards],
+                           [shard_tets(w.T, world, s, block=256) for s in range(world)], w.T))
     finally:
         dist.destroy_process_group()
+
+
+def _reorder(shards, ids, T):
+    """Test-side reorder of all-gathered per-rank CSRs into global tet order (the product path
+    does this in rpd_gather_pieces, tested against the single-GPU result in -m gpu)."""
+    per_tet = [None] * T
+    for d, tid in zip(shards, ids):
+        po, io = d["piece_off"], d["inc_off"]
+        for a, t in enumerate(tid):
+            pcs = []
+            for p in range(po[a], po[a + 1]):
+                pcs.append((d["piece_sphere"][p], d["piece_vol"][p], tuple(d["piece_m1"][p]),
+                            d["piece_facemask"][p], list(d["inc_sphere"][io[p]:io[p + 1]])))
+            per_tet[t] = pcs
+    out = {k: [] for k in ("piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
+                           "inc_sphere")}
+    off, ioff = [0], [0]
+    for pcs in per_tet:
+        for (s, v, m, f, inc) in pcs:
+            out["piece_sphere"].append(s)
+            out["piece_vol"].append(v)
+            out["piece_m1"].append(m)
+            out["piece_facemask"].append(f)
+            out["inc_sphere"] += inc
+            ioff.append(len(out["inc_sphere"]))
+        off.append(len(out["piece_sphere"]))
+    out = {k: np.array(v) for k, v in out.items()}
+    out["piece_off"], out["inc_off"] = np.array(off, np.int32), np.array(ioff, np.int32)
+    return out
 
 
 def test_gather_equals_single_rank():
