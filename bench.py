@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--partial-iters", type=int, default=-1,
                     help="partial updates per step (-1: all batches of the config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-small", action="store_true",
+                    help="skip the M = 1 / M = 10 partial-update latency side measurement")
     ap.add_argument("--no-euler", action="store_true",
                     help="skip the fractional-Euler (NEXT-1) side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -424,6 +426,36 @@ def main():
                          "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find); "
                          "medial_mesh_ms = dual medial mesh extraction (host-timed, two syncs)"}
 
+    # ---- the paper's regime of few insertions per iteration ("also report
+    # M = 1 and M = 10 per-iteration latency"; "few (even single) spheres"): the
+    # same C3 start, batches of M = 1 and M = 10 spheres, per-update device time
+    small = None
+    if world == 1 and args.config == "C4" and not args.no_small:
+        small = {}
+        t_, n_, mode_, _, _ = W.CONFIGS["C3"]
+        for M in (1, 10):
+            ws = W.make_shape_workload(f"C4m{M}", t_, n_, seed=0, radius_mode=mode_,
+                                       n_batches=6, batch_m=M, clusters=min(M, 10))
+            ctx.relations(d_verts, d_tets, to_dev(ws.spheres), to_dev(ws.nbr_off),
+                          to_dev(ws.nbr_idx))
+            ctx.clip()
+            n_prev, lat = ws.N, []
+            for b, (sph, off, idx) in enumerate(ws.batches):
+                args_b = (to_dev(sph), to_dev(off), to_dev(idx),
+                          to_dev(np.arange(n_prev, len(sph), dtype=np.int32)))
+                n_prev = len(sph)
+                torch.cuda.synchronize()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                _, nd = ctx.update_partial(*args_b)
+                ev1.record()
+                torch.cuda.synchronize()
+                if b > 0:   # the first update warms the new shapes up
+                    lat.append((ev0.elapsed_time(ev1), nd))
+            small[f"M{M}"] = {"partial_ms": float(np.median([x[0] for x in lat])),
+                              "dirty_tets": float(np.median([x[1] for x in lat])),
+                              "updates": len(lat)}
+
     # ---- roofline of the dominant kernel
     fmed = float(np.median([r["filter_ms"] for r in recs]))
     cmed = float(np.median([r["clip_ms"] for r in recs]))
@@ -479,6 +511,7 @@ def main():
                 "note": "the bench step (full RPD + partial updates) through the C ABI with pinned "
                         "host inputs and a pinned host download of the final pieces"},
         "euler": euler,
+        "partial_small_m": small,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches // max(args.steps, 1)),
     }
