@@ -347,3 +347,35 @@ def test_medial_mesh_c3(ctx):
     assert len(got["faces"]) > 1000
     for (i, j, k) in got["faces"][:: max(1, len(got["faces"]) // 2000)].tolist():
         assert (i, j) in E and (i, k) in E and (j, k) in E
+
+
+def test_euler_topology_c4_partial_equals_full(ctx):
+    """BASELINE.json configs[3] at full size with the Euler / topology data on: after the 10
+    partial updates (M = 500 each) the per-sphere Euler sums, CC numbers and the medial mesh
+    equal those of a full recompute on the final sphere set (R11/R12: pieces of dirty tets are
+    recomputed, clean ones kept)."""
+    w = W.make_config("C4")
+    ctx.set_euler(w.tets, len(w.verts))
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        n_old = w.N
+        for (sph, off, idx) in w.batches:
+            ctx.update_partial(sph, off, idx, np.arange(n_old, len(sph), dtype=np.int32))
+            n_old = len(sph)
+        zero_hits = ctx.stats()["zero_hits"]
+        part = ctx.download_euler()
+        part.update(ctx.download_topology())
+        part_mm = ctx.medial_mesh()
+        sph, off, idx = w.batches[-1]
+        ctx.relations(w.verts, w.tets, sph, off, idx)
+        ctx.clip()
+        full = ctx.download_euler()
+        full.update(ctx.download_topology())
+        full_mm = ctx.medial_mesh()
+    finally:
+        ctx.set_euler(None, 0)
+    for k in ("rpc_sum", "rpf_sum", "rpc_cc", "rpf_cc"):
+        assert np.array_equal(part[k], full[k]), (k, zero_hits)
+    assert np.array_equal(part_mm["edges"], full_mm["edges"])
+    assert np.array_equal(part_mm["faces"], full_mm["faces"])

@@ -9,6 +9,10 @@ import torch
 
 import paper_2403_18761_b200 as P
 import rpd_workloads as W
+if len(sys.argv) > 2:   # a prebuilt library variant
+    import paper_2403_18761_b200.rpd as R
+    R._lib = None
+    R.load_library(sys.argv[2])
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 ws = W.make_shape_workload(f"C4m{M}", 200_000, 20_000, seed=0, radius_mode="uniform",
