@@ -128,7 +128,10 @@ struct MergeDst {
   unsigned long long* p_radj;
 };
 
-constexpr int MT = 256;  // tets per merge tile (one block)
+#ifndef RPD_MERGE_MT
+#define RPD_MERGE_MT 256
+#endif
+constexpr int MT = RPD_MERGE_MT;  // tets per merge tile (one block of MT threads)
 
 // block-wide copy dst[k] = f(src[k]), k < n, with 8 independent loads in flight per thread
 // before their stores (the source and destination sets never overlap)
@@ -167,7 +170,7 @@ __device__ __forceinline__ int tile_seg(const int* off, int n, int q) {
 // staged in shared memory, then the block copies the tile's candidates, pieces and incidences
 // (each a contiguous destination range) with coalesced element loops; an element's tet is
 // found by binary search over the staged offsets (no global-memory searches).
-__global__ void __launch_bounds__(256) k_merge_copy(int64_t T, const int32_t* __restrict__ dpos,
+__global__ void __launch_bounds__(MT) k_merge_copy(int64_t T, const int32_t* __restrict__ dpos,
                                                     MergeSrc o, MergeSrc n, MergeDst D) {
   __shared__ int s_nc[MT + 1], s_np[MT + 1], s_ni[MT + 1];
   __shared__ int s_sc[MT], s_sp[MT], s_si[MT], s_nw[MT], s_sw[MT];
@@ -329,7 +332,7 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
              pn.rpf_j.as<int32_t>(),   pn.rpf_e.as<long long>(), pn.sfm.as<uint8_t>(),
              pn.rfm.as<uint8_t>(),     pn.radj.as<unsigned long long>()};
   if (T > 0) {
-    k_merge_copy<<<nblk(T, MT), 256, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
+    k_merge_copy<<<nblk(T, MT), MT, 0, c->stream>>>(T, c->d_pos.as<int32_t>(), o, n, D);
     ++c->launches;
   }
   return cudaGetLastError();
