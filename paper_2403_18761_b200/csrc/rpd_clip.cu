@@ -47,6 +47,9 @@
 #ifndef RPD_CLIP_MID_VPL
 #define RPD_CLIP_MID_VPL 2  // vertex slots per lane of the middle (first overflow) tier, GW = 32
 #endif
+#ifndef RPD_CLIP_SMALL
+#define RPD_CLIP_SMALL 2048  // below this many pairs the 64-slot tier clips all pairs directly
+#endif
 #ifndef RPD_CLIP_MID32
 #define RPD_CLIP_MID32 0    // 1: a 32-slot tier (GW = 32, one slot per lane) before the middle one (measured slower)
 #endif
@@ -1302,7 +1305,20 @@ static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pa
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
                         int wide) {
+  c->clip_small = 0;
   if (n_pairs == 0) return cudaSuccess;
+  if (!wide && n_pairs < RPD_CLIP_SMALL) {
+    // few pairs (small partial updates): latency, not throughput -- one pass of the 64-slot
+    // tier over every pair instead of the fast tier plus a re-run of its overflows
+    c->clip_small = 1;
+    return c->euler
+               ? launch_clip_t<32, RPD_CLIP_MID_VPL, true>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                           cand_idx, moff,
+                                                           c->p_over2.as<int32_t>(), nullptr)
+               : launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs, nullptr, pair_tet,
+                                                            tet_ids, cand_idx, moff,
+                                                            c->p_over2.as<int32_t>(), nullptr);
+  }
   return c->euler ? launch_clip_eu<true>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide)
                   : launch_clip_eu<false>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide);
 }
@@ -1334,6 +1350,13 @@ static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const
 
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff) {
+  if (c->clip_small)  // only the 64-slot tier's overflows remain, for the 128-slot tier
+    return c->euler ? launch_clip_t<32, 4, true>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
+                                                 pair_tet, tet_ids, cand_idx, moff, nullptr,
+                                                 c->p_over2.as<int32_t>())
+                    : launch_clip_t<32, 4, false>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
+                                                  pair_tet, tet_ids, cand_idx, moff, nullptr,
+                                                  c->p_over2.as<int32_t>());
   return c->euler ? launch_overflow_eu<true>(c, pair_tet, tet_ids, cand_idx, moff)
                   : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff);
 }
