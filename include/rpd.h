@@ -76,8 +76,11 @@ enum {
   RPD_OPT_STREAM = 3,        /* value = (intptr_t) cudaStream_t to switch the ctx stream */
   RPD_OPT_CLIP_WIDE = 4,     /* 1: clip every pair with the wide (128-vertex) kernel instead of
                                 only the pairs that overflow the fast (32-vertex) one; for tests */
-  RPD_OPT_PROFILE = 5        /* 1: time the filter and clip kernels with CUDA events on the ctx
+  RPD_OPT_PROFILE = 5,       /* 1: time the filter and clip kernels with CUDA events on the ctx
                                 stream (rpd_stats.filter_ms / clip_ms) */
+  RPD_OPT_CLIP_TIERS = 6     /* 1: always the fast (16-vertex) tier and its overflow cascade, also
+                                for fewer than 2048 pairs (which otherwise go straight to the
+                                64-slot tier); for tests */
 };
 enum { RPD_FILTER_ALL_PAIRS = 0, RPD_FILTER_PRUNED = 1 };
 rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);

@@ -225,6 +225,9 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
     case RPD_OPT_CLIP_WIDE:
       c->clip_wide = value ? 1 : 0;
       return RPD_OK;
+    case RPD_OPT_CLIP_TIERS:
+      c->clip_tiers = value ? 1 : 0;
+      return RPD_OK;
     case RPD_OPT_STREAM:
       if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
       c->own_stream = false;

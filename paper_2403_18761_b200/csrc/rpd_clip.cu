@@ -1307,7 +1307,7 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         int wide) {
   c->clip_small = 0;
   if (n_pairs == 0) return cudaSuccess;
-  if (!wide && n_pairs < RPD_CLIP_SMALL) {
+  if (!wide && n_pairs < RPD_CLIP_SMALL && !c->clip_tiers) {
     // few pairs (small partial updates): latency, not throughput -- one pass of the 64-slot
     // tier over every pair instead of the fast tier plus a re-run of its overflows
     c->clip_small = 1;

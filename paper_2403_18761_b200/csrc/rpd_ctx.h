@@ -167,6 +167,7 @@ struct rpd_ctx {
   void* pinned_dev = nullptr;  // its device-side address
   int clip_wide = 0;           // testing: run every pair through the wide kernel
   int clip_small = 0;          // the last clip ran the 64-slot tier on all pairs (few pairs)
+  int clip_tiers = 0;          // testing: always the fast tier + overflow cascade
 
   // fractional Euler characteristics (rpd_euler.cu; rpd_set_euler)
   int euler = 0;               // payloads set for the current tets

@@ -188,6 +188,10 @@ class RPDContext:
         """Testing: route every pair through the wide (128-vertex) clip kernel."""
         self._check(self.L.rpd_set_option(self.h, OPT_CLIP_WIDE, int(bool(on))))
 
+    def set_clip_tiers(self, on: bool):
+        """Testing: the fast clip tier and its overflow cascade also for < 2048 pairs."""
+        self._check(self.L.rpd_set_option(self.h, 6, int(bool(on))))
+
     def set_profile(self, on: bool):
         """Time the filter and clip kernels with CUDA events (stats filter_ms / clip_ms)."""
         self._check(self.L.rpd_set_option(self.h, OPT_PROFILE, int(bool(on))))

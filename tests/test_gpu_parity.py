@@ -239,3 +239,18 @@ def test_c5_sampled(ctx_pruned):
     s = np.zeros(w.T)
     np.add.at(s, piece_tet(got), got["piece_vol"])
     assert np.max(np.abs(s - vt) / vt) < 1e-9
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(1, degenerate=True),
+                                  lambda: W.make_c1(6, degenerate=True, big=True),
+                                  lambda: W.random_tiny(3, n_spheres=14, grid=2, coarse=True),
+                                  lambda: W.make_shape_workload("T3", 2000, 150, seed=3,
+                                                                cache=False)])
+def test_fast_tier_parity_small_inputs(ctx, make):
+    """Fewer than 2048 pairs normally go straight to the 64-slot tier; the fast 16-slot tier
+    and its overflow cascade, forced on the same small (and degenerate) inputs, agree."""
+    ctx.set_clip_tiers(True)
+    try:
+        check(ctx, make())
+    finally:
+        ctx.set_clip_tiers(False)
