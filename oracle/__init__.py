@@ -87,6 +87,12 @@ def lib():
             L.oracle_power_distance.restype = C.c_double
             L.oracle_power_distance.argtypes = [C.c_void_p, C.c_void_p]
             L.oracle_max_threads.restype = C.c_int
+            L.oracle_envelope.restype = None
+            L.oracle_envelope.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_void_p, C.c_int]
+            L.oracle_envelope_one.restype = C.c_double
+            L.oracle_envelope_one.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
             _lib = L
     return _lib
 
@@ -400,6 +406,32 @@ def medial_mesh(res):
                 if (int(adj[a]) >> b) & 1:
                     faces.add(tuple(sorted((i, j, js[b]))))
     return sorted(edges), sorted(faces)
+
+
+def envelope(samples, spheres, edges, faces, nthreads=0):
+    """Geometry preservation: per surface sample the minimum over the medial
+    mesh's spheres, cones (edges) and slabs (faces) of min_params |p - c| - r (golden-section
+    search on the convex interpolation parameters, see oracle.c); returns (g [S], prim [S]);
+    the envelope distance is max(g, 0)."""
+    smp = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 3)
+    sph = np.ascontiguousarray(spheres, dtype=np.float64).reshape(-1, 4)
+    e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+    f = np.ascontiguousarray(faces, dtype=np.int32).reshape(-1, 3)
+    g = np.zeros(len(smp))
+    prim = np.zeros(len(smp), np.int32)
+    lib().oracle_envelope(smp.ctypes.data, len(smp), sph.ctypes.data, len(sph),
+                          e.ctypes.data if len(e) else None, len(e),
+                          f.ctypes.data if len(f) else None, len(f), g.ctypes.data,
+                          prim.ctypes.data, int(nthreads))
+    return g, prim
+
+
+def envelope_one(p, spheres, ids):
+    """Signed value of one primitive (1 id: sphere, 2: cone, 3: slab) at p."""
+    pp = np.ascontiguousarray(p, dtype=np.float64)
+    sph = np.ascontiguousarray(spheres, dtype=np.float64).reshape(-1, 4)
+    ii = np.ascontiguousarray(ids, dtype=np.int32)
+    return lib().oracle_envelope_one(pp.ctypes.data, sph.ctypes.data, len(ii) - 1, ii.ctypes.data)
 
 
 def max_threads() -> int:

@@ -1043,3 +1043,106 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------ envelope distance
+ *
+ * Geometry preservation (Sec. 4.3): "For each surface sample, we compute its
+ * distance to the closest enveloping volume of the medial mesh (sphere, cone, slab ...) in GPU".
+ * A medial cone is the union of the spheres linearly interpolated between two medial spheres,
+ * a slab between three.  The signed value of a primitive at p is
+ *     g = min over the interpolation parameters of  |p - c(t)| - r(t)
+ * (t in [0, 1] for a cone, (u, v) >= 0, u + v <= 1 for a slab); the distance to the envelope
+ * is max(min over primitives of g, 0).  |p - c(t)| - r(t) is convex in the parameters (a norm of
+ * an affine map minus an affine map), so the oracle minimises it by golden-section search: on t
+ * for a cone, nested (u outer, v inner) for a slab -- no closed form is used here. */
+
+static double env_g(const double* p, const double* c, double r) {
+  double dx = p[0] - c[0], dy = p[1] - c[1], dz = p[2] - c[2];
+  return sqrt(dx * dx + dy * dy + dz * dz) - r;
+}
+
+/* value of the (u, v) interpolated sphere of (s1, s2, s3) at p */
+static double env_gs(const double* p, const double* s1, const double* s2, const double* s3,
+                     double u, double v) {
+  double c[3];
+  for (int k = 0; k < 3; ++k) c[k] = s1[k] + u * (s2[k] - s1[k]) + v * (s3[k] - s1[k]);
+  return env_g(p, c, s1[3] + u * (s2[3] - s1[3]) + v * (s3[3] - s1[3]));
+}
+
+static const double GOLD = 0.6180339887498949;
+
+static double env_cone(const double* p, const double* s1, const double* s2) {
+  double a = 0.0, b = 1.0;
+  for (int it = 0; it < 120; ++it) {
+    double x1 = b - GOLD * (b - a), x2 = a + GOLD * (b - a);
+    if (env_gs(p, s1, s2, s1, x1, 0.0) <= env_gs(p, s1, s2, s1, x2, 0.0)) b = x2;
+    else a = x1;
+  }
+  double t = 0.5 * (a + b), g = env_gs(p, s1, s2, s1, t, 0.0);
+  double g0 = env_gs(p, s1, s2, s1, 0.0, 0.0), g1 = env_gs(p, s1, s2, s1, 1.0, 0.0);
+  return fmin(g, fmin(g0, g1));
+}
+
+/* min over v in [0, 1 - u] at fixed u */
+static double env_slab_u(const double* p, const double* s1, const double* s2, const double* s3,
+                         double u) {
+  double a = 0.0, b = 1.0 - u;
+  for (int it = 0; it < 90; ++it) {
+    double x1 = b - GOLD * (b - a), x2 = a + GOLD * (b - a);
+    if (env_gs(p, s1, s2, s3, u, x1) <= env_gs(p, s1, s2, s3, u, x2)) b = x2;
+    else a = x1;
+  }
+  double v = 0.5 * (a + b);
+  double g = env_gs(p, s1, s2, s3, u, v);
+  return fmin(g, fmin(env_gs(p, s1, s2, s3, u, 0.0), env_gs(p, s1, s2, s3, u, 1.0 - u)));
+}
+
+static double env_slab(const double* p, const double* s1, const double* s2, const double* s3) {
+  double a = 0.0, b = 1.0;
+  for (int it = 0; it < 90; ++it) {
+    double x1 = b - GOLD * (b - a), x2 = a + GOLD * (b - a);
+    if (env_slab_u(p, s1, s2, s3, x1) <= env_slab_u(p, s1, s2, s3, x2)) b = x2;
+    else a = x1;
+  }
+  double u = 0.5 * (a + b);
+  return fmin(env_slab_u(p, s1, s2, s3, u),
+              fmin(env_slab_u(p, s1, s2, s3, 0.0), env_slab_u(p, s1, s2, s3, 1.0)));
+}
+
+/* per sample: the minimum signed value over all primitives (g_out) and the first primitive
+ * reaching it (prim_out: sphere i -> i, cone e -> N + e, slab f -> N + NE + f) */
+void oracle_envelope(const double* samples, int64_t S, const double* spheres, int64_t N,
+                     const int32_t* edges, int64_t NE, const int32_t* faces, int64_t NF,
+                     double* g_out, int32_t* prim_out, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 4)
+#endif
+  for (int64_t s = 0; s < S; ++s) {
+    const double* p = samples + 3 * s;
+    double best = INFINITY;
+    int32_t arg = -1;
+    for (int64_t i = 0; i < N; ++i) {
+      double g = env_g(p, spheres + 4 * i, spheres[4 * i + 3]);
+      if (g < best) { best = g; arg = (int32_t)i; }
+    }
+    for (int64_t e = 0; e < NE; ++e) {
+      double g = env_cone(p, spheres + 4 * edges[2 * e], spheres + 4 * edges[2 * e + 1]);
+      if (g < best) { best = g; arg = (int32_t)(N + e); }
+    }
+    for (int64_t f = 0; f < NF; ++f) {
+      double g = env_slab(p, spheres + 4 * faces[3 * f], spheres + 4 * faces[3 * f + 1],
+                          spheres + 4 * faces[3 * f + 2]);
+      if (g < best) { best = g; arg = (int32_t)(N + NE + f); }
+    }
+    g_out[s] = best;
+    prim_out[s] = arg;
+  }
+}
+
+/* one primitive at one point (tests) */
+double oracle_envelope_one(const double* p, const double* spheres, int kind, const int32_t* ids) {
+  if (kind == 0) return env_g(p, spheres + 4 * ids[0], spheres[4 * ids[0] + 3]);
+  if (kind == 1) return env_cone(p, spheres + 4 * ids[0], spheres + 4 * ids[1]);
+  return env_slab(p, spheres + 4 * ids[0], spheres + 4 * ids[1], spheres + 4 * ids[2]);
+}

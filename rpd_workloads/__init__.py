@@ -493,3 +493,24 @@ def stats(w: Workload):
     k = np.diff(w.nbr_off)
     return {"T": w.T, "N": w.N, "V": int(len(w.verts)), "k_site_mean": float(k.mean()),
             "k_site_max": int(k.max()) if len(k) else 0, "hidden": int((k == 0).sum())}
+
+
+def boundary_samples(verts, tets, n: int, seed: int = 0):
+    """``n`` random points on the boundary surface of a tet mesh (the input shape's surface,
+    PAPER.md:532 "randomly sample surface points"): boundary faces are the tet faces that
+    belong to one tet; a face is drawn with probability proportional to its area and a point
+    uniformly inside it.  Input generation only (no method arithmetic)."""
+    t = np.asarray(tets)
+    faces = np.concatenate([t[:, [1, 2, 3]], t[:, [0, 2, 3]], t[:, [0, 1, 3]], t[:, [0, 1, 2]]])
+    key = np.sort(faces, axis=1)
+    _, inv, cnt = np.unique(key, axis=0, return_inverse=True, return_counts=True)
+    bnd = faces[cnt[inv.reshape(-1)] == 1]
+    v = np.asarray(verts)
+    a, b, c = v[bnd[:, 0]], v[bnd[:, 1]], v[bnd[:, 2]]
+    area = 0.5 * np.linalg.norm(np.cross(b - a, c - a), axis=1)
+    rng = np.random.default_rng(seed)
+    pick = rng.choice(len(bnd), size=n, p=area / area.sum())
+    r1, r2 = rng.random(n), rng.random(n)
+    s = np.sqrt(r1)
+    return (1 - s)[:, None] * a[pick] + (s * (1 - r2))[:, None] * b[pick] + \
+        (s * r2)[:, None] * c[pick]

@@ -496,3 +496,70 @@ def test_medial_faces_equal_explicit_extraction(make):
     edges = set(oracle.medial_mesh(r)[0])
     for (i, j, k) in faces:
         assert {(i, j), (i, k), (j, k)} <= edges
+
+
+# ----------------------------------------------------------------------------- envelope distance
+# distance of surface samples to the enveloping
+# volume of the medial mesh (sphere / cone / slab)
+
+ENV = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "envelope_examples.json")))
+
+
+@pytest.mark.parametrize("case", ENV["cases"])
+def test_envelope_spec_examples(case):
+    d = oracle.envelope_one(case["p"], np.array(case["spheres"], float), case["ids"])
+    assert max(d, 0.0) == pytest.approx(case["distance"], abs=1e-12)
+
+
+def _seg_dist(p, a, b):
+    d = b - a
+    t = np.clip(np.dot(p - a, d) / np.dot(d, d), 0.0, 1.0)
+    return np.linalg.norm(p - (a + t * d))
+
+
+def test_envelope_equal_radii_cone_is_capsule():
+    """Equal radii: the cone is a capsule -- value = distance to the segment minus r."""
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        a, b, p = rng.normal(size=3), rng.normal(size=3), 3 * rng.normal(size=3)
+        r = rng.uniform(0.1, 1.0)
+        sph = np.array([[*a, r], [*b, r]])
+        assert oracle.envelope_one(p, sph, [0, 1]) == pytest.approx(_seg_dist(p, a, b) - r,
+                                                                    abs=1e-10)
+
+
+def test_envelope_slab_vs_dense_sampling():
+    """SPEC.md: a random slab at a random p matches the brute-force minimum over densely
+    sampled (u, v) (10^4 samples of the triangle) within 1e-4 -- the oracle, being exact up to
+    rounding, is at most the sampled minimum and within the sampling error of it."""
+    rng = np.random.default_rng(1)
+    n = 141
+    u, v = np.meshgrid(np.linspace(0, 1, n), np.linspace(0, 1, n))
+    keep = u + v <= 1.0
+    u, v = u[keep], v[keep]
+    for _ in range(60):
+        sph = np.c_[rng.normal(size=(3, 3)), rng.uniform(0.0, 0.8, 3)]
+        p = 2.5 * rng.normal(size=3)
+        c = sph[0, :3] + u[:, None] * (sph[1, :3] - sph[0, :3]) + v[:, None] * (sph[2, :3] - sph[0, :3])
+        r = sph[0, 3] + u * (sph[1, 3] - sph[0, 3]) + v * (sph[2, 3] - sph[0, 3])
+        brute = np.min(np.linalg.norm(p - c, axis=1) - r)
+        got = oracle.envelope_one(p, sph, [0, 1, 2])
+        assert got <= brute + 1e-12 and brute - got < 1e-3
+
+
+def test_envelope_min_over_primitives():
+    """The per-sample value is the minimum over every sphere, cone and slab; a slab is never
+    above its cones, a cone never above its spheres (they belong to its family)."""
+    rng = np.random.default_rng(2)
+    sph = np.c_[rng.uniform(0, 10, (6, 3)), rng.uniform(0, 1.5, 6)]
+    edges = np.array([[0, 1], [1, 2], [0, 2], [3, 4]], np.int32)
+    faces = np.array([[0, 1, 2]], np.int32)
+    smp = rng.uniform(-2, 12, (40, 3))
+    g, prim = oracle.envelope(smp, sph, edges, faces)
+    for s in range(len(smp)):
+        vals = [oracle.envelope_one(smp[s], sph, [i]) for i in range(6)] + \
+               [oracle.envelope_one(smp[s], sph, list(e)) for e in edges] + \
+               [oracle.envelope_one(smp[s], sph, list(f)) for f in faces]
+        assert g[s] == min(vals) and vals[prim[s]] == g[s]
+        assert vals[10] <= min(vals[6], vals[7], vals[8]) + 1e-12
+        assert vals[6] <= min(vals[0], vals[1]) + 1e-12
