@@ -399,6 +399,19 @@ def main():
                 torch.cuda.synchronize()
                 if s >= args.warmup:
                     mm.append(1e3 * (time.perf_counter() - t0))
+            # NEXT-4: envelope distance of 100k boundary samples to that medial mesh
+            smp = to_dev(W.boundary_samples(w.verts, w.tets, 100_000, seed=5))
+            env = []
+            for s in range(args.warmup + args.steps):
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                _, _, n_eval = ctx.envelope(smp, d_base[0], med["edges"], med["faces"],
+                                            device=True)
+                ev1.record()
+                torch.cuda.synchronize()
+                if s >= args.warmup:
+                    env.append(ev0.elapsed_time(ev1))
+            n_prims = w.N + int(med["edges"].shape[0]) + int(med["faces"].shape[0])
         eu = ctx.download_euler(device=True)
         if world > 1:
             eu = allreduce_euler(eu)
@@ -421,6 +434,13 @@ def main():
                  "medial_mesh_ms": float(np.median(mm)) if cc_ms is not None else None,
                  "medial_edges": int(med["edges"].shape[0]) if cc_ms is not None else None,
                  "medial_faces": int(med["faces"].shape[0]) if cc_ms is not None else None,
+                 "envelope": {"samples": 100_000, "primitives": n_prims,
+                              "ms": float(np.median(env)), "pairs_evaluated": int(n_eval),
+                              "pairs_total": 100_000 * n_prims,
+                              "note": "NEXT-4 envelope distance (PAPER.md:520-542): boundary "
+                                      "samples vs the medial mesh's spheres/cones/slabs, "
+                                      "closed forms with exact tile culling"}
+                 if cc_ms is not None else None,
                  "note": "fractional Euler characteristics (PAPER.md:482-506) fused into the "
                          "clip; full_rpd_ms = relations + clip + per-sphere sums (CUDA events); "
                          "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find); "

@@ -294,6 +294,25 @@ rpd_status rpd_gather_pieces(rpd_ctx* ctx, const rpd_shards* shards, int32_t* pi
                              int32_t* piece_sphere, double* piece_vol, double* piece_m1,
                              uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
 
+/* ---- Envelope distance (Sec. 4.3)
+ *
+ * "For each surface sample, we compute its distance to the closest enveloping volume of the
+ * medial mesh (sphere, cone, slab ...) in GPU".  A cone is the family of spheres linearly
+ * interpolated between two medial spheres, a slab between three; the value of a primitive at
+ * p is min over the interpolation parameters of |p - c| - r and the envelope distance is
+ * max(min over primitives, 0).  Exact closed forms in fp64, brute force over
+ * all primitives with exact tile culling.
+ *   samples [S][3] double, spheres [N][4] double (x, y, z, r), edges [NE][2] / faces [NF][3]
+ *   int32 sphere ids (e.g. the medial mesh of rpd_medial_mesh); host or device pointers
+ *   g_out [S] double     the minimum value (negative inside the envelope)
+ *   prim_out [S] int32   the primitive reaching it (sphere i -> i, edge e -> N + e, face f ->
+ *                        N + NE + f; the smallest index among equal values)
+ *   *n_eval (host, may be NULL): (sample, primitive) pairs evaluated after culling
+ * No lattice requirement (geometry only; no combinatorial output). */
+rpd_status rpd_envelope(rpd_ctx* ctx, const double* samples, int64_t S, const double* spheres,
+                        int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
+                        int64_t NF, double* g_out, int32_t* prim_out, int64_t* n_eval);
+
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */
 typedef struct {

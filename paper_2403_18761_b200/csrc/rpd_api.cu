@@ -168,7 +168,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
-                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
   for (CandSet* x : cs) {
@@ -979,6 +979,40 @@ rpd_status rpd_gather_pieces(rpd_ctx* c, const rpd_shards* sh, int32_t* piece_of
   CK(launch_gather(c, sh, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask, inc_off,
                    inc_sphere), "gather");
   CK(cudaStreamSynchronize(c->stream), "gather");
+  return RPD_OK;
+}
+
+rpd_status rpd_envelope(rpd_ctx* c, const double* samples, int64_t S, const double* spheres,
+                        int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
+                        int64_t NF, double* g_out, int32_t* prim_out, int64_t* n_eval) {
+  if (!c) return RPD_EINVAL;
+  if (S < 0 || N < 0 || NE < 0 || NF < 0 || S > 0x7fffffff || N + NE + NF > 0x7fffffff ||
+      (S > 0 && (!samples || !g_out || !prim_out)) || (N > 0 && !spheres) ||
+      (NE > 0 && !edges) || (NF > 0 && !faces) || (S > 0 && N + NE + NF == 0))
+    return fail(c, RPD_EINVAL, "rpd_envelope: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const double *d_smp = nullptr, *d_sph = nullptr;
+  const int32_t *d_e = nullptr, *d_f = nullptr;
+  CK(resolve(c, samples, 3 * S, c->h_env, &d_smp), "stage samples");
+  CK(resolve(c, spheres, 4 * N, c->h_env2, &d_sph), "stage spheres");
+  CK(resolve(c, edges, 2 * NE, c->h_env3, &d_e), "stage edges");
+  CK(resolve(c, faces, 3 * NF, c->h_env4, &d_f), "stage faces");
+  const bool host_out = is_host_ptr(g_out) || is_host_ptr(prim_out);
+  CK(c->env_out.ensure((sizeof(double) + sizeof(int32_t)) * (S + 1) + 16), "alloc");
+  double* dg = host_out ? c->env_out.as<double>() : g_out;
+  int32_t* dp = host_out ? reinterpret_cast<int32_t*>(c->env_out.as<double>() + (S + 1)) : prim_out;
+  unsigned long long* ne = c->stats.as<unsigned long long>() + ST_ENV_EVAL;
+  CK(cudaMemsetAsync(ne, 0, sizeof(unsigned long long), c->stream), "memset");
+  CK(launch_envelope(c, d_smp, S, d_sph, N, d_e, NE, d_f, NF, dg, dp, ne), "envelope");
+  if (host_out && S > 0) {
+    CK(cudaMemcpyAsync(g_out, dg, sizeof(double) * S, cudaMemcpyDefault, c->stream), "download");
+    CK(cudaMemcpyAsync(prim_out, dp, sizeof(int32_t) * S, cudaMemcpyDefault, c->stream),
+       "download");
+  }
+  unsigned long long h_ne = 0;
+  CK(cudaMemcpyAsync(&h_ne, ne, sizeof(h_ne), cudaMemcpyDeviceToHost, c->stream), "download");
+  CK(cudaStreamSynchronize(c->stream), "envelope");
+  if (n_eval) *n_eval = (int64_t)h_ne;
   return RPD_OK;
 }
 

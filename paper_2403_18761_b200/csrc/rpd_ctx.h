@@ -65,7 +65,8 @@ enum StatIdx {
   ST_CLIP_CONSTR = 10,  // vertex constructions
   ST_CLIP_FAN = 11,     // fan triangles of the volume/moment integration
   ST_EU_OVER = 15,      // pieces with more than 64 radical facets (topology mode)
-  ST_N = 16
+  ST_ENV_EVAL = 16,     // envelope distance: (sample, primitive) evaluations
+  ST_N = 17
 };
 
 struct Stage {
@@ -130,6 +131,8 @@ struct rpd_ctx {
   rpd::DevBuf k_tet, k_words, slab, w_off;
   rpd::DevBuf cand_long;   // compaction: count + tets with more than 16 candidates
   rpd::DevBuf g_cnt;       // multi-GPU gather: per global tet piece / incidence counts, offsets
+  rpd::DevBuf env_buf, env_out, h_env;  // envelope distance (NEXT-4): scratch, outputs, inputs
+  rpd::DevBuf h_env2, h_env3, h_env4;
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
   rpd::DevBuf bvh_all;     // leaf + super boxes of the whole mesh (valid per staged mesh)
   bool bvh_all_valid = false;
@@ -251,6 +254,11 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
 cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
                           int32_t* piece_sphere, double* piece_vol, double* piece_m1,
                           uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
+// envelope distance (rpd_envelope.cu)
+cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const double* sph,
+                            int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
+                            int64_t NF, double* g_out, int32_t* prim_out,
+                            unsigned long long* n_eval);
 // fractional Euler characteristics (rpd_euler.cu)
 cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
                                const int32_t* local_ids, int64_t T_local);

@@ -1,0 +1,389 @@
+// rpd_envelope.cu -- SURVEY.md §8(f) NEXT-4: geometry preservation, the paper's second GPU
+// workload (Sec. 4.3): "For each surface sample, we compute its distance to
+// the closest enveloping volume of the medial mesh (sphere, cone, slab ...) in GPU".
+//
+// A medial cone is the family of spheres linearly interpolated between two medial spheres, a
+// slab between three.  The value of a primitive at p is
+//     g = min over the interpolation parameters of |p - c| - r,
+// convex in the parameters; the envelope distance of a sample is max(min over primitives, 0).
+// Closed forms (fp64):
+//   sphere  g = |p - c| - r
+//   cone    with d = c2 - c1, L = |d|, dr = r2 - r1, q = p - c1, a = q.d / L, h = dist to the
+//           axis: the stationary t = (a + dr h / sqrt(L^2 - dr^2)) / L (|n.d| = -dr for the unit
+//           normal n of the tangent direction), clamped to [0, 1] (1-D convex); if |dr| >= L one
+//           end sphere contains the other: the better end
+//   slab    the unit normal n of the stationary sphere satisfies n.e1 = -dr1, n.e2 = -dr2 (its
+//           in-plane part from the 2x2 Gram system), its out-of-plane part points to p's side;
+//           the touching centre c = p - rho n lies in the plane; if its (u, v) is inside the
+//           triangle that is the minimum, otherwise the minimum is on one of the three cones.
+//
+// B200 mapping: samples and primitives are sorted by the Morton code of their position (CUB
+// radix sort, a library primitive), primitives grouped by kind in tiles of 32 with the box of
+// their sphere centres and their largest radius.  A warp takes 32 consecutive sorted samples
+// (lane = sample), walks the tiles (spheres first, so every lane holds an upper bound early),
+// skips a tile when for every lane  dist(p, tile box) - r_max  exceeds its current best (an
+// exact lower bound of every member's value), else stages the tile's records in shared memory
+// and evaluates them.  Work per evaluated (sample, primitive) pair: ~10 (sphere), ~45 (cone),
+// ~150 (slab) fp64 flops.
+#include <cub/cub.cuh>
+
+#include "rpd_ctx.h"
+
+namespace rpd {
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+constexpr int ENV_TILE = 32;
+constexpr int ENV_WARPS = 4;
+
+struct EnvPrim {      // one primitive: up to three spheres (x, y, z, r); kind = #spheres - 1
+  double s[3][4];
+  int kind, id;       // id: the primitive's index in the caller's numbering
+};
+
+struct EnvTile {      // box of the tile's sphere centres and the largest radius
+  double lo[3], hi[3], rmax;
+  int first, count, kind;
+};
+
+__device__ __forceinline__ double env_norm(double x, double y, double z) {
+  return sqrt(fma(x, x, fma(y, y, z * z)));
+}
+
+__device__ __forceinline__ double env_sphere(const double* p, const double* s) {
+  return env_norm(p[0] - s[0], p[1] - s[1], p[2] - s[2]) - s[3];
+}
+
+__device__ double env_cone(const double* p, const double* s1, const double* s2) {
+  const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
+  const double dr = s2[3] - s1[3];
+  const double L2 = fma(d0, d0, fma(d1, d1, d2 * d2));
+  const double g1 = env_sphere(p, s1), g2 = env_sphere(p, s2);
+  if (!(dr * dr < L2)) return fmin(g1, g2);  // nested end spheres (or coincident centres)
+  const double q0 = p[0] - s1[0], q1 = p[1] - s1[1], q2 = p[2] - s1[2];
+  const double L = sqrt(L2);
+  const double a = fma(q0, d0, fma(q1, d1, q2 * d2)) / L;
+  const double h = sqrt(fmax(fma(q0, q0, fma(q1, q1, q2 * q2)) - a * a, 0.0));
+  double t = (a + dr * h / sqrt(L2 - dr * dr)) / L;
+  t = fmin(fmax(t, 0.0), 1.0);
+  const double g = env_norm(q0 - t * d0, q1 - t * d1, q2 - t * d2) - fma(t, dr, s1[3]);
+  return fmin(g, fmin(g1, g2));
+}
+
+__device__ double env_slab(const double* p, const double* s1, const double* s2,
+                           const double* s3) {
+  const double e1[3] = {s2[0] - s1[0], s2[1] - s1[1], s2[2] - s1[2]};
+  const double e2[3] = {s3[0] - s1[0], s3[1] - s1[1], s3[2] - s1[2]};
+  const double dr1 = s2[3] - s1[3], dr2 = s3[3] - s1[3];
+  const double g11 = fma(e1[0], e1[0], fma(e1[1], e1[1], e1[2] * e1[2]));
+  const double g12 = fma(e1[0], e2[0], fma(e1[1], e2[1], e1[2] * e2[2]));
+  const double g22 = fma(e2[0], e2[0], fma(e2[1], e2[1], e2[2] * e2[2]));
+  const double det = g11 * g22 - g12 * g12;
+  const double edges = fmin(env_cone(p, s1, s2), fmin(env_cone(p, s1, s3), env_cone(p, s2, s3)));
+  if (!(det > 1e-14 * g11 * g22)) return edges;  // (nearly) collinear centres
+  // in-plane part of the stationary sphere's unit normal: G [al, be] = [-dr1, -dr2]
+  const double al = (-dr1 * g22 + dr2 * g12) / det, be = (-dr2 * g11 + dr1 * g12) / det;
+  const double np2 = -al * dr1 - be * dr2;  // |n_plane|^2
+  if (!(np2 < 1.0)) return edges;
+  double N[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                 e1[0] * e2[1] - e1[1] * e2[0]};
+  const double nl = env_norm(N[0], N[1], N[2]);
+  N[0] /= nl;
+  N[1] /= nl;
+  N[2] /= nl;
+  const double q[3] = {p[0] - s1[0], p[1] - s1[1], p[2] - s1[2]};
+  const double z = fma(q[0], N[0], fma(q[1], N[1], q[2] * N[2]));
+  if (z == 0.0) return edges;
+  const double w = sqrt(1.0 - np2);
+  const double rho = fabs(z) / w;
+  const double sg = z > 0.0 ? 1.0 : -1.0;
+  double c[3];  // touching centre relative to s1: q - rho n
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = q[k] - rho * (al * e1[k] + be * e2[k] + sg * w * N[k]);
+  const double b1 = fma(c[0], e1[0], fma(c[1], e1[1], c[2] * e1[2]));
+  const double b2 = fma(c[0], e2[0], fma(c[1], e2[1], c[2] * e2[2]));
+  const double u = (b1 * g22 - b2 * g12) / det, v = (b2 * g11 - b1 * g12) / det;
+  if (u >= 0.0 && v >= 0.0 && u + v <= 1.0) {
+    const double g = rho - (s1[3] + u * dr1 + v * dr2);
+    return fmin(g, edges);
+  }
+  return edges;
+}
+
+__device__ __forceinline__ double env_eval(const double* p, const EnvPrim& e) {
+  if (e.kind == 0) return env_sphere(p, e.s[0]);
+  if (e.kind == 1) return env_cone(p, e.s[0], e.s[1]);
+  return env_slab(p, e.s[0], e.s[1], e.s[2]);
+}
+
+// ---- Morton ordering
+
+__device__ __forceinline__ unsigned long long spread3(unsigned long long x) {  // 20 bits used
+  x &= 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+__device__ __forceinline__ unsigned long long morton(const double* x, const double* lo,
+                                                     double inv) {
+  unsigned long long m = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double f = (x[k] - lo[k]) * inv;
+    f = fmin(fmax(f, 0.0), 1048575.0);
+    m |= spread3((unsigned long long)f) << k;
+  }
+  return m;
+}
+
+// primitives of one kind -> records + Morton keys of their centroid (kind in the top bits)
+__global__ void k_env_prims(int kind, int64_t n, int64_t id0, const double* __restrict__ sph,
+                            const int32_t* __restrict__ ids, EnvPrim* __restrict__ prims,
+                            unsigned long long* __restrict__ keys, int32_t* __restrict__ idx,
+                            const double* __restrict__ box, int64_t out0) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  EnvPrim e;
+  e.kind = kind;
+  e.id = (int)(id0 + x);
+  double cen[3] = {0.0, 0.0, 0.0};
+  for (int a = 0; a < 3; ++a) {
+    const int64_t sid = kind == 0 ? x : (a <= kind ? (int64_t)ids[(kind + 1) * x + a] : -1);
+    const int64_t src = sid >= 0 ? sid : (kind == 0 ? x : (int64_t)ids[(kind + 1) * x]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) e.s[a][c] = sph[4 * src + c];
+    if (a <= kind)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cen[c] += e.s[a][c] / (kind + 1);
+  }
+  prims[out0 + x] = e;
+  keys[out0 + x] = ((unsigned long long)kind << 62) |
+                   morton(cen, box, box[3]);
+  idx[out0 + x] = (int32_t)(out0 + x);
+}
+
+__global__ void k_env_sample_keys(int64_t S, const double* __restrict__ smp,
+                                  const double* __restrict__ box,
+                                  unsigned long long* __restrict__ keys,
+                                  int32_t* __restrict__ idx) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= S) return;
+  keys[x] = morton(smp + 3 * x, box, box[3]);
+  idx[x] = (int32_t)x;
+}
+
+// bounding box of the samples and sphere centres (lo[3], 1 / cell) -- one block
+__global__ void k_env_box(int64_t S, const double* __restrict__ smp, int64_t N,
+                          const double* __restrict__ sph, double* __restrict__ box) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t x = threadIdx.x; x < S + N; x += blockDim.x) {
+    const double* v = x < S ? smp + 3 * x : sph + 4 * (x - S);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], v[c]);
+      hi[c] = fmax(hi[c], v[c]);
+    }
+  }
+  __shared__ double s_lo[3][32], s_hi[3][32];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int c = 0; c < 3; ++c) {
+      s_lo[c][w] = lo[c];
+      s_hi[c][w] = hi[c];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ext = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      double a = s_lo[c][0], b = s_hi[c][0];
+      for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+        a = fmin(a, s_lo[c][k]);
+        b = fmax(b, s_hi[c][k]);
+      }
+      box[c] = a;
+      ext = fmax(ext, b - a);
+    }
+    box[3] = ext > 0.0 ? 1048575.0 / ext : 1.0;  // 20 bits per axis (the kind in bits 62-63)
+  }
+}
+
+// tiles of ENV_TILE consecutive sorted primitives of one kind
+__global__ void k_env_tiles(int64_t n_tiles, const int64_t* __restrict__ kind_end,
+                            const EnvPrim* __restrict__ prims, const int32_t* __restrict__ order,
+                            EnvPrim* __restrict__ sorted, EnvTile* __restrict__ tiles) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  // tiles never straddle kinds: kind k occupies tiles [tile_begin(k), tile_begin(k+1))
+  int64_t tb[4] = {0, 0, 0, 0};
+  for (int k = 0; k < 3; ++k) {
+    const int64_t b = k == 0 ? 0 : kind_end[k - 1];
+    tb[k + 1] = tb[k] + (kind_end[k] - b + ENV_TILE - 1) / ENV_TILE;
+  }
+  int kind = 0;
+  while (kind < 2 && t >= tb[kind + 1]) ++kind;
+  const int64_t begin = (kind == 0 ? 0 : kind_end[kind - 1]) + (t - tb[kind]) * ENV_TILE;
+  const int64_t end = min(begin + ENV_TILE, kind_end[kind]);
+  EnvTile T;
+  for (int c = 0; c < 3; ++c) {
+    T.lo[c] = 1e300;
+    T.hi[c] = -1e300;
+  }
+  T.rmax = -1e300;
+  T.first = (int)begin;
+  T.count = (int)(end - begin);
+  T.kind = kind;
+  for (int64_t x = begin; x < end; ++x) {
+    const EnvPrim e = prims[order[x]];
+    sorted[x] = e;
+    for (int a = 0; a <= e.kind; ++a) {
+      for (int c = 0; c < 3; ++c) {
+        T.lo[c] = fmin(T.lo[c], e.s[a][c]);
+        T.hi[c] = fmax(T.hi[c], e.s[a][c]);
+      }
+      T.rmax = fmax(T.rmax, e.s[a][3]);
+    }
+  }
+  tiles[t] = T;
+}
+
+// one warp per 32 sorted samples; tiles culled by their exact lower bound
+__global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
+    int64_t S, const double* __restrict__ smp, const int32_t* __restrict__ sorder,
+    int64_t n_tiles, const EnvTile* __restrict__ tiles, const EnvPrim* __restrict__ prims,
+    double* __restrict__ g_out, int32_t* __restrict__ prim_out,
+    unsigned long long* __restrict__ n_eval) {
+  __shared__ EnvPrim s_p[ENV_WARPS][ENV_TILE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long evals = 0;
+  for (int64_t base = gw * 32; base < S; base += nw * 32) {
+    const int64_t si = base + lane;
+    const bool valid = si < S;
+    const int64_t o = valid ? sorder[si] : 0;
+    const double p[3] = {valid ? smp[3 * o] : 0.0, valid ? smp[3 * o + 1] : 0.0,
+                         valid ? smp[3 * o + 2] : 0.0};
+    double best = valid ? 1e300 : -1e300;
+    int arg = -1;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+      const EnvTile T = tiles[t];
+      double dx = fmax(fmax(T.lo[0] - p[0], p[0] - T.hi[0]), 0.0);
+      double dy = fmax(fmax(T.lo[1] - p[1], p[1] - T.hi[1]), 0.0);
+      double dz = fmax(fmax(T.lo[2] - p[2], p[2] - T.hi[2]), 0.0);
+      const double lb = env_norm(dx, dy, dz) - T.rmax;
+      // (the lower bound is exact up to rounding: a small margin keeps the culling safe)
+      const bool need = lb <= best + 1e-9 * (fabs(best) + 1.0);
+      if (!__any_sync(0xffffffffu, need)) continue;
+      __syncwarp();
+      for (int x = lane; x < T.count; x += 32) s_p[warp][x] = prims[T.first + x];
+      __syncwarp();
+      if (need)
+        for (int x = 0; x < T.count; ++x) {
+          const double g = env_eval(p, s_p[warp][x]);
+          ++evals;
+          if (g < best || (g == best && s_p[warp][x].id < arg)) {
+            best = g;
+            arg = s_p[warp][x].id;
+          }
+        }
+    }
+    if (valid) {
+      g_out[o] = best;
+      prim_out[o] = arg;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, off);
+  if (lane == 0 && evals) atomicAdd(n_eval, evals);
+}
+
+template <class K, class V>
+static cudaError_t sort_pairs(rpd_ctx* c, K* k_in, K* k_out, V* v_in, V* v_out, int64_t n) {
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in, k_out, v_in, v_out,
+                                                  (int)n, 0, 64, c->stream);
+  if (e) return e;
+  if ((e = c->mm_tmp.ensure(bytes))) return e;
+  bytes = c->mm_tmp.cap;
+  e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bytes, k_in, k_out, v_in, v_out, (int)n, 0,
+                                      64, c->stream);
+  ++c->launches;
+  return e;
+}
+
+cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const double* sph,
+                            int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
+                            int64_t NF, double* g_out, int32_t* prim_out,
+                            unsigned long long* n_eval) {
+  const int64_t P = N + NE + NF;
+  const int64_t n_tiles = (N + ENV_TILE - 1) / ENV_TILE + (NE + ENV_TILE - 1) / ENV_TILE +
+                          (NF + ENV_TILE - 1) / ENV_TILE;
+  const size_t bytes = sizeof(EnvPrim) * 2 * (P + 1) + sizeof(EnvTile) * (n_tiles + 1) +
+                       sizeof(unsigned long long) * 2 * (P + S + 2) +
+                       sizeof(int32_t) * 2 * (P + S + 2) + sizeof(double) * 8 +
+                       sizeof(int64_t) * 4 + 256;
+  cudaError_t e = c->env_buf.ensure(bytes);
+  if (e) return e;
+  char* b = c->env_buf.as<char>();
+  auto take = [&](size_t n) {
+    char* r = b;
+    b += (n + 15) & ~size_t(15);
+    return r;
+  };
+  EnvPrim* prims = reinterpret_cast<EnvPrim*>(take(sizeof(EnvPrim) * (P + 1)));
+  EnvPrim* sorted = reinterpret_cast<EnvPrim*>(take(sizeof(EnvPrim) * (P + 1)));
+  EnvTile* tiles = reinterpret_cast<EnvTile*>(take(sizeof(EnvTile) * (n_tiles + 1)));
+  unsigned long long* pk = reinterpret_cast<unsigned long long*>(take(8 * (P + 1)));
+  unsigned long long* pk2 = reinterpret_cast<unsigned long long*>(take(8 * (P + 1)));
+  int32_t* pi = reinterpret_cast<int32_t*>(take(4 * (P + 1)));
+  int32_t* pi2 = reinterpret_cast<int32_t*>(take(4 * (P + 1)));
+  unsigned long long* sk = reinterpret_cast<unsigned long long*>(take(8 * (S + 1)));
+  unsigned long long* sk2 = reinterpret_cast<unsigned long long*>(take(8 * (S + 1)));
+  int32_t* si = reinterpret_cast<int32_t*>(take(4 * (S + 1)));
+  int32_t* si2 = reinterpret_cast<int32_t*>(take(4 * (S + 1)));
+  double* box = reinterpret_cast<double*>(take(sizeof(double) * 8));
+  int64_t* kind_end = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * 4));
+  k_env_box<<<1, 1024, 0, c->stream>>>(S, smp, N, sph, box);
+  ++c->launches;
+  const int64_t ends[3] = {N, N + NE, N + NE + NF};
+  if ((e = cudaMemcpyAsync(kind_end, ends, sizeof(ends), cudaMemcpyHostToDevice, c->stream)))
+    return e;
+  const int32_t* ids[3] = {nullptr, edges, faces};
+  const int64_t cnt[3] = {N, NE, NF};
+  int64_t off = 0;
+  for (int k = 0; k < 3; ++k) {
+    if (cnt[k] > 0) {
+      k_env_prims<<<nblk(cnt[k], 256), 256, 0, c->stream>>>(k, cnt[k], off, sph, ids[k], prims,
+                                                            pk, pi, box, off);
+      ++c->launches;
+    }
+    off += cnt[k];
+  }
+  if (P > 0 && (e = sort_pairs(c, pk, pk2, pi, pi2, P))) return e;
+  if (n_tiles > 0) {
+    k_env_tiles<<<nblk(n_tiles, 128), 128, 0, c->stream>>>(n_tiles, kind_end, prims, pi2, sorted,
+                                                           tiles);
+    ++c->launches;
+  }
+  if (S == 0) return cudaGetLastError();
+  k_env_sample_keys<<<nblk(S, 256), 256, 0, c->stream>>>(S, smp, box, sk, si);
+  ++c->launches;
+  if ((e = sort_pairs(c, sk, sk2, si, si2, S))) return e;
+  int64_t blocks = (S + 32 * ENV_WARPS - 1) / (32 * ENV_WARPS);
+  if (blocks > (int64_t)c->sms * 16) blocks = (int64_t)c->sms * 16;
+  k_env_dist<<<(unsigned)blocks, ENV_WARPS * 32, 0, c->stream>>>(S, smp, si2, n_tiles, tiles,
+                                                                 sorted, g_out, prim_out, n_eval);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rpd

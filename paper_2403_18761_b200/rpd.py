@@ -26,7 +26,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
-            "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces"]
+            "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope"]
 
 
 class RPDError(RuntimeError):
@@ -119,12 +119,13 @@ def load_library(path: str = LIB_PATH):
     L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
     L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
+    L.rpd_envelope.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(i64)]
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
               "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
               "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
-              "rpd_gather_pieces"):
+              "rpd_gather_pieces", "rpd_envelope"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -383,6 +384,22 @@ class RPDContext:
             self._p(out[k]) for k in ("piece_off", "piece_sphere", "piece_vol", "piece_m1",
                                       "piece_facemask", "inc_off", "inc_sphere")]))
         return out
+
+    def envelope(self, samples, spheres, edges, faces, device=False):
+        """Envelope distance of surface samples to the medial mesh's spheres / cones / slabs
+        (PAPER.md:520-542): returns (g [S], prim [S], evaluated pairs); distance = max(g, 0)."""
+        ps, ks = _ptr(samples, np.float64)
+        pp, kp = _ptr(spheres, np.float64)
+        pe, ke = _ptr(edges, np.int32)
+        pf, kf = _ptr(faces, np.int32)
+        S = int(np.prod(ks.shape)) // 3
+        g, prim = self._alloc([(S, np.float64), (S, np.int32)], device)
+        ne = C.c_int64()
+        self._check(self.L.rpd_envelope(self.h, ps, S, pp, int(np.prod(kp.shape)) // 4, pe,
+                                        int(np.prod(ke.shape)) // 2, pf,
+                                        int(np.prod(kf.shape)) // 3, self._p(g), self._p(prim),
+                                        C.byref(ne)))
+        return g, prim, ne.value
 
     def stats(self) -> dict:
         s = _Stats()
