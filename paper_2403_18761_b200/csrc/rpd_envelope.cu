@@ -18,13 +18,17 @@
 //           triangle that is the minimum, otherwise the minimum is on one of the three cones.
 //
 // B200 mapping: samples and primitives are sorted by the Morton code of their position (CUB
-// radix sort, a library primitive), primitives grouped by kind in tiles of 32 with the box of
-// their sphere centres and their largest radius.  A warp takes 32 consecutive sorted samples
-// (lane = sample), walks the tiles (spheres first, so every lane holds an upper bound early),
-// skips a tile when for every lane  dist(p, tile box) - r_max  exceeds its current best (an
-// exact lower bound of every member's value), else stages the tile's records in shared memory
-// and evaluates them.  Work per evaluated (sample, primitive) pair: ~10 (sphere), ~45 (cone),
-// ~150 (slab) fp64 flops.
+// radix sort, a library primitive; primitives by kind first), primitives in tiles of 32 of
+// one kind with the boxes of their balls and of their centres.  A warp takes 32
+// Morton-consecutive samples (lane = sample) and, per kind (spheres first: cheap, and a good
+// first bound), walks that kind's tiles outward from its own place in the Morton order.  A
+// tile is skipped when every lane's lower bound exceeds the lane's best: outside the box of
+// the balls the distance to it (a cone or slab is the convex hull of its balls), inside the
+// distance to the box of the centres minus the largest radius.  Otherwise each lane loads one
+// member and the warp evaluates all 32 members for each needing sample in turn, with a warp
+// min-reduce of (value, id): no idle lanes, no divergence by kind.  Work per evaluated
+// (sample, primitive) pair: ~10 (sphere), ~40 (cone), ~100 (slab) fp64 flops plus 1-5 fp64
+// square roots and divisions.
 #include <cub/cub.cuh>
 
 #include "rpd_ctx.h"
@@ -38,11 +42,12 @@ constexpr int ENV_WARPS = 4;
 
 struct EnvPrim {      // one primitive: up to three spheres (x, y, z, r); kind = #spheres - 1
   double s[3][4];
+  double k[12];       // per-primitive constants of the closed forms (env_prep)
   int kind, id;       // id: the primitive's index in the caller's numbering
 };
 
-struct EnvTile {      // box of the tile's sphere centres and the largest radius
-  double lo[3], hi[3], rmax;
+struct EnvTile {      // box of the tile's balls (centre -/+ radius), of its centres, largest radius
+  double lo[3], hi[3], clo[3], chi[3], rmax;
   int first, count, kind;
 };
 
@@ -58,16 +63,17 @@ __device__ double env_cone(const double* p, const double* s1, const double* s2) 
   const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
   const double dr = s2[3] - s1[3];
   const double L2 = fma(d0, d0, fma(d1, d1, d2 * d2));
-  const double g1 = env_sphere(p, s1), g2 = env_sphere(p, s2);
-  if (!(dr * dr < L2)) return fmin(g1, g2);  // nested end spheres (or coincident centres)
+  if (!(dr * dr < L2))  // nested end spheres (or coincident centres): the better end
+    return fmin(env_sphere(p, s1), env_sphere(p, s2));
   const double q0 = p[0] - s1[0], q1 = p[1] - s1[1], q2 = p[2] - s1[2];
   const double L = sqrt(L2);
   const double a = fma(q0, d0, fma(q1, d1, q2 * d2)) / L;
   const double h = sqrt(fmax(fma(q0, q0, fma(q1, q1, q2 * q2)) - a * a, 0.0));
   double t = (a + dr * h / sqrt(L2 - dr * dr)) / L;
   t = fmin(fmax(t, 0.0), 1.0);
-  const double g = env_norm(q0 - t * d0, q1 - t * d1, q2 - t * d2) - fma(t, dr, s1[3]);
-  return fmin(g, fmin(g1, g2));
+  // (the clamped stationary point is the minimum of the convex g(t) on [0, 1], the ends
+  // included)
+  return env_norm(q0 - t * d0, q1 - t * d1, q2 - t * d2) - fma(t, dr, s1[3]);
 }
 
 __device__ double env_slab(const double* p, const double* s1, const double* s2,
@@ -79,12 +85,14 @@ __device__ double env_slab(const double* p, const double* s1, const double* s2,
   const double g12 = fma(e1[0], e2[0], fma(e1[1], e2[1], e1[2] * e2[2]));
   const double g22 = fma(e2[0], e2[0], fma(e2[1], e2[1], e2[2] * e2[2]));
   const double det = g11 * g22 - g12 * g12;
-  const double edges = fmin(env_cone(p, s1, s2), fmin(env_cone(p, s1, s3), env_cone(p, s2, s3)));
-  if (!(det > 1e-14 * g11 * g22)) return edges;  // (nearly) collinear centres
+  // the minimum is the interior stationary point when it exists inside the triangle (g is
+  // convex), otherwise on the boundary: the three cones
+#define EDGES fmin(env_cone(p, s1, s2), fmin(env_cone(p, s1, s3), env_cone(p, s2, s3)))
+  if (!(det > 1e-14 * g11 * g22)) return EDGES;  // (nearly) collinear centres
   // in-plane part of the stationary sphere's unit normal: G [al, be] = [-dr1, -dr2]
   const double al = (-dr1 * g22 + dr2 * g12) / det, be = (-dr2 * g11 + dr1 * g12) / det;
   const double np2 = -al * dr1 - be * dr2;  // |n_plane|^2
-  if (!(np2 < 1.0)) return edges;
+  if (!(np2 < 1.0)) return EDGES;
   double N[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
                  e1[0] * e2[1] - e1[1] * e2[0]};
   const double nl = env_norm(N[0], N[1], N[2]);
@@ -93,7 +101,7 @@ __device__ double env_slab(const double* p, const double* s1, const double* s2,
   N[2] /= nl;
   const double q[3] = {p[0] - s1[0], p[1] - s1[1], p[2] - s1[2]};
   const double z = fma(q[0], N[0], fma(q[1], N[1], q[2] * N[2]));
-  if (z == 0.0) return edges;
+  if (z == 0.0) return EDGES;
   const double w = sqrt(1.0 - np2);
   const double rho = fabs(z) / w;
   const double sg = z > 0.0 ? 1.0 : -1.0;
@@ -103,17 +111,101 @@ __device__ double env_slab(const double* p, const double* s1, const double* s2,
   const double b1 = fma(c[0], e1[0], fma(c[1], e1[1], c[2] * e1[2]));
   const double b2 = fma(c[0], e2[0], fma(c[1], e2[1], c[2] * e2[2]));
   const double u = (b1 * g22 - b2 * g12) / det, v = (b2 * g11 - b1 * g12) / det;
-  if (u >= 0.0 && v >= 0.0 && u + v <= 1.0) {
-    const double g = rho - (s1[3] + u * dr1 + v * dr2);
-    return fmin(g, edges);
+  if (u >= 0.0 && v >= 0.0 && u + v <= 1.0) return rho - (s1[3] + u * dr1 + v * dr2);
+  return EDGES;
+#undef EDGES
+}
+
+// Per-primitive constants, so that an evaluation needs no division and at most two square
+// roots (the interior case of a slab none):
+//   cone  k0 = 1 / L^2, k1 = dr / (L sqrt(L^2 - dr^2)), k2 = 1 if the end spheres are nested:
+//         t = (q.d) k0 + k1 h, h = sqrt(|q|^2 - (q.d)^2 k0)
+//   slab  k0..2 = the inverse Gram matrix (i11, i12, i22), k3..5 = the in-plane part of the
+//         stationary normal, k6..8 = the unit plane normal N, k9 = w = sqrt(1 - |n_plane|^2),
+//         k10 = 1 / w, k11 = 1 if an interior stationary point can exist
+__device__ void env_prep(EnvPrim& e) {
+  for (int q = 0; q < 12; ++q) e.k[q] = 0.0;
+  if (e.kind == 1) {
+    const double* s1 = e.s[0];
+    const double* s2 = e.s[1];
+    const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
+    const double dr = s2[3] - s1[3];
+    const double L2 = d0 * d0 + d1 * d1 + d2 * d2;
+    if (!(dr * dr < L2)) {
+      e.k[2] = 1.0;
+      return;
+    }
+    e.k[0] = 1.0 / L2;
+    e.k[1] = dr / (sqrt(L2) * sqrt(L2 - dr * dr));
+  } else if (e.kind == 2) {
+    const double* s1 = e.s[0];
+    const double e1[3] = {e.s[1][0] - s1[0], e.s[1][1] - s1[1], e.s[1][2] - s1[2]};
+    const double e2[3] = {e.s[2][0] - s1[0], e.s[2][1] - s1[1], e.s[2][2] - s1[2]};
+    const double dr1 = e.s[1][3] - s1[3], dr2 = e.s[2][3] - s1[3];
+    const double g11 = e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2];
+    const double g12 = e1[0] * e2[0] + e1[1] * e2[1] + e1[2] * e2[2];
+    const double g22 = e2[0] * e2[0] + e2[1] * e2[1] + e2[2] * e2[2];
+    const double det = g11 * g22 - g12 * g12;
+    if (!(det > 1e-14 * g11 * g22)) return;  // (nearly) collinear centres: edges only
+    const double al = (-dr1 * g22 + dr2 * g12) / det, be = (-dr2 * g11 + dr1 * g12) / det;
+    const double np2 = -al * dr1 - be * dr2;
+    if (!(np2 < 1.0)) return;
+    double N[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                   e1[0] * e2[1] - e1[1] * e2[0]};
+    const double nl = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
+    e.k[0] = g22 / det;
+    e.k[1] = -g12 / det;
+    e.k[2] = g11 / det;
+    for (int c = 0; c < 3; ++c) {
+      e.k[3 + c] = al * e1[c] + be * e2[c];
+      e.k[6 + c] = N[c] / nl;
+    }
+    e.k[9] = sqrt(1.0 - np2);
+    e.k[10] = 1.0 / e.k[9];
+    e.k[11] = 1.0;
   }
-  return edges;
+}
+
+__device__ __forceinline__ double env_cone_k(const double* p, const EnvPrim& e) {
+  const double* s1 = e.s[0];
+  const double* s2 = e.s[1];
+  if (e.k[2] != 0.0) return fmin(env_sphere(p, s1), env_sphere(p, s2));
+  const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
+  const double q0 = p[0] - s1[0], q1 = p[1] - s1[1], q2 = p[2] - s1[2];
+  const double qd = fma(q0, d0, fma(q1, d1, q2 * d2));
+  const double h = sqrt(fmax(fma(q0, q0, fma(q1, q1, q2 * q2)) - qd * qd * e.k[0], 0.0));
+  const double t = fmin(fmax(fma(qd, e.k[0], e.k[1] * h), 0.0), 1.0);
+  return env_norm(q0 - t * d0, q1 - t * d1, q2 - t * d2) - fma(t, s2[3] - s1[3], s1[3]);
+}
+
+__device__ __forceinline__ double env_slab_k(const double* p, const EnvPrim& e) {
+  const double* s1 = e.s[0];
+  if (e.k[11] != 0.0) {
+    const double q[3] = {p[0] - s1[0], p[1] - s1[1], p[2] - s1[2]};
+    const double z = fma(q[0], e.k[6], fma(q[1], e.k[7], q[2] * e.k[8]));
+    if (z != 0.0) {
+      const double rho = fabs(z) * e.k[10];
+      const double sw = z > 0.0 ? e.k[9] : -e.k[9];
+      double c[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) c[a] = q[a] - rho * fma(sw, e.k[6 + a], e.k[3 + a]);
+      const double b1 = (c[0] * (e.s[1][0] - s1[0]) + c[1] * (e.s[1][1] - s1[1])) +
+                        c[2] * (e.s[1][2] - s1[2]);
+      const double b2 = (c[0] * (e.s[2][0] - s1[0]) + c[1] * (e.s[2][1] - s1[1])) +
+                        c[2] * (e.s[2][2] - s1[2]);
+      const double u = fma(e.k[0], b1, e.k[1] * b2), v = fma(e.k[1], b1, e.k[2] * b2);
+      if (u >= 0.0 && v >= 0.0 && u + v <= 1.0)
+        return rho - (s1[3] + u * (e.s[1][3] - s1[3]) + v * (e.s[2][3] - s1[3]));
+    }
+  }
+  return fmin(env_cone(p, e.s[0], e.s[1]), fmin(env_cone(p, e.s[0], e.s[2]),
+                                                 env_cone(p, e.s[1], e.s[2])));
 }
 
 __device__ __forceinline__ double env_eval(const double* p, const EnvPrim& e) {
   if (e.kind == 0) return env_sphere(p, e.s[0]);
-  if (e.kind == 1) return env_cone(p, e.s[0], e.s[1]);
-  return env_slab(p, e.s[0], e.s[1], e.s[2]);
+  if (e.kind == 1) return env_cone_k(p, e);
+  return env_slab_k(p, e);
 }
 
 // ---- Morton ordering
@@ -160,9 +252,9 @@ __global__ void k_env_prims(int kind, int64_t n, int64_t id0, const double* __re
 #pragma unroll
       for (int c = 0; c < 3; ++c) cen[c] += e.s[a][c] / (kind + 1);
   }
+  env_prep(e);
   prims[out0 + x] = e;
-  keys[out0 + x] = ((unsigned long long)kind << 62) |
-                   morton(cen, box, box[3]);
+  keys[out0 + x] = ((unsigned long long)kind << 62) | morton(cen, box, box[3]);
   idx[out0 + x] = (int32_t)(out0 + x);
 }
 
@@ -217,26 +309,30 @@ __global__ void k_env_box(int64_t S, const double* __restrict__ smp, int64_t N,
   }
 }
 
-// tiles of ENV_TILE consecutive sorted primitives of one kind
-__global__ void k_env_tiles(int64_t n_tiles, const int64_t* __restrict__ kind_end,
-                            const EnvPrim* __restrict__ prims, const int32_t* __restrict__ order,
-                            EnvPrim* __restrict__ sorted, EnvTile* __restrict__ tiles) {
+struct TileRanges {
+  int64_t tb[4];   // kind k owns tiles [tb[k], tb[k+1])
+  int64_t pb[4];   // and sorted primitives [pb[k], pb[k+1])
+};
+
+constexpr unsigned long long MORTON_MASK = (1ull << 62) - 1ull;
+
+// tiles of ENV_TILE consecutive Morton-sorted primitives of one kind (the sort key leads with
+// the kind), with the box of their balls
+__global__ void k_env_tiles(TileRanges R, const EnvPrim* __restrict__ prims,
+                            const int32_t* __restrict__ order,
+                            const unsigned long long* __restrict__ keys,
+                            EnvPrim* __restrict__ sorted, EnvTile* __restrict__ tiles,
+                            unsigned long long* __restrict__ tile_key) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n_tiles) return;
-  // tiles never straddle kinds: kind k occupies tiles [tile_begin(k), tile_begin(k+1))
-  int64_t tb[4] = {0, 0, 0, 0};
-  for (int k = 0; k < 3; ++k) {
-    const int64_t b = k == 0 ? 0 : kind_end[k - 1];
-    tb[k + 1] = tb[k] + (kind_end[k] - b + ENV_TILE - 1) / ENV_TILE;
-  }
+  if (t >= R.tb[3]) return;
   int kind = 0;
-  while (kind < 2 && t >= tb[kind + 1]) ++kind;
-  const int64_t begin = (kind == 0 ? 0 : kind_end[kind - 1]) + (t - tb[kind]) * ENV_TILE;
-  const int64_t end = min(begin + ENV_TILE, kind_end[kind]);
+  while (kind < 2 && t >= R.tb[kind + 1]) ++kind;
+  const int64_t begin = R.pb[kind] + (t - R.tb[kind]) * ENV_TILE;
+  const int64_t end = min(begin + ENV_TILE, R.pb[kind + 1]);
   EnvTile T;
   for (int c = 0; c < 3; ++c) {
-    T.lo[c] = 1e300;
-    T.hi[c] = -1e300;
+    T.lo[c] = T.clo[c] = 1e300;
+    T.hi[c] = T.chi[c] = -1e300;
   }
   T.rmax = -1e300;
   T.first = (int)begin;
@@ -246,24 +342,34 @@ __global__ void k_env_tiles(int64_t n_tiles, const int64_t* __restrict__ kind_en
     const EnvPrim e = prims[order[x]];
     sorted[x] = e;
     for (int a = 0; a <= e.kind; ++a) {
-      for (int c = 0; c < 3; ++c) {
-        T.lo[c] = fmin(T.lo[c], e.s[a][c]);
-        T.hi[c] = fmax(T.hi[c], e.s[a][c]);
+      for (int c = 0; c < 3; ++c) {  // box of the balls: it holds their convex hull
+        T.lo[c] = fmin(T.lo[c], e.s[a][c] - e.s[a][3]);
+        T.hi[c] = fmax(T.hi[c], e.s[a][c] + e.s[a][3]);
+        T.clo[c] = fmin(T.clo[c], e.s[a][c]);
+        T.chi[c] = fmax(T.chi[c], e.s[a][c]);
       }
       T.rmax = fmax(T.rmax, e.s[a][3]);
     }
   }
   tiles[t] = T;
+  tile_key[t] = keys[begin] & MORTON_MASK;
 }
 
-// one warp per 32 sorted samples; tiles culled by their exact lower bound
+// One warp per 32 Morton-consecutive samples (lane = sample).  Per kind (spheres, then cones,
+// then slabs) the kind's tiles are visited outward from the warp's place in their Morton
+// order; a tile is skipped when for every lane the distance to the box of its balls exceeds
+// the lane's best (a cone or slab is the convex hull of its balls, so that distance bounds
+// every member's value), else every lane loads one member and the warp evaluates the 32
+// members for each sample that needs the tile in turn (one member per lane, a warp min-reduce
+// of (value, id)): full lanes whatever the number of samples needing the tile.
 __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
     int64_t S, const double* __restrict__ smp, const int32_t* __restrict__ sorder,
-    int64_t n_tiles, const EnvTile* __restrict__ tiles, const EnvPrim* __restrict__ prims,
-    double* __restrict__ g_out, int32_t* __restrict__ prim_out,
-    unsigned long long* __restrict__ n_eval) {
-  __shared__ EnvPrim s_p[ENV_WARPS][ENV_TILE];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long* __restrict__ skey, TileRanges R,
+    const EnvTile* __restrict__ tiles, const unsigned long long* __restrict__ tile_key,
+    const EnvPrim* __restrict__ prims, double* __restrict__ g_out,
+    int32_t* __restrict__ prim_out, unsigned long long* __restrict__ n_eval) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long evals = 0;
@@ -274,35 +380,73 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
     const double p[3] = {valid ? smp[3 * o] : 0.0, valid ? smp[3 * o + 1] : 0.0,
                          valid ? smp[3 * o + 2] : 0.0};
     double best = valid ? 1e300 : -1e300;
-    int arg = -1;
-    for (int64_t t = 0; t < n_tiles; ++t) {
-      const EnvTile T = tiles[t];
-      double dx = fmax(fmax(T.lo[0] - p[0], p[0] - T.hi[0]), 0.0);
-      double dy = fmax(fmax(T.lo[1] - p[1], p[1] - T.hi[1]), 0.0);
-      double dz = fmax(fmax(T.lo[2] - p[2], p[2] - T.hi[2]), 0.0);
-      const double lb = env_norm(dx, dy, dz) - T.rmax;
-      // (the lower bound is exact up to rounding: a small margin keeps the culling safe)
-      const bool need = lb <= best + 1e-9 * (fabs(best) + 1.0);
-      if (!__any_sync(0xffffffffu, need)) continue;
-      __syncwarp();
-      for (int x = lane; x < T.count; x += 32) s_p[warp][x] = prims[T.first + x];
-      __syncwarp();
-      if (need)
-        for (int x = 0; x < T.count; ++x) {
-          const double g = env_eval(p, s_p[warp][x]);
-          ++evals;
-          if (g < best || (g == best && s_p[warp][x].id < arg)) {
+    int arg = 0x7fffffff;
+    const unsigned long long k0 = skey[base];
+    for (int kind = 0; kind < 3; ++kind) {
+      const int64_t lo_t = R.tb[kind], hi_t = R.tb[kind + 1];
+      if (lo_t == hi_t) continue;
+      int64_t lo = lo_t, hi = hi_t;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (tile_key[mid] <= k0) lo = mid + 1;
+        else hi = mid;
+      }
+      const int64_t t0 = lo > lo_t ? lo - 1 : lo_t;
+      for (int64_t j = 0;; ++j) {
+        const int64_t up = t0 + (j >> 1), dn = t0 - 1 - (j >> 1);
+        if (up >= hi_t && dn < lo_t) break;
+        const int64_t t = (j & 1) ? dn : up;
+        if (t < lo_t || t >= hi_t) continue;
+        const EnvTile T = tiles[t];
+        // lower bound of every member's value: outside the box of the balls, the distance to
+        // it (the member lies in the convex hull of its balls, inside that box); inside, the
+        // distance to the box of the centres minus the largest radius
+        const double db = env_norm(fmax(fmax(T.lo[0] - p[0], p[0] - T.hi[0]), 0.0),
+                                   fmax(fmax(T.lo[1] - p[1], p[1] - T.hi[1]), 0.0),
+                                   fmax(fmax(T.lo[2] - p[2], p[2] - T.hi[2]), 0.0));
+        const double dc = env_norm(fmax(fmax(T.clo[0] - p[0], p[0] - T.chi[0]), 0.0),
+                                   fmax(fmax(T.clo[1] - p[1], p[1] - T.chi[1]), 0.0),
+                                   fmax(fmax(T.clo[2] - p[2], p[2] - T.chi[2]), 0.0)) -
+                          T.rmax;
+        const double lb = db > 0.0 ? db : dc;
+        // (exact up to rounding: a small margin keeps the culling safe)
+        const bool need = lb <= best + 1e-9 * (fabs(best) + 1.0);
+        unsigned m = __ballot_sync(FULL, need);
+        if (!m) continue;
+        const bool has = lane < T.count;
+        EnvPrim e;
+        if (has) e = prims[T.first + lane];
+        else e.kind = kind;
+        const int my_id = has ? e.id : 0x7fffffff;
+        evals += (unsigned long long)__popc(m) * T.count;
+        while (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const double q[3] = {__shfl_sync(FULL, p[0], l), __shfl_sync(FULL, p[1], l),
+                               __shfl_sync(FULL, p[2], l)};
+          double g = has ? env_eval(q, e) : 1e300;
+          int id = my_id;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double og = __shfl_xor_sync(FULL, g, off);
+            const int oid = __shfl_xor_sync(FULL, id, off);
+            if (og < g || (og == g && oid < id)) {
+              g = og;
+              id = oid;
+            }
+          }
+          if (lane == l && (g < best || (g == best && id < arg))) {
             best = g;
-            arg = s_p[warp][x].id;
+            arg = id;
           }
         }
+      }
     }
     if (valid) {
       g_out[o] = best;
       prim_out[o] = arg;
     }
   }
-  for (int off = 16; off > 0; off >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, off);
   if (lane == 0 && evals) atomicAdd(n_eval, evals);
 }
 
@@ -325,12 +469,21 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
                             int64_t NF, double* g_out, int32_t* prim_out,
                             unsigned long long* n_eval) {
   const int64_t P = N + NE + NF;
-  const int64_t n_tiles = (N + ENV_TILE - 1) / ENV_TILE + (NE + ENV_TILE - 1) / ENV_TILE +
-                          (NF + ENV_TILE - 1) / ENV_TILE;
+  TileRanges R;
+  {
+    const int64_t cnt[3] = {N, NE, NF};
+    R.tb[0] = 0;
+    R.pb[0] = 0;
+    for (int k = 0; k < 3; ++k) {
+      R.tb[k + 1] = R.tb[k] + (cnt[k] + ENV_TILE - 1) / ENV_TILE;
+      R.pb[k + 1] = R.pb[k] + cnt[k];
+    }
+  }
+  const int64_t n_tiles = R.tb[3];
   const size_t bytes = sizeof(EnvPrim) * 2 * (P + 1) + sizeof(EnvTile) * (n_tiles + 1) +
                        sizeof(unsigned long long) * 2 * (P + S + 2) +
                        sizeof(int32_t) * 2 * (P + S + 2) + sizeof(double) * 8 +
-                       sizeof(int64_t) * 4 + 256;
+                       sizeof(unsigned long long) * (n_tiles + 1) + 512;
   cudaError_t e = c->env_buf.ensure(bytes);
   if (e) return e;
   char* b = c->env_buf.as<char>();
@@ -351,12 +504,9 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
   int32_t* si = reinterpret_cast<int32_t*>(take(4 * (S + 1)));
   int32_t* si2 = reinterpret_cast<int32_t*>(take(4 * (S + 1)));
   double* box = reinterpret_cast<double*>(take(sizeof(double) * 8));
-  int64_t* kind_end = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * 4));
+  unsigned long long* tile_key = reinterpret_cast<unsigned long long*>(take(8 * (n_tiles + 1)));
   k_env_box<<<1, 1024, 0, c->stream>>>(S, smp, N, sph, box);
   ++c->launches;
-  const int64_t ends[3] = {N, N + NE, N + NE + NF};
-  if ((e = cudaMemcpyAsync(kind_end, ends, sizeof(ends), cudaMemcpyHostToDevice, c->stream)))
-    return e;
   const int32_t* ids[3] = {nullptr, edges, faces};
   const int64_t cnt[3] = {N, NE, NF};
   int64_t off = 0;
@@ -370,8 +520,8 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
   }
   if (P > 0 && (e = sort_pairs(c, pk, pk2, pi, pi2, P))) return e;
   if (n_tiles > 0) {
-    k_env_tiles<<<nblk(n_tiles, 128), 128, 0, c->stream>>>(n_tiles, kind_end, prims, pi2, sorted,
-                                                           tiles);
+    k_env_tiles<<<nblk(n_tiles, 128), 128, 0, c->stream>>>(R, prims, pi2, pk2, sorted, tiles,
+                                                           tile_key);
     ++c->launches;
   }
   if (S == 0) return cudaGetLastError();
@@ -380,8 +530,8 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
   if ((e = sort_pairs(c, sk, sk2, si, si2, S))) return e;
   int64_t blocks = (S + 32 * ENV_WARPS - 1) / (32 * ENV_WARPS);
   if (blocks > (int64_t)c->sms * 16) blocks = (int64_t)c->sms * 16;
-  k_env_dist<<<(unsigned)blocks, ENV_WARPS * 32, 0, c->stream>>>(S, smp, si2, n_tiles, tiles,
-                                                                 sorted, g_out, prim_out, n_eval);
+  k_env_dist<<<(unsigned)blocks, ENV_WARPS * 32, 0, c->stream>>>(
+      S, smp, si2, sk2, R, tiles, tile_key, sorted, g_out, prim_out, n_eval);
   ++c->launches;
   return cudaGetLastError();
 }
