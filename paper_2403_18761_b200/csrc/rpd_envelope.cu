@@ -38,11 +38,15 @@ namespace rpd {
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 constexpr int ENV_TILE = 32;
+#ifndef RPD_ENV_SMEM
+#define RPD_ENV_SMEM 1  // members' records read from shared memory (fewer registers)
+#endif
 constexpr int ENV_WARPS = 4;
 
 struct EnvPrim {      // one primitive: up to three spheres (x, y, z, r); kind = #spheres - 1
   double s[3][4];
   double k[12];       // per-primitive constants of the closed forms (env_prep)
+  double ek[3][3];    // slab: the constants k0..k2 of its three edge cones (s0s1, s0s2, s1s2)
   int kind, id;       // id: the primitive's index in the caller's numbering
 };
 
@@ -123,8 +127,37 @@ __device__ double env_slab(const double* p, const double* s1, const double* s2,
 //   slab  k0..2 = the inverse Gram matrix (i11, i12, i22), k3..5 = the in-plane part of the
 //         stationary normal, k6..8 = the unit plane normal N, k9 = w = sqrt(1 - |n_plane|^2),
 //         k10 = 1 / w, k11 = 1 if an interior stationary point can exist
+__device__ void cone_consts(const double* s1, const double* s2, double* k) {
+  const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
+  const double dr = s2[3] - s1[3];
+  const double L2 = d0 * d0 + d1 * d1 + d2 * d2;
+  k[0] = k[1] = k[2] = 0.0;
+  if (!(dr * dr < L2)) {
+    k[2] = 1.0;
+    return;
+  }
+  k[0] = 1.0 / L2;
+  k[1] = dr / (sqrt(L2) * sqrt(L2 - dr * dr));
+}
+
+__device__ __forceinline__ double cone_eval(const double* p, const double* s1, const double* s2,
+                                            const double* k) {
+  if (k[2] != 0.0) return fmin(env_sphere(p, s1), env_sphere(p, s2));
+  const double d0 = s2[0] - s1[0], d1 = s2[1] - s1[1], d2 = s2[2] - s1[2];
+  const double q0 = p[0] - s1[0], q1 = p[1] - s1[1], q2 = p[2] - s1[2];
+  const double qd = fma(q0, d0, fma(q1, d1, q2 * d2));
+  const double h = sqrt(fmax(fma(q0, q0, fma(q1, q1, q2 * q2)) - qd * qd * k[0], 0.0));
+  const double t = fmin(fmax(fma(qd, k[0], k[1] * h), 0.0), 1.0);
+  return env_norm(q0 - t * d0, q1 - t * d1, q2 - t * d2) - fma(t, s2[3] - s1[3], s1[3]);
+}
+
 __device__ void env_prep(EnvPrim& e) {
   for (int q = 0; q < 12; ++q) e.k[q] = 0.0;
+  if (e.kind == 2) {
+    cone_consts(e.s[0], e.s[1], e.ek[0]);
+    cone_consts(e.s[0], e.s[2], e.ek[1]);
+    cone_consts(e.s[1], e.s[2], e.ek[2]);
+  }
   if (e.kind == 1) {
     const double* s1 = e.s[0];
     const double* s2 = e.s[1];
@@ -198,8 +231,8 @@ __device__ __forceinline__ double env_slab_k(const double* p, const EnvPrim& e) 
         return rho - (s1[3] + u * (e.s[1][3] - s1[3]) + v * (e.s[2][3] - s1[3]));
     }
   }
-  return fmin(env_cone(p, e.s[0], e.s[1]), fmin(env_cone(p, e.s[0], e.s[2]),
-                                                 env_cone(p, e.s[1], e.s[2])));
+  return fmin(cone_eval(p, e.s[0], e.s[1], e.ek[0]),
+              fmin(cone_eval(p, e.s[0], e.s[2], e.ek[1]), cone_eval(p, e.s[1], e.s[2], e.ek[2])));
 }
 
 __device__ __forceinline__ double env_eval(const double* p, const EnvPrim& e) {
@@ -370,6 +403,10 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
     int32_t* __restrict__ prim_out, unsigned long long* __restrict__ n_eval) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+#if RPD_ENV_SMEM
+  __shared__ EnvPrim s_rec[ENV_WARPS][ENV_TILE];
+  EnvPrim& e_sm = s_rec[threadIdx.x >> 5][lane];
+#endif
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long evals = 0;
@@ -414,9 +451,16 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
         unsigned m = __ballot_sync(FULL, need);
         if (!m) continue;
         const bool has = lane < T.count;
+#if RPD_ENV_SMEM
+        __syncwarp();
+        if (has) e_sm = prims[T.first + lane];
+        __syncwarp();
+        const EnvPrim& e = e_sm;
+#else
         EnvPrim e;
         if (has) e = prims[T.first + lane];
         else e.kind = kind;
+#endif
         const int my_id = has ? e.id : 0x7fffffff;
         evals += (unsigned long long)__popc(m) * T.count;
         while (m) {
