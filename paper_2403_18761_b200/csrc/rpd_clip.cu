@@ -925,11 +925,18 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
             S.dsc[pl] = 0u;  // (free after the cuts) tet faces next to each facet
             reinterpret_cast<unsigned long long*>(S.KM)[pl] = 0ull;  // adjacent radical facets
             // rank of a radical facet among the piece's radical facets by ascending j (the
-            // order of the compacted rpf entries)
+            // order of the compacted rpf entries): the cutting planes were added in CSR order,
+            // i.e. ascending j, so it is the number of radical facets with a smaller plane id
             if (pl >= 4 && facets_all.has(pl)) {
               int rk = 0;
-              for (int f = facets_all.next(4); f >= 0; f = facets_all.next(f + 1))
-                rk += S.src[f] < S.src[pl];
+#pragma unroll
+              for (int w = 0; w < VPL; ++w) {
+                const int lo = 32 * w, hi = lo + 32;
+                unsigned m = facets_all.w[w];
+                if (lo < 4) m &= ~0xfu;                       // radical planes only
+                if (pl < hi) m &= pl > lo ? (1u << (pl - lo)) - 1u : 0u;  // below pl
+                rk += __popc(m);
+              }
               S.c0[pl] = (unsigned char)(rk < 64 ? rk : 255);
             }
           }
