@@ -976,6 +976,12 @@ rpd_status rpd_gather_pieces(rpd_ctx* c, const rpd_shards* sh, int32_t* piece_of
                                                     !sh->inc_off[r])))
       return fail(c, RPD_EINVAL, "rpd_gather_pieces: bad shard");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  CK(launch_gather_check(c, sh), "gather check");
+  CK(readback(c, RbSpec{{}, nullptr, c->errw.as<int>()}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "gather check");
+  if (((Readback*)c->pinned)->err[0] != 0)
+    return fail(c, RPD_EINVAL, "rpd_gather_pieces: a tet id is out of range");
   CK(launch_gather(c, sh, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask, inc_off,
                    inc_sphere), "gather");
   CK(cudaStreamSynchronize(c->stream), "gather");
@@ -1003,6 +1009,14 @@ rpd_status rpd_envelope(rpd_ctx* c, const double* samples, int64_t S, const doub
   int32_t* dp = host_out ? reinterpret_cast<int32_t*>(c->env_out.as<double>() + (S + 1)) : prim_out;
   unsigned long long* ne = c->stats.as<unsigned long long>() + ST_ENV_EVAL;
   CK(cudaMemsetAsync(ne, 0, sizeof(unsigned long long), c->stream), "memset");
+  if (NE + NF > 0) {  // sphere ids validated before any kernel dereferences them
+    CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+    CK(launch_envelope_check(c, N, d_e, NE, d_f, NF), "envelope check");
+    CK(readback(c, RbSpec{{}, nullptr, c->errw.as<int>()}), "readback");
+    CK(cudaStreamSynchronize(c->stream), "envelope check");
+    if (((Readback*)c->pinned)->err[0] != 0)
+      return fail(c, RPD_EINVAL, "rpd_envelope: a cone / slab sphere id is out of range");
+  }
   CK(launch_envelope(c, d_smp, S, d_sph, N, d_e, NE, d_f, NF, dg, dp, ne), "envelope");
   if (host_out && S > 0) {
     CK(cudaMemcpyAsync(g_out, dg, sizeof(double) * S, cudaMemcpyDefault, c->stream), "download");

@@ -251,10 +251,13 @@ cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSe
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase);
 // multi-GPU gather of the pieces (rpd_gather.cu)
+cudaError_t launch_gather_check(rpd_ctx* c, const rpd_shards* in);
 cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
                           int32_t* piece_sphere, double* piece_vol, double* piece_m1,
                           uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
 // envelope distance (rpd_envelope.cu)
+cudaError_t launch_envelope_check(rpd_ctx* c, int64_t N, const int32_t* edges, int64_t NE,
+                                  const int32_t* faces, int64_t NF);
 cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const double* sph,
                             int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
                             int64_t NF, double* g_out, int32_t* prim_out,

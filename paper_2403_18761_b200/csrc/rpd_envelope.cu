@@ -301,6 +301,15 @@ __global__ void k_env_sample_keys(int64_t S, const double* __restrict__ smp,
   idx[x] = (int32_t)x;
 }
 
+// every sphere id of the cones and slabs in [0, N)
+__global__ void k_env_check(int64_t n, const int32_t* __restrict__ ids, int64_t N, int* err) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < n && (ids[x] < 0 || ids[x] >= N) && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+    err[1] = ERR_NBR_INDEX;
+    err[2] = (int)x;
+  }
+}
+
 // bounding box of the samples and sphere centres (lo[3], 1 / cell) -- one block
 __global__ void k_env_box(int64_t S, const double* __restrict__ smp, int64_t N,
                           const double* __restrict__ sph, double* __restrict__ box) {
@@ -492,6 +501,20 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
     }
   }
   if (lane == 0 && evals) atomicAdd(n_eval, evals);
+}
+
+// validation of the primitives' sphere ids (before any kernel dereferences them)
+cudaError_t launch_envelope_check(rpd_ctx* c, int64_t N, const int32_t* edges, int64_t NE,
+                                  const int32_t* faces, int64_t NF) {
+  if (NE > 0) {
+    k_env_check<<<nblk(2 * NE, 256), 256, 0, c->stream>>>(2 * NE, edges, N, c->errw.as<int>());
+    ++c->launches;
+  }
+  if (NF > 0) {
+    k_env_check<<<nblk(3 * NF, 256), 256, 0, c->stream>>>(3 * NF, faces, N, c->errw.as<int>());
+    ++c->launches;
+  }
+  return cudaGetLastError();
 }
 
 template <class K, class V>

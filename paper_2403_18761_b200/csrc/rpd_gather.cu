@@ -32,6 +32,18 @@ __device__ __forceinline__ int rank_of(const ShardView& v, int64_t x) {
   return r;
 }
 
+// every rank's global tet ids in [0, T) (before any kernel writes through them)
+__global__ void k_g_check(ShardView v, int64_t T, int* err) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= v.base[v.world]) return;
+  const int r = rank_of(v, x);
+  const int t = v.tet_ids[r][x - v.base[r]];
+  if ((t < 0 || t >= T) && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+    err[1] = ERR_TET_INDEX;
+    err[2] = (int)x;
+  }
+}
+
 // per global tet: pieces and incidences (from the owning rank)
 __global__ void k_g_count(ShardView v, int32_t* __restrict__ pc, int32_t* __restrict__ ic) {
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -74,9 +86,7 @@ __global__ void k_g_copy(ShardView v, const int32_t* __restrict__ goff,
   for (int k = i0; k < io[p1]; ++k) inc[gi0 + (k - i0)] = v.inc_sphere[r][k];
 }
 
-cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
-                          int32_t* piece_sphere, double* piece_vol, double* piece_m1,
-                          uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere) {
+static ShardView view_of(const rpd_shards* in) {
   ShardView v{};
   v.world = in->world;
   v.base[0] = 0;
@@ -91,6 +101,23 @@ cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
     v.inc_off[r] = in->inc_off[r];
     v.inc_sphere[r] = in->inc_sphere[r];
   }
+  return v;
+}
+
+cudaError_t launch_gather_check(rpd_ctx* c, const rpd_shards* in) {
+  const ShardView v = view_of(in);
+  const int64_t n = v.base[in->world];
+  if (n > 0) {
+    k_g_check<<<nblk(n, 256), 256, 0, c->stream>>>(v, in->T, c->errw.as<int>());
+    ++c->launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
+                          int32_t* piece_sphere, double* piece_vol, double* piece_m1,
+                          uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere) {
+  const ShardView v = view_of(in);
   const int64_t T = in->T, n = v.base[in->world];
   cudaError_t e = c->g_cnt.ensure(sizeof(int32_t) * (3 * (T + 1) + 1));
   if (e) return e;

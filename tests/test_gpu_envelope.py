@@ -92,3 +92,14 @@ def test_envelope_c3_sampled(ctx):
     ids = np.random.default_rng(0).choice(len(smp), 6, replace=False)
     g_ref, _ = oracle.envelope(smp[ids], w.spheres, mm["edges"], mm["faces"])
     assert np.max(np.abs(g[ids] - g_ref)) <= 1e-9 * 100.0
+
+
+def test_envelope_bad_ids(ctx):
+    import paper_2403_18761_b200 as P
+    sph = np.array([[0, 0, 0, 1.0], [3, 0, 0, 1.0]])
+    with pytest.raises(P.RPDError) as e:
+        ctx.envelope(np.zeros((4, 3)), sph, np.array([[0, 2]], np.int32), np.zeros((0, 3), np.int32))
+    assert e.value.status == -1
+    g, _, _ = ctx.envelope(np.array([[1.5, 2.0, 0.0]]), sph, np.array([[0, 1]], np.int32),
+                           np.zeros((0, 3), np.int32))  # the ctx still works
+    assert g[0] == pytest.approx(1.0, abs=1e-12)

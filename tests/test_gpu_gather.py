@@ -64,3 +64,21 @@ def test_dist_gather_pieces_nccl_world1():
     finally:
         ctx.close()
         dist.destroy_process_group()
+
+
+def test_gather_bad_tet_id():
+    import torch
+    import paper_2403_18761_b200 as P
+    ctx = P.RPDContext(0)
+    try:
+        w = W.make_c1(0)
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        loc = {k: v.clone() for k, v in ctx.download_pieces(device=True).items()}
+        ids = torch.arange(6, dtype=torch.int32, device="cuda")
+        ids[5] = 99
+        with pytest.raises(P.RPDError) as e:
+            ctx.gather_pieces([loc], [ids], 6)
+        assert e.value.status == -1
+    finally:
+        ctx.close()
