@@ -14,6 +14,8 @@ Parity status of each function (DESIGN.md §Oracle pins):
   pieces: non-empty, facemask, incidences, vol, m1 ... pinned (exact checker, brute force,
           Kuhn closed forms, partition, Voronoi reduction, power membership)
   partial update (R11) ... pinned (partial == full recompute, M = 0 identity)
+  box neighbours (NEXT-3) ... pinned (subset of the Qhull regular-triangulation edges, two-sphere
+          closed form, sufficiency: same pieces as with the regular-triangulation lists)
   fractional Euler characteristics (NEXT-1) ... pinned (mesh Euler by V-E+F-T, a single
           sphere gives the mesh's Euler, explicit extraction of every RPC / RPF complex by
           exact rational vertex enumeration, RPF symmetry on generic inputs)
@@ -171,6 +173,29 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
     finally:
         L.oracle_free(rp)
     return out
+
+
+def box_neighbours(spheres, box, nthreads=0):
+    """NEXT-3 definition (DESIGN.md §10 "Sphere neighbours"): j is a box
+    neighbour of i iff the radical plane h_ij holds a positive-area 2-face of C_i ∩ B, B the
+    axis box ``box`` = (lo, hi).  Computed literally: B split into its 6 Kuhn tets, every piece
+    P(t, i) clipped in brute-force mode (N(i) = all j != i), and the
+    incidences (geometric, positive-area faces: C1 step 7) of i's pieces united.  Returns the
+    CSR (off [N+1], idx ascending)."""
+    import rpd_workloads as W
+    sp = np.ascontiguousarray(spheres, dtype=np.float64).reshape(-1, 4)
+    N = len(sp)
+    bx = np.asarray(box, dtype=np.float64).reshape(6)
+    bv, bt = W.box_6tets(bx[:3], bx[3:])
+    z = np.zeros(N + 1, dtype=np.int32)
+    r = rpd(bv, bt, sp, z, np.zeros(0, dtype=np.int32), brute=True, nthreads=nthreads)
+    rows = [set() for _ in range(N)]
+    for p, i in enumerate(r["piece_sphere"]):
+        rows[int(i)].update(r["inc_sphere"][r["inc_off"][p]:r["inc_off"][p + 1]].tolist())
+    off = np.zeros(N + 1, dtype=np.int32)
+    off[1:] = np.cumsum([len(x) for x in rows])
+    idx = np.array([j for x in rows for j in sorted(x)], dtype=np.int32)
+    return off, idx
 
 
 def relation_matrix(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, sphere_lo=0,

@@ -161,6 +161,23 @@ def unit_cube_6tets(scale: float = 1.0, origin=(0.0, 0.0, 0.0)):
     return kuhn_grid_mesh((1, 1, 1), s, o, morton=False)
 
 
+def box_6tets(lo, hi):
+    """The axis box [lo, hi] (lattice multiples, hi > lo per axis) split into its 6 Kuhn tets:
+    the domain the NEXT-3 neighbour definition restricts power cells to."""
+    v, t = kuhn_grid_mesh((1, 1, 1), 1, (0, 0, 0), morton=False)
+    u = np.round(v * LATTICE)                     # unit cube corners, 0 / 1
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    assert np.all(hi > lo)
+    return lo + u * (hi - lo), t
+
+
+def mesh_box(verts):
+    """(lo_x, lo_y, lo_z, hi_x, hi_y, hi_z) of a mesh: the box passed to rpd_neighbors."""
+    v = np.asarray(verts, dtype=np.float64)
+    return np.concatenate([v.min(0), v.max(0)])
+
+
 @dataclass
 class BoxWithHole:
     """Axis box [lo,hi] with a cylindrical through-hole along z (genus-1 CAD-like solid)."""
