@@ -313,6 +313,37 @@ rpd_status rpd_envelope(rpd_ctx* ctx, const double* samples, int64_t S, const do
                         int64_t N, const int32_t* edges, int64_t NE, const int32_t* faces,
                         int64_t NF, double* g_out, int32_t* prim_out, int64_t* n_eval);
 
+/* ---- Sphere neighbours on the GPU
+ *
+ * "we compute the neighbors of each site ... using a Regular Triangulation";
+ * the neighbour lists are the k_site input of rpd_relations.  This call computes a certified
+ * SUPERSET of the neighbours whose radical plane holds a positive-area facet of the power cell
+ * restricted to the axis box `box` (DESIGN.md §10 "Sphere neighbours"): the RPD of any tets
+ * inside the box is the same as with the regular-triangulation lists (redundant planes do not
+ * change a piece), and every list may hold a few redundant spheres.
+ *   spheres [N][4] double (x, y, z, r), host or device; no lattice requirement
+ *   box     host double[6] = (lo_x, lo_y, lo_z, hi_x, hi_y, hi_z), e.g. the mesh's bounds
+ * Outputs (ctx-owned DEVICE arrays, valid until the next rpd_neighbors or destroy; they can be
+ * passed straight to rpd_relations / rpd_update_partial): nbr_off [N+1], nbr_idx [E], rows
+ * ascending, no self or same-centre entries.  A sphere hidden by a same-centre sphere with a
+ * larger radius (equal radius: the smaller id wins) or whose cell misses the box gets an empty
+ * row; if a cell covers the whole box its row lists one redundant sphere (so that R4 does not
+ * apply).  n_hidden counts the former; n_vertex_overflow counts spheres whose bounding
+ * polytope overflowed the vertex buffer (their lists are computed against the whole box --
+ * still a superset).  RPD_EINVAL: NULL arguments, non-finite box or lo > hi, NaN / Inf sphere
+ * values or a negative radius. */
+typedef struct {
+  const int32_t* nbr_off;
+  const int32_t* nbr_idx;
+  int64_t N, E;
+  int64_t n_hidden, n_vertex_overflow;
+} rpd_nbr_lists;
+rpd_status rpd_neighbors(rpd_ctx* ctx, const double* spheres, int64_t N, const double* box,
+                         rpd_nbr_lists* out);
+/* Copy the last lists to caller-owned arrays (host or device; NULL skips).  RPD_ESTATE before
+ * any rpd_neighbors. */
+rpd_status rpd_download_neighbors(rpd_ctx* ctx, int32_t* nbr_off, int32_t* nbr_idx);
+
 /* Counters of the last call (host).  Algorithmic counts are what the method computed (for
  * the roofline), kernel_launches counts this library's kernel launches since rpd_create. */
 typedef struct {

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include <chrono>
+#include <cmath>
 
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
@@ -1027,6 +1028,86 @@ rpd_status rpd_envelope(rpd_ctx* c, const double* samples, int64_t S, const doub
   CK(cudaMemcpyAsync(&h_ne, ne, sizeof(h_ne), cudaMemcpyDeviceToHost, c->stream), "download");
   CK(cudaStreamSynchronize(c->stream), "envelope");
   if (n_eval) *n_eval = (int64_t)h_ne;
+  return RPD_OK;
+}
+
+rpd_status rpd_neighbors(rpd_ctx* c, const double* spheres, int64_t N, const double* box,
+                         rpd_nbr_lists* out) {
+  if (!c) return RPD_EINVAL;
+  if (N < 0 || N > 0x3fffffff || (N > 0 && !spheres) || !box || !out)
+    return fail(c, RPD_EINVAL, "rpd_neighbors: bad argument");
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(box[k]) || !std::isfinite(box[3 + k]) || !(box[k] <= box[3 + k]))
+      return fail(c, RPD_EINVAL, "rpd_neighbors: box must be finite with lo <= hi");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const double bx[6] = {box[0], box[1], box[2], box[3], box[4], box[5]};
+  const double* d_sph = nullptr;
+  CK(resolve(c, spheres, 4 * N, c->h_nb, &d_sph), "stage spheres");
+  CK(c->nb_off.ensure(sizeof(int32_t) * (N + 1)), "alloc");
+  CK(c->nb_cnt.ensure(sizeof(int32_t) * (N + 1)), "alloc");
+  c->nb_N = -1;
+  int32_t* off = c->nb_off.as<int32_t>();
+  if (N == 0) {
+    CK(cudaMemsetAsync(off, 0, sizeof(int32_t), c->stream), "memset");
+    CK(cudaStreamSynchronize(c->stream), "neighbors");
+    c->nb_N = 0;
+    c->nb_E = 0;
+    *out = rpd_nbr_lists{off, c->nb_idx.as<int32_t>(), 0, 0, 0, 0};
+    return RPD_OK;
+  }
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  const char* dbg_path = getenv("RPD_NB_DEBUG");  // development aid: per-sphere counters
+  if (dbg_path) {
+    if (c->nb_dbg) cudaFree(c->nb_dbg);
+    c->nb_dbg = nullptr;
+    CK(cudaMalloc(&c->nb_dbg, sizeof(long long) * 8 * N), "alloc");
+    CK(cudaMemsetAsync(c->nb_dbg, 0, sizeof(long long) * 8 * N, c->stream), "memset");
+  }
+  CK(launch_neighbors_pass1(c, d_sph, N, bx, c->nb_cnt.as<int32_t>(), off), "neighbors");
+  RbSpec rs{};
+  rs.i32[0] = off + N;
+  rs.i32[1] = c->nb_long;
+  rs.err = c->errw.as<int>();
+  CK(readback(c, rs), "readback");
+  CK(cudaStreamSynchronize(c->stream), "neighbors");
+  const Readback* rb = (const Readback*)c->pinned;
+  if (rb->err[0] != 0) return check_err(c, rb);
+  const int64_t E = rb->i32[0];
+  if (dbg_path && c->nb_dbg) {
+    std::vector<long long> h(8 * N);
+    CK(cudaMemcpy(h.data(), c->nb_dbg, sizeof(long long) * 8 * N, cudaMemcpyDeviceToHost), "dbg");
+    FILE* f = fopen(dbg_path, "wb");
+    if (f) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
+    cudaFree(c->nb_dbg);
+    c->nb_dbg = nullptr;
+  }
+  CK(c->nb_idx.ensure(sizeof(int32_t) * (E + 1)), "alloc");
+  CK(c->nb_tmp.ensure(sizeof(int32_t) * (E + 1)), "alloc");
+  CK(launch_neighbors_pass2(c, d_sph, N, bx, c->nb_cnt.as<int32_t>(), off, c->nb_tmp.as<int32_t>(),
+                            c->nb_idx.as<int32_t>()),
+     "neighbors");
+  unsigned long long h_st[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(h_st, c->nb_stats, sizeof(h_st), cudaMemcpyDeviceToHost, c->stream), "download");
+  CK(cudaStreamSynchronize(c->stream), "neighbors");
+  c->nb_N = N;
+  c->nb_E = E;
+  *out = rpd_nbr_lists{off, c->nb_idx.as<int32_t>(), N, E, (int64_t)h_st[1], (int64_t)h_st[0]};
+  return RPD_OK;
+}
+
+rpd_status rpd_download_neighbors(rpd_ctx* c, int32_t* nbr_off, int32_t* nbr_idx) {
+  if (!c) return RPD_EINVAL;
+  if (c->nb_N < 0) return fail(c, RPD_ESTATE, "no neighbour lists (call rpd_neighbors)");
+  if (nbr_off)
+    CK(cudaMemcpyAsync(nbr_off, c->nb_off.p, sizeof(int32_t) * (c->nb_N + 1), cudaMemcpyDefault,
+                       c->stream), "download");
+  if (nbr_idx && c->nb_E)
+    CK(cudaMemcpyAsync(nbr_idx, c->nb_idx.p, sizeof(int32_t) * c->nb_E, cudaMemcpyDefault,
+                       c->stream), "download");
+  CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }
 

@@ -188,6 +188,15 @@ struct rpd_ctx {
   bool eu_whole = false;       // payloads built with the ctx holding the whole mesh in order
   rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
   rpd::DevBuf cc_par, cc_out;  // CC numbers: union-find parents, outputs
+  // sphere neighbours (NEXT-3): scratch (grid, pass-1 rows), outputs (off, idx), pass-2 rows
+  rpd::DevBuf nb_buf, nb_off, nb_idx, nb_tmp, nb_cnt, h_nb;
+  void* nb_grid = nullptr;
+  unsigned long long* nb_stats = nullptr;
+  int32_t *nb_start = nullptr, *nb_items = nullptr, *nb_long = nullptr, *nb_long_ids = nullptr,
+          *nb_slab = nullptr;
+  double nb_args_tol0 = 0.0;
+  void* nb_dbg = nullptr;  // development aid: device int64 [N][8] per-sphere counters
+  int64_t nb_N = -1, nb_E = 0;
 };
 
 namespace rpd {
@@ -198,6 +207,10 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                  const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                                  bool reuse_rows, int epoch);
+cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                                   int32_t* cnt, int32_t* off);
+cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                                   int32_t* cnt, const int32_t* off, int32_t* tmp, int32_t* idx);
 void clip_phase_dump();  // development aid (RPD_CLIP_PHASES builds)
 cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
 cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);

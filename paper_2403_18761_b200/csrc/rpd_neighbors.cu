@@ -1,0 +1,781 @@
+// rpd_neighbors.cu -- SURVEY.md §8(f) NEXT-3: the sphere neighbour lists (k_site) on the GPU,
+// the step right before the RPD ("we compute the neighbors of each site ...
+// using a Regular Triangulation ... Euclidean security radius ... is not enough for power
+// diagrams").  Instead of a regular triangulation we compute a *certified superset* of the
+// neighbours whose power cell facets meet the domain box B (DESIGN.md §10 "Sphere
+// neighbours"): every sphere j whose radical plane holds a positive-area facet of C_i ∩ B is
+// listed.  The RPD restricted to tets inside B is unchanged by redundant planes (SURVEY §8(c)
+// C0: "supersets are harmless"), so the pieces equal those of the regular-triangulation lists.
+//
+// Per sphere i (one warp), in coordinates y = x - theta_i:
+//   1. K = the KSEL spheres of smallest power distance PD_j(theta_i) found in the grid rings
+//      around i (a heuristic choice: correctness does not depend on it);
+//   2. P_K = B ∩ ⋂_{k∈K} {h_ik >= 0} ⊇ C_i ∩ B; its vertices by brute-force enumeration of
+//      plane triples (fp64, each with an error radius e_v from its conditioning), kept when
+//      every half-space holds within e_v + tol0 (so no true vertex is lost);
+//   3. j is listed iff h_ij(v) <= e_v + tol0 at some vertex v of P_K (convexity: if h_ij > 0 at
+//      every vertex, the plane misses P_K ⊇ C_i ∩ B); only spheres in the ball
+//      |theta_j - theta_i| <= rho + sqrt(PDmax + rmax^2) (+ margins) can pass, found through
+//      the uniform grid.
+// Special cases: a sphere with the same centre and a larger radius (or the same radius and a
+// smaller id) hides i (empty row); a non-empty P_K with no cutting plane and N > 1 (i's cell
+// covers B) lists its nearest sphere, a redundant plane, so that R4 (k_site = 0 -> no
+// relation) does not apply.  If the vertex list overflows, P_K is replaced by B (conservative).
+//
+// Passes: bounds (centre box, r_max) -> grid counting sort -> pass 1 (count, rows <= CAP1 kept)
+// -> scan -> pass 2 (recompute rows > CAP1) -> per-row rank sort into ascending CSR.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "rpd_ctx.h"
+
+namespace rpd {
+namespace {
+
+constexpr int NB_KSEL0 = 16;              // planes of the first P_K besides the 6 box planes
+constexpr int NB_KSEL = 48;               // planes of a refined P_K (facets + deepest cuts)
+constexpr int NB_MAXP = 6 + NB_KSEL;
+constexpr int NB_MAXV = 224;              // vertex candidates of P_K per sphere
+constexpr int NB_CAPC = 128;              // selection candidates: 4 per lane
+constexpr int NB_CAP1 = 64;               // row entries kept by pass 1
+constexpr int NB_WARPS = 4;               // warps per block of the main kernel
+constexpr int NB_GMAX = 160;              // grid cells per axis (max)
+constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
+
+struct NbGrid {
+  double lo[3], h[3];
+  double rmax;
+  int G;
+};
+
+struct NbSmem {
+  int cid[NB_CAPC];
+  double key[NB_CAPC];
+  double4 pl[NB_MAXP];        // unit normal a, offset b: a.y + b >= 0 inside
+  double4 vx[NB_MAXV];        // y, error radius
+  int out[NB_CAP1];
+  int kid[NB_KSEL];
+  int n_v, n_o, flags, first;
+};
+
+// per-lane smallest NB_TOPL keys (ties: smaller id), kept sorted; deterministic because every
+// lane visits its cells and their (id-sorted) spheres in a fixed order
+struct LaneTop {
+  double k[4];
+  int j[4];
+  __device__ void init() {
+    for (int t = 0; t < 4; ++t) {
+      k[t] = 1e300;
+      j[t] = -1;
+    }
+  }
+  __device__ void push(double key, int id) {
+    if (!(key < k[3] || (key == k[3] && id < j[3]))) return;
+    int t = 3;
+    while (t > 0 && (key < k[t - 1] || (key == k[t - 1] && id < j[t - 1]))) {
+      k[t] = k[t - 1];
+      j[t] = j[t - 1];
+      --t;
+    }
+    k[t] = key;
+    j[t] = id;
+  }
+};
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void k_nb_bounds(const double* __restrict__ sph, int64_t N, int G, NbGrid* g) {
+  __shared__ double s[6][32];
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300}, rm = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int k = 0; k < 3; ++k) {
+      const double c = sph[4 * i + k];
+      mn[k] = fmin(mn[k], c);
+      mx[k] = fmax(mx[k], c);
+    }
+    rm = fmax(rm, sph[4 * i + 3]);
+  }
+  double v[7] = {-mn[0], -mn[1], -mn[2], mx[0], mx[1], mx[2], rm};
+  for (int k = 0; k < 7; ++k) v[k] = warp_max(v[k]);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ double s7[32];
+  if (l == 0) {
+    for (int k = 0; k < 6; ++k) s[k][w] = v[k];
+    s7[w] = v[6];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[7] = {-1e300, -1e300, -1e300, -1e300, -1e300, -1e300, 0.0};
+    for (int q = 0; q < nw; ++q) {
+      for (int k = 0; k < 6; ++k) r[k] = fmax(r[k], s[k][q]);
+      r[6] = fmax(r[6], s7[q]);
+    }
+    for (int k = 0; k < 3; ++k) {
+      const double lo = -r[k], hi = r[3 + k];
+      const double ext = hi - lo;
+      g->lo[k] = lo;
+      g->h[k] = ext > 0 ? ext * (1.0 + 1e-12) / G : 1.0;
+    }
+    g->rmax = r[6];
+    g->G = G;
+  }
+}
+
+// NaN / Inf coordinates or a negative radius -> RPD_EINVAL (error word, first offender)
+__global__ void k_nb_check(const double* __restrict__ sph, int64_t N, int* __restrict__ err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = sph[4 * i], y = sph[4 * i + 1], z = sph[4 * i + 2], r = sph[4 * i + 3];
+    const bool bad_nan = !isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(r);
+    if (bad_nan || r < 0) {
+      if (atomicCAS(&err[0], 0, (int)RPD_EINVAL) == 0) {
+        err[1] = bad_nan ? ERR_SPHERE_NAN : ERR_RADIUS_NEG;
+        err[2] = (int)i;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int nb_cell_axis(double c, const NbGrid& g, int k) {
+  int q = (int)floor((c - g.lo[k]) / g.h[k]);
+  return q < 0 ? 0 : (q >= g.G ? g.G - 1 : q);
+}
+
+__global__ void k_nb_count(const double* __restrict__ sph, int64_t N, const NbGrid* __restrict__ gp,
+                           int32_t* __restrict__ cnt, int32_t* __restrict__ cell_of) {
+  const NbGrid g = *gp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int cx = nb_cell_axis(sph[4 * i], g, 0), cy = nb_cell_axis(sph[4 * i + 1], g, 1),
+              cz = nb_cell_axis(sph[4 * i + 2], g, 2);
+    const int c = (cz * g.G + cy) * g.G + cx;
+    cell_of[i] = c;
+    atomicAdd(&cnt[c], 1);
+  }
+}
+
+__global__ void k_nb_scatter(int64_t N, const int32_t* __restrict__ cell_of,
+                             const int32_t* __restrict__ start, int32_t* __restrict__ fill,
+                             int32_t* __restrict__ items) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = cell_of[i];
+    items[start[c] + atomicAdd(&fill[c], 1)] = (int)i;
+  }
+}
+
+// deterministic cell contents: insertion sort of each (small) cell by sphere id
+__global__ void k_nb_cellsort(int64_t n_cells, const int32_t* __restrict__ start,
+                              int32_t* __restrict__ items) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int a = start[c], b = start[c + 1];
+    for (int p = a + 1; p < b; ++p) {
+      const int v = items[p];
+      int q = p - 1;
+      while (q >= a && items[q] > v) {
+        items[q + 1] = items[q];
+        --q;
+      }
+      items[q + 1] = v;
+    }
+  }
+}
+
+struct NbArgs {
+  const double* sph;
+  int64_t N;
+  const NbGrid* grid;
+  const int32_t* start;   // [G^3 + 1]
+  const int32_t* items;   // spheres by cell
+  double blo[3], bhi[3];  // the domain box B
+  double tol0;            // absolute slack (distance units)
+  int32_t* cnt;           // [N] row lengths (pass 1 writes)
+  int32_t* slab;          // [N][CAP1] pass-1 rows (unsorted)
+  const int32_t* off;     // [N+1] (pass 2)
+  int32_t* tmp;           // [E] pass-2 rows (unsorted)
+  int32_t* n_long;        // rows longer than CAP1: count, then ids
+  int32_t* long_ids;
+  unsigned long long* stats;  // [0] vertex overflows, [1] hidden, [2] triples
+  int* err;
+  long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
+};
+
+// One warp computes sphere i's row.  PASS2: writes the row into tmp at off[i] (rows > CAP1).
+template <bool PASS2>
+__device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
+  const NbGrid& g = *A.grid;
+  const double4 si = make_double4(A.sph[4 * i], A.sph[4 * i + 1], A.sph[4 * i + 2], A.sph[4 * i + 3]);
+  const int G = g.G;
+  const int ci[3] = {nb_cell_axis(si.x, g, 0), nb_cell_axis(si.y, g, 1), nb_cell_axis(si.z, g, 2)};
+  if (lane == 0) {
+    S.n_v = 0;
+    S.n_o = 0;
+    S.flags = 0;
+  }
+  __syncwarp();
+  LaneTop top;
+  top.init();
+  int n_seen = 0;
+  const long long t_start = clock64();
+  long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0;
+  int dbg_rounds = 0;
+  // ---- 1. ring collection of candidates for K (and the hiding test)
+  for (int r = 0;; ++r) {
+    const int w = 2 * r + 1, nc = w * w * w;
+    for (int q = lane; q < nc; q += 32) {
+      const int dx = q % w - r, dy = (q / w) % w - r, dz = q / (w * w) - r;
+      if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;
+      const int x = ci[0] + dx, y = ci[1] + dy, z = ci[2] + dz;
+      if (x < 0 || y < 0 || z < 0 || x >= G || y >= G || z >= G) continue;
+      const int c = (z * G + y) * G + x;
+      for (int p = A.start[c]; p < A.start[c + 1]; ++p) {
+        const int j = A.items[p];
+        if (j == i) continue;
+        const double4 sj = make_double4(A.sph[4 * j], A.sph[4 * j + 1], A.sph[4 * j + 2], A.sph[4 * j + 3]);
+        const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z;
+        const double d2 = ux * ux + uy * uy + uz * uz;
+        if (d2 == 0.0) {
+          if (sj.w > si.w || (sj.w == si.w && j < i)) atomicOr(&S.flags, 1);  // hidden
+          continue;
+        }
+        top.push(d2 - sj.w * sj.w, j);
+        ++n_seen;
+      }
+    }
+    int n = n_seen;
+    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (n >= NB_KSEL0 + 8 || r >= G) break;
+  }
+  for (int t = 0; t < 4; ++t) {
+    S.cid[4 * lane + t] = top.j[t];
+    S.key[4 * lane + t] = top.k[t];
+  }
+  __syncwarp();
+  if (S.flags & 1) {
+    if (!PASS2 && lane == 0) {
+      A.cnt[i] = 0;
+      atomicAdd(&A.stats[1], 1ull);
+    }
+    return;
+  }
+  // box planes (fixed), then rounds: select KSEL planes, enumerate P_K, scan the ball
+  if (lane < 6) {
+    const int k = lane >> 1;
+    const double cth = k == 0 ? si.x : (k == 1 ? si.y : si.z);
+    // lo: y_k + (cth - lo) >= 0 ; hi: -y_k + (hi - cth) >= 0
+    double4 p = make_double4(0, 0, 0, 0);
+    const double sgn = (lane & 1) ? -1.0 : 1.0;
+    if (k == 0) p.x = sgn;
+    if (k == 1) p.y = sgn;
+    if (k == 2) p.z = sgn;
+    p.w = (lane & 1) ? (A.bhi[k] - cth) : (cth - A.blo[k]);
+    S.pl[lane] = p;
+  }
+  const double L = sqrt((A.bhi[0] - A.blo[0]) * (A.bhi[0] - A.blo[0]) +
+                        (A.bhi[1] - A.blo[1]) * (A.bhi[1] - A.blo[1]) +
+                        (A.bhi[2] - A.blo[2]) * (A.bhi[2] - A.blo[2]));
+  const int base = PASS2 ? A.off[i] : 0;
+
+  // select up to `want` planes from the candidates S.cid / S.key (smallest key first, ties:
+  // smaller id), appended after the nK kept ones
+  auto select = [&](int nK, int want) {
+    int sel = nK;
+    for (; sel < want; ++sel) {
+      double bk = 1e300;
+      int bi = 0x7fffffff, bs = -1;
+      for (int s2 = lane; s2 < NB_CAPC; s2 += 32) {
+        const int j = S.cid[s2];
+        if (j < 0) continue;
+        const double k = S.key[s2];
+        if (k < bk || (k == bk && j < bi)) {
+          bk = k;
+          bi = j;
+          bs = s2;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+        if (ok < bk || (ok == bk && oi < bi)) {
+          bk = ok;
+          bi = oi;
+          bs = os;
+        }
+      }
+      if (bs < 0) break;
+      if (lane == 0) {
+        const int j = S.cid[bs];
+        S.cid[bs] = -1;
+        const double ux = A.sph[4 * j] - si.x, uy = A.sph[4 * j + 1] - si.y,
+                     uz = A.sph[4 * j + 2] - si.z, rj = A.sph[4 * j + 3];
+        const double u2 = ux * ux + uy * uy + uz * uz, un = sqrt(u2);
+        // h_ij(y) = -2 u.y + |u|^2 - r_j^2 + r_i^2 >= 0, normalised by 2|u|
+        S.pl[6 + sel] = make_double4(-ux / un, -uy / un, -uz / un,
+                                     (u2 - rj * rj + si.w * si.w) / (2.0 * un));
+        S.kid[sel] = j;
+      }
+      __syncwarp();
+    }
+    return sel;
+  };
+  // round 0: K = the KSEL smallest power distances at theta_i.  Later rounds (monotone, the
+  // polytope only shrinks): K = the planes of K that are facets of P_K (the others are
+  // redundant for it) + the deepest cuts into P_K among the ball's spheres.  Converged when no
+  // sphere cuts deeper than tolF: the final scan lists the hits.
+  int nK = select(0, NB_KSEL0);
+  if (lane == 0) S.first = nK > 0 ? S.kid[0] : -1;
+  __syncwarp();
+  const int n_sel = nK;
+  int n_v = 0;
+  double R = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, rs = 0.0;
+  double bc[3] = {0, 0, 0}, be[3] = {0, 0, 0}, rho_v = 0.0, pdm_v = 0.0, evm_v = 0.0;
+  unsigned long long n_tri = 0;
+  const double tolF = 1e-6 * L + 1e-9;
+  bool converged = false;
+  for (int round = 0;; ++round) {
+    const bool final_round = converged || round == NB_ROUNDS - 1;
+    if (!converged) {
+    const int M = 6 + nK;
+    if (lane == 0) S.n_v = 0;
+    __syncwarp();
+    // ---- 3. vertices of P_K: every plane triple a < b < c, lane = pair (a, b)
+    const int n_pairs = M * (M - 1) / 2;
+    for (int q = lane; q < n_pairs; q += 32) {
+      int a = 0, rem = q;
+      while (rem >= M - 1 - a) {
+        rem -= M - 1 - a;
+        ++a;
+      }
+      const int b = a + 1 + rem;
+      const double4 pa = S.pl[a], pb = S.pl[b];
+      const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
+                   ab_z = pa.x * pb.y - pa.y * pb.x;
+      for (int cc = b + 1; cc < M; ++cc) {
+        const double4 pc = S.pl[cc];
+        ++n_tri;
+        const double det = pc.x * ab_x + pc.y * ab_y + pc.z * ab_z;
+        if (fabs(det) < 1e-13) continue;
+        const double bc_x = pb.y * pc.z - pb.z * pc.y, bc_y = pb.z * pc.x - pb.x * pc.z,
+                     bc_z = pb.x * pc.y - pb.y * pc.x;
+        const double ca_x = pc.y * pa.z - pc.z * pa.y, ca_y = pc.z * pa.x - pc.x * pa.z,
+                     ca_z = pc.x * pa.y - pc.y * pa.x;
+        const double inv = -1.0 / det;
+        const double yx = (pa.w * bc_x + pb.w * ca_x + pc.w * ab_x) * inv;
+        const double yy = (pa.w * bc_y + pb.w * ca_y + pc.w * ab_y) * inv;
+        const double yz = (pa.w * bc_z + pb.w * ca_z + pc.w * ab_z) * inv;
+        // error radius: rounding of the offsets and cofactors amplified by 1/|det|
+        const double ev = 64.0 * 1.1102230246251565e-16 *
+                          (fabs(pa.w) + fabs(pb.w) + fabs(pc.w) + L) / fabs(det);
+        bool ok = true;
+        for (int k = 0; k < M && ok; ++k) {
+          const double4 pk = S.pl[k];
+          const double h = pk.x * yx + pk.y * yy + pk.z * yz + pk.w;
+          ok = h >= -(ev + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+        }
+        if (!ok) continue;
+        const int s2 = atomicAdd(&S.n_v, 1);
+        if (s2 < NB_MAXV) S.vx[s2] = make_double4(yx, yy, yz, ev);
+      }
+    }
+    __syncwarp();
+    n_v = S.n_v;
+    if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
+      if (!PASS2 && lane == 0) A.cnt[i] = 0;
+      if (!PASS2) {
+        for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
+        if (lane == 0) atomicAdd(&A.stats[2], n_tri);
+      }
+      return;
+    }
+    if (n_v > NB_MAXV) {  // conservative fallback: the box corners
+      __syncwarp();
+      if (lane < 8)
+        S.vx[lane] = make_double4(((lane & 1) ? A.bhi[0] : A.blo[0]) - si.x,
+                                  ((lane & 2) ? A.bhi[1] : A.blo[1]) - si.y,
+                                  ((lane & 4) ? A.bhi[2] : A.blo[2]) - si.z, A.tol0);
+      if (!PASS2 && lane == 0 && final_round) atomicAdd(&A.stats[0], 1ull);
+      n_v = 8;
+      __syncwarp();
+    }
+    // ---- 4. search ball
+    double rho = 0.0, pdm = -1e300, evm = 0.0;
+    for (int s2 = lane; s2 < n_v; s2 += 32) {
+      const double4 v = S.vx[s2];
+      const double d2 = v.x * v.x + v.y * v.y + v.z * v.z, d = sqrt(d2) + v.w;
+      rho = fmax(rho, d);
+      pdm = fmax(pdm, d * d - si.w * si.w);
+      evm = fmax(evm, v.w);
+    }
+    rho = warp_max(rho);
+    pdm = warp_max(pdm);
+    evm = warp_max(evm);
+    R = (rho + sqrt(fmax(pdm, 0.0) + g.rmax * g.rmax)) * (1.0 + 1e-9) +
+        4.0 * (evm + A.tol0) + 1e-9 * L;
+    // bounding ball of P_K around the vertex centroid: a plane farther than its radius from
+    // the centre misses P_K (one dot product instead of a loop over the vertices)
+    {
+      double sx = 0, sy = 0, sz = 0;
+      for (int s2 = lane; s2 < n_v; s2 += 32) {
+        sx += S.vx[s2].x;
+        sy += S.vx[s2].y;
+        sz += S.vx[s2].z;
+      }
+      for (int o = 16; o; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+      }
+      cx = sx / n_v;
+      cy = sy / n_v;
+      cz = sz / n_v;
+      double rr = 0.0;
+      for (int s2 = lane; s2 < n_v; s2 += 32) {
+        const double4 v = S.vx[s2];
+        const double dx = v.x - cx, dy = v.y - cy, dz = v.z - cz;
+        rr = fmax(rr, sqrt(dx * dx + dy * dy + dz * dz) + v.w);
+      }
+      rs = warp_max(rr) * (1.0 + 1e-12) + 1e-12 * L;
+      // axis box of the vertices (grown by their error radii): centre bc, half extents be
+      double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+      for (int s2 = lane; s2 < n_v; s2 += 32) {
+        const double4 v = S.vx[s2];
+        mn[0] = fmin(mn[0], v.x - v.w);
+        mn[1] = fmin(mn[1], v.y - v.w);
+        mn[2] = fmin(mn[2], v.z - v.w);
+        mx[0] = fmax(mx[0], v.x + v.w);
+        mx[1] = fmax(mx[1], v.y + v.w);
+        mx[2] = fmax(mx[2], v.z + v.w);
+      }
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = -warp_max(-mn[k]);
+        mx[k] = warp_max(mx[k]);
+        bc[k] = 0.5 * (mn[k] + mx[k]);
+        be[k] = 0.5 * (mx[k] - mn[k]) * (1.0 + 1e-12) + 1e-12 * L;
+      }
+      rho_v = rho;
+      pdm_v = pdm;
+      evm_v = evm;
+    }
+    }  // !converged
+    unsigned long long fmask = 0;  // facets of P_K among the K planes (lane = plane)
+    if (!final_round) {
+      for (int p0 = 0; p0 < nK; p0 += 32) {
+        const int p = p0 + lane;
+        bool facet = false;
+        if (p < nK) {
+          const double4 pk = S.pl[6 + p];
+          const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w);
+          double depth = 1e300;
+          for (int s2 = 0; s2 < n_v && depth > slack; ++s2) {
+            const double4 v = S.vx[s2];
+            depth = fmin(depth, pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w - v.w);
+          }
+          facet = depth <= slack;
+        }
+        fmask |= (unsigned long long)__ballot_sync(0xffffffffu, facet) << p0;
+      }
+      top.init();
+    }
+    // ---- 5. every sphere of the ball whose plane reaches a vertex of P_K: collected with its
+    // depth (selection of the next round) or, in the final round, listed
+    int lo[3], hi[3];
+    {
+      const double c[3] = {si.x, si.y, si.z};
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = nb_cell_axis(c[k] - R, g, k);
+        hi[k] = nb_cell_axis(c[k] + R, g, k);
+      }
+    }
+    const int nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+    const long long ncell = (long long)nx * ny * nz;
+    dbg_cells += ncell;
+    ++dbg_rounds;
+    for (long long q = lane; q < ncell; q += 32) {
+      const int x = lo[0] + (int)(q % nx), y = lo[1] + (int)((q / nx) % ny),
+                z = lo[2] + (int)(q / ((long long)nx * ny));
+      double dd = 0.0;  // distance from theta_i to the cell's box
+      {
+        const int cc[3] = {x, y, z};
+        const double c[3] = {si.x, si.y, si.z};
+        for (int k = 0; k < 3; ++k) {
+          const double a = g.lo[k] + cc[k] * g.h[k], b = a + g.h[k];
+          const double e = c[k] < a ? a - c[k] : (c[k] > b ? c[k] - b : 0.0);
+          dd += e * e;
+        }
+      }
+      if (dd > R * R * (1.0 + 1e-9)) continue;
+      const int cid = (z * G + y) * G + x;
+      for (int p = A.start[cid]; p < A.start[cid + 1]; ++p) {
+        const int j = A.items[p];
+        if (j == i) continue;
+        const double ux = A.sph[4 * j] - si.x, uy = A.sph[4 * j + 1] - si.y,
+                     uz = A.sph[4 * j + 2] - si.z, rj = A.sph[4 * j + 3];
+        const double u2 = ux * ux + uy * uy + uz * uz;
+        if (u2 == 0.0 || u2 > R * R) continue;
+        {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack)
+          const double Rj = (rho_v + sqrt(fmax(pdm_v, 0.0) + rj * rj)) * (1.0 + 1e-9) +
+                            4.0 * (evm_v + A.tol0) + 1e-9 * L;
+          if (u2 > Rj * Rj) continue;
+        }
+        const double un = sqrt(u2);
+        const double ax = -ux / un, ay = -uy / un, az = -uz / un;
+        const double bw = (u2 - rj * rj + si.w * si.w) / (2.0 * un);
+        const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(bw);
+        ++dbg_scan;
+        const double hcen = ax * cx + ay * cy + az * cz + bw;  // plane value at the centre
+        // lower bounds of the plane's minimum over P_K: the centroid ball and the vertex box
+        const double lb = fmax(hcen - rs, ax * bc[0] + ay * bc[1] + az * bc[2] + bw -
+                                              (fabs(ax) * be[0] + fabs(ay) * be[1] + fabs(az) * be[2]));
+        if (final_round ? lb > slack : lb >= -tolF) continue;
+        // final round: a hit once some vertex is within slack; earlier rounds: a deep cut once
+        // some vertex is cut by more than tolF (ranked by the value at the centre)
+        const double thr = final_round ? slack : -tolF;
+        double depth = 1e300;
+        for (int s2 = 0; s2 < n_v; ++s2) {
+          const double4 v = S.vx[s2];
+          depth = fmin(depth, ax * v.x + ay * v.y + az * v.z + bw - v.w);
+          ++dbg_vloop;
+          if (final_round ? depth <= thr : depth < thr) break;
+        }
+        if (final_round ? depth > thr : depth >= thr) continue;
+        if (final_round) {
+          const int s2 = atomicAdd(&S.n_o, 1);
+          if (PASS2) {
+            A.tmp[base + s2] = j;
+          } else if (s2 < NB_CAP1) {
+            S.out[s2] = j;
+          }
+        } else {
+          top.push(hcen, j);
+        }
+      }
+    }
+    __syncwarp();
+    if (final_round) break;
+    int n_deep = 0;
+    for (int t = 0; t < 4; ++t) {
+      S.cid[4 * lane + t] = top.j[t];
+      S.key[4 * lane + t] = top.k[t];
+      n_deep += top.j[t] >= 0;
+    }
+    for (int o = 16; o; o >>= 1) n_deep += __shfl_xor_sync(0xffffffffu, n_deep, o);
+    if (n_deep == 0) {
+      converged = true;
+      continue;
+    }
+    // keep the facet planes (compacted in order), then the deepest cuts
+    __syncwarp();
+    if (lane == 0) {
+      int q = 0;
+      for (int p = 0; p < nK; ++p)
+        if (fmask >> p & 1ull) {
+          S.pl[6 + q] = S.pl[6 + p];
+          S.kid[q] = S.kid[p];
+          ++q;
+        }
+    }
+    __syncwarp();
+    nK = select(__popcll(fmask), NB_KSEL);
+  }
+  if (!PASS2) {
+    for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
+    if (lane == 0) atomicAdd(&A.stats[2], n_tri);
+  }
+  __syncwarp();
+  int n_o = S.n_o;
+  if (n_o == 0 && A.N > 1) {  // i's cell covers B: list the nearest sphere (redundant plane)
+    if (n_sel > 0 && lane == 0) {  // not hit: h_ij > 0 on P_K, so the plane is redundant
+      if (PASS2) A.tmp[base] = S.first;
+      else S.out[0] = S.first;
+      S.n_o = 1;
+    }
+    __syncwarp();
+    n_o = S.n_o;
+  }
+  if (A.dbg && !PASS2) {
+    for (int o = 16; o; o >>= 1) {
+      dbg_scan += __shfl_xor_sync(0xffffffffu, dbg_scan, o);
+      dbg_vloop += __shfl_xor_sync(0xffffffffu, dbg_vloop, o);
+    }
+    if (lane == 0) {
+      long long* d = A.dbg + 8 * (long long)i;
+      d[0] = clock64() - t_start;
+      d[1] = dbg_rounds;
+      d[2] = dbg_cells;
+      d[3] = dbg_scan;
+      d[4] = dbg_vloop;
+      d[5] = n_v;
+      d[6] = n_o;
+      d[7] = R * 1000;
+    }
+  }
+  if (!PASS2) {
+    if (lane == 0) {
+      A.cnt[i] = n_o;
+      if (n_o > NB_CAP1) A.long_ids[atomicAdd(A.n_long, 1)] = i;
+    }
+    if (n_o <= NB_CAP1)
+      for (int s = lane; s < n_o; s += 32) A.slab[(int64_t)i * NB_CAP1 + s] = S.out[s];
+  }
+}
+
+__global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
+  __shared__ NbSmem sm[NB_WARPS];
+  if (*(volatile int*)A.err != 0) {  // invalid input: empty rows, no dereference of NaN cells
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.N;
+         i += (int64_t)gridDim.x * blockDim.x)
+      A.cnt[i] = 0;
+    return;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = (int64_t)blockIdx.x * NB_WARPS + w; i < A.N; i += (int64_t)gridDim.x * NB_WARPS)
+    nb_row<false>(A, sm[w], (int)i, lane);
+}
+
+__global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass2(NbArgs A) {
+  __shared__ NbSmem sm[NB_WARPS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = *A.n_long;
+  for (int q = blockIdx.x * NB_WARPS + w; q < n; q += gridDim.x * NB_WARPS)
+    nb_row<true>(A, sm[w], A.long_ids[q], lane);
+}
+
+// rows into ascending order: rank of each entry among its row (entries are distinct)
+__global__ void k_nb_sort(int64_t N, const int32_t* __restrict__ off, const int32_t* __restrict__ slab,
+                          const int32_t* __restrict__ tmp, int32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int a = off[i], n = off[i + 1] - a;
+    const int32_t* src = n <= NB_CAP1 ? slab + i * NB_CAP1 : tmp + a;
+    for (int s = lane; s < n; s += 32) {
+      const int v = src[s];
+      int rk = 0;
+      for (int t = 0; t < n; ++t) rk += src[t] < v;
+      idx[a + rk] = v;
+    }
+  }
+}
+
+}  // namespace
+
+size_t nb_grid_cells(int64_t N) {
+  int G = 1;
+  while ((int64_t)G * G * G * 2 < N && G < NB_GMAX) ++G;
+  return (size_t)G * G * G;
+}
+
+// Pass 1 and the scan; *E_dev = total entries (off[N]).  Buffers in c->nb_buf.
+cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                                   int32_t* cnt, int32_t* off) {
+  int G = 1;
+  while ((int64_t)G * G * G * 2 < N && G < NB_GMAX) ++G;
+  const int64_t ncell = (int64_t)G * G * G;
+  const size_t bytes = sizeof(NbGrid) + 16 + sizeof(int32_t) * (3 * (ncell + 1) + 2 * (N + 1) + 2) +
+                       sizeof(int32_t) * (size_t)N * NB_CAP1 + sizeof(unsigned long long) * 4 + 256;
+  cudaError_t e = c->nb_buf.ensure(bytes);
+  if (e) return e;
+  char* b = c->nb_buf.as<char>();
+  auto take = [&](size_t n) {
+    char* r = b;
+    b += (n + 15) & ~size_t(15);
+    return r;
+  };
+  NbGrid* g = reinterpret_cast<NbGrid*>(take(sizeof(NbGrid)));
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(take(8 * 4));
+  int32_t* ccnt = reinterpret_cast<int32_t*>(take(4 * (ncell + 1)));
+  int32_t* start = reinterpret_cast<int32_t*>(take(4 * (ncell + 1)));
+  int32_t* fill = reinterpret_cast<int32_t*>(take(4 * (ncell + 1)));
+  int32_t* cell_of = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
+  int32_t* items = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
+  int32_t* nlong = reinterpret_cast<int32_t*>(take(4 * 2));
+  int32_t* slab = reinterpret_cast<int32_t*>(take(4 * (size_t)N * NB_CAP1));
+  c->nb_grid = g;
+  c->nb_stats = st;
+  c->nb_start = start;
+  c->nb_items = items;
+  c->nb_long = nlong;
+  c->nb_slab = slab;
+  c->nb_long_ids = cell_of;
+  if ((e = cudaMemsetAsync(ccnt, 0, 4 * (ncell + 1), c->stream))) return e;
+  if ((e = cudaMemsetAsync(fill, 0, 4 * (ncell + 1), c->stream))) return e;
+  if ((e = cudaMemsetAsync(st, 0, 8 * 4, c->stream))) return e;
+  if ((e = cudaMemsetAsync(nlong, 0, 8, c->stream))) return e;
+  const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
+  k_nb_check<<<blocks, 256, 0, c->stream>>>(sph, N, c->errw.as<int>());
+  ++c->launches;
+  k_nb_bounds<<<1, 1024, 0, c->stream>>>(sph, N, G, g);
+  ++c->launches;
+  k_nb_count<<<blocks, 256, 0, c->stream>>>(sph, N, g, ccnt, cell_of);
+  ++c->launches;
+  if ((e = launch_scan_i32(c, ccnt, start, ncell))) return e;
+  k_nb_scatter<<<blocks, 256, 0, c->stream>>>(N, cell_of, start, fill, items);
+  ++c->launches;
+  k_nb_cellsort<<<(int)std::min<int64_t>((ncell + 255) / 256, 8 * (int64_t)c->sms), 256, 0,
+                  c->stream>>>(ncell, start, items);
+  ++c->launches;
+  NbArgs A{};
+  A.sph = sph;
+  A.N = N;
+  A.grid = g;
+  A.start = start;
+  A.items = items;
+  double L2 = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    A.blo[k] = box[k];
+    A.bhi[k] = box[3 + k];
+    L2 += (box[3 + k] - box[k]) * (box[3 + k] - box[k]);
+  }
+  A.tol0 = 1e-9 * sqrt(L2) + 1e-12;
+  A.cnt = cnt;
+  A.slab = slab;
+  A.n_long = nlong;
+  A.long_ids = reinterpret_cast<int32_t*>(cell_of);  // cell_of is dead after the scatter
+  A.stats = st;
+  A.err = c->errw.as<int>();
+  A.dbg = (long long*)c->nb_dbg;
+  c->nb_args_tol0 = A.tol0;
+  const int mb = (int)std::min<int64_t>((N + NB_WARPS - 1) / NB_WARPS, 16 * (int64_t)c->sms);
+  k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  if ((e = cudaGetLastError())) return e;
+  if ((e = launch_scan_i32(c, cnt, off, N))) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                                   int32_t* cnt, const int32_t* off, int32_t* tmp, int32_t* idx) {
+  NbArgs A{};
+  A.sph = sph;
+  A.N = N;
+  A.grid = reinterpret_cast<const NbGrid*>(c->nb_grid);
+  A.start = c->nb_start;
+  A.items = c->nb_items;
+  for (int k = 0; k < 3; ++k) {
+    A.blo[k] = box[k];
+    A.bhi[k] = box[3 + k];
+  }
+  A.tol0 = c->nb_args_tol0;
+  A.cnt = cnt;
+  A.slab = c->nb_slab;
+  A.off = off;
+  A.tmp = tmp;
+  A.n_long = c->nb_long;
+  A.long_ids = c->nb_long_ids;
+  A.stats = c->nb_stats;
+  k_nb_pass2<<<2 * c->sms, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
+  k_nb_sort<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, off, c->nb_slab, tmp, idx);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+}  // namespace rpd

@@ -26,7 +26,8 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
-            "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope"]
+            "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
+            "rpd_neighbors", "rpd_download_neighbors"]
 
 
 class RPDError(RuntimeError):
@@ -54,6 +55,11 @@ class _Topology(C.Structure):
                 ("rpf_comp", C.c_void_p), ("piece_sosfm", C.c_void_p), ("rpf_fm", C.c_void_p),
                 ("rpf_adj", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
                 ("E", C.c_int64)]
+
+
+class _NbrLists(C.Structure):
+    _fields_ = [("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("N", C.c_int64),
+                ("E", C.c_int64), ("n_hidden", C.c_int64), ("n_vertex_overflow", C.c_int64)]
 
 
 class _Medial(C.Structure):
@@ -118,6 +124,8 @@ def load_library(path: str = LIB_PATH):
     L.rpd_download_topology.argtypes = [vp] * 8
     L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
     L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
+    L.rpd_neighbors.argtypes = [vp, vp, i64, vp, C.POINTER(_NbrLists)]
+    L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
     L.rpd_envelope.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(i64)]
     L.rpd_version.restype = C.c_char_p
@@ -125,7 +133,8 @@ def load_library(path: str = LIB_PATH):
               "rpd_download_pieces", "rpd_download_cands", "rpd_get_stats", "rpd_set_euler",
               "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
-              "rpd_gather_pieces", "rpd_envelope"):
+              "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
+              "rpd_download_neighbors"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -347,6 +356,20 @@ class RPDContext:
         e, f = self._alloc([(2 * m.n_edges, np.int32), (3 * m.n_faces, np.int32)], device)
         self._check(self.L.rpd_download_medial_mesh(self.h, self._p(e), self._p(f)))
         return {"edges": e.reshape(-1, 2), "faces": f.reshape(-1, 3)}
+
+    def neighbors(self, spheres, box, device=False) -> dict:
+        """Sphere neighbour lists on the GPU (NEXT-3): a certified superset of
+        the power-cell neighbours inside the axis box ``box`` = (lo_x, lo_y, lo_z, hi_x, hi_y,
+        hi_z); returns nbr_off [N+1], nbr_idx [E] (rows ascending) and counters."""
+        ps, ks = _ptr(spheres, np.float64)
+        bx = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
+        n = _NbrLists()
+        N = int(np.prod(ks.shape)) // 4
+        self._check(self.L.rpd_neighbors(self.h, ps, N, bx.ctypes.data, C.byref(n)))
+        off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
+        self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
+        return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
+                "n_vertex_overflow": n.n_vertex_overflow}
 
     def gather_pieces(self, shards, tet_ids, T: int) -> dict:
         """Global piece CSR (torch CUDA tensors) from per-rank piece CSRs (``shards``: one dict

@@ -1,0 +1,150 @@
+"""Sphere neighbours on the GPU through the C ABI
+(-m gpu).  Several neighbour lists are correct (any superset of the box neighbours gives the
+same RPD), so the tests check what is unique and that the rest is valid:
+  * every GPU row contains the oracle's box-neighbour row (``oracle.box_neighbours``), and
+    every extra entry is a real sphere != i with a distinct centre (rows ascending, no dups);
+  * the pieces computed with the GPU lists equal the oracle's pieces with the regular-
+    triangulation lists (ids, facemasks, incidences bit-exact; vol / m1 at 1e-9), and at C2 /
+    C3 size the GPU pieces with either list set are equal;
+  * edge cases: N = 0, N = 1, same-centre hiding, a cell covering the box, bad inputs."""
+import numpy as np
+import pytest
+
+import oracle
+import rpd_workloads as W
+from tests.helpers import compare_results
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2403_18761_b200 as P
+    P.build()
+    c = P.RPDContext(0, filter_mode="pruned")
+    yield c
+    c.close()
+
+
+def rows(off, idx):
+    return [idx[off[i]:off[i + 1]].tolist() for i in range(len(off) - 1)]
+
+
+def check_valid(sp, got):
+    off, idx = np.asarray(got["nbr_off"]), np.asarray(got["nbr_idx"])
+    assert off[0] == 0 and np.all(np.diff(off) >= 0) and off[-1] == len(idx)
+    for i, r in enumerate(rows(off, idx)):
+        assert r == sorted(set(r)), i
+        for j in r:
+            assert 0 <= j < len(sp) and j != i
+            assert not np.array_equal(sp[i, :3], sp[j, :3])
+    return off, idx
+
+
+WORKLOADS = [lambda: W.make_shape_workload("nb_smoke", 1200, 100, seed=11, cache=False),
+             lambda: W.make_shape_workload("nb_small", 600, 60, seed=4, cache=False),
+             lambda: W.make_c1(3), lambda: W.make_c1(1, degenerate=True),
+             lambda: W.random_tiny(5, n_spheres=14),
+             lambda: W.random_tiny(2, n_spheres=20, coarse=True)]
+
+
+@pytest.mark.parametrize("k", range(len(WORKLOADS)))
+def test_neighbors_superset_and_pieces(ctx, k):
+    import paper_2403_18761_b200 as P
+    w = WORKLOADS[k]()
+    box = W.mesh_box(w.verts)
+    got = ctx.neighbors(w.spheres, box)
+    off, idx = check_valid(w.spheres, got)
+    roff, ridx = oracle.box_neighbours(w.spheres, box)
+    g, r = rows(off, idx), rows(roff, ridx)
+    for i in range(w.N):
+        assert set(r[i]) <= set(g[i]), (i, sorted(set(r[i]) - set(g[i])))
+    # not much looser than the definition (the bound polytope uses 16 planes)
+    assert len(idx) <= 3 * max(len(ridx), 1) + 8
+    a = P.rpd_full(w.verts, w.tets, w.spheres, off, idx, ctx=ctx)
+    b = oracle.rpd_workload(w)
+    assert compare_results(a, b, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_neighbors_full_size_same_pieces(ctx, name):
+    import paper_2403_18761_b200 as P
+    w = W.make_config(name)
+    got = ctx.neighbors(w.spheres, W.mesh_box(w.verts))
+    off, idx = np.asarray(got["nbr_off"]), np.asarray(got["nbr_idx"])
+    assert off[-1] == len(idx) and np.all(np.diff(off) >= 0)
+    a = P.rpd_full(w.verts, w.tets, w.spheres, off, idx, ctx=ctx)
+    b = P.rpd_full(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx, ctx=ctx)
+    assert compare_results(a, b, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+    # the GPU rows contain every regular-triangulation neighbour that carries an incidence
+    g = rows(off, idx)
+    ps = np.asarray(b["piece_sphere"])
+    for p in range(0, len(ps), max(1, len(ps) // 5000)):
+        inc = b["inc_sphere"][b["inc_off"][p]:b["inc_off"][p + 1]]
+        assert set(inc.tolist()) <= set(g[int(ps[p])])
+
+
+def test_neighbors_edge_cases(ctx):
+    import paper_2403_18761_b200 as P
+    box = (0, 0, 0, 32, 32, 32)
+    got = ctx.neighbors(np.zeros((0, 4)), box)
+    assert list(got["nbr_off"]) == [0] and len(got["nbr_idx"]) == 0
+    got = ctx.neighbors(np.array([[5.0, 5, 5, 1]]), box)
+    assert list(got["nbr_off"]) == [0, 0]
+    # same centre: the larger radius hides the smaller one; equal spheres: the smaller id wins
+    sp = np.array([[8, 8, 8, 2], [8, 8, 8, 3], [20, 20, 20, 1], [20, 20, 20, 1.0]])
+    got = ctx.neighbors(sp, box)
+    r = rows(got["nbr_off"], got["nbr_idx"])
+    assert r[0] == [] and r[3] == [] and got["n_hidden"] == 2
+    assert 2 in r[1] and 1 in r[2]
+    # a cell covering the whole box: one redundant entry so that R4 does not apply
+    sp = np.array([[16, 16, 16, 30.0], [60, 60, 60, 0]])
+    got = ctx.neighbors(sp, box)
+    r = rows(got["nbr_off"], got["nbr_idx"])
+    assert r == [[1], []]
+    v, t = W.box_6tets((0, 0, 0), (32, 32, 32))
+    a = P.rpd_full(v, t, sp, got["nbr_off"], got["nbr_idx"], ctx=ctx)
+    assert list(a["piece_sphere"]) == [0] * 6
+    # dominated sphere (oracle closed form in test_neighbors_oracle)
+    sp = np.array([[16, 16, 16, 6], [17, 16, 16, 1], [28, 16, 16, 1]], dtype=np.float64)
+    got = ctx.neighbors(sp, box)
+    r = rows(got["nbr_off"], got["nbr_idx"])
+    assert r[1] == [] and 2 in r[0] and 0 in r[2]
+
+
+def test_neighbors_invalid(ctx):
+    import paper_2403_18761_b200 as P
+    sp = np.array([[1.0, 2, 3, 1], [4, 5, 6, 1]])
+    for bad_box in [(0, 0, 0, -1, 1, 1), (0, 0, np.nan, 1, 1, 1)]:
+        with pytest.raises(P.RPDError, match="EINVAL"):
+            ctx.neighbors(sp, bad_box)
+    for k, v in [(3, -1.0), (0, np.nan), (1, np.inf)]:
+        s = sp.copy()
+        s[1, k] = v
+        with pytest.raises(P.RPDError, match="EINVAL"):
+            ctx.neighbors(s, (0, 0, 0, 8, 8, 8))
+    # the ctx stays usable
+    got = ctx.neighbors(sp, (0, 0, 0, 8, 8, 8))
+    assert rows(got["nbr_off"], got["nbr_idx"]) == [[1], [0]]
+    import torch
+    d = torch.tensor(sp, device="cuda")
+    got = ctx.neighbors(d, (0, 0, 0, 8, 8, 8), device=True)
+    assert got["nbr_idx"].is_cuda and got["nbr_idx"].tolist() == [1, 0]
+
+
+def test_neighbors_partial_update(ctx):
+    """C4-style: lists recomputed on the GPU after an insertion batch feed rpd_update_partial;
+    the result equals a full recompute with the regular-triangulation lists."""
+    import paper_2403_18761_b200 as P
+    w = W.make_shape_workload("nb_part", 3000, 150, seed=6, n_batches=1, batch_m=20, cache=False)
+    box = W.mesh_box(w.verts)
+    g0 = ctx.neighbors(w.spheres, box)
+    ctx.relations(w.verts, w.tets, w.spheres, g0["nbr_off"], g0["nbr_idx"])
+    ctx.clip()
+    sp1, off1, idx1 = w.batches[0]
+    g1 = ctx.neighbors(sp1, box)
+    n_old = w.N
+    ctx.update_partial(sp1, g1["nbr_off"], g1["nbr_idx"], np.arange(n_old, len(sp1), dtype=np.int32))
+    got = ctx.download_pieces()
+    ref = P.rpd_full(w.verts, w.tets, sp1, off1, idx1, ctx=None, filter_mode="pruned")
+    assert compare_results(got, ref, w.verts, w.tets, rel=1e-9, check_cands=False) == []
