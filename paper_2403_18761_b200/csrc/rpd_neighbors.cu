@@ -39,9 +39,10 @@ constexpr int NB_KSEL = 48;               // planes of a refined P_K (facets + d
 constexpr int NB_MAXP = 6 + NB_KSEL;
 constexpr int NB_MAXV = 224;              // vertex candidates of P_K per sphere
 constexpr int NB_CAPC = 128;              // selection candidates: 4 per lane
-constexpr int NB_CAP1 = 64;               // row entries kept by pass 1
+constexpr int NB_CAP1 = 256;              // row entries kept by pass 1
 constexpr int NB_WARPS = 4;               // warps per block of the main kernel
 constexpr int NB_GMAX = 160;              // grid cells per axis (max)
+constexpr int NB_RB = 256;                // radius buckets of the work order
 constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
 
 struct NbGrid {
@@ -187,12 +188,46 @@ __global__ void k_nb_cellsort(int64_t n_cells, const int32_t* __restrict__ start
   }
 }
 
+__global__ void k_nb_gather(int64_t N, const int32_t* __restrict__ items,
+                            const double* __restrict__ sph, double4* __restrict__ sorted) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int j = items[p];
+    sorted[p] = make_double4(sph[4 * j], sph[4 * j + 1], sph[4 * j + 2], sph[4 * j + 3]);
+  }
+}
+
+// work order: spheres by descending radius (the big spheres have the big cells and the long
+// scans), taken from a counter, so that the longest rows start first
+__device__ __forceinline__ int nb_rbucket(double r, double rmax) {
+  const int b = rmax > 0 ? (int)((1.0 - r / rmax) * NB_RB) : 0;
+  return b < 0 ? 0 : (b >= NB_RB ? NB_RB - 1 : b);
+}
+__global__ void k_nb_rcount(const double* __restrict__ sph, int64_t N, const NbGrid* __restrict__ g,
+                            int32_t* __restrict__ cnt) {
+  const double rmax = g->rmax;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[nb_rbucket(sph[4 * i + 3], rmax)], 1);
+}
+__global__ void k_nb_rscatter(const double* __restrict__ sph, int64_t N,
+                              const NbGrid* __restrict__ g, const int32_t* __restrict__ start,
+                              int32_t* __restrict__ fill, int32_t* __restrict__ order) {
+  const double rmax = g->rmax;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = nb_rbucket(sph[4 * i + 3], rmax);
+    order[start[b] + atomicAdd(&fill[b], 1)] = (int)i;
+  }
+}
+
 struct NbArgs {
   const double* sph;
   int64_t N;
   const NbGrid* grid;
   const int32_t* start;   // [G^3 + 1]
   const int32_t* items;   // spheres by cell
+  const double4* sorted;  // their (x, y, z, r), same order
   double blo[3], bhi[3];  // the domain box B
   double tol0;            // absolute slack (distance units)
   int32_t* cnt;           // [N] row lengths (pass 1 writes)
@@ -203,6 +238,8 @@ struct NbArgs {
   int32_t* long_ids;
   unsigned long long* stats;  // [0] vertex overflows, [1] hidden, [2] triples
   int* err;
+  const int32_t* order;   // work order (pass 1)
+  int32_t* work;          // work counter (pass 1)
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
 };
 
@@ -339,13 +376,42 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
   unsigned long long n_tri = 0;
   const double tolF = 1e-6 * L + 1e-9;
   bool converged = false;
+  bool list_exact = true;  // S.vx holds the vertices of P_K (not the box fallback)
+  int first_new = 0;
   for (int round = 0;; ++round) {
     const bool final_round = converged || round == NB_ROUNDS - 1;
     if (!converged) {
     const int M = 6 + nK;
-    if (lane == 0) S.n_v = 0;
+    // ---- 3. vertices of P_K.  Round 0: every plane triple a < b < c.  Later rounds (P_K =
+    // P_old ∩ new planes, planes [first_new, M) new): the old vertices that satisfy the new
+    // planes (every old vertex lies on >= 3 kept facet planes), plus the triples whose largest
+    // index is a new plane.  lane = pair (a, b)
+    if (first_new > 0) {
+      int kept = 0;
+      for (int c0 = 0; c0 < n_v; c0 += 32) {
+        const int s2 = c0 + lane;
+        bool ok = false;
+        double4 v = make_double4(0, 0, 0, 0);
+        if (s2 < n_v) {
+          v = S.vx[s2];
+          ok = true;
+          for (int k = first_new; k < M && ok; ++k) {
+            const double4 pk = S.pl[k];
+            ok = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w >=
+                 -(v.w + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        __syncwarp();
+        if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;  // in place: <= s2
+        kept += __popc(m);
+        __syncwarp();
+      }
+      if (lane == 0) S.n_v = kept;
+    } else if (lane == 0) {
+      S.n_v = 0;
+    }
     __syncwarp();
-    // ---- 3. vertices of P_K: every plane triple a < b < c, lane = pair (a, b)
     const int n_pairs = M * (M - 1) / 2;
     for (int q = lane; q < n_pairs; q += 32) {
       int a = 0, rem = q;
@@ -357,7 +423,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       const double4 pa = S.pl[a], pb = S.pl[b];
       const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
                    ab_z = pa.x * pb.y - pa.y * pb.x;
-      for (int cc = b + 1; cc < M; ++cc) {
+      for (int cc = max(b + 1, first_new); cc < M; ++cc) {
         const double4 pc = S.pl[cc];
         ++n_tri;
         const double det = pc.x * ab_x + pc.y * ab_y + pc.z * ab_z;
@@ -395,6 +461,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       return;
     }
     if (n_v > NB_MAXV) {  // conservative fallback: the box corners
+      list_exact = false;
       __syncwarp();
       if (lane < 8)
         S.vx[lane] = make_double4(((lane & 1) ? A.bhi[0] : A.blo[0]) - si.x,
@@ -494,29 +561,54 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       }
     }
     const int nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
-    const long long ncell = (long long)nx * ny * nz;
-    dbg_cells += ncell;
     ++dbg_rounds;
-    for (long long q = lane; q < ncell; q += 32) {
-      const int x = lo[0] + (int)(q % nx), y = lo[1] + (int)((q / nx) % ny),
-                z = lo[2] + (int)(q / ((long long)nx * ny));
-      double dd = 0.0;  // distance from theta_i to the cell's box
+    // rows of cells (fixed y, z) are contiguous in the cell-sorted arrays: lane = row for the
+    // ranges, then the warp walks the concatenated ranges (coalesced id / sphere loads)
+    const int nrows = ny * nz;
+    for (int r0 = 0; r0 < nrows; r0 += 32) {
+      int pb = 0, pe = 0;
       {
-        const int cc[3] = {x, y, z};
-        const double c[3] = {si.x, si.y, si.z};
-        for (int k = 0; k < 3; ++k) {
-          const double a = g.lo[k] + cc[k] * g.h[k], b = a + g.h[k];
-          const double e = c[k] < a ? a - c[k] : (c[k] > b ? c[k] - b : 0.0);
-          dd += e * e;
+        const int rr = r0 + lane;
+        if (rr < nrows) {
+          const int y = lo[1] + rr % ny, z = lo[2] + rr / ny;
+          double dd = 0.0;  // distance from theta_i to the row's (y, z) extent
+          {
+            const double ay0 = g.lo[1] + y * g.h[1], ay1 = ay0 + g.h[1];
+            const double az0 = g.lo[2] + z * g.h[2], az1 = az0 + g.h[2];
+            const double ey = si.y < ay0 ? ay0 - si.y : (si.y > ay1 ? si.y - ay1 : 0.0);
+            const double ez = si.z < az0 ? az0 - si.z : (si.z > az1 ? si.z - az1 : 0.0);
+            dd = ey * ey + ez * ez;
+          }
+          if (dd <= R * R * (1.0 + 1e-9)) {
+            const int c0 = (z * G + y) * G;
+            pb = A.start[c0 + lo[0]];
+            pe = A.start[c0 + hi[0] + 1];
+          }
         }
       }
-      if (dd > R * R * (1.0 + 1e-9)) continue;
-      const int cid = (z * G + y) * G + x;
-      for (int p = A.start[cid]; p < A.start[cid + 1]; ++p) {
+      const int len = pe - pb;
+      int incl = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int excl = incl - len;
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        int k = 0;  // the row holding t: the largest k with excl_k <= t
+        for (int step = 16; step; step >>= 1) {
+          const int e = __shfl_sync(0xffffffffu, excl, k + step);
+          if (e <= t) k += step;
+        }
+        const int pbk = __shfl_sync(0xffffffffu, pb, k), exk = __shfl_sync(0xffffffffu, excl, k);
+        if (t >= total) continue;
+        const int p = pbk + (t - exk);
         const int j = A.items[p];
+        const double4 sj = A.sorted[p];
+        dbg_cells += 1;
         if (j == i) continue;
-        const double ux = A.sph[4 * j] - si.x, uy = A.sph[4 * j + 1] - si.y,
-                     uz = A.sph[4 * j + 2] - si.z, rj = A.sph[4 * j + 3];
+        const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z, rj = sj.w;
         const double u2 = ux * ux + uy * uy + uz * uz;
         if (u2 == 0.0 || u2 > R * R) continue;
         {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack)
@@ -583,6 +675,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
     }
     __syncwarp();
     nK = select(__popcll(fmask), NB_KSEL);
+    first_new = list_exact ? 6 + __popcll(fmask) : 0;
   }
   if (!PASS2) {
     for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
@@ -635,8 +728,13 @@ __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
     return;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t i = (int64_t)blockIdx.x * NB_WARPS + w; i < A.N; i += (int64_t)gridDim.x * NB_WARPS)
-    nb_row<false>(A, sm[w], (int)i, lane);
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(A.work, 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= A.N) break;
+    nb_row<false>(A, sm[w], A.order[q], lane);
+  }
 }
 
 __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass2(NbArgs A) {
@@ -679,7 +777,9 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   while ((int64_t)G * G * G * 2 < N && G < NB_GMAX) ++G;
   const int64_t ncell = (int64_t)G * G * G;
   const size_t bytes = sizeof(NbGrid) + 16 + sizeof(int32_t) * (3 * (ncell + 1) + 2 * (N + 1) + 2) +
-                       sizeof(int32_t) * (size_t)N * NB_CAP1 + sizeof(unsigned long long) * 4 + 256;
+                       sizeof(int32_t) * (size_t)N * NB_CAP1 + sizeof(unsigned long long) * 4 +
+                       sizeof(double4) * (N + 1) + sizeof(int32_t) * (3 * (NB_RB + 1) + 2 + N + 1) +
+                       1024;
   cudaError_t e = c->nb_buf.ensure(bytes);
   if (e) return e;
   char* b = c->nb_buf.as<char>();
@@ -696,7 +796,10 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   int32_t* cell_of = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
   int32_t* items = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
   int32_t* nlong = reinterpret_cast<int32_t*>(take(4 * 2));
+  int32_t* rb = reinterpret_cast<int32_t*>(take(4 * (3 * (NB_RB + 1) + 2)));  // cnt, start, fill, work
+  int32_t* order = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
   int32_t* slab = reinterpret_cast<int32_t*>(take(4 * (size_t)N * NB_CAP1));
+  double4* sorted = reinterpret_cast<double4*>(take(sizeof(double4) * (N + 1)));
   c->nb_grid = g;
   c->nb_stats = st;
   c->nb_start = start;
@@ -704,10 +807,12 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   c->nb_long = nlong;
   c->nb_slab = slab;
   c->nb_long_ids = cell_of;
+  c->nb_sorted = sorted;
   if ((e = cudaMemsetAsync(ccnt, 0, 4 * (ncell + 1), c->stream))) return e;
   if ((e = cudaMemsetAsync(fill, 0, 4 * (ncell + 1), c->stream))) return e;
   if ((e = cudaMemsetAsync(st, 0, 8 * 4, c->stream))) return e;
   if ((e = cudaMemsetAsync(nlong, 0, 8, c->stream))) return e;
+  if ((e = cudaMemsetAsync(rb, 0, 4 * (3 * (NB_RB + 1) + 2), c->stream))) return e;
   const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
   k_nb_check<<<blocks, 256, 0, c->stream>>>(sph, N, c->errw.as<int>());
   ++c->launches;
@@ -721,12 +826,23 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   k_nb_cellsort<<<(int)std::min<int64_t>((ncell + 255) / 256, 8 * (int64_t)c->sms), 256, 0,
                   c->stream>>>(ncell, start, items);
   ++c->launches;
+  k_nb_gather<<<blocks, 256, 0, c->stream>>>(N, items, sph, sorted);
+  ++c->launches;
+  k_nb_rcount<<<blocks, 256, 0, c->stream>>>(sph, N, g, rb);
+  ++c->launches;
+  if ((e = launch_scan_i32(c, rb, rb + (NB_RB + 1), NB_RB))) return e;
+  k_nb_rscatter<<<blocks, 256, 0, c->stream>>>(sph, N, g, rb + (NB_RB + 1), rb + 2 * (NB_RB + 1),
+                                                order);
+  ++c->launches;
   NbArgs A{};
   A.sph = sph;
   A.N = N;
   A.grid = g;
   A.start = start;
   A.items = items;
+  A.sorted = sorted;
+  A.order = order;
+  A.work = rb + 3 * (NB_RB + 1);
   double L2 = 0.0;
   for (int k = 0; k < 3; ++k) {
     A.blo[k] = box[k];
@@ -742,7 +858,10 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   A.err = c->errw.as<int>();
   A.dbg = (long long*)c->nb_dbg;
   c->nb_args_tol0 = A.tol0;
-  const int mb = (int)std::min<int64_t>((N + NB_WARPS - 1) / NB_WARPS, 16 * (int64_t)c->sms);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nb_pass1, 32 * NB_WARPS, 0) || occ < 1)
+    occ = 4;
+  const int mb = (int)std::min<int64_t>((N + NB_WARPS - 1) / NB_WARPS, (int64_t)occ * c->sms);
   k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
   if ((e = cudaGetLastError())) return e;
@@ -758,6 +877,7 @@ cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, con
   A.grid = reinterpret_cast<const NbGrid*>(c->nb_grid);
   A.start = c->nb_start;
   A.items = c->nb_items;
+  A.sorted = reinterpret_cast<const double4*>(c->nb_sorted);
   for (int k = 0; k < 3; ++k) {
     A.blo[k] = box[k];
     A.bhi[k] = box[3 + k];
