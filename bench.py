@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--partial-iters", type=int, default=-1,
                     help="partial updates per step (-1: all batches of the config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nbr", action="store_true",
+                    help="skip the NEXT-3 side record (sphere neighbour lists on the GPU)")
     ap.add_argument("--no-small", action="store_true",
                     help="skip the M = 1 / M = 10 partial-update latency side measurement")
     ap.add_argument("--no-euler", action="store_true",
@@ -446,6 +448,45 @@ def main():
                          "cc_ms = CC numbers of all RPCs / RPFs (PAPER.md:461-466, union-find); "
                          "medial_mesh_ms = dual medial mesh extraction (host-timed, two syncs)"}
 
+    # ---- NEXT-3 side measurement: the sphere neighbour lists on the GPU, the
+    # step before the RPD (an input in the timed step); then the full RPD with those lists
+    nbr = None
+    if not args.no_nbr:
+        box = W.mesh_box(w.verts)
+        nb_ms = []
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g = ctx.neighbors(d_base[0], box, device=True)
+            torch.cuda.synchronize()
+            if s >= args.warmup:
+                nb_ms.append(1e3 * (time.perf_counter() - t0))
+
+        def full_rpd(off, idx):
+            ms = []
+            for s in range(2):
+                flush.zero_()
+                torch.cuda.synchronize()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                ctx.relations(d_verts, d_tets, d_base[0], off, idx)
+                c = ctx.clip()
+                ev1.record()
+                torch.cuda.synchronize()
+                ms.append(ev0.elapsed_time(ev1))
+            return ms[-1], c.n_pieces, c.n_inc
+
+        t_gpu, np_gpu, ni_gpu = full_rpd(g["nbr_off"], g["nbr_idx"])
+        t_rt, np_rt, ni_rt = full_rpd(d_base[1], d_base[2])
+        nbr = {"ms": float(np.median(nb_ms)), "E": int(g["nbr_idx"].numel()),
+               "E_regular_triangulation": int(len(w.nbr_idx)),
+               "hidden": int(g["n_hidden"]), "vertex_overflow": int(g["n_vertex_overflow"]),
+               "full_rpd_ms_gpu_lists": float(t_gpu), "full_rpd_ms_rt_lists": float(t_rt),
+               "pieces_equal_counts": bool(np_gpu == np_rt and ni_gpu == ni_rt),
+               "note": "NEXT-3 rpd_neighbors (host-timed around the call, two syncs): certified "
+                       "superset of the mesh-box power-cell neighbours; full RPD = relations + "
+                       "clip (CUDA events, L2 flushed) with the GPU lists vs the Qhull lists"}
+
     # ---- the paper's regime of few insertions per iteration ("also report
     # M = 1 and M = 10 per-iteration latency"; "few (even single) spheres"): the
     # same C3 start, batches of M = 1 and M = 10 spheres, per-update device time
@@ -532,6 +573,7 @@ def main():
                         "host inputs and a pinned host download of the final pieces"},
         "euler": euler,
         "partial_small_m": small,
+        "neighbors": nbr,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches // max(args.steps, 1)),
     }
