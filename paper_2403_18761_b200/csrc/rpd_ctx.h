@@ -189,7 +189,7 @@ struct rpd_ctx {
   rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
   rpd::DevBuf cc_par, cc_out;  // CC numbers: union-find parents, outputs
   // sphere neighbours (NEXT-3): scratch (grid, pass-1 rows), outputs (off, idx), pass-2 rows
-  rpd::DevBuf nb_buf, nb_off, nb_idx, nb_tmp, nb_cnt, h_nb;
+  rpd::DevBuf nb_buf, nb_off, nb_idx, nb_tmp, nb_cnt, h_nb, nb_hits;
   void* nb_grid = nullptr;
   unsigned long long* nb_stats = nullptr;
   int32_t *nb_start = nullptr, *nb_items = nullptr, *nb_long = nullptr, *nb_long_ids = nullptr,

@@ -44,6 +44,7 @@ constexpr int NB_WARPS = 4;               // warps per block of the main kernel
 constexpr int NB_GMAX = 160;              // grid cells per axis (max)
 constexpr int NB_RB = 256;                // radius buckets of the work order
 constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
+constexpr int NB_HCAP = 4096;             // hit list of a round (per warp slot, global memory)
 
 struct NbGrid {
   double lo[3], h[3];
@@ -241,11 +242,12 @@ struct NbArgs {
   const int32_t* order;   // work order (pass 1)
   int32_t* work;          // work counter (pass 1)
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
+  int32_t* hits;   // [warp slots][NB_HCAP] positions (cell-sorted arrays) of a round's hits
 };
 
 // One warp computes sphere i's row.  PASS2: writes the row into tmp at off[i] (rows > CAP1).
 template <bool PASS2>
-__device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
+__device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __restrict__ hb) {
   const NbGrid& g = *A.grid;
   const double4 si = make_double4(A.sph[4 * i], A.sph[4 * i + 1], A.sph[4 * i + 2], A.sph[4 * i + 3]);
   const int G = g.G;
@@ -260,7 +262,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
   top.init();
   int n_seen = 0;
   const long long t_start = clock64();
-  long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0;
+  long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0, dbg_enum = 0;
   int dbg_rounds = 0;
   // ---- 1. ring collection of candidates for K (and the hiding test)
   for (int r = 0;; ++r) {
@@ -378,9 +380,11 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
   bool converged = false;
   bool list_exact = true;  // S.vx holds the vertices of P_K (not the box fallback)
   int first_new = 0;
+  int n_list = -1;  // hits of the previous round in hb (-1: none, scan the grid)
   for (int round = 0;; ++round) {
     const bool final_round = converged || round == NB_ROUNDS - 1;
     if (!converged) {
+    const long long t_enum = clock64();
     const int M = 6 + nK;
     // ---- 3. vertices of P_K.  Round 0: every plane triple a < b < c.  Later rounds (P_K =
     // P_old ∩ new planes, planes [first_new, M) new): the old vertices that satisfy the new
@@ -451,6 +455,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       }
     }
     __syncwarp();
+    dbg_enum += clock64() - t_enum;
     n_v = S.n_v;
     if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
       if (!PASS2 && lane == 0) A.cnt[i] = 0;
@@ -551,7 +556,81 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       top.init();
     }
     // ---- 5. every sphere of the ball whose plane reaches a vertex of P_K: collected with its
-    // depth (selection of the next round) or, in the final round, listed
+    // depth (selection of the next round) or, in the final round, listed.  The hits of a round
+    // (some vertex within slack) are kept in hb: P_K only shrinks, so a plane that reaches a
+    // later P_K (or cuts it) reached this one, and the next round scans the list, not the grid
+    // (sound for any list that holds every hit; a full list falls back to the grid)
+    // visit position p: bit 0 = hit, bit 1 = deep cut (not in the final round)
+    auto visit = [&](int p, double& key, int& jo) -> int {
+      const int j = A.items[p];
+      jo = j;
+      dbg_cells += 1;
+      if (j == i) return 0;
+      const double4 sj = A.sorted[p];
+      const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z, rj = sj.w;
+      const double u2 = ux * ux + uy * uy + uz * uz;
+      if (u2 == 0.0 || u2 > R * R) return 0;
+      {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack)
+        const double Rj = (rho_v + sqrt(fmax(pdm_v, 0.0) + rj * rj)) * (1.0 + 1e-9) +
+                          4.0 * (evm_v + A.tol0) + 1e-9 * L;
+        if (u2 > Rj * Rj) return 0;
+      }
+      const double un = sqrt(u2);
+      const double ax = -ux / un, ay = -uy / un, az = -uz / un;
+      const double bw = (u2 - rj * rj + si.w * si.w) / (2.0 * un);
+      const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(bw);
+      ++dbg_scan;
+      const double hcen = ax * cx + ay * cy + az * cz + bw;  // plane value at the centre
+      // lower bounds of the plane's minimum over P_K: the centroid ball and the vertex box
+      const double lb = fmax(hcen - rs, ax * bc[0] + ay * bc[1] + az * bc[2] + bw -
+                                            (fabs(ax) * be[0] + fabs(ay) * be[1] + fabs(az) * be[2]));
+      if (lb > slack) return 0;
+      // final round: a hit once some vertex is within slack; earlier rounds: a deep cut once
+      // some vertex is cut by more than tolF (ranked by the value at the centre)
+      const double thr = final_round ? slack : -tolF;
+      double depth = 1e300;
+      for (int s2 = 0; s2 < n_v; ++s2) {
+        const double4 v = S.vx[s2];
+        depth = fmin(depth, ax * v.x + ay * v.y + az * v.z + bw - v.w);
+        ++dbg_vloop;
+        if (final_round ? depth <= thr : depth < thr) break;
+      }
+      key = hcen;
+      return (depth <= slack ? 1 : 0) | (!final_round && depth < -tolF ? 2 : 0);
+    };
+    auto take = [&](int code, double key, int j) {
+      if (final_round) {
+        if (code & 1) {
+          const int s2 = atomicAdd(&S.n_o, 1);
+          if (PASS2) {
+            A.tmp[base + s2] = j;
+          } else if (s2 < NB_CAP1) {
+            S.out[s2] = j;
+          }
+        }
+      } else if (code & 2) {
+        top.push(key, j);
+      }
+    };
+    int n_hit = 0;  // hits recorded this round (> NB_HCAP: overflow)
+    if (n_list >= 0) {  // ---- scan the previous round's hits, compacted in place
+      ++dbg_rounds;
+      for (int t0 = 0; t0 < n_list; t0 += 32) {
+        const int t = t0 + lane;
+        int code = 0, j = -1, p = 0;
+        double key = 0.0;
+        if (t < n_list) {
+          p = hb[t];
+          code = visit(p, key, j);
+          take(code, key, j);
+        }
+        if (!final_round) {
+          const unsigned m = __ballot_sync(0xffffffffu, code & 1);
+          if (code & 1) hb[n_hit + __popc(m & ((1u << lane) - 1u))] = p;  // index <= t
+          n_hit += __popc(m);
+        }
+      }
+    } else {
     int lo[3], hi[3];
     {
       const double c[3] = {si.x, si.y, si.z};
@@ -561,6 +640,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       }
     }
     const int nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+    (void)nx;
     ++dbg_rounds;
     // rows of cells (fixed y, z) are contiguous in the cell-sorted arrays: lane = row for the
     // ranges, then the warp walks the concatenated ranges (coalesced id / sphere loads)
@@ -602,53 +682,23 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
           if (e <= t) k += step;
         }
         const int pbk = __shfl_sync(0xffffffffu, pb, k), exk = __shfl_sync(0xffffffffu, excl, k);
-        if (t >= total) continue;
-        const int p = pbk + (t - exk);
-        const int j = A.items[p];
-        const double4 sj = A.sorted[p];
-        dbg_cells += 1;
-        if (j == i) continue;
-        const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z, rj = sj.w;
-        const double u2 = ux * ux + uy * uy + uz * uz;
-        if (u2 == 0.0 || u2 > R * R) continue;
-        {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack)
-          const double Rj = (rho_v + sqrt(fmax(pdm_v, 0.0) + rj * rj)) * (1.0 + 1e-9) +
-                            4.0 * (evm_v + A.tol0) + 1e-9 * L;
-          if (u2 > Rj * Rj) continue;
+        int code = 0, j = -1, p = 0;
+        double key = 0.0;
+        if (t < total) {
+          p = pbk + (t - exk);
+          code = visit(p, key, j);
+          take(code, key, j);
         }
-        const double un = sqrt(u2);
-        const double ax = -ux / un, ay = -uy / un, az = -uz / un;
-        const double bw = (u2 - rj * rj + si.w * si.w) / (2.0 * un);
-        const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(bw);
-        ++dbg_scan;
-        const double hcen = ax * cx + ay * cy + az * cz + bw;  // plane value at the centre
-        // lower bounds of the plane's minimum over P_K: the centroid ball and the vertex box
-        const double lb = fmax(hcen - rs, ax * bc[0] + ay * bc[1] + az * bc[2] + bw -
-                                              (fabs(ax) * be[0] + fabs(ay) * be[1] + fabs(az) * be[2]));
-        if (final_round ? lb > slack : lb >= -tolF) continue;
-        // final round: a hit once some vertex is within slack; earlier rounds: a deep cut once
-        // some vertex is cut by more than tolF (ranked by the value at the centre)
-        const double thr = final_round ? slack : -tolF;
-        double depth = 1e300;
-        for (int s2 = 0; s2 < n_v; ++s2) {
-          const double4 v = S.vx[s2];
-          depth = fmin(depth, ax * v.x + ay * v.y + az * v.z + bw - v.w);
-          ++dbg_vloop;
-          if (final_round ? depth <= thr : depth < thr) break;
-        }
-        if (final_round ? depth > thr : depth >= thr) continue;
-        if (final_round) {
-          const int s2 = atomicAdd(&S.n_o, 1);
-          if (PASS2) {
-            A.tmp[base + s2] = j;
-          } else if (s2 < NB_CAP1) {
-            S.out[s2] = j;
-          }
-        } else {
-          top.push(hcen, j);
+        if (!final_round) {
+          const unsigned m = __ballot_sync(0xffffffffu, code & 1);
+          const int at = n_hit + __popc(m & ((1u << lane) - 1u));
+          if ((code & 1) && at < NB_HCAP) hb[at] = p;
+          n_hit += __popc(m);
         }
       }
     }
+    }
+    n_list = n_hit <= NB_HCAP ? n_hit : -1;
     __syncwarp();
     if (final_round) break;
     int n_deep = 0;
@@ -701,7 +751,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane) {
       long long* d = A.dbg + 8 * (long long)i;
       d[0] = clock64() - t_start;
       d[1] = dbg_rounds;
-      d[2] = dbg_cells;
+      d[2] = dbg_enum;  // cycles in the vertex enumeration (lane 0)
       d[3] = dbg_scan;
       d[4] = dbg_vloop;
       d[5] = n_v;
@@ -733,7 +783,8 @@ __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
     if (lane == 0) q = atomicAdd(A.work, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
     if (q >= A.N) break;
-    nb_row<false>(A, sm[w], A.order[q], lane);
+    nb_row<false>(A, sm[w], A.order[q], lane,
+                  A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
   }
 }
 
@@ -742,7 +793,8 @@ __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass2(NbArgs A) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = *A.n_long;
   for (int q = blockIdx.x * NB_WARPS + w; q < n; q += gridDim.x * NB_WARPS)
-    nb_row<true>(A, sm[w], A.long_ids[q], lane);
+    nb_row<true>(A, sm[w], A.long_ids[q], lane,
+                 A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
 }
 
 // rows into ascending order: rank of each entry among its row (entries are distinct)
@@ -862,6 +914,10 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nb_pass1, 32 * NB_WARPS, 0) || occ < 1)
     occ = 4;
   const int mb = (int)std::min<int64_t>((N + NB_WARPS - 1) / NB_WARPS, (int64_t)occ * c->sms);
+  // hit lists: one per warp slot of pass 1 or pass 2 (2 * sms blocks)
+  const size_t slots = (size_t)std::max(mb, 2 * c->sms) * NB_WARPS;
+  if ((e = c->nb_hits.ensure(sizeof(int32_t) * NB_HCAP * slots))) return e;
+  A.hits = c->nb_hits.as<int32_t>();
   k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
   if ((e = cudaGetLastError())) return e;
@@ -890,6 +946,7 @@ cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, con
   A.n_long = c->nb_long;
   A.long_ids = c->nb_long_ids;
   A.stats = c->nb_stats;
+  A.hits = c->nb_hits.as<int32_t>();
   k_nb_pass2<<<2 * c->sms, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
   const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
