@@ -200,6 +200,9 @@ __global__ void k_nb_gather(int64_t N, const int32_t* __restrict__ items,
 
 // work order: spheres by descending radius (the big spheres have the big cells and the long
 // scans), taken from a counter, so that the longest rows start first
+// work order: descending radius (the big spheres have the big cells and the long scans; the
+// near-zero ones are heavy too, but moving them first or going ascending measured no better:
+// DESIGN.md "Sphere neighbours")
 __device__ __forceinline__ int nb_rbucket(double r, double rmax) {
   const int b = rmax > 0 ? (int)((1.0 - r / rmax) * NB_RB) : 0;
   return b < 0 ? 0 : (b >= NB_RB ? NB_RB - 1 : b);
@@ -262,6 +265,8 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
   top.init();
   int n_seen = 0;
   const long long t_start = clock64();
+  unsigned long long g_start = 0;
+  if (A.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0, dbg_enum = 0;
   int dbg_rounds = 0;
   // ---- 1. ring collection of candidates for K (and the hiding test)
@@ -756,7 +761,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
       d[4] = dbg_vloop;
       d[5] = n_v;
       d[6] = n_o;
-      d[7] = R * 1000;
+      d[7] = (long long)g_start;  // start (ns, global timer)
     }
   }
   if (!PASS2) {

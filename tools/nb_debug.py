@@ -13,7 +13,7 @@ w = W.make_config(sys.argv[1] if len(sys.argv) > 1 else "C3")
 ctx = P.RPDContext(0)
 g = ctx.neighbors(w.spheres, W.mesh_box(w.verts))
 d = np.fromfile("gpurun_out/nb_dbg.bin", dtype=np.int64).reshape(-1, 8)
-names = ["clk", "rounds", "enum_clk", "scan", "vloop", "n_v", "n_o", "R_milli"]
+names = ["clk", "rounds", "enum_clk", "scan", "vloop", "n_v", "n_o", "start_ns"]
 print("total clk", d[:, 0].sum(), "max", d[:, 0].max(), "enum share", d[:, 2].sum() / d[:, 0].sum())
 for k, n in enumerate(names):
     print(f"{n:8s} mean {d[:, k].mean():12.1f} p50 {np.median(d[:, k]):10.0f} p99 {np.percentile(d[:, k], 99):10.0f} max {d[:, k].max():10d}")
@@ -25,3 +25,18 @@ for i in o:
 for r in range(1, 6):
     m = d[:, 1] == r
     print("rounds", r, "spheres", m.sum(), "clk share", d[m, 0].sum() / d[:, 0].sum())
+# tail: start / end (ns from the first start) against the radius order
+ok = d[:, 7] > 0  # rows written (hidden / empty spheres return early)
+t0 = d[ok, 7].min()
+d = d.copy()
+d[~ok, 7] = t0
+st = (d[:, 7] - t0) / 1e6
+en = st + d[:, 0] / 1.965e6
+print(f"kernel span ~{en.max():.2f} ms; last start {st.max():.2f} ms")
+for q in (0.5, 0.9, 0.99):
+    print(f"end time p{int(q*100)} {np.quantile(en, q):.2f} ms")
+late = np.argsort(-en)[:10]
+print("latest finishers: id r start_ms dur_ms")
+for i in late:
+    print(i, round(float(w.spheres[i][3]), 3), round(st[i], 2), round(d[i, 0] / 1.965e6, 2))
+print("r quantiles", np.quantile(w.spheres[:, 3], [0.1, 0.5, 0.9, 1.0]))
