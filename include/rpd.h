@@ -60,7 +60,8 @@ typedef enum {
 } rpd_status;
 
 /* Create a context on CUDA `device`.  `cuda_stream` is a cudaStream_t to order all work on
- * (NULL: the ctx creates its own non-blocking stream). */
+ * (NULL: the ctx creates its own non-blocking stream, NOT ordered with other streams; pass
+ * cudaStreamLegacy to run on the legacy default stream). */
 rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream);
 void rpd_destroy(rpd_ctx* ctx);
 /* Human-readable description of the last failure on ctx (host string owned by ctx, valid
@@ -315,7 +316,8 @@ rpd_status rpd_envelope(rpd_ctx* ctx, const double* samples, int64_t S, const do
 
 /* ---- Sphere neighbours on the GPU
  *
- * "we compute the neighbors of each site ... using a Regular Triangulation";
+ * "we use the Regular Triangulation in CGAL to compute all possible neighbors (k_site) of a
+ * given sphere";
  * the neighbour lists are the k_site input of rpd_relations.  This call computes a certified
  * SUPERSET of the neighbours whose radical plane holds a positive-area facet of the power cell
  * restricted to the axis box `box` (DESIGN.md §10 "Sphere neighbours"): the RPD of any tets

@@ -304,7 +304,54 @@ def from_per_tet_lists(L):
             "inc_sphere": np.array(inc, np.int32)}
 
 
+def _segments(off, sel):
+    """Element indices of the CSR segments ``sel`` (in that order) of offsets ``off``."""
+    off = np.asarray(off, np.int64)
+    sel = np.asarray(sel, np.int64)
+    lens = off[sel + 1] - off[sel]
+    if lens.sum() == 0:
+        return np.zeros(0, np.int64)
+    first = np.repeat(off[sel] - np.concatenate(([0], np.cumsum(lens)[:-1])), lens)
+    return first + np.arange(lens.sum())
+
+
+def _csr_of(lens):
+    return np.concatenate(([0], np.cumsum(lens))).astype(np.int32)
+
+
 def merge_per_tet(old, new, dirty, T):
+    """Tet t's candidates and pieces from ``new`` (row a) when t = dirty[a], else from
+    ``old`` (row t) -- the R11 merge.  Plain CSR row selection; Euler results go through
+    the per-tet lists."""
+    if "rpf_off" not in old:
+        dirty = np.asarray(dirty, np.int64)
+        src_new = np.zeros(T, bool)
+        src_new[dirty] = True
+        row = np.arange(T, dtype=np.int64)
+        row[dirty] = T + np.arange(len(dirty))       # rows T.. are new's rows
+        nn = new if new is not None else {k: old[k][:0] for k in old if k != "stats"}
+        if new is None:
+            nn["cand_off"] = nn["piece_off"] = np.zeros(1, np.int32)
+            nn["inc_off"] = np.zeros(1, np.int32)
+
+        def cat_off(a, b):  # offsets of the concatenated segment lists a then b
+            a, b = np.asarray(a, np.int64), np.asarray(b, np.int64)
+            return np.concatenate((a, a[-1] + b[1:]))
+        c_off = cat_off(old["cand_off"], nn["cand_off"])
+        c_idx = np.concatenate((old["cand_idx"], nn["cand_idx"]))
+        p_off = cat_off(old["piece_off"], nn["piece_off"])
+        i_off = cat_off(old["inc_off"], nn["inc_off"])
+        cs = _segments(c_off, row)
+        ps = _segments(p_off, row)
+        out = {"cand_off": _csr_of(c_off[row + 1] - c_off[row]),
+               "cand_idx": c_idx[cs].astype(np.int32),
+               "piece_off": _csr_of(p_off[row + 1] - p_off[row])}
+        for k in ("piece_sphere", "piece_vol", "piece_m1", "piece_facemask"):
+            out[k] = np.concatenate((old[k], nn[k]))[ps]
+        out["inc_off"] = _csr_of(i_off[ps + 1] - i_off[ps])
+        out["inc_sphere"] = np.concatenate((old["inc_sphere"], nn["inc_sphere"]))[
+            _segments(i_off, ps)].astype(np.int32)
+        return out
     L = per_tet_lists(old, T)
     if new is not None:
         Ln = per_tet_lists(new, len(dirty))

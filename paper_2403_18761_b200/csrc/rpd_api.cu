@@ -78,6 +78,8 @@ const char* err_kind_str(int k) {
     case ERR_NBR_DUP: return "duplicate neighbour";
     case ERR_NBR_SAME_CENTRE: return "neighbour with the same centre (radical plane undefined)";
     case ERR_NBR_OFF: return "bad neighbour CSR offsets";
+    case ERR_SPHERE_CHANGED:
+      return "partial update: an existing sphere [0, N_old) changed (only appending is allowed)";
     default: return "invalid input";
   }
 }
@@ -162,7 +164,7 @@ void rpd_destroy(rpd_ctx* c) {
   DevBuf* bufs[] = {&c->h_verts, &c->h_tets, &c->h_spheres, &c->h_off, &c->h_idx, &c->h_new,
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
                     &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
-                    &c->st.old_twin, &c->st.old_hkey, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
+                    &c->st.old_twin, &c->st.old_hkey, &c->st.old_sw, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
@@ -599,11 +601,34 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   return fill_pieces(c, out);
 }
 
+static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t N_new,
+                                      const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                      const int32_t* new_ids, int64_t M, rpd_pieces* out,
+                                      const int32_t** dirty_tets, int64_t* n_dirty,
+                                      bool* mutated);
+
 rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
                               const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                               const int32_t* new_ids, int64_t M, rpd_pieces* out,
                               const int32_t** dirty_tets, int64_t* n_dirty) {
   if (!c) return RPD_EINVAL;
+  bool mutated = false;
+  rpd_status s = update_partial_impl(c, spheres, N_new, nbr_off, nbr_idx, E, new_ids, M, out,
+                                     dirty_tets, n_dirty, &mutated);
+  if (s != RPD_OK && mutated) {
+    // the staged rows / epochs already describe the new sphere set while the candidates and
+    // pieces do not: the ctx state is inconsistent, so a full rpd_relations is required
+    c->have_rel = c->have_pieces = c->eu_valid = false;
+    c->err += " (ctx state reset: call rpd_relations + rpd_clip again)";
+  }
+  return s;
+}
+
+static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t N_new,
+                                      const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                      const int32_t* new_ids, int64_t M, rpd_pieces* out,
+                                      const int32_t** dirty_tets, int64_t* n_dirty,
+                                      bool* mutated) {
   if (!out || !dirty_tets || !n_dirty || M < 0 || (M > 0 && !new_ids))
     return fail(c, RPD_EINVAL, "rpd_update_partial: bad argument");
   if (!c->have_pieces) return fail(c, RPD_ESTATE, "rpd_update_partial before rpd_clip");
@@ -632,6 +657,7 @@ rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
+  *mutated = true;
   ++c->epoch;
   rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, E, true, c->epoch);
   if (s) return s;

@@ -25,6 +25,8 @@
 // Outputs per pair: non-empty flag, volume, first moment (facet fans, deterministic warp
 // reduction), tet-face mask and incidences as a bitmask over the positions of N(i)
 // (positive-area SoS facets expanded by exactly coincident sources, R7).
+#include <mutex>
+
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -1258,16 +1260,23 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
-  // kernel attributes and occupancy are set / queried once per instantiation (host API calls
-  // cost microseconds per launch)
-  static int occ = 0;
-  if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL, EU>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e) return e;
-    int o = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_clip<GW, VPL, EU>, THREADS, smem);
-    occ = o < 1 ? 1 : o;
+  // kernel attributes are per device: set / queried once per (instantiation, device) (host API
+  // calls cost microseconds per launch); the table is guarded for ctxs on several threads
+  static int occ_dev[RPD_MAX_DEVICES] = {};
+  static std::mutex mu;
+  if (c->device < 0 || c->device >= RPD_MAX_DEVICES) return cudaErrorInvalidDevice;
+  int occ;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    occ = occ_dev[c->device];
+    if (occ == 0) {
+      cudaError_t e = cudaFuncSetAttribute(k_clip<GW, VPL, EU>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+      int o = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_clip<GW, VPL, EU>, THREADS, smem);
+      occ = occ_dev[c->device] = o < 1 ? 1 : o;
+    }
   }
   const int sms = c->sms;
   int64_t want = (n + GROUPS - 1) / GROUPS;

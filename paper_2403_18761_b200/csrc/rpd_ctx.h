@@ -7,6 +7,8 @@
 
 #include "../../include/rpd.h"
 
+#define RPD_MAX_DEVICES 64
+
 namespace rpd {
 
 // Growable ctx-owned device buffer.
@@ -47,7 +49,8 @@ enum ErrKind {
   ERR_NBR_SELF = 9,
   ERR_NBR_DUP = 10,
   ERR_NBR_SAME_CENTRE = 11,
-  ERR_NBR_OFF = 12
+  ERR_NBR_OFF = 12,
+  ERR_SPHERE_CHANGED = 13
 };
 
 // device statistics (uint64 counters)
@@ -81,7 +84,7 @@ struct Stage {
   DevBuf repoch;   // int32 per sphere: epoch (update index) at which its row was last built
   DevBuf htab;     // uint64 scratch: per-row hash tables of the twin search
   // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
-  DevBuf old_off, old_idx, old_planes, old_twin, old_hkey, old_repoch;
+  DevBuf old_off, old_idx, old_planes, old_twin, old_hkey, old_repoch, old_sw;
   int64_t T = 0, N = 0, V = 0, E = 0;
 };
 

@@ -21,6 +21,8 @@
 //    T x N.
 // Positive pairs go to a per-tet slab slab[a * cap + c]; the compaction sorts each tet's list
 // (ascending sphere id, R9) and writes the CSR.
+#include <mutex>
+
 #include "rpd_ctx.h"
 #include "rpd_internal.cuh"
 
@@ -727,12 +729,19 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       k_bvh_super<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
           leaf, n_leaf, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), sitems,
           n_sitems, (int)cap_sup, items, (int)cap_items, n_items);
-      static bool attr_set = false;
+      // the smem attribute is per device (set once per device, guarded across threads)
+      static bool attr_set[RPD_MAX_DEVICES] = {};
+      static std::mutex mu;
       const int lsmem = (int)(sizeof(double4) * BVH_LCAP * BVH_WARPS);
-      if (!attr_set) {
-        e = cudaFuncSetAttribute(k_bvh_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem);
-        if (e) return e;
-        attr_set = true;
+      if (c->device < 0 || c->device >= RPD_MAX_DEVICES) return cudaErrorInvalidDevice;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (!attr_set[c->device]) {
+          e = cudaFuncSetAttribute(k_bvh_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   lsmem);
+          if (e) return e;
+          attr_set[c->device] = true;
+        }
       }
       k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, lsmem, c->stream>>>(
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,

@@ -1,7 +1,7 @@
 // rpd_neighbors.cu -- SURVEY.md §8(f) NEXT-3: the sphere neighbour lists (k_site) on the GPU,
-// the step right before the RPD ("we compute the neighbors of each site ...
-// using a Regular Triangulation ... Euclidean security radius ... is not enough for power
-// diagrams").  Instead of a regular triangulation we compute a *certified superset* of the
+// the step right before the RPD (the 'Security Radius' criterion "is not
+// sufficient anymore", so "we use the Regular Triangulation in CGAL to compute all possible
+// neighbors (k_site) of a given sphere").  Instead of a regular triangulation we compute a *certified superset* of the
 // neighbours whose power cell facets meet the domain box B (DESIGN.md §10 "Sphere
 // neighbours"): every sphere j whose radical plane holds a positive-area facet of C_i ∩ B is
 // listed.  The RPD restricted to tets inside B is unchanged by redundant planes (SURVEY §8(c)

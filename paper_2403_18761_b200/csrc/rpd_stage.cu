@@ -73,8 +73,11 @@ __global__ void k_stage_tets(const double* __restrict__ verts, int64_t V,
   if (!(det > 0.0)) report(err, RPD_EINVAL, ERR_TET_ORIENT, t);
 }
 
+// old_sw (partial updates): the previous staging of spheres [0, N_old), which must not change
+// (rpd.h: new spheres are appended; their rows and planes are reused)
 __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
-                                double4* __restrict__ sw, int* err) {
+                                double4* __restrict__ sw, const double4* __restrict__ old_sw,
+                                int64_t N_old, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
   double S[4];
@@ -94,7 +97,15 @@ __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
     }
   }
   double W = S[0] * S[0] + S[1] * S[1] + S[2] * S[2] - S[3] * S[3];
-  sw[i] = make_double4(S[0], S[1], S[2], W);
+  const double4 v = make_double4(S[0], S[1], S[2], W);
+  if (old_sw && i < N_old) {
+    const double4 o = old_sw[i];
+    if (o.x != v.x || o.y != v.y || o.z != v.z || o.w != v.w) {
+      report(err, RPD_EINVAL, ERR_SPHERE_CHANGED, i);
+      return;
+    }
+  }
+  sw[i] = v;
 }
 
 struct OldRows {  // previous staged CSR (partial updates: unchanged rows are copied)
@@ -333,6 +344,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   std::swap(s.twin, s.old_twin);
   std::swap(s.hkey, s.old_hkey);
   std::swap(s.repoch, s.old_repoch);
+  std::swap(s.sw, s.old_sw);
   const int64_t N_old = s.N;
   if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
   if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
@@ -351,7 +363,8 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   s.E = E;
   int* err = c->errw.as<int>();
   if (N > 0) {
-    k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(spheres, N, s.sw.as<double4>(), err);
+    k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(
+        spheres, N, s.sw.as<double4>(), old.off ? s.old_sw.as<double4>() : nullptr, N_old, err);
     ++c->launches;
     k_stage_rows<STAGE_RG><<<nblk(STAGE_RG * N, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),

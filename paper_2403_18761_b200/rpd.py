@@ -21,6 +21,7 @@ STATUS_NAMES = {0: "RPD_OK", -1: "RPD_EINVAL", -2: "RPD_ENOMEM", -3: "RPD_ECUDA"
                 -4: "RPD_EOVERFLOW", -5: "RPD_ESTATE", -6: "RPD_ENOTEXACT"}
 OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM, OPT_CLIP_WIDE, OPT_PROFILE = 1, 2, 3, 4, 5
 FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rpd_relations",
             "rpd_clip", "rpd_update_partial", "rpd_download_pieces", "rpd_download_cands",
@@ -175,7 +176,12 @@ class RPDContext:
             stream = torch.cuda.current_stream(device)
         self._stream = stream
         h = C.c_void_p()
-        st = self.L.rpd_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
+        # torch's default stream has handle 0, which rpd_create would read as "make a private
+        # non-blocking stream" -- unordered with torch / NCCL work.  Bind the ctx to the legacy
+        # default stream (cudaStreamLegacy) instead, so every call is ordered after the work
+        # torch queued before it (dtype conversions in _ptr, NCCL all-gathers, ...).
+        handle = stream.cuda_stream or CUDA_STREAM_LEGACY
+        st = self.L.rpd_create(C.byref(h), device, C.c_void_p(handle))
         if st != 0:
             raise RPDError(st, "rpd_create failed")
         self.h = h
@@ -263,6 +269,21 @@ class RPDContext:
         return self.counts, nd.value
 
     # ------------------------------------------------------------------ outputs
+    def dirty_tets(self):
+        """The dirty tets of the last update_partial (ascending) as a torch CUDA int32 tensor
+        (a copy of the ctx-owned device array)."""
+        import torch
+
+        class _View:  # __cuda_array_interface__ over the ctx-owned device array
+            def __init__(s, ptr, n):
+                s.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
+                                              "data": (ptr or 0, False), "version": 3,
+                                              "stream": None}
+        n = int(getattr(self, "n_dirty", 0))
+        if n == 0:
+            return torch.zeros(0, dtype=torch.int32, device="cuda")
+        return torch.as_tensor(_View(self._dirty_ptr, n), device="cuda").clone()
+
     def download_cands(self, device=False):
         """Candidate CSR as numpy (host) or torch CUDA tensors (device=True)."""
         T, n = self.T, self.n_cand

@@ -25,3 +25,28 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+# ---- full-size oracle results shared by the -m gpu parity tests (computed once per session)
+
+@pytest.fixture(scope="session")
+def c4_workload():
+    import rpd_workloads as W
+    return W.make_config("C4")
+
+
+@pytest.fixture(scope="session")
+def oracle_c4_chain(c4_workload):
+    """The oracle's C3 full RPD and then its R11 partial update after each of the 10 C4
+    batches: a list of (result, dirty tets) -- element 0 is the full RPD (dirty None)."""
+    import numpy as np
+    import oracle
+    w = c4_workload
+    prev = oracle.rpd_workload(w)
+    chain = [(prev, None)]
+    n_old = w.N
+    for (sph, off, idx) in w.batches:
+        prev, dirty = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old)
+        chain.append((prev, dirty))
+        n_old = len(sph)
+    return chain

@@ -3,6 +3,9 @@
 Bar (DESIGN.md §Parity): candidate CSR, non-empty set, facemasks and incidences bit-exact;
 |dvol| <= 1e-9 vol(t), |dm1| <= 1e-9 vol(t) diam(t) (north star tolerance, R10).
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -87,6 +90,24 @@ def test_host_inputs_equal_device_inputs(ctx):
             assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
 
 
+def test_torch_inputs_other_dtypes_are_stream_ordered(ctx):
+    """Inputs made by torch kernels just before the call (float32 -> float64 and int64 ->
+    int32 conversions inside the binding, all on torch's default stream) are read by the
+    library in stream order (the ctx runs on the legacy default stream)."""
+    import torch
+    w = W.make_shape_workload("Hd", 3000, 250, seed=21, cache=False)
+    for _ in range(3):
+        args = [torch.as_tensor(w.verts).cuda().float(), torch.as_tensor(w.tets).cuda().long(),
+                torch.as_tensor(w.spheres).cuda().float(),
+                torch.as_tensor(w.nbr_off).cuda().long(), torch.as_tensor(w.nbr_idx).cuda().long()]
+        ctx.relations(*args)
+        ctx.clip()
+        got = ctx.download_cands()
+        got.update(ctx.download_pieces())
+        errs = compare_results(got, oracle.rpd_workload(w), w.verts, w.tets, rel=REL)
+        assert not errs, errs[:5]
+
+
 def test_single_sphere(ctx):
     w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
     got, _ = check(ctx, w)
@@ -153,22 +174,41 @@ def test_input_errors(ctx):
     assert e.value.status == -5
 
 
-def test_bench_config_sampled(ctx):
+@pytest.mark.parametrize("mode", ["all_pairs", "pruned"])
+def test_bench_config_every_tet(ctx, ctx_pruned, c4_workload, oracle_c4_chain, mode):
     """At BASELINE.json's full size (C3: ~200k tets, 20k spheres), in the launch configuration
-    bench.py times: sampled tets compared one by one with the oracle, partition on all."""
-    w = W.make_config("C3")
-    got = run_gpu(ctx, w)
-    rng = np.random.default_rng(0)
-    ids = np.sort(rng.choice(w.T, 48, replace=False)).astype(np.int32)
-    ref = oracle.rpd_workload(w, tet_ids=ids)
-    # slice the GPU result to the sampled tets
-    sub = slice_tets(got, ids)
-    errs = compare_results(sub, ref, w.verts, w.tets, tet_ids=ids, rel=REL)
+    bench.py times: EVERY tet's candidates and pieces compared with the oracle's full RPD
+    (Alg. 1 over all 20k spheres), plus the partition of every tet."""
+    w = c4_workload
+    got = run_gpu(ctx if mode == "all_pairs" else ctx_pruned, w)
+    ref = oracle_c4_chain[0][0]
+    errs = compare_results(got, ref, w.verts, w.tets, rel=REL)
     assert not errs, errs[:5]
+    assert got["stats"]["n_cand"] == len(ref["cand_idx"])
+    if mode == "all_pairs":
+        assert got["stats"]["rel_tests"] == ref["stats"]["n_rel_tests"]
     vt = tet_volumes(w.verts, w.tets)
     s = np.zeros(w.T)
     np.add.at(s, piece_tet(got), got["piece_vol"])
     assert np.max(np.abs(s - vt) / vt) < 1e-9
+
+
+ALG1 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "alg1_cases.json")))
+
+
+@pytest.mark.parametrize("case", ALG1["cases"], ids=lambda c: c["name"])
+@pytest.mark.parametrize("mode", ["all_pairs", "pruned"])
+def test_alg1_golden_cases_gpu(ctx, ctx_pruned, case, mode):
+    """The hand-derived Alg. 1 answers (strict tie, over-report, first/last neighbour
+    rejection; tests/golden/alg1_cases.json) through the C ABI, both filter modes."""
+    from tests.test_oracle_pins import alg1_case, check_alg1_golden
+    c = ctx if mode == "all_pairs" else ctx_pruned
+    args = alg1_case(case)
+    c.relations(*args)
+    c.clip()
+    r = c.download_cands()
+    r.update(c.download_pieces())
+    check_alg1_golden(case, r)
 
 
 @pytest.mark.parametrize("make", [lambda: W.make_c1(1, degenerate=True),
@@ -226,12 +266,17 @@ def test_pruned_equals_allpairs_c3(ctx, ctx_pruned):
 
 def test_c5_sampled(ctx_pruned):
     """BASELINE.json configs[4] at full size (C5: ~4M tets, 50k spheres, high radius variance,
-    k_site tails of 1000+), pruned filter as bench.py --config C5 runs it: sampled tets compared
-    one by one with the oracle (Alg. 1 over all 50k spheres), partition on every tet."""
+    k_site tails of 1000+), pruned filter as bench.py --config C5 runs it: ~8k sampled tets
+    (random + one whole Morton block) compared one by one with the oracle (Alg. 1 over all 50k
+    spheres), partition on every tet."""
     w = W.make_config("C5")
     got = run_gpu(ctx_pruned, w)
     rng = np.random.default_rng(5)
-    ids = np.sort(rng.choice(w.T, 64, replace=False)).astype(np.int32)
+    # 4096 random tets + one whole 4096-tet Morton block (a rank's shard unit, spatially
+    # contiguous: shared faces, the same spheres' cells) in the middle of the mesh
+    blk = (w.T // 2) // 4096 * 4096
+    ids = np.union1d(rng.choice(w.T, 4096, replace=False),
+                     np.arange(blk, min(blk + 4096, w.T))).astype(np.int32)
     ref = oracle.rpd_workload(w, tet_ids=ids)
     errs = compare_results(slice_tets(got, ids), ref, w.verts, w.tets, tet_ids=ids, rel=REL)
     assert not errs, errs[:5]

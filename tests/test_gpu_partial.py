@@ -68,6 +68,39 @@ def test_partial_identity_and_errors(ctx):
     assert e.value.status == -1
 
 
+def test_partial_error_leaves_ctx_usable(ctx):
+    """A failed update (a changed old sphere, or new ids that are not the appended range)
+    resets the ctx instead of leaving it half-updated: the next rpd_clip / update is a state
+    error, and a fresh rpd_relations + rpd_clip gives the oracle's result again."""
+    import paper_2403_18761_b200 as P
+    w = W.make_shape_workload("S", 2000, 150, seed=3, n_batches=1, batch_m=12, clusters=3,
+                              cache=False)
+    sph, off, idx = w.batches[0]
+    new = np.arange(w.N, len(sph), dtype=np.int32)
+    for bad_case in ("moved", "ids"):
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        s2, ids = sph.copy(), new
+        if bad_case == "moved":
+            s2[5, 3] += 1.0 / 1024  # an existing sphere's radius changes
+        else:
+            ids = new[::-1].copy()
+        with pytest.raises(P.RPDError) as e:
+            ctx.update_partial(s2, off, idx, ids)
+        assert e.value.status == -1
+        with pytest.raises(P.RPDError) as e:
+            ctx.clip()
+        assert e.value.status == -5
+        with pytest.raises(P.RPDError) as e:
+            ctx.update_partial(sph, off, idx, new)
+        assert e.value.status == -5
+    ctx.relations(w.verts, w.tets, sph, off, idx)
+    ctx.clip()
+    errs = compare_results(gpu_state(ctx), oracle.rpd(w.verts, w.tets, sph, off, idx),
+                           w.verts, w.tets, rel=1e-9)
+    assert not errs, errs[:5]
+
+
 def test_partial_before_clip_is_state_error():
     import paper_2403_18761_b200 as P
     c = P.RPDContext(0)
@@ -78,24 +111,24 @@ def test_partial_before_clip_is_state_error():
     c.close()
 
 
-def test_c4_sampled(ctx):
-    """BASELINE.json configs[3] at full size: 10 iterations x M = 500 on the 200k-tet mesh;
-    after the last one, sampled tets equal the oracle's full recompute on the final sphere set,
-    and the last batch's dirty set equals Alg. 1 against the new spheres on the sample."""
-    w = W.make_config("C4")
+def test_c4_chain_every_tet(ctx, c4_workload, oracle_c4_chain):
+    """BASELINE.json configs[3] at full size, as bench.py runs it: the C3 full RPD, then 10
+    iterations x M = 500 on the 200k-tet mesh.  After EVERY iteration, the dirty-tet list, the
+    candidate CSR and the pieces of EVERY tet equal the oracle's R11 partial-update chain
+    (oracle.partial_update from the oracle's own full RPD)."""
+    w = c4_workload
     ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
     ctx.clip()
+    errs = compare_results(gpu_state(ctx), oracle_c4_chain[0][0], w.verts, w.tets, rel=1e-9)
+    assert not errs, errs[:5]
     n_old = w.N
-    for (sph, off, idx) in w.batches:
+    for it, (sph, off, idx) in enumerate(w.batches):
         new = np.arange(n_old, len(sph), dtype=np.int32)
         counts, nd = ctx.update_partial(sph, off, idx, new)
-        assert 0 < nd < w.T
-        n_prev, n_old = n_old, len(sph)
-    got = gpu_state(ctx)
-    sph, off, idx = w.batches[-1]
-    rng = np.random.default_rng(1)
-    ids = np.sort(rng.choice(w.T, 40, replace=False)).astype(np.int32)
-    full = oracle.rpd(w.verts, w.tets, sph, off, idx, tet_ids=ids)
-    sub = slice_tets(got, ids)
-    errs = compare_results(sub, full, w.verts, w.tets, tet_ids=ids, rel=1e-9, check_cands=False)
-    assert not errs, errs[:5]
+        ref, dirty = oracle_c4_chain[it + 1]
+        assert nd == len(dirty) and 0 < nd < w.T
+        assert np.array_equal(ctx.dirty_tets().cpu().numpy(), dirty), it
+        errs = compare_results(gpu_state(ctx), ref, w.verts, w.tets, rel=1e-9,
+                               label=f"iteration {it}: ")
+        assert not errs, errs[:5]
+        n_old = len(sph)
