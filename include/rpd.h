@@ -266,17 +266,18 @@ rpd_status rpd_medial_mesh(rpd_ctx* ctx, rpd_medial* out);
  * [n_edges][2], faces [n_faces][3].  RPD_ESTATE before any rpd_medial_mesh. */
 rpd_status rpd_download_medial_mesh(rpd_ctx* ctx, int32_t* edges, int32_t* faces);
 
-/* ---- Multi-GPU gather of the pieces
+/* ---- Multi-GPU exchange
  *
- * Each rank clips its own tet shard (rpd_relations on its tets); the per-rank piece CSRs are
- * all-gathered by the caller (NCCL over NVLink) and rpd_gather_pieces puts them back into
- * global tet order, on the ctx's device.  Every array below is a DEVICE pointer (the gathered
- * buffers); rank r holds n_tets[r] tets whose global ids are tet_ids[r] (each global tet in
- * exactly one rank), with its local piece CSR piece_off[r] [n_tets[r]+1] ... inc_sphere[r].
- * Outputs (caller-allocated device arrays): piece_off [T+1], piece_sphere / piece_vol /
- * piece_facemask [sum n_pieces], piece_m1 [3 sum n_pieces], inc_off [sum n_pieces + 1],
- * inc_sphere [sum n_inc] -- byte-identical to a single-GPU rpd_clip of all T tets.
- * RPD_EINVAL: world outside [1, RPD_MAX_RANKS] or a NULL array. */
+ * Each rank computes the RPD of its own tet shard (rpd_relations on its tets); the per-rank
+ * candidate and piece CSRs are all-gathered by the caller (NCCL over NVLink) and the calls
+ * below put them back into global tet order on the ctx's device -- byte-identical to a
+ * single-GPU run of all T tets.  In partial mode only the dirty tets' segments travel
+ * (rpd_download_tets of the dirty list) and rpd_merge_shards puts them into the previous
+ * global CSR.  Every array is a DEVICE pointer (the gathered buffers): rank r holds n_tets[r]
+ * tets (rows) whose global ids are tet_ids[r] (each global tet in at most one rank), with
+ * its local CSRs piece_off[r] [n_tets[r]+1] ... inc_sphere[r] and cand_off[r] / cand_idx[r].
+ * RPD_EINVAL: world outside [1, RPD_MAX_RANKS], a NULL array that the call needs, or a tet id
+ * outside [0, T) (checked on the device before any copy). */
 #define RPD_MAX_RANKS 16
 typedef struct {
   int32_t world;
@@ -290,10 +291,50 @@ typedef struct {
   const uint8_t* piece_facemask[RPD_MAX_RANKS];
   const int32_t* inc_off[RPD_MAX_RANKS];
   const int32_t* inc_sphere[RPD_MAX_RANKS];
+  const int32_t* cand_off[RPD_MAX_RANKS];   /* candidate CSR (rpd_gather_cands, merge) */
+  const int32_t* cand_idx[RPD_MAX_RANKS];
 } rpd_shards;
+
+/* A whole candidate + piece CSR over T tets (layouts as rpd_relations / rpd_pieces). */
+typedef struct {
+  int32_t* cand_off;      /* [T+1] */
+  int32_t* cand_idx;      /* [n_cand] */
+  int32_t* piece_off;     /* [T+1] */
+  int32_t* piece_sphere;  /* [n_pieces] */
+  double* piece_vol;      /* [n_pieces] */
+  double* piece_m1;       /* [n_pieces][3] */
+  uint8_t* piece_facemask;/* [n_pieces] */
+  int32_t* inc_off;       /* [n_pieces+1] */
+  int32_t* inc_sphere;    /* [n_inc] */
+  int64_t T, n_cand, n_pieces, n_inc;
+} rpd_csr;
+
+/* Gathered pieces in global tet order.  Outputs (caller-allocated device arrays):
+ * piece_off [T+1], piece_sphere / piece_vol / piece_facemask [sum n_pieces], piece_m1
+ * [3 sum n_pieces], inc_off [sum n_pieces + 1], inc_sphere [sum n_inc]. */
 rpd_status rpd_gather_pieces(rpd_ctx* ctx, const rpd_shards* shards, int32_t* piece_off,
                              int32_t* piece_sphere, double* piece_vol, double* piece_m1,
                              uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
+/* Gathered candidate CSR in global tet order: cand_off [T+1], cand_idx [sum n_cand]
+ * (caller-allocated device arrays). */
+rpd_status rpd_gather_cands(rpd_ctx* ctx, const rpd_shards* shards, int32_t* cand_off,
+                            int32_t* cand_idx);
+/* Partial-mode merge: the global CSR `old` (device arrays, any owner) with the rows of the
+ * dirty tets replaced by the shards' segments (shards: per rank its dirty tets' global ids
+ * and their candidate + piece CSRs); every other row is copied unchanged.  The result is
+ * written to ctx-owned device arrays returned in *out (valid until the next-but-one
+ * rpd_merge_shards or destroy: `old` may be the previous call's output).  One host sync. */
+rpd_status rpd_merge_shards(rpd_ctx* ctx, const rpd_shards* dirty, const rpd_csr* old,
+                            rpd_csr* out);
+/* The candidate and piece segments of the ctx's tets `tet_list` [n] (local ids, host or
+ * device; e.g. the dirty tets of the last rpd_update_partial) as one CSR over the list, into
+ * caller-allocated arrays in *out (host or device; cand_* or piece_* all NULL: that part is
+ * skipped).  All destination pointers NULL: only the sizes are computed.  Always sets out->T
+ * = n and out->n_cand / n_pieces / n_inc.  ids_out [n] (may be NULL) receives the global id
+ * id_map[tet_list[k]] of every listed tet (id_map [T_local], host or device; NULL: the local
+ * id).  RPD_EINVAL: a listed tet outside [0, T_local); RPD_ESTATE before rpd_clip. */
+rpd_status rpd_download_tets(rpd_ctx* ctx, const int32_t* tet_list, int64_t n,
+                             const int32_t* id_map, int32_t* ids_out, rpd_csr* out);
 
 /* ---- Envelope distance (Sec. 4.3)
  *
@@ -365,6 +406,8 @@ typedef struct {
   int64_t clip_constructions;    /* new vertices */
   int64_t clip_fan_triangles;    /* fan triangles integrated for volume and first moment */
   double filter_ms, clip_ms;     /* kernel times of the last call (RPD_OPT_PROFILE only) */
+  /* rpd_update_partial: sizes of the dirty tets' new segments (what a sharded job exchanges) */
+  int64_t n_cand_dirty, n_pieces_dirty, n_inc_dirty;
 } rpd_stats;
 rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
 

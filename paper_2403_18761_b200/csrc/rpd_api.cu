@@ -171,16 +171,16 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
-                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->g_map, &c->g_off, &c->g_dst, &c->g_ids, &c->h_dl, &c->h_dm, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
-  CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d};
+  CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d, &c->g_cand[0], &c->g_cand[1]};
   for (CandSet* x : cs) {
     x->off.release();
     x->idx.release();
     x->pair_tet.release();
     x->moff.release();
   }
-  PieceSet* ps[] = {&c->pcs[0], &c->pcs[1], &c->pcs_d};
+  PieceSet* ps[] = {&c->pcs[0], &c->pcs[1], &c->pcs_d, &c->g_pcs[0], &c->g_pcs[1]};
   for (PieceSet* x : ps) {
     x->off.release();
     x->sphere.release();
@@ -791,6 +791,9 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
   }
   pd.n_pieces = rb->i32[5];
   pd.n_inc = rb->i32[6];
+  c->last.n_cand_dirty = cd.n;
+  c->last.n_pieces_dirty = pd.n_pieces;
+  c->last.n_inc_dirty = pd.n_inc;
   cn.n = rb->i32[0];
   cn.n_tets = T;
   cn.n_words = rb->i32[3];
@@ -991,27 +994,255 @@ rpd_status rpd_download_medial_mesh(rpd_ctx* c, int32_t* edges, int32_t* faces) 
   return RPD_OK;
 }
 
+// ---- segment gather engine (rpd_gather.cu): multi-GPU gather, partial-mode merge, download
+}  // extern "C"
+
+static bool shards_ok(const rpd_shards* sh, bool pieces, bool cands) {
+  if (!sh || sh->world < 1 || sh->world > RPD_MAX_RANKS || sh->T < 0 || sh->T > 0x7fffffff)
+    return false;
+  for (int r = 0; r < sh->world; ++r) {
+    if (sh->n_tets[r] < 0) return false;
+    if (sh->n_tets[r] == 0) continue;
+    if (!sh->tet_ids[r]) return false;
+    if (pieces && (!sh->piece_off[r] || !sh->inc_off[r])) return false;
+    if (cands && !sh->cand_off[r]) return false;
+  }
+  return true;
+}
+
+static void shard_sources(const rpd_shards* sh, SegShards* v, SegSources* S, int first) {
+  *v = SegShards{};
+  v->world = sh->world;
+  for (int r = 0; r < sh->world; ++r) {
+    v->base[r + 1] = v->base[r] + sh->n_tets[r];
+    v->tet_ids[r] = sh->tet_ids[r];
+    S->s[first + r] = seg_src_csr(sh->cand_off[r], sh->cand_idx[r], sh->piece_off[r],
+                                  sh->piece_sphere[r], sh->piece_vol[r], sh->piece_m1[r],
+                                  sh->piece_facemask[r], sh->inc_off[r], sh->inc_sphere[r]);
+    if (sh->n_tets[r] == 0) S->s[first + r] = SegSrc{};
+  }
+}
+
+// map -> counts -> (sync: sizes, errors) -> copy; dst arrays sized by the caller (gather,
+// download) or here (merge: ctx-owned, ensure_dst)
+template <class EnsureDst>
+static rpd_status seg_run(rpd_ctx* c, int kind, int64_t n_out, const int32_t* list,
+                          const SegShards* v, int64_t T, const SegSources& S, SegDst D,
+                          int64_t* n_cand, int64_t* n_pieces, int64_t* n_inc, bool copy,
+                          EnsureDst ensure_dst) {
+  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
+  CK(launch_map(c, kind, n_out, list, v, T), "row map");
+  // the offsets go to the destination when it is known, else to scratch first
+  CK(c->g_off.ensure(sizeof(int32_t) * 2 * (n_out + 1)), "alloc");
+  int32_t* co = D.cand_off ? D.cand_off : (n_cand ? c->g_off.as<int32_t>() : nullptr);
+  int32_t* po = D.piece_off ? D.piece_off
+                            : (n_pieces ? c->g_off.as<int32_t>() + (n_out + 1) : nullptr);
+  int32_t* it = nullptr;
+  CK(launch_seg_counts(c, n_out, S, co, po, &it), "segment counts");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{co ? co + n_out : nullptr, po ? po + n_out : nullptr,
+                         po ? it + n_out : nullptr},
+                        nullptr, c->errw.as<int>()}),
+     "readback");
+  CK(cudaStreamSynchronize(c->stream), "segment counts");
+  if (rb->err[0] != 0) return fail(c, RPD_EINVAL, "a tet id is out of range");
+  if (n_cand) *n_cand = rb->i32[0];
+  if (n_pieces) *n_pieces = rb->i32[1];
+  if (n_inc) *n_inc = rb->i32[2];
+  if (!copy) return RPD_OK;
+  rpd_status s = ensure_dst(rb->i32[0], rb->i32[1], rb->i32[2], &D);
+  if (s) return s;
+  if (D.cand_off && D.cand_off != co && co)
+    CK(cudaMemcpyAsync(D.cand_off, co, sizeof(int32_t) * (n_out + 1), cudaMemcpyDefault,
+                       c->stream), "copy offsets");
+  if (D.piece_off && D.piece_off != po && po)
+    CK(cudaMemcpyAsync(D.piece_off, po, sizeof(int32_t) * (n_out + 1), cudaMemcpyDefault,
+                       c->stream), "copy offsets");
+  D.i_tet = it;
+  CK(launch_seg_copy(c, n_out, S, D), "segment copy");
+  CK(cudaStreamSynchronize(c->stream), "segment copy");
+  return RPD_OK;
+}
+
+static rpd_status no_ensure(int64_t, int64_t, int64_t, SegDst*) { return RPD_OK; }
+
+extern "C" {
+
 rpd_status rpd_gather_pieces(rpd_ctx* c, const rpd_shards* sh, int32_t* piece_off,
                              int32_t* piece_sphere, double* piece_vol, double* piece_m1,
                              uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere) {
   if (!c) return RPD_EINVAL;
-  if (!sh || sh->world < 1 || sh->world > RPD_MAX_RANKS || sh->T < 0 || sh->T > 0x7fffffff ||
-      !piece_off || !inc_off)
+  if (!shards_ok(sh, true, false) || !piece_off || !inc_off)
     return fail(c, RPD_EINVAL, "rpd_gather_pieces: bad argument");
-  for (int r = 0; r < sh->world; ++r)
-    if (sh->n_tets[r] < 0 || (sh->n_tets[r] > 0 && (!sh->tet_ids[r] || !sh->piece_off[r] ||
-                                                    !sh->inc_off[r])))
-      return fail(c, RPD_EINVAL, "rpd_gather_pieces: bad shard");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
-  CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
-  CK(launch_gather_check(c, sh), "gather check");
-  CK(readback(c, RbSpec{{}, nullptr, c->errw.as<int>()}), "readback");
-  CK(cudaStreamSynchronize(c->stream), "gather check");
-  if (((Readback*)c->pinned)->err[0] != 0)
-    return fail(c, RPD_EINVAL, "rpd_gather_pieces: a tet id is out of range");
-  CK(launch_gather(c, sh, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask, inc_off,
-                   inc_sphere), "gather");
-  CK(cudaStreamSynchronize(c->stream), "gather");
+  rpd_shards p = *sh;
+  for (int r = 0; r < p.world; ++r) p.cand_off[r] = p.cand_idx[r] = nullptr;
+  SegShards v;
+  SegSources S{};
+  shard_sources(&p, &v, &S, 1);
+  SegDst D{nullptr, nullptr, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask,
+           inc_off, inc_sphere, nullptr};
+  return seg_run(c, 3, sh->T, nullptr, &v, sh->T, S, D, nullptr, nullptr, nullptr, true,
+                 no_ensure);
+}
+
+rpd_status rpd_gather_cands(rpd_ctx* c, const rpd_shards* sh, int32_t* cand_off,
+                            int32_t* cand_idx) {
+  if (!c) return RPD_EINVAL;
+  if (!shards_ok(sh, false, true) || !cand_off)
+    return fail(c, RPD_EINVAL, "rpd_gather_cands: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  rpd_shards p = *sh;
+  for (int r = 0; r < p.world; ++r) p.piece_off[r] = nullptr;
+  SegShards v;
+  SegSources S{};
+  shard_sources(&p, &v, &S, 1);
+  SegDst D{cand_off, cand_idx, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+           nullptr};
+  return seg_run(c, 3, sh->T, nullptr, &v, sh->T, S, D, nullptr, nullptr, nullptr, true,
+                 no_ensure);
+}
+
+static SegSrc state_source(rpd_ctx* c) {
+  const CandSet& cs = c->cand[c->cur];
+  const PieceSet& ps = c->pcs[c->cur];
+  return seg_src_csr(cs.off.as<int32_t>(), cs.idx.as<int32_t>(), ps.off.as<int32_t>(),
+                     ps.sphere.as<int32_t>(), ps.vol.as<double>(), ps.m1.as<double>(),
+                     ps.fm.as<uint8_t>(), ps.inc_off.as<int32_t>(), ps.inc.as<int32_t>());
+}
+
+rpd_status rpd_download_tets(rpd_ctx* c, const int32_t* tet_list, int64_t n,
+                             const int32_t* id_map, int32_t* ids_out, rpd_csr* out) {
+  if (!c) return RPD_EINVAL;
+  if (!out || n < 0 || n > 0x7fffffff || (n > 0 && !tet_list))
+    return fail(c, RPD_EINVAL, "rpd_download_tets: bad argument");
+  if (!c->have_pieces) return fail(c, RPD_ESTATE, "rpd_download_tets before rpd_clip");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int32_t* d_list = nullptr;
+  CK(resolve(c, tet_list, n, c->h_dl, &d_list), "stage tet list");
+  if (ids_out && n > 0) {
+    const int32_t* d_map = nullptr;
+    CK(resolve(c, id_map, id_map ? c->st.T : 0, c->h_dm, &d_map), "stage id map");
+    const bool host = is_host_ptr(ids_out);
+    CK(c->g_ids.ensure(sizeof(int32_t) * n), "alloc");
+    int32_t* dst = host ? c->g_ids.as<int32_t>() : ids_out;
+    CK(launch_map_ids(c, d_list, n, d_map, c->st.T, dst), "ids");
+    if (host)
+      CK(cudaMemcpyAsync(ids_out, dst, sizeof(int32_t) * n, cudaMemcpyDefault, c->stream),
+         "download ids");
+  }
+  SegSources S{};
+  S.s[0] = state_source(c);
+  const bool copy = out->cand_off || out->piece_off;
+  // a host destination is filled through device staging (g_dst) and one copy per array
+  const bool host = (out->cand_off && is_host_ptr(out->cand_off)) ||
+                    (out->piece_off && is_host_ptr(out->piece_off));
+  rpd_csr user = *out;
+  auto ensure = [&](int64_t nc, int64_t np, int64_t ni, SegDst* D) -> rpd_status {
+    if (!host) return RPD_OK;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
+    const size_t o_co = take(4 * (n + 1)), o_ci = take(4 * nc), o_po = take(4 * (n + 1)),
+                 o_ps = take(4 * np), o_pv = take(8 * np), o_pm = take(24 * np),
+                 o_pf = take(np), o_io = take(4 * (np + 1)), o_is = take(4 * ni);
+    if (c->g_dst.ensure(off)) return fail(c, RPD_ENOMEM, "alloc");
+    char* b = c->g_dst.as<char>();
+    if (D->cand_off) {
+      D->cand_off = (int32_t*)(b + o_co);
+      D->cand_idx = (int32_t*)(b + o_ci);
+    }
+    if (D->piece_off) {
+      D->piece_off = (int32_t*)(b + o_po);
+      D->piece_sphere = (int32_t*)(b + o_ps);
+      D->piece_vol = (double*)(b + o_pv);
+      D->piece_m1 = (double*)(b + o_pm);
+      D->piece_fm = (uint8_t*)(b + o_pf);
+      D->inc_off = (int32_t*)(b + o_io);
+      D->inc_sphere = (int32_t*)(b + o_is);
+    }
+    return RPD_OK;
+  };
+  SegDst D{out->cand_off, out->cand_idx, out->piece_off, out->piece_sphere, out->piece_vol,
+           out->piece_m1, out->piece_facemask, out->inc_off, out->inc_sphere, nullptr};
+  int64_t nc = 0, np = 0, ni = 0;
+  if (host) {
+    // sizes first (the staging is laid out from them), then the copy into the staging
+    rpd_status s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, SegDst{}, &nc, &np, &ni,
+                           false, no_ensure);
+    if (s) return s;
+    SegDst Dd = D;
+    if ((s = ensure(nc, np, ni, &Dd))) return s;
+    s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, Dd, &nc, &np, &ni, true, no_ensure);
+    if (s) return s;
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+      if (!dst || bytes == 0) return cudaSuccess;
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+    };
+    CK(cp(user.cand_off, Dd.cand_off, 4 * (n + 1)), "download");
+    CK(cp(user.cand_idx, Dd.cand_idx, 4 * nc), "download");
+    CK(cp(user.piece_off, Dd.piece_off, 4 * (n + 1)), "download");
+    CK(cp(user.piece_sphere, Dd.piece_sphere, 4 * np), "download");
+    CK(cp(user.piece_vol, Dd.piece_vol, 8 * np), "download");
+    CK(cp(user.piece_m1, Dd.piece_m1, 24 * np), "download");
+    CK(cp(user.piece_facemask, Dd.piece_fm, np), "download");
+    CK(cp(user.inc_off, Dd.inc_off, 4 * (np + 1)), "download");
+    CK(cp(user.inc_sphere, Dd.inc_sphere, 4 * ni), "download");
+    CK(cudaStreamSynchronize(c->stream), "download");
+  } else {
+    rpd_status s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, D, &nc, &np, &ni, copy,
+                           no_ensure);
+    if (s) return s;
+  }
+  out->T = n;
+  out->n_cand = nc;
+  out->n_pieces = np;
+  out->n_inc = ni;
+  return RPD_OK;
+}
+
+rpd_status rpd_merge_shards(rpd_ctx* c, const rpd_shards* dirty, const rpd_csr* old,
+                            rpd_csr* out) {
+  if (!c) return RPD_EINVAL;
+  if (!dirty || !old || !out || !shards_ok(dirty, true, true) || old->T != dirty->T ||
+      !old->cand_off || !old->piece_off || !old->inc_off)
+    return fail(c, RPD_EINVAL, "rpd_merge_shards: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int64_t T = dirty->T;
+  SegShards v;
+  SegSources S{};
+  S.s[0] = seg_src_csr(old->cand_off, old->cand_idx, old->piece_off, old->piece_sphere,
+                       old->piece_vol, old->piece_m1, old->piece_facemask, old->inc_off,
+                       old->inc_sphere);
+  shard_sources(dirty, &v, &S, 1);
+  // output: the ctx-owned buffer set that `old` does not live in
+  int g = c->g_cur ^ 1;
+  if (old->cand_off == c->g_cand[g].off.as<int32_t>()) g ^= 1;
+  CandSet& cn = c->g_cand[g];
+  PieceSet& pn = c->g_pcs[g];
+  CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  auto ensure = [&](int64_t nc, int64_t np, int64_t ni, SegDst* D) -> rpd_status {
+    const size_t a = nc > 0 ? nc : 1, b = np > 0 ? np : 1, d = ni > 0 ? ni : 1;
+    if (cn.idx.ensure(4 * a) || pn.sphere.ensure(4 * b) || pn.vol.ensure(8 * b) ||
+        pn.m1.ensure(24 * b) || pn.fm.ensure(b) || pn.inc_off.ensure(4 * (np + 1)) ||
+        pn.inc.ensure(4 * d))
+      return fail(c, RPD_ENOMEM, "alloc");
+    *D = SegDst{cn.off.as<int32_t>(),    cn.idx.as<int32_t>(),  pn.off.as<int32_t>(),
+                pn.sphere.as<int32_t>(), pn.vol.as<double>(),   pn.m1.as<double>(),
+                pn.fm.as<uint8_t>(),     pn.inc_off.as<int32_t>(), pn.inc.as<int32_t>(),
+                nullptr};
+    return RPD_OK;
+  };
+  SegDst D{cn.off.as<int32_t>(), nullptr, pn.off.as<int32_t>(), nullptr, nullptr, nullptr,
+           nullptr, nullptr, nullptr, nullptr};
+  int64_t nc = 0, np = 0, ni = 0;
+  rpd_status s = seg_run(c, 2, T, nullptr, &v, T, S, D, &nc, &np, &ni, true, ensure);
+  if (s) return s;
+  c->g_cur = g;
+  *out = rpd_csr{cn.off.as<int32_t>(),    cn.idx.as<int32_t>(), pn.off.as<int32_t>(),
+                 pn.sphere.as<int32_t>(), pn.vol.as<double>(),  pn.m1.as<double>(),
+                 pn.fm.as<uint8_t>(),     pn.inc_off.as<int32_t>(), pn.inc.as<int32_t>(),
+                 T, nc, np, ni};
   return RPD_OK;
 }
 

@@ -133,7 +133,13 @@ struct rpd_ctx {
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
   rpd::DevBuf cand_long;   // compaction: count + tets with more than 16 candidates
-  rpd::DevBuf g_cnt;       // multi-GPU gather: per global tet piece / incidence counts, offsets
+  rpd::DevBuf g_cnt;       // segment gather: per output row counts and tet-level inc offsets
+  rpd::DevBuf g_map;       // segment gather: int2 (source, row) per output row
+  rpd::DevBuf g_off, g_dst;  // segment gather: offsets scratch, staging of host destinations
+  rpd::DevBuf g_ids, h_dl, h_dm;  // rpd_download_tets: ids staging, host list / id map
+  rpd::CandSet g_cand[2];  // rpd_merge_shards outputs (alternating: the old CSR may be the
+  rpd::PieceSet g_pcs[2];  // previous output)
+  int g_cur = 0;
   rpd::DevBuf env_buf, env_out, h_env;  // envelope distance (NEXT-4): scratch, outputs, inputs
   rpd::DevBuf h_env2, h_env3, h_env4;
   rpd::DevBuf bvh;         // leaf and super-node boxes of the pruned filter
@@ -267,11 +273,44 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
 cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
                          const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
                          int phase);
-// multi-GPU gather of the pieces (rpd_gather.cu)
-cudaError_t launch_gather_check(rpd_ctx* c, const rpd_shards* in);
-cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
-                          int32_t* piece_sphere, double* piece_vol, double* piece_m1,
-                          uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere);
+// segment gather engine (rpd_gather.cu): multi-GPU gather / partial-mode merge / download
+// of a tet list.  A source holds per-row candidate and piece segments [beg[r], end[r]) and a
+// per-piece incidence CSR i_off (piece p: [i_off[p], i_off[p+1])); NULL parts are skipped.
+struct SegSrc {
+  const int32_t *c_beg, *c_end, *c_idx;
+  const int32_t *p_beg, *p_end, *p_sphere;
+  const double *p_vol, *p_m1;
+  const uint8_t* p_fm;
+  const int32_t *i_off, *i_sph;
+};
+struct SegSources {
+  SegSrc s[RPD_MAX_RANKS + 1];  // [0]: previous global CSR / the ctx state; [1 + r]: rank r
+};
+struct SegShards {
+  int world;
+  int64_t base[RPD_MAX_RANKS + 1];  // prefix of the ranks' row counts
+  const int32_t* tet_ids[RPD_MAX_RANKS];
+};
+struct SegDst {
+  int32_t *cand_off, *cand_idx;
+  int32_t *piece_off, *piece_sphere;
+  double *piece_vol, *piece_m1;
+  uint8_t* piece_fm;
+  int32_t *inc_off, *inc_sphere;
+  const int32_t* i_tet;  // tet-level incidence offsets (from launch_seg_counts)
+};
+SegSrc seg_src_csr(const int32_t* c_off, const int32_t* c_idx, const int32_t* p_off,
+                   const int32_t* p_sphere, const double* p_vol, const double* p_m1,
+                   const uint8_t* p_fm, const int32_t* i_off, const int32_t* i_sph);
+// kind 0: identity rows of source 0; 1: source-0 rows `list`; 2: identity overwritten by the
+// shards' rows (merge); 3: only the shards' rows (gather)
+cudaError_t launch_map(rpd_ctx* c, int kind, int64_t n_out, const int32_t* list,
+                       const SegShards* sh, int64_t T);
+cudaError_t launch_seg_counts(rpd_ctx* c, int64_t n_out, const SegSources& S, int32_t* cand_off,
+                              int32_t* piece_off, int32_t** i_tet_out);
+cudaError_t launch_seg_copy(rpd_ctx* c, int64_t n_out, const SegSources& S, const SegDst& D);
+cudaError_t launch_map_ids(rpd_ctx* c, const int32_t* list, int64_t n, const int32_t* id_map,
+                           int64_t T, int32_t* ids_out);
 // envelope distance (rpd_envelope.cu)
 cudaError_t launch_envelope_check(rpd_ctx* c, int64_t N, const int32_t* edges, int64_t NE,
                                   const int32_t* faces, int64_t NF);

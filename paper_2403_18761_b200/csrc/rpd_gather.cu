@@ -1,141 +1,215 @@
-// rpd_gather.cu -- SURVEY.md §8(a) row a7 / §8(e): the multi-GPU gather of the pieces.
+// rpd_gather.cu -- SURVEY.md §8(a) row a7 / §8(e): the multi-GPU exchange of the RPD.
 //
-// Every rank clips its own tet shard; the per-rank piece CSRs are all-gathered by NCCL
-// (torch.distributed, plumbing) and this kernel pair puts them back into global tet order on
-// every rank: per global tet its piece count and incidence count are scattered from the
-// owning rank (k_g_count), scanned into the global offsets, and every rank's pieces and
-// incidences copied to their global positions (k_g_copy; one thread per local tet, its few
-// pieces and incidences contiguous in source and destination).  Integer work and copies: the
-// result is byte-identical to a single-GPU run (per-tet outputs do not depend on the shard).
+// Every rank clips its own tet shard; the per-rank candidate and piece CSRs are all-gathered
+// by NCCL (torch.distributed, plumbing) and the kernels here put them back into global tet
+// order.  In partial mode only the dirty tets' segments travel, and they replace those tets'
+// segments of the previous global CSR (the clean tets keep theirs byte-identically, R11).
+//
+// One segment-gather engine serves every case: a row map sends each output row (a tet) to
+// (source, row) -- source 0 the previous global CSR or the ctx's own state, sources 1.. the
+// ranks' gathered shards -- then per output row its candidate / piece / incidence counts are
+// read (k_seg_count), scanned into the output offsets, and its segments copied (k_seg_copy;
+// one thread per row: a tet's few candidates, pieces and incidences are contiguous in source
+// and destination).  Integer work and copies only: results are byte-identical to a
+// single-GPU run (per-tet outputs do not depend on the shard).
 #include "rpd_ctx.h"
 
 namespace rpd {
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-struct ShardView {
-  int world;
-  int64_t base[RPD_MAX_RANKS + 1];  // prefix of the ranks' local tet counts
-  const int32_t* tet_ids[RPD_MAX_RANKS];
-  const int32_t* piece_off[RPD_MAX_RANKS];
-  const int32_t* piece_sphere[RPD_MAX_RANKS];
-  const double* piece_vol[RPD_MAX_RANKS];
-  const double* piece_m1[RPD_MAX_RANKS];
-  const uint8_t* piece_facemask[RPD_MAX_RANKS];
-  const int32_t* inc_off[RPD_MAX_RANKS];
-  const int32_t* inc_sphere[RPD_MAX_RANKS];
-};
+__global__ void k_map_fill(int64_t n, int2* __restrict__ map) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o < n) map[o] = make_int2(0, (int)o);  // row o of source 0
+}
 
-__device__ __forceinline__ int rank_of(const ShardView& v, int64_t x) {
+__global__ void k_map_list(const int32_t* __restrict__ list, int64_t n, int64_t T,
+                           int2* __restrict__ map, int* err) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  const int t = list[o];
+  if (t < 0 || t >= T) {
+    if (atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+      err[1] = ERR_TET_INDEX;
+      err[2] = (int)o;
+    }
+    map[o] = make_int2(-1, 0);
+    return;
+  }
+  map[o] = make_int2(0, t);
+}
+
+// shard r's local row a -> output row tet_ids[r][a], source 1 + r (checked: ids in [0, T))
+__global__ void k_map_shards(SegShards v, int64_t T, int2* __restrict__ map, int* err) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= v.base[v.world]) return;
   int r = 0;
   while (r + 1 < v.world && v.base[r + 1] <= x) ++r;
-  return r;
-}
-
-// every rank's global tet ids in [0, T) (before any kernel writes through them)
-__global__ void k_g_check(ShardView v, int64_t T, int* err) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= v.base[v.world]) return;
-  const int r = rank_of(v, x);
-  const int t = v.tet_ids[r][x - v.base[r]];
-  if ((t < 0 || t >= T) && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
-    err[1] = ERR_TET_INDEX;
-    err[2] = (int)x;
-  }
-}
-
-// per global tet: pieces and incidences (from the owning rank)
-__global__ void k_g_count(ShardView v, int32_t* __restrict__ pc, int32_t* __restrict__ ic) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= v.base[v.world]) return;
-  const int r = rank_of(v, x);
-  const int64_t a = x - v.base[r];
-  const int32_t* po = v.piece_off[r];
-  const int32_t* io = v.inc_off[r];
-  const int t = v.tet_ids[r][a];
-  const int p0 = po[a], p1 = po[a + 1];
-  pc[t] = p1 - p0;
-  ic[t] = io[p1] - io[p0];
-}
-
-__global__ void k_g_copy(ShardView v, const int32_t* __restrict__ goff,
-                         const int32_t* __restrict__ gioff, int32_t* __restrict__ sphere,
-                         double* __restrict__ vol, double* __restrict__ m1,
-                         uint8_t* __restrict__ fm, int32_t* __restrict__ inc_off,
-                         int32_t* __restrict__ inc, int64_t T) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x == 0) inc_off[goff[T]] = gioff[T];  // terminal entry
-  if (x >= v.base[v.world]) return;
-  const int r = rank_of(v, x);
   const int64_t a = x - v.base[r];
   const int t = v.tet_ids[r][a];
-  const int32_t* po = v.piece_off[r];
-  const int32_t* io = v.inc_off[r];
-  const int p0 = po[a], p1 = po[a + 1];
-  const int q0 = goff[t], i0 = io[p0], gi0 = gioff[t];
-  for (int p = p0; p < p1; ++p) {
-    const int q = q0 + (p - p0);
-    sphere[q] = v.piece_sphere[r][p];
-    vol[q] = v.piece_vol[r][p];
-    m1[3 * (int64_t)q] = v.piece_m1[r][3 * (int64_t)p];
-    m1[3 * (int64_t)q + 1] = v.piece_m1[r][3 * (int64_t)p + 1];
-    m1[3 * (int64_t)q + 2] = v.piece_m1[r][3 * (int64_t)p + 2];
-    fm[q] = v.piece_facemask[r][p];
-    inc_off[q] = gi0 + (io[p] - i0);
+  if (t < 0 || t >= T) {
+    if (atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+      err[1] = ERR_TET_INDEX;
+      err[2] = (int)x;
+    }
+    return;
   }
-  for (int k = i0; k < io[p1]; ++k) inc[gi0 + (k - i0)] = v.inc_sphere[r][k];
+  map[t] = make_int2(1 + r, (int)a);
 }
 
-static ShardView view_of(const rpd_shards* in) {
-  ShardView v{};
-  v.world = in->world;
-  v.base[0] = 0;
-  for (int r = 0; r < in->world; ++r) {
-    v.base[r + 1] = v.base[r] + in->n_tets[r];
-    v.tet_ids[r] = in->tet_ids[r];
-    v.piece_off[r] = in->piece_off[r];
-    v.piece_sphere[r] = in->piece_sphere[r];
-    v.piece_vol[r] = in->piece_vol[r];
-    v.piece_m1[r] = in->piece_m1[r];
-    v.piece_facemask[r] = in->piece_facemask[r];
-    v.inc_off[r] = in->inc_off[r];
-    v.inc_sphere[r] = in->inc_sphere[r];
+// per output row: candidates, pieces, incidences of its source segment (0 for unmapped rows)
+__global__ void k_seg_count(int64_t n, const int2* __restrict__ map, SegSources S,
+                            int32_t* __restrict__ cc, int32_t* __restrict__ pc,
+                            int32_t* __restrict__ ic) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  const int2 m = map[o];
+  int nc = 0, np = 0, ni = 0;
+  if (m.x >= 0) {
+    const SegSrc& s = S.s[m.x];
+    if (s.c_beg) nc = s.c_end[m.y] - s.c_beg[m.y];
+    if (s.p_beg) {
+      const int p0 = s.p_beg[m.y], p1 = s.p_end[m.y];
+      np = p1 - p0;
+      ni = p1 > p0 ? s.i_off[p1] - s.i_off[p0] : 0;
+    }
   }
-  return v;
+  if (cc) cc[o] = nc;
+  if (pc) pc[o] = np;
+  if (ic) ic[o] = ni;
 }
 
-cudaError_t launch_gather_check(rpd_ctx* c, const rpd_shards* in) {
-  const ShardView v = view_of(in);
-  const int64_t n = v.base[in->world];
-  if (n > 0) {
-    k_g_check<<<nblk(n, 256), 256, 0, c->stream>>>(v, in->T, c->errw.as<int>());
+__global__ void k_seg_copy(int64_t n, const int2* __restrict__ map, SegSources S, SegDst D) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o == 0 && D.piece_off) D.inc_off[D.piece_off[n]] = D.i_tet[n];  // terminal entry
+  if (o >= n) return;
+  const int2 m = map[o];
+  if (m.x < 0) return;
+  const SegSrc& s = S.s[m.x];
+  if (D.cand_idx && s.c_beg) {
+    const int c0 = s.c_beg[m.y], c1 = s.c_end[m.y], q0 = D.cand_off[o];
+    for (int k = c0; k < c1; ++k) D.cand_idx[q0 + (k - c0)] = s.c_idx[k];
+  }
+  if (D.piece_off && s.p_beg) {
+    const int p0 = s.p_beg[m.y], p1 = s.p_end[m.y];
+    if (p1 <= p0) return;
+    const int q0 = D.piece_off[o], i0 = s.i_off[p0], gi0 = D.i_tet[o];
+    for (int p = p0; p < p1; ++p) {
+      const int q = q0 + (p - p0);
+      D.piece_sphere[q] = s.p_sphere[p];
+      D.piece_vol[q] = s.p_vol[p];
+      D.piece_m1[3 * (int64_t)q] = s.p_m1[3 * (int64_t)p];
+      D.piece_m1[3 * (int64_t)q + 1] = s.p_m1[3 * (int64_t)p + 1];
+      D.piece_m1[3 * (int64_t)q + 2] = s.p_m1[3 * (int64_t)p + 2];
+      D.piece_fm[q] = s.p_fm[p];
+      D.inc_off[q] = gi0 + (s.i_off[p] - i0);
+    }
+    const int i1 = s.i_off[p1];
+    for (int k = i0; k < i1; ++k) D.inc_sphere[gi0 + (k - i0)] = s.i_sph[k];
+  }
+}
+
+// ids_out[k] = id_map[list[k]] (or list[k]): the global ids of downloaded local tets
+__global__ void k_map_ids(const int32_t* __restrict__ list, int64_t n,
+                          const int32_t* __restrict__ id_map, int64_t T,
+                          int32_t* __restrict__ ids_out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int t = list[k];
+  ids_out[k] = id_map && t >= 0 && t < T ? id_map[t] : t;
+}
+
+cudaError_t launch_map_ids(rpd_ctx* c, const int32_t* list, int64_t n, const int32_t* id_map,
+                           int64_t T, int32_t* ids_out) {
+  if (n == 0) return cudaSuccess;
+  k_map_ids<<<nblk(n, 256), 256, 0, c->stream>>>(list, n, id_map, T, ids_out);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+SegSrc seg_src_csr(const int32_t* c_off, const int32_t* c_idx, const int32_t* p_off,
+                   const int32_t* p_sphere, const double* p_vol, const double* p_m1,
+                   const uint8_t* p_fm, const int32_t* i_off, const int32_t* i_sph) {
+  SegSrc s{};
+  if (c_off) {
+    s.c_beg = c_off;
+    s.c_end = c_off + 1;
+    s.c_idx = c_idx;
+  }
+  if (p_off) {
+    s.p_beg = p_off;
+    s.p_end = p_off + 1;
+    s.p_sphere = p_sphere;
+    s.p_vol = p_vol;
+    s.p_m1 = p_m1;
+    s.p_fm = p_fm;
+    s.i_off = i_off;
+    s.i_sph = i_sph;
+  }
+  return s;
+}
+
+cudaError_t launch_map(rpd_ctx* c, int kind, int64_t n_out, const int32_t* list,
+                       const SegShards* sh, int64_t T) {
+  cudaError_t e = c->g_map.ensure(sizeof(int2) * (n_out > 0 ? n_out : 1));
+  if (e) return e;
+  int2* map = c->g_map.as<int2>();
+  if (n_out == 0) return cudaSuccess;
+  if (kind == 0 || kind == 2) {  // identity (source 0), optionally overwritten by shards
+    k_map_fill<<<nblk(n_out, 256), 256, 0, c->stream>>>(n_out, map);
+    ++c->launches;
+  } else if (kind == 1) {  // explicit list of source-0 rows
+    k_map_list<<<nblk(n_out, 256), 256, 0, c->stream>>>(list, n_out, T, map, c->errw.as<int>());
+    ++c->launches;
+  }
+  if (kind == 3) {  // unmapped rows (no rank holds them) count zero
+    if ((e = cudaMemsetAsync(map, 0xff, sizeof(int2) * n_out, c->stream))) return e;
+  }
+  if ((kind == 2 || kind == 3) && sh->base[sh->world] > 0) {
+    k_map_shards<<<nblk(sh->base[sh->world], 256), 256, 0, c->stream>>>(*sh, T, map,
+                                                                         c->errw.as<int>());
     ++c->launches;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather(rpd_ctx* c, const rpd_shards* in, int32_t* piece_off,
-                          int32_t* piece_sphere, double* piece_vol, double* piece_m1,
-                          uint8_t* piece_facemask, int32_t* inc_off, int32_t* inc_sphere) {
-  const ShardView v = view_of(in);
-  const int64_t T = in->T, n = v.base[in->world];
-  cudaError_t e = c->g_cnt.ensure(sizeof(int32_t) * (3 * (T + 1) + 1));
+// counts of the mapped rows -> output offsets (cand_off / piece_off / tet-level incidence
+// offsets); totals at [n_out]
+cudaError_t launch_seg_counts(rpd_ctx* c, int64_t n_out, const SegSources& S, int32_t* cand_off,
+                              int32_t* piece_off, int32_t** i_tet_out) {
+  cudaError_t e = c->g_cnt.ensure(sizeof(int32_t) * 4 * (n_out + 1));
   if (e) return e;
-  int32_t* pc = c->g_cnt.as<int32_t>();
-  int32_t* ic = pc + (T + 1);
-  int32_t* gioff = ic + (T + 1);
-  // tets no rank holds count zero (every tet belongs to one shard; this keeps the scan defined)
-  if ((e = cudaMemsetAsync(pc, 0, sizeof(int32_t) * 2 * (T + 1), c->stream))) return e;
-  if (n > 0) {
-    k_g_count<<<nblk(n, 256), 256, 0, c->stream>>>(v, pc, ic);
+  int32_t* cc = c->g_cnt.as<int32_t>();
+  int32_t* pc = cc + (n_out + 1);
+  int32_t* ic = pc + (n_out + 1);
+  int32_t* it = ic + (n_out + 1);
+  *i_tet_out = it;
+  if (n_out > 0) {
+    k_seg_count<<<nblk(n_out, 256), 256, 0, c->stream>>>(n_out, c->g_map.as<int2>(), S,
+                                                         cand_off ? cc : nullptr,
+                                                         piece_off ? pc : nullptr,
+                                                         piece_off ? ic : nullptr);
     ++c->launches;
   }
-  const int32_t* sin[2] = {pc, ic};
-  int32_t* sout[2] = {piece_off, gioff};
-  if ((e = launch_scan_i32_multi(c, sin, sout, 2, T))) return e;
-  k_g_copy<<<nblk(n > 0 ? n : 1, 256), 256, 0, c->stream>>>(v, piece_off, gioff, piece_sphere,
-                                                           piece_vol, piece_m1, piece_facemask,
-                                                           inc_off, inc_sphere, T);
+  const int32_t* in[3];
+  int32_t* out[3];
+  int K = 0;
+  if (cand_off) {
+    in[K] = cc;
+    out[K++] = cand_off;
+  }
+  if (piece_off) {
+    in[K] = pc;
+    out[K++] = piece_off;
+    in[K] = ic;
+    out[K++] = it;
+  }
+  return K ? launch_scan_i32_multi(c, in, out, K, n_out) : cudaSuccess;
+}
+
+cudaError_t launch_seg_copy(rpd_ctx* c, int64_t n_out, const SegSources& S, const SegDst& D) {
+  k_seg_copy<<<nblk(n_out > 0 ? n_out : 1, 256), 256, 0, c->stream>>>(n_out, c->g_map.as<int2>(),
+                                                                      S, D);
   ++c->launches;
   return cudaGetLastError();
 }

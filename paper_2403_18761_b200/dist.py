@@ -1,79 +1,166 @@
 """Multi-GPU plumbing: tets sharded block-cyclically over the ranks of one
-node, spheres and neighbour lists replicated, per-rank RPD outputs all-gathered with NCCL.
+node, spheres and neighbour lists replicated, and the per-rank RPD outputs exchanged with NCCL.
 
 The exchange is the only cross-rank step of the path (every (tet, sphere) pair is
-independent).  Outputs of every rank are downloaded into torch tensors on the rank's device,
-their sizes all-gathered, the payloads all-gathered padded to the largest rank (NCCL over
-NVLink; gloo in the CPU tests), and the pieces put back in global tet order by the library's
-rpd_gather_pieces kernels (no torch compute on the path).
+independent).  Per exchange there is ONE counts all-gather (4 int64 per rank, one host sync)
+and ONE payload all-gather: every rank packs its segments into one byte buffer (the library
+copies them in, ``rpd_download_*`` / ``rpd_download_tets``), the buffers are all-gathered
+padded to the largest rank (NCCL over NVLink/NVSwitch; gloo in the CPU tests), and the library
+puts them into global tet order on every rank:
+
+* full RPD: the candidate and piece CSRs of every shard -> ``rpd_gather_cands`` +
+  ``rpd_gather_pieces``;
+* partial update: only the dirty tets' segments and their global ids -> ``rpd_merge_shards``
+  replaces those rows of the previous global CSR (SURVEY.md §8(e) "all-gathers only the
+  changed segments plus the dirty-tet ids").
+
+No torch compute runs on the path: torch provides the buffers and the collectives.
 """
 from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
-def shard_tets(T: int, world: int, rank: int, block: int = 4096) -> np.ndarray:
+BLOCK = 4096
+
+
+def shard_tets(T: int, world: int, rank: int, block: int = BLOCK) -> np.ndarray:
     """Global ids of this rank's tets: Morton-ordered blocks of ``block`` tets dealt
     round-robin (balances the O(T N) filter and spatially clustered partial updates)."""
     ids = np.arange(T, dtype=np.int64)
     return ids[(ids // block) % world == rank].astype(np.int32)
 
 
-def _all_gather_padded(x: torch.Tensor, group=None):
-    """All-gather a 1-D (or row) tensor of per-rank length; returns the list of pieces."""
+# ------------------------------------------------------------------ packed payload layout
+
+# (key, dtype, length as a function of the counts (rows, n_cand, n_pieces, n_inc))
+SECTIONS = {
+    "ids": ("tet_ids", np.int32, lambda n, c, p, i: n),
+    "cands": [("cand_off", np.int32, lambda n, c, p, i: n + 1),
+              ("cand_idx", np.int32, lambda n, c, p, i: c)],
+    "pieces": [("piece_off", np.int32, lambda n, c, p, i: n + 1),
+               ("piece_sphere", np.int32, lambda n, c, p, i: p),
+               ("piece_vol", np.float64, lambda n, c, p, i: p),
+               ("piece_m1", np.float64, lambda n, c, p, i: 3 * p),
+               ("piece_facemask", np.uint8, lambda n, c, p, i: p),
+               ("inc_off", np.int32, lambda n, c, p, i: p + 1),
+               ("inc_sphere", np.int32, lambda n, c, p, i: i)],
+}
+
+
+def layout(counts, with_ids: bool):
+    """Byte layout of one rank's packed payload: [(key, dtype, length, byte offset)], each
+    section 16-byte aligned; returns (sections, total bytes)."""
+    n, c, p, i = (int(x) for x in counts)
+    secs = ([SECTIONS["ids"]] if with_ids else []) + SECTIONS["cands"] + SECTIONS["pieces"]
+    out, off = [], 0
+    for key, dt, f in secs:
+        ln = int(f(n, c, p, i))
+        out.append((key, dt, ln, off))
+        off += (ln * np.dtype(dt).itemsize + 15) // 16 * 16
+    return out, off
+
+
+_TDT = {np.int32: torch.int32, np.float64: torch.float64, np.uint8: torch.uint8}
+
+
+def views(buf: torch.Tensor, secs) -> dict:
+    """Typed views of the sections of a packed byte buffer."""
+    out = {}
+    for key, dt, ln, off in secs:
+        nb = ln * np.dtype(dt).itemsize
+        out[key] = buf[off:off + nb].view(_TDT[dt])
+    out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
+    return out
+
+
+def exchange(counts_local, fill, device, group=None, with_ids=False):
+    """The collective of one exchange: counts all-gathered (one host sync), every rank's
+    payload packed by ``fill(views)`` into one buffer, all-gathered padded to the largest rank.
+    Returns (per-rank typed views of the gathered payloads, per-rank counts [world, 4])."""
     world = dist.get_world_size(group)
-    n = torch.tensor([x.shape[0]], dtype=torch.int64, device=x.device)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    ns = [int(v.item()) for v in ns]
-    m = max(ns) if ns else 0
-    pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-    pad[:x.shape[0]] = x
-    bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
-    return [b[:k] for b, k in zip(bufs, ns)]
+    cl = torch.tensor([int(x) for x in counts_local], dtype=torch.int64, device=device)
+    ca = torch.empty(world * 4, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(ca, cl, group=group)
+    counts = ca.view(world, 4).cpu().numpy()                       # the one host sync
+    lay = [layout(counts[r], with_ids) for r in range(world)]
+    maxb = max(b for _, b in lay)
+    rank = dist.get_rank(group)
+    buf = torch.empty(maxb, dtype=torch.uint8, device=device)
+    fill(views(buf, lay[rank][0]))
+    big = torch.empty(world * maxb, dtype=torch.uint8, device=device)
+    dist.all_gather_into_tensor(big, buf, group=group)
+    return [views(big[r * maxb:(r + 1) * maxb], lay[r][0]) for r in range(world)], counts
 
 
-PIECE_ARRAYS = ("piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
-                "inc_off", "inc_sphere")
+# ------------------------------------------------------------------ the sharded RPD
 
 
-def all_gather_pieces(local: dict, group=None) -> list:
-    """The collective of the gather (plumbing): every rank's piece CSR (tensors on its device)
-    all-gathered -- sizes first, then the payloads padded to the largest rank -- so that every
-    rank holds all ranks' CSRs.  Returns one dict per rank."""
-    world = dist.get_world_size(group)
-    g = {k: _all_gather_padded(local[k].reshape(local[k].shape[0], -1) if k == "piece_m1"
-                                else local[k], group) for k in PIECE_ARRAYS}
-    return [{k: g[k][r] for k in PIECE_ARRAYS} for r in range(world)]
+class ShardedRPD:
+    """The RPD of all T tets on every rank of ``group``: each rank clips its block-cyclic
+    shard with its own librpd ctx, and the exchanges above assemble the global candidate and
+    piece CSRs (torch CUDA tensors / ctx-owned arrays) on every rank."""
 
+    def __init__(self, ctx, T: int, group=None, block: int = BLOCK):
+        self.ctx, self.T, self.group, self.block = ctx, int(T), group, block
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.dev = torch.device("cuda", ctx.device)
+        self.ids = shard_tets(self.T, self.world, self.rank, block)
+        self.ids_dev = torch.as_tensor(self.ids, device=self.dev)
+        self.all_ids = [torch.as_tensor(shard_tets(self.T, self.world, r, block),
+                                        device=self.dev) for r in range(self.world)]
+        self.glob = None      # the global CSR: dict of device tensors (views of ctx arrays)
+        self.bytes_sent = 0
 
-_IDS = {}
+    def local_tets(self, tets):
+        return tets[self.ids]
 
+    def full(self, verts, tets_local, spheres, nbr_off, nbr_idx):
+        """rpd_relations + rpd_clip of this rank's shard, then the gather of every shard."""
+        self.ctx.relations(verts, tets_local, spheres, nbr_off, nbr_idx)
+        self.ctx.clip()
+        return self.gather_full()
 
-def gather_pieces(local: dict, tet_ids_local, T: int, ctx, group=None) -> dict:
-    """Global piece CSR on every rank: NCCL all-gather of the per-rank piece
-    CSRs, then rpd_gather_pieces (CUDA) puts them in global tet order.  The ranks' global tet
-    ids follow from the block-cyclic sharding (no exchange)."""
-    world = dist.get_world_size(group)
-    shards = all_gather_pieces(local, group)
-    dev = local["piece_vol"].device
-    key = (T, world, str(dev), len(tet_ids_local))
-    if key not in _IDS:
-        blk = _shard_block(T, world, tet_ids_local, dist.get_rank(group))
-        _IDS[key] = [torch.as_tensor(shard_tets(T, world, r, blk), device=dev)
-                     for r in range(world)]
-    return ctx.gather_pieces(shards, _IDS[key], T)
+    def gather_full(self):
+        """The exchange after a full RPD of every shard: all candidate + piece CSRs."""
+        ctx = self.ctx
+        counts = (len(self.ids), ctx.n_cand, ctx.counts.n_pieces, ctx.counts.n_inc)
 
+        def fill(v):
+            ctx.download_cands(out=v)
+            ctx.download_pieces(out=v)
+        shards, cnt = exchange(counts, fill, self.dev, self.group)
+        self.bytes_sent = int(sum(layout(cnt[r], False)[1] for r in range(self.world)))
+        nc, npc, ni = (int(cnt[:, k].sum()) for k in (1, 2, 3))
+        self.glob = ctx.gather_all(shards, self.all_ids, self.T, nc, npc, ni)
+        return self.glob
 
-def _shard_block(T, world, ids, rank):
-    """The block size of the shard ``ids`` of ``rank`` (default 4096)."""
-    for blk in (4096, 256, 1024, 2048, 8192):
-        s = shard_tets(T, world, rank, blk)
-        if len(s) == len(ids) and np.array_equal(s, np.asarray(ids)):
-            return blk
-    raise ValueError("tet ids are not a block-cyclic shard")
+    def partial(self, spheres, nbr_off, nbr_idx, new_ids):
+        """rpd_update_partial of this rank's shard, then the exchange of the dirty tets'
+        segments and their global ids, merged into the global CSR (rpd_merge_shards)."""
+        _, nd = self.ctx.update_partial(spheres, nbr_off, nbr_idx, new_ids)
+        return self.exchange_partial(nd)
+
+    def exchange_partial(self, nd: int):
+        """The exchange after a partial update of every shard: the dirty tets' segments with
+        their global ids, merged into the global CSR; returns (global CSR, total dirty)."""
+        ctx = self.ctx
+        st = ctx.stats()
+        counts = (nd, st["n_cand_dirty"], st["n_pieces_dirty"], st["n_inc_dirty"])
+
+        def fill(v):
+            ctx.download_tets(ctx.dirty_ptr(), nd, v, id_map=self.ids_dev)
+        shards, cnt = exchange(counts, fill, self.dev, self.group, with_ids=True)
+        self.bytes_sent = int(sum(layout(cnt[r], True)[1] for r in range(self.world)))
+        self.glob = ctx.merge_shards(shards, self.glob, self.T)
+        return self.glob, int(cnt[:, 0].sum())
 
 
 def allreduce_euler(local: dict, group=None) -> dict:
@@ -87,3 +174,25 @@ def allreduce_euler(local: dict, group=None) -> dict:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         out[k] = t
     return out
+
+
+# ------------------------------------------------------------------ launcher
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(n: int, script: str, argv) -> int:
+    """Run ``script argv`` as n ranks of one node through torch.distributed.run (rendezvous on
+    127.0.0.1); returns the launcher's exit code.  Rank 0's stdout passes through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           script, *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)

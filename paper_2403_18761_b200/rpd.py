@@ -28,7 +28,8 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_get_stats", "rpd_version", "rpd_set_euler", "rpd_get_euler",
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
-            "rpd_neighbors", "rpd_download_neighbors"]
+            "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
+            "rpd_download_tets"]
 
 
 class RPDError(RuntimeError):
@@ -71,11 +72,20 @@ class _Medial(C.Structure):
 MAX_RANKS = 16
 
 
+SHARD_KEYS = ("tet_ids", "piece_off", "piece_sphere", "piece_vol", "piece_m1",
+              "piece_facemask", "inc_off", "inc_sphere", "cand_off", "cand_idx")
+CSR_KEYS = ("cand_off", "cand_idx", "piece_off", "piece_sphere", "piece_vol", "piece_m1",
+            "piece_facemask", "inc_off", "inc_sphere")
+
+
 class _Shards(C.Structure):
     _fields_ = [("world", C.c_int32), ("T", C.c_int64), ("n_tets", C.c_int64 * MAX_RANKS)] + \
-               [(k, C.c_void_p * MAX_RANKS) for k in
-                ("tet_ids", "piece_off", "piece_sphere", "piece_vol", "piece_m1",
-                 "piece_facemask", "inc_off", "inc_sphere")]
+               [(k, C.c_void_p * MAX_RANKS) for k in SHARD_KEYS]
+
+
+class _Csr(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in CSR_KEYS] + \
+               [(k, C.c_int64) for k in ("T", "n_cand", "n_pieces", "n_inc")]
 
 
 class _Stats(C.Structure):
@@ -89,7 +99,8 @@ class _Stats(C.Structure):
                 ("rel_tests", C.c_int64), ("clip_plane_evals", C.c_int64),
                 ("clip_vertex_tests", C.c_int64), ("clip_constructions", C.c_int64),
                 ("clip_fan_triangles", C.c_int64), ("filter_ms", C.c_double),
-                ("clip_ms", C.c_double)]
+                ("clip_ms", C.c_double), ("n_cand_dirty", C.c_int64),
+                ("n_pieces_dirty", C.c_int64), ("n_inc_dirty", C.c_int64)]
 
 
 _lib = None
@@ -128,6 +139,9 @@ def load_library(path: str = LIB_PATH):
     L.rpd_neighbors.argtypes = [vp, vp, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
+    L.rpd_gather_cands.argtypes = [vp, C.POINTER(_Shards), vp, vp]
+    L.rpd_merge_shards.argtypes = [vp, C.POINTER(_Shards), C.POINTER(_Csr), C.POINTER(_Csr)]
+    L.rpd_download_tets.argtypes = [vp, vp, i64, vp, vp, C.POINTER(_Csr)]
     L.rpd_envelope.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(i64)]
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
@@ -135,7 +149,8 @@ def load_library(path: str = LIB_PATH):
               "rpd_get_euler", "rpd_download_euler", "rpd_get_topology",
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
-              "rpd_download_neighbors"):
+              "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
+              "rpd_download_tets"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -272,24 +287,31 @@ class RPDContext:
     def dirty_tets(self):
         """The dirty tets of the last update_partial (ascending) as a torch CUDA int32 tensor
         (a copy of the ctx-owned device array)."""
-        import torch
+        return _device_view(self.dirty_ptr(), int(getattr(self, "n_dirty", 0)), "<i4").clone()
 
-        class _View:  # __cuda_array_interface__ over the ctx-owned device array
-            def __init__(s, ptr, n):
-                s.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4",
-                                              "data": (ptr or 0, False), "version": 3,
-                                              "stream": None}
-        n = int(getattr(self, "n_dirty", 0))
-        if n == 0:
-            return torch.zeros(0, dtype=torch.int32, device="cuda")
-        return torch.as_tensor(_View(self._dirty_ptr, n), device="cuda").clone()
-
-    def download_cands(self, device=False):
-        """Candidate CSR as numpy (host) or torch CUDA tensors (device=True)."""
+    def download_cands(self, device=False, out=None):
+        """Candidate CSR as numpy (host) or torch CUDA tensors (device=True); ``out``: optional
+        preallocated destinations (numpy or torch, host or device) keyed like the result."""
         T, n = self.T, self.n_cand
-        off, idx = self._alloc([(T + 1, np.int32), (n, np.int32)], device)
-        self._check(self.L.rpd_download_cands(self.h, self._p(off), self._p(idx)))
-        return {"cand_off": off, "cand_idx": idx}
+        specs = [(T + 1, np.int32), (n, np.int32)]
+        keys = ["cand_off", "cand_idx"]
+        arrs = self._alloc(specs, device) if out is None else self._outs(out, keys, specs)
+        self._check(self.L.rpd_download_cands(self.h, self._p(arrs[0]), self._p(arrs[1])))
+        return dict(zip(keys, arrs))
+
+    @staticmethod
+    def _outs(out, keys, specs):
+        """Views [:n] of caller destinations, checked for dtype and length."""
+        arrs = []
+        for k, (n, dt) in zip(keys, specs):
+            a = out[k].reshape(-1)
+            adt = np.dtype(dt)
+            ok = (a.dtype == adt) if isinstance(a, np.ndarray) else \
+                (a.element_size() == adt.itemsize and str(a.dtype).endswith(adt.name))
+            if not ok or (a.size if isinstance(a, np.ndarray) else a.numel()) < n:
+                raise ValueError(f"out[{k!r}] needs {n} x {adt}")
+            arrs.append(a[:n])
+        return arrs
 
     def download_pieces(self, device=False, out=None):
         """Piece CSR as numpy (host) or torch CUDA tensors (device=True).  `out`: optional
@@ -301,15 +323,7 @@ class RPDContext:
                  (3 * npc, np.float64), (npc, np.uint8), (npc + 1, np.int32), (ni, np.int32)]
         keys = ["piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
                 "inc_off", "inc_sphere"]
-        if out is None:
-            arrs = self._alloc(specs, device)
-        else:
-            arrs = []
-            for k, (n, dt) in zip(keys, specs):
-                a = out[k].reshape(-1)
-                if a.dtype != dt or a.size < n:
-                    raise ValueError(f"download_pieces: out[{k!r}] needs {n} x {np.dtype(dt)}")
-                arrs.append(a[:n])
+        arrs = self._alloc(specs, device) if out is None else self._outs(out, keys, specs)
         self._check(self.L.rpd_download_pieces(self.h, *[self._p(a) for a in arrs]))
         out = dict(zip(keys, arrs))
         out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
@@ -392,28 +406,106 @@ class RPDContext:
         return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
                 "n_vertex_overflow": n.n_vertex_overflow}
 
-    def gather_pieces(self, shards, tet_ids, T: int) -> dict:
-        """Global piece CSR (torch CUDA tensors) from per-rank piece CSRs (``shards``: one dict
-        per rank of CUDA tensors piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask,
-        inc_off, inc_sphere; ``tet_ids``: per rank the CUDA int32 global ids of its tets), put
-        in global tet order by rpd_gather_pieces (SURVEY.md §8(e))."""
-        import torch
+    def dirty_ptr(self):
+        """Device address of the ctx-owned dirty-tet list of the last update_partial."""
+        return getattr(self, "_dirty_ptr", None)
+
+    def download_tets(self, tet_list, n: int, out: dict, id_map=None):
+        """Candidate + piece segments of the ctx's tets ``tet_list`` (a device address or an
+        array of local ids) as one CSR over the list into the destinations ``out`` (numpy or
+        torch, keyed like download_cands / download_pieces, plus ``tet_ids`` for the global
+        ids ``id_map[tet_list]``); returns the sizes (n_cand, n_pieces, n_inc)."""
+        keep = []
+        if isinstance(tet_list, int) or tet_list is None:
+            pl = tet_list
+        else:
+            pl, kl = _ptr(tet_list, np.int32)
+            keep.append(kl)
+        pm = None
+        if id_map is not None:
+            pm, km = _ptr(id_map, np.int32)
+            keep.append(km)
+        cs = _Csr()
+        for k in CSR_KEYS:
+            if k in out:
+                setattr(cs, k, self._p(out[k]))
+        ids = out.get("tet_ids")
+        self._check(self.L.rpd_download_tets(self.h, pl, int(n), pm,
+                                             self._p(ids) if ids is not None else None,
+                                             C.byref(cs)))
+        return cs.n_cand, cs.n_pieces, cs.n_inc
+
+    def _shards(self, shards, T, tet_ids=None):
         world = len(shards)
         if world > MAX_RANKS:
             raise ValueError("too many ranks")
         sh = _Shards()
         sh.world, sh.T = world, int(T)
         keep = []
-        for r, (d, ids) in enumerate(zip(shards, tet_ids)):
+        for r, d in enumerate(shards):
+            ids = d["tet_ids"] if tet_ids is None else tet_ids[r]
             sh.n_tets[r] = int(ids.numel())
-            for k in ("piece_off", "piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
-                      "inc_off", "inc_sphere"):
-                t = d[k].contiguous()
+            for k in SHARD_KEYS:
+                t = ids if k == "tet_ids" else d.get(k)
+                if t is None:
+                    continue
+                t = t.contiguous()
                 keep.append(t)
                 getattr(sh, k)[r] = t.data_ptr() if t.numel() else None
-            ids = ids.to(torch.int32).contiguous()
-            keep.append(ids)
-            sh.tet_ids[r] = ids.data_ptr() if ids.numel() else None
+        return sh, keep
+
+    def gather_all(self, shards, tet_ids, T: int, n_cand: int, n_pieces: int,
+                   n_inc: int) -> dict:
+        """Global candidate + piece CSRs (torch CUDA tensors) from the per-rank CSRs
+        ``shards`` (dicts of CUDA tensors, e.g. views of the all-gathered payload) of the
+        ranks' tets ``tet_ids`` (global ids): rpd_gather_cands + rpd_gather_pieces."""
+        import torch
+        sh, keep = self._shards(shards, T, tet_ids)
+        dev = torch.device("cuda", self.device)
+        e = lambda n, dt: torch.empty(max(n, 0), dtype=dt, device=dev)
+        out = {"cand_off": e(T + 1, torch.int32), "cand_idx": e(n_cand, torch.int32),
+               "piece_off": e(T + 1, torch.int32), "piece_sphere": e(n_pieces, torch.int32),
+               "piece_vol": e(n_pieces, torch.float64),
+               "piece_m1": e(3 * n_pieces, torch.float64).reshape(-1, 3),
+               "piece_facemask": e(n_pieces, torch.uint8), "inc_off": e(n_pieces + 1, torch.int32),
+               "inc_sphere": e(n_inc, torch.int32)}
+        self._check(self.L.rpd_gather_cands(self.h, C.byref(sh), self._p(out["cand_off"]),
+                                            self._p(out["cand_idx"])))
+        self._check(self.L.rpd_gather_pieces(self.h, C.byref(sh), *[
+            self._p(out[k]) for k in ("piece_off", "piece_sphere", "piece_vol", "piece_m1",
+                                      "piece_facemask", "inc_off", "inc_sphere")]))
+        return out
+
+    def merge_shards(self, shards, glob: dict, T: int) -> dict:
+        """Partial-mode merge (rpd_merge_shards): the global CSR ``glob`` with the dirty rows
+        replaced by the shards' segments (each shard dict holds ``tet_ids``, the global ids
+        of its dirty tets, and their candidate + piece CSRs).  Returns torch tensors viewing
+        the ctx-owned result (valid until the next-but-one merge)."""
+        sh, keep = self._shards(shards, T)
+        old = _Csr()
+        for k in CSR_KEYS:
+            setattr(old, k, self._p(glob[k]))
+        old.T = int(T)
+        res = _Csr()
+        self._check(self.L.rpd_merge_shards(self.h, C.byref(sh), C.byref(old), C.byref(res)))
+        spec = {"cand_off": (T + 1, "<i4"), "cand_idx": (res.n_cand, "<i4"),
+                "piece_off": (T + 1, "<i4"), "piece_sphere": (res.n_pieces, "<i4"),
+                "piece_vol": (res.n_pieces, "<f8"), "piece_m1": (3 * res.n_pieces, "<f8"),
+                "piece_facemask": (res.n_pieces, "|u1"), "inc_off": (res.n_pieces + 1, "<i4"),
+                "inc_sphere": (res.n_inc, "<i4")}
+        out = {k: _device_view(getattr(res, k), n, ts) for k, (n, ts) in spec.items()}
+        out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
+        return out
+
+    def gather_pieces(self, shards, tet_ids, T: int) -> dict:
+        """Global piece CSR (torch CUDA tensors) from per-rank piece CSRs (``shards``: one dict
+        per rank of CUDA tensors piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask,
+        inc_off, inc_sphere; ``tet_ids``: per rank the CUDA int32 global ids of its tets), put
+        in global tet order by rpd_gather_pieces (SURVEY.md §8(e))."""
+        import torch
+        tet_ids = [ids.to(torch.int32) for ids in tet_ids]
+        shards = [{k: v for k, v in d.items() if not k.startswith("cand")} for d in shards]
+        sh, keep = self._shards(shards, T, tet_ids)
         npc = sum(int(d["piece_sphere"].numel()) for d in shards)
         ninc = sum(int(d["inc_sphere"].numel()) for d in shards)
         dev = shards[0]["piece_vol"].device
@@ -468,6 +560,23 @@ class RPDContext:
         except ImportError:
             pass
         return a.ctypes.data if a.size else None
+
+
+class _View:
+    """__cuda_array_interface__ over a device array owned by librpd (no copy)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (ptr or 0, False), "version": 3,
+                                         "stream": None}
+
+
+def _device_view(ptr, n, typestr):
+    import torch
+    if n <= 0 or not ptr:
+        tdt = {"<i4": torch.int32, "<f8": torch.float64, "|u1": torch.uint8}[typestr]
+        return torch.zeros(0, dtype=tdt, device="cuda")
+    return torch.as_tensor(_View(ptr, n, typestr), device="cuda")
 
 
 def rpd_full(verts, tets, spheres, nbr_off, nbr_idx, ctx: RPDContext = None, **kw):

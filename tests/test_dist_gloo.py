@@ -1,8 +1,9 @@
-"""Multi-rank path on CPU (gloo, world_size 2): block-cyclic tet shards of the oracle's
-results all-gathered (dist.all_gather_pieces, the collective of the gather) and reordered
-equal the single-rank result byte for byte.  The CUDA kernels are
-per-tet independent, so the same holds on NCCL; the reorder kernel (rpd_gather_pieces) is
-tested against a single-GPU run in tests/test_gpu_gather.py."""
+"""Multi-rank path on CPU (gloo, world_size 2), started through bench.py's launcher: block-cyclic
+tet shards of the oracle's results exchanged by dist.exchange (the collective of the gather:
+counts all-gather + padded payload all-gather) and reordered equal the single-rank result byte
+for byte, also for the dirty-segment exchange of partial updates.  The
+CUDA reorder / merge kernels (rpd_gather_*, rpd_merge_shards) are tested against the oracle in
+tests/test_gpu_gather.py."""
 import os
 import socket
 
@@ -24,72 +25,49 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from paper_2403_18761_b200.dist import all_gather_pieces, shard_tets
-        w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
-        ids = shard_tets(w.T, world, rank, block=256)
-        r = oracle.rpd_workload(w, tet_ids=ids)
-        local = {k: torch.as_tensor(np.asarray(v)) for k, v in r.items() if k != "stats"}
-        local["piece_m1"] = local["piece_m1"].reshape(-1, 3)
-        shards = all_gather_pieces(local)
-        if rank == 0:
-            q.put(_reorder([{k: v.numpy() for k, v in d.items()} for d in shards],
-                           [shard_tets(w.T, world, s, block=256) for s in range(world)], w.T))
-    finally:
-        dist.destroy_process_group()
-
-
 def _reorder(shards, ids, T):
     """Test-side reorder of all-gathered per-rank CSRs into global tet order (the product path
-    does this in rpd_gather_pieces, tested against the single-GPU result in -m gpu)."""
-    per_tet = [None] * T
+    does this in rpd_gather_cands / rpd_gather_pieces, tested against the oracle in -m gpu)."""
+    L = [None] * T
     for d, tid in zip(shards, ids):
-        po, io = d["piece_off"], d["inc_off"]
-        for a, t in enumerate(tid):
-            pcs = []
-            for p in range(po[a], po[a + 1]):
-                pcs.append((d["piece_sphere"][p], d["piece_vol"][p], tuple(d["piece_m1"][p]),
-                            d["piece_facemask"][p], list(d["inc_sphere"][io[p]:io[p + 1]])))
-            per_tet[t] = pcs
-    out = {k: [] for k in ("piece_sphere", "piece_vol", "piece_m1", "piece_facemask",
-                           "inc_sphere")}
-    off, ioff = [0], [0]
-    for pcs in per_tet:
-        for (s, v, m, f, inc) in pcs:
-            out["piece_sphere"].append(s)
-            out["piece_vol"].append(v)
-            out["piece_m1"].append(m)
-            out["piece_facemask"].append(f)
-            out["inc_sphere"] += inc
-            ioff.append(len(out["inc_sphere"]))
-        off.append(len(out["piece_sphere"]))
-    out = {k: np.array(v) for k, v in out.items()}
-    out["piece_off"], out["inc_off"] = np.array(off, np.int32), np.array(ioff, np.int32)
-    return out
+        for a, row in enumerate(oracle.per_tet_lists(d, len(tid))):
+            L[int(tid[a])] = row
+    return oracle.from_per_tet_lists(L)
 
 
-def test_gather_equals_single_rank():
-    world = 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
+def test_launcher_two_gloo_ranks(tmp_path):
+    """bench.py's launcher (dist.launch_ranks: torch.distributed.run, 127.0.0.1) starts 2 gloo
+    ranks; through dist.exchange (one counts all-gather + one padded payload all-gather per
+    exchange) every rank receives every shard, and the shards reordered into global tet order
+    equal the single-rank oracle -- for the full RPD and, after each partial update, with only
+    the dirty segments (and their global ids) exchanged and merged."""
+    import pickle
+    from paper_2403_18761_b200.dist import launch_ranks, shard_tets
+    out = tmp_path / "rounds.pkl"
+    rc = launch_ranks(2, os.path.join(os.path.dirname(__file__), "dist_worker.py"), [str(out)])
+    assert rc == 0
+    rounds = pickle.load(open(out, "rb"))
+    w = W.make_shape_workload("G", 3000, 200, seed=12, n_batches=2, batch_m=12, clusters=3,
+                              cache=False)
+    ids = [shard_tets(w.T, 2, r, block=256) for r in range(2)]
     ref = oracle.rpd_workload(w)
-    for k in ("piece_off", "piece_sphere", "piece_vol", "piece_facemask", "inc_off",
-              "inc_sphere"):
+    got = _reorder(rounds[0]["full"], ids, w.T)
+    for k in got:
         assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), k
-    assert np.array_equal(got["piece_m1"].reshape(-1, 3), ref["piece_m1"])
+    n_old = w.N
+    for rd, (sph, off, idx) in zip(rounds[1:], w.batches):
+        ref, dirty = oracle.partial_update(ref, w.verts, w.tets, sph, off, idx, n_old)
+        shards = rd["dirty"]
+        gids = np.concatenate([s["tet_ids"] for s in shards])
+        assert np.array_equal(np.sort(gids), dirty)
+        L = oracle.per_tet_lists(got, w.T)
+        for s in shards:
+            for a, row in enumerate(oracle.per_tet_lists(s, len(s["tet_ids"]))):
+                L[int(s["tet_ids"][a])] = row
+        got = oracle.from_per_tet_lists(L)
+        for k in got:
+            assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), k
+        n_old = len(sph)
 
 
 def test_shards_partition_the_tets():

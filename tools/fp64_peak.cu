@@ -17,7 +17,7 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   double* out; cudaMalloc(&out, 8);
-  int iters = 1 << 16, blocks = sms * 8, threads = 256;
+  int iters = 1 << 20, blocks = sms * 8, threads = 256;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   k<<<blocks, threads>>>(out, 1024, 0.999999, 1e-7);
   double best = 0;
