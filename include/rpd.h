@@ -107,10 +107,16 @@ rpd_status rpd_relations(rpd_ctx* ctx, const double* verts, int64_t V, const int
                          const int32_t* nbr_idx, int64_t E, const int32_t** cand_off,
                          const int32_t** cand_idx, int64_t* n_cand);
 
-/* Pieces of the RPD restricted to the ctx's tets (device arrays owned by ctx). */
+/* Pieces of the RPD restricted to the ctx's tets (device arrays owned by ctx).
+ * Layout: a pool of n_slots piece slots; tet t's pieces are the slots
+ * [piece_rows[2t], piece_rows[2t+1]), ascending sphere id, and piece p's incidences are
+ * inc_sphere[inc_off[p], inc_off[p+1]).  After rpd_clip the pool is a plain CSR (piece_off,
+ * n_slots == n_pieces); a partial update appends the dirty tets' new pieces at the pool's
+ * tail and re-points their rows -- clean tets are never copied -- and piece_off is NULL
+ * until the next rpd_clip (rpd_download_pieces always writes a plain CSR). */
 typedef struct {
   const int32_t* piece_off;      /* [T+1] pieces of tet t: [piece_off[t], piece_off[t+1]),
-                                    ascending sphere id */
+                                    ascending sphere id; NULL after a partial update */
   const int32_t* piece_sphere;   /* [n_pieces] owning sphere i */
   const double* piece_vol;       /* [n_pieces] volume of P(t,i) > 0 */
   const double* piece_m1;        /* [n_pieces][3] first moment = vol * centroid */
@@ -120,7 +126,9 @@ typedef struct {
   const int32_t* inc_sphere;     /* neighbour ids j whose radical plane holds a positive-area
                                     2-face of the piece, ascending; coincident sources all
                                     listed (R7) */
-  int64_t n_pieces, n_inc;       /* host values */
+  int64_t n_pieces, n_inc;       /* host values: live pieces and incidences */
+  const int32_t* piece_rows;     /* [T][2] the slots of every tet's pieces (always valid) */
+  int64_t n_slots;               /* pool slots in use (live + replaced) */
 } rpd_pieces;
 
 /* Step 2 -- clip every candidate of the last rpd_relations:

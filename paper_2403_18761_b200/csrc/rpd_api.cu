@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -90,12 +91,14 @@ struct Readback {
   int32_t i32[8];
   unsigned long long u64[ST_N];
   int32_t err[4];
+  unsigned long long u4[4];
 };
 
 struct RbSpec {
   const int32_t* i32[8];           // nullptr -> 0
   const unsigned long long* u64;   // stats (ST_N words) or nullptr (kept)
   const int* err;                  // error word (4) or nullptr (kept)
+  const unsigned long long* u4 = nullptr;  // 4 more u64 words or nullptr (kept)
 };
 
 __global__ void k_readback(RbSpec s, Readback* rb) {
@@ -103,6 +106,7 @@ __global__ void k_readback(RbSpec s, Readback* rb) {
   if (t < 8) rb->i32[t] = s.i32[t] ? *s.i32[t] : 0;
   if (s.u64 && t < ST_N) rb->u64[t] = s.u64[t];
   if (s.err && t < 4) rb->err[t] = s.err[t];
+  if (s.u4 && t < 4) rb->u4[t] = s.u4[t];
   __threadfence_system();
 }
 
@@ -122,6 +126,9 @@ rpd_status check_err(rpd_ctx* c, const Readback* rb) {
 }
 
 }  // namespace
+
+static rpd_status download_rows(rpd_ctx* c, int kind, const int32_t* d_list, int64_t n,
+                                rpd_csr* out);
 
 extern "C" {
 
@@ -309,8 +316,15 @@ struct Restrict {
   const CandSet* old;
 };
 
+static rpd_status reserve_pools(rpd_ctx* c, int64_t add_c, int64_t add_p, int64_t add_i,
+                                int64_t add_r);
+
+// Alg. 1 + compaction of tets (tet_ids, or all) into the candidate set cs.  append: cs is
+// the batch of a partial update whose candidates go to the tail of the state pool (which
+// is first made large enough for them and for the batch's pieces).
 static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int lo,
-                             int hi, CandSet& cs, bool timed, const Restrict* rs = nullptr) {
+                             int hi, CandSet& cs, bool timed, const Restrict* rs = nullptr,
+                             bool append = false) {
   Readback* rb = (Readback*)c->pinned;
   size_t nt = n_tets > 0 ? n_tets : 1;
   CK(c->k_tet.ensure(sizeof(int32_t) * nt), "alloc");
@@ -376,11 +390,22 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   cs.n = nc;
   cs.n_tets = n_tets;
   cs.n_words = rb->i32[1];
-  CK(cs.idx.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
+  cs.idx_ext = nullptr;
+  if (append) {
+    // the batch's candidates, and (upper bounds) its pieces, incidences and radical facets
+    const int64_t nw32 = 32 * cs.n_words;
+    rpd_status s = reserve_pools(c, nc, nc, nw32, c->euler ? nw32 : 0);
+    if (s) return s;
+    CandSet& pool = c->cand[c->cur];
+    cs.idx_ext = pool.idx.as<int32_t>() + pool.fill;
+  } else {
+    // the state pool: room for the appends of later partial updates
+    CK(cs.idx.ensure_slack(sizeof(int32_t) * (nc > 0 ? nc : 1), 2), "alloc");
+  }
   CK(cs.pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
   CK(cs.moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
   CK(launch_compact_cands(c, n_tets, c->slab_cap, c->k_tet.as<int32_t>(), c->slab.as<int32_t>(),
-                          cs.off.as<int32_t>(), cs.idx.as<int32_t>(), cs.pair_tet.as<int32_t>(),
+                          cs.off.as<int32_t>(), cs.idxp(), cs.pair_tet.as<int32_t>(),
                           c->w_off.as<int32_t>(), cs.moff.as<int32_t>(), nc), "compact");
   c->last.max_k_tet = (int32_t)rb->u64[ST_MAXK];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
@@ -415,6 +440,8 @@ static void absorb_clip_stats(rpd_ctx* c, const Readback* rb, int n_wide) {
 // deferred: no host round trip; the piece set is sized by upper bounds (one piece per pair,
 // 32 incidences per mask word) and ps.n_pieces / ps.n_inc hold those bounds until the caller
 // reads the exact totals (p_scan[n], i_scan[n]), the overflow counter and the clip stats.
+// deferred (partial updates): ps is the batch -- only its per-tet CSR offsets (ps.off) are
+// its own, the pieces go to the tail of the state pool (reserved by run_filter's append).
 static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids,
                            PieceSet& ps, bool deferred = false) {
   const int64_t n = cs.n, nt = cs.n_tets;
@@ -454,11 +481,11 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
                      sizeof(unsigned long long) * 8, c->stream), "memset");
   if (c->profile) cudaEventRecord(c->ev[2], c->stream);
-  CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff,
-                 c->clip_wide), "clip");
+  CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff, c->clip_wide),
+     "clip");
   tmark(c, "clip-fast");
   if (!c->clip_wide && n > 0)
-    CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idx.as<int32_t>(), moff),
+    CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff),
        "clip (wide)");
   tmark(c, "clip-wide");
   if (c->profile) cudaEventRecord(c->ev[3], c->stream);
@@ -485,29 +512,48 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
       fprintf(stderr, "[rpd clip] pairs %lld overflow 16->32 %d 32->128 %d maxv %d maxp %d\n",
               (long long)n, rb->i32[2], rb->i32[3], c->last.max_vertices, c->last.max_planes);
   }
-  const size_t npp = np > 0 ? np : 1;
   CK(ps.off.ensure(sizeof(int32_t) * (nt + 1)), "alloc");
-  CK(ps.sphere.ensure(sizeof(int32_t) * npp), "alloc");
-  CK(ps.vol.ensure(sizeof(double) * npp), "alloc");
-  CK(ps.m1.ensure(sizeof(double) * 3 * npp), "alloc");
-  CK(ps.fm.ensure(npp), "alloc");
-  CK(ps.inc_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
-  CK(ps.inc.ensure(sizeof(int32_t) * (ni > 0 ? ni : 1)), "alloc");
-  if (c->euler) {
-    CK(ps.eu.ensure(sizeof(long long) * npp), "alloc");
-    CK(ps.rpf_off.ensure(sizeof(int32_t) * (np + 1)), "alloc");
-    CK(ps.rpf_j.ensure(sizeof(int32_t) * (nr > 0 ? nr : 1)), "alloc");
-    CK(ps.rpf_e.ensure(sizeof(long long) * (nr > 0 ? nr : 1)), "alloc");
-    CK(ps.sfm.ensure(npp), "alloc");
-    CK(ps.rfm.ensure(nr > 0 ? nr : 1), "alloc");
-    CK(ps.radj.ensure(sizeof(unsigned long long) * (nr > 0 ? nr : 1)), "alloc");
+  // the destination: the state's own arrays (full clip; slack for later appends) or the tail
+  // of the state pool (a partial update's batch)
+  PieceSet& dst = deferred ? c->pcs[c->cur] : ps;
+  const int64_t P0 = deferred ? dst.fill_p : 0, I0 = deferred ? dst.fill_i : 0,
+                R0 = deferred ? dst.fill_r : 0;
+  if (!deferred) {
+    const size_t npp = np > 0 ? np : 1;
+    CK(ps.sphere.ensure_slack(sizeof(int32_t) * npp, 2), "alloc");
+    CK(ps.vol.ensure_slack(sizeof(double) * npp, 2), "alloc");
+    CK(ps.m1.ensure_slack(sizeof(double) * 3 * npp, 2), "alloc");
+    CK(ps.fm.ensure_slack(npp, 2), "alloc");
+    CK(ps.inc_off.ensure_slack(sizeof(int32_t) * (np + 1), 2), "alloc");
+    CK(ps.inc.ensure_slack(sizeof(int32_t) * (ni > 0 ? ni : 1), 2), "alloc");
+    if (c->euler) {
+      const size_t nrr = nr > 0 ? nr : 1;
+      CK(ps.eu.ensure_slack(sizeof(long long) * npp, 2), "alloc");
+      CK(ps.rpf_off.ensure_slack(sizeof(int32_t) * (np + 1), 2), "alloc");
+      CK(ps.rpf_j.ensure_slack(sizeof(int32_t) * nrr, 2), "alloc");
+      CK(ps.rpf_e.ensure_slack(sizeof(long long) * nrr, 2), "alloc");
+      CK(ps.sfm.ensure_slack(npp, 2), "alloc");
+      CK(ps.rfm.ensure_slack(nrr, 2), "alloc");
+      CK(ps.radj.ensure_slack(sizeof(unsigned long long) * nrr, 2), "alloc");
+    }
   }
-  PieceDst d{ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.vol.as<double>(),
-             ps.m1.as<double>(),  ps.fm.as<uint8_t>(),     ps.inc_off.as<int32_t>(),
-             ps.inc.as<int32_t>(), ps.eu.as<long long>(),  ps.rpf_off.as<int32_t>(),
-             ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
-             ps.rfm.as<uint8_t>(), ps.radj.as<unsigned long long>()};
-  CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idx.as<int32_t>(), moff, d),
+  PieceDst d{ps.off.as<int32_t>(),
+             dst.sphere.as<int32_t>() + P0,
+             dst.vol.as<double>() + P0,
+             dst.m1.as<double>() + 3 * P0,
+             dst.fm.as<uint8_t>() + P0,
+             dst.inc_off.as<int32_t>() + P0,
+             dst.inc.as<int32_t>() + I0,
+             c->euler ? dst.eu.as<long long>() + P0 : nullptr,
+             c->euler ? dst.rpf_off.as<int32_t>() + P0 : nullptr,
+             c->euler ? dst.rpf_j.as<int32_t>() + R0 : nullptr,
+             c->euler ? dst.rpf_e.as<long long>() + R0 : nullptr,
+             c->euler ? dst.sfm.as<uint8_t>() + P0 : nullptr,
+             c->euler ? dst.rfm.as<uint8_t>() + R0 : nullptr,
+             c->euler ? dst.radj.as<unsigned long long>() + R0 : nullptr,
+             (int32_t)I0,
+             (int32_t)R0};
+  CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idxp(), moff, d),
      "compact pieces");
   ps.n_tets = nt;
   ps.n_pieces = np;
@@ -524,6 +570,98 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   return RPD_OK;
 }
 
+// Compaction (garbage collection) of the state pools: every tet's live segments gathered by
+// its rows into the other buffer set as plain CSRs (pair_tet / moff of the candidates rebuilt),
+// with room for `extra` appended entries of each kind; then that set is the state.
+static rpd_status compact_state(rpd_ctx* c, int64_t extra) {
+  if (c->compact) return RPD_OK;
+  const int64_t T = c->st.T;
+  CandSet& co = c->cand[c->cur];
+  PieceSet& po = c->pcs[c->cur];
+  CandSet& cn = c->cand[c->cur ^ 1];
+  PieceSet& pn = c->pcs[c->cur ^ 1];
+  CK(c->m_cnt.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1) + 64), "alloc");
+  CK(c->m_off.ensure(sizeof(int32_t) * 3 * (T + 1)), "alloc");
+  CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
+  CK(launch_compact_state(c, T, co, po, cn, pn, 0), "compact counts");
+  Readback* rb = (Readback*)c->pinned;
+  const int32_t* m_off = c->m_off.as<int32_t>();
+  CK(readback(c, RbSpec{{cn.off.as<int32_t>() + T, pn.off.as<int32_t>() + T, m_off + T,
+                         c->euler ? m_off + 2 * (T + 1) + T : nullptr},
+                        nullptr, nullptr}),
+     "readback");
+  CK(cudaStreamSynchronize(c->stream), "compact");
+  const int64_t nc = rb->i32[0], np = rb->i32[1], ni = rb->i32[2], nr = rb->i32[3];
+  auto room = [&](int64_t n) { return (size_t)((n + extra) + (n + extra) / 2 + 1); };
+  CK(cn.idx.ensure(sizeof(int32_t) * room(nc)), "alloc");
+  CK(cn.pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
+  CK(cn.moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
+  CK(pn.sphere.ensure(sizeof(int32_t) * room(np)), "alloc");
+  CK(pn.vol.ensure(sizeof(double) * room(np)), "alloc");
+  CK(pn.m1.ensure(sizeof(double) * 3 * room(np)), "alloc");
+  CK(pn.fm.ensure(room(np)), "alloc");
+  CK(pn.inc_off.ensure(sizeof(int32_t) * (room(np) + 1)), "alloc");
+  CK(pn.inc.ensure(sizeof(int32_t) * room(ni)), "alloc");
+  if (c->euler) {
+    CK(pn.eu.ensure(sizeof(long long) * room(np)), "alloc");
+    CK(pn.rpf_off.ensure(sizeof(int32_t) * (room(np) + 1)), "alloc");
+    CK(pn.rpf_j.ensure(sizeof(int32_t) * room(nr)), "alloc");
+    CK(pn.rpf_e.ensure(sizeof(long long) * room(nr)), "alloc");
+    CK(pn.sfm.ensure(room(np)), "alloc");
+    CK(pn.rfm.ensure(room(nr)), "alloc");
+    CK(pn.radj.ensure(sizeof(unsigned long long) * room(nr)), "alloc");
+  }
+  CK(c->m_cnt.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1) + sizeof(int32_t) * (nc + 1) + 64),
+     "alloc");
+  cn.n = nc;
+  CK(launch_compact_state(c, T, co, po, cn, pn, 1), "compact copy");
+  CK(launch_rows_from_off(c, T, &cn, &pn, &cn), "rows");
+  CK(readback(c, RbSpec{{cn.moff.as<int32_t>() + nc}, nullptr, nullptr}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "compact");
+  cn.n_tets = T;
+  cn.n_words = rb->i32[0];
+  cn.fill = nc;
+  cn.idx_ext = nullptr;
+  pn.n_tets = T;
+  pn.n_pieces = np;
+  pn.n_inc = ni;
+  pn.n_rpf = c->euler ? nr : 0;
+  pn.fill_p = np;
+  pn.fill_i = ni;
+  pn.fill_r = pn.n_rpf;
+  c->cur ^= 1;
+  c->compact = true;
+  ++c->n_compactions;
+  return RPD_OK;
+}
+
+// make room at the pools' tails for a batch of add_* entries (compacting when they are full)
+static rpd_status reserve_pools(rpd_ctx* c, int64_t add_c, int64_t add_p, int64_t add_i,
+                                int64_t add_r) {
+  const CandSet& pc = c->cand[c->cur];
+  const PieceSet& pp = c->pcs[c->cur];
+  const bool fits =
+      (pc.fill + add_c) * sizeof(int32_t) <= pc.idx.cap &&
+      (pp.fill_p + add_p) * sizeof(double) * 3 <= pp.m1.cap &&
+      (pp.fill_p + add_p + 1) * sizeof(int32_t) <= pp.inc_off.cap &&
+      (pp.fill_p + add_p) * sizeof(int32_t) <= pp.sphere.cap &&
+      (pp.fill_p + add_p) * sizeof(double) <= pp.vol.cap && pp.fill_p + add_p <= (int64_t)pp.fm.cap &&
+      (pp.fill_i + add_i) * sizeof(int32_t) <= pp.inc.cap &&
+      (!c->euler ||
+       ((pp.fill_p + add_p) * sizeof(long long) <= pp.eu.cap &&
+        (pp.fill_p + add_p + 1) * sizeof(int32_t) <= pp.rpf_off.cap &&
+        pp.fill_p + add_p <= (int64_t)pp.sfm.cap &&
+        (pp.fill_r + add_r) * sizeof(int32_t) <= pp.rpf_j.cap &&
+        (pp.fill_r + add_r) * sizeof(long long) <= pp.rpf_e.cap &&
+        pp.fill_r + add_r <= (int64_t)pp.rfm.cap &&
+        (pp.fill_r + add_r) * sizeof(unsigned long long) <= pp.radj.cap));
+  if (fits) return RPD_OK;
+  c->compact = false;  // (force: a compact pool without room is re-laid out with room)
+  const int64_t extra = std::max(std::max(add_c, add_p), std::max(add_i, add_r));
+  return compact_state(c, extra);
+}
+
 static void reset_last(rpd_ctx* c) {
   c->last = rpd_stats{};
   c->last.T = c->st.T;
@@ -532,7 +670,9 @@ static void reset_last(rpd_ctx* c) {
 
 static rpd_status fill_pieces(rpd_ctx* c, rpd_pieces* out) {
   const PieceSet& ps = c->pcs[c->cur];
-  out->piece_off = ps.off.as<int32_t>();
+  out->piece_off = c->compact ? ps.off.as<int32_t>() : nullptr;
+  out->piece_rows = ps.rows.as<int32_t>();
+  out->n_slots = ps.fill_p;
   out->piece_sphere = ps.sphere.as<int32_t>();
   out->piece_vol = ps.vol.as<double>();
   out->piece_m1 = ps.m1.as<double>();
@@ -576,6 +716,9 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   CandSet& cs = c->cand[0];
   s = run_filter(c, nullptr, T, 0, (int)N, cs, true);
   if (s) return s;
+  CK(launch_rows_from_off(c, T, &cs, nullptr, &cs), "rows");
+  cs.fill = cs.n;
+  c->compact = true;
   c->have_rel = true;
   c->last.n_cand = cs.n;
   c->last.pairs_filtered = T * N;
@@ -589,11 +732,19 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   if (!c || !out) return fail(c, RPD_EINVAL, "rpd_clip: bad argument");
   if (!c->have_rel) return fail(c, RPD_ESTATE, "rpd_clip before rpd_relations");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
+  // after partial updates the candidate pool is re-laid out as a plain CSR first
+  rpd_status s = compact_state(c, 0);
+  if (s) return s;
   CandSet& cs = c->cand[c->cur];
   c->last.clip_ms = 0.0;
   c->eu_valid = false;
-  rpd_status s = run_clip(c, cs, nullptr, c->pcs[c->cur]);
+  PieceSet& ps = c->pcs[c->cur];
+  s = run_clip(c, cs, nullptr, ps);
   if (s) return s;
+  CK(launch_rows_from_off(c, c->st.T, nullptr, &ps, nullptr), "rows");
+  ps.fill_p = ps.n_pieces;
+  ps.fill_i = ps.n_inc;
+  ps.fill_r = ps.n_rpf;
   c->have_pieces = true;
   c->eu_valid = c->euler != 0;
   c->last.n_pieces = c->pcs[c->cur].n_pieces;
@@ -715,66 +866,37 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
   }
   const int32_t* dl = c->d_list.as<int32_t>();
 
-  // (2) re-candidate the dirty tets against all spheres, (3) clip them
+  // (2) re-candidate the dirty tets against all spheres -- their new candidate lists go to the
+  // tail of the state pool --, (3) clip them, their pieces also appended to the pool
+  CandSet& cd = c->cand_d;
+  PieceSet& pd = c->pcs_d;
   if (c->filter_mode == RPD_FILTER_PRUNED) {
     Restrict rs{c->c_list.as<int32_t>(), c->c_scan.as<int>() + N_new, (int)N_new,
                 &c->cand[c->cur]};
-    s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true, &rs);
+    s = run_filter(c, dl, nd, 0, (int)N_new, cd, true, &rs, /*append=*/true);
   } else {
-    s = run_filter(c, dl, nd, 0, (int)N_new, c->cand_d, true);
+    s = run_filter(c, dl, nd, 0, (int)N_new, cd, true, nullptr, /*append=*/true);
   }
   if (s) return s;
   tmark(c, "filter-sync");
-  s = run_clip(c, c->cand_d, dl, c->pcs_d, /*deferred=*/true);
+  // (the pools may have been compacted by the reservation: take them after it)
+  CandSet& pool_c = c->cand[c->cur];
+  PieceSet& pool_p = c->pcs[c->cur];
+  const int64_t cbase = pool_c.fill, pbase = pool_p.fill_p;
+  s = run_clip(c, cd, dl, pd, /*deferred=*/true);
   if (s) return s;
   tmark(c, "clip-launched");
 
-  // (4) merge clean old tets + dirty new tets into the other buffer set.  Sized by host upper
-  // bounds; the exact totals, the clip overflow counter and the stats come back in one
-  // readback at the end (the only host round trip after the re-filter).
-  const int nxt = c->cur ^ 1;
-  CandSet& co = c->cand[c->cur];
-  PieceSet& po = c->pcs[c->cur];
-  CandSet& cd = c->cand_d;
-  PieceSet& pd = c->pcs_d;
-  CandSet& cn = c->cand[nxt];
-  PieceSet& pn = c->pcs[nxt];
-  CK(c->m_cnt.ensure(sizeof(int32_t) * 5 * (T > 0 ? T : 1)), "alloc");
-  CK(c->m_off.ensure(sizeof(int32_t) * 3 * (T + 1)), "alloc");
-  CK(cn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  CK(pn.off.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  cn.n = co.n + cd.n;
-  pn.n_pieces = po.n_pieces + pd.n_pieces;
-  pn.n_inc = po.n_inc + pd.n_inc;
-  const size_t ncn = cn.n > 0 ? cn.n : 1, npn = pn.n_pieces > 0 ? pn.n_pieces : 1;
-  CK(cn.idx.ensure(sizeof(int32_t) * ncn), "alloc");
-  CK(cn.pair_tet.ensure(sizeof(int32_t) * ncn), "alloc");
-  CK(cn.moff.ensure(sizeof(int32_t) * (cn.n + 1)), "alloc");
-  CK(pn.sphere.ensure(sizeof(int32_t) * npn), "alloc");
-  CK(pn.vol.ensure(sizeof(double) * npn), "alloc");
-  CK(pn.m1.ensure(sizeof(double) * 3 * npn), "alloc");
-  CK(pn.fm.ensure(npn), "alloc");
-  CK(pn.inc_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
-  CK(pn.inc.ensure(sizeof(int32_t) * (pn.n_inc > 0 ? pn.n_inc : 1)), "alloc");
-  if (c->euler) {
-    pn.n_rpf = po.n_rpf + pd.n_rpf;
-    CK(pn.eu.ensure(sizeof(long long) * npn), "alloc");
-    CK(pn.rpf_off.ensure(sizeof(int32_t) * (pn.n_pieces + 1)), "alloc");
-    CK(pn.rpf_j.ensure(sizeof(int32_t) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
-    CK(pn.rpf_e.ensure(sizeof(long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
-    CK(pn.sfm.ensure(npn), "alloc");
-    CK(pn.rfm.ensure(pn.n_rpf > 0 ? pn.n_rpf : 1), "alloc");
-    CK(pn.radj.ensure(sizeof(unsigned long long) * (pn.n_rpf > 0 ? pn.n_rpf : 1)), "alloc");
-  }
-  CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 0), "merge counts");
-  tmark(c, "merge-counts");
-  CK(launch_merge(c, T, co, po, cd, pd, cn, pn, 1), "merge copy");
-  const int32_t* m_off = c->m_off.as<int32_t>();
-  CK(readback(c, RbSpec{{cn.off.as<int32_t>() + T, pn.off.as<int32_t>() + T, m_off + T,
-                         m_off + (T + 1) + T, c->p_over.as<int32_t>(),
-                         c->p_scan.as<int32_t>() + cd.n, c->i_scan.as<int32_t>() + cd.n,
-                         c->euler ? m_off + 2 * (T + 1) + T : nullptr},
-                        c->stats.as<unsigned long long>(), nullptr}),
+  // (4) re-point the dirty tets' rows at the batch (clean tets are not touched); the batch
+  // totals, the removed segments' sizes, the overflow counter and the stats come back in one
+  // readback at the end (the only host round trip after the re-filter)
+  CK(c->m_cnt.ensure(sizeof(unsigned long long) * 4), "alloc");
+  unsigned long long* rm = c->m_cnt.as<unsigned long long>();
+  CK(launch_rows_update(c, dl, nd, pool_c, pool_p, cd, pd, cbase, pbase, rm), "rows");
+  CK(readback(c, RbSpec{{c->p_over.as<int32_t>(), c->p_scan.as<int32_t>() + cd.n,
+                         c->i_scan.as<int32_t>() + cd.n,
+                         c->euler ? c->r_scan.as<int32_t>() + cd.n : nullptr},
+                        c->stats.as<unsigned long long>(), nullptr, rm}),
      "readback");
   CK(cudaStreamSynchronize(c->stream), "partial update");
   tmark(c, "final-sync");
@@ -783,35 +905,40 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
     return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
   if (rb->u64[ST_EU_OVER])
     return fail(c, RPD_EOVERFLOW, "topology mode: a piece has more than 64 radical facets");
-  absorb_clip_stats(c, rb, rb->i32[4]);
+  absorb_clip_stats(c, rb, rb->i32[0]);
   if (c->profile) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
     c->last.clip_ms += ms;
   }
-  pd.n_pieces = rb->i32[5];
-  pd.n_inc = rb->i32[6];
+  const unsigned long long* removed = rb->u4;
+  pd.n_pieces = rb->i32[1];
+  pd.n_inc = rb->i32[2];
+  pd.n_rpf = c->euler ? rb->i32[3] : 0;
+  pd.n_tets = nd;
+  pool_c.fill += cd.n;
+  pool_p.fill_p += pd.n_pieces;
+  pool_p.fill_i += pd.n_inc;
+  pool_p.fill_r += pd.n_rpf;
+  pool_c.n += cd.n - (int64_t)removed[0];
+  pool_p.n_pieces += pd.n_pieces - (int64_t)removed[1];
+  pool_p.n_inc += pd.n_inc - (int64_t)removed[2];
+  pool_p.n_rpf += pd.n_rpf - (int64_t)removed[3];
+  c->compact = false;
   c->last.n_cand_dirty = cd.n;
   c->last.n_pieces_dirty = pd.n_pieces;
   c->last.n_inc_dirty = pd.n_inc;
-  cn.n = rb->i32[0];
-  cn.n_tets = T;
-  cn.n_words = rb->i32[3];
-  pn.n_pieces = rb->i32[1];
-  pn.n_inc = rb->i32[2];
-  pn.n_rpf = rb->i32[7];
-  pn.n_tets = T;
-  if (c->euler) {
-    CK(launch_euler_sums(c, pn), "euler sums");
-    pd.n_rpf = 0;
+  if (c->euler) {  // the Euler / topology consumers read plain CSRs
+    s = compact_state(c, 0);
+    if (s) return s;
+    CK(launch_euler_sums(c, c->pcs[c->cur]), "euler sums");
   }
-  c->cur = nxt;
   c->eu_valid = c->euler != 0;
   c->n_dirty = nd;
   c->last.n_dirty = nd;
-  c->last.n_cand = cn.n;
-  c->last.n_pieces = pn.n_pieces;
-  c->last.n_inc = pn.n_inc;
+  c->last.n_cand = c->cand[c->cur].n;
+  c->last.n_pieces = c->pcs[c->cur].n_pieces;
+  c->last.n_inc = c->pcs[c->cur].n_inc;
   c->last.pairs_filtered = T * M + nd * N_new;
   *dirty_tets = dl;
   *n_dirty = nd;
@@ -823,6 +950,13 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
                                int32_t* inc_off, int32_t* inc_sphere) {
   if (!c) return RPD_EINVAL;
   if (!c->have_pieces) return fail(c, RPD_ESTATE, "no pieces");
+  if (!c->compact) {  // the pools after partial updates: gathered by their rows
+    if (!piece_off) return fail(c, RPD_EINVAL, "rpd_download_pieces: piece_off is needed");
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    rpd_csr o{nullptr, nullptr, piece_off, piece_sphere, piece_vol, piece_m1, piece_facemask,
+              inc_off, inc_sphere, 0, 0, 0, 0};
+    return download_rows(c, 0, nullptr, c->st.T, &o);
+  }
   const PieceSet& ps = c->pcs[c->cur];
   const int64_t T = c->st.T, np = ps.n_pieces, ni = ps.n_inc;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
@@ -1104,12 +1238,80 @@ rpd_status rpd_gather_cands(rpd_ctx* c, const rpd_shards* sh, int32_t* cand_off,
 }
 
 static SegSrc state_source(rpd_ctx* c) {
-  const CandSet& cs = c->cand[c->cur];
-  const PieceSet& ps = c->pcs[c->cur];
-  return seg_src_csr(cs.off.as<int32_t>(), cs.idx.as<int32_t>(), ps.off.as<int32_t>(),
-                     ps.sphere.as<int32_t>(), ps.vol.as<double>(), ps.m1.as<double>(),
-                     ps.fm.as<uint8_t>(), ps.inc_off.as<int32_t>(), ps.inc.as<int32_t>());
+  SegSrc s = seg_src_state(c->cand[c->cur], c->pcs[c->cur]);
+  if (!c->have_pieces) {  // candidates only (after rpd_relations)
+    s.p_beg = s.p_end = nullptr;
+  }
+  return s;
 }
+
+}  // extern "C"
+
+// the segments of the state rows `list` (kind 1) or of all tets (kind 0, n = T) into the
+// caller's arrays (host destinations through device staging and one copy per array)
+static rpd_status download_rows(rpd_ctx* c, int kind, const int32_t* d_list, int64_t n,
+                                rpd_csr* out) {
+  SegSources S{};
+  S.s[0] = state_source(c);
+  const bool copy = out->cand_off || out->piece_off;
+  const bool host = (out->cand_off && is_host_ptr(out->cand_off)) ||
+                    (out->piece_off && is_host_ptr(out->piece_off));
+  SegDst D{out->cand_off, out->cand_idx, out->piece_off, out->piece_sphere, out->piece_vol,
+           out->piece_m1, out->piece_facemask, out->inc_off, out->inc_sphere, nullptr};
+  int64_t nc = 0, np = 0, ni = 0;
+  if (host) {
+    // sizes first (the staging is laid out from them), then the copy into the staging
+    rpd_status s = seg_run(c, kind, n, d_list, nullptr, c->st.T, S, SegDst{}, &nc, &np, &ni,
+                           false, no_ensure);
+    if (s) return s;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
+    const size_t o_co = take(4 * (n + 1)), o_ci = take(4 * nc), o_po = take(4 * (n + 1)),
+                 o_ps = take(4 * np), o_pv = take(8 * np), o_pm = take(24 * np),
+                 o_pf = take(np), o_io = take(4 * (np + 1)), o_is = take(4 * ni);
+    CK(c->g_dst.ensure(off), "alloc");
+    char* b = c->g_dst.as<char>();
+    SegDst Dd{};
+    if (out->cand_off)
+      Dd.cand_off = (int32_t*)(b + o_co), Dd.cand_idx = (int32_t*)(b + o_ci);
+    if (out->piece_off) {
+      Dd.piece_off = (int32_t*)(b + o_po);
+      Dd.piece_sphere = (int32_t*)(b + o_ps);
+      Dd.piece_vol = (double*)(b + o_pv);
+      Dd.piece_m1 = (double*)(b + o_pm);
+      Dd.piece_fm = (uint8_t*)(b + o_pf);
+      Dd.inc_off = (int32_t*)(b + o_io);
+      Dd.inc_sphere = (int32_t*)(b + o_is);
+    }
+    s = seg_run(c, kind, n, d_list, nullptr, c->st.T, S, Dd, &nc, &np, &ni, true, no_ensure);
+    if (s) return s;
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+      if (!dst || !src || bytes == 0) return cudaSuccess;
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+    };
+    CK(cp(out->cand_off, Dd.cand_off, 4 * (n + 1)), "download");
+    CK(cp(out->cand_idx, Dd.cand_idx, 4 * nc), "download");
+    CK(cp(out->piece_off, Dd.piece_off, 4 * (n + 1)), "download");
+    CK(cp(out->piece_sphere, Dd.piece_sphere, 4 * np), "download");
+    CK(cp(out->piece_vol, Dd.piece_vol, 8 * np), "download");
+    CK(cp(out->piece_m1, Dd.piece_m1, 24 * np), "download");
+    CK(cp(out->piece_facemask, Dd.piece_fm, np), "download");
+    CK(cp(out->inc_off, Dd.inc_off, 4 * (np + 1)), "download");
+    CK(cp(out->inc_sphere, Dd.inc_sphere, 4 * ni), "download");
+    CK(cudaStreamSynchronize(c->stream), "download");
+  } else {
+    rpd_status s = seg_run(c, kind, n, d_list, nullptr, c->st.T, S, D, &nc, &np, &ni, copy,
+                           no_ensure);
+    if (s) return s;
+  }
+  out->T = n;
+  out->n_cand = nc;
+  out->n_pieces = np;
+  out->n_inc = ni;
+  return RPD_OK;
+}
+
+extern "C" {
 
 rpd_status rpd_download_tets(rpd_ctx* c, const int32_t* tet_list, int64_t n,
                              const int32_t* id_map, int32_t* ids_out, rpd_csr* out) {
@@ -1131,73 +1333,7 @@ rpd_status rpd_download_tets(rpd_ctx* c, const int32_t* tet_list, int64_t n,
       CK(cudaMemcpyAsync(ids_out, dst, sizeof(int32_t) * n, cudaMemcpyDefault, c->stream),
          "download ids");
   }
-  SegSources S{};
-  S.s[0] = state_source(c);
-  const bool copy = out->cand_off || out->piece_off;
-  // a host destination is filled through device staging (g_dst) and one copy per array
-  const bool host = (out->cand_off && is_host_ptr(out->cand_off)) ||
-                    (out->piece_off && is_host_ptr(out->piece_off));
-  rpd_csr user = *out;
-  auto ensure = [&](int64_t nc, int64_t np, int64_t ni, SegDst* D) -> rpd_status {
-    if (!host) return RPD_OK;
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
-    const size_t o_co = take(4 * (n + 1)), o_ci = take(4 * nc), o_po = take(4 * (n + 1)),
-                 o_ps = take(4 * np), o_pv = take(8 * np), o_pm = take(24 * np),
-                 o_pf = take(np), o_io = take(4 * (np + 1)), o_is = take(4 * ni);
-    if (c->g_dst.ensure(off)) return fail(c, RPD_ENOMEM, "alloc");
-    char* b = c->g_dst.as<char>();
-    if (D->cand_off) {
-      D->cand_off = (int32_t*)(b + o_co);
-      D->cand_idx = (int32_t*)(b + o_ci);
-    }
-    if (D->piece_off) {
-      D->piece_off = (int32_t*)(b + o_po);
-      D->piece_sphere = (int32_t*)(b + o_ps);
-      D->piece_vol = (double*)(b + o_pv);
-      D->piece_m1 = (double*)(b + o_pm);
-      D->piece_fm = (uint8_t*)(b + o_pf);
-      D->inc_off = (int32_t*)(b + o_io);
-      D->inc_sphere = (int32_t*)(b + o_is);
-    }
-    return RPD_OK;
-  };
-  SegDst D{out->cand_off, out->cand_idx, out->piece_off, out->piece_sphere, out->piece_vol,
-           out->piece_m1, out->piece_facemask, out->inc_off, out->inc_sphere, nullptr};
-  int64_t nc = 0, np = 0, ni = 0;
-  if (host) {
-    // sizes first (the staging is laid out from them), then the copy into the staging
-    rpd_status s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, SegDst{}, &nc, &np, &ni,
-                           false, no_ensure);
-    if (s) return s;
-    SegDst Dd = D;
-    if ((s = ensure(nc, np, ni, &Dd))) return s;
-    s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, Dd, &nc, &np, &ni, true, no_ensure);
-    if (s) return s;
-    auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
-      if (!dst || bytes == 0) return cudaSuccess;
-      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
-    };
-    CK(cp(user.cand_off, Dd.cand_off, 4 * (n + 1)), "download");
-    CK(cp(user.cand_idx, Dd.cand_idx, 4 * nc), "download");
-    CK(cp(user.piece_off, Dd.piece_off, 4 * (n + 1)), "download");
-    CK(cp(user.piece_sphere, Dd.piece_sphere, 4 * np), "download");
-    CK(cp(user.piece_vol, Dd.piece_vol, 8 * np), "download");
-    CK(cp(user.piece_m1, Dd.piece_m1, 24 * np), "download");
-    CK(cp(user.piece_facemask, Dd.piece_fm, np), "download");
-    CK(cp(user.inc_off, Dd.inc_off, 4 * (np + 1)), "download");
-    CK(cp(user.inc_sphere, Dd.inc_sphere, 4 * ni), "download");
-    CK(cudaStreamSynchronize(c->stream), "download");
-  } else {
-    rpd_status s = seg_run(c, 1, n, d_list, nullptr, c->st.T, S, D, &nc, &np, &ni, copy,
-                           no_ensure);
-    if (s) return s;
-  }
-  out->T = n;
-  out->n_cand = nc;
-  out->n_pieces = np;
-  out->n_inc = ni;
-  return RPD_OK;
+  return download_rows(c, 1, d_list, n, out);
 }
 
 rpd_status rpd_merge_shards(rpd_ctx* c, const rpd_shards* dirty, const rpd_csr* old,
@@ -1371,6 +1507,13 @@ rpd_status rpd_download_neighbors(rpd_ctx* c, int32_t* nbr_off, int32_t* nbr_idx
 rpd_status rpd_download_cands(rpd_ctx* c, int32_t* cand_off, int32_t* cand_idx) {
   if (!c) return RPD_EINVAL;
   if (!c->have_rel) return fail(c, RPD_ESTATE, "no candidates");
+  if (!c->compact) {
+    if (!cand_off) return fail(c, RPD_EINVAL, "rpd_download_cands: cand_off is needed");
+    CK(cudaSetDevice(c->device), "cudaSetDevice");
+    rpd_csr o{cand_off, cand_idx, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+              nullptr, 0, 0, 0, 0};
+    return download_rows(c, 0, nullptr, c->st.T, &o);
+  }
   const CandSet& cs = c->cand[c->cur];
   if (cand_off)
     CK(cudaMemcpyAsync(cand_off, cs.off.p, sizeof(int32_t) * (c->st.T + 1),

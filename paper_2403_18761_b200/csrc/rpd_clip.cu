@@ -1166,6 +1166,7 @@ struct EuCompact {
   uint8_t *sfm, *rfm;            // ... compacted (per piece, per radical facet)
   const unsigned long long* p_radj;  // radical-facet adjacency (per pair slot)
   unsigned long long* radj;          // ... compacted (per radical facet)
+  int32_t inc_base, rpf_base;        // value offsets of inc_off / rpf_off (pool append)
 };
 
 __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ cand_idx,
@@ -1183,8 +1184,8 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   if (p == n_pairs - 1) {
-    inc_off[pscan[n_pairs]] = iscan[n_pairs];
-    if (eu.rmask) eu.rpf_off[pscan[n_pairs]] = eu.rscan[n_pairs];
+    inc_off[pscan[n_pairs]] = eu.inc_base + iscan[n_pairs];
+    if (eu.rmask) eu.rpf_off[pscan[n_pairs]] = eu.rpf_base + eu.rscan[n_pairs];
   }
   if (flag[p] != 1) return;
   const int q = pscan[p];
@@ -1196,7 +1197,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
   piece_m1[3 * q + 2] = pm1[3 * p + 2];
   piece_fm[q] = pfm[p];
   int o = iscan[p];
-  inc_off[q] = o;
+  inc_off[q] = eu.inc_base + o;
   const int e0 = nbr_off[i];
   const int w0 = mask_off[p];
   for (int w = w0; w < mask_off[p + 1]; ++w) {
@@ -1211,7 +1212,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
     eu.piece[q] = eu.p_eu[p];
     eu.sfm[q] = eu.p_sfm[p];
     int r = eu.rscan[p];
-    eu.rpf_off[q] = r;
+    eu.rpf_off[q] = eu.rpf_base + r;
     for (int w = w0; w < mask_off[p + 1]; ++w) {
       unsigned m = eu.rmask[w];
       while (m) {
@@ -1403,11 +1404,13 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
         EuCompact{c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_rval.as<long long>(),
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
                   d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm,
-                  c->p_radj.as<unsigned long long>(), d.radj});
+                  c->p_radj.as<unsigned long long>(), d.radj, d.inc_base, d.rpf_base});
     ++c->launches;
   } else {
-    cudaMemsetAsync(d.inc_off, 0, sizeof(int32_t), c->stream);
-    if (c->euler) cudaMemsetAsync(d.rpf_off, 0, sizeof(int32_t), c->stream);
+    // the terminal offsets of an empty batch (the pool's current fill levels)
+    cudaMemcpyAsync(d.inc_off, &d.inc_base, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
+    if (c->euler)
+      cudaMemcpyAsync(d.rpf_off, &d.rpf_base, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
   }
   k_piece_off<<<nblk(n_tets + 1, 256), 256, 0, c->stream>>>(n_tets, cand_off,
                                                           c->p_scan.as<int32_t>(), d.off);

@@ -25,6 +25,11 @@ struct DevBuf {
     if (e == cudaSuccess) cap = want;
     return e;
   }
+  // like ensure, but a (re)allocation reserves `factor` x bytes (pools that grow by appends)
+  cudaError_t ensure_slack(size_t bytes, int factor) {
+    if (bytes <= cap && p) return cudaSuccess;
+    return ensure(bytes * factor);
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -91,22 +96,33 @@ struct Stage {
 }  // namespace rpd
 
 namespace rpd {
-// candidate CSR over a list of tets (all tets of the ctx, or the dirty tets of an update)
+// Candidate set over a list of tets.  As the ctx STATE (cand[cur]) it is a pool: tet t's
+// candidates are idx[rows[t].x, rows[t].y); after rpd_relations the pool is compact (rows ==
+// the CSR off) and a partial update appends the dirty tets' new lists at the pool's tail and
+// re-points their rows (clean tets are never copied).  As a batch (cand_d: the dirty tets of an
+// update) it is a CSR over the batch whose idx may live in the state pool (idx_ext).
 struct CandSet {
-  DevBuf off;       // int32 [n_tets+1]
-  DevBuf idx;       // int32 [n]   candidate sphere ids, ascending per tet
-  DevBuf pair_tet;  // int32 [n]   local tet index of every pair
-  DevBuf moff;      // int32 [n+1] incidence-mask word offsets of every pair
+  DevBuf off;       // int32 [n_tets+1]  CSR offsets (compact pool / batch)
+  DevBuf idx;       // int32 [fill]  candidate sphere ids, ascending per tet
+  DevBuf pair_tet;  // int32 [n]   local tet index of every pair (compact pool / batch)
+  DevBuf moff;      // int32 [n+1] incidence-mask word offsets of every pair (compact / batch)
+  DevBuf rows;      // int2 [n_tets]  state: [beg, end) of every tet's candidates in idx
+  int32_t* idx_ext = nullptr;  // batch: candidates written here (the state pool's tail)
   int64_t n = 0, n_tets = 0, n_words = 0;
+  int64_t fill = 0;            // state: pool entries in use (live + dead)
+  int32_t* idxp() const { return idx_ext ? idx_ext : idx.as<int32_t>(); }
 };
-// piece CSR over a list of tets
+// Piece set over a list of tets: the same pool scheme (rows [beg, end) of piece slots per
+// tet; inc_off / rpf_off are CSRs over the pool's piece slots, appended in order).
 struct PieceSet {
   DevBuf off, sphere, vol, m1, fm, inc_off, inc;
   // fractional Euler characteristics (Euler mode): per piece, and per radical SoS facet
   DevBuf eu, rpf_off, rpf_j, rpf_e;
   DevBuf sfm, rfm;  // CC flags: SoS tet facets per piece, tet faces next to each radical facet
   DevBuf radj;      // per radical facet: the piece's radical facets sharing an edge (by rank)
-  int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;
+  DevBuf rows;      // int2 [n_tets]  state: [beg, end) of every tet's piece slots
+  int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;  // live counts
+  int64_t fill_p = 0, fill_i = 0, fill_r = 0;              // state: pool slots in use
 };
 }  // namespace rpd
 
@@ -154,6 +170,8 @@ struct rpd_ctx {
   rpd::PieceSet pcs[2], pcs_d;
   int cur = 0;
   bool have_rel = false, have_pieces = false;
+  bool compact = true;         // the state pools are plain CSRs (no partial update since)
+  int64_t n_compactions = 0;   // pool compactions (garbage collection) since rpd_create
 
   // clip per-pair scratch
   rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_over3, p_scan, i_scan;
@@ -263,6 +281,8 @@ struct PieceDst {
   uint8_t* sfm;       // [n_pieces], [n_rpf]
   uint8_t* rfm;
   unsigned long long* radj;  // [n_rpf]
+  int32_t inc_base = 0;      // added to every inc_off / rpf_off value (appending to a pool
+  int32_t rpf_base = 0;      // whose incidences / radical facets already hold this many)
 };
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
@@ -270,13 +290,23 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
 // partial update (rpd_partial.cu)
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old);
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
-cudaError_t launch_merge(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
-                         const CandSet& cd, const PieceSet& pd, CandSet& cn, PieceSet& pn,
-                         int phase);
+// state rows from the compact CSRs (cand and / or piece; NULL skips)
+cudaError_t launch_rows_from_off(rpd_ctx* c, int64_t T, const CandSet* cs, PieceSet* ps,
+                                 CandSet* cs_rows);
+// partial update: re-point the dirty tets' rows at the batch appended to the pools, and count
+// the removed (old) segments' sizes into rm[0..3] = cands, pieces, incidences, radical facets
+cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, CandSet& pool_c,
+                               PieceSet& pool_p, const CandSet& cd, const PieceSet& pd,
+                               int64_t cbase, int64_t pbase, unsigned long long* rm);
+// compaction of the state pools (by rows) into the plain CSRs cn / pn (pair_tet and moff of
+// the candidates rebuilt); phase 0: counts + scans, phase 1: copies
+cudaError_t launch_compact_state(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,
+                                 CandSet& cn, PieceSet& pn, int phase);
 // segment gather engine (rpd_gather.cu): multi-GPU gather / partial-mode merge / download
 // of a tet list.  A source holds per-row candidate and piece segments [beg[r], end[r]) and a
 // per-piece incidence CSR i_off (piece p: [i_off[p], i_off[p+1])); NULL parts are skipped.
 struct SegSrc {
+  int rs;  // row stride of the beg / end arrays: 1 (CSR offsets) or 2 (int2 rows)
   const int32_t *c_beg, *c_end, *c_idx;
   const int32_t *p_beg, *p_end, *p_sphere;
   const double *p_vol, *p_m1;
@@ -302,6 +332,7 @@ struct SegDst {
 SegSrc seg_src_csr(const int32_t* c_off, const int32_t* c_idx, const int32_t* p_off,
                    const int32_t* p_sphere, const double* p_vol, const double* p_m1,
                    const uint8_t* p_fm, const int32_t* i_off, const int32_t* i_sph);
+SegSrc seg_src_state(const CandSet& cs, const PieceSet& ps);
 // kind 0: identity rows of source 0; 1: source-0 rows `list`; 2: identity overwritten by the
 // shards' rows (merge); 3: only the shards' rows (gather)
 cudaError_t launch_map(rpd_ctx* c, int kind, int64_t n_out, const int32_t* list,

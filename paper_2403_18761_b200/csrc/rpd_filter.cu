@@ -595,7 +595,7 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 // Dirty tet a keeps its old candidates i whose neighbour row is unchanged: rel(t, i) only
 // depends on t and N(i), so the boolean is the same as before (R11).
 __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
-                           const int32_t* __restrict__ co_off, const int32_t* __restrict__ co_idx,
+                           const int2* __restrict__ co_rows, const int32_t* __restrict__ co_idx,
                            const int32_t* __restrict__ repoch, const int* __restrict__ min_epoch,
                            const int32_t* __restrict__ nbr_off, int cap,
                            int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
@@ -606,7 +606,8 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
   const unsigned FULL = 0xffffffffu;
   const int t = dirty[a];
   const int me = *min_epoch;
-  const int q0 = co_off[t], q1 = co_off[t + 1];
+  const int2 rw = co_rows[t];  // the tet's old candidates in the state pool
+  const int q0 = rw.x, q1 = rw.y;
   for (int qb = q0; qb < q1; qb += 32) {
     const int q = qb + lane;
     const int i = q < q1 ? co_idx[q] : 0;
@@ -634,7 +635,7 @@ cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
                             int32_t* k_words) {
   if (n_dirty == 0) return cudaSuccess;
   k_keep_old<<<nblk(n_dirty * 32, 256), 256, 0, c->stream>>>(
-      n_dirty, dirty, co.off.as<int32_t>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
+      n_dirty, dirty, co.rows.as<int2>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
       c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab, k_words);
   ++c->launches;
   return cudaGetLastError();

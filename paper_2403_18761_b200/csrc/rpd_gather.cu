@@ -67,9 +67,10 @@ __global__ void k_seg_count(int64_t n, const int2* __restrict__ map, SegSources 
   int nc = 0, np = 0, ni = 0;
   if (m.x >= 0) {
     const SegSrc& s = S.s[m.x];
-    if (s.c_beg) nc = s.c_end[m.y] - s.c_beg[m.y];
+    const int64_t r = (int64_t)m.y * s.rs;
+    if (s.c_beg) nc = s.c_end[r] - s.c_beg[r];
     if (s.p_beg) {
-      const int p0 = s.p_beg[m.y], p1 = s.p_end[m.y];
+      const int p0 = s.p_beg[r], p1 = s.p_end[r];
       np = p1 - p0;
       ni = p1 > p0 ? s.i_off[p1] - s.i_off[p0] : 0;
     }
@@ -86,12 +87,13 @@ __global__ void k_seg_copy(int64_t n, const int2* __restrict__ map, SegSources S
   const int2 m = map[o];
   if (m.x < 0) return;
   const SegSrc& s = S.s[m.x];
+  const int64_t r = (int64_t)m.y * s.rs;
   if (D.cand_idx && s.c_beg) {
-    const int c0 = s.c_beg[m.y], c1 = s.c_end[m.y], q0 = D.cand_off[o];
+    const int c0 = s.c_beg[r], c1 = s.c_end[r], q0 = D.cand_off[o];
     for (int k = c0; k < c1; ++k) D.cand_idx[q0 + (k - c0)] = s.c_idx[k];
   }
   if (D.piece_off && s.p_beg) {
-    const int p0 = s.p_beg[m.y], p1 = s.p_end[m.y];
+    const int p0 = s.p_beg[r], p1 = s.p_end[r];
     if (p1 <= p0) return;
     const int q0 = D.piece_off[o], i0 = s.i_off[p0], gi0 = D.i_tet[o];
     for (int p = p0; p < p1; ++p) {
@@ -131,6 +133,7 @@ SegSrc seg_src_csr(const int32_t* c_off, const int32_t* c_idx, const int32_t* p_
                    const int32_t* p_sphere, const double* p_vol, const double* p_m1,
                    const uint8_t* p_fm, const int32_t* i_off, const int32_t* i_sph) {
   SegSrc s{};
+  s.rs = 1;
   if (c_off) {
     s.c_beg = c_off;
     s.c_end = c_off + 1;
@@ -145,6 +148,30 @@ SegSrc seg_src_csr(const int32_t* c_off, const int32_t* c_idx, const int32_t* p_
     s.p_fm = p_fm;
     s.i_off = i_off;
     s.i_sph = i_sph;
+  }
+  return s;
+}
+
+// the ctx state: the pools addressed by their int2 rows
+SegSrc seg_src_state(const CandSet& cs, const PieceSet& ps) {
+  SegSrc s{};
+  s.rs = 2;
+  const int32_t* cr = reinterpret_cast<const int32_t*>(cs.rows.p);
+  const int32_t* pr = reinterpret_cast<const int32_t*>(ps.rows.p);
+  if (cr) {
+    s.c_beg = cr;
+    s.c_end = cr + 1;
+    s.c_idx = cs.idx.as<int32_t>();
+  }
+  if (pr) {
+    s.p_beg = pr;
+    s.p_end = pr + 1;
+    s.p_sphere = ps.sphere.as<int32_t>();
+    s.p_vol = ps.vol.as<double>();
+    s.p_m1 = ps.m1.as<double>();
+    s.p_fm = ps.fm.as<uint8_t>();
+    s.i_off = ps.inc_off.as<int32_t>();
+    s.i_sph = ps.inc.as<int32_t>();
   }
   return s;
 }

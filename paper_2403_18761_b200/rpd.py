@@ -42,7 +42,8 @@ class _Pieces(C.Structure):
     _fields_ = [("piece_off", C.c_void_p), ("piece_sphere", C.c_void_p),
                 ("piece_vol", C.c_void_p), ("piece_m1", C.c_void_p),
                 ("piece_facemask", C.c_void_p), ("inc_off", C.c_void_p),
-                ("inc_sphere", C.c_void_p), ("n_pieces", C.c_int64), ("n_inc", C.c_int64)]
+                ("inc_sphere", C.c_void_p), ("n_pieces", C.c_int64), ("n_inc", C.c_int64),
+                ("piece_rows", C.c_void_p), ("n_slots", C.c_int64)]
 
 
 class _Euler(C.Structure):
