@@ -26,15 +26,22 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+def _objdir():
+    """Objects live in a directory per flag set (variant builds do not mix with the default)."""
+    import hashlib
+    h = hashlib.sha1(" ".join(NVCC_FLAGS).encode()).hexdigest()[:10]
+    return os.path.join(OBJ, h)
+
+
 def _obj(src):
-    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    return os.path.join(_objdir(), os.path.basename(src)[:-3] + ".o")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(_objdir(), exist_ok=True)
     hdr_t = max(os.path.getmtime(h) for h in HDRS)
 
     def compile_one(src):

@@ -172,7 +172,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.tx, &c->st.sw, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
                     &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
                     &c->st.old_twin, &c->st.old_hkey, &c->st.old_sw, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
-                    &c->slab, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
+                    &c->slab, &c->slab_m, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
@@ -186,6 +186,8 @@ void rpd_destroy(rpd_ctx* c) {
     x->idx.release();
     x->pair_tet.release();
     x->moff.release();
+    x->cut.release();
+    x->rows.release();
   }
   PieceSet* ps[] = {&c->pcs[0], &c->pcs[1], &c->pcs_d, &c->g_pcs[0], &c->g_pcs[1]};
   for (PieceSet* x : ps) {
@@ -203,6 +205,7 @@ void rpd_destroy(rpd_ctx* c) {
     x->sfm.release();
     x->rfm.release();
     x->radj.release();
+    x->rows.release();
   }
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
@@ -334,6 +337,7 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   for (int attempt = 0; attempt < 3; ++attempt) {
     const int cap = c->slab_cap;
     CK(c->slab.ensure(sizeof(int32_t) * (size_t)cap * nt), "alloc slab");
+    CK(c->slab_m.ensure(sizeof(uint2) * (size_t)cap * nt), "alloc slab");
     // ST_MAXK, ST_TESTED, ST_REL_TESTS
     CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_MAXK, 0,
                        sizeof(unsigned long long) * 3, c->stream), "memset");
@@ -404,9 +408,11 @@ static rpd_status run_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets,
   }
   CK(cs.pair_tet.ensure(sizeof(int32_t) * (nc > 0 ? nc : 1)), "alloc");
   CK(cs.moff.ensure(sizeof(int32_t) * (nc + 1)), "alloc");
+  CK(cs.cut.ensure(sizeof(unsigned) * (cs.n_words > 0 ? cs.n_words : 1)), "alloc");
   CK(launch_compact_cands(c, n_tets, c->slab_cap, c->k_tet.as<int32_t>(), c->slab.as<int32_t>(),
                           cs.off.as<int32_t>(), cs.idxp(), cs.pair_tet.as<int32_t>(),
-                          c->w_off.as<int32_t>(), cs.moff.as<int32_t>(), nc), "compact");
+                          c->w_off.as<int32_t>(), cs.moff.as<int32_t>(), nc,
+                          cs.cut.as<unsigned>()), "compact");
   c->last.max_k_tet = (int32_t)rb->u64[ST_MAXK];
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
   c->last.pairs_tested += c->filter_mode == RPD_FILTER_PRUNED
@@ -481,11 +487,13 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
   CK(cudaMemsetAsync(c->stats.as<unsigned long long>() + ST_CLIP_PLANES, 0,
                      sizeof(unsigned long long) * 8, c->stream), "memset");
   if (c->profile) cudaEventRecord(c->ev[2], c->stream);
-  CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff, c->clip_wide),
+  CK(launch_clip(c, n, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff,
+                 cs.cut.as<unsigned>(), c->clip_wide),
      "clip");
   tmark(c, "clip-fast");
   if (!c->clip_wide && n > 0)
-    CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff),
+    CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff,
+                            cs.cut.as<unsigned>()),
        "clip (wide)");
   tmark(c, "clip-wide");
   if (c->profile) cudaEventRecord(c->ev[3], c->stream);
@@ -621,6 +629,10 @@ static rpd_status compact_state(rpd_ctx* c, int64_t extra) {
   CK(cudaStreamSynchronize(c->stream), "compact");
   cn.n_tets = T;
   cn.n_words = rb->i32[0];
+  // no filter values for the re-laid-out pairs: every plane is classified by the clip
+  CK(cn.cut.ensure(sizeof(unsigned) * (cn.n_words > 0 ? cn.n_words : 1)), "alloc");
+  CK(cudaMemsetAsync(cn.cut.p, 0xff, sizeof(unsigned) * (cn.n_words > 0 ? cn.n_words : 1),
+                     c->stream), "memset");
   cn.fill = nc;
   cn.idx_ext = nullptr;
   pn.n_tets = T;

@@ -363,6 +363,7 @@ struct PairOut {
   uint8_t* fm;
   unsigned* incmask;   // incidence bitmask words of every pair (positions in N(i))
   const int32_t* mask_off;
+  const unsigned* cut; // per pair (mask_off layout): the planes that can cut (filter values)
   int32_t* over_list;  // pairs that overflowed (re-run by the next wider kernel)
   int32_t* over_count;
   // Euler (eu_rec == nullptr: off)
@@ -482,11 +483,31 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     unsigned live[VPL];  // live vertex slots (group-uniform)
 #pragma unroll
     for (int k = 0; k < VPL; ++k) live[k] = k == 0 ? 0xfu : 0u;
-    c_planes += e1 - e0;
-
-    for (int base = e0; base < e1 && status == ST_ALIVE; base += GW) {
-      const int e = base + lane;
-      const bool have = e < e1;
+    // the planes to classify: the pair's cut mask (planes with a corner value <= 0, from the
+    // relation filter's exact Alg. 1 values), taken GW set bits at a time in
+    // CSR order; each selected plane is still checked here (a superset mask is safe)
+    const int kp = e1 - e0;
+    int cw = 0;                       // current mask word
+    unsigned cmask = 0u;              // its unprocessed bits
+    if (kp > 0) {
+      cmask = out.cut[mo];
+      if (kp < 32) cmask &= (1u << kp) - 1u;
+    }
+    while (status == ST_ALIVE) {
+      while (cmask == 0u && ++cw < nwp) {
+        cmask = out.cut[mo + cw];
+        if (kp - 32 * cw < 32) cmask &= (1u << (kp - 32 * cw)) - 1u;
+      }
+      if (cmask == 0u) break;
+      const int nset = __popc(cmask);
+      const bool have = lane < nset;
+      const int bit = have ? (int)__fns(cmask, 0, lane + 1) : 0;
+      const int e = e0 + 32 * cw + bit;
+      {  // drop the bits taken by this batch
+        const int last = __shfl_sync(FULL, bit, min(nset, GW) - 1, GW);
+        cmask = nset <= GW ? 0u : (cmask & ~((2u << last) - 1u));
+      }
+      c_planes += min(nset, GW);
       double g[4];
       bool allpos = false;
       if (have) {
@@ -523,7 +544,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           s[2] = b.x;
           s[3] = b.y;
         }
-        const int es = base + l;
+        const int es = __shfl_sync(FULL, e, l, GW);
         const int js = __ldg(nbr_idx + es);
         const int tws = __ldg(twin + es);
         const double sabs = fabs(s[0]) + fabs(s[1]) + fabs(s[2]) + fabs(s[3]);
@@ -1257,7 +1278,8 @@ template <int GW, int VPL, bool EU>
 static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list,
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
-                                 int32_t* over, const int32_t* n_dev, int* dyn = nullptr) {
+                                 const unsigned* cut, int32_t* over, const int32_t* n_dev,
+                                 int* dyn = nullptr) {
   constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
@@ -1285,7 +1307,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
-            c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff,
+            c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff, cut,
             over ? over + 1 : nullptr, over,
             c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
             c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>(),
@@ -1305,15 +1327,15 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
 template <bool EU>
 static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                                   const int32_t* tet_ids, const int32_t* cand_idx,
-                                  const int32_t* moff, int wide) {
+                                  const int32_t* moff, const unsigned* cut, int wide) {
   if (wide)
-    return launch_clip_t<32, 4, EU>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff,
+    return launch_clip_t<32, 4, EU>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, cut,
                                     nullptr, nullptr);
   cudaError_t e = c->p_dyn.ensure(sizeof(int));
   if (e) return e;
   if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
   return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, EU>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                      cand_idx, moff, c->p_over.as<int32_t>(),
+                                                      cand_idx, moff, cut, c->p_over.as<int32_t>(),
                                                       nullptr, c->p_dyn.as<int>());
 }
 
@@ -1321,7 +1343,7 @@ static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pa
 // or the widest kernel over all pairs when `wide`
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
-                        int wide) {
+                        const unsigned* cut, int wide) {
   c->clip_small = 0;
   if (n_pairs == 0) return cudaSuccess;
   if (!wide && n_pairs < RPD_CLIP_SMALL && !c->clip_tiers) {
@@ -1330,52 +1352,54 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
     c->clip_small = 1;
     return c->euler
                ? launch_clip_t<32, RPD_CLIP_MID_VPL, true>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                           cand_idx, moff,
+                                                           cand_idx, moff, cut,
                                                            c->p_over2.as<int32_t>(), nullptr)
                : launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs, nullptr, pair_tet,
-                                                            tet_ids, cand_idx, moff,
+                                                            tet_ids, cand_idx, moff, cut,
                                                             c->p_over2.as<int32_t>(), nullptr);
   }
-  return c->euler ? launch_clip_eu<true>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide)
-                  : launch_clip_eu<false>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, wide);
+  return c->euler ? launch_clip_eu<true>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, cut, wide)
+                  : launch_clip_eu<false>(c, n_pairs, pair_tet, tet_ids, cand_idx, moff, cut, wide);
 }
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
 // 64-slot kernel <32, RPD_CLIP_MID_VPL = 2>; its own overflows (p_over2) by the 128-slot <32, 4>
 template <bool EU>
 static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
-                                      const int32_t* cand_idx, const int32_t* moff) {
+                                      const int32_t* cand_idx, const int32_t* moff,
+                                      const unsigned* cut) {
   cudaError_t e;
 #if RPD_CLIP_MID32
   // 32-slot tier (one slot per lane: the fast tier's program on a full warp) for the fast
   // tier's overflows; its own overflows go on to the 64-slot tier
   e = launch_clip_t<32, 1, EU>(c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids,
-                               cand_idx, moff, c->p_over3.as<int32_t>(), c->p_over.as<int32_t>());
+                               cand_idx, moff, cut, c->p_over3.as<int32_t>(), c->p_over.as<int32_t>());
   if (e) return e;
   e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
-      c, 1 << 30, c->p_over3.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff,
+      c, 1 << 30, c->p_over3.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff, cut,
       c->p_over2.as<int32_t>(), c->p_over3.as<int32_t>());
 #else
   e = launch_clip_t<32, RPD_CLIP_MID_VPL, EU>(
-      c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff,
+      c, 1 << 30, c->p_over.as<int32_t>() + 1, pair_tet, tet_ids, cand_idx, moff, cut,
       c->p_over2.as<int32_t>(), c->p_over.as<int32_t>());
 #endif
   if (e) return e;
   return launch_clip_t<32, 4, EU>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
-                                  cand_idx, moff, nullptr, c->p_over2.as<int32_t>());
+                                  cand_idx, moff, cut, nullptr, c->p_over2.as<int32_t>());
 }
 
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
-                                 const int32_t* cand_idx, const int32_t* moff) {
+                                 const int32_t* cand_idx, const int32_t* moff,
+                                 const unsigned* cut) {
   if (c->clip_small)  // only the 64-slot tier's overflows remain, for the 128-slot tier
     return c->euler ? launch_clip_t<32, 4, true>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
-                                                 pair_tet, tet_ids, cand_idx, moff, nullptr,
+                                                 pair_tet, tet_ids, cand_idx, moff, cut, nullptr,
                                                  c->p_over2.as<int32_t>())
                     : launch_clip_t<32, 4, false>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
-                                                  pair_tet, tet_ids, cand_idx, moff, nullptr,
+                                                  pair_tet, tet_ids, cand_idx, moff, cut, nullptr,
                                                   c->p_over2.as<int32_t>());
-  return c->euler ? launch_overflow_eu<true>(c, pair_tet, tet_ids, cand_idx, moff)
-                  : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff);
+  return c->euler ? launch_overflow_eu<true>(c, pair_tet, tet_ids, cand_idx, moff, cut)
+                  : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff, cut);
 }
 
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {

@@ -107,6 +107,9 @@ struct CandSet {
   DevBuf pair_tet;  // int32 [n]   local tet index of every pair (compact pool / batch)
   DevBuf moff;      // int32 [n+1] incidence-mask word offsets of every pair (compact / batch)
   DevBuf rows;      // int2 [n_tets]  state: [beg, end) of every tet's candidates in idx
+  DevBuf cut;       // uint32 [n_words] per pair, incidence-mask layout: the planes of N(i)
+                    // that are not positive at all 4 corners (the only ones that can cut;
+                    // from the filter's Alg. 1 values; all ones where unknown)
   int32_t* idx_ext = nullptr;  // batch: candidates written here (the state pool's tail)
   int64_t n = 0, n_tets = 0, n_words = 0;
   int64_t fill = 0;            // state: pool entries in use (live + dead)
@@ -148,6 +151,7 @@ struct rpd_ctx {
 
   // filter scratch
   rpd::DevBuf k_tet, k_words, slab, w_off;
+  rpd::DevBuf slab_m;      // uint2 per slab entry: the candidate's 64-plane cut mask
   rpd::DevBuf cand_long;   // compaction: count + tets with more than 16 candidates
   rpd::DevBuf g_cnt;       // segment gather: per output row counts and tet-level inc offsets
   rpd::DevBuf g_map;       // segment gather: int2 (source, row) per output row
@@ -258,12 +262,13 @@ cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet);
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t T, int cap, const int32_t* k_tet,
                                  int32_t* slab, const int32_t* cand_off,
                                  int32_t* cand_idx, int32_t* pair_tet, const int32_t* w_off,
-                                 int32_t* p_moff, int64_t n_pairs);
+                                 int32_t* p_moff, int64_t n_pairs, unsigned* p_cut);
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const int32_t* tet_ids, const int32_t* cand_idx, const int32_t* moff,
-                        int wide);
+                        const unsigned* cut, int wide);
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
-                                 const int32_t* cand_idx, const int32_t* moff);
+                                 const int32_t* cand_idx, const int32_t* moff,
+                                 const unsigned* cut);
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff);
 // destination of a piece compaction
 struct PieceDst {

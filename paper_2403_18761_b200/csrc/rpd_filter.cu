@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
     const int32_t* __restrict__ nbr_off, const double4* __restrict__ planes, int N, int lo,
     int hi, int cap, int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-    int32_t* __restrict__ k_words, unsigned long long* __restrict__ stats) {
+    uint2* __restrict__ slab_m, int32_t* __restrict__ k_words,
+    unsigned long long* __restrict__ stats) {
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   bool valid = a < n;
   int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
   for (int i = lo; i < hi; ++i) {
     int e0 = __ldg(nbr_off + i), e1 = __ldg(nbr_off + i + 1);
     bool alive = valid;
+    uint2 cm = make_uint2(0u, 0u);  // cut mask: planes (first 64) not positive at all corners
     if (e0 == e1) {
       alive = alive && (N == 1);
     } else {
@@ -64,13 +66,21 @@ __global__ void __launch_bounds__(256) k_filter_allpairs(
           hk[k] = pos(h);
         }
         const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+        const int q = e - e0;
+        if (!(hk[0] & hk[1] & hk[2] & hk[3]) && q < 64) {
+          if (q < 32) cm.x |= 1u << q;
+          else cm.y |= 1u << (q - 32);
+        }
         if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
         alive = alive && hit;
         if (!__any_sync(0xffffffffu, alive)) break;
       }
     }
     if (alive) {
-      if (cnt < cap) slab[a * cap + cnt] = i;
+      if (cnt < cap) {
+        slab[a * cap + cnt] = i;
+        if (slab_m) slab_m[a * cap + cnt] = cm;
+      }
       ++cnt;
       words += (e1 - e0 + 31) >> 5;  // incidence-mask words of this candidate pair
     }
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, const int2* __restrict__ items,
     const int* __restrict__ n_items_p, int cap_items, int cap, int32_t* __restrict__ k_tet,
-    int32_t* __restrict__ slab, int32_t* __restrict__ k_words,
+    int32_t* __restrict__ slab, uint2* __restrict__ slab_m, int32_t* __restrict__ k_words,
     unsigned long long* __restrict__ stats) {
   extern __shared__ double4 s_lpl[];  // BVH_WARPS x BVH_LCAP planes
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -403,6 +413,8 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
       // planes with min over the leaf box > 0 hold at every vertex of every tet of the leaf;
       // only the planes crossing the box are tested per tet
       bool alive = valid;
+      uint2 cutm = make_uint2(0u, 0u);  // cut mask (first 64 planes): crossing planes not
+                                      // positive at all 4 corners of this lane's tet
       for (int c0 = 0; c0 < k; c0 += 32) {
         const int ec = c0 + lane;
         bool crosses = false;
@@ -427,6 +439,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
             hk[q] = pos(h);
           }
           const bool hit = hk[0] | hk[1] | hk[2] | hk[3];
+          if (!(hk[0] & hk[1] & hk[2] & hk[3]) && e < 64) {
+            if (e < 32) cutm.x |= 1u << e;
+            else cutm.y |= 1u << (e - 32);
+          }
           if (alive) ntests += hk[0] ? 1 : (hk[1] ? 2 : (hk[2] ? 3 : 4));
           alive = alive && hit;
           if (!__any_sync(FULL, alive)) break;
@@ -439,7 +455,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
 #endif
       if (alive) {
         const int slot = atomicAdd(k_tet + a, 1);
-        if (slot < cap) slab[a * cap + slot] = i;
+        if (slot < cap) {
+          slab[a * cap + slot] = i;
+          if (slab_m) slab_m[a * cap + slot] = cutm;
+        }
         if (k_words) atomicAdd(k_words + a, words);
       }
     }
@@ -482,13 +501,22 @@ __global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
 // the incidence-mask words of the smaller ids) counted by compare loops, and written to its
 // sorted position -- no warp-wide shuffles for lists of one or two entries.  Longer lists go
 // to a warp each (second kernel).
+// the pair's cut-mask words (incidence-mask layout): the filter's 64-plane mask, all ones
+// beyond it (the clip then classifies those planes itself; any superset is safe, the clip
+// re-checks every selected plane)
+__device__ __forceinline__ void write_cut(unsigned* dst, int words, const uint2* m) {
+  const uint2 v = m ? *m : make_uint2(~0u, ~0u);
+  for (int w = 0; w < words; ++w) dst[w] = w == 0 ? v.x : (w == 1 ? v.y : ~0u);
+}
+
 constexpr int CC_REG = 16;
 __global__ void __launch_bounds__(256) k_compact_cands_t(
     int64_t n, int cap, const int32_t* __restrict__ k_tet, const int32_t* __restrict__ slab,
     const int32_t* __restrict__ cand_off, int32_t* __restrict__ cand_idx,
     int32_t* __restrict__ pair_tet, const int32_t* __restrict__ w_off,
     int32_t* __restrict__ p_moff, const int32_t* __restrict__ nbr_off, int64_t n_pairs,
-    int32_t* __restrict__ long_list, int* __restrict__ n_long) {
+    int32_t* __restrict__ long_list, int* __restrict__ n_long, const uint2* __restrict__ slab_m,
+    unsigned* __restrict__ p_cut) {
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   const int k = min(k_tet[a], cap);
@@ -520,6 +548,7 @@ __global__ void __launch_bounds__(256) k_compact_cands_t(
       cand_idx[o + rank] = v[j];
       if (pair_tet) pair_tet[o + rank] = (int32_t)a;
       if (p_moff) p_moff[o + rank] = w0 + pre;
+      if (p_cut) write_cut(p_cut + w0 + pre, wd[j], slab_m + a * cap + j);
     }
   } else {  // a long list: one warp per tet in k_compact_cands_w (rare)
     long_list[atomicAdd(n_long, 1)] = (int32_t)a;
@@ -542,7 +571,8 @@ __global__ void k_compact_cands_w(const int32_t* __restrict__ list, const int* _
                                 const int32_t* __restrict__ cand_off,
                                 int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
                                 const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
-                                const int32_t* __restrict__ nbr_off, int64_t n_pairs) {
+                                const int32_t* __restrict__ nbr_off, int64_t n_pairs,
+                                const uint2* __restrict__ slab_m, unsigned* __restrict__ p_cut) {
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -582,7 +612,15 @@ __global__ void k_compact_cands_w(const int32_t* __restrict__ list, const int* _
       const int y = __shfl_up_sync(FULL, x, d);
       if (lane >= d) x += y;
     }
-    if (j < k) p_moff[o + j] = w + x - words;
+    if (j < k) {
+      p_moff[o + j] = w + x - words;
+      if (p_cut) {  // the cut mask of sorted candidate j: found by its id in the slab
+        const int i = cand_idx[o + j];
+        int src = 0;
+        for (int m = 0; m < k; ++m) src = s[m] == i ? m : src;
+        write_cut(p_cut + w + x - words, words, slab_m + a * cap + src);
+      }
+    }
     w += __shfl_sync(FULL, x, 31);
   }
   __syncwarp();
@@ -599,7 +637,7 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
                            const int32_t* __restrict__ repoch, const int* __restrict__ min_epoch,
                            const int32_t* __restrict__ nbr_off, int cap,
                            int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-                           int32_t* __restrict__ k_words) {
+                           uint2* __restrict__ slab_m, int32_t* __restrict__ k_words) {
   const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;  // warp per tet
   if (a >= n) return;
   const int lane = threadIdx.x & 31;
@@ -625,7 +663,10 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
     base = __shfl_sync(FULL, base, 0);
     if (keep) {
       const int slot = base + __popc(km & ((1u << lane) - 1u));
-      if (slot < cap) slab[a * cap + slot] = i;
+      if (slot < cap) {
+        slab[a * cap + slot] = i;
+        if (slab_m) slab_m[a * cap + slot] = make_uint2(~0u, ~0u);  // (no mask: all planes)
+      }
     }
   }
 }
@@ -636,7 +677,8 @@ cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
   if (n_dirty == 0) return cudaSuccess;
   k_keep_old<<<nblk(n_dirty * 32, 256), 256, 0, c->stream>>>(
       n_dirty, dirty, co.rows.as<int2>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
-      c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab, k_words);
+      c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab,
+      slab ? c->slab_m.as<uint2>() : nullptr, k_words);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -747,7 +789,8 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       k_bvh_leaf<<<(unsigned)(sms * 16), BVH_WARPS * 32, lsmem, c->stream>>>(
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
           c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,
-          (int)cap_items, cap, k_tet, slab, k_words, c->stats.as<unsigned long long>());
+          (int)cap_items, cap, k_tet, slab, slab ? c->slab_m.as<uint2>() : nullptr, k_words,
+          c->stats.as<unsigned long long>());
       c->launches += 3;
       c->bvh_cap_items = cap_items < cap_sup ? cap_items : cap_sup;
     }
@@ -759,7 +802,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
   k_filter_allpairs<<<nblk(n_tets, 256), 256, 0, c->stream>>>(
       c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, c->st.nbr_off.as<int32_t>(),
       c->st.planes.as<double4>(), (int)c->st.N, sphere_lo, sphere_hi, cap, k_tet, slab,
-      k_words, c->stats.as<unsigned long long>());
+      slab ? c->slab_m.as<uint2>() : nullptr, k_words, c->stats.as<unsigned long long>());
   ++c->launches;
   return cudaGetLastError();
 }
@@ -767,7 +810,7 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
 cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* k_tet,
                                  int32_t* slab, const int32_t* cand_off, int32_t* cand_idx,
                                  int32_t* pair_tet, const int32_t* w_off, int32_t* p_moff,
-                                 int64_t n_pairs) {
+                                 int64_t n_pairs, unsigned* p_cut) {
   if (n == 0) {
     if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
     return cudaSuccess;
@@ -777,14 +820,15 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
   int* n_long = c->cand_long.as<int>();
   int32_t* long_list = c->cand_long.as<int32_t>() + 1;
   if ((e = cudaMemsetAsync(n_long, 0, sizeof(int), c->stream))) return e;
+  const uint2* slab_m = p_cut ? c->slab_m.as<uint2>() : nullptr;
   k_compact_cands_t<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off,
                                                         cand_idx, pair_tet, w_off, p_moff,
                                                         c->st.nbr_off.as<int32_t>(), n_pairs,
-                                                        long_list, n_long);
+                                                        long_list, n_long, slab_m, p_cut);
   // (grid for every list, exits on the device count: long lists are rare)
   k_compact_cands_w<<<(unsigned)c->sms * 4, 256, 0, c->stream>>>(
       long_list, n_long, n, cap, k_tet, slab, cand_off, cand_idx, pair_tet, w_off, p_moff,
-      c->st.nbr_off.as<int32_t>(), n_pairs);
+      c->st.nbr_off.as<int32_t>(), n_pairs, slab_m, p_cut);
   c->launches += 2;
   return cudaGetLastError();
 }
