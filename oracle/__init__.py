@@ -69,6 +69,9 @@ class _Result(C.Structure):
                 ("piece_sosfm", C.POINTER(C.c_uint8)), ("rpf_fm", C.POINTER(C.c_uint8)),
                 ("rpf_adj", C.POINTER(C.c_uint64)),
                 ("n_rpf", C.c_int64),
+                ("rpe_off", C.POINTER(C.c_int32)), ("rpe_j", C.POINTER(C.c_int32)),
+                ("rpe_k", C.POINTER(C.c_int32)), ("rpe_euler", C.POINTER(C.c_int64)),
+                ("rpe_fm", C.POINTER(C.c_uint8)), ("n_rpe", C.c_int64),
                 ("n_rel_tests", C.c_int64), ("n_clip_tests", C.c_int64),
                 ("n_constructions", C.c_int64), ("n_fan_triangles", C.c_int64),
                 ("n_zero_hits", C.c_int64),
@@ -169,7 +172,12 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
                         "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64),
                         "piece_sosfm": arr(r.piece_sosfm, r.n_pieces, np.uint8),
                         "rpf_fm": arr(r.rpf_fm, r.n_rpf, np.uint8),
-                        "rpf_adj": arr(r.rpf_adj, r.n_rpf, np.uint64)})
+                        "rpf_adj": arr(r.rpf_adj, r.n_rpf, np.uint64),
+                        "rpe_off": arr(r.rpe_off, r.n_pieces + 1, np.int32),
+                        "rpe_j": arr(r.rpe_j, r.n_rpe, np.int32),
+                        "rpe_k": arr(r.rpe_k, r.n_rpe, np.int32),
+                        "rpe_euler": arr(r.rpe_euler, r.n_rpe, np.int64),
+                        "rpe_fm": arr(r.rpe_fm, r.n_rpe, np.uint8)})
     finally:
         L.oracle_free(rp)
     return out
@@ -254,12 +262,17 @@ def per_tet_lists(res, T):
         for p in range(po[a], po[a + 1]):
             eu = None
             if ro is not None and len(ro) == len(res["piece_sphere"]) + 1:
+                eo = res["rpe_off"]
                 eu = (int(res["piece_euler"][p]),
                       tuple(res["rpf_sphere"][ro[p]:ro[p + 1]].tolist()),
                       tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()),
                       int(res["piece_sosfm"][p]),
                       tuple(res["rpf_fm"][ro[p]:ro[p + 1]].tolist()),
-                      tuple(res["rpf_adj"][ro[p]:ro[p + 1]].tolist()))
+                      tuple(res["rpf_adj"][ro[p]:ro[p + 1]].tolist()),
+                      tuple(zip(res["rpe_j"][eo[p]:eo[p + 1]].tolist(),
+                                res["rpe_k"][eo[p]:eo[p + 1]].tolist(),
+                                res["rpe_euler"][eo[p]:eo[p + 1]].tolist(),
+                                res["rpe_fm"][eo[p]:eo[p + 1]].tolist())))
             pcs.append((int(res["piece_sphere"][p]), float(res["piece_vol"][p]),
                         tuple(res["piece_m1"][p].tolist()), int(res["piece_facemask"][p]),
                         tuple(res["inc_sphere"][io[p]:io[p + 1]].tolist()), eu))
@@ -271,6 +284,7 @@ def from_per_tet_lists(L):
     cand_off = [0]
     cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
     pe, rpf_off, rpf_j, rpf_e, sfm, rfm, radj = [], [0], [], [], [], [], []
+    rpe_off, rpe = [0], []
     for cands, pcs in L:
         cand_idx += cands
         cand_off.append(len(cand_idx))
@@ -289,13 +303,20 @@ def from_per_tet_lists(L):
                 rfm += list(eu[4])
                 radj += list(eu[5])
                 rpf_off.append(len(rpf_j))
+                rpe += list(eu[6])
+                rpe_off.append(len(rpe))
         piece_off.append(len(ps))
     eul = {}
     if len(pe) == len(ps) and len(rpf_off) == len(ps) + 1:
         eul = {"piece_euler": np.array(pe, np.int64), "rpf_off": np.array(rpf_off, np.int32),
                "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64),
                "piece_sosfm": np.array(sfm, np.uint8), "rpf_fm": np.array(rfm, np.uint8),
-               "rpf_adj": np.array(radj, np.uint64)}
+               "rpf_adj": np.array(radj, np.uint64),
+               "rpe_off": np.array(rpe_off, np.int32),
+               "rpe_j": np.array([x[0] for x in rpe], np.int32),
+               "rpe_k": np.array([x[1] for x in rpe], np.int32),
+               "rpe_euler": np.array([x[2] for x in rpe], np.int64),
+               "rpe_fm": np.array([x[3] for x in rpe], np.uint8)}
     return {**eul, "cand_off": np.array(cand_off, np.int32), "cand_idx": np.array(cand_idx, np.int32),
             "piece_off": np.array(piece_off, np.int32), "piece_sphere": np.array(ps, np.int32),
             "piece_vol": np.array(pv, np.float64),
@@ -381,6 +402,62 @@ def euler_sums(res, N, nbr_off, nbr_idx):
             key = (i, int(res["rpf_sphere"][r]))
             rpf[key] = rpf.get(key, Fraction(0)) + Fraction(int(res["rpf_euler"][r]), L)
     return rpc, rpf
+
+
+def rpe_sums(res):
+    """Per-sphere fractional Euler sums of the restricted power edges ("the
+    fractional Euler characteristic of all restricted elements (RPCs, RPFs, RPEs)"): rpe[(i,
+    j, k)] = Euler(RPE(m_i, m_j, m_k)) seen from m_i (j < k) = sum over m_i's pieces of their
+    edge on h_ij and h_ik, as exact Fractions."""
+    from fractions import Fraction
+    L = res["euler_denom"]
+    eo = res["rpe_off"]
+    out = {}
+    for p, i in enumerate(res["piece_sphere"].tolist()):
+        for r in range(eo[p], eo[p + 1]):
+            key = (i, int(res["rpe_j"][r]), int(res["rpe_k"][r]))
+            out[key] = out.get(key, Fraction(0)) + Fraction(int(res["rpe_euler"][r]), L)
+    return out
+
+
+def rpe_topology(res, tets):
+    """CC numbers of the restricted power edges: RPE(m_i, m_j, m_k) seen from
+    m_i is the union of the edges of m_i's pieces on h_ij and h_ik; two of them in tets sharing
+    face f are connected when both have an endpoint on f (a line meets the face plane once, so
+    those endpoints are the same point).  Plain union-find.  Returns {(i, j, k): cc}."""
+    parent = {}
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    adj = face_adjacency(tets)
+    po, eo = res["piece_off"], res["rpe_off"]
+    ps = res["piece_sphere"].tolist()
+    items = {}  # (t, i, j, k) -> endpoint tet-face mask
+    for t in range(len(tets)):
+        for q in range(po[t], po[t + 1]):
+            for r in range(eo[q], eo[q + 1]):
+                key = (t, ps[q], int(res["rpe_j"][r]), int(res["rpe_k"][r]))
+                items[key] = int(res["rpe_fm"][r])
+                parent[key] = key
+    for (t, i, j, k), fm in items.items():
+        for f in range(4):
+            if not (fm >> f) & 1 or adj[t][f] is None:
+                continue
+            t2, f2 = adj[t][f]
+            o = (t2, i, j, k)
+            if o in items and (items[o] >> f2) & 1:
+                ra, rb = find((t, i, j, k)), find(o)
+                if ra != rb:
+                    parent[max(ra, rb)] = min(ra, rb)
+    cc = {}
+    for x in parent:
+        if find(x) == x:
+            cc[x[1:]] = cc.get(x[1:], 0) + 1
+    return cc
 
 
 def face_adjacency(tets):

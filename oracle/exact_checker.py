@@ -329,3 +329,49 @@ def explicit_medial_faces(verts, tets, spheres, nbr_off, nbr_idx):
                     for b in range(a + 1, len(rad)):
                         faces.add(tuple(sorted((i, rad[a], rad[b]))))
     return sorted(faces), generic
+
+
+def explicit_rpe(verts, tets, spheres, nbr_off, nbr_idx, i):
+    """Restricted power edges of sphere i extracted explicitly (exact rational vertices, no
+    SoS): in every piece of i, an edge lying on the radical planes h_ij and h_ik (j < k) is
+    part of RPE(m_i, m_j, m_k); the parts are glued across tets by their exact endpoints.
+    Returns ({(j, k): V - E}, {(j, k): connected components}, generic)."""
+    sph_X = [tuple(_lat(s[c]) for c in range(4)) for s in spheres]
+    S = [int(j) for j in nbr_idx[nbr_off[i]:nbr_off[i + 1]]]
+    if not S and len(spheres) > 1:
+        return {}, {}, True
+    per = {}  # (j, k) -> set of edges (frozensets of two exact vertices)
+    generic = True
+    for t in range(len(tets)):
+        tet_X = [tuple(_lat(verts[v][c]) for c in range(3)) for v in tets[t]]
+        cell = exact_piece_cells(tet_X, sph_X, i, S)
+        if cell is None:
+            continue
+        generic &= cell["generic"]
+        pls = planes_for(tet_X, sph_X, i, S)
+        act = {v: frozenset(k for k, pl in enumerate(pls) if _val(pl, v) == 0)
+               for v in cell["vertices"]}
+        for e in cell["edges"]:
+            u, w = tuple(e)
+            rad = sorted(pls[k][2][1] for k in act[u] & act[w] if pls[k][2][0] == "r")
+            for a in range(len(rad)):
+                for b in range(a + 1, len(rad)):
+                    per.setdefault((rad[a], rad[b]), set()).add(e)
+    euler, cc = {}, {}
+    for key, edges in per.items():
+        vs = set().union(*edges)
+        euler[key] = len(vs) - len(edges)
+        parent = {v: v for v in vs}
+
+        def find(x):
+            while parent[x] != x:
+                parent[x] = parent[parent[x]]
+                x = parent[x]
+            return x
+        for e in edges:
+            u, w = tuple(e)
+            ru, rw = find(u), find(w)
+            if ru != rw:
+                parent[ru] = rw
+        cc[key] = len({find(v) for v in vs})
+    return euler, cc, generic

@@ -171,6 +171,12 @@ typedef struct {
   uint64_t* rpf_adj;             /* [n_rpf] the piece's radical facets (bit = rank by ascending
                                     j) this one shares an edge with: restricted power edges */
   int64_t n_rpf;
+  /* restricted power edges RPE(m_i, m_j, m_k) of every piece: the
+     piece's edge on the radical planes h_ij and h_ik, j < k, ascending (j, k) */
+  int32_t *rpe_off, *rpe_j, *rpe_k; /* [n_pieces + 1], [n_rpe], [n_rpe] */
+  int64_t* rpe_euler;            /* [n_rpe] its fractional Euler characteristic V - E over L */
+  uint8_t* rpe_fm;               /* [n_rpe] tet faces holding an endpoint of the edge */
+  int64_t n_rpe;
   /* instrumentation (C1 step 9) */
   int64_t n_rel_tests, n_clip_tests, n_constructions, n_fan_triangles, n_zero_hits;
   int status;
@@ -582,6 +588,10 @@ typedef struct {
   uint8_t* rpf_fm;    /* ... and the tet faces it has an edge on */
   uint64_t* rpf_adj;  /* ... and the radical facets it shares an edge with (by rank) */
   int32_t nrpf;
+  int32_t *rpe_j, *rpe_k; /* restricted power edges (j < k, ascending) ... */
+  int64_t* rpe_e;     /* ... their fractional Euler characteristic V - E, over L */
+  uint8_t* rpe_fm;    /* ... and the tet faces holding their endpoints */
+  int32_t nrpe;
   uint8_t sosfm;      /* tet faces among the piece's facets */
 } piece_t;
 
@@ -595,6 +605,12 @@ static unsigned faces_of(const poly_t* P, const int32_t* planes, int n) {
   for (int k = 0; k < n; ++k)
     if (P->pl[planes[k]].src < 0) fm |= 1u << (-1 - P->pl[planes[k]].src);
   return fm;
+}
+
+static int cmp_rpe(const void* a, const void* b) {
+  const int64_t *x = (const int64_t*)a, *y = (const int64_t*)b;
+  if (x[0] != y[0]) return (x[0] > y[0]) - (x[0] < y[0]);
+  return (x[1] > y[1]) - (x[1] < y[1]);
 }
 
 static int cmp_rpf(const void* a, const void* b) {
@@ -615,6 +631,7 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
   int64_t* fe = (int64_t*)calloc(npl, sizeof(int64_t)); /* Euler of each facet */
   unsigned* ffm = (unsigned*)calloc(npl, sizeof(unsigned)); /* tet faces sharing an edge */
   int32_t* rre = (int32_t*)malloc(sizeof(int32_t) * 2 * (3 * nv / 2 + 1)); /* radical-radical edges */
+  int64_t* rpe = (int64_t*)malloc(sizeof(int64_t) * 4 * (3 * nv / 2 + 1)); /* (j, k, V - E, fm) */
   int nrre = 0;
   for (int v = 0; v < nv; ++v) {
     int64_t pv = carrier_payload(A14, L, faces_of(P, P->v[v].p, 3));
@@ -639,6 +656,15 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
       if (P->pl[e[0]].src >= 0 && P->pl[e[1]].src >= 0) {
         rre[2 * nrre] = e[0];
         rre[2 * nrre + 1] = e[1];
+        /* its part of RPE(m_i, m_j, m_k): Euler = V - E = payload(u) + payload(w) - payload(e)
+           (the edge inside the tet: payload 1; an endpoint on tet face f: f's payload, inside
+           the tet: 1), and the tet faces its endpoints lie on (the third planes of u, w) */
+        int64_t j = P->pl[e[0]].src, k = P->pl[e[1]].src;
+        rpe[4 * nrre] = j < k ? j : k;
+        rpe[4 * nrre + 1] = j < k ? k : j;
+        rpe[4 * nrre + 2] = carrier_payload(A14, L, faces_of(P, P->v[u].p, 3)) +
+                            carrier_payload(A14, L, faces_of(P, P->v[w].p, 3)) - pe;
+        rpe[4 * nrre + 3] = faces_of(P, P->v[u].p, 3) | faces_of(P, P->v[w].p, 3);
         ++nrre;
       }
     }
@@ -683,6 +709,20 @@ static void piece_euler(const poly_t* P, const int64_t* A14, int64_t L, piece_t*
       out->rpf_adj[b] |= (uint64_t)1 << a;
     }
   }
+  /* the RPE list, ascending (j, k) */
+  qsort(rpe, nrre, 4 * sizeof(int64_t), cmp_rpe);
+  out->nrpe = nrre;
+  out->rpe_j = (int32_t*)malloc(sizeof(int32_t) * (nrre > 0 ? nrre : 1));
+  out->rpe_k = (int32_t*)malloc(sizeof(int32_t) * (nrre > 0 ? nrre : 1));
+  out->rpe_e = (int64_t*)malloc(sizeof(int64_t) * (nrre > 0 ? nrre : 1));
+  out->rpe_fm = (uint8_t*)malloc(nrre > 0 ? nrre : 1);
+  for (int k = 0; k < nrre; ++k) {
+    out->rpe_j[k] = (int32_t)rpe[4 * k];
+    out->rpe_k[k] = (int32_t)rpe[4 * k + 1];
+    out->rpe_e[k] = rpe[4 * k + 2];
+    out->rpe_fm[k] = (uint8_t)rpe[4 * k + 3];
+  }
+  free(rpe);
   free(rank_of);
   free(rre);
   free(pairs);
@@ -862,6 +902,10 @@ static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piec
     out->rpf_e = NULL;
     out->rpf_fm = NULL;
     out->rpf_adj = NULL;
+    out->nrpe = 0;
+    out->rpe_j = out->rpe_k = NULL;
+    out->rpe_e = NULL;
+    out->rpe_fm = NULL;
     out->sosfm = 0;
     if (A14) piece_euler(&P, A14, Lden, out);
   }
@@ -903,6 +947,11 @@ void oracle_free(oracle_result* r) {
   free(r->piece_sosfm);
   free(r->rpf_fm);
   free(r->rpf_adj);
+  free(r->rpe_off);
+  free(r->rpe_j);
+  free(r->rpe_k);
+  free(r->rpe_euler);
+  free(r->rpe_fm);
   free(r);
 }
 
@@ -956,15 +1005,24 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
     }
   }
   /* concatenate in tet order */
-  int64_t nc = 0, np = 0, ni = 0, nr = 0;
+  int64_t nc = 0, np = 0, ni = 0, nr = 0, ne = 0;
   for (int64_t a = 0; a < n_tets; ++a) {
     nc += O[a].ncand;
     np += O[a].npieces;
     for (int32_t p = 0; p < O[a].npieces; ++p) {
       ni += O[a].pieces[p].ninc;
       nr += O[a].pieces[p].nrpf;
+      ne += O[a].pieces[p].nrpe;
     }
   }
+  R->n_rpe = ne;
+  R->rpe_off = (int32_t*)malloc(sizeof(int32_t) * (np + 1));
+  R->rpe_j = (int32_t*)malloc(sizeof(int32_t) * (ne ? ne : 1));
+  R->rpe_k = (int32_t*)malloc(sizeof(int32_t) * (ne ? ne : 1));
+  R->rpe_euler = (int64_t*)malloc(sizeof(int64_t) * (ne ? ne : 1));
+  R->rpe_fm = (uint8_t*)malloc(ne ? ne : 1);
+  R->rpe_off[0] = 0;
+  int64_t e0 = 0;
   free(A);
   R->n_rpf = nr;
   R->piece_euler = (int64_t*)malloc(sizeof(int64_t) * (np ? np : 1));
@@ -1019,6 +1077,18 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
       free(pc->rpf_e);
       free(pc->rpf_fm);
       free(pc->rpf_adj);
+      if (pc->nrpe) {
+        memcpy(R->rpe_j + e0, pc->rpe_j, sizeof(int32_t) * pc->nrpe);
+        memcpy(R->rpe_k + e0, pc->rpe_k, sizeof(int32_t) * pc->nrpe);
+        memcpy(R->rpe_euler + e0, pc->rpe_e, sizeof(int64_t) * pc->nrpe);
+        memcpy(R->rpe_fm + e0, pc->rpe_fm, pc->nrpe);
+      }
+      e0 += pc->nrpe;
+      R->rpe_off[p0 + 1] = (int32_t)e0;
+      free(pc->rpe_j);
+      free(pc->rpe_k);
+      free(pc->rpe_e);
+      free(pc->rpe_fm);
       ++p0;
       R->inc_off[p0] = (int32_t)i0;
       free(pc->inc);

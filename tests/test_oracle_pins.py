@@ -451,6 +451,63 @@ def test_euler_sums_are_integers(make):
     assert sum(1 for x in rpc if x == 1) >= 0.5 * sum(1 for x in rpc if x != 0)
 
 
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(1), lambda: W.make_c1(3),
+                                  lambda: W.random_tiny(0, n_spheres=14, grid=2),
+                                  lambda: W.random_tiny(2, n_spheres=14, grid=2)])
+def test_rpe_euler_and_cc_equal_explicit_extraction(make):
+    """PAPER.md:439, 497, 506 ("RPC, RPF, RPE to have CC=1 and Euler=1"; the fractional Euler
+    characteristics of "all of its restricted elements (RPCs, RPFs, RPEs)"): the fractional
+    sums over the pieces' edges on h_ij and h_ik and the face-glued CC numbers equal V - E and
+    the components of the restricted power edges extracted explicitly (exact rational piece
+    vertices, no SoS, glued across tets by coordinates)."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    eu = oracle.rpe_sums(r)
+    cc = oracle.rpe_topology(r, w.tets)
+    assert eu and set(eu) == set(cc)
+    for i in range(w.N):
+        e_eu, e_cc, generic = X.explicit_rpe(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx,
+                                            i)
+        assert generic
+        assert {(j, k): v for (a, j, k), v in eu.items() if a == i} == e_eu, i
+        assert {(j, k): v for (a, j, k), v in cc.items() if a == i} == e_cc, i
+
+
+def test_rpe_through_the_hole_has_two_components():
+    """Three equal spheres whose centres are a right triangle in the plane x = 32 with its
+    circumcentre on the hole's diameter line (y = 26, z = 20): their cells meet along that line
+    (it lies on all three bisector planes), which crosses the genus-1 solid twice (x in
+    [2, 23] and [41, 62]; the hole spans x in [23, 41]).  So RPE(m_0, m_1, m_2) is two segments:
+    Euler 2 and CC 2, seen from each of the three spheres (the edge analogue of the paper's
+    Fig. 4(b) RPF with CC = 2)."""
+    w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
+    sph = np.array([[32.0, 32.0, 20.0, 1.0], [32.0, 20.0, 20.0, 1.0], [32.0, 26.0, 26.0, 1.0]])
+    off, idx = np.array([0, 2, 4, 6], np.int32), np.array([1, 2, 0, 2, 0, 1], np.int32)
+    r = oracle.rpd(w.verts, w.tets, sph, off, idx, euler=True)
+    assert oracle.rpe_sums(r) == {(0, 1, 2): 2, (1, 0, 2): 2, (2, 0, 1): 2}
+    assert oracle.rpe_topology(r, w.tets) == {(0, 1, 2): 2, (1, 0, 2): 2, (2, 0, 1): 2}
+
+
+@pytest.mark.parametrize("make", [lambda: W.make_c1(0, degenerate=True),
+                                  lambda: W.random_tiny(3, n_spheres=14, grid=2, coarse=True),
+                                  lambda: W.make_shape_workload("E", 1500, 120, seed=4,
+                                                                cache=False)])
+def test_rpe_sums_are_integers_and_symmetric(make):
+    """Every RPE sum is an integer (shared endpoints on tet faces add 1/2 + 1/2), also on
+    degenerate inputs, and RPE(m_i, m_j, m_k) is the same element seen from each of its three
+    spheres when no exact-zero predicate occurred."""
+    w = make()
+    r = oracle.rpd_workload(w, euler=True)
+    eu = oracle.rpe_sums(r)
+    assert eu and all(v.denominator == 1 for v in eu.values())
+    if r["stats"]["n_zero_hits"] == 0:
+        for (i, j, k), v in eu.items():
+            tri = sorted((i, j, k))
+            for a in tri:
+                b, c = [x for x in tri if x != a]
+                assert eu.get((a, b, c)) == v, (i, j, k)
+
+
 def test_euler_partial_update_equals_full(small_shape):
     """R11 with the Euler payloads: the partially updated pieces carry the same fractional
     Euler characteristics as a full recompute."""
@@ -461,7 +518,8 @@ def test_euler_partial_update_equals_full(small_shape):
         part, _ = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old, euler=True)
         full = oracle.rpd(w.verts, w.tets, sph, off, idx, euler=True)
         assert part["euler_denom"] == full["euler_denom"]
-        for k in ("piece_euler", "rpf_off", "rpf_sphere", "rpf_euler"):
+        for k in ("piece_euler", "rpf_off", "rpf_sphere", "rpf_euler", "rpe_off", "rpe_j",
+                  "rpe_k", "rpe_euler", "rpe_fm"):
             assert np.array_equal(part[k], full[k]), k
         prev, n_old = part, len(sph)
 
