@@ -255,6 +255,40 @@ rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
                                  int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,
                                  uint8_t* rpf_fm, uint64_t* rpf_adj);
 
+/* ---- Restricted power edges
+ *
+ * "we are expecting each restricted element (i.e., RPC, RPF, RPE) to have CC=1 and Euler=1"
+ * (PAPER.md:439); "we collect the fractional Euler characteristics for all of its restricted
+ * elements (RPCs, RPFs, RPEs)".  RPE(m_i, m_j, m_k) seen from m_i (j < k) is
+ * the union of the edges of m_i's pieces lying on both radical planes h_ij and h_ik (elements
+ * of the symbolically perturbed pieces, like rpd_get_euler).  Per piece its RPE list; per
+ * (i, j, k) the fractional Euler characteristic V - E (exact numerator over denom, as
+ * rpd_get_euler) and the CC number (the parts glued across shared tet faces at their common
+ * endpoint; needs the whole mesh in the ctx, else tri_cc is NULL).  Needs rpd_set_euler before
+ * the last rpd_clip / rpd_update_partial (RPD_ESTATE) and N < 2^21 (RPD_EINVAL).
+ * Outputs (ctx-owned device arrays, valid until the next mutating call or rpd_get_rpe):
+ *   rpe_off [n_pieces+1], rpe_j / rpe_k [n_rpe] (j < k, ascending per piece), rpe_euler
+ *   [n_rpe] (numerator over denom), rpe_fm [n_rpe] (bit f: an endpoint on tet face f);
+ *   tri [n_tri][3] (i, j, k) ascending, tri_euler [n_tri], tri_cc [n_tri]. */
+typedef struct {
+  int64_t denom;
+  const int32_t* rpe_off;
+  const int32_t* rpe_j;
+  const int32_t* rpe_k;
+  const int64_t* rpe_euler;
+  const uint8_t* rpe_fm;
+  const int32_t* tri;
+  const int64_t* tri_euler;
+  const int32_t* tri_cc;
+  int64_t n_pieces, n_rpe, n_tri;
+} rpd_rpe;
+rpd_status rpd_get_rpe(rpd_ctx* ctx, rpd_rpe* out);
+/* Copy the last rpd_get_rpe outputs (host or device destinations; NULL skips); RPD_ESTATE
+ * before any rpd_get_rpe. */
+rpd_status rpd_download_rpe(rpd_ctx* ctx, int32_t* rpe_off, int32_t* rpe_j, int32_t* rpe_k,
+                            int64_t* rpe_euler, uint8_t* rpe_fm, int32_t* tri,
+                            int64_t* tri_euler, int32_t* tri_cc);
+
 /* ---- Dual medial mesh
  * "Each sub-domain RPC(m_i) ... is dual to a vertex", "the face shared by two adjacent RPCs
  * (RPF) ... dual to an edge e_ij", "the edge shared by three RPCs (RPE) ... dual to a triangle

@@ -178,7 +178,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
-                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->g_map, &c->g_off, &c->g_dst, &c->g_ids, &c->h_dl, &c->h_dm, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->mm_keys, &c->mm_tmp, &c->mm_out};
+                    &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->g_map, &c->g_off, &c->g_dst, &c->g_ids, &c->h_dl, &c->h_dm, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->p_rep, &c->rpe_off, &c->rpe_buf, &c->rpe_ee, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
   CandSet* cs[] = {&c->cand[0], &c->cand[1], &c->cand_d, &c->g_cand[0], &c->g_cand[1]};
   for (CandSet* x : cs) {
@@ -205,6 +205,7 @@ void rpd_destroy(rpd_ctx* c) {
     x->sfm.release();
     x->rfm.release();
     x->radj.release();
+    x->rep.release();
     x->rows.release();
   }
   if (c->pinned) cudaFreeHost(c->pinned);
@@ -476,6 +477,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
     CK(c->p_sfm.ensure(nn), "alloc");
     CK(c->p_rfm.ensure(32 * nw), "alloc");
     CK(c->p_radj.ensure(sizeof(unsigned long long) * 32 * nw), "alloc");
+    CK(c->p_rep.ensure(sizeof(unsigned long long) * 32 * nw), "alloc");
   }
   const int32_t* moff = cs.moff.as<int32_t>();
   // (no memset of the incidence masks: the clip kernels write every word of non-empty pairs)
@@ -543,6 +545,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
       CK(ps.sfm.ensure_slack(npp, 2), "alloc");
       CK(ps.rfm.ensure_slack(nrr, 2), "alloc");
       CK(ps.radj.ensure_slack(sizeof(unsigned long long) * nrr, 2), "alloc");
+      CK(ps.rep.ensure_slack(sizeof(unsigned long long) * nrr, 2), "alloc");
     }
   }
   PieceDst d{ps.off.as<int32_t>(),
@@ -559,6 +562,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
              c->euler ? dst.sfm.as<uint8_t>() + P0 : nullptr,
              c->euler ? dst.rfm.as<uint8_t>() + R0 : nullptr,
              c->euler ? dst.radj.as<unsigned long long>() + R0 : nullptr,
+             c->euler ? dst.rep.as<unsigned long long>() + R0 : nullptr,
              (int32_t)I0,
              (int32_t)R0};
   CK(launch_compact_pieces(c, nt, n, cs.off.as<int32_t>(), cs.idxp(), moff, d),
@@ -619,6 +623,7 @@ static rpd_status compact_state(rpd_ctx* c, int64_t extra) {
     CK(pn.sfm.ensure(room(np)), "alloc");
     CK(pn.rfm.ensure(room(nr)), "alloc");
     CK(pn.radj.ensure(sizeof(unsigned long long) * room(nr)), "alloc");
+    CK(pn.rep.ensure(sizeof(unsigned long long) * room(nr)), "alloc");
   }
   CK(c->m_cnt.ensure(sizeof(int32_t) * 4 * (T > 0 ? T : 1) + sizeof(int32_t) * (nc + 1) + 64),
      "alloc");
@@ -667,7 +672,8 @@ static rpd_status reserve_pools(rpd_ctx* c, int64_t add_c, int64_t add_p, int64_
         (pp.fill_r + add_r) * sizeof(int32_t) <= pp.rpf_j.cap &&
         (pp.fill_r + add_r) * sizeof(long long) <= pp.rpf_e.cap &&
         pp.fill_r + add_r <= (int64_t)pp.rfm.cap &&
-        (pp.fill_r + add_r) * sizeof(unsigned long long) <= pp.radj.cap));
+        (pp.fill_r + add_r) * sizeof(unsigned long long) <= pp.radj.cap &&
+        (pp.fill_r + add_r) * sizeof(unsigned long long) <= pp.rep.cap));
   if (fits) return RPD_OK;
   c->compact = false;  // (force: a compact pool without room is re-laid out with room)
   const int64_t extra = std::max(std::max(add_c, add_p), std::max(add_i, add_r));
@@ -711,6 +717,7 @@ rpd_status rpd_relations(rpd_ctx* c, const double* verts, int64_t V, const int32
   c->have_rel = false;
   c->have_pieces = false;
   c->eu_valid = false;
+  c->rpe_n = -1;
   const double* d_verts = nullptr;
   const int32_t* d_tets = nullptr;
   CK(resolve(c, verts, 3 * V, c->h_verts, &d_verts), "stage verts");
@@ -750,6 +757,7 @@ rpd_status rpd_clip(rpd_ctx* c, rpd_pieces* out) {
   CandSet& cs = c->cand[c->cur];
   c->last.clip_ms = 0.0;
   c->eu_valid = false;
+  c->rpe_n = -1;
   PieceSet& ps = c->pcs[c->cur];
   s = run_clip(c, cs, nullptr, ps);
   if (s) return s;
@@ -821,6 +829,7 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
   CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream), "memset");
   CK(launch_check_new_ids(c, d_new, M, N_old), "check ids");
   *mutated = true;
+  c->rpe_n = -1;
   ++c->epoch;
   rpd_status s = stage_spheres(c, spheres, N_new, nbr_off, nbr_idx, E, true, c->epoch);
   if (s) return s;
@@ -1106,6 +1115,65 @@ rpd_status rpd_download_topology(rpd_ctx* c, int32_t* rpc_cc, int32_t* rpf_cc,
   CK(cp(piece_sosfm, t.piece_sosfm, t.n_pieces), "download");
   CK(cp(rpf_fm, t.rpf_fm, t.n_rpf), "download");
   CK(cp(rpf_adj, t.rpf_adj, sizeof(uint64_t) * t.n_rpf), "download");
+  CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+static rpd_rpe rpe_view(rpd_ctx* c) {
+  const int64_t n = c->rpe_n, n1 = n > 0 ? n : 1;
+  unsigned long long* keys = c->rpe_buf.as<unsigned long long>();
+  int32_t* ej = reinterpret_cast<int32_t*>(keys + 6 * n1);
+  int32_t* ek = ej + n1;
+  int32_t* cc = ek + n1;
+  int32_t* tri = cc + n1;
+  int32_t* par = tri + 3 * n1;
+  rpd_rpe r{};
+  r.denom = c->eu_L;
+  r.rpe_off = c->rpe_off.as<int32_t>();
+  r.rpe_j = ej;
+  r.rpe_k = ek;
+  r.rpe_euler = c->rpe_ee.as<int64_t>();
+  r.rpe_fm = reinterpret_cast<uint8_t*>(par + n1);
+  r.tri = tri;
+  r.tri_euler = reinterpret_cast<int64_t*>(keys + 5 * n1);
+  r.tri_cc = c->eu_whole ? cc : nullptr;
+  r.n_pieces = c->pcs[c->cur].n_pieces;
+  r.n_rpe = n;
+  r.n_tri = c->rpe_nu;
+  return r;
+}
+
+rpd_status rpd_get_rpe(rpd_ctx* c, rpd_rpe* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_get_rpe: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no Euler data (rpd_set_euler, then rpd_clip)");
+  if (c->st.N >= (1 << 21)) return fail(c, RPD_EINVAL, "RPE keys need N < 2^21");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  int64_t n = 0, nu = 0;
+  CK(launch_rpe(c, c->pcs[c->cur], c->eu_whole, &n, &nu), "restricted power edges");
+  CK(cudaStreamSynchronize(c->stream), "restricted power edges");
+  *out = rpe_view(c);
+  return RPD_OK;
+}
+
+rpd_status rpd_download_rpe(rpd_ctx* c, int32_t* rpe_off, int32_t* rpe_j, int32_t* rpe_k,
+                            int64_t* rpe_euler, uint8_t* rpe_fm, int32_t* tri,
+                            int64_t* tri_euler, int32_t* tri_cc) {
+  if (!c) return RPD_EINVAL;
+  if (c->rpe_n < 0 || !c->eu_valid) return fail(c, RPD_ESTATE, "no rpd_get_rpe results");
+  const rpd_rpe r = rpe_view(c);
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst || !src || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
+  };
+  CK(cp(rpe_off, r.rpe_off, sizeof(int32_t) * (r.n_pieces + 1)), "download");
+  CK(cp(rpe_j, r.rpe_j, sizeof(int32_t) * r.n_rpe), "download");
+  CK(cp(rpe_k, r.rpe_k, sizeof(int32_t) * r.n_rpe), "download");
+  CK(cp(rpe_euler, r.rpe_euler, sizeof(int64_t) * r.n_rpe), "download");
+  CK(cp(rpe_fm, r.rpe_fm, r.n_rpe), "download");
+  CK(cp(tri, r.tri, sizeof(int32_t) * 3 * r.n_tri), "download");
+  CK(cp(tri_euler, r.tri_euler, sizeof(int64_t) * r.n_tri), "download");
+  CK(cp(tri_cc, r.tri_cc, sizeof(int32_t) * r.n_tri), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }

@@ -355,6 +355,13 @@ __device__ unsigned long long g_phase[8];
 // when two faces meet, corner c when three do
 __constant__ unsigned char EU_BIDX[16] = {14, 10, 11, 9, 12, 8, 6, 3, 13, 7, 5, 2, 4, 1, 0, 14};
 __device__ __forceinline__ unsigned eu_pm(int p) { return p < 4 ? 1u << p : 0u; }
+// the RPE endpoint record of radical plane x: 16 bits per tet face (ranks + 1 of two planes)
+__device__ __forceinline__ unsigned long long rep_of(const unsigned* epw, int x) {
+  unsigned long long r = 0ull;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) r |= (unsigned long long)((epw[4 * x + f] >> 8) & 0xffffu) << (16 * f);
+  return r;
+}
 
 struct PairOut {
   double* vol;
@@ -376,6 +383,7 @@ struct PairOut {
   uint8_t* sfm;             // per pair: tet faces that are SoS facets (CC numbers, NEXT-2)
   uint8_t* rfm;             // per (pair, row position): tet faces the facet has an edge on
   unsigned long long* radj; // per (pair, row position): radical facets sharing an edge (rank)
+  unsigned long long* rep;  // per (pair, row position): RPE endpoint faces (rpd_ctx.h PieceSet)
 };
 
 // EU: also the fractional Euler characteristics (a separate instantiation, so that the plain
@@ -965,6 +973,18 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           }
         }
       }
+      // RPE endpoint faces: per (radical plane x, tet face f) a count byte and the ranks + 1 of
+      // the (at most two) radical planes y whose edge with x ends on f (free scratch: the
+      // classification batch / the cut staging, unused after the cuts)
+      unsigned* epw = VPL == 1 ? reinterpret_cast<unsigned*>(&S.gb[0][0])
+                               : reinterpret_cast<unsigned*>(&S.Kn[0][0]);
+      static_assert(VPL == 1 ? (int)sizeof(S.gb) >= 16 * MAXP : (int)sizeof(S.Kn) >= 16 * MAXP,
+                    "RPE endpoint scratch");
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int pl = GW * k + lane;
+        if (pl < np) reinterpret_cast<uint4*>(epw)[pl] = make_uint4(0u, 0u, 0u, 0u);
+      }
       __syncwarp(FULL);
       unsigned long long* adj = reinterpret_cast<unsigned long long*>(S.KM);
       long long c2 = 0, cf = 0;
@@ -990,15 +1010,22 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
         if (cc >= 4 && (ma | mb)) atomicOr(S.dsc + cc, ma | mb);
         // medial mesh: a plane pair of the triplet on two radical planes is a restricted power
         // edge RPE(m_i, m_j, m_k) (a triangle of the dual medial mesh)
-        const int pr[3][2] = {{a, b}, {b, cc}, {cc, a}};
+        const int pr[3][3] = {{a, b, cc}, {b, cc, a}, {cc, a, b}};
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-          const int x = pr[r][0], y = pr[r][1];
+          const int x = pr[r][0], y = pr[r][1], z = pr[r][2];
           if (x >= 4 && y >= 4) {
             const int rx = S.c0[x], ry = S.c0[y];
             if (rx < 64 && ry < 64) {
               atomicOr(adj + x, 1ull << ry);
               atomicOr(adj + y, 1ull << rx);
+              if (z < 4) {  // this vertex is an endpoint of RPE (x, y) on tet face z
+                const unsigned sx = atomicAdd(epw + 4 * x + z, 1u) & 0xffu;
+                const unsigned sy = atomicAdd(epw + 4 * y + z, 1u) & 0xffu;
+                if (sx < 2) atomicOr(epw + 4 * x + z, (unsigned)(ry + 1) << (8 * (1 + sx)));
+                if (sy < 2) atomicOr(epw + 4 * y + z, (unsigned)(rx + 1) << (8 * (1 + sy)));
+                if (sx >= 2 || sy >= 2) ++n_euover;  // (not with SoS: a line meets f once)
+              }
             } else {
               ++n_euover;
             }
@@ -1024,6 +1051,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
             rv[pos] = acc[pl] / 2 + out.eu_L;
             out.rfm[32 * (int64_t)mo + pos] = (uint8_t)S.dsc[pl];
             out.radj[32 * (int64_t)mo + pos] = adj[pl];
+            out.rep[32 * (int64_t)mo + pos] = rep_of(epw, pl);
             if (one_word) rbits |= 1u << pos;
             else atomicOr(rw + (pos >> 5), 1u << (pos & 31));
           }
@@ -1187,6 +1215,8 @@ struct EuCompact {
   uint8_t *sfm, *rfm;            // ... compacted (per piece, per radical facet)
   const unsigned long long* p_radj;  // radical-facet adjacency (per pair slot)
   unsigned long long* radj;          // ... compacted (per radical facet)
+  const unsigned long long* p_rep;   // RPE endpoint faces (per pair slot)
+  unsigned long long* rep;           // ... compacted (per radical facet)
   int32_t inc_base, rpf_base;        // value offsets of inc_off / rpf_off (pool append)
 };
 
@@ -1244,6 +1274,7 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
         eu.rpf_e[r] = eu.rval[32 * (int64_t)w0 + pos];
         eu.rfm[r] = eu.p_rfm[32 * (int64_t)w0 + pos];
         eu.radj[r] = eu.p_radj[32 * (int64_t)w0 + pos];
+        eu.rep[r] = eu.p_rep[32 * (int64_t)w0 + pos];
         ++r;
       }
     }
@@ -1312,7 +1343,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
             c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
             c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>(),
             c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(),
-            c->p_radj.as<unsigned long long>()};
+            c->p_radj.as<unsigned long long>(), c->p_rep.as<unsigned long long>()};
   k_clip<GW, VPL, EU><<<(unsigned)grid, THREADS, smem, c->stream>>>(
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
@@ -1428,7 +1459,8 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
         EuCompact{c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_rval.as<long long>(),
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
                   d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm,
-                  c->p_radj.as<unsigned long long>(), d.radj, d.inc_base, d.rpf_base});
+                  c->p_radj.as<unsigned long long>(), d.radj, c->p_rep.as<unsigned long long>(),
+                  d.rep, d.inc_base, d.rpf_base});
     ++c->launches;
   } else {
     // the terminal offsets of an empty batch (the pool's current fill levels)

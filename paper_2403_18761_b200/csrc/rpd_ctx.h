@@ -123,6 +123,9 @@ struct PieceSet {
   DevBuf eu, rpf_off, rpf_j, rpf_e;
   DevBuf sfm, rfm;  // CC flags: SoS tet facets per piece, tet faces next to each radical facet
   DevBuf radj;      // per radical facet: the piece's radical facets sharing an edge (by rank)
+  DevBuf rep;       // per radical facet x: for each tet face f (16 bits each) the ranks + 1 of
+                    // the (at most two) radical facets y whose edge with x -- a restricted
+                    // power edge -- has an endpoint on f
   DevBuf rows;      // int2 [n_tets]  state: [beg, end) of every tet's piece slots
   int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;  // live counts
   int64_t fill_p = 0, fill_i = 0, fill_r = 0;              // state: pool slots in use
@@ -213,8 +216,10 @@ struct rpd_ctx {
   rpd::DevBuf eu_A;            // int64 [256] L / n, then L, then the counts-present bitmap
   rpd::DevBuf eu_sum;          // int64 [N + E + 1]: per-sphere RPC, per-CSR-entry RPF, misses
   rpd::DevBuf p_eu, p_rmask, p_rval, p_nrpf, r_scan;  // per-pair clip outputs
-  rpd::DevBuf p_sfm, p_rfm, p_radj;                   // per-pair CC / medial-mesh flags
+  rpd::DevBuf p_sfm, p_rfm, p_radj, p_rep;            // per-pair CC / medial-mesh flags
   rpd::DevBuf mm_keys, mm_tmp, mm_out;                // medial-mesh extraction scratch
+  rpd::DevBuf rpe_off, rpe_buf, rpe_ee;               // restricted power edges (launch_rpe)
+  int64_t rpe_n = -1, rpe_nu = -1;                     // sizes of the last rpd_get_rpe
   int64_t mm_ne = -1, mm_nf = -1;                     // sizes of the last extraction
   bool eu_whole = false;       // payloads built with the ctx holding the whole mesh in order
   rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
@@ -286,6 +291,7 @@ struct PieceDst {
   uint8_t* sfm;       // [n_pieces], [n_rpf]
   uint8_t* rfm;
   unsigned long long* radj;  // [n_rpf]
+  unsigned long long* rep;   // [n_rpf]
   int32_t inc_base = 0;      // added to every inc_off / rpf_off value (appending to a pool
   int32_t rpf_base = 0;      // whose incidences / radical facets already hold this many)
 };
@@ -359,6 +365,9 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
                                const int32_t* local_ids, int64_t T_local);
 cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps);
 cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
+// restricted power edges: per-piece lists, per-(i, j, k) Euler sums, CC numbers (with_cc)
+cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_rpe,
+                       int64_t* n_tri);
 // medial mesh: unique sorted edge keys (i << 32 | j) and face keys (i << 42 | j << 21 | k)
 cudaError_t launch_medial_mesh(rpd_ctx* c, const PieceSet& ps, int64_t* n_edges,
                                int64_t* n_faces);

@@ -587,4 +587,230 @@ cudaError_t launch_medial_mesh(rpd_ctx* c, const PieceSet& ps, int64_t* n_edges,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- restricted power edges
+//
+// RPE(m_i, m_j, m_k) seen from m_i ("we are expecting each restricted element
+// (i.e., RPC, RPF, RPE) to have CC=1 and Euler=1", 497, 506): in every piece of m_i the edge
+// on the radical planes h_ij and h_ik (j < k).  The clip records, per radical facet x, which
+// other radical facets y share an edge with it (rpf_adj) and on which tet faces those edges
+// end (rep: 16 bits per face holding the ranks + 1 of at most two y).  Here one thread per
+// tet expands them into the per-piece RPE list (ascending (j, k)) with the edge's fractional
+// Euler characteristic V - E = pay(end 1) + pay(end 2) - pay(edge): the edge lies inside the
+// tet (payload 1), an end on tet face f carries f's payload, an end inside the tet 1.  Per-
+// (i, j, k) sums by CUB sort + reduce-by-key (library primitives); CC numbers by union-find
+// over the per-piece edges, two joined across a shared tet face when both end on it (a line
+// meets the face's plane once, so the two ends are the same point).
+
+__device__ __forceinline__ unsigned rep_faces(unsigned long long rep, int b) {
+  unsigned F = 0u;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const unsigned w = (unsigned)(rep >> (16 * f)) & 0xffffu;
+    if ((w & 0xffu) == (unsigned)(b + 1) || ((w >> 8) & 0xffu) == (unsigned)(b + 1)) F |= 1u << f;
+  }
+  return F;
+}
+
+// one thread per tet: the RPE list of each of its pieces (count at rpe_off, emitted in
+// (rank a, rank b) order = ascending (j, k)); keys (i << 42 | j << 21 | k) and values for the
+// per-(i, j, k) sums
+__global__ void k_rpe_emit(int64_t T, const int32_t* __restrict__ poff,
+                           const int32_t* __restrict__ psph, const int32_t* __restrict__ roff,
+                           const int32_t* __restrict__ rj,
+                           const unsigned long long* __restrict__ radj,
+                           const unsigned long long* __restrict__ rep,
+                           const int32_t* __restrict__ eoff, const uint4* __restrict__ rec,
+                           const long long* __restrict__ A, long long L,
+                           int32_t* __restrict__ ej, int32_t* __restrict__ ek,
+                           long long* __restrict__ ee, uint8_t* __restrict__ efm,
+                           unsigned long long* __restrict__ keys, long long* __restrict__ vals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint4 rc = rec[t];
+  long long pf[4];  // payload numerators of the tet's 4 faces (record bytes 10..13)
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int m = 10 + f;
+    const unsigned w = m < 12 ? rc.z : rc.w;
+    pf[f] = A[(w >> (8 * (m & 3))) & 0xffu];
+  }
+  for (int q = poff[t]; q < poff[t + 1]; ++q) {
+    const long long i = psph[q];
+    const int r0 = roff[q], r1 = roff[q + 1];
+    int m = eoff[q];
+    for (int r = r0; r < r1; ++r) {
+      const int a = r - r0;
+      unsigned long long bits = a < 63 ? radj[r] >> (a + 1) : 0ull;
+      while (bits) {
+        const int b = a + __ffsll((long long)bits);
+        bits &= bits - 1ull;
+        const unsigned F = rep_faces(rep[r], b);
+        long long v = L;  // (1 - |F|) L + sum of the faces' payloads
+        for (int f = 0; f < 4; ++f)
+          if ((F >> f) & 1u) v += pf[f] - L;
+        const long long j = rj[r], k = rj[r0 + b];
+        ej[m] = (int32_t)j;
+        ek[m] = (int32_t)k;
+        ee[m] = v;
+        efm[m] = (uint8_t)F;
+        keys[m] = ((unsigned long long)i << 42) | ((unsigned long long)j << 21) |
+                  (unsigned long long)k;
+        vals[m] = v;
+        ++m;
+      }
+    }
+  }
+}
+
+// index of RPE (j, k) in a piece's list [lo, hi), or -1 (lists are short)
+__device__ __forceinline__ int rpe_find(const int32_t* ej, const int32_t* ek, int lo, int hi,
+                                        int j, int k) {
+  for (int m = lo; m < hi; ++m)
+    if (ej[m] == j && ek[m] == k) return m;
+  return -1;
+}
+
+__global__ void k_rpe_link(int64_t T, const int* __restrict__ adj, const int32_t* __restrict__ poff,
+                           const int32_t* __restrict__ psph, const int32_t* __restrict__ eoff,
+                           const int32_t* __restrict__ ej, const int32_t* __restrict__ ek,
+                           const uint8_t* __restrict__ efm, int* __restrict__ par) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  for (int f = 0; f < 4; ++f) {
+    const int nb = adj[4 * t + f];
+    if (nb < 0 || (nb >> 2) < t) continue;  // each shared face once
+    const int t2 = nb >> 2, f2 = nb & 3;
+    const int q0 = poff[t2], q1 = poff[t2 + 1];
+    for (int q = p0; q < p1; ++q) {
+      const int q2 = find_sorted(psph, q0, q1, psph[q]);
+      if (q2 < 0) continue;
+      for (int m = eoff[q]; m < eoff[q + 1]; ++m) {
+        if (!((efm[m] >> f) & 1)) continue;
+        const int m2 = rpe_find(ej, ek, eoff[q2], eoff[q2 + 1], ej[m], ek[m]);
+        if (m2 >= 0 && ((efm[m2] >> f2) & 1)) uf_union(par, m, m2);
+      }
+    }
+  }
+}
+
+// a root edge counts one component of its (i, j, k): binary search of its key among the
+// sorted unique keys
+__global__ void k_rpe_cc(int64_t n, int* __restrict__ par, const unsigned long long* __restrict__ keys,
+                         const unsigned long long* __restrict__ ukeys, int64_t nu,
+                         int* __restrict__ cc) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n || uf_find(par, (int)m) != m) return;
+  const unsigned long long key = keys[m];
+  int64_t lo = 0, hi = nu;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (ukeys[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < nu && ukeys[lo] == key) atomicAdd(cc + lo, 1);
+}
+
+__global__ void k_rpe_decode(int64_t nu, const unsigned long long* __restrict__ uk,
+                             int32_t* __restrict__ tri) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= nu) return;
+  const unsigned long long k = uk[x];
+  tri[3 * x] = (int32_t)(k >> 42);
+  tri[3 * x + 1] = (int32_t)((k >> 21) & 0x1fffffull);
+  tri[3 * x + 2] = (int32_t)(k & 0x1fffffull);
+}
+
+// the per-piece RPE lists, their per-(i, j, k) sums and (with_cc) CC numbers.  Layout in
+// c->rpe_buf: eoff [np+1] | ej, ek [n] | efm [n] | ee [n] | keys, vals, sorted keys / vals
+// [n] | unique keys, sums [n] | cc [n] | tri [3n] | union-find parents [n]
+cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_rpe,
+                       int64_t* n_tri) {
+  const int64_t np = ps.n_pieces, nr = ps.n_rpf, T = ps.n_tets;
+  cudaError_t e;
+  if ((e = c->cc_par.ensure(sizeof(int32_t) * (2 * np + 2)))) return e;
+  int32_t* cnt = c->cc_par.as<int32_t>();
+  if ((e = c->rpe_off.ensure(sizeof(int32_t) * (np + 1)))) return e;
+  int32_t* eoff = c->rpe_off.as<int32_t>();
+  if (np > 0) {
+    k_mm_count<<<nblk(np, 256), 256, 0, c->stream>>>(np, ps.rpf_off.as<int32_t>(),
+                                                     ps.radj.as<unsigned long long>(), cnt);
+    ++c->launches;
+  }
+  if ((e = launch_scan_i32(c, cnt, eoff, np))) return e;
+  int32_t nn = 0;
+  if ((e = cudaMemcpyAsync(&nn, eoff + np, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream)))
+    return e;
+  if ((e = cudaStreamSynchronize(c->stream))) return e;
+  const int64_t n = nn, n1 = n > 0 ? n : 1;
+  // 8-byte arrays first, then 4-byte, then bytes
+  const size_t bytes = 8 * (6 * n1) + 4 * (2 * n1 + n1 + 3 * n1 + n1) + n1 + 64;
+  if ((e = c->rpe_buf.ensure(bytes))) return e;
+  unsigned long long* keys = c->rpe_buf.as<unsigned long long>();
+  long long* vals = reinterpret_cast<long long*>(keys + n1);
+  unsigned long long* skeys = keys + 2 * n1;
+  long long* svals = reinterpret_cast<long long*>(keys + 3 * n1);
+  unsigned long long* ukeys = keys + 4 * n1;
+  long long* usums = reinterpret_cast<long long*>(keys + 5 * n1);
+  int32_t* ej = reinterpret_cast<int32_t*>(keys + 6 * n1);
+  int32_t* ek = ej + n1;
+  int32_t* cc = ek + n1;
+  int32_t* tri = cc + n1;
+  int32_t* par = tri + 3 * n1;
+  uint8_t* efm = reinterpret_cast<uint8_t*>(par + n1);
+  if ((e = c->rpe_ee.ensure(sizeof(long long) * n1))) return e;
+  long long* ee = c->rpe_ee.as<long long>();
+  if (T > 0 && np > 0) {
+    k_rpe_emit<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.rpf_off.as<int32_t>(),
+        ps.rpf_j.as<int32_t>(), ps.radj.as<unsigned long long>(),
+        ps.rep.as<unsigned long long>(), eoff, c->eu_rec.as<uint4>(), c->eu_A.as<long long>(),
+        c->eu_L, ej, ek, ee, efm, keys, vals);
+    ++c->launches;
+  }
+  int64_t nu = 0;
+  if (n > 0) {
+    // per-(i, j, k) sums: sort by key, reduce by key (CUB)
+    size_t b1 = 0, b2 = 0;
+    int* d_nu = par;  // (scratch: parents are initialised below)
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, b1, keys, skeys, vals, svals, (int)n, 0,
+                                             63, c->stream)))
+      return e;
+    if ((e = cub::DeviceReduce::ReduceByKey(nullptr, b2, skeys, ukeys, svals, usums, d_nu,
+                                            cuda::std::plus<long long>(), (int)n, c->stream)))
+      return e;
+    if ((e = c->mm_tmp.ensure(b1 > b2 ? b1 : b2))) return e;
+    size_t bt = c->mm_tmp.cap;
+    if ((e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bt, keys, skeys, vals, svals, (int)n,
+                                             0, 63, c->stream)))
+      return e;
+    bt = c->mm_tmp.cap;
+    if ((e = cub::DeviceReduce::ReduceByKey(c->mm_tmp.p, bt, skeys, ukeys, svals, usums, d_nu,
+                                            cuda::std::plus<long long>(), (int)n, c->stream)))
+      return e;
+    c->launches += 2;
+    int hnu = 0;
+    if ((e = cudaMemcpyAsync(&hnu, d_nu, sizeof(int), cudaMemcpyDeviceToHost, c->stream)))
+      return e;
+    if ((e = cudaStreamSynchronize(c->stream))) return e;
+    nu = hnu;
+    if ((e = cudaMemsetAsync(cc, 0, sizeof(int32_t) * n1, c->stream))) return e;
+    k_rpe_decode<<<nblk(nu, 256), 256, 0, c->stream>>>(nu, ukeys, tri);
+    ++c->launches;
+    if (with_cc) {
+      k_cc_init<<<nblk(n, 256), 256, 0, c->stream>>>(n, par);
+      k_rpe_link<<<nblk(T, 128), 128, 0, c->stream>>>(
+          T, c->eu_adj.as<int>(), ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), eoff, ej, ek,
+          efm, par);
+      k_rpe_cc<<<nblk(n, 256), 256, 0, c->stream>>>(n, par, keys, ukeys, nu, cc);
+      c->launches += 3;
+    }
+  }
+  c->rpe_n = n;
+  c->rpe_nu = nu;
+  *n_rpe = n;
+  *n_tri = nu;
+  return cudaGetLastError();
+}
+
 }  // namespace rpd

@@ -162,6 +162,7 @@ struct PoolSrc {
   const long long* p_rpf_e;
   const uint8_t *p_sfm, *p_rfm;
   const unsigned long long* p_radj;
+  const unsigned long long* p_rep;
 };
 
 // per-tet counts of the compacted sets: candidates, pieces, incidences, radical facets
@@ -185,6 +186,7 @@ struct PoolDst {
   long long* p_rpf_e;
   uint8_t *p_sfm, *p_rfm;
   unsigned long long* p_radj;
+  unsigned long long* p_rep;
   int32_t* c_words;  // incidence-mask words of every candidate (scanned into moff)
   const int32_t* nbr_off;
 };
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(MT) k_pool_copy(int64_t T, PoolSrc s, PoolDst 
       D.p_rpf_e[r] = s.p_rpf_e[src];
       D.p_rfm[r] = s.p_rfm[src];
       D.p_radj[r] = s.p_radj[src];
+      D.p_rep[r] = s.p_rep[src];
     }
   for (int r = s_ni[0] + threadIdx.x; r < s_ni[nt]; r += blockDim.x) {
     const int l = tile_seg(s_ni, nt, r);
@@ -277,7 +280,8 @@ static PoolSrc pool_src(const CandSet& cs, const PieceSet& ps, bool eu) {
                  ps.vol.as<double>(),      ps.m1.as<double>(),      ps.fm.as<uint8_t>(),
                  eu ? ps.eu.as<long long>() : nullptr, ps.rpf_off.as<int32_t>(),
                  ps.rpf_j.as<int32_t>(),   ps.rpf_e.as<long long>(), ps.sfm.as<uint8_t>(),
-                 ps.rfm.as<uint8_t>(),     ps.radj.as<unsigned long long>()};
+                 ps.rfm.as<uint8_t>(),     ps.radj.as<unsigned long long>(),
+                 ps.rep.as<unsigned long long>()};
 }
 
 // phase 0: per-tet counts and their scans (cand offsets -> cn.off, piece offsets -> pn.off,
@@ -307,6 +311,7 @@ cudaError_t launch_compact_state(rpd_ctx* c, int64_t T, const CandSet& co, const
             eu ? pn.eu.as<long long>() : nullptr, pn.rpf_off.as<int32_t>(),
             pn.rpf_j.as<int32_t>(),     pn.rpf_e.as<long long>(), pn.sfm.as<uint8_t>(),
             pn.rfm.as<uint8_t>(),       pn.radj.as<unsigned long long>(),
+            pn.rep.as<unsigned long long>(),
             c->m_cnt.as<int32_t>(),     c->st.nbr_off.as<int32_t>()};
   if (T > 0) {
     k_pool_copy<<<nblk(T, MT), MT, 0, c->stream>>>(T, s, D);

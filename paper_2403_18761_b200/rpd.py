@@ -29,7 +29,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-            "rpd_download_tets"]
+            "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe"]
 
 
 class RPDError(RuntimeError):
@@ -58,6 +58,12 @@ class _Topology(C.Structure):
                 ("rpf_comp", C.c_void_p), ("piece_sosfm", C.c_void_p), ("rpf_fm", C.c_void_p),
                 ("rpf_adj", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
                 ("E", C.c_int64)]
+
+
+class _Rpe(C.Structure):
+    _fields_ = [("denom", C.c_int64)] + [(k, C.c_void_p) for k in (
+        "rpe_off", "rpe_j", "rpe_k", "rpe_euler", "rpe_fm", "tri", "tri_euler", "tri_cc")] + \
+        [("n_pieces", C.c_int64), ("n_rpe", C.c_int64), ("n_tri", C.c_int64)]
 
 
 class _NbrLists(C.Structure):
@@ -143,6 +149,8 @@ def load_library(path: str = LIB_PATH):
     L.rpd_gather_cands.argtypes = [vp, C.POINTER(_Shards), vp, vp]
     L.rpd_merge_shards.argtypes = [vp, C.POINTER(_Shards), C.POINTER(_Csr), C.POINTER(_Csr)]
     L.rpd_download_tets.argtypes = [vp, vp, i64, vp, vp, C.POINTER(_Csr)]
+    L.rpd_get_rpe.argtypes = [vp, C.POINTER(_Rpe)]
+    L.rpd_download_rpe.argtypes = [vp] * 9
     L.rpd_envelope.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, C.POINTER(i64)]
     L.rpd_version.restype = C.c_char_p
     for f in ("rpd_create", "rpd_set_option", "rpd_relations", "rpd_clip", "rpd_update_partial",
@@ -151,7 +159,7 @@ def load_library(path: str = LIB_PATH):
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-              "rpd_download_tets"):
+              "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -383,6 +391,27 @@ class RPDContext:
         self._check(self.L.rpd_download_topology(self.h, *[self._p(a) for a in arrs]))
         return dict(zip(["rpc_cc", "rpf_cc", "piece_comp", "rpf_comp", "piece_sosfm", "rpf_fm",
                          "rpf_adj"], arrs))
+
+    def rpe(self, device=False) -> dict:
+        """Restricted power edges of the current pieces: per piece
+        its RPEs (rpe_off, rpe_j < rpe_k, rpe_euler numerators, rpe_fm endpoint tet faces) and
+        per (i, j, k) seen from m_i (tri [n, 3]) the Euler characteristic (tri_euler over
+        euler_denom) and the CC number (tri_cc; None unless the ctx holds the whole mesh)."""
+        r = _Rpe()
+        self._check(self.L.rpd_get_rpe(self.h, C.byref(r)))
+        specs = [(r.n_pieces + 1, np.int32), (r.n_rpe, np.int32), (r.n_rpe, np.int32),
+                 (r.n_rpe, np.int64), (r.n_rpe, np.uint8), (3 * r.n_tri, np.int32),
+                 (r.n_tri, np.int64), (r.n_tri, np.int32)]
+        arrs = self._alloc(specs, device)
+        if not r.tri_cc:
+            arrs[-1] = None
+        self._check(self.L.rpd_download_rpe(self.h, *[self._p(a) if a is not None else None
+                                                       for a in arrs]))
+        out = dict(zip(["rpe_off", "rpe_j", "rpe_k", "rpe_euler", "rpe_fm", "tri", "tri_euler",
+                        "tri_cc"], arrs))
+        out["tri"] = out["tri"].reshape(-1, 3)
+        out["euler_denom"] = int(r.denom)
+        return out
 
     def medial_mesh(self, device=False) -> dict:
         """The dual medial mesh of the current pieces: unique sorted edges

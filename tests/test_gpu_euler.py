@@ -367,15 +367,112 @@ def test_euler_topology_c4_partial_equals_full(ctx):
         part = ctx.download_euler()
         part.update(ctx.download_topology())
         part_mm = ctx.medial_mesh()
+        part_rpe = ctx.rpe()
         sph, off, idx = w.batches[-1]
         ctx.relations(w.verts, w.tets, sph, off, idx)
         ctx.clip()
         full = ctx.download_euler()
         full.update(ctx.download_topology())
         full_mm = ctx.medial_mesh()
+        full_rpe = ctx.rpe()
     finally:
         ctx.set_euler(None, 0)
     for k in ("rpc_sum", "rpf_sum", "rpc_cc", "rpf_cc"):
         assert np.array_equal(part[k], full[k]), (k, zero_hits)
+    for k in ("tri", "tri_euler", "tri_cc"):
+        assert np.array_equal(part_rpe[k], full_rpe[k]), k
     assert np.array_equal(part_mm["edges"], full_mm["edges"])
     assert np.array_equal(part_mm["faces"], full_mm["faces"])
+
+
+# ---------------------------------------------------------------- restricted power edges
+
+
+def run_gpu_rpe(ctx, w, tets=None, local_ids=None):
+    ctx.set_euler(w.tets, len(w.verts), local_ids)
+    try:
+        ctx.relations(w.verts, w.tets if tets is None else tets, w.spheres, w.nbr_off,
+                      w.nbr_idx)
+        ctx.clip()
+        out = ctx.rpe()
+    finally:
+        ctx.set_euler(None, 0)
+    return out
+
+
+def check_rpe(got, ref, w):
+    """Per-piece RPE lists exactly (ids, endpoint faces, Euler as exact rationals) and the
+    per-(i, j, k) Euler sums and CC numbers against the oracle."""
+    La, Lb = got["euler_denom"], ref["euler_denom"]
+    for k in ("rpe_off", "rpe_j", "rpe_k", "rpe_fm"):
+        assert np.array_equal(got[k], ref[k]), k
+    assert [int(v) * Lb for v in got["rpe_euler"]] == [int(v) * La for v in ref["rpe_euler"]]
+    sums = oracle.rpe_sums(ref)
+    keys = sorted(sums)
+    assert [tuple(x) for x in got["tri"].tolist()] == keys
+    assert [Fraction(int(v), La) for v in got["tri_euler"]] == [sums[k] for k in keys]
+    if got["tri_cc"] is not None:
+        cc = oracle.rpe_topology(ref, w.tets)
+        assert got["tri_cc"].tolist() == [cc[k] for k in keys]
+
+
+@pytest.mark.parametrize("make", MAKERS)
+def test_rpe_parity(ctx, make):
+    """NEXT-1 / PAPER.md:439, 497, 506: the restricted power edges of every piece, their
+    fractional Euler characteristics and the per-(i, j, k) Euler sums and CC numbers equal the
+    oracle's (pinned by explicit exact extraction in test_oracle_pins)."""
+    w = make()
+    got = run_gpu_rpe(ctx, w)
+    check_rpe(got, oracle.rpd_workload(w, euler=True), w)
+
+
+def test_rpe_through_the_hole(ctx):
+    """The RPE of three spheres whose common line crosses the genus-1 solid twice: Euler 2 and
+    CC 2 seen from each sphere (tests/test_oracle_pins.py derives it by hand)."""
+    import copy
+    w = copy.copy(W.make_shape_workload("one", 700, 1, seed=2, cache=False))
+    w.spheres = np.array([[32.0, 32.0, 20.0, 1.0], [32.0, 20.0, 20.0, 1.0],
+                          [32.0, 26.0, 26.0, 1.0]])
+    w.nbr_off = np.array([0, 2, 4, 6], np.int32)
+    w.nbr_idx = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    got = run_gpu_rpe(ctx, w)
+    assert got["tri"].tolist() == [[0, 1, 2], [1, 0, 2], [2, 0, 1]]
+    assert [Fraction(int(v), got["euler_denom"]) for v in got["tri_euler"]] == [2, 2, 2]
+    assert got["tri_cc"].tolist() == [2, 2, 2]
+
+
+def test_rpe_c3_sampled(ctx):
+    """At C3 size (BASELINE.json configs[2]): every per-(i, j, k) RPE Euler sum is an integer
+    and RPE(m_i, m_j, m_k) has the same Euler and CC seen from each of its spheres; the pieces
+    of sampled tets carry the oracle's RPE lists."""
+    w = W.make_config("C3")
+    ctx.set_euler(w.tets, len(w.verts))
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        got = ctx.rpe()
+        pcs = ctx.download_pieces()
+        zh = ctx.stats()["zero_hits"]
+    finally:
+        ctx.set_euler(None, 0)
+    L = got["euler_denom"]
+    assert len(got["tri"]) > 1000
+    assert np.all(got["tri_euler"] % L == 0)
+    if zh == 0:
+        val = {tuple(k): (int(e), int(c)) for k, e, c in zip(got["tri"].tolist(),
+                                                            got["tri_euler"], got["tri_cc"])}
+        for (i, j, k), v in val.items():
+            a, b, c = sorted((i, j, k))
+            assert val.get((a, b, c)) == v and val.get((b, a, c)) == v and val.get((c, a, b)) == v
+    rng = np.random.default_rng(2)
+    ids = np.sort(rng.choice(w.T, 32, replace=False)).astype(np.int32)
+    ref = oracle.rpd_workload(w, tet_ids=ids, euler=True)
+    po, eo = pcs["piece_off"], got["rpe_off"]
+    for a, t in enumerate(ids):
+        for q, qr in zip(range(po[t], po[t + 1]), range(ref["piece_off"][a], ref["piece_off"][a + 1])):
+            g = list(zip(got["rpe_j"][eo[q]:eo[q + 1]].tolist(), got["rpe_k"][eo[q]:eo[q + 1]].tolist(),
+                         got["rpe_fm"][eo[q]:eo[q + 1]].tolist()))
+            ro = ref["rpe_off"]
+            r = list(zip(ref["rpe_j"][ro[qr]:ro[qr + 1]].tolist(), ref["rpe_k"][ro[qr]:ro[qr + 1]].tolist(),
+                         ref["rpe_fm"][ro[qr]:ro[qr + 1]].tolist()))
+            assert g == r, (t, q)
