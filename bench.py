@@ -306,6 +306,14 @@ def side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, t
                 cc.append(ev0.elapsed_time(ev1))
         cc_ms = float(np.median(cc))
         topo = ctx.download_topology()
+        rp = []
+        for s in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rpe = ctx.rpe(device=True)
+            torch.cuda.synchronize()
+            if s >= args.warmup:
+                rp.append(1e3 * (time.perf_counter() - t0))
         mm = []
         for s in range(args.warmup + args.steps):
             torch.cuda.synchronize()
@@ -347,6 +355,12 @@ def side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, t
              "rpc_cc_eq_1": int(np.sum(topo["rpc_cc"] == 1)) if cc_ms is not None else None,
              "rpc_cc_gt_1": int(np.sum(topo["rpc_cc"] > 1)) if cc_ms is not None else None,
              "medial_mesh_ms": float(np.median(mm)) if cc_ms is not None else None,
+             "rpe_ms": float(np.median(rp)) if cc_ms is not None else None,
+             "rpe_triples": int(rpe["tri"].shape[0]) if cc_ms is not None else None,
+             "rpe_euler_eq_1": int(((rpe["tri_euler"] // L) == 1).sum().item())
+             if cc_ms is not None else None,
+             "rpe_cc_eq_1": int((rpe["tri_cc"] == 1).sum().item())
+             if cc_ms is not None else None,
              "medial_edges": int(med["edges"].shape[0]) if cc_ms is not None else None,
              "medial_faces": int(med["faces"].shape[0]) if cc_ms is not None else None,
              "envelope": {"samples": 100_000, "primitives": n_prims,
