@@ -493,7 +493,7 @@ static rpd_status run_clip(rpd_ctx* c, const CandSet& cs, const int32_t* tet_ids
                  cs.cut.as<unsigned>(), c->clip_wide),
      "clip");
   tmark(c, "clip-fast");
-  if (!c->clip_wide && n > 0)
+  if (n > 0)
     CK(launch_clip_overflow(c, cs.pair_tet.as<int32_t>(), tet_ids, cs.idxp(), moff,
                             cs.cut.as<unsigned>()),
        "clip (wide)");

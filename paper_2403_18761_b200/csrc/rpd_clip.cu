@@ -78,7 +78,7 @@ struct alignas(16) WarpState {  // (16-byte aligned: double2 accesses)
   double Fn[MAXS];
   double KMn[MAXS];
   unsigned dsc[MAXV];      // new-vertex descriptors: u | v << 8 | x << 16 | y << 24
-  unsigned char dq[MAXV];  // and their target slot codes (slot, or MAXV + extra number)
+  unsigned short dq[MAXV];  // and their target slot codes (slot, or MAXV + extra number)
   unsigned char xs[MAXV];  // slot of every extra new vertex of the current cut
   unsigned char c0[MAXP];  // cut step: the new vertex whose first (second) plane is p
   unsigned char c1[MAXP];
@@ -389,7 +389,8 @@ struct PairOut {
 // EU: also the fractional Euler characteristics (a separate instantiation, so that the plain
 // clip keeps its register allocation)
 template <int GW, int VPL, bool EU>
-__global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64),
+__global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS
+                                  : (VPL <= 2 ? 256 : (VPL <= 4 ? 64 : 32)),
                                   VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_MINB : (VPL <= 2 ? 2 : 1)) k_clip(
     int64_t n_pairs, const int32_t* __restrict__ pair_list, const int32_t* __restrict__ pair_tet,
     const int32_t* __restrict__ tet_ids, const int32_t* __restrict__ cand_idx,
@@ -716,7 +717,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
               const int x = tri_at(tr, r), y = tri_at(tr, (r + 1) % 3);
               S.dsc[d0 + j] = (unsigned)u | ((unsigned)v << 8) | ((unsigned)x << 16) |
                               ((unsigned)y << 24);
-              S.dq[d0 + j] = (unsigned char)qc;
+              S.dq[d0 + j] = (unsigned short)qc;
               ++j;
             }
           }
@@ -773,7 +774,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
             S.KMn[d] = KMv;
             int qd = S.dq[d];
             if (qd >= WS::MAXV) qd = S.xs[qd - WS::MAXV];
-            S.dq[d] = (unsigned char)qd;  // decoded for the store loop below
+            S.dq[d] = (unsigned short)qd;  // decoded for the store loop below
             const int ru = S.nb[u][0] == v ? 0 : (S.nb[u][1] == v ? 1 : 2);
             S.nb[u][ru] = (unsigned char)qd;
           }
@@ -1311,7 +1312,8 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
                                  const int32_t* cand_idx, const int32_t* moff,
                                  const unsigned* cut, int32_t* over, const int32_t* n_dev,
                                  int* dyn = nullptr) {
-  constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS : (VPL <= 2 ? 256 : 64);
+  constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS
+                         : (VPL <= 2 ? 256 : (VPL <= 4 ? 64 : 32));
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
   size_t smem = sizeof(WarpState<GW, VPL>) * GROUPS;
   // kernel attributes are per device: set / queried once per (instantiation, device) (host API
@@ -1361,7 +1363,7 @@ static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pa
                                   const int32_t* moff, const unsigned* cut, int wide) {
   if (wide)
     return launch_clip_t<32, 4, EU>(c, n_pairs, nullptr, pair_tet, tet_ids, cand_idx, moff, cut,
-                                    nullptr, nullptr);
+                                    c->p_over3.as<int32_t>(), nullptr);
   cudaError_t e = c->p_dyn.ensure(sizeof(int));
   if (e) return e;
   if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
@@ -1395,6 +1397,17 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
 
 // the overflow list p_over[1 .. p_over[0]] (count read on the device) is re-run by the
 // 64-slot kernel <32, RPD_CLIP_MID_VPL = 2>; its own overflows (p_over2) by the 128-slot <32, 4>
+// the slow path: the 128-slot tier's overflows (list p_over3) re-run with 256 vertex / plane
+// slots (one 32-lane group per block, ~45 KB of shared memory); beyond that the clip fails
+// with RPD_EOVERFLOW (8-bit vertex and plane ids)
+template <bool EU>
+static cudaError_t launch_slow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
+                               const int32_t* cand_idx, const int32_t* moff,
+                               const unsigned* cut) {
+  return launch_clip_t<32, 8, EU>(c, 1 << 30, c->p_over3.as<int32_t>() + 1, pair_tet, tet_ids,
+                                  cand_idx, moff, cut, nullptr, c->p_over3.as<int32_t>());
+}
+
 template <bool EU>
 static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                       const int32_t* cand_idx, const int32_t* moff,
@@ -1415,20 +1428,31 @@ static cudaError_t launch_overflow_eu(rpd_ctx* c, const int32_t* pair_tet, const
       c->p_over2.as<int32_t>(), c->p_over.as<int32_t>());
 #endif
   if (e) return e;
-  return launch_clip_t<32, 4, EU>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
-                                  cand_idx, moff, cut, nullptr, c->p_over2.as<int32_t>());
+  e = launch_clip_t<32, 4, EU>(c, 1 << 30, c->p_over2.as<int32_t>() + 1, pair_tet, tet_ids,
+                               cand_idx, moff, cut, c->p_over3.as<int32_t>(),
+                               c->p_over2.as<int32_t>());
+  if (e) return e;
+  return launch_slow<EU>(c, pair_tet, tet_ids, cand_idx, moff, cut);
 }
 
 cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
                                  const unsigned* cut) {
-  if (c->clip_small)  // only the 64-slot tier's overflows remain, for the 128-slot tier
-    return c->euler ? launch_clip_t<32, 4, true>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
-                                                 pair_tet, tet_ids, cand_idx, moff, cut, nullptr,
-                                                 c->p_over2.as<int32_t>())
-                    : launch_clip_t<32, 4, false>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
-                                                  pair_tet, tet_ids, cand_idx, moff, cut, nullptr,
-                                                  c->p_over2.as<int32_t>());
+  if (c->clip_small) {  // only the 64-slot tier's overflows remain: 128 slots, then 256
+    cudaError_t e =
+        c->euler ? launch_clip_t<32, 4, true>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
+                                              pair_tet, tet_ids, cand_idx, moff, cut,
+                                              c->p_over3.as<int32_t>(), c->p_over2.as<int32_t>())
+                 : launch_clip_t<32, 4, false>(c, 1 << 30, c->p_over2.as<int32_t>() + 1,
+                                               pair_tet, tet_ids, cand_idx, moff, cut,
+                                               c->p_over3.as<int32_t>(), c->p_over2.as<int32_t>());
+    if (e) return e;
+    return c->euler ? launch_slow<true>(c, pair_tet, tet_ids, cand_idx, moff, cut)
+                    : launch_slow<false>(c, pair_tet, tet_ids, cand_idx, moff, cut);
+  }
+  if (c->clip_wide)  // the 128-slot tier ran on every pair: its overflows
+    return c->euler ? launch_slow<true>(c, pair_tet, tet_ids, cand_idx, moff, cut)
+                    : launch_slow<false>(c, pair_tet, tet_ids, cand_idx, moff, cut);
   return c->euler ? launch_overflow_eu<true>(c, pair_tet, tet_ids, cand_idx, moff, cut)
                   : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff, cut);
 }

@@ -108,6 +108,44 @@ def test_torch_inputs_other_dtypes_are_stream_ordered(ctx):
         assert not errs, errs[:5]
 
 
+def _shell_workload(n_shell=100):
+    """One big tet; a sphere at c = (12.5, 12.5, 12.5) surrounded by n_shell spheres on a shell
+    of radius 6 (Fibonacci points on the 2^-10 lattice), all radii 0, all-pairs neighbour lists
+    (a superset): the inner sphere's piece is its whole Voronoi cell, a
+    polytope with ~n_shell facets and ~2 n_shell vertices."""
+    import types
+    verts = np.array([[0.0, 0.0, 0.0], [60.0, 0.0, 0.0], [0.0, 60.0, 0.0], [0.0, 0.0, 60.0]])
+    tets = np.array([[0, 1, 2, 3]], np.int32)
+    k = np.arange(n_shell) + 0.5
+    phi = np.arccos(1 - 2 * k / n_shell)
+    th = np.pi * (1 + 5 ** 0.5) * k
+    pts = 12.5 + 6.0 * np.c_[np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)]
+    pts = np.round(pts * 1024) / 1024
+    sph = np.vstack([[12.5, 12.5, 12.5, 0.0], np.c_[pts, np.zeros(n_shell)]])
+    N = len(sph)
+    off = np.arange(N + 1, dtype=np.int32) * (N - 1)
+    idx = np.array([j for i in range(N) for j in range(N) if j != i], np.int32)
+    return types.SimpleNamespace(verts=verts, tets=tets, spheres=sph, nbr_off=off, nbr_idx=idx,
+                                 T=1, N=N)
+
+
+@pytest.mark.parametrize("tiers", [False, True])
+def test_slow_path_large_piece(ctx, tiers):
+    """a piece beyond the 128-slot tier (here ~200 vertices, 104 planes) is
+    clipped by the 256-slot slow path, not dropped: parity with the oracle, and the stats show
+    the large piece."""
+    w = _shell_workload()
+    ctx.set_clip_tiers(tiers)
+    try:
+        got, ref = check(ctx, w)
+    finally:
+        ctx.set_clip_tiers(False)
+    assert got["stats"]["max_vertices"] > 128
+    inner = [p for p in range(len(got["piece_sphere"])) if got["piece_sphere"][p] == 0]
+    assert len(inner) == 1 and len(got["inc_sphere"][got["inc_off"][inner[0]]:
+                                                     got["inc_off"][inner[0] + 1]]) > 90
+
+
 def test_single_sphere(ctx):
     w = W.make_shape_workload("one", 700, 1, seed=2, cache=False)
     got, _ = check(ctx, w)

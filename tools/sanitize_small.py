@@ -24,9 +24,13 @@ for mode in ("all_pairs", "pruned"):
                 ctx.update_partial(s, o, i, np.arange(n_old, len(s), dtype=np.int32))
                 n_old = len(s)
             ctx.download_pieces()
+            ctx.download_cands()
+            if ctx.n_dirty if hasattr(ctx, "n_dirty") else 0:
+                ctx.download_tets(ctx.dirty_ptr(), ctx.n_dirty, {})
             if euler:
                 ctx.download_euler()
                 ctx.download_topology()
+                ctx.rpe()
                 mm = ctx.medial_mesh()
                 smp = W.boundary_samples(w.verts, w.tets, 200, seed=1)
                 sph = w.batches[-1][0] if w.batches else w.spheres
@@ -42,5 +46,13 @@ for mode in ("all_pairs", "pruned"):
         shards.append({k: v.clone() for k, v in ctx.download_pieces(device=True).items()})
         ids.append(torch.as_tensor(tid, device="cuda"))
     ctx.gather_pieces(shards, ids, w.T)
+    # the 256-slot slow path: one tet, a sphere inside a shell of 100 spheres
+    from tests.test_gpu_parity import _shell_workload
+    ws = _shell_workload()
+    ctx.relations(ws.verts, ws.tets, ws.spheres, ws.nbr_off, ws.nbr_idx)
+    ctx.clip()
+    ctx.download_pieces()
+    # sphere neighbours (NEXT-3) of a small set
+    ctx.neighbors(w.spheres, W.mesh_box(w.verts))
     ctx.close()
 print("sanitize run ok")
