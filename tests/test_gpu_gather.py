@@ -166,3 +166,37 @@ def test_gather_bad_tet_id():
         assert e.value.status == -1
     finally:
         ctx.close()
+
+
+def test_gather_c5_two_ranks_equals_single_gpu():
+    """a world-2 gather at C5 size (4M tets, 50k spheres, pruned filter): the two
+    block-cyclic shards, clipped by two ctxs and put back in global order by the gather kernels,
+    are byte-identical to the single-ctx RPD of all tets (candidates and pieces)."""
+    import torch
+    import paper_2403_18761_b200 as P
+    from paper_2403_18761_b200.dist import shard_tets
+    w = W.make_config("C5")
+    ctx = P.RPDContext(0, filter_mode="pruned")
+    try:
+        ctx.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        ctx.clip()
+        ref = ctx.download_cands(device=True)
+        ref.update(ctx.download_pieces(device=True))
+        ref = {k: v.clone() for k, v in ref.items()}
+        shards, ids = [], []
+        for r in range(2):
+            tid = shard_tets(w.T, 2, r)
+            ctx.relations(w.verts, w.tets[tid], w.spheres, w.nbr_off, w.nbr_idx)
+            ctx.clip()
+            counts = (len(tid), ctx.n_cand, ctx.counts.n_pieces, ctx.counts.n_inc)
+            shards.append(_pack(ctx, counts, lambda v: (ctx.download_cands(out=v),
+                                                        ctx.download_pieces(out=v))))
+            ids.append(torch.as_tensor(tid, device="cuda"))
+        nc = sum(int(s["cand_idx"].numel()) for s in shards)
+        npc = sum(int(s["piece_sphere"].numel()) for s in shards)
+        ni = sum(int(s["inc_sphere"].numel()) for s in shards)
+        got = ctx.gather_all(shards, ids, w.T, nc, npc, ni)
+        for k in ref:
+            assert torch.equal(got[k].reshape(ref[k].shape), ref[k]), k
+    finally:
+        ctx.close()
