@@ -8,7 +8,7 @@
 #                                       python tools/ncu_summary.py gpurun_out/prof_TAG.ncu-rep
 set -x
 TAG=${1:-r1}
-python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+python bench.py --no-nbr > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}.csv \
@@ -19,7 +19,14 @@ ncu --set full --clock-control none --import-source on -k regex:"k_clip" -c 2 \
     > gpurun_out/ncu_full_${TAG}.log 2>&1
 # the filter / stage / merge kernels of the first full RPD and first partial update
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_bvh_leaf|k_bvh_super|k_bvh_top|k_stage_rows|k_compact_cands_t|k_merge_copy|k_merge_counts|k_scan" -c 24 \
+    -k regex:"k_bvh_leaf|k_bvh_super|k_bvh_top|k_stage_rows|k_compact_cands_t|k_compact_pieces|k_rows_update|k_dirty_list|k_scan" -c 40 \
     -o gpurun_out/prof_${TAG}_aux python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_aux_${TAG}.log 2>&1
 tail -c 600 gpurun_out/bench_${TAG}.json
+# summaries on the box (the .ncu-rep files are too large to bring back)
+python tools/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep --json gpurun_out/ncu_clip_${TAG}.json > gpurun_out/ncu_clip_${TAG}.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_${TAG}_aux.ncu-rep --json gpurun_out/ncu_aux_${TAG}.json > gpurun_out/ncu_aux_${TAG}.txt 2>&1
+python tools/launch_summary.py gpurun_out/launches_${TAG}.csv > gpurun_out/launch_summary_${TAG}.txt 2>&1
+gzip -f gpurun_out/launches_${TAG}.csv
+ls -la gpurun_out/*.ncu-rep
+rm -f gpurun_out/*.ncu-rep
