@@ -506,26 +506,32 @@ def main():
         nc = ctx.relations(d_verts, d_tets, *d_base)
         ctx.clip()
         e[1].record()
-        st = ctx.stats()
+        st = ctx.stats_struct()  # (ctypes copy; turned into dicts after the timed region)
         if S:
             S.gather_full()
         e[2].record()
-        rec = {"n_cand": nc, "n_pieces": ctx.counts.n_pieces, "filter_ms": st["filter_ms"],
-               "clip_ms": st["clip_ms"], "ev": e, "counters": {k: st[k] for k in CNT},
+        rec = {"n_cand": nc, "n_pieces": ctx.counts.n_pieces, "st": st, "ev": e,
                "bytes": S.bytes_sent if S else 0, "partial": []}
         for (sph, off, idx, new) in d_batches:
             pe = [ev() for _ in range(3)]
             pe[0].record()
             counts, nd = ctx.update_partial(sph, off, idx, new)
             pe[1].record()
-            st = ctx.stats()
+            st = ctx.stats_struct()
             if S:
                 S.exchange_partial(nd)
             pe[2].record()
-            rec["partial"].append({"n_dirty": nd, "ev": pe, "filter_ms": st["filter_ms"],
-                                   "clip_ms": st["clip_ms"], "bytes": S.bytes_sent if S else 0,
-                                   "counters": {k: st[k] for k in CNT}})
+            rec["partial"].append({"n_dirty": nd, "ev": pe, "st": st,
+                                   "bytes": S.bytes_sent if S else 0})
         record.append(rec)
+
+    def unpack(recs):
+        """ctypes stats -> the fields used below (after the timed region)."""
+        for r in recs:
+            for d in [r] + r["partial"]:
+                st = d.pop("st")
+                d["filter_ms"], d["clip_ms"] = st.filter_ms, st.clip_ms
+                d["counters"] = {k: getattr(st, k) for k in CNT}
 
     for s in range(args.warmup):
         step([])
@@ -548,6 +554,7 @@ def main():
     launches = ctx.stats()["kernel_launches"] - launches0
     clocks = sampler.stop()
     torch.cuda.synchronize()
+    unpack(recs)
 
     def el(p):
         return p[0].elapsed_time(p[1]), p[1].elapsed_time(p[2])

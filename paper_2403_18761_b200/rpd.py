@@ -170,8 +170,9 @@ def _ptr(x, dtype):
     try:
         import torch
         if isinstance(x, torch.Tensor):
-            tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
-            x = x.to(tdt).contiguous()
+            tdt = torch.float64 if dtype is np.float64 else torch.int32
+            if x.dtype is not tdt or not x.is_contiguous():  # (fast path: no torch dispatch)
+                x = x.to(tdt).contiguous()
             return (x.data_ptr() if x.numel() else None), x
     except ImportError:
         pass
@@ -286,7 +287,9 @@ class RPDContext:
                                               C.byref(dt), C.byref(nd)))
         self.N = N_new
         self.counts = PieceCounts(P.n_pieces, P.n_inc)
-        self.n_cand = self.stats()["n_cand"]
+        sb = self._sbuf = getattr(self, "_sbuf", None) or _Stats()
+        self._check(self.L.rpd_get_stats(self.h, C.byref(sb)))  # (no dict: on the timed path)
+        self.n_cand = sb.n_cand
         self.n_dirty = nd.value
         self._dirty_ptr = dt.value
         self._keep_p = (ks, ko, ki, kn)
@@ -566,6 +569,12 @@ class RPDContext:
                                         int(np.prod(kf.shape)) // 3, self._p(g), self._p(prim),
                                         C.byref(ne)))
         return g, prim, ne.value
+
+    def stats_struct(self):
+        """The raw rpd_stats struct (a fresh ctypes copy; cheaper than stats() on timed paths)."""
+        st = _Stats()
+        self._check(self.L.rpd_get_stats(self.h, C.byref(st)))
+        return st
 
     def stats(self) -> dict:
         s = _Stats()
