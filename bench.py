@@ -337,9 +337,9 @@ def side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, t
         n_prims = w.N + int(med["edges"].shape[0]) + int(med["faces"].shape[0])
     eu = ctx.download_euler(device=True)
     if world > 1:
-        eu = allreduce_euler(eu)
-    chi = (eu["rpc_sum"] // L).cpu().numpy()
-    integral = bool(torch.all(eu["rpc_sum"] % L == 0).item())
+        eu = allreduce_euler(eu, ctx)
+    chi = eu["rpc_sum"].cpu().numpy()
+    integral = bool(torch.all(eu["rpc_exact"] == 1).item())
     ctx.set_euler(None, 0)
     ef = torch.tensor([float(np.median(e_full)), float(np.median(e_clip))],
                       dtype=torch.float64, device=dev)
@@ -348,7 +348,7 @@ def side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, t
     euler = {"full_rpd_ms": float(ef[0]), "clip_ms": float(ef[1]),
              "clip_overhead_vs_plain": float(ef[1]) / max(float(np.median(
                  [r["clip_ms"] for r in recs])), 1e-9) - 1.0,
-             "denominator": int(L), "rpc_sums_integral": integral,
+             "n_primes": int(L), "rpc_sums_integral": integral,
              "spheres_with_cells": int(np.sum(chi != 0)),
              "rpc_euler_eq_1": int(np.sum(chi == 1)),
              "cc_ms": cc_ms,
@@ -357,7 +357,7 @@ def side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, t
              "medial_mesh_ms": float(np.median(mm)) if cc_ms is not None else None,
              "rpe_ms": float(np.median(rp)) if cc_ms is not None else None,
              "rpe_triples": int(rpe["tri"].shape[0]) if cc_ms is not None else None,
-             "rpe_euler_eq_1": int(((rpe["tri_euler"] // L) == 1).sum().item())
+             "rpe_euler_eq_1": int(((rpe["tri_euler"] // rpe["euler_denom"]) == 1).sum().item())
              if cc_ms is not None else None,
              "rpe_cc_eq_1": int((rpe["tri_cc"] == 1).sum().item())
              if cc_ms is not None else None,

@@ -175,9 +175,12 @@ rpd_status rpd_download_cands(rpd_ctx* ctx, int32_t* cand_off, int32_t* cand_idx
  * over the symbolically perturbed (simple) polytope, and the library reduces them per sphere:
  *   Euler(RPC(m_i))      = sum over the pieces of m_i
  *   Euler(RPF(m_i, m_j)) = sum over their facets on the radical plane h_ij (seen from m_i).
- * All values are EXACT rationals num / denom with denom = lcm of the sharing counts present
- * (integer arithmetic: identical across kernels, launches and ranks); the per-sphere sums of
- * a closed mesh are integers.
+ * All values are EXACT, for any mesh (R24): a piece's values are numerators over its
+ * tet's denominator L_t = lcm of the tet's 14 sharing counts (< 2^62), and every per-sphere sum
+ * is accumulated exactly as an integer part plus one residue modulo p^E per prime p <= 255 that
+ * divides a sharing count (p^E the largest power <= 255): the sum is an integer iff every
+ * residue vanishes, and then the integer is exact.  Integer adds only: identical across
+ * kernels, launches and ranks; the per-sphere sums of a closed mesh are integers.
  *
  * rpd_set_euler: build the payloads of the ctx's tets (call after or before rpd_relations,
  * before rpd_clip; stays on until switched off with tets_all = NULL, T_all = 0).
@@ -187,35 +190,51 @@ rpd_status rpd_download_cands(rpd_ctx* ctx, int32_t* cand_off, int32_t* cand_idx
  *   local_ids [T_local] int32   global index of every ctx-local tet (the tets given to
  *                               rpd_relations), or NULL when the ctx holds all tets in order
  *                               (then T_local must equal T_all)
- *   *denom    host out          the common denominator L (< 2^50)
+ *   *n_primes host out          P, the number of residues of a sum's accumulator row (rows
+ *                               are 1 + P int64: integer part, then the residues)
  * Errors: RPD_EINVAL (bad argument, vertex index out of range), RPD_EOVERFLOW (an element
- * shared by more than 255 tets, or L >= 2^50), RPD_ENOMEM.  rpd_clip fails with RPD_EINVAL
- * if the ctx's tet count differs from T_local. */
+ * shared by more than 255 tets, or some L_t >= 2^62), RPD_ENOMEM.  rpd_clip fails with
+ * RPD_EINVAL if the ctx's tet count differs from T_local. */
 rpd_status rpd_set_euler(rpd_ctx* ctx, const int32_t* tets_all, int64_t T_all, int64_t V,
-                         const int32_t* local_ids, int64_t T_local, int64_t* denom);
+                         const int32_t* local_ids, int64_t T_local, int64_t* n_primes);
 
 /* Euler data of the current pieces (ctx-owned device arrays, valid until the next mutating
  * call).  RPD_ESTATE unless rpd_set_euler preceded the last rpd_clip / rpd_update_partial. */
 typedef struct {
-  int64_t denom;               /* L: every value below is a numerator over L */
-  const int64_t* piece_euler;  /* [n_pieces] Euler of each piece (rpd_pieces order) */
+  int64_t n_primes;            /* P: accumulator rows are [integer part, P residues] */
+  const int64_t* piece_euler;  /* [n_pieces] Euler of each piece, numerator ... */
+  const int64_t* piece_denom;  /* [n_pieces] ... over its tet's L_t (rpd_pieces order) */
   const int32_t* rpf_off;      /* [n_pieces+1] radical facets of each piece ... */
   const int32_t* rpf_sphere;   /* [n_rpf] ... their neighbour j, ascending */
-  const int64_t* rpf_euler;    /* [n_rpf] ... and the Euler of the facet */
-  const int64_t* rpc_sum;      /* [N] Euler(RPC(m_i)) x L over this ctx's tets */
-  const int64_t* rpf_sum;      /* [E] Euler(RPF(m_i, m_j)) x L at the CSR entry of j in row i,
+  const int64_t* rpf_euler;    /* [n_rpf] ... and the Euler of the facet (over the piece's
+                                  denominator) */
+  const int64_t* rpc_sum;      /* [N] Euler(RPC(m_i)) over this ctx's tets: the exact integer
+                                  when rpc_exact[i], else its integer part */
+  const uint8_t* rpc_exact;    /* [N] 1: the sum is an integer */
+  const double* rpc_value;     /* [N] the sum as a double */
+  const int64_t* rpf_sum;      /* [E] Euler(RPF(m_i, m_j)) at the CSR entry of j in row i,
                                   rows sorted ascending by neighbour id (the input order when
-                                  the caller's rows are sorted) */
+                                  the caller's rows are sorted); as rpc_sum */
+  const uint8_t* rpf_exact;    /* [E] */
+  const double* rpf_value;     /* [E] */
+  const int64_t* rpc_acc;      /* [N][1+P] the raw accumulator rows (a sharded job adds them */
+  const int64_t* rpf_acc;      /* [E][1+P]  over the ranks, then rpd_euler_finalize) */
   int64_t n_pieces, n_rpf, N, E;
 } rpd_euler;
 rpd_status rpd_get_euler(rpd_ctx* ctx, rpd_euler* out);
 
-/* Copy the Euler data to caller-owned arrays (host or device; any pointer may be NULL):
- * piece_euler [n_pieces], rpf_off [n_pieces+1], rpf_sphere / rpf_euler [n_rpf],
- * rpc_sum [N], rpf_sum [E].  A sharded job adds rpc_sum / rpf_sum over the ranks. */
-rpd_status rpd_download_euler(rpd_ctx* ctx, int64_t* piece_euler, int32_t* rpf_off,
-                              int32_t* rpf_sphere, int64_t* rpf_euler, int64_t* rpc_sum,
-                              int64_t* rpf_sum);
+/* Copy the Euler data to caller-owned arrays (host or device; any pointer may be NULL; sizes as
+ * in rpd_euler). */
+rpd_status rpd_download_euler(rpd_ctx* ctx, int64_t* piece_euler, int64_t* piece_denom,
+                              int32_t* rpf_off, int32_t* rpf_sphere, int64_t* rpf_euler,
+                              int64_t* rpc_sum, uint8_t* rpc_exact, double* rpc_value,
+                              int64_t* rpf_sum, uint8_t* rpf_exact, double* rpf_value,
+                              int64_t* rpc_acc, int64_t* rpf_acc);
+
+/* Accumulator rows acc [n_rows][1+P] (device; e.g. rpc_acc summed over the ranks of a sharded
+ * job) -> out_sum / out_exact / out_value [n_rows] (device), with the ctx's primes. */
+rpd_status rpd_euler_finalize(rpd_ctx* ctx, const int64_t* acc, int64_t n_rows,
+                              int64_t* out_sum, uint8_t* out_exact, double* out_value);
 
 /* ---- CC numbers (Sec. 4.1.1)
  *
@@ -262,8 +281,9 @@ rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
  * elements (RPCs, RPFs, RPEs)".  RPE(m_i, m_j, m_k) seen from m_i (j < k) is
  * the union of the edges of m_i's pieces lying on both radical planes h_ij and h_ik (elements
  * of the symbolically perturbed pieces, like rpd_get_euler).  Per piece its RPE list; per
- * (i, j, k) the fractional Euler characteristic V - E (exact numerator over denom, as
- * rpd_get_euler) and the CC number (the parts glued across shared tet faces at their common
+ * (i, j, k) the fractional Euler characteristic V - E (exact: tri_euler is a numerator over
+ * denom = 2 -- the endpoint payloads are 1 or 1/2; per-piece rpe_euler over the piece's L_t,
+ * as rpd_get_euler) and the CC number (the parts glued across shared tet faces at their common
  * endpoint; needs the whole mesh in the ctx, else tri_cc is NULL).  Needs rpd_set_euler before
  * the last rpd_clip / rpd_update_partial (RPD_ESTATE) and N < 2^21 (RPD_EINVAL).
  * Outputs (ctx-owned device arrays, valid until the next mutating call or rpd_get_rpe):

@@ -64,6 +64,7 @@ class _Result(C.Structure):
                 ("inc_off", C.POINTER(C.c_int32)), ("inc_sphere", C.POINTER(C.c_int32)),
                 ("n_pieces", C.c_int64), ("n_inc", C.c_int64),
                 ("euler_denom", C.c_int64), ("piece_euler", C.POINTER(C.c_int64)),
+                ("piece_euler_den", C.POINTER(C.c_int64)),
                 ("rpf_off", C.POINTER(C.c_int32)), ("rpf_sphere", C.POINTER(C.c_int32)),
                 ("rpf_euler", C.POINTER(C.c_int64)),
                 ("piece_sosfm", C.POINTER(C.c_uint8)), ("rpf_fm", C.POINTER(C.c_uint8)),
@@ -167,6 +168,7 @@ def rpd(verts, tets, spheres, nbr_off, nbr_idx, tet_ids=None, brute=False, clip=
         if euler and clip:
             out.update({"euler_denom": int(r.euler_denom),
                         "piece_euler": arr(r.piece_euler, r.n_pieces, np.int64),
+                        "piece_euler_den": arr(r.piece_euler_den, r.n_pieces, np.int64),
                         "rpf_off": arr(r.rpf_off, r.n_pieces + 1, np.int32),
                         "rpf_sphere": arr(r.rpf_sphere, r.n_rpf, np.int32),
                         "rpf_euler": arr(r.rpf_euler, r.n_rpf, np.int64),
@@ -263,7 +265,7 @@ def per_tet_lists(res, T):
             eu = None
             if ro is not None and len(ro) == len(res["piece_sphere"]) + 1:
                 eo = res["rpe_off"]
-                eu = (int(res["piece_euler"][p]),
+                eu = ((int(res["piece_euler"][p]), int(res["piece_euler_den"][p])),
                       tuple(res["rpf_sphere"][ro[p]:ro[p + 1]].tolist()),
                       tuple(res["rpf_euler"][ro[p]:ro[p + 1]].tolist()),
                       int(res["piece_sosfm"][p]),
@@ -284,6 +286,7 @@ def from_per_tet_lists(L):
     cand_off = [0]
     cand_idx, piece_off, ps, pv, pm, pf, inc_off, inc = [], [0], [], [], [], [], [0], []
     pe, rpf_off, rpf_j, rpf_e, sfm, rfm, radj = [], [0], [], [], [], [], []
+    pden = []
     rpe_off, rpe = [0], []
     for cands, pcs in L:
         cand_idx += cands
@@ -296,7 +299,8 @@ def from_per_tet_lists(L):
             inc += list(ii)
             inc_off.append(len(inc))
             if eu is not None:
-                pe.append(eu[0])
+                pe.append(eu[0][0])
+                pden.append(eu[0][1])
                 rpf_j += list(eu[1])
                 rpf_e += list(eu[2])
                 sfm.append(eu[3])
@@ -308,7 +312,9 @@ def from_per_tet_lists(L):
         piece_off.append(len(ps))
     eul = {}
     if len(pe) == len(ps) and len(rpf_off) == len(ps) + 1:
-        eul = {"piece_euler": np.array(pe, np.int64), "rpf_off": np.array(rpf_off, np.int32),
+        eul = {"piece_euler": np.array(pe, np.int64),
+               "piece_euler_den": np.array(pden, np.int64),
+               "rpf_off": np.array(rpf_off, np.int32),
                "rpf_sphere": np.array(rpf_j, np.int32), "rpf_euler": np.array(rpf_e, np.int64),
                "piece_sosfm": np.array(sfm, np.uint8), "rpf_fm": np.array(rfm, np.uint8),
                "rpf_adj": np.array(radj, np.uint64),
@@ -392,11 +398,11 @@ def euler_sums(res, N, nbr_off, nbr_idx):
     Fractions: rpc[i] = Euler(RPC(m_i)) = sum over the pieces of m_i; rpf[(i, j)] =
     Euler(RPF(m_i, m_j)) seen from m_i = sum over its pieces' facets on h_ij."""
     from fractions import Fraction
-    L = res["euler_denom"]
     rpc = [Fraction(0)] * N
     rpf = {}
     po, ro = res["piece_off"], res["rpf_off"]
     for p, i in enumerate(res["piece_sphere"].tolist()):
+        L = int(res["piece_euler_den"][p])  # the piece's tet denominator L_t
         rpc[i] += Fraction(int(res["piece_euler"][p]), L)
         for r in range(ro[p], ro[p + 1]):
             key = (i, int(res["rpf_sphere"][r]))
@@ -410,10 +416,10 @@ def rpe_sums(res):
     j, k)] = Euler(RPE(m_i, m_j, m_k)) seen from m_i (j < k) = sum over m_i's pieces of their
     edge on h_ij and h_ik, as exact Fractions."""
     from fractions import Fraction
-    L = res["euler_denom"]
     eo = res["rpe_off"]
     out = {}
     for p, i in enumerate(res["piece_sphere"].tolist()):
+        L = int(res["piece_euler_den"][p])
         for r in range(eo[p], eo[p + 1]):
             key = (i, int(res["rpe_j"][r]), int(res["rpe_k"][r]))
             out[key] = out.get(key, Fraction(0)) + Fraction(int(res["rpe_euler"][r]), L)

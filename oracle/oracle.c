@@ -161,9 +161,11 @@ typedef struct {
   uint8_t* piece_facemask;
   int32_t *inc_off, *inc_sphere;
   int64_t n_pieces, n_inc;
-  /* fractional Euler characteristics (euler = 1): exact rationals num / euler_denom */
-  int64_t euler_denom;
-  int64_t* piece_euler;          /* [n_pieces] Euler of the piece's fractional complex */
+  /* fractional Euler characteristics (euler = 1): exact rationals.  Every value of a piece is a
+     numerator over its tet's denominator L_t = lcm of the tet's 14 sharing counts */
+  int64_t euler_denom;           /* unused (0): the denominators are per tet */
+  int64_t* piece_euler;          /* [n_pieces] Euler of the piece's fractional complex (num) */
+  int64_t* piece_euler_den;      /* [n_pieces] its denominator L_t */
   int32_t *rpf_off, *rpf_sphere; /* [n_pieces + 1], [n_rpf]: radical facets j, ascending */
   int64_t* rpf_euler;            /* [n_rpf] Euler of the piece's facet on h_ij */
   uint8_t* piece_sosfm;          /* [n_pieces] tet faces that are facets of the piece (SoS) */
@@ -330,8 +332,9 @@ int oracle_relation_matrix(const oracle_input* in, const int32_t* tet_ids, int64
  * vertex / edge / face of the tet complex carries 1 / (number of tets sharing it) inside each
  * of those tets ("both vertex b or d are shared between A and B, so their fractional Euler
  * characteristic inside each triangle is only 1/2"), a tet carries 1.  The oracle keeps every
- * payload as an exact integer numerator over the common denominator L = lcm of all sharing
- * counts: payload(element) = L / count.
+ * payload as an exact integer numerator over the tet's own denominator L_t = lcm of the 14
+ * sharing counts of its elements: payload(element) = L_t / count (so any mesh works: no common
+ * denominator of the whole mesh is formed; per-sphere sums are exact Fractions in Python).
  *
  * Per tet t, A[14 t + m]: m = 0..3 corners, 4..9 edges (corner pairs 01 02 03 12 13 23),
  * 10..13 faces (face k opposite corner k).  Counts come from sorting the keys of all
@@ -376,8 +379,9 @@ static int64_t count_key3(const key3* sorted, int64_t n, const key3* key) {
 
 static const int EDGE_CORNERS[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 
-/* payload numerators of every element of every tet and their denominator; 0 or -2 (L too big) */
-static int euler_payloads(const oracle_input* in, int64_t** A_out, int64_t* L_out) {
+/* payload numerators of every element of every tet over the tet's denominator L_t (Lt[t]);
+ * 0, or -2 if some L_t exceeds 2^62 */
+static int euler_payloads(const oracle_input* in, int64_t** A_out, int64_t** Lt_out) {
   int64_t T = in->T, n = T > 0 ? T : 1;
   int64_t* cnt14 = (int64_t*)malloc(sizeof(int64_t) * 14 * n);
   int64_t* vkeys = (int64_t*)malloc(sizeof(int64_t) * 4 * n);
@@ -408,23 +412,25 @@ static int euler_payloads(const oracle_input* in, int64_t** A_out, int64_t* L_ou
   qsort(vs, 4 * T, sizeof(int64_t), cmp_i64);
   qsort(es, 6 * T, sizeof(int64_t), cmp_i64);
   qsort(fs, 4 * T, sizeof(key3), cmp_key3);
-  int64_t L = 1;
+  int64_t* Lt = (int64_t*)malloc(sizeof(int64_t) * n);
   int st = 0;
   for (int64_t t = 0; t < T; ++t) {
     for (int k = 0; k < 4; ++k) cnt14[14 * t + k] = count_i64(vs, 4 * T, vkeys[4 * t + k]);
     for (int e = 0; e < 6; ++e) cnt14[14 * t + 4 + e] = count_i64(es, 6 * T, ekeys[6 * t + e]);
     for (int k = 0; k < 4; ++k) cnt14[14 * t + 10 + k] = count_key3(fs, 4 * T, &fkeys[4 * t + k]);
-    for (int m = 0; m < 14 && !st; ++m) {
+    int64_t L = 1;
+    for (int m = 0; m < 14; ++m) {
       int64_t c = cnt14[14 * t + m];
       int64_t g = gcd64(L, c);
-      if (L / g > ((int64_t)1 << 50) / c) st = -2;
-      else L = L / g * c;
+      if (L / g > ((int64_t)1 << 62) / c) { st = -2; L = 1; break; }
+      L = L / g * c;
     }
+    Lt[t] = L;
+    for (int m = 0; m < 14; ++m) cnt14[14 * t + m] = L / cnt14[14 * t + m];
   }
-  for (int64_t k = 0; k < 14 * T; ++k) cnt14[k] = L / cnt14[k];
   free(vkeys); free(ekeys); free(fkeys); free(vs); free(es); free(fs);
   *A_out = cnt14;
-  *L_out = L;
+  *Lt_out = Lt;
   return st;
 }
 
@@ -582,7 +588,8 @@ typedef struct {
   uint8_t facemask;
   int32_t* inc;
   int32_t ninc;
-  int64_t euler;      /* fractional Euler characteristic of the piece, numerator over L */
+  int64_t euler;      /* fractional Euler characteristic of the piece, numerator over L_t */
+  int64_t den;        /* L_t of the piece's tet */
   int32_t* rpf_j;     /* radical facets of the piece (neighbour j) ... */
   int64_t* rpf_e;     /* ... and the fractional Euler characteristic of each, over L */
   uint8_t* rpf_fm;    /* ... and the tet faces it has an edge on */
@@ -907,6 +914,7 @@ static int clip_piece(const oracle_input* in, const tet_lat* tl, int64_t i, piec
     out->rpe_e = NULL;
     out->rpe_fm = NULL;
     out->sosfm = 0;
+    out->den = Lden;
     if (A14) piece_euler(&P, A14, Lden, out);
   }
   stats_acc->n_clip_tests += P.n_clip_tests;
@@ -941,6 +949,7 @@ void oracle_free(oracle_result* r) {
   free(r->inc_off);
   free(r->inc_sphere);
   free(r->piece_euler);
+  free(r->piece_euler_den);
   free(r->rpf_off);
   free(r->rpf_sphere);
   free(r->rpf_euler);
@@ -965,16 +974,17 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
   if (!tet_ids) n_tets = in->T;
   R->n_tets = n_tets;
   int64_t* A = NULL;
-  int64_t Lden = 0;
+  int64_t* Lt = NULL;
   if (in->euler && do_clip) {
-    if (euler_payloads(in, &A, &Lden)) {
+    if (euler_payloads(in, &A, &Lt)) {
       R->status = -4;
-      snprintf(R->err, 256, "Euler payload denominator exceeds 2^50");
+      snprintf(R->err, 256, "Euler payload denominator of a tet exceeds 2^62");
       free(A);
+      free(Lt);
       return R;
     }
   }
-  R->euler_denom = Lden;
+  R->euler_denom = 0;
   tet_out* O = (tet_out*)calloc(n_tets > 0 ? n_tets : 1, sizeof(tet_out));
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -1000,7 +1010,7 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
       to->pieces = (piece_t*)malloc(sizeof(piece_t) * (to->ncand > 0 ? to->ncand : 1));
       for (int32_t c = 0; c < to->ncand; ++c)
         if (clip_piece(in, &tl, to->cand[c], &to->pieces[to->npieces], &to->st,
-                       A ? A + 14 * t : NULL, Lden))
+                       A ? A + 14 * t : NULL, Lt ? Lt[t] : 0))
           ++to->npieces;
     }
   }
@@ -1024,8 +1034,10 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
   R->rpe_off[0] = 0;
   int64_t e0 = 0;
   free(A);
+  free(Lt);
   R->n_rpf = nr;
   R->piece_euler = (int64_t*)malloc(sizeof(int64_t) * (np ? np : 1));
+  R->piece_euler_den = (int64_t*)malloc(sizeof(int64_t) * (np ? np : 1));
   R->rpf_off = (int32_t*)malloc(sizeof(int32_t) * (np + 1));
   R->rpf_sphere = (int32_t*)malloc(sizeof(int32_t) * (nr ? nr : 1));
   R->rpf_euler = (int64_t*)malloc(sizeof(int64_t) * (nr ? nr : 1));
@@ -1064,6 +1076,7 @@ oracle_result* oracle_rpd(const oracle_input* in, const int32_t* tet_ids, int64_
       memcpy(R->inc_sphere + i0, pc->inc, sizeof(int32_t) * pc->ninc);
       i0 += pc->ninc;
       R->piece_euler[p0] = pc->euler;
+      R->piece_euler_den[p0] = pc->den;
       R->piece_sosfm[p0] = pc->sosfm;
       if (pc->nrpf) {
         memcpy(R->rpf_sphere + r0, pc->rpf_j, sizeof(int32_t) * pc->nrpf);

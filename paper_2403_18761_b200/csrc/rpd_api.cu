@@ -176,7 +176,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
-                    &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->p_eu,
+                    &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->eu_Lt, &c->eu_acc, &c->eu_fin, &c->eu_den, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
                     &c->p_sfm, &c->p_rfm, &c->eu_adj, &c->cc_par, &c->cc_out, &c->cand_long, &c->g_cnt, &c->g_map, &c->g_off, &c->g_dst, &c->g_ids, &c->h_dl, &c->h_dm, &c->env_buf, &c->env_out, &c->h_env, &c->h_env2, &c->h_env3, &c->h_env4, &c->p_radj, &c->p_rep, &c->rpe_off, &c->rpe_buf, &c->rpe_ee, &c->mm_keys, &c->mm_tmp, &c->mm_out};
   for (DevBuf* b : bufs) b->release();
@@ -996,43 +996,47 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
 }
 
 rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
-                         const int32_t* local_ids, int64_t T_local, int64_t* denom) {
+                         const int32_t* local_ids, int64_t T_local, int64_t* n_primes) {
   if (!c) return RPD_EINVAL;
   c->eu_valid = false;
   if (!tets_all && T_all == 0) {  // switch off
     c->euler = 0;
-    if (denom) *denom = 0;
+    if (n_primes) *n_primes = 0;
     return RPD_OK;
   }
   if (!tets_all || T_all < 0 || T_all > 0x7fffffff || V <= 0 || V >= (1ll << 21) ||
-      T_local < 0 || T_local > 0x7fffffff || (!local_ids && T_local != T_all) || !denom)
+      T_local < 0 || T_local > 0x7fffffff || (!local_ids && T_local != T_all) || !n_primes)
     return fail(c, RPD_EINVAL, "rpd_set_euler: bad argument (V must be in (0, 2^21))");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   const int32_t *d_tets = nullptr, *d_ids = nullptr;
   CK(resolve(c, tets_all, 4 * T_all, c->h_eut, &d_tets), "stage tets");
   CK(resolve(c, local_ids, local_ids ? T_local : 0, c->h_euid, &d_ids), "stage ids");
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
-  CK(c->eu_A.ensure(sizeof(long long) * 512), "alloc");
   CK(launch_euler_setup(c, d_tets, T_all, V, d_ids, T_local), "euler setup");
-  Readback* rb = (Readback*)c->pinned;
-  CK(readback(c, RbSpec{{}, reinterpret_cast<const unsigned long long*>(c->eu_A.as<long long>() + 256),
-                        c->errw.as<int>()}),
+  long long table[129];
+  CK(cudaMemcpyAsync(table, c->eu_A.p, sizeof(table), cudaMemcpyDeviceToHost, c->stream),
      "readback");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{}, nullptr, c->errw.as<int>()}), "readback");
   CK(cudaStreamSynchronize(c->stream), "euler setup");
   c->eu_tab.release();  // (hash tables: scratch of the setup only)
   if (rb->err[0] != 0) {
     if (rb->err[1] == 200)
       return fail(c, RPD_EOVERFLOW, "Euler mode: a mesh element is shared by more than 255 tets");
+    if (rb->err[1] == 201)
+      return fail(c, RPD_EOVERFLOW, "Euler mode: a tet's denominator (lcm of its counts) >= 2^62");
     if (rb->err[0] == RPD_ENOMEM) return fail(c, RPD_ENOMEM, "Euler mode: hash table full");
     return check_err(c, rb);
   }
-  const long long L = (long long)rb->u64[0];
-  if (L <= 0) return fail(c, RPD_EOVERFLOW, "Euler payload denominator exceeds 2^50");
+  c->eu_P = (int)table[128];
+  for (int j = 0; j < c->eu_P; ++j) {
+    c->eu_primes[j] = (int)table[j];
+    c->eu_ppow[j] = (int)table[64 + j];
+  }
   c->euler = 1;
   c->eu_whole = local_ids == nullptr;
-  c->eu_L = L;
   c->eu_T = T_local;
-  *denom = L;
+  *n_primes = c->eu_P;
   return RPD_OK;
 }
 
@@ -1040,38 +1044,75 @@ rpd_status rpd_get_euler(rpd_ctx* c, rpd_euler* out) {
   if (!c || !out) return fail(c, RPD_EINVAL, "rpd_get_euler: bad argument");
   if (!c->euler || !c->eu_valid || !c->have_pieces)
     return fail(c, RPD_ESTATE, "no Euler data (rpd_set_euler, then rpd_clip)");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
   const PieceSet& ps = c->pcs[c->cur];
-  out->denom = c->eu_L;
+  CK(launch_piece_den(c, ps), "piece denominators");
+  const int64_t N = c->st.N, E = c->st.E, rows = N + E, W = 1 + c->eu_P;
+  long long* vi = c->eu_fin.as<long long>();
+  double* vd = reinterpret_cast<double*>(vi + rows + 1);
+  uint8_t* ex = reinterpret_cast<uint8_t*>(vd + rows + 1);
+  out->n_primes = c->eu_P;
   out->piece_euler = ps.eu.as<int64_t>();
+  out->piece_denom = c->eu_den.as<int64_t>();
   out->rpf_off = ps.rpf_off.as<int32_t>();
   out->rpf_sphere = ps.rpf_j.as<int32_t>();
   out->rpf_euler = ps.rpf_e.as<int64_t>();
-  out->rpc_sum = c->eu_sum.as<int64_t>();
-  out->rpf_sum = c->eu_sum.as<int64_t>() + c->st.N;
+  out->rpc_sum = reinterpret_cast<const int64_t*>(vi);
+  out->rpc_exact = ex;
+  out->rpc_value = vd;
+  out->rpf_sum = reinterpret_cast<const int64_t*>(vi + N);
+  out->rpf_exact = ex + N;
+  out->rpf_value = vd + N;
+  out->rpc_acc = c->eu_acc.as<int64_t>();
+  out->rpf_acc = c->eu_acc.as<int64_t>() + W * N;
   out->n_pieces = ps.n_pieces;
   out->n_rpf = ps.n_rpf;
-  out->N = c->st.N;
-  out->E = c->st.E;
+  out->N = N;
+  out->E = E;
   return RPD_OK;
 }
 
-rpd_status rpd_download_euler(rpd_ctx* c, int64_t* piece_euler, int32_t* rpf_off,
-                              int32_t* rpf_sphere, int64_t* rpf_euler, int64_t* rpc_sum,
-                              int64_t* rpf_sum) {
+rpd_status rpd_download_euler(rpd_ctx* c, int64_t* piece_euler, int64_t* piece_denom,
+                              int32_t* rpf_off, int32_t* rpf_sphere, int64_t* rpf_euler,
+                              int64_t* rpc_sum, uint8_t* rpc_exact, double* rpc_value,
+                              int64_t* rpf_sum, uint8_t* rpf_exact, double* rpf_value,
+                              int64_t* rpc_acc, int64_t* rpf_acc) {
   rpd_euler e;
   rpd_status s = rpd_get_euler(c, &e);
   if (s) return s;
+  const int64_t W = 1 + e.n_primes;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
     if (!dst || bytes == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream);
   };
   CK(cp(piece_euler, e.piece_euler, sizeof(int64_t) * e.n_pieces), "download");
+  CK(cp(piece_denom, e.piece_denom, sizeof(int64_t) * e.n_pieces), "download");
   CK(cp(rpf_off, e.rpf_off, sizeof(int32_t) * (e.n_pieces + 1)), "download");
   CK(cp(rpf_sphere, e.rpf_sphere, sizeof(int32_t) * e.n_rpf), "download");
   CK(cp(rpf_euler, e.rpf_euler, sizeof(int64_t) * e.n_rpf), "download");
   CK(cp(rpc_sum, e.rpc_sum, sizeof(int64_t) * e.N), "download");
+  CK(cp(rpc_exact, e.rpc_exact, e.N), "download");
+  CK(cp(rpc_value, e.rpc_value, sizeof(double) * e.N), "download");
   CK(cp(rpf_sum, e.rpf_sum, sizeof(int64_t) * e.E), "download");
+  CK(cp(rpf_exact, e.rpf_exact, e.E), "download");
+  CK(cp(rpf_value, e.rpf_value, sizeof(double) * e.E), "download");
+  CK(cp(rpc_acc, e.rpc_acc, sizeof(int64_t) * W * e.N), "download");
+  CK(cp(rpf_acc, e.rpf_acc, sizeof(int64_t) * W * e.E), "download");
   CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_euler_finalize(rpd_ctx* c, const int64_t* acc, int64_t n_rows, int64_t* out_sum,
+                              uint8_t* out_exact, double* out_value) {
+  if (!c) return RPD_EINVAL;
+  if (!c->euler) return fail(c, RPD_ESTATE, "rpd_euler_finalize: Euler mode is off");
+  if (n_rows < 0 || (n_rows > 0 && (!acc || !out_sum || !out_exact || !out_value)))
+    return fail(c, RPD_EINVAL, "rpd_euler_finalize: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(launch_euler_final(c, reinterpret_cast<const unsigned long long*>(acc), n_rows,
+                        reinterpret_cast<long long*>(out_sum), out_value, out_exact),
+     "finalize");
+  CK(cudaStreamSynchronize(c->stream), "finalize");
   return RPD_OK;
 }
 
@@ -1128,7 +1169,7 @@ static rpd_rpe rpe_view(rpd_ctx* c) {
   int32_t* tri = cc + n1;
   int32_t* par = tri + 3 * n1;
   rpd_rpe r{};
-  r.denom = c->eu_L;
+  r.denom = 2;  // tri_euler: halves
   r.rpe_off = c->rpe_off.as<int32_t>();
   r.rpe_j = ej;
   r.rpe_k = ek;

@@ -375,8 +375,7 @@ struct PairOut {
   int32_t* over_count;
   // Euler (eu_rec == nullptr: off)
   const uint4* eu_rec;      // per ctx-local tet: the 14 sharing counts of its elements
-  const long long* eu_A;    // A[n] = L / n
-  long long eu_L;           // common denominator
+  const long long* eu_Lt;   // per ctx-local tet: its denominator L_t = lcm of its 14 counts
   long long* eu_piece;      // per pair: Euler of the piece x L
   unsigned* rmask;          // per pair: SoS radical facets (bits over N(i), incmask layout)
   long long* rval;          // per (pair, row position): Euler of that facet x L
@@ -942,12 +941,15 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     if constexpr (EU) {
       long long* acc = reinterpret_cast<long long*>(S.val);  // per plane: doubled facet sums
       {
+        // payload numerators over the tet's own denominator L_t: L_t / count (any mesh: no
+        // common denominator of the whole mesh is formed)
         const uint4 rc = __ldg(out.eu_rec + t_cur);
+        const long long Lt = __ldg(out.eu_Lt + t_cur);
         if (lane < 14) {
           const unsigned w = lane < 4 ? rc.x : (lane < 8 ? rc.y : (lane < 12 ? rc.z : rc.w));
-          S.pay[lane] = __ldg(out.eu_A + ((w >> (8 * (lane & 3))) & 0xffu));
+          S.pay[lane] = Lt / (long long)((w >> (8 * (lane & 3))) & 0xffu);
         } else if (lane == 14) {
-          S.pay[14] = out.eu_L;
+          S.pay[14] = Lt;
         }
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
@@ -1049,7 +1051,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
           sbits |= eu_pm(pl);
           if (pl >= 4) {  // radical facet: its part of the RPF between m_i and m_j
             const int pos = S.eidx[pl] - e0;
-            rv[pos] = acc[pl] / 2 + out.eu_L;
+            rv[pos] = acc[pl] / 2 + S.pay[14];
             out.rfm[32 * (int64_t)mo + pos] = (uint8_t)S.dsc[pl];
             out.radj[32 * (int64_t)mo + pos] = adj[pl];
             out.rep[32 * (int64_t)mo + pos] = rep_of(epw, pl);
@@ -1069,7 +1071,7 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
       }
       sbits = __reduce_or_sync(FULL, sbits);
       if (lane == 0) {
-        out.eu_piece[p] = c2 / 2 + cf - out.eu_L;
+        out.eu_piece[p] = c2 / 2 + cf - S.pay[14];
         out.sfm[p] = (uint8_t)sbits;
       }
       __syncwarp(FULL);
@@ -1342,7 +1344,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff, cut,
             over ? over + 1 : nullptr, over,
-            c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_A.as<long long>(), c->eu_L,
+            c->euler ? c->eu_rec.as<uint4>() : nullptr, c->eu_Lt.as<long long>(),
             c->p_eu.as<long long>(), c->p_rmask.as<unsigned>(), c->p_rval.as<long long>(),
             c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(),
             c->p_radj.as<unsigned long long>(), c->p_rep.as<unsigned long long>()};

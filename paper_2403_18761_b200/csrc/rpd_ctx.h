@@ -210,10 +210,18 @@ struct rpd_ctx {
   int euler = 0;               // payloads set for the current tets
   bool eu_valid = false;       // the current pieces carry Euler data
   rpd::DevBuf h_eut, h_euid;   // host-input staging of rpd_set_euler
-  int64_t eu_L = 0, eu_T = 0;  // denominator; ctx-local tet count the payloads were built for
+  int64_t eu_T = 0;            // ctx-local tet count the payloads were built for
+  int eu_P = 0;                // primes p <= 255 dividing some sharing count (sum layout)
+  int eu_primes[64] = {}, eu_ppow[64] = {};  // those primes and their powers p^E <= 255
   rpd::DevBuf eu_tab;          // scratch hash tables of the payload setup
   rpd::DevBuf eu_rec;          // uint4 per local tet: sharing counts of its 14 elements
-  rpd::DevBuf eu_A;            // int64 [256] L / n, then L, then the counts-present bitmap
+  rpd::DevBuf eu_A;            // int64 [512]: primes [0, 64), p^E [64, 128), P [128],
+                               // the counts-present bitmap from [257]
+  rpd::DevBuf eu_Lt;           // int64 [T_local]: per tet L_t = lcm of its 14 sharing counts
+  rpd::DevBuf eu_acc;          // int64 [(N + E) (1 + P)]: per-sphere / per-CSR-entry sums as an
+                               // integer part + one residue per prime (exact, any mesh)
+  rpd::DevBuf eu_fin;          // finalised sums: int64 [N + E], double [N + E], uint8 [N + E]
+  rpd::DevBuf eu_den;          // int64 [n_pieces]: each piece's denominator (rpd_get_euler)
   rpd::DevBuf eu_sum;          // int64 [N + E + 1]: per-sphere RPC, per-CSR-entry RPF, misses
   rpd::DevBuf p_eu, p_rmask, p_rval, p_nrpf, r_scan;  // per-pair clip outputs
   rpd::DevBuf p_sfm, p_rfm, p_radj, p_rep;            // per-pair CC / medial-mesh flags
@@ -364,6 +372,10 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
 cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
                                const int32_t* local_ids, int64_t T_local);
 cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps);
+// accumulator rows [K, R_1 .. R_P] -> values (rpd_euler_finalize)
+cudaError_t launch_euler_final(rpd_ctx* c, const unsigned long long* acc, int64_t n,
+                               long long* vi, double* vd, uint8_t* ex);
+cudaError_t launch_piece_den(rpd_ctx* c, const PieceSet& ps);
 cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
 // restricted power edges: per-piece lists, per-(i, j, k) Euler sums, CC numbers (with_cc)
 cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_rpe,

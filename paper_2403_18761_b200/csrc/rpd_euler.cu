@@ -138,7 +138,8 @@ __global__ void k_eu_records(int64_t T_local, const int32_t* __restrict__ local_
                              const unsigned long long* __restrict__ fkeys,
                              const unsigned* __restrict__ fcnt, unsigned long long fmask,
                              const int* __restrict__ fown, int* __restrict__ adj,
-                             uint4* __restrict__ rec, unsigned* __restrict__ present, int* err) {
+                             uint4* __restrict__ rec, long long* __restrict__ Lt,
+                             unsigned* __restrict__ present, int* err) {
   const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (l >= T_local) return;
   const int64_t t = local_ids ? (int64_t)local_ids[l] : l;
@@ -169,6 +170,7 @@ __global__ void k_eu_records(int64_t T_local, const int32_t* __restrict__ local_
   }
   c[14] = c[15] = 0u;
   unsigned w[4] = {0u, 0u, 0u, 0u};
+  long long L = 1;  // the tet's denominator: lcm of its 14 sharing counts
 #pragma unroll
   for (int m = 0; m < 14; ++m) {
     if (c[m] == 0u || c[m] > 255u) {
@@ -180,8 +182,24 @@ __global__ void k_eu_records(int64_t T_local, const int32_t* __restrict__ local_
     }
     w[m >> 2] |= c[m] << (8 * (m & 3));
     atomicOr(present + (c[m] >> 5), 1u << (c[m] & 31));
+    const long long n = c[m];
+    long long a = L, b = n;
+    while (b) {
+      const long long r = a % b;
+      a = b;
+      b = r;
+    }
+    if (L / a > (1ll << 62) / n) {
+      if (atomicCAS(err, 0, (int)RPD_EOVERFLOW) == 0) {
+        err[1] = 201;  // L_t > 2^62
+        err[2] = (int)l;
+      }
+      return;
+    }
+    L = L / a * n;
   }
   rec[l] = make_uint4(w[0], w[1], w[2], w[3]);
+  Lt[l] = L;
 }
 
 __device__ long long gcd_ll(long long a, long long b) {
@@ -193,22 +211,26 @@ __device__ long long gcd_ll(long long a, long long b) {
   return a;
 }
 
-// L = lcm of the counts present; A[n] = L / n (payload numerators); out[0] = L or -1
-__global__ void k_eu_lcm(const unsigned* __restrict__ present, long long* __restrict__ A,
-                         long long* __restrict__ Lout) {
+// The primes p <= 255 dividing some sharing count present, with p^E the largest power of p
+// <= 255 (every denominator's p-part divides it): table[j] = p, table[64 + j] = p^E,
+// table[128] = P.  The per-sphere sums keep one residue modulo p^E per prime (see k_eu_sums).
+__global__ void k_eu_primes(const unsigned* __restrict__ present, long long* __restrict__ table) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  long long L = 1;
-  for (int n = 1; n < 256; ++n) {
-    if (!((present[n >> 5] >> (n & 31)) & 1u)) continue;
-    const long long g = gcd_ll(L, n);
-    if (L / g > (1ll << 50) / n) {
-      *Lout = -1;
-      return;
-    }
-    L = L / g * n;
+  int P = 0;
+  for (int p = 2; p < 256; ++p) {
+    bool prime = true;
+    for (int d = 2; d * d <= p && prime; ++d) prime = p % d != 0;
+    if (!prime) continue;
+    bool used = false;
+    for (int n = p; n < 256 && !used; n += p) used = (present[n >> 5] >> (n & 31)) & 1u;
+    if (!used) continue;
+    long long pe = p;
+    while (pe * p <= 255) pe *= p;
+    table[P] = p;
+    table[64 + P] = pe;
+    ++P;
   }
-  for (int n = 0; n < 256; ++n) A[n] = n > 0 ? L / n : 0;
-  *Lout = L;
+  table[128] = P;
 }
 
 cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int64_t V,
@@ -233,8 +255,8 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
     return e;
   if ((e = c->eu_rec.ensure(sizeof(uint4) * (T_local > 0 ? T_local : 1)))) return e;
   if ((e = c->eu_adj.ensure(sizeof(int) * 4 * (T_local > 0 ? T_local : 1)))) return e;
-  if ((e = c->eu_A.ensure(sizeof(long long) * 256 + sizeof(unsigned) * 8 + sizeof(long long))))
-    return e;
+  if ((e = c->eu_A.ensure(sizeof(long long) * 512))) return e;
+  if ((e = c->eu_Lt.ensure(sizeof(long long) * (T_local > 0 ? T_local : 1)))) return e;
   unsigned* present = reinterpret_cast<unsigned*>(c->eu_A.as<long long>() + 257);
   if ((e = cudaMemsetAsync(present, 0, sizeof(unsigned) * 8, c->stream))) return e;
   int* err = c->errw.as<int>();
@@ -246,59 +268,170 @@ cudaError_t launch_euler_setup(rpd_ctx* c, const int32_t* tets_all, int64_t T_al
   if (T_local > 0) {
     k_eu_records<<<nblk(T_local, 256), 256, 0, c->stream>>>(
         T_local, local_ids, tets_all, V, vcnt, ekeys, ecnt, he - 1, fkeys, fcnt, hf - 1, fown,
-        c->eu_adj.as<int>(), c->eu_rec.as<uint4>(), present, err);
+        c->eu_adj.as<int>(), c->eu_rec.as<uint4>(), c->eu_Lt.as<long long>(), present, err);
     ++c->launches;
   }
-  k_eu_lcm<<<1, 32, 0, c->stream>>>(present, c->eu_A.as<long long>(),
-                                    c->eu_A.as<long long>() + 256);
+  k_eu_primes<<<1, 32, 0, c->stream>>>(present, c->eu_A.as<long long>());
   ++c->launches;
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- per-sphere sums
 
-// rpc[i] += Euler of every piece of sphere i; rpf[e] += Euler of every radical facet whose
-// neighbour j sits at CSR entry e of row i (binary search: rows are sorted ascending).
-// Integer atomics: the sums are exact and independent of the order.
-__global__ void k_eu_sums(int64_t n_pieces, const int32_t* __restrict__ sphere,
-                          const long long* __restrict__ peu, const int32_t* __restrict__ roff,
-                          const int32_t* __restrict__ rj, const long long* __restrict__ re,
+// Exact sums of fractions with different denominators, for any mesh (no common denominator of
+// the whole mesh): a value num / L_t is split by partial fractions into an integer K plus, for
+// every prime power q = p^e exactly dividing L_t, a residue a / q (0 <= a < q), scaled to the
+// prime's fixed power p^E (the largest <= 255, which every sharing count's p-part divides).  The
+// accumulator row of a sum is [K, R_1 .. R_P] (integer adds, order-independent); the value is
+// K + sum_j R_j / p_j^E, an integer iff every R_j is a multiple of p_j^E (partial fractions
+// are unique), then carried into K (k_eu_final).
+struct EuTable {
+  int P;
+  int p[64];
+  int pe[64];
+};
+
+__device__ __forceinline__ long long inv_mod(long long a, long long m) {  // a, m coprime
+  long long g = m, x = 0, x1 = 1, b = a % m;
+  while (b) {  // extended Euclid on (m, b)
+    const long long qq = g / b, t = g - qq * b;
+    g = b;
+    b = t;
+    const long long tx = x - qq * x1;
+    x = x1;
+    x1 = tx;
+  }
+  x %= m;
+  return x < 0 ? x + m : x;
+}
+
+__device__ void frac_add(unsigned long long* acc, long long num, long long L, const EuTable& tb) {
+  __int128 rest = num;
+  for (int j = 0; j < tb.P; ++j) {
+    const long long p = tb.p[j];
+    if (L % p) continue;
+    long long q = p;
+    while (L % (q * p) == 0) q *= p;
+    const long long m = L / q;
+    long long nm = num % q;
+    if (nm < 0) nm += q;
+    const long long a = nm * inv_mod(m % q, q) % q;
+    rest -= (__int128)a * m;
+    if (a) atomicAdd(acc + 1 + j, (unsigned long long)(a * (tb.pe[j] / q)));
+  }
+  const long long K = (long long)(rest / L);  // exact: rest = K L
+  if (K) atomicAdd(acc, (unsigned long long)K);
+}
+
+// one thread per tet: every piece's Euler into its sphere's row, every radical facet's into the
+// row of the CSR entry of (i, j) (binary search: rows are sorted ascending)
+__global__ void k_eu_sums(int64_t T, const int32_t* __restrict__ poff,
+                          const int32_t* __restrict__ sphere, const long long* __restrict__ peu,
+                          const int32_t* __restrict__ roff, const int32_t* __restrict__ rj,
+                          const long long* __restrict__ re, const long long* __restrict__ Lt,
                           const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
-                          unsigned long long* __restrict__ rpc, unsigned long long* __restrict__ rpf,
+                          int64_t N, unsigned long long* __restrict__ acc, EuTable tb,
                           unsigned long long* __restrict__ miss) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n_pieces) return;
-  const int i = sphere[q];
-  atomicAdd(rpc + i, (unsigned long long)peu[q]);
-  const int e0 = nbr_off[i], e1 = nbr_off[i + 1];
-  for (int r = roff[q]; r < roff[q + 1]; ++r) {
-    const int j = rj[r];
-    int lo = e0, hi = e1;  // first entry >= j
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (nbr_idx[mid] < j) lo = mid + 1;
-      else hi = mid;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const long long L = Lt[t];
+  const int W = 1 + tb.P;
+  for (int q = poff[t]; q < poff[t + 1]; ++q) {
+    const int i = sphere[q];
+    frac_add(acc + (int64_t)W * i, peu[q], L, tb);
+    const int e0 = nbr_off[i], e1 = nbr_off[i + 1];
+    for (int r = roff[q]; r < roff[q + 1]; ++r) {
+      const int j = rj[r];
+      int lo = e0, hi = e1;  // first entry >= j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (nbr_idx[mid] < j) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < e1 && nbr_idx[lo] == j) frac_add(acc + (int64_t)W * (N + lo), re[r], L, tb);
+      else atomicAdd(miss, 1ull);  // a kept facet whose neighbour left the row (R12 degenerate)
     }
-    if (lo < e1 && nbr_idx[lo] == j) atomicAdd(rpf + lo, (unsigned long long)re[r]);
-    else atomicAdd(miss, 1ull);  // a kept facet whose neighbour left the row (R12 degenerate)
   }
 }
 
+// accumulator rows -> integer value (exact when `exact`), value as a double
+__global__ void k_eu_final(int64_t n, const unsigned long long* __restrict__ acc, EuTable tb,
+                           long long* __restrict__ vi, double* __restrict__ vd,
+                           uint8_t* __restrict__ ex) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const unsigned long long* a = acc + (int64_t)(1 + tb.P) * x;
+  long long K = (long long)a[0];
+  double frac = 0.0;
+  bool exact = true;
+  for (int j = 0; j < tb.P; ++j) {
+    const unsigned long long R = a[1 + j], pe = (unsigned long long)tb.pe[j];
+    K += (long long)(R / pe);
+    const unsigned long long rho = R % pe;
+    exact &= rho == 0ull;
+    frac += (double)rho / (double)pe;
+  }
+  vi[x] = K;
+  vd[x] = (double)K + frac;
+  ex[x] = exact ? 1 : 0;
+}
+
+static EuTable eu_table(rpd_ctx* c) {
+  EuTable tb{};
+  tb.P = c->eu_P;
+  for (int j = 0; j < c->eu_P && j < 64; ++j) {
+    tb.p[j] = c->eu_primes[j];
+    tb.pe[j] = c->eu_ppow[j];
+  }
+  return tb;
+}
+
+cudaError_t launch_euler_final(rpd_ctx* c, const unsigned long long* acc, int64_t n,
+                               long long* vi, double* vd, uint8_t* ex) {
+  if (n <= 0) return cudaSuccess;
+  k_eu_final<<<nblk(n, 256), 256, 0, c->stream>>>(n, acc, eu_table(c), vi, vd, ex);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+// eu_acc [(N + E) (1 + P)] accumulators; eu_fin: int64 [N+E] values, double [N+E], uint8 [N+E]
+// exactness, and one miss counter
 cudaError_t launch_euler_sums(rpd_ctx* c, const PieceSet& ps) {
-  const int64_t N = c->st.N, E = c->st.E;
+  const int64_t N = c->st.N, E = c->st.E, W = 1 + c->eu_P, rows = N + E;
   cudaError_t e;
-  if ((e = c->eu_sum.ensure(sizeof(long long) * (N + E + 1)))) return e;
-  long long* rpc = c->eu_sum.as<long long>();
-  if ((e = cudaMemsetAsync(rpc, 0, sizeof(long long) * (N + E + 1), c->stream))) return e;
-  if (ps.n_pieces > 0) {
-    k_eu_sums<<<nblk(ps.n_pieces, 256), 256, 0, c->stream>>>(
-        ps.n_pieces, ps.sphere.as<int32_t>(), ps.eu.as<long long>(), ps.rpf_off.as<int32_t>(),
-        ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>(), c->st.nbr_off.as<int32_t>(),
-        c->st.nbr_idx.as<int32_t>(), reinterpret_cast<unsigned long long*>(rpc),
-        reinterpret_cast<unsigned long long*>(rpc + N),
-        reinterpret_cast<unsigned long long*>(rpc + N + E));
+  if ((e = c->eu_acc.ensure(sizeof(long long) * (W * rows + 1)))) return e;
+  if ((e = c->eu_fin.ensure((sizeof(long long) + sizeof(double) + 1) * (rows + 1) + 64))) return e;
+  unsigned long long* acc = c->eu_acc.as<unsigned long long>();
+  if ((e = cudaMemsetAsync(acc, 0, sizeof(long long) * (W * rows + 1), c->stream))) return e;
+  const int64_t T = ps.n_tets;
+  if (T > 0 && ps.n_pieces > 0) {
+    k_eu_sums<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.eu.as<long long>(),
+        ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(), ps.rpf_e.as<long long>(),
+        c->eu_Lt.as<long long>(), c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), N,
+        acc, eu_table(c), acc + W * rows);
     ++c->launches;
   }
+  long long* vi = c->eu_fin.as<long long>();
+  double* vd = reinterpret_cast<double*>(vi + rows + 1);
+  uint8_t* ex = reinterpret_cast<uint8_t*>(vd + rows + 1);
+  return launch_euler_final(c, acc, rows, vi, vd, ex);
+}
+
+// per piece its tet's denominator (rpd_get_euler)
+__global__ void k_piece_den(int64_t T, const int32_t* __restrict__ poff,
+                            const long long* __restrict__ Lt, long long* __restrict__ den) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  for (int q = poff[t]; q < poff[t + 1]; ++q) den[q] = Lt[t];
+}
+
+cudaError_t launch_piece_den(rpd_ctx* c, const PieceSet& ps) {
+  cudaError_t e = c->eu_den.ensure(sizeof(long long) * (ps.n_pieces > 0 ? ps.n_pieces : 1));
+  if (e || ps.n_tets == 0) return e;
+  k_piece_den<<<nblk(ps.n_tets, 256), 256, 0, c->stream>>>(
+      ps.n_tets, ps.off.as<int32_t>(), c->eu_Lt.as<long long>(), c->eu_den.as<long long>());
+  ++c->launches;
   return cudaGetLastError();
 }
 
@@ -620,19 +753,20 @@ __global__ void k_rpe_emit(int64_t T, const int32_t* __restrict__ poff,
                            const unsigned long long* __restrict__ radj,
                            const unsigned long long* __restrict__ rep,
                            const int32_t* __restrict__ eoff, const uint4* __restrict__ rec,
-                           const long long* __restrict__ A, long long L,
+                           const long long* __restrict__ Lt,
                            int32_t* __restrict__ ej, int32_t* __restrict__ ek,
                            long long* __restrict__ ee, uint8_t* __restrict__ efm,
                            unsigned long long* __restrict__ keys, long long* __restrict__ vals) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint4 rc = rec[t];
-  long long pf[4];  // payload numerators of the tet's 4 faces (record bytes 10..13)
+  const long long L = Lt[t];
+  long long h2[4];  // twice the payload of the tet's 4 faces minus 2: 2 / count - 2 (0 or -1)
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const int m = 10 + f;
     const unsigned w = m < 12 ? rc.z : rc.w;
-    pf[f] = A[(w >> (8 * (m & 3))) & 0xffu];
+    h2[f] = 2 / (long long)((w >> (8 * (m & 3))) & 0xffu) - 2;
   }
   for (int q = poff[t]; q < poff[t + 1]; ++q) {
     const long long i = psph[q];
@@ -645,17 +779,18 @@ __global__ void k_rpe_emit(int64_t T, const int32_t* __restrict__ poff,
         const int b = a + __ffsll((long long)bits);
         bits &= bits - 1ull;
         const unsigned F = rep_faces(rep[r], b);
-        long long v = L;  // (1 - |F|) L + sum of the faces' payloads
+        long long v2 = 2;  // twice V - E: 2 (1 - |F|) + sum of twice the faces' payloads
         for (int f = 0; f < 4; ++f)
-          if ((F >> f) & 1u) v += pf[f] - L;
+          if ((F >> f) & 1u) v2 += h2[f];
         const long long j = rj[r], k = rj[r0 + b];
         ej[m] = (int32_t)j;
         ek[m] = (int32_t)k;
-        ee[m] = v;
+        // numerator over L_t: (v2 / 2) L_t (v2 odd only with a face of count 2: L_t even)
+        ee[m] = (L & 1) ? (v2 / 2) * L : v2 * (L / 2);
         efm[m] = (uint8_t)F;
         keys[m] = ((unsigned long long)i << 42) | ((unsigned long long)j << 21) |
                   (unsigned long long)k;
-        vals[m] = v;
+        vals[m] = v2;
         ++m;
       }
     }
@@ -764,8 +899,8 @@ cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_
     k_rpe_emit<<<nblk(T, 128), 128, 0, c->stream>>>(
         T, ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.rpf_off.as<int32_t>(),
         ps.rpf_j.as<int32_t>(), ps.radj.as<unsigned long long>(),
-        ps.rep.as<unsigned long long>(), eoff, c->eu_rec.as<uint4>(), c->eu_A.as<long long>(),
-        c->eu_L, ej, ek, ee, efm, keys, vals);
+        ps.rep.as<unsigned long long>(), eoff, c->eu_rec.as<uint4>(), c->eu_Lt.as<long long>(),
+        ej, ek, ee, efm, keys, vals);
     ++c->launches;
   }
   int64_t nu = 0;

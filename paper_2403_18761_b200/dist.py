@@ -163,16 +163,19 @@ class ShardedRPD:
         return self.glob, int(cnt[:, 0].sum())
 
 
-def allreduce_euler(local: dict, group=None) -> dict:
+def allreduce_euler(local: dict, ctx, group=None) -> dict:
     """Per-sphere fractional Euler sums of the whole job (SURVEY.md §8(e) "validation
-    aggregates"): every rank's rpc_sum [N] and rpf_sum [E] (int64 numerators over the common
-    denominator, identical on all ranks because the payloads are built from the whole mesh)
-    are summed by one all-reduce each.  Integer sums: exact and order-independent."""
+    aggregates"): every rank's exact accumulator rows rpc_acc [N, 1+P] and rpf_acc [E, 1+P]
+    (integer part + one residue per prime, identical layouts on all ranks because the payloads
+    are built from the whole mesh) are summed by one all-reduce each, then finalised by the
+    library (rpd_euler_finalize).  Integer sums: exact and order-independent."""
     out = dict(local)
-    for k in ("rpc_sum", "rpf_sum"):
-        t = local[k].to(torch.int64).clone()
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        out[k] = t
+    for k in ("rpc", "rpf"):
+        acc = local[k + "_acc"].to(torch.int64).clone()
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+        out[k + "_acc"] = acc
+        if ctx is not None:
+            out[k + "_sum"], out[k + "_exact"], out[k + "_value"] = ctx.euler_finalize(acc)
     return out
 
 

@@ -29,7 +29,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-            "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe"]
+            "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize"]
 
 
 class RPDError(RuntimeError):
@@ -46,11 +46,14 @@ class _Pieces(C.Structure):
                 ("piece_rows", C.c_void_p), ("n_slots", C.c_int64)]
 
 
+EULER_KEYS = ("piece_euler", "piece_denom", "rpf_off", "rpf_sphere", "rpf_euler", "rpc_sum",
+              "rpc_exact", "rpc_value", "rpf_sum", "rpf_exact", "rpf_value", "rpc_acc",
+              "rpf_acc")
+
+
 class _Euler(C.Structure):
-    _fields_ = [("denom", C.c_int64), ("piece_euler", C.c_void_p), ("rpf_off", C.c_void_p),
-                ("rpf_sphere", C.c_void_p), ("rpf_euler", C.c_void_p), ("rpc_sum", C.c_void_p),
-                ("rpf_sum", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64),
-                ("N", C.c_int64), ("E", C.c_int64)]
+    _fields_ = [("n_primes", C.c_int64)] + [(k, C.c_void_p) for k in EULER_KEYS] + \
+        [("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64), ("E", C.c_int64)]
 
 
 class _Topology(C.Structure):
@@ -138,7 +141,8 @@ def load_library(path: str = LIB_PATH):
     L.rpd_get_stats.argtypes = [vp, C.POINTER(_Stats)]
     L.rpd_set_euler.argtypes = [vp, vp, i64, i64, vp, i64, C.POINTER(i64)]
     L.rpd_get_euler.argtypes = [vp, C.POINTER(_Euler)]
-    L.rpd_download_euler.argtypes = [vp] * 7
+    L.rpd_download_euler.argtypes = [vp] * 14
+    L.rpd_euler_finalize.argtypes = [vp, vp, i64, vp, vp, vp]
     L.rpd_get_topology.argtypes = [vp, C.POINTER(_Topology)]
     L.rpd_download_topology.argtypes = [vp] * 8
     L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
@@ -159,7 +163,7 @@ def load_library(path: str = LIB_PATH):
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-              "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe"):
+              "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -344,8 +348,8 @@ class RPDContext:
     def set_euler(self, tets_all, V: int, local_ids=None) -> int:
         """Fractional Euler payloads of the ctx's tets from the whole mesh ``tets_all``
         (PAPER.md:491); ``local_ids``: global index of every ctx-local tet (None: the ctx holds
-        all tets in order).  Returns the common denominator L.  ``tets_all=None`` switches
-        Euler mode off."""
+        all tets in order).  Returns P, the number of prime residues of a sum's accumulator
+        row (R24).  ``tets_all=None`` switches Euler mode off."""
         L = C.c_int64()
         if tets_all is None:
             self._check(self.L.rpd_set_euler(self.h, None, 0, 0, None, 0, C.byref(L)))
@@ -362,18 +366,40 @@ class RPDContext:
         return L.value
 
     def download_euler(self, device=False) -> dict:
-        """Euler data of the current pieces (exact numerators over ``euler_denom``):
-        piece_euler, rpf_off / rpf_sphere / rpf_euler (radical facets of each piece),
-        rpc_sum [N] and rpf_sum [E] (per sphere / per CSR entry of the row-sorted CSR)."""
+        """Euler data of the current pieces (exact, R24): piece_euler numerators over
+        piece_denom (the tet's L_t), rpf_off / rpf_sphere / rpf_euler (radical facets of each
+        piece, over the piece's denominator), per sphere rpc_sum / rpc_exact / rpc_value and
+        per CSR entry of the row-sorted CSR rpf_sum / rpf_exact / rpf_value (the integer sum,
+        whether it is exact, the value as a double), and the raw accumulator rows rpc_acc
+        [N, 1+P] / rpf_acc [E, 1+P] (summed over the ranks of a sharded job, then
+        euler_finalize)."""
         e = _Euler()
         self._check(self.L.rpd_get_euler(self.h, C.byref(e)))
-        specs = [(e.n_pieces, np.int64), (e.n_pieces + 1, np.int32), (e.n_rpf, np.int32),
-                 (e.n_rpf, np.int64), (e.N, np.int64), (e.E, np.int64)]
+        W = 1 + e.n_primes
+        specs = [(e.n_pieces, np.int64), (e.n_pieces, np.int64), (e.n_pieces + 1, np.int32),
+                 (e.n_rpf, np.int32), (e.n_rpf, np.int64), (e.N, np.int64), (e.N, np.uint8),
+                 (e.N, np.float64), (e.E, np.int64), (e.E, np.uint8), (e.E, np.float64),
+                 (W * e.N, np.int64), (W * e.E, np.int64)]
         arrs = self._alloc(specs, device)
         self._check(self.L.rpd_download_euler(self.h, *[self._p(a) for a in arrs]))
-        out = dict(zip(["piece_euler", "rpf_off", "rpf_sphere", "rpf_euler", "rpc_sum",
-                        "rpf_sum"], arrs))
-        out["euler_denom"] = int(e.denom)
+        out = dict(zip(EULER_KEYS, arrs))
+        out["rpc_acc"] = out["rpc_acc"].reshape(-1, W)
+        out["rpf_acc"] = out["rpf_acc"].reshape(-1, W)
+        out["n_primes"] = int(e.n_primes)
+        return out
+
+    def euler_finalize(self, acc):
+        """Accumulator rows acc [n, 1+P] (torch CUDA int64, e.g. all-reduced over the ranks) ->
+        (sum int64 [n], exact uint8 [n], value float64 [n]) as CUDA tensors."""
+        import torch
+        acc = acc.to(torch.int64).contiguous()
+        n = int(acc.shape[0])
+        dev = acc.device
+        out = (torch.empty(n, dtype=torch.int64, device=dev),
+               torch.empty(n, dtype=torch.uint8, device=dev),
+               torch.empty(n, dtype=torch.float64, device=dev))
+        self._check(self.L.rpd_euler_finalize(self.h, self._p(acc), n, self._p(out[0]),
+                                              self._p(out[1]), self._p(out[2])))
         return out
 
     def topology(self):

@@ -413,6 +413,28 @@ def random_tiny(seed: int, n_spheres: int = 12, grid: int = 2, coarse: bool = Fa
     return Workload(f"tiny{seed}", verts, tets, sph, off, idx, meta={"seed": seed})
 
 
+def delaunay_workload(n_points: int, n_spheres: int, seed: int = 0, box: float = 16.0):
+    """An unstructured tet mesh (fTetWild-like vertex valences, unlike Kuhn grids):
+    the Delaunay tetrahedralisation (Qhull) of random lattice points in [1, 1 + box)^3 -- distinct
+    points on the 2^-6 grid, slivers of zero volume dropped, every tet positively oriented --
+    and random zero-or-small-radius spheres inside with their regular-triangulation lists."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    P = np.unique(rng.integers(0, int(box * 64), size=(n_points, 3)), axis=0) / 64.0 + 1.0
+    tets = Delaunay(P).simplices.astype(np.int64)
+    det = _orient_det(P[tets] * LATTICE)
+    tets = tets[det != 0]
+    det = det[det != 0]
+    neg = det < 0
+    tets[neg] = tets[neg][:, [0, 2, 1, 3]]
+    sph = np.c_[rng.integers(0, int(box * 64), size=(n_spheres, 3)) / 64.0 + 1.0,
+                rng.integers(0, 64, size=n_spheres) / 64.0]
+    sph = np.unique(sph, axis=0)
+    off, idx = power_neighbours(sph)
+    return Workload(f"delaunay{n_points}_{seed}", P, tets.astype(np.int32), sph, off, idx,
+                    meta={"seed": seed})
+
+
 def make_c1(seed: int = 0, degenerate: bool = False, big: bool = False):
     verts, tets = unit_cube_6tets()
     sph = c1_spheres(seed, degenerate, big=big)

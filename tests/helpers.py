@@ -78,29 +78,41 @@ def slice_tets(res, ids):
     return out
 
 
+def piece_dens(res):
+    """Per-piece Euler denominators (library: piece_denom; oracle: piece_euler_den)."""
+    return np.asarray(res["piece_denom"] if "piece_denom" in res else res["piece_euler_den"])
+
+
 def slice_euler(res, piece_ids):
     """Euler arrays of the pieces ``piece_ids`` (per-piece value and radical-facet CSR)."""
     ro = np.asarray(res["rpf_off"])
     rs = [np.arange(ro[p], ro[p + 1]) for p in piece_ids]
     ridx = np.concatenate(rs) if rs else np.zeros(0, int)
-    return {"piece_euler": np.asarray(res["piece_euler"])[np.asarray(piece_ids, int)],
+    pid = np.asarray(piece_ids, int)
+    return {"piece_euler": np.asarray(res["piece_euler"])[pid],
+            "piece_euler_den": piece_dens(res)[pid],
             "rpf_off": np.r_[0, np.cumsum([len(r) for r in rs])].astype(np.int32),
             "rpf_sphere": np.asarray(res["rpf_sphere"])[ridx],
-            "rpf_euler": np.asarray(res["rpf_euler"])[ridx], "euler_denom": res["euler_denom"]}
+            "rpf_euler": np.asarray(res["rpf_euler"])[ridx]}
 
 
 def compare_euler(a, b):
-    """Exact comparison of two Euler results (numerators over their own denominators):
-    a[x] / La == b[x] / Lb  <=>  a[x] * Lb == b[x] * La (Python integers)."""
+    """Exact comparison of two Euler results: every piece value and radical-facet value
+    num / den (each over its piece's denominator) compared as rationals, x_a / L_a == x_b / L_b
+    <=> x_a L_b == x_b L_a (Python integers)."""
     errs = []
-    La, Lb = int(a["euler_denom"]), int(b["euler_denom"])
     for k in ("rpf_off", "rpf_sphere"):
         if not np.array_equal(np.asarray(a[k]), np.asarray(b[k])):
             errs.append(f"{k} differs")
             return errs
-    for k in ("piece_euler", "rpf_euler"):
-        x = [int(v) * Lb for v in np.asarray(a[k]).tolist()]
-        y = [int(v) * La for v in np.asarray(b[k]).tolist()]
+    da, db = piece_dens(a).tolist(), piece_dens(b).tolist()
+    if len(da) != len(db):
+        return [f"piece counts {len(da)} vs {len(db)}"]
+    nr = np.diff(np.asarray(a["rpf_off"]))
+    ra, rb = np.repeat(da, nr).tolist(), np.repeat(db, nr).tolist()
+    for k, (La, Lb) in (("piece_euler", (da, db)), ("rpf_euler", (ra, rb))):
+        x = [int(v) * int(L) for v, L in zip(np.asarray(a[k]).tolist(), Lb)]
+        y = [int(v) * int(L) for v, L in zip(np.asarray(b[k]).tolist(), La)]
         bad = [i for i in range(len(x)) if x[i] != y[i]]
         if len(x) != len(y) or bad:
             errs.append(f"{k}: {len(bad)} of {len(x)} differ (first {bad[:3]})")

@@ -80,18 +80,45 @@ def test_shards_partition_the_tets():
         assert max(sizes) - min(sizes) <= 4096
 
 
+PRIMES = [p for p in range(2, 256) if all(p % d for d in range(2, int(p ** 0.5) + 1))]
+PPOW = [max(p ** e for e in range(1, 9) if p ** e <= 255) for p in PRIMES]
+
+
+def _acc_row(fr):
+    """A Fraction as the library's accumulator row [K, R_1 .. R_P] over PRIMES (test side:
+    partial fractions by Python integers; residues scaled to p^E)."""
+    from fractions import Fraction
+    num, L = fr.numerator, fr.denominator
+    row = [0] * (1 + len(PRIMES))
+    rest = Fraction(num, L)
+    for j, p in enumerate(PRIMES):
+        if L % p:
+            continue
+        q = p
+        while L % (q * p) == 0:
+            q *= p
+        a = num * pow(L // q, -1, q) % q
+        row[1 + j] = a * (PPOW[j] // q)
+        rest -= Fraction(a, q)
+    assert rest.denominator == 1
+    row[0] = int(rest)
+    return row
+
+
 def _euler_csr(r, w):
-    """Oracle per-piece Euler numerators summed per sphere (rpc [N]) and per CSR entry of its
-    neighbour row (rpf [E]) as int64 -- the layout of rpd_download_euler."""
-    rpc = np.zeros(w.N, np.int64)
-    rpf = np.zeros(len(w.nbr_idx), np.int64)
+    """Oracle per-piece Euler values summed per sphere (rpc [N, 1+P]) and per CSR entry of
+    its neighbour row (rpf [E, 1+P]) as accumulator rows -- the layout of rpd_download_euler."""
+    from fractions import Fraction
+    rpc = np.zeros((w.N, 1 + len(PRIMES)), np.int64)
+    rpf = np.zeros((len(w.nbr_idx), 1 + len(PRIMES)), np.int64)
     ro = r["rpf_off"]
     for p, i in enumerate(r["piece_sphere"].tolist()):
-        rpc[i] += r["piece_euler"][p]
+        L = int(r["piece_euler_den"][p])
+        rpc[i] += _acc_row(Fraction(int(r["piece_euler"][p]), L))
         row = w.nbr_idx[w.nbr_off[i]:w.nbr_off[i + 1]]
         for k in range(ro[p], ro[p + 1]):
             e = w.nbr_off[i] + int(np.nonzero(row == r["rpf_sphere"][k])[0][0])
-            rpf[e] += r["rpf_euler"][k]
+            rpf[e] += _acc_row(Fraction(int(r["rpf_euler"][k]), L))
     return rpc, rpf
 
 
@@ -105,16 +132,20 @@ def _euler_worker(rank, world, port, q):
         ids = shard_tets(w.T, world, rank, block=256)
         r = oracle.rpd_workload(w, tet_ids=ids, euler=True)
         rpc, rpf = _euler_csr(r, w)
-        out = allreduce_euler({"rpc_sum": torch.as_tensor(rpc), "rpf_sum": torch.as_tensor(rpf)})
+        out = allreduce_euler({"rpc_acc": torch.as_tensor(rpc), "rpf_acc": torch.as_tensor(rpf)},
+                              None)
         if rank == 0:
-            q.put({k: v.numpy() for k, v in out.items()} | {"L": r["euler_denom"]})
+            q.put({k: v.numpy() for k, v in out.items()})
     finally:
         dist.destroy_process_group()
 
 
 def test_euler_allreduce_equals_single_rank():
-    """NEXT-1 on the sharded path: the per-rank RPC / RPF sums of the tet shards, all-reduced,
-    equal the single-rank sums (payloads built from the whole mesh on every rank)."""
+    """NEXT-1 on the sharded path: the per-rank exact accumulator rows of the RPC / RPF sums
+    (integer part + one residue per prime, R24), all-reduced, equal the single-rank
+    rows, and decode to the oracle's exact sums (payloads built from the whole mesh on every
+    rank)."""
+    from fractions import Fraction
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -129,5 +160,7 @@ def test_euler_allreduce_equals_single_rank():
     w = W.make_shape_workload("G", 3000, 200, seed=12, cache=False)
     ref = oracle.rpd_workload(w, euler=True)
     rpc, rpf = _euler_csr(ref, w)
-    assert got["L"] == ref["euler_denom"]
-    assert np.array_equal(got["rpc_sum"], rpc) and np.array_equal(got["rpf_sum"], rpf)
+    assert np.array_equal(got["rpc_acc"], rpc) and np.array_equal(got["rpf_acc"], rpf)
+    want, _ = oracle.euler_sums(ref, w.N, w.nbr_off, w.nbr_idx)
+    dec = [int(row[0]) + sum(Fraction(int(x), q) for x, q in zip(row[1:], PPOW)) for row in rpc]
+    assert dec == want

@@ -451,6 +451,41 @@ def test_euler_sums_are_integers(make):
     assert sum(1 for x in rpc if x == 1) >= 0.5 * sum(1 for x in rpc if x != 0)
 
 
+def test_euler_unstructured_mesh():
+    """an unstructured (Delaunay) mesh whose sharing counts have a common multiple
+    far beyond 2^50 (valences up to ~60): the per-tet denominators keep every value exact --
+    one sphere gives the mesh's Euler characteristic V - E + F - T = 1 (a convex ball), and
+    with many spheres every RPC / RPF sum is an integer."""
+    import math
+    w = W.delaunay_workload(2000, 60, seed=1)
+    L = 1  # the common denominator a global-lcm scheme would need
+    r1 = oracle.rpd(w.verts, w.tets, np.array([[8.0, 8.0, 8.0, 0.5]]), np.zeros(2, np.int32),
+                    np.zeros(0, np.int32), euler=True)
+    rpc1, _ = oracle.euler_sums(r1, 1, np.zeros(2, np.int32), np.zeros(0, np.int32))
+    assert _mesh_euler(w.tets) == 1 and rpc1 == [1]
+    for d in set(r1["piece_euler_den"].tolist()):
+        L = L * d // math.gcd(L, d)
+    assert math.log2(L) > 60
+    r = oracle.rpd_workload(w, euler=True)
+    rpc, rpf = oracle.euler_sums(r, w.N, w.nbr_off, w.nbr_idx)
+    assert all(x.denominator == 1 for x in rpc) and all(x.denominator == 1 for x in rpf.values())
+    assert sum(1 for x in rpc if x == 1) >= 0.5 * sum(1 for x in rpc if x != 0)
+
+
+def test_euler_unstructured_explicit_extraction():
+    """The per-tet-denominator sums equal the explicit extraction on a small Delaunay mesh."""
+    w = W.delaunay_workload(40, 8, seed=3, box=4.0)
+    r = oracle.rpd_workload(w, euler=True)
+    rpc, rpf = oracle.euler_sums(r, w.N, w.nbr_off, w.nbr_idx)
+    for i in range(w.N):
+        e_rpc, e_rpf, generic = X.explicit_euler(w.verts, w.tets, w.spheres, w.nbr_off,
+                                                 w.nbr_idx, i)
+        if not generic:
+            continue
+        assert rpc[i] == e_rpc, i
+        assert {j: v for (a, j), v in rpf.items() if a == i} == e_rpf, i
+
+
 @pytest.mark.parametrize("make", [lambda: W.make_c1(0), lambda: W.make_c1(1), lambda: W.make_c1(3),
                                   lambda: W.random_tiny(0, n_spheres=14, grid=2),
                                   lambda: W.random_tiny(2, n_spheres=14, grid=2)])
