@@ -305,21 +305,51 @@ __device__ __forceinline__ long long inv_mod(long long a, long long m) {  // a, 
   return x < 0 ? x + m : x;
 }
 
-__device__ void frac_add(unsigned long long* acc, long long num, long long L, const EuTable& tb) {
-  __int128 rest = num;
-  for (int j = 0; j < tb.P; ++j) {
+// the partial-fraction factors of a tet's denominator L_t (computed once per tet): for every
+// prime p_j | L_t, q = p_j^e exactly dividing L_t, m = L_t / q, inv = m^{-1} mod q, and the
+// scale p^E / q of the residue; at most 15 distinct primes (14 counts <= 255)
+struct FracFactors {
+  int n;
+  int slot[16];
+  long long q[16], m[16], inv[16], sc[16];
+};
+
+__device__ void frac_factors(long long L, const EuTable& tb, FracFactors& f) {
+  f.n = 0;
+  long long r = L;
+  for (int j = 0; j < tb.P && r > 1 && f.n < 16; ++j) {
     const long long p = tb.p[j];
-    if (L % p) continue;
-    long long q = p;
-    while (L % (q * p) == 0) q *= p;
-    const long long m = L / q;
-    long long nm = num % q;
-    if (nm < 0) nm += q;
-    const long long a = nm * inv_mod(m % q, q) % q;
-    rest -= (__int128)a * m;
-    if (a) atomicAdd(acc + 1 + j, (unsigned long long)(a * (tb.pe[j] / q)));
+    if (r % p) continue;
+    long long q = 1;
+    while (r % p == 0) {
+      r /= p;
+      q *= p;
+    }
+    const int k = f.n++;
+    f.slot[k] = j;
+    f.q[k] = q;
+    f.m[k] = L / q;
+    f.inv[k] = inv_mod(f.m[k] % q, q);
+    f.sc[k] = tb.pe[j] / q;
   }
-  const long long K = (long long)(rest / L);  // exact: rest = K L
+}
+
+// acc[0..P] += num / L as integer part + residues (num / L = K + sum_k a_k / q_k)
+__device__ void frac_add(unsigned long long* acc, long long num, long long L,
+                         const FracFactors& f) {
+  long long s = 0;      // sum_k a_k m_k (each term < L)
+  __int128 s128 = 0;    // (when L is large)
+  const bool big = L > (1ll << 58);
+  for (int k = 0; k < f.n; ++k) {
+    long long nm = num % f.q[k];
+    if (nm < 0) nm += f.q[k];
+    const long long a = nm * f.inv[k] % f.q[k];
+    if (big) s128 += (__int128)a * f.m[k];
+    else s += a * f.m[k];
+    if (a) atomicAdd(acc + 1 + f.slot[k], (unsigned long long)(a * f.sc[k]));
+  }
+  // K = (num - s) / L exactly (partial fractions); floor division of exact multiples
+  const long long K = big ? (long long)(((__int128)num - s128) / L) : (num - s) / L;
   if (K) atomicAdd(acc, (unsigned long long)K);
 }
 
@@ -334,11 +364,15 @@ __global__ void k_eu_sums(int64_t T, const int32_t* __restrict__ poff,
                           unsigned long long* __restrict__ miss) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= T) return;
+  const int q0 = poff[t], q1 = poff[t + 1];
+  if (q0 == q1) return;
   const long long L = Lt[t];
+  FracFactors f;
+  frac_factors(L, tb, f);
   const int W = 1 + tb.P;
-  for (int q = poff[t]; q < poff[t + 1]; ++q) {
+  for (int q = q0; q < q1; ++q) {
     const int i = sphere[q];
-    frac_add(acc + (int64_t)W * i, peu[q], L, tb);
+    frac_add(acc + (int64_t)W * i, peu[q], L, f);
     const int e0 = nbr_off[i], e1 = nbr_off[i + 1];
     for (int r = roff[q]; r < roff[q + 1]; ++r) {
       const int j = rj[r];
@@ -348,7 +382,7 @@ __global__ void k_eu_sums(int64_t T, const int32_t* __restrict__ poff,
         if (nbr_idx[mid] < j) lo = mid + 1;
         else hi = mid;
       }
-      if (lo < e1 && nbr_idx[lo] == j) frac_add(acc + (int64_t)W * (N + lo), re[r], L, tb);
+      if (lo < e1 && nbr_idx[lo] == j) frac_add(acc + (int64_t)W * (N + lo), re[r], L, f);
       else atomicAdd(miss, 1ull);  // a kept facet whose neighbour left the row (R12 degenerate)
     }
   }
