@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--no-euler", action="store_true",
                     help="skip the fractional-Euler (NEXT-1) side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the sharded path (exchanges over a process group) even with one "
+                         "rank, e.g. under torch.distributed.run --nproc-per-node 1 (testing)")
     return ap.parse_args()
 
 
@@ -469,20 +472,22 @@ def main():
     from paper_2403_18761_b200.dist import ShardedRPD
 
     world, rank, local = dist_env()
-    if world > 1:
+    # the sharded path (process group, exchanges) whenever several ranks run, or on request
+    sharded = world > 1 or (args.force_shard and "WORLD_SIZE" in os.environ)
+    if sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if rank == 0:
         P.build()
-    if world > 1:
+    if sharded:
         dist.barrier()
 
     w = W.make_config(args.config)
     batches = w.batches if args.partial_iters < 0 else w.batches[:args.partial_iters]
     ctx = P.RPDContext(local, filter_mode=args.filter)
     ctx.set_profile(True)
-    S = ShardedRPD(ctx, w.T) if world > 1 else None
+    S = ShardedRPD(ctx, w.T) if sharded else None
     ids = S.ids if S else np.arange(w.T, dtype=np.int32)
     tets_local = w.tets[ids]
     to_dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(dev)
@@ -542,7 +547,7 @@ def main():
     recs, times = [], []
     for s in range(args.steps):
         flush.zero_()
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
@@ -564,7 +569,7 @@ def main():
                       for r in recs)
     t = torch.tensor([float(np.sum(times)), float(pairs_local)], dtype=torch.float64,
                      device=dev)
-    if world > 1:
+    if sharded:
         tm = t[:1].clone()
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -617,7 +622,7 @@ def main():
     h_out = None
     for s in range(max(2, min(args.steps, 5)) + 1):
         flush.zero_()
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -654,14 +659,15 @@ def main():
                   np.asarray(v).nbytes for v in out.values())
     et = torch.tensor([float(np.sum(e2e_times)), float(np.sum(e2e_pairs))],
                       dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         etm = et[:1].clone()
         dist.all_reduce(etm, op=dist.ReduceOp.MAX)
         dist.all_reduce(et, op=dist.ReduceOp.SUM)
         et[0] = etm[0]
     e2e_value = float(et[1]) / float(et[0])
 
-    euler = side_euler(args, ctx, w, ids, world, recs, flush, d_verts, d_tets, d_base, to_dev) \
+    euler = side_euler(args, ctx, w, ids, world if not sharded else max(world, 2), recs, flush,
+                       d_verts, d_tets, d_base, to_dev) \
         if not args.no_euler else None
     nbr = side_neighbors(args, ctx, w, flush, d_verts, d_tets, d_base) \
         if not args.no_nbr else None
@@ -741,7 +747,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
