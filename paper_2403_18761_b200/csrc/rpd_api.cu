@@ -1315,7 +1315,7 @@ static rpd_status seg_run(rpd_ctx* c, int kind, int64_t n_out, const int32_t* li
                        c->stream), "copy offsets");
   D.i_tet = it;
   CK(launch_seg_copy(c, n_out, S, D), "segment copy");
-  CK(cudaStreamSynchronize(c->stream), "segment copy");
+  // (no sync: device destinations are stream-ordered; host ones are synced by the caller)
   return RPD_OK;
 }
 

@@ -8,9 +8,8 @@
 // One segment-gather engine serves every case: a row map sends each output row (a tet) to
 // (source, row) -- source 0 the previous global CSR or the ctx's own state, sources 1.. the
 // ranks' gathered shards -- then per output row its candidate / piece / incidence counts are
-// read (k_seg_count), scanned into the output offsets, and its segments copied (k_seg_copy;
-// one thread per row: a tet's few candidates, pieces and incidences are contiguous in source
-// and destination).  Integer work and copies only: results are byte-identical to a
+// read (k_seg_count), scanned into the output offsets, and its segments copied
+// (k_seg_copy_tiled: coalesced element loops per tile of output rows).  Integer work and copies only: results are byte-identical to a
 // single-GPU run (per-tet outputs do not depend on the shard).
 #include "rpd_ctx.h"
 
@@ -78,37 +77,6 @@ __global__ void k_seg_count(int64_t n, const int2* __restrict__ map, SegSources 
   if (cc) cc[o] = nc;
   if (pc) pc[o] = np;
   if (ic) ic[o] = ni;
-}
-
-__global__ void k_seg_copy(int64_t n, const int2* __restrict__ map, SegSources S, SegDst D) {
-  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (o == 0 && D.piece_off) D.inc_off[D.piece_off[n]] = D.i_tet[n];  // terminal entry
-  if (o >= n) return;
-  const int2 m = map[o];
-  if (m.x < 0) return;
-  const SegSrc& s = S.s[m.x];
-  const int64_t r = (int64_t)m.y * s.rs;
-  if (D.cand_idx && s.c_beg) {
-    const int c0 = s.c_beg[r], c1 = s.c_end[r], q0 = D.cand_off[o];
-    for (int k = c0; k < c1; ++k) D.cand_idx[q0 + (k - c0)] = s.c_idx[k];
-  }
-  if (D.piece_off && s.p_beg) {
-    const int p0 = s.p_beg[r], p1 = s.p_end[r];
-    if (p1 <= p0) return;
-    const int q0 = D.piece_off[o], i0 = s.i_off[p0], gi0 = D.i_tet[o];
-    for (int p = p0; p < p1; ++p) {
-      const int q = q0 + (p - p0);
-      D.piece_sphere[q] = s.p_sphere[p];
-      D.piece_vol[q] = s.p_vol[p];
-      D.piece_m1[3 * (int64_t)q] = s.p_m1[3 * (int64_t)p];
-      D.piece_m1[3 * (int64_t)q + 1] = s.p_m1[3 * (int64_t)p + 1];
-      D.piece_m1[3 * (int64_t)q + 2] = s.p_m1[3 * (int64_t)p + 2];
-      D.piece_fm[q] = s.p_fm[p];
-      D.inc_off[q] = gi0 + (s.i_off[p] - i0);
-    }
-    const int i1 = s.i_off[p1];
-    for (int k = i0; k < i1; ++k) D.inc_sphere[gi0 + (k - i0)] = s.i_sph[k];
-  }
 }
 
 // ids_out[k] = id_map[list[k]] (or list[k]): the global ids of downloaded local tets
@@ -234,8 +202,81 @@ cudaError_t launch_seg_counts(rpd_ctx* c, int64_t n_out, const SegSources& S, in
   return K ? launch_scan_i32_multi(c, in, out, K, n_out) : cudaSuccess;
 }
 
+// Tiled copy (one block per SEG_TILE output rows): the rows' source bases and destination
+// offsets staged in shared memory, then coalesced loops over the tile's destination ranges of
+// candidates, pieces and incidences (an element's row by binary search over the staged
+// offsets).  Rows taken in order from one source (a gather's shard, the clean rows of a merge)
+// read contiguous source memory.
+constexpr int SEG_TILE = 256;
+
+__device__ __forceinline__ int seg_of(const int* off, int n, int q) {
+  int lo = 0, hi = n;  // off[lo] <= q < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= q) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(SEG_TILE) k_seg_copy_tiled(int64_t n, const int2* __restrict__ map,
+                                                              SegSources S, SegDst D) {
+  __shared__ int s_dc[SEG_TILE + 1], s_dp[SEG_TILE + 1], s_di[SEG_TILE + 1];
+  __shared__ int s_src[SEG_TILE], s_sc[SEG_TILE], s_sp[SEG_TILE], s_si[SEG_TILE];
+  const int64_t o0 = (int64_t)blockIdx.x * SEG_TILE;
+  const int nt = (int)min((int64_t)SEG_TILE, n - o0);
+  const bool cands = D.cand_idx != nullptr, pieces = D.piece_off != nullptr;
+  for (int l = threadIdx.x; l <= nt; l += blockDim.x) {
+    const int64_t o = o0 + l;
+    s_dc[l] = cands ? D.cand_off[o] : 0;
+    s_dp[l] = pieces ? D.piece_off[o] : 0;
+    s_di[l] = pieces ? D.i_tet[o] : 0;
+    if (l < nt) {
+      const int2 m = map[o];
+      s_src[l] = m.x;
+      if (m.x >= 0) {
+        const SegSrc& s = S.s[m.x];
+        const int64_t r = (int64_t)m.y * s.rs;
+        s_sc[l] = s.c_beg ? s.c_beg[r] : 0;
+        const int p0 = s.p_beg ? s.p_beg[r] : 0;
+        s_sp[l] = p0;
+        s_si[l] = s.p_beg && s.p_end[r] > p0 ? s.i_off[p0] : 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (cands)
+    for (int q = s_dc[0] + threadIdx.x; q < s_dc[nt]; q += blockDim.x) {
+      const int l = seg_of(s_dc, nt, q);
+      D.cand_idx[q] = S.s[s_src[l]].c_idx[s_sc[l] + (q - s_dc[l])];
+    }
+  if (pieces) {
+    for (int q = s_dp[0] + threadIdx.x; q < s_dp[nt]; q += blockDim.x) {
+      const int l = seg_of(s_dp, nt, q);
+      const SegSrc& s = S.s[s_src[l]];
+      const int p = s_sp[l] + (q - s_dp[l]);
+      D.piece_sphere[q] = s.p_sphere[p];
+      D.piece_vol[q] = s.p_vol[p];
+      D.piece_m1[3 * (int64_t)q] = s.p_m1[3 * (int64_t)p];
+      D.piece_m1[3 * (int64_t)q + 1] = s.p_m1[3 * (int64_t)p + 1];
+      D.piece_m1[3 * (int64_t)q + 2] = s.p_m1[3 * (int64_t)p + 2];
+      D.piece_fm[q] = s.p_fm[p];
+      D.inc_off[q] = s_di[l] + (s.i_off[p] - s_si[l]);
+    }
+    for (int q = s_di[0] + threadIdx.x; q < s_di[nt]; q += blockDim.x) {
+      const int l = seg_of(s_di, nt, q);
+      D.inc_sphere[q] = S.s[s_src[l]].i_sph[s_si[l] + (q - s_di[l])];
+    }
+    if (o0 + nt == n && threadIdx.x == 0) D.inc_off[s_dp[nt]] = s_di[nt];  // terminal entry
+  }
+}
+
 cudaError_t launch_seg_copy(rpd_ctx* c, int64_t n_out, const SegSources& S, const SegDst& D) {
-  k_seg_copy<<<nblk(n_out > 0 ? n_out : 1, 256), 256, 0, c->stream>>>(n_out, c->g_map.as<int2>(),
+  if (n_out == 0) {
+    if (D.piece_off) return cudaMemsetAsync(D.inc_off, 0, sizeof(int32_t), c->stream);
+    return cudaSuccess;
+  }
+  k_seg_copy_tiled<<<nblk(n_out, SEG_TILE), SEG_TILE, 0, c->stream>>>(n_out, c->g_map.as<int2>(),
                                                                       S, D);
   ++c->launches;
   return cudaGetLastError();
