@@ -991,7 +991,9 @@ rpd_status rpd_download_pieces(rpd_ctx* c, int32_t* piece_off, int32_t* piece_sp
   CK(cp(piece_facemask, ps.fm.p, np), "download");
   CK(cp(inc_off, ps.inc_off.p, sizeof(int32_t) * (np + 1)), "download");
   CK(cp(inc_sphere, ps.inc.p, sizeof(int32_t) * ni), "download");
-  CK(cudaStreamSynchronize(c->stream), "download");
+  // host destinations are complete on return; device ones are stream-ordered
+  if (is_host_ptr(piece_off) || is_host_ptr(piece_vol) || is_host_ptr(inc_sphere))
+    CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }
 
@@ -1642,7 +1644,8 @@ rpd_status rpd_download_cands(rpd_ctx* c, int32_t* cand_off, int32_t* cand_idx) 
   if (cand_idx && cs.n > 0)
     CK(cudaMemcpyAsync(cand_idx, cs.idx.p, sizeof(int32_t) * cs.n, cudaMemcpyDefault,
                        c->stream), "download");
-  CK(cudaStreamSynchronize(c->stream), "download");
+  if (is_host_ptr(cand_off) || is_host_ptr(cand_idx))
+    CK(cudaStreamSynchronize(c->stream), "download");
   return RPD_OK;
 }
 
