@@ -535,26 +535,23 @@ class RPDContext:
                                       "piece_facemask", "inc_off", "inc_sphere")]))
         return out
 
-    def merge_shards(self, shards, glob: dict, T: int) -> dict:
-        """Partial-mode merge (rpd_merge_shards): the global CSR ``glob`` with the dirty rows
-        replaced by the shards' segments (each shard dict holds ``tet_ids``, the global ids
-        of its dirty tets, and their candidate + piece CSRs).  Returns torch tensors viewing
-        the ctx-owned result (valid until the next-but-one merge)."""
+    def merge_shards(self, shards, glob, T: int) -> "GlobalCSR":
+        """Partial-mode merge (rpd_merge_shards): the global CSR ``glob`` (a dict of tensors or
+        the GlobalCSR of the previous merge) with the dirty rows replaced by the shards'
+        segments (each shard dict holds ``tet_ids``, the global ids of its dirty tets, and
+        their candidate + piece CSRs).  Returns a GlobalCSR over the ctx-owned result (valid
+        until the next-but-one merge); it behaves as a dict of torch tensors, made on demand."""
         sh, keep = self._shards(shards, T)
-        old = _Csr()
-        for k in CSR_KEYS:
-            setattr(old, k, self._p(glob[k]))
-        old.T = int(T)
+        if isinstance(glob, GlobalCSR):
+            old = glob.raw
+        else:
+            old = _Csr()
+            for k in CSR_KEYS:
+                setattr(old, k, self._p(glob[k]))
+            old.T = int(T)
         res = _Csr()
         self._check(self.L.rpd_merge_shards(self.h, C.byref(sh), C.byref(old), C.byref(res)))
-        spec = {"cand_off": (T + 1, "<i4"), "cand_idx": (res.n_cand, "<i4"),
-                "piece_off": (T + 1, "<i4"), "piece_sphere": (res.n_pieces, "<i4"),
-                "piece_vol": (res.n_pieces, "<f8"), "piece_m1": (3 * res.n_pieces, "<f8"),
-                "piece_facemask": (res.n_pieces, "|u1"), "inc_off": (res.n_pieces + 1, "<i4"),
-                "inc_sphere": (res.n_inc, "<i4")}
-        out = {k: _device_view(getattr(res, k), n, ts) for k, (n, ts) in spec.items()}
-        out["piece_m1"] = out["piece_m1"].reshape(-1, 3)
-        return out
+        return GlobalCSR(res, T)
 
     def gather_pieces(self, shards, tet_ids, T: int) -> dict:
         """Global piece CSR (torch CUDA tensors) from per-rank piece CSRs (``shards``: one dict
@@ -625,6 +622,44 @@ class RPDContext:
         except ImportError:
             pass
         return a.ctypes.data if a.size else None
+
+
+class GlobalCSR:
+    """A whole candidate + piece CSR in ctx-owned device arrays (rpd_merge_shards output): the
+    raw pointers are kept (the next merge reads them directly); the torch views of the arrays
+    are made on first access, dict-style (keys as rpd_csr)."""
+
+    SPEC = {"cand_off": "<i4", "cand_idx": "<i4", "piece_off": "<i4", "piece_sphere": "<i4",
+            "piece_vol": "<f8", "piece_m1": "<f8", "piece_facemask": "|u1", "inc_off": "<i4",
+            "inc_sphere": "<i4"}
+
+    def __init__(self, raw, T):
+        self.raw, self.T, self._v = raw, int(T), {}
+
+    def _len(self, k):
+        r, T = self.raw, self.T
+        return {"cand_off": T + 1, "cand_idx": r.n_cand, "piece_off": T + 1,
+                "piece_sphere": r.n_pieces, "piece_vol": r.n_pieces, "piece_m1": 3 * r.n_pieces,
+                "piece_facemask": r.n_pieces, "inc_off": r.n_pieces + 1,
+                "inc_sphere": r.n_inc}[k]
+
+    def __getitem__(self, k):
+        if k not in self._v:
+            v = _device_view(getattr(self.raw, k), self._len(k), self.SPEC[k])
+            self._v[k] = v.reshape(-1, 3) if k == "piece_m1" else v
+        return self._v[k]
+
+    def keys(self):
+        return list(self.SPEC)
+
+    def items(self):
+        return [(k, self[k]) for k in self.SPEC]
+
+    def values(self):
+        return [self[k] for k in self.SPEC]
+
+    def __iter__(self):
+        return iter(self.SPEC)
 
 
 class _View:
