@@ -1,6 +1,7 @@
 """A/B of a clip environment switch (development aid): C3 full RPD + the C4 partial updates,
-median clip / filter / step times and a hash of the pieces.  Run once per setting (the switch is
-read once per process), e.g.  RPD_CLIP_SORT=1 python tools/clip_ab.py"""
+median clip / step times and a hash of the pieces.  Run once per setting (switches are read
+once per process).  Round 2 used it for RPD_CLIP_SORT (pairs in cut-plane-count order; slower,
+removed: see DESIGN.md §Clip)."""
 import hashlib
 import os
 import sys
