@@ -173,7 +173,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.twin, &c->st.hkey, &c->st.old_off, &c->st.old_idx, &c->st.old_planes,
                     &c->st.old_twin, &c->st.old_hkey, &c->st.old_sw, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->slab_m, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
-                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_sort, &c->p_scan, &c->i_scan, &c->d_count,
+                    &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
                     &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->eu_Lt, &c->eu_acc, &c->eu_fin, &c->eu_den, &c->p_eu,

@@ -25,8 +25,6 @@
 // Outputs per pair: non-empty flag, volume, first moment (facet fans, deterministic warp
 // reduction), tet-face mask and incidences as a bitmask over the positions of N(i)
 // (positive-area SoS facets expanded by exactly coincident sources, R7).
-#include <stdlib.h>
-
 #include <mutex>
 
 #include "rpd_ctx.h"
@@ -1359,62 +1357,6 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   return cudaGetLastError();
 }
 
-// Experiment (RPD_CLIP_SORT=1): the fast tier takes its pairs ordered by their number of
-// cut-mask planes (counting sort into 65 bins), so that the two 16-lane groups of a warp clip
-// pairs of similar work (less divergence between them); results are per pair, so only the
-// scheduling changes.
-__global__ void k_pair_hist(int64_t n, const int32_t* __restrict__ moff,
-                            const unsigned* __restrict__ cut, uint8_t* __restrict__ key,
-                            int* __restrict__ hist) {
-  __shared__ int h[65];
-  for (int b = threadIdx.x; b < 65; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < n) {
-    int k = 0;
-    for (int w = moff[p]; w < moff[p + 1] && k < 64; ++w) k += __popc(cut[w]);
-    k = min(k, 64);
-    key[p] = (uint8_t)k;
-    atomicAdd(&h[k], 1);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < 65; b += blockDim.x)
-    if (h[b]) atomicAdd(hist + b, h[b]);
-}
-
-__global__ void k_pair_bins(int* __restrict__ hist) {  // exclusive scan of 65 bins in place
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int b = 0; b < 65; ++b) {
-      const int v = hist[b];
-      hist[b] = run;
-      run += v;
-    }
-  }
-}
-
-__global__ void k_pair_scatter(int64_t n, const uint8_t* __restrict__ key, int* __restrict__ cur,
-                               int32_t* __restrict__ list) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < n) list[atomicAdd(cur + key[p], 1)] = (int32_t)p;
-}
-
-static cudaError_t sorted_pairs(rpd_ctx* c, int64_t n, const int32_t* moff, const unsigned* cut,
-                                const int32_t** list) {
-  cudaError_t e = c->p_sort.ensure(sizeof(int32_t) * (n + 1) + n + 65 * sizeof(int) + 64);
-  if (e) return e;
-  int32_t* lst = c->p_sort.as<int32_t>();
-  int* hist = reinterpret_cast<int*>(lst + n + 1);
-  uint8_t* key = reinterpret_cast<uint8_t*>(hist + 65);
-  if ((e = cudaMemsetAsync(hist, 0, 65 * sizeof(int), c->stream))) return e;
-  k_pair_hist<<<nblk(n, 256), 256, 0, c->stream>>>(n, moff, cut, key, hist);
-  k_pair_bins<<<1, 32, 0, c->stream>>>(hist);
-  k_pair_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, key, hist, lst);
-  c->launches += 3;
-  *list = lst;
-  return cudaGetLastError();
-}
-
 // fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
 // or the widest kernel over all pairs when `wide`
 template <bool EU>
@@ -1427,10 +1369,7 @@ static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pa
   cudaError_t e = c->p_dyn.ensure(sizeof(int));
   if (e) return e;
   if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
-  const int32_t* list = nullptr;
-  static const bool sort = getenv("RPD_CLIP_SORT") && atoi(getenv("RPD_CLIP_SORT")) != 0;
-  if (sort && (e = sorted_pairs(c, n_pairs, moff, cut, &list))) return e;
-  return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, EU>(c, n_pairs, list, pair_tet, tet_ids,
+  return launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, EU>(c, n_pairs, nullptr, pair_tet, tet_ids,
                                                       cand_idx, moff, cut, c->p_over.as<int32_t>(),
                                                       nullptr, c->p_dyn.as<int>());
 }

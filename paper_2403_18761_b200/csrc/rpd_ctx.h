@@ -183,7 +183,6 @@ struct rpd_ctx {
   // clip per-pair scratch
   rpd::DevBuf p_flag, p_f01, p_vol, p_m1, p_fm, p_ninc, p_mask, p_over, p_over2, p_over3, p_scan, i_scan;
   rpd::DevBuf p_dyn;  // dynamic pair counter of the fast clip kernel
-  rpd::DevBuf p_sort; // (experiment RPD_CLIP_SORT) pair order of the fast tier
 
   // partial update scratch
   rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off;
