@@ -66,10 +66,19 @@ def test_neighbors_superset_and_pieces(ctx, k):
     assert compare_results(a, b, w.verts, w.tets, rel=1e-9, check_cands=False) == []
 
 
-@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4-final", "C5"])
 def test_neighbors_full_size_same_pieces(ctx, name):
+    """Certifies the generator's Qhull neighbour lists at full size: the
+    GPU lists are a certified superset of the box neighbours (R30), and every piece computed
+    with them equals the piece computed with the Qhull lists -- so no missing Qhull neighbour
+    changes any piece.  C4-final: the sphere set after the 10 partial-update batches."""
+    import copy
     import paper_2403_18761_b200 as P
-    w = W.make_config(name)
+    if name == "C4-final":
+        w = copy.copy(W.make_config("C4"))
+        w.spheres, w.nbr_off, w.nbr_idx = w.batches[-1]
+    else:
+        w = W.make_config(name)
     got = ctx.neighbors(w.spheres, W.mesh_box(w.verts))
     off, idx = np.asarray(got["nbr_off"]), np.asarray(got["nbr_idx"])
     assert off[-1] == len(idx) and np.all(np.diff(off) >= 0)
