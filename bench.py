@@ -696,6 +696,8 @@ def main():
     traffic, ncu = None, None
     try:
         ncu = json.load(open(NCU_TRAFFIC)).get("clip")
+        if isinstance(ncu, dict) and ncu.get("config", args.config) != args.config:
+            ncu = None  # (the committed capture is of another workload)
         traffic = ncu.get("traffic") if isinstance(ncu, dict) else None
     except Exception:
         pass
