@@ -79,9 +79,14 @@ enum {
                                 only the pairs that overflow the fast (32-vertex) one; for tests */
   RPD_OPT_PROFILE = 5,       /* 1: time the filter and clip kernels with CUDA events on the ctx
                                 stream (rpd_stats.filter_ms / clip_ms) */
-  RPD_OPT_CLIP_TIERS = 6     /* 1: always the fast (16-vertex) tier and its overflow cascade, also
+  RPD_OPT_CLIP_TIERS = 6,    /* 1: always the fast (16-vertex) tier and its overflow cascade, also
                                 for fewer than 2048 pairs (which otherwise go straight to the
                                 64-slot tier); for tests */
+  RPD_OPT_GRAPH = 7          /* 1 (default; env RPD_GRAPH=0 sets 0 at rpd_create): a partial
+                                update of 1..64 new spheres (pruned filter, no Euler payloads,
+                                no profiling) runs as ONE device-driven CUDA graph with one host
+                                round trip (DESIGN.md §8 "latency path"); 0: eager launches with
+                                three round trips.  Same results either way. */
 };
 enum { RPD_FILTER_ALL_PAIRS = 0, RPD_FILTER_PRUNED = 1 };
 rpd_status rpd_set_option(rpd_ctx* ctx, int option, int64_t value);
@@ -470,6 +475,10 @@ typedef struct {
   double filter_ms, clip_ms;     /* kernel times of the last call (RPD_OPT_PROFILE only) */
   /* rpd_update_partial: sizes of the dirty tets' new segments (what a sharded job exchanges) */
   int64_t n_cand_dirty, n_pieces_dirty, n_inc_dirty;
+  /* CUDA-graph partial updates since rpd_create (RPD_OPT_GRAPH): replays, captures (one per
+   * buffer layout), and replays whose batch was redone eagerly (a device-side capacity check
+   * failed: work queue, slab, pool room or the graph's batch bound) */
+  int64_t graph_updates, graph_captures, graph_fallbacks;
 } rpd_stats;
 rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
 

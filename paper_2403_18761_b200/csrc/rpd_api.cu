@@ -160,9 +160,15 @@ rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream) {
     rpd_destroy(c);
     return RPD_ENOMEM;
   }
+  {
+    const char* g = getenv("RPD_GRAPH");
+    if (g && *g == '0') c->graph = 0;
+  }
   *out = c;
   return RPD_OK;
 }
+
+static void graph_clear(rpd_ctx* c);
 
 void rpd_destroy(rpd_ctx* c) {
   if (!c) return;
@@ -208,6 +214,12 @@ void rpd_destroy(rpd_ctx* c) {
     x->rep.release();
     x->rows.release();
   }
+  graph_clear(c);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->pd_host) cudaFreeHost(c->pd_host);
+  for (DevBuf* b : {&c->pd_buf, &c->g_scan, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
+                    &c->st.twin, &c->st.hkey, &c->st.old_repoch, &c->st.repoch})
+    b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
     if (c->ev[k]) cudaEventDestroy(c->ev[k]);
@@ -241,6 +253,9 @@ rpd_status rpd_set_option(rpd_ctx* c, int option, int64_t value) {
       return RPD_OK;
     case RPD_OPT_CLIP_TIERS:
       c->clip_tiers = value ? 1 : 0;
+      return RPD_OK;
+    case RPD_OPT_GRAPH:
+      c->graph = value ? 1 : 0;
       return RPD_OK;
     case RPD_OPT_STREAM:
       if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -289,7 +304,10 @@ static rpd_status stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
 
 // development trace (env RPD_TRACE_HOST=1): marks on the host clock and on the ctx stream
 static void tmark(rpd_ctx* c, const char* name) {
-  if (c->tr_on < 0) c->tr_on = getenv("RPD_TRACE_HOST") ? 1 : 0;
+  if (c->tr_on < 0) {
+    const char* v = getenv("RPD_TRACE_HOST");
+    c->tr_on = v && *v ? 1 : 0;
+  }
   if (!c->tr_on || c->tr_n >= 16) return;
   if (!c->tr_ev[c->tr_n]) cudaEventCreate(&c->tr_ev[c->tr_n]);
   cudaEventRecord(c->tr_ev[c->tr_n], c->stream);
@@ -777,6 +795,13 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
                                       const int32_t* new_ids, int64_t M, rpd_pieces* out,
                                       const int32_t** dirty_tets, int64_t* n_dirty,
                                       bool* mutated);
+static rpd_status partial_batch(rpd_ctx* c, int64_t nd, int64_t N_new, int64_t M,
+                                rpd_pieces* out, const int32_t** dirty_tets, int64_t* n_dirty);
+static bool graph_eligible(const rpd_ctx* c, int64_t M);
+static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new,
+                                const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                const int32_t* new_ids, int64_t M, rpd_pieces* out,
+                                const int32_t** dirty_tets, int64_t* n_dirty);
 
 rpd_status rpd_update_partial(rpd_ctx* c, const double* spheres, int64_t N_new,
                               const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
@@ -821,6 +846,11 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
     c->last.n_pieces = c->pcs[c->cur].n_pieces;
     c->last.n_inc = c->pcs[c->cur].n_inc;
     return fill_pieces(c, out);
+  }
+  if (graph_eligible(c, M)) {
+    *mutated = true;
+    return partial_graph(c, spheres, N_new, nbr_off, nbr_idx, E, new_ids, M, out, dirty_tets,
+                         n_dirty);
   }
   const int32_t* d_new = nullptr;
   tmark(c, "start");
@@ -885,6 +915,15 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     c->last.filter_ms += ms;
   }
+  return partial_batch(c, nd, N_new, M, out, dirty_tets, n_dirty);
+}
+
+// steps (2)-(4) of a partial update for the nd dirty tets listed in d_list (eager launches)
+static rpd_status partial_batch(rpd_ctx* c, int64_t nd, int64_t N_new, int64_t M,
+                                rpd_pieces* out, const int32_t** dirty_tets, int64_t* n_dirty) {
+  const int64_t T = c->st.T;
+  Readback* rb = (Readback*)c->pinned;
+  rpd_status s;
   const int32_t* dl = c->d_list.as<int32_t>();
 
   // (2) re-candidate the dirty tets against all spheres -- their new candidate lists go to the
@@ -963,6 +1002,310 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
   c->last.pairs_filtered = T * M + nd * N_new;
   *dirty_tets = dl;
   *n_dirty = nd;
+  return fill_pieces(c, out);
+}
+
+// ------------------------------------------------------------------ device-driven updates
+//
+// The latency path for few insertions ("launch latency matters, use
+// CUDA Graphs"; "few (even single) spheres" per iteration).  The eager update
+// reads three sizes back to the host between its ~35 launches (dirty count, candidate count,
+// totals).  Here every size lives in a device record (PDyn) that the kernels read, the grids
+// are sized by bounds, and the whole update -- staging, dirty detection, re-filter, clip,
+// piece output, row update -- is ONE CUDA graph, captured once per buffer layout and replayed
+// with one host round trip.  Checks the eager path makes on the host (slab capacity, work
+// queues, pool room) are made on the device; a failed check idles the rest of the graph and
+// the host redoes the batch eagerly (partial_batch), so the results are the eager path's.
+
+#ifndef RPD_GRAPH_MAX_M
+#define RPD_GRAPH_MAX_M 64  // largest M that takes the graph path
+#endif
+#ifndef RPD_GRAPH_NC_MAX
+#define RPD_GRAPH_NC_MAX (1 << 15)  // batch-candidate bound of the graph's grids
+#endif
+
+static bool graph_eligible(const rpd_ctx* c, int64_t M) {
+  return c->graph && M > 0 && M <= RPD_GRAPH_MAX_M && c->filter_mode == RPD_FILTER_PRUNED &&
+         !c->euler && !c->clip_wide && !c->clip_tiers && !c->profile && c->st.T > 0 &&
+         c->st.N > 0 && c->tr_on != 1;
+}
+
+static inline int64_t tiles_of(int64_t n) { return n > 0 ? (n + 4095) / 4096 : 1; }
+
+// the launch sequence (issued once per buffer layout into a capturing stream)
+static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
+  const int64_t T = c->st.T;
+  PDyn* pd = c->pdd;
+  cudaError_t e;
+  unsigned long long* st = c->stats.as<unsigned long long>();
+  if ((e = cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream))) return e;
+  if ((e = cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream)))
+    return e;
+  if ((e = launch_pd_init(c))) return e;
+  if ((e = launch_check_new_ids(c, nullptr, RPD_GRAPH_MAX_M, 0))) return e;
+  if ((e = stage_launch(c, nullptr, nullptr, nullptr, true, 0))) return e;
+  // (1) dirty tets: Alg. 1 of every tet against the new spheres only
+  if ((e = launch_filter(c, nullptr, T, 0, 0, RPD_GRAPH_MAX_M, c->d_count.as<int32_t>(),
+                         nullptr, nullptr)))
+    return e;
+  if ((e = launch_dirty_list(c, T))) return e;
+  if ((e = launch_changed_list(c, Nb))) return e;
+  // (2) re-filter of the dirty tets over the changed rows; kept old candidates
+  CandSet& cd = c->cand_d;
+  CandSet& pool_c = c->cand[c->cur];
+  PieceSet& pool_p = c->pcs[c->cur];
+  const int32_t* dl = c->d_list.as<int32_t>();
+  const int cap = c->slab_cap;
+  int32_t* k_tet = c->k_tet.as<int32_t>();
+  int32_t* k_words = c->k_words.as<int32_t>();
+  int32_t* slab = c->slab.as<int32_t>();
+  if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
+  if ((e = launch_filter(c, dl, T, cap, 0, (int)Nb, k_tet, slab, k_words, c->c_list.as<int32_t>(),
+                         &pd->n_chg)))
+    return e;
+  if ((e = launch_keep_old(c, dl, T, pool_c, cap, k_tet, slab, k_words))) return e;
+  if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
+  if ((e = launch_max_ktet(c, T, k_tet))) return e;
+  {
+    const int32_t* in[2] = {k_tet, k_words};
+    int32_t* out[2] = {cd.off.as<int32_t>(), c->w_off.as<int32_t>()};
+    if ((e = launch_scan_i32_multi(c, in, out, 2, T, &pd->nb))) return e;
+  }
+  if ((e = launch_pd_check(c, cd.off.as<int32_t>(), c->w_off.as<int32_t>()))) return e;
+  int32_t* pool_idx = pool_c.idx.as<int32_t>();  // (the kernels add the fill level)
+  if ((e = launch_compact_cands(c, T, cap, k_tet, slab, cd.off.as<int32_t>(), pool_idx,
+                                cd.pair_tet.as<int32_t>(), c->w_off.as<int32_t>(),
+                                cd.moff.as<int32_t>(), nc_max, cd.cut.as<unsigned>())))
+    return e;
+  // (3) clip the batch; its pieces to the pool's tail
+  for (DevBuf* b : {&c->p_over, &c->p_over2, &c->p_over3})
+    if ((e = cudaMemsetAsync(b->p, 0, sizeof(int32_t), c->stream))) return e;
+  if ((e = cudaMemsetAsync(st + ST_EXACT, 0, sizeof(unsigned long long) * 5, c->stream))) return e;
+  if ((e = cudaMemsetAsync(st + ST_CLIP_PLANES, 0, sizeof(unsigned long long) * 8, c->stream)))
+    return e;
+  if ((e = launch_clip(c, nc_max, cd.pair_tet.as<int32_t>(), dl, pool_idx, cd.moff.as<int32_t>(),
+                       cd.cut.as<unsigned>(), 0)))
+    return e;
+  if ((e = launch_clip_overflow(c, cd.pair_tet.as<int32_t>(), dl, pool_idx,
+                                cd.moff.as<int32_t>(), cd.cut.as<unsigned>())))
+    return e;
+  if ((e = launch_piece_scans(c, nc_max, cd.moff.as<int32_t>()))) return e;
+  PieceDst d{c->pcs_d.off.as<int32_t>(), pool_p.sphere.as<int32_t>(), pool_p.vol.as<double>(),
+             pool_p.m1.as<double>(), pool_p.fm.as<uint8_t>(), pool_p.inc_off.as<int32_t>(),
+             pool_p.inc.as<int32_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+             nullptr, nullptr, 0, 0};
+  if ((e = launch_compact_pieces(c, T, nc_max, cd.off.as<int32_t>(), pool_idx,
+                                 cd.moff.as<int32_t>(), d)))
+    return e;
+  // (4) re-point the dirty tets' rows; the totals back to the host
+  unsigned long long* rm = c->m_cnt.as<unsigned long long>();
+  if ((e = launch_rows_update(c, dl, T, pool_c, pool_p, cd, c->pcs_d, 0, 0, rm))) return e;
+  if ((e = launch_pd_final(c))) return e;
+  return readback(c, RbSpec{{c->p_over.as<int32_t>()}, st, c->errw.as<int>(), rm});
+}
+
+static void graph_clear(rpd_ctx* c) {
+  for (int k = 0; k < rpd_ctx::G_CACHE; ++k) {
+    if (c->g_exec[k]) cudaGraphExecDestroy(c->g_exec[k]);
+    c->g_exec[k] = nullptr;
+    c->g_sig[k] = 0;
+  }
+}
+
+static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new,
+                                const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                const int32_t* new_ids, int64_t M, rpd_pieces* out,
+                                const int32_t** dirty_tets, int64_t* n_dirty) {
+  const int64_t N_old = c->st.N, T = c->st.T;
+  // inputs on the device (host arrays are copied on the ctx stream ahead of the graph)
+  rpd_status s = read_E(c, nbr_off, N_new, &E);
+  if (s) return s;
+  if (E > 0 && !nbr_idx) return fail(c, RPD_EINVAL, "nbr_idx is NULL");
+  const double* d_sph = nullptr;
+  const int32_t *d_off = nullptr, *d_idx = nullptr, *d_new = nullptr;
+  CK(resolve(c, spheres, 4 * N_new, c->h_spheres, &d_sph), "stage spheres");
+  CK(resolve(c, nbr_off, N_new + 1, c->h_off, &d_off), "stage nbr_off");
+  CK(resolve(c, nbr_idx, E, c->h_idx, &d_idx), "stage nbr_idx");
+  CK(resolve(c, new_ids, M, c->h_new, &d_new), "stage new ids");
+  // room at the pools' tails for a batch at the graph's bounds (a compaction, when the pools
+  // are full, runs here -- before the new rows are staged, like every state read of the pools)
+  const int64_t nc_max = RPD_GRAPH_NC_MAX, nw_max = 4 * nc_max;
+  s = reserve_pools(c, nc_max, nc_max, 32 * nc_max, 0);  // (checked exactly on the device)
+  if (s) return s;
+  c->rpe_n = -1;
+  ++c->epoch;
+  c->last.N = N_new;
+  CK(stage_prepare(c, N_new, E), "stage");
+  // every buffer sized for the graph's bounds (allocation moves buffers: a new capture)
+  const int64_t Nb = (int64_t)(c->st.sw.cap / sizeof(double4));
+  const int64_t n_leaf = (T + 31) / 32, n_sup = (n_leaf + 31) / 32;
+  {
+    const int64_t ci0 = RPD_GRAPH_MAX_M * n_leaf + 4096, cs0 = RPD_GRAPH_MAX_M * n_sup + 4096;
+    int64_t ci1 = std::max<int64_t>(48 * Nb + 4 * n_leaf + 4096, c->bvh_min_items);
+    int64_t cs1 = std::max<int64_t>(8 * Nb + 4 * n_sup + 4096, c->bvh_min_items);
+    ci1 = std::min<int64_t>(ci1, 1 << 30);
+    cs1 = std::min<int64_t>(cs1, 1 << 30);
+    c->dd_cap[0][0] = ci0;
+    c->dd_cap[0][1] = cs0;
+    c->dd_cap[1][0] = ci1;
+    c->dd_cap[1][1] = cs1;
+    CK(c->bvh_items.ensure(sizeof(int2) * (std::max(ci0 + cs0, ci1 + cs1) + 1)), "alloc");
+  }
+  const size_t nt = (size_t)T;
+  const size_t scan_words = 8 + (1 + tiles_of(T)) + (1 + tiles_of(Nb)) + (1 + 2 * tiles_of(T)) +
+                            (1 + 2 * tiles_of(nc_max));
+  struct {
+    DevBuf* b;
+    size_t bytes;
+  } need[] = {
+      {&c->d_count, 4 * nt},          {&c->d_flag, nt},
+      {&c->d_scan, 4 * (nt + 1)},     {&c->d_pos, 4 * nt},
+      {&c->min_epoch, 4},             {&c->c_flag, (size_t)Nb},
+      {&c->c_scan, 4 * (size_t)(Nb + 1)}, {&c->c_list, 4 * (size_t)Nb},
+      {&c->k_tet, 4 * nt},            {&c->k_words, 4 * nt},
+      {&c->cand_d.off, 4 * (nt + 1)}, {&c->w_off, 4 * (nt + 1)},
+      {&c->slab, 4 * (size_t)c->slab_cap * nt}, {&c->slab_m, 8 * (size_t)c->slab_cap * nt},
+      {&c->cand_d.pair_tet, 4 * (size_t)nc_max}, {&c->cand_d.moff, 4 * (size_t)(nc_max + 1)},
+      {&c->cand_d.cut, 4 * (size_t)nw_max}, {&c->pcs_d.off, 4 * (nt + 1)},
+      {&c->p_flag, (size_t)nc_max},   {&c->p_f01, 4 * (size_t)nc_max},
+      {&c->p_fm, (size_t)nc_max},     {&c->p_vol, 8 * (size_t)nc_max},
+      {&c->p_m1, 24 * (size_t)nc_max}, {&c->p_ninc, 4 * (size_t)nc_max},
+      {&c->p_over, 4 * (size_t)(nc_max + 1)}, {&c->p_over2, 4 * (size_t)(nc_max + 1)},
+      {&c->p_over3, 4 * (size_t)(nc_max + 1)}, {&c->p_mask, 4 * (size_t)nw_max},
+      {&c->p_scan, 4 * (size_t)(nc_max + 1)}, {&c->i_scan, 4 * (size_t)(nc_max + 1)},
+      {&c->p_dyn, 4},                 {&c->m_cnt, 32},
+      {&c->cand_long, 4 * (nt + 1)},  {&c->bvh, 8 * 6 * (size_t)(n_leaf + n_sup)},
+      {&c->g_scan, 8 * scan_words},   {&c->pd_buf, sizeof(PDyn)}};
+  for (auto& x : need) CK(x.b->ensure(x.bytes), "alloc");
+  if (!c->pd_host) {
+    void* h = nullptr;
+    CK(cudaHostAlloc(&h, sizeof(PDyn), cudaHostAllocMapped), "alloc");
+    c->pd_host = (PDyn*)h;
+    void* hd = nullptr;
+    CK(cudaHostGetDevicePointer(&hd, h, 0), "alloc");
+    c->pd_hdev = (PDyn*)hd;
+  }
+  CandSet& pool_c = c->cand[c->cur];
+  PieceSet& pool_p = c->pcs[c->cur];
+  PDyn& h = *c->pd_host;
+  h = PDyn{};
+  h.spheres = d_sph;
+  h.nbr_off = d_off;
+  h.nbr_idx = d_idx;
+  h.new_ids = d_new;
+  h.N = (int)N_new;
+  h.N_old = (int)N_old;
+  h.E = (int)E;
+  h.M = (int)M;
+  h.epoch = c->epoch;
+  h.fill_c = (int)pool_c.fill;
+  h.fill_p = (int)pool_p.fill_p;
+  h.fill_i = (int)pool_p.fill_i;
+  h.room_c = (int)std::min<size_t>(pool_c.idx.cap / 4, INT32_MAX);
+  h.room_p = (int)std::min<size_t>(
+      std::min(std::min(pool_p.sphere.cap / 4, pool_p.vol.cap / 8),
+               std::min(std::min(pool_p.m1.cap / 24, pool_p.fm.cap), pool_p.inc_off.cap / 4 - 1)),
+      INT32_MAX);
+  h.room_i = (int)std::min<size_t>(pool_p.inc.cap / 4, INT32_MAX);
+  h.nc_max = (int)nc_max;
+  h.nw_max = (int)nw_max;
+  h.cap_items = (int)c->dd_cap[1][0];
+  h.cap_sup = (int)c->dd_cap[1][1];
+  // the graph of this buffer layout (captured on first use)
+  unsigned long long sig = 1469598103934665603ull;
+  for (unsigned long long v :
+       {(unsigned long long)g_alloc_gen.load(), (unsigned long long)(uintptr_t)c->st.sw.p,
+        (unsigned long long)(uintptr_t)c->st.old_sw.p, (unsigned long long)c->cur,
+        (unsigned long long)c->slab_cap, (unsigned long long)T,
+        (unsigned long long)c->bvh_min_items, (unsigned long long)c->sms})
+    sig = (sig ^ v) * 1099511628211ull;
+  int slot = -1;
+  for (int k = 0; k < rpd_ctx::G_CACHE; ++k)
+    if (c->g_exec[k] && c->g_sig[k] == sig) slot = k;
+  if (slot < 0) {
+    if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
+    // (the capture is ordered after the work already queued on the ctx stream by the graph's
+    // launch below, not by the capture itself: nothing is executed while capturing)
+    cudaStream_t saved = c->stream;
+    c->stream = c->cap_stream;
+    c->pdd = c->pd_buf.as<PDyn>();
+    c->g_scan_used = 0;
+    const int64_t l0 = c->launches;
+    cudaError_t e = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed);
+    cudaError_t e1 = e ? e : issue_dd(c, Nb, nc_max);
+    cudaGraph_t g = nullptr;
+    cudaError_t e2 = e ? cudaSuccess : cudaStreamEndCapture(c->cap_stream, &g);
+    c->stream = saved;
+    c->pdd = nullptr;
+    c->g_nodes = c->launches - l0;
+    c->launches = l0;
+    if (e1 || e2) {
+      if (g) cudaGraphDestroy(g);
+      return cuda_fail(c, e1 ? e1 : e2, "graph capture");
+    }
+    cudaGraphExec_t x = nullptr;
+    e = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    CK(e, "graph instantiate");
+    slot = c->g_next;
+    c->g_next = (c->g_next + 1) % rpd_ctx::G_CACHE;
+    if (c->g_exec[slot]) cudaGraphExecDestroy(c->g_exec[slot]);
+    c->g_exec[slot] = x;
+    c->g_sig[slot] = sig;
+    c->g_kernels[slot] = c->g_nodes;
+    ++c->g_captures;
+  }
+  CK(cudaGraphLaunch(c->g_exec[slot], c->stream), "graph launch");
+  c->launches += c->g_kernels[slot];
+  ++c->g_launches;
+  CK(cudaStreamSynchronize(c->stream), "partial update");
+  const PDyn r = *c->pd_host;
+  const Readback* rb = (const Readback*)c->pinned;
+  if (rb->err[0] != 0) {
+    if (rb->err[1] == 100) return fail(c, RPD_EINVAL, "new_ids is not the appended id range");
+    return check_err(c, rb);
+  }
+  c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
+  c->last.pairs_tested += (int64_t)rb->u64[ST_TESTED];
+  if (r.abort) {  // a device-side check failed: the batch again, eagerly (same results)
+    ++c->g_fallbacks;
+    return partial_batch(c, r.nd, N_new, M, out, dirty_tets, n_dirty);
+  }
+  if (rb->u64[ST_OVERFLOW])
+    return fail(c, RPD_EOVERFLOW, "a piece exceeded the wide clip capacity (128 vertices/planes)");
+  absorb_clip_stats(c, rb, rb->i32[0]);
+  c->last.max_k_tet = r.maxk;
+  c->last.pairs_clipped += r.nc;
+  CandSet& cd = c->cand_d;
+  PieceSet& pd = c->pcs_d;
+  cd.n = r.nc;
+  cd.n_tets = r.nd;
+  cd.n_words = r.nw;
+  cd.idx_ext = pool_c.idx.as<int32_t>() + pool_c.fill;
+  pd.n_tets = r.nd;
+  pd.n_pieces = r.np;
+  pd.n_inc = r.ni;
+  pd.n_rpf = 0;
+  const unsigned long long* removed = rb->u4;
+  pool_c.fill += r.nc;
+  pool_p.fill_p += r.np;
+  pool_p.fill_i += r.ni;
+  pool_c.n += r.nc - (int64_t)removed[0];
+  pool_p.n_pieces += r.np - (int64_t)removed[1];
+  pool_p.n_inc += r.ni - (int64_t)removed[2];
+  c->compact = false;
+  c->eu_valid = false;
+  c->last.n_cand_dirty = r.nc;
+  c->last.n_pieces_dirty = r.np;
+  c->last.n_inc_dirty = r.ni;
+  c->n_dirty = r.nd;
+  c->last.n_dirty = r.nd;
+  c->last.n_cand = pool_c.n;
+  c->last.n_pieces = pool_p.n_pieces;
+  c->last.n_inc = pool_p.n_inc;
+  c->last.pairs_filtered = T * M + (int64_t)r.nd * N_new;
+  *dirty_tets = c->d_list.as<int32_t>();
+  *n_dirty = r.nd;
   return fill_pieces(c, out);
 }
 
@@ -1653,6 +1996,9 @@ rpd_status rpd_get_stats(rpd_ctx* c, rpd_stats* out) {
   if (!c || !out) return RPD_EINVAL;
   *out = c->last;
   out->kernel_launches = c->launches;
+  out->graph_updates = c->g_launches;
+  out->graph_captures = c->g_captures;
+  out->graph_fallbacks = c->g_fallbacks;
   return RPD_OK;
 }
 

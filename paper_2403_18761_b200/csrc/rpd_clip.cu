@@ -397,9 +397,13 @@ __global__ void __launch_bounds__(VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREA
     const int32_t* __restrict__ nbr_idx, const double4* __restrict__ planes,
     const int32_t* __restrict__ twin, long long N, PairOut out,
     unsigned long long* __restrict__ stats, const int32_t* __restrict__ n_dev,
-    int* __restrict__ dyn) {
+    int* __restrict__ dyn, const PDyn* __restrict__ pd) {
   using WS = WarpState<GW, VPL>;
   if (n_dev) n_pairs = *n_dev;
+  if (pd) {  // device-driven update: the sphere count and the pool tail from the device
+    N = pd->N;
+    cand_idx += pd->fill_c;
+  }
   constexpr int MAXP = WS::MAXP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WS& S = reinterpret_cast<WS*>(smem_raw)[threadIdx.x / GW];
@@ -1191,7 +1195,8 @@ __global__ void k_count_inc(int64_t n_pairs, const uint8_t* __restrict__ flag,
                             const int32_t* __restrict__ mask_off,
                             const unsigned* __restrict__ mask, int32_t* __restrict__ ninc,
                             int32_t* __restrict__ f01, const unsigned* __restrict__ rmask,
-                            int32_t* __restrict__ nrpf) {
+                            int32_t* __restrict__ nrpf, const int* __restrict__ n_dev) {
+  if (n_dev) n_pairs = *n_dev;
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
   int n = 0, r = 0;
@@ -1234,14 +1239,26 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
                                  int32_t* __restrict__ piece_sphere, double* __restrict__ piece_vol,
                                  double* __restrict__ piece_m1, uint8_t* __restrict__ piece_fm,
                                  int32_t* __restrict__ inc_off, int32_t* __restrict__ inc_sphere,
-                                 EuCompact eu) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n_pairs) return;
+                                 EuCompact eu, const PDyn* __restrict__ pd) {
+  if (pd) {  // device-driven update: the batch size and the pool tails from the device
+    n_pairs = pd->nc;
+    cand_idx += pd->fill_c;
+    piece_sphere += pd->fill_p;
+    piece_vol += pd->fill_p;
+    piece_m1 += 3 * (int64_t)pd->fill_p;
+    piece_fm += pd->fill_p;
+    inc_off += pd->fill_p;
+    inc_sphere += pd->fill_i;
+    eu.inc_base = pd->fill_i;
+    if (n_pairs == 0 && blockIdx.x == 0 && threadIdx.x == 0) inc_off[0] = eu.inc_base;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_pairs; p += stride) {
   if (p == n_pairs - 1) {
     inc_off[pscan[n_pairs]] = eu.inc_base + iscan[n_pairs];
     if (eu.rmask) eu.rpf_off[pscan[n_pairs]] = eu.rpf_base + eu.rscan[n_pairs];
   }
-  if (flag[p] != 1) return;
+  if (flag[p] != 1) continue;
   const int q = pscan[p];
   const int i = cand_idx[p];
   piece_sphere[q] = i;
@@ -1282,13 +1299,16 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
       }
     }
   }
+  }
 }
 
 __global__ void k_piece_off(int64_t T, const int32_t* __restrict__ cand_off,
-                            const int32_t* __restrict__ pscan, int32_t* __restrict__ piece_off) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t > T) return;
-  piece_off[t] = pscan[cand_off[t]];
+                            const int32_t* __restrict__ pscan, int32_t* __restrict__ piece_off,
+                            const int* __restrict__ n_dev) {
+  if (n_dev) T = *n_dev;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= T; t += stride)
+    piece_off[t] = pscan[cand_off[t]];
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
@@ -1352,7 +1372,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
       n, pair_list, pair_tet, tet_ids, cand_idx, c->st.tx.as<double>(), c->st.T,
       c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), c->st.planes.as<double4>(),
       c->st.twin.as<int32_t>(), (long long)c->st.N, o, c->stats.as<unsigned long long>(),
-      n_dev, dyn);
+      n_dev, dyn, c->pdd);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -1381,6 +1401,14 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
                         const unsigned* cut, int wide) {
   c->clip_small = 0;
   if (n_pairs == 0) return cudaSuccess;
+  if (c->pdd) {
+    // device-driven update (few insertions): the 64-slot tier on every pair, n_pairs is the
+    // bound of the grid, the count is read on the device
+    c->clip_small = 1;
+    return launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                      cand_idx, moff, cut,
+                                                      c->p_over2.as<int32_t>(), &c->pdd->nc);
+  }
   if (!wide && n_pairs < RPD_CLIP_SMALL && !c->clip_tiers) {
     // few pairs (small partial updates): latency, not throughput -- one pass of the 64-slot
     // tier over every pair instead of the fast tier plus a re-run of its overflows
@@ -1459,24 +1487,29 @@ cudaError_t launch_clip_overflow(rpd_ctx* c, const int32_t* pair_tet, const int3
                   : launch_overflow_eu<false>(c, pair_tet, tet_ids, cand_idx, moff, cut);
 }
 
+// (device-driven update: n_pairs is the bound, the count is pd->nc)
 cudaError_t launch_piece_scans(rpd_ctx* c, int64_t n_pairs, const int32_t* moff) {
+  const int* n_dev = c->pdd ? &c->pdd->nc : nullptr;
   if (n_pairs > 0) {
     k_count_inc<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
         n_pairs, c->p_flag.as<uint8_t>(), moff, c->p_mask.as<unsigned>(),
         c->p_ninc.as<int32_t>(), c->p_f01.as<int32_t>(),
-        c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_nrpf.as<int32_t>());
+        c->euler ? c->p_rmask.as<unsigned>() : nullptr, c->p_nrpf.as<int32_t>(), n_dev);
     ++c->launches;
   }
   const int32_t* in[3] = {c->p_f01.as<int32_t>(), c->p_ninc.as<int32_t>(), c->p_nrpf.as<int32_t>()};
   int32_t* out[3] = {c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(), c->r_scan.as<int32_t>()};
-  return launch_scan_i32_multi(c, in, out, c->euler ? 3 : 2, n_pairs);
+  return launch_scan_i32_multi(c, in, out, c->euler ? 3 : 2, n_pairs, n_dev);
 }
 
 cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                                   const int32_t* cand_off, const int32_t* cand_idx,
                                   const int32_t* moff, const PieceDst& d) {
-  if (n_pairs > 0) {
-    k_compact_pieces<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(
+  const PDyn* pd = c->pdd;  // device-driven update: bounds here, counts / pool tails in pd
+  if (n_pairs > 0 || pd) {
+    unsigned grid = nblk(n_pairs > 0 ? n_pairs : 1, 256);
+    if (pd && grid > (unsigned)c->sms * 4) grid = c->sms * 4;  // (grid-stride over the bound)
+    k_compact_pieces<<<grid, 256, 0, c->stream>>>(
         n_pairs, cand_idx, c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(),
         c->p_flag.as<uint8_t>(), c->p_scan.as<int32_t>(), c->i_scan.as<int32_t>(),
         c->p_vol.as<double>(), c->p_m1.as<double>(), c->p_fm.as<uint8_t>(),
@@ -1486,7 +1519,7 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
                   d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm,
                   c->p_radj.as<unsigned long long>(), d.radj, c->p_rep.as<unsigned long long>(),
-                  d.rep, d.inc_base, d.rpf_base});
+                  d.rep, d.inc_base, d.rpf_base}, pd);
     ++c->launches;
   } else {
     // the terminal offsets of an empty batch (the pool's current fill levels)
@@ -1494,8 +1527,10 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
     if (c->euler)
       cudaMemcpyAsync(d.rpf_off, &d.rpf_base, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);
   }
-  k_piece_off<<<nblk(n_tets + 1, 256), 256, 0, c->stream>>>(n_tets, cand_off,
-                                                          c->p_scan.as<int32_t>(), d.off);
+  unsigned g2 = nblk(n_tets + 1, 256);
+  if (pd && g2 > (unsigned)c->sms * 2) g2 = c->sms * 2;
+  k_piece_off<<<g2, 256, 0, c->stream>>>(n_tets, cand_off, c->p_scan.as<int32_t>(), d.off,
+                                         pd ? &pd->nb : nullptr);
   ++c->launches;
   return cudaGetLastError();
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/rpd.h"
@@ -10,6 +11,10 @@
 #define RPD_MAX_DEVICES 64
 
 namespace rpd {
+
+// Every (re)allocation of a DevBuf bumps this generation: captured CUDA graphs bake device
+// addresses, so a cached graph is valid only while no buffer moved (rpd_graph.cu).
+inline std::atomic<unsigned long long> g_alloc_gen{0};
 
 // Growable ctx-owned device buffer.
 struct DevBuf {
@@ -23,6 +28,7 @@ struct DevBuf {
     size_t want = bytes < 256 ? 256 : bytes + bytes / 8;
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
+    g_alloc_gen.fetch_add(1);
     return e;
   }
   // like ensure, but a (re)allocation reserves `factor` x bytes (pools that grow by appends)
@@ -91,6 +97,7 @@ struct Stage {
   // the previous rows (partial updates copy the rows whose neighbour list is unchanged)
   DevBuf old_off, old_idx, old_planes, old_twin, old_hkey, old_repoch, old_sw;
   int64_t T = 0, N = 0, V = 0, E = 0;
+  int64_t N_prev = 0;  // N of the previous staging (the old rows)
 };
 
 }  // namespace rpd
@@ -130,6 +137,31 @@ struct PieceSet {
   int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;  // live counts
   int64_t fill_p = 0, fill_i = 0, fill_r = 0;              // state: pool slots in use
 };
+// Sizes of a device-driven partial update (the CUDA-graph latency path, rpd_graph.cu): the
+// host writes the inputs part once per update; every size the eager path reads back to the
+// host between its launches is produced and consumed on the device here instead.
+enum PdAbort { PD_SLAB = 1, PD_QUEUE = 2, PD_POOL = 4, PD_BATCH = 8, PD_ERR = 16 };
+struct PDyn {
+  // inputs (host-written per update)
+  const double* spheres;
+  const int32_t* nbr_off;
+  const int32_t* nbr_idx;
+  const int32_t* new_ids;
+  int N, N_old, E, M, epoch;
+  int fill_c, fill_p, fill_i;  // state-pool fill levels (the batch is appended there)
+  int room_c, room_p, room_i;  // state-pool capacities (entries)
+  int nc_max, nw_max;          // batch candidate / mask-word bounds of the captured grids
+  int cap_items, cap_sup;      // BVH work-queue capacities of the restricted re-filter
+  // outputs (device-written)
+  int nd;      // dirty tets
+  int nb;      // tets of the batch: nd, or 0 once aborted (the rest of the graph idles)
+  int n_chg;   // spheres whose rows changed since the dirty tets' candidate lists
+  int nc, nw;  // batch candidates and incidence-mask words (0 once aborted)
+  int np, ni;  // batch pieces and incidences
+  int maxk, need;  // largest k_tet, work-queue demand of the re-filter
+  int abort;   // PdAbort bits: the eager path redoes the batch (re-filter onwards)
+};
+
 }  // namespace rpd
 
 struct rpd_ctx {
@@ -192,6 +224,24 @@ struct rpd_ctx {
   int epoch = 0;               // 0 after rpd_relations, +1 per partial update
   int64_t n_dirty = 0;
 
+  // device-driven partial updates captured as CUDA graphs (rpd_graph.cu)
+  rpd::PDyn* pdd = nullptr;     // non-null while the device-driven sequence is being issued
+  rpd::DevBuf pd_buf;           // PDyn (device)
+  rpd::PDyn* pd_host = nullptr; // PDyn (mapped pinned): inputs in, outputs back
+  rpd::PDyn* pd_hdev = nullptr; // its device-side address
+  rpd::DevBuf g_scan;           // look-back state of the graph's scans (reset by memset nodes)
+  size_t g_scan_used = 0;
+  cudaStream_t cap_stream = nullptr;  // capture stream (the legacy stream cannot capture)
+  static constexpr int G_CACHE = 4;
+  unsigned long long g_sig[G_CACHE] = {};
+  cudaGraphExec_t g_exec[G_CACHE] = {};
+  int64_t g_kernels[G_CACHE] = {};  // kernel nodes per cached graph
+  int64_t g_nodes = 0;
+  int g_next = 0;
+  int graph = 1;                // RPD_OPT_GRAPH (env RPD_GRAPH=0 turns it off)
+  int64_t g_launches = 0, g_captures = 0, g_fallbacks = 0;
+  int64_t dd_cap[2][2] = {};    // BVH queue capacities {items, super items}: dirty, re-filter
+
   rpd_stats last{};
   int profile = 0;             // record CUDA events around the filter and clip kernels
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -252,15 +302,22 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
 cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
                                  const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                                  bool reuse_rows, int epoch);
+// launch_stage_spheres = stage_prepare (host: buffer swap + sizes) + stage_launch (kernels)
+cudaError_t stage_prepare(rpd_ctx* c, int64_t N, int64_t E);
+cudaError_t stage_launch(rpd_ctx* c, const double* spheres, const int32_t* nbr_off,
+                         const int32_t* nbr_idx, bool reuse_rows, int epoch);
 cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
                                    int32_t* cnt, int32_t* off);
 cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
                                    int32_t* cnt, const int32_t* off, int32_t* tmp, int32_t* idx);
 void clip_phase_dump();  // development aid (RPD_CLIP_PHASES builds)
-cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n);
-cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n);
+// n_dev (device-driven update): the length read on the device, n its bound
+cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n,
+                            const int* n_dev = nullptr);
+cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n,
+                           const int* n_dev = nullptr);
 cudaError_t launch_scan_i32_multi(rpd_ctx* c, const int32_t* const* in, int32_t* const* out,
-                                  int K, int64_t n);
+                                  int K, int64_t n, const int* n_dev = nullptr);
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
                           int sphere_lo, int sphere_hi, int32_t* k_tet, int32_t* slab,
                           int32_t* k_words, const int32_t* sphere_list = nullptr,
@@ -317,6 +374,11 @@ cudaError_t launch_rows_from_off(rpd_ctx* c, int64_t T, const CandSet* cs, Piece
 cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, CandSet& pool_c,
                                PieceSet& pool_p, const CandSet& cd, const PieceSet& pd,
                                int64_t cbase, int64_t pbase, unsigned long long* rm);
+// device-driven partial update (rpd_graph): PDyn init from the pinned mirror, the checks
+// after the re-filter (batch totals, capacities; abort), the totals back to the mirror
+cudaError_t launch_pd_init(rpd_ctx* c);
+cudaError_t launch_pd_check(rpd_ctx* c, const int32_t* c_off, const int32_t* w_off);
+cudaError_t launch_pd_final(rpd_ctx* c);
 // compaction of the state pools (by rows) into the plain CSRs cn / pn (pair_tet and moff of
 // the candidates rebuilt); phase 0: counts + scans, phase 1: copies
 cudaError_t launch_compact_state(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,

@@ -129,7 +129,12 @@ constexpr int BVH_LCAP = 256;   // planes staged per warp in the leaf kernel
 // exact lattice AABB of every leaf (32 consecutive tets of the list)
 __global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
                              const int32_t* __restrict__ tet_ids, int64_t n,
-                             double* __restrict__ leaf, int64_t n_leaf) {
+                             double* __restrict__ leaf, int64_t n_leaf,
+                             const int* __restrict__ n_dev) {
+  if (n_dev) {  // device-driven update: the list length from the device
+    n = *n_dev;
+    n_leaf = (n + BVH_LEAF - 1) / BVH_LEAF;
+  }
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool valid = a < n;
@@ -164,7 +169,12 @@ __global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
 
 // AABB of every super node (32 consecutive leaves)
 __global__ void k_super_boxes(const double* __restrict__ leaf, int64_t n_leaf,
-                              double* __restrict__ sup, int64_t n_sup) {
+                              double* __restrict__ sup, int64_t n_sup,
+                              const int* __restrict__ n_dev) {
+  if (n_dev) {
+    n_leaf = (*n_dev + BVH_LEAF - 1) / BVH_LEAF;
+    n_sup = (n_leaf + BVH_FAN - 1) / BVH_FAN;
+  }
   const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   double bl[3] = {1e300, 1e300, 1e300}, bh[3] = {-1e300, -1e300, -1e300};
@@ -228,7 +238,16 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_top(
     const double* __restrict__ sup, int64_t n_sup, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, int N, int lo, int hi, int2* __restrict__ items,
     int cap_items, int* __restrict__ n_items, const int32_t* __restrict__ list,
-    const int* __restrict__ n_list_dev, const double4* __restrict__ sw) {
+    const int* __restrict__ n_list_dev, const double4* __restrict__ sw,
+    const PDyn* __restrict__ pd, int sub) {
+  if (pd) {  // device-driven update: sphere range / count and the subset's size from the device
+    N = pd->N;
+    if (!list) {
+      lo = pd->N_old;
+      hi = pd->N;
+    }
+    if (sub) n_sup = ((pd->nb + BVH_LEAF - 1) / BVH_LEAF + BVH_FAN - 1) / BVH_FAN;
+  }
   if (n_list_dev) hi = lo + *n_list_dev;
   __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
 #if RPD_BVH_SORT
@@ -311,7 +330,8 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
     const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, const int2* __restrict__ sitems,
     const int* __restrict__ n_sitems_p, int cap_sitems, int2* __restrict__ items,
-    int cap_items, int* __restrict__ n_items) {
+    int cap_items, int* __restrict__ n_items, const int* __restrict__ n_dev) {
+  if (n_dev) n_leaf = (*n_dev + BVH_LEAF - 1) / BVH_LEAF;
   __shared__ double4 s_pl[BVH_WARPS][BVH_PCAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -355,7 +375,11 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
     const double4* __restrict__ planes, const int2* __restrict__ items,
     const int* __restrict__ n_items_p, int cap_items, int cap, int32_t* __restrict__ k_tet,
     int32_t* __restrict__ slab, uint2* __restrict__ slab_m, int32_t* __restrict__ k_words,
-    unsigned long long* __restrict__ stats) {
+    unsigned long long* __restrict__ stats, const int* __restrict__ n_dev) {
+  if (n_dev) {
+    n = *n_dev;
+    n_leaf = (n + BVH_LEAF - 1) / BVH_LEAF;
+  }
   extern __shared__ double4 s_lpl[];  // BVH_WARPS x BVH_LCAP planes
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -482,7 +506,8 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
 }
 
 __global__ void k_max_ktet(int64_t n, const int32_t* __restrict__ k_tet,
-                           unsigned long long* __restrict__ stats) {
+                           unsigned long long* __restrict__ stats, const int* __restrict__ n_dev) {
+  if (n_dev) n = *n_dev;
   int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int m = a < n ? k_tet[a] : 0;
 #pragma unroll
@@ -516,8 +541,14 @@ __global__ void __launch_bounds__(256) k_compact_cands_t(
     int32_t* __restrict__ pair_tet, const int32_t* __restrict__ w_off,
     int32_t* __restrict__ p_moff, const int32_t* __restrict__ nbr_off, int64_t n_pairs,
     int32_t* __restrict__ long_list, int* __restrict__ n_long, const uint2* __restrict__ slab_m,
-    unsigned* __restrict__ p_cut) {
+    unsigned* __restrict__ p_cut, const PDyn* __restrict__ pd) {
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pd) {  // device-driven update: batch sizes and the pool tail from the device
+    n = pd->nb;
+    n_pairs = pd->nc;
+    cand_idx += pd->fill_c;
+    if (n == 0 && a == 0 && p_moff) p_moff[0] = 0;
+  }
   if (a >= n) return;
   const int k = min(k_tet[a], cap);
   const int32_t* s = slab + a * cap;
@@ -572,7 +603,9 @@ __global__ void k_compact_cands_w(const int32_t* __restrict__ list, const int* _
                                 int32_t* __restrict__ cand_idx, int32_t* __restrict__ pair_tet,
                                 const int32_t* __restrict__ w_off, int32_t* __restrict__ p_moff,
                                 const int32_t* __restrict__ nbr_off, int64_t n_pairs,
-                                const uint2* __restrict__ slab_m, unsigned* __restrict__ p_cut) {
+                                const uint2* __restrict__ slab_m, unsigned* __restrict__ p_cut,
+                                const PDyn* __restrict__ pd) {
+  if (pd) cand_idx += pd->fill_c;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -637,11 +670,14 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
                            const int32_t* __restrict__ repoch, const int* __restrict__ min_epoch,
                            const int32_t* __restrict__ nbr_off, int cap,
                            int32_t* __restrict__ k_tet, int32_t* __restrict__ slab,
-                           uint2* __restrict__ slab_m, int32_t* __restrict__ k_words) {
-  const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;  // warp per tet
-  if (a >= n) return;
+                           uint2* __restrict__ slab_m, int32_t* __restrict__ k_words,
+                           const int* __restrict__ n_dev) {
+  if (n_dev) n = *n_dev;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // warp per tet (grid-stride)
+  for (int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; a < n; a += nwarp) {
   const int t = dirty[a];
   const int me = *min_epoch;
   const int2 rw = co_rows[t];  // the tet's old candidates in the state pool
@@ -669,52 +705,65 @@ __global__ void k_keep_old(int64_t n, const int32_t* __restrict__ dirty,
       }
     }
   }
+  }
 }
 
 cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
                             const CandSet& co, int cap, int32_t* k_tet, int32_t* slab,
                             int32_t* k_words) {
   if (n_dirty == 0) return cudaSuccess;
-  k_keep_old<<<nblk(n_dirty * 32, 256), 256, 0, c->stream>>>(
+  const PDyn* pd = c->pdd;
+  unsigned grid = nblk(n_dirty * 32, 256);
+  if (pd && grid > (unsigned)c->sms * 8) grid = c->sms * 8;  // (grid-stride over the bound)
+  k_keep_old<<<grid, 256, 0, c->stream>>>(
       n_dirty, dirty, co.rows.as<int2>(), co.idx.as<int32_t>(), c->st.repoch.as<int32_t>(),
       c->min_epoch.as<int>(), c->st.nbr_off.as<int32_t>(), cap, k_tet, slab,
-      slab ? c->slab_m.as<uint2>() : nullptr, k_words);
+      slab ? c->slab_m.as<uint2>() : nullptr, k_words, pd ? &pd->nb : nullptr);
   ++c->launches;
   return cudaGetLastError();
 }
 
 __global__ void k_chg_flags(int64_t N, const int32_t* __restrict__ repoch,
-                            const int* __restrict__ min_epoch, uint8_t* __restrict__ flag) {
+                            const int* __restrict__ min_epoch, uint8_t* __restrict__ flag,
+                            const PDyn* __restrict__ pd) {
+  if (pd) N = pd->N;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N) flag[i] = repoch[i] > *min_epoch;
 }
 
 __global__ void k_chg_list(int64_t N, const uint8_t* __restrict__ flag,
-                           const int32_t* __restrict__ scan, int32_t* __restrict__ list) {
+                           const int32_t* __restrict__ scan, int32_t* __restrict__ list,
+                           PDyn* __restrict__ pd) {
+  if (pd) N = pd->N;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N && flag[i]) list[scan[i]] = (int32_t)i;
+  if (pd && i == N - 1) pd->n_chg = scan[i] + flag[i];
 }
 
 // list of the spheres whose rows changed (count at c_scan[N])
 cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet) {
   if (n == 0) return cudaSuccess;
-  k_max_ktet<<<nblk(n, 256), 256, 0, c->stream>>>(n, k_tet, c->stats.as<unsigned long long>());
+  k_max_ktet<<<nblk(n, 256), 256, 0, c->stream>>>(n, k_tet, c->stats.as<unsigned long long>(),
+                                                 c->pdd ? &c->pdd->nb : nullptr);
   ++c->launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_changed_list(rpd_ctx* c, int64_t N) {
+  // (device-driven update: N is the grids' bound, the count comes from the device)
+  PDyn* pd = c->pdd;
   if (N > 0) {
     k_chg_flags<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->st.repoch.as<int32_t>(),
                                                      c->min_epoch.as<int>(),
-                                                     c->c_flag.as<uint8_t>());
+                                                     c->c_flag.as<uint8_t>(), pd);
     ++c->launches;
   }
-  cudaError_t e = launch_scan_u8(c, c->c_flag.as<uint8_t>(), c->c_scan.as<int32_t>(), N);
+  cudaError_t e = launch_scan_u8(c, c->c_flag.as<uint8_t>(), c->c_scan.as<int32_t>(), N,
+                                 pd ? &pd->N : nullptr);
   if (e || N == 0) return e;
   k_chg_list<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->c_flag.as<uint8_t>(),
                                                   c->c_scan.as<int32_t>(),
-                                                  c->c_list.as<int32_t>());
+                                                  c->c_list.as<int32_t>(), pd);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -724,6 +773,10 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
                           int32_t* k_words, const int32_t* sphere_list,
                           const int* n_list_dev) {
   if (n_tets == 0) return cudaSuccess;
+  // device-driven update (c->pdd): n_tets is the grids' bound; a tet subset's length and the
+  // sphere range come from the device, the work-queue capacities from the host prologue
+  PDyn* pd = c->pdd;
+  const int* nsub = pd && tet_ids ? &pd->nb : nullptr;
   if (c->filter_mode == RPD_FILTER_PRUNED) {
     const int64_t n_leaf = (n_tets + BVH_LEAF - 1) / BVH_LEAF;
     const int64_t n_sup = (n_leaf + BVH_FAN - 1) / BVH_FAN;
@@ -739,8 +792,9 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
     if (e) return e;
     if (tet_ids || !c->bvh_all_valid) {
       k_leaf_boxes<<<nblk(n_leaf * BVH_LEAF, 256), 256, 0, c->stream>>>(
-          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf);
-      k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup);
+          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf, nsub);
+      k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup,
+                                                                      nsub);
       c->launches += 2;
       if (!tet_ids) c->bvh_all_valid = true;
     }
@@ -754,6 +808,10 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       if (cap_sup < c->bvh_min_items) cap_sup = c->bvh_min_items;
       if (cap_items > (1 << 30)) cap_items = 1 << 30;
       if (cap_sup > (1 << 30)) cap_sup = 1 << 30;
+      if (pd) {
+        cap_items = c->dd_cap[tet_ids ? 1 : 0][0];
+        cap_sup = c->dd_cap[tet_ids ? 1 : 0][1];
+      }
       e = c->bvh_items.ensure(sizeof(int2) * (cap_items + cap_sup + 1));
       if (e) return e;
       int* n_items = c->bvh_items.as<int>();
@@ -764,14 +822,14 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       if (e) return e;
       const int64_t n_chunk = (n_sup + 31) / 32;
       int64_t blocks = (ns * n_chunk + BVH_WARPS - 1) / BVH_WARPS;
-      if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+      if (blocks > (int64_t)sms * (pd ? 4 : 16)) blocks = (int64_t)sms * (pd ? 4 : 16);
       k_bvh_top<<<(unsigned)blocks, BVH_WARPS * 32, 0, c->stream>>>(
           sup, n_sup, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), (int)c->st.N,
           sphere_lo, sphere_hi, sitems, (int)cap_sup, n_sitems, sphere_list, n_list_dev,
-          c->st.sw.as<double4>());
+          c->st.sw.as<double4>(), pd, tet_ids != nullptr);
       k_bvh_super<<<(unsigned)(sms * 16), BVH_WARPS * 32, 0, c->stream>>>(
           leaf, n_leaf, c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), sitems,
-          n_sitems, (int)cap_sup, items, (int)cap_items, n_items);
+          n_sitems, (int)cap_sup, items, (int)cap_items, n_items, nsub);
       // the smem attribute is per device (set once per device, guarded across threads)
       static bool attr_set[RPD_MAX_DEVICES] = {};
       static std::mutex mu;
@@ -790,12 +848,12 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
           c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf,
           c->st.nbr_off.as<int32_t>(), c->st.planes.as<double4>(), items, n_items,
           (int)cap_items, cap, k_tet, slab, slab ? c->slab_m.as<uint2>() : nullptr, k_words,
-          c->stats.as<unsigned long long>());
+          c->stats.as<unsigned long long>(), nsub);
       c->launches += 3;
       c->bvh_cap_items = cap_items < cap_sup ? cap_items : cap_sup;
     }
     k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
-                                                        c->stats.as<unsigned long long>());
+                                                        c->stats.as<unsigned long long>(), nsub);
     ++c->launches;
     return cudaGetLastError();
   }
@@ -811,6 +869,7 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
                                  int32_t* slab, const int32_t* cand_off, int32_t* cand_idx,
                                  int32_t* pair_tet, const int32_t* w_off, int32_t* p_moff,
                                  int64_t n_pairs, unsigned* p_cut) {
+  const PDyn* pd = c->pdd;  // device-driven update: n, n_pairs are bounds (kernels read pd)
   if (n == 0) {
     if (p_moff) return cudaMemsetAsync(p_moff, 0, sizeof(int32_t), c->stream);
     return cudaSuccess;
@@ -824,11 +883,11 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
   k_compact_cands_t<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off,
                                                         cand_idx, pair_tet, w_off, p_moff,
                                                         c->st.nbr_off.as<int32_t>(), n_pairs,
-                                                        long_list, n_long, slab_m, p_cut);
+                                                        long_list, n_long, slab_m, p_cut, pd);
   // (grid for every list, exits on the device count: long lists are rare)
   k_compact_cands_w<<<(unsigned)c->sms * 4, 256, 0, c->stream>>>(
       long_list, n_long, n, cap, k_tet, slab, cand_off, cand_idx, pair_tet, w_off, p_moff,
-      c->st.nbr_off.as<int32_t>(), n_pairs, slab_m, p_cut);
+      c->st.nbr_off.as<int32_t>(), n_pairs, slab_m, p_cut, pd);
   c->launches += 2;
   return cudaGetLastError();
 }

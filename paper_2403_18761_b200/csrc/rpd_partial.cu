@@ -17,7 +17,12 @@ namespace rpd {
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 __global__ void k_check_new_ids(const int32_t* __restrict__ new_ids, int64_t M, int64_t N_old,
-                                int* err) {
+                                int* err, const PDyn* __restrict__ pd) {
+  if (pd) {  // device-driven update (grid sized for the largest M of the graph path)
+    new_ids = pd->new_ids;
+    M = pd->M;
+    N_old = pd->N_old;
+  }
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= M) return;
   if (new_ids[k] != N_old + k && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
@@ -37,8 +42,12 @@ __global__ void k_dirty_flag(int64_t T, const int32_t* __restrict__ count,
 __global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
                              const int32_t* __restrict__ scan, int32_t* __restrict__ list,
                              int32_t* __restrict__ pos, int32_t* __restrict__ cepoch,
-                             int* __restrict__ min_epoch, int epoch) {
+                             int* __restrict__ min_epoch, int epoch, PDyn* __restrict__ pd) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (pd) {  // device-driven update: the epoch from the device, the dirty count to it
+    epoch = pd->epoch;
+    if (t == T - 1) pd->nd = pd->nb = scan[t] + flag[t];
+  }
   int ep = 0x7fffffff;
   if (t < T) {
     if (flag[t]) {
@@ -57,7 +66,8 @@ __global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
 
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old) {
   if (M == 0) return cudaSuccess;
-  k_check_new_ids<<<nblk(M, 256), 256, 0, c->stream>>>(new_ids, M, N_old, c->errw.as<int>());
+  k_check_new_ids<<<nblk(M, 256), 256, 0, c->stream>>>(new_ids, M, N_old, c->errw.as<int>(),
+                                                       c->pdd);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -74,7 +84,8 @@ cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
   if (e) return e;
   k_dirty_list<<<nblk(T, 256), 256, 0, c->stream>>>(
       T, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), c->d_list.as<int32_t>(),
-      c->d_pos.as<int32_t>(), c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch);
+      c->d_pos.as<int32_t>(), c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch,
+      c->pdd);
   ++c->launches;
   return cudaGetLastError();
 }
@@ -110,17 +121,23 @@ __global__ void k_rows_update(int64_t nd, const int32_t* __restrict__ dirty,
                               const int32_t* __restrict__ inc_off,
                               const int32_t* __restrict__ rpf_off,
                               const int32_t* __restrict__ dc_off, const int32_t* __restrict__ dp_off,
-                              int cbase, int pbase, unsigned long long* __restrict__ rm) {
-  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                              int cbase, int pbase, unsigned long long* __restrict__ rm,
+                              const PDyn* __restrict__ pd) {
+  if (pd) {  // device-driven update: batch size and pool fill levels from the device
+    nd = pd->nb;
+    cbase = pd->fill_c;
+    pbase = pd->fill_p;
+  }
   unsigned long long v[4] = {0, 0, 0, 0};
-  if (a < nd) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nd; a += stride) {
     const int t = dirty[a];
     const int2 oc = crow[t], op = prow[t];
-    v[0] = oc.y - oc.x;
-    v[1] = op.y - op.x;
+    v[0] += oc.y - oc.x;
+    v[1] += op.y - op.x;
     if (op.y > op.x) {
-      v[2] = inc_off[op.y] - inc_off[op.x];
-      if (rpf_off) v[3] = rpf_off[op.y] - rpf_off[op.x];
+      v[2] += inc_off[op.y] - inc_off[op.x];
+      if (rpf_off) v[3] += rpf_off[op.y] - rpf_off[op.x];
     }
     crow[t] = make_int2(cbase + dc_off[a], cbase + dc_off[a + 1]);
     prow[t] = make_int2(pbase + dp_off[a], pbase + dp_off[a + 1]);
@@ -140,10 +157,83 @@ cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, Can
                                int64_t cbase, int64_t pbase, unsigned long long* rm) {
   cudaError_t e = cudaMemsetAsync(rm, 0, sizeof(unsigned long long) * 4, c->stream);
   if (e || nd == 0) return e;
-  k_rows_update<<<nblk(nd, 256), 256, 0, c->stream>>>(
+  unsigned grid = nblk(nd, 256);
+  if (c->pdd && grid > (unsigned)c->sms * 2) grid = c->sms * 2;  // (grid-stride over the bound)
+  k_rows_update<<<grid, 256, 0, c->stream>>>(
       nd, dirty, pool_c.rows.as<int2>(), pool_p.rows.as<int2>(), pool_p.inc_off.as<int32_t>(),
       c->euler ? pool_p.rpf_off.as<int32_t>() : nullptr, cd.off.as<int32_t>(),
-      pd.off.as<int32_t>(), (int)cbase, (int)pbase, rm);
+      pd.off.as<int32_t>(), (int)cbase, (int)pbase, rm, c->pdd);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- device-driven updates
+
+// the inputs of this update from the mapped pinned mirror; the outputs cleared
+__global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host) {
+  if (threadIdx.x != 0) return;
+  PDyn v = *host;
+  v.nd = v.nb = v.n_chg = v.nc = v.nw = v.np = v.ni = v.maxk = v.need = v.abort = 0;
+  *pd = v;
+}
+
+// after the batch's re-filter and scans: its candidate / mask-word totals, and the checks the
+// eager path makes on the host (slab capacity, work queues, batch bounds, pool room).  Any
+// failure aborts the rest of the graph (batch sizes set to 0) and the host redoes the batch
+__global__ void k_pd_check(PDyn* __restrict__ pd, const int32_t* __restrict__ c_off,
+                           const int32_t* __restrict__ w_off,
+                           const unsigned long long* __restrict__ stats,
+                           const int* __restrict__ queue, const int* __restrict__ err,
+                           int slab_cap) {
+  if (threadIdx.x != 0) return;
+  const int nb = pd->nb;
+  int nc = c_off[nb], nw = w_off[nb], ab = 0;
+  const int maxk = (int)stats[ST_MAXK];
+  if (maxk > slab_cap) ab |= PD_SLAB;
+  if (queue[0] > pd->cap_items || queue[1] > pd->cap_sup) ab |= PD_QUEUE;
+  if (nc > pd->nc_max || nw > pd->nw_max) ab |= PD_BATCH;
+  if ((long long)pd->fill_c + nc > pd->room_c || (long long)pd->fill_p + nc > pd->room_p ||
+      (long long)pd->fill_i + 32ll * nw > pd->room_i)
+    ab |= PD_POOL;
+  if (err[0] != 0) ab |= PD_ERR;
+  pd->maxk = maxk;
+  pd->need = max(queue[0], queue[1]);
+  if (ab) {
+    pd->abort = ab;
+    pd->nb = 0;
+    nc = nw = 0;
+  }
+  pd->nc = nc;
+  pd->nw = nw;
+}
+
+// the batch's piece / incidence totals; the whole record back to the mapped mirror
+__global__ void k_pd_final(PDyn* __restrict__ pd, PDyn* __restrict__ host,
+                           const int32_t* __restrict__ p_scan, const int32_t* __restrict__ i_scan) {
+  if (threadIdx.x != 0) return;
+  PDyn v = *pd;
+  v.np = p_scan[v.nc];
+  v.ni = i_scan[v.nc];
+  *host = v;
+  __threadfence_system();
+}
+
+cudaError_t launch_pd_init(rpd_ctx* c) {
+  k_pd_init<<<1, 32, 0, c->stream>>>(c->pdd, c->pd_hdev);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pd_check(rpd_ctx* c, const int32_t* c_off, const int32_t* w_off) {
+  k_pd_check<<<1, 32, 0, c->stream>>>(c->pdd, c_off, w_off, c->stats.as<unsigned long long>(),
+                                      c->bvh_items.as<int>(), c->errw.as<int>(), c->slab_cap);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pd_final(rpd_ctx* c) {
+  k_pd_final<<<1, 32, 0, c->stream>>>(c->pdd, c->pd_hdev, c->p_scan.as<int32_t>(),
+                                      c->i_scan.as<int32_t>());
   ++c->launches;
   return cudaGetLastError();
 }

@@ -66,13 +66,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanIO<T> io, int64_t n, 
                                                       unsigned long long* __restrict__ ticket,
                                                       unsigned long long ticket_base,
                                                       unsigned long long* state_base,
-                                                      unsigned epoch) {
+                                                      unsigned epoch, const int* n_dev) {
   __shared__ int sm[32];
   __shared__ int s_tile, s_prefix;
   if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ticket, 1ull) - ticket_base);
   __syncthreads();
   const int arr = s_tile / nb;
   const int tile = s_tile - arr * nb;
+  // device-driven length (nb tiles per array launched for a bound): the tiles beyond it leave
+  // at once (no successor waits on them: look-back only reads smaller tickets)
+  int nb_act = nb;
+  if (n_dev) {
+    n = *n_dev;
+    nb_act = n > 0 ? (int)((n + SCAN_TILE - 1) / SCAN_TILE) : 1;
+    if (tile >= nb_act) return;
+  }
   const T* __restrict__ in = io.in[arr];
   int* __restrict__ out = io.out[arr];
   unsigned long long* state = state_base + (int64_t)arr * nb;
@@ -126,19 +134,35 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(ScanIO<T> io, int64_t n, 
     if (base + k < n) out[base + k] = ex;
     ex += v[k];
   }
-  if (tile == nb - 1 && threadIdx.x == 0) out[n] = s_prefix + tot;
+  if (tile == nb_act - 1 && threadIdx.x == 0) out[n] = s_prefix + tot;
 }
 
+// n_dev (device-driven update): the length is read on the device; n is its bound.  Inside a
+// captured graph (c->pdd) the look-back state is a fresh region reset by a memset node (ticket
+// base 0, epoch 1), so that every replay starts clean.
 template <class T>
-static cudaError_t scan_impl(rpd_ctx* c, const ScanIO<T>& io, int K, int64_t n) {
-  if (n == 0) {
+static cudaError_t scan_impl(rpd_ctx* c, const ScanIO<T>& io, int K, int64_t n,
+                             const int* n_dev = nullptr) {
+  if (n == 0 && !n_dev) {
     for (int a = 0; a < K; ++a) {
       cudaError_t e = cudaMemsetAsync(io.out[a], 0, sizeof(int32_t), c->stream);
       if (e) return e;
     }
     return cudaSuccess;
   }
-  const int nb = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
+  const int nb = n > 0 ? (int)((n + SCAN_TILE - 1) / SCAN_TILE) : 1;
+  if (c->pdd) {
+    const size_t words = 1 + (size_t)K * nb;
+    if ((c->g_scan_used + words) * sizeof(unsigned long long) > c->g_scan.cap)
+      return cudaErrorInvalidValue;  // (the prologue sizes the region: a bug if reached)
+    unsigned long long* r = c->g_scan.as<unsigned long long>() + c->g_scan_used;
+    c->g_scan_used += words;
+    cudaError_t e = cudaMemsetAsync(r, 0, words * sizeof(unsigned long long), c->stream);
+    if (e) return e;
+    k_scan<T><<<nb * K, SCAN_THREADS, 0, c->stream>>>(io, n, nb, r, 0ull, r + 1, 1u, n_dev);
+    ++c->launches;
+    return cudaGetLastError();
+  }
   const size_t bytes = sizeof(unsigned long long) * ((size_t)K * nb + 1);
   if (bytes > c->scratch.cap || !c->scratch.p) {
     cudaError_t e = c->scratch.ensure(bytes);
@@ -151,27 +175,30 @@ static cudaError_t scan_impl(rpd_ctx* c, const ScanIO<T>& io, int K, int64_t n) 
   c->scan_epoch = (c->scan_epoch + 1) & ((1u << 30) - 1);
   if (c->scan_epoch == 0) c->scan_epoch = 1;
   k_scan<T><<<nb * K, SCAN_THREADS, 0, c->stream>>>(io, n, nb, ticket,
-                                                     c->scan_ticket, ticket + 1, c->scan_epoch);
+                                                     c->scan_ticket, ticket + 1, c->scan_epoch,
+                                                     n_dev);
   c->scan_ticket += (unsigned long long)nb * K;
   ++c->launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
-  return scan_impl<int32_t>(c, ScanIO<int32_t>{{in}, {out}}, 1, n);
+cudaError_t launch_scan_i32(rpd_ctx* c, const int32_t* in, int32_t* out, int64_t n,
+                            const int* n_dev) {
+  return scan_impl<int32_t>(c, ScanIO<int32_t>{{in}, {out}}, 1, n, n_dev);
 }
-cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n) {
-  return scan_impl<uint8_t>(c, ScanIO<uint8_t>{{in}, {out}}, 1, n);
+cudaError_t launch_scan_u8(rpd_ctx* c, const uint8_t* in, int32_t* out, int64_t n,
+                           const int* n_dev) {
+  return scan_impl<uint8_t>(c, ScanIO<uint8_t>{{in}, {out}}, 1, n, n_dev);
 }
 // K <= 5 equal-length int32 scans in[a] -> out[a] in one launch
 cudaError_t launch_scan_i32_multi(rpd_ctx* c, const int32_t* const* in, int32_t* const* out,
-                                  int K, int64_t n) {
+                                  int K, int64_t n, const int* n_dev) {
   ScanIO<int32_t> io{};
   for (int a = 0; a < K; ++a) {
     io.in[a] = in[a];
     io.out[a] = out[a];
   }
-  return scan_impl<int32_t>(c, io, K, n);
+  return scan_impl<int32_t>(c, io, K, n, n_dev);
 }
 
 }  // namespace rpd

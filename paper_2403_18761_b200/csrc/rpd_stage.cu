@@ -77,7 +77,12 @@ __global__ void k_stage_tets(const double* __restrict__ verts, int64_t V,
 // (rpd.h: new spheres are appended; their rows and planes are reused)
 __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
                                 double4* __restrict__ sw, const double4* __restrict__ old_sw,
-                                int64_t N_old, int* err) {
+                                int64_t N_old, int* err, const PDyn* __restrict__ pd) {
+  if (pd) {  // device-driven update: inputs and sizes from the device (grid sized by a bound)
+    spheres = pd->spheres;
+    N = pd->N;
+    N_old = pd->N_old;
+  }
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
   double S[4];
@@ -128,7 +133,15 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
                              unsigned long long* __restrict__ hkey, int32_t* __restrict__ repoch,
                              int epoch, unsigned long long* __restrict__ htab, OldRows old,
-                             int* err) {
+                             int* err, const PDyn* __restrict__ pd) {
+  if (pd) {  // device-driven update (see k_stage_spheres)
+    off_in = pd->nbr_off;
+    idx_in = pd->nbr_idx;
+    N = pd->N;
+    E = pd->E;
+    old.N = pd->N_old;
+    epoch = pd->epoch;
+  }
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / RG;
   const int lane = threadIdx.x & (RG - 1);
   const unsigned FULL = (RG == 32 ? 0xffffffffu : ((1u << RG) - 1u))
@@ -332,12 +345,11 @@ cudaError_t launch_stage_mesh(rpd_ctx* c, const double* verts, int64_t V, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
-                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
-                                 bool reuse_rows, int epoch) {
+// host part of a sphere staging: the previous rows become the "old" buffers (copied for
+// unchanged rows when reusing), the buffers are sized for N spheres / E entries
+cudaError_t stage_prepare(rpd_ctx* c, int64_t N, int64_t E) {
   Stage& s = c->st;
   cudaError_t e;
-  // the previous rows become the "old" buffers (copied for unchanged rows when reuse_rows)
   std::swap(s.nbr_off, s.old_off);
   std::swap(s.nbr_idx, s.old_idx);
   std::swap(s.planes, s.old_planes);
@@ -345,7 +357,7 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   std::swap(s.hkey, s.old_hkey);
   std::swap(s.repoch, s.old_repoch);
   std::swap(s.sw, s.old_sw);
-  const int64_t N_old = s.N;
+  s.N_prev = s.N;
   if ((e = s.sw.ensure(sizeof(double4) * (N > 0 ? N : 1)))) return e;
   if ((e = s.nbr_off.ensure(sizeof(int32_t) * (N + 1)))) return e;
   if ((e = s.nbr_idx.ensure(sizeof(int32_t) * (E > 0 ? E : 1)))) return e;
@@ -354,29 +366,49 @@ cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
   if ((e = s.repoch.ensure(sizeof(int32_t) * (N > 0 ? N : 1)))) return e;
   if ((e = s.htab.ensure(sizeof(unsigned long long) * 4 * (E > 0 ? E : 1)))) return e;
+  s.N = N;
+  s.E = E;
+  return cudaSuccess;
+}
+
+// the staging kernels (after stage_prepare).  Device-driven mode (c->pdd): inputs and sizes
+// come from the device, the grids cover the buffers' capacity
+cudaError_t stage_launch(rpd_ctx* c, const double* spheres, const int32_t* nbr_off,
+                         const int32_t* nbr_idx, bool reuse_rows, int epoch) {
+  Stage& s = c->st;
+  const int64_t N = s.N, E = s.E, N_old = s.N_prev;
+  const PDyn* pd = c->pdd;
   OldRows old{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   if (reuse_rows && s.old_off.p)
     old = OldRows{s.old_off.as<int32_t>(),  s.old_idx.as<int32_t>(),
                   s.old_planes.as<double4>(), s.old_twin.as<int32_t>(),
                   s.old_hkey.as<unsigned long long>(), s.old_repoch.as<int32_t>(), N_old};
-  s.N = N;
-  s.E = E;
   int* err = c->errw.as<int>();
+  const int64_t Ng = pd ? (int64_t)(s.sw.cap / sizeof(double4)) : N;  // grid rows
   if (N > 0) {
-    k_stage_spheres<<<nblk(N, 256), 256, 0, c->stream>>>(
-        spheres, N, s.sw.as<double4>(), old.off ? s.old_sw.as<double4>() : nullptr, N_old, err);
+    k_stage_spheres<<<nblk(Ng, 256), 256, 0, c->stream>>>(
+        spheres, N, s.sw.as<double4>(), old.off ? s.old_sw.as<double4>() : nullptr, N_old, err,
+        pd);
     ++c->launches;
-    k_stage_rows<STAGE_RG><<<nblk(STAGE_RG * N, 256), 256, 0, c->stream>>>(
+    k_stage_rows<STAGE_RG><<<nblk(STAGE_RG * Ng, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
         s.hkey.as<unsigned long long>(), s.repoch.as<int32_t>(), epoch,
-        s.htab.as<unsigned long long>(), old, err);
+        s.htab.as<unsigned long long>(), old, err, pd);
     ++c->launches;
   } else {
-    e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
+    cudaError_t e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
     if (e) return e;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_stage_spheres(rpd_ctx* c, const double* spheres, int64_t N,
+                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
+                                 bool reuse_rows, int epoch) {
+  cudaError_t e = stage_prepare(c, N, E);
+  if (e) return e;
+  return stage_launch(c, spheres, nbr_off, nbr_idx, reuse_rows, epoch);
 }
 
 }  // namespace rpd

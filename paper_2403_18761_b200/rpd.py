@@ -20,6 +20,7 @@ RPD_OK, RPD_EINVAL, RPD_ENOMEM, RPD_ECUDA, RPD_EOVERFLOW, RPD_ESTATE, RPD_ENOTEX
 STATUS_NAMES = {0: "RPD_OK", -1: "RPD_EINVAL", -2: "RPD_ENOMEM", -3: "RPD_ECUDA",
                 -4: "RPD_EOVERFLOW", -5: "RPD_ESTATE", -6: "RPD_ENOTEXACT"}
 OPT_FILTER_MODE, OPT_VALIDATE, OPT_STREAM, OPT_CLIP_WIDE, OPT_PROFILE = 1, 2, 3, 4, 5
+OPT_CLIP_TIERS, OPT_GRAPH = 6, 7
 FILTER_ALL_PAIRS, FILTER_PRUNED = 0, 1
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
@@ -110,7 +111,9 @@ class _Stats(C.Structure):
                 ("clip_vertex_tests", C.c_int64), ("clip_constructions", C.c_int64),
                 ("clip_fan_triangles", C.c_int64), ("filter_ms", C.c_double),
                 ("clip_ms", C.c_double), ("n_cand_dirty", C.c_int64),
-                ("n_pieces_dirty", C.c_int64), ("n_inc_dirty", C.c_int64)]
+                ("n_pieces_dirty", C.c_int64), ("n_inc_dirty", C.c_int64),
+                ("graph_updates", C.c_int64), ("graph_captures", C.c_int64),
+                ("graph_fallbacks", C.c_int64)]
 
 
 _lib = None
@@ -235,7 +238,11 @@ class RPDContext:
 
     def set_clip_tiers(self, on: bool):
         """Testing: the fast clip tier and its overflow cascade also for < 2048 pairs."""
-        self._check(self.L.rpd_set_option(self.h, 6, int(bool(on))))
+        self._check(self.L.rpd_set_option(self.h, OPT_CLIP_TIERS, int(bool(on))))
+
+    def set_graph(self, on: bool):
+        """Partial updates of 1..64 spheres as one device-driven CUDA graph (default on)."""
+        self._check(self.L.rpd_set_option(self.h, OPT_GRAPH, int(bool(on))))
 
     def set_profile(self, on: bool):
         """Time the filter and clip kernels with CUDA events (stats filter_ms / clip_ms)."""
