@@ -543,7 +543,8 @@ def main():
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    launches0 = ctx.stats()["kernel_launches"]
+    st0 = ctx.stats()
+    launches0 = st0["kernel_launches"]
     recs, times = [], []
     for s in range(args.steps):
         flush.zero_()
@@ -556,7 +557,12 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
-    launches = ctx.stats()["kernel_launches"] - launches0
+    st1 = ctx.stats()
+    launches = st1["kernel_launches"] - launches0
+    # partial updates replayed as CUDA graphs in the timed region (RPD_OPT_GRAPH): replays,
+    # captures (one per buffer layout; 0 once warm), eager redos of a batch
+    graphs = {k: int(st1["graph_" + k] - st0["graph_" + k])
+              for k in ("updates", "captures", "fallbacks")}
     clocks = sampler.stop()
     torch.cuda.synchronize()
     unpack(recs)
@@ -743,6 +749,7 @@ def main():
         "neighbors": nbr,
         "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches // max(args.steps, 1)),
+        "graph_updates": graphs,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)

@@ -163,6 +163,8 @@ rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream) {
   {
     const char* g = getenv("RPD_GRAPH");
     if (g && *g == '0') c->graph = 0;
+    const char* n = getenv("RPD_GRAPH_NC_MAX");  // testing: a fixed batch bound
+    if (n && *n) c->g_nc_fix = atoll(n);
   }
   *out = c;
   return RPD_OK;
@@ -223,6 +225,7 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (int k = 0; k < 4; ++k)
     if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1017,17 +1020,28 @@ static rpd_status partial_batch(rpd_ctx* c, int64_t nd, int64_t N_new, int64_t M
 // queues, pool room) are made on the device; a failed check idles the rest of the graph and
 // the host redoes the batch eagerly (partial_batch), so the results are the eager path's.
 
-#ifndef RPD_GRAPH_MAX_M
-#define RPD_GRAPH_MAX_M 64  // largest M that takes the graph path
+#ifndef RPD_GRAPH_NC_MIN
+#define RPD_GRAPH_NC_MIN (1 << 15)  // smallest batch-candidate bound of the graph's grids
 #endif
-#ifndef RPD_GRAPH_NC_MAX
-#define RPD_GRAPH_NC_MAX (1 << 15)  // batch-candidate bound of the graph's grids
+#ifndef RPD_GRAPH_QUEUE_MAX
+#define RPD_GRAPH_QUEUE_MAX (1 << 25)  // dirty-detection queue (worst case sized) limit, items
 #endif
 
+static inline int64_t pow2_at_least(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// new-sphere bound of a graph: M rounded up to a power of two (at least 64)
+static inline int64_t graph_mb(int64_t M) { return pow2_at_least(M < 64 ? 64 : M); }
+
 static bool graph_eligible(const rpd_ctx* c, int64_t M) {
-  return c->graph && M > 0 && M <= RPD_GRAPH_MAX_M && c->filter_mode == RPD_FILTER_PRUNED &&
-         !c->euler && !c->clip_wide && !c->clip_tiers && !c->profile && c->st.T > 0 &&
-         c->st.N > 0 && c->tr_on != 1;
+  // (the dirty detection's work queue is sized for its worst case: every (new sphere, leaf))
+  const int64_t n_leaf = (c->st.T + 31) / 32;
+  return c->graph && M > 0 && graph_mb(M) * (n_leaf + 1) <= RPD_GRAPH_QUEUE_MAX &&
+         c->filter_mode == RPD_FILTER_PRUNED && !c->euler && !c->clip_wide && !c->clip_tiers &&
+         c->st.T > 0 && c->st.N > 0 && c->tr_on != 1;
 }
 
 static inline int64_t tiles_of(int64_t n) { return n > 0 ? (n + 4095) / 4096 : 1; }
@@ -1042,12 +1056,17 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   if ((e = cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream)))
     return e;
   if ((e = launch_pd_init(c))) return e;
-  if ((e = launch_check_new_ids(c, nullptr, RPD_GRAPH_MAX_M, 0))) return e;
+  if ((e = launch_check_new_ids(c, nullptr, c->g_mb, 0))) return e;
   if ((e = stage_launch(c, nullptr, nullptr, nullptr, true, 0))) return e;
+  // (RPD_OPT_PROFILE: timer stamps around the filter and clip kernels, as the eager path's
+  // events)
+  auto mark = [&](int k) { return c->profile ? launch_pd_stamp(c, k) : cudaSuccess; };
   // (1) dirty tets: Alg. 1 of every tet against the new spheres only
-  if ((e = launch_filter(c, nullptr, T, 0, 0, RPD_GRAPH_MAX_M, c->d_count.as<int32_t>(),
+  if ((e = mark(0))) return e;
+  if ((e = launch_filter(c, nullptr, T, 0, 0, (int)c->g_mb, c->d_count.as<int32_t>(),
                          nullptr, nullptr)))
     return e;
+  if ((e = mark(1))) return e;
   if ((e = launch_dirty_list(c, T))) return e;
   if ((e = launch_changed_list(c, Nb))) return e;
   // (2) re-filter of the dirty tets over the changed rows; kept old candidates
@@ -1060,10 +1079,12 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   int32_t* k_words = c->k_words.as<int32_t>();
   int32_t* slab = c->slab.as<int32_t>();
   if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
+  if ((e = mark(2))) return e;
   if ((e = launch_filter(c, dl, T, cap, 0, (int)Nb, k_tet, slab, k_words, c->c_list.as<int32_t>(),
                          &pd->n_chg)))
     return e;
   if ((e = launch_keep_old(c, dl, T, pool_c, cap, k_tet, slab, k_words))) return e;
+  if ((e = mark(3))) return e;
   if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
   if ((e = launch_max_ktet(c, T, k_tet))) return e;
   {
@@ -1083,12 +1104,14 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   if ((e = cudaMemsetAsync(st + ST_EXACT, 0, sizeof(unsigned long long) * 5, c->stream))) return e;
   if ((e = cudaMemsetAsync(st + ST_CLIP_PLANES, 0, sizeof(unsigned long long) * 8, c->stream)))
     return e;
+  if ((e = mark(4))) return e;
   if ((e = launch_clip(c, nc_max, cd.pair_tet.as<int32_t>(), dl, pool_idx, cd.moff.as<int32_t>(),
                        cd.cut.as<unsigned>(), 0)))
     return e;
   if ((e = launch_clip_overflow(c, cd.pair_tet.as<int32_t>(), dl, pool_idx,
                                 cd.moff.as<int32_t>(), cd.cut.as<unsigned>())))
     return e;
+  if ((e = mark(5))) return e;
   if ((e = launch_piece_scans(c, nc_max, cd.moff.as<int32_t>()))) return e;
   PieceDst d{c->pcs_d.off.as<int32_t>(), pool_p.sphere.as<int32_t>(), pool_p.vol.as<double>(),
              pool_p.m1.as<double>(), pool_p.fm.as<uint8_t>(), pool_p.inc_off.as<int32_t>(),
@@ -1129,8 +1152,22 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
   CK(resolve(c, new_ids, M, c->h_new, &d_new), "stage new ids");
   // room at the pools' tails for a batch at the graph's bounds (a compaction, when the pools
   // are full, runs here -- before the new rows are staged, like every state read of the pools)
-  const int64_t nc_max = RPD_GRAPH_NC_MAX, nw_max = 4 * nc_max;
-  s = reserve_pools(c, nc_max, nc_max, 32 * nc_max, 0);  // (checked exactly on the device)
+  // the batch bound: twice the last batch (never shrinking: no recapture for smaller ones)
+  const int64_t nc_max =
+      c->g_nc_fix > 0 ? c->g_nc_fix
+                      : std::max(std::max<int64_t>(c->g_nc_max, RPD_GRAPH_NC_MIN),
+                                 pow2_at_least(2 * c->g_last_nc));
+  if (c->g_nc_fix <= 0) c->g_nc_max = nc_max;
+  const int64_t nw_max = 4 * nc_max;
+  const int64_t Mb = graph_mb(M);
+  c->g_mb = Mb;
+  // (the room is checked exactly on the device; the host reserves what the last batch needed
+  // plus a quarter, like the eager path's exact reservation; a shortfall redoes the batch)
+  {
+    const int64_t ec = std::max<int64_t>(4096, c->g_last_nc + c->g_last_nc / 4);
+    const int64_t ew = std::max<int64_t>(4096, c->g_last_nw + c->g_last_nw / 4);
+    s = reserve_pools(c, ec, ec, 32 * ew, 0);
+  }
   if (s) return s;
   c->rpe_n = -1;
   ++c->epoch;
@@ -1140,7 +1177,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
   const int64_t Nb = (int64_t)(c->st.sw.cap / sizeof(double4));
   const int64_t n_leaf = (T + 31) / 32, n_sup = (n_leaf + 31) / 32;
   {
-    const int64_t ci0 = RPD_GRAPH_MAX_M * n_leaf + 4096, cs0 = RPD_GRAPH_MAX_M * n_sup + 4096;
+    const int64_t ci0 = Mb * n_leaf + 4096, cs0 = Mb * n_sup + 4096;
     int64_t ci1 = std::max<int64_t>(48 * Nb + 4 * n_leaf + 4096, c->bvh_min_items);
     int64_t cs1 = std::max<int64_t>(8 * Nb + 4 * n_sup + 4096, c->bvh_min_items);
     ci1 = std::min<int64_t>(ci1, 1 << 30);
@@ -1212,13 +1249,33 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
   h.cap_items = (int)c->dd_cap[1][0];
   h.cap_sup = (int)c->dd_cap[1][1];
   // the graph of this buffer layout (captured on first use)
+  // the signature: every device address and every host value the captured launches bake in
   unsigned long long sig = 1469598103934665603ull;
-  for (unsigned long long v :
-       {(unsigned long long)g_alloc_gen.load(), (unsigned long long)(uintptr_t)c->st.sw.p,
-        (unsigned long long)(uintptr_t)c->st.old_sw.p, (unsigned long long)c->cur,
-        (unsigned long long)c->slab_cap, (unsigned long long)T,
-        (unsigned long long)c->bvh_min_items, (unsigned long long)c->sms})
-    sig = (sig ^ v) * 1099511628211ull;
+  auto mix = [&](unsigned long long v) { sig = (sig ^ v) * 1099511628211ull; };
+  {
+    const Stage& S = c->st;
+    const CandSet& cd = c->cand_d;
+    const DevBuf* bufs[] = {
+        &c->errw, &c->stats, &c->pd_buf, &S.tx, &S.sw, &S.old_sw, &S.nbr_off, &S.old_off,
+        &S.nbr_idx, &S.old_idx, &S.planes, &S.old_planes, &S.twin, &S.old_twin, &S.hkey,
+        &S.old_hkey, &S.repoch, &S.old_repoch, &S.htab, &c->bvh_all, &c->bvh, &c->bvh_items,
+        &c->d_count, &c->d_flag, &c->d_scan, &c->d_pos, &c->d_list, &c->cepoch, &c->min_epoch,
+        &c->c_flag, &c->c_scan, &c->c_list, &c->g_scan, &c->k_tet, &c->k_words, &c->slab,
+        &c->slab_m, &cd.off, &cd.pair_tet, &cd.moff, &cd.cut, &c->w_off, &c->cand_long,
+        &pool_c.rows, &pool_c.idx, &pool_p.rows, &pool_p.sphere, &pool_p.vol, &pool_p.m1,
+        &pool_p.fm, &pool_p.inc_off, &pool_p.inc, &c->pcs_d.off, &c->p_flag, &c->p_f01,
+        &c->p_fm, &c->p_vol, &c->p_m1, &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2,
+        &c->p_over3, &c->p_scan, &c->i_scan, &c->p_dyn, &c->m_cnt};
+    for (const DevBuf* b : bufs) mix((unsigned long long)(uintptr_t)b->p);
+    for (unsigned long long v :
+         {(unsigned long long)(S.sw.cap / sizeof(double4)), (unsigned long long)c->slab_cap,
+          (unsigned long long)T, (unsigned long long)c->dd_cap[0][0],
+          (unsigned long long)c->dd_cap[0][1], (unsigned long long)c->dd_cap[1][0],
+          (unsigned long long)c->dd_cap[1][1], (unsigned long long)c->sms,
+          (unsigned long long)nc_max, (unsigned long long)Mb, (unsigned long long)c->profile,
+          (unsigned long long)(uintptr_t)c->pinned_dev, (unsigned long long)(uintptr_t)c->pd_hdev})
+      mix(v);
+  }
   int slot = -1;
   for (int k = 0; k < rpd_ctx::G_CACHE; ++k)
     if (c->g_exec[k] && c->g_sig[k] == sig) slot = k;
@@ -1261,12 +1318,18 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
   CK(cudaStreamSynchronize(c->stream), "partial update");
   const PDyn r = *c->pd_host;
   const Readback* rb = (const Readback*)c->pinned;
+  if (c->profile) {
+    c->last.filter_ms += 1e-6 * (double)((r.stamp[1] - r.stamp[0]) + (r.stamp[3] - r.stamp[2]));
+    c->last.clip_ms += 1e-6 * (double)(r.stamp[5] - r.stamp[4]);
+  }
   if (rb->err[0] != 0) {
     if (rb->err[1] == 100) return fail(c, RPD_EINVAL, "new_ids is not the appended id range");
     return check_err(c, rb);
   }
   c->last.rel_tests += (int64_t)rb->u64[ST_REL_TESTS];
   c->last.pairs_tested += (int64_t)rb->u64[ST_TESTED];
+  c->g_last_nc = r.nc_req;
+  c->g_last_nw = r.nw_req;
   if (r.abort) {  // a device-side check failed: the batch again, eagerly (same results)
     ++c->g_fallbacks;
     return partial_batch(c, r.nd, N_new, M, out, dirty_tets, n_dirty);

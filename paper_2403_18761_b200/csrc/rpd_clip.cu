@@ -49,9 +49,6 @@
 #ifndef RPD_CLIP_MID_VPL
 #define RPD_CLIP_MID_VPL 2  // vertex slots per lane of the middle (first overflow) tier, GW = 32
 #endif
-#ifndef RPD_CLIP_SMALL
-#define RPD_CLIP_SMALL 2048  // below this many pairs the 64-slot tier clips all pairs directly
-#endif
 #ifndef RPD_CLIP_MID32
 #define RPD_CLIP_MID32 0    // 1: a 32-slot tier (GW = 32, one slot per lane) before the middle one (measured slower)
 #endif
@@ -1402,12 +1399,21 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
   c->clip_small = 0;
   if (n_pairs == 0) return cudaSuccess;
   if (c->pdd) {
-    // device-driven update (few insertions): the 64-slot tier on every pair, n_pairs is the
-    // bound of the grid, the count is read on the device
-    c->clip_small = 1;
-    return launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                      cand_idx, moff, cut,
-                                                      c->p_over2.as<int32_t>(), &c->pdd->nc);
+    // device-driven update: n_pairs is the grids' bound; the count is read on the device by
+    // both entry tiers, and only the one the eager path would choose gets it (nc_fast /
+    // nc_small, the other sees 0).  The fast tier's overflows go down the usual cascade.
+    cudaError_t e = c->p_dyn.ensure(sizeof(int));
+    if (e) return e;
+    if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
+    e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                        cand_idx, moff, cut,
+                                                        c->p_over.as<int32_t>(),
+                                                        &c->pdd->nc_fast, c->p_dyn.as<int>());
+    if (e) return e;
+    return launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs < RPD_CLIP_SMALL ? n_pairs : RPD_CLIP_SMALL,
+                                                      nullptr, pair_tet, tet_ids, cand_idx, moff,
+                                                      cut, c->p_over2.as<int32_t>(),
+                                                      &c->pdd->nc_small);
   }
   if (!wide && n_pairs < RPD_CLIP_SMALL && !c->clip_tiers) {
     // few pairs (small partial updates): latency, not throughput -- one pass of the 64-slot

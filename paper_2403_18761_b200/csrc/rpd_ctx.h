@@ -3,7 +3,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <atomic>
 #include <string>
 
 #include "../../include/rpd.h"
@@ -11,10 +10,6 @@
 #define RPD_MAX_DEVICES 64
 
 namespace rpd {
-
-// Every (re)allocation of a DevBuf bumps this generation: captured CUDA graphs bake device
-// addresses, so a cached graph is valid only while no buffer moved (rpd_graph.cu).
-inline std::atomic<unsigned long long> g_alloc_gen{0};
 
 // Growable ctx-owned device buffer.
 struct DevBuf {
@@ -28,7 +23,6 @@ struct DevBuf {
     size_t want = bytes < 256 ? 256 : bytes + bytes / 8;
     cudaError_t e = cudaMalloc(&p, want);
     if (e == cudaSuccess) cap = want;
-    g_alloc_gen.fetch_add(1);
     return e;
   }
   // like ensure, but a (re)allocation reserves `factor` x bytes (pools that grow by appends)
@@ -137,6 +131,10 @@ struct PieceSet {
   int64_t n_tets = 0, n_pieces = 0, n_inc = 0, n_rpf = 0;  // live counts
   int64_t fill_p = 0, fill_i = 0, fill_r = 0;              // state: pool slots in use
 };
+#ifndef RPD_CLIP_SMALL
+#define RPD_CLIP_SMALL 2048  // below this many pairs the 64-slot tier clips all pairs directly
+#endif
+
 // Sizes of a device-driven partial update (the CUDA-graph latency path, rpd_graph.cu): the
 // host writes the inputs part once per update; every size the eager path reads back to the
 // host between its launches is produced and consumed on the device here instead.
@@ -157,9 +155,12 @@ struct PDyn {
   int nb;      // tets of the batch: nd, or 0 once aborted (the rest of the graph idles)
   int n_chg;   // spheres whose rows changed since the dirty tets' candidate lists
   int nc, nw;  // batch candidates and incidence-mask words (0 once aborted)
+  int nc_fast, nc_small;  // nc for the clip tier that takes the batch (the other gets 0)
+  int nc_req, nw_req;  // the batch's candidates / mask words also when aborted (next sizes)
   int np, ni;  // batch pieces and incidences
   int maxk, need;  // largest k_tet, work-queue demand of the re-filter
   int abort;   // PdAbort bits: the eager path redoes the batch (re-filter onwards)
+  unsigned long long stamp[6];  // RPD_OPT_PROFILE: %globaltimer around filter / re-filter / clip
 };
 
 }  // namespace rpd
@@ -241,6 +242,10 @@ struct rpd_ctx {
   int graph = 1;                // RPD_OPT_GRAPH (env RPD_GRAPH=0 turns it off)
   int64_t g_launches = 0, g_captures = 0, g_fallbacks = 0;
   int64_t dd_cap[2][2] = {};    // BVH queue capacities {items, super items}: dirty, re-filter
+  int64_t g_mb = 64;            // new-sphere bound of the current graph (grid of the id check)
+  int64_t g_nc_max = 0;         // batch-candidate bound of the graphs (grows, never shrinks)
+  int64_t g_nc_fix = 0;         // env RPD_GRAPH_NC_MAX: a fixed bound (tests of the fallback)
+  int64_t g_last_nc = 0, g_last_nw = 0;  // candidates / mask words of the last batch
 
   rpd_stats last{};
   int profile = 0;             // record CUDA events around the filter and clip kernels
@@ -379,6 +384,7 @@ cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, Can
 cudaError_t launch_pd_init(rpd_ctx* c);
 cudaError_t launch_pd_check(rpd_ctx* c, const int32_t* c_off, const int32_t* w_off);
 cudaError_t launch_pd_final(rpd_ctx* c);
+cudaError_t launch_pd_stamp(rpd_ctx* c, int k);
 // compaction of the state pools (by rows) into the plain CSRs cn / pn (pair_tet and moff of
 // the candidates rebuilt); phase 0: counts + scans, phase 1: copies
 cudaError_t launch_compact_state(rpd_ctx* c, int64_t T, const CandSet& co, const PieceSet& po,

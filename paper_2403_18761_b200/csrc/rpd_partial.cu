@@ -174,6 +174,8 @@ __global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host) 
   if (threadIdx.x != 0) return;
   PDyn v = *host;
   v.nd = v.nb = v.n_chg = v.nc = v.nw = v.np = v.ni = v.maxk = v.need = v.abort = 0;
+  v.nc_fast = v.nc_small = v.nc_req = v.nw_req = 0;
+  for (int k = 0; k < 6; ++k) v.stamp[k] = 0;
   *pd = v;
 }
 
@@ -198,6 +200,8 @@ __global__ void k_pd_check(PDyn* __restrict__ pd, const int32_t* __restrict__ c_
   if (err[0] != 0) ab |= PD_ERR;
   pd->maxk = maxk;
   pd->need = max(queue[0], queue[1]);
+  pd->nc_req = nc;
+  pd->nw_req = nw;
   if (ab) {
     pd->abort = ab;
     pd->nb = 0;
@@ -205,6 +209,10 @@ __global__ void k_pd_check(PDyn* __restrict__ pd, const int32_t* __restrict__ c_
   }
   pd->nc = nc;
   pd->nw = nw;
+  // the tier that takes the batch: few pairs go straight to the 64-slot tier (latency), more
+  // to the fast tier and its overflow cascade (the eager launch_clip's choice)
+  pd->nc_small = nc < RPD_CLIP_SMALL ? nc : 0;
+  pd->nc_fast = nc < RPD_CLIP_SMALL ? 0 : nc;
 }
 
 // the batch's piece / incidence totals; the whole record back to the mapped mirror
@@ -216,6 +224,19 @@ __global__ void k_pd_final(PDyn* __restrict__ pd, PDyn* __restrict__ host,
   v.ni = i_scan[v.nc];
   *host = v;
   __threadfence_system();
+}
+
+// profiling marks inside a graph (event timing of captured event records is not relied on)
+__global__ void k_pd_stamp(PDyn* __restrict__ pd, int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) pd->stamp[k] = t;
+}
+
+cudaError_t launch_pd_stamp(rpd_ctx* c, int k) {
+  k_pd_stamp<<<1, 32, 0, c->stream>>>(c->pdd, k);
+  ++c->launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pd_init(rpd_ctx* c) {
