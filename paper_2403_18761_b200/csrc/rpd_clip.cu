@@ -1357,6 +1357,9 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   int64_t want = (n + GROUPS - 1) / GROUPS;
   int64_t grid = (int64_t)sms * occ;
   if (want < grid) grid = want;
+  // the 128- and 256-slot tiers over an overflow list (a handful of pairs, often none; the
+  // count is read on the device): one block per SM, so an empty launch costs little
+  if (pair_list && VPL >= 4 && grid > sms) grid = sms;
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff, cut,

@@ -371,6 +371,9 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
 // partial update (rpd_partial.cu)
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old);
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T);
+// fused scans (rpd_scan.cu): dirty tets (list, positions, epochs) and changed-row spheres
+cudaError_t launch_dirty_scan(rpd_ctx* c, int64_t T);
+cudaError_t launch_changed_scan(rpd_ctx* c, int64_t N);
 // state rows from the compact CSRs (cand and / or piece; NULL skips)
 cudaError_t launch_rows_from_off(rpd_ctx* c, int64_t T, const CandSet* cs, PieceSet* ps,
                                  CandSet* cs_rows);

@@ -723,23 +723,6 @@ cudaError_t launch_keep_old(rpd_ctx* c, const int32_t* dirty, int64_t n_dirty,
   return cudaGetLastError();
 }
 
-__global__ void k_chg_flags(int64_t N, const int32_t* __restrict__ repoch,
-                            const int* __restrict__ min_epoch, uint8_t* __restrict__ flag,
-                            const PDyn* __restrict__ pd) {
-  if (pd) N = pd->N;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N) flag[i] = repoch[i] > *min_epoch;
-}
-
-__global__ void k_chg_list(int64_t N, const uint8_t* __restrict__ flag,
-                           const int32_t* __restrict__ scan, int32_t* __restrict__ list,
-                           PDyn* __restrict__ pd) {
-  if (pd) N = pd->N;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < N && flag[i]) list[scan[i]] = (int32_t)i;
-  if (pd && i == N - 1) pd->n_chg = scan[i] + flag[i];
-}
-
 // list of the spheres whose rows changed (count at c_scan[N])
 cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet) {
   if (n == 0) return cudaSuccess;
@@ -750,22 +733,9 @@ cudaError_t launch_max_ktet(rpd_ctx* c, int64_t n, const int32_t* k_tet) {
 }
 
 cudaError_t launch_changed_list(rpd_ctx* c, int64_t N) {
-  // (device-driven update: N is the grids' bound, the count comes from the device)
-  PDyn* pd = c->pdd;
-  if (N > 0) {
-    k_chg_flags<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->st.repoch.as<int32_t>(),
-                                                     c->min_epoch.as<int>(),
-                                                     c->c_flag.as<uint8_t>(), pd);
-    ++c->launches;
-  }
-  cudaError_t e = launch_scan_u8(c, c->c_flag.as<uint8_t>(), c->c_scan.as<int32_t>(), N,
-                                 pd ? &pd->N : nullptr);
-  if (e || N == 0) return e;
-  k_chg_list<<<nblk(N, 256), 256, 0, c->stream>>>(N, c->c_flag.as<uint8_t>(),
-                                                  c->c_scan.as<int32_t>(),
-                                                  c->c_list.as<int32_t>(), pd);
-  ++c->launches;
-  return cudaGetLastError();
+  // (device-driven update: N is the grid's bound, the count comes from the device)
+  if (N == 0) return cudaMemsetAsync(c->c_scan.p, 0, sizeof(int32_t), c->stream);
+  return launch_changed_scan(c, N);
 }
 
 cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, int cap,
@@ -852,9 +822,11 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       c->launches += 3;
       c->bvh_cap_items = cap_items < cap_sup ? cap_items : cap_sup;
     }
-    k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
-                                                        c->stats.as<unsigned long long>(), nsub);
-    ++c->launches;
+    if (slab) {  // (the count-only dirty detection needs no maximum)
+      k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
+                                                          c->stats.as<unsigned long long>(), nsub);
+      ++c->launches;
+    }
     return cudaGetLastError();
   }
   k_filter_allpairs<<<nblk(n_tets, 256), 256, 0, c->stream>>>(

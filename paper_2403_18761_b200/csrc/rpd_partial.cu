@@ -31,39 +31,6 @@ __global__ void k_check_new_ids(const int32_t* __restrict__ new_ids, int64_t M, 
   }
 }
 
-__global__ void k_dirty_flag(int64_t T, const int32_t* __restrict__ count,
-                             uint8_t* __restrict__ flag) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < T) flag[t] = count[t] > 0;
-}
-
-// dirty list + position map; the oldest candidate-list epoch among the dirty tets, whose
-// lists are re-stamped with the current epoch
-__global__ void k_dirty_list(int64_t T, const uint8_t* __restrict__ flag,
-                             const int32_t* __restrict__ scan, int32_t* __restrict__ list,
-                             int32_t* __restrict__ pos, int32_t* __restrict__ cepoch,
-                             int* __restrict__ min_epoch, int epoch, PDyn* __restrict__ pd) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (pd) {  // device-driven update: the epoch from the device, the dirty count to it
-    epoch = pd->epoch;
-    if (t == T - 1) pd->nd = pd->nb = scan[t] + flag[t];
-  }
-  int ep = 0x7fffffff;
-  if (t < T) {
-    if (flag[t]) {
-      list[scan[t]] = (int32_t)t;
-      pos[t] = scan[t];
-      ep = cepoch[t];
-      cepoch[t] = epoch;
-    } else {
-      pos[t] = -1;
-    }
-  }
-  // one atomic per warp (per-tet atomics on one address serialise in L2)
-  ep = __reduce_min_sync(0xffffffffu, ep);
-  if ((threadIdx.x & 31) == 0 && ep != 0x7fffffff) atomicMin(min_epoch, ep);
-}
-
 cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, int64_t N_old) {
   if (M == 0) return cudaSuccess;
   k_check_new_ids<<<nblk(M, 256), 256, 0, c->stream>>>(new_ids, M, N_old, c->errw.as<int>(),
@@ -72,22 +39,13 @@ cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, 
   return cudaGetLastError();
 }
 
-// d_count (filter counts over the new spheres) -> d_flag -> d_scan -> d_list, d_pos
+// d_count (filter counts over the new spheres) -> d_list, d_pos, d_scan[T] = count, cepoch
+// re-stamped, min_epoch: one fused scan (rpd_scan.cu)
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
   if (T == 0) return cudaMemsetAsync(c->d_scan.p, 0, sizeof(int32_t), c->stream);
-  k_dirty_flag<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_count.as<int32_t>(),
-                                                    c->d_flag.as<uint8_t>());
-  ++c->launches;
-  cudaError_t e = launch_scan_u8(c, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), T);
+  cudaError_t e = cudaMemsetAsync(c->min_epoch.p, 0x7f, sizeof(int), c->stream);
   if (e) return e;
-  e = cudaMemsetAsync(c->min_epoch.p, 0x7f, sizeof(int), c->stream);
-  if (e) return e;
-  k_dirty_list<<<nblk(T, 256), 256, 0, c->stream>>>(
-      T, c->d_flag.as<uint8_t>(), c->d_scan.as<int32_t>(), c->d_list.as<int32_t>(),
-      c->d_pos.as<int32_t>(), c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch,
-      c->pdd);
-  ++c->launches;
-  return cudaGetLastError();
+  return launch_dirty_scan(c, T);
 }
 
 // ---------------------------------------------------------------- state pools

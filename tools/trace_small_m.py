@@ -1,8 +1,10 @@
 """Host/stream timeline of few-insertion partial updates (M = 1 / 10 from the C3 start,
-bench.py side_small_m's workload; development aid): RPD_TRACE_HOST marks per update, and the
+bench.py side_small_m's workload; development aid): RPD_TRACE_HOST marks per update (argument
+"trace"; eager path only), and the
 per-update device time by CUDA events.  Under ncu, torch fill kernels separate the updates."""
 import sys, os
-os.environ.setdefault("RPD_TRACE_HOST", "1")
+if "trace" in sys.argv[3:]:
+    os.environ["RPD_TRACE_HOST"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2403_18761_b200 as P
