@@ -411,14 +411,34 @@ def side_neighbors(args, ctx, w, flush, d_verts, d_tets, d_base):
 
     t_gpu, np_gpu, ni_gpu = full_rpd(g["nbr_off"], g["nbr_idx"])
     t_rt, np_rt, ni_rt = full_rpd(d_base[1], d_base[2])
+    # incremental lists along the C4 batches (rpd_neighbors_update: only the rows a batch can
+    # change are recomputed; reading R34)
+    inc_ms, inc_rows = [], []
+    if w.batches:
+        dev = d_verts.device
+        ctx.neighbors(d_base[0], box, device=True)
+        n_prev = w.N
+        for (sph, _, _) in w.batches:
+            d_sph = torch.as_tensor(np.ascontiguousarray(sph)).to(dev)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            u = ctx.neighbors_update(d_sph, len(sph) - n_prev, box, device=True)
+            torch.cuda.synchronize()
+            inc_ms.append(1e3 * (time.perf_counter() - t0))
+            inc_rows.append(int(u["n_rows"]))
+            n_prev = len(sph)
     nbr = {"ms": float(np.median(nb_ms)), "E": int(g["nbr_idx"].numel()),
+           "update_ms_per_batch": float(np.median(inc_ms)) if inc_ms else None,
+           "update_rows_per_batch": float(np.median(inc_rows)) if inc_rows else None,
            "E_regular_triangulation": int(len(w.nbr_idx)),
            "hidden": int(g["n_hidden"]), "vertex_overflow": int(g["n_vertex_overflow"]),
            "full_rpd_ms_gpu_lists": float(t_gpu), "full_rpd_ms_rt_lists": float(t_rt),
            "pieces_equal_counts": bool(np_gpu == np_rt and ni_gpu == ni_rt),
            "note": "NEXT-3 rpd_neighbors (host-timed around the call, two syncs): certified "
                    "superset of the mesh-box power-cell neighbours; full RPD = relations + "
-                   "clip (CUDA events, L2 flushed) with the GPU lists vs the Qhull lists"}
+                   "clip (CUDA events, L2 flushed) with the GPU lists vs the Qhull lists; "
+                   "update_*: rpd_neighbors_update after each C4 batch (host-timed), median "
+                   "time and rows recomputed"}
     return nbr
 
 
@@ -436,8 +456,16 @@ def side_small_m(args, ctx, w, d_verts, d_tets, to_dev):
         ctx.relations(d_verts, d_tets, to_dev(ws.spheres), to_dev(ws.nbr_off),
                       to_dev(ws.nbr_idx))
         ctx.clip()
-        n_prev, lat = ws.N, []
+        n_prev, lat, nb_lat = ws.N, [], []
+        box = W.mesh_box(ws.verts)
+        ctx.neighbors(to_dev(ws.spheres), box, device=True)
         for b, (sph, off, idx) in enumerate(ws.batches):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            u = ctx.neighbors_update(to_dev(sph), len(sph) - n_prev, box, device=True)
+            torch.cuda.synchronize()
+            if b > 0:
+                nb_lat.append((1e3 * (time.perf_counter() - t0), int(u["n_rows"])))
             args_b = (to_dev(sph), to_dev(off), to_dev(idx),
                       to_dev(np.arange(n_prev, len(sph), dtype=np.int32)))
             n_prev = len(sph)
@@ -451,7 +479,9 @@ def side_small_m(args, ctx, w, d_verts, d_tets, to_dev):
                 lat.append((ev0.elapsed_time(ev1), nd))
         small[f"M{M}"] = {"partial_ms": float(np.median([x[0] for x in lat])),
                           "dirty_tets": float(np.median([x[1] for x in lat])),
-                          "updates": len(lat)}
+                          "updates": len(lat),
+                          "neighbors_update_ms": float(np.median([x[0] for x in nb_lat])),
+                          "neighbors_rows": float(np.median([x[1] for x in nb_lat]))}
     return small
 
 

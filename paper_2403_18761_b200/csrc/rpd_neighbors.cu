@@ -244,6 +244,8 @@ struct NbArgs {
   int* err;
   const int32_t* order;   // work order (pass 1)
   int32_t* work;          // work counter (pass 1)
+  int64_t n_work;         // pass 1 rows: order[0, n_work) (0: all N) ...
+  const int32_t* n_work_dev;  // ... or a device count (incremental update)
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
   int32_t* hits;   // [warp slots][NB_HCAP] positions (cell-sorted arrays) of a round's hits
 };
@@ -783,11 +785,12 @@ __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
     return;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwork = A.n_work_dev ? *A.n_work_dev : (A.n_work > 0 ? A.n_work : A.N);
   for (;;) {
     int q = 0;
     if (lane == 0) q = atomicAdd(A.work, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= A.N) break;
+    if (q >= nwork) break;
     nb_row<false>(A, sm[w], A.order[q], lane,
                   A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
   }
@@ -827,9 +830,10 @@ size_t nb_grid_cells(int64_t N) {
   return (size_t)G * G * G;
 }
 
-// Pass 1 and the scan; *E_dev = total entries (off[N]).  Buffers in c->nb_buf.
-cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
-                                   int32_t* cnt, int32_t* off) {
+// The uniform grid of the spheres, their cell-ordered copy and the radius work order; the
+// pass arguments in *A and the pass-1 grid size in *mb.  Buffers in c->nb_buf.
+static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                            int32_t* cnt, NbArgs* Ap, int* mbp) {
   int G = 1;
   while ((int64_t)G * G * G * 2 < N && G < NB_GMAX) ++G;
   const int64_t ncell = (int64_t)G * G * G;
@@ -923,6 +927,20 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   const size_t slots = (size_t)std::max(mb, 2 * c->sms) * NB_WARPS;
   if ((e = c->nb_hits.ensure(sizeof(int32_t) * NB_HCAP * slots))) return e;
   A.hits = c->nb_hits.as<int32_t>();
+  c->nb_work = A.work;
+  c->nb_order = order;
+  *Ap = A;
+  *mbp = mb;
+  return cudaGetLastError();
+}
+
+// Pass 1 and the scan; *E_dev = total entries (off[N]).
+cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                                   int32_t* cnt, int32_t* off) {
+  NbArgs A{};
+  int mb = 0;
+  cudaError_t e = nb_build(c, sph, N, box, cnt, &A, &mb);
+  if (e) return e;
   k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
   if ((e = cudaGetLastError())) return e;
@@ -956,6 +974,274 @@ cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, con
   ++c->launches;
   const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
   k_nb_sort<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, off, c->nb_slab, tmp, idx);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- incremental update
+//
+// After M spheres are appended (DESIGN.md §10 "Sphere neighbours", reading R34), the
+// box-restricted cell of an old sphere i changes only if new cells take volume from it.  Then
+// either i's new cell shares a facet with a new sphere j -- i is in j's (superset) row -- or
+// i's cell is swallowed (empty within B); a swallowed cell's region is covered by new cells,
+// so its old neighbours that survive border a new cell and are in a new row.  Recomputed:
+//   R1: the old spheres listed in the new spheres' rows (and old spheres a new one hides);
+//   R2: the old neighbours (old rows) of R1 -- where a swallowed cell can be;
+//   then, round by round, the old neighbours of every recomputed row that came out empty
+//   (swallowed clusters), until none is left.
+// Every other old row is kept: its cell, hence its certified superset, is unchanged.  Flags
+// of the old spheres: 0 kept, 1 recomputed, 2 (R2) / 3 (next round) to be recomputed.
+
+static __global__ void k_nb_iota(int32_t* __restrict__ list, int64_t base, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    list[k] = (int32_t)(base + k);
+}
+
+// the old spheres [0, N_old) must be the previous call's (the update appends)
+static __global__ void k_nb_same(const double* __restrict__ sph, const double* __restrict__ prev,
+                                 int64_t n4, int* __restrict__ err) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4;
+       k += (int64_t)gridDim.x * blockDim.x)
+    if (!(sph[k] == prev[k]) && atomicCAS(&err[0], 0, (int)RPD_EINVAL) == 0) {
+      err[1] = ERR_SPHERE_CHANGED;
+      err[2] = (int)(k / 4);
+    }
+}
+
+// warp per new sphere j: R1 = the old spheres of its row and the old ones with its centre.
+// misc[1] |= 1: a new row longer than the pass-1 slab; misc[3]: new non-empty rows; misc[5]:
+// R1 flags set (both only tested against 0)
+static __global__ void k_nb_mark(int64_t N_old, int64_t N, const int32_t* __restrict__ cnt,
+                                 const int32_t* __restrict__ slab, const double* __restrict__ sph,
+                                 const NbGrid* __restrict__ gp, const int32_t* __restrict__ start,
+                                 const int32_t* __restrict__ items, uint8_t* __restrict__ flag,
+                                 int* __restrict__ misc) {
+  const int lane = threadIdx.x & 31;
+  const NbGrid g = *gp;
+  for (int64_t j = N_old + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); j < N;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int n = cnt[j];
+    if (n > NB_CAP1) {
+      if (lane == 0) atomicOr(&misc[1], 1);
+      continue;
+    }
+    if (n > 0 && lane == 0) atomicAdd(&misc[3], 1);
+    int set = 0;
+    for (int s = lane; s < n; s += 32) {
+      const int i = slab[j * NB_CAP1 + s];
+      if (i < N_old) {
+        flag[i] = 1;
+        set = 1;
+      }
+    }
+    const double x = sph[4 * j], y = sph[4 * j + 1], z = sph[4 * j + 2];
+    const int c = (nb_cell_axis(z, g, 2) * g.G + nb_cell_axis(y, g, 1)) * g.G + nb_cell_axis(x, g, 0);
+    for (int p = start[c] + lane; p < start[c + 1]; p += 32) {
+      const int k = items[p];
+      if (k < N_old && sph[4 * k] == x && sph[4 * k + 1] == y && sph[4 * k + 2] == z) {
+        flag[k] = 1;
+        set = 1;
+      }
+    }
+    if (__any_sync(0xffffffffu, set) && lane == 0) atomicAdd(&misc[5], 1);
+  }
+}
+
+// R2: warp per old sphere of R1 (flag 1): its old neighbours not yet flagged get flag 2
+static __global__ void k_nb_expand(int64_t N_old, const int32_t* __restrict__ old_off,
+                                   const int32_t* __restrict__ old_idx, uint8_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N_old;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (flag[i] != 1) continue;
+    for (int e = old_off[i] + lane; e < old_off[i + 1]; e += 32) {
+      const int k = old_idx[e];
+      if (k < N_old && flag[k] == 0) flag[k] = 2;
+    }
+  }
+}
+
+// after a round of rows list[0, *n): they are recomputed (flag 1); a row that came out empty
+// while its old row was not (a swallowed cell) puts its unflagged old neighbours in the next
+// round (flag 3, misc[2] > 0)
+static __global__ void k_nb_swallow(const int32_t* __restrict__ list, const int* __restrict__ n,
+                                    int64_t N_old, const int32_t* __restrict__ cnt,
+                                    const int32_t* __restrict__ old_off,
+                                    const int32_t* __restrict__ old_idx,
+                                    uint8_t* __restrict__ flag, int* __restrict__ misc) {
+  const int lane = threadIdx.x & 31;
+  const int nn = *n;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < nn;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int i = list[q];
+    if (lane == 0) flag[i] = 1;
+    if (cnt[i] != 0 || old_off[i + 1] == old_off[i]) continue;
+    int added = 0;
+    for (int e = old_off[i] + lane; e < old_off[i + 1]; e += 32) {
+      const int k = old_idx[e];
+      if (k < N_old && flag[k] == 0) {
+        flag[k] = 3;
+        added = 1;
+      }
+    }
+    if (__any_sync(0xffffffffu, added) && lane == 0) atomicAdd(&misc[2], 1);
+  }
+}
+
+// row lengths of the merged lists: recomputed rows from pass 1, kept rows from the old CSR
+static __global__ void k_nb_len(int64_t N, int64_t N_old, const int32_t* __restrict__ cnt,
+                                const uint8_t* __restrict__ flag,
+                                const int32_t* __restrict__ old_off, int32_t* __restrict__ len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    len[i] = (i >= N_old || flag[i]) ? cnt[i] : old_off[i + 1] - old_off[i];
+}
+
+// warp per row: recomputed rows rank-sorted from the slab / pass-2 rows, kept rows copied
+static __global__ void k_nb_merge(int64_t N, int64_t N_old, const uint8_t* __restrict__ flag,
+                                  const int32_t* __restrict__ old_off,
+                                  const int32_t* __restrict__ old_idx,
+                                  const int32_t* __restrict__ off, const int32_t* __restrict__ slab,
+                                  const int32_t* __restrict__ tmp, int32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int a = off[i], n = off[i + 1] - a;
+    if (i < N_old && !flag[i]) {
+      const int o = old_off[i];
+      for (int s = lane; s < n; s += 32) idx[a + s] = old_idx[o + s];
+      continue;
+    }
+    const int32_t* src = n <= NB_CAP1 ? slab + i * NB_CAP1 : tmp + a;
+    for (int s = lane; s < n; s += 32) {
+      const int v = src[s];
+      int rk = 0;
+      for (int t = 0; t < n; ++t) rk += src[t] < v;
+      idx[a + rk] = v;
+    }
+  }
+}
+
+// the pass-1 arguments of the current grid (nb_build's), for a row list with a device count
+static NbArgs nb_args_list(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
+                           int32_t* cnt, const int32_t* list, const int* n_dev) {
+  NbArgs A{};
+  A.sph = sph;
+  A.N = N;
+  A.grid = reinterpret_cast<const NbGrid*>(c->nb_grid);
+  A.start = c->nb_start;
+  A.items = c->nb_items;
+  A.sorted = reinterpret_cast<const double4*>(c->nb_sorted);
+  for (int k = 0; k < 3; ++k) {
+    A.blo[k] = box[k];
+    A.bhi[k] = box[3 + k];
+  }
+  A.tol0 = c->nb_args_tol0;
+  A.cnt = cnt;
+  A.slab = c->nb_slab;
+  A.n_long = c->nb_long;
+  A.long_ids = c->nb_long_ids;
+  A.stats = c->nb_stats;
+  A.err = c->errw.as<int>();
+  A.dbg = nullptr;
+  A.hits = c->nb_hits.as<int32_t>();
+  A.order = list;
+  A.work = c->nb_work;
+  A.n_work_dev = n_dev;
+  return A;
+}
+
+static inline int nb_warp_grid(rpd_ctx* c, int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n * 32 + 255) / 256, 8 * (int64_t)c->sms));
+}
+
+// Part 1 of an incremental update: grid, rows of the new spheres, R1, R2, their rows, the
+// first swallow check.  misc: [0] rows of R1 + R2, [1] long new row, [2] next-round flags,
+// [3] new non-empty rows, [4] rows of a round, [5] R1 flags
+cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
+                              const double box[6], const double* prev, const int32_t* old_off,
+                              const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
+                              int32_t* list, int* misc) {
+  cudaError_t e;
+  const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
+  k_nb_same<<<blocks, 256, 0, c->stream>>>(sph, prev, 4 * N_old, c->errw.as<int>());
+  ++c->launches;
+  NbArgs A0{};
+  int mb = 0;
+  if ((e = nb_build(c, sph, N, box, cnt, &A0, &mb))) return e;
+  c->nb_mb = mb;
+  if ((e = cudaMemsetAsync(flag, 0, N > 0 ? N : 1, c->stream))) return e;
+  if ((e = cudaMemsetAsync(misc, 0, sizeof(int) * 8, c->stream))) return e;
+  // rows of the new spheres
+  const int64_t M = N - N_old;
+  k_nb_iota<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
+              c->stream>>>(list, N_old, M);
+  ++c->launches;
+  NbArgs A = nb_args_list(c, sph, N, box, cnt, list, nullptr);
+  A.n_work = M;
+  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
+  const int mb1 = (int)std::max<int64_t>(1, std::min<int64_t>((M + NB_WARPS - 1) / NB_WARPS, mb));
+  k_nb_pass1<<<mb1, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  k_nb_mark<<<nb_warp_grid(c, M), 256, 0, c->stream>>>(
+      N_old, N, cnt, c->nb_slab, sph, reinterpret_cast<const NbGrid*>(c->nb_grid), c->nb_start,
+      c->nb_items, flag, misc);
+  ++c->launches;
+  k_nb_expand<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(N_old, old_off, old_idx, flag);
+  ++c->launches;
+  // rows of R1 + R2 (count on the device), then the swallow check
+  if ((e = launch_flag_list(c, flag, N_old, list, misc, -1))) return e;
+  A = nb_args_list(c, sph, N, box, cnt, list, misc);
+  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
+  k_nb_pass1<<<mb, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  k_nb_swallow<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(list, misc, N_old, cnt, old_off,
+                                                               old_idx, flag, misc);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nb_update_round(rpd_ctx* c, int64_t N_old, const int32_t* old_off,
+                                   const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
+                                   int32_t* list, int* misc) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(misc + 2, 0, sizeof(int), c->stream))) return e;
+  if ((e = launch_flag_list(c, flag, N_old, list, misc + 4, 3))) return e;
+  NbArgs A = nb_args_list(c, c->nb_sph, c->nb_cur_N, c->nb_box, cnt, list, misc + 4);
+  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
+  k_nb_pass1<<<c->nb_mb, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  k_nb_swallow<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(list, misc + 4, N_old, cnt,
+                                                               old_off, old_idx, flag, misc);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nb_update_len(rpd_ctx* c, int64_t N, int64_t N_old, const int32_t* cnt,
+                                 const uint8_t* flag, const int32_t* old_off, int32_t* len,
+                                 int32_t* off) {
+  const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
+  k_nb_len<<<blocks, 256, 0, c->stream>>>(N, N_old, cnt, flag, old_off, len);
+  ++c->launches;
+  cudaError_t e = launch_scan_i32(c, len, off, N);
+  if (e) return e;
+  return cudaGetLastError();
+}
+
+// Part 2: the recomputed long rows (pass 2) and the merged, ascending CSR
+cudaError_t launch_nb_update2(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
+                              const double box[6], int32_t* cnt, const uint8_t* flag,
+                              const int32_t* old_off, const int32_t* old_idx, const int32_t* off,
+                              int32_t* tmp, int32_t* idx) {
+  NbArgs A = nb_args_list(c, sph, N, box, cnt, nullptr, nullptr);
+  A.off = off;
+  A.tmp = tmp;
+  k_nb_pass2<<<2 * c->sms, 32 * NB_WARPS, 0, c->stream>>>(A);
+  ++c->launches;
+  const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
+  k_nb_merge<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, N_old, flag, old_off, old_idx, off,
+                                                      c->nb_slab, tmp, idx);
   ++c->launches;
   return cudaGetLastError();
 }

@@ -277,6 +277,24 @@ struct ChangedOp {
   }
 };
 
+// the positions of the flags equal to val (val < 0: any non-zero flag), ascending; the
+// count at *count
+struct FlagListOp {
+  const uint8_t* flag;
+  int32_t* list;
+  int* count;
+  int val;
+  typedef int Acc;
+  __device__ static Acc acc0() { return 0; }
+  __device__ void init() {}
+  __device__ int load(int64_t i) const { return val < 0 ? flag[i] != 0 : flag[i] == val; }
+  __device__ void emit(int64_t i, int p, int f, Acc&) const {
+    if (f) list[p] = (int32_t)i;
+  }
+  __device__ void flush(Acc) const {}
+  __device__ void total(int64_t, int tot) const { *count = tot; }
+};
+
 template <class Op>
 static cudaError_t scan_op_impl(rpd_ctx* c, const Op& op, int64_t n, const int* n_dev) {
   const int nb = n > 0 ? (int)((n + SCAN_TILE - 1) / SCAN_TILE) : 1;
@@ -311,6 +329,12 @@ static cudaError_t scan_op_impl(rpd_ctx* c, const Op& op, int64_t n, const int* 
   k_scan_op<Op><<<nb, SCAN_THREADS, 0, c->stream>>>(op, n, nb, ticket, base, state, epoch, n_dev);
   ++c->launches;
   return cudaGetLastError();
+}
+
+cudaError_t launch_flag_list(rpd_ctx* c, const uint8_t* flag, int64_t n, int32_t* list,
+                             int* count, int val) {
+  if (n == 0) return cudaMemsetAsync(count, 0, sizeof(int), c->stream);
+  return scan_op_impl(c, FlagListOp{flag, list, count, val}, n, nullptr);
 }
 
 cudaError_t launch_dirty_scan(rpd_ctx* c, int64_t T) {

@@ -30,7 +30,8 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_download_euler", "rpd_get_topology", "rpd_download_topology",
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-            "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize"]
+            "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
+            "rpd_neighbors_update"]
 
 
 class RPDError(RuntimeError):
@@ -72,7 +73,8 @@ class _Rpe(C.Structure):
 
 class _NbrLists(C.Structure):
     _fields_ = [("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("N", C.c_int64),
-                ("E", C.c_int64), ("n_hidden", C.c_int64), ("n_vertex_overflow", C.c_int64)]
+                ("E", C.c_int64), ("n_hidden", C.c_int64), ("n_vertex_overflow", C.c_int64),
+                ("n_rows_computed", C.c_int64)]
 
 
 class _Medial(C.Structure):
@@ -151,6 +153,7 @@ def load_library(path: str = LIB_PATH):
     L.rpd_medial_mesh.argtypes = [vp, C.POINTER(_Medial)]
     L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
     L.rpd_neighbors.argtypes = [vp, vp, i64, vp, C.POINTER(_NbrLists)]
+    L.rpd_neighbors_update.argtypes = [vp, vp, i64, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
     L.rpd_gather_cands.argtypes = [vp, C.POINTER(_Shards), vp, vp]
@@ -166,7 +169,8 @@ def load_library(path: str = LIB_PATH):
               "rpd_download_topology", "rpd_medial_mesh", "rpd_download_medial_mesh",
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
-              "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize"):
+              "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
+              "rpd_neighbors_update"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -470,7 +474,22 @@ class RPDContext:
         off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
         self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
         return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
-                "n_vertex_overflow": n.n_vertex_overflow}
+                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed}
+
+    def neighbors_update(self, spheres, M: int, box, device=False) -> dict:
+        """Incremental lists after appending the last M of ``spheres`` (the previous call's
+        spheres unchanged, same box): only the rows of the new spheres, of the old spheres
+        they list and of old spheres they hide are recomputed (rpd_neighbors_update)."""
+        ps, ks = _ptr(spheres, np.float64)
+        bx = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
+        n = _NbrLists()
+        N = int(np.prod(ks.shape)) // 4
+        self._check(self.L.rpd_neighbors_update(self.h, ps, N, int(M), bx.ctypes.data,
+                                                C.byref(n)))
+        off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
+        self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
+        return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
+                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed}
 
     def dirty_ptr(self):
         """Device address of the ctx-owned dirty-tet list of the last update_partial."""

@@ -157,3 +157,89 @@ def test_neighbors_partial_update(ctx):
     got = ctx.download_pieces()
     ref = P.rpd_full(w.verts, w.tets, sp1, off1, idx1, ctx=None, filter_mode="pruned")
     assert compare_results(got, ref, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+
+
+def _rows_superset(ctx_lists, sp, box):
+    off, idx = check_valid(sp, ctx_lists)
+    roff, ridx = oracle.box_neighbours(sp, box)
+    g, r = rows(off, idx), rows(roff, ridx)
+    for i in range(len(sp)):
+        assert set(r[i]) <= set(g[i]), (i, sorted(set(r[i]) - set(g[i])))
+    return off, idx
+
+
+@pytest.mark.parametrize("m,clusters", [(1, 1), (5, 2), (20, 4)])
+def test_neighbors_incremental_superset_and_pieces(ctx, m, clusters):
+    """rpd_neighbors_update (reading R34): after each insertion batch only the rows of the new
+    spheres, of the old spheres they list and of old spheres they hide are recomputed; every
+    row is still a certified superset of the oracle's box neighbours, and the pieces with the
+    incremental lists equal the oracle's pieces with the regular-triangulation lists."""
+    import paper_2403_18761_b200 as P
+    w = W.make_shape_workload(f"nb_inc{m}", 1200, 100, seed=11 + m, n_batches=3, batch_m=m,
+                              clusters=clusters, cache=False)
+    box = W.mesh_box(w.verts)
+    ctx.neighbors(w.spheres, box)
+    for (sp, off1, idx1) in w.batches:
+        got = ctx.neighbors_update(sp, m, box)
+        assert 0 < got["n_rows"] < len(sp)
+        off, idx = _rows_superset(got, sp, box)
+        off, idx = off.copy(), idx.copy()
+        a = P.rpd_full(w.verts, w.tets, sp, off, idx, ctx=ctx)
+        # the oracle with the same lists, and the GPU with fully recomputed lists
+        b = oracle.rpd(w.verts, w.tets, sp, off, idx)
+        assert compare_results(a, b, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+        full = ctx.neighbors(sp, box)
+        c = P.rpd_full(w.verts, w.tets, sp, full["nbr_off"], full["nbr_idx"], ctx=ctx)
+        assert compare_results(a, c, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+        q = oracle.rpd(w.verts, w.tets, sp, off1, idx1)  # (the generator's Qhull lists)
+        print("qhull lists give the same pieces:",
+              compare_results(a, q, w.verts, w.tets, rel=1e-9, check_cands=False) == [])
+        # (the full recompute replaced the ctx's lists: the chain continues from them)
+
+
+def test_neighbors_incremental_c4(ctx):
+    """The C4 chain at full size (10 batches of 500 spheres on the C3 set): incremental lists
+    after every batch, then the final RPD with them equals the RPD with the Qhull lists."""
+    import paper_2403_18761_b200 as P
+    w = W.make_config("C4")
+    box = W.mesh_box(w.verts)
+    ctx.neighbors(w.spheres, box)
+    n_rows = []
+    for (sp, off1, idx1) in w.batches:
+        got = ctx.neighbors_update(sp, 500, box)
+        n_rows.append(got["n_rows"])
+    sp, off1, idx1 = w.batches[-1]
+    off, idx = np.asarray(got["nbr_off"]), np.asarray(got["nbr_idx"])
+    assert off[-1] == len(idx) and np.all(np.diff(off) >= 0)
+    assert max(n_rows) < len(sp) // 2
+    a = P.rpd_full(w.verts, w.tets, sp, off, idx, ctx=ctx)
+    b = P.rpd_full(w.verts, w.tets, sp, off1, idx1, ctx=ctx)
+    assert compare_results(a, b, w.verts, w.tets, rel=1e-9, check_cands=False) == []
+
+
+def test_neighbors_incremental_edge_cases(ctx):
+    import paper_2403_18761_b200 as P
+    box = (0, 0, 0, 32, 32, 32)
+    sp = np.array([[8, 8, 8, 2], [20, 20, 20, 1], [8, 20, 8, 1.5]], dtype=np.float64)
+    ctx.neighbors(sp, box)
+    # a new sphere with an old one's centre and a larger radius hides it: its row empties
+    sp2 = np.concatenate([sp, [[8, 8, 8, 3.0]]])
+    got = ctx.neighbors_update(sp2, 1, box)
+    full = ctx.neighbors(sp2, box)
+    assert rows(got["nbr_off"], got["nbr_idx"])[0] == []
+    assert rows(got["nbr_off"], got["nbr_idx"]) == rows(full["nbr_off"], full["nbr_idx"])
+    # M = 0: the same lists
+    same = ctx.neighbors_update(sp2, 0, box)
+    assert rows(same["nbr_off"], same["nbr_idx"]) == rows(full["nbr_off"], full["nbr_idx"])
+    # state errors: another box, or lists of another sphere count
+    with pytest.raises(P.RPDError, match="ESTATE"):
+        ctx.neighbors_update(np.concatenate([sp2, [[1, 1, 1, 1.0]]]), 1, (0, 0, 0, 33, 32, 32))
+    with pytest.raises(P.RPDError, match="ESTATE"):
+        ctx.neighbors_update(np.concatenate([sp2, [[1, 1, 1, 1.0]]]), 2, box)
+    # an old sphere that moved
+    bad = np.concatenate([sp2, [[1, 1, 1, 1.0]]])
+    bad[1, 0] += 1
+    with pytest.raises(P.RPDError, match="EINVAL"):
+        ctx.neighbors_update(bad, 1, box)
+    with pytest.raises(P.RPDError, match="ESTATE"):  # (the rejected call left no lists)
+        ctx.neighbors_update(bad, 1, box)
