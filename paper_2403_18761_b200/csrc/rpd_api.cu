@@ -220,7 +220,8 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (DevBuf* b : {&c->nb_buf, &c->nb_off, &c->nb_idx, &c->nb_tmp, &c->nb_cnt, &c->h_nb,
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
-                    &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch})
+                    &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch,
+                    &c->nb_ball})
     b->release();
   if (c->pd_host) cudaFreeHost(c->pd_host);
   for (DevBuf* b : {&c->pd_buf, &c->g_scan, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
@@ -1990,6 +1991,7 @@ rpd_status rpd_neighbors(rpd_ctx* c, const double* spheres, int64_t N, const dou
     CK(cudaMalloc(&c->nb_dbg, sizeof(long long) * 8 * N), "alloc");
     CK(cudaMemsetAsync(c->nb_dbg, 0, sizeof(long long) * 8 * N, c->stream), "memset");
   }
+  CK(c->nb_ball.ensure(sizeof(double4) * N), "alloc");  // (for rpd_neighbors_update)
   CK(launch_neighbors_pass1(c, d_sph, N, bx, c->nb_cnt.as<int32_t>(), off), "neighbors");
   RbSpec rs{};
   rs.i32[0] = off + N;
@@ -2043,7 +2045,12 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
     if (!(box[k] == c->nb_box[k]))
       return fail(c, RPD_ESTATE, "rpd_neighbors_update: the box differs from the previous call's");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
-  if (M == 0 || N_old == 0) return rpd_neighbors(c, spheres, N, box, out);
+  if (M == 0) {  // the current lists
+    c->nb_rows = 0;
+    *out = rpd_nbr_lists{c->nb_off.as<int32_t>(), c->nb_idx.as<int32_t>(), N, c->nb_E, 0, 0, 0};
+    return RPD_OK;
+  }
+  if (N_old == 0) return rpd_neighbors(c, spheres, N, box, out);
   const double bx[6] = {box[0], box[1], box[2], box[3], box[4], box[5]};
   const double* d_sph = nullptr;
   CK(resolve(c, spheres, 4 * N, c->h_nb, &d_sph), "stage spheres");
@@ -2053,21 +2060,29 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
   CK(c->nb_len.ensure(sizeof(int32_t) * (N + 1)), "alloc");
   CK(c->nb_off2.ensure(sizeof(int32_t) * (N + 1)), "alloc");
   CK(c->nb_misc.ensure(sizeof(int) * 8), "alloc");
+  // the balls of the old rows, grown (with their content) for the new ones
+  if (c->nb_ball.cap < sizeof(double4) * N) {
+    DevBuf nb;
+    CK(nb.ensure(sizeof(double4) * 2 * N), "alloc");
+    CK(cudaMemcpyAsync(nb.p, c->nb_ball.p, sizeof(double4) * N_old, cudaMemcpyDeviceToDevice,
+                       c->stream), "copy");
+    CK(cudaStreamSynchronize(c->stream), "copy");
+    std::swap(c->nb_ball, nb);
+    nb.release();
+  }
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   int32_t* off = c->nb_off2.as<int32_t>();
   int* misc = c->nb_misc.as<int>();
   int32_t* cnt = c->nb_cnt.as<int32_t>();
   uint8_t* flag = c->nb_flag.as<uint8_t>();
-  int32_t* list = c->nb_list.as<int32_t>();
   const int32_t* o_off = c->nb_off.as<int32_t>();
   const int32_t* o_idx = c->nb_idx.as<int32_t>();
-  c->nb_sph = d_sph;
-  c->nb_cur_N = N;
-  CK(launch_nb_update1(c, d_sph, N, N_old, bx, c->nb_prev.as<double>(), o_off, o_idx, cnt, flag,
-                       list, misc),
+  CK(launch_nb_update1(c, d_sph, N, N_old, bx, c->nb_prev.as<double>(), cnt, flag,
+                       c->nb_list.as<int32_t>(), c->nb_len.as<int32_t>(), o_off, off, misc),
      "neighbors update");
   RbSpec rs{};
-  for (int k = 0; k < 6; ++k) rs.i32[k] = misc + k;
+  rs.i32[0] = off + N;
+  rs.i32[1] = misc;
   rs.err = c->errw.as<int>();
   CK(readback(c, rs), "readback");
   CK(cudaStreamSynchronize(c->stream), "neighbors update");
@@ -2076,32 +2091,10 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
     c->nb_N = -1;  // (the grid scratch now describes the rejected spheres)
     return check_err(c, rb);
   }
-  // a new row longer than the slab, or new cells that border no old one (every old cell may be
-  // swallowed): recompute every row
-  if (rb->i32[1] != 0 || (rb->i32[3] > 0 && rb->i32[5] == 0))
-    return rpd_neighbors(c, spheres, N, box, out);
-  int64_t n_rows = M + rb->i32[0];
-  for (int round = 0; rb->i32[2] > 0; ++round) {  // swallowed cells: their old neighbours
-    if (round >= 64) return rpd_neighbors(c, spheres, N, box, out);
-    CK(launch_nb_update_round(c, N_old, o_off, o_idx, cnt, flag, list, misc), "neighbors update");
-    RbSpec r2{};
-    r2.i32[2] = misc + 2;
-    r2.i32[4] = misc + 4;
-    CK(readback(c, r2), "readback");
-    CK(cudaStreamSynchronize(c->stream), "neighbors update");
-    n_rows += rb->i32[4];
-  }
-  CK(launch_nb_update_len(c, N, N_old, cnt, flag, o_off, c->nb_len.as<int32_t>(), off),
-     "neighbors update");
-  RbSpec r3{};
-  r3.i32[0] = off + N;
-  CK(readback(c, r3), "readback");
-  CK(cudaStreamSynchronize(c->stream), "neighbors update");
-  const int64_t E = rb->i32[0];
+  const int64_t E = rb->i32[0], n_rows = rb->i32[1];
   CK(c->nb_idx2.ensure(sizeof(int32_t) * (E + 1)), "alloc");
   CK(c->nb_tmp.ensure(sizeof(int32_t) * (E + 1)), "alloc");
-  CK(launch_nb_update2(c, d_sph, N, N_old, bx, c->nb_cnt.as<int32_t>(), c->nb_flag.as<uint8_t>(),
-                       c->nb_off.as<int32_t>(), c->nb_idx.as<int32_t>(), off,
+  CK(launch_nb_update2(c, d_sph, N, N_old, bx, cnt, flag, o_off, o_idx, off,
                        c->nb_tmp.as<int32_t>(), c->nb_idx2.as<int32_t>()),
      "neighbors update");
   unsigned long long h_st[4] = {0, 0, 0, 0};
@@ -2116,7 +2109,7 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
   c->nb_E = E;
   c->nb_rows = n_rows;
   *out = rpd_nbr_lists{c->nb_off.as<int32_t>(), c->nb_idx.as<int32_t>(), N, E, (int64_t)h_st[1],
-                       (int64_t)h_st[0], c->nb_rows};
+                       (int64_t)h_st[0], n_rows};
   return RPD_OK;
 }
 

@@ -304,9 +304,7 @@ struct rpd_ctx {
   rpd::DevBuf nb_off2, nb_idx2; // the merged lists of an incremental update (swapped in)
   rpd::DevBuf nb_flag, nb_list, nb_len, nb_misc;
   int64_t nb_rows = 0;          // rows computed by the last call
-  int nb_mb = 1;                // pass-1 grid of the current spheres (incremental rounds)
-  const double* nb_sph = nullptr;  // the spheres and count of an update in progress
-  int64_t nb_cur_N = 0;
+  rpd::DevBuf nb_ball;          // double4 per sphere: ball around its last P_K (r < 0: empty)
 };
 
 namespace rpd {
@@ -323,23 +321,21 @@ cudaError_t stage_launch(rpd_ctx* c, const double* spheres, const int32_t* nbr_o
                          const int32_t* nbr_idx, bool reuse_rows, int epoch);
 cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
                                    int32_t* cnt, int32_t* off);
-// incremental update of the lists after appending spheres [N_old, N) (rpd_neighbors_update)
+// incremental update of the lists after appending spheres [N_old, N) (rpd_neighbors_update):
+// part 1 flags the rows to recompute (new spheres, old rows whose P_K ball a new radical plane
+// reaches), runs their pass 1 and the merged offsets (off[N] = E, misc[0] = rows); part 2 the
+// long rows and the merged CSR
 cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
-                              const double box[6], const double* prev, const int32_t* old_off,
-                              const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
-                              int32_t* list, int* misc);
-// a further round: the rows of the swallowed cells' old neighbours (flag 3), next frontier
-cudaError_t launch_nb_update_round(rpd_ctx* c, int64_t N_old, const int32_t* old_off,
-                                   const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
-                                   int32_t* list, int* misc);
-// row lengths and offsets of the merged lists (off[N] = E)
-cudaError_t launch_nb_update_len(rpd_ctx* c, int64_t N, int64_t N_old, const int32_t* cnt,
-                                 const uint8_t* flag, const int32_t* old_off, int32_t* len,
-                                 int32_t* off);
+                              const double box[6], const double* prev, int32_t* cnt,
+                              uint8_t* flag, int32_t* list, int32_t* len,
+                              const int32_t* old_off, int32_t* off, int* misc);
 cudaError_t launch_nb_update2(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
                               const double box[6], int32_t* cnt, const uint8_t* flag,
                               const int32_t* old_off, const int32_t* old_idx, const int32_t* off,
                               int32_t* tmp, int32_t* idx);
+cudaError_t launch_neighbors_pass2_rows(rpd_ctx* c, const double* sph, int64_t N,
+                                        const double box[6], int32_t* cnt, const int32_t* off,
+                                        int32_t* tmp);
 // list of the flags equal to val (val < 0: non-zero; ascending) and their count (rpd_scan.cu)
 cudaError_t launch_flag_list(rpd_ctx* c, const uint8_t* flag, int64_t n, int32_t* list,
                              int* count, int val = -1);

@@ -247,6 +247,7 @@ struct NbArgs {
   int64_t n_work;         // pass 1 rows: order[0, n_work) (0: all N) ...
   const int32_t* n_work_dev;  // ... or a device count (incremental update)
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
+  double4* ball;   // [N] bounding ball of each row's final P_K (center, radius; r < 0: empty)
   int32_t* hits;   // [warp slots][NB_HCAP] positions (cell-sorted arrays) of a round's hits
 };
 
@@ -307,6 +308,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
     if (!PASS2 && lane == 0) {
       A.cnt[i] = 0;
       atomicAdd(&A.stats[1], 1ull);
+      if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);  // (empty cell)
     }
     return;
   }
@@ -465,7 +467,10 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
     dbg_enum += clock64() - t_enum;
     n_v = S.n_v;
     if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
-      if (!PASS2 && lane == 0) A.cnt[i] = 0;
+      if (!PASS2 && lane == 0) {
+        A.cnt[i] = 0;
+        if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);
+      }
       if (!PASS2) {
         for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
         if (lane == 0) atomicAdd(&A.stats[2], n_tri);
@@ -769,6 +774,8 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
   if (!PASS2) {
     if (lane == 0) {
       A.cnt[i] = n_o;
+      // a ball around P_K ⊇ C_i ∩ B (world coordinates; incremental updates test it)
+      if (A.ball) A.ball[i] = make_double4(si.x + cx, si.y + cy, si.z + cz, rs + A.tol0);
       if (n_o > NB_CAP1) A.long_ids[atomicAdd(A.n_long, 1)] = i;
     }
     if (n_o <= NB_CAP1)
@@ -918,6 +925,7 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   A.stats = st;
   A.err = c->errw.as<int>();
   A.dbg = (long long*)c->nb_dbg;
+  A.ball = c->nb_ball.as<double4>();
   c->nb_args_tol0 = A.tol0;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nb_pass1, 32 * NB_WARPS, 0) || occ < 1)
@@ -948,8 +956,20 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   return cudaGetLastError();
 }
 
+// pass 2 (rows longer than the pass-1 slab, into tmp at off) and the ascending sort
 cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
                                    int32_t* cnt, const int32_t* off, int32_t* tmp, int32_t* idx) {
+  cudaError_t e = launch_neighbors_pass2_rows(c, sph, N, box, cnt, off, tmp);
+  if (e) return e;
+  const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
+  k_nb_sort<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, off, c->nb_slab, tmp, idx);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_neighbors_pass2_rows(rpd_ctx* c, const double* sph, int64_t N,
+                                        const double box[6], int32_t* cnt, const int32_t* off,
+                                        int32_t* tmp) {
   NbArgs A{};
   A.sph = sph;
   A.N = N;
@@ -972,33 +992,20 @@ cudaError_t launch_neighbors_pass2(rpd_ctx* c, const double* sph, int64_t N, con
   A.hits = c->nb_hits.as<int32_t>();
   k_nb_pass2<<<2 * c->sms, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
-  const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
-  k_nb_sort<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, off, c->nb_slab, tmp, idx);
-  ++c->launches;
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- incremental update
 //
 // After M spheres are appended (DESIGN.md §10 "Sphere neighbours", reading R34), the
-// box-restricted cell of an old sphere i changes only if new cells take volume from it.  Then
-// either i's new cell shares a facet with a new sphere j -- i is in j's (superset) row -- or
-// i's cell is swallowed (empty within B); a swallowed cell's region is covered by new cells,
-// so its old neighbours that survive border a new cell and are in a new row.  Recomputed:
-//   R1: the old spheres listed in the new spheres' rows (and old spheres a new one hides);
-//   R2: the old neighbours (old rows) of R1 -- where a swallowed cell can be;
-//   then, round by round, the old neighbours of every recomputed row that came out empty
-//   (swallowed clusters), until none is left.
-// Every other old row is kept: its cell, hence its certified superset, is unchanged.  Flags
-// of the old spheres: 0 kept, 1 recomputed, 2 (R2) / 3 (next round) to be recomputed.
+// box-restricted cell C_i ∩ B of an old sphere i changes only if some new sphere j wins a
+// part of it: pow_j < pow_i there, i.e. the radical plane h_ij is negative somewhere on
+// C_i ∩ B.  Every row stores a ball around its last bounding polytope P_K ⊇ C_i ∩ B; if h_ij
+// is positive on the whole ball for every new j, the cell -- hence its certified superset --
+// is unchanged and the row is kept.  Recomputed: the new spheres' rows and the rows whose ball
+// some new plane reaches (a superset of the changed cells: neighbours of the new spheres,
+// cells they swallow, spheres they hide).
 
-static __global__ void k_nb_iota(int32_t* __restrict__ list, int64_t base, int64_t n) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    list[k] = (int32_t)(base + k);
-}
-
-// the old spheres [0, N_old) must be the previous call's (the update appends)
 static __global__ void k_nb_same(const double* __restrict__ sph, const double* __restrict__ prev,
                                  int64_t n4, int* __restrict__ err) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4;
@@ -1009,83 +1016,51 @@ static __global__ void k_nb_same(const double* __restrict__ sph, const double* _
     }
 }
 
-// warp per new sphere j: R1 = the old spheres of its row and the old ones with its centre.
-// misc[1] |= 1: a new row longer than the pass-1 slab; misc[3]: new non-empty rows; misc[5]:
-// R1 flags set (both only tested against 0)
-static __global__ void k_nb_mark(int64_t N_old, int64_t N, const int32_t* __restrict__ cnt,
-                                 const int32_t* __restrict__ slab, const double* __restrict__ sph,
-                                 const NbGrid* __restrict__ gp, const int32_t* __restrict__ start,
-                                 const int32_t* __restrict__ items, uint8_t* __restrict__ flag,
-                                 int* __restrict__ misc) {
-  const int lane = threadIdx.x & 31;
-  const NbGrid g = *gp;
-  for (int64_t j = N_old + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); j < N;
-       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int n = cnt[j];
-    if (n > NB_CAP1) {
-      if (lane == 0) atomicOr(&misc[1], 1);
-      continue;
+// flag[i] = 1 for the rows to recompute: every new sphere, and every old sphere whose ball a
+// new radical plane reaches (tiles of new spheres staged in shared memory)
+constexpr int NB_AT = 256;
+static __global__ void __launch_bounds__(NB_AT) k_nb_affect(
+    int64_t N_old, int64_t N, const double* __restrict__ sph, const double4* __restrict__ ball,
+    double margin, uint8_t* __restrict__ flag) {
+  __shared__ double4 s_new[NB_AT];
+  for (int64_t i = N_old + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = 1;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N_old;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    double4 b = make_double4(0, 0, 0, -1.0), si = make_double4(0, 0, 0, 0);
+    if (i < N_old) {
+      b = ball[i];
+      si = make_double4(sph[4 * i], sph[4 * i + 1], sph[4 * i + 2], sph[4 * i + 3]);
     }
-    if (n > 0 && lane == 0) atomicAdd(&misc[3], 1);
-    int set = 0;
-    for (int s = lane; s < n; s += 32) {
-      const int i = slab[j * NB_CAP1 + s];
-      if (i < N_old) {
-        flag[i] = 1;
-        set = 1;
+    bool hit = false;
+    for (int64_t j0 = N_old; j0 < N; j0 += NB_AT) {
+      __syncthreads();
+      if (j0 + threadIdx.x < N) {
+        const int64_t j = j0 + threadIdx.x;
+        s_new[threadIdx.x] = make_double4(sph[4 * j], sph[4 * j + 1], sph[4 * j + 2], sph[4 * j + 3]);
+      }
+      __syncthreads();
+      const int nj = (int)(N - j0 < NB_AT ? N - j0 : NB_AT);
+      if (b.w < 0.0 || hit) continue;
+      for (int q = 0; q < nj && !hit; ++q) {
+        const double4 sj = s_new[q];
+        const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z;
+        const double u2 = ux * ux + uy * uy + uz * uz;
+        if (u2 == 0.0) {  // same centre: one of the two hides the other
+          hit = true;
+          break;
+        }
+        // h_ij(x) = (-u.(x - theta_i) + (|u|^2 - r_j^2 + r_i^2) / 2) / |u| >= 0 on C_i; its
+        // minimum over the ball: at the centre minus the radius
+        const double un = sqrt(u2);
+        const double yx = b.x - si.x, yy = b.y - si.y, yz = b.z - si.z;
+        const double hc = (-(ux * yx + uy * yy + uz * yz) + 0.5 * (u2 - sj.w * sj.w + si.w * si.w)) / un;
+        hit = hc - b.w <= margin;
       }
     }
-    const double x = sph[4 * j], y = sph[4 * j + 1], z = sph[4 * j + 2];
-    const int c = (nb_cell_axis(z, g, 2) * g.G + nb_cell_axis(y, g, 1)) * g.G + nb_cell_axis(x, g, 0);
-    for (int p = start[c] + lane; p < start[c + 1]; p += 32) {
-      const int k = items[p];
-      if (k < N_old && sph[4 * k] == x && sph[4 * k + 1] == y && sph[4 * k + 2] == z) {
-        flag[k] = 1;
-        set = 1;
-      }
-    }
-    if (__any_sync(0xffffffffu, set) && lane == 0) atomicAdd(&misc[5], 1);
-  }
-}
-
-// R2: warp per old sphere of R1 (flag 1): its old neighbours not yet flagged get flag 2
-static __global__ void k_nb_expand(int64_t N_old, const int32_t* __restrict__ old_off,
-                                   const int32_t* __restrict__ old_idx, uint8_t* __restrict__ flag) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N_old;
-       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    if (flag[i] != 1) continue;
-    for (int e = old_off[i] + lane; e < old_off[i + 1]; e += 32) {
-      const int k = old_idx[e];
-      if (k < N_old && flag[k] == 0) flag[k] = 2;
-    }
-  }
-}
-
-// after a round of rows list[0, *n): they are recomputed (flag 1); a row that came out empty
-// while its old row was not (a swallowed cell) puts its unflagged old neighbours in the next
-// round (flag 3, misc[2] > 0)
-static __global__ void k_nb_swallow(const int32_t* __restrict__ list, const int* __restrict__ n,
-                                    int64_t N_old, const int32_t* __restrict__ cnt,
-                                    const int32_t* __restrict__ old_off,
-                                    const int32_t* __restrict__ old_idx,
-                                    uint8_t* __restrict__ flag, int* __restrict__ misc) {
-  const int lane = threadIdx.x & 31;
-  const int nn = *n;
-  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < nn;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int i = list[q];
-    if (lane == 0) flag[i] = 1;
-    if (cnt[i] != 0 || old_off[i + 1] == old_off[i]) continue;
-    int added = 0;
-    for (int e = old_off[i] + lane; e < old_off[i + 1]; e += 32) {
-      const int k = old_idx[e];
-      if (k < N_old && flag[k] == 0) {
-        flag[k] = 3;
-        added = 1;
-      }
-    }
-    if (__any_sync(0xffffffffu, added) && lane == 0) atomicAdd(&misc[2], 1);
+    if (i < N_old) flag[i] = hit ? 1 : 0;
   }
 }
 
@@ -1123,109 +1098,35 @@ static __global__ void k_nb_merge(int64_t N, int64_t N_old, const uint8_t* __res
   }
 }
 
-// the pass-1 arguments of the current grid (nb_build's), for a row list with a device count
-static NbArgs nb_args_list(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
-                           int32_t* cnt, const int32_t* list, const int* n_dev) {
-  NbArgs A{};
-  A.sph = sph;
-  A.N = N;
-  A.grid = reinterpret_cast<const NbGrid*>(c->nb_grid);
-  A.start = c->nb_start;
-  A.items = c->nb_items;
-  A.sorted = reinterpret_cast<const double4*>(c->nb_sorted);
-  for (int k = 0; k < 3; ++k) {
-    A.blo[k] = box[k];
-    A.bhi[k] = box[3 + k];
-  }
-  A.tol0 = c->nb_args_tol0;
-  A.cnt = cnt;
-  A.slab = c->nb_slab;
-  A.n_long = c->nb_long;
-  A.long_ids = c->nb_long_ids;
-  A.stats = c->nb_stats;
-  A.err = c->errw.as<int>();
-  A.dbg = nullptr;
-  A.hits = c->nb_hits.as<int32_t>();
-  A.order = list;
-  A.work = c->nb_work;
-  A.n_work_dev = n_dev;
-  return A;
-}
-
-static inline int nb_warp_grid(rpd_ctx* c, int64_t n) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((n * 32 + 255) / 256, 8 * (int64_t)c->sms));
-}
-
-// Part 1 of an incremental update: grid, rows of the new spheres, R1, R2, their rows, the
-// first swallow check.  misc: [0] rows of R1 + R2, [1] long new row, [2] next-round flags,
-// [3] new non-empty rows, [4] rows of a round, [5] R1 flags
+// Part 1 of an incremental update: grid, the rows to recompute (flag), their pass 1, the row
+// lengths and offsets (off[N] = E); misc[0] = rows recomputed
 cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
-                              const double box[6], const double* prev, const int32_t* old_off,
-                              const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
-                              int32_t* list, int* misc) {
+                              const double box[6], const double* prev, int32_t* cnt,
+                              uint8_t* flag, int32_t* list, int32_t* len,
+                              const int32_t* old_off, int32_t* off, int* misc) {
   cudaError_t e;
   const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
   k_nb_same<<<blocks, 256, 0, c->stream>>>(sph, prev, 4 * N_old, c->errw.as<int>());
   ++c->launches;
-  NbArgs A0{};
+  NbArgs A{};
   int mb = 0;
-  if ((e = nb_build(c, sph, N, box, cnt, &A0, &mb))) return e;
-  c->nb_mb = mb;
-  if ((e = cudaMemsetAsync(flag, 0, N > 0 ? N : 1, c->stream))) return e;
-  if ((e = cudaMemsetAsync(misc, 0, sizeof(int) * 8, c->stream))) return e;
-  // rows of the new spheres
-  const int64_t M = N - N_old;
-  k_nb_iota<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
-              c->stream>>>(list, N_old, M);
+  if ((e = nb_build(c, sph, N, box, cnt, &A, &mb))) return e;
+  double L2 = 0.0;
+  for (int k = 0; k < 3; ++k) L2 += (box[3 + k] - box[k]) * (box[3 + k] - box[k]);
+  const double margin = 1e-9 * sqrt(L2) + 1e-12;
+  k_nb_affect<<<(int)std::min<int64_t>((N + NB_AT - 1) / NB_AT, 8 * (int64_t)c->sms), NB_AT, 0,
+                c->stream>>>(N_old, N, sph, c->nb_ball.as<double4>(), margin, flag);
   ++c->launches;
-  NbArgs A = nb_args_list(c, sph, N, box, cnt, list, nullptr);
-  A.n_work = M;
+  if ((e = launch_flag_list(c, flag, N, list, misc, -1))) return e;
+  A.order = list;
+  A.n_work = 0;
+  A.n_work_dev = misc;
   if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
-  const int mb1 = (int)std::max<int64_t>(1, std::min<int64_t>((M + NB_WARPS - 1) / NB_WARPS, mb));
-  k_nb_pass1<<<mb1, 32 * NB_WARPS, 0, c->stream>>>(A);
+  k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
-  k_nb_mark<<<nb_warp_grid(c, M), 256, 0, c->stream>>>(
-      N_old, N, cnt, c->nb_slab, sph, reinterpret_cast<const NbGrid*>(c->nb_grid), c->nb_start,
-      c->nb_items, flag, misc);
-  ++c->launches;
-  k_nb_expand<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(N_old, old_off, old_idx, flag);
-  ++c->launches;
-  // rows of R1 + R2 (count on the device), then the swallow check
-  if ((e = launch_flag_list(c, flag, N_old, list, misc, -1))) return e;
-  A = nb_args_list(c, sph, N, box, cnt, list, misc);
-  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
-  k_nb_pass1<<<mb, 32 * NB_WARPS, 0, c->stream>>>(A);
-  ++c->launches;
-  k_nb_swallow<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(list, misc, N_old, cnt, old_off,
-                                                               old_idx, flag, misc);
-  ++c->launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_nb_update_round(rpd_ctx* c, int64_t N_old, const int32_t* old_off,
-                                   const int32_t* old_idx, int32_t* cnt, uint8_t* flag,
-                                   int32_t* list, int* misc) {
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(misc + 2, 0, sizeof(int), c->stream))) return e;
-  if ((e = launch_flag_list(c, flag, N_old, list, misc + 4, 3))) return e;
-  NbArgs A = nb_args_list(c, c->nb_sph, c->nb_cur_N, c->nb_box, cnt, list, misc + 4);
-  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
-  k_nb_pass1<<<c->nb_mb, 32 * NB_WARPS, 0, c->stream>>>(A);
-  ++c->launches;
-  k_nb_swallow<<<nb_warp_grid(c, N_old), 256, 0, c->stream>>>(list, misc + 4, N_old, cnt,
-                                                               old_off, old_idx, flag, misc);
-  ++c->launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_nb_update_len(rpd_ctx* c, int64_t N, int64_t N_old, const int32_t* cnt,
-                                 const uint8_t* flag, const int32_t* old_off, int32_t* len,
-                                 int32_t* off) {
-  const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
   k_nb_len<<<blocks, 256, 0, c->stream>>>(N, N_old, cnt, flag, old_off, len);
   ++c->launches;
-  cudaError_t e = launch_scan_i32(c, len, off, N);
-  if (e) return e;
+  if ((e = launch_scan_i32(c, len, off, N))) return e;
   return cudaGetLastError();
 }
 
@@ -1234,11 +1135,8 @@ cudaError_t launch_nb_update2(rpd_ctx* c, const double* sph, int64_t N, int64_t 
                               const double box[6], int32_t* cnt, const uint8_t* flag,
                               const int32_t* old_off, const int32_t* old_idx, const int32_t* off,
                               int32_t* tmp, int32_t* idx) {
-  NbArgs A = nb_args_list(c, sph, N, box, cnt, nullptr, nullptr);
-  A.off = off;
-  A.tmp = tmp;
-  k_nb_pass2<<<2 * c->sms, 32 * NB_WARPS, 0, c->stream>>>(A);
-  ++c->launches;
+  cudaError_t e = launch_neighbors_pass2_rows(c, sph, N, box, cnt, off, tmp);
+  if (e) return e;
   const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
   k_nb_merge<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, N_old, flag, old_off, old_idx, off,
                                                       c->nb_slab, tmp, idx);
