@@ -2091,10 +2091,10 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
     c->nb_N = -1;  // (the grid scratch now describes the rejected spheres)
     return check_err(c, rb);
   }
-  const int64_t E = rb->i32[0], n_rows = rb->i32[1];
+  const int64_t E = rb->i32[0], n_rows = M + rb->i32[1];  // (new rows + changed old rows)
   CK(c->nb_idx2.ensure(sizeof(int32_t) * (E + 1)), "alloc");
   CK(c->nb_tmp.ensure(sizeof(int32_t) * (E + 1)), "alloc");
-  CK(launch_nb_update2(c, d_sph, N, N_old, bx, cnt, flag, o_off, o_idx, off,
+  CK(launch_nb_update2(c, d_sph, N, N_old, bx, cnt, c->nb_len.as<int32_t>(), o_off, o_idx, off,
                        c->nb_tmp.as<int32_t>(), c->nb_idx2.as<int32_t>()),
      "neighbors update");
   unsigned long long h_st[4] = {0, 0, 0, 0};

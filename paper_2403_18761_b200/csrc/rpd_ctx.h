@@ -322,15 +322,15 @@ cudaError_t stage_launch(rpd_ctx* c, const double* spheres, const int32_t* nbr_o
 cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
                                    int32_t* cnt, int32_t* off);
 // incremental update of the lists after appending spheres [N_old, N) (rpd_neighbors_update):
-// part 1 flags the rows to recompute (new spheres, old rows whose P_K ball a new radical plane
-// reaches), runs their pass 1 and the merged offsets (off[N] = E, misc[0] = rows); part 2 the
-// long rows and the merged CSR
+// part 1 the new rows (pass 1), the old rows' lengths (old row + the new spheres whose plane
+// reaches the row's P_K ball; 0 when hidden), the merged offsets (off[N] = E, misc[0] = old rows
+// changed); part 2 the new long rows and the merged CSR
 cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
                               const double box[6], const double* prev, int32_t* cnt,
                               uint8_t* flag, int32_t* list, int32_t* len,
                               const int32_t* old_off, int32_t* off, int* misc);
 cudaError_t launch_nb_update2(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
-                              const double box[6], int32_t* cnt, const uint8_t* flag,
+                              const double box[6], int32_t* cnt, const int32_t* len,
                               const int32_t* old_off, const int32_t* old_idx, const int32_t* off,
                               int32_t* tmp, int32_t* idx);
 cudaError_t launch_neighbors_pass2_rows(rpd_ctx* c, const double* sph, int64_t N,

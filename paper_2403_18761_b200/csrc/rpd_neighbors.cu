@@ -997,14 +997,16 @@ cudaError_t launch_neighbors_pass2_rows(rpd_ctx* c, const double* sph, int64_t N
 
 // ---------------------------------------------------------------- incremental update
 //
-// After M spheres are appended (DESIGN.md §10 "Sphere neighbours", reading R34), the
-// box-restricted cell C_i ∩ B of an old sphere i changes only if some new sphere j wins a
-// part of it: pow_j < pow_i there, i.e. the radical plane h_ij is negative somewhere on
-// C_i ∩ B.  Every row stores a ball around its last bounding polytope P_K ⊇ C_i ∩ B; if h_ij
-// is positive on the whole ball for every new j, the cell -- hence its certified superset --
-// is unchanged and the row is kept.  Recomputed: the new spheres' rows and the rows whose ball
-// some new plane reaches (a superset of the changed cells: neighbours of the new spheres,
-// cells they swallow, spheres they hide).
+// After M spheres are appended (DESIGN.md §10 "Sphere neighbours", reading R34) the cells only
+// shrink: a facet of the new cell C_i ∩ B between i and an old sphere k is part of an old facet,
+// so the new neighbours of an old sphere i are among its old neighbours and the new spheres.
+// And a new sphere j can cut C_i ∩ B only where h_ij < 0; every row stores a ball around its
+// last bounding polytope P_K ⊇ C_i ∩ B.  So the row of an old sphere becomes its old row
+// followed by the new spheres whose radical plane reaches its ball (ids > N_old: the row stays
+// ascending) -- a certified superset again: B ∩ (planes of the row) = the new cell exactly,
+// since the new spheres that miss the ball do not cut the old cell.  A new sphere with the same
+// centre that hides i (larger radius) empties i's row.  The new spheres' rows are computed by
+// pass 1 / pass 2.  Rows only grow; a full rpd_neighbors tightens them again.
 
 static __global__ void k_nb_same(const double* __restrict__ sph, const double* __restrict__ prev,
                                  int64_t n4, int* __restrict__ err) {
@@ -1016,16 +1018,22 @@ static __global__ void k_nb_same(const double* __restrict__ sph, const double* _
     }
 }
 
-// flag[i] = 1 for the rows to recompute: every new sphere, and every old sphere whose ball a
-// new radical plane reaches (tiles of new spheres staged in shared memory)
+static __global__ void k_nb_iota(int32_t* __restrict__ list, int64_t base, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    list[k] = (int32_t)(base + k);
+}
+
+// old sphere i against the new spheres (tiles in shared memory): WRITE = false counts the new
+// spheres whose plane reaches i's ball into len[i] (+ the old row; 0 when a new sphere hides
+// i, whose ball is then emptied) and flags the extended rows; WRITE = true appends their ids
 constexpr int NB_AT = 256;
-static __global__ void __launch_bounds__(NB_AT) k_nb_affect(
-    int64_t N_old, int64_t N, const double* __restrict__ sph, const double4* __restrict__ ball,
-    double margin, uint8_t* __restrict__ flag) {
+template <bool WRITE>
+static __global__ void __launch_bounds__(NB_AT) k_nb_extend(
+    int64_t N_old, int64_t N, const double* __restrict__ sph, double4* __restrict__ ball,
+    double margin, const int32_t* __restrict__ old_off, int32_t* __restrict__ len,
+    uint8_t* __restrict__ flag, const int32_t* __restrict__ off, int32_t* __restrict__ idx) {
   __shared__ double4 s_new[NB_AT];
-  for (int64_t i = N_old + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    flag[i] = 1;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N_old;
        i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + threadIdx.x;
@@ -1034,7 +1042,9 @@ static __global__ void __launch_bounds__(NB_AT) k_nb_affect(
       b = ball[i];
       si = make_double4(sph[4 * i], sph[4 * i + 1], sph[4 * i + 2], sph[4 * i + 3]);
     }
-    bool hit = false;
+    const int o0 = i < N_old ? old_off[i] : 0, o1 = i < N_old ? old_off[i + 1] : 0;
+    int n_hit = 0, pos = WRITE && i < N_old ? off[i] + (o1 - o0) : 0;
+    bool hidden = false;
     for (int64_t j0 = N_old; j0 < N; j0 += NB_AT) {
       __syncthreads();
       if (j0 + threadIdx.x < N) {
@@ -1043,38 +1053,41 @@ static __global__ void __launch_bounds__(NB_AT) k_nb_affect(
       }
       __syncthreads();
       const int nj = (int)(N - j0 < NB_AT ? N - j0 : NB_AT);
-      if (b.w < 0.0 || hit) continue;
-      for (int q = 0; q < nj && !hit; ++q) {
+      if (b.w < 0.0 || hidden) continue;  // (an empty cell stays empty)
+      for (int q = 0; q < nj; ++q) {
         const double4 sj = s_new[q];
         const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z;
         const double u2 = ux * ux + uy * uy + uz * uz;
-        if (u2 == 0.0) {  // same centre: one of the two hides the other
-          hit = true;
-          break;
+        if (u2 == 0.0) {  // same centre: the larger radius hides the other (ties: smaller id, i)
+          if (sj.w > si.w) {
+            hidden = true;
+            break;
+          }
+          continue;
         }
-        // h_ij(x) = (-u.(x - theta_i) + (|u|^2 - r_j^2 + r_i^2) / 2) / |u| >= 0 on C_i; its
-        // minimum over the ball: at the centre minus the radius
+        // h_ij(x) = (-u.(x - theta_i) + (|u|^2 - r_j^2 + r_i^2) / 2) / |u| >= 0 on C_i: its
+        // minimum over the ball is at the centre minus the radius
         const double un = sqrt(u2);
         const double yx = b.x - si.x, yy = b.y - si.y, yz = b.z - si.z;
-        const double hc = (-(ux * yx + uy * yy + uz * yz) + 0.5 * (u2 - sj.w * sj.w + si.w * si.w)) / un;
-        hit = hc - b.w <= margin;
+        const double hc =
+            (-(ux * yx + uy * yy + uz * yz) + 0.5 * (u2 - sj.w * sj.w + si.w * si.w)) / un;
+        if (hc - b.w <= margin) {
+          if (WRITE) idx[pos++] = (int32_t)(j0 + q);
+          ++n_hit;
+        }
       }
     }
-    if (i < N_old) flag[i] = hit ? 1 : 0;
+    if (!WRITE && i < N_old) {
+      len[i] = hidden ? 0 : (o1 - o0) + n_hit;
+      flag[i] = hidden || n_hit > 0;
+      if (hidden) ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);
+    }
   }
 }
 
-// row lengths of the merged lists: recomputed rows from pass 1, kept rows from the old CSR
-static __global__ void k_nb_len(int64_t N, int64_t N_old, const int32_t* __restrict__ cnt,
-                                const uint8_t* __restrict__ flag,
-                                const int32_t* __restrict__ old_off, int32_t* __restrict__ len) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-       i += (int64_t)gridDim.x * blockDim.x)
-    len[i] = (i >= N_old || flag[i]) ? cnt[i] : old_off[i + 1] - old_off[i];
-}
-
-// warp per row: recomputed rows rank-sorted from the slab / pass-2 rows, kept rows copied
-static __global__ void k_nb_merge(int64_t N, int64_t N_old, const uint8_t* __restrict__ flag,
+// warp per row: the old rows' kept entries (copied; the appended ones are written by
+// k_nb_extend<true>), the new rows rank-sorted from the slab / pass-2 rows
+static __global__ void k_nb_merge(int64_t N, int64_t N_old, const int32_t* __restrict__ len,
                                   const int32_t* __restrict__ old_off,
                                   const int32_t* __restrict__ old_idx,
                                   const int32_t* __restrict__ off, const int32_t* __restrict__ slab,
@@ -1083,9 +1096,10 @@ static __global__ void k_nb_merge(int64_t N, int64_t N_old, const uint8_t* __res
   for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N;
        i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int a = off[i], n = off[i + 1] - a;
-    if (i < N_old && !flag[i]) {
-      const int o = old_off[i];
-      for (int s = lane; s < n; s += 32) idx[a + s] = old_idx[o + s];
+    if (i < N_old) {
+      if (len[i] == 0) continue;  // (hidden)
+      const int o = old_off[i], k = old_off[i + 1] - o;
+      for (int s = lane; s < k; s += 32) idx[a + s] = old_idx[o + s];
       continue;
     }
     const int32_t* src = n <= NB_CAP1 ? slab + i * NB_CAP1 : tmp + a;
@@ -1098,8 +1112,22 @@ static __global__ void k_nb_merge(int64_t N, int64_t N_old, const uint8_t* __res
   }
 }
 
-// Part 1 of an incremental update: grid, the rows to recompute (flag), their pass 1, the row
-// lengths and offsets (off[N] = E); misc[0] = rows recomputed
+// new rows' lengths from pass 1
+static __global__ void k_nb_newlen(int64_t N_old, int64_t N, const int32_t* __restrict__ cnt,
+                                   int32_t* __restrict__ len) {
+  for (int64_t i = N_old + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    len[i] = cnt[i];
+}
+
+static double nb_margin(const double box[6]) {
+  double L2 = 0.0;
+  for (int k = 0; k < 3; ++k) L2 += (box[3 + k] - box[k]) * (box[3 + k] - box[k]);
+  return 1e-9 * sqrt(L2) + 1e-12;
+}
+
+// Part 1 of an incremental update: grid, the new rows (pass 1), the old rows' lengths, the
+// merged offsets (off[N] = E); misc[0] = old rows extended or emptied (flag)
 cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
                               const double box[6], const double* prev, int32_t* cnt,
                               uint8_t* flag, int32_t* list, int32_t* len,
@@ -1111,35 +1139,46 @@ cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t 
   NbArgs A{};
   int mb = 0;
   if ((e = nb_build(c, sph, N, box, cnt, &A, &mb))) return e;
-  double L2 = 0.0;
-  for (int k = 0; k < 3; ++k) L2 += (box[3 + k] - box[k]) * (box[3 + k] - box[k]);
-  const double margin = 1e-9 * sqrt(L2) + 1e-12;
-  k_nb_affect<<<(int)std::min<int64_t>((N + NB_AT - 1) / NB_AT, 8 * (int64_t)c->sms), NB_AT, 0,
-                c->stream>>>(N_old, N, sph, c->nb_ball.as<double4>(), margin, flag);
+  const int64_t M = N - N_old;
+  k_nb_iota<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
+              c->stream>>>(list, N_old, M);
   ++c->launches;
-  if ((e = launch_flag_list(c, flag, N, list, misc, -1))) return e;
   A.order = list;
-  A.n_work = 0;
-  A.n_work_dev = misc;
+  A.n_work = M;
   if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
-  k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
+  const int mb1 = (int)std::max<int64_t>(1, std::min<int64_t>((M + NB_WARPS - 1) / NB_WARPS, mb));
+  k_nb_pass1<<<mb1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
-  k_nb_len<<<blocks, 256, 0, c->stream>>>(N, N_old, cnt, flag, old_off, len);
+  k_nb_newlen<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
+                c->stream>>>(N_old, N, cnt, len);
   ++c->launches;
+  const int eb = (int)std::max<int64_t>(1, std::min<int64_t>((N_old + NB_AT - 1) / NB_AT,
+                                                             8 * (int64_t)c->sms));
+  k_nb_extend<false><<<eb, NB_AT, 0, c->stream>>>(N_old, N, sph, c->nb_ball.as<double4>(),
+                                                  nb_margin(box), old_off, len, flag, nullptr,
+                                                  nullptr);
+  ++c->launches;
+  if ((e = launch_flag_list(c, flag, N_old, list, misc, -1))) return e;  // (the count)
   if ((e = launch_scan_i32(c, len, off, N))) return e;
   return cudaGetLastError();
 }
 
-// Part 2: the recomputed long rows (pass 2) and the merged, ascending CSR
+// Part 2: the new long rows (pass 2) and the merged, ascending CSR
 cudaError_t launch_nb_update2(rpd_ctx* c, const double* sph, int64_t N, int64_t N_old,
-                              const double box[6], int32_t* cnt, const uint8_t* flag,
+                              const double box[6], int32_t* cnt, const int32_t* len,
                               const int32_t* old_off, const int32_t* old_idx, const int32_t* off,
                               int32_t* tmp, int32_t* idx) {
   cudaError_t e = launch_neighbors_pass2_rows(c, sph, N, box, cnt, off, tmp);
   if (e) return e;
   const int sb = (int)std::min<int64_t>((N * 32 + 255) / 256, 16 * (int64_t)c->sms);
-  k_nb_merge<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, N_old, flag, old_off, old_idx, off,
+  k_nb_merge<<<sb > 0 ? sb : 1, 256, 0, c->stream>>>(N, N_old, len, old_off, old_idx, off,
                                                       c->nb_slab, tmp, idx);
+  ++c->launches;
+  const int eb = (int)std::max<int64_t>(1, std::min<int64_t>((N_old + NB_AT - 1) / NB_AT,
+                                                             8 * (int64_t)c->sms));
+  k_nb_extend<true><<<eb, NB_AT, 0, c->stream>>>(N_old, N, sph, c->nb_ball.as<double4>(),
+                                                 nb_margin(box), old_off, nullptr, nullptr, off,
+                                                 idx);
   ++c->launches;
   return cudaGetLastError();
 }
