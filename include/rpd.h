@@ -249,7 +249,8 @@ rpd_status rpd_euler_finalize(rpd_ctx* ctx, const int64_t* acc, int64_t n_rows,
  * its facets on h_ij in such tets when both have an edge on f (elements of the symbolically
  * perturbed pieces, like the Euler sums; R26-R27).  Union-find on the device over
  * the current pieces; needs rpd_set_euler with the ctx holding the whole mesh
- * (local_ids == NULL, else RPD_ESTATE) before the last rpd_clip / rpd_update_partial.
+ * (local_ids == NULL, else RPD_ESTATE: a sharded job uses rpd_cc_shard / rpd_cc_merge below)
+ * before the last rpd_clip / rpd_update_partial.
  * Outputs (ctx-owned device arrays, valid until the next mutating call):
  *   rpc_cc     [N]        components of RPC(m_i) (0: no cell)
  *   rpf_cc     [E]        components of RPF(m_i, m_j) at the CSR entry of j in row i (rows
@@ -274,6 +275,37 @@ typedef struct {
   int64_t n_pieces, n_rpf, N, E;
 } rpd_topology;
 rpd_status rpd_get_topology(rpd_ctx* ctx, rpd_topology* out);
+
+/* CC numbers of a tet-SHARDED job (the tets are split over ranks, every
+ * rank's ctx built with rpd_set_euler(local_ids = its tets)): a distributed union-find
+ * (DESIGN.md §10 "CC numbers of a sharded job").
+ * rpd_cc_shard: joins the rank's pieces / radical facets across its interior faces and
+ *   returns the records of its shard-boundary faces (ctx-owned device arrays, valid until the
+ *   next mutating call): RPC records key_c = (f << 21 | i) -- f the smaller 4 t + k id of the
+ *   shared face (global tet ids), i the sphere -- with lab_c = the global id of the piece's
+ *   local component (piece_base + its smallest local piece index); RPF records key_f, j_f (the
+ *   facet's neighbour sphere), lab_f (rpf_base + ...).  piece_base / rpf_base: the sum of the
+ *   lower ranks' n_pieces / n_rpf (rpd_get_euler).  N < 2^21.  RPD_ESTATE without sharded
+ *   Euler data (a whole-mesh ctx uses rpd_get_topology).
+ * rpd_cc_merge: the records of ALL ranks (concatenated in any order; device arrays) ->
+ *   this rank's counts [N + E] (device, caller-owned): RPC components of every sphere, then
+ *   RPF components of every CSR entry, counted at the components' smallest global ids that
+ *   lie on this rank -- the sum over ranks (an all-reduce) gives rpd_topology's rpc_cc and
+ *   rpf_cc of the whole mesh. */
+typedef struct {
+  const uint64_t* key_c;
+  const int32_t* lab_c;
+  int64_t n_c;
+  const uint64_t* key_f;
+  const int32_t* j_f;
+  const int32_t* lab_f;
+  int64_t n_f;
+  int64_t n_pieces, n_rpf;
+} rpd_cc_records;
+rpd_status rpd_cc_shard(rpd_ctx* ctx, int64_t piece_base, int64_t rpf_base, rpd_cc_records* out);
+rpd_status rpd_cc_merge(rpd_ctx* ctx, const uint64_t* key_c, const int32_t* lab_c, int64_t n_c,
+                        const uint64_t* key_f, const int32_t* j_f, const int32_t* lab_f,
+                        int64_t n_f, int64_t total_pieces, int64_t total_rpf, int32_t* counts);
 /* Copy (host or device destinations; any pointer may be NULL). */
 rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
                                  int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,

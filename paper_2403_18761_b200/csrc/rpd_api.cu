@@ -221,7 +221,8 @@ void rpd_destroy(rpd_ctx* c) {
   for (DevBuf* b : {&c->nb_buf, &c->nb_off, &c->nb_idx, &c->nb_tmp, &c->nb_cnt, &c->h_nb,
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
                     &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch,
-                    &c->nb_ball})
+                    &c->nb_ball, &c->eu_ids, &c->eu_g2l, &c->cc_bnd, &c->cc_gpar, &c->cc_sort,
+                    &c->cc_nrec})
     b->release();
   if (c->pd_host) cudaFreeHost(c->pd_host);
   for (DevBuf* b : {&c->pd_buf, &c->g_scan, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
@@ -1418,7 +1419,8 @@ rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int
     return RPD_OK;
   }
   if (!tets_all || T_all < 0 || T_all > 0x7fffffff || V <= 0 || V >= (1ll << 21) ||
-      T_local < 0 || T_local > 0x7fffffff || (!local_ids && T_local != T_all) || !n_primes)
+      T_local < 0 || T_local > 0x7fffffff || (!local_ids && T_local != T_all && T_local != 0) ||
+      !n_primes)
     return fail(c, RPD_EINVAL, "rpd_set_euler: bad argument (V must be in (0, 2^21))");
   CK(cudaSetDevice(c->device), "cudaSetDevice");
   const int32_t *d_tets = nullptr, *d_ids = nullptr;
@@ -1426,6 +1428,14 @@ rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int
   CK(resolve(c, local_ids, local_ids ? T_local : 0, c->h_euid, &d_ids), "stage ids");
   CK(cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream), "memset");
   CK(launch_euler_setup(c, d_tets, T_all, V, d_ids, T_local), "euler setup");
+  const bool whole = local_ids == nullptr && T_local == T_all;
+  if (!whole) {  // (sharded CC numbers: the global ids of the ctx's tets and back)
+    CK(c->eu_ids.ensure(sizeof(int32_t) * (T_local > 0 ? T_local : 1)), "alloc");
+    if (T_local > 0)
+      CK(cudaMemcpyAsync(c->eu_ids.p, d_ids, sizeof(int32_t) * T_local, cudaMemcpyDeviceToDevice,
+                         c->stream), "copy ids");
+    CK(launch_g2l(c, d_ids, T_local, T_all), "id map");
+  }
   long long table[129];
   CK(cudaMemcpyAsync(table, c->eu_A.p, sizeof(table), cudaMemcpyDeviceToHost, c->stream),
      "readback");
@@ -1447,7 +1457,7 @@ rpd_status rpd_set_euler(rpd_ctx* c, const int32_t* tets_all, int64_t T_all, int
     c->eu_ppow[j] = (int)table[64 + j];
   }
   c->euler = 1;
-  c->eu_whole = local_ids == nullptr;
+  c->eu_whole = whole;
   c->eu_T = T_local;
   *n_primes = c->eu_P;
   return RPD_OK;
@@ -1549,6 +1559,58 @@ rpd_status rpd_get_topology(rpd_ctx* c, rpd_topology* out) {
   out->n_rpf = ps.n_rpf;
   out->N = c->st.N;
   out->E = c->st.E;
+  return RPD_OK;
+}
+
+rpd_status rpd_cc_shard(rpd_ctx* c, int64_t piece_base, int64_t rpf_base, rpd_cc_records* out) {
+  if (!c || !out || piece_base < 0 || rpf_base < 0)
+    return fail(c, RPD_EINVAL, "rpd_cc_shard: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no topology data (rpd_set_euler, then rpd_clip)");
+  if (c->eu_whole)
+    return fail(c, RPD_ESTATE, "rpd_cc_shard: the ctx holds the whole mesh (rpd_get_topology)");
+  if (c->st.N >= (1 << 21)) return fail(c, RPD_EINVAL, "rpd_cc_shard: record keys need N < 2^21");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const PieceSet& ps = c->pcs[c->cur];
+  if (piece_base + ps.n_pieces > 0x7fffffff || rpf_base + ps.n_rpf > 0x7fffffff)
+    return fail(c, RPD_EINVAL, "rpd_cc_shard: global ids beyond int32");
+  CK(c->cc_nrec.ensure(sizeof(int) * 2), "alloc");
+  int* n_rec = c->cc_nrec.as<int>();
+  CK(launch_cc_shard(c, ps, piece_base, rpf_base, n_rec), "cc shard");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{n_rec, n_rec + 1}, nullptr, nullptr}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "cc shard");
+  c->cc_base_c = piece_base;
+  c->cc_base_f = rpf_base;
+  const size_t nc = 4 * (size_t)ps.n_pieces + 1, nf = 4 * (size_t)ps.n_rpf + 1;
+  const uint64_t* key_c = c->cc_bnd.as<uint64_t>();
+  const uint64_t* key_f = key_c + nc;
+  const int32_t* lab_c = reinterpret_cast<const int32_t*>(key_f + nf);
+  const int32_t* j_f = lab_c + nc;
+  const int32_t* lab_f = j_f + nf;
+  *out = rpd_cc_records{key_c, lab_c, rb->i32[0], key_f, j_f, lab_f, rb->i32[1],
+                        ps.n_pieces, ps.n_rpf};
+  return RPD_OK;
+}
+
+rpd_status rpd_cc_merge(rpd_ctx* c, const uint64_t* key_c, const int32_t* lab_c, int64_t n_c,
+                        const uint64_t* key_f, const int32_t* j_f, const int32_t* lab_f,
+                        int64_t n_f, int64_t total_pieces, int64_t total_rpf, int32_t* counts) {
+  if (!c || n_c < 0 || n_f < 0 || (n_c > 0 && (!key_c || !lab_c)) ||
+      (n_f > 0 && (!key_f || !j_f || !lab_f)) || !counts || total_pieces < 0 || total_rpf < 0 ||
+      total_pieces > 0x7ffffffe || total_rpf > 0x7ffffffe || n_c > 0x7fffffff || n_f > 0x7fffffff)
+    return fail(c, RPD_EINVAL, "rpd_cc_merge: bad argument");
+  if (c->cc_base_c < 0 || !c->euler || !c->eu_valid)
+    return fail(c, RPD_ESTATE, "rpd_cc_merge before rpd_cc_shard");
+  const PieceSet& ps = c->pcs[c->cur];
+  if (c->cc_base_c + ps.n_pieces > total_pieces || c->cc_base_f + ps.n_rpf > total_rpf)
+    return fail(c, RPD_EINVAL, "rpd_cc_merge: totals smaller than this rank's range");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(launch_cc_merge(c, ps, reinterpret_cast<const unsigned long long*>(key_c), lab_c, n_c,
+                     reinterpret_cast<const unsigned long long*>(key_f), j_f, lab_f, n_f,
+                     total_pieces, total_rpf, c->cc_base_c, c->cc_base_f, counts),
+     "cc merge");
+  CK(cudaStreamSynchronize(c->stream), "cc merge");
   return RPD_OK;
 }
 

@@ -287,6 +287,9 @@ struct rpd_ctx {
   bool eu_whole = false;       // payloads built with the ctx holding the whole mesh in order
   rpd::DevBuf eu_adj;          // int32 [4 T_local]: face neighbour 4 t' + k' (global) or -1
   rpd::DevBuf cc_par, cc_out;  // CC numbers: union-find parents, outputs
+  rpd::DevBuf eu_ids, eu_g2l;  // sharded Euler mode: local -> global tet ids and back (-1: remote)
+  rpd::DevBuf cc_bnd, cc_gpar, cc_sort, cc_nrec;  // CC of a sharded job: records, global parents
+  int64_t cc_base_c = -1, cc_base_f = -1;  // this rank's global id bases (rpd_cc_shard)
   // sphere neighbours (NEXT-3): scratch (grid, pass-1 rows), outputs (off, idx), pass-2 rows
   rpd::DevBuf nb_buf, nb_off, nb_idx, nb_tmp, nb_cnt, h_nb, nb_hits;
   void* nb_grid = nullptr;
@@ -474,6 +477,15 @@ cudaError_t launch_euler_final(rpd_ctx* c, const unsigned long long* acc, int64_
                                long long* vi, double* vd, uint8_t* ex);
 cudaError_t launch_piece_den(rpd_ctx* c, const PieceSet& ps);
 cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
+// CC numbers of a tet-sharded job (distributed union-find, rpd_cc_shard / rpd_cc_merge)
+cudaError_t launch_g2l(rpd_ctx* c, const int32_t* local_ids, int64_t T_local, int64_t T_all);
+cudaError_t launch_cc_shard(rpd_ctx* c, const PieceSet& ps, long long base_c, long long base_f,
+                            int* n_rec);
+cudaError_t launch_cc_merge(rpd_ctx* c, const PieceSet& ps, const unsigned long long* key_c,
+                            const int32_t* lab_c, int64_t n_c, const unsigned long long* key_f,
+                            const int32_t* j_f, const int32_t* lab_f, int64_t n_f,
+                            int64_t tot_c, int64_t tot_f, long long base_c, long long base_f,
+                            int32_t* counts);
 // restricted power edges: per-piece lists, per-(i, j, k) Euler sums, CC numbers (with_cc)
 cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_rpe,
                        int64_t* n_tri);

@@ -617,6 +617,263 @@ cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- CC numbers of a sharded job
+//
+// The tets are sharded over ranks (rpd_set_euler with local_ids; face neighbours are global
+// tet ids).  A distributed union-find (DESIGN.md §10 "CC numbers of a sharded job"):
+//   1. every rank joins its own pieces (and radical facets) across its interior faces, as
+//      launch_cc, and labels each by the global id of its local component's root (its rank's
+//      base + the smallest local index: roots are component minima whatever the order);
+//   2. for each shard-boundary face f (the neighbour tet is on another rank) every piece of m_i
+//      with f as a facet emits a record (key = (f, i), label), every radical facet on h_ij with
+//      an edge on f a record (key = (f, i), j, label) -- f = the smaller of the two 4 t + k ids
+//      of the shared face, so both sides produce the same key;
+//   3. the records of all ranks (all-gathered by the caller) are sorted by key and equal keys
+//      (and equal j) joined in a union-find over the global ids -- every rank runs the same
+//      unions, and the roots are the component minima, so the partition is the same on all;
+//   4. each rank counts its local roots that are global roots (a global component's minimum is
+//      its local component's minimum): the sums over ranks are the CC numbers.
+
+__global__ void k_g2l(int64_t T_local, const int32_t* __restrict__ local_ids,
+                      int32_t* __restrict__ g2l) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l < T_local) g2l[local_ids[l]] = (int32_t)l;
+}
+
+// k_cc_link on a shard: the face neighbour's local index through g2l (remote ones skipped)
+__global__ void k_cc_link_sh(int64_t T, const int* __restrict__ adj, const int32_t* __restrict__ g2l,
+                             const int32_t* __restrict__ poff, const int32_t* __restrict__ psph,
+                             const uint8_t* __restrict__ sfm, const int32_t* __restrict__ roff,
+                             const int32_t* __restrict__ rj, const uint8_t* __restrict__ rfm,
+                             int* __restrict__ par_c, int* __restrict__ par_f) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  if (p0 == p1) return;
+  for (int k = 0; k < 4; ++k) {
+    const int nb = adj[4 * t + k];
+    if (nb < 0) continue;
+    const int t2 = g2l[nb >> 2], k2 = nb & 3;
+    if (t2 < 0 || t2 < t) continue;  // remote, or this face from the other side
+    const int q0 = poff[t2], q1 = poff[t2 + 1];
+    for (int q = p0; q < p1; ++q) {
+      const int i = psph[q];
+      const int q2 = find_sorted(psph, q0, q1, i);
+      if (q2 < 0) continue;
+      if (((sfm[q] >> k) & 1) && ((sfm[q2] >> k2) & 1)) uf_union(par_c, q, q2);
+      const int r20 = roff[q2], r21 = roff[q2 + 1];
+      for (int r = roff[q]; r < roff[q + 1]; ++r) {
+        if (!((rfm[r] >> k) & 1)) continue;
+        const int r2 = find_sorted(rj, r20, r21, rj[r]);
+        if (r2 >= 0 && ((rfm[r2] >> k2) & 1)) uf_union(par_f, r, r2);
+      }
+    }
+  }
+}
+
+// boundary records of the shard (atomic append; sorted later): RPC key (f << 21 | i), label;
+// RPF key (f << 21 | i), j, label.  Labels: global ids of the local roots.
+__global__ void k_cc_bnd(int64_t T, const int32_t* __restrict__ local_ids,
+                         const int* __restrict__ adj, const int32_t* __restrict__ g2l,
+                         const int32_t* __restrict__ poff, const int32_t* __restrict__ psph,
+                         const uint8_t* __restrict__ sfm, const int32_t* __restrict__ roff,
+                         const int32_t* __restrict__ rj, const uint8_t* __restrict__ rfm,
+                         int* __restrict__ par_c, int* __restrict__ par_f, long long base_c,
+                         long long base_f, unsigned long long* __restrict__ key_c,
+                         int32_t* __restrict__ lab_c, unsigned long long* __restrict__ key_f,
+                         int32_t* __restrict__ j_f, int32_t* __restrict__ lab_f,
+                         int* __restrict__ n_rec) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  if (p0 == p1) return;
+  const long long tg = local_ids[t];
+  for (int k = 0; k < 4; ++k) {
+    const int nb = adj[4 * t + k];
+    if (nb < 0 || g2l[nb >> 2] >= 0) continue;  // boundary of the mesh, or an interior face
+    const unsigned long long f = (unsigned long long)min(4 * tg + k, (long long)nb);
+    for (int q = p0; q < p1; ++q) {
+      const unsigned long long key = (f << 21) | (unsigned long long)psph[q];
+      if ((sfm[q] >> k) & 1) {
+        const int s = atomicAdd(n_rec, 1);
+        key_c[s] = key;
+        lab_c[s] = (int32_t)(base_c + uf_find(par_c, q));
+      }
+      for (int r = roff[q]; r < roff[q + 1]; ++r) {
+        if (!((rfm[r] >> k) & 1)) continue;
+        const int s = atomicAdd(n_rec + 1, 1);
+        key_f[s] = key;
+        j_f[s] = rj[r];
+        lab_f[s] = (int32_t)(base_f + uf_find(par_f, r));
+      }
+    }
+  }
+}
+
+__global__ void k_cc_init_range(int64_t n, int* __restrict__ par) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    par[x] = (int)x;
+}
+
+// sorted RPC records: equal neighbouring keys are the two sides of a face -> join
+__global__ void k_cc_join_c(int64_t n, const unsigned long long* __restrict__ key,
+                            const int32_t* __restrict__ lab, int* __restrict__ par) {
+  for (int64_t p = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (key[p] == key[p - 1]) uf_union(par, lab[p], lab[p - 1]);
+}
+
+// sorted RPF records (value = record index): within a run of equal keys, equal j -> join
+__global__ void k_cc_join_f(int64_t n, const unsigned long long* __restrict__ key,
+                            const int32_t* __restrict__ idx, const int32_t* __restrict__ jf,
+                            const int32_t* __restrict__ lab, int* __restrict__ par) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int a = idx[p];
+    for (int64_t q = p + 1; q < n && key[q] == key[p]; ++q) {
+      const int b = idx[q];
+      if (jf[a] == jf[b]) uf_union(par, lab[a], lab[b]);
+    }
+  }
+}
+
+// this rank's contributions: its local roots that are global roots, per sphere / CSR entry
+__global__ void k_cc_count_sh(int64_t n_pieces, const int32_t* __restrict__ psph,
+                              const int32_t* __restrict__ roff, const int32_t* __restrict__ rj,
+                              const int32_t* __restrict__ nbr_off,
+                              const int32_t* __restrict__ nbr_idx, int* __restrict__ lpar_c,
+                              int* __restrict__ lpar_f, int* __restrict__ gpar_c,
+                              int* __restrict__ gpar_f, long long base_c, long long base_f,
+                              int* __restrict__ rpc_cc, int* __restrict__ rpf_cc) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_pieces) return;
+  const int i = psph[q];
+  if (uf_find(lpar_c, (int)q) == q && uf_find(gpar_c, (int)(base_c + q)) == base_c + q)
+    atomicAdd(rpc_cc + i, 1);
+  const int e0 = nbr_off[i], e1 = nbr_off[i + 1];
+  for (int r = roff[q]; r < roff[q + 1]; ++r) {
+    if (uf_find(lpar_f, r) != r || uf_find(gpar_f, (int)(base_f + r)) != base_f + r) continue;
+    const int e = find_sorted(nbr_idx, e0, e1, rj[r]);
+    if (e >= 0) atomicAdd(rpf_cc + e, 1);
+  }
+}
+
+cudaError_t launch_g2l(rpd_ctx* c, const int32_t* local_ids, int64_t T_local, int64_t T_all) {
+  cudaError_t e = c->eu_g2l.ensure(sizeof(int32_t) * (T_all > 0 ? T_all : 1));
+  if (e) return e;
+  if ((e = cudaMemsetAsync(c->eu_g2l.p, 0xff, sizeof(int32_t) * (T_all > 0 ? T_all : 1),
+                           c->stream)))
+    return e;
+  if (T_local > 0 && local_ids) {
+    k_g2l<<<nblk(T_local, 256), 256, 0, c->stream>>>(T_local, local_ids, c->eu_g2l.as<int32_t>());
+    ++c->launches;
+  }
+  return cudaGetLastError();
+}
+
+// step 1 + 2: local union-find (cc_par: pieces, then radical facets) and the boundary records
+// into cc_bnd (counts at n_rec[0..1] on the device)
+cudaError_t launch_cc_shard(rpd_ctx* c, const PieceSet& ps, long long base_c, long long base_f,
+                            int* n_rec) {
+  const int64_t T = ps.n_tets, np = ps.n_pieces, nr = ps.n_rpf;
+  cudaError_t e;
+  if ((e = c->cc_par.ensure(sizeof(int) * (np + nr + 1)))) return e;
+  int* par_c = c->cc_par.as<int>();
+  int* par_f = par_c + np;
+  // record buffers: at most 4 per piece / per radical facet
+  const size_t nc = 4 * (size_t)np + 1, nf = 4 * (size_t)nr + 1;
+  if ((e = c->cc_bnd.ensure(nc * 12 + nf * 16 + 64))) return e;
+  unsigned long long* key_c = c->cc_bnd.as<unsigned long long>();
+  unsigned long long* key_f = key_c + nc;
+  int32_t* lab_c = reinterpret_cast<int32_t*>(key_f + nf);
+  int32_t* j_f = lab_c + nc;
+  int32_t* lab_f = j_f + nf;
+  if ((e = cudaMemsetAsync(n_rec, 0, sizeof(int) * 2, c->stream))) return e;
+  if (np > 0) {
+    k_cc_init_range<<<nblk(np, 256), 256, 0, c->stream>>>(np, par_c);
+    ++c->launches;
+  }
+  if (nr > 0) {
+    k_cc_init_range<<<nblk(nr, 256), 256, 0, c->stream>>>(nr, par_f);
+    ++c->launches;
+  }
+  if (T > 0 && np > 0) {
+    k_cc_link_sh<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, c->eu_adj.as<int>(), c->eu_g2l.as<int32_t>(), ps.off.as<int32_t>(),
+        ps.sphere.as<int32_t>(), ps.sfm.as<uint8_t>(), ps.rpf_off.as<int32_t>(),
+        ps.rpf_j.as<int32_t>(), ps.rfm.as<uint8_t>(), par_c, par_f);
+    k_cc_bnd<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, c->eu_ids.as<int32_t>(), c->eu_adj.as<int>(), c->eu_g2l.as<int32_t>(),
+        ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), ps.sfm.as<uint8_t>(),
+        ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(), ps.rfm.as<uint8_t>(), par_c, par_f,
+        base_c, base_f, key_c, lab_c, key_f, j_f, lab_f, n_rec);
+    c->launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+// step 3 + 4 on this rank: the gathered records of all ranks -> this rank's counts [N + E]
+cudaError_t launch_cc_merge(rpd_ctx* c, const PieceSet& ps, const unsigned long long* key_c,
+                            const int32_t* lab_c, int64_t n_c, const unsigned long long* key_f,
+                            const int32_t* j_f, const int32_t* lab_f, int64_t n_f,
+                            int64_t tot_c, int64_t tot_f, long long base_c, long long base_f,
+                            int32_t* counts) {
+  const int64_t N = c->st.N, E = c->st.E, np = ps.n_pieces;
+  cudaError_t e;
+  const size_t nc1 = n_c > 0 ? n_c : 1, nf1 = n_f > 0 ? n_f : 1;
+  if ((e = c->cc_gpar.ensure(sizeof(int) * (tot_c + tot_f + 2)))) return e;
+  if ((e = c->cc_sort.ensure(nc1 * 12 + nf1 * 16 + 64))) return e;
+  int* gpar_c = c->cc_gpar.as<int>();
+  int* gpar_f = gpar_c + tot_c + 1;
+  unsigned long long* sk_c = c->cc_sort.as<unsigned long long>();
+  unsigned long long* sk_f = sk_c + nc1;
+  int32_t* sl_c = reinterpret_cast<int32_t*>(sk_f + nf1);
+  int32_t* si_f = sl_c + nc1;
+  int32_t* ix_f = si_f + nf1;  // record indices (values of the RPF sort)
+  const int g = 8 * c->sms;
+  k_cc_init_range<<<g, 256, 0, c->stream>>>(tot_c, gpar_c);
+  k_cc_init_range<<<g, 256, 0, c->stream>>>(tot_f, gpar_f);
+  c->launches += 2;
+  size_t b1 = 0, b2 = 0;
+  if (n_c > 0 &&
+      (e = cub::DeviceRadixSort::SortPairs(nullptr, b1, key_c, sk_c, lab_c, sl_c, (int)n_c, 0, 64,
+                                           c->stream)))
+    return e;
+  if (n_f > 0 &&
+      (e = cub::DeviceRadixSort::SortPairs(nullptr, b2, key_f, sk_f, ix_f, si_f, (int)n_f, 0, 64,
+                                           c->stream)))
+    return e;
+  if ((e = c->mm_tmp.ensure((b1 > b2 ? b1 : b2) + 16))) return e;
+  if (n_c > 0) {
+    size_t bt = c->mm_tmp.cap;
+    if ((e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bt, key_c, sk_c, lab_c, sl_c, (int)n_c,
+                                             0, 64, c->stream)))
+      return e;
+    k_cc_join_c<<<g, 256, 0, c->stream>>>(n_c, sk_c, sl_c, gpar_c);
+    c->launches += 2;
+  }
+  if (n_f > 0) {
+    k_cc_init_range<<<g, 256, 0, c->stream>>>(n_f, ix_f);  // (identity indices)
+    size_t bt = c->mm_tmp.cap;
+    if ((e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bt, key_f, sk_f, ix_f, si_f, (int)n_f,
+                                             0, 64, c->stream)))
+      return e;
+    k_cc_join_f<<<g, 256, 0, c->stream>>>(n_f, sk_f, si_f, j_f, lab_f, gpar_f);
+    c->launches += 3;
+  }
+  if ((e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * (N + E), c->stream))) return e;
+  if (np > 0) {
+    int* lpar_c = c->cc_par.as<int>();
+    k_cc_count_sh<<<nblk(np, 256), 256, 0, c->stream>>>(
+        np, ps.sphere.as<int32_t>(), ps.rpf_off.as<int32_t>(), ps.rpf_j.as<int32_t>(),
+        c->st.nbr_off.as<int32_t>(), c->st.nbr_idx.as<int32_t>(), lpar_c, lpar_c + np, gpar_c,
+        gpar_f, base_c, base_f, counts, counts + N);
+    ++c->launches;
+  }
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- dual medial mesh (NEXT-2)
 //
 // RPC -> vertex, RPF(m_i, m_j) -> edge e_ij, RPE(m_i, m_j, m_k) -> triangle

@@ -163,6 +163,67 @@ class ShardedRPD:
         return self.glob, int(cnt[:, 0].sum())
 
 
+def gather_records(parts: dict, device, group=None) -> dict:
+    """All-gather variable-length 1-D tensors (the same keys and dtypes on every rank): one
+    counts all-gather (one host sync) and one all-gather of a packed byte buffer padded to the
+    largest rank; returns, per key, the concatenation over the ranks in rank order."""
+    world = dist.get_world_size(group)
+    keys = sorted(parts)
+    K = len(keys)
+    cl = torch.tensor([int(parts[k].numel()) for k in keys], dtype=torch.int64, device=device)
+    ca = torch.empty(world * K, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(ca, cl, group=group)
+    counts = ca.view(world, K).cpu().numpy()                       # the one host sync
+    isz = [parts[k].element_size() for k in keys]
+    def lay(r):
+        offs, off = [], 0
+        for q in range(K):
+            offs.append(off)
+            off += (int(counts[r, q]) * isz[q] + 15) // 16 * 16
+        return offs, off
+    lays = [lay(r) for r in range(world)]
+    maxb = max(max(b for _, b in lays), 16)
+    rank = dist.get_rank(group)
+    buf = torch.zeros(maxb, dtype=torch.uint8, device=device)
+    for q, k in enumerate(keys):
+        nb = int(counts[rank, q]) * isz[q]
+        if nb:
+            buf[lays[rank][0][q]:lays[rank][0][q] + nb] = parts[k].contiguous().view(torch.uint8)
+    big = torch.empty(world * maxb, dtype=torch.uint8, device=device)
+    dist.all_gather_into_tensor(big, buf, group=group)
+    out = {}
+    for q, k in enumerate(keys):
+        segs = []
+        for r in range(world):
+            o = r * maxb + lays[r][0][q]
+            segs.append(big[o:o + int(counts[r, q]) * isz[q]].view(parts[k].dtype))
+        out[k] = torch.cat(segs)
+    return out
+
+
+def cc_sharded(ctx, group=None) -> dict:
+    """CC numbers of every RPC and RPF of a tet-sharded job (DESIGN.md §10
+    "CC numbers of a sharded job"): the ranks' piece / radical-facet counts all-gathered into
+    global id bases, each rank's local union-find and shard-boundary records (rpd_cc_shard),
+    the records all-gathered (one packed all-gather), the global union-find and this rank's
+    counts (rpd_cc_merge), summed by one all-reduce.  Returns rpc_cc [N], rpf_cc [E] (int32
+    CUDA tensors, identical on every rank)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = torch.device("cuda", ctx.device)
+    npc, nrf, N, E = ctx.euler_sizes()
+    sz = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(sz, torch.tensor([npc, nrf], dtype=torch.int64, device=dev),
+                                group=group)
+    sz = sz.view(world, 2).cpu().numpy()
+    base_c, base_f = int(sz[:rank, 0].sum()), int(sz[:rank, 1].sum())
+    rec = ctx.cc_shard(base_c, base_f)
+    allrec = gather_records({k: rec[k] for k in ("key_c", "lab_c", "key_f", "j_f", "lab_f")},
+                            dev, group)
+    counts = ctx.cc_merge(allrec, int(sz[:, 0].sum()), int(sz[:, 1].sum()))
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    return {"rpc_cc": counts[:N], "rpf_cc": counts[N:N + E]}
+
+
 def allreduce_euler(local: dict, ctx, group=None) -> dict:
     """Per-sphere fractional Euler sums of the whole job (SURVEY.md §8(e) "validation
     aggregates"): every rank's exact accumulator rows rpc_acc [N, 1+P] and rpf_acc [E, 1+P]

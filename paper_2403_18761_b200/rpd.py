@@ -31,7 +31,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
             "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-            "rpd_neighbors_update"]
+            "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge"]
 
 
 class RPDError(RuntimeError):
@@ -63,6 +63,12 @@ class _Topology(C.Structure):
                 ("rpf_comp", C.c_void_p), ("piece_sosfm", C.c_void_p), ("rpf_fm", C.c_void_p),
                 ("rpf_adj", C.c_void_p), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64), ("N", C.c_int64),
                 ("E", C.c_int64)]
+
+
+class _CcRecords(C.Structure):
+    _fields_ = [("key_c", C.c_void_p), ("lab_c", C.c_void_p), ("n_c", C.c_int64),
+                ("key_f", C.c_void_p), ("j_f", C.c_void_p), ("lab_f", C.c_void_p),
+                ("n_f", C.c_int64), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64)]
 
 
 class _Rpe(C.Structure):
@@ -154,6 +160,8 @@ def load_library(path: str = LIB_PATH):
     L.rpd_download_medial_mesh.argtypes = [vp, vp, vp]
     L.rpd_neighbors.argtypes = [vp, vp, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_neighbors_update.argtypes = [vp, vp, i64, i64, vp, C.POINTER(_NbrLists)]
+    L.rpd_cc_shard.argtypes = [vp, i64, i64, C.POINTER(_CcRecords)]
+    L.rpd_cc_merge.argtypes = [vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, vp]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
     L.rpd_gather_cands.argtypes = [vp, C.POINTER(_Shards), vp, vp]
@@ -170,7 +178,7 @@ def load_library(path: str = LIB_PATH):
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
               "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-              "rpd_neighbors_update"):
+              "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -411,6 +419,39 @@ class RPDContext:
                torch.empty(n, dtype=torch.float64, device=dev))
         self._check(self.L.rpd_euler_finalize(self.h, self._p(acc), n, self._p(out[0]),
                                               self._p(out[1]), self._p(out[2])))
+        return out
+
+    def euler_sizes(self):
+        """(n_pieces, n_rpf, N, E) of the current pieces in Euler mode."""
+        e = _Euler()
+        self._check(self.L.rpd_get_euler(self.h, C.byref(e)))
+        return int(e.n_pieces), int(e.n_rpf), int(e.N), int(e.E)
+
+    def cc_shard(self, piece_base: int, rpf_base: int) -> dict:
+        """CC numbers of a sharded job, step 1 (rpd_cc_shard): local union-find and the records
+        of the shard-boundary faces as torch CUDA views of ctx-owned arrays (key_c / key_f are
+        int64 views of the uint64 keys)."""
+        r = _CcRecords()
+        self._check(self.L.rpd_cc_shard(self.h, int(piece_base), int(rpf_base), C.byref(r)))
+        return {"key_c": _device_view(r.key_c, r.n_c, "<i8"), "lab_c": _device_view(r.lab_c, r.n_c, "<i4"),
+                "key_f": _device_view(r.key_f, r.n_f, "<i8"), "j_f": _device_view(r.j_f, r.n_f, "<i4"),
+                "lab_f": _device_view(r.lab_f, r.n_f, "<i4"), "n_pieces": int(r.n_pieces),
+                "n_rpf": int(r.n_rpf)}
+
+    def cc_merge(self, rec: dict, total_pieces: int, total_rpf: int):
+        """Step 2 (rpd_cc_merge): the records of all ranks (dict of CUDA tensors, as cc_shard
+        returns, concatenated) -> this rank's counts, an int32 CUDA tensor [N + E] (rpc then rpf
+        components; sum over the ranks)."""
+        import torch
+        rec = {k: v.contiguous() for k, v in rec.items() if torch.is_tensor(v)}
+        nc, nf = int(rec["key_c"].numel()), int(rec["key_f"].numel())
+        e = _Euler()
+        self._check(self.L.rpd_get_euler(self.h, C.byref(e)))
+        out = torch.empty(int(e.N) + int(e.E), dtype=torch.int32, device=rec["key_c"].device)
+        self._check(self.L.rpd_cc_merge(self.h, self._p(rec["key_c"]), self._p(rec["lab_c"]), nc,
+                                        self._p(rec["key_f"]), self._p(rec["j_f"]),
+                                        self._p(rec["lab_f"]), nf, int(total_pieces),
+                                        int(total_rpf), self._p(out)))
         return out
 
     def topology(self):
@@ -700,7 +741,8 @@ class _View:
 def _device_view(ptr, n, typestr):
     import torch
     if n <= 0 or not ptr:
-        tdt = {"<i4": torch.int32, "<f8": torch.float64, "|u1": torch.uint8}[typestr]
+        tdt = {"<i4": torch.int32, "<f8": torch.float64, "|u1": torch.uint8,
+               "<i8": torch.int64}[typestr]
         return torch.zeros(0, dtype=tdt, device="cuda")
     return torch.as_tensor(_View(ptr, n, typestr), device="cuda")
 

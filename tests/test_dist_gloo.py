@@ -164,3 +164,47 @@ def test_euler_allreduce_equals_single_rank():
     want, _ = oracle.euler_sums(ref, w.N, w.nbr_off, w.nbr_idx)
     dec = [int(row[0]) + sum(Fraction(int(x), q) for x, q in zip(row[1:], PPOW)) for row in rpc]
     assert dec == want
+
+
+def _records_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_18761_b200.dist import gather_records
+        rng = np.random.default_rng(rank)
+        n = [5, 0, 37][rank]  # (ragged, one rank empty)
+        parts = {"key_c": torch.as_tensor(rng.integers(0, 1 << 50, n), dtype=torch.int64),
+                 "lab_c": torch.arange(n, dtype=torch.int32) + 1000 * rank,
+                 "j_f": torch.as_tensor(rng.integers(0, 99, 2 * n), dtype=torch.int32)}
+        out = gather_records(parts, torch.device("cpu"))
+        if rank == 0:
+            q.put({k: v.numpy() for k, v in out.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_records_three_gloo_ranks():
+    """The record exchange of the sharded CC numbers (dist.gather_records: one counts
+    all-gather + one padded byte all-gather) concatenates the ranks' ragged arrays in rank
+    order, every dtype intact."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_records_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = {"key_c": [], "lab_c": [], "j_f": []}
+    for r in range(world):
+        rng = np.random.default_rng(r)
+        n = [5, 0, 37][r]
+        want["key_c"].append(rng.integers(0, 1 << 50, n))
+        want["lab_c"].append(np.arange(n, dtype=np.int32) + 1000 * r)
+        want["j_f"].append(rng.integers(0, 99, 2 * n))
+    for k in want:
+        assert np.array_equal(got[k], np.concatenate(want[k]).astype(got[k].dtype)), k
