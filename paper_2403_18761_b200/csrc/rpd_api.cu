@@ -1058,9 +1058,7 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   PDyn* pd = c->pdd;
   cudaError_t e;
   unsigned long long* st = c->stats.as<unsigned long long>();
-  if ((e = cudaMemsetAsync(c->errw.p, 0, sizeof(int) * 4, c->stream))) return e;
-  if ((e = cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long) * ST_N, c->stream)))
-    return e;
+  // (k_pd_init also zeroes the error word, the stats and every small counter of the graph)
   if ((e = launch_pd_init(c))) return e;
   if ((e = launch_check_new_ids(c, nullptr, c->g_mb, 0))) return e;
   if ((e = stage_launch(c, nullptr, nullptr, nullptr, true, 0))) return e;
@@ -1084,15 +1082,13 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   int32_t* k_tet = c->k_tet.as<int32_t>();
   int32_t* k_words = c->k_words.as<int32_t>();
   int32_t* slab = c->slab.as<int32_t>();
-  if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
   if ((e = mark(2))) return e;
   if ((e = launch_filter(c, dl, T, cap, 0, (int)Nb, k_tet, slab, k_words, c->c_list.as<int32_t>(),
                          &pd->n_chg)))
     return e;
   if ((e = launch_keep_old(c, dl, T, pool_c, cap, k_tet, slab, k_words))) return e;
   if ((e = mark(3))) return e;
-  if ((e = cudaMemsetAsync(st + ST_MAXK, 0, sizeof(unsigned long long), c->stream))) return e;
-  if ((e = launch_max_ktet(c, T, k_tet))) return e;
+  if ((e = launch_max_ktet(c, T, k_tet))) return e;  // (atomicMax: no reset needed)
   {
     const int32_t* in[2] = {k_tet, k_words};
     int32_t* out[2] = {cd.off.as<int32_t>(), c->w_off.as<int32_t>()};
@@ -1105,11 +1101,6 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
                                 cd.moff.as<int32_t>(), nc_max, cd.cut.as<unsigned>())))
     return e;
   // (3) clip the batch; its pieces to the pool's tail
-  for (DevBuf* b : {&c->p_over, &c->p_over2, &c->p_over3})
-    if ((e = cudaMemsetAsync(b->p, 0, sizeof(int32_t), c->stream))) return e;
-  if ((e = cudaMemsetAsync(st + ST_EXACT, 0, sizeof(unsigned long long) * 5, c->stream))) return e;
-  if ((e = cudaMemsetAsync(st + ST_CLIP_PLANES, 0, sizeof(unsigned long long) * 8, c->stream)))
-    return e;
   if ((e = mark(4))) return e;
   if ((e = launch_clip(c, nc_max, cd.pair_tet.as<int32_t>(), dl, pool_idx, cd.moff.as<int32_t>(),
                        cd.cut.as<unsigned>(), 0)))
@@ -1145,6 +1136,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
                                 const int32_t* nbr_off, const int32_t* nbr_idx, int64_t E,
                                 const int32_t* new_ids, int64_t M, rpd_pieces* out,
                                 const int32_t** dirty_tets, int64_t* n_dirty) {
+  const auto h0 = std::chrono::steady_clock::now();
   const int64_t N_old = c->st.N, T = c->st.T;
   // inputs on the device (host arrays are copied on the ctx stream ahead of the graph)
   rpd_status s = read_E(c, nbr_off, N_new, &E);
@@ -1318,10 +1310,30 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
     c->g_kernels[slot] = c->g_nodes;
     ++c->g_captures;
   }
+  static const int g_time = getenv("RPD_GRAPH_TIME") ? 1 : 0;  // development: graph duration
+  cudaEvent_t gt[2] = {nullptr, nullptr};
+  const auto h1 = std::chrono::steady_clock::now();
+  if (g_time) {
+    cudaEventCreate(&gt[0]);
+    cudaEventCreate(&gt[1]);
+    cudaEventRecord(gt[0], c->stream);
+  }
   CK(cudaGraphLaunch(c->g_exec[slot], c->stream), "graph launch");
+  if (g_time) cudaEventRecord(gt[1], c->stream);
   c->launches += c->g_kernels[slot];
   ++c->g_launches;
   CK(cudaStreamSynchronize(c->stream), "partial update");
+  if (g_time) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, gt[0], gt[1]);
+    fprintf(stderr, "[rpd graph] %.3f ms on the device, %lld kernel nodes; host prologue %.3f ms, "
+            "launch to sync %.3f ms\n", ms, (long long)c->g_kernels[slot],
+            std::chrono::duration<double, std::milli>(h1 - h0).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1)
+                .count());
+    cudaEventDestroy(gt[0]);
+    cudaEventDestroy(gt[1]);
+  }
   const PDyn r = *c->pd_host;
   const Readback* rb = (const Readback*)c->pinned;
   if (c->profile) {

@@ -1405,11 +1405,9 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
     // device-driven update: n_pairs is the grids' bound; the count is read on the device by
     // both entry tiers, and only the one the eager path would choose gets it (nc_fast /
     // nc_small, the other sees 0).  The fast tier's overflows go down the usual cascade.
-    cudaError_t e = c->p_dyn.ensure(sizeof(int));
-    if (e) return e;
-    if ((e = cudaMemsetAsync(c->p_dyn.p, 0, sizeof(int), c->stream))) return e;
-    e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, nullptr, pair_tet, tet_ids,
-                                                        cand_idx, moff, cut,
+    // (the pair counter p_dyn is zeroed by k_pd_init)
+    cudaError_t e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, nullptr, pair_tet,
+                                                        tet_ids, cand_idx, moff, cut,
                                                         c->p_over.as<int32_t>(),
                                                         &c->pdd->nc_fast, c->p_dyn.as<int>());
     if (e) return e;

@@ -130,12 +130,17 @@ constexpr int BVH_LCAP = 256;   // planes staged per warp in the leaf kernel
 __global__ void k_leaf_boxes(const double* __restrict__ tx, int64_t T,
                              const int32_t* __restrict__ tet_ids, int64_t n,
                              double* __restrict__ leaf, int64_t n_leaf,
-                             const int* __restrict__ n_dev) {
+                             const int* __restrict__ n_dev, int32_t* __restrict__ zero_a,
+                             int32_t* __restrict__ zero_b) {
   if (n_dev) {  // device-driven update: the list length from the device
     n = *n_dev;
     n_leaf = (n + BVH_LEAF - 1) / BVH_LEAF;
   }
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (zero_a && a < n) {  // (graph: the counters of the subset, instead of memsets over T)
+    zero_a[a] = 0;
+    if (zero_b) zero_b[a] = 0;
+  }
   const int lane = threadIdx.x & 31;
   const bool valid = a < n;
   const int64_t t = valid ? (tet_ids ? (int64_t)tet_ids[a] : a) : 0;
@@ -757,12 +762,15 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
     if (e) return e;
     double* leaf = bb.as<double>();
     double* sup = leaf + 6 * n_leaf;
-    e = cudaMemsetAsync(k_tet, 0, sizeof(int32_t) * n_tets, c->stream);
-    if (!e && k_words) e = cudaMemsetAsync(k_words, 0, sizeof(int32_t) * n_tets, c->stream);
-    if (e) return e;
+    if (!nsub) {  // (a graph's subset: zeroed by k_leaf_boxes)
+      e = cudaMemsetAsync(k_tet, 0, sizeof(int32_t) * n_tets, c->stream);
+      if (!e && k_words) e = cudaMemsetAsync(k_words, 0, sizeof(int32_t) * n_tets, c->stream);
+      if (e) return e;
+    }
     if (tet_ids || !c->bvh_all_valid) {
       k_leaf_boxes<<<nblk(n_leaf * BVH_LEAF, 256), 256, 0, c->stream>>>(
-          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf, nsub);
+          c->st.tx.as<double>(), c->st.T, tet_ids, n_tets, leaf, n_leaf, nsub,
+          nsub ? k_tet : nullptr, nsub ? k_words : nullptr);
       k_super_boxes<<<nblk(n_sup * BVH_FAN, 256), 256, 0, c->stream>>>(leaf, n_leaf, sup, n_sup,
                                                                       nsub);
       c->launches += 2;
@@ -788,8 +796,10 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       int* n_sitems = n_items + 1;
       int2* items = reinterpret_cast<int2*>(c->bvh_items.as<char>() + sizeof(int2));
       int2* sitems = items + cap_items;
-      e = cudaMemsetAsync(n_items, 0, sizeof(int2), c->stream);
-      if (e) return e;
+      if (!pd) {  // (a graph: zeroed by k_pd_init / the dirty scan)
+        e = cudaMemsetAsync(n_items, 0, sizeof(int2), c->stream);
+        if (e) return e;
+      }
       const int64_t n_chunk = (n_sup + 31) / 32;
       int64_t blocks = (ns * n_chunk + BVH_WARPS - 1) / BVH_WARPS;
       if (blocks > (int64_t)sms * (pd ? 4 : 16)) blocks = (int64_t)sms * (pd ? 4 : 16);
@@ -850,7 +860,7 @@ cudaError_t launch_compact_cands(rpd_ctx* c, int64_t n, int cap, const int32_t* 
   if (e) return e;
   int* n_long = c->cand_long.as<int>();
   int32_t* long_list = c->cand_long.as<int32_t>() + 1;
-  if ((e = cudaMemsetAsync(n_long, 0, sizeof(int), c->stream))) return e;
+  if (!pd && (e = cudaMemsetAsync(n_long, 0, sizeof(int), c->stream))) return e;
   const uint2* slab_m = p_cut ? c->slab_m.as<uint2>() : nullptr;
   k_compact_cands_t<<<nblk(n, 256), 256, 0, c->stream>>>(n, cap, k_tet, slab, cand_off,
                                                         cand_idx, pair_tet, w_off, p_moff,

@@ -43,8 +43,10 @@ cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, 
 // re-stamped, min_epoch: one fused scan (rpd_scan.cu)
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
   if (T == 0) return cudaMemsetAsync(c->d_scan.p, 0, sizeof(int32_t), c->stream);
-  cudaError_t e = cudaMemsetAsync(c->min_epoch.p, 0x7f, sizeof(int), c->stream);
-  if (e) return e;
+  if (!c->pdd) {  // (in a graph k_pd_init sets it)
+    cudaError_t e = cudaMemsetAsync(c->min_epoch.p, 0x7f, sizeof(int), c->stream);
+    if (e) return e;
+  }
   return launch_dirty_scan(c, T);
 }
 
@@ -113,7 +115,8 @@ __global__ void k_rows_update(int64_t nd, const int32_t* __restrict__ dirty,
 cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, CandSet& pool_c,
                                PieceSet& pool_p, const CandSet& cd, const PieceSet& pd,
                                int64_t cbase, int64_t pbase, unsigned long long* rm) {
-  cudaError_t e = cudaMemsetAsync(rm, 0, sizeof(unsigned long long) * 4, c->stream);
+  cudaError_t e = c->pdd ? cudaSuccess  // (in a graph k_pd_init zeroes rm)
+                         : cudaMemsetAsync(rm, 0, sizeof(unsigned long long) * 4, c->stream);
   if (e || nd == 0) return e;
   unsigned grid = nblk(nd, 256);
   if (c->pdd && grid > (unsigned)c->sms * 2) grid = c->sms * 2;  // (grid-stride over the bound)
@@ -127,14 +130,42 @@ cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, Can
 
 // ---------------------------------------------------------------- device-driven updates
 
-// the inputs of this update from the mapped pinned mirror; the outputs cleared
-__global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host) {
-  if (threadIdx.x != 0) return;
-  PDyn v = *host;
-  v.nd = v.nb = v.n_chg = v.nc = v.nw = v.np = v.ni = v.maxk = v.need = v.abort = 0;
-  v.nc_fast = v.nc_small = v.nc_req = v.nw_req = 0;
-  for (int k = 0; k < 6; ++k) v.stamp[k] = 0;
-  *pd = v;
+// the inputs of this update from the mapped pinned mirror; the outputs cleared; and every
+// small counter / flag the graph's kernels accumulate into, zeroed here in one launch instead
+// of ~20 memset nodes (the eager path's memsets): error word, stats, overflow lists' counts,
+// the pair counter, the work-queue header, the removed-segment sums, min epoch, the look-back
+// state of the graph's scans
+struct PdZero {
+  int* errw;
+  unsigned long long* stats;
+  int* min_epoch;
+  int32_t *over1, *over2, *over3;
+  int* pair_ctr;
+  int* n_long;
+  int* qhdr;
+  unsigned long long* rm;
+  unsigned long long* scan_state;
+  int64_t scan_words;
+};
+__global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host, PdZero z) {
+  if (threadIdx.x == 0) {
+    PDyn v = *host;
+    v.nd = v.nb = v.n_chg = v.nc = v.nw = v.np = v.ni = v.maxk = v.need = v.abort = 0;
+    v.nc_fast = v.nc_small = v.nc_req = v.nw_req = 0;
+    for (int k = 0; k < 6; ++k) v.stamp[k] = 0;
+    *pd = v;
+    *z.min_epoch = 0x7f7f7f7f;
+    *z.over1 = *z.over2 = *z.over3 = 0;
+    *z.pair_ctr = 0;
+    *z.n_long = 0;
+    z.qhdr[0] = z.qhdr[1] = 0;
+  }
+  if (threadIdx.x < 4) {
+    z.errw[threadIdx.x] = 0;
+    z.rm[threadIdx.x] = 0ull;
+  }
+  if (threadIdx.x < ST_N) z.stats[threadIdx.x] = 0ull;
+  for (int64_t k = threadIdx.x; k < z.scan_words; k += blockDim.x) z.scan_state[k] = 0ull;
 }
 
 // after the batch's re-filter and scans: its candidate / mask-word totals, and the checks the
@@ -198,7 +229,19 @@ cudaError_t launch_pd_stamp(rpd_ctx* c, int k) {
 }
 
 cudaError_t launch_pd_init(rpd_ctx* c) {
-  k_pd_init<<<1, 32, 0, c->stream>>>(c->pdd, c->pd_hdev);
+  PdZero z{c->errw.as<int>(),
+           c->stats.as<unsigned long long>(),
+           c->min_epoch.as<int>(),
+           c->p_over.as<int32_t>(),
+           c->p_over2.as<int32_t>(),
+           c->p_over3.as<int32_t>(),
+           c->p_dyn.as<int>(),
+           c->cand_long.as<int>(),
+           c->bvh_items.as<int>(),
+           c->m_cnt.as<unsigned long long>(),
+           c->g_scan.as<unsigned long long>(),
+           (int64_t)(c->g_scan.cap / sizeof(unsigned long long))};
+  k_pd_init<<<1, 256, 0, c->stream>>>(c->pdd, c->pd_hdev, z);
   ++c->launches;
   return cudaGetLastError();
 }

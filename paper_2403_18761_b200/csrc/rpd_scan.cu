@@ -228,6 +228,7 @@ struct DirtyOp {
   int epoch;
   int32_t* scan_out;
   PDyn* pd;
+  int* qhdr;  // graph: the BVH work-queue header, zeroed for the re-filter that follows
   typedef int Acc;
   __device__ static Acc acc0() { return 0x7fffffff; }
   __device__ void init() {
@@ -251,6 +252,7 @@ struct DirtyOp {
   __device__ void total(int64_t n, int tot) const {
     scan_out[n] = tot;
     if (pd) pd->nd = pd->nb = tot;
+    if (qhdr) qhdr[0] = qhdr[1] = 0;
   }
 };
 
@@ -306,8 +308,7 @@ static cudaError_t scan_op_impl(rpd_ctx* c, const Op& op, int64_t n, const int* 
     if ((c->g_scan_used + words) * sizeof(unsigned long long) > c->g_scan.cap)
       return cudaErrorInvalidValue;
     ticket = c->g_scan.as<unsigned long long>() + c->g_scan_used;
-    c->g_scan_used += words;
-    if ((e = cudaMemsetAsync(ticket, 0, words * sizeof(unsigned long long), c->stream))) return e;
+    c->g_scan_used += words;  // (zeroed by k_pd_init)
     state = ticket + 1;
     base = 0;
     epoch = 1;
@@ -341,7 +342,7 @@ cudaError_t launch_dirty_scan(rpd_ctx* c, int64_t T) {
   PDyn* pd = c->pdd;
   DirtyOp op{c->d_count.as<int32_t>(), c->d_list.as<int32_t>(), c->d_pos.as<int32_t>(),
              c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch,
-             c->d_scan.as<int32_t>(), pd};
+             c->d_scan.as<int32_t>(), pd, pd ? c->bvh_items.as<int>() : nullptr};
   return scan_op_impl(c, op, T, nullptr);
 }
 
@@ -368,9 +369,7 @@ static cudaError_t scan_impl(rpd_ctx* c, const ScanIO<T>& io, int K, int64_t n,
     if ((c->g_scan_used + words) * sizeof(unsigned long long) > c->g_scan.cap)
       return cudaErrorInvalidValue;  // (the prologue sizes the region: a bug if reached)
     unsigned long long* r = c->g_scan.as<unsigned long long>() + c->g_scan_used;
-    c->g_scan_used += words;
-    cudaError_t e = cudaMemsetAsync(r, 0, words * sizeof(unsigned long long), c->stream);
-    if (e) return e;
+    c->g_scan_used += words;  // (zeroed by k_pd_init at the start of every replay)
     k_scan<T><<<nb * K, SCAN_THREADS, 0, c->stream>>>(io, n, nb, r, 0ull, r + 1, 1u, n_dev);
     ++c->launches;
     return cudaGetLastError();

@@ -184,6 +184,12 @@ def load_library(path: str = LIB_PATH):
     return L
 
 
+def _numel(a) -> int:
+    """Element count of a torch tensor or numpy array (no numpy reduction on the timed path)."""
+    n = a.numel() if callable(getattr(a, "numel", None)) else a.size
+    return int(n)
+
+
 def _ptr(x, dtype):
     """(pointer, keepalive) of a torch tensor (CUDA or CPU) or array-like, C-contiguous."""
     try:
@@ -279,11 +285,11 @@ class RPDContext:
         ps, ks = _ptr(spheres, np.float64)
         po, ko = _ptr(nbr_off, np.int32)
         pi, ki = _ptr(nbr_idx, np.int32)
-        V = int(np.prod(kv.shape)) // 3
-        T = int(np.prod(kt.shape)) // 4
-        N = int(np.prod(ks.shape)) // 4
+        V = _numel(kv) // 3
+        T = _numel(kt) // 4
+        N = _numel(ks) // 4
         co, ci, nc = C.c_void_p(), C.c_void_p(), C.c_int64()
-        E = int(np.prod(ki.shape))  # length of nbr_idx (no device read of nbr_off[N])
+        E = _numel(ki)  # length of nbr_idx (no device read of nbr_off[N])
         self._check(self.L.rpd_relations(self.h, pv, V, pt, T, ps, N, po, pi, E, C.byref(co),
                                          C.byref(ci), C.byref(nc)))
         self.T, self.N, self.n_cand = T, N, nc.value
@@ -301,11 +307,11 @@ class RPDContext:
         po, ko = _ptr(nbr_off, np.int32)
         pi, ki = _ptr(nbr_idx, np.int32)
         pn, kn = _ptr(new_ids, np.int32)
-        N_new = int(np.prod(ks.shape)) // 4
-        M = int(np.prod(kn.shape))
+        N_new = _numel(ks) // 4
+        M = _numel(kn)
         P = _Pieces()
         dt, nd = C.c_void_p(), C.c_int64()
-        E = int(np.prod(ki.shape))
+        E = _numel(ki)
         self._check(self.L.rpd_update_partial(self.h, ps, N_new, po, pi, E, pn, M, C.byref(P),
                                               C.byref(dt), C.byref(nd)))
         self.N = N_new
@@ -374,12 +380,12 @@ class RPDContext:
             self._check(self.L.rpd_set_euler(self.h, None, 0, 0, None, 0, C.byref(L)))
             return 0
         pt, kt = _ptr(tets_all, np.int32)
-        T_all = int(np.prod(kt.shape)) // 4
+        T_all = _numel(kt) // 4
         if local_ids is None:
             pl, kl, T_local = None, None, T_all
         else:
             pl, kl = _ptr(local_ids, np.int32)
-            T_local = int(np.prod(kl.shape))
+            T_local = _numel(kl)
         self._check(self.L.rpd_set_euler(self.h, pt, T_all, int(V), pl, T_local, C.byref(L)))
         self._keep_eu = (kt, kl)
         return L.value
@@ -510,7 +516,7 @@ class RPDContext:
         ps, ks = _ptr(spheres, np.float64)
         bx = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
         n = _NbrLists()
-        N = int(np.prod(ks.shape)) // 4
+        N = _numel(ks) // 4
         self._check(self.L.rpd_neighbors(self.h, ps, N, bx.ctypes.data, C.byref(n)))
         off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
         self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
@@ -524,7 +530,7 @@ class RPDContext:
         ps, ks = _ptr(spheres, np.float64)
         bx = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
         n = _NbrLists()
-        N = int(np.prod(ks.shape)) // 4
+        N = _numel(ks) // 4
         self._check(self.L.rpd_neighbors_update(self.h, ps, N, int(M), bx.ctypes.data,
                                                 C.byref(n)))
         off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
@@ -651,12 +657,12 @@ class RPDContext:
         pp, kp = _ptr(spheres, np.float64)
         pe, ke = _ptr(edges, np.int32)
         pf, kf = _ptr(faces, np.int32)
-        S = int(np.prod(ks.shape)) // 3
+        S = _numel(ks) // 3
         g, prim = self._alloc([(S, np.float64), (S, np.int32)], device)
         ne = C.c_int64()
-        self._check(self.L.rpd_envelope(self.h, ps, S, pp, int(np.prod(kp.shape)) // 4, pe,
-                                        int(np.prod(ke.shape)) // 2, pf,
-                                        int(np.prod(kf.shape)) // 3, self._p(g), self._p(prim),
+        self._check(self.L.rpd_envelope(self.h, ps, S, pp, _numel(kp) // 4, pe,
+                                        _numel(ke) // 2, pf,
+                                        _numel(kf) // 3, self._p(g), self._p(prim),
                                         C.byref(ne)))
         return g, prim, ne.value
 
