@@ -1060,7 +1060,7 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   unsigned long long* st = c->stats.as<unsigned long long>();
   // (k_pd_init also zeroes the error word, the stats and every small counter of the graph)
   if ((e = launch_pd_init(c))) return e;
-  if ((e = launch_check_new_ids(c, nullptr, c->g_mb, 0))) return e;
+  // (the new ids are checked by k_stage_spheres in a graph)
   if ((e = stage_launch(c, nullptr, nullptr, nullptr, true, 0))) return e;
   // (RPD_OPT_PROFILE: timer stamps around the filter and clip kernels, as the eager path's
   // events)
@@ -1120,8 +1120,7 @@ static cudaError_t issue_dd(rpd_ctx* c, int64_t Nb, int64_t nc_max) {
   // (4) re-point the dirty tets' rows; the totals back to the host
   unsigned long long* rm = c->m_cnt.as<unsigned long long>();
   if ((e = launch_rows_update(c, dl, T, pool_c, pool_p, cd, c->pcs_d, 0, 0, rm))) return e;
-  if ((e = launch_pd_final(c))) return e;
-  return readback(c, RbSpec{{c->p_over.as<int32_t>()}, st, c->errw.as<int>(), rm});
+  return launch_pd_final(c);  // (the one readback: into the mapped PDyn mirror)
 }
 
 static void graph_clear(rpd_ctx* c) {
@@ -1335,7 +1334,14 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
     cudaEventDestroy(gt[1]);
   }
   const PDyn r = *c->pd_host;
-  const Readback* rb = (const Readback*)c->pinned;
+  // the readback fields of the eager path, from the mirror
+  Readback* rb = (Readback*)c->pinned;
+  for (int k = 0; k < ST_N; ++k) rb->u64[k] = r.stats[k];
+  for (int k = 0; k < 4; ++k) {
+    rb->err[k] = r.err[k];
+    rb->u4[k] = r.removed[k];
+  }
+  rb->i32[0] = r.n_wide;
   if (c->profile) {
     c->last.filter_ms += 1e-6 * (double)((r.stamp[1] - r.stamp[0]) + (r.stamp[3] - r.stamp[2]));
     c->last.clip_ms += 1e-6 * (double)(r.stamp[5] - r.stamp[4]);

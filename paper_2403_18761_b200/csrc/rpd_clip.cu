@@ -1236,7 +1236,15 @@ __global__ void k_compact_pieces(int64_t n_pairs, const int32_t* __restrict__ ca
                                  int32_t* __restrict__ piece_sphere, double* __restrict__ piece_vol,
                                  double* __restrict__ piece_m1, uint8_t* __restrict__ piece_fm,
                                  int32_t* __restrict__ inc_off, int32_t* __restrict__ inc_sphere,
-                                 EuCompact eu, const PDyn* __restrict__ pd) {
+                                 EuCompact eu, const PDyn* __restrict__ pd,
+                                 const int32_t* __restrict__ cand_off,
+                                 int32_t* __restrict__ piece_off) {
+  if (pd) {  // (graph: the batch's per-tet piece offsets too -- k_piece_off of the eager path)
+    const int64_t nt = pd->nb;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nt;
+         t += (int64_t)gridDim.x * blockDim.x)
+      piece_off[t] = pscan[cand_off[t]];
+  }
   if (pd) {  // device-driven update: the batch size and the pool tails from the device
     n_pairs = pd->nc;
     cand_idx += pd->fill_c;
@@ -1526,8 +1534,9 @@ cudaError_t launch_compact_pieces(rpd_ctx* c, int64_t n_tets, int64_t n_pairs,
                   c->p_eu.as<long long>(), c->r_scan.as<int32_t>(), d.eu, d.rpf_off, d.rpf_j,
                   d.rpf_e, c->p_sfm.as<uint8_t>(), c->p_rfm.as<uint8_t>(), d.sfm, d.rfm,
                   c->p_radj.as<unsigned long long>(), d.radj, c->p_rep.as<unsigned long long>(),
-                  d.rep, d.inc_base, d.rpf_base}, pd);
+                  d.rep, d.inc_base, d.rpf_base}, pd, cand_off, d.off);
     ++c->launches;
+    if (pd) return cudaGetLastError();
   } else {
     // the terminal offsets of an empty batch (the pool's current fill levels)
     cudaMemcpyAsync(d.inc_off, &d.inc_base, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream);

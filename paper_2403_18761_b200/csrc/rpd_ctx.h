@@ -161,6 +161,11 @@ struct PDyn {
   int maxk, need;  // largest k_tet, work-queue demand of the re-filter
   int abort;   // PdAbort bits: the eager path redoes the batch (re-filter onwards)
   unsigned long long stamp[6];  // RPD_OPT_PROFILE: %globaltimer around filter / re-filter / clip
+  // copied back by the graph's last kernel (host mirror only)
+  unsigned long long stats[ST_N];
+  unsigned long long removed[4];  // the dirty tets' old segment sizes (cands, pieces, inc, rpf)
+  int err[4];
+  int n_wide;                     // pairs the fast clip tier passed on
 };
 
 }  // namespace rpd

@@ -832,7 +832,8 @@ cudaError_t launch_filter(rpd_ctx* c, const int32_t* tet_ids, int64_t n_tets, in
       c->launches += 3;
       c->bvh_cap_items = cap_items < cap_sup ? cap_items : cap_sup;
     }
-    if (slab) {  // (the count-only dirty detection needs no maximum)
+    if (slab && !nsub) {  // (count-only dirty detection: no maximum; a graph's re-filter takes
+                          // it after keep_old)
       k_max_ktet<<<nblk(n_tets, 256), 256, 0, c->stream>>>(n_tets, k_tet,
                                                           c->stats.as<unsigned long long>(), nsub);
       ++c->launches;

@@ -204,13 +204,24 @@ __global__ void k_pd_check(PDyn* __restrict__ pd, const int32_t* __restrict__ c_
   pd->nc_fast = nc < RPD_CLIP_SMALL ? 0 : nc;
 }
 
-// the batch's piece / incidence totals; the whole record back to the mapped mirror
+// the batch's piece / incidence totals; the whole record, the stats, the error word, the
+// removed-segment sums and the fast tier's overflow count back to the mapped mirror (the
+// update's one readback)
 __global__ void k_pd_final(PDyn* __restrict__ pd, PDyn* __restrict__ host,
-                           const int32_t* __restrict__ p_scan, const int32_t* __restrict__ i_scan) {
+                           const int32_t* __restrict__ p_scan, const int32_t* __restrict__ i_scan,
+                           const unsigned long long* __restrict__ stats,
+                           const int* __restrict__ errw, const unsigned long long* __restrict__ rm,
+                           const int32_t* __restrict__ over) {
   if (threadIdx.x != 0) return;
   PDyn v = *pd;
   v.np = p_scan[v.nc];
   v.ni = i_scan[v.nc];
+  for (int k = 0; k < ST_N; ++k) v.stats[k] = stats[k];
+  for (int k = 0; k < 4; ++k) {
+    v.removed[k] = rm[k];
+    v.err[k] = errw[k];
+  }
+  v.n_wide = *over;
   *host = v;
   __threadfence_system();
 }
@@ -255,7 +266,9 @@ cudaError_t launch_pd_check(rpd_ctx* c, const int32_t* c_off, const int32_t* w_o
 
 cudaError_t launch_pd_final(rpd_ctx* c) {
   k_pd_final<<<1, 32, 0, c->stream>>>(c->pdd, c->pd_hdev, c->p_scan.as<int32_t>(),
-                                      c->i_scan.as<int32_t>());
+                                      c->i_scan.as<int32_t>(),
+                                      c->stats.as<unsigned long long>(), c->errw.as<int>(),
+                                      c->m_cnt.as<unsigned long long>(), c->p_over.as<int32_t>());
   ++c->launches;
   return cudaGetLastError();
 }

@@ -78,12 +78,17 @@ __global__ void k_stage_tets(const double* __restrict__ verts, int64_t V,
 __global__ void k_stage_spheres(const double* __restrict__ spheres, int64_t N,
                                 double4* __restrict__ sw, const double4* __restrict__ old_sw,
                                 int64_t N_old, int* err, const PDyn* __restrict__ pd) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (pd) {  // device-driven update: inputs and sizes from the device (grid sized by a bound)
     spheres = pd->spheres;
     N = pd->N;
     N_old = pd->N_old;
+    // ... and the new ids must be the appended range (k_check_new_ids of the eager path)
+    if (i < pd->M && pd->new_ids[i] != N_old + i && atomicCAS(err, 0, (int)RPD_EINVAL) == 0) {
+      err[1] = 100;
+      err[2] = (int)i;
+    }
   }
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
   double S[4];
   for (int c = 0; c < 4; ++c) {
