@@ -222,7 +222,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
                     &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch,
                     &c->nb_ball, &c->eu_ids, &c->eu_g2l, &c->cc_bnd, &c->cc_gpar, &c->cc_sort,
-                    &c->cc_nrec})
+                    &c->cc_nrec, &c->st.long_rows})
     b->release();
   if (c->pd_host) cudaFreeHost(c->pd_host);
   for (DevBuf* b : {&c->pd_buf, &c->g_scan, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
@@ -1255,7 +1255,8 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
     const DevBuf* bufs[] = {
         &c->errw, &c->stats, &c->pd_buf, &S.tx, &S.sw, &S.old_sw, &S.nbr_off, &S.old_off,
         &S.nbr_idx, &S.old_idx, &S.planes, &S.old_planes, &S.twin, &S.old_twin, &S.hkey,
-        &S.old_hkey, &S.repoch, &S.old_repoch, &S.htab, &c->bvh_all, &c->bvh, &c->bvh_items,
+        &S.old_hkey, &S.repoch, &S.old_repoch, &S.htab, &S.long_rows, &c->bvh_all, &c->bvh,
+        &c->bvh_items,
         &c->d_count, &c->d_flag, &c->d_scan, &c->d_pos, &c->d_list, &c->cepoch, &c->min_epoch,
         &c->c_flag, &c->c_scan, &c->c_list, &c->g_scan, &c->k_tet, &c->k_words, &c->slab,
         &c->slab_m, &cd.off, &cd.pair_tet, &cd.moff, &cd.cut, &c->w_off, &c->cand_long,

@@ -92,6 +92,7 @@ struct Stage {
   DevBuf old_off, old_idx, old_planes, old_twin, old_hkey, old_repoch, old_sw;
   int64_t T = 0, N = 0, V = 0, E = 0;
   int64_t N_prev = 0;  // N of the previous staging (the old rows)
+  DevBuf long_rows;    // partial updates: the long rows deferred to k_stage_long (+ count)
 };
 
 }  // namespace rpd

@@ -143,6 +143,7 @@ struct PdZero {
   int* pair_ctr;
   int* n_long;
   int* qhdr;
+  int* n_stage_long;
   unsigned long long* rm;
   unsigned long long* scan_state;
   int64_t scan_words;
@@ -159,6 +160,7 @@ __global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host, 
     *z.pair_ctr = 0;
     *z.n_long = 0;
     z.qhdr[0] = z.qhdr[1] = 0;
+    *z.n_stage_long = 0;
   }
   if (threadIdx.x < 4) {
     z.errw[threadIdx.x] = 0;
@@ -249,6 +251,7 @@ cudaError_t launch_pd_init(rpd_ctx* c) {
            c->p_dyn.as<int>(),
            c->cand_long.as<int>(),
            c->bvh_items.as<int>(),
+           c->st.long_rows.as<int>() + (c->st.long_rows.cap / sizeof(int32_t)) - 1,
            c->m_cnt.as<unsigned long long>(),
            c->g_scan.as<unsigned long long>(),
            (int64_t)(c->g_scan.cap / sizeof(unsigned long long))};

@@ -128,17 +128,168 @@ struct OldRows {  // previous staged CSR (partial updates: unchanged rows are co
   int64_t N;
 };
 
-// One group of RG lanes per sphere row (STAGE_RG): validation, ascending order (fast path for sorted input rows,
-// else rank sort), radical planes and twins.  In a partial update a row of an old sphere
-// whose neighbour list is unchanged is copied from the previous stage instead.
+// The lanes that build one row: a group of RG lanes of a warp (k_stage_rows) or a whole block
+// (k_stage_long, the long rows of a partial update); same code, different votes and barriers.
 template <int RG>
-__global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
+struct WarpRows {
+  int lane;
+  unsigned full;
+  static constexpr int size = RG;
+  __device__ bool all(bool x) const { return __all_sync(full, x); }
+  __device__ bool any(bool x) const { return __any_sync(full, x); }
+  __device__ void sync() const { __syncwarp(full); }
+};
+struct BlockRows {
+  int lane;
+  int size;
+  __device__ bool all(bool x) const { return __syncthreads_and(x); }
+  __device__ bool any(bool x) const { return __syncthreads_or(x); }
+  __device__ void sync() const { __syncthreads(); }
+};
+
+// Build row i (entries [e0, e1)): validation, ascending order (input order kept when sorted,
+// else rank sort), radical planes, twin keys and twins.  tab: the row's duplicate-key hash
+// table (at least pow2 >= 2k entries; global scratch or shared memory).
+template <class G>
+__device__ void stage_build(const G& g, int64_t i, int32_t e0, int32_t e1, bool sorted,
+                            int64_t N, const int32_t* __restrict__ idx_in,
+                            const double4* __restrict__ sw, int32_t* __restrict__ idx_out,
+                            double4* __restrict__ planes, int32_t* __restrict__ twin,
+                            unsigned long long* __restrict__ hkey, int32_t* __restrict__ repoch,
+                            int epoch, unsigned long long* tab, int* err) {
+  const int lane = g.lane, S = g.size;
+  const int k = e1 - e0;
+  if (lane == 0) repoch[i] = epoch;
+  bool bad = false;
+  for (int32_t e = e0 + lane; e < e1; e += S) {
+    const int32_t j = idx_in[e];
+    if (j < 0 || j >= N) {
+      report(err, RPD_EINVAL, ERR_NBR_INDEX, i);
+      bad = true;
+      break;
+    }
+    if (j == i) {
+      report(err, RPD_EINVAL, ERR_NBR_SELF, i);
+      bad = true;
+      break;
+    }
+    if (sorted) {
+      idx_out[e] = j;
+      continue;
+    }
+    int rank = 0;
+    for (int32_t f = e0; f < e1; ++f) {
+      const int32_t x = idx_in[f];
+      if (x == j && f != e) {
+        report(err, RPD_EINVAL, ERR_NBR_DUP, i);
+        bad = true;
+      }
+      rank += x < j;
+    }
+    if (bad) break;
+    idx_out[e0 + rank] = j;
+  }
+  if (g.any(bad)) return;
+  g.sync();
+  const double4 si = sw[i];
+  // planes, and the twin key: bit patterns of the ratios to the first non-zero normal
+  // component (correctly rounded quotients of exactly proportional integers are equal)
+  for (int32_t e = e0 + lane; e < e1; e += S) {
+    const int32_t j = idx_out[e];
+    const double4 sj = sw[j];
+    const double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
+    if (nx == 0.0 && ny == 0.0 && nz == 0.0) report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
+    const double4 a = make_double4(nx, ny, nz, sj.w - si.w);
+    planes[e] = a;
+    const double piv = fabs(a.x != 0.0 ? a.x : (a.y != 0.0 ? a.y : a.z));
+    const int which = a.x != 0.0 ? 0 : (a.y != 0.0 ? 1 : 2);
+    unsigned long long h = 1469598103934665603ull ^ (unsigned long long)which;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.x / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.y / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.z / piv)) * 1099511628211ull;
+    h = (h ^ (unsigned long long)__double_as_longlong(a.w / piv)) * 1099511628211ull;
+    // final avalanche (the ratios of small integers have all-zero low mantissa bits, so the
+    // low bits of the raw product barely vary and would cluster the hash-table slots)
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
+    hkey[e] = h;
+  }
+  g.sync();
+  // twins: next entry of the row with the same oriented plane (equal keys compared exactly).
+  // Long rows first check for a repeated key with the row's hash table; without a repeat every
+  // entry has no twin.
+  bool maybe = true;
+  if (k > 64) {
+    int tsz = 1;
+    while (tsz < 2 * k) tsz <<= 1;
+    for (int q = lane; q < tsz; q += S) tab[q] = 0ull;
+    g.sync();
+    bool dup = false;
+    for (int32_t e = e0 + lane; e < e1; e += S) {
+      const unsigned long long h = hkey[e] | 1ull;
+      int slot = (int)(h & (unsigned long long)(tsz - 1));
+      while (true) {
+        const unsigned long long prev = atomicCAS(tab + slot, 0ull, h);
+        if (prev == 0ull) break;
+        if (prev == h) {
+          dup = true;
+          break;
+        }
+        slot = (slot + 1) & (tsz - 1);
+      }
+    }
+    maybe = g.any(dup);
+  }
+  for (int32_t e = e0 + lane; e < e1; e += S) {
+    int32_t tw = -1;
+    if (maybe) {
+      const unsigned long long h = hkey[e];
+      for (int32_t f = e + 1; f < e1 && tw < 0; f += 4) {
+        unsigned long long hf[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hf[q] = f + q < e1 ? hkey[f + q] : ~h;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (tw >= 0 || hf[q] != h) continue;
+          const double4 a = planes[e], b = planes[f + q];
+          const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
+                            a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
+                            a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
+          const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
+          if (prop && dot > 0.0) tw = f + q;
+        }
+      }
+    }
+    twin[e] = tw;
+  }
+}
+
+#ifndef RPD_STAGE_LONG
+#define RPD_STAGE_LONG 96  // rows longer than this that need building go to k_stage_long
+#endif
+constexpr int STAGE_LONG_THREADS = 256;
+constexpr int STAGE_LONG_TAB = 2048;  // shared hash slots of k_stage_long (rows up to 1024)
+
+// One group of RG lanes per sphere row (STAGE_RG): validation, ascending order, radical planes
+// and twins (stage_build).  In a partial update a row of an old sphere whose neighbour list is
+// unchanged is copied from the previous stage instead, and a long row that must be built is
+// deferred to k_stage_long (a block per row: its hash table in shared memory) when long_list
+// is given.
+#ifndef RPD_STAGE_MINB
+#define RPD_STAGE_MINB 1  // min resident blocks of k_stage_rows (a register cap; A/B knob)
+#endif
+template <int RG>
+__global__ void __launch_bounds__(256, RPD_STAGE_MINB) k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in,
                              int64_t N, int64_t E, const double4* __restrict__ sw,
                              int32_t* __restrict__ off_out, int32_t* __restrict__ idx_out,
                              double4* __restrict__ planes, int32_t* __restrict__ twin,
                              unsigned long long* __restrict__ hkey, int32_t* __restrict__ repoch,
                              int epoch, unsigned long long* __restrict__ htab, OldRows old,
-                             int* err, const PDyn* __restrict__ pd) {
+                             int* err, const PDyn* __restrict__ pd, int32_t* __restrict__ long_list,
+                             int* __restrict__ n_long) {
   if (pd) {  // device-driven update (see k_stage_spheres)
     off_in = pd->nbr_off;
     idx_in = pd->nbr_idx;
@@ -152,10 +303,6 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
   const unsigned FULL = (RG == 32 ? 0xffffffffu : ((1u << RG) - 1u))
                         << (RG * ((threadIdx.x & 31) / RG));  // this row's lanes
   if (i >= N) return;
-#ifdef RPD_DEBUG_STAGE
-  long long dbg_t[5];
-  dbg_t[0] = clock64();
-#endif
   const int32_t e0 = off_in[i], e1 = off_in[i + 1];
   // the previous stage's row bounds, loaded together with the new ones (partial updates)
   const bool has_old = old.off && i < old.N;
@@ -199,129 +346,50 @@ __global__ void k_stage_rows(const int32_t* __restrict__ off_in, const int32_t* 
       return;
     }
   }
-  if (lane == 0) repoch[i] = epoch;
-  bool bad = false;
-  for (int32_t e = e0 + lane; e < e1; e += RG) {
-    const int32_t j = idx_in[e];
-    if (j < 0 || j >= N) {
-      report(err, RPD_EINVAL, ERR_NBR_INDEX, i);
-      bad = true;
-      break;
-    }
-    if (j == i) {
-      report(err, RPD_EINVAL, ERR_NBR_SELF, i);
-      bad = true;
-      break;
-    }
-    if (sorted) {
-      idx_out[e] = j;
-      continue;
-    }
-    int rank = 0;
-    for (int32_t f = e0; f < e1; ++f) {
-      const int32_t x = idx_in[f];
-      if (x == j && f != e) {
-        report(err, RPD_EINVAL, ERR_NBR_DUP, i);
-        bad = true;
-      }
-      rank += x < j;
-    }
-    if (bad) break;
-    idx_out[e0 + rank] = j;
-  }
-  if (__any_sync(FULL, bad)) return;
-  __syncwarp(FULL);
-#ifdef RPD_DEBUG_STAGE
-  dbg_t[1] = clock64();
-#endif
-  const double4 si = sw[i];
-  // planes, and the twin key: bit patterns of the ratios to the first non-zero normal
-  // component (correctly rounded quotients of exactly proportional integers are equal)
-  for (int32_t e = e0 + lane; e < e1; e += RG) {
-    const int32_t j = idx_out[e];
-    const double4 sj = sw[j];
-    const double nx = 2.0 * (si.x - sj.x), ny = 2.0 * (si.y - sj.y), nz = 2.0 * (si.z - sj.z);
-    if (nx == 0.0 && ny == 0.0 && nz == 0.0) report(err, RPD_EINVAL, ERR_NBR_SAME_CENTRE, i);
-    const double4 a = make_double4(nx, ny, nz, sj.w - si.w);
-    planes[e] = a;
-    const double piv = fabs(a.x != 0.0 ? a.x : (a.y != 0.0 ? a.y : a.z));
-    const int which = a.x != 0.0 ? 0 : (a.y != 0.0 ? 1 : 2);
-    unsigned long long h = 1469598103934665603ull ^ (unsigned long long)which;
-    h = (h ^ (unsigned long long)__double_as_longlong(a.x / piv)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(a.y / piv)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(a.z / piv)) * 1099511628211ull;
-    h = (h ^ (unsigned long long)__double_as_longlong(a.w / piv)) * 1099511628211ull;
-    // final avalanche (the ratios of small integers have all-zero low mantissa bits, so the
-    // low bits of the raw product barely vary and would cluster the hash-table slots)
-    h ^= h >> 33;
-    h *= 0xff51afd7ed558ccdull;
-    h ^= h >> 33;
-    h *= 0xc4ceb9fe1a85ec53ull;
-    h ^= h >> 33;
-    hkey[e] = h;
-  }
-  __syncwarp(FULL);
-#ifdef RPD_DEBUG_STAGE
-  dbg_t[2] = clock64();
-#endif
-  // twins: next entry of the row with the same oriented plane (equal keys compared exactly).
-  // Long rows first check for a repeated key with a per-row hash table in global scratch
-  // (region [4 e0, 4 e0 + 4k)); without a repeat every entry has no twin.
-  bool maybe = true;
-  if (k > 64) {
-    int tsz = 1;
-    while (tsz < 2 * k) tsz <<= 1;
-    unsigned long long* tab = htab + 4 * (int64_t)e0;
-    for (int q = lane; q < tsz; q += RG) tab[q] = 0ull;
-    __syncwarp(FULL);
-    bool dup = false;
-    for (int32_t e = e0 + lane; e < e1; e += RG) {
-      const unsigned long long h = hkey[e] | 1ull;
-      int slot = (int)(h & (unsigned long long)(tsz - 1));
-      while (true) {
-        const unsigned long long prev = atomicCAS(tab + slot, 0ull, h);
-        if (prev == 0ull) break;
-        if (prev == h) {
-          dup = true;
-          break;
-        }
-        slot = (slot + 1) & (tsz - 1);
-      }
-    }
-    maybe = __any_sync(FULL, dup);
+  if (long_list && k > RPD_STAGE_LONG) {  // a long row to build: a block of its own
+    if (lane == 0) long_list[atomicAdd(n_long, 1)] = (int32_t)i;
+    return;
   }
 #ifdef RPD_DEBUG_STAGE
-  dbg_t[3] = clock64();
+  const long long t0 = clock64();
 #endif
-  for (int32_t e = e0 + lane; e < e1; e += RG) {
-    int32_t tw = -1;
-    if (maybe) {
-      const unsigned long long h = hkey[e];
-      for (int32_t f = e + 1; f < e1 && tw < 0; f += 4) {
-        unsigned long long hf[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) hf[q] = f + q < e1 ? hkey[f + q] : ~h;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (tw >= 0 || hf[q] != h) continue;
-          const double4 a = planes[e], b = planes[f + q];
-          const bool prop = a.x * b.y == a.y * b.x && a.x * b.z == a.z * b.x &&
-                            a.y * b.z == a.z * b.y && a.x * b.w == a.w * b.x &&
-                            a.y * b.w == a.w * b.y && a.z * b.w == a.w * b.z;
-          const double dot = a.x * b.x + a.y * b.y + a.z * b.z;
-          if (prop && dot > 0.0) tw = f + q;
-        }
-      }
-    }
-    twin[e] = tw;
-  }
+  stage_build(WarpRows<RG>{lane, FULL}, i, e0, e1, sorted, N, idx_in, sw, idx_out, planes, twin,
+              hkey, repoch, epoch, htab + 4 * (int64_t)e0, err);
 #ifdef RPD_DEBUG_STAGE
-  dbg_t[4] = clock64();
-  if (lane == 0 && dbg_t[4] - dbg_t[0] > 100000)
-    printf("stage row %lld k %d sorted %d maybe %d cycles sort %lld planes %lld hash %lld twins %lld\n",
-           (long long)i, k, (int)sorted, (int)maybe, dbg_t[1] - dbg_t[0], dbg_t[2] - dbg_t[1],
-           dbg_t[3] - dbg_t[2], dbg_t[4] - dbg_t[3]);
+  const long long dt = clock64() - t0;
+  if (lane == 0 && dt > RPD_DEBUG_STAGE_MIN)
+    printf("stage row %lld k %d sorted %d cycles %lld\n", (long long)i, k, (int)sorted, dt);
 #endif
+}
+
+// The deferred long rows of a partial update: a block per row (grid-stride over the list)
+__global__ void __launch_bounds__(STAGE_LONG_THREADS) k_stage_long(
+    const int32_t* __restrict__ off_in, const int32_t* __restrict__ idx_in, int64_t N,
+    const double4* __restrict__ sw, int32_t* __restrict__ idx_out, double4* __restrict__ planes,
+    int32_t* __restrict__ twin, unsigned long long* __restrict__ hkey,
+    int32_t* __restrict__ repoch, int epoch, unsigned long long* __restrict__ htab, int* err,
+    const PDyn* __restrict__ pd, const int32_t* __restrict__ long_list,
+    const int* __restrict__ n_long) {
+  __shared__ unsigned long long s_tab[STAGE_LONG_TAB];
+  if (pd) {
+    off_in = pd->nbr_off;
+    idx_in = pd->nbr_idx;
+    N = pd->N;
+    epoch = pd->epoch;
+  }
+  const int n = *n_long;
+  const BlockRows g{(int)threadIdx.x, (int)blockDim.x};
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    const int64_t i = long_list[q];
+    const int32_t e0 = off_in[i], e1 = off_in[i + 1];
+    bool sorted = true;
+    for (int32_t e = e0 + g.lane; e + 1 < e1; e += g.size) sorted &= idx_in[e] < idx_in[e + 1];
+    sorted = g.all(sorted);
+    unsigned long long* tab = 2 * (e1 - e0) <= STAGE_LONG_TAB ? s_tab : htab + 4 * (int64_t)e0;
+    stage_build(g, i, e0, e1, sorted, N, idx_in, sw, idx_out, planes, twin, hkey, repoch, epoch,
+                tab, err);
+    g.sync();  // (the shared table is reused by the next row)
+  }
 }
 
 #ifndef STAGE_RG
@@ -371,6 +439,7 @@ cudaError_t stage_prepare(rpd_ctx* c, int64_t N, int64_t E) {
   if ((e = s.hkey.ensure(sizeof(unsigned long long) * (E > 0 ? E : 1)))) return e;
   if ((e = s.repoch.ensure(sizeof(int32_t) * (N > 0 ? N : 1)))) return e;
   if ((e = s.htab.ensure(sizeof(unsigned long long) * 4 * (E > 0 ? E : 1)))) return e;
+  if ((e = s.long_rows.ensure(sizeof(int32_t) * (N + 2)))) return e;  // (list + its count)
   s.N = N;
   s.E = E;
   return cudaSuccess;
@@ -395,12 +464,31 @@ cudaError_t stage_launch(rpd_ctx* c, const double* spheres, const int32_t* nbr_o
         spheres, N, s.sw.as<double4>(), old.off ? s.old_sw.as<double4>() : nullptr, N_old, err,
         pd);
     ++c->launches;
+    // partial updates defer the long rows that must be built to a block each
+    int32_t* long_list = nullptr;
+    int* n_long = nullptr;
+    if (old.off) {
+      long_list = s.long_rows.as<int32_t>();
+      n_long = long_list + (s.long_rows.cap / sizeof(int32_t)) - 1;  // (count: the last word)
+      if (!pd) {  // (a graph: zeroed by k_pd_init)
+        cudaError_t e = cudaMemsetAsync(n_long, 0, sizeof(int), c->stream);
+        if (e) return e;
+      }
+    }
     k_stage_rows<STAGE_RG><<<nblk(STAGE_RG * Ng, 256), 256, 0, c->stream>>>(
         nbr_off, nbr_idx, N, E, s.sw.as<double4>(), s.nbr_off.as<int32_t>(),
         s.nbr_idx.as<int32_t>(), s.planes.as<double4>(), s.twin.as<int32_t>(),
         s.hkey.as<unsigned long long>(), s.repoch.as<int32_t>(), epoch,
-        s.htab.as<unsigned long long>(), old, err, pd);
+        s.htab.as<unsigned long long>(), old, err, pd, long_list, n_long);
     ++c->launches;
+    if (long_list) {
+      k_stage_long<<<c->sms, STAGE_LONG_THREADS, 0, c->stream>>>(
+          nbr_off, nbr_idx, N, s.sw.as<double4>(), s.nbr_idx.as<int32_t>(),
+          s.planes.as<double4>(), s.twin.as<int32_t>(), s.hkey.as<unsigned long long>(),
+          s.repoch.as<int32_t>(), epoch, s.htab.as<unsigned long long>(), err, pd, long_list,
+          n_long);
+      ++c->launches;
+    }
   } else {
     cudaError_t e = cudaMemsetAsync(s.nbr_off.p, 0, sizeof(int32_t), c->stream);
     if (e) return e;

@@ -63,7 +63,7 @@ for spec in sys.argv[2:]:
         e1.record()
         torch.cuda.synchronize()
         parts.append(e0.elapsed_time(e1))
-    if bat:   # second round (the first one allocates)
+    for rnd in range(2 if bat else 0):   # later rounds (the first allocates / captures)
         parts = []
         ctx.relations(*base)
         ctx.clip()
@@ -84,7 +84,7 @@ for spec in sys.argv[2:]:
             bad += ["partial:" + k for k in KEYS
                     if not np.array_equal(np.asarray(part[k]), np.asarray(ref_part[k]))]
         same = "SAME" if not bad else "DIFF " + ",".join(bad)
-    ps = f" partial {np.mean(parts):.3f} ms" if parts else ""
+    ps = f" partial {np.median(parts):.3f} ms (median)" if parts else ""
     print(f"{tag:12s} filter {np.median(fs):.3f} clip {np.median(cs):.3f} full {np.median(tot):.3f} ms"
           f"{ps}  pieces {len(full['piece_vol'])}  {same}", flush=True)
     ctx.close()

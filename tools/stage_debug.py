@@ -7,6 +7,7 @@ import numpy as np
 import torch
 import paper_2403_18761_b200._build as B
 B.NVCC_FLAGS.append("-DRPD_DEBUG_STAGE")
+B.NVCC_FLAGS.append("-DRPD_DEBUG_STAGE_MIN=" + os.environ.get("STAGE_MIN", "100000"))
 B.LIB = B.LIB.replace("librpd.so", "librpd_dbgstage.so")
 B.build(force=True)
 import paper_2403_18761_b200.rpd as R
