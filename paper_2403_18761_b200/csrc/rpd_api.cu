@@ -165,6 +165,8 @@ rpd_status rpd_create(rpd_ctx** out, int device, void* cuda_stream) {
     if (g && *g == '0') c->graph = 0;
     const char* n = getenv("RPD_GRAPH_NC_MAX");  // testing: a fixed batch bound
     if (n && *n) c->g_nc_fix = atoll(n);
+    const char* r = getenv("RPD_CLIP_ROUTE");  // graph clip routing threshold (cut planes)
+    if (r && *r) c->clip_route = atoi(r);
   }
   *out = c;
   return RPD_OK;
@@ -218,6 +220,9 @@ void rpd_destroy(rpd_ctx* c) {
   }
   graph_clear(c);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->g_fork) cudaEventDestroy(c->g_fork);
+  if (c->g_join) cudaEventDestroy(c->g_join);
   for (DevBuf* b : {&c->nb_buf, &c->nb_off, &c->nb_idx, &c->nb_tmp, &c->nb_cnt, &c->h_nb,
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
                     &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch,
@@ -1209,7 +1214,8 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
       {&c->p_scan, 4 * (size_t)(nc_max + 1)}, {&c->i_scan, 4 * (size_t)(nc_max + 1)},
       {&c->p_dyn, 4},                 {&c->m_cnt, 32},
       {&c->cand_long, 4 * (nt + 1)},  {&c->bvh, 8 * 6 * (size_t)(n_leaf + n_sup)},
-      {&c->g_scan, 8 * scan_words},   {&c->pd_buf, sizeof(PDyn)}};
+      {&c->g_scan, 8 * scan_words},   {&c->pd_buf, sizeof(PDyn)},
+      {&c->p_route, 4 * (2 + 2 * (size_t)nc_max)}};
   for (auto& x : need) CK(x.b->ensure(x.bytes), "alloc");
   if (!c->pd_host) {
     void* h = nullptr;
@@ -1263,7 +1269,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
         &pool_c.rows, &pool_c.idx, &pool_p.rows, &pool_p.sphere, &pool_p.vol, &pool_p.m1,
         &pool_p.fm, &pool_p.inc_off, &pool_p.inc, &c->pcs_d.off, &c->p_flag, &c->p_f01,
         &c->p_fm, &c->p_vol, &c->p_m1, &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2,
-        &c->p_over3, &c->p_scan, &c->i_scan, &c->p_dyn, &c->m_cnt};
+        &c->p_over3, &c->p_scan, &c->i_scan, &c->p_dyn, &c->m_cnt, &c->p_route};
     for (const DevBuf* b : bufs) mix((unsigned long long)(uintptr_t)b->p);
     for (unsigned long long v :
          {(unsigned long long)(S.sw.cap / sizeof(double4)), (unsigned long long)c->slab_cap,
@@ -1271,6 +1277,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
           (unsigned long long)c->dd_cap[0][1], (unsigned long long)c->dd_cap[1][0],
           (unsigned long long)c->dd_cap[1][1], (unsigned long long)c->sms,
           (unsigned long long)nc_max, (unsigned long long)Mb, (unsigned long long)c->profile,
+          (unsigned long long)c->clip_route,
           (unsigned long long)(uintptr_t)c->pinned_dev, (unsigned long long)(uintptr_t)c->pd_hdev})
       mix(v);
   }
@@ -1279,6 +1286,12 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
     if (c->g_exec[k] && c->g_sig[k] == sig) slot = k;
   if (slot < 0) {
     if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "stream");
+    if (!c->side_stream) {  // (the concurrent branch: clip routing)
+      CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking), "stream");
+      CK(cudaEventCreateWithFlags(&c->g_fork, cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&c->g_join, cudaEventDisableTiming), "event");
+    }
+    c->pdd_nc_max = nc_max;
     // (the capture is ordered after the work already queued on the ctx stream by the graph's
     // launch below, not by the capture itself: nothing is executed while capturing)
     cudaStream_t saved = c->stream;

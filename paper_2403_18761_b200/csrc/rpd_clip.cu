@@ -1338,7 +1338,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
                                  const int32_t* pair_tet, const int32_t* tet_ids,
                                  const int32_t* cand_idx, const int32_t* moff,
                                  const unsigned* cut, int32_t* over, const int32_t* n_dev,
-                                 int* dyn = nullptr) {
+                                 int* dyn = nullptr, int64_t grid_cap = 0) {
   constexpr int THREADS = VPL == 1 && GW == RPD_CLIP_GW ? RPD_CLIP_THREADS
                          : (VPL <= 2 ? 256 : (VPL <= 4 ? 64 : 32));
   constexpr int GROUPS = THREADS / GW;  // pairs in flight per block
@@ -1368,6 +1368,7 @@ static cudaError_t launch_clip_t(rpd_ctx* c, int64_t n, const int32_t* pair_list
   // the 128- and 256-slot tiers over an overflow list (a handful of pairs, often none; the
   // count is read on the device): one block per SM, so an empty launch costs little
   if (pair_list && VPL >= 4 && grid > sms) grid = sms;
+  if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
   if (grid < 1) grid = 1;
   PairOut o{c->p_vol.as<double>(),   c->p_m1.as<double>(),    c->p_flag.as<uint8_t>(),
             c->p_fm.as<uint8_t>(),   c->p_mask.as<unsigned>(), moff, cut,
@@ -1402,6 +1403,51 @@ static cudaError_t launch_clip_eu(rpd_ctx* c, int64_t n_pairs, const int32_t* pa
                                                       nullptr, c->p_dyn.as<int>());
 }
 
+// graph path: the fast tier's pairs split by their number of cut planes (cut-mask bits within
+// the row): more than `thresh` -> the big list (clipped by the 64-slot tier concurrently with
+// the fast tier), else the small list (warp-aggregated appends; order is irrelevant)
+__global__ void k_pair_route(const PDyn* __restrict__ pd, const int32_t* __restrict__ moff,
+                             const unsigned* __restrict__ cut, const int32_t* __restrict__ cand_idx,
+                             const int32_t* __restrict__ nbr_off, int thresh,
+                             int32_t* __restrict__ route) {
+  const int n = pd->nc_fast;
+  cand_idx += pd->fill_c;
+  int* n_small = route;
+  int* n_big = route + 1;
+  int32_t* small_list = route + 2;
+  int32_t* big_list = small_list + pd->nc_max;
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; p0 < n;
+       p0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = p0 + lane;
+    bool big = false;
+    if (p < n) {
+      const int i = cand_idx[p];
+      const int kp = nbr_off[i + 1] - nbr_off[i];
+      int pc = 0;
+      for (int w = moff[p], q = 0; w < moff[p + 1]; ++w, ++q) {
+        unsigned m = cut[w];
+        if (kp - 32 * q < 32) m &= (1u << (kp - 32 * q)) - 1u;
+        pc += __popc(m);
+      }
+      big = pc > thresh;
+    }
+    const unsigned bm = __ballot_sync(0xffffffffu, big && p < n);
+    const unsigned sm = __ballot_sync(0xffffffffu, !big && p < n);
+    int bb = 0, sb = 0;
+    if (lane == 0) {
+      if (bm) bb = atomicAdd(n_big, __popc(bm));
+      if (sm) sb = atomicAdd(n_small, __popc(sm));
+    }
+    bb = __shfl_sync(0xffffffffu, bb, 0);
+    sb = __shfl_sync(0xffffffffu, sb, 0);
+    if (p < n) {
+      if (big) big_list[bb + __popc(bm & ((1u << lane) - 1u))] = (int32_t)p;
+      else small_list[sb + __popc(sm & ((1u << lane) - 1u))] = (int32_t)p;
+    }
+  }
+}
+
 // fast kernel over all pairs (overflowing pairs are listed in p_over[1..], count p_over[0]),
 // or the widest kernel over all pairs when `wide`
 cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
@@ -1414,10 +1460,38 @@ cudaError_t launch_clip(rpd_ctx* c, int64_t n_pairs, const int32_t* pair_tet,
     // both entry tiers, and only the one the eager path would choose gets it (nc_fast /
     // nc_small, the other sees 0).  The fast tier's overflows go down the usual cascade.
     // (the pair counter p_dyn is zeroed by k_pd_init)
-    cudaError_t e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, nullptr, pair_tet,
-                                                        tet_ids, cand_idx, moff, cut,
-                                                        c->p_over.as<int32_t>(),
-                                                        &c->pdd->nc_fast, c->p_dyn.as<int>());
+    cudaError_t e;
+    if (c->clip_route > 0) {
+      // the pairs with many cut planes (the fast tier's likely overflows) clipped by the
+      // 64-slot tier in a concurrent branch of the graph, the others by the fast tier
+      int32_t* route = c->p_route.as<int32_t>();
+      const int32_t* small_list = route + 2;
+      const int32_t* big_list = small_list + c->pdd_nc_max;
+      k_pair_route<<<(unsigned)(c->sms * 4), 256, 0, c->stream>>>(
+          c->pdd, moff, cut, cand_idx, c->st.nbr_off.as<int32_t>(), c->clip_route, route);
+      ++c->launches;
+      if ((e = cudaEventRecord(c->g_fork, c->stream))) return e;
+      if ((e = cudaStreamWaitEvent(c->side_stream, c->g_fork, 0))) return e;
+      cudaStream_t main = c->stream;
+      c->stream = c->side_stream;
+      e = launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs, big_list, pair_tet, tet_ids,
+                                                     cand_idx, moff, cut, c->p_over2.as<int32_t>(),
+                                                     route + 1, nullptr, c->sms);
+      c->stream = main;
+      if (e) return e;
+      if ((e = cudaEventRecord(c->g_join, c->side_stream))) return e;
+      e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, small_list, pair_tet,
+                                                         tet_ids, cand_idx, moff, cut,
+                                                         c->p_over.as<int32_t>(), route,
+                                                         c->p_dyn.as<int>());
+      if (e) return e;
+      if ((e = cudaStreamWaitEvent(c->stream, c->g_join, 0))) return e;
+    } else {
+      e = launch_clip_t<RPD_CLIP_GW, RPD_CLIP_VPL, false>(c, n_pairs, nullptr, pair_tet, tet_ids,
+                                                         cand_idx, moff, cut,
+                                                         c->p_over.as<int32_t>(),
+                                                         &c->pdd->nc_fast, c->p_dyn.as<int>());
+    }
     if (e) return e;
     return launch_clip_t<32, RPD_CLIP_MID_VPL, false>(c, n_pairs < RPD_CLIP_SMALL ? n_pairs : RPD_CLIP_SMALL,
                                                       nullptr, pair_tet, tet_ids, cand_idx, moff,

@@ -266,6 +266,12 @@ struct rpd_ctx {
   int clip_wide = 0;           // testing: run every pair through the wide kernel
   int clip_small = 0;          // the last clip ran the 64-slot tier on all pairs (few pairs)
   int clip_tiers = 0;          // testing: always the fast tier + overflow cascade
+  int clip_route = 0;          // graph path: pairs with more cut planes than this go straight to
+                               // the 64-slot tier, concurrently with the fast tier (0: off)
+  rpd::DevBuf p_route;         // routed pair lists: [small count, big count, small.., big..]
+  cudaStream_t side_stream = nullptr;  // the concurrent branch of a captured graph
+  cudaEvent_t g_fork = nullptr, g_join = nullptr;
+  int64_t pdd_nc_max = 0;      // the batch bound of the graph being captured
 
   // fractional Euler characteristics (rpd_euler.cu; rpd_set_euler)
   int euler = 0;               // payloads set for the current tets

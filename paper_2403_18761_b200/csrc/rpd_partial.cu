@@ -144,6 +144,7 @@ struct PdZero {
   int* n_long;
   int* qhdr;
   int* n_stage_long;
+  int* route;  // the routed-pair counts (2)
   unsigned long long* rm;
   unsigned long long* scan_state;
   int64_t scan_words;
@@ -161,6 +162,7 @@ __global__ void k_pd_init(PDyn* __restrict__ pd, const PDyn* __restrict__ host, 
     *z.n_long = 0;
     z.qhdr[0] = z.qhdr[1] = 0;
     *z.n_stage_long = 0;
+    z.route[0] = z.route[1] = 0;
   }
   if (threadIdx.x < 4) {
     z.errw[threadIdx.x] = 0;
@@ -252,6 +254,7 @@ cudaError_t launch_pd_init(rpd_ctx* c) {
            c->cand_long.as<int>(),
            c->bvh_items.as<int>(),
            c->st.long_rows.as<int>() + (c->st.long_rows.cap / sizeof(int32_t)) - 1,
+           c->p_route.as<int>(),
            c->m_cnt.as<unsigned long long>(),
            c->g_scan.as<unsigned long long>(),
            (int64_t)(c->g_scan.cap / sizeof(unsigned long long))};

@@ -141,6 +141,29 @@ def test_graph_bench_sized_batches():
         ctx.close()
 
 
+@pytest.mark.parametrize("route", [4, 10])
+def test_graph_clip_routing(monkeypatch, route):
+    """RPD_CLIP_ROUTE: the graph sends the pairs with more cut planes than the threshold to the
+    64-slot tier in a concurrent branch; same state as the eager chain."""
+    import paper_2403_18761_b200 as P
+    w = W.make_shape_workload("Gr", 20000, 1500, seed=4, n_batches=3, batch_m=200, clusters=10,
+                              cache=False)
+    ctx = P.RPDContext(0, filter_mode="pruned")
+    try:
+        eager = _chain(ctx, w, graph=False)
+    finally:
+        ctx.close()
+    monkeypatch.setenv("RPD_CLIP_ROUTE", str(route))
+    ctx = P.RPDContext(0, filter_mode="pruned")
+    try:
+        graph = _chain(ctx, w, graph=True)
+        for g, e in zip(graph, eager):
+            _same(g, e)
+        assert ctx.stats()["graph_updates"] == len(w.batches)
+    finally:
+        ctx.close()
+
+
 def test_graph_errors_reset_ctx():
     """Input errors found inside the graph (new ids not the appended range, a moved old
     sphere) fail the call like the eager path and reset the ctx."""
