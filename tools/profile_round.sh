@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on -k regex:"k_clip" -c 2 \
     > gpurun_out/ncu_full_${TAG}.log 2>&1
 # the filter / stage / merge kernels of the first full RPD and first partial update
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_bvh_leaf|k_bvh_super|k_bvh_top|k_stage_rows|k_compact_cands_t|k_compact_pieces|k_rows_update|k_dirty_list|k_scan" -c 40 \
+    -k regex:"k_bvh_leaf|k_bvh_super|k_bvh_top|k_stage_rows|k_stage_long|k_compact_cands_t|k_compact_pieces|k_rows_update|k_scan|k_pd_" -c 48 \
     -o gpurun_out/prof_${TAG}_aux python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/ncu_aux_${TAG}.log 2>&1
 tail -c 600 gpurun_out/bench_${TAG}.json
