@@ -184,7 +184,7 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->st.old_twin, &c->st.old_hkey, &c->st.old_sw, &c->errw, &c->stats, &c->scratch, &c->k_tet, &c->k_words,
                     &c->slab, &c->slab_m, &c->w_off, &c->bvh, &c->bvh_all, &c->bvh_items, &c->p_flag, &c->p_f01, &c->p_vol, &c->p_m1, &c->p_fm,
                     &c->p_ninc, &c->p_mask, &c->p_over, &c->p_over2, &c->p_over3, &c->p_dyn, &c->p_scan, &c->i_scan, &c->d_count,
-                    &c->d_flag, &c->d_scan, &c->d_list, &c->d_pos, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
+                    &c->d_flag, &c->d_scan, &c->d_list, &c->m_cnt, &c->m_off, &c->c_scan, &c->c_list,
                     &c->st.repoch, &c->st.old_repoch, &c->st.htab, &c->c_flag, &c->cepoch,
                     &c->min_epoch, &c->eu_tab, &c->eu_rec, &c->eu_A, &c->eu_sum, &c->eu_Lt, &c->eu_acc, &c->eu_fin, &c->eu_den, &c->p_eu,
                     &c->p_rmask, &c->p_rval, &c->p_nrpf, &c->r_scan, &c->h_eut, &c->h_euid,
@@ -225,7 +225,7 @@ void rpd_destroy(rpd_ctx* c) {
   if (c->g_join) cudaEventDestroy(c->g_join);
   for (DevBuf* b : {&c->nb_buf, &c->nb_off, &c->nb_idx, &c->nb_tmp, &c->nb_cnt, &c->h_nb,
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
-                    &c->nb_len, &c->nb_misc, &c->d_pos, &c->bvh_items, &c->min_epoch,
+                    &c->nb_len, &c->nb_misc, &c->bvh_items, &c->min_epoch,
                     &c->nb_ball, &c->eu_ids, &c->eu_g2l, &c->cc_bnd, &c->cc_gpar, &c->cc_sort,
                     &c->cc_nrec, &c->st.long_rows})
     b->release();
@@ -884,7 +884,6 @@ static rpd_status update_partial_impl(rpd_ctx* c, const double* spheres, int64_t
   CK(c->d_count.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
   CK(c->d_flag.ensure(T > 0 ? T : 1), "alloc");
   CK(c->d_scan.ensure(sizeof(int32_t) * (T + 1)), "alloc");
-  CK(c->d_pos.ensure(sizeof(int32_t) * (T > 0 ? T : 1)), "alloc");
   if (c->profile) cudaEventRecord(c->ev[0], c->stream);
   CK(launch_filter(c, nullptr, T, 0, (int)N_old, (int)N_new, c->d_count.as<int32_t>(), nullptr,
                    nullptr), "dirty filter");
@@ -1198,7 +1197,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
     size_t bytes;
   } need[] = {
       {&c->d_count, 4 * nt},          {&c->d_flag, nt},
-      {&c->d_scan, 4 * (nt + 1)},     {&c->d_pos, 4 * nt},
+      {&c->d_scan, 4 * (nt + 1)},
       {&c->min_epoch, 4},             {&c->c_flag, (size_t)Nb},
       {&c->c_scan, 4 * (size_t)(Nb + 1)}, {&c->c_list, 4 * (size_t)Nb},
       {&c->k_tet, 4 * nt},            {&c->k_words, 4 * nt},
@@ -1263,7 +1262,7 @@ static rpd_status partial_graph(rpd_ctx* c, const double* spheres, int64_t N_new
         &S.nbr_idx, &S.old_idx, &S.planes, &S.old_planes, &S.twin, &S.old_twin, &S.hkey,
         &S.old_hkey, &S.repoch, &S.old_repoch, &S.htab, &S.long_rows, &c->bvh_all, &c->bvh,
         &c->bvh_items,
-        &c->d_count, &c->d_flag, &c->d_scan, &c->d_pos, &c->d_list, &c->cepoch, &c->min_epoch,
+        &c->d_count, &c->d_flag, &c->d_scan, &c->d_list, &c->cepoch, &c->min_epoch,
         &c->c_flag, &c->c_scan, &c->c_list, &c->g_scan, &c->k_tet, &c->k_words, &c->slab,
         &c->slab_m, &cd.off, &cd.pair_tet, &cd.moff, &cd.cut, &c->w_off, &c->cand_long,
         &pool_c.rows, &pool_c.idx, &pool_p.rows, &pool_p.sphere, &pool_p.vol, &pool_p.m1,

@@ -224,7 +224,7 @@ struct rpd_ctx {
   rpd::DevBuf p_dyn;  // dynamic pair counter of the fast clip kernel
 
   // partial update scratch
-  rpd::DevBuf d_count, d_flag, d_scan, d_list, d_pos, m_cnt, m_off;
+  rpd::DevBuf d_count, d_flag, d_scan, d_list, m_cnt, m_off;
   rpd::DevBuf c_flag, c_scan, c_list;  // changed-row spheres of a partial update
   rpd::DevBuf cepoch;          // int32 per tet: epoch of its candidate list
   rpd::DevBuf min_epoch;       // int32: oldest candidate-list epoch among the dirty tets

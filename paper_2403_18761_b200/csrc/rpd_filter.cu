@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_super(
 
 // phase 3: one warp per (sphere, leaf) item: the remaining planes on the leaf box, then the
 // exact Alg. 1 (lane = tet)
-__global__ void __launch_bounds__(BVH_WARPS * 32) k_bvh_leaf(
+#ifndef RPD_BVH_LEAF_MINB
+#define RPD_BVH_LEAF_MINB 1  // min resident blocks of k_bvh_leaf (a register cap; A/B knob)
+#endif
+__global__ void __launch_bounds__(BVH_WARPS * 32, RPD_BVH_LEAF_MINB) k_bvh_leaf(
     const double* __restrict__ tx, int64_t T, const int32_t* __restrict__ tet_ids, int64_t n,
     const double* __restrict__ leaf, int64_t n_leaf, const int32_t* __restrict__ nbr_off,
     const double4* __restrict__ planes, const int2* __restrict__ items,

@@ -39,7 +39,7 @@ cudaError_t launch_check_new_ids(rpd_ctx* c, const int32_t* new_ids, int64_t M, 
   return cudaGetLastError();
 }
 
-// d_count (filter counts over the new spheres) -> d_list, d_pos, d_scan[T] = count, cepoch
+// d_count (filter counts over the new spheres) -> d_list, d_scan[T] = count, cepoch
 // re-stamped, min_epoch: one fused scan (rpd_scan.cu)
 cudaError_t launch_dirty_list(rpd_ctx* c, int64_t T) {
   if (T == 0) return cudaMemsetAsync(c->d_scan.p, 0, sizeof(int32_t), c->stream);

@@ -217,12 +217,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_op(Op op, int64_t n, int 
 }
 
 // dirty tets (partial update): flag = the tet relates to a new sphere (count > 0); the list
-// (ascending), the position map, the oldest candidate-list epoch of the dirty tets (whose
+// (ascending), the oldest candidate-list epoch of the dirty tets (whose
 // lists are re-stamped with the current epoch), the count at scan_out[T] (and in pd)
 struct DirtyOp {
   const int32_t* count;
   int32_t* list;
-  int32_t* pos;
   int32_t* cepoch;
   int* min_epoch;
   int epoch;
@@ -238,11 +237,8 @@ struct DirtyOp {
   __device__ void emit(int64_t t, int p, int f, Acc& acc) const {
     if (f) {
       list[p] = (int32_t)t;
-      pos[t] = p;
       acc = min(acc, cepoch[t]);
       cepoch[t] = epoch;
-    } else {
-      pos[t] = -1;
     }
   }
   __device__ void flush(Acc acc) const {
@@ -340,7 +336,7 @@ cudaError_t launch_flag_list(rpd_ctx* c, const uint8_t* flag, int64_t n, int32_t
 
 cudaError_t launch_dirty_scan(rpd_ctx* c, int64_t T) {
   PDyn* pd = c->pdd;
-  DirtyOp op{c->d_count.as<int32_t>(), c->d_list.as<int32_t>(), c->d_pos.as<int32_t>(),
+  DirtyOp op{c->d_count.as<int32_t>(), c->d_list.as<int32_t>(),
              c->cepoch.as<int32_t>(), c->min_epoch.as<int>(), c->epoch,
              c->d_scan.as<int32_t>(), pd, pd ? c->bvh_items.as<int>() : nullptr};
   return scan_op_impl(c, op, T, nullptr);
