@@ -152,8 +152,8 @@ class ShardedRPD:
         """The exchange after a partial update of every shard: the dirty tets' segments with
         their global ids, merged into the global CSR; returns (global CSR, total dirty)."""
         ctx = self.ctx
-        st = ctx.stats()
-        counts = (nd, st["n_cand_dirty"], st["n_pieces_dirty"], st["n_inc_dirty"])
+        st = ctx.stats_struct()  # (a ctypes struct: no dict on the timed path)
+        counts = (nd, st.n_cand_dirty, st.n_pieces_dirty, st.n_inc_dirty)
 
         def fill(v):
             ctx.download_tets(ctx.dirty_ptr(), nd, v, id_map=self.ids_dev)
