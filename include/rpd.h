@@ -434,6 +434,12 @@ rpd_status rpd_merge_shards(rpd_ctx* ctx, const rpd_shards* dirty, const rpd_csr
  * id).  RPD_EINVAL: a listed tet outside [0, T_local); RPD_ESTATE before rpd_clip. */
 rpd_status rpd_download_tets(rpd_ctx* ctx, const int32_t* tet_list, int64_t n,
                              const int32_t* id_map, int32_t* ids_out, rpd_csr* out);
+/* Validation aggregate of a sharded job (SURVEY.md §8(e) "per-sphere RPC volume ... all_reduce
+ * sum"): out [N] (host or device, caller-owned) = the volume of every sphere's restricted power
+ * cell over the ctx's tets, i.e. the sum of its pieces' volumes (fp64 atomics: the summation
+ * order, hence the last bits, may vary between runs); a sharded job all-reduces the ranks'
+ * vectors.  RPD_ESTATE before rpd_clip. */
+rpd_status rpd_sphere_volumes(rpd_ctx* ctx, double* out);
 
 /* ---- Envelope distance (Sec. 4.3)
  *

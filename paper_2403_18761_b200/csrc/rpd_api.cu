@@ -1940,6 +1940,25 @@ static rpd_status download_rows(rpd_ctx* c, int kind, const int32_t* d_list, int
 
 extern "C" {
 
+rpd_status rpd_sphere_volumes(rpd_ctx* c, double* out) {
+  if (!c || !out) return fail(c, RPD_EINVAL, "rpd_sphere_volumes: bad argument");
+  if (!c->have_pieces) return fail(c, RPD_ESTATE, "rpd_sphere_volumes before rpd_clip");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  const int64_t N = c->st.N;
+  const bool host = is_host_ptr(out);
+  double* d = out;
+  if (host) {
+    CK(c->g_dst.ensure(sizeof(double) * (N > 0 ? N : 1)), "alloc");
+    d = c->g_dst.as<double>();
+  }
+  CK(launch_sphere_volumes(c, d), "sphere volumes");
+  if (host) {
+    CK(cudaMemcpyAsync(out, d, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream), "download");
+    CK(cudaStreamSynchronize(c->stream), "download");
+  }
+  return RPD_OK;
+}
+
 rpd_status rpd_download_tets(rpd_ctx* c, const int32_t* tet_list, int64_t n,
                              const int32_t* id_map, int32_t* ids_out, rpd_csr* out) {
   if (!c) return RPD_EINVAL;

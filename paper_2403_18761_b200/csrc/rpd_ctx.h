@@ -426,6 +426,8 @@ cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, Can
 // device-driven partial update (rpd_graph): PDyn init from the pinned mirror, the checks
 // after the re-filter (batch totals, capacities; abort), the totals back to the mirror
 cudaError_t launch_pd_init(rpd_ctx* c);
+// per-sphere RPC volumes of the current pieces into out [N] (device)
+cudaError_t launch_sphere_volumes(rpd_ctx* c, double* out);
 cudaError_t launch_pd_check(rpd_ctx* c, const int32_t* c_off, const int32_t* w_off);
 cudaError_t launch_pd_final(rpd_ctx* c);
 cudaError_t launch_pd_stamp(rpd_ctx* c, int k);

@@ -128,6 +128,30 @@ cudaError_t launch_rows_update(rpd_ctx* c, const int32_t* dirty, int64_t nd, Can
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- validation aggregates
+
+// per-sphere RPC volume: every tet's piece slots (state rows) added to their spheres
+__global__ void k_sphere_vol(int64_t T, const int2* __restrict__ prow,
+                             const int32_t* __restrict__ psph, const double* __restrict__ pvol,
+                             double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int2 r = prow[t];
+    for (int q = r.x; q < r.y; ++q) atomicAdd(out + psph[q], pvol[q]);
+  }
+}
+
+cudaError_t launch_sphere_volumes(rpd_ctx* c, double* out) {
+  const PieceSet& ps = c->pcs[c->cur];
+  const int64_t T = c->st.T, N = c->st.N;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double) * (N > 0 ? N : 1), c->stream);
+  if (e || T == 0) return e;
+  k_sphere_vol<<<nblk(T, 256), 256, 0, c->stream>>>(T, ps.rows.as<int2>(), ps.sphere.as<int32_t>(),
+                                                    ps.vol.as<double>(), out);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- device-driven updates
 
 // the inputs of this update from the mapped pinned mirror; the outputs cleared; and every

@@ -224,6 +224,14 @@ def cc_sharded(ctx, group=None) -> dict:
     return {"rpc_cc": counts[:N], "rpf_cc": counts[N:N + E]}
 
 
+def sphere_volumes(ctx, group=None):
+    """Per-sphere RPC volume of the whole job (SURVEY.md §8(e) validation aggregate): every
+    rank's vector (rpd_sphere_volumes over its tets) summed by one all-reduce."""
+    v = ctx.sphere_volumes(device=True)
+    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+    return v
+
+
 def allreduce_euler(local: dict, ctx, group=None) -> dict:
     """Per-sphere fractional Euler sums of the whole job (SURVEY.md §8(e) "validation
     aggregates"): every rank's exact accumulator rows rpc_acc [N, 1+P] and rpf_acc [E, 1+P]

@@ -31,7 +31,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
             "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-            "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge"]
+            "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes"]
 
 
 class RPDError(RuntimeError):
@@ -161,6 +161,7 @@ def load_library(path: str = LIB_PATH):
     L.rpd_neighbors.argtypes = [vp, vp, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_neighbors_update.argtypes = [vp, vp, i64, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_cc_shard.argtypes = [vp, i64, i64, C.POINTER(_CcRecords)]
+    L.rpd_sphere_volumes.argtypes = [vp, vp]
     L.rpd_cc_merge.argtypes = [vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, vp]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
@@ -178,7 +179,7 @@ def load_library(path: str = LIB_PATH):
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
               "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-              "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge"):
+              "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -425,6 +426,12 @@ class RPDContext:
                torch.empty(n, dtype=torch.float64, device=dev))
         self._check(self.L.rpd_euler_finalize(self.h, self._p(acc), n, self._p(out[0]),
                                               self._p(out[1]), self._p(out[2])))
+        return out
+
+    def sphere_volumes(self, device=False):
+        """Per-sphere RPC volume over the ctx's tets (fp64 [N]; rpd_sphere_volumes)."""
+        (out,) = self._alloc([(int(self.N), np.float64)], device)
+        self._check(self.L.rpd_sphere_volumes(self.h, self._p(out)))
         return out
 
     def euler_sizes(self):

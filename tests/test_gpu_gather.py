@@ -200,3 +200,61 @@ def test_gather_c5_two_ranks_equals_single_gpu():
             assert torch.equal(got[k].reshape(ref[k].shape), ref[k]), k
     finally:
         ctx.close()
+
+
+def test_sphere_volumes_shards_sum_to_whole():
+    """The validation aggregate of a sharded job: per-sphere RPC volumes of
+    the shards (rpd_sphere_volumes) add up to the single ctx's and to the oracle's piece
+    volumes summed per sphere (to 1e-12 of the mesh volume: fp64 sums in another order); also
+    after partial updates (state pools) and through dist.sphere_volumes on NCCL world 1."""
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2403_18761_b200 as P
+    from paper_2403_18761_b200.dist import free_port, shard_tets, sphere_volumes
+    w = W.make_shape_workload("Sv", 3000, 250, seed=9, n_batches=2, batch_m=20, clusters=4,
+                              cache=False)
+    ref = oracle.rpd_workload(w)
+    want = np.bincount(np.asarray(ref["piece_sphere"]), weights=np.asarray(ref["piece_vol"]),
+                       minlength=w.N)
+    Vt = w.verts[w.tets]
+    tol = 1e-12 * np.abs(np.linalg.det(np.stack([Vt[:, k] - Vt[:, 0] for k in (1, 2, 3)],
+                                                axis=1))).sum() / 6
+    ctxs = [P.RPDContext(0, filter_mode="pruned") for _ in range(3)]
+    try:
+        whole = ctxs[0]
+        whole.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        whole.clip()
+        got = whole.sphere_volumes()
+        assert np.max(np.abs(got - want)) <= tol
+        parts = []
+        for r, c in enumerate(ctxs[1:]):
+            ids = shard_tets(w.T, 2, r, 256)
+            c.relations(w.verts, w.tets[ids], w.spheres, w.nbr_off, w.nbr_idx)
+            c.clip()
+            parts.append(c.sphere_volumes())
+        assert np.max(np.abs(parts[0] + parts[1] - want)) <= tol
+        # after the partial updates (pools): still the whole mesh's per-sphere volumes
+        n_old, prev = w.N, ref
+        for (sph, off, idx) in w.batches:
+            new = np.arange(n_old, len(sph), dtype=np.int32)
+            whole.update_partial(sph, off, idx, new)
+            prev, _ = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old)
+            n_old = len(sph)
+        want2 = np.bincount(np.asarray(prev["piece_sphere"]),
+                            weights=np.asarray(prev["piece_vol"]), minlength=n_old)
+        assert np.max(np.abs(whole.sphere_volumes() - want2)) <= tol
+    finally:
+        for c in ctxs:
+            c.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    c = P.RPDContext(0, filter_mode="pruned")
+    try:
+        c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        c.clip()
+        v = sphere_volumes(c)
+        assert np.max(np.abs(v.cpu().numpy() - want)) <= tol
+    finally:
+        c.close()
+        dist.destroy_process_group()
