@@ -43,6 +43,15 @@ def workload_name(cfg):
     return WORKLOADS.get(cfg, cfg)
 
 
+def bench_config(args, w, world):
+    """The line's `config` (both arms: the reference arm runs the same workload)."""
+    batches = w.batches if args.partial_iters < 0 else w.batches[:args.partial_iters]
+    return {"workload": workload_name(args.config), "config": args.config, "T": w.T, "N": w.N,
+            "partial_iters": len(batches), "M": (len(batches[0][0]) - w.N) if batches else 0,
+            "filter": args.filter, "parallelism": f"tet-shard x{world}",
+            "l2": "flushed (256 MB write) before every timed step"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -177,8 +186,8 @@ def run_reference(args):
     line = {"metric": "tet-sphere pairs clipped/s", "value": value, "unit": "pairs/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "config": {"workload": workload_name(args.config), "config": args.config},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": bench_config(args, w, max(world, 1)),
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
@@ -754,11 +763,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(args.config), "config": args.config, "T": w.T,
-                   "N": w.N, "partial_iters": len(d_batches),
-                   "M": (len(batches[0][0]) - w.N) if batches else 0,
-                   "filter": args.filter, "parallelism": f"tet-shard x{world}",
-                   "l2": "flushed (256 MB write) before every timed step"},
+        "config": bench_config(args, w, world),
         "full_rpd_ms": breakdown["full"]["total"], "filter_ms": fmed, "clip_ms": cmed,
         "pairs_filtered_per_s": float(recs[0]["counters"]["pairs_filtered"]) * world /
         (fmed * 1e-3),
