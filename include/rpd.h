@@ -536,6 +536,11 @@ rpd_status rpd_get_stats(rpd_ctx* ctx, rpd_stats* out);
 /* Library version string. */
 const char* rpd_version(void);
 
+/* Debugging aid (env RPD_CANARY=1 at the first allocation: every library buffer carries a
+ * 256-byte canary past its capacity): RPD_ECUDA if any live buffer's canary was overwritten
+ * (a write past its end), after synchronising the device; RPD_OK otherwise or when off. */
+rpd_status rpd_debug_check(rpd_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,41 @@ using namespace rpd;
 
 #define RPD_VERSION "rpd-b200 0.1 (sm_100a)"
 
+#include <mutex>
+#include <set>
+
+namespace rpd {
+bool canary_on() {
+  static const bool on = [] {
+    const char* v = getenv("RPD_CANARY");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+static std::mutex& canary_mu() {
+  static std::mutex m;
+  return m;
+}
+static std::set<DevBuf*>& canary_set() {
+  static std::set<DevBuf*>* s = new std::set<DevBuf*>();  // (never destroyed: exit order)
+  return *s;
+}
+void canary_register(DevBuf* b) {
+  std::lock_guard<std::mutex> g(canary_mu());
+  canary_set().insert(b);
+}
+void canary_unregister(DevBuf* b) {
+  std::lock_guard<std::mutex> g(canary_mu());
+  canary_set().erase(b);
+}
+__global__ void k_canary(const unsigned char* const* __restrict__ tails, int n,
+                         int* __restrict__ bad) {
+  for (int q = blockIdx.x; q < n; q += gridDim.x)
+    for (int k = threadIdx.x; k < (int)CANARY_BYTES; k += blockDim.x)
+      if (tails[q][k] != 0xA5) atomicCAS(bad, -1, q);
+}
+}  // namespace rpd
+
 namespace {
 
 rpd_status fail(rpd_ctx* c, rpd_status s, const std::string& msg) {
@@ -2257,6 +2292,41 @@ rpd_status rpd_download_cands(rpd_ctx* c, int32_t* cand_off, int32_t* cand_idx) 
                        c->stream), "download");
   if (is_host_ptr(cand_off) || is_host_ptr(cand_idx))
     CK(cudaStreamSynchronize(c->stream), "download");
+  return RPD_OK;
+}
+
+rpd_status rpd_debug_check(rpd_ctx* c) {
+  if (!c) return RPD_EINVAL;
+  if (!canary_on()) return RPD_OK;
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(cudaDeviceSynchronize(), "debug check");
+  std::vector<const unsigned char*> tails;
+  std::vector<size_t> caps;
+  {
+    std::lock_guard<std::mutex> g(canary_mu());
+    for (DevBuf* b : canary_set())
+      if (b->p) {
+        tails.push_back(static_cast<const unsigned char*>(b->p) + b->cap);
+        caps.push_back(b->cap);
+      }
+  }
+  if (tails.empty()) return RPD_OK;
+  const unsigned char** d_tails = nullptr;
+  int* d_bad = nullptr;
+  CK(cudaMalloc(&d_tails, sizeof(void*) * tails.size()), "debug check");
+  CK(cudaMalloc(&d_bad, sizeof(int)), "debug check");
+  CK(cudaMemcpy(d_tails, tails.data(), sizeof(void*) * tails.size(), cudaMemcpyHostToDevice),
+     "debug check");
+  CK(cudaMemset(d_bad, 0xff, sizeof(int)), "debug check");
+  k_canary<<<256, 256>>>(d_tails, (int)tails.size(), d_bad);
+  int bad = -1;
+  cudaError_t e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d_tails);
+  cudaFree(d_bad);
+  CK(e, "debug check");
+  if (bad >= 0)
+    return fail(c, RPD_ECUDA, "debug check: a write past the end of a " +
+                                  std::to_string(caps[bad]) + "-byte library buffer");
   return RPD_OK;
 }
 

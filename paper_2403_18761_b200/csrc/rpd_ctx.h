@@ -11,18 +11,41 @@
 
 namespace rpd {
 
+// Debug builds of the test runs (env RPD_CANARY=1; a stand-in for compute-sanitizer, which is
+// closed on this GPU pool): every buffer gets a 256-byte canary past its capacity, and
+// rpd_debug_check verifies all live canaries (a write past the end of any ctx buffer).
+constexpr size_t CANARY_BYTES = 256;
+bool canary_on();
+struct DevBuf;
+void canary_register(DevBuf* b);
+void canary_unregister(DevBuf* b);
+
 // Growable ctx-owned device buffer.
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = default;
+  DevBuf& operator=(const DevBuf&) = default;
+  ~DevBuf() {
+    if (canary_on()) canary_unregister(this);
+  }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap && p) return cudaSuccess;
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
     size_t want = bytes < 256 ? 256 : bytes + bytes / 8;
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) cap = want;
+    const bool can = canary_on();
+    cudaError_t e = cudaMalloc(&p, want + (can ? CANARY_BYTES : 0));
+    if (e == cudaSuccess) {
+      cap = want;
+      if (can) {  // (debug only: synchronous)
+        e = cudaMemset(static_cast<char*>(p) + want, 0xA5, CANARY_BYTES);
+        if (!e) e = cudaDeviceSynchronize();
+        canary_register(this);
+      }
+    }
     return e;
   }
   // like ensure, but a (re)allocation reserves `factor` x bytes (pools that grow by appends)
@@ -34,6 +57,7 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
+    if (canary_on()) canary_unregister(this);
   }
   template <class T>
   T* as() const { return reinterpret_cast<T*>(p); }

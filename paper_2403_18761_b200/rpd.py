@@ -31,7 +31,8 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_medial_mesh", "rpd_download_medial_mesh", "rpd_gather_pieces", "rpd_envelope",
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
             "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-            "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes"]
+            "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes",
+            "rpd_debug_check"]
 
 
 class RPDError(RuntimeError):
@@ -162,6 +163,7 @@ def load_library(path: str = LIB_PATH):
     L.rpd_neighbors_update.argtypes = [vp, vp, i64, i64, vp, C.POINTER(_NbrLists)]
     L.rpd_cc_shard.argtypes = [vp, i64, i64, C.POINTER(_CcRecords)]
     L.rpd_sphere_volumes.argtypes = [vp, vp]
+    L.rpd_debug_check.argtypes = [vp]
     L.rpd_cc_merge.argtypes = [vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, vp]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
@@ -179,7 +181,8 @@ def load_library(path: str = LIB_PATH):
               "rpd_gather_pieces", "rpd_envelope", "rpd_neighbors",
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
               "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
-              "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes"):
+              "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes",
+              "rpd_debug_check"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -243,9 +246,15 @@ class RPDContext:
         self.n_cand = 0
         self.counts = None
 
+    _CANARY = os.environ.get("RPD_CANARY", "0") not in ("", "0")
+
     def _check(self, st):
         if st != 0:
             raise RPDError(st, self.L.rpd_last_error(self.h).decode())
+        if self._CANARY and self.h:  # debugging: every buffer's canary after every call
+            st = self.L.rpd_debug_check(self.h)
+            if st != 0:
+                raise RPDError(st, self.L.rpd_last_error(self.h).decode())
 
     def set_filter_mode(self, mode: str):
         m = {"all_pairs": FILTER_ALL_PAIRS, "pruned": FILTER_PRUNED}[mode]
