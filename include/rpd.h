@@ -306,6 +306,36 @@ rpd_status rpd_cc_shard(rpd_ctx* ctx, int64_t piece_base, int64_t rpf_base, rpd_
 rpd_status rpd_cc_merge(rpd_ctx* ctx, const uint64_t* key_c, const int32_t* lab_c, int64_t n_c,
                         const uint64_t* key_f, const int32_t* j_f, const int32_t* lab_f,
                         int64_t n_f, int64_t total_pieces, int64_t total_rpf, int32_t* counts);
+
+/* Restricted power edges of a tet-SHARDED job: the per-(i, j, k) Euler
+ * characteristics and CC numbers of the whole mesh from the ranks' shards, by the same
+ * distributed union-find (DESIGN.md §10 "CC numbers of a sharded job").
+ * rpd_rpe_shard: the rank's RPEs (as rpd_get_rpe: per-piece lists and per-key sums over its
+ *   tets) joined across its interior faces; out (ctx-owned device arrays): tri_key / tri_euler
+ *   [n_tri] -- the keys (i << 42 | j << 21 | k) ascending and their Euler numerators over 2 on
+ *   this rank's tets -- and the records of its shard-boundary faces: key_b (f << 21 | i), jk_b
+ *   (j << 21 | k), lab_b (rpe_base + the smallest local index of the part's component).
+ *   rpe_base: the lower ranks' n_rpe (out->n_rpe).
+ * rpd_rpe_merge: the records of ALL ranks (device) -> this rank's component counts per key at
+ *   the components' smallest global ids: keys / counts [n] (ctx-owned device arrays).
+ * rpd_reduce_by_key: the sums of vals per key, keys ascending (device arrays; out_* sized n
+ *   by the caller; *n_out host) -- the ranks' concatenated (tri_key, tri_euler) lists give the
+ *   whole mesh's Euler numerators, their (keys, counts) lists its CC numbers.  N < 2^21. */
+typedef struct {
+  const uint64_t* tri_key;
+  const int64_t* tri_euler;
+  int64_t n_tri, n_rpe;
+  const uint64_t* key_b;
+  const uint64_t* jk_b;
+  const int32_t* lab_b;
+  int64_t n_b;
+} rpd_rpe_records;
+rpd_status rpd_rpe_shard(rpd_ctx* ctx, int64_t rpe_base, rpd_rpe_records* out);
+rpd_status rpd_rpe_merge(rpd_ctx* ctx, const uint64_t* key_b, const uint64_t* jk_b,
+                         const int32_t* lab_b, int64_t n_b, int64_t total_rpe,
+                         const uint64_t** keys, const int64_t** counts, int64_t* n);
+rpd_status rpd_reduce_by_key(rpd_ctx* ctx, const uint64_t* keys, const int64_t* vals, int64_t n,
+                             uint64_t* out_keys, int64_t* out_vals, int64_t* n_out);
 /* Copy (host or device destinations; any pointer may be NULL). */
 rpd_status rpd_download_topology(rpd_ctx* ctx, int32_t* rpc_cc, int32_t* rpf_cc,
                                  int32_t* piece_comp, int32_t* rpf_comp, uint8_t* piece_sosfm,

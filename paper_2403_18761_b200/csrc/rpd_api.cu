@@ -262,7 +262,8 @@ void rpd_destroy(rpd_ctx* c) {
                     &c->nb_hits, &c->nb_prev, &c->nb_off2, &c->nb_idx2, &c->nb_flag, &c->nb_list,
                     &c->nb_len, &c->nb_misc, &c->bvh_items, &c->min_epoch,
                     &c->nb_ball, &c->eu_ids, &c->eu_g2l, &c->cc_bnd, &c->cc_gpar, &c->cc_sort,
-                    &c->cc_nrec, &c->st.long_rows})
+                    &c->cc_nrec, &c->st.long_rows, &c->p_route, &c->rpe_bnd, &c->rpe_cnt,
+                    &c->rk_buf, &c->rk_out})
     b->release();
   if (c->pd_host) cudaFreeHost(c->pd_host);
   for (DevBuf* b : {&c->pd_buf, &c->g_scan, &c->st.nbr_off, &c->st.nbr_idx, &c->st.planes,
@@ -1677,6 +1678,84 @@ rpd_status rpd_cc_merge(rpd_ctx* c, const uint64_t* key_c, const int32_t* lab_c,
                      total_pieces, total_rpf, c->cc_base_c, c->cc_base_f, counts),
      "cc merge");
   CK(cudaStreamSynchronize(c->stream), "cc merge");
+  return RPD_OK;
+}
+
+rpd_status rpd_rpe_shard(rpd_ctx* c, int64_t rpe_base, rpd_rpe_records* out) {
+  if (!c || !out || rpe_base < 0) return fail(c, RPD_EINVAL, "rpd_rpe_shard: bad argument");
+  if (!c->euler || !c->eu_valid || !c->have_pieces)
+    return fail(c, RPD_ESTATE, "no topology data (rpd_set_euler, then rpd_clip)");
+  if (c->eu_whole)
+    return fail(c, RPD_ESTATE, "rpd_rpe_shard: the ctx holds the whole mesh (rpd_get_rpe)");
+  if (c->st.N >= (1 << 21)) return fail(c, RPD_EINVAL, "RPE keys need N < 2^21");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(c->cc_nrec.ensure(sizeof(int) * 2), "alloc");
+  int* n_rec = c->cc_nrec.as<int>();
+  int64_t n = 0, nu = 0;
+  CK(launch_rpe_shard(c, c->pcs[c->cur], rpe_base, n_rec, &n, &nu), "rpe shard");
+  if (rpe_base + n > 0x7fffffff) return fail(c, RPD_EINVAL, "rpd_rpe_shard: ids beyond int32");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{n_rec}, nullptr, nullptr}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "rpe shard");
+  c->rpe_n = n;
+  c->rpe_nu = nu;
+  c->rpe_base = rpe_base;
+  const int64_t n1 = n > 0 ? n : 1, nb = 4 * n1;
+  const unsigned long long* keys = c->rpe_buf.as<unsigned long long>();
+  const unsigned long long* key_b = c->rpe_bnd.as<unsigned long long>();
+  *out = rpd_rpe_records{reinterpret_cast<const uint64_t*>(keys + 4 * n1),
+                         reinterpret_cast<const int64_t*>(keys + 5 * n1), nu, n,
+                         reinterpret_cast<const uint64_t*>(key_b),
+                         reinterpret_cast<const uint64_t*>(key_b + nb),
+                         reinterpret_cast<const int32_t*>(key_b + 2 * nb), rb->i32[0]};
+  return RPD_OK;
+}
+
+rpd_status rpd_rpe_merge(rpd_ctx* c, const uint64_t* key_b, const uint64_t* jk_b,
+                         const int32_t* lab_b, int64_t n_b, int64_t total_rpe,
+                         const uint64_t** keys, const int64_t** counts, int64_t* n) {
+  if (!c || n_b < 0 || (n_b > 0 && (!key_b || !jk_b || !lab_b)) || !keys || !counts || !n ||
+      total_rpe < 0 || total_rpe > 0x7ffffffe || n_b > 0x7fffffff)
+    return fail(c, RPD_EINVAL, "rpd_rpe_merge: bad argument");
+  if (c->rpe_base < 0 || c->rpe_n < 0)
+    return fail(c, RPD_ESTATE, "rpd_rpe_merge before rpd_rpe_shard");
+  if (c->rpe_base + c->rpe_n > total_rpe)
+    return fail(c, RPD_EINVAL, "rpd_rpe_merge: total smaller than this rank's range");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(c->cc_nrec.ensure(sizeof(int) * 2), "alloc");
+  int* n_out = c->cc_nrec.as<int>();
+  CK(launch_rpe_merge(c, reinterpret_cast<const unsigned long long*>(key_b),
+                      reinterpret_cast<const unsigned long long*>(jk_b), lab_b, n_b, total_rpe,
+                      c->rpe_base, n_out),
+     "rpe merge");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{n_out}, nullptr, nullptr}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "rpe merge");
+  const int64_t n1 = c->rpe_n > 0 ? c->rpe_n : 1;
+  const unsigned long long* rk = c->rpe_cnt.as<unsigned long long>();
+  *keys = reinterpret_cast<const uint64_t*>(rk + 2 * n1);
+  *counts = reinterpret_cast<const int64_t*>(rk + 3 * n1);
+  *n = rb->i32[0];
+  return RPD_OK;
+}
+
+rpd_status rpd_reduce_by_key(rpd_ctx* c, const uint64_t* keys, const int64_t* vals, int64_t n,
+                             uint64_t* out_keys, int64_t* out_vals, int64_t* n_out) {
+  if (!c || n < 0 || n > 0x7fffffff || (n > 0 && (!keys || !vals || !out_keys || !out_vals)) ||
+      !n_out)
+    return fail(c, RPD_EINVAL, "rpd_reduce_by_key: bad argument");
+  CK(cudaSetDevice(c->device), "cudaSetDevice");
+  CK(c->cc_nrec.ensure(sizeof(int) * 2), "alloc");
+  int* d_n = c->cc_nrec.as<int>();
+  CK(launch_reduce_by_key(c, reinterpret_cast<const unsigned long long*>(keys),
+                          reinterpret_cast<const long long*>(vals), n,
+                          reinterpret_cast<unsigned long long*>(out_keys),
+                          reinterpret_cast<long long*>(out_vals), d_n),
+     "reduce by key");
+  Readback* rb = (Readback*)c->pinned;
+  CK(readback(c, RbSpec{{d_n}, nullptr, nullptr}), "readback");
+  CK(cudaStreamSynchronize(c->stream), "reduce by key");
+  *n_out = rb->i32[0];
   return RPD_OK;
 }
 

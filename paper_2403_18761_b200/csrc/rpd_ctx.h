@@ -326,6 +326,8 @@ struct rpd_ctx {
   rpd::DevBuf eu_ids, eu_g2l;  // sharded Euler mode: local -> global tet ids and back (-1: remote)
   rpd::DevBuf cc_bnd, cc_gpar, cc_sort, cc_nrec;  // CC of a sharded job: records, global parents
   int64_t cc_base_c = -1, cc_base_f = -1;  // this rank's global id bases (rpd_cc_shard)
+  rpd::DevBuf rpe_bnd, rpe_cnt, rk_buf, rk_out;  // RPEs of a sharded job; reduce-by-key
+  int64_t rpe_base = -1;
   // sphere neighbours (NEXT-3): scratch (grid, pass-1 rows), outputs (off, idx), pass-2 rows
   rpd::DevBuf nb_buf, nb_off, nb_idx, nb_tmp, nb_cnt, h_nb, nb_hits;
   void* nb_grid = nullptr;
@@ -519,6 +521,15 @@ cudaError_t launch_cc(rpd_ctx* c, const PieceSet& ps);
 cudaError_t launch_g2l(rpd_ctx* c, const int32_t* local_ids, int64_t T_local, int64_t T_all);
 cudaError_t launch_cc_shard(rpd_ctx* c, const PieceSet& ps, long long base_c, long long base_f,
                             int* n_rec);
+// RPEs of a sharded job (rpd_rpe_shard / rpd_rpe_merge) and the generic key reduction
+cudaError_t launch_rpe_shard(rpd_ctx* c, const PieceSet& ps, long long base, int* n_rec,
+                             int64_t* n_rpe, int64_t* n_tri);
+cudaError_t launch_rpe_merge(rpd_ctx* c, const unsigned long long* key_b,
+                             const unsigned long long* jk_b, const int32_t* lab_b, int64_t n_b,
+                             int64_t total, long long base, int* n_out);
+cudaError_t launch_reduce_by_key(rpd_ctx* c, const unsigned long long* keys, const long long* vals,
+                                 int64_t n, unsigned long long* out_k, long long* out_v,
+                                 int* n_out);
 cudaError_t launch_cc_merge(rpd_ctx* c, const PieceSet& ps, const unsigned long long* key_c,
                             const int32_t* lab_c, int64_t n_c, const unsigned long long* key_f,
                             const int32_t* j_f, const int32_t* lab_f, int64_t n_f,

@@ -1239,4 +1239,204 @@ cudaError_t launch_rpe(rpd_ctx* c, const PieceSet& ps, bool with_cc, int64_t* n_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- RPEs of a sharded job
+//
+// As the CC numbers of RPCs / RPFs (rpd_cc_shard / rpd_cc_merge): the rank's RPE parts joined
+// across its interior faces (k_rpe_link through the global -> local tet map), records of its
+// shard-boundary faces, a global union-find over the gathered records, and per rank the
+// components whose smallest global id it holds, counted per (i, j, k); the ranks' per-key
+// lists (Euler numerators, component counts) are summed by key (rpd_reduce_by_key).
+
+__global__ void k_rpe_link_sh(int64_t T, const int* __restrict__ adj,
+                              const int32_t* __restrict__ g2l, const int32_t* __restrict__ poff,
+                              const int32_t* __restrict__ psph, const int32_t* __restrict__ eoff,
+                              const int32_t* __restrict__ ej, const int32_t* __restrict__ ek,
+                              const uint8_t* __restrict__ efm, int* __restrict__ par) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  for (int f = 0; f < 4; ++f) {
+    const int nb = adj[4 * t + f];
+    if (nb < 0) continue;
+    const int t2 = g2l[nb >> 2], f2 = nb & 3;
+    if (t2 < 0 || t2 < t) continue;  // remote, or this face from the other side
+    const int q0 = poff[t2], q1 = poff[t2 + 1];
+    for (int q = p0; q < p1; ++q) {
+      const int q2 = find_sorted(psph, q0, q1, psph[q]);
+      if (q2 < 0) continue;
+      for (int m = eoff[q]; m < eoff[q + 1]; ++m) {
+        if (!((efm[m] >> f) & 1)) continue;
+        const int m2 = rpe_find(ej, ek, eoff[q2], eoff[q2 + 1], ej[m], ek[m]);
+        if (m2 >= 0 && ((efm[m2] >> f2) & 1)) uf_union(par, m, m2);
+      }
+    }
+  }
+}
+
+// records of the RPE parts with an endpoint on a shard-boundary face: key (f << 21 | i), the
+// pair (j << 21 | k), label = global id of the local root
+__global__ void k_rpe_bnd(int64_t T, const int32_t* __restrict__ local_ids,
+                          const int* __restrict__ adj, const int32_t* __restrict__ g2l,
+                          const int32_t* __restrict__ poff, const int32_t* __restrict__ psph,
+                          const int32_t* __restrict__ eoff, const int32_t* __restrict__ ej,
+                          const int32_t* __restrict__ ek, const uint8_t* __restrict__ efm,
+                          int* __restrict__ par, long long base,
+                          unsigned long long* __restrict__ key_b,
+                          unsigned long long* __restrict__ jk_b, int32_t* __restrict__ lab_b,
+                          int* __restrict__ n_rec) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int p0 = poff[t], p1 = poff[t + 1];
+  const long long tg = local_ids[t];
+  for (int f = 0; f < 4; ++f) {
+    const int nb = adj[4 * t + f];
+    if (nb < 0 || g2l[nb >> 2] >= 0) continue;
+    const unsigned long long fid = (unsigned long long)min(4 * tg + f, (long long)nb);
+    for (int q = p0; q < p1; ++q)
+      for (int m = eoff[q]; m < eoff[q + 1]; ++m) {
+        if (!((efm[m] >> f) & 1)) continue;
+        const int s = atomicAdd(n_rec, 1);
+        key_b[s] = (fid << 21) | (unsigned long long)psph[q];
+        jk_b[s] = ((unsigned long long)ej[m] << 21) | (unsigned long long)ek[m];
+        lab_b[s] = (int32_t)(base + uf_find(par, m));
+      }
+  }
+}
+
+// sorted boundary records (value = record index): equal key and pair -> join
+__global__ void k_rpe_join(int64_t n, const unsigned long long* __restrict__ key,
+                           const int32_t* __restrict__ idx, const unsigned long long* __restrict__ jk,
+                           const int32_t* __restrict__ lab, int* __restrict__ par) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int a = idx[p];
+    for (int64_t q = p + 1; q < n && key[q] == key[p]; ++q) {
+      const int b = idx[q];
+      if (jk[a] == jk[b]) uf_union(par, lab[a], lab[b]);
+    }
+  }
+}
+
+// this rank's RPE parts that are local and global roots: (triple key, 1) pairs (0 elsewhere)
+__global__ void k_rpe_roots(int64_t n, const unsigned long long* __restrict__ keys,
+                            int* __restrict__ lpar, int* __restrict__ gpar, long long base,
+                            unsigned long long* __restrict__ out_k, long long* __restrict__ out_v) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const bool root = uf_find(lpar, (int)m) == m && uf_find(gpar, (int)(base + m)) == base + m;
+  out_k[m] = keys[m];
+  out_v[m] = root ? 1 : 0;
+}
+
+// sum of vals per key, keys ascending (CUB radix sort + reduce-by-key); *n_out on the device
+cudaError_t launch_reduce_by_key(rpd_ctx* c, const unsigned long long* keys, const long long* vals,
+                                 int64_t n, unsigned long long* out_k, long long* out_v,
+                                 int* n_out) {
+  cudaError_t e;
+  if (n <= 0) return cudaMemsetAsync(n_out, 0, sizeof(int), c->stream);
+  if ((e = c->rk_buf.ensure(16 * (size_t)n + 64))) return e;
+  unsigned long long* sk = c->rk_buf.as<unsigned long long>();
+  long long* sv = reinterpret_cast<long long*>(sk + n);
+  size_t b1 = 0, b2 = 0;
+  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, b1, keys, sk, vals, sv, (int)n, 0, 64,
+                                           c->stream)))
+    return e;
+  if ((e = cub::DeviceReduce::ReduceByKey(nullptr, b2, sk, out_k, sv, out_v, n_out,
+                                          cuda::std::plus<long long>(), (int)n, c->stream)))
+    return e;
+  if ((e = c->mm_tmp.ensure((b1 > b2 ? b1 : b2) + 16))) return e;
+  size_t bt = c->mm_tmp.cap;
+  if ((e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bt, keys, sk, vals, sv, (int)n, 0, 64,
+                                           c->stream)))
+    return e;
+  bt = c->mm_tmp.cap;
+  if ((e = cub::DeviceReduce::ReduceByKey(c->mm_tmp.p, bt, sk, out_k, sv, out_v, n_out,
+                                          cuda::std::plus<long long>(), (int)n, c->stream)))
+    return e;
+  c->launches += 2;
+  return cudaGetLastError();
+}
+
+// rpd_rpe_shard: launch_rpe (per-piece lists, per-key sums) + local union + boundary records
+// into c->rpe_bnd (count at n_rec on the device)
+cudaError_t launch_rpe_shard(rpd_ctx* c, const PieceSet& ps, long long base, int* n_rec,
+                             int64_t* n_rpe, int64_t* n_tri) {
+  cudaError_t e = launch_rpe(c, ps, false, n_rpe, n_tri);
+  if (e) return e;
+  const int64_t n = *n_rpe, n1 = n > 0 ? n : 1, T = ps.n_tets, np = ps.n_pieces;
+  unsigned long long* keys = c->rpe_buf.as<unsigned long long>();
+  int32_t* ej = reinterpret_cast<int32_t*>(keys + 6 * n1);
+  int32_t* ek = ej + n1;
+  int32_t* par = ek + n1 + n1 + 3 * n1;  // (layout of launch_rpe)
+  uint8_t* efm = reinterpret_cast<uint8_t*>(par + n1);
+  const int32_t* eoff = c->rpe_off.as<int32_t>();
+  const size_t nb = 4 * (size_t)n1;  // at most 2 endpoint faces per part, each on <= 2 faces
+  if ((e = c->rpe_bnd.ensure(nb * 20 + 64))) return e;
+  unsigned long long* key_b = c->rpe_bnd.as<unsigned long long>();
+  unsigned long long* jk_b = key_b + nb;
+  int32_t* lab_b = reinterpret_cast<int32_t*>(jk_b + nb);
+  if ((e = cudaMemsetAsync(n_rec, 0, sizeof(int), c->stream))) return e;
+  if (n > 0) {
+    k_cc_init<<<nblk(n, 256), 256, 0, c->stream>>>(n, par);
+    ++c->launches;
+  }
+  if (T > 0 && np > 0 && n > 0) {
+    k_rpe_link_sh<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, c->eu_adj.as<int>(), c->eu_g2l.as<int32_t>(), ps.off.as<int32_t>(),
+        ps.sphere.as<int32_t>(), eoff, ej, ek, efm, par);
+    k_rpe_bnd<<<nblk(T, 128), 128, 0, c->stream>>>(
+        T, c->eu_ids.as<int32_t>(), c->eu_adj.as<int>(), c->eu_g2l.as<int32_t>(),
+        ps.off.as<int32_t>(), ps.sphere.as<int32_t>(), eoff, ej, ek, efm, par, base, key_b,
+        jk_b, lab_b, n_rec);
+    c->launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+// rpd_rpe_merge: the gathered records -> global union -> this rank's (key, count) of its
+// global-root parts, reduced by key into c->rpe_cnt (keys [.], counts [.], *n_out on device)
+cudaError_t launch_rpe_merge(rpd_ctx* c, const unsigned long long* key_b,
+                             const unsigned long long* jk_b, const int32_t* lab_b, int64_t n_b,
+                             int64_t total, long long base, int* n_out) {
+  const int64_t n = c->rpe_n, n1 = n > 0 ? n : 1, nb1 = n_b > 0 ? n_b : 1;
+  cudaError_t e;
+  if ((e = c->cc_gpar.ensure(sizeof(int) * (total + 1)))) return e;
+  if ((e = c->cc_sort.ensure(nb1 * 16 + 64))) return e;
+  int* gpar = c->cc_gpar.as<int>();
+  unsigned long long* sk = c->cc_sort.as<unsigned long long>();
+  int32_t* ix = reinterpret_cast<int32_t*>(sk + nb1);
+  int32_t* six = ix + nb1;
+  const int g = 8 * c->sms;
+  k_cc_init_range<<<g, 256, 0, c->stream>>>(total, gpar);
+  ++c->launches;
+  if (n_b > 0) {
+    k_cc_init_range<<<g, 256, 0, c->stream>>>(n_b, ix);
+    size_t b1 = 0;
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, b1, key_b, sk, ix, six, (int)n_b, 0, 64,
+                                             c->stream)))
+      return e;
+    if ((e = c->mm_tmp.ensure(b1 + 16))) return e;
+    size_t bt = c->mm_tmp.cap;
+    if ((e = cub::DeviceRadixSort::SortPairs(c->mm_tmp.p, bt, key_b, sk, ix, six, (int)n_b, 0,
+                                             64, c->stream)))
+      return e;
+    k_rpe_join<<<g, 256, 0, c->stream>>>(n_b, sk, six, jk_b, lab_b, gpar);
+    c->launches += 3;
+  }
+  // this rank's root parts per triple key
+  unsigned long long* keys = c->rpe_buf.as<unsigned long long>();
+  int32_t* ej = reinterpret_cast<int32_t*>(keys + 6 * n1);
+  int32_t* lpar = ej + n1 + n1 + n1 + 3 * n1;
+  if ((e = c->rpe_cnt.ensure(32 * (size_t)n1 + 64))) return e;
+  unsigned long long* rk = c->rpe_cnt.as<unsigned long long>();
+  long long* rv = reinterpret_cast<long long*>(rk + n1);
+  unsigned long long* ok = rk + 2 * n1;
+  long long* ov = reinterpret_cast<long long*>(rk + 3 * n1);
+  if (n > 0) {
+    k_rpe_roots<<<nblk(n, 256), 256, 0, c->stream>>>(n, keys, lpar, gpar, base, rk, rv);
+    ++c->launches;
+  }
+  return launch_reduce_by_key(c, rk, rv, n, ok, ov, n_out);
+}
+
 }  // namespace rpd

@@ -224,6 +224,35 @@ def cc_sharded(ctx, group=None) -> dict:
     return {"rpc_cc": counts[:N], "rpf_cc": counts[N:N + E]}
 
 
+def rpe_sharded(ctx, group=None) -> dict:
+    """Restricted power edges of a tet-sharded job: every (i, j, k)
+    with its Euler characteristic (numerator over 2) and CC number over the whole mesh.  The
+    ranks' n_rpe give global id bases; each rank's per-key Euler numerators and shard-boundary
+    records (rpd_rpe_shard) are all-gathered (one packed all-gather each); the Euler numerators
+    and the ranks' component counts (rpd_rpe_merge over all records) are summed per key
+    (rpd_reduce_by_key).  Returns tri [n][3], tri_euler [n], tri_cc [n] (CUDA tensors, keys
+    ascending, identical on every rank)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = torch.device("cuda", ctx.device)
+    rec = ctx.rpe_shard(0)  # (sizes first; the base is applied by a second call below)
+    n = torch.tensor([rec["n_rpe"]], dtype=torch.int64, device=dev)
+    alln = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(alln, n, group=group)
+    alln = alln.cpu().numpy()
+    base = int(alln[:rank].sum())
+    if base:
+        rec = ctx.rpe_shard(base)
+    eu = gather_records({"k": rec["tri_key"], "v": rec["tri_euler"]}, dev, group)
+    keys, euler = ctx.reduce_by_key(eu["k"], eu["v"])
+    allb = gather_records({k: rec[k] for k in ("key_b", "jk_b", "lab_b")}, dev, group)
+    ck, cv = ctx.rpe_merge(allb, int(alln.sum()))
+    cc = gather_records({"k": ck.clone(), "v": cv.clone()}, dev, group)
+    ckeys, counts = ctx.reduce_by_key(cc["k"], cc["v"])
+    assert torch.equal(ckeys, keys), "every (i, j, k) has one component root"
+    tri = torch.stack([keys >> 42, (keys >> 21) & 0x1FFFFF, keys & 0x1FFFFF], 1).to(torch.int32)
+    return {"tri": tri, "tri_euler": euler, "tri_cc": counts}
+
+
 def sphere_volumes(ctx, group=None):
     """Per-sphere RPC volume of the whole job (SURVEY.md §8(e) validation aggregate): every
     rank's vector (rpd_sphere_volumes over its tets) summed by one all-reduce."""

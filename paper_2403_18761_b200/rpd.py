@@ -32,7 +32,7 @@ EXPORTED = ["rpd_create", "rpd_destroy", "rpd_last_error", "rpd_set_option", "rp
             "rpd_neighbors", "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
             "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
             "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes",
-            "rpd_debug_check"]
+            "rpd_debug_check", "rpd_rpe_shard", "rpd_rpe_merge", "rpd_reduce_by_key"]
 
 
 class RPDError(RuntimeError):
@@ -70,6 +70,12 @@ class _CcRecords(C.Structure):
     _fields_ = [("key_c", C.c_void_p), ("lab_c", C.c_void_p), ("n_c", C.c_int64),
                 ("key_f", C.c_void_p), ("j_f", C.c_void_p), ("lab_f", C.c_void_p),
                 ("n_f", C.c_int64), ("n_pieces", C.c_int64), ("n_rpf", C.c_int64)]
+
+
+class _RpeRecords(C.Structure):
+    _fields_ = [("tri_key", C.c_void_p), ("tri_euler", C.c_void_p), ("n_tri", C.c_int64),
+                ("n_rpe", C.c_int64), ("key_b", C.c_void_p), ("jk_b", C.c_void_p),
+                ("lab_b", C.c_void_p), ("n_b", C.c_int64)]
 
 
 class _Rpe(C.Structure):
@@ -164,6 +170,10 @@ def load_library(path: str = LIB_PATH):
     L.rpd_cc_shard.argtypes = [vp, i64, i64, C.POINTER(_CcRecords)]
     L.rpd_sphere_volumes.argtypes = [vp, vp]
     L.rpd_debug_check.argtypes = [vp]
+    L.rpd_rpe_shard.argtypes = [vp, i64, C.POINTER(_RpeRecords)]
+    L.rpd_rpe_merge.argtypes = [vp, vp, vp, vp, i64, i64, C.POINTER(C.c_void_p),
+                                C.POINTER(C.c_void_p), C.POINTER(i64)]
+    L.rpd_reduce_by_key.argtypes = [vp, vp, vp, i64, vp, vp, C.POINTER(i64)]
     L.rpd_cc_merge.argtypes = [vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, vp]
     L.rpd_download_neighbors.argtypes = [vp, vp, vp]
     L.rpd_gather_pieces.argtypes = [vp, C.POINTER(_Shards)] + [vp] * 7
@@ -182,7 +192,7 @@ def load_library(path: str = LIB_PATH):
               "rpd_download_neighbors", "rpd_gather_cands", "rpd_merge_shards",
               "rpd_download_tets", "rpd_get_rpe", "rpd_download_rpe", "rpd_euler_finalize",
               "rpd_neighbors_update", "rpd_cc_shard", "rpd_cc_merge", "rpd_sphere_volumes",
-              "rpd_debug_check"):
+              "rpd_debug_check", "rpd_rpe_shard", "rpd_rpe_merge", "rpd_reduce_by_key"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -442,6 +452,40 @@ class RPDContext:
         (out,) = self._alloc([(int(self.N), np.float64)], device)
         self._check(self.L.rpd_sphere_volumes(self.h, self._p(out)))
         return out
+
+    def rpe_shard(self, rpe_base: int) -> dict:
+        """RPEs of a sharded job, step 1 (rpd_rpe_shard): this rank's per-key Euler numerators
+        (tri_key, tri_euler; over 2) and its shard-boundary records, as torch CUDA views of
+        ctx-owned arrays (uint64 keys as int64); n_rpe sizes the next rank's base."""
+        r = _RpeRecords()
+        self._check(self.L.rpd_rpe_shard(self.h, int(rpe_base), C.byref(r)))
+        return {"tri_key": _device_view(r.tri_key, r.n_tri, "<i8"),
+                "tri_euler": _device_view(r.tri_euler, r.n_tri, "<i8"),
+                "key_b": _device_view(r.key_b, r.n_b, "<i8"),
+                "jk_b": _device_view(r.jk_b, r.n_b, "<i8"),
+                "lab_b": _device_view(r.lab_b, r.n_b, "<i4"), "n_rpe": int(r.n_rpe)}
+
+    def rpe_merge(self, rec: dict, total_rpe: int):
+        """Step 2 (rpd_rpe_merge): all ranks' boundary records -> this rank's (keys, counts)
+        of RPE components at their smallest global ids (torch CUDA views)."""
+        kb, jb, lb = (rec[k].contiguous() for k in ("key_b", "jk_b", "lab_b"))
+        pk, pc, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        self._check(self.L.rpd_rpe_merge(self.h, self._p(kb), self._p(jb), self._p(lb),
+                                         int(kb.numel()), int(total_rpe), C.byref(pk),
+                                         C.byref(pc), C.byref(n)))
+        return _device_view(pk.value, n.value, "<i8"), _device_view(pc.value, n.value, "<i8")
+
+    def reduce_by_key(self, keys, vals):
+        """Sums of vals per key, keys ascending (rpd_reduce_by_key; int64 CUDA tensors)."""
+        import torch
+        keys, vals = keys.contiguous(), vals.to(torch.int64).contiguous()
+        n = int(keys.numel())
+        ok = torch.empty(max(n, 1), dtype=torch.int64, device=keys.device)
+        ov = torch.empty(max(n, 1), dtype=torch.int64, device=keys.device)
+        m = C.c_int64()
+        self._check(self.L.rpd_reduce_by_key(self.h, self._p(keys), self._p(vals), n,
+                                             self._p(ok), self._p(ov), C.byref(m)))
+        return ok[:m.value], ov[:m.value]
 
     def euler_sizes(self):
         """(n_pieces, n_rpf, N, E) of the current pieces in Euler mode."""

@@ -143,3 +143,108 @@ def test_cc_shard_state_errors():
         assert e.value.status == -5
     finally:
         c.close()
+
+
+RPE_KEYS = ("key_b", "jk_b", "lab_b")
+
+
+def sharded_rpe(w, world, block):
+    """RPEs of the sharded job on simulated ranks (dist.rpe_sharded's protocol without the
+    collectives): (tri [n][3], tri_euler [n], tri_cc [n]) as numpy."""
+    import torch
+    import paper_2403_18761_b200 as P
+    ctxs = [P.RPDContext(0, filter_mode="pruned") for _ in range(world)]
+    try:
+        for r, c in enumerate(ctxs):
+            ids = W.block_cyclic_shard(w.T, world, r, block=block).astype(np.int32)
+            c.set_euler(w.tets, len(w.verts), ids)
+            c.relations(w.verts, w.tets[ids], w.spheres, w.nbr_off, w.nbr_idx)
+            c.clip()
+        n_rpe = [c.rpe_shard(0)["n_rpe"] for c in ctxs]
+        recs = []
+        for r, c in enumerate(ctxs):
+            rec = c.rpe_shard(int(sum(n_rpe[:r])))
+            recs.append({k: v.clone() if torch.is_tensor(v) else v for k, v in rec.items()})
+        cat = lambda k: torch.cat([x[k] for x in recs])
+        keys, euler = ctxs[0].reduce_by_key(cat("tri_key"), cat("tri_euler"))
+        allb = {k: cat(k) for k in RPE_KEYS}
+        parts = [tuple(t.clone() for t in c.rpe_merge(allb, sum(n_rpe))) for c in ctxs]
+        ck, cc = ctxs[0].reduce_by_key(torch.cat([p[0] for p in parts]),
+                                       torch.cat([p[1] for p in parts]))
+        assert torch.equal(ck, keys)
+        k = keys.cpu().numpy()
+        tri = np.stack([k >> 42, (k >> 21) & 0x1FFFFF, k & 0x1FFFFF], 1).astype(np.int32)
+        return tri, euler.cpu().numpy(), cc.cpu().numpy(), sum(int(x["key_b"].numel())
+                                                               for x in recs)
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def whole_rpe(w):
+    import paper_2403_18761_b200 as P
+    c = P.RPDContext(0, filter_mode="pruned")
+    try:
+        c.set_euler(w.tets, len(w.verts))
+        c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        c.clip()
+        return c.rpe()
+    finally:
+        c.close()
+
+
+def rpe_crossing_the_hole():
+    """Three spheres whose common line crosses the genus-1 solid twice (Euler 2, CC 2)."""
+    w = copy.copy(W.make_shape_workload("one", 700, 1, seed=2, cache=False))
+    w.spheres = np.array([[32.0, 32.0, 20.0, 1.0], [32.0, 20.0, 20.0, 1.0],
+                          [32.0, 26.0, 26.0, 1.0]])
+    w.nbr_off = np.array([0, 2, 4, 6], np.int32)
+    w.nbr_idx = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    return w
+
+
+RPE_MAKERS = [lambda: W.make_shape_workload("E3", 2000, 150, seed=3, cache=False),
+              lambda: W.make_shape_workload("E5", 3000, 300, seed=5,
+                                            radius_mode="high_variance", cache=False),
+              lambda: W.delaunay_workload(2000, 60, seed=1), rpe_crossing_the_hole]
+
+
+@pytest.mark.parametrize("k", range(len(RPE_MAKERS)))
+@pytest.mark.parametrize("world,block", [(2, 64), (3, 32)])
+def test_rpe_sharded_equals_whole(k, world, block):
+    """Per-(i, j, k) RPE Euler characteristics and CC numbers of a sharded job equal those of
+    the ctx holding the whole mesh (whose RPEs are pinned against the oracle's explicit
+    extraction in tests/test_gpu_euler.py)."""
+    w = RPE_MAKERS[k]()
+    tri, euler, cc, n_bnd = sharded_rpe(w, world, block)
+    ref = whole_rpe(w)
+    assert np.array_equal(tri, ref["tri"])
+    assert np.array_equal(euler, ref["tri_euler"])
+    assert np.array_equal(cc, ref["tri_cc"])
+    if k == len(RPE_MAKERS) - 1:
+        assert cc.tolist() == [2, 2, 2] and n_bnd > 0
+
+
+def test_rpe_sharded_nccl_world1():
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2403_18761_b200 as P
+    from paper_2403_18761_b200.dist import free_port, rpe_sharded
+    w = W.make_shape_workload("E3", 2000, 150, seed=3, cache=False)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    c = P.RPDContext(0, filter_mode="pruned")
+    try:
+        ids = np.arange(w.T, dtype=np.int32)
+        c.set_euler(w.tets, len(w.verts), ids)
+        c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        c.clip()
+        got = rpe_sharded(c)
+        ref = whole_rpe(w)
+        assert np.array_equal(got["tri"].cpu().numpy(), ref["tri"])
+        assert np.array_equal(got["tri_euler"].cpu().numpy(), ref["tri_euler"])
+        assert np.array_equal(got["tri_cc"].cpu().numpy(), ref["tri_cc"])
+    finally:
+        c.close()
+        dist.destroy_process_group()
