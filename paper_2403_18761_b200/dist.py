@@ -253,6 +253,23 @@ def rpe_sharded(ctx, group=None) -> dict:
     return {"tri": tri, "tri_euler": euler, "tri_cc": counts}
 
 
+def medial_mesh_sharded(ctx, group=None) -> dict:
+    """The dual medial mesh of a tet-sharded job: every rank's edges and
+    triangles (rpd_medial_mesh over its tets) as keys, all-gathered (one packed all-gather) and
+    deduplicated by the library (rpd_reduce_by_key).  Returns edges [n, 2], faces [n, 3]
+    (int32 CUDA tensors, ascending, identical on every rank)."""
+    dev = torch.device("cuda", ctx.device)
+    mm = ctx.medial_mesh(device=True)
+    e, f = mm["edges"].to(torch.int64), mm["faces"].to(torch.int64)
+    parts = {"e": (e[:, 0] << 21) | e[:, 1], "f": (f[:, 0] << 42) | (f[:, 1] << 21) | f[:, 2]}
+    allk = gather_records(parts, dev, group)
+    ek, _ = ctx.reduce_by_key(allk["e"], torch.zeros_like(allk["e"]))
+    fk, _ = ctx.reduce_by_key(allk["f"], torch.zeros_like(allk["f"]))
+    edges = torch.stack([ek >> 21, ek & 0x1FFFFF], 1).to(torch.int32)
+    faces = torch.stack([fk >> 42, (fk >> 21) & 0x1FFFFF, fk & 0x1FFFFF], 1).to(torch.int32)
+    return {"edges": edges, "faces": faces}
+
+
 def sphere_volumes(ctx, group=None):
     """Per-sphere RPC volume of the whole job (SURVEY.md §8(e) validation aggregate): every
     rank's vector (rpd_sphere_volumes over its tets) summed by one all-reduce."""

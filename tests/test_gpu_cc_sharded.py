@@ -248,3 +248,45 @@ def test_rpe_sharded_nccl_world1():
     finally:
         c.close()
         dist.destroy_process_group()
+
+
+def test_medial_mesh_sharded_nccl_world1():
+    """dist.medial_mesh_sharded (keys all-gathered, deduplicated by rpd_reduce_by_key) through
+    a size-1 NCCL group, and the library dedupe of two shards' keys, equal the whole mesh's."""
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2403_18761_b200 as P
+    from paper_2403_18761_b200.dist import free_port, medial_mesh_sharded
+    w = W.make_shape_workload("Sh", 3000, 200, seed=6, cache=False)
+    c = P.RPDContext(0, filter_mode="pruned")
+    try:
+        c.set_euler(w.tets, len(w.verts))
+        c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        c.clip()
+        full = c.medial_mesh()
+        keys = []
+        for r in range(2):  # two shards' face keys, deduplicated by the library
+            ids = W.block_cyclic_shard(w.T, 2, r, block=256).astype(np.int32)
+            c.set_euler(w.tets, len(w.verts), ids)
+            c.relations(w.verts, w.tets[ids], w.spheres, w.nbr_off, w.nbr_idx)
+            c.clip()
+            f = torch.as_tensor(c.medial_mesh()["faces"].astype(np.int64)).cuda()
+            keys.append((f[:, 0] << 42) | (f[:, 1] << 21) | f[:, 2])
+        fk, _ = c.reduce_by_key(torch.cat(keys), torch.zeros(sum(len(k) for k in keys),
+                                                             dtype=torch.int64, device="cuda"))
+        got = torch.stack([fk >> 42, (fk >> 21) & 0x1FFFFF, fk & 0x1FFFFF], 1).cpu().numpy()
+        assert np.array_equal(got, full["faces"])
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        try:
+            c.set_euler(w.tets, len(w.verts), np.arange(w.T, dtype=np.int32))
+            c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+            c.clip()
+            mm = medial_mesh_sharded(c)
+            assert np.array_equal(mm["edges"].cpu().numpy(), full["edges"])
+            assert np.array_equal(mm["faces"].cpu().numpy(), full["faces"])
+        finally:
+            dist.destroy_process_group()
+    finally:
+        c.close()
