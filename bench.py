@@ -48,7 +48,7 @@ def bench_config(args, w, world):
     batches = w.batches if args.partial_iters < 0 else w.batches[:args.partial_iters]
     return {"workload": workload_name(args.config), "config": args.config, "T": w.T, "N": w.N,
             "partial_iters": len(batches), "M": (len(batches[0][0]) - w.N) if batches else 0,
-            "filter": args.filter, "parallelism": f"tet-shard x{world}",
+            "filter": args.filter, "parallelism": f"tet-shard x{world}", "seed": args.seed,
             "l2": "flushed (256 MB write) before every timed step"}
 
 
@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--no-euler", action="store_true",
                     help="skip the fractional-Euler (NEXT-1) side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--seed", type=int, default=0,
+                    help="workload seed (SURVEY.md §8(d): seeds 0, 1, 2 per config, median "
+                         "reported; tools/seeds.py runs all three)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the sharded path (exchanges over a process group) even with one "
                          "rank, e.g. under torch.distributed.run --nproc-per-node 1 (testing)")
@@ -164,7 +167,7 @@ def run_reference(args):
         return
     import oracle
     import rpd_workloads as W
-    w = W.make_config(args.config)
+    w = W.make_config(args.config, seed=args.seed)
     cores = oracle.max_threads()
     rng = np.random.default_rng(0)
     # calibrate the sample so the whole run ends in a few minutes
@@ -236,7 +239,15 @@ def cpu_baseline(w, seconds):
         r = oracle.rpd_workload(w, tet_ids=ids, clip=clip, nthreads=nthreads)
         return time.perf_counter() - t0, r
 
-    ids = np.sort(rng.choice(w.T, n_s, replace=False)).astype(np.int32)
+    # deterministic subset (BASELINE.md CPU-baseline plan): every k-th block of 1024
+    # consecutive tets -- the tets are in Morton order of their centroids (rpd_workloads), so a
+    # block is a compact patch of the mesh -- with k set by the time budget
+    blk = 1024
+    n_blk = -(-w.T // blk)
+    stride = max(1, -(-n_blk * blk // max(n_s, 1)))
+    ids = np.concatenate([np.arange(b * blk, min((b + 1) * blk, w.T))
+                          for b in range(0, n_blk, stride)]).astype(np.int32)
+    n_s = len(ids)
     t_full, r = timed(ids, True, cores)
     t_filt, _ = timed(ids, False, cores)
     n_cand = len(r["cand_idx"])
@@ -250,8 +261,9 @@ def cpu_baseline(w, seconds):
     st = r["stats"]
     return {"value": n_cand / t_full, "unit": "pairs/s", "cores": cores, "kind": "oracle",
             "cpu": cpu_model(),
-            "sample": f"{n_s} random tets of {w.T} (full RPD of the {w.N}-sphere set: Alg. 1 over "
-                      f"all {w.N} spheres + clip), {t_full:.1f} s; partial updates not sampled",
+            "sample": f"{n_s} tets of {w.T} ({n_s / w.T:.2%}: every {stride}-th Morton block of "
+                      f"{blk} tets; full RPD of the {w.N}-sphere set: Alg. 1 over all {w.N} "
+                      f"spheres + clip), {t_full:.1f} s; partial updates not sampled",
             "all_cores": {"threads": cores, "tets": int(n_s), "pairs_filtered_per_s":
                           n_s * w.N / t_filt, "pairs_clipped_per_s": n_cand / t_clip,
                           "filter_s": t_filt, "clip_s": t_clip, "full_s": t_full},
@@ -460,7 +472,7 @@ def side_small_m(args, ctx, w, d_verts, d_tets, to_dev):
     small = {}
     t_, n_, mode_, _, _ = W.CONFIGS["C3"]
     for M in (1, 10):
-        ws = W.make_shape_workload(f"C4m{M}", t_, n_, seed=0, radius_mode=mode_,
+        ws = W.make_shape_workload(f"C4m{M}", t_, n_, seed=args.seed, radius_mode=mode_,
                                    n_batches=6, batch_m=M, clusters=min(M, 10))
         ctx.relations(d_verts, d_tets, to_dev(ws.spheres), to_dev(ws.nbr_off),
                       to_dev(ws.nbr_idx))
@@ -522,7 +534,7 @@ def main():
     if sharded:
         dist.barrier()
 
-    w = W.make_config(args.config)
+    w = W.make_config(args.config, seed=args.seed)
     batches = w.batches if args.partial_iters < 0 else w.batches[:args.partial_iters]
     ctx = P.RPDContext(local, filter_mode=args.filter)
     ctx.set_profile(True)
@@ -723,7 +735,8 @@ def main():
     # step) against the FP64 peak; algorithmic flops counted by the ORACLE on the same input
     # (tools/oracle_work.py -> profiles/oracle_work.json) when present
     peak, peak_src = fp64_peak_tflops()
-    ow = load_oracle_work(args.config) if len(d_batches) == len(w.batches) else None
+    ow = load_oracle_work(args.config) \
+        if len(d_batches) == len(w.batches) and args.seed == 0 else None
     kc = {k: int(np.median([r["counters"][k] + sum(p["counters"][k] for p in r["partial"])
                             for r in recs])) for k in CNT}
     kernel_flops = (24 * kc["clip_plane_evals"] + 8 * kc["clip_vertex_tests"] +
