@@ -202,7 +202,7 @@ def _oracle_per_tet(oracle, w, rng):
     """Oracle seconds per tet: two probe sizes, so that the per-call input validation (a pass
     over the whole mesh) cancels; if timing noise makes the difference vanish, the larger
     probe's average (an over-estimate, so the sample only gets smaller)."""
-    ts, ns = [], (32, 288)
+    ts, ns = [], (256, 2048)
     for n in ns:
         ids = np.sort(rng.choice(w.T, min(n, w.T), replace=False)).astype(np.int32)
         t0 = time.perf_counter()
