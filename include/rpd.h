@@ -516,18 +516,23 @@ typedef struct {
   int64_t N, E;
   int64_t n_hidden, n_vertex_overflow;
   int64_t n_rows_computed;  /* rows computed by this call (N for rpd_neighbors) */
+  int64_t n_rows_block;     /* of these, rows computed by a whole block (heavy rows: more than
+                               RPD_NB_HEAVY = 2048 spheres in their first search ball; the
+                               same rows as a warp would give) */
 } rpd_nbr_lists;
 rpd_status rpd_neighbors(rpd_ctx* ctx, const double* spheres, int64_t N, const double* box,
                          rpd_nbr_lists* out);
 /* Incremental lists after appending M spheres (the paper recomputes the neighbours at every
  * insertion; its spheres are inserted a few at a time):
  * spheres [N][4] are the previous call's N - M spheres, unchanged, followed by M new ones;
- * `box` must be the previous call's.  Recomputed: the rows of the new spheres, of the old
- * spheres they list and of old spheres a new one hides (same centre); every other row is
- * kept -- its box-restricted cell is unchanged, so it is still a certified superset
- * (DESIGN.md §10 "Sphere neighbours", reading R34).  Same outputs and lifetime as
- * rpd_neighbors (n_hidden / n_vertex_overflow count the recomputed rows only); a new row
- * longer than 256 entries recomputes every row.  RPD_ESTATE: no previous lists of N - M
+ * `box` must be the previous call's.  The rows of the new spheres are computed as by
+ * rpd_neighbors; every old row is kept and extended by the new spheres whose radical plane
+ * reaches the ball stored around its last bounding polytope (cells only shrink when spheres
+ * are added, so the new neighbours of an old sphere are old neighbours or new spheres: a
+ * certified superset again, DESIGN.md §10 "Sphere neighbours", reading R34); an old sphere
+ * that a new one hides (same centre, larger radius) gets an empty row.  Same outputs and
+ * lifetime as rpd_neighbors (n_hidden / n_vertex_overflow / n_rows_block count the new rows
+ * only; n_rows_computed = M + the old rows extended or emptied).  RPD_ESTATE: no previous lists of N - M
  * spheres or another box; RPD_EINVAL: as rpd_neighbors, or an old sphere changed. */
 rpd_status rpd_neighbors_update(rpd_ctx* ctx, const double* spheres, int64_t N, int64_t M,
                                 const double* box, rpd_nbr_lists* out);

@@ -116,6 +116,8 @@ const char* err_kind_str(int k) {
     case ERR_NBR_OFF: return "bad neighbour CSR offsets";
     case ERR_SPHERE_CHANGED:
       return "partial update: an existing sphere [0, N_old) changed (only appending is allowed)";
+    case ERR_NB_RECOMPUTE:
+      return "neighbour lists: a long row recomputed with another length (internal error)";
     default: return "invalid input";
   }
 }
@@ -2255,7 +2257,7 @@ rpd_status rpd_neighbors(rpd_ctx* c, const double* spheres, int64_t N, const dou
   CK(cudaMemcpyAsync(c->nb_prev.p, d_sph, sizeof(double) * 4 * N, cudaMemcpyDeviceToDevice,
                      c->stream), "copy");
   *out = rpd_nbr_lists{off, c->nb_idx.as<int32_t>(), N, E, (int64_t)h_st[1], (int64_t)h_st[0],
-                       N};
+                       N, (int64_t)h_st[3]};
   return RPD_OK;
 }
 
@@ -2335,7 +2337,7 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
   c->nb_E = E;
   c->nb_rows = n_rows;
   *out = rpd_nbr_lists{c->nb_off.as<int32_t>(), c->nb_idx.as<int32_t>(), N, E, (int64_t)h_st[1],
-                       (int64_t)h_st[0], n_rows};
+                       (int64_t)h_st[0], n_rows, (int64_t)h_st[3]};
   return RPD_OK;
 }
 

@@ -79,7 +79,8 @@ enum ErrKind {
   ERR_NBR_DUP = 10,
   ERR_NBR_SAME_CENTRE = 11,
   ERR_NBR_OFF = 12,
-  ERR_SPHERE_CHANGED = 13
+  ERR_SPHERE_CHANGED = 13,
+  ERR_NB_RECOMPUTE = 14  // neighbour pass 2 found another row length than pass 1 (unreachable)
 };
 
 // device statistics (uint64 counters)

@@ -41,6 +41,7 @@ constexpr int NB_MAXV = 224;              // vertex candidates of P_K per sphere
 constexpr int NB_CAPC = 128;              // selection candidates: 4 per lane
 constexpr int NB_CAP1 = 256;              // row entries kept by pass 1
 constexpr int NB_WARPS = 4;               // warps per block of the main kernel
+constexpr int NB_BT = 256;                // threads per sphere of the heavy-row kernel
 constexpr int NB_GMAX = 160;              // grid cells per axis (max)
 constexpr int NB_RB = 256;                // radius buckets of the work order
 constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
@@ -240,7 +241,7 @@ struct NbArgs {
   int32_t* tmp;           // [E] pass-2 rows (unsorted)
   int32_t* n_long;        // rows longer than CAP1: count, then ids
   int32_t* long_ids;
-  unsigned long long* stats;  // [0] vertex overflows, [1] hidden, [2] triples
+  unsigned long long* stats;  // [0] vertex overflows, [1] hidden, [2] triples, [3] block rows
   int* err;
   const int32_t* order;   // work order (pass 1)
   int32_t* work;          // work counter (pass 1)
@@ -249,63 +250,109 @@ struct NbArgs {
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
   double4* ball;   // [N] bounding ball of each row's final P_K (center, radius; r < 0: empty)
   int32_t* hits;   // [warp slots][NB_HCAP] positions (cell-sorted arrays) of a round's hits
+  // heavy rows: pass 1 (a warp per sphere) hands a sphere whose round-0 search ball holds more
+  // than heavy_items grid entries to the block kernel (a block of NB_BT threads per sphere)
+  int heavy_items;    // 0: off
+  int32_t* heavy_ids;  // [N]
+  int32_t* n_heavy;    // their count
+  int32_t* work2;      // the block kernel's work counter
 };
 
-// One warp computes sphere i's row.  PASS2: writes the row into tmp at off[i] (rows > CAP1).
-template <bool PASS2>
-__device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __restrict__ hb) {
+// The per-sphere computation runs on a warp (NT = 32) or on a block of NT threads (heavy
+// rows).  Both give the same row, bit for bit: the block's extra warps only share the loops
+// whose results do not depend on which thread did what (the vertex enumeration, whose vertex
+// SET is the result -- nothing downstream depends on the vertex order -- and the scans, whose
+// per-thread candidate lists are merged into the 32 "virtual lanes" the warp would have had,
+// t mod 32, and whose hit lists are compacted in scan order); everything else is done by warp
+// 0 with the warp's code and broadcast through shared memory.
+template <int NT>
+struct NbBlk {
+  double tk[4 * NT];  // per-thread LaneTop (merged into the 32 virtual lanes)
+  int tj[4 * NT];
+  int wc[NT / 32];    // per-warp counts (ordered compaction)
+};
+template <>
+struct NbBlk<32> {};
+
+struct NbBc {  // warp 0 -> the block
+  double R, rho_v, pdm_v, evm_v, cx, cy, cz, rs, bc[3], be[3];
+  int nK, first_new, n_deep;
+};
+
+template <int NT>
+struct NbSm {
+  NbSmem s;
+  NbBc b;
+  NbBlk<NT> k;
+};
+
+// One group (warp or block) computes sphere i's row.  PASS2: writes the row into tmp at off[i]
+// (rows > CAP1).
+template <int NT, bool PASS2>
+__device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* __restrict__ hb) {
+  constexpr bool BLK = NT > 32;
+  NbSmem& S = SM.s;
+  NbBc& Bc = SM.b;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool w0 = warp == 0;
+  auto gsync = [&]() {
+    if constexpr (BLK) __syncthreads();
+    else __syncwarp();
+  };
   const NbGrid& g = *A.grid;
   const double4 si = make_double4(A.sph[4 * i], A.sph[4 * i + 1], A.sph[4 * i + 2], A.sph[4 * i + 3]);
   const int G = g.G;
   const int ci[3] = {nb_cell_axis(si.x, g, 0), nb_cell_axis(si.y, g, 1), nb_cell_axis(si.z, g, 2)};
-  if (lane == 0) {
+  if (tid == 0) {
     S.n_v = 0;
     S.n_o = 0;
     S.flags = 0;
   }
-  __syncwarp();
+  gsync();
   LaneTop top;
   top.init();
-  int n_seen = 0;
   const long long t_start = clock64();
   unsigned long long g_start = 0;
-  if (A.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+  if (!BLK && A.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0, dbg_enum = 0;
   int dbg_rounds = 0;
-  // ---- 1. ring collection of candidates for K (and the hiding test)
-  for (int r = 0;; ++r) {
-    const int w = 2 * r + 1, nc = w * w * w;
-    for (int q = lane; q < nc; q += 32) {
-      const int dx = q % w - r, dy = (q / w) % w - r, dz = q / (w * w) - r;
-      if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;
-      const int x = ci[0] + dx, y = ci[1] + dy, z = ci[2] + dz;
-      if (x < 0 || y < 0 || z < 0 || x >= G || y >= G || z >= G) continue;
-      const int c = (z * G + y) * G + x;
-      for (int p = A.start[c]; p < A.start[c + 1]; ++p) {
-        const int j = A.items[p];
-        if (j == i) continue;
-        const double4 sj = make_double4(A.sph[4 * j], A.sph[4 * j + 1], A.sph[4 * j + 2], A.sph[4 * j + 3]);
-        const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z;
-        const double d2 = ux * ux + uy * uy + uz * uz;
-        if (d2 == 0.0) {
-          if (sj.w > si.w || (sj.w == si.w && j < i)) atomicOr(&S.flags, 1);  // hidden
-          continue;
+  // ---- 1. ring collection of candidates for K (and the hiding test): warp 0
+  if (w0) {
+    int n_seen = 0;
+    for (int r = 0;; ++r) {
+      const int w = 2 * r + 1, nc = w * w * w;
+      for (int q = lane; q < nc; q += 32) {
+        const int dx = q % w - r, dy = (q / w) % w - r, dz = q / (w * w) - r;
+        if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;
+        const int x = ci[0] + dx, y = ci[1] + dy, z = ci[2] + dz;
+        if (x < 0 || y < 0 || z < 0 || x >= G || y >= G || z >= G) continue;
+        const int c = (z * G + y) * G + x;
+        for (int p = A.start[c]; p < A.start[c + 1]; ++p) {
+          const int j = A.items[p];
+          if (j == i) continue;
+          const double4 sj = make_double4(A.sph[4 * j], A.sph[4 * j + 1], A.sph[4 * j + 2], A.sph[4 * j + 3]);
+          const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z;
+          const double d2 = ux * ux + uy * uy + uz * uz;
+          if (d2 == 0.0) {
+            if (sj.w > si.w || (sj.w == si.w && j < i)) atomicOr(&S.flags, 1);  // hidden
+            continue;
+          }
+          top.push(d2 - sj.w * sj.w, j);
+          ++n_seen;
         }
-        top.push(d2 - sj.w * sj.w, j);
-        ++n_seen;
       }
+      int n = n_seen;
+      for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (n >= NB_KSEL0 + 8 || r >= G) break;
     }
-    int n = n_seen;
-    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-    if (n >= NB_KSEL0 + 8 || r >= G) break;
+    for (int t = 0; t < 4; ++t) {
+      S.cid[4 * lane + t] = top.j[t];
+      S.key[4 * lane + t] = top.k[t];
+    }
   }
-  for (int t = 0; t < 4; ++t) {
-    S.cid[4 * lane + t] = top.j[t];
-    S.key[4 * lane + t] = top.k[t];
-  }
-  __syncwarp();
+  gsync();
   if (S.flags & 1) {
-    if (!PASS2 && lane == 0) {
+    if (!PASS2 && tid == 0) {
       A.cnt[i] = 0;
       atomicAdd(&A.stats[1], 1ull);
       if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);  // (empty cell)
@@ -313,25 +360,26 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
     return;
   }
   // box planes (fixed), then rounds: select KSEL planes, enumerate P_K, scan the ball
-  if (lane < 6) {
-    const int k = lane >> 1;
+  if (tid < 6) {
+    const int k = tid >> 1;
     const double cth = k == 0 ? si.x : (k == 1 ? si.y : si.z);
     // lo: y_k + (cth - lo) >= 0 ; hi: -y_k + (hi - cth) >= 0
     double4 p = make_double4(0, 0, 0, 0);
-    const double sgn = (lane & 1) ? -1.0 : 1.0;
+    const double sgn = (tid & 1) ? -1.0 : 1.0;
     if (k == 0) p.x = sgn;
     if (k == 1) p.y = sgn;
     if (k == 2) p.z = sgn;
-    p.w = (lane & 1) ? (A.bhi[k] - cth) : (cth - A.blo[k]);
-    S.pl[lane] = p;
+    p.w = (tid & 1) ? (A.bhi[k] - cth) : (cth - A.blo[k]);
+    S.pl[tid] = p;
   }
   const double L = sqrt((A.bhi[0] - A.blo[0]) * (A.bhi[0] - A.blo[0]) +
                         (A.bhi[1] - A.blo[1]) * (A.bhi[1] - A.blo[1]) +
                         (A.bhi[2] - A.blo[2]) * (A.bhi[2] - A.blo[2]));
   const int base = PASS2 ? A.off[i] : 0;
+  const int cap2 = PASS2 ? A.cnt[i] : 0;  // pass 2: the pass-1 length bounds the writes
 
   // select up to `want` planes from the candidates S.cid / S.key (smallest key first, ties:
-  // smaller id), appended after the nK kept ones
+  // smaller id), appended after the nK kept ones (warp 0)
   auto select = [&](int nK, int want) {
     int sel = nK;
     for (; sel < want; ++sel) {
@@ -377,9 +425,18 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
   // polytope only shrinks): K = the planes of K that are facets of P_K (the others are
   // redundant for it) + the deepest cuts into P_K among the ball's spheres.  Converged when no
   // sphere cuts deeper than tolF: the final scan lists the hits.
-  int nK = select(0, NB_KSEL0);
-  if (lane == 0) S.first = nK > 0 ? S.kid[0] : -1;
-  __syncwarp();
+  int nK = 0;
+  if (w0) {
+    nK = select(0, NB_KSEL0);
+    if (lane == 0) S.first = nK > 0 ? S.kid[0] : -1;
+  }
+  if constexpr (BLK) {
+    if (tid == 0) Bc.nK = nK;
+    __syncthreads();
+    nK = Bc.nK;
+  } else {
+    __syncwarp();
+  }
   const int n_sel = nK;
   int n_v = 0;
   double R = 0.0, cx = 0.0, cy = 0.0, cz = 0.0, rs = 0.0;
@@ -390,6 +447,12 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
   bool list_exact = true;  // S.vx holds the vertices of P_K (not the box fallback)
   int first_new = 0;
   int n_list = -1;  // hits of the previous round in hb (-1: none, scan the grid)
+  auto flush_tri = [&]() {  // (per warp)
+    if constexpr (!PASS2) {
+      for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
+      if (lane == 0 && n_tri) atomicAdd(&A.stats[2], n_tri);
+    }
+  };
   for (int round = 0;; ++round) {
     const bool final_round = converged || round == NB_ROUNDS - 1;
     if (!converged) {
@@ -398,35 +461,37 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
     // ---- 3. vertices of P_K.  Round 0: every plane triple a < b < c.  Later rounds (P_K =
     // P_old ∩ new planes, planes [first_new, M) new): the old vertices that satisfy the new
     // planes (every old vertex lies on >= 3 kept facet planes), plus the triples whose largest
-    // index is a new plane.  lane = pair (a, b)
-    if (first_new > 0) {
-      int kept = 0;
-      for (int c0 = 0; c0 < n_v; c0 += 32) {
-        const int s2 = c0 + lane;
-        bool ok = false;
-        double4 v = make_double4(0, 0, 0, 0);
-        if (s2 < n_v) {
-          v = S.vx[s2];
-          ok = true;
-          for (int k = first_new; k < M && ok; ++k) {
-            const double4 pk = S.pl[k];
-            ok = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w >=
-                 -(v.w + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+    // index is a new plane.  thread = pair (a, b)
+    if (w0) {
+      if (first_new > 0) {
+        int kept = 0;
+        for (int c0 = 0; c0 < n_v; c0 += 32) {
+          const int s2 = c0 + lane;
+          bool ok = false;
+          double4 v = make_double4(0, 0, 0, 0);
+          if (s2 < n_v) {
+            v = S.vx[s2];
+            ok = true;
+            for (int k = first_new; k < M && ok; ++k) {
+              const double4 pk = S.pl[k];
+              ok = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w >=
+                   -(v.w + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+            }
           }
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          __syncwarp();
+          if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;  // in place: <= s2
+          kept += __popc(m);
+          __syncwarp();
         }
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        __syncwarp();
-        if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;  // in place: <= s2
-        kept += __popc(m);
-        __syncwarp();
+        if (lane == 0) S.n_v = kept;
+      } else if (lane == 0) {
+        S.n_v = 0;
       }
-      if (lane == 0) S.n_v = kept;
-    } else if (lane == 0) {
-      S.n_v = 0;
     }
-    __syncwarp();
+    gsync();
     const int n_pairs = M * (M - 1) / 2;
-    for (int q = lane; q < n_pairs; q += 32) {
+    for (int q = tid; q < n_pairs; q += NT) {
       int a = 0, rem = q;
       while (rem >= M - 1 - a) {
         rem -= M - 1 - a;
@@ -463,69 +528,45 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
         if (s2 < NB_MAXV) S.vx[s2] = make_double4(yx, yy, yz, ev);
       }
     }
-    __syncwarp();
+    gsync();
     dbg_enum += clock64() - t_enum;
     n_v = S.n_v;
     if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
-      if (!PASS2 && lane == 0) {
+      if (!PASS2 && tid == 0) {
         A.cnt[i] = 0;
         if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);
       }
-      if (!PASS2) {
-        for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
-        if (lane == 0) atomicAdd(&A.stats[2], n_tri);
-      }
+      flush_tri();
       return;
     }
     if (n_v > NB_MAXV) {  // conservative fallback: the box corners
       list_exact = false;
-      __syncwarp();
-      if (lane < 8)
-        S.vx[lane] = make_double4(((lane & 1) ? A.bhi[0] : A.blo[0]) - si.x,
-                                  ((lane & 2) ? A.bhi[1] : A.blo[1]) - si.y,
-                                  ((lane & 4) ? A.bhi[2] : A.blo[2]) - si.z, A.tol0);
-      if (!PASS2 && lane == 0 && final_round) atomicAdd(&A.stats[0], 1ull);
+      if (tid < 8)
+        S.vx[tid] = make_double4(((tid & 1) ? A.bhi[0] : A.blo[0]) - si.x,
+                                 ((tid & 2) ? A.bhi[1] : A.blo[1]) - si.y,
+                                 ((tid & 4) ? A.bhi[2] : A.blo[2]) - si.z, A.tol0);
+      if (!PASS2 && tid == 0 && final_round) atomicAdd(&A.stats[0], 1ull);
       n_v = 8;
-      __syncwarp();
+      gsync();
     }
-    // ---- 4. search ball
-    double rho = 0.0, pdm = -1e300, evm = 0.0;
-    for (int s2 = lane; s2 < n_v; s2 += 32) {
-      const double4 v = S.vx[s2];
-      const double d2 = v.x * v.x + v.y * v.y + v.z * v.z, d = sqrt(d2) + v.w;
-      rho = fmax(rho, d);
-      pdm = fmax(pdm, d * d - si.w * si.w);
-      evm = fmax(evm, v.w);
-    }
-    rho = warp_max(rho);
-    pdm = warp_max(pdm);
-    evm = warp_max(evm);
-    R = (rho + sqrt(fmax(pdm, 0.0) + g.rmax * g.rmax)) * (1.0 + 1e-9) +
-        4.0 * (evm + A.tol0) + 1e-9 * L;
-    // bounding ball of P_K around the vertex centroid: a plane farther than its radius from
-    // the centre misses P_K (one dot product instead of a loop over the vertices)
-    {
-      double sx = 0, sy = 0, sz = 0;
-      for (int s2 = lane; s2 < n_v; s2 += 32) {
-        sx += S.vx[s2].x;
-        sy += S.vx[s2].y;
-        sz += S.vx[s2].z;
-      }
-      for (int o = 16; o; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        sz += __shfl_xor_sync(0xffffffffu, sz, o);
-      }
-      cx = sx / n_v;
-      cy = sy / n_v;
-      cz = sz / n_v;
-      double rr = 0.0;
+    // ---- 4. search ball (warp 0): radius R around theta_i; a bounding ball of P_K around the
+    // centre of its vertex box (a plane farther than its radius from the centre misses P_K: one
+    // dot product instead of a loop over the vertices) and the vertex box itself.  Only max /
+    // min reductions: independent of the vertex order.
+    if (w0) {
+      double rho = 0.0, pdm = -1e300, evm = 0.0;
       for (int s2 = lane; s2 < n_v; s2 += 32) {
         const double4 v = S.vx[s2];
-        const double dx = v.x - cx, dy = v.y - cy, dz = v.z - cz;
-        rr = fmax(rr, sqrt(dx * dx + dy * dy + dz * dz) + v.w);
+        const double d2 = v.x * v.x + v.y * v.y + v.z * v.z, d = sqrt(d2) + v.w;
+        rho = fmax(rho, d);
+        pdm = fmax(pdm, d * d - si.w * si.w);
+        evm = fmax(evm, v.w);
       }
-      rs = warp_max(rr) * (1.0 + 1e-12) + 1e-12 * L;
+      rho = warp_max(rho);
+      pdm = warp_max(pdm);
+      evm = warp_max(evm);
+      R = (rho + sqrt(fmax(pdm, 0.0) + g.rmax * g.rmax)) * (1.0 + 1e-9) +
+          4.0 * (evm + A.tol0) + 1e-9 * L;
       // axis box of the vertices (grown by their error radii): centre bc, half extents be
       double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
       for (int s2 = lane; s2 < n_v; s2 += 32) {
@@ -543,13 +584,104 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
         bc[k] = 0.5 * (mn[k] + mx[k]);
         be[k] = 0.5 * (mx[k] - mn[k]) * (1.0 + 1e-12) + 1e-12 * L;
       }
+      cx = bc[0];
+      cy = bc[1];
+      cz = bc[2];
+      double rr = 0.0;
+      for (int s2 = lane; s2 < n_v; s2 += 32) {
+        const double4 v = S.vx[s2];
+        const double dx = v.x - cx, dy = v.y - cy, dz = v.z - cz;
+        rr = fmax(rr, sqrt(dx * dx + dy * dy + dz * dz) + v.w);
+      }
+      rs = warp_max(rr) * (1.0 + 1e-12) + 1e-12 * L;
       rho_v = rho;
       pdm_v = pdm;
       evm_v = evm;
     }
+    if constexpr (BLK) {
+      if (tid == 0) {
+        Bc.R = R;
+        Bc.rho_v = rho_v;
+        Bc.pdm_v = pdm_v;
+        Bc.evm_v = evm_v;
+        Bc.cx = cx;
+        Bc.cy = cy;
+        Bc.cz = cz;
+        Bc.rs = rs;
+        for (int k = 0; k < 3; ++k) {
+          Bc.bc[k] = bc[k];
+          Bc.be[k] = be[k];
+        }
+      }
+      __syncthreads();
+      if (!w0) {
+        R = Bc.R;
+        rho_v = Bc.rho_v;
+        pdm_v = Bc.pdm_v;
+        evm_v = Bc.evm_v;
+        cx = Bc.cx;
+        cy = Bc.cy;
+        cz = Bc.cz;
+        rs = Bc.rs;
+        for (int k = 0; k < 3; ++k) {
+          bc[k] = Bc.bc[k];
+          be[k] = Bc.be[k];
+        }
+      }
+    }
     }  // !converged
-    unsigned long long fmask = 0;  // facets of P_K among the K planes (lane = plane)
-    if (!final_round) {
+    // the search ball's cell box and its rows of cells (fixed y, z: contiguous in the
+    // cell-sorted arrays)
+    int lo[3], hi[3];
+    {
+      const double c[3] = {si.x, si.y, si.z};
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = nb_cell_axis(c[k] - R, g, k);
+        hi[k] = nb_cell_axis(c[k] + R, g, k);
+      }
+    }
+    const int ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1, nrows = ny * nz;
+    // lane = row r0 + lane of a 32-row chunk: its position range [pb, pe) (empty if the row's
+    // (y, z) extent is beyond R)
+    auto row_range = [&](int r0, int& pb, int& pe) {
+      pb = pe = 0;
+      const int rr = r0 + lane;
+      if (rr < nrows) {
+        const int y = lo[1] + rr % ny, z = lo[2] + rr / ny;
+        double dd = 0.0;  // distance from theta_i to the row's (y, z) extent
+        {
+          const double ay0 = g.lo[1] + y * g.h[1], ay1 = ay0 + g.h[1];
+          const double az0 = g.lo[2] + z * g.h[2], az1 = az0 + g.h[2];
+          const double ey = si.y < ay0 ? ay0 - si.y : (si.y > ay1 ? si.y - ay1 : 0.0);
+          const double ez = si.z < az0 ? az0 - si.z : (si.z > az1 ? si.z - az1 : 0.0);
+          dd = ey * ey + ez * ez;
+        }
+        if (dd <= R * R * (1.0 + 1e-9)) {
+          const int c0 = (z * G + y) * G;
+          pb = A.start[c0 + lo[0]];
+          pe = A.start[c0 + hi[0] + 1];
+        }
+      }
+    };
+    if constexpr (!BLK) {
+      // heavy row (pass 1, round 0): more than heavy_items grid entries in the search ball --
+      // handed to the block kernel, which recomputes it from the start (same row)
+      if (!PASS2 && round == 0 && !final_round && A.heavy_items != 0 && n_list < 0) {
+        int tot = 0;
+        for (int r0 = 0; r0 < nrows; r0 += 32) {
+          int pb, pe;
+          row_range(r0, pb, pe);
+          tot += pe - pb;
+        }
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (tot > A.heavy_items) {
+          if (lane == 0) A.heavy_ids[atomicAdd(A.n_heavy, 1)] = i;
+          return;
+        }
+      }
+    }
+    unsigned long long fmask = 0;  // facets of P_K among the K planes (lane = plane; warp 0)
+    if (!final_round && w0) {
       for (int p0 = 0; p0 < nK; p0 += 32) {
         const int p = p0 + lane;
         bool facet = false;
@@ -565,8 +697,8 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
         }
         fmask |= (unsigned long long)__ballot_sync(0xffffffffu, facet) << p0;
       }
-      top.init();
     }
+    if (!final_round) top.init();
     // ---- 5. every sphere of the ball whose plane reaches a vertex of P_K: collected with its
     // depth (selection of the next round) or, in the final round, listed.  The hits of a round
     // (some vertex within slack) are kept in hb: P_K only shrinks, so a plane that reaches a
@@ -593,7 +725,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
       const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(bw);
       ++dbg_scan;
       const double hcen = ax * cx + ay * cy + az * cz + bw;  // plane value at the centre
-      // lower bounds of the plane's minimum over P_K: the centroid ball and the vertex box
+      // lower bounds of the plane's minimum over P_K: the centre ball and the vertex box
       const double lb = fmax(hcen - rs, ax * bc[0] + ay * bc[1] + az * bc[2] + bw -
                                             (fabs(ax) * be[0] + fabs(ay) * be[1] + fabs(az) * be[2]));
       if (lb > slack) return 0;
@@ -615,7 +747,7 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
         if (code & 1) {
           const int s2 = atomicAdd(&S.n_o, 1);
           if (PASS2) {
-            A.tmp[base + s2] = j;
+            if (s2 < cap2) A.tmp[base + s2] = j;
           } else if (s2 < NB_CAP1) {
             S.out[s2] = j;
           }
@@ -624,11 +756,34 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
         top.push(key, j);
       }
     };
+    // ordered compaction of a step's hits into hb (in place: a hit's new index <= its old one)
+    auto compact = [&](bool f, int p, int nh) -> int {
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if constexpr (!BLK) {
+        const int at = nh + __popc(m & ((1u << lane) - 1u));
+        if (f && at < NB_HCAP) hb[at] = p;
+        return nh + __popc(m);
+      } else {
+        if (lane == 0) SM.k.wc[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+          const int c = SM.k.wc[w];
+          before += w < warp ? c : 0;
+          tot += c;
+        }
+        const int at = nh + before + __popc(m & ((1u << lane) - 1u));
+        if (f && at < NB_HCAP) hb[at] = p;
+        __syncthreads();  // (wc is reused by the next step)
+        return nh + tot;
+      }
+    };
     int n_hit = 0;  // hits recorded this round (> NB_HCAP: overflow)
     if (n_list >= 0) {  // ---- scan the previous round's hits, compacted in place
       ++dbg_rounds;
-      for (int t0 = 0; t0 < n_list; t0 += 32) {
-        const int t = t0 + lane;
+      for (int t0 = 0; t0 < n_list; t0 += NT) {
+        const int t = t0 + tid;
         int code = 0, j = -1, p = 0;
         double key = 0.0;
         if (t < n_list) {
@@ -636,125 +791,118 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
           code = visit(p, key, j);
           take(code, key, j);
         }
-        if (!final_round) {
-          const unsigned m = __ballot_sync(0xffffffffu, code & 1);
-          if (code & 1) hb[n_hit + __popc(m & ((1u << lane) - 1u))] = p;  // index <= t
-          n_hit += __popc(m);
-        }
+        if (!final_round) n_hit = compact(code & 1, p, n_hit);
       }
     } else {
-    int lo[3], hi[3];
-    {
-      const double c[3] = {si.x, si.y, si.z};
-      for (int k = 0; k < 3; ++k) {
-        lo[k] = nb_cell_axis(c[k] - R, g, k);
-        hi[k] = nb_cell_axis(c[k] + R, g, k);
-      }
-    }
-    const int nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
-    (void)nx;
-    ++dbg_rounds;
-    // rows of cells (fixed y, z) are contiguous in the cell-sorted arrays: lane = row for the
-    // ranges, then the warp walks the concatenated ranges (coalesced id / sphere loads)
-    const int nrows = ny * nz;
-    for (int r0 = 0; r0 < nrows; r0 += 32) {
-      int pb = 0, pe = 0;
-      {
-        const int rr = r0 + lane;
-        if (rr < nrows) {
-          const int y = lo[1] + rr % ny, z = lo[2] + rr / ny;
-          double dd = 0.0;  // distance from theta_i to the row's (y, z) extent
-          {
-            const double ay0 = g.lo[1] + y * g.h[1], ay1 = ay0 + g.h[1];
-            const double az0 = g.lo[2] + z * g.h[2], az1 = az0 + g.h[2];
-            const double ey = si.y < ay0 ? ay0 - si.y : (si.y > ay1 ? si.y - ay1 : 0.0);
-            const double ez = si.z < az0 ? az0 - si.z : (si.z > az1 ? si.z - az1 : 0.0);
-            dd = ey * ey + ez * ez;
+      ++dbg_rounds;
+      // every warp walks the same 32-row chunks: lane = row for the ranges, then the group
+      // walks the concatenated ranges (coalesced id / sphere loads), item t on thread t mod NT
+      for (int r0 = 0; r0 < nrows; r0 += 32) {
+        int pb = 0, pe = 0;
+        row_range(r0, pb, pe);
+        const int len = pe - pb;
+        int incl = len;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - len;
+        for (int t0 = 0; t0 < total; t0 += NT) {
+          const int t = t0 + tid;
+          int k = 0;  // the row holding t: the largest k with excl_k <= t
+          for (int step = 16; step; step >>= 1) {
+            const int e = __shfl_sync(0xffffffffu, excl, k + step);
+            if (e <= t) k += step;
           }
-          if (dd <= R * R * (1.0 + 1e-9)) {
-            const int c0 = (z * G + y) * G;
-            pb = A.start[c0 + lo[0]];
-            pe = A.start[c0 + hi[0] + 1];
+          const int pbk = __shfl_sync(0xffffffffu, pb, k), exk = __shfl_sync(0xffffffffu, excl, k);
+          int code = 0, j = -1, p = 0;
+          double key = 0.0;
+          if (t < total) {
+            p = pbk + (t - exk);
+            code = visit(p, key, j);
+            take(code, key, j);
           }
+          if (!final_round) n_hit = compact(code & 1, p, n_hit);
         }
       }
-      const int len = pe - pb;
-      int incl = len;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      const int excl = incl - len;
-      for (int t0 = 0; t0 < total; t0 += 32) {
-        const int t = t0 + lane;
-        int k = 0;  // the row holding t: the largest k with excl_k <= t
-        for (int step = 16; step; step >>= 1) {
-          const int e = __shfl_sync(0xffffffffu, excl, k + step);
-          if (e <= t) k += step;
-        }
-        const int pbk = __shfl_sync(0xffffffffu, pb, k), exk = __shfl_sync(0xffffffffu, excl, k);
-        int code = 0, j = -1, p = 0;
-        double key = 0.0;
-        if (t < total) {
-          p = pbk + (t - exk);
-          code = visit(p, key, j);
-          take(code, key, j);
-        }
-        if (!final_round) {
-          const unsigned m = __ballot_sync(0xffffffffu, code & 1);
-          const int at = n_hit + __popc(m & ((1u << lane) - 1u));
-          if ((code & 1) && at < NB_HCAP) hb[at] = p;
-          n_hit += __popc(m);
-        }
-      }
-    }
     }
     n_list = n_hit <= NB_HCAP ? n_hit : -1;
-    __syncwarp();
+    gsync();
     if (final_round) break;
+    if constexpr (BLK) {  // the 32 virtual lanes' candidate lists: thread t -> lane t mod 32
+      for (int t = 0; t < 4; ++t) {
+        SM.k.tk[4 * tid + t] = top.k[t];
+        SM.k.tj[4 * tid + t] = top.j[t];
+      }
+      __syncthreads();
+      if (w0) {
+        for (int w = 1; w < NT / 32; ++w)
+          for (int t = 0; t < 4; ++t) {
+            const int s = 4 * (32 * w + lane) + t;
+            if (SM.k.tj[s] >= 0) top.push(SM.k.tk[s], SM.k.tj[s]);
+          }
+      }
+    }
     int n_deep = 0;
-    for (int t = 0; t < 4; ++t) {
-      S.cid[4 * lane + t] = top.j[t];
-      S.key[4 * lane + t] = top.k[t];
-      n_deep += top.j[t] >= 0;
-    }
-    for (int o = 16; o; o >>= 1) n_deep += __shfl_xor_sync(0xffffffffu, n_deep, o);
-    if (n_deep == 0) {
-      converged = true;
-      continue;
-    }
-    // keep the facet planes (compacted in order), then the deepest cuts
-    __syncwarp();
-    if (lane == 0) {
-      int q = 0;
-      for (int p = 0; p < nK; ++p)
-        if (fmask >> p & 1ull) {
-          S.pl[6 + q] = S.pl[6 + p];
-          S.kid[q] = S.kid[p];
-          ++q;
+    if (w0) {
+      for (int t = 0; t < 4; ++t) {
+        S.cid[4 * lane + t] = top.j[t];
+        S.key[4 * lane + t] = top.k[t];
+        n_deep += top.j[t] >= 0;
+      }
+      for (int o = 16; o; o >>= 1) n_deep += __shfl_xor_sync(0xffffffffu, n_deep, o);
+      __syncwarp();
+      if (n_deep > 0) {
+        // keep the facet planes (compacted in order), then the deepest cuts
+        if (lane == 0) {
+          int q = 0;
+          for (int p = 0; p < nK; ++p)
+            if (fmask >> p & 1ull) {
+              S.pl[6 + q] = S.pl[6 + p];
+              S.kid[q] = S.kid[p];
+              ++q;
+            }
         }
+        __syncwarp();
+        nK = select(__popcll(fmask), NB_KSEL);
+        first_new = list_exact ? 6 + __popcll(fmask) : 0;
+      }
     }
-    __syncwarp();
-    nK = select(__popcll(fmask), NB_KSEL);
-    first_new = list_exact ? 6 + __popcll(fmask) : 0;
+    if constexpr (BLK) {
+      if (tid == 0) {
+        Bc.n_deep = n_deep;
+        Bc.nK = nK;
+        Bc.first_new = first_new;
+      }
+      __syncthreads();
+      nK = Bc.nK;
+      first_new = Bc.first_new;
+      n_deep = Bc.n_deep;
+      __syncthreads();  // (Bc is rewritten by the next round)
+    }
+    if (n_deep == 0) converged = true;
   }
-  if (!PASS2) {
-    for (int o = 16; o; o >>= 1) n_tri += __shfl_xor_sync(0xffffffffu, n_tri, o);
-    if (lane == 0) atomicAdd(&A.stats[2], n_tri);
-  }
-  __syncwarp();
+  flush_tri();
+  gsync();
   int n_o = S.n_o;
   if (n_o == 0 && A.N > 1) {  // i's cell covers B: list the nearest sphere (redundant plane)
-    if (n_sel > 0 && lane == 0) {  // not hit: h_ij > 0 on P_K, so the plane is redundant
-      if (PASS2) A.tmp[base] = S.first;
-      else S.out[0] = S.first;
+    if (n_sel > 0 && tid == 0) {  // not hit: h_ij > 0 on P_K, so the plane is redundant
+      if (PASS2) {
+        if (cap2 > 0) A.tmp[base] = S.first;
+      } else {
+        S.out[0] = S.first;
+      }
       S.n_o = 1;
     }
-    __syncwarp();
+    gsync();
     n_o = S.n_o;
   }
-  if (A.dbg && !PASS2) {
+  if (PASS2 && n_o != cap2 && tid == 0 && atomicCAS(A.err, 0, (int)RPD_EOVERFLOW) == 0) {
+    A.err[1] = ERR_NB_RECOMPUTE;
+    A.err[2] = i;
+  }
+  if (!BLK && A.dbg && !PASS2) {
     for (int o = 16; o; o >>= 1) {
       dbg_scan += __shfl_xor_sync(0xffffffffu, dbg_scan, o);
       dbg_vloop += __shfl_xor_sync(0xffffffffu, dbg_vloop, o);
@@ -771,20 +919,21 @@ __device__ void nb_row(const NbArgs& A, NbSmem& S, int i, int lane, int32_t* __r
       d[7] = (long long)g_start;  // start (ns, global timer)
     }
   }
+  (void)dbg_cells;
   if (!PASS2) {
-    if (lane == 0) {
+    if (tid == 0) {
       A.cnt[i] = n_o;
       // a ball around P_K ⊇ C_i ∩ B (world coordinates; incremental updates test it)
       if (A.ball) A.ball[i] = make_double4(si.x + cx, si.y + cy, si.z + cz, rs + A.tol0);
       if (n_o > NB_CAP1) A.long_ids[atomicAdd(A.n_long, 1)] = i;
     }
     if (n_o <= NB_CAP1)
-      for (int s = lane; s < n_o; s += 32) A.slab[(int64_t)i * NB_CAP1 + s] = S.out[s];
+      for (int s = tid; s < n_o; s += NT) A.slab[(int64_t)i * NB_CAP1 + s] = S.out[s];
   }
 }
 
 __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
-  __shared__ NbSmem sm[NB_WARPS];
+  __shared__ NbSm<32> sm[NB_WARPS];
   if (*(volatile int*)A.err != 0) {  // invalid input: empty rows, no dereference of NaN cells
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.N;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -798,18 +947,41 @@ __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
     if (lane == 0) q = atomicAdd(A.work, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
     if (q >= nwork) break;
-    nb_row<false>(A, sm[w], A.order[q], lane,
-                  A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
+    nb_row<32, false>(A, sm[w], A.order[q], lane,
+                      A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
+  }
+}
+
+// the heavy rows handed over by pass 1: a block per sphere, taken from a counter
+__global__ void __launch_bounds__(NB_BT) k_nb_heavy(NbArgs A) {
+  __shared__ NbSm<NB_BT> sm;
+  __shared__ int q_s;
+  const int n = *A.n_heavy;
+  if (*(volatile int*)A.err != 0) {  // invalid input: empty rows (as pass 1)
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+      A.cnt[A.heavy_ids[q]] = 0;
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) q_s = atomicAdd(A.work2, 1);
+    __syncthreads();
+    const int q = q_s;
+    __syncthreads();
+    if (q >= n) break;
+    if (threadIdx.x == 0) atomicAdd(&A.stats[3], 1ull);
+    nb_row<NB_BT, false>(A, sm, A.heavy_ids[q], threadIdx.x,
+                         A.hits + (size_t)blockIdx.x * NB_HCAP);
+    __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass2(NbArgs A) {
-  __shared__ NbSmem sm[NB_WARPS];
+  __shared__ NbSm<32> sm[NB_WARPS];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = *A.n_long;
   for (int q = blockIdx.x * NB_WARPS + w; q < n; q += gridDim.x * NB_WARPS)
-    nb_row<true>(A, sm[w], A.long_ids[q], lane,
-                 A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
+    nb_row<32, true>(A, sm[w], A.long_ids[q], lane,
+                     A.hits + (size_t)(blockIdx.x * NB_WARPS + w) * NB_HCAP);
 }
 
 // rows into ascending order: rank of each entry among its row (entries are distinct)
@@ -837,6 +1009,26 @@ size_t nb_grid_cells(int64_t N) {
   return (size_t)G * G * G;
 }
 
+// heavy-row hand-off threshold (grid entries in a row's round-0 search ball; RPD_NB_HEAVY,
+// 0 = every row on a warp, -1 = every row on a block: the equivalence tests)
+static int nb_heavy_items(int dflt) {
+  const char* s = getenv("RPD_NB_HEAVY");
+  return s ? atoi(s) : dflt;
+}
+constexpr int NB_HEAVY_DEFAULT = 8192;  // (C3 / C5 sweep: DESIGN.md §10)
+
+// the block kernel over the heavy rows (device count; persistent grid, at most n_max blocks)
+static cudaError_t nb_launch_heavy(rpd_ctx* c, const NbArgs& A, int64_t n_max) {
+  if (A.heavy_items == 0 || n_max <= 0) return cudaSuccess;
+  static int occ[RPD_MAX_DEVICES] = {};
+  int& o = occ[c->device < RPD_MAX_DEVICES ? c->device : 0];
+  if (o == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_nb_heavy, NB_BT, 0) || o < 1))
+    o = 1;
+  k_nb_heavy<<<(int)std::min<int64_t>(n_max, (int64_t)o * c->sms), NB_BT, 0, c->stream>>>(A);
+  ++c->launches;
+  return cudaGetLastError();
+}
+
 // The uniform grid of the spheres, their cell-ordered copy and the radius work order; the
 // pass arguments in *A and the pass-1 grid size in *mb.  Buffers in c->nb_buf.
 static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const double box[6],
@@ -847,7 +1039,7 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   const size_t bytes = sizeof(NbGrid) + 16 + sizeof(int32_t) * (3 * (ncell + 1) + 2 * (N + 1) + 2) +
                        sizeof(int32_t) * (size_t)N * NB_CAP1 + sizeof(unsigned long long) * 4 +
                        sizeof(double4) * (N + 1) + sizeof(int32_t) * (3 * (NB_RB + 1) + 2 + N + 1) +
-                       1024;
+                       sizeof(int32_t) * (N + 1 + 4) + 1024;
   cudaError_t e = c->nb_buf.ensure(bytes);
   if (e) return e;
   char* b = c->nb_buf.as<char>();
@@ -868,6 +1060,8 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   int32_t* order = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
   int32_t* slab = reinterpret_cast<int32_t*>(take(4 * (size_t)N * NB_CAP1));
   double4* sorted = reinterpret_cast<double4*>(take(sizeof(double4) * (N + 1)));
+  int32_t* hvy = reinterpret_cast<int32_t*>(take(4 * 4));  // n_heavy, work2
+  int32_t* hvy_ids = reinterpret_cast<int32_t*>(take(4 * (N + 1)));
   c->nb_grid = g;
   c->nb_stats = st;
   c->nb_start = start;
@@ -880,6 +1074,7 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   if ((e = cudaMemsetAsync(fill, 0, 4 * (ncell + 1), c->stream))) return e;
   if ((e = cudaMemsetAsync(st, 0, 8 * 4, c->stream))) return e;
   if ((e = cudaMemsetAsync(nlong, 0, 8, c->stream))) return e;
+  if ((e = cudaMemsetAsync(hvy, 0, 16, c->stream))) return e;
   if ((e = cudaMemsetAsync(rb, 0, 4 * (3 * (NB_RB + 1) + 2), c->stream))) return e;
   const int blocks = (int)std::min<int64_t>((N + 255) / 256, 8 * (int64_t)c->sms) + 1;
   k_nb_check<<<blocks, 256, 0, c->stream>>>(sph, N, c->errw.as<int>());
@@ -926,6 +1121,10 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   A.err = c->errw.as<int>();
   A.dbg = (long long*)c->nb_dbg;
   A.ball = c->nb_ball.as<double4>();
+  A.heavy_items = nb_heavy_items(NB_HEAVY_DEFAULT);
+  A.heavy_ids = hvy_ids;
+  A.n_heavy = hvy;
+  A.work2 = hvy + 1;
   c->nb_args_tol0 = A.tol0;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nb_pass1, 32 * NB_WARPS, 0) || occ < 1)
@@ -952,6 +1151,7 @@ cudaError_t launch_neighbors_pass1(rpd_ctx* c, const double* sph, int64_t N, con
   k_nb_pass1<<<mb > 0 ? mb : 1, 32 * NB_WARPS, 0, c->stream>>>(A);
   ++c->launches;
   if ((e = cudaGetLastError())) return e;
+  if ((e = nb_launch_heavy(c, A, N))) return e;
   if ((e = launch_scan_i32(c, cnt, off, N))) return e;
   return cudaGetLastError();
 }
@@ -1018,7 +1218,9 @@ static __global__ void k_nb_same(const double* __restrict__ sph, const double* _
     }
 }
 
-static __global__ void k_nb_iota(int32_t* __restrict__ list, int64_t base, int64_t n) {
+static __global__ void k_nb_iota(int32_t* __restrict__ list, int64_t base, int64_t n,
+                                 int32_t* __restrict__ count) {
+  if (count && blockIdx.x == 0 && threadIdx.x == 0) *count = (int32_t)n;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
     list[k] = (int32_t)(base + k);
@@ -1140,15 +1342,23 @@ cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t 
   int mb = 0;
   if ((e = nb_build(c, sph, N, box, cnt, &A, &mb))) return e;
   const int64_t M = N - N_old;
-  k_nb_iota<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
-              c->stream>>>(list, N_old, M);
-  ++c->launches;
-  A.order = list;
-  A.n_work = M;
-  if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
-  const int mb1 = (int)std::max<int64_t>(1, std::min<int64_t>((M + NB_WARPS - 1) / NB_WARPS, mb));
-  k_nb_pass1<<<mb1, 32 * NB_WARPS, 0, c->stream>>>(A);
-  ++c->launches;
+  // few new rows (latency): every one on a block; else pass 1 with the heavy-row hand-off
+  A.heavy_items = nb_heavy_items(M <= 4 * (int64_t)c->sms ? -1 : NB_HEAVY_DEFAULT);
+  const int ib = (int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms);
+  if (A.heavy_items < 0) {
+    k_nb_iota<<<ib, 256, 0, c->stream>>>(A.heavy_ids, N_old, M, A.n_heavy);
+    ++c->launches;
+  } else {
+    k_nb_iota<<<ib, 256, 0, c->stream>>>(list, N_old, M, nullptr);
+    ++c->launches;
+    A.order = list;
+    A.n_work = M;
+    if ((e = cudaMemsetAsync(A.work, 0, sizeof(int32_t), c->stream))) return e;
+    const int mb1 = (int)std::max<int64_t>(1, std::min<int64_t>((M + NB_WARPS - 1) / NB_WARPS, mb));
+    k_nb_pass1<<<mb1, 32 * NB_WARPS, 0, c->stream>>>(A);
+    ++c->launches;
+  }
+  if ((e = nb_launch_heavy(c, A, M))) return e;
   k_nb_newlen<<<(int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms), 256, 0,
                 c->stream>>>(N_old, N, cnt, len);
   ++c->launches;

@@ -87,7 +87,7 @@ class _Rpe(C.Structure):
 class _NbrLists(C.Structure):
     _fields_ = [("nbr_off", C.c_void_p), ("nbr_idx", C.c_void_p), ("N", C.c_int64),
                 ("E", C.c_int64), ("n_hidden", C.c_int64), ("n_vertex_overflow", C.c_int64),
-                ("n_rows_computed", C.c_int64)]
+                ("n_rows_computed", C.c_int64), ("n_rows_block", C.c_int64)]
 
 
 class _Medial(C.Structure):
@@ -581,12 +581,13 @@ class RPDContext:
         off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
         self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
         return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
-                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed}
+                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed,
+                "n_rows_block": n.n_rows_block}
 
     def neighbors_update(self, spheres, M: int, box, device=False) -> dict:
         """Incremental lists after appending the last M of ``spheres`` (the previous call's
-        spheres unchanged, same box): only the rows of the new spheres, of the old spheres
-        they list and of old spheres they hide are recomputed (rpd_neighbors_update)."""
+        spheres unchanged, same box): the new spheres' rows are computed, the old rows
+        extended by the new spheres that reach their cell's ball (rpd_neighbors_update)."""
         ps, ks = _ptr(spheres, np.float64)
         bx = np.ascontiguousarray(np.asarray(box, dtype=np.float64).reshape(6))
         n = _NbrLists()
@@ -596,7 +597,8 @@ class RPDContext:
         off, idx = self._alloc([(n.N + 1, np.int32), (n.E, np.int32)], device)
         self._check(self.L.rpd_download_neighbors(self.h, self._p(off), self._p(idx)))
         return {"nbr_off": off, "nbr_idx": idx, "n_hidden": n.n_hidden,
-                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed}
+                "n_vertex_overflow": n.n_vertex_overflow, "n_rows": n.n_rows_computed,
+                "n_rows_block": n.n_rows_block}
 
     def dirty_ptr(self):
         """Device address of the ctx-owned dirty-tet list of the last update_partial."""

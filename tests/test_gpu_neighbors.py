@@ -246,3 +246,48 @@ def test_neighbors_incremental_edge_cases(ctx):
         ctx.neighbors_update(bad, 1, box)
     with pytest.raises(P.RPDError, match="ESTATE"):  # (the rejected call left no lists)
         ctx.neighbors_update(bad, 1, box)
+
+
+def _lists(ctx, sp, box, mode, monkeypatch, m=None):
+    monkeypatch.setenv("RPD_NB_HEAVY", str(mode))
+    got = ctx.neighbors(sp, box) if m is None else ctx.neighbors_update(sp, m, box)
+    return np.array(got["nbr_off"]), np.array(got["nbr_idx"]), got
+
+
+@pytest.mark.parametrize("name", ["nb_smoke", "nb_small", "tiny", "C2", "C3"])
+def test_neighbors_block_rows_equal_warp_rows(ctx, name, monkeypatch):
+    """Heavy rows run on a whole block (k_nb_heavy): the same rows as the warp computes, entry
+    for entry -- every row on a warp (RPD_NB_HEAVY=0), every row on a block (-1) and the
+    default hand-off give identical CSRs."""
+    if name == "nb_smoke":
+        w = W.make_shape_workload("nb_smoke", 1200, 100, seed=11, cache=False)
+    elif name == "nb_small":
+        w = W.make_shape_workload("nb_small", 600, 60, seed=4, cache=False)
+    elif name == "tiny":
+        w = W.random_tiny(2, n_spheres=20, coarse=True)
+    else:
+        w = W.make_config(name)
+    box = W.mesh_box(w.verts)
+    o0, i0, g0 = _lists(ctx, w.spheres, box, 0, monkeypatch)
+    o1, i1, g1 = _lists(ctx, w.spheres, box, -1, monkeypatch)
+    o2, i2, g2 = _lists(ctx, w.spheres, box, 2048, monkeypatch)
+    assert g0["n_rows_block"] == 0 and g1["n_rows_block"] > 0
+    if name == "C3":
+        assert 0 < g2["n_rows_block"] < w.N
+    assert np.array_equal(o0, o1) and np.array_equal(i0, i1)
+    assert np.array_equal(o0, o2) and np.array_equal(i0, i2)
+    assert g0["n_vertex_overflow"] == g1["n_vertex_overflow"] == g2["n_vertex_overflow"]
+
+
+def test_neighbors_block_rows_incremental(ctx, monkeypatch):
+    """The incremental update's new rows on blocks equal them on warps (C4 chain, 3 batches)."""
+    w = W.make_config("C4")
+    box = W.mesh_box(w.verts)
+    res = {}
+    for mode in (0, -1):
+        monkeypatch.setenv("RPD_NB_HEAVY", str(mode))
+        ctx.neighbors(w.spheres, box)
+        res[mode] = [_lists(ctx, sp, box, mode, monkeypatch, m=500)[:2]
+                     for (sp, _, _) in w.batches[:3]]
+    for (a, b), (c, d) in zip(res[0], res[-1]):
+        assert np.array_equal(a, c) and np.array_equal(b, d)

@@ -40,3 +40,8 @@ print("latest finishers: id r start_ms dur_ms")
 for i in late:
     print(i, round(float(w.spheres[i][3]), 3), round(st[i], 2), round(d[i, 0] / 1.965e6, 2))
 print("r quantiles", np.quantile(w.spheres[:, 3], [0.1, 0.5, 0.9, 1.0]))
+# concurrency: spheres in flight over time (a tail of few heavy spheres shows as a low count)
+for tq in (0.25, 0.5, 1, 2, 4, 8, 12, 16, 20):
+    act = int(((st <= tq) & (en > tq)).sum())
+    print(f"t={tq:5.2f} ms: {act} spheres in flight, {int((en <= tq).sum())} done")
+print("spheres with dur > 2 ms:", int((d[:, 0] / 1.965e6 > 2).sum()), "> 5 ms:", int((d[:, 0] / 1.965e6 > 5).sum()))
