@@ -1024,7 +1024,9 @@ static cudaError_t nb_launch_heavy(rpd_ctx* c, const NbArgs& A, int64_t n_max) {
   int& o = occ[c->device < RPD_MAX_DEVICES ? c->device : 0];
   if (o == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_nb_heavy, NB_BT, 0) || o < 1))
     o = 1;
-  k_nb_heavy<<<(int)std::min<int64_t>(n_max, (int64_t)o * c->sms), NB_BT, 0, c->stream>>>(A);
+  // (one hit-list slot per block: nb_build allocates at least 2 * sms * NB_WARPS slots)
+  const int64_t g = std::min<int64_t>(n_max, (int64_t)std::min(o, 2 * NB_WARPS) * c->sms);
+  k_nb_heavy<<<(int)g, NB_BT, 0, c->stream>>>(A);
   ++c->launches;
   return cudaGetLastError();
 }
