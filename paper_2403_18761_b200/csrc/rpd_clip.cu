@@ -40,7 +40,7 @@
 #define RPD_CLIP_MINB 2  // min resident blocks per SM for the fast kernel
 #endif
 #ifndef RPD_CLIP_STATIC
-#define RPD_CLIP_STATIC 70  // percent of the fast kernel's pairs assigned grid-stride
+#define RPD_CLIP_STATIC 90  // percent of the fast kernel's pairs assigned grid-stride
 #endif
 #ifndef RPD_CLIP_THREADS
 #define RPD_CLIP_THREADS 256  // threads per block of the fast kernel
