@@ -2282,11 +2282,12 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
   const double bx[6] = {box[0], box[1], box[2], box[3], box[4], box[5]};
   const double* d_sph = nullptr;
   CK(resolve(c, spheres, 4 * N, c->h_nb, &d_sph), "stage spheres");
-  CK(c->nb_cnt.ensure(sizeof(int32_t) * (N + 1)), "alloc");
-  CK(c->nb_flag.ensure(N), "alloc");
-  CK(c->nb_list.ensure(sizeof(int32_t) * N), "alloc");
-  CK(c->nb_len.ensure(sizeof(int32_t) * (N + 1)), "alloc");
-  CK(c->nb_off2.ensure(sizeof(int32_t) * (N + 1)), "alloc");
+  // (2x on a reallocation: the sphere set grows a batch at a time)
+  CK(c->nb_cnt.ensure_slack(sizeof(int32_t) * (N + 1), 2), "alloc");
+  CK(c->nb_flag.ensure_slack(N, 2), "alloc");
+  CK(c->nb_list.ensure_slack(sizeof(int32_t) * N, 2), "alloc");
+  CK(c->nb_len.ensure_slack(sizeof(int32_t) * (N + 1), 2), "alloc");
+  CK(c->nb_off2.ensure_slack(sizeof(int32_t) * (N + 1), 2), "alloc");
   CK(c->nb_misc.ensure(sizeof(int) * 8), "alloc");
   // the balls of the old rows, grown (with their content) for the new ones
   if (c->nb_ball.cap < sizeof(double4) * N) {
@@ -2320,14 +2321,14 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
     return check_err(c, rb);
   }
   const int64_t E = rb->i32[0], n_rows = M + rb->i32[1];  // (new rows + changed old rows)
-  CK(c->nb_idx2.ensure(sizeof(int32_t) * (E + 1)), "alloc");
-  CK(c->nb_tmp.ensure(sizeof(int32_t) * (E + 1)), "alloc");
+  CK(c->nb_idx2.ensure_slack(sizeof(int32_t) * (E + 1), 2), "alloc");
+  CK(c->nb_tmp.ensure_slack(sizeof(int32_t) * (E + 1), 2), "alloc");
   CK(launch_nb_update2(c, d_sph, N, N_old, bx, cnt, c->nb_len.as<int32_t>(), o_off, o_idx, off,
                        c->nb_tmp.as<int32_t>(), c->nb_idx2.as<int32_t>()),
      "neighbors update");
   unsigned long long h_st[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(h_st, c->nb_stats, sizeof(h_st), cudaMemcpyDeviceToHost, c->stream), "download");
-  CK(c->nb_prev.ensure(sizeof(double) * 4 * N), "alloc");  // (all old spheres were checked)
+  CK(c->nb_prev.ensure_slack(sizeof(double) * 4 * N, 2), "alloc");  // (all old spheres were checked)
   CK(cudaMemcpyAsync(c->nb_prev.p, d_sph, sizeof(double) * 4 * N, cudaMemcpyDeviceToDevice,
                      c->stream), "copy");
   CK(cudaStreamSynchronize(c->stream), "neighbors update");

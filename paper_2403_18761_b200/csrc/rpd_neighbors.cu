@@ -1016,6 +1016,8 @@ static int nb_heavy_items(int dflt) {
   return s ? atoi(s) : dflt;
 }
 constexpr int NB_HEAVY_DEFAULT = 8192;  // (C3 / C5 sweep: DESIGN.md §10)
+constexpr int NB_HEAVY_UPDATE = 2048;   // incremental updates with more new rows than:
+constexpr int NB_UPDATE_ALL_BLOCKS = 2048;
 
 // the block kernel over the heavy rows (device count; persistent grid, at most n_max blocks)
 static cudaError_t nb_launch_heavy(rpd_ctx* c, const NbArgs& A, int64_t n_max) {
@@ -1042,7 +1044,8 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
                        sizeof(int32_t) * (size_t)N * NB_CAP1 + sizeof(unsigned long long) * 4 +
                        sizeof(double4) * (N + 1) + sizeof(int32_t) * (3 * (NB_RB + 1) + 2 + N + 1) +
                        sizeof(int32_t) * (N + 1 + 4) + 1024;
-  cudaError_t e = c->nb_buf.ensure(bytes);
+  // (2x on a reallocation: incremental updates grow N a batch at a time)
+  cudaError_t e = c->nb_buf.ensure_slack(bytes, 2);
   if (e) return e;
   char* b = c->nb_buf.as<char>();
   auto take = [&](size_t n) {
@@ -1344,8 +1347,9 @@ cudaError_t launch_nb_update1(rpd_ctx* c, const double* sph, int64_t N, int64_t 
   int mb = 0;
   if ((e = nb_build(c, sph, N, box, cnt, &A, &mb))) return e;
   const int64_t M = N - N_old;
-  // few new rows (latency): every one on a block; else pass 1 with the heavy-row hand-off
-  A.heavy_items = nb_heavy_items(M <= 4 * (int64_t)c->sms ? -1 : NB_HEAVY_DEFAULT);
+  // few new rows (latency): every one on a block; else pass 1 with the heavy-row hand-off at
+  // a lower threshold than the full recompute's (the GPU is not full: latency decides)
+  A.heavy_items = nb_heavy_items(M <= NB_UPDATE_ALL_BLOCKS ? -1 : NB_HEAVY_UPDATE);
   const int ib = (int)std::min<int64_t>((M + 255) / 256 + 1, 4 * (int64_t)c->sms);
   if (A.heavy_items < 0) {
     k_nb_iota<<<ib, 256, 0, c->stream>>>(A.heavy_ids, N_old, M, A.n_heavy);
