@@ -132,3 +132,34 @@ def test_c4_chain_every_tet(ctx, c4_workload, oracle_c4_chain):
                                label=f"iteration {it}: ")
         assert not errs, errs[:5]
         n_old = len(sph)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_c4_chain_every_tet_other_seeds(seed):
+    """The C4 workload of seeds 1 and 2 (seeds 0, 1, 2 per config; bench.py
+    --seed, tools/seeds.py) as the bench runs it (pruned filter, graph updates): the C3 full
+    RPD and the 10 x 500 chain equal the oracle's on every tet after every iteration."""
+    import paper_2403_18761_b200 as P
+    P.build()
+    w = W.make_config("C4", seed=seed)
+    c = P.RPDContext(0, filter_mode="pruned")
+    try:
+        c.relations(w.verts, w.tets, w.spheres, w.nbr_off, w.nbr_idx)
+        c.clip()
+        prev = oracle.rpd_workload(w)
+        errs = compare_results(gpu_state(c), prev, w.verts, w.tets, rel=1e-9)
+        assert not errs, errs[:5]
+        n_old = w.N
+        for it, (sph, off, idx) in enumerate(w.batches):
+            new = np.arange(n_old, len(sph), dtype=np.int32)
+            counts, nd = c.update_partial(sph, off, idx, new)
+            prev, dirty = oracle.partial_update(prev, w.verts, w.tets, sph, off, idx, n_old)
+            assert nd == len(dirty)
+            assert np.array_equal(c.dirty_tets().cpu().numpy(), dirty), it
+            errs = compare_results(gpu_state(c), prev, w.verts, w.tets, rel=1e-9,
+                                   label=f"seed {seed} iteration {it}: ")
+            assert not errs, errs[:5]
+            n_old = len(sph)
+        assert c.stats()["graph_updates"] == len(w.batches)
+    finally:
+        c.close()
