@@ -291,3 +291,31 @@ def test_neighbors_block_rows_incremental(ctx, monkeypatch):
                      for (sp, _, _) in w.batches[:3]]
     for (a, b), (c, d) in zip(res[0], res[-1]):
         assert np.array_equal(a, c) and np.array_equal(b, d)
+
+
+def _shell(n=400, seed=0):
+    """A big central sphere inside a shell of n small ones (Fibonacci directions): the central
+    row lists every shell sphere (longer than the 256-entry pass-1 slab: pass 2)."""
+    k = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * k / n)
+    th = np.pi * (1 + 5 ** 0.5) * k
+    d = np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+    c = np.array([16.0, 16.0, 16.0])
+    sp = np.concatenate([[[*c, 6.0]], np.c_[c + 10.0 * d, np.full(n, 0.5)]])
+    return np.round(sp * 1024) / 1024, (0, 0, 0, 32, 32, 32)  # (on the oracle's lattice)
+
+
+def test_neighbors_long_row_block_and_warp(ctx, monkeypatch):
+    """A row longer than the pass-1 slab (pass 2 recomputes it on a warp): with every row on a
+    block in pass 1 (RPD_NB_HEAVY=-1) the recomputed row has the same length (no
+    ERR_NB_RECOMPUTE) and the lists equal the all-warp ones; the long row lists every shell
+    sphere and contains the oracle's row."""
+    sp, box = _shell()
+    o0, i0, g0 = _lists(ctx, sp, box, 0, monkeypatch)
+    o1, i1, g1 = _lists(ctx, sp, box, -1, monkeypatch)
+    assert g1["n_rows_block"] > 0
+    assert np.array_equal(o0, o1) and np.array_equal(i0, i1)
+    assert o0[1] - o0[0] > 256
+    assert set(range(1, len(sp))) <= set(i0[o0[0]:o0[1]].tolist())
+    roff, ridx = oracle.box_neighbours(sp, box)
+    assert set(ridx[roff[0]:roff[1]].tolist()) <= set(i0[o0[0]:o0[1]].tolist())
