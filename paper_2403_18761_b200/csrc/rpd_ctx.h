@@ -336,6 +336,7 @@ struct rpd_ctx {
   int32_t *nb_start = nullptr, *nb_items = nullptr, *nb_long = nullptr, *nb_long_ids = nullptr,
           *nb_slab = nullptr;
   double nb_args_tol0 = 0.0;
+  int nb_ball_test = 1;  // the neighbour enumeration's ball pre-test of the last nb_build (pass 2 matches it)
   void* nb_dbg = nullptr;
   void* nb_sorted = nullptr;  // double4 per sphere in cell order  // development aid: device int64 [N][8] per-sphere counters
   int64_t nb_N = -1, nb_E = 0;

@@ -256,6 +256,7 @@ struct NbArgs {
   int32_t* heavy_ids;  // [N]
   int32_t* n_heavy;    // their count
   int32_t* work2;      // the block kernel's work counter
+  int ball_test;       // enumeration: skip plane pairs whose line misses the previous ball
 };
 
 // The per-sphere computation runs on a warp (NT = 32) or on a block of NT threads (heavy
@@ -491,6 +492,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     }
     gsync();
     const int n_pairs = M * (M - 1) / 2;
+    const bool ball_ok = A.ball_test && first_new > 0;  // (a previous round's ball exists)
     for (int q = tid; q < n_pairs; q += NT) {
       int a = 0, rem = q;
       while (rem >= M - 1 - a) {
@@ -501,6 +503,20 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
       const double4 pa = S.pl[a], pb = S.pl[b];
       const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
                    ab_z = pa.x * pb.y - pa.y * pb.x;
+      if (ball_ok) {
+        // refinement rounds: P_K only shrinks, so every vertex of the new P_K lies in the
+        // previous round's ball (centre c, radius rs: error radii included); a pair whose
+        // line a ∩ b passes farther from c than rs (+ slack) carries none.  Squared distance
+        // of c to the line, no division: (ha^2 + hb^2 - 2 cab ha hb) / |n_a x n_b|^2
+        const double D2 = ab_x * ab_x + ab_y * ab_y + ab_z * ab_z;
+        if (D2 >= 1e-6) {
+          const double ha = pa.x * cx + pa.y * cy + pa.z * cz + pa.w;
+          const double hb = pb.x * cx + pb.y * cy + pb.z * cz + pb.w;
+          const double cab = pa.x * pb.x + pa.y * pb.y + pa.z * pb.z;
+          const double rr = rs + 1e-7 * (L + fabs(pa.w) + fabs(pb.w));
+          if (ha * ha + hb * hb - 2.0 * cab * ha * hb > rr * rr * D2) continue;
+        }
+      }
       for (int cc = max(b + 1, first_new); cc < M; ++cc) {
         const double4 pc = S.pl[cc];
         ++n_tri;
@@ -1127,6 +1143,11 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   A.dbg = (long long*)c->nb_dbg;
   A.ball = c->nb_ball.as<double4>();
   A.heavy_items = nb_heavy_items(NB_HEAVY_DEFAULT);
+  {
+    const char* bt = getenv("RPD_NB_BALLT");
+    A.ball_test = bt ? atoi(bt) : 1;
+  }
+  c->nb_ball_test = A.ball_test;
   A.heavy_ids = hvy_ids;
   A.n_heavy = hvy;
   A.work2 = hvy + 1;
@@ -1187,6 +1208,7 @@ cudaError_t launch_neighbors_pass2_rows(rpd_ctx* c, const double* sph, int64_t N
     A.bhi[k] = box[3 + k];
   }
   A.tol0 = c->nb_args_tol0;
+  A.ball_test = c->nb_ball_test;
   A.cnt = cnt;
   A.slab = c->nb_slab;
   A.off = off;
