@@ -60,7 +60,7 @@ struct NbSmem {
   double4 vx[NB_MAXV];        // y, error radius
   int out[NB_CAP1];
   int kid[NB_KSEL];
-  int n_v, n_o, flags, first;
+  int n_v, n_o, flags, first, n_pair;
 };
 
 // per-lane smallest NB_TOPL keys (ties: smaller id), kept sorted; deterministic because every
@@ -463,88 +463,212 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     // P_old ∩ new planes, planes [first_new, M) new): the old vertices that satisfy the new
     // planes (every old vertex lies on >= 3 kept facet planes), plus the triples whose largest
     // index is a new plane.  thread = pair (a, b)
-    if (w0) {
-      if (first_new > 0) {
-        int kept = 0;
-        for (int c0 = 0; c0 < n_v; c0 += 32) {
-          const int s2 = c0 + lane;
-          bool ok = false;
-          double4 v = make_double4(0, 0, 0, 0);
-          if (s2 < n_v) {
-            v = S.vx[s2];
-            ok = true;
-            for (int k = first_new; k < M && ok; ++k) {
+    if (A.ball_test & 2) {
+      // Sequential clip (default): P_K is cut by one new plane c at a time.  A vertex of
+      // P ∩ {h_c >= 0} is a vertex of P on the kept side or lies on an edge a ∩ b of P that
+      // crosses h_c = 0, whose removed endpoint u is a vertex of P tight at a and b.  So the
+      // new vertices are the triples (a, b, c) over the pairs of planes tight at the vertices
+      // that h_c may remove -- with margins: "may remove" is h_c < 2 m_v, "tight" |h| <= 2 m_v,
+      // kept is h_c >= -m_v (m_v = e_v + tol0 + 8 eps |w|, the keep margin of the enumeration).
+      // Every true vertex of the true polytope stays recorded within its error radius after
+      // each cut, as with the triple enumeration, whose
+      // triples (a, b, c) below are a subset; runs on warp 0.
+      if (w0) {
+        unsigned* const pm = reinterpret_cast<unsigned*>(S.key);  // pair bits (S.key free here)
+        int* const plist = S.out;                                  // pair list (free here)
+        constexpr double EPS = 1.1102230246251565e-16;
+        // the triple a ∩ b ∩ c: y, error radius; false if (near) singular
+        auto solve3 = [&](const double4& pa, const double4& pb, const double4& pc,
+                          double4& y) -> bool {
+          const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
+                       ab_z = pa.x * pb.y - pa.y * pb.x;
+          const double det = pc.x * ab_x + pc.y * ab_y + pc.z * ab_z;
+          if (fabs(det) < 1e-13) return false;
+          const double bc_x = pb.y * pc.z - pb.z * pc.y, bc_y = pb.z * pc.x - pb.x * pc.z,
+                       bc_z = pb.x * pc.y - pb.y * pc.x;
+          const double ca_x = pc.y * pa.z - pc.z * pa.y, ca_y = pc.z * pa.x - pc.x * pa.z,
+                       ca_z = pc.x * pa.y - pc.y * pa.x;
+          const double inv = -1.0 / det;
+          y.x = (pa.w * bc_x + pb.w * ca_x + pc.w * ab_x) * inv;
+          y.y = (pa.w * bc_y + pb.w * ca_y + pc.w * ab_y) * inv;
+          y.z = (pa.w * bc_z + pb.w * ca_z + pc.w * ab_z) * inv;
+          y.w = 64.0 * EPS * (fabs(pa.w) + fabs(pb.w) + fabs(pc.w) + L) / fabs(det);
+          return true;
+        };
+        int nv = n_v, c0 = first_new;
+        bool over = false;
+        if (first_new == 0) {  // round 0 (or after a box fallback): start from the box
+          if (lane < 8) {
+            double4 y;
+            solve3(S.pl[lane & 1], S.pl[2 + ((lane >> 1) & 1)], S.pl[4 + ((lane >> 2) & 1)], y);
+            S.vx[lane] = y;
+          }
+          nv = 8;
+          c0 = 6;
+          __syncwarp();
+        }
+        for (int c = c0; c < M && nv > 0 && !over; ++c) {
+          const double4 pc = S.pl[c];
+          const double mc = A.tol0 + 8.0 * EPS * fabs(pc.w);
+          const int nwp = (c * (c - 1) / 2 + 31) >> 5;
+          for (int q = lane; q < nwp; q += 32) pm[q] = 0u;
+          if (lane == 0) S.n_pair = 0;
+          __syncwarp();
+          // (a) the pairs of planes tight at the vertices h_c may remove (deduplicated)
+          for (int s2 = lane; s2 < nv; s2 += 32) {
+            const double4 v = S.vx[s2];
+            if (pc.x * v.x + pc.y * v.y + pc.z * v.z + pc.w >= 2.0 * (v.w + mc)) continue;
+            unsigned long long tm = 0;
+            for (int k = 0; k < c; ++k) {
               const double4 pk = S.pl[k];
-              ok = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w >=
-                   -(v.w + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+              const double h = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w;
+              if (h <= 2.0 * (v.w + A.tol0 + 8.0 * EPS * fabs(pk.w))) tm |= 1ull << k;
+            }
+            for (unsigned long long ma = tm; ma; ma &= ma - 1) {
+              const int a = __ffsll((long long)ma) - 1;
+              for (unsigned long long mb = ma & (ma - 1); mb; mb &= mb - 1) {
+                const int b = __ffsll((long long)mb) - 1;
+                const int q = a * (2 * c - a - 1) / 2 + (b - a - 1);
+                const unsigned bit = 1u << (q & 31);
+                if (!(atomicOr(&pm[q >> 5], bit) & bit)) {
+                  const int t = atomicAdd(&S.n_pair, 1);
+                  if (t < NB_CAP1) plist[t] = a | (b << 8);
+                }
+              }
             }
           }
-          const unsigned m = __ballot_sync(0xffffffffu, ok);
           __syncwarp();
-          if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;  // in place: <= s2
-          kept += __popc(m);
+          const int np = S.n_pair;
+          if (np > NB_CAP1) {
+            over = true;
+            break;
+          }
+          // (b) the kept vertices, compacted in place (in order)
+          int kept = 0;
+          for (int b0 = 0; b0 < nv; b0 += 32) {
+            const int s2 = b0 + lane;
+            double4 v = make_double4(0, 0, 0, 0);
+            bool ok = false;
+            if (s2 < nv) {
+              v = S.vx[s2];
+              ok = pc.x * v.x + pc.y * v.y + pc.z * v.z + pc.w >= -(v.w + mc);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            __syncwarp();
+            if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;
+            kept += __popc(m);
+            __syncwarp();
+          }
+          if (lane == 0) S.n_v = kept;
+          __syncwarp();
+          // (c) the new vertices (a, b, c) that hold every plane up to c within their margin
+          for (int t = lane; t < np; t += 32) {
+            const int a = plist[t] & 0xff, b = plist[t] >> 8;
+            double4 y;
+            ++n_tri;
+            if (!solve3(S.pl[a], S.pl[b], pc, y)) continue;
+            bool ok = true;
+            for (int k = 0; k < c && ok; ++k) {
+              const double4 pk = S.pl[k];
+              ok = pk.x * y.x + pk.y * y.y + pk.z * y.z + pk.w >=
+                   -(y.w + A.tol0 + 8.0 * EPS * fabs(pk.w));
+            }
+            if (!ok) continue;
+            const int s2 = atomicAdd(&S.n_v, 1);
+            if (s2 < NB_MAXV) S.vx[s2] = y;
+          }
+          __syncwarp();
+          nv = S.n_v;
+          if (nv > NB_MAXV) over = true;
           __syncwarp();
         }
-        if (lane == 0) S.n_v = kept;
-      } else if (lane == 0) {
-        S.n_v = 0;
+        if (lane == 0) S.n_v = over ? NB_MAXV + 1 : nv;
       }
-    }
-    gsync();
-    const int n_pairs = M * (M - 1) / 2;
-    const bool ball_ok = A.ball_test && first_new > 0;  // (a previous round's ball exists)
-    for (int q = tid; q < n_pairs; q += NT) {
-      int a = 0, rem = q;
-      while (rem >= M - 1 - a) {
-        rem -= M - 1 - a;
-        ++a;
-      }
-      const int b = a + 1 + rem;
-      const double4 pa = S.pl[a], pb = S.pl[b];
-      const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
-                   ab_z = pa.x * pb.y - pa.y * pb.x;
-      if (ball_ok) {
-        // refinement rounds: P_K only shrinks, so every vertex of the new P_K lies in the
-        // previous round's ball (centre c, radius rs: error radii included); a pair whose
-        // line a ∩ b passes farther from c than rs (+ slack) carries none.  Squared distance
-        // of c to the line, no division: (ha^2 + hb^2 - 2 cab ha hb) / |n_a x n_b|^2
-        const double D2 = ab_x * ab_x + ab_y * ab_y + ab_z * ab_z;
-        if (D2 >= 1e-6) {
-          const double ha = pa.x * cx + pa.y * cy + pa.z * cz + pa.w;
-          const double hb = pb.x * cx + pb.y * cy + pb.z * cz + pb.w;
-          const double cab = pa.x * pb.x + pa.y * pb.y + pa.z * pb.z;
-          const double rr = rs + 1e-7 * (L + fabs(pa.w) + fabs(pb.w));
-          if (ha * ha + hb * hb - 2.0 * cab * ha * hb > rr * rr * D2) continue;
+      gsync();
+    } else {  // the triple enumeration (RPD_NB_SEQ=0)
+      if (w0) {
+        if (first_new > 0) {
+          int kept = 0;
+          for (int c0 = 0; c0 < n_v; c0 += 32) {
+            const int s2 = c0 + lane;
+            bool ok = false;
+            double4 v = make_double4(0, 0, 0, 0);
+            if (s2 < n_v) {
+              v = S.vx[s2];
+              ok = true;
+              for (int k = first_new; k < M && ok; ++k) {
+                const double4 pk = S.pl[k];
+                ok = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w >=
+                     -(v.w + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+              }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            __syncwarp();
+            if (ok) S.vx[kept + __popc(m & ((1u << lane) - 1u))] = v;  // in place: <= s2
+            kept += __popc(m);
+            __syncwarp();
+          }
+          if (lane == 0) S.n_v = kept;
+        } else if (lane == 0) {
+          S.n_v = 0;
         }
       }
-      for (int cc = max(b + 1, first_new); cc < M; ++cc) {
-        const double4 pc = S.pl[cc];
-        ++n_tri;
-        const double det = pc.x * ab_x + pc.y * ab_y + pc.z * ab_z;
-        if (fabs(det) < 1e-13) continue;
-        const double bc_x = pb.y * pc.z - pb.z * pc.y, bc_y = pb.z * pc.x - pb.x * pc.z,
-                     bc_z = pb.x * pc.y - pb.y * pc.x;
-        const double ca_x = pc.y * pa.z - pc.z * pa.y, ca_y = pc.z * pa.x - pc.x * pa.z,
-                     ca_z = pc.x * pa.y - pc.y * pa.x;
-        const double inv = -1.0 / det;
-        const double yx = (pa.w * bc_x + pb.w * ca_x + pc.w * ab_x) * inv;
-        const double yy = (pa.w * bc_y + pb.w * ca_y + pc.w * ab_y) * inv;
-        const double yz = (pa.w * bc_z + pb.w * ca_z + pc.w * ab_z) * inv;
-        // error radius: rounding of the offsets and cofactors amplified by 1/|det|
-        const double ev = 64.0 * 1.1102230246251565e-16 *
-                          (fabs(pa.w) + fabs(pb.w) + fabs(pc.w) + L) / fabs(det);
-        bool ok = true;
-        for (int k = 0; k < M && ok; ++k) {
-          const double4 pk = S.pl[k];
-          const double h = pk.x * yx + pk.y * yy + pk.z * yz + pk.w;
-          ok = h >= -(ev + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+      gsync();
+      const int n_pairs = M * (M - 1) / 2;
+      const bool ball_ok = (A.ball_test & 1) && first_new > 0;  // (a previous round's ball exists)
+      for (int q = tid; q < n_pairs; q += NT) {
+        int a = 0, rem = q;
+        while (rem >= M - 1 - a) {
+          rem -= M - 1 - a;
+          ++a;
         }
-        if (!ok) continue;
-        const int s2 = atomicAdd(&S.n_v, 1);
-        if (s2 < NB_MAXV) S.vx[s2] = make_double4(yx, yy, yz, ev);
+        const int b = a + 1 + rem;
+        const double4 pa = S.pl[a], pb = S.pl[b];
+        const double ab_x = pa.y * pb.z - pa.z * pb.y, ab_y = pa.z * pb.x - pa.x * pb.z,
+                     ab_z = pa.x * pb.y - pa.y * pb.x;
+        if (ball_ok) {
+          // refinement rounds: P_K only shrinks, so every vertex of the new P_K lies in the
+          // previous round's ball (centre c, radius rs: error radii included); a pair whose
+          // line a ∩ b passes farther from c than rs (+ slack) carries none.  Squared distance
+          // of c to the line, no division: (ha^2 + hb^2 - 2 cab ha hb) / |n_a x n_b|^2
+          const double D2 = ab_x * ab_x + ab_y * ab_y + ab_z * ab_z;
+          if (D2 >= 1e-6) {
+            const double ha = pa.x * cx + pa.y * cy + pa.z * cz + pa.w;
+            const double hb = pb.x * cx + pb.y * cy + pb.z * cz + pb.w;
+            const double cab = pa.x * pb.x + pa.y * pb.y + pa.z * pb.z;
+            const double rr = rs + 1e-7 * (L + fabs(pa.w) + fabs(pb.w));
+            if (ha * ha + hb * hb - 2.0 * cab * ha * hb > rr * rr * D2) continue;
+          }
+        }
+        for (int cc = max(b + 1, first_new); cc < M; ++cc) {
+          const double4 pc = S.pl[cc];
+          ++n_tri;
+          const double det = pc.x * ab_x + pc.y * ab_y + pc.z * ab_z;
+          if (fabs(det) < 1e-13) continue;
+          const double bc_x = pb.y * pc.z - pb.z * pc.y, bc_y = pb.z * pc.x - pb.x * pc.z,
+                       bc_z = pb.x * pc.y - pb.y * pc.x;
+          const double ca_x = pc.y * pa.z - pc.z * pa.y, ca_y = pc.z * pa.x - pc.x * pa.z,
+                       ca_z = pc.x * pa.y - pc.y * pa.x;
+          const double inv = -1.0 / det;
+          const double yx = (pa.w * bc_x + pb.w * ca_x + pc.w * ab_x) * inv;
+          const double yy = (pa.w * bc_y + pb.w * ca_y + pc.w * ab_y) * inv;
+          const double yz = (pa.w * bc_z + pb.w * ca_z + pc.w * ab_z) * inv;
+          // error radius: rounding of the offsets and cofactors amplified by 1/|det|
+          const double ev = 64.0 * 1.1102230246251565e-16 *
+                            (fabs(pa.w) + fabs(pb.w) + fabs(pc.w) + L) / fabs(det);
+          bool ok = true;
+          for (int k = 0; k < M && ok; ++k) {
+            const double4 pk = S.pl[k];
+            const double h = pk.x * yx + pk.y * yy + pk.z * yz + pk.w;
+            ok = h >= -(ev + A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(pk.w));
+          }
+          if (!ok) continue;
+          const int s2 = atomicAdd(&S.n_v, 1);
+          if (s2 < NB_MAXV) S.vx[s2] = make_double4(yx, yy, yz, ev);
+        }
       }
+      gsync();
     }
-    gsync();
     dbg_enum += clock64() - t_enum;
     n_v = S.n_v;
     if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
@@ -1144,8 +1268,11 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   A.ball = c->nb_ball.as<double4>();
   A.heavy_items = nb_heavy_items(NB_HEAVY_DEFAULT);
   {
+    // bit 0: the ball pre-test of the triple enumeration's refinement pairs; bit 1: the
+    // sequential clip in place of the triple enumeration (RPD_NB_SEQ=0: the enumeration)
     const char* bt = getenv("RPD_NB_BALLT");
-    A.ball_test = bt ? atoi(bt) : 1;
+    const char* sq = getenv("RPD_NB_SEQ");
+    A.ball_test = (bt ? (atoi(bt) & 1) : 1) | ((sq ? atoi(sq) : 1) ? 2 : 0);
   }
   c->nb_ball_test = A.ball_test;
   A.heavy_ids = hvy_ids;
