@@ -315,7 +315,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
   const long long t_start = clock64();
   unsigned long long g_start = 0;
   if (!BLK && A.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
-  long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0, dbg_enum = 0;
+  long long dbg_scan = 0, dbg_cells = 0, dbg_vloop = 0, dbg_enum = 0, dbg_sclk = 0;
   int dbg_rounds = 0;
   // ---- 1. ring collection of candidates for K (and the hiding test): warp 0
   if (w0) {
@@ -515,9 +515,11 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
           if (lane == 0) S.n_pair = 0;
           __syncwarp();
           // (a) the pairs of planes tight at the vertices h_c may remove (deduplicated)
+          bool cuts = false;
           for (int s2 = lane; s2 < nv; s2 += 32) {
             const double4 v = S.vx[s2];
             if (pc.x * v.x + pc.y * v.y + pc.z * v.z + pc.w >= 2.0 * (v.w + mc)) continue;
+            cuts = true;
             unsigned long long tm = 0;
             for (int k = 0; k < c; ++k) {
               const double4 pk = S.pl[k];
@@ -538,6 +540,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
             }
           }
           __syncwarp();
+          if (!__any_sync(0xffffffffu, cuts)) continue;  // h_c >= 2 m_v at every vertex: P unchanged
           const int np = S.n_pair;
           if (np > NB_CAP1) {
             over = true;
@@ -848,20 +851,23 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     auto visit = [&](int p, double& key, int& jo) -> int {
       const int j = A.items[p];
       jo = j;
-      dbg_cells += 1;
+      dbg_cells += 1 + (n_list < 0 ? (1ll << 32) : 0ll);
       if (j == i) return 0;
       const double4 sj = A.sorted[p];
       const double ux = sj.x - si.x, uy = sj.y - si.y, uz = sj.z - si.z, rj = sj.w;
       const double u2 = ux * ux + uy * uy + uz * uz;
       if (u2 == 0.0 || u2 > R * R) return 0;
-      {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack)
-        const double Rj = (rho_v + sqrt(fmax(pdm_v, 0.0) + rj * rj)) * (1.0 + 1e-9) +
-                          4.0 * (evm_v + A.tol0) + 1e-9 * L;
-        if (u2 > Rj * Rj) return 0;
-      }
       const double un = sqrt(u2);
-      const double ax = -ux / un, ay = -uy / un, az = -uz / un;
-      const double bw = (u2 - rj * rj + si.w * si.w) / (2.0 * un);
+      {  // j reaches a vertex v only if |v - theta_j|^2 <= PD_i(v) + r_j^2 (+ slack):
+         // |theta_j - theta_i| <= (rho + sqrt(PDmax + r_j^2)) (1 + 1e-9) + 4 (e_max + tol0) + 1e-9 L,
+         // tested without a second square root (the right side's relative margin doubled)
+        const double d = un - rho_v * (1.0 + 1e-9) - 4.0 * (evm_v + A.tol0) - 1e-9 * L;
+        if (d > 0.0 && d * d > (fmax(pdm_v, 0.0) + rj * rj) * ((1.0 + 2e-9) * (1.0 + 2e-9)))
+          return 0;
+      }
+      const double iun = 1.0 / un;
+      const double ax = -ux * iun, ay = -uy * iun, az = -uz * iun;
+      const double bw = (u2 - rj * rj + si.w * si.w) * (0.5 * iun);
       const double slack = A.tol0 + 8.0 * 1.1102230246251565e-16 * fabs(bw);
       ++dbg_scan;
       const double hcen = ax * cx + ay * cy + az * cz + bw;  // plane value at the centre
@@ -872,12 +878,26 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
       // final round: a hit once some vertex is within slack; earlier rounds: a deep cut once
       // some vertex is cut by more than tolF (ranked by the value at the centre)
       const double thr = final_round ? slack : -tolF;
+      // (4 vertices per step: the test after a step only sees a smaller minimum, so both
+      // result bits are those of the vertex-by-vertex loop)
       double depth = 1e300;
-      for (int s2 = 0; s2 < n_v; ++s2) {
+      int s2 = 0;
+      bool stop = false;
+      for (; s2 + 4 <= n_v && !stop; s2 += 4) {
+        const double4 v0 = S.vx[s2], v1 = S.vx[s2 + 1], v2 = S.vx[s2 + 2], v3 = S.vx[s2 + 3];
+        const double h0 = ax * v0.x + ay * v0.y + az * v0.z + bw - v0.w;
+        const double h1 = ax * v1.x + ay * v1.y + az * v1.z + bw - v1.w;
+        const double h2 = ax * v2.x + ay * v2.y + az * v2.z + bw - v2.w;
+        const double h3 = ax * v3.x + ay * v3.y + az * v3.z + bw - v3.w;
+        depth = fmin(depth, fmin(fmin(h0, h1), fmin(h2, h3)));
+        dbg_vloop += 4;
+        stop = final_round ? depth <= thr : depth < thr;
+      }
+      for (; s2 < n_v && !stop; ++s2) {
         const double4 v = S.vx[s2];
         depth = fmin(depth, ax * v.x + ay * v.y + az * v.z + bw - v.w);
         ++dbg_vloop;
-        if (final_round ? depth <= thr : depth < thr) break;
+        stop = final_round ? depth <= thr : depth < thr;
       }
       key = hcen;
       return (depth <= slack ? 1 : 0) | (!final_round && depth < -tolF ? 2 : 0);
@@ -920,6 +940,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
       }
     };
     int n_hit = 0;  // hits recorded this round (> NB_HCAP: overflow)
+    const long long t_scan = clock64();
     if (n_list >= 0) {  // ---- scan the previous round's hits, compacted in place
       ++dbg_rounds;
       for (int t0 = 0; t0 < n_list; t0 += NT) {
@@ -969,6 +990,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     }
     n_list = n_hit <= NB_HCAP ? n_hit : -1;
     gsync();
+    dbg_sclk += clock64() - t_scan;
     if (final_round) break;
     if constexpr (BLK) {  // the 32 virtual lanes' candidate lists: thread t -> lane t mod 32
       for (int t = 0; t < 4; ++t) {
@@ -1046,20 +1068,20 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     for (int o = 16; o; o >>= 1) {
       dbg_scan += __shfl_xor_sync(0xffffffffu, dbg_scan, o);
       dbg_vloop += __shfl_xor_sync(0xffffffffu, dbg_vloop, o);
+      dbg_cells += __shfl_xor_sync(0xffffffffu, dbg_cells, o);
     }
     if (lane == 0) {
       long long* d = A.dbg + 8 * (long long)i;
       d[0] = clock64() - t_start;
       d[1] = dbg_rounds;
       d[2] = dbg_enum;  // cycles in the vertex enumeration (lane 0)
-      d[3] = dbg_scan;
+      d[3] = dbg_sclk;  // cycles in the ball scans (lane 0)
       d[4] = dbg_vloop;
       d[5] = n_v;
-      d[6] = n_o;
+      d[6] = dbg_cells;  // items visited by the scans (grid scans << 32)
       d[7] = (long long)g_start;  // start (ns, global timer)
     }
   }
-  (void)dbg_cells;
   if (!PASS2) {
     if (tid == 0) {
       A.cnt[i] = n_o;
@@ -1155,7 +1177,7 @@ static int nb_heavy_items(int dflt) {
   const char* s = getenv("RPD_NB_HEAVY");
   return s ? atoi(s) : dflt;
 }
-constexpr int NB_HEAVY_DEFAULT = 8192;  // (C3 / C5 sweep: DESIGN.md §10)
+constexpr int NB_HEAVY_DEFAULT = 0;  // no hand-off in a full recompute (C3 / C5 sweep: DESIGN.md §10)
 constexpr int NB_HEAVY_UPDATE = 2048;   // incremental updates with more new rows than:
 constexpr int NB_UPDATE_ALL_BLOCKS = 2048;
 

@@ -13,8 +13,10 @@ w = W.make_config(sys.argv[1] if len(sys.argv) > 1 else "C3")
 ctx = P.RPDContext(0)
 g = ctx.neighbors(w.spheres, W.mesh_box(w.verts))
 d = np.fromfile("gpurun_out/nb_dbg.bin", dtype=np.int64).reshape(-1, 8)
-names = ["clk", "rounds", "enum_clk", "scan", "vloop", "n_v", "n_o", "start_ns"]
-print("total clk", d[:, 0].sum(), "max", d[:, 0].max(), "enum share", d[:, 2].sum() / d[:, 0].sum())
+d = np.concatenate([d, (d[:, 6] >> 32)[:, None]], axis=1)
+d[:, 6] &= 0xffffffff
+names = ["clk", "rounds", "enum_clk", "scan_clk", "vloop", "n_v", "visits", "start_ns", "visits_grid"]
+print("total clk", d[:, 0].sum(), "max", d[:, 0].max(), "enum share", d[:, 2].sum() / d[:, 0].sum(), "scan share", d[:, 3].sum() / d[:, 0].sum())
 for k, n in enumerate(names):
     print(f"{n:8s} mean {d[:, k].mean():12.1f} p50 {np.median(d[:, k]):10.0f} p99 {np.percentile(d[:, k], 99):10.0f} max {d[:, k].max():10d}")
 o = np.argsort(-d[:, 0])[:10]
