@@ -1094,7 +1094,12 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
   }
 }
 
-__global__ void __launch_bounds__(32 * NB_WARPS) k_nb_pass1(NbArgs A) {
+#ifdef RPD_NB_MINB  // min resident blocks of pass 1 (a register budget; A/B knob)
+#define NB_PASS1_BOUNDS __launch_bounds__(32 * NB_WARPS, RPD_NB_MINB)
+#else
+#define NB_PASS1_BOUNDS __launch_bounds__(32 * NB_WARPS)
+#endif
+__global__ void NB_PASS1_BOUNDS k_nb_pass1(NbArgs A) {
   __shared__ NbSm<32> sm[NB_WARPS];
   if (*(volatile int*)A.err != 0) {  // invalid input: empty rows, no dereference of NaN cells
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.N;
