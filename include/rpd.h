@@ -516,9 +516,10 @@ typedef struct {
   int64_t N, E;
   int64_t n_hidden, n_vertex_overflow;
   int64_t n_rows_computed;  /* rows computed by this call (N for rpd_neighbors) */
-  int64_t n_rows_block;     /* of these, rows computed by a whole block (heavy rows: more than
-                               RPD_NB_HEAVY = 2048 spheres in their first search ball; the
-                               same rows as a warp would give) */
+  int64_t n_rows_block;     /* of these, rows computed by a whole block (the new rows of an
+                               incremental update of at most 2048 spheres, or rows with more
+                               than RPD_NB_HEAVY spheres in their first search ball; the same
+                               rows as a warp would give) */
 } rpd_nbr_lists;
 rpd_status rpd_neighbors(rpd_ctx* ctx, const double* spheres, int64_t N, const double* box,
                          rpd_nbr_lists* out);
