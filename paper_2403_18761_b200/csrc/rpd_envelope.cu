@@ -354,7 +354,13 @@ __global__ void k_env_box(int64_t S, const double* __restrict__ smp, int64_t N,
 struct TileRanges {
   int64_t tb[4];   // kind k owns tiles [tb[k], tb[k+1])
   int64_t pb[4];   // and sorted primitives [pb[k], pb[k+1])
+  int64_t sb[4];   // and super tiles [sb[k], sb[k+1]) (ENV_SUP consecutive tiles each)
 };
+
+#ifndef RPD_ENV_SUP
+#define RPD_ENV_SUP 16  // tiles per super tile (0: no super tiles; A/B knob)
+#endif
+constexpr int ENV_SUP = RPD_ENV_SUP > 0 ? RPD_ENV_SUP : 1;
 
 constexpr unsigned long long MORTON_MASK = (1ull << 62) - 1ull;
 
@@ -397,6 +403,53 @@ __global__ void k_env_tiles(TileRanges R, const EnvPrim* __restrict__ prims,
   tile_key[t] = keys[begin] & MORTON_MASK;
 }
 
+// super tiles: ENV_SUP consecutive tiles of one kind, the union of their boxes and their
+// largest radius (first / count: the tile range)
+__global__ void k_env_supers(TileRanges R, const EnvTile* __restrict__ tiles,
+                             EnvTile* __restrict__ sup) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= R.sb[3]) return;
+  int kind = 0;
+  while (kind < 2 && t >= R.sb[kind + 1]) ++kind;
+  const int64_t begin = R.tb[kind] + (t - R.sb[kind]) * ENV_SUP;
+  const int64_t end = min(begin + (int64_t)ENV_SUP, R.tb[kind + 1]);
+  EnvTile U;
+  for (int c = 0; c < 3; ++c) {
+    U.lo[c] = U.clo[c] = 1e300;
+    U.hi[c] = U.chi[c] = -1e300;
+  }
+  U.rmax = -1e300;
+  U.first = (int)begin;
+  U.count = (int)(end - begin);
+  U.kind = kind;
+  for (int64_t x = begin; x < end; ++x) {
+    const EnvTile T = tiles[x];
+    for (int c = 0; c < 3; ++c) {
+      U.lo[c] = fmin(U.lo[c], T.lo[c]);
+      U.hi[c] = fmax(U.hi[c], T.hi[c]);
+      U.clo[c] = fmin(U.clo[c], T.clo[c]);
+      U.chi[c] = fmax(U.chi[c], T.chi[c]);
+    }
+    U.rmax = fmax(U.rmax, T.rmax);
+  }
+  sup[t] = U;
+}
+
+// a lower bound of the value of every member under box T at p: outside the box of the balls
+// the distance to it (a member lies in the convex hull of its balls, inside that box); inside,
+// the distance to the box of the centres minus the largest radius.  Valid for a super tile's
+// union boxes as well (every member lies in one of its tiles' boxes).
+__device__ __forceinline__ double env_tile_lb(const EnvTile& T, const double* p) {
+  const double db = env_norm(fmax(fmax(T.lo[0] - p[0], p[0] - T.hi[0]), 0.0),
+                             fmax(fmax(T.lo[1] - p[1], p[1] - T.hi[1]), 0.0),
+                             fmax(fmax(T.lo[2] - p[2], p[2] - T.hi[2]), 0.0));
+  if (db > 0.0) return db;
+  return env_norm(fmax(fmax(T.clo[0] - p[0], p[0] - T.chi[0]), 0.0),
+                  fmax(fmax(T.clo[1] - p[1], p[1] - T.chi[1]), 0.0),
+                  fmax(fmax(T.clo[2] - p[2], p[2] - T.chi[2]), 0.0)) -
+         T.rmax;
+}
+
 // One warp per 32 Morton-consecutive samples (lane = sample).  Per kind (spheres, then cones,
 // then slabs) the kind's tiles are visited outward from the warp's place in their Morton
 // order; a tile is skipped when for every lane the distance to the box of its balls exceeds
@@ -408,7 +461,7 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
     int64_t S, const double* __restrict__ smp, const int32_t* __restrict__ sorder,
     const unsigned long long* __restrict__ skey, TileRanges R,
     const EnvTile* __restrict__ tiles, const unsigned long long* __restrict__ tile_key,
-    const EnvPrim* __restrict__ prims, double* __restrict__ g_out,
+    const EnvTile* __restrict__ sup, const EnvPrim* __restrict__ prims, double* __restrict__ g_out,
     int32_t* __restrict__ prim_out, unsigned long long* __restrict__ n_eval) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -438,25 +491,34 @@ __global__ void __launch_bounds__(ENV_WARPS * 32) k_env_dist(
         else hi = mid;
       }
       const int64_t t0 = lo > lo_t ? lo - 1 : lo_t;
-      for (int64_t j = 0;; ++j) {
-        const int64_t up = t0 + (j >> 1), dn = t0 - 1 - (j >> 1);
-        if (up >= hi_t && dn < lo_t) break;
-        const int64_t t = (j & 1) ? dn : up;
-        if (t < lo_t || t >= hi_t) continue;
-        const EnvTile T = tiles[t];
-        // lower bound of every member's value: outside the box of the balls, the distance to
-        // it (the member lies in the convex hull of its balls, inside that box); inside, the
-        // distance to the box of the centres minus the largest radius
-        const double db = env_norm(fmax(fmax(T.lo[0] - p[0], p[0] - T.hi[0]), 0.0),
-                                   fmax(fmax(T.lo[1] - p[1], p[1] - T.hi[1]), 0.0),
-                                   fmax(fmax(T.lo[2] - p[2], p[2] - T.hi[2]), 0.0));
-        const double dc = env_norm(fmax(fmax(T.clo[0] - p[0], p[0] - T.chi[0]), 0.0),
-                                   fmax(fmax(T.clo[1] - p[1], p[1] - T.chi[1]), 0.0),
-                                   fmax(fmax(T.clo[2] - p[2], p[2] - T.chi[2]), 0.0)) -
-                          T.rmax;
-        const double lb = db > 0.0 ? db : dc;
+      // super tiles outward from the warp's place (RPD_ENV_SUP > 0), each needed one's tiles
+      // in order; or every tile outward (RPD_ENV_SUP = 0).  Any visiting order and any valid
+      // culling give the same result: a culled member's value exceeds the lane's best
+      const bool use_sup = RPD_ENV_SUP > 0;
+      const int64_t lo_u = use_sup ? R.sb[kind] : lo_t, hi_u = use_sup ? R.sb[kind + 1] : hi_t;
+      const int64_t u0 = use_sup ? R.sb[kind] + (t0 - lo_t) / ENV_SUP : t0;
+      int64_t t = 0, t_end = 0;  // the current super tile's remaining tiles
+      for (int64_t j = 0;;) {
+        if (t >= t_end) {  // next super tile (or tile) outward
+          const int64_t up = u0 + (j >> 1), dn = u0 - 1 - (j >> 1);
+          if (up >= hi_u && dn < lo_u) break;
+          const int64_t u = (j & 1) ? dn : up;
+          ++j;
+          if (u < lo_u || u >= hi_u) continue;
+          if (!use_sup) {
+            t = u;
+            t_end = u + 1;
+          } else {
+            const EnvTile U = sup[u];
+            const bool need_u = env_tile_lb(U, p) <= best + 1e-9 * (fabs(best) + 1.0);
+            if (!__any_sync(FULL, need_u)) continue;
+            t = U.first;
+            t_end = U.first + U.count;
+          }
+        }
+        const EnvTile T = tiles[t++];
         // (exact up to rounding: a small margin keeps the culling safe)
-        const bool need = lb <= best + 1e-9 * (fabs(best) + 1.0);
+        const bool need = env_tile_lb(T, p) <= best + 1e-9 * (fabs(best) + 1.0);
         unsigned m = __ballot_sync(FULL, need);
         if (!m) continue;
         const bool has = lane < T.count;
@@ -545,9 +607,11 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
       R.tb[k + 1] = R.tb[k] + (cnt[k] + ENV_TILE - 1) / ENV_TILE;
       R.pb[k + 1] = R.pb[k] + cnt[k];
     }
+    R.sb[0] = 0;
+    for (int k = 0; k < 3; ++k) R.sb[k + 1] = R.sb[k] + (R.tb[k + 1] - R.tb[k] + ENV_SUP - 1) / ENV_SUP;
   }
-  const int64_t n_tiles = R.tb[3];
-  const size_t bytes = sizeof(EnvPrim) * 2 * (P + 1) + sizeof(EnvTile) * (n_tiles + 1) +
+  const int64_t n_tiles = R.tb[3], n_sup = R.sb[3];
+  const size_t bytes = sizeof(EnvPrim) * 2 * (P + 1) + sizeof(EnvTile) * (n_tiles + n_sup + 2) +
                        sizeof(unsigned long long) * 2 * (P + S + 2) +
                        sizeof(int32_t) * 2 * (P + S + 2) + sizeof(double) * 8 +
                        sizeof(unsigned long long) * (n_tiles + 1) + 512;
@@ -562,6 +626,7 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
   EnvPrim* prims = reinterpret_cast<EnvPrim*>(take(sizeof(EnvPrim) * (P + 1)));
   EnvPrim* sorted = reinterpret_cast<EnvPrim*>(take(sizeof(EnvPrim) * (P + 1)));
   EnvTile* tiles = reinterpret_cast<EnvTile*>(take(sizeof(EnvTile) * (n_tiles + 1)));
+  EnvTile* sup = reinterpret_cast<EnvTile*>(take(sizeof(EnvTile) * (n_sup + 1)));
   unsigned long long* pk = reinterpret_cast<unsigned long long*>(take(8 * (P + 1)));
   unsigned long long* pk2 = reinterpret_cast<unsigned long long*>(take(8 * (P + 1)));
   int32_t* pi = reinterpret_cast<int32_t*>(take(4 * (P + 1)));
@@ -590,6 +655,10 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
     k_env_tiles<<<nblk(n_tiles, 128), 128, 0, c->stream>>>(R, prims, pi2, pk2, sorted, tiles,
                                                            tile_key);
     ++c->launches;
+    if (RPD_ENV_SUP > 0) {
+      k_env_supers<<<nblk(n_sup, 128), 128, 0, c->stream>>>(R, tiles, sup);
+      ++c->launches;
+    }
   }
   if (S == 0) return cudaGetLastError();
   k_env_sample_keys<<<nblk(S, 256), 256, 0, c->stream>>>(S, smp, box, sk, si);
@@ -598,7 +667,7 @@ cudaError_t launch_envelope(rpd_ctx* c, const double* smp, int64_t S, const doub
   int64_t blocks = (S + 32 * ENV_WARPS - 1) / (32 * ENV_WARPS);
   if (blocks > (int64_t)c->sms * 16) blocks = (int64_t)c->sms * 16;
   k_env_dist<<<(unsigned)blocks, ENV_WARPS * 32, 0, c->stream>>>(
-      S, smp, si2, sk2, R, tiles, tile_key, sorted, g_out, prim_out, n_eval);
+      S, smp, si2, sk2, R, tiles, tile_key, sup, sorted, g_out, prim_out, n_eval);
   ++c->launches;
   return cudaGetLastError();
 }

@@ -26,6 +26,25 @@ for spec in sys.argv[2:]:
     R.load_library(B.LIB)
     ctx = R.RPDContext(0, filter_mode="pruned")
     for name in cfgs:
+        if name.endswith("inc"):  # the incremental chain of a C4-like workload (C4inc)
+            w = W.make_config(name[:-3])
+            box = W.mesh_box(w.verts)
+            ts = []
+            for rep in range(2):
+                ctx.neighbors(torch.tensor(w.spheres, device="cuda"), box, device=True)
+                n_prev = w.N
+                for (sp, _, _) in w.batches:
+                    d = torch.tensor(sp, device="cuda")
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    g = ctx.neighbors_update(d, len(sp) - n_prev, box, device=True)
+                    torch.cuda.synchronize()
+                    if rep:
+                        ts.append((time.perf_counter() - t0) * 1e3)
+                    n_prev = len(sp)
+            print(f"{tag:10s} {name} update median {np.median(ts):8.3f} ms  "
+                  f"E={len(g['nbr_idx'])}", flush=True)
+            continue
         w = W.make_config(name)
         box = W.mesh_box(w.verts)
         sp = torch.tensor(w.spheres, device="cuda")
