@@ -41,7 +41,10 @@ constexpr int NB_MAXV = 224;              // vertex candidates of P_K per sphere
 constexpr int NB_CAPC = 128;              // selection candidates: 4 per lane
 constexpr int NB_CAP1 = 256;              // row entries kept by pass 1
 constexpr int NB_WARPS = 4;               // warps per block of the main kernel
-constexpr int NB_BT = 256;                // threads per sphere of the heavy-row kernel
+#ifndef RPD_NB_BT
+#define RPD_NB_BT 256
+#endif
+constexpr int NB_BT = RPD_NB_BT;          // threads per sphere of the heavy-row kernel (A/B knob)
 constexpr int NB_GMAX = 160;              // grid cells per axis (max)
 constexpr int NB_RB = 256;                // radius buckets of the work order
 constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
