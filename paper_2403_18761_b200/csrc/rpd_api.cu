@@ -2219,7 +2219,7 @@ rpd_status rpd_neighbors(rpd_ctx* c, const double* spheres, int64_t N, const dou
     CK(cudaMalloc(&c->nb_dbg, sizeof(long long) * 8 * N), "alloc");
     CK(cudaMemsetAsync(c->nb_dbg, 0, sizeof(long long) * 8 * N, c->stream), "memset");
   }
-  CK(c->nb_ball.ensure(sizeof(double4) * N), "alloc");  // (for rpd_neighbors_update)
+  CK(c->nb_ball.ensure(sizeof(double4) * 2 * N), "alloc");  // (for rpd_neighbors_update)
   CK(launch_neighbors_pass1(c, d_sph, N, bx, c->nb_cnt.as<int32_t>(), off), "neighbors");
   RbSpec rs{};
   rs.i32[0] = off + N;
@@ -2290,10 +2290,10 @@ rpd_status rpd_neighbors_update(rpd_ctx* c, const double* spheres, int64_t N, in
   CK(c->nb_off2.ensure_slack(sizeof(int32_t) * (N + 1), 2), "alloc");
   CK(c->nb_misc.ensure(sizeof(int) * 8), "alloc");
   // the balls of the old rows, grown (with their content) for the new ones
-  if (c->nb_ball.cap < sizeof(double4) * N) {
+  if (c->nb_ball.cap < sizeof(double4) * 2 * N) {  // (ball + vertex box per row)
     DevBuf nb;
-    CK(nb.ensure(sizeof(double4) * 2 * N), "alloc");
-    CK(cudaMemcpyAsync(nb.p, c->nb_ball.p, sizeof(double4) * N_old, cudaMemcpyDeviceToDevice,
+    CK(nb.ensure(sizeof(double4) * 4 * N), "alloc");
+    CK(cudaMemcpyAsync(nb.p, c->nb_ball.p, sizeof(double4) * 2 * N_old, cudaMemcpyDeviceToDevice,
                        c->stream), "copy");
     CK(cudaStreamSynchronize(c->stream), "copy");
     std::swap(c->nb_ball, nb);

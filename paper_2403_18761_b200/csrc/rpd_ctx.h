@@ -347,7 +347,7 @@ struct rpd_ctx {
   rpd::DevBuf nb_off2, nb_idx2; // the merged lists of an incremental update (swapped in)
   rpd::DevBuf nb_flag, nb_list, nb_len, nb_misc;
   int64_t nb_rows = 0;          // rows computed by the last call
-  rpd::DevBuf nb_ball;          // double4 per sphere: ball around its last P_K (r < 0: empty)
+  rpd::DevBuf nb_ball;          // 2 double4 per sphere: ball around its last P_K (r < 0: empty), vertex-box half extents
 };
 
 namespace rpd {

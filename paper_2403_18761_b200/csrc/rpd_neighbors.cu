@@ -251,7 +251,8 @@ struct NbArgs {
   int64_t n_work;         // pass 1 rows: order[0, n_work) (0: all N) ...
   const int32_t* n_work_dev;  // ... or a device count (incremental update)
   long long* dbg;  // development aid (RPD_NB_DEBUG): per sphere 8 counters, or null
-  double4* ball;   // [N] bounding ball of each row's final P_K (center, radius; r < 0: empty)
+  double4* ball;   // [2N] per row: bounding ball of its final P_K (center, radius; r < 0:
+                   // empty), then the half extents of P_K's vertex box around that centre
   int32_t* hits;   // [warp slots][NB_HCAP] positions (cell-sorted arrays) of a round's hits
   // heavy rows: pass 1 (a warp per sphere) hands a sphere whose round-0 search ball holds more
   // than heavy_items grid entries to the block kernel (a block of NB_BT threads per sphere)
@@ -359,7 +360,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     if (!PASS2 && tid == 0) {
       A.cnt[i] = 0;
       atomicAdd(&A.stats[1], 1ull);
-      if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);  // (empty cell)
+      if (A.ball) A.ball[2 * i] = make_double4(0.0, 0.0, 0.0, -1.0);  // (empty cell)
     }
     return;
   }
@@ -680,7 +681,7 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     if (n_v == 0) {  // P_K empty: C_i ∩ B is empty
       if (!PASS2 && tid == 0) {
         A.cnt[i] = 0;
-        if (A.ball) A.ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);
+        if (A.ball) A.ball[2 * i] = make_double4(0.0, 0.0, 0.0, -1.0);
       }
       flush_tri();
       return;
@@ -1089,7 +1090,10 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
     if (tid == 0) {
       A.cnt[i] = n_o;
       // a ball around P_K ⊇ C_i ∩ B (world coordinates; incremental updates test it)
-      if (A.ball) A.ball[i] = make_double4(si.x + cx, si.y + cy, si.z + cz, rs + A.tol0);
+      if (A.ball) {  // and the half extents of its vertex box (same centre)
+        A.ball[2 * i] = make_double4(si.x + cx, si.y + cy, si.z + cz, rs + A.tol0);
+        A.ball[2 * i + 1] = make_double4(be[0] + A.tol0, be[1] + A.tol0, be[2] + A.tol0, 0.0);
+      }
       if (n_o > NB_CAP1) A.long_ids[atomicAdd(A.n_long, 1)] = i;
     }
     if (n_o <= NB_CAP1)
@@ -1423,9 +1427,11 @@ static __global__ void __launch_bounds__(NB_AT) k_nb_extend(
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N_old;
        i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + threadIdx.x;
-    double4 b = make_double4(0, 0, 0, -1.0), si = make_double4(0, 0, 0, 0);
+    double4 b = make_double4(0, 0, 0, -1.0), bx = make_double4(0, 0, 0, 0),
+            si = make_double4(0, 0, 0, 0);
     if (i < N_old) {
-      b = ball[i];
+      b = ball[2 * i];
+      bx = ball[2 * i + 1];
       si = make_double4(sph[4 * i], sph[4 * i + 1], sph[4 * i + 2], sph[4 * i + 3]);
     }
     const int o0 = i < N_old ? old_off[i] : 0, o1 = i < N_old ? old_off[i + 1] : 0;
@@ -1452,12 +1458,14 @@ static __global__ void __launch_bounds__(NB_AT) k_nb_extend(
           continue;
         }
         // h_ij(x) = (-u.(x - theta_i) + (|u|^2 - r_j^2 + r_i^2) / 2) / |u| >= 0 on C_i: its
-        // minimum over the ball is at the centre minus the radius
+        // minimum over the ball is the value at the centre minus the radius, over the vertex
+        // box the value at the centre minus sum |u_k| e_k / |u|; both bound it over P_K
         const double un = sqrt(u2);
         const double yx = b.x - si.x, yy = b.y - si.y, yz = b.z - si.z;
         const double hc =
             (-(ux * yx + uy * yy + uz * yz) + 0.5 * (u2 - sj.w * sj.w + si.w * si.w)) / un;
-        if (hc - b.w <= margin) {
+        const double hb = hc - (fabs(ux) * bx.x + fabs(uy) * bx.y + fabs(uz) * bx.z) / un;
+        if (hc - b.w <= margin && hb <= margin) {
           if (WRITE) idx[pos++] = (int32_t)(j0 + q);
           ++n_hit;
         }
@@ -1466,7 +1474,7 @@ static __global__ void __launch_bounds__(NB_AT) k_nb_extend(
     if (!WRITE && i < N_old) {
       len[i] = hidden ? 0 : (o1 - o0) + n_hit;
       flag[i] = hidden || n_hit > 0;
-      if (hidden) ball[i] = make_double4(0.0, 0.0, 0.0, -1.0);
+      if (hidden) ball[2 * i] = make_double4(0.0, 0.0, 0.0, -1.0);
     }
   }
 }
