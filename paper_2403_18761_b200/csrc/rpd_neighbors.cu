@@ -1048,6 +1048,23 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
       __syncthreads();  // (Bc is rewritten by the next round)
     }
     if (n_deep == 0) converged = true;
+    if (converged && n_list >= 0 && (A.ball_test & 4)) {
+      // the final list is this round's hit list: the listing round would scan exactly these
+      // positions against the same P_K with the same test (some vertex within slack; this
+      // round's loop only stopped early on a deep cut, which there is none of), so every one
+      // is listed (RPD_NB_REUSE=0: the listing scan)
+      for (int t = tid; t < n_list; t += NT) {
+        const int j = A.items[hb[t]];
+        if (PASS2) {
+          if (t < cap2) A.tmp[base + t] = j;
+        } else if (t < NB_CAP1) {
+          S.out[t] = j;
+        }
+      }
+      if (tid == 0) S.n_o = n_list;
+      gsync();
+      break;
+    }
   }
   flush_tri();
   gsync();
@@ -1303,10 +1320,13 @@ static cudaError_t nb_build(rpd_ctx* c, const double* sph, int64_t N, const doub
   A.heavy_items = nb_heavy_items(NB_HEAVY_DEFAULT);
   {
     // bit 0: the ball pre-test of the triple enumeration's refinement pairs; bit 1: the
-    // sequential clip in place of the triple enumeration (RPD_NB_SEQ=0: the enumeration)
+    // sequential clip in place of the triple enumeration (RPD_NB_SEQ=0: the enumeration);
+    // bit 2: the converged round's hit list taken as the row (RPD_NB_REUSE=0: a listing scan)
     const char* bt = getenv("RPD_NB_BALLT");
     const char* sq = getenv("RPD_NB_SEQ");
-    A.ball_test = (bt ? (atoi(bt) & 1) : 1) | ((sq ? atoi(sq) : 1) ? 2 : 0);
+    const char* ru = getenv("RPD_NB_REUSE");
+    A.ball_test = (bt ? (atoi(bt) & 1) : 1) | ((sq ? atoi(sq) : 1) ? 2 : 0) |
+                  ((ru ? atoi(ru) : 1) ? 4 : 0);
   }
   c->nb_ball_test = A.ball_test;
   A.heavy_ids = hvy_ids;
