@@ -35,9 +35,12 @@ namespace rpd {
 namespace {
 
 constexpr int NB_KSEL0 = 16;              // planes of the first P_K besides the 6 box planes
-constexpr int NB_KSEL = 48;               // planes of a refined P_K (facets + deepest cuts)
-constexpr int NB_MAXP = 6 + NB_KSEL;
-constexpr int NB_MAXV = 224;              // vertex candidates of P_K per sphere
+#ifndef RPD_NB_KSEL
+#define RPD_NB_KSEL 48
+#endif
+constexpr int NB_KSEL = RPD_NB_KSEL;      // planes of a refined P_K (facets + deepest cuts), <= 64
+constexpr int NB_MAXP = 6 + NB_KSEL;      // (< 128: the tight-plane masks below)
+constexpr int NB_MAXV = NB_KSEL > 48 ? 200 : 224;  // vertex candidates of P_K per sphere
 constexpr int NB_CAPC = 128;              // selection candidates: 4 per lane
 constexpr int NB_CAP1 = 256;              // row entries kept by pass 1
 constexpr int NB_WARPS = 4;               // warps per block of the main kernel
@@ -524,24 +527,28 @@ __device__ void nb_row(const NbArgs& A, NbSm<NT>& SM, int i, int tid, int32_t* _
             const double4 v = S.vx[s2];
             if (pc.x * v.x + pc.y * v.y + pc.z * v.z + pc.w >= 2.0 * (v.w + mc)) continue;
             cuts = true;
-            unsigned long long tm = 0;
+            unsigned long long tm[2] = {0ull, 0ull};  // planes [0, 64), [64, 128)
             for (int k = 0; k < c; ++k) {
               const double4 pk = S.pl[k];
               const double h = pk.x * v.x + pk.y * v.y + pk.z * v.z + pk.w;
-              if (h <= 2.0 * (v.w + A.tol0 + 8.0 * EPS * fabs(pk.w))) tm |= 1ull << k;
+              if (h <= 2.0 * (v.w + A.tol0 + 8.0 * EPS * fabs(pk.w)))
+                tm[k >> 6] |= 1ull << (k & 63);
             }
-            for (unsigned long long ma = tm; ma; ma &= ma - 1) {
-              const int a = __ffsll((long long)ma) - 1;
-              for (unsigned long long mb = ma & (ma - 1); mb; mb &= mb - 1) {
-                const int b = __ffsll((long long)mb) - 1;
-                const int q = a * (2 * c - a - 1) / 2 + (b - a - 1);
-                const unsigned bit = 1u << (q & 31);
-                if (!(atomicOr(&pm[q >> 5], bit) & bit)) {
-                  const int t = atomicAdd(&S.n_pair, 1);
-                  if (t < NB_CAP1) plist[t] = a | (b << 8);
-                }
+            for (int wa = 0; wa < 2; ++wa)
+              for (unsigned long long ma = tm[wa]; ma; ma &= ma - 1) {
+                const int a = __ffsll((long long)ma) - 1 + 64 * wa;
+                for (int wb = wa; wb < 2; ++wb)
+                  for (unsigned long long mb = wb == wa ? (ma & (ma - 1)) : tm[1]; mb;
+                       mb &= mb - 1) {
+                    const int b = __ffsll((long long)mb) - 1 + 64 * wb;
+                    const int q = a * (2 * c - a - 1) / 2 + (b - a - 1);
+                    const unsigned bit = 1u << (q & 31);
+                    if (!(atomicOr(&pm[q >> 5], bit) & bit)) {
+                      const int t = atomicAdd(&S.n_pair, 1);
+                      if (t < NB_CAP1) plist[t] = a | (b << 8);
+                    }
+                  }
               }
-            }
           }
           __syncwarp();
           if (!__any_sync(0xffffffffu, cuts)) continue;  // h_c >= 2 m_v at every vertex: P unchanged
