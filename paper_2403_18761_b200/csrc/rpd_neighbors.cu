@@ -51,7 +51,10 @@ constexpr int NB_BT = RPD_NB_BT;          // threads per sphere of the heavy-row
 constexpr int NB_GMAX = 160;              // grid cells per axis (max)
 constexpr int NB_RB = 256;                // radius buckets of the work order
 constexpr int NB_ROUNDS = 6;              // polytope refinements (the last one lists)
-constexpr int NB_HCAP = 4096;             // hit list of a round (per warp slot, global memory)
+#ifndef RPD_NB_HCAP
+#define RPD_NB_HCAP 16384
+#endif
+constexpr int NB_HCAP = RPD_NB_HCAP;      // hit list of a round (per warp slot, global memory)
 
 struct NbGrid {
   double lo[3], h[3];
