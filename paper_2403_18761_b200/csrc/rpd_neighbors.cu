@@ -34,9 +34,12 @@
 namespace rpd {
 namespace {
 
-constexpr int NB_KSEL0 = 16;              // planes of the first P_K besides the 6 box planes
+#ifndef RPD_NB_KSEL0
+#define RPD_NB_KSEL0 56
+#endif
+constexpr int NB_KSEL0 = RPD_NB_KSEL0;    // planes of the first P_K besides the 6 box planes
 #ifndef RPD_NB_KSEL
-#define RPD_NB_KSEL 48
+#define RPD_NB_KSEL 64
 #endif
 constexpr int NB_KSEL = RPD_NB_KSEL;      // planes of a refined P_K (facets + deepest cuts), <= 64
 constexpr int NB_MAXP = 6 + NB_KSEL;      // (< 128: the tight-plane masks below)
