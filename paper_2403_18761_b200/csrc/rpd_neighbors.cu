@@ -216,9 +216,14 @@ __global__ void k_nb_gather(int64_t N, const int32_t* __restrict__ items,
 // work order: descending radius (the big spheres have the big cells and the long scans; the
 // near-zero ones are heavy too, but moving them first or going ascending measured no better:
 // DESIGN.md "Sphere neighbours")
+#ifndef RPD_NB_TINY_FIRST
+#define RPD_NB_TINY_FIRST 0  // the smallest radius bucket first, then descending (A/B knob)
+#endif
 __device__ __forceinline__ int nb_rbucket(double r, double rmax) {
-  const int b = rmax > 0 ? (int)((1.0 - r / rmax) * NB_RB) : 0;
-  return b < 0 ? 0 : (b >= NB_RB ? NB_RB - 1 : b);
+  int b = rmax > 0 ? (int)((1.0 - r / rmax) * NB_RB) : 0;
+  b = b < 0 ? 0 : (b >= NB_RB ? NB_RB - 1 : b);
+  if (RPD_NB_TINY_FIRST) b = b == NB_RB - 1 ? 0 : b + 1;
+  return b;
 }
 __global__ void k_nb_rcount(const double* __restrict__ sph, int64_t N, const NbGrid* __restrict__ g,
                             int32_t* __restrict__ cnt) {
