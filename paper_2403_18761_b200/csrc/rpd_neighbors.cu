@@ -10,9 +10,12 @@
 // Per sphere i (one warp), in coordinates y = x - theta_i:
 //   1. K = the KSEL spheres of smallest power distance PD_j(theta_i) found in the grid rings
 //      around i (a heuristic choice: correctness does not depend on it);
-//   2. P_K = B ∩ ⋂_{k∈K} {h_ik >= 0} ⊇ C_i ∩ B; its vertices by brute-force enumeration of
-//      plane triples (fp64, each with an error radius e_v from its conditioning), kept when
-//      every half-space holds within e_v + tol0 (so no true vertex is lost);
+//   2. P_K = B ∩ ⋂_{k∈K} {h_ik >= 0} ⊇ C_i ∩ B; its vertices by a sequential clip of B's
+//      corners, one plane at a time (triples only from the plane pairs tight at a vertex the
+//      plane may remove; or, RPD_NB_SEQ=0, by enumeration of all plane triples), in fp64,
+//      each vertex with an error radius e_v from its conditioning, kept when every half-space
+//      holds within e_v + tol0 (so no true vertex is lost); refined over rounds by the planes
+//      that cut it deepest;
 //   3. j is listed iff h_ij(v) <= e_v + tol0 at some vertex v of P_K (convexity: if h_ij > 0 at
 //      every vertex, the plane misses P_K ⊇ C_i ∩ B); only spheres in the ball
 //      |theta_j - theta_i| <= rho + sqrt(PDmax + rmax^2) (+ margins) can pass, found through
